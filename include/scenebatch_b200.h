@@ -1,0 +1,254 @@
+/*
+ * scenebatch_b200.h -- C ABI of the B200-native Sceniris hot path
+ * (batched candidate-pose sampling -> collision check -> first-valid accept).
+ *
+ * The reference (/root/reference/proj, namespace scenebatch) has no FFI layer; its
+ * boundary is the C++ class API that its (absent) engine would call. Every entry point
+ * below names the reference interface it replaces (file:line, relative to
+ * /root/reference/proj). include/scenebatch_b200.hpp re-creates that C++ class API on
+ * top of these functions and rethrows the same exception types.
+ *
+ * Conventions
+ *  - Every function returns an sb_status; on failure sb_last_error() holds the message
+ *    (thread-local). Status codes map 1:1 onto the reference's exception types.
+ *  - Poses are 4x4 homogeneous matrices stored column-major as double[16], exactly the
+ *    memory of the reference's Eigen::Matrix4d / TransformBatch (transform.hpp:10-27),
+ *    so a TransformBatch's data() can be passed without conversion. The bottom row must
+ *    be (0,0,0,1) exactly (SPEC TransformBatch invariant); other poses are rejected.
+ *  - All buffers are caller-owned host memory, copied in and out. No torch types.
+ *  - A handle is single-writer; calls on one handle are serialized on its CUDA stream.
+ *  - There is no CPU fallback: without a usable sm_100 device every compute entry point
+ *    fails with SB_ERR_CUDA.
+ */
+#ifndef SCENEBATCH_B200_H_
+#define SCENEBATCH_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SB_ABI_VERSION 1
+
+typedef enum sb_status {
+  SB_OK = 0,
+  SB_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+  SB_ERR_OUT_OF_RANGE = 2,     /* std::out_of_range (bad ids, .at()) */
+  SB_ERR_LOGIC = 3,            /* std::logic_error */
+  SB_ERR_RUNTIME = 4,          /* std::runtime_error */
+  SB_ERR_CUDA = 5              /* device missing / CUDA failure (no CPU fallback) */
+} sb_status;
+
+const char* sb_last_error(void);
+int sb_abi_version(void);
+/* 1 if a CUDA device of compute capability 10.x is usable, else 0 (reason in sb_last_error). */
+int sb_device_available(void);
+
+/* ------------------------------------------------------------------------------------
+ * Mesh primitives: trimesh.hpp:27-32 (make_box / make_cylinder / make_sphere),
+ * trimesh.hpp:35 (transformed). Vertices are xyz triples, triangles index triples.
+ * Pass NULL buffers to query the sizes first.
+ * ---------------------------------------------------------------------------------- */
+sb_status sb_make_box(double sx, double sy, double sz, double* vertices, uint32_t* n_vertices,
+                      uint32_t* triangles, uint32_t* n_triangles);
+sb_status sb_make_cylinder(double radius, double height, int segments, double* vertices,
+                           uint32_t* n_vertices, uint32_t* triangles, uint32_t* n_triangles);
+sb_status sb_make_sphere(double radius, int stacks, int slices, double* vertices,
+                         uint32_t* n_vertices, uint32_t* triangles, uint32_t* n_triangles);
+/* In-place rigid transform of n vertices: v <- R v + t (transform.hpp:71-73). */
+sb_status sb_transform_vertices(const double pose[16], double* vertices, uint32_t n_vertices);
+/* mesh_fingerprint (trimesh.cpp:120-135). */
+sb_status sb_mesh_fingerprint(const double* vertices, uint32_t n_vertices,
+                              const uint32_t* triangles, uint32_t n_triangles, uint64_t* out);
+/* rest_pose(mesh).z_offset = -aabb.min.z + kRestClearance (sampler.cpp:45-52). */
+sb_status sb_rest_z_offset(const double* vertices, uint32_t n_vertices, double* z_offset);
+
+/* Host-side BVH preparation summary for a mesh (MeshBvh, collision.cpp:217-281):
+ * info = {reference node count, reference depth, effective DAG nodes, reachable triangles}.
+ * The effective DAG is what the reference's traversal can reach (children read as
+ * {left, left+1}, collision.hpp:46); the GPU narrow phase runs on exactly that. */
+sb_status sb_bvh_info(const double* vertices, uint32_t n_vertices, const uint32_t* triangles,
+                      uint32_t n_triangles, int32_t info[4]);
+
+/* ------------------------------------------------------------------------------------
+ * RNG: rng.hpp:9-67. Exposed for known-answer tests and for hosts that pre-draw.
+ * ---------------------------------------------------------------------------------- */
+uint64_t sb_mix64(uint64_t x);                                       /* rng.hpp:9-14  */
+uint64_t sb_stream_key(const uint64_t* parts, uint32_t n);           /* rng.hpp:17-21 */
+/* make_stream(seed, counters) then `n_draws` x next_double() into out (rng.hpp:46-48,63-67). */
+sb_status sb_stream_doubles(uint64_t seed, const uint64_t* counters, uint32_t n_counters,
+                            double* out, uint32_t n_draws);
+
+/* ------------------------------------------------------------------------------------
+ * CollisionWorld: collision.hpp:76-127, collision.cpp:334-461.
+ * ---------------------------------------------------------------------------------- */
+typedef struct sb_world sb_world;
+
+typedef struct sb_stats {          /* CollisionStats, collision.hpp:65-72 */
+  uint64_t geometry_registrations;
+  uint64_t bvh_builds;
+  uint64_t check_calls;
+  uint64_t checked_instances;
+  uint64_t narrow_phase_tests;
+  /* Triangle-pair predicate evaluations. The reference counts BVH leaf re-visits
+   * (collision.cpp:320-324 push left and left+1); this build visits each reachable
+   * node pair once, so this counter is <= the reference's. */
+  uint64_t triangle_pair_tests;
+} sb_stats;
+
+/* CollisionWorld(batch_size, margin): collision.cpp:334-337. margin must be 0 (the only
+ * value the reference's configs use; margin > 0 = tri_tri_distance path, not built yet). */
+sb_status sb_world_create(uint64_t batch_size, double margin, int device, sb_world** out);
+void sb_world_destroy(sb_world* w);
+/* register_geometry: collision.cpp:339-355 (fingerprint dedupe, drop_degenerate, MeshBvh). */
+sb_status sb_register_geometry(sb_world* w, const double* vertices, uint32_t n_vertices,
+                               const uint32_t* triangles, uint32_t n_triangles,
+                               int32_t* geom_id);
+/* add_object: collision.cpp:365-376; objects start disabled with identity poses. */
+sb_status sb_add_object(sb_world* w, const char* name, int32_t geom_id, int32_t* object_id);
+/* set_enabled / set_enabled_all: collision.cpp:386-393. */
+sb_status sb_set_enabled(sb_world* w, int32_t object, const uint32_t* instances, uint64_t n,
+                         int enabled);
+sb_status sb_set_enabled_all(sb_world* w, int32_t object, int enabled);
+/* update_transforms (N poses) / update_transform (one): collision.cpp:395-412. */
+sb_status sb_update_transforms(sb_world* w, int32_t object, const double* poses_colmajor16xN);
+sb_status sb_update_transform(sb_world* w, int32_t object, uint64_t instance,
+                              const double pose[16]);
+/* object_pose / enabled accessors: collision.cpp:383-385,414-416. */
+sb_status sb_object_pose(sb_world* w, int32_t object, uint64_t instance, double pose[16]);
+sb_status sb_enabled(sb_world* w, int32_t object, uint64_t instance, int* enabled);
+/* check_batch: collision.cpp:418-461. poses[j] (column-major 16 doubles) is the candidate
+ * in instance active[j]. free_out / contact_out have length N; inactive instances get
+ * free = 1, contact = -1 (collision.cpp:424-426). */
+sb_status sb_check_batch(sb_world* w, int32_t geom_id, const double* poses_colmajor16xM,
+                         const uint32_t* active, uint64_t m, uint8_t* free_out,
+                         int32_t* contact_out);
+sb_status sb_get_stats(sb_world* w, sb_stats* out);
+sb_status sb_reset_stats(sb_world* w);
+
+/* ------------------------------------------------------------------------------------
+ * Scene description + generation engine. The reference's rejection loop is specified
+ * but absent from proj/; this is that loop, with the driver contract
+ * frozen in DESIGN.md ("Appendix C contract"). It composes PositionSampler
+ * (sampler.cpp:54-127), sample_orientations (sampler.cpp:129-156), rest_pose, pose
+ * compose (transform.hpp:40-54), build_constraint_region (relationships.cpp:161-218) and
+ * CollisionWorld::check_batch into one on-device pipeline.
+ * ---------------------------------------------------------------------------------- */
+enum { SB_DIST_NONE = 0, SB_DIST_GREATER = 1, SB_DIST_LESS = 2, SB_DIST_EQUAL = 3 };
+enum { SB_DIR_NONE = 0, SB_DIR_LEFT = 1, SB_DIR_RIGHT = 2, SB_DIR_FRONT = 3, SB_DIR_BACK = 4,
+       SB_DIR_VECTOR = 5 };                                   /* relationships.hpp:12-14 */
+enum { SB_FRAME_GLOBAL = 0, SB_FRAME_LOCAL = 1 };
+enum { SB_ORIENT_FIXED = 0, SB_ORIENT_UNIFORM_YAW = 1, SB_ORIENT_FACE_TO = 2 }; /* sampler.hpp:53-57 */
+
+typedef struct sb_mesh {
+  const double* vertices; /* n_vertices x 3 */
+  uint32_t n_vertices;
+  const uint32_t* triangles; /* n_triangles x 3 */
+  uint32_t n_triangles;
+} sb_mesh;
+
+/* An object present and enabled in every instance at a fixed pose (table, container). */
+typedef struct sb_fixed_object {
+  int32_t mesh;
+  double pose[16];
+} sb_fixed_object;
+
+/* A support surface: axis-aligned rect [x0,x1]x[y0,y1] in the z=0 plane of `pose`
+ * (SupportSurface, surface.hpp:15-20, given directly: surface extraction is out of scope). */
+typedef struct sb_support {
+  double pose[16];
+  double rect[4]; /* x0, y0, x1, y1 */
+} sb_support;
+
+/* RelationshipSpec (relationships.hpp:18-38) restricted to zero or one anchor. */
+typedef struct sb_relation {
+  int32_t anchor;          /* placement index of the anchor (< this placement), -1 = none */
+  int32_t distance_type;   /* SB_DIST_* */
+  int32_t direction;       /* SB_DIR_* */
+  int32_t frame;           /* SB_FRAME_* */
+  double direction_vector[2];
+  double distance;
+  double angle_threshold;  /* <= 0: default (pi/4 with a direction, pi without) */
+} sb_relation;
+
+/* PlacementSpec (config.hpp:45-54) subset on the hot path. */
+typedef struct sb_placement {
+  int32_t mesh;
+  int32_t support;
+  int32_t orientation;     /* SB_ORIENT_* */
+  int32_t face_target;     /* placement index for SB_ORIENT_FACE_TO, else -1 */
+  sb_relation relation;
+} sb_placement;
+
+typedef struct sb_scene {
+  uint64_t n_instances;    /* N variations */
+  int32_t attempts;        /* candidates per object K = max_retries + 1 (config.hpp:67) */
+  int32_t reserved;
+  uint32_t n_meshes;
+  const sb_mesh* meshes;
+  uint32_t n_fixed;
+  const sb_fixed_object* fixed;
+  uint32_t n_supports;
+  const sb_support* supports;
+  uint32_t n_placements;
+  const sb_placement* placements;
+} sb_scene;
+
+/* Host-side outputs of one generation run (any pointer may be NULL to skip it).
+ * Object order: fixed objects first, then placements; only placements are reported. */
+typedef struct sb_result {
+  int16_t* accepted;      /* [n_placements][n_local] accepted attempt index, -1 = none */
+  double* poses;          /* [n_placements][n_local][16] accepted pose (identity if none) */
+  uint8_t* valid;         /* [n_local] BatchedSceneGraph::valid_mask (scene_graph.hpp:68) */
+} sb_result;
+
+typedef struct sb_run_stats {
+  uint64_t valid_instances;
+  uint64_t candidates_sampled;   /* incl. non-placeable draws */
+  uint64_t candidate_checks;     /* check_batch checked_instances summed over rounds */
+  uint64_t narrow_phase_tests;
+  uint64_t triangle_pair_tests;
+  uint64_t rounds;               /* (placement, attempt) rounds executed */
+  uint64_t per_instance_placements;
+} sb_run_stats;
+
+/* Count exchange between shards (one process per GPU). Called with this rank's n values;
+ * must return every rank's values in rank order (recv has n * world_size slots). */
+typedef int (*sb_allgather_fn)(void* ctx, const uint64_t* send, uint32_t n, uint64_t* recv);
+
+typedef struct sb_shard {
+  uint64_t begin, end;     /* this rank owns global instances [begin, end) */
+  int32_t rank, world_size;
+  sb_allgather_fn allgather; /* required when world_size > 1 */
+  void* ctx;
+} sb_shard;
+
+typedef struct sb_engine sb_engine;
+
+/* initialize: registers meshes, adds fixed + placement objects, uploads
+ * everything once. shard == NULL: this engine owns all n_instances. */
+sb_status sb_engine_create(const sb_scene* scene, const sb_shard* shard, int device,
+                           sb_engine** out);
+void sb_engine_destroy(sb_engine* e);
+/* generate / warm_generate: one full rejection-sampling pass over every
+ * placement. Results stay in HBM; `out` (optional) is filled from them afterwards. */
+sb_status sb_engine_generate(sb_engine* e, uint64_t run_seed, sb_result* out,
+                             sb_run_stats* stats);
+/* Copy the last run's results to host buffers (D2H). */
+sb_status sb_engine_download(sb_engine* e, sb_result* out);
+/* The engine's collision world (for check_batch-level access); owned by the engine. */
+sb_world* sb_engine_world(sb_engine* e);
+uint64_t sb_engine_local_instances(const sb_engine* e);
+/* Kernel launches issued by the last generate call (counted on the host). */
+uint64_t sb_engine_last_launches(const sb_engine* e);
+/* Device time of the last generate call in ms (CUDA events on the engine stream), and of
+ * its check kernels alone (the dominant kernel; roofline numerator). */
+sb_status sb_engine_last_timing(const sb_engine* e, double* total_ms, double* check_ms,
+                                uint64_t* check_launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SCENEBATCH_B200_H_ */

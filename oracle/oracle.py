@@ -1,0 +1,262 @@
+"""TEST INFRASTRUCTURE ONLY: ctypes face of the oracle (oracle/_ref/libsbref.so).
+
+libsbref.so is the UNMODIFIED reference (/root/reference/proj/src/*.cpp, compiled in place
+by oracle/Makefile against oracle/shim) plus the builder-written rejection-loop driver
+(oracle/ref_driver.cpp). Only tests/, __graft_entry__.smoke() and bench.py's reference /
+cpu_baseline legs may import this module -- and only as the checker or the timed CPU
+baseline, never as part of the product path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from typing import Optional
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF_LIB = os.path.join(HERE, "_ref", "libsbref.so")
+REF_SRC = "/root/reference/proj"
+
+_lib = None
+
+
+def build() -> str:
+    """Compile the oracle (needs /root/reference; on the GPU box the prebuilt .so is used)."""
+    if os.path.isdir(REF_SRC):
+        subprocess.run(["make", "-s", "-C", HERE, "-j8"], check=True)
+    if not os.path.exists(REF_LIB):
+        raise FileNotFoundError(f"{REF_LIB} missing and /root/reference unavailable to build it")
+    return REF_LIB
+
+
+def available() -> bool:
+    return os.path.exists(REF_LIB)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(REF_LIB):
+            build()
+        L = C.CDLL(REF_LIB)
+        u64, d = C.c_uint64, C.POINTER(C.c_double)
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_mix64.restype = u64
+        L.ref_mix64.argtypes = [u64]
+        L.ref_stream_key2.restype = u64
+        L.ref_stream_key2.argtypes = [u64, u64]
+        L.ref_stream_key3.restype = u64
+        L.ref_stream_key3.argtypes = [u64, u64, u64]
+        L.ref_pcg_next_u64.restype = u64
+        L.ref_pcg_next_u64.argtypes = [u64]
+        L.ref_pcg_u32s.argtypes = [u64, C.c_void_p, C.c_uint32]
+        L.ref_stream_doubles.argtypes = [u64, C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint32]
+        L.ref_mesh_fingerprint.restype = u64
+        L.ref_mesh_fingerprint.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint32]
+        L.ref_region_fingerprint_rect.restype = u64
+        L.ref_region_fingerprint_rect.argtypes = [C.c_double] * 4
+        for name in ("ref_make_box",):
+            getattr(L, name).argtypes = [C.c_double] * 3 + [C.c_void_p] * 4
+        L.ref_make_cylinder.argtypes = [C.c_double, C.c_double, C.c_int] + [C.c_void_p] * 4
+        L.ref_make_sphere.argtypes = [C.c_double, C.c_int, C.c_int] + [C.c_void_p] * 4
+        L.ref_tri_tri.argtypes = [C.c_void_p]
+        L.ref_tri_tri_batch.argtypes = [C.c_void_p, u64, C.c_void_p]
+        L.ref_polygon_draws.argtypes = [C.c_void_p, C.c_uint32, u64, C.c_void_p, C.c_uint32,
+                                        C.c_void_p, C.c_uint32]
+        L.ref_triangulate.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint32, C.c_void_p]
+        L.ref_relation_region.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_double,
+                                          C.c_double, C.c_void_p, C.c_uint32, C.c_void_p,
+                                          C.c_void_p]
+        L.ref_world_create.restype = C.c_void_p
+        L.ref_world_create.argtypes = [u64, C.c_double, C.c_int]
+        L.ref_world_destroy.argtypes = [C.c_void_p]
+        L.ref_register_geometry.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p,
+                                            C.c_uint32, C.c_void_p]
+        L.ref_add_object.argtypes = [C.c_void_p, C.c_int32, C.c_void_p]
+        L.ref_set_enabled.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, u64, C.c_int]
+        L.ref_set_enabled_all.argtypes = [C.c_void_p, C.c_int32, C.c_int]
+        L.ref_update_transforms.argtypes = [C.c_void_p, C.c_int32, C.c_void_p]
+        L.ref_update_transform.argtypes = [C.c_void_p, C.c_int32, u64, C.c_void_p]
+        L.ref_check_batch.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, u64,
+                                      C.c_void_p, C.c_void_p]
+        L.ref_get_stats.argtypes = [C.c_void_p, C.c_void_p]
+        L.ref_generate.argtypes = [C.c_void_p, C.c_void_p, u64, C.c_int, C.c_void_p, C.c_void_p,
+                                   C.c_void_p, C.c_void_p]
+        _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def check(rc: int):
+    if rc != 0:
+        msg = lib().ref_last_error().decode(errors="replace")
+        if rc == 1:
+            raise ValueError(msg)
+        if rc == 2:
+            raise IndexError(msg)
+        raise RuntimeError(msg)
+
+
+# ------------------------------------------------------------------ meshes / KATs
+def make_box(sx, sy, sz):
+    return _mesh(lib().ref_make_box, C.c_double(sx), C.c_double(sy), C.c_double(sz))
+
+
+def make_cylinder(r, h, seg=32):
+    return _mesh(lib().ref_make_cylinder, C.c_double(r), C.c_double(h), C.c_int(seg))
+
+
+def make_sphere(r, stacks=12, slices=16):
+    return _mesh(lib().ref_make_sphere, C.c_double(r), C.c_int(stacks), C.c_int(slices))
+
+
+def _mesh(fn, *args):
+    nv, nt = C.c_uint32(), C.c_uint32()
+    check(fn(*args, None, C.byref(nv), None, C.byref(nt)))
+    v = np.zeros((nv.value, 3))
+    t = np.zeros((nt.value, 3), np.uint32)
+    check(fn(*args, _p(v), C.byref(nv), _p(t), C.byref(nt)))
+    return v, t
+
+
+def tri_tri(p: np.ndarray) -> np.ndarray:
+    """tri_tri_intersect over (n, 18) sextuples -> uint8 (n,)."""
+    p = np.ascontiguousarray(p, dtype=np.float64).reshape(-1, 18)
+    out = np.zeros(len(p), np.uint8)
+    lib().ref_tri_tri_batch(_p(p), len(p), _p(out))
+    return out
+
+
+def stream_doubles(seed: int, counters, n: int) -> np.ndarray:
+    c = np.ascontiguousarray(counters, dtype=np.uint64)
+    out = np.zeros(n)
+    lib().ref_stream_doubles(C.c_uint64(seed), _p(c), len(c), _p(out), n)
+    return out
+
+
+def polygon_draws(ring, seed: int, counters, n: int) -> np.ndarray:
+    r = np.ascontiguousarray(ring, dtype=np.float64).reshape(-1, 2)
+    c = np.ascontiguousarray(counters, dtype=np.uint64)
+    out = np.zeros((n, 2))
+    check(lib().ref_polygon_draws(_p(r), len(r), C.c_uint64(seed), _p(c), len(c), _p(out), n))
+    return out
+
+
+def triangulate(ring) -> np.ndarray:
+    r = np.ascontiguousarray(ring, dtype=np.float64).reshape(-1, 2)
+    out = np.zeros((512, 6))
+    nt = C.c_uint32()
+    check(lib().ref_triangulate(_p(r), len(r), _p(out), 512, C.byref(nt)))
+    return out[: nt.value].reshape(-1, 3, 2)
+
+
+def relation_region(rel_c, rect, ax, ay, ayaw):
+    """build_constraint_region for one anchor state -> (exterior ring of part 0, n_parts)."""
+    rc = np.ascontiguousarray(rect, dtype=np.float64)
+    out = np.zeros((512, 2))
+    npts, nparts = C.c_uint32(), C.c_uint32()
+    check(lib().ref_relation_region(C.byref(rel_c), _p(rc), ax, ay, ayaw, _p(out), 512,
+                                    C.byref(npts), C.byref(nparts)))
+    return out[: npts.value].copy(), nparts.value
+
+
+# ------------------------------------------------------------------ CollisionWorld
+class RefWorld:
+    def __init__(self, n: int, margin: float = 0.0, threads: int = 1):
+        self.n = n
+        self.h = lib().ref_world_create(n, margin, threads)
+        if not self.h:
+            raise ValueError(lib().ref_last_error().decode())
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().ref_world_destroy(self.h)
+            self.h = None
+
+    def register_geometry(self, v, t) -> int:
+        v = np.ascontiguousarray(v, np.float64)
+        t = np.ascontiguousarray(t, np.uint32)
+        out = C.c_int32()
+        check(lib().ref_register_geometry(self.h, _p(v), len(v), _p(t), len(t), C.byref(out)))
+        return out.value
+
+    def add_object(self, geom: int) -> int:
+        out = C.c_int32()
+        check(lib().ref_add_object(self.h, geom, C.byref(out)))
+        return out.value
+
+    def set_enabled(self, obj, inst, flag):
+        i = np.ascontiguousarray(inst, np.uint32)
+        check(lib().ref_set_enabled(self.h, obj, _p(i), len(i), int(flag)))
+
+    def set_enabled_all(self, obj, flag):
+        check(lib().ref_set_enabled_all(self.h, obj, int(flag)))
+
+    def update_transforms(self, obj, poses_colmajor):
+        p = np.ascontiguousarray(poses_colmajor, np.float64)
+        check(lib().ref_update_transforms(self.h, obj, _p(p)))
+
+    def update_transform(self, obj, inst, pose_colmajor):
+        p = np.ascontiguousarray(pose_colmajor, np.float64)
+        check(lib().ref_update_transform(self.h, obj, inst, _p(p)))
+
+    def check_batch(self, geom, poses_colmajor, active):
+        p = np.ascontiguousarray(poses_colmajor, np.float64).reshape(-1, 16)
+        a = np.ascontiguousarray(active, np.uint32)
+        free = np.ones(self.n, np.uint8)
+        contact = np.full(self.n, -1, np.int32)
+        check(lib().ref_check_batch(self.h, geom, _p(p), _p(a), len(a), _p(free), _p(contact)))
+        return free, contact
+
+    def stats(self):
+        out = np.zeros(6, np.uint64)
+        lib().ref_get_stats(self.h, _p(out))
+        keys = ("geometry_registrations", "bvh_builds", "check_calls", "checked_instances",
+                "narrow_phase_tests", "triangle_pair_tests")
+        return dict(zip(keys, map(int, out)))
+
+
+# ------------------------------------------------------------------ generation
+TRACE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int32, C.c_int32, C.c_uint64,
+                       C.POINTER(C.c_uint32), C.POINTER(C.c_double), C.POINTER(C.c_uint8),
+                       C.POINTER(C.c_uint8))
+
+
+def generate(scene, run_seed: int, threads: int = 1, shard=None, with_poses: bool = True,
+             trace=None):
+    """Run the reference rejection loop on `scene` (a paper_2512_16896_b200.world.Scene).
+
+    Returns dict(accepted (P, n) int16, valid (n,) uint8, poses (P, n, 16) colmajor | None,
+    stats dict). `shard` is a paper_2512_16896_b200.world.Shard (or None)."""
+    from paper_2512_16896_b200 import _capi as A  # data layout only
+
+    sc, keep = scene.to_c()
+    n = scene.n_instances if shard is None else shard.end - shard.begin
+    P = len(scene.placements)
+    acc = np.empty((P, n), np.int16)
+    valid = np.empty(n, np.uint8)
+    poses = np.empty((P, n, 16)) if with_poses else None
+    res = A.sb_result(acc.ctypes.data_as(C.POINTER(C.c_int16)),
+                      poses.ctypes.data_as(C.POINTER(C.c_double)) if with_poses else None,
+                      valid.ctypes.data_as(C.POINTER(C.c_uint8)))
+    st = A.sb_run_stats()
+    sh = shard.to_c() if shard is not None else None
+    cb = None
+    if trace is not None:
+        def _t(ctx, p, a, m, act, poses16, placeable, free):
+            trace(p, a, np.ctypeslib.as_array(act, (m,)).copy(),
+                  np.ctypeslib.as_array(poses16, (m, 16)).copy(),
+                  np.ctypeslib.as_array(placeable, (m,)).copy(),
+                  np.ctypeslib.as_array(free, (m,)).copy())
+        cb = TRACE_FN(_t)
+    rc = lib().ref_generate(C.byref(sc), C.byref(sh) if sh is not None else None,
+                            C.c_uint64(run_seed), threads, C.byref(res), C.byref(st),
+                            cb, None)
+    check(rc)
+    stats = {k: getattr(st, k) for k, _ in A.sb_run_stats._fields_}
+    return {"accepted": acc, "valid": valid, "poses": poses, "stats": stats}

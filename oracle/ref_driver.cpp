@@ -1,0 +1,506 @@
+// TEST INFRASTRUCTURE ONLY -- the oracle. Never linked into the product.
+//
+// Builder-written driver around the UNMODIFIED reference sources (compiled in place from
+// /root/reference/proj/src by oracle/Makefile against oracle/shim). The reference has no
+// engine; this file is the rejection loop SPEC.md:516-542 describes,
+// with the ordering choices frozen in DESIGN.md ("Appendix C contract"):
+//   1. `active` ascending; attempt 0 = all valid instances, then the still-failing ones.
+//   2. salt = placement index; run_seed as given.
+//   3. pose = translation(p + z_off * z) * rotation_z(yaw)   (transform.hpp:40-54).
+//   4. candidates are checked against every enabled object, fixed ones included.
+//   5. accept = update_transform + set_enabled(inst); after K attempts the instance is
+//      invalid and later placements skip it.
+//   6. placeable == 0 (empty region) counts as a failed attempt (not checked).
+//   7. margin 0.
+// Exposes a C ABI (prefix ref_) for ctypes; data layouts come from include/scenebatch_b200.h.
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "scenebatch/collision.hpp"
+#include "scenebatch/parallel.hpp"
+#include "scenebatch/polygon.hpp"
+#include "scenebatch/relationships.hpp"
+#include "scenebatch/rng.hpp"
+#include "scenebatch/sampler.hpp"
+#include "scenebatch/trimesh.hpp"
+#include "scenebatch_b200.h"
+
+using namespace scenebatch;
+
+namespace {
+thread_local std::string g_err;
+
+int fail(const std::exception& e, int code) {
+  g_err = e.what();
+  return code;
+}
+
+#define REF_TRY(...)                                        \
+  try {                                                      \
+    __VA_ARGS__;                                                  \
+    return 0;                                                \
+  } catch (const std::invalid_argument& e) {                 \
+    return fail(e, SB_ERR_INVALID_ARGUMENT);                 \
+  } catch (const std::out_of_range& e) {                     \
+    return fail(e, SB_ERR_OUT_OF_RANGE);                     \
+  } catch (const std::logic_error& e) {                      \
+    return fail(e, SB_ERR_LOGIC);                            \
+  } catch (const std::exception& e) {                        \
+    return fail(e, SB_ERR_RUNTIME);                          \
+  }
+
+Mat4 mat_from(const double* p) {
+  Mat4 m;
+  for (int k = 0; k < 16; ++k) m.data()[k] = p[k];
+  return m;
+}
+void mat_to(const Mat4& m, double* p) {
+  for (int k = 0; k < 16; ++k) p[k] = m.data()[k];
+}
+
+TriMesh mesh_from(const double* v, uint32_t nv, const uint32_t* t, uint32_t nt) {
+  TriMesh m;
+  m.vertices.reserve(nv);
+  for (uint32_t i = 0; i < nv; ++i) m.vertices.emplace_back(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+  m.triangles.reserve(nt);
+  for (uint32_t i = 0; i < nt; ++i) m.triangles.push_back({t[3 * i], t[3 * i + 1], t[3 * i + 2]});
+  return m;
+}
+
+void mesh_out(const TriMesh& m, double* v, uint32_t* nv, uint32_t* t, uint32_t* nt) {
+  if (nv) *nv = static_cast<uint32_t>(m.vertices.size());
+  if (nt) *nt = static_cast<uint32_t>(m.triangles.size());
+  if (v)
+    for (std::size_t i = 0; i < m.vertices.size(); ++i)
+      for (int c = 0; c < 3; ++c) v[3 * i + c] = m.vertices[i][c];
+  if (t)
+    for (std::size_t i = 0; i < m.triangles.size(); ++i)
+      for (int c = 0; c < 3; ++c) t[3 * i + c] = m.triangles[i][c];
+}
+
+struct RefWorld {
+  CollisionWorld world;
+  std::unique_ptr<ThreadPool> pool;
+  RefWorld(std::size_t n, double margin, int threads) : world(n, margin) {
+    if (threads != 1) pool = std::make_unique<ThreadPool>(threads);
+  }
+};
+
+RelationshipSpec spec_from(const sb_relation& r) {
+  RelationshipSpec s;
+  s.kind = SurfaceMode::on;
+  if (r.anchor >= 0) s.anchors.push_back("p" + std::to_string(r.anchor));
+  s.distance_type = static_cast<DistanceType>(r.distance_type);
+  s.direction = static_cast<DirectionKind>(r.direction);
+  s.frame = static_cast<DirectionFrame>(r.frame);
+  s.direction_vector = Vec2(r.direction_vector[0], r.direction_vector[1]);
+  s.distance = r.distance;
+  if (r.angle_threshold > 0.0) s.angle_threshold = r.angle_threshold;
+  return s;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+// ---------------------------------------------------------------- RNG / geometry KATs
+uint64_t ref_mix64(uint64_t x) { return mix64(x); }
+uint64_t ref_stream_key2(uint64_t a, uint64_t b) { return stream_key({a, b}); }
+uint64_t ref_stream_key3(uint64_t a, uint64_t b, uint64_t c) { return stream_key({a, b, c}); }
+uint64_t ref_pcg_next_u64(uint64_t seed) {
+  Pcg32 r(seed);
+  return r.next_u64();
+}
+void ref_pcg_u32s(uint64_t seed, uint32_t* out, uint32_t n) {
+  Pcg32 r(seed);
+  for (uint32_t i = 0; i < n; ++i) out[i] = r.next_u32();
+}
+// make_stream(seed, {c...}) then n next_double()
+void ref_stream_doubles(uint64_t seed, const uint64_t* c, uint32_t nc, double* out, uint32_t n) {
+  uint64_t h = mix64(seed);
+  for (uint32_t i = 0; i < nc; ++i) h = mix64(h ^ c[i]);
+  Pcg32 r(h);
+  for (uint32_t i = 0; i < n; ++i) out[i] = r.next_double();
+}
+
+int ref_make_box(double sx, double sy, double sz, double* v, uint32_t* nv, uint32_t* t,
+                 uint32_t* nt) {
+  REF_TRY(mesh_out(make_box(sx, sy, sz), v, nv, t, nt));
+}
+int ref_make_cylinder(double r, double h, int seg, double* v, uint32_t* nv, uint32_t* t,
+                      uint32_t* nt) {
+  REF_TRY(mesh_out(make_cylinder(r, h, seg), v, nv, t, nt));
+}
+int ref_make_sphere(double r, int st, int sl, double* v, uint32_t* nv, uint32_t* t,
+                    uint32_t* nt) {
+  REF_TRY(mesh_out(make_sphere(r, st, sl), v, nv, t, nt));
+}
+uint64_t ref_mesh_fingerprint(const double* v, uint32_t nv, const uint32_t* t, uint32_t nt) {
+  return mesh_fingerprint(mesh_from(v, nv, t, nt));
+}
+int ref_tri_tri(const double* p /*18*/) {
+  Vec3 a(p[0], p[1], p[2]), b(p[3], p[4], p[5]), c(p[6], p[7], p[8]);
+  Vec3 d(p[9], p[10], p[11]), e(p[12], p[13], p[14]), f(p[15], p[16], p[17]);
+  return tri_tri_intersect(a, b, c, d, e, f) ? 1 : 0;
+}
+// Batched tri_tri_intersect over n sextuples (18 doubles each).
+void ref_tri_tri_batch(const double* p, uint64_t n, uint8_t* out) {
+  for (uint64_t i = 0; i < n; ++i) out[i] = static_cast<uint8_t>(ref_tri_tri(p + 18 * i));
+}
+// PolygonSampler over one region (rect or polygon ring), n draws from make_stream(seed,{c})
+int ref_polygon_draws(const double* ring, uint32_t nring, uint64_t seed, const uint64_t* c,
+                      uint32_t nc, double* out, uint32_t n) {
+  REF_TRY({
+    Polygon2D poly;
+    for (uint32_t i = 0; i < nring; ++i) poly.exterior.emplace_back(ring[2 * i], ring[2 * i + 1]);
+    PolygonSampler s(MultiPolygon2D::from(poly));
+    uint64_t h = mix64(seed);
+    for (uint32_t i = 0; i < nc; ++i) h = mix64(h ^ c[i]);
+    Pcg32 r(h);
+    for (uint32_t i = 0; i < n; ++i) {
+      Vec2 q = s.draw(r);
+      out[2 * i] = q.x();
+      out[2 * i + 1] = q.y();
+    }
+  });
+}
+// triangulate(ring) -> up to max_tris triangles (6 doubles each); returns count via *nt.
+int ref_triangulate(const double* ring, uint32_t nring, double* out, uint32_t max_tris,
+                    uint32_t* nt) {
+  REF_TRY({
+    Polygon2D poly;
+    for (uint32_t i = 0; i < nring; ++i) poly.exterior.emplace_back(ring[2 * i], ring[2 * i + 1]);
+    auto tris = triangulate(poly);
+    *nt = static_cast<uint32_t>(tris.size());
+    for (std::size_t i = 0; i < tris.size() && i < max_tris; ++i)
+      for (int k = 0; k < 3; ++k) {
+        out[6 * i + 2 * k] = tris[i][k].x();
+        out[6 * i + 2 * k + 1] = tris[i][k].y();
+      }
+  });
+}
+uint64_t ref_region_fingerprint_rect(double x0, double y0, double x1, double y1) {
+  return region_fingerprint(MultiPolygon2D::from(make_rect(x0, y0, x1, y1)));
+}
+// build_constraint_region for one anchor state, return the region's exterior ring(s).
+// out: flattened xy of part 0 exterior (max_pts), *npts, *nparts.
+int ref_relation_region(const sb_relation* rel, const double* rect, double ax, double ay,
+                        double ayaw, double* out, uint32_t max_pts, uint32_t* npts,
+                        uint32_t* nparts) {
+  REF_TRY({
+    RelationshipSpec spec = spec_from(*rel);
+    MultiPolygon2D support = MultiPolygon2D::from(make_rect(rect[0], rect[1], rect[2], rect[3]));
+    std::vector<std::vector<AnchorState>> anchors;
+    if (rel->anchor >= 0) {
+      AnchorState s;
+      s.position = Vec2(ax, ay);
+      s.yaw = ayaw;
+      anchors.push_back({s});
+    }
+    ConstraintRegion cr = build_constraint_region(spec, support, anchors, 1);
+    *nparts = static_cast<uint32_t>(cr.region.parts.size());
+    *npts = 0;
+    if (!cr.region.parts.empty()) {
+      const auto& ext = cr.region.parts[0].exterior;
+      *npts = static_cast<uint32_t>(ext.size());
+      for (std::size_t i = 0; i < ext.size() && i < max_pts; ++i) {
+        out[2 * i] = ext[i].x();
+        out[2 * i + 1] = ext[i].y();
+      }
+    }
+  });
+}
+
+// ---------------------------------------------------------------- CollisionWorld
+void* ref_world_create(uint64_t n, double margin, int threads) {
+  try {
+    return new RefWorld(n, margin, threads);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+void ref_world_destroy(void* h) { delete static_cast<RefWorld*>(h); }
+int ref_register_geometry(void* h, const double* v, uint32_t nv, const uint32_t* t, uint32_t nt,
+                          int32_t* id) {
+  REF_TRY(*id = static_cast<RefWorld*>(h)->world.register_geometry(mesh_from(v, nv, t, nt)));
+}
+int ref_add_object(void* h, int32_t geom, int32_t* id) {
+  REF_TRY(*id = static_cast<RefWorld*>(h)->world.add_object("o", geom));
+}
+int ref_set_enabled(void* h, int32_t obj, const uint32_t* inst, uint64_t n, int flag) {
+  REF_TRY(static_cast<RefWorld*>(h)->world.set_enabled(obj, std::span<const uint32_t>(inst, n),
+                                                       flag != 0));
+}
+int ref_set_enabled_all(void* h, int32_t obj, int flag) {
+  REF_TRY(static_cast<RefWorld*>(h)->world.set_enabled_all(obj, flag != 0));
+}
+int ref_update_transforms(void* h, int32_t obj, const double* poses) {
+  REF_TRY({
+    RefWorld* w = static_cast<RefWorld*>(h);
+    TransformBatch b(w->world.batch_size());
+    for (std::size_t i = 0; i < b.size(); ++i) b[i] = mat_from(poses + 16 * i);
+    w->world.update_transforms(obj, b);
+  });
+}
+int ref_update_transform(void* h, int32_t obj, uint64_t inst, const double* pose) {
+  REF_TRY(static_cast<RefWorld*>(h)->world.update_transform(obj, inst, mat_from(pose)));
+}
+int ref_check_batch(void* h, int32_t geom, const double* poses, const uint32_t* active,
+                    uint64_t m, uint8_t* free_out, int32_t* contact_out) {
+  REF_TRY({
+    RefWorld* w = static_cast<RefWorld*>(h);
+    std::vector<Mat4> p(m);
+    for (uint64_t j = 0; j < m; ++j) p[j] = mat_from(poses + 16 * j);
+    CollisionMask mask = w->world.check_batch(geom, p, std::span<const uint32_t>(active, m),
+                                              w->pool.get());
+    std::memcpy(free_out, mask.free.data(), mask.free.size());
+    std::memcpy(contact_out, mask.contact_object.data(), mask.contact_object.size() * 4);
+  });
+}
+void ref_get_stats(void* h, uint64_t* out) {
+  const CollisionStats& s = static_cast<RefWorld*>(h)->world.stats();
+  out[0] = s.geometry_registrations;
+  out[1] = s.bvh_builds;
+  out[2] = s.check_calls;
+  out[3] = s.checked_instances;
+  out[4] = s.narrow_phase_tests;
+  out[5] = s.triangle_pair_tests;
+}
+
+// ---------------------------------------------------------------- generation driver
+// Optional per-round trace (debugging parity): global instance ids, candidate poses,
+// placeable flags, free flags per active slot.
+typedef void (*ref_trace_fn)(void* ctx, int32_t placement, int32_t attempt, uint64_t m,
+                             const uint32_t* active_global, const double* poses16,
+                             const uint8_t* placeable, const uint8_t* free_by_slot);
+
+// Runs the rejection loop. shard may be NULL (whole batch). threads: ThreadPool size
+// (0 = hardware concurrency, 1 = serial). Outputs follow sb_result (local instances).
+int ref_generate(const sb_scene* sc, const sb_shard* shard, uint64_t run_seed, int threads,
+                 sb_result* out, sb_run_stats* st, ref_trace_fn trace, void* trace_ctx) {
+  REF_TRY({
+    const uint64_t n_total = sc->n_instances;
+    uint64_t begin = 0, end = n_total;
+    int rank = 0, world_size = 1;
+    if (shard) {
+      begin = shard->begin;
+      end = shard->end;
+      rank = shard->rank;
+      world_size = shard->world_size;
+    }
+    if (begin > end || end > n_total) throw std::invalid_argument("bad shard range");
+    const std::size_t n_local = end - begin;
+    if (n_local == 0) throw std::invalid_argument("empty shard");
+    if (world_size > 1 && (!shard || !shard->allgather))
+      throw std::invalid_argument("sharded run needs an allgather callback");
+    auto allgather = [&](std::vector<uint64_t> send) {
+      std::vector<uint64_t> recv(send.size() * world_size);
+      if (world_size == 1) return send;
+      if (shard->allgather(shard->ctx, send.data(), static_cast<uint32_t>(send.size()),
+                           recv.data()) != 0)
+        throw std::runtime_error("allgather callback failed");
+      return recv;
+    };
+
+    RefWorld w(n_local, 0.0, threads);
+    std::vector<TriMesh> meshes;
+    std::vector<int> geom_of_mesh;
+    for (uint32_t i = 0; i < sc->n_meshes; ++i) {
+      const sb_mesh& m = sc->meshes[i];
+      meshes.push_back(mesh_from(m.vertices, m.n_vertices, m.triangles, m.n_triangles));
+      geom_of_mesh.push_back(w.world.register_geometry(meshes.back()));
+    }
+    for (uint32_t f = 0; f < sc->n_fixed; ++f) {
+      int obj = w.world.add_object("fixed", geom_of_mesh.at(sc->fixed[f].mesh));
+      w.world.update_transforms(obj, TransformBatch(n_local, mat_from(sc->fixed[f].pose)));
+      w.world.set_enabled_all(obj, true);
+    }
+    std::vector<int> obj_of_placement;
+    for (uint32_t p = 0; p < sc->n_placements; ++p)
+      obj_of_placement.push_back(
+          w.world.add_object("p" + std::to_string(p), geom_of_mesh.at(sc->placements[p].mesh)));
+
+    std::vector<uint8_t> valid(n_local, 1);
+    const int K = sc->attempts;
+    uint64_t rounds = 0, sampled = 0, per_inst = 0;
+    if (out && out->accepted)
+      for (std::size_t k = 0; k < sc->n_placements * n_local; ++k) out->accepted[k] = -1;
+
+    for (uint32_t p = 0; p < sc->n_placements; ++p) {
+      const sb_placement& pl = sc->placements[p];
+      const sb_support& sup = sc->supports[pl.support];
+      const int obj = obj_of_placement[p];
+      const int geom = geom_of_mesh.at(pl.mesh);
+      const double z_off = rest_pose(meshes.at(pl.mesh)).z_offset;
+      Mat4 sup_pose = mat_from(sup.pose);
+      MultiPolygon2D support_region =
+          MultiPolygon2D::from(make_rect(sup.rect[0], sup.rect[1], sup.rect[2], sup.rect[3]));
+      RelationshipSpec spec = spec_from(pl.relation);
+
+      // Anchor states in the support frame, indexed by GLOBAL instance id.
+      std::vector<std::vector<AnchorState>> anchors;
+      if (pl.relation.anchor >= 0) {
+        const int aobj = obj_of_placement.at(pl.relation.anchor);
+        Mat4 inv_sup = inverse_rigid(sup_pose);
+        std::vector<AnchorState> local(n_local);
+        for (std::size_t i = 0; i < n_local; ++i) {
+          Mat4 rel = inv_sup * w.world.object_pose(aobj, i);
+          local[i].position = Vec2(rel(0, 3), rel(1, 3));
+          local[i].yaw = yaw_of(rel);
+        }
+        std::vector<AnchorState> all(n_total);
+        if (world_size == 1) {
+          all = local;
+        } else {
+          // instance 0 lives on rank 0; exchange its state and each rank's vary flag
+          // (relationships.cpp:178-186 compares every instance against instance 0).
+          std::vector<uint64_t> send(4, 0);
+          if (begin == 0) {
+            std::memcpy(&send[0], &local[0].position.x(), 8);
+            std::memcpy(&send[1], &local[0].position.y(), 8);
+            std::memcpy(&send[2], &local[0].yaw, 8);
+          }
+          std::vector<uint64_t> recv = allgather(send);
+          AnchorState s0;
+          double tmp[3];
+          std::memcpy(tmp, &recv[0], 24);  // rank 0's slots
+          s0.position = Vec2(tmp[0], tmp[1]);
+          s0.yaw = tmp[2];
+          bool local_vary = false;
+          for (std::size_t i = 0; i < n_local; ++i)
+            if ((local[i].position - s0.position).norm() > 1e-12 ||
+                std::abs(local[i].yaw - s0.yaw) > 1e-12)
+              local_vary = true;
+          std::vector<uint64_t> flags = allgather({local_vary ? 1ull : 0ull});
+          bool global_vary = false;
+          for (uint64_t f : flags) global_vary = global_vary || f != 0;
+          for (std::size_t i = 0; i < n_total; ++i) all[i] = s0;
+          for (std::size_t i = 0; i < n_local; ++i) all[begin + i] = local[i];
+          if (global_vary && !local_vary) {
+            // force the per-instance path through a non-local slot (never sampled here)
+            std::size_t slot = begin == 0 ? n_total - 1 : 0;
+            all[slot].position = s0.position + Vec2(1.0, 0.0);
+          }
+        }
+        anchors.push_back(std::move(all));
+      }
+      ConstraintRegion cr = build_constraint_region(spec, support_region, anchors, n_total);
+      if (cr.per_instance) ++per_inst;
+      PositionSampler sampler(p);
+      sampler.prepare(&cr, n_total, run_seed);
+      TransformBatch support_world(n_total, sup_pose);
+      OrientationRule rule;
+      rule.kind = static_cast<OrientationRule::Kind>(pl.orientation);
+      std::vector<Vec2> face_targets;
+      if (pl.orientation == SB_ORIENT_FACE_TO) {
+        const int tobj = obj_of_placement.at(pl.face_target);
+        face_targets.assign(n_total, Vec2(0, 0));
+        for (std::size_t i = 0; i < n_local; ++i) {
+          const Mat4& tp = w.world.object_pose(tobj, i);
+          face_targets[begin + i] = Vec2(tp(0, 3), tp(1, 3));
+        }
+      }
+
+      std::vector<uint32_t> active;  // GLOBAL ids, ascending
+      for (std::size_t i = 0; i < n_local; ++i)
+        if (valid[i]) active.push_back(static_cast<uint32_t>(begin + i));
+
+      for (int a = 0; a < K; ++a) {
+        // Fast-path stream: this rank's draws start after the lower ranks' draws.
+        std::vector<uint64_t> counts = allgather({static_cast<uint64_t>(active.size())});
+        uint64_t total = 0, before = 0;
+        for (int r = 0; r < world_size; ++r) {
+          if (r < rank) before += counts[r];
+          total += counts[r];
+        }
+        if (total == 0) break;
+        ++rounds;
+        std::vector<Vec3> pos;
+        std::vector<uint8_t> placeable;
+        const bool fast = sampler.fast_path();
+        auto skip = [&](uint64_t k) {
+          if (k == 0 || !fast) return;
+          std::vector<uint32_t> dummy(k, 0);
+          std::vector<Vec3> dp;
+          std::vector<uint8_t> dpl;
+          sampler.sample(support_world, dummy, a, dp, dpl, nullptr);
+        };
+        skip(before);
+        if (!active.empty()) {
+          sampler.sample(support_world, active, a, pos, placeable, w.pool.get());
+          sampled += active.size();
+        }
+        skip(total - before - active.size());
+        if (active.empty()) continue;
+        std::vector<double> yaws =
+            sample_orientations(rule, active, pos, face_targets.empty() ? nullptr : &face_targets,
+                                run_seed, p, a);
+        std::vector<Mat4> poses(active.size());
+        std::vector<Mat4> chk_poses;
+        std::vector<uint32_t> chk_local;
+        for (std::size_t j = 0; j < active.size(); ++j) {
+          poses[j] = translation(pos[j] + Vec3(0, 0, z_off)) * rotation_z(yaws[j]);
+          if (placeable[j]) {
+            chk_poses.push_back(poses[j]);
+            chk_local.push_back(static_cast<uint32_t>(active[j] - begin));
+          }
+        }
+        CollisionMask mask;
+        if (!chk_local.empty()) mask = w.world.check_batch(geom, chk_poses, chk_local, w.pool.get());
+        std::vector<uint32_t> next;
+        std::vector<uint8_t> free_by_slot(active.size(), 0);
+        for (std::size_t j = 0; j < active.size(); ++j) {
+          uint32_t li = static_cast<uint32_t>(active[j] - begin);
+          bool ok = placeable[j] && mask.free[li];
+          free_by_slot[j] = ok ? 1 : 0;
+          if (ok) {
+            w.world.update_transform(obj, li, poses[j]);
+            uint32_t one[1] = {li};
+            w.world.set_enabled(obj, std::span<const uint32_t>(one, 1), true);
+            if (out && out->accepted) out->accepted[p * n_local + li] = static_cast<int16_t>(a);
+          } else {
+            next.push_back(active[j]);
+          }
+        }
+        if (trace) {
+          std::vector<double> flat(16 * active.size());
+          for (std::size_t j = 0; j < active.size(); ++j) mat_to(poses[j], flat.data() + 16 * j);
+          trace(trace_ctx, static_cast<int32_t>(p), a, active.size(), active.data(), flat.data(),
+                placeable.data(), free_by_slot.data());
+        }
+        active.swap(next);
+      }
+      for (uint32_t g : active) valid[g - begin] = 0;
+    }
+
+    if (out) {
+      if (out->valid) std::memcpy(out->valid, valid.data(), n_local);
+      if (out->poses)
+        for (uint32_t p = 0; p < sc->n_placements; ++p)
+          for (std::size_t i = 0; i < n_local; ++i)
+            mat_to(w.world.object_pose(obj_of_placement[p], i), out->poses + 16 * (p * n_local + i));
+    }
+    if (st) {
+      const CollisionStats& cs = w.world.stats();
+      uint64_t nv = 0;
+      for (uint8_t v : valid) nv += v;
+      st->valid_instances = nv;
+      st->candidates_sampled = sampled;
+      st->candidate_checks = cs.checked_instances;
+      st->narrow_phase_tests = cs.narrow_phase_tests;
+      st->triangle_pair_tests = cs.triangle_pair_tests;
+      st->rounds = rounds;
+      st->per_instance_placements = per_inst;
+    }
+  });
+}
+
+}  // extern "C"

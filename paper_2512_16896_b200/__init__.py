@@ -1,0 +1,13 @@
+"""B200-native Sceniris hot path: batched candidate-pose sampling, collision checking
+against placed geometry and first-valid acceptance, behind a C-ABI drop-in
+(include/scenebatch_b200.h). The Python layer is a thin ctypes face used by tests and
+bench.py; the product is libscenebatch_b200.so (sm_100a CUDA + C++ host runtime).
+"""
+from ._capi import LIB_PATH, SbCudaError, SbError, lib  # noqa: F401
+from .world import (CollisionWorld, Engine, Fixed, GenerationResult, Placement, Relation,  # noqa: F401
+                    Scene, Shard, Support, TriMesh, colmajor, from_colmajor, make_box,
+                    make_cylinder, make_sphere, merge, transformed, translation)
+
+
+def device_available() -> bool:
+    return bool(lib().sb_device_available())

@@ -1,0 +1,415 @@
+// Device-side restatements of the reference hot-path arithmetic (sm_100a, FP64).
+//
+// Compiled with -fmad=false: every +,-,*,/ rounds once, exactly as the reference's
+// default x86-64 build (SSE2, no FMA) does, and every reduction follows the reference's
+// Eigen expression order (left to right; oracle/shim/Eigen/Dense). sqrt and division are
+// IEEE correctly rounded on both sides, so masks, accepted indices and sampled positions
+// are bit-identical to the reference except where a libm transcendental (sin, cos, atan2)
+// is involved -- see DESIGN.md "libm".
+#pragma once
+
+#include <stdint.h>
+
+#include "sb_layout.h"
+
+namespace sbd {
+
+constexpr double kEps = 1e-12;  // collision.cpp:11
+
+// ------------------------------------------------------------------------- RNG
+constexpr uint64_t kPcgMult = 6364136223846793005ULL;
+constexpr uint64_t kPcgSeq = 0xda3e39cb94b95bdbULL;
+constexpr uint64_t kPcgInc = (kPcgSeq << 1u) | 1u;
+constexpr uint64_t kCacheSalt = 0x63616368ULL;     // "cach" sampler.cpp:9
+constexpr uint64_t kFallbackSalt = 0x66616c6cULL;  // "fall" sampler.cpp:10
+constexpr uint64_t kYawSalt = 0x79617721ULL;       // "yaw!" sampler.cpp:11
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {  // rng.hpp:9-14
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+// Pcg32 (rng.hpp:24-60). Only the state is carried; inc is the fixed default sequence.
+struct Pcg {
+  uint64_t state;
+
+  // Pcg32(seed): state=0, step, state += seed, step (rng.hpp:26-31).
+  __host__ __device__ __forceinline__ static Pcg seeded(uint64_t seed) {
+    Pcg p{0};
+    p.state = kPcgInc;  // 0 * mult + inc
+    p.state += seed;
+    p.state = p.state * kPcgMult + kPcgInc;
+    return p;
+  }
+  __host__ __device__ __forceinline__ uint32_t next_u32() {
+    uint64_t old = state;
+    state = old * kPcgMult + kPcgInc;
+    uint32_t xorshifted = static_cast<uint32_t>(((old >> 18u) ^ old) >> 27u);
+    uint32_t rot = static_cast<uint32_t>(old >> 59u);
+    return (xorshifted >> rot) | (xorshifted << ((32u - rot) & 31u));
+  }
+  // GCC evaluates the unsequenced operands left to right: first draw is the high word
+  // (rng.hpp:42; pinned by the KAT Pcg32(12345).next_u64() = 8630b53a16ac2a2c).
+  __host__ __device__ __forceinline__ uint64_t next_u64() {
+    uint64_t hi = next_u32();
+    uint64_t lo = next_u32();
+    return (hi << 32) | lo;
+  }
+  __host__ __device__ __forceinline__ double next_double() {
+    return static_cast<double>(next_u64() >> 11) * 0x1.0p-53;
+  }
+  // LCG jump-ahead by `delta` steps (Brown, "Random number generation with arbitrary
+  // strides"): the j-th drained fast-path point is draw j, i.e. 6j steps in.
+  __host__ __device__ __forceinline__ void advance(uint64_t delta) {
+    uint64_t cur_mult = kPcgMult, cur_plus = kPcgInc, acc_mult = 1u, acc_plus = 0u;
+    while (delta > 0) {
+      if (delta & 1u) {
+        acc_mult *= cur_mult;
+        acc_plus = acc_plus * cur_mult + cur_plus;
+      }
+      cur_plus = (cur_mult + 1u) * cur_plus;
+      cur_mult *= cur_mult;
+      delta >>= 1u;
+    }
+    state = acc_mult * state + acc_plus;
+  }
+};
+
+// make_stream(seed, {c0, c1, ...}) (rng.hpp:63-67)
+__host__ __device__ __forceinline__ uint64_t stream_seed2(uint64_t seed, uint64_t c0, uint64_t c1) {
+  return mix64(mix64(mix64(seed) ^ c0) ^ c1);
+}
+__host__ __device__ __forceinline__ uint64_t stream_seed4(uint64_t seed, uint64_t c0, uint64_t c1,
+                                                          uint64_t c2, uint64_t c3) {
+  return mix64(mix64(mix64(mix64(mix64(seed) ^ c0) ^ c1) ^ c2) ^ c3);
+}
+
+// ------------------------------------------------------------------ transforms
+// Rigid pose as a 3x4 row-major block [R | t]; the bottom row is (0,0,0,1) by contract.
+struct M34 {
+  double m[12];
+  __device__ __forceinline__ double r(int i, int j) const { return m[4 * i + j]; }
+  __device__ __forceinline__ double t(int i) const { return m[4 * i + 3]; }
+};
+
+// Mat4 product A*B as the reference computes it (shim: ((a0 b0 + a1 b1) + a2 b2) + a3 b3),
+// with both bottom rows (0,0,0,1); rows 0..2 only (row 3 is never read downstream).
+__device__ __forceinline__ void mul34(const M34& A, const M34& B, M34& C) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      double b3 = j == 3 ? 1.0 : 0.0;
+      double s = A.m[4 * i + 0] * B.m[0 + j];
+      s = s + A.m[4 * i + 1] * B.m[4 + j];
+      s = s + A.m[4 * i + 2] * B.m[8 + j];
+      s = s + A.m[4 * i + 3] * b3;
+      C.m[4 * i + j] = s;
+    }
+  }
+}
+
+// inverse_rigid (transform.hpp:63-69): [R^T | (-R^T) t]
+__device__ __forceinline__ void inverse_rigid(const M34& P, M34& I) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) I.m[4 * i + k] = P.m[4 * k + i];
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    double s = (-I.m[4 * i + 0]) * P.m[3];
+    s = s + (-I.m[4 * i + 1]) * P.m[7];
+    s = s + (-I.m[4 * i + 2]) * P.m[11];
+    I.m[4 * i + 3] = s;
+  }
+}
+
+// transform_point (transform.hpp:71-73): R p + t, left to right.
+__device__ __forceinline__ void xform(const M34& M, double px, double py, double pz, double& ox,
+                                      double& oy, double& oz) {
+  ox = ((M.m[0] * px + M.m[1] * py) + M.m[2] * pz) + M.m[3];
+  oy = ((M.m[4] * px + M.m[5] * py) + M.m[6] * pz) + M.m[7];
+  oz = ((M.m[8] * px + M.m[9] * py) + M.m[10] * pz) + M.m[11];
+}
+
+// transform_aabb (aabb.hpp:54-62) from a precomputed center c / half extent h.
+__device__ __forceinline__ void xform_aabb(const M34& M, const double c[3], const double h[3],
+                                           double mn[3], double mx[3]) {
+  double cx, cy, cz;
+  xform(M, c[0], c[1], c[2], cx, cy, cz);
+  double wx = (fabs(M.m[0]) * h[0] + fabs(M.m[1]) * h[1]) + fabs(M.m[2]) * h[2];
+  double wy = (fabs(M.m[4]) * h[0] + fabs(M.m[5]) * h[1]) + fabs(M.m[6]) * h[2];
+  double wz = (fabs(M.m[8]) * h[0] + fabs(M.m[9]) * h[1]) + fabs(M.m[10]) * h[2];
+  mn[0] = cx - wx;
+  mn[1] = cy - wy;
+  mn[2] = cz - wz;
+  mx[0] = cx + wx;
+  mx[1] = cy + wy;
+  mx[2] = cz + wz;
+}
+
+// Aabb3::overlaps with margin 0 (aabb.hpp:29-33): inclusive.
+__device__ __forceinline__ bool overlaps(const double amn[3], const double amx[3],
+                                         const double bmn[3], const double bmx[3]) {
+  return amn[0] <= bmx[0] && bmn[0] <= amx[0] && amn[1] <= bmx[1] && bmn[1] <= amx[1] &&
+         amn[2] <= bmx[2] && bmn[2] <= amx[2];
+}
+
+// ------------------------------------------------------- triangle-triangle test
+__device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }  // std::min
+__device__ __forceinline__ double dmax(double a, double b) { return a < b ? b : a; }  // std::max
+
+// isect_interval (collision.cpp:14-20)
+__device__ __forceinline__ void isect_interval(double vv0, double vv1, double vv2, double d0,
+                                               double d1, double d2, double& lo, double& hi) {
+  double t0 = vv0 + (vv1 - vv0) * d0 / (d0 - d1);
+  double t1 = vv2 + (vv1 - vv2) * d2 / (d2 - d1);
+  lo = dmin(t0, t1);
+  hi = dmax(t0, t1);
+}
+
+// compute_interval (collision.cpp:23-40); false = coplanar
+__device__ __forceinline__ bool compute_interval(double p0, double p1, double p2, double d0,
+                                                 double d1, double d2, double& lo, double& hi) {
+  if (d0 * d1 > 0.0) {
+    isect_interval(p0, p2, p1, d0, d2, d1, lo, hi);
+  } else if (d0 * d2 > 0.0) {
+    isect_interval(p0, p1, p2, d0, d1, d2, lo, hi);
+  } else if (d1 * d2 > 0.0 || d0 != 0.0) {
+    isect_interval(p1, p0, p2, d1, d0, d2, lo, hi);
+  } else if (d1 != 0.0) {
+    isect_interval(p0, p1, p2, d0, d1, d2, lo, hi);
+  } else if (d2 != 0.0) {
+    isect_interval(p0, p2, p1, d0, d2, d1, lo, hi);
+  } else {
+    return false;
+  }
+  return true;
+}
+
+__device__ __forceinline__ double orient2(double px, double py, double qx, double qy, double rx,
+                                          double ry) {
+  return (qx - px) * (ry - py) - (qy - py) * (rx - px);
+}
+
+// seg_seg_cross_2d (collision.cpp:42-51): strict crossing only
+__device__ __forceinline__ bool seg_cross(double ax, double ay, double bx, double by, double cx,
+                                          double cy, double dx, double dy) {
+  double o1 = orient2(ax, ay, bx, by, cx, cy), o2 = orient2(ax, ay, bx, by, dx, dy);
+  double o3 = orient2(cx, cy, dx, dy, ax, ay), o4 = orient2(cx, cy, dx, dy, bx, by);
+  return ((o1 > kEps && o2 < -kEps) || (o1 < -kEps && o2 > kEps)) &&
+         ((o3 > kEps && o4 < -kEps) || (o3 < -kEps && o4 > kEps));
+}
+
+// point_in_tri_2d (collision.cpp:53-61)
+__device__ __forceinline__ bool point_in_tri(double px, double py, double ax, double ay, double bx,
+                                             double by, double cx, double cy) {
+  double d1 = orient2(ax, ay, bx, by, px, py);
+  double d2 = orient2(bx, by, cx, cy, px, py);
+  double d3 = orient2(cx, cy, ax, ay, px, py);
+  bool has_neg = d1 < -kEps || d2 < -kEps || d3 < -kEps;
+  bool has_pos = d1 > kEps || d2 > kEps || d3 > kEps;
+  return !(has_neg && has_pos) && (has_neg || has_pos);
+}
+
+// coplanar_tri_tri (collision.cpp:63-83)
+__device__ __noinline__ bool coplanar_tri_tri(const double n[3], const double* p, const double* q) {
+  int axis = 0;
+  double an0 = fabs(n[0]), an1 = fabs(n[1]), an2 = fabs(n[2]);
+  if (an1 > an0) axis = 1;
+  if (an2 > (axis == 0 ? an0 : an1)) axis = 2;
+  int u = (axis + 1) % 3, v = (axis + 2) % 3;
+  double t1x[3] = {p[u], p[3 + u], p[6 + u]}, t1y[3] = {p[v], p[3 + v], p[6 + v]};
+  double t2x[3] = {q[u], q[3 + u], q[6 + u]}, t2y[3] = {q[v], q[3 + v], q[6 + v]};
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      if (seg_cross(t1x[i], t1y[i], t1x[(i + 1) % 3], t1y[(i + 1) % 3], t2x[j], t2y[j],
+                    t2x[(j + 1) % 3], t2y[(j + 1) % 3]))
+        return true;
+  double c1x = (t1x[0] + t1x[1] + t1x[2]) / 3.0, c1y = (t1y[0] + t1y[1] + t1y[2]) / 3.0;
+  double c2x = (t2x[0] + t2x[1] + t2x[2]) / 3.0, c2y = (t2y[0] + t2y[1] + t2y[2]) / 3.0;
+  if (point_in_tri(c1x, c1y, t2x[0], t2y[0], t2x[1], t2y[1], t2x[2], t2y[2])) return true;
+  if (point_in_tri(c2x, c2y, t1x[0], t1y[0], t1x[1], t1y[1], t1x[2], t1y[2])) return true;
+  return false;
+}
+
+// tri_tri_intersect (collision.cpp:87-130). p, q: 9 doubles each (three xyz vertices).
+__device__ __forceinline__ bool tri_tri_intersect(const double* p, const double* q) {
+  double e1x = q[3] - q[0], e1y = q[4] - q[1], e1z = q[5] - q[2];
+  double e2x = q[6] - q[0], e2y = q[7] - q[1], e2z = q[8] - q[2];
+  double n2[3] = {e1y * e2z - e1z * e2y, e1z * e2x - e1x * e2z, e1x * e2y - e1y * e2x};
+  double d2c = -((n2[0] * q[0] + n2[1] * q[1]) + n2[2] * q[2]);
+  double dp0 = ((n2[0] * p[0] + n2[1] * p[1]) + n2[2] * p[2]) + d2c;
+  double dp1 = ((n2[0] * p[3] + n2[1] * p[4]) + n2[2] * p[5]) + d2c;
+  double dp2 = ((n2[0] * p[6] + n2[1] * p[7]) + n2[2] * p[8]) + d2c;
+  double scale2 = sqrt((n2[0] * n2[0] + n2[1] * n2[1]) + n2[2] * n2[2]);
+  double tol2 = kEps * dmax(1.0, scale2);
+  if (fabs(dp0) < tol2) dp0 = 0.0;
+  if (fabs(dp1) < tol2) dp1 = 0.0;
+  if (fabs(dp2) < tol2) dp2 = 0.0;
+  if ((dp0 > 0 && dp1 > 0 && dp2 > 0) || (dp0 < 0 && dp1 < 0 && dp2 < 0)) return false;
+
+  double f1x = p[3] - p[0], f1y = p[4] - p[1], f1z = p[5] - p[2];
+  double f2x = p[6] - p[0], f2y = p[7] - p[1], f2z = p[8] - p[2];
+  double n1[3] = {f1y * f2z - f1z * f2y, f1z * f2x - f1x * f2z, f1x * f2y - f1y * f2x};
+  double d1c = -((n1[0] * p[0] + n1[1] * p[1]) + n1[2] * p[2]);
+  double dq0 = ((n1[0] * q[0] + n1[1] * q[1]) + n1[2] * q[2]) + d1c;
+  double dq1 = ((n1[0] * q[3] + n1[1] * q[4]) + n1[2] * q[5]) + d1c;
+  double dq2 = ((n1[0] * q[6] + n1[1] * q[7]) + n1[2] * q[8]) + d1c;
+  double scale1 = sqrt((n1[0] * n1[0] + n1[1] * n1[1]) + n1[2] * n1[2]);
+  double tol1 = kEps * dmax(1.0, scale1);
+  if (fabs(dq0) < tol1) dq0 = 0.0;
+  if (fabs(dq1) < tol1) dq1 = 0.0;
+  if (fabs(dq2) < tol1) dq2 = 0.0;
+  if ((dq0 > 0 && dq1 > 0 && dq2 > 0) || (dq0 < 0 && dq1 < 0 && dq2 < 0)) return false;
+
+  if (dp0 == 0 && dp1 == 0 && dp2 == 0) return coplanar_tri_tri(n1, p, q);
+
+  double dir0 = n1[1] * n2[2] - n1[2] * n2[1];
+  double dir1 = n1[2] * n2[0] - n1[0] * n2[2];
+  double dir2 = n1[0] * n2[1] - n1[1] * n2[0];
+  int axis = 0;
+  double ad0 = fabs(dir0), ad1 = fabs(dir1), ad2 = fabs(dir2);
+  if (ad1 > ad0) axis = 1;
+  if (ad2 > (axis == 0 ? ad0 : ad1)) axis = 2;
+
+  double lo1, hi1, lo2, hi2;
+  if (!compute_interval(p[axis], p[3 + axis], p[6 + axis], dp0, dp1, dp2, lo1, hi1))
+    return coplanar_tri_tri(n1, p, q);
+  if (!compute_interval(q[axis], q[3 + axis], q[6 + axis], dq0, dq1, dq2, lo2, hi2))
+    return coplanar_tri_tri(n1, p, q);
+  return hi1 > lo2 + kEps && hi2 > lo1 + kEps;
+}
+
+// ---------------------------------------------------------- BVH-vs-BVH collide
+// MeshBvh::collide (collision.cpp:285-329) over the effective DAGs of A (candidate, frame
+// of reference) and B (placed object, posed by M = other_in_self). Each node pair is
+// visited once (the reference revisits pairs reachable along several {left, left+1}
+// paths; the boolean result is the same existential). Pairs are processed in
+// lexicographic (a, b) order, which is a topological order of the pair DAG because every
+// child id exceeds its parent's, so a pending bit is never set after it was consumed.
+__device__ __forceinline__ bool collide(const SbNode* __restrict__ A, int nA,
+                                        const SbNode* __restrict__ B,
+                                        const SbTri* __restrict__ trisA,
+                                        const SbTri* __restrict__ trisB, const M34& M,
+                                        uint64_t& pair_tests) {
+  uint32_t pend[SB_MAX_NODES_PER_GEOM];
+  for (int a = 0; a < nA; ++a) pend[a] = 0u;
+  pend[0] = 1u;
+  for (int a = 0; a < nA; ++a) {
+    while (pend[a] != 0u) {
+      const int b = __ffs(pend[a]) - 1;
+      pend[a] &= pend[a] - 1u;
+      const SbNode& na = A[a];
+      const SbNode& nb = B[b];
+      double bmn[3], bmx[3];
+      xform_aabb(M, nb.c, nb.h, bmn, bmx);
+      if (!overlaps(na.bmin, na.bmax, bmn, bmx)) continue;
+      const bool la = na.child0 < 0, lb = nb.child0 < 0;
+      if (la && lb) {
+        for (int j = 0; j < nb.tri_count; ++j) {
+          const double* tb = trisB[nb.tri_start + j].v;
+          double q[9];
+          xform(M, tb[0], tb[1], tb[2], q[0], q[1], q[2]);
+          xform(M, tb[3], tb[4], tb[5], q[3], q[4], q[5]);
+          xform(M, tb[6], tb[7], tb[8], q[6], q[7], q[8]);
+          for (int i = 0; i < na.tri_count; ++i) {
+            ++pair_tests;
+            if (tri_tri_intersect(trisA[na.tri_start + i].v, q)) return true;
+          }
+        }
+      } else {
+        bool descend_a = lb;
+        if (!descend_a && !la) {
+          double e0 = bmx[0] - bmn[0], e1 = bmx[1] - bmn[1], e2 = bmx[2] - bmn[2];
+          descend_a = na.ext2 >= (e0 * e0 + e1 * e1) + e2 * e2;
+        }
+        if (descend_a) {
+          pend[na.child0] |= 1u << b;
+          pend[na.child1] |= 1u << b;
+        } else {
+          pend[a] |= (1u << nb.child0) | (1u << nb.child1);
+        }
+      }
+    }
+  }
+  return false;
+}
+
+// ------------------------------------------------------------------ world view
+using WorldView = SbWorldView;
+
+struct CheckCounters {
+  uint64_t narrow;
+  uint64_t pairs;
+};
+
+// One candidate of CollisionWorld::check_batch (collision.cpp:433-449): candidate box,
+// inverse pose, then every enabled object in ascending id order, AABB broad phase, BVH
+// narrow phase; returns the first colliding object or -1.
+__device__ __forceinline__ int check_candidate(const WorldView& w, int32_t geom, const M34& pose,
+                                               uint64_t inst, CheckCounters& cnt) {
+  const SbGeom g = w.geoms[geom];
+  double cmn[3], cmx[3];
+  xform_aabb(pose, g.box_c, g.box_h, cmn, cmx);
+  M34 inv;
+  inverse_rigid(pose, inv);
+  const SbNode* nA = w.nodes + g.node_offset;
+  const SbTri* tA = w.tris + g.tri_offset;
+  for (int ob0 = 0; ob0 < w.n_objects; ob0 += 32) {
+    uint32_t bits = w.enabled[(uint64_t)(ob0 >> 5) * w.n + inst];
+    while (bits) {
+      const int ob = ob0 + __ffs(bits) - 1;
+      bits &= bits - 1u;
+      const double2* bp = reinterpret_cast<const double2*>(w.box + ((uint64_t)ob * w.n + inst) * 6);
+      double2 b0 = bp[0], b1 = bp[1], b2 = bp[2];
+      double omn[3] = {b0.x, b0.y, b1.x}, omx[3] = {b1.y, b2.x, b2.y};
+      if (!overlaps(cmn, cmx, omn, omx)) continue;
+      ++cnt.narrow;
+      const double2* pp =
+          reinterpret_cast<const double2*>(w.pose + ((uint64_t)ob * w.n + inst) * 12);
+      M34 P;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        double2 v = pp[k];
+        P.m[2 * k] = v.x;
+        P.m[2 * k + 1] = v.y;
+      }
+      M34 rel;
+      mul34(inv, P, rel);
+      const SbGeom gb = w.geoms[w.obj_geom[ob]];
+      if (collide(nA, g.n_nodes, w.nodes + gb.node_offset, tA, w.tris + gb.tri_offset, rel,
+                  cnt.pairs))
+        return ob;
+    }
+  }
+  return -1;
+}
+
+// Store an accepted pose: record + world box (update_transform, collision.cpp:408-412).
+__device__ __forceinline__ void store_pose(const WorldView& w, int32_t obj, uint64_t inst,
+                                           const M34& P) {
+  double2* pp = reinterpret_cast<double2*>(w.pose + ((uint64_t)obj * w.n + inst) * 12);
+#pragma unroll
+  for (int k = 0; k < 6; ++k) pp[k] = make_double2(P.m[2 * k], P.m[2 * k + 1]);
+  const SbGeom g = w.geoms[w.obj_geom[obj]];
+  double mn[3], mx[3];
+  xform_aabb(P, g.box_c, g.box_h, mn, mx);
+  double2* bp = reinterpret_cast<double2*>(w.box + ((uint64_t)obj * w.n + inst) * 6);
+  bp[0] = make_double2(mn[0], mn[1]);
+  bp[1] = make_double2(mn[2], mx[0]);
+  bp[2] = make_double2(mx[1], mx[2]);
+}
+
+// Column-major Mat4 (16 doubles) -> 3x4 row-major record.
+__device__ __forceinline__ void from_colmajor(const double* c, M34& P) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) P.m[4 * i + j] = c[4 * j + i];
+}
+
+}  // namespace sbd

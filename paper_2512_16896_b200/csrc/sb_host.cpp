@@ -1,0 +1,317 @@
+// Host-side geometry preparation. See sb_host.hpp.
+#include "sb_host.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <stdexcept>
+
+#include "sb_poly.h"
+
+namespace sbh {
+
+uint64_t mix64(uint64_t x) {  // rng.hpp:9-14
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+Mesh make_box(double sx, double sy, double sz) {  // trimesh.cpp:40-53
+  Mesh m;
+  double x = sx / 2, y = sy / 2, z = sz / 2;
+  m.v = {{-x, -y, -z}, {x, -y, -z}, {x, y, -z}, {-x, y, -z},
+         {-x, -y, z},  {x, -y, z},  {x, y, z},  {-x, y, z}};
+  m.t = {{0, 2, 1}, {0, 3, 2}, {4, 5, 6}, {4, 6, 7}, {0, 1, 5}, {0, 5, 4},
+         {2, 3, 7}, {2, 7, 6}, {1, 2, 6}, {1, 6, 5}, {3, 0, 4}, {3, 4, 7}};
+  return m;
+}
+
+Mesh make_cylinder(double radius, double height, int segments) {  // trimesh.cpp:55-76
+  if (segments < 3) throw std::invalid_argument("make_cylinder: segments must be >= 3");
+  Mesh m;
+  double h = height / 2;
+  for (int i = 0; i < segments; ++i) {
+    double a = 2.0 * M_PI * i / segments;
+    m.v.push_back({radius * std::cos(a), radius * std::sin(a), -h});
+    m.v.push_back({radius * std::cos(a), radius * std::sin(a), h});
+  }
+  uint32_t bottom_c = static_cast<uint32_t>(m.v.size());
+  m.v.push_back({0, 0, -h});
+  uint32_t top_c = bottom_c + 1;
+  m.v.push_back({0, 0, h});
+  for (int i = 0; i < segments; ++i) {
+    uint32_t b0 = 2 * i, t0 = 2 * i + 1;
+    uint32_t b1 = 2 * ((i + 1) % segments), t1 = b1 + 1;
+    m.t.push_back({b0, b1, t1});
+    m.t.push_back({b0, t1, t0});
+    m.t.push_back({bottom_c, b1, b0});
+    m.t.push_back({top_c, t0, t1});
+  }
+  return m;
+}
+
+Mesh make_sphere(double radius, int stacks, int slices) {  // trimesh.cpp:78-104
+  if (stacks < 2 || slices < 3) throw std::invalid_argument("make_sphere: stacks>=2, slices>=3");
+  Mesh m;
+  m.v.push_back({0, 0, radius});
+  for (int s = 1; s < stacks; ++s) {
+    double phi = M_PI * s / stacks;
+    for (int k = 0; k < slices; ++k) {
+      double lam = 2.0 * M_PI * k / slices;
+      m.v.push_back({radius * std::sin(phi) * std::cos(lam), radius * std::sin(phi) * std::sin(lam),
+                     radius * std::cos(phi)});
+    }
+  }
+  uint32_t south = static_cast<uint32_t>(m.v.size());
+  m.v.push_back({0, 0, -radius});
+  auto ring = [&](int s, int k) -> uint32_t {
+    return 1 + static_cast<uint32_t>((s - 1) * slices + (k % slices));
+  };
+  for (int k = 0; k < slices; ++k) m.t.push_back({0, ring(1, k), ring(1, k + 1)});
+  for (int s = 1; s < stacks - 1; ++s)
+    for (int k = 0; k < slices; ++k) {
+      m.t.push_back({ring(s, k), ring(s + 1, k), ring(s + 1, k + 1)});
+      m.t.push_back({ring(s, k), ring(s + 1, k + 1), ring(s, k + 1)});
+    }
+  for (int k = 0; k < slices; ++k) m.t.push_back({south, ring(stacks - 1, k + 1), ring(stacks - 1, k)});
+  return m;
+}
+
+uint64_t mesh_fingerprint(const Mesh& m) {  // trimesh.cpp:120-135
+  static_assert(sizeof(V3) == 24 && sizeof(std::array<uint32_t, 3>) == 12, "packed layout");
+  uint64_t h = 0x6a09e667f3bcc908ULL;
+  auto feed = [&h](const void* p, std::size_t bytes) {
+    const unsigned char* c = static_cast<const unsigned char*>(p);
+    for (std::size_t i = 0; i + 8 <= bytes; i += 8) {
+      uint64_t w;
+      std::memcpy(&w, c + i, 8);
+      h = mix64(h ^ w);
+    }
+  };
+  h = mix64(h ^ m.v.size());
+  h = mix64(h ^ m.t.size());
+  if (!m.v.empty()) feed(m.v.data(), m.v.size() * sizeof(V3));
+  if (!m.t.empty()) feed(m.t.data(), m.t.size() * 12);
+  return h;
+}
+
+namespace {
+inline V3 sub(const V3& a, const V3& b) { return {a[0] - b[0], a[1] - b[1], a[2] - b[2]}; }
+inline V3 cross(const V3& a, const V3& b) {
+  return {a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2], a[0] * b[1] - a[1] * b[0]};
+}
+inline double sqnorm(const V3& a) { return a[0] * a[0] + a[1] * a[1] + a[2] * a[2]; }
+// std::min / std::max semantics of Eigen's cwiseMin / cwiseMax.
+inline void expand(double mn[3], double mx[3], const V3& p) {
+  for (int k = 0; k < 3; ++k) {
+    mn[k] = std::min(mn[k], p[k]);
+    mx[k] = std::max(mx[k], p[k]);
+  }
+}
+constexpr double kInf = std::numeric_limits<double>::infinity();
+}  // namespace
+
+std::size_t drop_degenerate(Mesh& m, double area_eps) {  // trimesh.cpp:16-29
+  std::size_t before = m.t.size();
+  std::vector<std::array<uint32_t, 3>> kept;
+  kept.reserve(before);
+  for (const auto& t : m.t) {
+    if (t[0] >= m.v.size() || t[1] >= m.v.size() || t[2] >= m.v.size()) continue;
+    V3 e1 = sub(m.v[t[1]], m.v[t[0]]);
+    V3 e2 = sub(m.v[t[2]], m.v[t[0]]);
+    if (0.5 * std::sqrt(sqnorm(cross(e1, e2))) <= area_eps) continue;
+    kept.push_back(t);
+  }
+  m.t.swap(kept);
+  return before - m.t.size();
+}
+
+void mesh_aabb(const Mesh& m, double box[6]) {
+  double mn[3] = {kInf, kInf, kInf}, mx[3] = {-kInf, -kInf, -kInf};
+  for (const auto& v : m.v) expand(mn, mx, v);
+  for (int k = 0; k < 3; ++k) {
+    box[k] = mn[k];
+    box[3 + k] = mx[k];
+  }
+}
+
+// ---------------------------------------------------------------------------- BVH
+namespace {
+struct RefNode {
+  double mn[3], mx[3];
+  int left = -1;
+  uint32_t start = 0, count = 0;
+};
+
+struct Builder {
+  const Mesh& mesh;
+  const std::vector<V3>& centroids;
+  std::vector<RefNode>& nodes;
+  std::vector<uint32_t>& leaf_tris;  // mesh triangle ids in leaf order (tris_ order)
+  int max_depth = 0;
+
+  // collision.cpp:253-276 restated: median split on the longest centroid axis.
+  int build(std::vector<uint32_t>& tris, uint32_t begin, uint32_t end, int depth) {
+    max_depth = std::max(max_depth, depth);
+    int idx = static_cast<int>(nodes.size());
+    nodes.emplace_back();
+    double mn[3] = {kInf, kInf, kInf}, mx[3] = {-kInf, -kInf, -kInf};
+    for (uint32_t i = begin; i < end; ++i) {
+      // tri_box then Aabb3::expand(Aabb3): cwiseMin/cwiseMax of the boxes
+      double tmn[3] = {kInf, kInf, kInf}, tmx[3] = {-kInf, -kInf, -kInf};
+      for (uint32_t vi : mesh.t[tris[i]]) expand(tmn, tmx, mesh.v[vi]);
+      for (int k = 0; k < 3; ++k) {
+        mn[k] = std::min(mn[k], tmn[k]);
+        mx[k] = std::max(mx[k], tmx[k]);
+      }
+    }
+    std::memcpy(nodes[idx].mn, mn, sizeof mn);
+    std::memcpy(nodes[idx].mx, mx, sizeof mx);
+    if (end - begin <= 4) {
+      nodes[idx].start = static_cast<uint32_t>(leaf_tris.size());
+      nodes[idx].count = end - begin;
+      for (uint32_t i = begin; i < end; ++i) leaf_tris.push_back(tris[i]);
+      return idx;
+    }
+    double cmn[3] = {kInf, kInf, kInf}, cmx[3] = {-kInf, -kInf, -kInf};
+    for (uint32_t i = begin; i < end; ++i) expand(cmn, cmx, centroids[tris[i]]);
+    double ext[3] = {cmx[0] - cmn[0], cmx[1] - cmn[1], cmx[2] - cmn[2]};
+    int axis = 0;
+    if (ext[1] > ext[0]) axis = 1;
+    if (ext[2] > ext[axis]) axis = 2;
+    uint32_t mid = (begin + end) / 2;
+    // Same libstdc++ nth_element as the reference build -> same permutation.
+    std::nth_element(tris.begin() + begin, tris.begin() + mid, tris.begin() + end,
+                     [&](uint32_t a, uint32_t b) { return centroids[a][axis] < centroids[b][axis]; });
+    int left = build(tris, begin, mid, depth + 1);
+    nodes[idx].left = left;
+    build(tris, mid, end, depth + 1);
+    return idx;
+  }
+};
+}  // namespace
+
+EffectiveBvh build_effective_bvh(const Mesh& mesh) {
+  if (mesh.t.empty()) throw std::invalid_argument("MeshBvh: empty mesh");
+  const std::size_t n = mesh.t.size();
+  std::vector<V3> centroids(n);
+  std::vector<uint32_t> order(n);
+  for (std::size_t t = 0; t < n; ++t) {
+    const auto& tri = mesh.t[t];
+    const V3& a = mesh.v[tri[0]];
+    const V3& b = mesh.v[tri[1]];
+    const V3& c = mesh.v[tri[2]];
+    centroids[t] = {(a[0] + b[0] + c[0]) / 3.0, (a[1] + b[1] + c[1]) / 3.0,
+                    (a[2] + b[2] + c[2]) / 3.0};
+    order[t] = static_cast<uint32_t>(t);
+  }
+  std::vector<RefNode> nodes;
+  nodes.reserve(2 * n);
+  std::vector<uint32_t> leaf_tris;
+  leaf_tris.reserve(n);
+  Builder b{mesh, centroids, nodes, leaf_tris};
+  b.build(order, 0, static_cast<uint32_t>(n), 1);
+
+  // Reachable set under the reference's child indexing {left, left+1}.
+  std::vector<char> reach(nodes.size(), 0);
+  std::vector<int> stack{0};
+  while (!stack.empty()) {
+    int i = stack.back();
+    stack.pop_back();
+    if (reach[i]) continue;
+    reach[i] = 1;
+    if (nodes[i].left >= 0) {
+      stack.push_back(nodes[i].left);
+      stack.push_back(nodes[i].left + 1);
+    }
+  }
+  std::vector<int> compact(nodes.size(), -1);
+  EffectiveBvh out;
+  out.full_nodes = static_cast<int>(nodes.size());
+  out.full_depth = b.max_depth;
+  for (std::size_t i = 0; i < nodes.size(); ++i)
+    if (reach[i]) compact[i] = static_cast<int>(out.nodes.size()), out.nodes.emplace_back();
+  for (std::size_t i = 0; i < nodes.size(); ++i) {
+    if (!reach[i]) continue;
+    const RefNode& r = nodes[i];
+    SbNode& d = out.nodes[compact[i]];
+    std::memset(&d, 0, sizeof d);
+    for (int k = 0; k < 3; ++k) {
+      d.bmin[k] = r.mn[k];
+      d.bmax[k] = r.mx[k];
+      d.c[k] = (r.mn[k] + r.mx[k]) * 0.5;  // Aabb3::center: 0.5 * (min + max)
+      d.h[k] = (r.mx[k] - r.mn[k]) * 0.5;  // 0.5 * extent()
+    }
+    double e0 = r.mx[0] - r.mn[0], e1 = r.mx[1] - r.mn[1], e2 = r.mx[2] - r.mn[2];
+    d.ext2 = e0 * e0 + e1 * e1 + e2 * e2;
+    if (r.left >= 0) {
+      d.child0 = compact[r.left];
+      d.child1 = compact[r.left + 1];
+      d.tri_start = d.tri_count = 0;
+    } else {
+      d.child0 = d.child1 = -1;
+      d.tri_start = static_cast<int32_t>(out.tris.size());
+      d.tri_count = static_cast<int32_t>(r.count);
+      for (uint32_t k = 0; k < r.count; ++k) {
+        const auto& tri = mesh.t[leaf_tris[r.start + k]];
+        SbTri t;
+        for (int v = 0; v < 3; ++v)
+          for (int c = 0; c < 3; ++c) t.v[3 * v + c] = mesh.v[tri[v]][c];
+        out.tris.push_back(t);
+      }
+    }
+  }
+  out.reachable_tris = static_cast<int>(out.tris.size());
+  return out;
+}
+
+// ----------------------------------------------------------------- triangulation
+std::vector<std::array<V2, 3>> triangulate_ring(const std::vector<V2>& ring) {
+  std::vector<std::array<V2, 3>> tris;
+  if (ring.size() < 3 || ring.size() > static_cast<std::size_t>(sbp::kCap))
+    throw std::invalid_argument("triangulate_ring: ring size outside [3, capacity]");
+  static thread_local sbp::Ring r;
+  r.n = static_cast<int>(ring.size());
+  for (int i = 0; i < r.n; ++i) {
+    r.x[i] = ring[i][0];
+    r.y[i] = ring[i][1];
+  }
+  SbRegionTri buf[sbp::kCap];
+  double cum[sbp::kCap];
+  // Capture every emitted triangle (the sink drops zero-area ones, so use a raw copy).
+  sbp::TableSink sink{buf, cum, 0, sbp::kCap, 0.0};
+  // ear_clip_into filters zero-area triangles through the sink; triangulate() itself does
+  // not, but PolygonSampler (its only hot-path consumer) does, so tables are identical.
+  if (!sbp::ear_clip_into(r, sink)) throw std::runtime_error("triangulate_ring: overflow");
+  for (int i = 0; i < sink.n; ++i)
+    tris.push_back({V2{buf[i].a[0], buf[i].a[1]}, V2{buf[i].b[0], buf[i].b[1]},
+                    V2{buf[i].c[0], buf[i].c[1]}});
+  return tris;
+}
+
+SamplerTable sampler_table(const std::vector<std::vector<V2>>& part_rings) {
+  SamplerTable out;
+  std::vector<SbRegionTri> buf(sbp::kCap * part_rings.size() + 1);
+  std::vector<double> cum(buf.size());
+  sbp::TableSink sink{buf.data(), cum.data(), 0, static_cast<int>(buf.size()), 0.0};
+  static thread_local sbp::Ring r;
+  for (const auto& ring : part_rings) {
+    if (ring.size() < 3) continue;
+    if (ring.size() > static_cast<std::size_t>(sbp::kCap))
+      throw std::invalid_argument("sampler_table: ring exceeds capacity");
+    r.n = static_cast<int>(ring.size());
+    for (int i = 0; i < r.n; ++i) {
+      r.x[i] = ring[i][0];
+      r.y[i] = ring[i][1];
+    }
+    if (!sbp::ear_clip_into(r, sink)) throw std::runtime_error("sampler_table: overflow");
+  }
+  int n = sbp::finish_table(sink);
+  out.tris.assign(buf.begin(), buf.begin() + n);
+  out.cum.assign(cum.begin(), cum.begin() + n);
+  return out;
+}
+
+}  // namespace sbh

@@ -1,0 +1,61 @@
+// Host-side geometry preparation for the B200 hot path (C++, no CUDA).
+//
+// Everything here runs once per geometry / support (cold start), and produces the
+// flat, device-ready tables the kernels read. Arithmetic is written operation by
+// operation so that results are bit-identical to the reference built without FMA
+// (the reference's Eigen expressions reduce left to right -- see oracle/shim/Eigen/Dense).
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "sb_layout.h"
+
+namespace sbh {
+
+using V3 = std::array<double, 3>;
+using V2 = std::array<double, 2>;
+
+struct Mesh {
+  std::vector<V3> v;
+  std::vector<std::array<uint32_t, 3>> t;
+};
+
+// trimesh.cpp:40-104 (make_box / make_cylinder / make_sphere)
+Mesh make_box(double sx, double sy, double sz);
+Mesh make_cylinder(double radius, double height, int segments);
+Mesh make_sphere(double radius, int stacks, int slices);
+// trimesh.cpp:120-135
+uint64_t mesh_fingerprint(const Mesh& m);
+// trimesh.cpp:16-29 (returns number removed)
+std::size_t drop_degenerate(Mesh& m, double area_eps = 1e-12);
+// TriMesh::aabb (trimesh.cpp:10-14); box[0..2] = min, box[3..5] = max
+void mesh_aabb(const Mesh& m, double box[6]);
+
+// Reference-identical MeshBvh (collision.cpp:217-281), then the "effective DAG": the
+// nodes reachable from the root when children are read as {left, left+1}
+// (collision.hpp:46, collision.cpp:320-324) -- the reference's actual traversal graph.
+struct EffectiveBvh {
+  std::vector<SbNode> nodes;     // compact, topologically ordered (parents first)
+  std::vector<SbTri> tris;       // triangles of reachable leaves, grouped per leaf
+  int full_nodes = 0;            // nodes in the reference BVH
+  int full_depth = 0;            // MeshBvh::depth()
+  int reachable_tris = 0;
+};
+EffectiveBvh build_effective_bvh(const Mesh& m);
+
+// triangulate(Polygon2D) for a single simple ring (polygon.cpp:260-368, no holes).
+std::vector<std::array<V2, 3>> triangulate_ring(const std::vector<V2>& ring);
+// PolygonSampler ctor (polygon.cpp:370-388): triangles with positive area + cum table.
+struct SamplerTable {
+  std::vector<SbRegionTri> tris;
+  std::vector<double> cum;
+};
+SamplerTable sampler_table(const std::vector<std::vector<V2>>& part_rings);
+
+// splitmix64 / make_stream seed derivation (rng.hpp:9-21,63-67)
+uint64_t mix64(uint64_t x);
+
+}  // namespace sbh

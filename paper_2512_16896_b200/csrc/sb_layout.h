@@ -1,0 +1,66 @@
+// Device-resident table layouts shared by the host preparation code and the kernels.
+// Plain PODs, no CUDA types, so both g++ and nvcc compile them.
+#pragma once
+
+#include <stdint.h>
+
+// One node of a geometry's effective BVH DAG (see sb_host.hpp).
+struct SbNode {
+  double bmin[3], bmax[3];  // node box, A-side overlap test (aabb.hpp:29-33)
+  double c[3], h[3];        // 0.5*(min+max), 0.5*(max-min): B-side transform_aabb
+  double ext2;              // box.extent().squaredNorm(): descent rule (collision.cpp:320)
+  int32_t child0, child1;   // compact child ids, -1 for a leaf
+  int32_t tri_start, tri_count;
+  int32_t pad[2];
+};
+
+struct SbTri {
+  double v[9];  // p0.xyz p1.xyz p2.xyz in the mesh frame
+};
+
+struct SbGeom {
+  int32_t node_offset, n_nodes;
+  int32_t tri_offset, n_tris;
+  double box_c[3], box_h[3];   // local_box center / half extent (transform_aabb)
+  double box_min[3], box_max[3];
+};
+
+// Region triangle for the exact-uniform polygon sampler (polygon.cpp:336-338).
+struct SbRegionTri {
+  double a[2], b[2], c[2];
+};
+
+// Placement descriptor consumed by the generation kernels.
+struct SbPlacementDev {
+  int32_t geom;            // candidate geometry
+  int32_t object;          // world object id receiving accepted poses
+  int32_t orientation;     // SB_ORIENT_*
+  int32_t face_object;     // world object id of the face_to target, -1
+  double z_off;            // rest_pose z offset (sampler.cpp:45-52)
+  double support[12];      // support frame -> world, row-major 3x4
+  double rect[4];          // support rect x0 y0 x1 y1
+  // relation (relationships.hpp:18-38), single anchor
+  int32_t anchor_object;   // world object id of the anchor, -1 = none
+  int32_t distance_type, direction, frame;
+  double direction_vector[2];
+  double distance;
+  double angle_threshold;  // <= 0: default
+  uint64_t salt;           // placement index (Appendix C)
+};
+
+// Device view of a collision world (plain pointers; built by the host World class).
+struct SbWorldView {
+  uint64_t n;                // instances held on this device
+  int32_t n_objects;
+  int32_t n_words;           // enable-bit words per instance = ceil(n_objects / 32)
+  const int32_t* obj_geom;   // [n_objects]
+  double* pose;              // [object][n][12]  row-major 3x4 [R | t]
+  double* box;               // [object][n][6]   world AABB min xyz, max xyz
+  uint32_t* enabled;         // [word][n]        bit (object & 31) of word (object >> 5)
+  const SbGeom* geoms;
+  const SbNode* nodes;
+  const SbTri* tris;
+};
+
+#define SB_MAX_NODES_PER_GEOM 32   // effective DAG nodes (bitmask traversal width)
+#define SB_REGION_MAX_VERTS 96     // per-instance constraint region ring capacity

@@ -1,0 +1,322 @@
+// Constraint-region polygon pipeline, shared by host preparation (g++) and the
+// per-instance region kernel (nvcc): annulus sector -> clip to the support rect ->
+// ear-clipping triangulation -> exact-uniform sampler table -> draw.
+//
+// Each function restates the reference operation by operation (no FMA: host built with
+// -ffp-contract=off, device with -fmad=false) so a region built here is bit-identical to
+// the reference's, up to the libm used for sin/cos/atan2.
+// Fixed-capacity arrays (SB_REGION_MAX_VERTS) keep it allocation-free on the device.
+#pragma once
+
+#include <math.h>
+#include <stdint.h>
+
+#include "sb_layout.h"
+
+#ifdef __CUDACC__
+#define SB_HD __host__ __device__ __forceinline__
+#else
+#define SB_HD inline
+#endif
+
+namespace sbp {
+
+constexpr double kPi = 3.14159265358979323846;  // M_PI
+constexpr int kCap = SB_REGION_MAX_VERTS;
+
+struct Ring {
+  double x[kCap];
+  double y[kCap];
+  int n;
+};
+
+enum RegionStatus { kRegionOk = 0, kRegionEmpty = 1, kRegionOverflow = 2, kRegionBadArg = 3 };
+
+// cross2 (polygon.cpp:54-56)
+SB_HD double cross2(double ox, double oy, double ax, double ay, double bx, double by) {
+  return (ax - ox) * (by - oy) - (ay - oy) * (bx - ox);
+}
+
+// ring_area (polygon.cpp:58-66); shoelace, left to right.
+SB_HD double ring_area(const Ring& r) {
+  double s = 0.0;
+  for (int i = 0; i < r.n; ++i) {
+    int j = (i + 1) % r.n;
+    s += r.x[i] * r.y[j] - r.x[j] * r.y[i];
+  }
+  return 0.5 * s;
+}
+
+SB_HD void reverse_ring(Ring& r) {
+  for (int i = 0, j = r.n - 1; i < j; ++i, --j) {
+    double tx = r.x[i], ty = r.y[i];
+    r.x[i] = r.x[j];
+    r.y[i] = r.y[j];
+    r.x[j] = tx;
+    r.y[j] = ty;
+  }
+}
+
+SB_HD bool push(Ring& r, double x, double y) {
+  if (r.n >= kCap) return false;
+  r.x[r.n] = x;
+  r.y[r.n] = y;
+  ++r.n;
+  return true;
+}
+
+// annulus_sector (polygon.cpp:136-176) for the non-full case and the full disc without
+// a hole. clip_diag = clip_bound.diagonal() (only used when max_r is infinite).
+SB_HD int annulus_sector(double cx, double cy, double vx, double vy, double theta, double min_r,
+                         double max_r, double clip_diag, Ring& out) {
+  out.n = 0;
+  if (!(theta > 0.0) || theta > kPi + 1e-12) return kRegionBadArg;
+  if (isinf(max_r)) max_r = fmax(clip_diag, min_r + 1e-6);
+  if (!(min_r < max_r)) return kRegionBadArg;
+  double base = atan2(vy, vx);
+  bool full = theta >= kPi - 1e-12;
+  double step = 5.0 * kPi / 180.0;
+  auto arc = [&](double radius, double a0, double a1) -> bool {
+    double span = fabs(a1 - a0) / step;
+    int n = (int)ceil(span);
+    if (n < 1) n = 1;
+    for (int i = 0; i <= n; ++i) {
+      double a = a0 + (a1 - a0) * (double)i / (double)n;
+      if (!push(out, cx + radius * cos(a), cy + radius * sin(a))) return false;
+    }
+    return true;
+  };
+  if (full) {
+    if (min_r > 0.0) return kRegionBadArg;  // annulus with a hole: not on the device path
+    if (!arc(max_r, 0.0, 2.0 * kPi)) return kRegionOverflow;
+    out.n -= 1;  // closing vertex
+    return kRegionOk;
+  }
+  if (!arc(max_r, base - theta, base + theta)) return kRegionOverflow;
+  if (min_r > 0.0) {
+    if (!arc(min_r, base + theta, base - theta)) return kRegionOverflow;
+  } else {
+    if (!push(out, cx, cy)) return kRegionOverflow;
+  }
+  return kRegionOk;
+}
+
+// One Sutherland-Hodgman pass against an axis-aligned half plane; the stand-in for
+// Boost intersection documented in oracle/shim/boost/geometry.hpp (same operation order).
+SB_HD bool clip_half(const Ring& in, Ring& out, int axis, double bound, bool keep_ge) {
+  out.n = 0;
+  int n = in.n;
+  for (int i = 0; i < n; ++i) {
+    int ip = (i + n - 1) % n;
+    double cur_a = axis == 0 ? in.x[i] : in.y[i];
+    double prv_a = axis == 0 ? in.x[ip] : in.y[ip];
+    bool ci = keep_ge ? cur_a >= bound : cur_a <= bound;
+    bool pi = keep_ge ? prv_a >= bound : prv_a <= bound;
+    if (ci != pi) {
+      double prv_o = axis == 0 ? in.y[ip] : in.x[ip];
+      double cur_o = axis == 0 ? in.y[i] : in.x[i];
+      double t = (bound - prv_a) / (cur_a - prv_a);
+      double o = prv_o + t * (cur_o - prv_o);
+      bool ok = axis == 0 ? push(out, bound, o) : push(out, o, bound);
+      if (!ok) return false;
+    }
+    if (ci && !push(out, in.x[i], in.y[i])) return false;
+  }
+  return true;
+}
+
+// intersect(ring, rect) as the oracle stand-in defines it: correct() orientation,
+// 4 half-plane passes (x>=x0, x<=x1, y>=y0, y<=y1), drop consecutive exact duplicates,
+// discard < 3 vertices or zero area. Result in `r` (open ring). Uses `tmp` as scratch.
+SB_HD int intersect_rect(Ring& r, Ring& tmp, const double rect[4]) {
+  if (r.n < 3) return kRegionEmpty;
+  // bg::correct (via to_boost, polygon.cpp:27-36) reverses the CLOSED ring, which keeps
+  // vertex 0 first: [p0, p(n-1), ..., p1].
+  if (ring_area(r) < 0.0) {
+    for (int i = 1, j = r.n - 1; i < j; ++i, --j) {
+      double tx = r.x[i], ty = r.y[i];
+      r.x[i] = r.x[j];
+      r.y[i] = r.y[j];
+      r.x[j] = tx;
+      r.y[j] = ty;
+    }
+  }
+  double x0 = fmin(rect[0], rect[2]);
+  double x1 = fmax(rect[0], rect[2]);
+  double y0 = fmin(rect[1], rect[3]);
+  double y1 = fmax(rect[1], rect[3]);
+  if (!clip_half(r, tmp, 0, x0, true)) return kRegionOverflow;
+  if (!clip_half(tmp, r, 0, x1, false)) return kRegionOverflow;
+  if (!clip_half(r, tmp, 1, y0, true)) return kRegionOverflow;
+  if (!clip_half(tmp, r, 1, y1, false)) return kRegionOverflow;
+  int m = 0;
+  for (int i = 0; i < r.n; ++i) {
+    if (m == 0 || r.x[i] != r.x[m - 1] || r.y[i] != r.y[m - 1]) {
+      r.x[m] = r.x[i];
+      r.y[m] = r.y[i];
+      ++m;
+    }
+  }
+  while (m > 1 && r.x[0] == r.x[m - 1] && r.y[0] == r.y[m - 1]) --m;
+  r.n = m;
+  if (r.n < 3 || ring_area(r) == 0.0) return kRegionEmpty;
+  return kRegionOk;
+}
+
+// point_in_tri_strict (polygon.cpp:189-195)
+SB_HD bool point_in_tri_strict(double px, double py, double ax, double ay, double bx, double by,
+                               double cx, double cy) {
+  const double eps = 1e-12;
+  double d1 = cross2(ax, ay, bx, by, px, py);
+  double d2 = cross2(bx, by, cx, cy, px, py);
+  double d3 = cross2(cx, cy, ax, ay, px, py);
+  return d1 > eps && d2 > eps && d3 > eps;
+}
+
+// Sampler table being built: triangles with positive area and their cumulative areas
+// (PolygonSampler ctor, polygon.cpp:370-388). Caller provides storage for kCap-2 tris.
+struct TableSink {
+  SbRegionTri* tris;
+  double* cum;
+  int n;
+  int cap;
+  double total;
+};
+
+SB_HD bool sink_tri(TableSink& s, double ax, double ay, double bx, double by, double cx,
+                    double cy) {
+  double a = 0.5 * fabs(cross2(ax, ay, bx, by, cx, cy));
+  if (a <= 0.0) return true;
+  if (s.n >= s.cap) return false;
+  SbRegionTri& t = s.tris[s.n];
+  t.a[0] = ax;
+  t.a[1] = ay;
+  t.b[0] = bx;
+  t.b[1] = by;
+  t.c[0] = cx;
+  t.c[1] = cy;
+  s.total += a;
+  s.cum[s.n] = s.total;
+  ++s.n;
+  return true;
+}
+
+// triangulate() of a hole-free polygon (polygon.cpp:344-368) feeding ear_clip_ring
+// (polygon.cpp:260-340) straight into the sampler table. `r` is consumed.
+SB_HD bool ear_clip_into(Ring& r, TableSink& sink) {
+  if (r.n < 3) return true;
+  if (ring_area(r) < 0.0) reverse_ring(r);
+  // drop consecutive duplicates (squared distance <= 1e-24)
+  int n = 0;
+  for (int i = 0; i < r.n; ++i) {
+    if (n > 0) {
+      double dx = r.x[i] - r.x[n - 1], dy = r.y[i] - r.y[n - 1];
+      if (!(dx * dx + dy * dy > 1e-24)) continue;
+    }
+    r.x[n] = r.x[i];
+    r.y[n] = r.y[i];
+    ++n;
+  }
+  while (n > 1) {
+    double dx = r.x[0] - r.x[n - 1], dy = r.y[0] - r.y[n - 1];
+    if (dx * dx + dy * dy <= 1e-24) --n;
+    else break;
+  }
+  if (n < 3) return true;
+  int prv[kCap], nxt[kCap];
+  bool reflex[kCap];
+  for (int i = 0; i < n; ++i) {
+    prv[i] = (i + n - 1) % n;
+    nxt[i] = (i + 1) % n;
+  }
+  auto update_reflex = [&](int i) {
+    reflex[i] = cross2(r.x[prv[i]], r.y[prv[i]], r.x[i], r.y[i], r.x[nxt[i]], r.y[nxt[i]]) < 0.0;
+  };
+  for (int i = 0; i < n; ++i) update_reflex(i);
+  auto is_ear = [&](int i) -> bool {
+    if (reflex[i]) return false;
+    int p = prv[i], q = nxt[i];
+    double ax = r.x[p], ay = r.y[p], bx = r.x[i], by = r.y[i], cx = r.x[q], cy = r.y[q];
+    if (fabs(cross2(ax, ay, bx, by, cx, cy)) < 1e-18) return false;
+    for (int j = nxt[q]; j != p; j = nxt[j]) {
+      if (reflex[j] && point_in_tri_strict(r.x[j], r.y[j], ax, ay, bx, by, cx, cy)) return false;
+    }
+    return true;
+  };
+  int remaining = n, cur = 0, since_clip = 0;
+  while (remaining > 3) {
+    if (is_ear(cur)) {
+      int p = prv[cur], q = nxt[cur];
+      if (!sink_tri(sink, r.x[p], r.y[p], r.x[cur], r.y[cur], r.x[q], r.y[q])) return false;
+      nxt[p] = q;
+      prv[q] = p;
+      update_reflex(p);
+      update_reflex(q);
+      cur = q;
+      --remaining;
+      since_clip = 0;
+      continue;
+    }
+    cur = nxt[cur];
+    if (++since_clip > remaining) {
+      int best = -1;
+      double best_a = -1.0;
+      for (int j = cur, k = 0; k < remaining; j = nxt[j], ++k) {
+        if (reflex[j]) continue;
+        double a = cross2(r.x[prv[j]], r.y[prv[j]], r.x[j], r.y[j], r.x[nxt[j]], r.y[nxt[j]]);
+        if (a > best_a) {
+          best_a = a;
+          best = j;
+        }
+      }
+      if (best < 0) break;
+      int p = prv[best], q = nxt[best];
+      if (!sink_tri(sink, r.x[p], r.y[p], r.x[best], r.y[best], r.x[q], r.y[q])) return false;
+      nxt[p] = q;
+      prv[q] = p;
+      update_reflex(p);
+      update_reflex(q);
+      cur = q;
+      --remaining;
+      since_clip = 0;
+    }
+  }
+  if (remaining == 3) {
+    int p = prv[cur], q = nxt[cur];
+    if (!sink_tri(sink, r.x[p], r.y[p], r.x[cur], r.y[cur], r.x[q], r.y[q])) return false;
+  }
+  return true;
+}
+
+// Normalise the cumulative table (polygon.cpp:381-387). Returns the triangle count
+// (0 = invalid sampler, i.e. placeable == 0).
+SB_HD int finish_table(TableSink& s) {
+  if (s.total > 0.0) {
+    for (int k = 0; k < s.n; ++k) s.cum[k] /= s.total;
+    s.cum[s.n - 1] = 1.0;
+    return s.n;
+  }
+  s.n = 0;
+  return 0;
+}
+
+// PolygonSampler::draw (polygon.cpp:390-400) given the three uniforms.
+SB_HD void draw_point(const SbRegionTri* tris, const double* cum, int n, double u, double r1,
+                      double r2, double& px, double& py) {
+  int lo = 0, hi = n;  // lower_bound: first k with !(cum[k] < u)
+  while (lo < hi) {
+    int mid = lo + ((hi - lo) >> 1);
+    if (cum[mid] < u) lo = mid + 1;
+    else hi = mid;
+  }
+  int idx = lo < n - 1 ? lo : n - 1;
+  const SbRegionTri& t = tris[idx];
+  double s = sqrt(r1);
+  double wa = 1.0 - s;
+  double wb = s * (1.0 - r2);
+  double wc = s * r2;
+  px = t.a[0] * wa + t.b[0] * wb + t.c[0] * wc;
+  py = t.a[1] * wa + t.b[1] * wb + t.c[1] * wc;
+}
+
+}  // namespace sbp

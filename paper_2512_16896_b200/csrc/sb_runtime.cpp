@@ -1,0 +1,1005 @@
+// Host runtime + C ABI (include/scenebatch_b200.h). C++17, CUDA runtime API only.
+//
+// World  = CollisionWorld (collision.hpp:76-127) with all per-instance state in HBM.
+// Engine = the reference's absent rejection loop (contract frozen in
+//          DESIGN.md) driving the fused per-round kernel; one engine per GPU / shard.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/scenebatch_b200.h"
+#include "sb_host.hpp"
+#include "sb_kernels.h"
+#include "sb_layout.h"
+
+namespace {
+
+thread_local std::string g_error;
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw std::runtime_error(std::string("CUDA: ") + what + ": " + cudaGetErrorString(e));
+  }
+}
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+template <class T>
+struct DevArray {
+  T* p = nullptr;
+  size_t count = 0;
+  DevArray() = default;
+  DevArray(const DevArray&) = delete;
+  DevArray& operator=(const DevArray&) = delete;
+  ~DevArray() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    count = 0;
+  }
+  void alloc(size_t n) {
+    release();
+    if (n == 0) return;
+    cuda_check(cudaMalloc(&p, n * sizeof(T)), "cudaMalloc");
+    count = n;
+  }
+  void ensure(size_t n) {
+    if (n > count) alloc(n);
+  }
+};
+
+template <class T>
+struct PinnedArray {
+  T* p = nullptr;
+  size_t count = 0;
+  ~PinnedArray() {
+    if (p) cudaFreeHost(p);
+  }
+  void ensure(size_t n) {
+    if (n <= count) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cuda_check(cudaMallocHost(&p, n * sizeof(T)), "cudaMallocHost");
+    count = n;
+  }
+};
+
+void require_homogeneous(const double* p) {
+  if (p[3] != 0.0 || p[7] != 0.0 || p[11] != 0.0 || p[15] != 1.0)
+    throw std::invalid_argument("pose bottom row must be exactly (0,0,0,1)");
+  for (int k = 0; k < 16; ++k)
+    if (!std::isfinite(p[k])) throw std::invalid_argument("pose must be finite");
+}
+
+// inverse_rigid (transform.hpp:63-69) on the host, same operation order as the device.
+void inverse_rigid34(const double* colmajor16, double out[12]) {
+  double R[3][3], t[3];
+  for (int i = 0; i < 3; ++i) {
+    for (int j = 0; j < 3; ++j) R[i][j] = colmajor16[4 * j + i];
+    t[i] = colmajor16[12 + i];
+  }
+  for (int i = 0; i < 3; ++i) {
+    for (int k = 0; k < 3; ++k) out[4 * i + k] = R[k][i];
+    double s = (-R[0][i]) * t[0];
+    s = s + (-R[1][i]) * t[1];
+    s = s + (-R[2][i]) * t[2];
+    out[4 * i + 3] = s;
+  }
+}
+
+void colmajor_to_34(const double* c, double out[12]) {
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 4; ++j) out[4 * i + j] = c[4 * j + i];
+}
+
+int current_device_checked(int device) {
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    throw CudaError("no CUDA device available (this build has no CPU fallback)");
+  }
+  if (device < 0 || device >= count) throw std::out_of_range("device index out of range");
+  cudaDeviceProp prop;
+  cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+  if (prop.major != 10)
+    throw CudaError("device " + std::to_string(device) + " is sm_" + std::to_string(prop.major) +
+                    std::to_string(prop.minor) + "; this build targets sm_100a only");
+  cuda_check(cudaSetDevice(device), "cudaSetDevice");
+  return device;
+}
+
+}  // namespace
+
+// ===================================================================== World
+struct sb_world {
+  uint64_t n;
+  int device;
+  cudaStream_t stream = nullptr;
+  sb_stats stats{};
+
+  struct Geom {
+    sbh::Mesh mesh;  // after drop_degenerate
+    uint64_t fingerprint;
+    SbGeom g;
+  };
+  std::vector<Geom> geoms;
+  std::vector<SbNode> nodes;
+  std::vector<SbTri> tris;
+  std::vector<int32_t> obj_geom;
+  std::vector<std::string> obj_name;
+
+  DevArray<SbGeom> d_geoms;
+  DevArray<SbNode> d_nodes;
+  DevArray<SbTri> d_tris;
+  DevArray<int32_t> d_obj_geom;
+  DevArray<double> d_pose;
+  DevArray<double> d_box;
+  DevArray<uint32_t> d_enabled;
+  int cap_objects = 0;
+  int cap_words = 0;
+
+  DevArray<double> d_scratch_poses;
+  DevArray<uint32_t> d_scratch_idx;
+  DevArray<uint8_t> d_free;
+  DevArray<int32_t> d_contact;
+  DevArray<unsigned long long> d_counters;
+
+  sb_world(uint64_t batch, double margin, int dev) : n(batch), device(dev) {
+    if (batch == 0) throw std::invalid_argument("CollisionWorld: batch_size must be >= 1");
+    if (margin != 0.0)
+      throw std::invalid_argument("CollisionWorld: margin > 0 (tri_tri_distance path) is not built");
+    if (batch > 0xffffffffull) throw std::invalid_argument("CollisionWorld: batch_size > 2^32-1");
+    current_device_checked(dev);
+    cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    d_counters.alloc(4);
+  }
+  ~sb_world() {
+    if (stream) {
+      cudaSetDevice(device);
+      cudaStreamSynchronize(stream);
+      cudaStreamDestroy(stream);
+    }
+  }
+
+  void activate() const { cuda_check(cudaSetDevice(device), "cudaSetDevice"); }
+  sb_stream_t s() const { return reinterpret_cast<sb_stream_t>(stream); }
+
+  SbWorldView view() const {
+    SbWorldView v;
+    v.n = n;
+    v.n_objects = static_cast<int32_t>(obj_geom.size());
+    v.n_words = (v.n_objects + 31) / 32;
+    v.obj_geom = d_obj_geom.p;
+    v.pose = d_pose.p;
+    v.box = d_box.p;
+    v.enabled = d_enabled.p;
+    v.geoms = d_geoms.p;
+    v.nodes = d_nodes.p;
+    v.tris = d_tris.p;
+    return v;
+  }
+
+  const Geom& geom_at(int id) const {
+    if (id < 0 || static_cast<size_t>(id) >= geoms.size())
+      throw std::out_of_range("unknown geometry id " + std::to_string(id));
+    return geoms[id];
+  }
+  void object_check(int obj) const {
+    if (obj < 0 || static_cast<size_t>(obj) >= obj_geom.size())
+      throw std::out_of_range("unknown object id " + std::to_string(obj));
+  }
+  void instance_check(uint64_t inst) const {
+    if (inst >= n) throw std::out_of_range("instance index out of range");
+  }
+
+  // register_geometry (collision.cpp:339-355)
+  int register_geometry(sbh::Mesh mesh) {
+    if (mesh.t.empty()) throw std::invalid_argument("register_geometry: empty mesh");
+    uint64_t fp = sbh::mesh_fingerprint(mesh);
+    for (size_t i = 0; i < geoms.size(); ++i)
+      if (geoms[i].fingerprint == fp) return static_cast<int>(i);
+    sbh::drop_degenerate(mesh);
+    sbh::EffectiveBvh bvh = sbh::build_effective_bvh(mesh);
+    if (bvh.nodes.size() > SB_MAX_NODES_PER_GEOM)
+      throw std::invalid_argument("register_geometry: effective BVH has " +
+                                  std::to_string(bvh.nodes.size()) + " nodes (> " +
+                                  std::to_string(SB_MAX_NODES_PER_GEOM) + " supported)");
+    Geom g;
+    g.fingerprint = fp;
+    double box[6];
+    sbh::mesh_aabb(mesh, box);  // local_box = mesh.aabb() after drop_degenerate
+    std::memset(&g.g, 0, sizeof g.g);
+    for (int k = 0; k < 3; ++k) {
+      g.g.box_min[k] = box[k];
+      g.g.box_max[k] = box[3 + k];
+      g.g.box_c[k] = (box[k] + box[3 + k]) * 0.5;
+      g.g.box_h[k] = (box[3 + k] - box[k]) * 0.5;
+    }
+    g.g.node_offset = static_cast<int32_t>(nodes.size());
+    g.g.n_nodes = static_cast<int32_t>(bvh.nodes.size());
+    g.g.tri_offset = static_cast<int32_t>(tris.size());
+    g.g.n_tris = static_cast<int32_t>(bvh.tris.size());
+    nodes.insert(nodes.end(), bvh.nodes.begin(), bvh.nodes.end());
+    tris.insert(tris.end(), bvh.tris.begin(), bvh.tris.end());
+    g.mesh = std::move(mesh);
+    geoms.push_back(std::move(g));
+    activate();
+    cuda_check(cudaStreamSynchronize(stream), "sync");
+    std::vector<SbGeom> gs;
+    for (auto& x : geoms) gs.push_back(x.g);
+    d_geoms.alloc(gs.size());
+    d_nodes.alloc(nodes.size());
+    d_tris.alloc(tris.size());
+    cuda_check(cudaMemcpy(d_geoms.p, gs.data(), gs.size() * sizeof(SbGeom), cudaMemcpyHostToDevice), "H2D geoms");
+    cuda_check(cudaMemcpy(d_nodes.p, nodes.data(), nodes.size() * sizeof(SbNode), cudaMemcpyHostToDevice), "H2D nodes");
+    cuda_check(cudaMemcpy(d_tris.p, tris.data(), tris.size() * sizeof(SbTri), cudaMemcpyHostToDevice), "H2D tris");
+    ++stats.geometry_registrations;
+    ++stats.bvh_builds;
+    return static_cast<int>(geoms.size() - 1);
+  }
+
+  void grow_objects(int need) {
+    if (need <= cap_objects) return;
+    int cap = std::max(need, std::max(8, cap_objects * 2));
+    int words = (cap + 31) / 32;
+    activate();
+    cuda_check(cudaStreamSynchronize(stream), "sync");
+    DevArray<double> np, nb;
+    DevArray<uint32_t> ne;
+    np.alloc(static_cast<size_t>(cap) * n * 12);
+    nb.alloc(static_cast<size_t>(cap) * n * 6);
+    ne.alloc(static_cast<size_t>(words) * n);
+    cuda_check(cudaMemset(ne.p, 0, ne.count * sizeof(uint32_t)), "memset enabled");
+    if (cap_objects > 0) {
+      cuda_check(cudaMemcpy(np.p, d_pose.p, sizeof(double) * cap_objects * n * 12, cudaMemcpyDeviceToDevice), "D2D");
+      cuda_check(cudaMemcpy(nb.p, d_box.p, sizeof(double) * cap_objects * n * 6, cudaMemcpyDeviceToDevice), "D2D");
+      cuda_check(cudaMemcpy(ne.p, d_enabled.p, sizeof(uint32_t) * cap_words * n, cudaMemcpyDeviceToDevice), "D2D");
+    }
+    std::swap(d_pose.p, np.p);
+    std::swap(d_pose.count, np.count);
+    std::swap(d_box.p, nb.p);
+    std::swap(d_box.count, nb.count);
+    std::swap(d_enabled.p, ne.p);
+    std::swap(d_enabled.count, ne.count);
+    cap_objects = cap;
+    cap_words = words;
+  }
+
+  // add_object (collision.cpp:365-376)
+  int add_object(const std::string& name, int geom) {
+    geom_at(geom);
+    int id = static_cast<int>(obj_geom.size());
+    grow_objects(id + 1);
+    obj_geom.push_back(geom);
+    obj_name.push_back(name);
+    d_obj_geom.alloc(obj_geom.size());
+    cuda_check(cudaMemcpy(d_obj_geom.p, obj_geom.data(), obj_geom.size() * 4, cudaMemcpyHostToDevice), "H2D obj_geom");
+    sbk::init_object(view(), id, s());
+    return id;
+  }
+
+  void set_enabled(int obj, const uint32_t* inst, uint64_t m, bool en) {
+    object_check(obj);
+    for (uint64_t j = 0; j < m; ++j) instance_check(inst[j]);
+    if (m == 0) return;
+    activate();
+    d_scratch_idx.ensure(m);
+    cuda_check(cudaMemcpyAsync(d_scratch_idx.p, inst, m * 4, cudaMemcpyHostToDevice, stream), "H2D");
+    sbk::set_enabled_list(view(), obj, d_scratch_idx.p, m, en ? 1 : 0, s());
+    cuda_check(cudaStreamSynchronize(stream), "sync");
+  }
+  void set_enabled_all(int obj, bool en) {
+    object_check(obj);
+    activate();
+    sbk::set_enabled_all(view(), obj, en ? 1 : 0, s());
+  }
+  void upload_poses(const double* poses16, uint64_t m) {
+    for (uint64_t j = 0; j < m; ++j) require_homogeneous(poses16 + 16 * j);
+    d_scratch_poses.ensure(m * 16);
+    cuda_check(cudaMemcpyAsync(d_scratch_poses.p, poses16, m * 16 * sizeof(double), cudaMemcpyHostToDevice, stream), "H2D poses");
+  }
+  void update_transforms(int obj, const double* poses16) {
+    object_check(obj);
+    activate();
+    upload_poses(poses16, n);
+    sbk::update_transforms(view(), obj, d_scratch_poses.p, nullptr, n, 16, s());
+    cuda_check(cudaStreamSynchronize(stream), "sync");
+  }
+  void update_transform(int obj, uint64_t inst, const double* pose16) {
+    object_check(obj);
+    instance_check(inst);
+    activate();
+    upload_poses(pose16, 1);
+    d_scratch_idx.ensure(1);
+    uint32_t i32 = static_cast<uint32_t>(inst);
+    cuda_check(cudaMemcpyAsync(d_scratch_idx.p, &i32, 4, cudaMemcpyHostToDevice, stream), "H2D");
+    sbk::update_transforms(view(), obj, d_scratch_poses.p, d_scratch_idx.p, 1, 16, s());
+    cuda_check(cudaStreamSynchronize(stream), "sync");
+  }
+  void object_pose(int obj, uint64_t inst, double* out16) {
+    object_check(obj);
+    instance_check(inst);
+    activate();
+    double rec[12];
+    cuda_check(cudaMemcpyAsync(rec, d_pose.p + (static_cast<size_t>(obj) * n + inst) * 12, sizeof rec, cudaMemcpyDeviceToHost, stream), "D2H");
+    cuda_check(cudaStreamSynchronize(stream), "sync");
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 4; ++j) out16[4 * j + i] = rec[4 * i + j];
+    out16[3] = out16[7] = out16[11] = 0.0;
+    out16[15] = 1.0;
+  }
+  bool enabled(int obj, uint64_t inst) {
+    object_check(obj);
+    instance_check(inst);
+    activate();
+    uint32_t w = 0;
+    cuda_check(cudaMemcpyAsync(&w, d_enabled.p + static_cast<size_t>(obj >> 5) * n + inst, 4, cudaMemcpyDeviceToHost, stream), "D2H");
+    cuda_check(cudaStreamSynchronize(stream), "sync");
+    return (w >> (obj & 31)) & 1u;
+  }
+
+  // check_batch (collision.cpp:418-461)
+  void check_batch(int geom, const double* poses16, const uint32_t* active, uint64_t m,
+                   uint8_t* free_out, int32_t* contact_out) {
+    geom_at(geom);
+    for (uint64_t j = 0; j < m; ++j) instance_check(active[j]);
+    activate();
+    d_free.ensure(n);
+    d_contact.ensure(n);
+    cuda_check(cudaMemsetAsync(d_free.p, 1, n, stream), "memset");
+    cuda_check(cudaMemsetAsync(d_contact.p, 0xff, n * 4, stream), "memset");
+    cuda_check(cudaMemsetAsync(d_counters.p, 0, 4 * sizeof(unsigned long long), stream), "memset");
+    if (m > 0) {
+      upload_poses(poses16, m);
+      d_scratch_idx.ensure(m);
+      cuda_check(cudaMemcpyAsync(d_scratch_idx.p, active, m * 4, cudaMemcpyHostToDevice, stream), "H2D");
+      sbk::check_batch(view(), geom, d_scratch_poses.p, d_scratch_idx.p, m, d_free.p, d_contact.p,
+                       d_counters.p, s());
+    }
+    unsigned long long c[4];
+    cuda_check(cudaMemcpyAsync(free_out, d_free.p, n, cudaMemcpyDeviceToHost, stream), "D2H");
+    cuda_check(cudaMemcpyAsync(contact_out, d_contact.p, n * 4, cudaMemcpyDeviceToHost, stream), "D2H");
+    cuda_check(cudaMemcpyAsync(c, d_counters.p, sizeof c, cudaMemcpyDeviceToHost, stream), "D2H");
+    cuda_check(cudaStreamSynchronize(stream), "sync");
+    ++stats.check_calls;
+    stats.checked_instances += m;
+    stats.narrow_phase_tests += c[1];
+    stats.triangle_pair_tests += c[2];
+  }
+};
+
+// ===================================================================== Engine
+struct sb_engine {
+  std::unique_ptr<sb_world> world;
+  uint64_t n_total = 0, begin = 0, end = 0, n = 0;
+  int rank = 0, world_size = 1;
+  sb_allgather_fn allgather = nullptr;
+  void* allgather_ctx = nullptr;
+  int attempts = 0;
+
+  struct Placement {
+    SbPlacementDev dev;
+    double support16[16];
+    double inv_support[12];
+    int canon_n = 0;  // host-built canonical table size (no anchor)
+  };
+  std::vector<Placement> places;
+  int32_t first_place_obj = 0;
+  int inst_cap = 0;
+
+  DevArray<uint8_t> d_valid;
+  DevArray<int16_t> d_accepted;
+  DevArray<uint32_t> d_act[2];
+  DevArray<uint8_t> d_fail;
+  DevArray<uint64_t> d_count;
+  DevArray<uint8_t> d_temp;
+  size_t temp_bytes = 0;
+  DevArray<unsigned long long> d_counters;
+  DevArray<double> d_anchor;
+  DevArray<double> d_s0;
+  DevArray<int32_t> d_flags;  // [0] vary, [1] region status
+  DevArray<SbRegionTri> d_canon_tris;
+  DevArray<double> d_canon_cum;
+  DevArray<int32_t> d_canon_n;
+  DevArray<SbRegionTri> d_inst_tris;
+  DevArray<double> d_inst_cum;
+  DevArray<int32_t> d_inst_n;
+  DevArray<double> d_pose16;
+  PinnedArray<uint64_t> h_count;
+  cudaEvent_t ev_start = nullptr, ev_stop = nullptr, ev_r0 = nullptr, ev_r1 = nullptr;
+
+  uint64_t last_launches = 0;
+  double last_total_ms = 0.0, last_check_ms = 0.0;
+  uint64_t last_check_launches = 0;
+
+  std::vector<uint64_t> exchange(const std::vector<uint64_t>& send) {
+    if (world_size == 1) return send;
+    std::vector<uint64_t> recv(send.size() * world_size);
+    if (allgather(allgather_ctx, send.data(), static_cast<uint32_t>(send.size()), recv.data()) != 0)
+      throw std::runtime_error("allgather callback failed");
+    return recv;
+  }
+
+  sb_engine(const sb_scene* sc, const sb_shard* shard, int device) {
+    if (!sc) throw std::invalid_argument("scene is NULL");
+    n_total = sc->n_instances;
+    begin = 0;
+    end = n_total;
+    if (shard) {
+      begin = shard->begin;
+      end = shard->end;
+      rank = shard->rank;
+      world_size = shard->world_size;
+      allgather = shard->allgather;
+      allgather_ctx = shard->ctx;
+      if (world_size < 1 || rank < 0 || rank >= world_size) throw std::invalid_argument("bad shard rank");
+      if (world_size > 1 && !allgather) throw std::invalid_argument("sharded engine needs an allgather callback");
+    }
+    if (begin >= end || end > n_total) throw std::invalid_argument("bad shard range");
+    n = end - begin;
+    attempts = sc->attempts;
+    if (attempts < 1 || attempts > 32767) throw std::invalid_argument("attempts must be in [1, 32767]");
+    world = std::make_unique<sb_world>(n, 0.0, device);
+
+    std::vector<int> geom_of_mesh;
+    std::vector<double> z_off;
+    for (uint32_t i = 0; i < sc->n_meshes; ++i) {
+      const sb_mesh& m = sc->meshes[i];
+      if (!m.vertices || !m.triangles) throw std::invalid_argument("mesh arrays are NULL");
+      sbh::Mesh h;
+      h.v.resize(m.n_vertices);
+      h.t.resize(m.n_triangles);
+      for (uint32_t k = 0; k < m.n_vertices; ++k)
+        h.v[k] = {m.vertices[3 * k], m.vertices[3 * k + 1], m.vertices[3 * k + 2]};
+      for (uint32_t k = 0; k < m.n_triangles; ++k)
+        h.t[k] = {m.triangles[3 * k], m.triangles[3 * k + 1], m.triangles[3 * k + 2]};
+      double box[6];
+      sbh::mesh_aabb(h, box);  // rest_pose uses the mesh as given (sampler.cpp:45-52)
+      if (!(box[2] <= box[5]) || !std::isfinite(box[2]) || !std::isfinite(box[5]))
+        throw std::invalid_argument("rest_pose: degenerate bounding box");
+      z_off.push_back(-box[2] + 1e-3);
+      geom_of_mesh.push_back(world->register_geometry(std::move(h)));
+    }
+    auto mesh_geom = [&](int32_t m) {
+      if (m < 0 || static_cast<uint32_t>(m) >= sc->n_meshes) throw std::out_of_range("mesh index");
+      return geom_of_mesh[m];
+    };
+    for (uint32_t f = 0; f < sc->n_fixed; ++f) {
+      int obj = world->add_object("fixed" + std::to_string(f), mesh_geom(sc->fixed[f].mesh));
+      require_homogeneous(sc->fixed[f].pose);
+      world->upload_poses(sc->fixed[f].pose, 1);
+      // broadcast one pose to every instance (stride 0)
+      sbk::update_transforms(world->view(), obj, world->d_scratch_poses.p, nullptr, n, 0, world->s());
+      cuda_check(cudaStreamSynchronize(world->stream), "sync");
+      world->set_enabled_all(obj, true);
+    }
+    first_place_obj = static_cast<int32_t>(sc->n_fixed);
+    bool any_anchor = false;
+    for (uint32_t p = 0; p < sc->n_placements; ++p) {
+      const sb_placement& sp = sc->placements[p];
+      int obj = world->add_object("p" + std::to_string(p), mesh_geom(sp.mesh));
+      if (sp.support < 0 || static_cast<uint32_t>(sp.support) >= sc->n_supports)
+        throw std::out_of_range("support index");
+      const sb_support& sup = sc->supports[sp.support];
+      require_homogeneous(sup.pose);
+      Placement pl;
+      std::memset(&pl.dev, 0, sizeof pl.dev);
+      pl.dev.geom = mesh_geom(sp.mesh);
+      pl.dev.object = obj;
+      pl.dev.orientation = sp.orientation;
+      if (sp.orientation < SB_ORIENT_FIXED || sp.orientation > SB_ORIENT_FACE_TO)
+        throw std::invalid_argument("orientation rule");
+      pl.dev.face_object = -1;
+      if (sp.orientation == SB_ORIENT_FACE_TO) {
+        if (sp.face_target < 0 || static_cast<uint32_t>(sp.face_target) >= p)
+          throw std::invalid_argument("sample_orientations: face_to target must be an earlier placement");
+        pl.dev.face_object = first_place_obj + sp.face_target;
+      }
+      pl.dev.z_off = z_off[sp.mesh];
+      std::memcpy(pl.support16, sup.pose, sizeof pl.support16);
+      colmajor_to_34(sup.pose, pl.dev.support);
+      inverse_rigid34(sup.pose, pl.inv_support);
+      for (int k = 0; k < 4; ++k) pl.dev.rect[k] = sup.rect[k];
+      const sb_relation& r = sp.relation;
+      // RelationshipSpec::validate (relationships.cpp:59-76) for the single-anchor subset
+      if (r.distance < 0.0) throw std::invalid_argument("relationship: distance must be >= 0");
+      if (r.angle_threshold > M_PI) throw std::invalid_argument("relationship: angle_threshold outside (0, pi]");
+      bool dist = r.distance_type == SB_DIST_GREATER || r.distance_type == SB_DIST_LESS ||
+                  r.distance_type == SB_DIST_EQUAL;
+      if (r.distance_type < SB_DIST_NONE || r.distance_type > SB_DIST_EQUAL)
+        throw std::invalid_argument("relationship: distance_type (middle is out of scope)");
+      if (dist && r.anchor < 0) throw std::invalid_argument("relationship: greater/less/equal require exactly 1 anchor");
+      if (r.direction != SB_DIR_NONE && r.anchor < 0) throw std::invalid_argument("relationship: direction requires exactly 1 anchor");
+      if (r.direction < SB_DIR_NONE || r.direction > SB_DIR_VECTOR) throw std::invalid_argument("relationship: direction");
+      if (r.direction == SB_DIR_VECTOR &&
+          std::sqrt(r.direction_vector[0] * r.direction_vector[0] + r.direction_vector[1] * r.direction_vector[1]) < 1e-12)
+        throw std::invalid_argument("relationship: zero-length direction vector");
+      if (r.distance_type == SB_DIST_LESS && !(0.0 < r.distance))
+        throw std::invalid_argument("annulus_sector: min_r >= max_r");
+      if (r.anchor >= 0 && static_cast<uint32_t>(r.anchor) >= p)
+        throw std::invalid_argument("relationship: anchor must be an earlier placement");
+      pl.dev.anchor_object = r.anchor >= 0 ? first_place_obj + r.anchor : -1;
+      pl.dev.distance_type = r.distance_type;
+      pl.dev.direction = r.direction;
+      pl.dev.frame = r.frame;
+      pl.dev.direction_vector[0] = r.direction_vector[0];
+      pl.dev.direction_vector[1] = r.direction_vector[1];
+      pl.dev.distance = r.distance;
+      pl.dev.angle_threshold = r.angle_threshold;
+      pl.dev.salt = p;
+      if (r.anchor >= 0) {
+        any_anchor = true;
+        double theta = r.angle_threshold > 0 ? r.angle_threshold : (r.direction == SB_DIR_NONE ? M_PI : M_PI / 4);
+        if (theta >= M_PI - 1e-12 && (r.distance_type == SB_DIST_GREATER || r.distance_type == SB_DIST_EQUAL))
+          throw std::invalid_argument("full annulus with a hole is not supported on the device path");
+      }
+      places.push_back(pl);
+    }
+    attempts = sc->attempts;
+
+    // canonical sampler tables (no-anchor placements: the support rect itself)
+    const size_t P = places.size();
+    d_canon_tris.alloc(std::max<size_t>(1, P) * SB_REGION_MAX_VERTS);
+    d_canon_cum.alloc(std::max<size_t>(1, P) * SB_REGION_MAX_VERTS);
+    d_canon_n.alloc(std::max<size_t>(1, P));
+    for (size_t p = 0; p < P; ++p) {
+      if (places[p].dev.anchor_object >= 0) continue;
+      const double* rc = places[p].dev.rect;
+      std::vector<sbh::V2> ring = {{rc[0], rc[1]}, {rc[2], rc[1]}, {rc[2], rc[3]}, {rc[0], rc[3]}};
+      sbh::SamplerTable t = sbh::sampler_table({ring});
+      places[p].canon_n = static_cast<int>(t.tris.size());
+      if (!t.tris.empty()) {
+        cuda_check(cudaMemcpy(d_canon_tris.p + p * SB_REGION_MAX_VERTS, t.tris.data(), t.tris.size() * sizeof(SbRegionTri), cudaMemcpyHostToDevice), "H2D canon");
+        cuda_check(cudaMemcpy(d_canon_cum.p + p * SB_REGION_MAX_VERTS, t.cum.data(), t.cum.size() * sizeof(double), cudaMemcpyHostToDevice), "H2D canon");
+      }
+    }
+    inst_cap = SB_REGION_MAX_VERTS;
+    if (any_anchor) {
+      d_inst_tris.alloc(n * inst_cap);
+      d_inst_cum.alloc(n * inst_cap);
+      d_inst_n.alloc(n);
+      d_anchor.alloc(3 * n);
+    }
+    d_s0.alloc(3);
+    d_flags.alloc(2);
+    d_valid.alloc(n);
+    d_accepted.alloc(std::max<size_t>(1, P) * n);
+    d_act[0].alloc(n);
+    d_act[1].alloc(n);
+    d_fail.alloc(n);
+    d_count.alloc(1);
+    temp_bytes = sbk::select_temp_bytes(n);
+    d_temp.alloc(temp_bytes);
+    d_counters.alloc(4);
+    h_count.ensure(4);
+    cuda_check(cudaEventCreate(&ev_start), "event");
+    cuda_check(cudaEventCreate(&ev_stop), "event");
+    cuda_check(cudaEventCreate(&ev_r0), "event");
+    cuda_check(cudaEventCreate(&ev_r1), "event");
+    cuda_check(cudaDeviceSynchronize(), "sync");
+  }
+
+  ~sb_engine() {
+    if (world) cudaSetDevice(world->device);
+    for (cudaEvent_t e : {ev_start, ev_stop, ev_r0, ev_r1})
+      if (e) cudaEventDestroy(e);
+  }
+
+  uint64_t read_count() {
+    cuda_check(cudaMemcpyAsync(h_count.p, d_count.p, sizeof(uint64_t), cudaMemcpyDeviceToHost, world->stream), "D2H count");
+    cuda_check(cudaStreamSynchronize(world->stream), "sync");
+    return h_count.p[0];
+  }
+
+  void generate(uint64_t run_seed, sb_run_stats* st) {
+    world->activate();
+    cudaStream_t stream = world->stream;
+    sb_stream_t s = world->s();
+    const SbWorldView wv = world->view();
+    uint64_t launches = 0, rounds = 0, per_inst = 0, round_launches = 0;
+    double check_ms = 0.0;
+    cuda_check(cudaEventRecord(ev_start, stream), "event");
+    cuda_check(cudaMemsetAsync(d_counters.p, 0, 4 * sizeof(unsigned long long), stream), "memset");
+    sbk::engine_reset(wv, first_place_obj, static_cast<int32_t>(places.size()), d_valid.p, d_accepted.p,
+                      static_cast<int32_t>(places.size()), s);
+    ++launches;
+    for (size_t p = 0; p < places.size(); ++p) {
+      Placement& pl = places[p];
+      bool fast = true;
+      int canon_n = pl.canon_n;
+      const SbRegionTri* canon_tris = d_canon_tris.p + p * SB_REGION_MAX_VERTS;
+      const double* canon_cum = d_canon_cum.p + p * SB_REGION_MAX_VERTS;
+      if (pl.dev.anchor_object >= 0) {
+        sbk::anchor_states(wv, pl.dev.anchor_object, pl.inv_support, d_anchor.p, s);
+        ++launches;
+        // instance 0 (global) lives on the rank whose shard starts at 0
+        double s0[3] = {0, 0, 0};
+        if (begin == 0) {
+          cuda_check(cudaMemcpyAsync(s0, d_anchor.p, sizeof s0, cudaMemcpyDeviceToHost, stream), "D2H s0");
+          cuda_check(cudaStreamSynchronize(stream), "sync");
+        }
+        if (world_size > 1) {
+          std::vector<uint64_t> send(4, 0);
+          std::memcpy(send.data(), s0, sizeof s0);
+          send[3] = begin == 0 ? 1 : 0;
+          std::vector<uint64_t> recv = exchange(send);
+          for (int r = 0; r < world_size; ++r)
+            if (recv[4 * r + 3]) std::memcpy(s0, &recv[4 * r], sizeof s0);
+        }
+        cuda_check(cudaMemsetAsync(d_flags.p, 0, 2 * sizeof(int32_t), stream), "memset");
+        sbk::vary_flag(d_anchor.p, n, s0[0], s0[1], s0[2], d_flags.p, s);
+        ++launches;
+        int32_t flags[2];
+        cuda_check(cudaMemcpyAsync(flags, d_flags.p, sizeof flags, cudaMemcpyDeviceToHost, stream), "D2H flag");
+        cuda_check(cudaStreamSynchronize(stream), "sync");
+        bool vary = flags[0] != 0;
+        if (world_size > 1) {
+          std::vector<uint64_t> f = exchange({vary ? 1ull : 0ull});
+          vary = false;
+          for (uint64_t x : f) vary = vary || x != 0;
+        }
+        sbk::RegionParams rp;
+        rp.pl = pl.dev;
+        rp.cap = inst_cap;
+        rp.status = d_flags.p + 1;
+        if (vary) {
+          ++per_inst;
+          fast = false;
+          rp.anchors = d_anchor.p;
+          rp.count = n;
+          rp.tris = d_inst_tris.p;
+          rp.cum = d_inst_cum.p;
+          rp.ntri = d_inst_n.p;
+        } else {
+          cuda_check(cudaMemcpyAsync(d_s0.p, s0, sizeof s0, cudaMemcpyHostToDevice, stream), "H2D s0");
+          rp.anchors = d_s0.p;
+          rp.count = 1;
+          rp.tris = d_canon_tris.p + p * SB_REGION_MAX_VERTS;
+          rp.cum = d_canon_cum.p + p * SB_REGION_MAX_VERTS;
+          rp.ntri = d_canon_n.p + p;
+        }
+        sbk::build_regions(rp, s);
+        ++launches;
+        int32_t status_and_n[2] = {0, 0};
+        cuda_check(cudaMemcpyAsync(&status_and_n[0], d_flags.p + 1, 4, cudaMemcpyDeviceToHost, stream), "D2H status");
+        if (!vary)
+          cuda_check(cudaMemcpyAsync(&status_and_n[1], d_canon_n.p + p, 4, cudaMemcpyDeviceToHost, stream), "D2H canon n");
+        cuda_check(cudaStreamSynchronize(stream), "sync");
+        if (status_and_n[0] != 0)
+          throw std::runtime_error("constraint region build failed (status " + std::to_string(status_and_n[0]) +
+                                   ": capacity overflow or unsupported annulus)");
+        if (!vary) canon_n = status_and_n[1];
+      }
+
+      sbk::select_valid(d_valid.p, n, d_act[0].p, d_count.p, d_temp.p, temp_bytes, s);
+      launches += 2;
+      int cur = 0;
+      uint64_t draws = 0;  // fast-path draws consumed by all ranks so far (S)
+      uint64_t m = read_count();
+      for (int a = 0; a < attempts; ++a) {
+        std::vector<uint64_t> counts = exchange({m});
+        uint64_t total = 0, before = 0;
+        for (int r = 0; r < world_size; ++r) {
+          if (r < rank) before += counts[r];
+          total += counts[r];
+        }
+        if (total == 0) break;
+        ++rounds;
+        const bool no_draw = fast && canon_n == 0;  // empty canonical region: placeable = 0
+        if (m > 0 && !no_draw) {
+          sbk::RoundParams rp;
+          rp.w = wv;
+          rp.pl = pl.dev;
+          rp.attempt = a;
+          rp.fast = fast ? 1 : 0;
+          rp.run_seed = run_seed;
+          rp.global_begin = begin;
+          rp.fast_state0 = 0;
+          if (fast) {
+            // Pcg32(make_stream(run_seed, {salt, "cach"})) state after the constructor
+            uint64_t h = sbh::mix64(sbh::mix64(sbh::mix64(run_seed) ^ pl.dev.salt) ^ 0x63616368ULL);
+            const uint64_t mult = 6364136223846793005ULL, inc = (0xda3e39cb94b95bdbULL << 1u) | 1u;
+            uint64_t st0 = inc;
+            st0 += h;
+            st0 = st0 * mult + inc;
+            rp.fast_state0 = st0;
+          }
+          rp.draw_base = draws + before;
+          rp.canon_tris = canon_tris;
+          rp.canon_cum = canon_cum;
+          rp.canon_n = canon_n;
+          rp.inst_cap = inst_cap;
+          rp.inst_tris = d_inst_tris.p;
+          rp.inst_cum = d_inst_cum.p;
+          rp.inst_n = d_inst_n.p;
+          rp.act = d_act[cur].p;
+          rp.m = m;
+          rp.fail = d_fail.p;
+          rp.accepted = d_accepted.p + p * n;
+          rp.counters = d_counters.p;
+          cuda_check(cudaEventRecord(ev_r0, stream), "event");
+          sbk::round_kernel(rp, s);
+          cuda_check(cudaEventRecord(ev_r1, stream), "event");
+          ++launches;
+          ++round_launches;
+          sbk::select_flagged(d_act[cur].p, d_fail.p, m, d_act[1 - cur].p, d_count.p, d_temp.p,
+                              temp_bytes, s);
+          launches += 2;
+          cur = 1 - cur;
+          m = read_count();
+          float ms = 0.f;
+          cuda_check(cudaEventElapsedTime(&ms, ev_r0, ev_r1), "elapsed");
+          check_ms += ms;
+        }
+        if (fast && !no_draw) draws += total;
+      }
+      sbk::invalidate(d_act[cur].p, m, d_valid.p, s);
+      ++launches;
+    }
+    cuda_check(cudaEventRecord(ev_stop, stream), "event");
+    unsigned long long c[4];
+    cuda_check(cudaMemcpyAsync(c, d_counters.p, sizeof c, cudaMemcpyDeviceToHost, stream), "D2H counters");
+    cuda_check(cudaStreamSynchronize(stream), "sync");
+    float total_ms = 0.f;
+    cuda_check(cudaEventElapsedTime(&total_ms, ev_start, ev_stop), "elapsed");
+    last_total_ms = total_ms;
+    last_check_ms = check_ms;
+    last_check_launches = round_launches;
+    last_launches = launches;
+    world->stats.check_calls += round_launches;
+    world->stats.checked_instances += c[0];
+    world->stats.narrow_phase_tests += c[1];
+    world->stats.triangle_pair_tests += c[2];
+    if (st) {
+      std::memset(st, 0, sizeof *st);
+      st->candidate_checks = c[0];
+      st->narrow_phase_tests = c[1];
+      st->triangle_pair_tests = c[2];
+      st->candidates_sampled = c[3];
+      st->rounds = rounds;
+      st->per_instance_placements = per_inst;
+      std::vector<uint8_t> v(n);
+      cuda_check(cudaMemcpy(v.data(), d_valid.p, n, cudaMemcpyDeviceToHost), "D2H valid");
+      uint64_t nv = 0;
+      for (uint8_t x : v) nv += x;
+      st->valid_instances = nv;
+    }
+  }
+
+  void download(sb_result* out) {
+    if (!out) return;
+    world->activate();
+    cudaStream_t stream = world->stream;
+    const size_t P = places.size();
+    if (out->accepted && P)
+      cuda_check(cudaMemcpyAsync(out->accepted, d_accepted.p, P * n * sizeof(int16_t), cudaMemcpyDeviceToHost, stream), "D2H accepted");
+    if (out->valid)
+      cuda_check(cudaMemcpyAsync(out->valid, d_valid.p, n, cudaMemcpyDeviceToHost, stream), "D2H valid");
+    if (out->poses && P) {
+      d_pose16.ensure(16 * n);
+      for (size_t p = 0; p < P; ++p) {
+        sbk::download_poses(world->view(), places[p].dev.object, d_pose16.p, world->s());
+        cuda_check(cudaMemcpyAsync(out->poses + 16 * n * p, d_pose16.p, 16 * n * sizeof(double), cudaMemcpyDeviceToHost, stream), "D2H poses");
+      }
+    }
+    cuda_check(cudaStreamSynchronize(stream), "sync");
+  }
+};
+
+// ===================================================================== C ABI
+namespace {
+template <class F>
+sb_status guard(F&& f) {
+  try {
+    f();
+    return SB_OK;
+  } catch (const std::invalid_argument& e) {
+    g_error = e.what();
+    return SB_ERR_INVALID_ARGUMENT;
+  } catch (const std::out_of_range& e) {
+    g_error = e.what();
+    return SB_ERR_OUT_OF_RANGE;
+  } catch (const std::logic_error& e) {
+    g_error = e.what();
+    return SB_ERR_LOGIC;
+  } catch (const CudaError& e) {
+    g_error = e.what();
+    return SB_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    std::string w = e.what();
+    return w.rfind("CUDA", 0) == 0 ? SB_ERR_CUDA : SB_ERR_RUNTIME;
+  }
+}
+
+sb_status mesh_out(const sbh::Mesh& m, double* v, uint32_t* nv, uint32_t* t, uint32_t* nt) {
+  if (nv) *nv = static_cast<uint32_t>(m.v.size());
+  if (nt) *nt = static_cast<uint32_t>(m.t.size());
+  if (v)
+    for (size_t i = 0; i < m.v.size(); ++i)
+      for (int c = 0; c < 3; ++c) v[3 * i + c] = m.v[i][c];
+  if (t)
+    for (size_t i = 0; i < m.t.size(); ++i)
+      for (int c = 0; c < 3; ++c) t[3 * i + c] = m.t[i][c];
+  return SB_OK;
+}
+
+sbh::Mesh mesh_in(const double* v, uint32_t nv, const uint32_t* t, uint32_t nt) {
+  if ((nv && !v) || (nt && !t)) throw std::invalid_argument("mesh arrays are NULL");
+  sbh::Mesh m;
+  m.v.resize(nv);
+  m.t.resize(nt);
+  for (uint32_t i = 0; i < nv; ++i) m.v[i] = {v[3 * i], v[3 * i + 1], v[3 * i + 2]};
+  for (uint32_t i = 0; i < nt; ++i) m.t[i] = {t[3 * i], t[3 * i + 1], t[3 * i + 2]};
+  return m;
+}
+}  // namespace
+
+extern "C" {
+
+const char* sb_last_error(void) { return g_error.c_str(); }
+int sb_abi_version(void) { return SB_ABI_VERSION; }
+int sb_device_available(void) {
+  return guard([] { current_device_checked(0); }) == SB_OK ? 1 : 0;
+}
+
+sb_status sb_make_box(double sx, double sy, double sz, double* v, uint32_t* nv, uint32_t* t,
+                      uint32_t* nt) {
+  return guard([&] { mesh_out(sbh::make_box(sx, sy, sz), v, nv, t, nt); });
+}
+sb_status sb_make_cylinder(double r, double h, int seg, double* v, uint32_t* nv, uint32_t* t,
+                           uint32_t* nt) {
+  return guard([&] { mesh_out(sbh::make_cylinder(r, h, seg), v, nv, t, nt); });
+}
+sb_status sb_make_sphere(double r, int st, int sl, double* v, uint32_t* nv, uint32_t* t,
+                         uint32_t* nt) {
+  return guard([&] { mesh_out(sbh::make_sphere(r, st, sl), v, nv, t, nt); });
+}
+sb_status sb_transform_vertices(const double pose[16], double* v, uint32_t nv) {
+  return guard([&] {
+    if (!pose || (nv && !v)) throw std::invalid_argument("NULL argument");
+    for (uint32_t i = 0; i < nv; ++i) {
+      double p[3] = {v[3 * i], v[3 * i + 1], v[3 * i + 2]};
+      for (int r = 0; r < 3; ++r)  // transform_point: ((R p) + t), left to right
+        v[3 * i + r] = ((pose[r] * p[0] + pose[4 + r] * p[1]) + pose[8 + r] * p[2]) + pose[12 + r];
+    }
+  });
+}
+sb_status sb_mesh_fingerprint(const double* v, uint32_t nv, const uint32_t* t, uint32_t nt,
+                              uint64_t* out) {
+  return guard([&] { *out = sbh::mesh_fingerprint(mesh_in(v, nv, t, nt)); });
+}
+sb_status sb_rest_z_offset(const double* v, uint32_t nv, double* z) {
+  return guard([&] {
+    sbh::Mesh m = mesh_in(v, nv, nullptr, 0);
+    double box[6];
+    sbh::mesh_aabb(m, box);
+    if (!(box[2] <= box[5]) || !std::isfinite(box[2])) throw std::invalid_argument("rest_pose: degenerate bounding box");
+    *z = -box[2] + 1e-3;
+  });
+}
+
+sb_status sb_bvh_info(const double* v, uint32_t nv, const uint32_t* t, uint32_t nt,
+                      int32_t info[4]) {
+  return guard([&] {
+    sbh::Mesh m = mesh_in(v, nv, t, nt);
+    sbh::drop_degenerate(m);
+    sbh::EffectiveBvh b = sbh::build_effective_bvh(m);
+    info[0] = b.full_nodes;
+    info[1] = b.full_depth;
+    info[2] = static_cast<int32_t>(b.nodes.size());
+    info[3] = b.reachable_tris;
+  });
+}
+
+uint64_t sb_mix64(uint64_t x) { return sbh::mix64(x); }
+uint64_t sb_stream_key(const uint64_t* parts, uint32_t n) {
+  uint64_t h = 0x853c49e6748fea9bULL;
+  for (uint32_t i = 0; i < n; ++i) h = sbh::mix64(h ^ parts[i]);
+  return h;
+}
+sb_status sb_stream_doubles(uint64_t seed, const uint64_t* c, uint32_t nc, double* out, uint32_t n) {
+  return guard([&] {
+    uint64_t h = sbh::mix64(seed);
+    for (uint32_t i = 0; i < nc; ++i) h = sbh::mix64(h ^ c[i]);
+    const uint64_t mult = 6364136223846793005ULL, inc = (0xda3e39cb94b95bdbULL << 1u) | 1u;
+    uint64_t st = inc;
+    st += h;
+    st = st * mult + inc;
+    for (uint32_t k = 0; k < n; ++k) {
+      uint64_t w = 0;
+      for (int half = 0; half < 2; ++half) {
+        uint64_t old = st;
+        st = old * mult + inc;
+        uint32_t xs = static_cast<uint32_t>(((old >> 18u) ^ old) >> 27u);
+        uint32_t rot = static_cast<uint32_t>(old >> 59u);
+        uint32_t r = (xs >> rot) | (xs << ((32u - rot) & 31u));
+        w = (w << 32) | r;
+      }
+      out[k] = static_cast<double>(w >> 11) * 0x1.0p-53;
+    }
+  });
+}
+
+sb_status sb_world_create(uint64_t n, double margin, int device, sb_world** out) {
+  return guard([&] {
+    if (!out) throw std::invalid_argument("out is NULL");
+    *out = new sb_world(n, margin, device);
+  });
+}
+void sb_world_destroy(sb_world* w) { delete w; }
+sb_status sb_register_geometry(sb_world* w, const double* v, uint32_t nv, const uint32_t* t,
+                               uint32_t nt, int32_t* id) {
+  return guard([&] { *id = w->register_geometry(mesh_in(v, nv, t, nt)); });
+}
+sb_status sb_add_object(sb_world* w, const char* name, int32_t geom, int32_t* id) {
+  return guard([&] { *id = w->add_object(name ? name : "", geom); });
+}
+sb_status sb_set_enabled(sb_world* w, int32_t obj, const uint32_t* inst, uint64_t n, int en) {
+  return guard([&] { w->set_enabled(obj, inst, n, en != 0); });
+}
+sb_status sb_set_enabled_all(sb_world* w, int32_t obj, int en) {
+  return guard([&] { w->set_enabled_all(obj, en != 0); });
+}
+sb_status sb_update_transforms(sb_world* w, int32_t obj, const double* poses) {
+  return guard([&] { w->update_transforms(obj, poses); });
+}
+sb_status sb_update_transform(sb_world* w, int32_t obj, uint64_t inst, const double pose[16]) {
+  return guard([&] { w->update_transform(obj, inst, pose); });
+}
+sb_status sb_object_pose(sb_world* w, int32_t obj, uint64_t inst, double pose[16]) {
+  return guard([&] { w->object_pose(obj, inst, pose); });
+}
+sb_status sb_enabled(sb_world* w, int32_t obj, uint64_t inst, int* en) {
+  return guard([&] { *en = w->enabled(obj, inst) ? 1 : 0; });
+}
+sb_status sb_check_batch(sb_world* w, int32_t geom, const double* poses, const uint32_t* active,
+                         uint64_t m, uint8_t* free_out, int32_t* contact_out) {
+  return guard([&] { w->check_batch(geom, poses, active, m, free_out, contact_out); });
+}
+sb_status sb_get_stats(sb_world* w, sb_stats* out) {
+  return guard([&] { *out = w->stats; });
+}
+sb_status sb_reset_stats(sb_world* w) {
+  return guard([&] { w->stats = sb_stats{}; });
+}
+
+sb_status sb_engine_create(const sb_scene* sc, const sb_shard* shard, int device, sb_engine** out) {
+  return guard([&] {
+    if (!out) throw std::invalid_argument("out is NULL");
+    *out = new sb_engine(sc, shard, device);
+  });
+}
+void sb_engine_destroy(sb_engine* e) { delete e; }
+sb_status sb_engine_generate(sb_engine* e, uint64_t run_seed, sb_result* out, sb_run_stats* st) {
+  return guard([&] {
+    e->generate(run_seed, st);
+    e->download(out);
+  });
+}
+sb_status sb_engine_download(sb_engine* e, sb_result* out) {
+  return guard([&] { e->download(out); });
+}
+sb_world* sb_engine_world(sb_engine* e) { return e->world.get(); }
+uint64_t sb_engine_local_instances(const sb_engine* e) { return e->n; }
+uint64_t sb_engine_last_launches(const sb_engine* e) { return e->last_launches; }
+sb_status sb_engine_last_timing(const sb_engine* e, double* total_ms, double* check_ms,
+                                uint64_t* check_launches) {
+  return guard([&] {
+    if (total_ms) *total_ms = e->last_total_ms;
+    if (check_ms) *check_ms = e->last_check_ms;
+    if (check_launches) *check_launches = e->last_check_launches;
+  });
+}
+
+}  // extern "C"

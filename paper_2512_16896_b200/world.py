@@ -1,0 +1,370 @@
+"""Python face of the C-ABI drop-in, mirroring the reference's scenebatch class API.
+
+Names and argument meaning follow /root/reference/proj/include/scenebatch:
+``TriMesh`` / ``make_box`` / ``make_cylinder`` / ``make_sphere`` (trimesh.hpp:12-38),
+``CollisionWorld`` (collision.hpp:76-127) and the generation engine the reference leaves
+unimplemented. Errors map onto the reference's exception types:
+std::invalid_argument -> ValueError, std::out_of_range -> IndexError.
+Poses are numpy (4, 4) float64 arrays (row, col) -- i.e. Eigen::Matrix4d semantics; they
+cross the C ABI column-major, exactly the reference's memory layout.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _capi as A
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _up(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_uint32))
+
+
+def colmajor(poses: np.ndarray) -> np.ndarray:
+    """(..., 4, 4) row/col matrices -> contiguous column-major doubles (..., 16)."""
+    p = np.asarray(poses, dtype=np.float64)
+    return np.ascontiguousarray(np.swapaxes(p, -1, -2)).reshape(p.shape[:-2] + (16,))
+
+
+def from_colmajor(flat: np.ndarray) -> np.ndarray:
+    f = np.asarray(flat, dtype=np.float64)
+    return np.swapaxes(f.reshape(f.shape[:-1] + (4, 4)), -1, -2).copy()
+
+
+def translation(x: float, y: float, z: float) -> np.ndarray:
+    m = np.eye(4)
+    m[:3, 3] = (x, y, z)
+    return m
+
+
+# ---------------------------------------------------------------------------- meshes
+@dataclass
+class TriMesh:
+    vertices: np.ndarray   # (n, 3) float64
+    triangles: np.ndarray  # (m, 3) uint32
+
+    def __post_init__(self):
+        self.vertices = np.ascontiguousarray(self.vertices, dtype=np.float64).reshape(-1, 3)
+        self.triangles = np.ascontiguousarray(self.triangles, dtype=np.uint32).reshape(-1, 3)
+
+    def aabb(self):
+        return self.vertices.min(axis=0), self.vertices.max(axis=0)
+
+    def fingerprint(self) -> int:
+        out = C.c_uint64()
+        A.check(A.lib().sb_mesh_fingerprint(_dp(self.vertices), len(self.vertices),
+                                            _up(self.triangles), len(self.triangles),
+                                            C.byref(out)))
+        return out.value
+
+    def bvh_info(self) -> dict:
+        info = (C.c_int32 * 4)()
+        A.check(A.lib().sb_bvh_info(_dp(self.vertices), len(self.vertices), _up(self.triangles),
+                                    len(self.triangles), info))
+        return dict(nodes=info[0], depth=info[1], effective_nodes=info[2], reachable_tris=info[3])
+
+    def rest_z_offset(self) -> float:
+        out = C.c_double()
+        A.check(A.lib().sb_rest_z_offset(_dp(self.vertices), len(self.vertices), C.byref(out)))
+        return out.value
+
+
+def _make(fn, *args) -> TriMesh:
+    nv, nt = C.c_uint32(), C.c_uint32()
+    A.check(fn(*args, None, C.byref(nv), None, C.byref(nt)))
+    v = np.zeros((nv.value, 3), np.float64)
+    t = np.zeros((nt.value, 3), np.uint32)
+    A.check(fn(*args, _dp(v), C.byref(nv), _up(t), C.byref(nt)))
+    return TriMesh(v, t)
+
+
+def make_box(sx: float, sy: float, sz: float) -> TriMesh:
+    """trimesh.hpp:27 -- axis-aligned box centred at the origin (12 triangles)."""
+    return _make(A.lib().sb_make_box, C.c_double(sx), C.c_double(sy), C.c_double(sz))
+
+
+def make_cylinder(radius: float, height: float, segments: int = 32) -> TriMesh:
+    """trimesh.hpp:30 -- capped cylinder along z (4 * segments triangles)."""
+    return _make(A.lib().sb_make_cylinder, C.c_double(radius), C.c_double(height),
+                 C.c_int(segments))
+
+
+def make_sphere(radius: float, stacks: int = 12, slices: int = 16) -> TriMesh:
+    """trimesh.hpp:32 -- UV sphere centred at the origin."""
+    return _make(A.lib().sb_make_sphere, C.c_double(radius), C.c_int(stacks), C.c_int(slices))
+
+
+def transformed(mesh: TriMesh, pose: np.ndarray) -> TriMesh:
+    """trimesh.hpp:35 -- rigidly transformed copy (transform_point per vertex)."""
+    v = mesh.vertices.copy()
+    A.check(A.lib().sb_transform_vertices(_dp(colmajor(pose)), _dp(v), len(v)))
+    return TriMesh(v, mesh.triangles.copy())
+
+
+def merge(meshes: Sequence[TriMesh]) -> TriMesh:
+    """Concatenate meshes into one TriMesh (how a sphere-set asset is built)."""
+    vs, ts, off = [], [], 0
+    for m in meshes:
+        vs.append(m.vertices)
+        ts.append(m.triangles.astype(np.uint64) + off)
+        off += len(m.vertices)
+    return TriMesh(np.concatenate(vs), np.concatenate(ts).astype(np.uint32))
+
+
+# --------------------------------------------------------------------- collision world
+class CollisionWorld:
+    """collision.hpp:76-127 on the GPU. All per-instance state lives in HBM."""
+
+    def __init__(self, batch_size: int, margin: float = 0.0, device: int = 0, _handle=None):
+        self._owned = _handle is None
+        if _handle is None:
+            h = C.c_void_p()
+            A.check(A.lib().sb_world_create(batch_size, margin, device, C.byref(h)))
+            _handle = h
+        self._h = _handle
+        self.n = batch_size
+
+    def close(self):
+        if self._owned and self._h:
+            A.lib().sb_world_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def batch_size(self) -> int:
+        return self.n
+
+    def register_geometry(self, mesh: TriMesh) -> int:
+        out = C.c_int32()
+        A.check(A.lib().sb_register_geometry(self._h, _dp(mesh.vertices), len(mesh.vertices),
+                                             _up(mesh.triangles), len(mesh.triangles),
+                                             C.byref(out)))
+        return out.value
+
+    def add_object(self, name: str, geom_id: int) -> int:
+        out = C.c_int32()
+        A.check(A.lib().sb_add_object(self._h, name.encode(), geom_id, C.byref(out)))
+        return out.value
+
+    def set_enabled(self, obj: int, instances: Sequence[int], enabled: bool) -> None:
+        idx = np.ascontiguousarray(instances, dtype=np.uint32)
+        A.check(A.lib().sb_set_enabled(self._h, obj, _up(idx), len(idx), int(bool(enabled))))
+
+    def set_enabled_all(self, obj: int, enabled: bool) -> None:
+        A.check(A.lib().sb_set_enabled_all(self._h, obj, int(bool(enabled))))
+
+    def update_transforms(self, obj: int, poses: np.ndarray) -> None:
+        p = colmajor(poses)
+        if p.shape != (self.n, 16):
+            raise ValueError("update_transforms: batch size mismatch")
+        A.check(A.lib().sb_update_transforms(self._h, obj, _dp(p)))
+
+    def update_transform(self, obj: int, instance: int, pose: np.ndarray) -> None:
+        A.check(A.lib().sb_update_transform(self._h, obj, instance, _dp(colmajor(pose))))
+
+    def object_pose(self, obj: int, instance: int) -> np.ndarray:
+        out = np.zeros(16)
+        A.check(A.lib().sb_object_pose(self._h, obj, instance, _dp(out)))
+        return from_colmajor(out)
+
+    def enabled(self, obj: int, instance: int) -> bool:
+        out = C.c_int()
+        A.check(A.lib().sb_enabled(self._h, obj, instance, C.byref(out)))
+        return bool(out.value)
+
+    def check_batch(self, geom_id: int, poses: np.ndarray, active: Sequence[int]):
+        """Returns (free uint8[N], contact_object int32[N]) like CollisionMask."""
+        act = np.ascontiguousarray(active, dtype=np.uint32)
+        p = colmajor(poses).reshape(-1, 16)
+        if len(p) != len(act):
+            raise ValueError("check_batch: poses/active size mismatch")
+        free = np.ones(self.n, np.uint8)
+        contact = np.full(self.n, -1, np.int32)
+        A.check(A.lib().sb_check_batch(self._h, geom_id, _dp(p), _up(act), len(act),
+                                       free.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                       contact.ctypes.data_as(C.POINTER(C.c_int32))))
+        return free, contact
+
+    def stats(self) -> dict:
+        s = A.sb_stats()
+        A.check(A.lib().sb_get_stats(self._h, C.byref(s)))
+        return {k: getattr(s, k) for k, _ in A.sb_stats._fields_}
+
+    def reset_stats(self) -> None:
+        A.check(A.lib().sb_reset_stats(self._h))
+
+
+# ------------------------------------------------------------------------ scene spec
+@dataclass
+class Relation:
+    """RelationshipSpec (relationships.hpp:18-38), zero or one anchor."""
+    anchor: int = -1
+    distance_type: int = A.SB_DIST_NONE
+    direction: int = A.SB_DIR_NONE
+    frame: int = A.SB_FRAME_GLOBAL
+    direction_vector: tuple = (0.0, 0.0)
+    distance: float = 0.0
+    angle_threshold: float = 0.0   # <= 0: default
+
+
+@dataclass
+class Placement:
+    mesh: int
+    support: int
+    orientation: int = A.SB_ORIENT_UNIFORM_YAW
+    face_target: int = -1
+    relation: Relation = field(default_factory=Relation)
+
+
+@dataclass
+class Support:
+    pose: np.ndarray
+    rect: tuple  # x0, y0, x1, y1 in the support frame
+
+
+@dataclass
+class Fixed:
+    mesh: int
+    pose: np.ndarray
+
+
+@dataclass
+class Scene:
+    name: str
+    n_instances: int
+    attempts: int
+    meshes: List[TriMesh]
+    fixed: List[Fixed]
+    supports: List[Support]
+    placements: List[Placement]
+
+    def to_c(self):
+        """Build the sb_scene struct; returns (struct, keepalive list)."""
+        keep = []
+        meshes = (A.sb_mesh * max(1, len(self.meshes)))()
+        for i, m in enumerate(self.meshes):
+            meshes[i] = A.sb_mesh(_dp(m.vertices), len(m.vertices), _up(m.triangles),
+                                  len(m.triangles))
+            keep.append(m)
+        fixed = (A.sb_fixed_object * max(1, len(self.fixed)))()
+        for i, f in enumerate(self.fixed):
+            fixed[i].mesh = f.mesh
+            fixed[i].pose[:] = list(colmajor(f.pose))
+        sups = (A.sb_support * max(1, len(self.supports)))()
+        for i, s in enumerate(self.supports):
+            sups[i].pose[:] = list(colmajor(s.pose))
+            sups[i].rect[:] = list(map(float, s.rect))
+        pls = (A.sb_placement * max(1, len(self.placements)))()
+        for i, p in enumerate(self.placements):
+            r = p.relation
+            pls[i] = A.sb_placement(
+                p.mesh, p.support, p.orientation, p.face_target,
+                A.sb_relation(r.anchor, r.distance_type, r.direction, r.frame,
+                              (C.c_double * 2)(*r.direction_vector), r.distance,
+                              r.angle_threshold))
+        sc = A.sb_scene(self.n_instances, self.attempts, 0,
+                        len(self.meshes), meshes, len(self.fixed), fixed,
+                        len(self.supports), sups, len(self.placements), pls)
+        keep += [meshes, fixed, sups, pls]
+        return sc, keep
+
+
+@dataclass
+class GenerationResult:
+    accepted: np.ndarray   # (placements, n) int16, -1 = none
+    valid: np.ndarray      # (n,) uint8
+    poses: Optional[np.ndarray]  # (placements, n, 4, 4) or None
+    stats: dict
+
+
+class Shard:
+    """Instance range [begin, end) of one rank plus the allgather used by the fast path."""
+
+    def __init__(self, begin: int, end: int, rank: int, world_size: int, allgather=None):
+        self.begin, self.end, self.rank, self.world_size = begin, end, rank, world_size
+        self._py = allgather
+
+        def _cb(ctx, send, n, recv):
+            try:
+                vals = [send[i] for i in range(n)]
+                out = self._py(vals)  # list of world_size * n ints
+                for i, v in enumerate(out):
+                    recv[i] = int(v)
+                return 0
+            except Exception:  # pragma: no cover - surfaced as an engine error
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        self._cb = A.ALLGATHER_FN(_cb) if allgather is not None else A.ALLGATHER_FN()
+
+    def to_c(self):
+        return A.sb_shard(self.begin, self.end, self.rank, self.world_size, self._cb, None)
+
+
+class Engine:
+    """initialize / generate on one GPU (one shard)."""
+
+    def __init__(self, scene: Scene, shard: Optional[Shard] = None, device: int = 0):
+        self.scene = scene
+        sc, self._keep = scene.to_c()
+        self._shard = shard
+        sh = C.byref(shard.to_c()) if shard is not None else None
+        h = C.c_void_p()
+        A.check(A.lib().sb_engine_create(C.byref(sc), sh, device, C.byref(h)))
+        self._h = h
+        self.n = A.lib().sb_engine_local_instances(h)
+
+    def close(self):
+        if self._h:
+            A.lib().sb_engine_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def world(self) -> CollisionWorld:
+        return CollisionWorld(self.n, _handle=A.lib().sb_engine_world(self._h))
+
+    def generate(self, run_seed: int, with_poses: bool = True,
+                 download: bool = True) -> GenerationResult:
+        P = len(self.scene.placements)
+        st = A.sb_run_stats()
+        acc = np.empty((P, self.n), np.int16)
+        valid = np.empty(self.n, np.uint8)
+        poses = np.empty((P, self.n, 16), np.float64) if with_poses else None
+        res = A.sb_result(acc.ctypes.data_as(C.POINTER(C.c_int16)),
+                          poses.ctypes.data_as(C.POINTER(C.c_double)) if with_poses else None,
+                          valid.ctypes.data_as(C.POINTER(C.c_uint8)))
+        A.check(A.lib().sb_engine_generate(self._h, run_seed, C.byref(res) if download else None,
+                                           C.byref(st)))
+        stats = {k: getattr(st, k) for k, _ in A.sb_run_stats._fields_}
+        return GenerationResult(acc, valid, from_colmajor(poses) if with_poses else None, stats)
+
+    def generate_into(self, run_seed: int, res: "A.sb_result") -> dict:
+        """generate + D2H into caller-owned (pinned) buffers already wrapped in sb_result."""
+        st = A.sb_run_stats()
+        A.check(A.lib().sb_engine_generate(self._h, run_seed, C.byref(res), C.byref(st)))
+        return {k: getattr(st, k) for k, _ in A.sb_run_stats._fields_}
+
+    def last_timing(self):
+        t, c, n = C.c_double(), C.c_double(), C.c_uint64()
+        A.check(A.lib().sb_engine_last_timing(self._h, C.byref(t), C.byref(c), C.byref(n)))
+        return t.value, c.value, n.value
+
+    def last_launches(self) -> int:
+        return A.lib().sb_engine_last_launches(self._h)

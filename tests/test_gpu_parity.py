@@ -1,0 +1,292 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference oracle.
+
+Bar (BASELINE.json north_star): accepted candidate indices and collision-free masks
+bit-exact; accepted poses within 1e-5 relative (tolerance written in assert_poses)."""
+import math
+import threading
+
+import numpy as np
+import pytest
+
+from paper_2512_16896_b200 import _capi as A
+from paper_2512_16896_b200 import scenes
+
+pytestmark = pytest.mark.gpu
+
+POSE_RTOL = 1e-5   # north_star: accepted poses within 1e-5 relative
+POSE_ATOL = 1e-12  # entries that are exactly 0 in one build and ~1e-17 in the other
+
+
+def rot_from_quat(q):
+    w, x, y, z = q / np.linalg.norm(q)
+    return np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - z * w), 2 * (x * z + y * w)],
+                     [2 * (x * y + z * w), 1 - 2 * (x * x + z * z), 2 * (y * z - x * w)],
+                     [2 * (x * z - y * w), 2 * (y * z + x * w), 1 - 2 * (x * x + y * y)]])
+
+
+def random_pose(rng, spread, upright, z=None):
+    m = np.eye(4)
+    if upright:
+        a = rng.uniform(0, 2 * math.pi)
+        c, s = math.cos(a), math.sin(a)
+        m[:2, :2] = [[c, -s], [s, c]]
+    else:
+        m[:3, :3] = rot_from_quat(rng.normal(size=4))
+    m[:3, 3] = rng.uniform(-spread, spread, size=3)
+    if z is not None:
+        m[2, 3] = z
+    return m
+
+
+def assert_poses(got, ref_colmajor, pkg):
+    ref = pkg.from_colmajor(ref_colmajor)
+    assert got.shape == ref.shape
+    bad = ~np.isclose(got, ref, rtol=POSE_RTOL, atol=POSE_ATOL)
+    assert not bad.any(), f"{bad.sum()} pose entries outside tolerance"
+
+
+def world_pair(pkg, ref, n, meshes):
+    W = pkg.CollisionWorld(n)
+    R = ref.RefWorld(n)
+    gids = []
+    for m in meshes:
+        g1 = W.register_geometry(m)
+        g2 = R.register_geometry(m.vertices, m.triangles)
+        assert g1 == g2
+        gids.append(g1)
+    return W, R, gids
+
+
+def mesh_zoo(pkg):
+    rng = scenes.Pcg32(99)
+    return [pkg.make_box(0.1, 0.08, 0.12), pkg.make_box(0.3, 0.2, 0.05),
+            pkg.make_cylinder(0.05, 0.1, 16), pkg.make_sphere(0.06, 8, 10),
+            scenes.sphere_set(rng), scenes.open_container(0.3, 0.25, 0.15, 0.01)]
+
+
+@pytest.mark.parametrize("upright", [True, False])
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_check_batch_random_worlds(gpu, ref, upright, seed):
+    pkg = gpu
+    rng = np.random.default_rng(seed)
+    n = 512
+    meshes = mesh_zoo(pkg)
+    W, R, gids = world_pair(pkg, ref, n, meshes)
+    n_obj = 8
+    for k in range(n_obj):
+        g = gids[rng.integers(len(gids))]
+        o1, o2 = W.add_object(f"o{k}", g), R.add_object(g)
+        assert o1 == o2
+        poses = np.stack([random_pose(rng, 0.12, upright) for _ in range(n)])
+        W.update_transforms(o1, poses)
+        R.update_transforms(o2, pkg.colmajor(poses))
+        en = np.nonzero(rng.random(n) < 0.7)[0].astype(np.uint32)
+        W.set_enabled(o1, en, True)
+        R.set_enabled(o2, en, True)
+    for trial in range(3):
+        act = np.sort(rng.choice(n, size=n // 2 + trial * 50, replace=False)).astype(np.uint32)
+        cand = np.stack([random_pose(rng, 0.12, upright) for _ in act])
+        g = gids[rng.integers(len(gids))]
+        f1, c1 = W.check_batch(g, cand, act)
+        f2, c2 = R.check_batch(g, pkg.colmajor(cand), act)
+        assert np.array_equal(f1, f2), f"free mask differs at {np.nonzero(f1 != f2)[0][:10]}"
+        assert np.array_equal(c1, c2), "contact_object differs"
+        assert 0 < (f1[act] == 0).sum() < len(act)  # both outcomes exercised
+    s1, s2 = W.stats(), R.stats()
+    assert s1["checked_instances"] == s2["checked_instances"]
+    assert s1["narrow_phase_tests"] == s2["narrow_phase_tests"]
+    assert s1["triangle_pair_tests"] <= s2["triangle_pair_tests"]
+
+
+def test_check_batch_resting_coplanar(gpu, ref):
+    """Objects resting on one plane share bottom faces: the coplanar branch
+    (collision.cpp:63-83) decides; SURVEY Appendix A scenario included."""
+    pkg = gpu
+    n = 256
+    big, small = pkg.make_box(0.4, 0.4, 0.4), pkg.make_box(0.1, 0.1, 0.1)
+    W, R, (gb, gs) = world_pair(pkg, ref, n, [big, small])
+    o = W.add_object("big", gb)
+    R.add_object(gb)
+    poses = np.stack([pkg.translation(0, 0, 0.201)] * n)
+    W.update_transforms(o, poses)
+    R.update_transforms(o, pkg.colmajor(poses))
+    W.set_enabled_all(o, True)
+    R.set_enabled_all(o, True)
+    rng = np.random.default_rng(5)
+    cand = []
+    for i in range(n):
+        c = random_pose(rng, 0.35, True, z=0.051)
+        cand.append(c)
+    # Appendix A fixed cases in the first slots
+    cases = [(0, 0, 0.051, 0.3), (0, 0, 0.201, 0.3), (0.2, 0, 0.051, 0.0), (0.5, 0, 0.051, 0.0)]
+    for i, (x, y, z, yaw) in enumerate(cases):
+        m = np.eye(4)
+        m[:2, :2] = [[math.cos(yaw), -math.sin(yaw)], [math.sin(yaw), math.cos(yaw)]]
+        m[:3, 3] = (x, y, z)
+        cand[i] = m
+    cand = np.stack(cand)
+    act = np.arange(n, dtype=np.uint32)
+    f1, c1 = W.check_batch(gs, cand, act)
+    f2, c2 = R.check_batch(gs, pkg.colmajor(cand), act)
+    assert np.array_equal(f1, f2) and np.array_equal(c1, c2)
+    assert list(f1[:4]) == [0, 1, 1, 1]  # collide, contained-free, straddle-free, free
+
+
+def test_world_api_semantics(gpu):
+    pkg = gpu
+    W = pkg.CollisionWorld(4)
+    g = W.register_geometry(pkg.make_box(1, 1, 1))
+    assert W.register_geometry(pkg.make_box(1, 1, 1)) == g  # fingerprint dedupe
+    o = W.add_object("cube", g)
+    assert not W.enabled(o, 0)
+    assert np.array_equal(W.object_pose(o, 3), np.eye(4))
+    cand = np.stack([pkg.translation(0.5, 0, 0)] * 4)
+    act = np.arange(4, dtype=np.uint32)
+    free, contact = W.check_batch(g, cand, act)
+    assert free.all()  # disabled objects never collide
+    W.set_enabled(o, [0, 2], True)
+    free, contact = W.check_batch(g, cand, act)
+    assert list(free) == [0, 1, 0, 1] and list(contact) == [0, -1, 0, -1]
+    W.update_transform(o, 2, pkg.translation(2, 0, 0))
+    free, _ = W.check_batch(g, cand, act)
+    assert list(free) == [0, 1, 1, 1]
+    free, contact = W.check_batch(g, cand[:1], [1])
+    assert free.all() and (contact == -1).all()  # inactive / free untouched
+    with pytest.raises(IndexError):
+        W.set_enabled(o, [9], True)
+    with pytest.raises(IndexError):
+        W.add_object("x", 42)
+    bad = np.eye(4)
+    bad[3, 3] = 2.0
+    with pytest.raises(ValueError):
+        W.update_transform(o, 0, bad)
+    assert W.stats()["check_calls"] == 4
+
+
+def run_generate_pair(pkg, ref, scene, seed=1):
+    eng = pkg.Engine(scene)
+    got = eng.generate(seed)
+    want = ref.generate(scene, seed, threads=8)
+    return eng, got, want
+
+
+def assert_same(pkg, got, want):
+    assert np.array_equal(got.valid, want["valid"]), "valid mask differs"
+    diff = np.argwhere(got.accepted != want["accepted"])
+    assert len(diff) == 0, f"accepted differs at (placement, inst) {diff[:10].tolist()}"
+    assert_poses(got.poses, want["poses"], pkg)
+    for k in ("valid_instances", "candidate_checks", "narrow_phase_tests", "rounds",
+              "per_instance_placements"):
+        assert got.stats[k] == want["stats"][k], k
+
+
+@pytest.mark.parametrize("name,factory", [
+    ("c1_tabletop_1024", lambda: scenes.tabletop_boxes(1024)),
+    ("c2_mixed_2048", lambda: scenes.tabletop_mixed(2048)),
+    ("c3_kitchen_1024", lambda: scenes.kitchen(1024, attempts=128)),
+    ("c4_clutter_512", lambda: scenes.dense_clutter(512, n_objects=60)),
+    ("c5_sweep_4096x50", lambda: scenes.scale_sweep(4096, 50)),
+])
+def test_generate_matches_reference(gpu, ref, name, factory):
+    scene = factory()
+    eng, got, want = run_generate_pair(gpu, ref, scene)
+    assert_same(gpu, got, want)
+    assert got.stats["valid_instances"] > 0
+
+
+def test_generate_is_deterministic_and_warm(gpu, ref):
+    scene = scenes.tabletop_mixed(1024, n_objects=12)
+    eng = gpu.Engine(scene)
+    a = eng.generate(5)
+    b = eng.generate(5)  # warm: same engine, same seed -> identical output
+    assert np.array_equal(a.accepted, b.accepted) and np.array_equal(a.poses, b.poses)
+    c = eng.generate(6)
+    assert not np.array_equal(a.accepted, c.accepted)
+    assert_same(gpu, c, ref.generate(scene, 6, threads=8))
+
+
+def test_generate_relations_variants(gpu, ref):
+    """greater / equal bands, explicit vector direction, local frame, face_to, fixed yaw."""
+    pkg = gpu
+    base = scenes.tabletop_boxes(1024, n_objects=8, table=(1.6, 1.2))
+    rels = {
+        2: pkg.Relation(anchor=1, distance_type=A.SB_DIST_GREATER, direction=A.SB_DIR_FRONT,
+                        distance=0.2, angle_threshold=math.pi / 3),
+        3: pkg.Relation(anchor=0, distance_type=A.SB_DIST_EQUAL, direction=A.SB_DIR_VECTOR,
+                        direction_vector=(0.3, -0.4), distance=0.3, frame=A.SB_FRAME_LOCAL),
+        5: pkg.Relation(anchor=4, distance_type=A.SB_DIST_LESS, distance=0.35),
+        6: pkg.Relation(anchor=2, direction=A.SB_DIR_RIGHT, frame=A.SB_FRAME_LOCAL),
+    }
+    for k, r in rels.items():
+        base.placements[k].relation = r
+    base.placements[4].orientation = A.SB_ORIENT_FACE_TO
+    base.placements[4].face_target = 0
+    base.placements[7].orientation = A.SB_ORIENT_FIXED
+    eng, got, want = run_generate_pair(pkg, ref, base, seed=3)
+    assert_same(pkg, got, want)
+
+
+def test_generate_canonical_relation_fast_path(gpu, ref):
+    """N=1: anchors cannot vary, so the relation region is canonical and the FIFO
+    fast path samples from it (relationships.cpp:188-190)."""
+    scene = scenes.tabletop_mixed(1, n_objects=9)
+    eng, got, want = run_generate_pair(gpu, ref, scene, seed=2)
+    assert got.stats["per_instance_placements"] == 0
+    assert_same(gpu, got, want)
+
+
+def test_generate_impossible_placement(gpu, ref):
+    """An object larger than its support can never be placed: every instance invalid."""
+    pkg = gpu
+    scene = scenes.tabletop_boxes(256, n_objects=3, attempts=5)
+    scene.meshes[2] = pkg.make_box(3.0, 3.0, 0.1)
+    eng, got, want = run_generate_pair(pkg, ref, scene)
+    assert got.valid.sum() == 0
+    assert_same(pkg, got, want)
+
+
+class ThreadAllgather:
+    """In-process allgather among `world` engine threads (one GPU, several shards)."""
+
+    def __init__(self, world):
+        self.world = world
+        self.barrier = threading.Barrier(world)
+        self.slots = [None] * world
+
+    def fn(self, rank):
+        def allgather(vals):
+            self.slots[rank] = list(vals)
+            self.barrier.wait()
+            out = [v for r in range(self.world) for v in self.slots[r]]
+            self.barrier.wait()
+            return out
+        return allgather
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_generate_equals_single(gpu, ref, world):
+    """Variation-batch sharding: G shards with the per-round count exchange
+    reproduce the single-shard run bit for bit (fast path and per-instance path)."""
+    pkg = gpu
+    scene = scenes.tabletop_mixed(1500, n_objects=10)
+    whole = pkg.Engine(scene).generate(4)
+    ag = ThreadAllgather(world)
+    bounds = [scene.n_instances * r // world for r in range(world + 1)]
+    engines = [pkg.Engine(scene, pkg.Shard(bounds[r], bounds[r + 1], r, world, ag.fn(r)))
+               for r in range(world)]
+    results = [None] * world
+
+    def run(r):
+        results[r] = engines[r].generate(4)
+
+    ts = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    acc = np.concatenate([r.accepted for r in results], axis=1)
+    valid = np.concatenate([r.valid for r in results])
+    poses = np.concatenate([r.poses for r in results], axis=1)
+    assert np.array_equal(acc, whole.accepted)
+    assert np.array_equal(valid, whole.valid)
+    assert np.array_equal(poses, whole.poses)
