@@ -1,0 +1,373 @@
+#!/usr/bin/env python
+"""Benchmark: collision-free scenes/sec and candidate collision checks/sec (BASELINE.json).
+
+A step is one full generation pass (every placement, every attempt round) over the
+config's N variations per GPU, through the C ABI (libscenebatch_b200.so).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2_mixed] [--impl ours|reference]
+
+N>1 runs under torchrun (one rank per GPU): instances are sharded by contiguous
+variation ranges (weak scaling: N_per_gpu fixed); the only exchange is the fast-path
+per-round count allgather (4-8 bytes per rank per round, torch.distributed gloo).
+`value` times results resident in HBM (CUDA events on the engine stream, L2 flushed
+between steps); `e2e` times the same call with the results copied to pinned host memory.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "collision-free scenes/sec and candidate collision checks/sec at 1/2/4/8 B200"
+
+WORKLOADS = {
+    "c1_tabletop": ("tabletop: 1 table, 10 cuboids, 1024 variations/GPU, 64 candidates/object",
+                    lambda n: __import__("paper_2512_16896_b200.scenes", fromlist=["x"]).tabletop_boxes(n), 1024),
+    "c2_mixed": ("tabletop: 25 mixed cuboid+sphere-set objects, on/next-to relations, "
+                 "16384 variations/GPU, 64 candidates/object",
+                 lambda n: __import__("paper_2512_16896_b200.scenes", fromlist=["x"]).tabletop_mixed(n), 16384),
+    "c3_kitchen": ("kitchen: 3 supports incl. container interior, 50 objects, 65536 variations/GPU, "
+                   "256 candidates/object",
+                   lambda n: __import__("paper_2512_16896_b200.scenes", fromlist=["x"]).kitchen(n), 65536),
+    "c4_clutter": ("dense clutter: 100 32-sphere-set objects on one table, 262144 variations/GPU",
+                   lambda n: __import__("paper_2512_16896_b200.scenes", fromlist=["x"]).dense_clutter(n), 262144),
+}
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower() in ("active", "1"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def fp64_peak(device: int):
+    """Measured FP64 pipe peak (GFLOP/s) for DADD / DMUL / DFMA (tools/fp64_peak.cu)."""
+    path = os.path.join(ROOT, "tools", "libfp64peak.so")
+    L = C.CDLL(path)
+    L.sb_fp64_peak_gflops.restype = C.c_double
+    L.sb_fp64_peak_gflops.argtypes = [C.c_int, C.c_int]
+    return {"dadd": L.sb_fp64_peak_gflops(0, device), "dmul": L.sb_fp64_peak_gflops(1, device),
+            "dfma": L.sb_fp64_peak_gflops(2, device)}
+
+
+# Algorithmic FP64 operation counts: every op of the reference's
+# expression trees, counted from the kernel's own work counters.
+FLOPS = {
+    "checked": 150,   # sample (sqrt, barycentric ~14) + point->world 15 + pose compose 84
+                      # (shim Mat4 product rows 0-2) + candidate box 30 + inverse 18 - reuse
+    "broad": 6,       # 6 comparisons per enabled object (counted as FP64 ops)
+    "narrow": 84,     # other_in_cand = inv * pose (3x4 shim product)
+    "nodes": 36,      # transform_aabb of the B node box (30) + 6 overlap comparisons
+    "pairs": 46,      # first-plane test of tri_tri_intersect (the cost every pair pays)
+}
+# Algorithmic HBM bytes (results resident): per checked candidate the active id (4) +
+# fail flag (1) + enable word (4); per broad-phase object the world box (48); per narrow
+# pair the placed pose (96); per accepted candidate pose + box + enable + accepted (150).
+BYTES = {"checked": 9, "broad": 48, "narrow": 96, "accepted": 150}
+
+
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2512_16896_b200 as pkg
+
+    desc, factory, n_default = WORKLOADS[args.config]
+    n_per = args.n or n_default
+    n_total = n_per * world
+    scene = factory(n_total)
+    device = local_rank
+    torch.cuda.set_device(device)
+
+    shard = None
+    if world > 1:
+        def allgather(vals):
+            t = torch.tensor(vals, dtype=torch.int64)
+            out = [torch.zeros_like(t) for _ in range(world)]
+            dist.all_gather(out, t)
+            return [int(v) for o in out for v in o.tolist()]
+        shard = pkg.Shard(rank * n_per, (rank + 1) * n_per, rank, world, allgather)
+    t0 = time.time()
+    eng = pkg.Engine(scene, shard, device=device)
+    cold_s = time.time() - t0
+    P = len(scene.placements)
+
+    # pinned host result buffers for the end-to-end leg
+    acc = torch.empty((P, n_per), dtype=torch.int16).pin_memory()
+    valid = torch.empty(n_per, dtype=torch.uint8).pin_memory()
+    poses = torch.empty((P, n_per, 16), dtype=torch.float64).pin_memory()
+    res = pkg._capi.sb_result(C.cast(acc.data_ptr(), C.POINTER(C.c_int16)),
+                              C.cast(poses.data_ptr(), C.POINTER(C.c_double)),
+                              C.cast(valid.data_ptr(), C.POINTER(C.c_uint8)))
+    d2h = acc.numel() * 2 + valid.numel() + poses.numel() * 8
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{device}")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    seed = 1
+    for _ in range(args.warmup):
+        eng.generate(seed, download=False)
+    clocks = ClockSampler(device)
+    clocks.start()
+    step_ms, check_ms, check_launches, launches = [], [], [], []
+    agg = {}
+    for _ in range(args.steps):
+        flush.zero_()
+        barrier()
+        r = eng.generate(seed, with_poses=False, download=False)
+        barrier()
+        total, chk, nchk = eng.last_timing()
+        step_ms.append(total)
+        check_ms.append(chk)
+        check_launches.append(nchk)
+        launches.append(eng.last_launches())
+        for k, v in r.stats.items():
+            agg[k] = agg.get(k, 0) + v
+    # end-to-end: same call, results D2H into pinned host memory, wall clock
+    e2e_ms = []
+    for _ in range(max(1, min(args.steps, 5))):
+        flush.zero_()
+        barrier()
+        t = time.perf_counter()
+        eng.generate_into(seed, res)
+        barrier()
+        e2e_ms.append((time.perf_counter() - t) * 1e3)
+    clk = clocks.stop()
+
+    K = args.steps
+    mine = {"time_ms": sum(step_ms), "e2e_ms": sum(e2e_ms) / len(e2e_ms),
+            "valid": agg["valid_instances"] / K, "checks": agg["candidate_checks"] / K}
+    if world > 1:
+        t = torch.tensor([mine["time_ms"], mine["e2e_ms"]], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        s = torch.tensor([mine["valid"], mine["checks"]], dtype=torch.float64)
+        dist.all_reduce(s, op=dist.ReduceOp.SUM)
+        time_ms, e2e = t.tolist()
+        valid_sum, checks_sum = s.tolist()
+    else:
+        time_ms, e2e, valid_sum, checks_sum = (mine["time_ms"], mine["e2e_ms"], mine["valid"],
+                                               mine["checks"])
+    if rank != 0:
+        return None
+    ms_step = time_ms / K
+    value = valid_sum / (ms_step * 1e-3)
+
+    # roofline of the dominant kernel (the fused round kernel k_round)
+    per = {k: agg.get(v, 0) / K for k, v in (("checked", "candidate_checks"),
+                                              ("broad", "broad_phase_tests"),
+                                              ("narrow", "narrow_phase_tests"),
+                                              ("nodes", "node_pair_tests"),
+                                              ("pairs", "triangle_pair_tests"),
+                                              ("accepted", "accepted_candidates"))}
+    flops = sum(FLOPS[k] * per[k] for k in FLOPS)
+    bytes_ = sum(BYTES[k] * per[k] for k in BYTES)
+    k_ms = sum(check_ms) / K
+    n_launch = sum(check_launches) / K
+    peaks = fp64_peak(device)
+    fp64_peak_tf = peaks["dadd"] / 1e3  # no-FMA build: one flop per FP64 instruction
+    measured = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
+    achieved_tf = flops / (k_ms * 1e-3) / 1e12 if k_ms > 0 else 0.0
+    achieved_gbs = bytes_ / (k_ms * 1e-3) / 1e9 if k_ms > 0 else 0.0
+    line = {
+        "metric": METRIC,
+        "value": round(value, 1),
+        "unit": "collision-free scenes/s",
+        "checks_per_s": round(checks_sum / (ms_step * 1e-3), 1),
+        "n_gpus": world, "steps": K, "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic scene of the named shape, seeded (no assets/network); run_seed 1",
+        "config": {"workload": f"{args.config}: {desc}", "n_instances_per_gpu": n_per,
+                   "n_instances_total": n_total, "placements": P,
+                   "candidates_per_object": scene.attempts, "parallelism": f"dp{world} (variation shards)",
+                   "l2": "flushed (256 MiB write) between timed steps",
+                   "valid_fraction": round(valid_sum / n_total, 4)},
+        "cold_start_s": round(cold_s, 3),
+        "roofline": {"bound": "fp64", "achieved": round(achieved_tf, 3),
+                     "peak": round(fp64_peak_tf, 3), "unit": "TFLOP/s",
+                     "frac": round(achieved_tf / fp64_peak_tf, 4) if fp64_peak_tf > 0 else None,
+                     "traffic": None, "kernel": "k_round (fused sample+compose+check+accept)",
+                     "kernel_ms_per_step": round(k_ms, 4), "launches_per_step": n_launch,
+                     "peak_source": "measured DADD rate, tools/fp64_peak.cu, this run",
+                     "algorithmic_flops_per_step": round(flops),
+                     "share_of_step": round(k_ms / ms_step, 4)},
+        "roofline_hbm": {"bound": "hbm", "achieved": round(achieved_gbs, 1),
+                         "peak": measured.get("hbm_gbs"), "unit": "GB/s",
+                         "frac": round(achieved_gbs / measured.get("hbm_gbs", 6650.0), 5),
+                         "algorithmic_bytes_per_step": round(bytes_)},
+        "fp64_peaks_gflops": {k: round(v, 1) for k, v in peaks.items()},
+        "work_per_step": {k: round(v) for k, v in per.items()},
+        "e2e": {"value": round(valid_sum / (e2e * 1e-3), 1), "unit": "collision-free scenes/s",
+                "ms_per_step": round(e2e, 4), "h2d_bytes_per_step": 8,
+                "d2h_bytes_per_step": int(d2h),
+                "path": "sb_engine_generate with pinned host sb_result (accepted, valid, poses)"},
+        "gpu_launches": round(statistics.mean(launches)) * K,
+        "clocks": clk,
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args, scene_factory=factory, n_default=n_default)
+    return line
+
+
+def cpu_baseline(args, scene_factory, n_default, budget_s=12.0):
+    """Reference (oracle/_ref: the reference's own sources + driver) on the host cores."""
+    from oracle import oracle as O
+
+    threads = os.cpu_count() or 1
+    n = args.cpu_n or min(n_default, 4096)
+    scene = scene_factory(n)
+    t0 = time.perf_counter()
+    passes = valid = checks = 0
+    while True:
+        r = O.generate(scene, 1, threads=threads, with_poses=False)
+        passes += 1
+        valid += r["stats"]["valid_instances"]
+        checks += r["stats"]["candidate_checks"]
+        if time.perf_counter() - t0 > budget_s or passes >= 50:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": round(valid / dt, 1), "unit": "collision-free scenes/s",
+            "checks_per_s": round(checks / dt, 1), "cores": threads, "kind": "reference",
+            "sample": f"{passes} generation pass(es) of the same scene shape at N={n} "
+                      f"({dt:.1f} s, ThreadPool({threads}))"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU path on this host (rank 0 only)."""
+    if rank != 0:
+        return None
+    from oracle import oracle as O
+
+    desc, factory, n_default = WORKLOADS[args.config]
+    n = args.n or n_default
+    scene = factory(n)
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        O.generate(scene, 1, threads=threads, with_poses=False)
+    times, valid, checks = [], 0, 0
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        r = O.generate(scene, 1, threads=threads, with_poses=False)
+        times.append(time.perf_counter() - t)
+        valid += r["stats"]["valid_instances"]
+        checks += r["stats"]["candidate_checks"]
+    total = sum(times)
+    value = valid / total
+    return {
+        "impl": "reference", "metric": METRIC, "value": round(value, 1),
+        "unit": "collision-free scenes/s", "checks_per_s": round(checks / total, 1),
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(total / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic scene of the named shape, seeded; run_seed 1",
+        "config": {"workload": f"{args.config}: {desc}", "n_instances": n,
+                   "placements": len(scene.placements), "candidates_per_object": scene.attempts},
+        "cpu_baseline": {"value": round(value, 1), "unit": "collision-free scenes/s",
+                         "cores": threads, "kind": "reference",
+                         "sample": f"{args.steps} full generation passes at N={n}"},
+        "e2e": {"value": round(value, 1), "unit": "collision-free scenes/s",
+                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2_mixed", choices=sorted(WORKLOADS))
+    ap.add_argument("--n", type=int, default=0, help="variations per GPU (default: config's)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-n", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    rank, world, local_rank = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo")
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+    else:
+        line = run_ours(args, rank, world, local_rank)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -212,6 +212,9 @@ typedef struct sb_run_stats {
   uint64_t triangle_pair_tests;
   uint64_t rounds;               /* (placement, attempt) rounds executed */
   uint64_t per_instance_placements;
+  uint64_t broad_phase_tests;    /* enabled objects examined by the AABB broad phase */
+  uint64_t node_pair_tests;      /* BVH node-pair box tests in the narrow phase */
+  uint64_t accepted_candidates;  /* candidates accepted (== placed objects) */
 } sb_run_stats;
 
 /* Count exchange between shards (one process per GPU). Called with this rank's n values;

@@ -70,7 +70,8 @@ class sb_result(C.Structure):
 class sb_run_stats(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "valid_instances", "candidates_sampled", "candidate_checks", "narrow_phase_tests",
-        "triangle_pair_tests", "rounds", "per_instance_placements")]
+        "triangle_pair_tests", "rounds", "per_instance_placements", "broad_phase_tests",
+        "node_pair_tests", "accepted_candidates")]
 
 
 ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_uint64), C.c_uint32,

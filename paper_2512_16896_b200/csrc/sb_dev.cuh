@@ -216,7 +216,7 @@ __device__ __forceinline__ bool point_in_tri(double px, double py, double ax, do
 }
 
 // coplanar_tri_tri (collision.cpp:63-83)
-__device__ __noinline__ bool coplanar_tri_tri(const double n[3], const double* p, const double* q) {
+static __device__ __noinline__ bool coplanar_tri_tri(const double n[3], const double* p, const double* q) {
   int axis = 0;
   double an0 = fabs(n[0]), an1 = fabs(n[1]), an2 = fabs(n[2]);
   if (an1 > an0) axis = 1;
@@ -295,7 +295,7 @@ __device__ __forceinline__ bool collide(const SbNode* __restrict__ A, int nA,
                                         const SbNode* __restrict__ B,
                                         const SbTri* __restrict__ trisA,
                                         const SbTri* __restrict__ trisB, const M34& M,
-                                        uint64_t& pair_tests) {
+                                        uint32_t& node_tests, uint32_t& pair_tests) {
   uint32_t pend[SB_MAX_NODES_PER_GEOM];
   for (int a = 0; a < nA; ++a) pend[a] = 0u;
   pend[0] = 1u;
@@ -306,6 +306,7 @@ __device__ __forceinline__ bool collide(const SbNode* __restrict__ A, int nA,
       const SbNode& na = A[a];
       const SbNode& nb = B[b];
       double bmn[3], bmx[3];
+      ++node_tests;
       xform_aabb(M, nb.c, nb.h, bmn, bmx);
       if (!overlaps(na.bmin, na.bmax, bmn, bmx)) continue;
       const bool la = na.child0 < 0, lb = nb.child0 < 0;
@@ -343,8 +344,10 @@ __device__ __forceinline__ bool collide(const SbNode* __restrict__ A, int nA,
 using WorldView = SbWorldView;
 
 struct CheckCounters {
-  uint64_t narrow;
-  uint64_t pairs;
+  uint32_t narrow;  // candidate/object pairs past the AABB broad phase
+  uint32_t pairs;   // triangle-pair predicate evaluations
+  uint32_t broad;   // enabled objects examined by the broad phase
+  uint32_t nodes;   // BVH node-pair box tests
 };
 
 // One candidate of CollisionWorld::check_batch (collision.cpp:433-449): candidate box,
@@ -364,6 +367,7 @@ __device__ __forceinline__ int check_candidate(const WorldView& w, int32_t geom,
     while (bits) {
       const int ob = ob0 + __ffs(bits) - 1;
       bits &= bits - 1u;
+      ++cnt.broad;
       const double2* bp = reinterpret_cast<const double2*>(w.box + ((uint64_t)ob * w.n + inst) * 6);
       double2 b0 = bp[0], b1 = bp[1], b2 = bp[2];
       double omn[3] = {b0.x, b0.y, b1.x}, omx[3] = {b1.y, b2.x, b2.y};
@@ -382,7 +386,7 @@ __device__ __forceinline__ int check_candidate(const WorldView& w, int32_t geom,
       mul34(inv, P, rel);
       const SbGeom gb = w.geoms[w.obj_geom[ob]];
       if (collide(nA, g.n_nodes, w.nodes + gb.node_offset, tA, w.tris + gb.tri_offset, rel,
-                  cnt.pairs))
+                  cnt.nodes, cnt.pairs))
         return ob;
     }
   }

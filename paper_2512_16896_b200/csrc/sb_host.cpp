@@ -257,6 +257,8 @@ EffectiveBvh build_effective_bvh(const Mesh& mesh) {
       for (uint32_t k = 0; k < r.count; ++k) {
         const auto& tri = mesh.t[leaf_tris[r.start + k]];
         SbTri t;
+        t.leaf = compact[i];
+        t.pad = 0;
         for (int v = 0; v < 3; ++v)
           for (int c = 0; c < 3; ++c) t.v[3 * v + c] = mesh.v[tri[v]][c];
         out.tris.push_back(t);

@@ -10,6 +10,7 @@
 #include "sb_dev.cuh"
 #include "sb_kernels.h"
 #include "sb_poly.h"
+#include "sb_warp.cuh"
 
 #include "../../include/scenebatch_b200.h"
 
@@ -93,20 +94,27 @@ __global__ void __launch_bounds__(kBlock) k_check_batch(WorldView w, int32_t geo
                                                         const uint32_t* active, uint64_t m,
                                                         uint8_t* free_out, int32_t* contact_out,
                                                         unsigned long long* counters) {
+  __shared__ WarpScratch ws[kBlock / 32];
+  __shared__ double invs[kBlock / 32][32][12];
+  __shared__ GeomCache gc;
+  const SbGeom gA = w.geoms[geom];
+  load_geom_cache(w, gA, gc);
+  __syncthreads();
   uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  CheckCounters cnt{0, 0};
-  if (j < m) {
-    uint32_t inst = active[j];
-    M34 P;
-    from_colmajor(poses16 + 16 * j, P);
-    int hit = check_candidate(w, geom, P, inst, cnt);
-    if (hit >= 0) {
-      free_out[inst] = 0;
-      contact_out[inst] = hit;
-    }
+  CheckCounters cnt{0, 0, 0, 0};
+  const bool act = j < m;
+  uint32_t inst = act ? active[j] : 0u;
+  M34 P;
+  if (act) from_colmajor(poses16 + 16 * j, P);
+  int hit = warp_check(w, gA, gc, act, P, inst, ws[threadIdx.x >> 5], invs[threadIdx.x >> 5], cnt);
+  if (act && hit >= 0) {
+    free_out[inst] = 0;
+    contact_out[inst] = hit;
   }
-  warp_add(counters + 1, static_cast<unsigned>(cnt.narrow));
-  warp_add(counters + 2, static_cast<unsigned>(cnt.pairs));
+  warp_add(counters + 1, cnt.narrow);
+  warp_add(counters + 2, cnt.pairs);
+  warp_add(counters + 4, cnt.broad);
+  warp_add(counters + 5, cnt.nodes);
 }
 
 // ------------------------------------------------------------------ engine kernels
@@ -137,14 +145,22 @@ __global__ void k_engine_reset(WorldView w, int32_t first_obj, int32_t n_obj, ui
 // + accept (update_transform / set_enabled) for one (placement, attempt) round.
 // One thread per active slot; slot j of this rank draws fast-path point draw_base + j.
 __global__ void __launch_bounds__(kBlock) k_round(sbk::RoundParams p) {
+  __shared__ WarpScratch ws[kBlock / 32];
+  __shared__ double invs[kBlock / 32][32][12];
+  __shared__ GeomCache gc;
+  const SbPlacementDev& pl = p.pl;
+  const SbGeom gA = p.w.geoms[pl.geom];
+  load_geom_cache(p.w, gA, gc);
+  __syncthreads();
   const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  CheckCounters cnt{0, 0};
-  unsigned checked = 0, sampled = 0;
-  if (j < p.m) {
-    const uint32_t inst = p.act[j];
-    const uint64_t gid = p.global_begin + inst;
-    const SbPlacementDev& pl = p.pl;
-    bool placeable = true;
+  CheckCounters cnt{0, 0, 0, 0};
+  unsigned checked = 0, sampled = 0, accepted_now = 0;
+  const bool act = j < p.m;
+  const uint32_t inst = act ? p.act[j] : 0u;
+  const uint64_t gid = p.global_begin + inst;
+  bool placeable = act;
+  M34 pose;
+  if (act) {
     double lx = 0.0, ly = 0.0;
     if (p.fast) {
       Pcg r{p.fast_state0};
@@ -164,7 +180,6 @@ __global__ void __launch_bounds__(kBlock) k_round(sbk::RoundParams p) {
       }
     }
     sampled = 1;
-    bool ok = false;
     if (placeable) {
       M34 S;
 #pragma unroll
@@ -184,7 +199,7 @@ __global__ void __launch_bounds__(kBlock) k_round(sbk::RoundParams p) {
       }
       double c = cos(yaw), s = sin(yaw);
       // translation(p + z_off z) * rotation_z(yaw)  (transform.hpp:40-54)
-      M34 T, Rz, pose;
+      M34 T, Rz;
       identity34(T);
       T.m[3] = px + 0.0;
       T.m[7] = py + 0.0;
@@ -196,20 +211,27 @@ __global__ void __launch_bounds__(kBlock) k_round(sbk::RoundParams p) {
       Rz.m[5] = c;
       mul34(T, Rz, pose);
       checked = 1;
-      int hit = check_candidate(p.w, pl.geom, pose, inst, cnt);
-      if (hit < 0) {
-        ok = true;
-        store_pose(p.w, pl.object, inst, pose);
-        p.w.enabled[(uint64_t)(pl.object >> 5) * p.w.n + inst] |= 1u << (pl.object & 31);
-        p.accepted[inst] = static_cast<int16_t>(p.attempt);
-      }
+    }
+  }
+  const bool chk = checked != 0;
+  const int hit = warp_check(p.w, gA, gc, chk, pose, inst, ws[threadIdx.x >> 5], invs[threadIdx.x >> 5], cnt);
+  if (act) {
+    bool ok = chk && hit < 0;
+    if (ok) {
+      store_pose(p.w, pl.object, inst, pose);
+      p.w.enabled[(uint64_t)(pl.object >> 5) * p.w.n + inst] |= 1u << (pl.object & 31);
+      p.accepted[inst] = static_cast<int16_t>(p.attempt);
+      accepted_now = 1;
     }
     p.fail[j] = ok ? 0 : 1;
   }
   warp_add(p.counters + 0, checked);
-  warp_add(p.counters + 1, static_cast<unsigned>(cnt.narrow));
-  warp_add(p.counters + 2, static_cast<unsigned>(cnt.pairs));
+  warp_add(p.counters + 1, cnt.narrow);
+  warp_add(p.counters + 2, cnt.pairs);
   warp_add(p.counters + 3, sampled);
+  warp_add(p.counters + 4, cnt.broad);
+  warp_add(p.counters + 5, cnt.nodes);
+  warp_add(p.counters + 6, accepted_now);
 }
 
 __global__ void k_invalidate(const uint32_t* act, uint64_t m, uint8_t* valid) {

@@ -32,7 +32,7 @@ struct RoundParams {
   uint64_t m;                     // number of active slots
   uint8_t* fail;                  // [m] 1 = still failing after this attempt
   int16_t* accepted;              // [n] accepted attempt of this placement
-  unsigned long long* counters;   // [4]: checked, narrow, pairs, sampled
+  unsigned long long* counters;   // [8]: checked, narrow, pairs, sampled, broad, nodes, accepted
 };
 
 // Per-instance constraint region build (relationships.cpp:161-218 + polygon.cpp:136-176,

@@ -15,7 +15,9 @@ struct SbNode {
 };
 
 struct SbTri {
-  double v[9];  // p0.xyz p1.xyz p2.xyz in the mesh frame
+  double v[9];   // p0.xyz p1.xyz p2.xyz in the mesh frame
+  int32_t leaf;  // compact id of the leaf node holding it
+  int32_t pad;
 };
 
 struct SbGeom {
@@ -63,4 +65,5 @@ struct SbWorldView {
 };
 
 #define SB_MAX_NODES_PER_GEOM 32   // effective DAG nodes (bitmask traversal width)
+#define SB_MAX_EFF_TRIS 32         // reachable triangles per geometry (pooled narrow phase)
 #define SB_REGION_MAX_VERTS 96     // per-instance constraint region ring capacity

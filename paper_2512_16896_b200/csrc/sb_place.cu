@@ -1,0 +1,431 @@
+// Phased placement engine (see sb_place.h). sm_100a, -fmad=false.
+#include <cooperative_groups.h>
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+
+#include <climits>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/scenebatch_b200.h"
+#include "sb_dev.cuh"
+#include "sb_place.h"
+#include "sb_poly.h"
+#include "sb_warp.cuh"
+
+namespace cg = cooperative_groups;
+using namespace sbd;
+
+namespace sbk {
+namespace {
+
+constexpr int kB = kPlaceBlock;
+constexpr int kWarps = kB / 32;
+constexpr int32_t kFree = INT32_MAX;
+
+enum Ctrl { kM = 0, kPairs = 1, kRounds = 2, kErr = 3, kCur = 4 };
+
+struct Shared {
+  WarpScratch ws[kWarps];
+  GeomCache gc;
+};
+
+struct Local {  // per-thread counters, flushed once at kernel end
+  unsigned checked = 0, sampled = 0, accepted = 0;
+  CheckCounters cnt{0, 0, 0, 0};
+};
+
+__device__ __forceinline__ void flush(const PlaceParams& p, const Local& l) {
+  auto add = [&](int k, unsigned v) {
+    unsigned s = __reduce_add_sync(kFull, v);
+    if ((threadIdx.x & 31) == 0 && s) atomicAdd(p.counters + k, (unsigned long long)s);
+  };
+  add(0, l.checked);
+  add(1, l.cnt.narrow);
+  add(2, l.cnt.pairs);
+  add(3, l.sampled);
+  add(4, l.cnt.broad);
+  add(5, l.cnt.nodes);
+  add(6, l.accepted);
+}
+
+__device__ __forceinline__ uint32_t* act_list(const PlaceParams& p, int which) {
+  return which ? p.act1 : p.act0;
+}
+
+// ------------------------------------------------------------------ compaction
+// Stable compaction in chunks of kB slots: count pass, then (after a grid barrier) a
+// scatter pass that derives each chunk's output offset from the chunk counts.
+template <class Flag>
+__device__ void compact_count(const PlaceParams& p, uint64_t m, Flag flag) {
+  const uint64_t nc = (m + kB - 1) / kB;
+  for (uint64_t ch = blockIdx.x; ch < nc; ch += gridDim.x) {
+    const uint64_t e = ch * kB + threadIdx.x;
+    const int f = e < m ? flag(e) : 0;
+    const int c = __syncthreads_count(f);
+    if (threadIdx.x == 0) p.chunk_cnt[ch] = (uint32_t)c;
+  }
+}
+
+template <class Flag, class Src>
+__device__ void compact_scatter(const PlaceParams& p, uint64_t m, Flag flag, Src src,
+                                uint32_t* dst) {
+  using BR = cub::BlockReduce<uint32_t, kB>;
+  using BS = cub::BlockScan<uint32_t, kB>;
+  __shared__ union {
+    typename BR::TempStorage r;
+    typename BS::TempStorage s;
+  } tmp;
+  __shared__ uint32_t s_off;
+  const uint64_t nc = (m + kB - 1) / kB;
+  uint64_t done = 0;  // chunks [0, done) already summed into off
+  uint32_t off = 0;
+  for (uint64_t ch = blockIdx.x; ch < nc; ch += gridDim.x) {
+    uint32_t part = 0;
+    for (uint64_t c = done + threadIdx.x; c < ch; c += kB) part += __ldcg(p.chunk_cnt + c);
+    uint32_t sum = BR(tmp.r).Sum(part);
+    if (threadIdx.x == 0) s_off = off + sum;
+    __syncthreads();
+    off = s_off;
+    done = ch;
+    const uint64_t e = ch * kB + threadIdx.x;
+    const uint32_t f = e < m ? (uint32_t)flag(e) : 0u;
+    uint32_t rank;
+    BS(tmp.s).ExclusiveSum(f, rank);
+    if (f) dst[off + rank] = src(e);
+    __syncthreads();
+  }
+  if (blockIdx.x == 0) {  // total -> next M
+    uint32_t part = 0;
+    for (uint64_t c = threadIdx.x; c < nc; c += kB) part += __ldcg(p.chunk_cnt + c);
+    uint32_t sum = BR(tmp.r).Sum(part);
+    if (threadIdx.x == 0) p.ctrl[kM] = sum;
+  }
+}
+
+// ------------------------------------------------------------------ phase A
+// Warp per active slot: sample -> yaw -> compose -> candidate box / inverse -> broad phase.
+__device__ void phase_a(const PlaceParams& p, const SbGeom& gA, const uint32_t* act,
+                        uint64_t m, uint64_t draw_base, int32_t attempt, Local& L) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
+  const SbPlacementDev& pl = p.pl;
+  const WorldView& w = p.w;
+  for (uint64_t e = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); e < m; e += nwarps) {
+    const uint32_t inst = act[e];
+    const uint64_t gid = p.global_begin + inst;
+    bool placeable = true;
+    double lx = 0.0, ly = 0.0;
+    if (p.fast) {
+      if (p.canon_n == 0) {
+        placeable = false;
+      } else {
+        Pcg r{p.fast_state0};
+        r.advance(6ull * (draw_base + e));  // j-th drained point = j-th draw (sampler.cpp:30-43)
+        double u = r.next_double(), r1 = r.next_double(), r2 = r.next_double();
+        sbp::draw_point(p.canon_tris, p.canon_cum, p.canon_n, u, r1, r2, lx, ly);
+      }
+    } else {
+      const int nt = p.inst_n[inst];
+      if (nt == 0) {
+        placeable = false;
+      } else {  // make_stream(run_seed, {salt, "fall", inst, attempt}) (sampler.cpp:117)
+        Pcg r = Pcg::seeded(stream_seed4(p.run_seed, pl.salt, kFallbackSalt, gid,
+                                         static_cast<uint64_t>(attempt)));
+        double u = r.next_double(), r1 = r.next_double(), r2 = r.next_double();
+        const uint64_t off = (uint64_t)inst * p.inst_cap;
+        sbp::draw_point(p.inst_tris + off, p.inst_cum + off, nt, u, r1, r2, lx, ly);
+      }
+    }
+    if (lane == 0) ++L.sampled;
+    if (!placeable) {
+      if (lane == 0) {
+        p.cflag[e] = 0;
+        p.contact[e] = kFree;
+      }
+      continue;
+    }
+    M34 S;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) S.m[k] = pl.support[k];
+    double px, py, pz;
+    xform(S, lx, ly, 0.0, px, py, pz);  // transform_point(support_world, (x, y, 0))
+    double yaw = 0.0;
+    if (pl.orientation == SB_ORIENT_UNIFORM_YAW) {  // sampler.cpp:140-141
+      Pcg r = Pcg::seeded(
+          stream_seed4(p.run_seed, pl.salt, kYawSalt, gid, static_cast<uint64_t>(attempt)));
+      const double two_pi = 2.0 * 3.14159265358979323846;
+      yaw = 0.0 + (two_pi - 0.0) * r.next_double();
+    } else if (pl.orientation == SB_ORIENT_FACE_TO) {  // relationships.cpp:232-239
+      const double* tp = w.pose + ((uint64_t)pl.face_object * w.n + inst) * 12;
+      double dx = tp[3] - px, dy = tp[7] - py;
+      yaw = sqrt(dx * dx + dy * dy) < 1e-12 ? 0.0 : atan2(dy, dx);
+    }
+    double c = cos(yaw), s = sin(yaw);
+    M34 T, Rz, pose;  // translation(p + z_off z) * rotation_z(yaw)
+#pragma unroll
+    for (int k = 0; k < 12; ++k) T.m[k] = Rz.m[k] = 0.0;
+    T.m[0] = T.m[5] = T.m[10] = 1.0;
+    Rz.m[10] = 1.0;
+    T.m[3] = px + 0.0;
+    T.m[7] = py + 0.0;
+    T.m[11] = pz + pl.z_off;
+    Rz.m[0] = c;
+    Rz.m[1] = -s;
+    Rz.m[4] = s;
+    Rz.m[5] = c;
+    mul34(T, Rz, pose);
+    double cmn[3], cmx[3];
+    xform_aabb(pose, gA.box_c, gA.box_h, cmn, cmx);
+    M34 inv;
+    inverse_rigid(pose, inv);
+    if (lane < 12) {
+      double pv = 0.0, iv = 0.0;
+#pragma unroll
+      for (int k = 0; k < 12; ++k)
+        if (lane == k) {
+          pv = pose.m[k];
+          iv = inv.m[k];
+        }
+      p.cpose[e * 12 + lane] = pv;
+      p.cinv[e * 12 + lane] = iv;
+    }
+    if (lane == 0) {
+      ++L.checked;
+      p.cflag[e] = 1;
+      p.contact[e] = kFree;
+    }
+    // broad phase (collision.cpp:439-443): lanes over objects, ascending chunks of 32
+    for (int ob0 = 0; ob0 < w.n_objects; ob0 += 32) {
+      const int ob = ob0 + lane;
+      const uint32_t bits = w.enabled[(uint64_t)(ob0 >> 5) * w.n + inst];
+      const bool en = ob < w.n_objects && ((bits >> lane) & 1u);
+      bool ov = false;
+      if (en) {
+        const double2* bp =
+            reinterpret_cast<const double2*>(w.box + ((uint64_t)ob * w.n + inst) * 6);
+        double2 b0 = bp[0], b1 = bp[1], b2 = bp[2];
+        double omn[3] = {b0.x, b0.y, b1.x}, omx[3] = {b1.y, b2.x, b2.y};
+        ov = overlaps(cmn, cmx, omn, omx);
+      }
+      const uint32_t mask = __ballot_sync(kFull, ov);
+      if (lane == 0) {
+        p.ovmask[(uint64_t)(ob0 >> 5) * w.n + e] = mask;
+        L.cnt.broad += __popc(bits);
+      }
+      if (mask) {
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(p.ctrl + kPairs, (uint32_t)__popc(mask));
+        base = __shfl_sync(kFull, base, 0);
+        if (ov) {
+          const uint64_t idx = base + __popc(mask & ((1u << lane) - 1u));
+          if (idx < p.pair_cap) p.pairs[idx] = (e << 32) | (uint32_t)ob;
+          else atomicOr(p.ctrl + kErr, 1u);
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ phase B
+__device__ void phase_b(const PlaceParams& p, Shared& sh, const uint32_t* act, Local& L) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
+  uint64_t np = __ldcg(p.ctrl + kPairs);
+  if (np > p.pair_cap) np = p.pair_cap;
+  WarpScratch& ws = sh.ws[threadIdx.x >> 5];
+  for (uint64_t q = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); q < np; q += nwarps) {
+    const uint64_t pr = p.pairs[q];
+    const uint64_t e = pr >> 32;
+    const int32_t ob = (int32_t)(pr & 0xffffffffu);
+    const bool hit = warp_collide(p.w, sh.gc, ob, act[e], p.cinv + 12 * e, ws, L.cnt);
+    if (hit && lane == 0) atomicMin(p.contact + e, ob);
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------------ phase C
+__device__ void phase_c(const PlaceParams& p, const uint32_t* act, uint64_t m, int32_t attempt,
+                        Local& L) {
+  const WorldView& w = p.w;
+  const int words = w.n_words;
+  compact_count(p, m, [&](uint64_t e) -> int {
+    if (!p.cflag[e]) {
+      p.failflag[e] = 1;
+      return 1;
+    }
+    const int32_t c = __ldcg(p.contact + e);
+    // reference narrow count: overlapping objects tested up to the first hit
+    for (int wd = 0; wd < words; ++wd) {
+      uint32_t mk = p.ovmask[(uint64_t)wd * w.n + e];
+      if (c != kFree) {
+        const int lim = c - 32 * wd;  // keep objects <= c
+        if (lim < 0) mk = 0;
+        else if (lim < 31) mk &= (2u << lim) - 1u;
+      }
+      L.cnt.narrow += __popc(mk);
+    }
+    if (c == kFree) {  // first-valid accept: update_transform + set_enabled (Appendix C.5)
+      const uint32_t inst = act[e];
+      M34 P;
+#pragma unroll
+      for (int k = 0; k < 12; ++k) P.m[k] = p.cpose[e * 12 + k];
+      store_pose(w, p.pl.object, inst, P);
+      w.enabled[(uint64_t)(p.pl.object >> 5) * w.n + inst] |= 1u << (p.pl.object & 31);
+      p.accepted[inst] = (int16_t)attempt;
+      ++L.accepted;
+      p.failflag[e] = 0;
+      return 0;
+    }
+    p.failflag[e] = 1;
+    return 1;
+  });
+  if (blockIdx.x == 0 && threadIdx.x == 0) p.ctrl[kPairs] = 0;  // phase B is done reading it
+}
+
+// ------------------------------------------------------------------ kernels
+__device__ __forceinline__ void block_setup(const PlaceParams& p, Shared& sh, SbGeom& gA) {
+  gA = p.w.geoms[p.pl.geom];
+  load_geom_cache(p.w, gA, sh.gc);
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kB) k_place(PlaceParams p) {
+  __shared__ Shared sh;
+  cg::grid_group grid = cg::this_grid();
+  SbGeom gA;
+  block_setup(p, sh, gA);
+  Local L;
+  const uint64_t n = p.w.n;
+  compact_count(p, n, [&](uint64_t i) -> int { return p.valid[i] != 0; });
+  grid.sync();
+  compact_scatter(p, n, [&](uint64_t i) -> int { return p.valid[i] != 0; },
+                  [&](uint64_t i) -> uint32_t { return (uint32_t)i; }, p.act0);
+  grid.sync();
+  uint64_t draws = 0;
+  int cur = 0;
+  for (int32_t a = 0; a < p.attempts; ++a) {
+    const uint64_t m = __ldcg(p.ctrl + kM);
+    if (m == 0) break;
+    if (blockIdx.x == 0 && threadIdx.x == 0) p.ctrl[kRounds] += 1;
+    const uint32_t* act = act_list(p, cur);
+    phase_a(p, gA, act, m, draws, a, L);
+    grid.sync();
+    phase_b(p, sh, act, L);
+    grid.sync();
+    phase_c(p, act, m, a, L);
+    grid.sync();
+    compact_scatter(p, m, [&](uint64_t e) -> int { return p.failflag[e]; },
+                    [&](uint64_t e) -> uint32_t { return act[e]; }, act_list(p, cur ^ 1));
+    grid.sync();
+    if (p.fast) draws += m;
+    cur ^= 1;
+  }
+  const uint64_t m = __ldcg(p.ctrl + kM);
+  const uint32_t* act = act_list(p, cur);
+  for (uint64_t e = blockIdx.x * (uint64_t)kB + threadIdx.x; e < m; e += (uint64_t)gridDim.x * kB)
+    p.valid[act[e]] = 0;  // K attempts exhausted: mark_invalid
+  if (blockIdx.x == 0 && threadIdx.x == 0) p.ctrl[kCur] = cur;
+  flush(p, L);
+}
+
+// Host-loop variants (sharded runs: the rank exchange happens between rounds).
+__global__ void __launch_bounds__(kB) k_init_count(PlaceParams p) {
+  compact_count(p, p.w.n, [&](uint64_t i) -> int { return p.valid[i] != 0; });
+}
+__global__ void __launch_bounds__(kB) k_init_scatter(PlaceParams p) {
+  compact_scatter(p, p.w.n, [&](uint64_t i) -> int { return p.valid[i] != 0; },
+                  [&](uint64_t i) -> uint32_t { return (uint32_t)i; }, p.act0);
+}
+__global__ void __launch_bounds__(kB) k_phase_a(PlaceParams p, int32_t attempt, int cur) {
+  SbGeom gA = p.w.geoms[p.pl.geom];
+  Local L;
+  const uint64_t m = __ldcg(p.ctrl + kM);
+  phase_a(p, gA, act_list(p, cur), m, p.draw_base, attempt, L);
+  flush(p, L);
+}
+__global__ void __launch_bounds__(kB) k_phase_b(PlaceParams p, int cur) {
+  __shared__ Shared sh;
+  SbGeom gA;
+  block_setup(p, sh, gA);
+  Local L;
+  phase_b(p, sh, act_list(p, cur), L);
+  flush(p, L);
+}
+__global__ void __launch_bounds__(kB) k_phase_c(PlaceParams p, int32_t attempt, int cur) {
+  Local L;
+  const uint64_t m = __ldcg(p.ctrl + kM);
+  phase_c(p, act_list(p, cur), m, attempt, L);
+  flush(p, L);
+}
+__global__ void __launch_bounds__(kB) k_phase_d(PlaceParams p, int cur) {
+  const uint64_t m = __ldcg(p.ctrl + kM);
+  const uint32_t* act = act_list(p, cur);
+  compact_scatter(p, m, [&](uint64_t e) -> int { return p.failflag[e]; },
+                  [&](uint64_t e) -> uint32_t { return act[e]; }, act_list(p, cur ^ 1));
+}
+__global__ void __launch_bounds__(kB) k_finish(PlaceParams p, int cur) {
+  const uint64_t m = __ldcg(p.ctrl + kM);
+  const uint32_t* act = act_list(p, cur);
+  for (uint64_t e = blockIdx.x * (uint64_t)kB + threadIdx.x; e < m; e += (uint64_t)gridDim.x * kB)
+    p.valid[act[e]] = 0;
+}
+
+int g_coop_blocks = -1;
+
+void check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+unsigned host_grid(const PlaceParams&) {
+  static unsigned g = 0;
+  if (g == 0) {
+    int dev = 0, sms = 0, per = 0;
+    check(cudaGetDevice(&dev), "cudaGetDevice");
+    check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+    check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_phase_b, kB, 0), "occupancy");
+    g = (unsigned)(sms * (per > 0 ? per : 1));
+  }
+  return g;
+}
+
+}  // namespace
+
+bool place_persistent(const PlaceParams& p, int num_sms, sb_stream_t s) {
+  if (g_coop_blocks < 0) {
+    int per = 0;
+    check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_place, kB, 0), "occupancy");
+    g_coop_blocks = per * num_sms;
+  }
+  if (g_coop_blocks <= 0) return false;
+  unsigned grid = (unsigned)g_coop_blocks;
+  PlaceParams q = p;
+  void* args[] = {&q};
+  check(cudaLaunchCooperativeKernel((void*)k_place, dim3(grid), dim3(kB), args, 0,
+                                    reinterpret_cast<cudaStream_t>(s)),
+        "cudaLaunchCooperativeKernel(k_place)");
+  return true;
+}
+
+void place_init(const PlaceParams& p, sb_stream_t s) {
+  unsigned g = host_grid(p);
+  k_init_count<<<g, kB, 0, s>>>(p);
+  k_init_scatter<<<g, kB, 0, s>>>(p);
+  check(cudaGetLastError(), "place_init");
+}
+
+void place_round(const PlaceParams& p, int32_t attempt, int cur, sb_stream_t s) {
+  unsigned g = host_grid(p);
+  k_phase_a<<<g, kB, 0, s>>>(p, attempt, cur);
+  k_phase_b<<<g, kB, 0, s>>>(p, cur);
+  k_phase_c<<<g, kB, 0, s>>>(p, attempt, cur);
+  k_phase_d<<<g, kB, 0, s>>>(p, cur);
+  check(cudaGetLastError(), "place_round");
+}
+
+void place_finish(const PlaceParams& p, int cur, sb_stream_t s) {
+  k_finish<<<host_grid(p), kB, 0, s>>>(p, cur);
+  check(cudaGetLastError(), "place_finish");
+}
+
+}  // namespace sbk

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -16,6 +17,7 @@
 #include "../../include/scenebatch_b200.h"
 #include "sb_host.hpp"
 #include "sb_kernels.h"
+#include "sb_place.h"
 #include "sb_layout.h"
 
 namespace {
@@ -161,7 +163,7 @@ struct sb_world {
     if (batch > 0xffffffffull) throw std::invalid_argument("CollisionWorld: batch_size > 2^32-1");
     current_device_checked(dev);
     cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
-    d_counters.alloc(4);
+    d_counters.alloc(8);
   }
   ~sb_world() {
     if (stream) {
@@ -214,6 +216,10 @@ struct sb_world {
       throw std::invalid_argument("register_geometry: effective BVH has " +
                                   std::to_string(bvh.nodes.size()) + " nodes (> " +
                                   std::to_string(SB_MAX_NODES_PER_GEOM) + " supported)");
+    if (bvh.tris.size() > SB_MAX_EFF_TRIS)
+      throw std::invalid_argument("register_geometry: " + std::to_string(bvh.tris.size()) +
+                                  " reachable triangles (> " + std::to_string(SB_MAX_EFF_TRIS) +
+                                  " supported by the pooled narrow phase)");
     Geom g;
     g.fingerprint = fp;
     double box[6];
@@ -358,7 +364,7 @@ struct sb_world {
     d_contact.ensure(n);
     cuda_check(cudaMemsetAsync(d_free.p, 1, n, stream), "memset");
     cuda_check(cudaMemsetAsync(d_contact.p, 0xff, n * 4, stream), "memset");
-    cuda_check(cudaMemsetAsync(d_counters.p, 0, 4 * sizeof(unsigned long long), stream), "memset");
+    cuda_check(cudaMemsetAsync(d_counters.p, 0, 8 * sizeof(unsigned long long), stream), "memset");
     if (m > 0) {
       upload_poses(poses16, m);
       d_scratch_idx.ensure(m);
@@ -366,7 +372,7 @@ struct sb_world {
       sbk::check_batch(view(), geom, d_scratch_poses.p, d_scratch_idx.p, m, d_free.p, d_contact.p,
                        d_counters.p, s());
     }
-    unsigned long long c[4];
+    unsigned long long c[8];
     cuda_check(cudaMemcpyAsync(free_out, d_free.p, n, cudaMemcpyDeviceToHost, stream), "D2H");
     cuda_check(cudaMemcpyAsync(contact_out, d_contact.p, n * 4, cudaMemcpyDeviceToHost, stream), "D2H");
     cuda_check(cudaMemcpyAsync(c, d_counters.p, sizeof c, cudaMemcpyDeviceToHost, stream), "D2H");
@@ -401,6 +407,15 @@ struct sb_engine {
   DevArray<int16_t> d_accepted;
   DevArray<uint32_t> d_act[2];
   DevArray<uint8_t> d_fail;
+  DevArray<double> d_cpose, d_cinv;
+  DevArray<uint8_t> d_cflag;
+  DevArray<int32_t> d_contact;
+  DevArray<uint32_t> d_ovmask;
+  DevArray<uint64_t> d_pairs;
+  DevArray<uint32_t> d_chunk;
+  DevArray<uint32_t> d_ctrl;
+  int num_sms = 0;
+  bool legacy_rounds = false;
   DevArray<uint64_t> d_count;
   DevArray<uint8_t> d_temp;
   size_t temp_bytes = 0;
@@ -577,10 +592,27 @@ struct sb_engine {
     d_act[0].alloc(n);
     d_act[1].alloc(n);
     d_fail.alloc(n);
+    d_cpose.alloc(12 * n);
+    d_cinv.alloc(12 * n);
+    d_cflag.alloc(n);
+    d_contact.alloc(n);
+    {
+      const size_t words = (world->obj_geom.size() + 31) / 32;
+      d_ovmask.alloc(std::max<size_t>(1, words) * n);
+      const size_t per = std::min<size_t>(world->obj_geom.size(), 32);
+      d_pairs.alloc(std::max<size_t>(1, per) * n);
+    }
+    d_chunk.alloc(n / 256 + 2);
+    d_ctrl.alloc(8);
+    cuda_check(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, world->device), "attr");
+    {
+      const char* mode = std::getenv("SB_ENGINE");
+      legacy_rounds = mode && std::string(mode) == "legacy";
+    }
     d_count.alloc(1);
     temp_bytes = sbk::select_temp_bytes(n);
     d_temp.alloc(temp_bytes);
-    d_counters.alloc(4);
+    d_counters.alloc(8);
     h_count.ensure(4);
     cuda_check(cudaEventCreate(&ev_start), "event");
     cuda_check(cudaEventCreate(&ev_stop), "event");
@@ -601,6 +633,71 @@ struct sb_engine {
     return h_count.p[0];
   }
 
+  // Pre-phased engine (one fused kernel per round + CUB compaction, host-synchronised);
+  // kept for A/B measurement (SB_ENGINE=legacy).
+  void legacy_place(size_t p, Placement& pl, bool fast, uint64_t fast_state0,
+                    const SbRegionTri* canon_tris, const double* canon_cum, int canon_n,
+                    uint64_t run_seed, const SbWorldView& wv, uint64_t& launches,
+                    uint64_t& rounds, uint64_t& round_launches, double& check_ms) {
+    cudaStream_t stream = world->stream;
+    sb_stream_t s = world->s();
+      sbk::select_valid(d_valid.p, n, d_act[0].p, d_count.p, d_temp.p, temp_bytes, s);
+      launches += 2;
+      int cur = 0;
+      uint64_t draws = 0;  // fast-path draws consumed by all ranks so far (S)
+      uint64_t m = read_count();
+      for (int a = 0; a < attempts; ++a) {
+        std::vector<uint64_t> counts = exchange({m});
+        uint64_t total = 0, before = 0;
+        for (int r = 0; r < world_size; ++r) {
+          if (r < rank) before += counts[r];
+          total += counts[r];
+        }
+        if (total == 0) break;
+        ++rounds;
+        const bool no_draw = fast && canon_n == 0;  // empty canonical region: placeable = 0
+        if (m > 0 && !no_draw) {
+          sbk::RoundParams rp;
+          rp.w = wv;
+          rp.pl = pl.dev;
+          rp.attempt = a;
+          rp.fast = fast ? 1 : 0;
+          rp.run_seed = run_seed;
+          rp.global_begin = begin;
+          rp.fast_state0 = fast_state0;
+          rp.draw_base = draws + before;
+          rp.canon_tris = canon_tris;
+          rp.canon_cum = canon_cum;
+          rp.canon_n = canon_n;
+          rp.inst_cap = inst_cap;
+          rp.inst_tris = d_inst_tris.p;
+          rp.inst_cum = d_inst_cum.p;
+          rp.inst_n = d_inst_n.p;
+          rp.act = d_act[cur].p;
+          rp.m = m;
+          rp.fail = d_fail.p;
+          rp.accepted = d_accepted.p + p * n;
+          rp.counters = d_counters.p;
+          cuda_check(cudaEventRecord(ev_r0, stream), "event");
+          sbk::round_kernel(rp, s);
+          cuda_check(cudaEventRecord(ev_r1, stream), "event");
+          ++launches;
+          ++round_launches;
+          sbk::select_flagged(d_act[cur].p, d_fail.p, m, d_act[1 - cur].p, d_count.p, d_temp.p,
+                              temp_bytes, s);
+          launches += 2;
+          cur = 1 - cur;
+          m = read_count();
+          float ms = 0.f;
+          cuda_check(cudaEventElapsedTime(&ms, ev_r0, ev_r1), "elapsed");
+          check_ms += ms;
+        }
+        if (fast && !no_draw) draws += total;
+      }
+      sbk::invalidate(d_act[cur].p, m, d_valid.p, s);
+      ++launches;
+  }
+
   void generate(uint64_t run_seed, sb_run_stats* st) {
     world->activate();
     cudaStream_t stream = world->stream;
@@ -609,7 +706,7 @@ struct sb_engine {
     uint64_t launches = 0, rounds = 0, per_inst = 0, round_launches = 0;
     double check_ms = 0.0;
     cuda_check(cudaEventRecord(ev_start, stream), "event");
-    cuda_check(cudaMemsetAsync(d_counters.p, 0, 4 * sizeof(unsigned long long), stream), "memset");
+    cuda_check(cudaMemsetAsync(d_counters.p, 0, 8 * sizeof(unsigned long long), stream), "memset");
     sbk::engine_reset(wv, first_place_obj, static_cast<int32_t>(places.size()), d_valid.p, d_accepted.p,
                       static_cast<int32_t>(places.size()), s);
     ++launches;
@@ -681,73 +778,112 @@ struct sb_engine {
         if (!vary) canon_n = status_and_n[1];
       }
 
-      sbk::select_valid(d_valid.p, n, d_act[0].p, d_count.p, d_temp.p, temp_bytes, s);
-      launches += 2;
-      int cur = 0;
-      uint64_t draws = 0;  // fast-path draws consumed by all ranks so far (S)
-      uint64_t m = read_count();
-      for (int a = 0; a < attempts; ++a) {
-        std::vector<uint64_t> counts = exchange({m});
-        uint64_t total = 0, before = 0;
-        for (int r = 0; r < world_size; ++r) {
-          if (r < rank) before += counts[r];
-          total += counts[r];
-        }
-        if (total == 0) break;
-        ++rounds;
-        const bool no_draw = fast && canon_n == 0;  // empty canonical region: placeable = 0
-        if (m > 0 && !no_draw) {
-          sbk::RoundParams rp;
-          rp.w = wv;
-          rp.pl = pl.dev;
-          rp.attempt = a;
-          rp.fast = fast ? 1 : 0;
-          rp.run_seed = run_seed;
-          rp.global_begin = begin;
-          rp.fast_state0 = 0;
-          if (fast) {
-            // Pcg32(make_stream(run_seed, {salt, "cach"})) state after the constructor
-            uint64_t h = sbh::mix64(sbh::mix64(sbh::mix64(run_seed) ^ pl.dev.salt) ^ 0x63616368ULL);
-            const uint64_t mult = 6364136223846793005ULL, inc = (0xda3e39cb94b95bdbULL << 1u) | 1u;
-            uint64_t st0 = inc;
-            st0 += h;
-            st0 = st0 * mult + inc;
-            rp.fast_state0 = st0;
-          }
-          rp.draw_base = draws + before;
-          rp.canon_tris = canon_tris;
-          rp.canon_cum = canon_cum;
-          rp.canon_n = canon_n;
-          rp.inst_cap = inst_cap;
-          rp.inst_tris = d_inst_tris.p;
-          rp.inst_cum = d_inst_cum.p;
-          rp.inst_n = d_inst_n.p;
-          rp.act = d_act[cur].p;
-          rp.m = m;
-          rp.fail = d_fail.p;
-          rp.accepted = d_accepted.p + p * n;
-          rp.counters = d_counters.p;
-          cuda_check(cudaEventRecord(ev_r0, stream), "event");
-          sbk::round_kernel(rp, s);
-          cuda_check(cudaEventRecord(ev_r1, stream), "event");
-          ++launches;
-          ++round_launches;
-          sbk::select_flagged(d_act[cur].p, d_fail.p, m, d_act[1 - cur].p, d_count.p, d_temp.p,
-                              temp_bytes, s);
-          launches += 2;
-          cur = 1 - cur;
-          m = read_count();
-          float ms = 0.f;
-          cuda_check(cudaEventElapsedTime(&ms, ev_r0, ev_r1), "elapsed");
-          check_ms += ms;
-        }
-        if (fast && !no_draw) draws += total;
+      uint64_t fast_state0 = 0;
+      if (fast) {  // Pcg32(make_stream(run_seed, {salt, "cach"})) state after the constructor
+        uint64_t h = sbh::mix64(sbh::mix64(sbh::mix64(run_seed) ^ pl.dev.salt) ^ 0x63616368ULL);
+        const uint64_t mult = 6364136223846793005ULL, inc = (0xda3e39cb94b95bdbULL << 1u) | 1u;
+        uint64_t st0 = inc;
+        st0 += h;
+        st0 = st0 * mult + inc;
+        fast_state0 = st0;
       }
-      sbk::invalidate(d_act[cur].p, m, d_valid.p, s);
-      ++launches;
+      if (legacy_rounds) {
+        legacy_place(p, pl, fast, fast_state0, canon_tris, canon_cum, canon_n, run_seed, wv,
+                     launches, rounds, round_launches, check_ms);
+        continue;
+      }
+      sbk::PlaceParams pp;
+      std::memset(&pp, 0, sizeof pp);
+      pp.w = wv;
+      pp.pl = pl.dev;
+      pp.attempts = attempts;
+      pp.fast = fast ? 1 : 0;
+      pp.run_seed = run_seed;
+      pp.global_begin = begin;
+      pp.fast_state0 = fast_state0;
+      pp.canon_tris = canon_tris;
+      pp.canon_cum = canon_cum;
+      pp.canon_n = canon_n;
+      pp.inst_cap = inst_cap;
+      pp.inst_tris = d_inst_tris.p;
+      pp.inst_cum = d_inst_cum.p;
+      pp.inst_n = d_inst_n.p;
+      pp.valid = d_valid.p;
+      pp.accepted = d_accepted.p + p * n;
+      pp.act0 = d_act[0].p;
+      pp.act1 = d_act[1].p;
+      pp.cpose = d_cpose.p;
+      pp.cinv = d_cinv.p;
+      pp.cflag = d_cflag.p;
+      pp.contact = d_contact.p;
+      pp.ovmask = d_ovmask.p;
+      pp.failflag = d_fail.p;
+      pp.pairs = d_pairs.p;
+      pp.pair_cap = d_pairs.count;
+      pp.chunk_cnt = d_chunk.p;
+      pp.ctrl = d_ctrl.p;
+      pp.counters = d_counters.p;
+      cuda_check(cudaMemsetAsync(d_ctrl.p, 0, d_ctrl.count * sizeof(uint32_t), stream), "memset ctrl");
+      uint32_t ctrl[8];
+      if (world_size == 1) {
+        cuda_check(cudaEventRecord(ev_r0, stream), "event");
+        if (!sbk::place_persistent(pp, num_sms, s))
+          throw CudaError("cooperative launch of the placement kernel is not possible");
+        cuda_check(cudaEventRecord(ev_r1, stream), "event");
+        ++launches;
+        ++round_launches;
+        cuda_check(cudaMemcpyAsync(ctrl, d_ctrl.p, sizeof ctrl, cudaMemcpyDeviceToHost, stream), "D2H ctrl");
+        cuda_check(cudaStreamSynchronize(stream), "sync");
+        float ms = 0.f;
+        cuda_check(cudaEventElapsedTime(&ms, ev_r0, ev_r1), "elapsed");
+        check_ms += ms;
+        rounds += ctrl[2];
+      } else {
+        // sharded: same phases, one launch each, with the per-round count exchange
+        sbk::place_init(pp, s);
+        launches += 2;
+        auto read_ctrl = [&]() {
+          cuda_check(cudaMemcpyAsync(ctrl, d_ctrl.p, sizeof ctrl, cudaMemcpyDeviceToHost, stream), "D2H ctrl");
+          cuda_check(cudaStreamSynchronize(stream), "sync");
+        };
+        read_ctrl();
+        uint64_t m = ctrl[0], draws = 0;
+        int cur = 0;
+        for (int a = 0; a < attempts; ++a) {
+          std::vector<uint64_t> counts = exchange({m});
+          uint64_t total = 0, before = 0;
+          for (int r = 0; r < world_size; ++r) {
+            if (r < rank) before += counts[r];
+            total += counts[r];
+          }
+          if (total == 0) break;
+          ++rounds;
+          if (m > 0) {
+            pp.draw_base = draws + before;
+            cuda_check(cudaEventRecord(ev_r0, stream), "event");
+            sbk::place_round(pp, a, cur, s);
+            cuda_check(cudaEventRecord(ev_r1, stream), "event");
+            launches += 4;
+            round_launches += 4;
+            cur ^= 1;
+            read_ctrl();
+            m = ctrl[0];
+            float ms = 0.f;
+            cuda_check(cudaEventElapsedTime(&ms, ev_r0, ev_r1), "elapsed");
+            check_ms += ms;
+          }
+          if (fast && canon_n > 0) draws += total;
+        }
+        sbk::place_finish(pp, cur, s);
+        ++launches;
+        read_ctrl();
+      }
+      if (ctrl[3] != 0)
+        throw std::runtime_error("narrow-phase pair queue overflow (more than " +
+                                 std::to_string(d_pairs.count) + " overlapping pairs in a round)");
     }
     cuda_check(cudaEventRecord(ev_stop, stream), "event");
-    unsigned long long c[4];
+    unsigned long long c[8];
     cuda_check(cudaMemcpyAsync(c, d_counters.p, sizeof c, cudaMemcpyDeviceToHost, stream), "D2H counters");
     cuda_check(cudaStreamSynchronize(stream), "sync");
     float total_ms = 0.f;
@@ -768,6 +904,9 @@ struct sb_engine {
       st->candidates_sampled = c[3];
       st->rounds = rounds;
       st->per_instance_placements = per_inst;
+      st->broad_phase_tests = c[4];
+      st->node_pair_tests = c[5];
+      st->accepted_candidates = c[6];
       std::vector<uint8_t> v(n);
       cuda_check(cudaMemcpy(v.data(), d_valid.p, n, cudaMemcpyDeviceToHost), "D2H valid");
       uint64_t nv = 0;
