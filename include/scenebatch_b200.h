@@ -72,6 +72,11 @@ sb_status sb_rest_z_offset(const double* vertices, uint32_t n_vertices, double* 
 sb_status sb_bvh_info(const double* vertices, uint32_t n_vertices, const uint32_t* triangles,
                       uint32_t n_triangles, int32_t info[4]);
 
+/* triangulate (polygon.cpp:344-368, hole-free ring) as PolygonSampler consumes it
+ * (zero-area triangles dropped, polygon.cpp:374-375): host-side region preparation. */
+sb_status sb_triangulate_ring(const double* ring_xy, uint32_t n, double* tris_out,
+                              uint32_t max_tris, uint32_t* n_tris);
+
 /* ------------------------------------------------------------------------------------
  * RNG: rng.hpp:9-67. Exposed for known-answer tests and for hosts that pre-draw.
  * ---------------------------------------------------------------------------------- */

@@ -98,6 +98,7 @@ SIGNATURES = {
     "sb_mesh_fingerprint": (C.c_int, [_D, C.c_uint32, _U32, C.c_uint32, C.POINTER(C.c_uint64)]),
     "sb_rest_z_offset": (C.c_int, [_D, C.c_uint32, _D]),
     "sb_bvh_info": (C.c_int, [_D, C.c_uint32, _U32, C.c_uint32, C.POINTER(C.c_int32)]),
+    "sb_triangulate_ring": (C.c_int, [_D, C.c_uint32, _D, C.c_uint32, _U32]),
     "sb_mix64": (C.c_uint64, [C.c_uint64]),
     "sb_stream_key": (C.c_uint64, [C.POINTER(C.c_uint64), C.c_uint32]),
     "sb_stream_doubles": (C.c_int, [C.c_uint64, C.POINTER(C.c_uint64), C.c_uint32, _D, C.c_uint32]),

@@ -22,6 +22,7 @@ namespace {
 constexpr int kB = kPlaceBlock;
 constexpr int kWarps = kB / 32;
 constexpr int32_t kFree = INT32_MAX;
+constexpr uint8_t kSlotVoid = 0, kSlotChecked = 1, kSlotUnplaceable = 2;
 
 enum Ctrl { kM = 0, kPairs = 1, kRounds = 2, kErr = 3, kCur = 4 };
 
@@ -53,8 +54,18 @@ __device__ __forceinline__ uint32_t* act_list(const PlaceParams& p, int which) {
   return which ? p.act1 : p.act0;
 }
 
+// Attempts evaluated per remaining instance this round (1 on the FIFO fast path).
+__device__ __forceinline__ int spec_width(const PlaceParams& p, uint64_t m, int32_t attempt) {
+  if (p.fast || m == 0) return 1;
+  uint64_t w = p.spec_budget / m;
+  const uint64_t cap = p.slot_cap / m;
+  if (w > cap) w = cap;
+  if (w > (uint64_t)(p.attempts - attempt)) w = (uint64_t)(p.attempts - attempt);
+  return w < 1 ? 1 : (int)w;
+}
+
 // ------------------------------------------------------------------ compaction
-// Stable compaction in chunks of kB slots: count pass, then (after a grid barrier) a
+// Stable compaction in chunks of kB entries: count pass, then (after a grid barrier) a
 // scatter pass that derives each chunk's output offset from the chunk counts.
 template <class Flag>
 __device__ void compact_count(const PlaceParams& p, uint64_t m, Flag flag) {
@@ -104,14 +115,18 @@ __device__ void compact_scatter(const PlaceParams& p, uint64_t m, Flag flag, Src
 }
 
 // ------------------------------------------------------------------ phase A
-// Warp per active slot: sample -> yaw -> compose -> candidate box / inverse -> broad phase.
+// Warp per virtual slot v = e * W + s (instance act[e], attempt `attempt + s`):
+// sample -> yaw -> compose -> candidate box / inverse -> broad phase -> pair queue.
 __device__ void phase_a(const PlaceParams& p, const SbGeom& gA, const uint32_t* act,
-                        uint64_t m, uint64_t draw_base, int32_t attempt, Local& L) {
+                        uint64_t m, int W, uint64_t draw_base, int32_t attempt, Local& L) {
   const int lane = threadIdx.x & 31;
   const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
   const SbPlacementDev& pl = p.pl;
   const WorldView& w = p.w;
-  for (uint64_t e = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); e < m; e += nwarps) {
+  const uint64_t nslots = m * (uint64_t)W;
+  for (uint64_t v = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); v < nslots; v += nwarps) {
+    const uint64_t e = v / W;
+    const int32_t at = attempt + (int32_t)(v - e * W);
     const uint32_t inst = act[e];
     const uint64_t gid = p.global_begin + inst;
     bool placeable = true;
@@ -131,17 +146,16 @@ __device__ void phase_a(const PlaceParams& p, const SbGeom& gA, const uint32_t* 
         placeable = false;
       } else {  // make_stream(run_seed, {salt, "fall", inst, attempt}) (sampler.cpp:117)
         Pcg r = Pcg::seeded(stream_seed4(p.run_seed, pl.salt, kFallbackSalt, gid,
-                                         static_cast<uint64_t>(attempt)));
+                                         static_cast<uint64_t>(at)));
         double u = r.next_double(), r1 = r.next_double(), r2 = r.next_double();
         const uint64_t off = (uint64_t)inst * p.inst_cap;
         sbp::draw_point(p.inst_tris + off, p.inst_cum + off, nt, u, r1, r2, lx, ly);
       }
     }
-    if (lane == 0) ++L.sampled;
     if (!placeable) {
       if (lane == 0) {
-        p.cflag[e] = 0;
-        p.contact[e] = kFree;
+        p.cflag[v] = kSlotUnplaceable;
+        p.contact[v] = kFree;
       }
       continue;
     }
@@ -153,7 +167,7 @@ __device__ void phase_a(const PlaceParams& p, const SbGeom& gA, const uint32_t* 
     double yaw = 0.0;
     if (pl.orientation == SB_ORIENT_UNIFORM_YAW) {  // sampler.cpp:140-141
       Pcg r = Pcg::seeded(
-          stream_seed4(p.run_seed, pl.salt, kYawSalt, gid, static_cast<uint64_t>(attempt)));
+          stream_seed4(p.run_seed, pl.salt, kYawSalt, gid, static_cast<uint64_t>(at)));
       const double two_pi = 2.0 * 3.14159265358979323846;
       yaw = 0.0 + (two_pi - 0.0) * r.next_double();
     } else if (pl.orientation == SB_ORIENT_FACE_TO) {  // relationships.cpp:232-239
@@ -187,13 +201,12 @@ __device__ void phase_a(const PlaceParams& p, const SbGeom& gA, const uint32_t* 
           pv = pose.m[k];
           iv = inv.m[k];
         }
-      p.cpose[e * 12 + lane] = pv;
-      p.cinv[e * 12 + lane] = iv;
+      p.cpose[v * 12 + lane] = pv;
+      p.cinv[v * 12 + lane] = iv;
     }
     if (lane == 0) {
-      ++L.checked;
-      p.cflag[e] = 1;
-      p.contact[e] = kFree;
+      p.cflag[v] = kSlotChecked;
+      p.contact[v] = kFree;
     }
     // broad phase (collision.cpp:439-443): lanes over objects, ascending chunks of 32
     for (int ob0 = 0; ob0 < w.n_objects; ob0 += 32) {
@@ -210,7 +223,7 @@ __device__ void phase_a(const PlaceParams& p, const SbGeom& gA, const uint32_t* 
       }
       const uint32_t mask = __ballot_sync(kFull, ov);
       if (lane == 0) {
-        p.ovmask[(uint64_t)(ob0 >> 5) * w.n + e] = mask;
+        p.ovmask[(uint64_t)(ob0 >> 5) * p.slot_cap + v] = mask;
         L.cnt.broad += __popc(bits);
       }
       if (mask) {
@@ -219,7 +232,7 @@ __device__ void phase_a(const PlaceParams& p, const SbGeom& gA, const uint32_t* 
         base = __shfl_sync(kFull, base, 0);
         if (ov) {
           const uint64_t idx = base + __popc(mask & ((1u << lane) - 1u));
-          if (idx < p.pair_cap) p.pairs[idx] = (e << 32) | (uint32_t)ob;
+          if (idx < p.pair_cap) p.pairs[idx] = (v << 32) | (uint32_t)ob;
           else atomicOr(p.ctrl + kErr, 1u);
         }
       }
@@ -228,7 +241,8 @@ __device__ void phase_a(const PlaceParams& p, const SbGeom& gA, const uint32_t* 
 }
 
 // ------------------------------------------------------------------ phase B
-__device__ void phase_b(const PlaceParams& p, Shared& sh, const uint32_t* act, Local& L) {
+__device__ void phase_b(const PlaceParams& p, Shared& sh, const uint32_t* act, int W,
+                        Local& L) {
   const int lane = threadIdx.x & 31;
   const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
   uint64_t np = __ldcg(p.ctrl + kPairs);
@@ -236,49 +250,55 @@ __device__ void phase_b(const PlaceParams& p, Shared& sh, const uint32_t* act, L
   WarpScratch& ws = sh.ws[threadIdx.x >> 5];
   for (uint64_t q = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); q < np; q += nwarps) {
     const uint64_t pr = p.pairs[q];
-    const uint64_t e = pr >> 32;
+    const uint64_t v = pr >> 32;
     const int32_t ob = (int32_t)(pr & 0xffffffffu);
-    const bool hit = warp_collide(p.w, sh.gc, ob, act[e], p.cinv + 12 * e, ws, L.cnt);
-    if (hit && lane == 0) atomicMin(p.contact + e, ob);
+    const bool hit = warp_collide(p.w, sh.gc, ob, act[v / W], p.cinv + 12 * v, ws, L.cnt);
+    if (hit && lane == 0) atomicMin(p.contact + v, ob);
     __syncwarp();
   }
 }
 
 // ------------------------------------------------------------------ phase C
-__device__ void phase_c(const PlaceParams& p, const uint32_t* act, uint64_t m, int32_t attempt,
-                        Local& L) {
+// Thread per remaining instance: first free attempt among its W slots is accepted
+// (update_transform + set_enabled, Appendix C.5); counters follow the sequential loop.
+__device__ void phase_c(const PlaceParams& p, const uint32_t* act, uint64_t m, int W,
+                        int32_t attempt, Local& L) {
   const WorldView& w = p.w;
   const int words = w.n_words;
   compact_count(p, m, [&](uint64_t e) -> int {
-    if (!p.cflag[e]) {
-      p.failflag[e] = 1;
-      return 1;
-    }
-    const int32_t c = __ldcg(p.contact + e);
-    // reference narrow count: overlapping objects tested up to the first hit
-    for (int wd = 0; wd < words; ++wd) {
-      uint32_t mk = p.ovmask[(uint64_t)wd * w.n + e];
-      if (c != kFree) {
-        const int lim = c - 32 * wd;  // keep objects <= c
-        if (lim < 0) mk = 0;
-        else if (lim < 31) mk &= (2u << lim) - 1u;
+    int32_t last = attempt;  // last attempt this instance made in the sequential loop
+    bool ok = false;
+    for (int s = 0; s < W && !ok; ++s) {
+      const uint64_t v = e * W + s;
+      last = attempt + s;
+      ++L.sampled;
+      if (p.cflag[v] != kSlotChecked) continue;  // placeable == 0 -> failed attempt
+      ++L.checked;
+      const int32_t c = __ldcg(p.contact + v);
+      for (int wd = 0; wd < words; ++wd) {  // narrow tests up to the first hit
+        uint32_t mk = p.ovmask[(uint64_t)wd * p.slot_cap + v];
+        if (c != kFree) {
+          const int lim = c - 32 * wd;  // keep objects <= c
+          if (lim < 0) mk = 0;
+          else if (lim < 31) mk &= (2u << lim) - 1u;
+        }
+        L.cnt.narrow += __popc(mk);
       }
-      L.cnt.narrow += __popc(mk);
-    }
-    if (c == kFree) {  // first-valid accept: update_transform + set_enabled (Appendix C.5)
-      const uint32_t inst = act[e];
-      M34 P;
+      if (c == kFree) {
+        const uint32_t inst = act[e];
+        M34 P;
 #pragma unroll
-      for (int k = 0; k < 12; ++k) P.m[k] = p.cpose[e * 12 + k];
-      store_pose(w, p.pl.object, inst, P);
-      w.enabled[(uint64_t)(p.pl.object >> 5) * w.n + inst] |= 1u << (p.pl.object & 31);
-      p.accepted[inst] = (int16_t)attempt;
-      ++L.accepted;
-      p.failflag[e] = 0;
-      return 0;
+        for (int k = 0; k < 12; ++k) P.m[k] = p.cpose[v * 12 + k];
+        store_pose(w, p.pl.object, inst, P);
+        w.enabled[(uint64_t)(p.pl.object >> 5) * w.n + inst] |= 1u << (p.pl.object & 31);
+        p.accepted[inst] = (int16_t)(attempt + s);
+        ++L.accepted;
+        ok = true;
+      }
     }
-    p.failflag[e] = 1;
-    return 1;
+    atomicMax(p.ctrl + kRounds, (uint32_t)(last + 1));  // reference round count
+    p.failflag[e] = ok ? 0 : 1;
+    return ok ? 0 : 1;
   });
   if (blockIdx.x == 0 && threadIdx.x == 0) p.ctrl[kPairs] = 0;  // phase B is done reading it
 }
@@ -304,22 +324,23 @@ __global__ void __launch_bounds__(kB) k_place(PlaceParams p) {
   grid.sync();
   uint64_t draws = 0;
   int cur = 0;
-  for (int32_t a = 0; a < p.attempts; ++a) {
+  for (int32_t a = 0; a < p.attempts;) {
     const uint64_t m = __ldcg(p.ctrl + kM);
     if (m == 0) break;
-    if (blockIdx.x == 0 && threadIdx.x == 0) p.ctrl[kRounds] += 1;
+    const int W = spec_width(p, m, a);
     const uint32_t* act = act_list(p, cur);
-    phase_a(p, gA, act, m, draws, a, L);
+    phase_a(p, gA, act, m, W, draws, a, L);
     grid.sync();
-    phase_b(p, sh, act, L);
+    phase_b(p, sh, act, W, L);
     grid.sync();
-    phase_c(p, act, m, a, L);
+    phase_c(p, act, m, W, a, L);
     grid.sync();
     compact_scatter(p, m, [&](uint64_t e) -> int { return p.failflag[e]; },
                     [&](uint64_t e) -> uint32_t { return act[e]; }, act_list(p, cur ^ 1));
     grid.sync();
     if (p.fast) draws += m;
     cur ^= 1;
+    a += W;
   }
   const uint64_t m = __ldcg(p.ctrl + kM);
   const uint32_t* act = act_list(p, cur);
@@ -339,9 +360,9 @@ __global__ void __launch_bounds__(kB) k_init_scatter(PlaceParams p) {
 }
 __global__ void __launch_bounds__(kB) k_phase_a(PlaceParams p, int32_t attempt, int cur) {
   SbGeom gA = p.w.geoms[p.pl.geom];
-  Local L;
   const uint64_t m = __ldcg(p.ctrl + kM);
-  phase_a(p, gA, act_list(p, cur), m, p.draw_base, attempt, L);
+  Local L;
+  phase_a(p, gA, act_list(p, cur), m, p.spec_width, p.draw_base, attempt, L);
   flush(p, L);
 }
 __global__ void __launch_bounds__(kB) k_phase_b(PlaceParams p, int cur) {
@@ -349,13 +370,13 @@ __global__ void __launch_bounds__(kB) k_phase_b(PlaceParams p, int cur) {
   SbGeom gA;
   block_setup(p, sh, gA);
   Local L;
-  phase_b(p, sh, act_list(p, cur), L);
+  phase_b(p, sh, act_list(p, cur), p.spec_width, L);
   flush(p, L);
 }
 __global__ void __launch_bounds__(kB) k_phase_c(PlaceParams p, int32_t attempt, int cur) {
   Local L;
   const uint64_t m = __ldcg(p.ctrl + kM);
-  phase_c(p, act_list(p, cur), m, attempt, L);
+  phase_c(p, act_list(p, cur), m, p.spec_width, attempt, L);
   flush(p, L);
 }
 __global__ void __launch_bounds__(kB) k_phase_d(PlaceParams p, int cur) {
@@ -377,7 +398,7 @@ void check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-unsigned host_grid(const PlaceParams&) {
+unsigned host_grid() {
   static unsigned g = 0;
   if (g == 0) {
     int dev = 0, sms = 0, per = 0;
@@ -391,13 +412,17 @@ unsigned host_grid(const PlaceParams&) {
 
 }  // namespace
 
-bool place_persistent(const PlaceParams& p, int num_sms, sb_stream_t s) {
+int place_grid_warps(int num_sms) {
   if (g_coop_blocks < 0) {
     int per = 0;
     check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_place, kB, 0), "occupancy");
     g_coop_blocks = per * num_sms;
   }
-  if (g_coop_blocks <= 0) return false;
+  return g_coop_blocks * kWarps;
+}
+
+bool place_persistent(const PlaceParams& p, int num_sms, sb_stream_t s) {
+  if (place_grid_warps(num_sms) <= 0) return false;
   unsigned grid = (unsigned)g_coop_blocks;
   PlaceParams q = p;
   void* args[] = {&q};
@@ -408,14 +433,14 @@ bool place_persistent(const PlaceParams& p, int num_sms, sb_stream_t s) {
 }
 
 void place_init(const PlaceParams& p, sb_stream_t s) {
-  unsigned g = host_grid(p);
+  unsigned g = host_grid();
   k_init_count<<<g, kB, 0, s>>>(p);
   k_init_scatter<<<g, kB, 0, s>>>(p);
   check(cudaGetLastError(), "place_init");
 }
 
 void place_round(const PlaceParams& p, int32_t attempt, int cur, sb_stream_t s) {
-  unsigned g = host_grid(p);
+  unsigned g = host_grid();
   k_phase_a<<<g, kB, 0, s>>>(p, attempt, cur);
   k_phase_b<<<g, kB, 0, s>>>(p, cur);
   k_phase_c<<<g, kB, 0, s>>>(p, attempt, cur);
@@ -424,7 +449,7 @@ void place_round(const PlaceParams& p, int32_t attempt, int cur, sb_stream_t s) 
 }
 
 void place_finish(const PlaceParams& p, int cur, sb_stream_t s) {
-  k_finish<<<host_grid(p), kB, 0, s>>>(p, cur);
+  k_finish<<<host_grid(), kB, 0, s>>>(p, cur);
   check(cudaGetLastError(), "place_finish");
 }
 

@@ -9,6 +9,12 @@
 //   C  thread per slot: first-valid accept (update_transform + set_enabled) or fail flag;
 //      reference-equivalent narrow-phase count; per-chunk failure counts
 //   D  stable compaction of the failing slots into the next round's active list
+// Per-instance (counter-stream) regions: attempt a of instance i depends only on
+// make_stream(run_seed, {salt, tag, i, a}) and on instance i's world, which is unchanged
+// until i accepts. A round may therefore evaluate W consecutive attempts of every remaining
+// instance at once ("virtual slots") and accept the lowest free one -- the sequential
+// first-valid result; counters are reported as the sequential loop would have counted
+// them. The FIFO fast path couples instances through the draw index, so W = 1 there.
 // Every (candidate, object) pair of a round is evaluated in parallel; contact_object is the
 // minimum colliding object id, i.e. the reference's first hit in ascending order
 // (collision.cpp:439-448). Single GPU: one cooperative kernel loops over all rounds with
@@ -55,6 +61,9 @@ struct PlaceParams {
   uint32_t* ctrl;               // [0] M, [1] pair count, [2] rounds, [3] error, [4] cur list
   unsigned long long* counters; // [8]
   uint64_t draw_base;           // sharded host loop: this rank's first draw index
+  uint64_t slot_cap;            // capacity of the per-slot candidate arrays
+  uint64_t spec_budget;         // target candidates per round for speculative attempts
+  int32_t spec_width;           // host loop: attempts per instance this round (1 = none)
 };
 
 constexpr int kPlaceBlock = 256;
@@ -62,6 +71,8 @@ constexpr int kPlaceBlock = 256;
 // Single GPU: whole placement in one cooperative launch. Returns false if the device
 // cannot co-schedule the grid (caller falls back to the host loop).
 bool place_persistent(const PlaceParams& p, int num_sms, sb_stream_t s);
+// Warps of the co-resident persistent grid (sizes the speculative-attempt budget).
+int place_grid_warps(int num_sms);
 // Host loop building blocks (sharded runs): init active list, then per round
 // phase_abcd(draw_base) with the count read back in between.
 void place_init(const PlaceParams& p, sb_stream_t s);

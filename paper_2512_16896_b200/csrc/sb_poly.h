@@ -223,6 +223,27 @@ SB_HD bool ear_clip_into(Ring& r, TableSink& sink) {
     else break;
   }
   if (n < 3) return true;
+  // Fast path, exact: when no vertex is reflex and every ear the loop would clip passes
+  // the sliver test, ear_clip_ring's sequence is cur = 0, 1, 2, ... with prev pinned at
+  // vertex n-1, i.e. the fan (n-1, k, k+1) for k = 0..n-3 (the last one emitted by the
+  // `remaining == 3` tail). Convex clipped sectors always take this path.
+  {
+    bool fan = true;
+    for (int i = 0; i < n && fan; ++i) {
+      const int a = (i + n - 1) % n, c = (i + 1) % n;
+      if (cross2(r.x[a], r.y[a], r.x[i], r.y[i], r.x[c], r.y[c]) < 0.0) fan = false;
+    }
+    for (int k = 0; k + 3 < n && fan; ++k) {
+      const double cr = cross2(r.x[n - 1], r.y[n - 1], r.x[k], r.y[k], r.x[k + 1], r.y[k + 1]);
+      if (cr < 0.0 || fabs(cr) < 1e-18) fan = false;
+    }
+    if (fan) {
+      for (int k = 0; k + 2 < n; ++k)
+        if (!sink_tri(sink, r.x[n - 1], r.y[n - 1], r.x[k], r.y[k], r.x[k + 1], r.y[k + 1]))
+          return false;
+      return true;
+    }
+  }
   int prv[kCap], nxt[kCap];
   bool reflex[kCap];
   for (int i = 0; i < n; ++i) {

@@ -415,6 +415,7 @@ struct sb_engine {
   DevArray<uint32_t> d_chunk;
   DevArray<uint32_t> d_ctrl;
   int num_sms = 0;
+  uint64_t spec_budget = 0, slot_cap = 0;
   bool legacy_rounds = false;
   DevArray<uint64_t> d_count;
   DevArray<uint8_t> d_temp;
@@ -592,19 +593,21 @@ struct sb_engine {
     d_act[0].alloc(n);
     d_act[1].alloc(n);
     d_fail.alloc(n);
-    d_cpose.alloc(12 * n);
-    d_cinv.alloc(12 * n);
-    d_cflag.alloc(n);
-    d_contact.alloc(n);
+    cuda_check(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, world->device), "attr");
+    spec_budget = 2ull * static_cast<uint64_t>(sbk::place_grid_warps(num_sms));
+    slot_cap = std::max<uint64_t>(n, spec_budget);
+    d_cpose.alloc(12 * slot_cap);
+    d_cinv.alloc(12 * slot_cap);
+    d_cflag.alloc(slot_cap);
+    d_contact.alloc(slot_cap);
     {
       const size_t words = (world->obj_geom.size() + 31) / 32;
-      d_ovmask.alloc(std::max<size_t>(1, words) * n);
+      d_ovmask.alloc(std::max<size_t>(1, words) * slot_cap);
       const size_t per = std::min<size_t>(world->obj_geom.size(), 32);
-      d_pairs.alloc(std::max<size_t>(1, per) * n);
+      d_pairs.alloc(std::max<size_t>(1, per) * slot_cap);
     }
     d_chunk.alloc(n / 256 + 2);
     d_ctrl.alloc(8);
-    cuda_check(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, world->device), "attr");
     {
       const char* mode = std::getenv("SB_ENGINE");
       legacy_rounds = mode && std::string(mode) == "legacy";
@@ -823,6 +826,9 @@ struct sb_engine {
       pp.chunk_cnt = d_chunk.p;
       pp.ctrl = d_ctrl.p;
       pp.counters = d_counters.p;
+      pp.slot_cap = slot_cap;
+      pp.spec_budget = spec_budget;
+      pp.spec_width = 1;
       cuda_check(cudaMemsetAsync(d_ctrl.p, 0, d_ctrl.count * sizeof(uint32_t), stream), "memset ctrl");
       uint32_t ctrl[8];
       if (world_size == 1) {
@@ -1038,6 +1044,21 @@ sb_status sb_bvh_info(const double* v, uint32_t nv, const uint32_t* t, uint32_t 
     info[1] = b.full_depth;
     info[2] = static_cast<int32_t>(b.nodes.size());
     info[3] = b.reachable_tris;
+  });
+}
+
+sb_status sb_triangulate_ring(const double* ring_xy, uint32_t n, double* tris_out,
+                              uint32_t max_tris, uint32_t* n_tris) {
+  return guard([&] {
+    std::vector<sbh::V2> ring(n);
+    for (uint32_t i = 0; i < n; ++i) ring[i] = {ring_xy[2 * i], ring_xy[2 * i + 1]};
+    auto t = sbh::triangulate_ring(ring);
+    *n_tris = static_cast<uint32_t>(t.size());
+    for (size_t i = 0; i < t.size() && i < max_tris; ++i)
+      for (int k = 0; k < 3; ++k) {
+        tris_out[6 * i + 2 * k] = t[i][k][0];
+        tris_out[6 * i + 2 * k + 1] = t[i][k][1];
+      }
   });
 }
 

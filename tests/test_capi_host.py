@@ -93,3 +93,45 @@ def test_effective_bvh_reachable_sets():
 def test_rest_offset():
     m = pkg.make_box(0.2, 0.2, 0.3)
     assert m.rest_z_offset() == 0.15 + 1e-3
+
+
+def _product_triangulate(ring):
+    import ctypes as C
+
+    r = np.ascontiguousarray(ring, np.float64).reshape(-1, 2)
+    out = np.zeros((256, 6))
+    nt = C.c_uint32()
+    A.check(pkg.lib().sb_triangulate_ring(r.ctypes.data_as(C.POINTER(C.c_double)), len(r),
+                                          out.ctypes.data_as(C.POINTER(C.c_double)), 256,
+                                          C.byref(nt)))
+    return out[: nt.value].reshape(-1, 3, 2)
+
+
+def _area2(t):
+    return (t[:, 1, 0] - t[:, 0, 0]) * (t[:, 2, 1] - t[:, 0, 1]) - \
+        (t[:, 1, 1] - t[:, 0, 1]) * (t[:, 2, 0] - t[:, 0, 0])
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_triangulation_matches_reference(ref, seed):
+    """Ear clipping (polygon.cpp:260-340): the exact fan fast path for convex rings and the
+    general path for star-shaped (reflex) rings reproduce the reference triangle by
+    triangle, in order."""
+    rng = np.random.default_rng(seed)
+    rings = []
+    for _ in range(40):
+        n = int(rng.integers(3, 40))
+        ang = np.sort(rng.uniform(0, 2 * np.pi, n))
+        convex = rng.random() < 0.5
+        rad = np.ones(n) if convex else rng.uniform(0.3, 1.0, n)
+        ring = np.stack([rad * np.cos(ang), rad * np.sin(ang)], 1) * rng.uniform(0.05, 2.0)
+        ring += rng.uniform(-1, 1, 2)
+        if rng.random() < 0.3:
+            ring = ring[::-1]  # clockwise input: triangulate reverses it
+        rings.append(ring)
+    rings.append(np.array([[0, 0], [1, 0], [1, 1], [0, 1]], float))
+    for ring in rings:
+        want = ref.triangulate(ring)
+        want = want[np.abs(_area2(want)) > 0]
+        got = _product_triangulate(ring)
+        assert np.array_equal(got, want)
