@@ -177,6 +177,7 @@ def run_ours(args, rank, world, local_rank):
     clocks = ClockSampler(device)
     clocks.start()
     step_ms, check_ms, check_launches, launches = [], [], [], []
+    phases = {}
     agg = {}
     for _ in range(args.steps):
         flush.zero_()
@@ -188,6 +189,8 @@ def run_ours(args, rank, world, local_rank):
         check_ms.append(chk)
         check_launches.append(nchk)
         launches.append(eng.last_launches())
+        for k, v in eng.phase_profile().items():
+            phases[k] = phases.get(k, 0.0) + v / args.steps
         for k, v in r.stats.items():
             agg[k] = agg.get(k, 0) + v
     # end-to-end: same call, results D2H into pinned host memory, wall clock
@@ -271,6 +274,7 @@ def run_ours(args, rank, world, local_rank):
                 "d2h_bytes_per_step": int(d2h),
                 "path": "sb_engine_generate with pinned host sb_result (accepted, valid, poses)"},
         "gpu_launches": round(statistics.mean(launches)) * K,
+        "phase_profile_per_step": {k: round(v, 4) for k, v in phases.items()},
         "clocks": clk,
     }
     if not args.no_cpu_baseline:

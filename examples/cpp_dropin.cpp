@@ -1,0 +1,35 @@
+// Minimal C++ client of the drop-in: the reference's CollisionWorld call sequence
+// (collision.hpp:76-127) against libscenebatch_b200.so. Build:
+//   g++ -std=c++20 -Iinclude examples/cpp_dropin.cpp -Lpaper_2512_16896_b200
+//       -lscenebatch_b200 -Wl,-rpath,$PWD/paper_2512_16896_b200 -o cpp_dropin
+// Prints the box fingerprint; with a GPU also runs SPEC.md:394-395's unit-cube checks.
+#include <cstdio>
+#include <vector>
+
+#include "scenebatch_b200.hpp"
+
+using namespace scenebatch_b200;
+
+int main() {
+  TriMesh box = make_box(1, 1, 1);
+  std::printf("box: %u vertices, %u triangles, fingerprint %016llx\n", box.n_vertices(),
+              box.n_triangles(), (unsigned long long)mesh_fingerprint(box));
+  try {
+    CollisionWorld world(4);
+    int g = world.register_geometry(box);
+    int o = world.add_object("cube", g);
+    world.set_enabled_all(o, true);
+    std::vector<Pose> cand(4);
+    const double offs[4] = {0.5, 0.9, 2.0, -0.5};
+    for (int i = 0; i < 4; ++i) {
+      cand[i] = {1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0, offs[i], 0, 0, 1};
+    }
+    std::vector<uint32_t> active = {0, 1, 2, 3};
+    CollisionMask m = world.check_batch(g, cand, active);
+    std::printf("free: %d %d %d %d\n", m.free[0], m.free[1], m.free[2], m.free[3]);
+    return (m.free[0] == 0 && m.free[1] == 0 && m.free[2] == 1 && m.free[3] == 0) ? 0 : 1;
+  } catch (const cuda_error& e) {
+    std::printf("no device: %s\n", e.what());
+    return 2;
+  }
+}

@@ -255,6 +255,12 @@ uint64_t sb_engine_last_launches(const sb_engine* e);
  * its check kernels alone (the dominant kernel; roofline numerator). */
 sb_status sb_engine_last_timing(const sb_engine* e, double* total_ms, double* check_ms,
                                 uint64_t* check_launches);
+/* Breakdown of the last generate call: out[0..4] = ms spent (device globaltimer, block 0)
+ * in the placement kernel's init / broad (A) / narrow (B) / accept (C) / compaction (D)
+ * phases summed over placements, out[5] = persistent rounds executed, out[6] = ms in
+ * relation-region preparation (anchor states, variation test, region build), out[7] =
+ * total ms (CUDA events). */
+sb_status sb_engine_phase_profile(const sb_engine* e, double out[8]);
 
 #ifdef __cplusplus
 }

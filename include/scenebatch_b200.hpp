@@ -1,0 +1,193 @@
+// scenebatch_b200.hpp -- the reference's C++ class API on top of the C ABI.
+//
+// Drop-in shape of /root/reference/proj/include/scenebatch/{collision,trimesh}.hpp plus
+// the generation engine the reference specifies but does not ship.
+// Header-only; link libscenebatch_b200.so. Errors are rethrown as the reference's
+// exception types (std::invalid_argument, std::out_of_range, std::logic_error,
+// std::runtime_error; CUDA failures as scenebatch_b200::cuda_error).
+//
+// Poses are column-major double[16] (Eigen::Matrix4d memory), so a reference
+// TransformBatch's data can be passed as `const double*` directly.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "scenebatch_b200.h"
+
+namespace scenebatch_b200 {
+
+struct cuda_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void check(sb_status s) {
+  if (s == SB_OK) return;
+  std::string msg = sb_last_error();
+  switch (s) {
+    case SB_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+    case SB_ERR_OUT_OF_RANGE: throw std::out_of_range(msg);
+    case SB_ERR_LOGIC: throw std::logic_error(msg);
+    case SB_ERR_CUDA: throw cuda_error(msg);
+    default: throw std::runtime_error(msg);
+  }
+}
+
+using Pose = std::array<double, 16>;  // column-major, like Eigen::Matrix4d::data()
+
+// TriMesh (trimesh.hpp:12-22), flat storage.
+struct TriMesh {
+  std::vector<double> vertices;    // xyz triples
+  std::vector<uint32_t> triangles; // index triples
+  uint32_t n_vertices() const { return static_cast<uint32_t>(vertices.size() / 3); }
+  uint32_t n_triangles() const { return static_cast<uint32_t>(triangles.size() / 3); }
+};
+
+namespace detail {
+template <class F, class... A>
+TriMesh make(F f, A... a) {
+  uint32_t nv = 0, nt = 0;
+  check(f(a..., nullptr, &nv, nullptr, &nt));
+  TriMesh m;
+  m.vertices.resize(3 * nv);
+  m.triangles.resize(3 * nt);
+  check(f(a..., m.vertices.data(), &nv, m.triangles.data(), &nt));
+  return m;
+}
+}  // namespace detail
+
+// trimesh.hpp:27-32
+inline TriMesh make_box(double sx, double sy, double sz) {
+  return detail::make(sb_make_box, sx, sy, sz);
+}
+inline TriMesh make_cylinder(double radius, double height, int segments = 32) {
+  return detail::make(sb_make_cylinder, radius, height, segments);
+}
+inline TriMesh make_sphere(double radius, int stacks = 12, int slices = 16) {
+  return detail::make(sb_make_sphere, radius, stacks, slices);
+}
+// trimesh.hpp:35
+inline TriMesh transformed(const TriMesh& m, const Pose& pose) {
+  TriMesh out = m;
+  check(sb_transform_vertices(pose.data(), out.vertices.data(), out.n_vertices()));
+  return out;
+}
+// trimesh.hpp:38
+inline uint64_t mesh_fingerprint(const TriMesh& m) {
+  uint64_t fp = 0;
+  check(sb_mesh_fingerprint(m.vertices.data(), m.n_vertices(), m.triangles.data(),
+                            m.n_triangles(), &fp));
+  return fp;
+}
+
+// CollisionMask / CollisionStats (collision.hpp:60-72)
+struct CollisionMask {
+  std::vector<uint8_t> free;
+  std::vector<int32_t> contact_object;
+};
+using CollisionStats = sb_stats;
+
+// CollisionWorld (collision.hpp:76-127), state resident on one B200.
+class CollisionWorld {
+ public:
+  explicit CollisionWorld(std::size_t batch_size, double margin = 0.0, int device = 0)
+      : n_(batch_size) {
+    check(sb_world_create(batch_size, margin, device, &w_));
+  }
+  ~CollisionWorld() {
+    if (owned_) sb_world_destroy(w_);
+  }
+  CollisionWorld(const CollisionWorld&) = delete;
+  CollisionWorld& operator=(const CollisionWorld&) = delete;
+
+  std::size_t batch_size() const { return n_; }
+  int register_geometry(const TriMesh& mesh) {
+    int32_t id = -1;
+    check(sb_register_geometry(w_, mesh.vertices.data(), mesh.n_vertices(),
+                               mesh.triangles.data(), mesh.n_triangles(), &id));
+    return id;
+  }
+  int add_object(const std::string& name, int geom_id) {
+    int32_t id = -1;
+    check(sb_add_object(w_, name.c_str(), geom_id, &id));
+    return id;
+  }
+  bool enabled(int object, std::size_t instance) const {
+    int e = 0;
+    check(sb_enabled(w_, object, instance, &e));
+    return e != 0;
+  }
+  void set_enabled(int object, std::span<const uint32_t> instances, bool enabled) {
+    check(sb_set_enabled(w_, object, instances.data(), instances.size(), enabled ? 1 : 0));
+  }
+  void set_enabled_all(int object, bool enabled) {
+    check(sb_set_enabled_all(w_, object, enabled ? 1 : 0));
+  }
+  // poses: N column-major Mat4 (TransformBatch::data memory)
+  void update_transforms(int object, const double* poses_colmajor16xN) {
+    check(sb_update_transforms(w_, object, poses_colmajor16xN));
+  }
+  void update_transform(int object, std::size_t instance, const Pose& pose) {
+    check(sb_update_transform(w_, object, instance, pose.data()));
+  }
+  Pose object_pose(int object, std::size_t instance) const {
+    Pose p{};
+    check(sb_object_pose(w_, object, instance, p.data()));
+    return p;
+  }
+  CollisionMask check_batch(int geom_id, std::span<const Pose> poses,
+                            std::span<const uint32_t> active) {
+    if (poses.size() != active.size())
+      throw std::invalid_argument("check_batch: poses/active size mismatch");
+    CollisionMask m;
+    m.free.assign(n_, 1);
+    m.contact_object.assign(n_, -1);
+    check(sb_check_batch(w_, geom_id, poses.empty() ? nullptr : poses[0].data(), active.data(),
+                         active.size(), m.free.data(), m.contact_object.data()));
+    return m;
+  }
+  CollisionStats stats() const {
+    sb_stats s{};
+    check(sb_get_stats(w_, &s));
+    return s;
+  }
+  void reset_stats() { check(sb_reset_stats(w_)); }
+  sb_world* handle() const { return w_; }
+
+ private:
+  friend class Engine;
+  CollisionWorld(sb_world* w, std::size_t n) : w_(w), n_(n), owned_(false) {}
+  sb_world* w_ = nullptr;
+  std::size_t n_ = 0;
+  bool owned_ = true;
+};
+
+// The reference's engine (initialize / generate) for one shard.
+class Engine {
+ public:
+  Engine(const sb_scene& scene, const sb_shard* shard = nullptr, int device = 0) {
+    check(sb_engine_create(&scene, shard, device, &e_));
+  }
+  ~Engine() { sb_engine_destroy(e_); }
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
+
+  std::size_t local_instances() const { return sb_engine_local_instances(e_); }
+  // One full generation; fills `out` (any member may be null) and returns the stats.
+  sb_run_stats generate(uint64_t run_seed, sb_result* out = nullptr) {
+    sb_run_stats st{};
+    check(sb_engine_generate(e_, run_seed, out, &st));
+    return st;
+  }
+  void download(sb_result& out) { check(sb_engine_download(e_, &out)); }
+  CollisionWorld world() { return CollisionWorld(sb_engine_world(e_), local_instances()); }
+
+ private:
+  sb_engine* e_ = nullptr;
+};
+
+}  // namespace scenebatch_b200

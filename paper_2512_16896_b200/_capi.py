@@ -124,6 +124,7 @@ SIGNATURES = {
     "sb_engine_local_instances": (C.c_uint64, [_P]),
     "sb_engine_last_launches": (C.c_uint64, [_P]),
     "sb_engine_last_timing": (C.c_int, [_P, _D, _D, C.POINTER(C.c_uint64)]),
+    "sb_engine_phase_profile": (C.c_int, [_P, _D]),
 }
 
 _lib = None

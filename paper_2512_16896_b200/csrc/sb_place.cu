@@ -54,9 +54,33 @@ __device__ __forceinline__ uint32_t* act_list(const PlaceParams& p, int which) {
   return which ? p.act1 : p.act0;
 }
 
+// Sampling source of the placement, resolved on the device when the host left the
+// fast-path/per-instance decision to the variation flag.
+struct Sampling {
+  int fast;
+  const SbRegionTri* tris;
+  const double* cum;
+  int n;
+};
+
+__device__ __forceinline__ Sampling resolve_sampling(const PlaceParams& p) {
+  Sampling s{p.fast, p.canon_tris, p.canon_cum, p.canon_n};
+  if (p.vary_flag) {
+    const bool vary = __ldcg(p.vary_flag) != 0;
+    s.fast = vary ? 0 : 1;
+    if (!vary) {
+      s.tris = p.inst_tris;
+      s.cum = p.inst_cum;
+      s.n = __ldcg(p.inst_n);
+    }
+  }
+  return s;
+}
+
 // Attempts evaluated per remaining instance this round (1 on the FIFO fast path).
-__device__ __forceinline__ int spec_width(const PlaceParams& p, uint64_t m, int32_t attempt) {
-  if (p.fast || m == 0) return 1;
+__device__ __forceinline__ int spec_width(const PlaceParams& p, int fast, uint64_t m,
+                                          int32_t attempt) {
+  if (fast || m == 0) return 1;
   uint64_t w = p.spec_budget / m;
   const uint64_t cap = p.slot_cap / m;
   if (w > cap) w = cap;
@@ -117,8 +141,9 @@ __device__ void compact_scatter(const PlaceParams& p, uint64_t m, Flag flag, Src
 // ------------------------------------------------------------------ phase A
 // Warp per virtual slot v = e * W + s (instance act[e], attempt `attempt + s`):
 // sample -> yaw -> compose -> candidate box / inverse -> broad phase -> pair queue.
-__device__ void phase_a(const PlaceParams& p, const SbGeom& gA, const uint32_t* act,
-                        uint64_t m, int W, uint64_t draw_base, int32_t attempt, Local& L) {
+__device__ void phase_a(const PlaceParams& p, const Sampling& S, const SbGeom& gA,
+                        const uint32_t* act, uint64_t m, int W, uint64_t draw_base,
+                        int32_t attempt, Local& L) {
   const int lane = threadIdx.x & 31;
   const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
   const SbPlacementDev& pl = p.pl;
@@ -131,14 +156,14 @@ __device__ void phase_a(const PlaceParams& p, const SbGeom& gA, const uint32_t* 
     const uint64_t gid = p.global_begin + inst;
     bool placeable = true;
     double lx = 0.0, ly = 0.0;
-    if (p.fast) {
-      if (p.canon_n == 0) {
+    if (S.fast) {
+      if (S.n == 0) {
         placeable = false;
       } else {
         Pcg r{p.fast_state0};
         r.advance(6ull * (draw_base + e));  // j-th drained point = j-th draw (sampler.cpp:30-43)
         double u = r.next_double(), r1 = r.next_double(), r2 = r.next_double();
-        sbp::draw_point(p.canon_tris, p.canon_cum, p.canon_n, u, r1, r2, lx, ly);
+        sbp::draw_point(S.tris, S.cum, S.n, u, r1, r2, lx, ly);
       }
     } else {
       const int nt = p.inst_n[inst];
@@ -310,9 +335,33 @@ __device__ __forceinline__ void block_setup(const PlaceParams& p, Shared& sh, Sb
   __syncthreads();
 }
 
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Phase timer: block 0 / thread 0 accumulates wall time between grid barriers into
+// p.prof[slot] (ns): 0 init, 1 A, 2 B, 3 C, 4 D; prof[5] counts rounds.
+struct PhaseClock {
+  uint64_t* prof;
+  uint64_t t;
+  __device__ PhaseClock(uint64_t* pr) : prof(pr), t(0) {
+    if (prof && blockIdx.x == 0 && threadIdx.x == 0) t = global_ns();
+  }
+  __device__ void lap(int slot) {
+    if (prof && blockIdx.x == 0 && threadIdx.x == 0) {
+      uint64_t now = global_ns();
+      prof[slot] += now - t;
+      t = now;
+    }
+  }
+};
+
 __global__ void __launch_bounds__(kB) k_place(PlaceParams p) {
   __shared__ Shared sh;
   cg::grid_group grid = cg::this_grid();
+  PhaseClock clk(p.prof);
   SbGeom gA;
   block_setup(p, sh, gA);
   Local L;
@@ -322,23 +371,32 @@ __global__ void __launch_bounds__(kB) k_place(PlaceParams p) {
   compact_scatter(p, n, [&](uint64_t i) -> int { return p.valid[i] != 0; },
                   [&](uint64_t i) -> uint32_t { return (uint32_t)i; }, p.act0);
   grid.sync();
+  clk.lap(0);
+  const Sampling S = resolve_sampling(p);
+  if (p.vary_flag && !S.fast && blockIdx.x == 0 && threadIdx.x == 0)
+    atomicAdd(p.counters + 7, 1ull);  // per-instance placement
   uint64_t draws = 0;
   int cur = 0;
   for (int32_t a = 0; a < p.attempts;) {
     const uint64_t m = __ldcg(p.ctrl + kM);
     if (m == 0) break;
-    const int W = spec_width(p, m, a);
+    const int W = spec_width(p, S.fast, m, a);
     const uint32_t* act = act_list(p, cur);
-    phase_a(p, gA, act, m, W, draws, a, L);
+    phase_a(p, S, gA, act, m, W, draws, a, L);
     grid.sync();
+    clk.lap(1);
     phase_b(p, sh, act, W, L);
     grid.sync();
+    clk.lap(2);
     phase_c(p, act, m, W, a, L);
     grid.sync();
+    clk.lap(3);
     compact_scatter(p, m, [&](uint64_t e) -> int { return p.failflag[e]; },
                     [&](uint64_t e) -> uint32_t { return act[e]; }, act_list(p, cur ^ 1));
     grid.sync();
-    if (p.fast) draws += m;
+    clk.lap(4);
+    if (p.prof && blockIdx.x == 0 && threadIdx.x == 0) p.prof[5] += 1;
+    if (S.fast) draws += m;
     cur ^= 1;
     a += W;
   }
@@ -362,7 +420,8 @@ __global__ void __launch_bounds__(kB) k_phase_a(PlaceParams p, int32_t attempt, 
   SbGeom gA = p.w.geoms[p.pl.geom];
   const uint64_t m = __ldcg(p.ctrl + kM);
   Local L;
-  phase_a(p, gA, act_list(p, cur), m, p.spec_width, p.draw_base, attempt, L);
+  const Sampling S = resolve_sampling(p);
+  phase_a(p, S, gA, act_list(p, cur), m, p.spec_width, p.draw_base, attempt, L);
   flush(p, L);
 }
 __global__ void __launch_bounds__(kB) k_phase_b(PlaceParams p, int cur) {

@@ -64,6 +64,11 @@ struct PlaceParams {
   uint64_t slot_cap;            // capacity of the per-slot candidate arrays
   uint64_t spec_budget;         // target candidates per round for speculative attempts
   int32_t spec_width;           // host loop: attempts per instance this round (1 = none)
+  uint64_t* prof;               // optional phase timers (ns) [init, A, B, C, D, rounds]
+  // Relation placements on one GPU: the path is chosen on the device. When non-null,
+  // *vary_flag != 0 selects the per-instance tables, else the FIFO fast path samples the
+  // canonical region_for(0) = local instance 0's table (relationships.cpp:188-190).
+  const int32_t* vary_flag;
 };
 
 constexpr int kPlaceBlock = 256;

@@ -1,0 +1,412 @@
+// Warp-cooperative per-instance constraint regions (relationships.cpp:161-218 with
+// polygon.cpp:136-176 annulus_sector, the rect-clip stand-in for Boost intersect, and
+// polygon.cpp:260-388 triangulate + PolygonSampler), one warp per instance, all on device.
+//
+// Lanes compute the arc points, the Sutherland-Hodgman passes (prefix-sum compaction
+// preserves the sequential output order) and the fan triangles in parallel; every step
+// whose rounding depends on evaluation order (ring areas, the tolerance-based duplicate
+// drop, the cumulative-area table) runs on lane 0 in the reference's order, so tables are
+// bit-identical to sbp::* (the single-thread restatement) and to the reference.
+#include <stdexcept>
+#include <string>
+
+#include "../../include/scenebatch_b200.h"
+#include "sb_dev.cuh"
+#include "sb_poly.h"
+#include "sb_region.h"
+
+using namespace sbd;
+
+namespace sbk {
+namespace {
+
+constexpr int kRB = 128;            // threads per block
+constexpr int kRW = kRB / 32;       // warps per block
+constexpr int kCap = sbp::kCap;
+constexpr unsigned kFull = 0xffffffffu;
+
+struct RegionScratch {
+  double x[2][kCap], y[2][kCap];
+  double area[kCap];
+};
+
+__device__ __forceinline__ double ring_area_seq(const double* x, const double* y, int n) {
+  double s = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const int j = (i + 1) % n;
+    s += x[i] * y[j] - x[j] * y[i];
+  }
+  return 0.5 * s;
+}
+
+// One Sutherland-Hodgman pass (same arithmetic and output order as sbp::clip_half);
+// returns the output size, or -1 on overflow.
+__device__ int warp_clip(const double* ix, const double* iy, int n, double* ox, double* oy,
+                         int axis, double bound, bool keep_ge) {
+  const int lane = threadIdx.x & 31;
+  int base = 0;
+  for (int i0 = 0; i0 < n; i0 += 32) {
+    const int i = i0 + lane;
+    int cnt = 0;
+    bool ci = false, pi = false;
+    double cx = 0, cy = 0, qx = 0, qy = 0;
+    if (i < n) {
+      const int ip = (i + n - 1) % n;
+      const double cur_a = axis == 0 ? ix[i] : iy[i];
+      const double prv_a = axis == 0 ? ix[ip] : iy[ip];
+      ci = keep_ge ? cur_a >= bound : cur_a <= bound;
+      pi = keep_ge ? prv_a >= bound : prv_a <= bound;
+      if (ci != pi) {
+        const double prv_o = axis == 0 ? iy[ip] : ix[ip];
+        const double cur_o = axis == 0 ? iy[i] : ix[i];
+        const double t = (bound - prv_a) / (cur_a - prv_a);
+        const double o = prv_o + t * (cur_o - prv_o);
+        qx = axis == 0 ? bound : o;
+        qy = axis == 0 ? o : bound;
+        ++cnt;
+      }
+      if (ci) {
+        cx = ix[i];
+        cy = iy[i];
+        ++cnt;
+      }
+    }
+    // exclusive prefix of cnt across the warp
+    int incl = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int v = __shfl_up_sync(kFull, incl, d);
+      if (lane >= d) incl += v;
+    }
+    const int total = __shfl_sync(kFull, incl, 31);
+    int pos = base + incl - cnt;
+    if (base + total <= kCap && i < n) {
+      if (ci != pi) {
+        ox[pos] = qx;
+        oy[pos] = qy;
+        ++pos;
+      }
+      if (ci) {
+        ox[pos] = cx;
+        oy[pos] = cy;
+      }
+    }
+    base += total;
+  }
+  __syncwarp();
+  return base <= kCap ? base : -1;
+}
+
+struct RegionStats {
+  int status;  // sbp::RegionStatus
+  int ntri;
+};
+
+// Region for one anchor state into (tris, cum) with capacity `cap`. All lanes call.
+__device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double ay, double ayaw,
+                                   SbRegionTri* tris, double* cum, int cap, RegionScratch& sc) {
+  const int lane = threadIdx.x & 31;
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  double min_r = 0.0, max_r = inf;  // distance_band (relationships.cpp:101-122)
+  if (pl.distance_type == SB_DIST_GREATER) {
+    min_r = pl.distance;
+  } else if (pl.distance_type == SB_DIST_LESS) {
+    max_r = pl.distance;
+  } else if (pl.distance_type == SB_DIST_EQUAL) {
+    const double half = dmax(0.05 * pl.distance, 0.01);
+    min_r = dmax(0.0, pl.distance - half);
+    max_r = pl.distance + half;
+  }
+  const double pi = 3.14159265358979323846;
+  const double theta = pl.angle_threshold > 0.0 ? pl.angle_threshold
+                                                : (pl.direction == SB_DIR_NONE ? pi : pi / 4.0);
+  double vx = 1.0, vy = 0.0;  // resolve_direction (relationships.cpp:78-99)
+  if (pl.direction != SB_DIR_NONE) {
+    switch (pl.direction) {
+      case SB_DIR_LEFT: vx = -1; vy = 0; break;
+      case SB_DIR_RIGHT: vx = 1; vy = 0; break;
+      case SB_DIR_FRONT: vx = 0; vy = -1; break;
+      case SB_DIR_BACK: vx = 0; vy = 1; break;
+      default: {
+        const double nrm = sqrt(pl.direction_vector[0] * pl.direction_vector[0] +
+                                pl.direction_vector[1] * pl.direction_vector[1]);
+        vx = pl.direction_vector[0] / nrm;
+        vy = pl.direction_vector[1] / nrm;
+      }
+    }
+    if (pl.frame == SB_FRAME_LOCAL) {
+      const double c = cos(ayaw), s = sin(ayaw);
+      const double nx = c * vx - s * vy, ny = s * vx + c * vy;
+      vx = nx;
+      vy = ny;
+    }
+  }
+  // clip bound = bounds(support) expanded by the anchor; only used for infinite max_r
+  const double* rc = pl.rect;
+  double bx0 = inf, by0 = inf, bx1 = -inf, by1 = -inf;
+  const double vxs[5] = {rc[0], rc[2], rc[2], rc[0], ax};
+  const double vys[5] = {rc[1], rc[1], rc[3], rc[3], ay};
+  for (int k = 0; k < 5; ++k) {
+    bx0 = dmin(bx0, vxs[k]);
+    by0 = dmin(by0, vys[k]);
+    bx1 = dmax(bx1, vxs[k]);
+    by1 = dmax(by1, vys[k]);
+  }
+  const double ddx = bx1 - bx0, ddy = by1 - by0;
+  const double diag = bx0 > bx1 ? 0.0 : sqrt(ddx * ddx + ddy * ddy);
+
+  // ---- annulus_sector (polygon.cpp:136-176), arc points in parallel
+  if (!(theta > 0.0) || theta > pi + 1e-12) return {sbp::kRegionBadArg, 0};
+  if (isinf(max_r)) max_r = fmax(diag, min_r + 1e-6);
+  if (!(min_r < max_r)) return {sbp::kRegionBadArg, 0};
+  const double base = atan2(vy, vx);
+  const bool full = theta >= pi - 1e-12;
+  const double step = 5.0 * pi / 180.0;
+  auto arc_n = [&](double a0, double a1) {
+    int n = (int)ceil(fabs(a1 - a0) / step);
+    return n < 1 ? 1 : n;
+  };
+  double* X = sc.x[0];
+  double* Y = sc.y[0];
+  int n = 0;
+  auto arc = [&](double radius, double a0, double a1, int off) -> int {
+    const int na = arc_n(a0, a1);
+    if (off + na + 1 > kCap) return -1;
+    for (int i = lane; i <= na; i += 32) {
+      const double a = a0 + (a1 - a0) * (double)i / (double)na;
+      X[off + i] = ax + radius * cos(a);
+      Y[off + i] = ay + radius * sin(a);
+    }
+    return off + na + 1;
+  };
+  if (full) {
+    if (min_r > 0.0) return {sbp::kRegionBadArg, 0};
+    n = arc(max_r, 0.0, 2.0 * pi, 0);
+    if (n < 0) return {sbp::kRegionOverflow, 0};
+    n -= 1;
+  } else {
+    n = arc(max_r, base - theta, base + theta, 0);
+    if (n < 0) return {sbp::kRegionOverflow, 0};
+    if (min_r > 0.0) {
+      n = arc(min_r, base + theta, base - theta, n);
+      if (n < 0) return {sbp::kRegionOverflow, 0};
+    } else {
+      if (n + 1 > kCap) return {sbp::kRegionOverflow, 0};
+      if (lane == 0) {
+        X[n] = ax;
+        Y[n] = ay;
+      }
+      ++n;
+    }
+  }
+  __syncwarp();
+
+  // ---- intersect with the support rect (oracle Boost stand-in): correct() orientation
+  if (n < 3) return {sbp::kRegionEmpty, 0};
+  double ar = 0.0;
+  if (lane == 0) ar = ring_area_seq(X, Y, n);
+  ar = __shfl_sync(kFull, ar, 0);
+  if (ar < 0.0) {  // reverse the closed ring: p0 stays first
+    for (int i = 1 + lane; i < n - i; i += 32) {
+      const int j = n - i;
+      const double tx = X[i], ty = Y[i];
+      X[i] = X[j];
+      Y[i] = Y[j];
+      X[j] = tx;
+      Y[j] = ty;
+    }
+    __syncwarp();
+  }
+  const double x0 = fmin(rc[0], rc[2]), x1 = fmax(rc[0], rc[2]);
+  const double y0 = fmin(rc[1], rc[3]), y1 = fmax(rc[1], rc[3]);
+  n = warp_clip(sc.x[0], sc.y[0], n, sc.x[1], sc.y[1], 0, x0, true);
+  if (n >= 0) n = warp_clip(sc.x[1], sc.y[1], n, sc.x[0], sc.y[0], 0, x1, false);
+  if (n >= 0) n = warp_clip(sc.x[0], sc.y[0], n, sc.x[1], sc.y[1], 1, y0, true);
+  if (n >= 0) n = warp_clip(sc.x[1], sc.y[1], n, sc.x[0], sc.y[0], 1, y1, false);
+  if (n < 0) return {sbp::kRegionOverflow, 0};
+  // drop consecutive exact duplicates (keep the first of each run), then trailing copies
+  // of vertex 0 -- lane 0, sequential like the stand-in
+  int m = 0;
+  if (lane == 0) {
+    for (int i = 0; i < n; ++i) {
+      if (m == 0 || X[i] != X[m - 1] || Y[i] != Y[m - 1]) {
+        X[m] = X[i];
+        Y[m] = Y[i];
+        ++m;
+      }
+    }
+    while (m > 1 && X[0] == X[m - 1] && Y[0] == Y[m - 1]) --m;
+    if (m >= 3 && ring_area_seq(X, Y, m) == 0.0) m = 0;
+  }
+  m = __shfl_sync(kFull, m, 0);
+  __syncwarp();
+  if (m < 3) return {sbp::kRegionEmpty, 0};
+
+  // ---- triangulate (polygon.cpp:344-368) + ear_clip_ring (:260-340): orientation,
+  // tolerance-based duplicate drop (lane 0, order-dependent), then the fan fast path
+  int k = 0;
+  if (lane == 0) {
+    if (ring_area_seq(X, Y, m) < 0.0) {
+      for (int i = 0, j = m - 1; i < j; ++i, --j) {
+        double tx = X[i], ty = Y[i];
+        X[i] = X[j];
+        Y[i] = Y[j];
+        X[j] = tx;
+        Y[j] = ty;
+      }
+    }
+    for (int i = 0; i < m; ++i) {
+      if (k > 0) {
+        const double dx = X[i] - X[k - 1], dy = Y[i] - Y[k - 1];
+        if (!(dx * dx + dy * dy > 1e-24)) continue;
+      }
+      X[k] = X[i];
+      Y[k] = Y[i];
+      ++k;
+    }
+    while (k > 1) {
+      const double dx = X[0] - X[k - 1], dy = Y[0] - Y[k - 1];
+      if (dx * dx + dy * dy <= 1e-24) --k;
+      else break;
+    }
+  }
+  k = __shfl_sync(kFull, k, 0);
+  __syncwarp();
+  if (k < 3) return {sbp::kRegionOk, 0};  // valid() == false -> placeable = 0
+  bool ok = true;
+  for (int i = lane; i < k; i += 32) {
+    const int a = (i + k - 1) % k, c = (i + 1) % k;
+    if (sbp::cross2(X[a], Y[a], X[i], Y[i], X[c], Y[c]) < 0.0) ok = false;
+    if (i + 3 < k) {
+      const double cr = sbp::cross2(X[k - 1], Y[k - 1], X[i], Y[i], X[i + 1], Y[i + 1]);
+      if (cr < 0.0 || fabs(cr) < 1e-18) ok = false;
+    }
+  }
+  const bool fan = __all_sync(kFull, ok);
+  int ntri = 0;
+  if (fan) {
+    // triangle i = (k-1, i, i+1); keep area > 0 (PolygonSampler ctor, polygon.cpp:374-375)
+    for (int i = lane; i + 2 < k; i += 32)
+      sc.area[i] = 0.5 * fabs(sbp::cross2(X[k - 1], Y[k - 1], X[i], Y[i], X[i + 1], Y[i + 1]));
+    __syncwarp();
+    if (lane == 0) {
+      double total = 0.0;
+      for (int i = 0; i + 2 < k; ++i) {
+        const double a = sc.area[i];
+        if (a <= 0.0) continue;
+        if (ntri >= cap) {
+          ntri = -1;
+          break;
+        }
+        SbRegionTri& t = tris[ntri];
+        t.a[0] = X[k - 1];
+        t.a[1] = Y[k - 1];
+        t.b[0] = X[i];
+        t.b[1] = Y[i];
+        t.c[0] = X[i + 1];
+        t.c[1] = Y[i + 1];
+        total += a;
+        cum[ntri++] = total;
+      }
+      if (ntri > 0) {  // polygon.cpp:381-387
+        if (total > 0.0) {
+          for (int j = 0; j < ntri; ++j) cum[j] /= total;
+          cum[ntri - 1] = 1.0;
+        } else {
+          ntri = 0;
+        }
+      }
+    }
+  } else if (lane == 0) {  // general ear clipping (reflex or sliver corners): restatement
+    sbp::Ring r;
+    r.n = k;
+    for (int i = 0; i < k; ++i) {
+      r.x[i] = X[i];
+      r.y[i] = Y[i];
+    }
+    sbp::TableSink sink{tris, cum, 0, cap, 0.0};
+    if (!sbp::ear_clip_into(r, sink)) ntri = -1;
+    else ntri = sbp::finish_table(sink);
+  }
+  ntri = __shfl_sync(kFull, ntri, 0);
+  __syncwarp();
+  if (ntri < 0) return {sbp::kRegionOverflow, 0};
+  return {sbp::kRegionOk, ntri};
+}
+
+// Warp per local instance: anchor state in the support frame (inverse_rigid(support) *
+// anchor pose, yaw_of), the variation test against instance 0 (relationships.cpp:178-186)
+// and the region table. Instance 0's state comes from `s0` (sharded runs) or, when this
+// shard owns global instance 0, is recomputed per warp from local instance 0.
+__global__ void __launch_bounds__(kRB) k_relation_regions(RelationRegionParams p) {
+  __shared__ RegionScratch scratch[kRW];
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * (uint64_t)kRB + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t)gridDim.x * kRW;
+  RegionScratch& sc = scratch[threadIdx.x >> 5];
+  M34 inv;
+#pragma unroll
+  for (int k = 0; k < 12; ++k) inv.m[k] = p.inv_support[k];
+  auto state = [&](uint64_t inst, double& x, double& y, double& yaw) {
+    const double* pp = p.w.pose + ((uint64_t)p.anchor_object * p.w.n + inst) * 12;
+    M34 P, rel;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) P.m[k] = pp[k];
+    mul34(inv, P, rel);
+    x = rel.m[3];
+    y = rel.m[7];
+    yaw = atan2(rel.m[4], rel.m[0]);
+  };
+  if (p.from_s0) {  // canonical region_for(0) from the exchanged instance-0 state
+    if (warp == 0) {
+      const RegionStats r = warp_region(p.pl, p.s0[0], p.s0[1], p.s0[2], p.tris, p.cum, p.cap, sc);
+      if (lane == 0) {
+        const bool good = r.status == sbp::kRegionOk || r.status == sbp::kRegionEmpty;
+        p.ntri[0] = good ? r.ntri : 0;
+        if (!good) atomicMax(p.flags + 1, r.status);
+      }
+    }
+    return;
+  }
+  double x0, y0, yaw0;
+  if (p.owns_instance0) {
+    state(0, x0, y0, yaw0);
+  } else {
+    x0 = p.s0[0];
+    y0 = p.s0[1];
+    yaw0 = p.s0[2];
+  }
+  bool vary = false;
+  int worst = 0;
+  for (uint64_t i = warp; i < p.w.n; i += nwarps) {
+    double ax, ay, ayaw;
+    state(i, ax, ay, ayaw);
+    const double dx = ax - x0, dy = ay - y0;
+    vary = vary || sqrt(dx * dx + dy * dy) > 1e-12 || fabs(ayaw - yaw0) > 1e-12;
+    const RegionStats r = warp_region(p.pl, ax, ay, ayaw, p.tris + i * p.cap, p.cum + i * p.cap,
+                                      p.cap, sc);
+    if (lane == 0) {
+      p.ntri[i] = r.status == sbp::kRegionOk || r.status == sbp::kRegionEmpty ? r.ntri : 0;
+      if (r.status != sbp::kRegionOk && r.status != sbp::kRegionEmpty && r.status > worst)
+        worst = r.status;
+    }
+  }
+  if (lane == 0) {
+    if (vary) atomicOr(p.flags + 0, 1);
+    if (worst) atomicMax(p.flags + 1, worst);
+  }
+}
+
+}  // namespace
+
+void relation_regions(const RelationRegionParams& p, int num_sms, sb_stream_t s) {
+  unsigned blocks = (unsigned)((p.w.n + kRW - 1) / kRW);
+  const unsigned cap_blocks = (unsigned)(num_sms * 16);
+  if (blocks > cap_blocks) blocks = cap_blocks;
+  if (blocks == 0) blocks = 1;
+  k_relation_regions<<<blocks, kRB, 0, s>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string("relation_regions: ") + cudaGetErrorString(e));
+}
+
+}  // namespace sbk

@@ -1,0 +1,28 @@
+// Per-instance constraint regions on the device (see sb_region.cu).
+#pragma once
+
+#include <cstdint>
+
+#include "sb_kernels.h"
+#include "sb_layout.h"
+
+namespace sbk {
+
+struct RelationRegionParams {
+  SbWorldView w;
+  SbPlacementDev pl;
+  int32_t anchor_object;
+  int32_t owns_instance0;  // 1: global instance 0 is local instance 0 (compute s0 in-kernel)
+  double inv_support[12];  // inverse_rigid(support pose), row-major 3x4 (host-computed)
+  const double* s0;        // instance 0's anchor state when !owns_instance0 (device)
+  int32_t from_s0;         // 1: build a single region from s0 (canonical, sharded runs)
+  int32_t cap;
+  SbRegionTri* tris;       // [n][cap] (or [1][cap] when from_s0)
+  double* cum;
+  int32_t* ntri;           // [n]
+  int32_t* flags;          // [0] |= anchors vary, [1] = max region error status
+};
+
+void relation_regions(const RelationRegionParams& p, int num_sms, sb_stream_t s);
+
+}  // namespace sbk

@@ -18,6 +18,7 @@
 #include "sb_host.hpp"
 #include "sb_kernels.h"
 #include "sb_place.h"
+#include "sb_region.h"
 #include "sb_layout.h"
 
 namespace {
@@ -414,12 +415,12 @@ struct sb_engine {
   DevArray<uint64_t> d_pairs;
   DevArray<uint32_t> d_chunk;
   DevArray<uint32_t> d_ctrl;
+  DevArray<uint64_t> d_prof;
+  DevArray<int32_t> d_rflags;
+  std::vector<cudaEvent_t> ev_place;
+  double last_prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   int num_sms = 0;
   uint64_t spec_budget = 0, slot_cap = 0;
-  bool legacy_rounds = false;
-  DevArray<uint64_t> d_count;
-  DevArray<uint8_t> d_temp;
-  size_t temp_bytes = 0;
   DevArray<unsigned long long> d_counters;
   DevArray<double> d_anchor;
   DevArray<double> d_s0;
@@ -607,16 +608,10 @@ struct sb_engine {
       d_pairs.alloc(std::max<size_t>(1, per) * slot_cap);
     }
     d_chunk.alloc(n / 256 + 2);
-    d_ctrl.alloc(8);
-    {
-      const char* mode = std::getenv("SB_ENGINE");
-      legacy_rounds = mode && std::string(mode) == "legacy";
-    }
-    d_count.alloc(1);
-    temp_bytes = sbk::select_temp_bytes(n);
-    d_temp.alloc(temp_bytes);
+    d_ctrl.alloc(8 * std::max<size_t>(1, places.size()));
+    d_rflags.alloc(2 * std::max<size_t>(1, places.size()));
+    d_prof.alloc(8);
     d_counters.alloc(8);
-    h_count.ensure(4);
     cuda_check(cudaEventCreate(&ev_start), "event");
     cuda_check(cudaEventCreate(&ev_stop), "event");
     cuda_check(cudaEventCreate(&ev_r0), "event");
@@ -628,77 +623,81 @@ struct sb_engine {
     if (world) cudaSetDevice(world->device);
     for (cudaEvent_t e : {ev_start, ev_stop, ev_r0, ev_r1})
       if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : ev_place) cudaEventDestroy(e);
   }
 
-  uint64_t read_count() {
-    cuda_check(cudaMemcpyAsync(h_count.p, d_count.p, sizeof(uint64_t), cudaMemcpyDeviceToHost, world->stream), "D2H count");
-    cuda_check(cudaStreamSynchronize(world->stream), "sync");
-    return h_count.p[0];
+
+  // One placement's relation region (single GPU: decided on the device, no host sync).
+  void relation_prep_device(size_t p, Placement& pl, const SbWorldView& wv, uint64_t& launches) {
+    sbk::RelationRegionParams rp;
+    std::memset(&rp, 0, sizeof rp);
+    rp.w = wv;
+    rp.pl = pl.dev;
+    rp.anchor_object = pl.dev.anchor_object;
+    rp.owns_instance0 = 1;
+    std::memcpy(rp.inv_support, pl.inv_support, sizeof rp.inv_support);
+    rp.cap = inst_cap;
+    rp.tris = d_inst_tris.p;
+    rp.cum = d_inst_cum.p;
+    rp.ntri = d_inst_n.p;
+    rp.flags = d_rflags.p + 2 * p;
+    sbk::relation_regions(rp, num_sms, world->s());
+    ++launches;
   }
 
-  // Pre-phased engine (one fused kernel per round + CUB compaction, host-synchronised);
-  // kept for A/B measurement (SB_ENGINE=legacy).
-  void legacy_place(size_t p, Placement& pl, bool fast, uint64_t fast_state0,
-                    const SbRegionTri* canon_tris, const double* canon_cum, int canon_n,
-                    uint64_t run_seed, const SbWorldView& wv, uint64_t& launches,
-                    uint64_t& rounds, uint64_t& round_launches, double& check_ms) {
+  // Sharded runs: instance 0's anchor state and the variation flag are exchanged.
+  // Returns true if the anchors vary (per-instance path); else fills the canonical slot.
+  bool relation_prep_sharded(size_t p, Placement& pl, const SbWorldView& wv, uint64_t& launches,
+                             int& canon_n) {
     cudaStream_t stream = world->stream;
     sb_stream_t s = world->s();
-      sbk::select_valid(d_valid.p, n, d_act[0].p, d_count.p, d_temp.p, temp_bytes, s);
-      launches += 2;
-      int cur = 0;
-      uint64_t draws = 0;  // fast-path draws consumed by all ranks so far (S)
-      uint64_t m = read_count();
-      for (int a = 0; a < attempts; ++a) {
-        std::vector<uint64_t> counts = exchange({m});
-        uint64_t total = 0, before = 0;
-        for (int r = 0; r < world_size; ++r) {
-          if (r < rank) before += counts[r];
-          total += counts[r];
-        }
-        if (total == 0) break;
-        ++rounds;
-        const bool no_draw = fast && canon_n == 0;  // empty canonical region: placeable = 0
-        if (m > 0 && !no_draw) {
-          sbk::RoundParams rp;
-          rp.w = wv;
-          rp.pl = pl.dev;
-          rp.attempt = a;
-          rp.fast = fast ? 1 : 0;
-          rp.run_seed = run_seed;
-          rp.global_begin = begin;
-          rp.fast_state0 = fast_state0;
-          rp.draw_base = draws + before;
-          rp.canon_tris = canon_tris;
-          rp.canon_cum = canon_cum;
-          rp.canon_n = canon_n;
-          rp.inst_cap = inst_cap;
-          rp.inst_tris = d_inst_tris.p;
-          rp.inst_cum = d_inst_cum.p;
-          rp.inst_n = d_inst_n.p;
-          rp.act = d_act[cur].p;
-          rp.m = m;
-          rp.fail = d_fail.p;
-          rp.accepted = d_accepted.p + p * n;
-          rp.counters = d_counters.p;
-          cuda_check(cudaEventRecord(ev_r0, stream), "event");
-          sbk::round_kernel(rp, s);
-          cuda_check(cudaEventRecord(ev_r1, stream), "event");
-          ++launches;
-          ++round_launches;
-          sbk::select_flagged(d_act[cur].p, d_fail.p, m, d_act[1 - cur].p, d_count.p, d_temp.p,
-                              temp_bytes, s);
-          launches += 2;
-          cur = 1 - cur;
-          m = read_count();
-          float ms = 0.f;
-          cuda_check(cudaEventElapsedTime(&ms, ev_r0, ev_r1), "elapsed");
-          check_ms += ms;
-        }
-        if (fast && !no_draw) draws += total;
-      }
-      sbk::invalidate(d_act[cur].p, m, d_valid.p, s);
+    double s0[3] = {0, 0, 0};
+    if (begin == 0) {
+      sbk::anchor_states(wv, pl.dev.anchor_object, pl.inv_support, d_anchor.p, s);
       ++launches;
+      cuda_check(cudaMemcpyAsync(s0, d_anchor.p, sizeof s0, cudaMemcpyDeviceToHost, stream), "D2H s0");
+      cuda_check(cudaStreamSynchronize(stream), "sync");
+    }
+    std::vector<uint64_t> send(4, 0);
+    std::memcpy(send.data(), s0, sizeof s0);
+    send[3] = begin == 0 ? 1 : 0;
+    std::vector<uint64_t> recv = exchange(send);
+    for (int r = 0; r < world_size; ++r)
+      if (recv[4 * r + 3]) std::memcpy(s0, &recv[4 * r], sizeof s0);
+    cuda_check(cudaMemcpyAsync(d_s0.p, s0, sizeof s0, cudaMemcpyHostToDevice, stream), "H2D s0");
+    sbk::RelationRegionParams rp;
+    std::memset(&rp, 0, sizeof rp);
+    rp.w = wv;
+    rp.pl = pl.dev;
+    rp.anchor_object = pl.dev.anchor_object;
+    rp.owns_instance0 = 0;
+    std::memcpy(rp.inv_support, pl.inv_support, sizeof rp.inv_support);
+    rp.s0 = d_s0.p;
+    rp.cap = inst_cap;
+    rp.tris = d_inst_tris.p;
+    rp.cum = d_inst_cum.p;
+    rp.ntri = d_inst_n.p;
+    rp.flags = d_rflags.p + 2 * p;
+    sbk::relation_regions(rp, num_sms, s);
+    ++launches;
+    int32_t flags[2];
+    cuda_check(cudaMemcpyAsync(flags, rp.flags, sizeof flags, cudaMemcpyDeviceToHost, stream), "D2H flags");
+    cuda_check(cudaStreamSynchronize(stream), "sync");
+    bool vary = flags[0] != 0;
+    std::vector<uint64_t> f = exchange({vary ? 1ull : 0ull});
+    vary = false;
+    for (uint64_t x : f) vary = vary || x != 0;
+    if (!vary) {
+      rp.from_s0 = 1;
+      rp.tris = d_canon_tris.p + p * SB_REGION_MAX_VERTS;
+      rp.cum = d_canon_cum.p + p * SB_REGION_MAX_VERTS;
+      rp.ntri = d_canon_n.p + p;
+      sbk::relation_regions(rp, num_sms, s);
+      ++launches;
+      cuda_check(cudaMemcpyAsync(&canon_n, d_canon_n.p + p, 4, cudaMemcpyDeviceToHost, stream), "D2H n");
+      cuda_check(cudaStreamSynchronize(stream), "sync");
+    }
+    return vary;
   }
 
   void generate(uint64_t run_seed, sb_run_stats* st) {
@@ -706,94 +705,47 @@ struct sb_engine {
     cudaStream_t stream = world->stream;
     sb_stream_t s = world->s();
     const SbWorldView wv = world->view();
-    uint64_t launches = 0, rounds = 0, per_inst = 0, round_launches = 0;
-    double check_ms = 0.0;
+    const size_t P = places.size();
+    uint64_t launches = 0, rounds_host = 0, per_inst_host = 0, round_launches = 0;
+    double sharded_check_ms = 0.0;
+    while (ev_place.size() < 2 * P + 2) {
+      cudaEvent_t e;
+      cuda_check(cudaEventCreate(&e), "event");
+      ev_place.push_back(e);
+    }
     cuda_check(cudaEventRecord(ev_start, stream), "event");
     cuda_check(cudaMemsetAsync(d_counters.p, 0, 8 * sizeof(unsigned long long), stream), "memset");
-    sbk::engine_reset(wv, first_place_obj, static_cast<int32_t>(places.size()), d_valid.p, d_accepted.p,
-                      static_cast<int32_t>(places.size()), s);
+    cuda_check(cudaMemsetAsync(d_prof.p, 0, 8 * sizeof(uint64_t), stream), "memset");
+    cuda_check(cudaMemsetAsync(d_ctrl.p, 0, d_ctrl.count * sizeof(uint32_t), stream), "memset");
+    cuda_check(cudaMemsetAsync(d_rflags.p, 0, d_rflags.count * sizeof(int32_t), stream), "memset");
+    sbk::engine_reset(wv, first_place_obj, static_cast<int32_t>(P), d_valid.p, d_accepted.p,
+                      static_cast<int32_t>(P), s);
     ++launches;
-    for (size_t p = 0; p < places.size(); ++p) {
+    for (size_t p = 0; p < P; ++p) {
       Placement& pl = places[p];
       bool fast = true;
       int canon_n = pl.canon_n;
       const SbRegionTri* canon_tris = d_canon_tris.p + p * SB_REGION_MAX_VERTS;
       const double* canon_cum = d_canon_cum.p + p * SB_REGION_MAX_VERTS;
-      if (pl.dev.anchor_object >= 0) {
-        sbk::anchor_states(wv, pl.dev.anchor_object, pl.inv_support, d_anchor.p, s);
-        ++launches;
-        // instance 0 (global) lives on the rank whose shard starts at 0
-        double s0[3] = {0, 0, 0};
-        if (begin == 0) {
-          cuda_check(cudaMemcpyAsync(s0, d_anchor.p, sizeof s0, cudaMemcpyDeviceToHost, stream), "D2H s0");
-          cuda_check(cudaStreamSynchronize(stream), "sync");
-        }
-        if (world_size > 1) {
-          std::vector<uint64_t> send(4, 0);
-          std::memcpy(send.data(), s0, sizeof s0);
-          send[3] = begin == 0 ? 1 : 0;
-          std::vector<uint64_t> recv = exchange(send);
-          for (int r = 0; r < world_size; ++r)
-            if (recv[4 * r + 3]) std::memcpy(s0, &recv[4 * r], sizeof s0);
-        }
-        cuda_check(cudaMemsetAsync(d_flags.p, 0, 2 * sizeof(int32_t), stream), "memset");
-        sbk::vary_flag(d_anchor.p, n, s0[0], s0[1], s0[2], d_flags.p, s);
-        ++launches;
-        int32_t flags[2];
-        cuda_check(cudaMemcpyAsync(flags, d_flags.p, sizeof flags, cudaMemcpyDeviceToHost, stream), "D2H flag");
-        cuda_check(cudaStreamSynchronize(stream), "sync");
-        bool vary = flags[0] != 0;
-        if (world_size > 1) {
-          std::vector<uint64_t> f = exchange({vary ? 1ull : 0ull});
-          vary = false;
-          for (uint64_t x : f) vary = vary || x != 0;
-        }
-        sbk::RegionParams rp;
-        rp.pl = pl.dev;
-        rp.cap = inst_cap;
-        rp.status = d_flags.p + 1;
-        if (vary) {
-          ++per_inst;
-          fast = false;
-          rp.anchors = d_anchor.p;
-          rp.count = n;
-          rp.tris = d_inst_tris.p;
-          rp.cum = d_inst_cum.p;
-          rp.ntri = d_inst_n.p;
+      const bool relation = pl.dev.anchor_object >= 0;
+      cuda_check(cudaEventRecord(ev_place[2 * p], stream), "event");
+      if (relation) {
+        if (world_size == 1) {
+          relation_prep_device(p, pl, wv, launches);
         } else {
-          cuda_check(cudaMemcpyAsync(d_s0.p, s0, sizeof s0, cudaMemcpyHostToDevice, stream), "H2D s0");
-          rp.anchors = d_s0.p;
-          rp.count = 1;
-          rp.tris = d_canon_tris.p + p * SB_REGION_MAX_VERTS;
-          rp.cum = d_canon_cum.p + p * SB_REGION_MAX_VERTS;
-          rp.ntri = d_canon_n.p + p;
+          fast = !relation_prep_sharded(p, pl, wv, launches, canon_n);
+          if (!fast) ++per_inst_host;
         }
-        sbk::build_regions(rp, s);
-        ++launches;
-        int32_t status_and_n[2] = {0, 0};
-        cuda_check(cudaMemcpyAsync(&status_and_n[0], d_flags.p + 1, 4, cudaMemcpyDeviceToHost, stream), "D2H status");
-        if (!vary)
-          cuda_check(cudaMemcpyAsync(&status_and_n[1], d_canon_n.p + p, 4, cudaMemcpyDeviceToHost, stream), "D2H canon n");
-        cuda_check(cudaStreamSynchronize(stream), "sync");
-        if (status_and_n[0] != 0)
-          throw std::runtime_error("constraint region build failed (status " + std::to_string(status_and_n[0]) +
-                                   ": capacity overflow or unsupported annulus)");
-        if (!vary) canon_n = status_and_n[1];
       }
-
+      cuda_check(cudaEventRecord(ev_place[2 * p + 1], stream), "event");
       uint64_t fast_state0 = 0;
-      if (fast) {  // Pcg32(make_stream(run_seed, {salt, "cach"})) state after the constructor
+      {  // Pcg32(make_stream(run_seed, {salt, "cach"})) state after the constructor
         uint64_t h = sbh::mix64(sbh::mix64(sbh::mix64(run_seed) ^ pl.dev.salt) ^ 0x63616368ULL);
         const uint64_t mult = 6364136223846793005ULL, inc = (0xda3e39cb94b95bdbULL << 1u) | 1u;
         uint64_t st0 = inc;
         st0 += h;
         st0 = st0 * mult + inc;
         fast_state0 = st0;
-      }
-      if (legacy_rounds) {
-        legacy_place(p, pl, fast, fast_state0, canon_tris, canon_cum, canon_n, run_seed, wv,
-                     launches, rounds, round_launches, check_ms);
-        continue;
       }
       sbk::PlaceParams pp;
       std::memset(&pp, 0, sizeof pp);
@@ -824,32 +776,25 @@ struct sb_engine {
       pp.pairs = d_pairs.p;
       pp.pair_cap = d_pairs.count;
       pp.chunk_cnt = d_chunk.p;
-      pp.ctrl = d_ctrl.p;
+      pp.ctrl = d_ctrl.p + 8 * p;
       pp.counters = d_counters.p;
       pp.slot_cap = slot_cap;
       pp.spec_budget = spec_budget;
       pp.spec_width = 1;
-      cuda_check(cudaMemsetAsync(d_ctrl.p, 0, d_ctrl.count * sizeof(uint32_t), stream), "memset ctrl");
-      uint32_t ctrl[8];
+      pp.prof = d_prof.p;
+      pp.vary_flag = (relation && world_size == 1) ? d_rflags.p + 2 * p : nullptr;
       if (world_size == 1) {
-        cuda_check(cudaEventRecord(ev_r0, stream), "event");
         if (!sbk::place_persistent(pp, num_sms, s))
           throw CudaError("cooperative launch of the placement kernel is not possible");
-        cuda_check(cudaEventRecord(ev_r1, stream), "event");
         ++launches;
         ++round_launches;
-        cuda_check(cudaMemcpyAsync(ctrl, d_ctrl.p, sizeof ctrl, cudaMemcpyDeviceToHost, stream), "D2H ctrl");
-        cuda_check(cudaStreamSynchronize(stream), "sync");
-        float ms = 0.f;
-        cuda_check(cudaEventElapsedTime(&ms, ev_r0, ev_r1), "elapsed");
-        check_ms += ms;
-        rounds += ctrl[2];
       } else {
         // sharded: same phases, one launch each, with the per-round count exchange
+        uint32_t ctrl[8];
         sbk::place_init(pp, s);
         launches += 2;
         auto read_ctrl = [&]() {
-          cuda_check(cudaMemcpyAsync(ctrl, d_ctrl.p, sizeof ctrl, cudaMemcpyDeviceToHost, stream), "D2H ctrl");
+          cuda_check(cudaMemcpyAsync(ctrl, pp.ctrl, sizeof ctrl, cudaMemcpyDeviceToHost, stream), "D2H ctrl");
           cuda_check(cudaStreamSynchronize(stream), "sync");
         };
         read_ctrl();
@@ -863,7 +808,7 @@ struct sb_engine {
             total += counts[r];
           }
           if (total == 0) break;
-          ++rounds;
+          ++rounds_host;
           if (m > 0) {
             pp.draw_base = draws + before;
             cuda_check(cudaEventRecord(ev_r0, stream), "event");
@@ -876,28 +821,55 @@ struct sb_engine {
             m = ctrl[0];
             float ms = 0.f;
             cuda_check(cudaEventElapsedTime(&ms, ev_r0, ev_r1), "elapsed");
-            check_ms += ms;
+            sharded_check_ms += ms;
           }
           if (fast && canon_n > 0) draws += total;
         }
         sbk::place_finish(pp, cur, s);
         ++launches;
-        read_ctrl();
       }
-      if (ctrl[3] != 0)
-        throw std::runtime_error("narrow-phase pair queue overflow (more than " +
-                                 std::to_string(d_pairs.count) + " overlapping pairs in a round)");
     }
+    cuda_check(cudaEventRecord(ev_place[2 * P], stream), "event");
     cuda_check(cudaEventRecord(ev_stop, stream), "event");
     unsigned long long c[8];
     cuda_check(cudaMemcpyAsync(c, d_counters.p, sizeof c, cudaMemcpyDeviceToHost, stream), "D2H counters");
+    std::vector<uint32_t> ctrl_all(8 * std::max<size_t>(1, P));
+    cuda_check(cudaMemcpyAsync(ctrl_all.data(), d_ctrl.p, ctrl_all.size() * 4, cudaMemcpyDeviceToHost, stream), "D2H ctrl");
+    std::vector<int32_t> rflags(2 * std::max<size_t>(1, P));
+    cuda_check(cudaMemcpyAsync(rflags.data(), d_rflags.p, rflags.size() * 4, cudaMemcpyDeviceToHost, stream), "D2H flags");
+    uint64_t prof[8];
+    cuda_check(cudaMemcpyAsync(prof, d_prof.p, sizeof prof, cudaMemcpyDeviceToHost, stream), "D2H prof");
     cuda_check(cudaStreamSynchronize(stream), "sync");
+    for (size_t p = 0; p < P; ++p) {
+      if (rflags[2 * p + 1] != 0)
+        throw std::runtime_error("constraint region build failed for placement " + std::to_string(p) +
+                                 " (status " + std::to_string(rflags[2 * p + 1]) +
+                                 ": capacity overflow or unsupported annulus)");
+      if (ctrl_all[8 * p + 3] != 0)
+        throw std::runtime_error("narrow-phase pair queue overflow (more than " +
+                                 std::to_string(d_pairs.count) + " overlapping pairs in a round)");
+    }
     float total_ms = 0.f;
     cuda_check(cudaEventElapsedTime(&total_ms, ev_start, ev_stop), "elapsed");
+    double regions_ms = 0.0, place_ms = 0.0;
+    for (size_t p = 0; p < P; ++p) {
+      float a = 0.f, b = 0.f;
+      cuda_check(cudaEventElapsedTime(&a, ev_place[2 * p], ev_place[2 * p + 1]), "elapsed");
+      cuda_check(cudaEventElapsedTime(&b, ev_place[2 * p + 1], ev_place[2 * p + 2]), "elapsed");
+      regions_ms += a;
+      place_ms += b;
+    }
+    uint64_t rounds = rounds_host;
+    if (world_size == 1)
+      for (size_t p = 0; p < P; ++p) rounds += ctrl_all[8 * p + 2];
     last_total_ms = total_ms;
-    last_check_ms = check_ms;
+    last_check_ms = world_size == 1 ? place_ms : sharded_check_ms;
     last_check_launches = round_launches;
     last_launches = launches;
+    for (int k = 0; k < 5; ++k) last_prof[k] = prof[k] * 1e-6;
+    last_prof[5] = static_cast<double>(prof[5]);
+    last_prof[6] = regions_ms;
+    last_prof[7] = total_ms;
     world->stats.check_calls += round_launches;
     world->stats.checked_instances += c[0];
     world->stats.narrow_phase_tests += c[1];
@@ -909,7 +881,7 @@ struct sb_engine {
       st->triangle_pair_tests = c[2];
       st->candidates_sampled = c[3];
       st->rounds = rounds;
-      st->per_instance_placements = per_inst;
+      st->per_instance_placements = c[7] + per_inst_host;
       st->broad_phase_tests = c[4];
       st->node_pair_tests = c[5];
       st->accepted_candidates = c[6];
@@ -1153,6 +1125,11 @@ sb_status sb_engine_download(sb_engine* e, sb_result* out) {
 sb_world* sb_engine_world(sb_engine* e) { return e->world.get(); }
 uint64_t sb_engine_local_instances(const sb_engine* e) { return e->n; }
 uint64_t sb_engine_last_launches(const sb_engine* e) { return e->last_launches; }
+sb_status sb_engine_phase_profile(const sb_engine* e, double out[8]) {
+  return guard([&] {
+    for (int k = 0; k < 8; ++k) out[k] = e->last_prof[k];
+  });
+}
 sb_status sb_engine_last_timing(const sb_engine* e, double* total_ms, double* check_ms,
                                 uint64_t* check_launches) {
   return guard([&] {

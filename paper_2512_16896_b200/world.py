@@ -366,5 +366,12 @@ class Engine:
         A.check(A.lib().sb_engine_last_timing(self._h, C.byref(t), C.byref(c), C.byref(n)))
         return t.value, c.value, n.value
 
+    def phase_profile(self) -> dict:
+        out = (C.c_double * 8)()
+        A.check(A.lib().sb_engine_phase_profile(self._h, out))
+        keys = ("init_ms", "broad_ms", "narrow_ms", "accept_ms", "compact_ms", "rounds",
+                "regions_ms", "total_ms")
+        return dict(zip(keys, list(out)))
+
     def last_launches(self) -> int:
         return A.lib().sb_engine_last_launches(self._h)
