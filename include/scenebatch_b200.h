@@ -262,6 +262,12 @@ sb_status sb_engine_last_timing(const sb_engine* e, double* total_ms, double* ch
  * total ms (CUDA events). */
 sb_status sb_engine_phase_profile(const sb_engine* e, double out[8]);
 
+/* Diagnostics: evaluate the device libm used on the hot path (correctly rounded
+ * double-double sin/cos/atan2, replacing glibc's std::sin/cos/atan2 in transform.hpp:47,
+ * polygon.cpp:151, relationships.cpp:184,238) on n inputs on device 0.
+ * fn 0: out[i] = sin(in[i]); 1: cos(in[i]); 2: atan2(in[2i], in[2i+1]). */
+sb_status sb_device_math(int fn, const double* in, uint64_t n, double* out);
+
 #ifdef __cplusplus
 }
 #endif

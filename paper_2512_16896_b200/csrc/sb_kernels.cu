@@ -5,6 +5,7 @@
 #include <string>
 
 #include "../../include/scenebatch_b200.h"
+#include "sb_crmath.cuh"
 #include "sb_dev.cuh"
 #include "sb_kernels.h"
 #include "sb_warp.cuh"
@@ -150,7 +151,7 @@ __global__ void k_anchor_states(WorldView w, int32_t anchor_obj, M34 inv_support
   mul34(inv_support, P, rel);
   out[3 * i + 0] = rel.m[3];
   out[3 * i + 1] = rel.m[7];
-  out[3 * i + 2] = atan2(rel.m[4], rel.m[0]);
+  out[3 * i + 2] = sbm::atan2_cr(rel.m[4], rel.m[0]);
 }
 
 __global__ void k_pose_colmajor(WorldView w, int32_t obj, double* out16) {
@@ -166,9 +167,29 @@ __global__ void k_pose_colmajor(WorldView w, int32_t obj, double* out16) {
   o[15] = 1.0;
 }
 
+// Test hook: fn 0 = sin, 1 = cos, 2 = atan2(in[2i], in[2i+1]) with the device functions the
+// hot path uses (sb_crmath.cuh).
+__global__ void k_debug_math(int fn, const double* in, uint64_t n, double* out) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (fn == 2) {
+    out[i] = sbm::atan2_cr(in[2 * i], in[2 * i + 1]);
+  } else {
+    double s, c;
+    sbm::sincos_cr(in[i], &s, &c);
+    out[i] = fn == 0 ? s : c;
+  }
+}
+
 }  // namespace
 
 namespace sbk {
+
+void debug_math(int fn, const double* in, uint64_t n, double* out, sb_stream_t s) {
+  if (n == 0) return;
+  k_debug_math<<<grid_for(n), kBlock, 0, s>>>(fn, in, n, out);
+  check_launch("debug_math");
+}
 
 void init_object(const SbWorldView& w, int32_t obj, sb_stream_t s) {
   k_init_object<<<grid_for(w.n), kBlock, 0, s>>>(w, obj);

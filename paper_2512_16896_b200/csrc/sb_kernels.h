@@ -33,6 +33,8 @@ void engine_reset(const SbWorldView& w, int32_t first_obj, int32_t n_obj, uint8_
 // AnchorState per instance (support frame): out[3i..3i+2] = x, y, yaw
 void anchor_states(const SbWorldView& w, int32_t anchor_obj, const double inv_support[12],
                    double* out, sb_stream_t s);
+// test hook for the device libm (sb_crmath.cuh): fn 0 sin, 1 cos, 2 atan2 (pairs y, x)
+void debug_math(int fn, const double* in, uint64_t n, double* out, sb_stream_t s);
 // accepted poses of one object as column-major Mat4 (N x 16 doubles)
 void download_poses(const SbWorldView& w, int32_t obj, double* out16, sb_stream_t s);
 

@@ -8,6 +8,7 @@
 #include <string>
 
 #include "../../include/scenebatch_b200.h"
+#include "sb_crmath.cuh"
 #include "sb_dev.cuh"
 #include "sb_place.h"
 #include "sb_poly.h"
@@ -198,9 +199,10 @@ __device__ void phase_a(const PlaceParams& p, const Sampling& S, const SbGeom& g
     } else if (pl.orientation == SB_ORIENT_FACE_TO) {  // relationships.cpp:232-239
       const double* tp = w.pose + ((uint64_t)pl.face_object * w.n + inst) * 12;
       double dx = tp[3] - px, dy = tp[7] - py;
-      yaw = sqrt(dx * dx + dy * dy) < 1e-12 ? 0.0 : atan2(dy, dx);
+      yaw = sqrt(dx * dx + dy * dy) < 1e-12 ? 0.0 : sbm::atan2_cr(dy, dx);
     }
-    double c = cos(yaw), s = sin(yaw);
+    double c, s;
+    sbm::sincos_cr(yaw, &s, &c);  // rotation_z: std::cos / std::sin (transform.hpp:47)
     M34 T, Rz, pose;  // translation(p + z_off z) * rotation_z(yaw)
 #pragma unroll
     for (int k = 0; k < 12; ++k) T.m[k] = Rz.m[k] = 0.0;

@@ -11,6 +11,7 @@
 #include <string>
 
 #include "../../include/scenebatch_b200.h"
+#include "sb_crmath.cuh"
 #include "sb_dev.cuh"
 #include "sb_poly.h"
 #include "sb_region.h"
@@ -135,7 +136,8 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
       }
     }
     if (pl.frame == SB_FRAME_LOCAL) {
-      const double c = cos(ayaw), s = sin(ayaw);
+      double c, s;
+      sbm::sincos_cr(ayaw, &s, &c);
       const double nx = c * vx - s * vy, ny = s * vx + c * vy;
       vx = nx;
       vy = ny;
@@ -159,7 +161,7 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
   if (!(theta > 0.0) || theta > pi + 1e-12) return {sbp::kRegionBadArg, 0};
   if (isinf(max_r)) max_r = fmax(diag, min_r + 1e-6);
   if (!(min_r < max_r)) return {sbp::kRegionBadArg, 0};
-  const double base = atan2(vy, vx);
+  const double base = sbm::atan2_cr(vy, vx);
   const bool full = theta >= pi - 1e-12;
   const double step = 5.0 * pi / 180.0;
   auto arc_n = [&](double a0, double a1) {
@@ -174,8 +176,10 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
     if (off + na + 1 > kCap) return -1;
     for (int i = lane; i <= na; i += 32) {
       const double a = a0 + (a1 - a0) * (double)i / (double)na;
-      X[off + i] = ax + radius * cos(a);
-      Y[off + i] = ay + radius * sin(a);
+      double sa, ca;
+      sbm::sincos_cr(a, &sa, &ca);
+      X[off + i] = ax + radius * ca;
+      Y[off + i] = ay + radius * sa;
     }
     return off + na + 1;
   };
@@ -347,16 +351,18 @@ __global__ void __launch_bounds__(kRB) k_relation_regions(RelationRegionParams p
   M34 inv;
 #pragma unroll
   for (int k = 0; k < 12; ++k) inv.m[k] = p.inv_support[k];
-  auto state = [&](uint64_t inst, double& x, double& y, double& yaw) {
+  // Anchor position (and, only when it can matter, yaw) in the support frame. The yaw
+  // feeds a local-frame direction and the variation test; the latter only needs it when
+  // the positions agree (relationships.cpp:180-181), so atan2 is skipped otherwise.
+  const bool yaw_used = p.pl.direction != SB_DIR_NONE && p.pl.frame == SB_FRAME_LOCAL;
+  auto rel_of = [&](uint64_t inst, M34& rel) {
     const double* pp = p.w.pose + ((uint64_t)p.anchor_object * p.w.n + inst) * 12;
-    M34 P, rel;
+    M34 P;
 #pragma unroll
     for (int k = 0; k < 12; ++k) P.m[k] = pp[k];
     mul34(inv, P, rel);
-    x = rel.m[3];
-    y = rel.m[7];
-    yaw = atan2(rel.m[4], rel.m[0]);
   };
+  auto yaw_of = [](const M34& rel) { return sbm::atan2_cr(rel.m[4], rel.m[0]); };  // transform.hpp:77
   if (p.from_s0) {  // canonical region_for(0) from the exchanged instance-0 state
     if (warp == 0) {
       const RegionStats r = warp_region(p.pl, p.s0[0], p.s0[1], p.s0[2], p.tris, p.cum, p.cap, sc);
@@ -368,21 +374,31 @@ __global__ void __launch_bounds__(kRB) k_relation_regions(RelationRegionParams p
     }
     return;
   }
-  double x0, y0, yaw0;
+  double x0, y0;
+  M34 rel0;
   if (p.owns_instance0) {
-    state(0, x0, y0, yaw0);
+    rel_of(0, rel0);
+    x0 = rel0.m[3];
+    y0 = rel0.m[7];
   } else {
     x0 = p.s0[0];
     y0 = p.s0[1];
-    yaw0 = p.s0[2];
   }
   bool vary = false;
   int worst = 0;
   for (uint64_t i = warp; i < p.w.n; i += nwarps) {
-    double ax, ay, ayaw;
-    state(i, ax, ay, ayaw);
+    M34 rel;
+    rel_of(i, rel);
+    const double ax = rel.m[3], ay = rel.m[7];
     const double dx = ax - x0, dy = ay - y0;
-    vary = vary || sqrt(dx * dx + dy * dy) > 1e-12 || fabs(ayaw - yaw0) > 1e-12;
+    const bool pos_vary = sqrt(dx * dx + dy * dy) > 1e-12;
+    double ayaw = 0.0;
+    if (yaw_used || !pos_vary) ayaw = yaw_of(rel);
+    if (!pos_vary) {
+      const double yaw0 = p.owns_instance0 ? yaw_of(rel0) : p.s0[2];
+      vary = vary || fabs(ayaw - yaw0) > 1e-12;
+    }
+    vary = vary || pos_vary;
     const RegionStats r = warp_region(p.pl, ax, ay, ayaw, p.tris + i * p.cap, p.cum + i * p.cap,
                                       p.cap, sc);
     if (lane == 0) {

@@ -1125,6 +1125,20 @@ sb_status sb_engine_download(sb_engine* e, sb_result* out) {
 sb_world* sb_engine_world(sb_engine* e) { return e->world.get(); }
 uint64_t sb_engine_local_instances(const sb_engine* e) { return e->n; }
 uint64_t sb_engine_last_launches(const sb_engine* e) { return e->last_launches; }
+sb_status sb_device_math(int fn, const double* in, uint64_t n, double* out) {
+  return guard([&] {
+    if (fn < 0 || fn > 2) throw std::invalid_argument("sb_device_math: fn must be 0, 1 or 2");
+    current_device_checked(0);
+    const uint64_t nin = fn == 2 ? 2 * n : n;
+    DevArray<double> din, dout;
+    din.alloc(nin);
+    dout.alloc(n);
+    cuda_check(cudaMemcpy(din.p, in, nin * sizeof(double), cudaMemcpyHostToDevice), "H2D");
+    sbk::debug_math(fn, din.p, n, dout.p, nullptr);
+    cuda_check(cudaMemcpy(out, dout.p, n * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+  });
+}
+
 sb_status sb_engine_phase_profile(const sb_engine* e, double out[8]) {
   return guard([&] {
     for (int k = 0; k < 8; ++k) out[k] = e->last_prof[k];

@@ -231,11 +231,10 @@ def test_generate_relations_variants(gpu, ref):
     assert_same(gpu, got, want)
 
 
-@pytest.mark.xfail(reason="local-frame / vector directions put the arc count "
-                          "ceil(2*theta/step) on an integer boundary, so it depends on the last "
-                          "bit of libm atan2/sin/cos (device vs glibc); see DESIGN.md libm",
-                   strict=False)
 def test_generate_relations_local_vector(gpu, ref):
+    """Local-frame vector direction: the arc count ceil(2*theta/step) sits on an integer
+    boundary, so it depends on the last bit of atan2 / sin / cos -- passes because the
+    device libm is correctly rounded like glibc (sb_crmath.cuh)."""
     eng, got, want = run_generate_pair(gpu, ref, _variant_scene(gpu, True), seed=3)
     assert_same(gpu, got, want)
 
