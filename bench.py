@@ -41,6 +41,10 @@ WORKLOADS = {
                    lambda n: __import__("paper_2512_16896_b200.scenes", fromlist=["x"]).kitchen(n), 65536),
     "c4_clutter": ("dense clutter: 100 32-sphere-set objects on one table, 262144 variations/GPU",
                    lambda n: __import__("paper_2512_16896_b200.scenes", fromlist=["x"]).dense_clutter(n), 262144),
+    "c5_sweep100": ("scale sweep point: 100 cuboids, 1048576 variations/GPU",
+                    lambda n: __import__("paper_2512_16896_b200.scenes", fromlist=["x"]).scale_sweep(n, 100), 1 << 20),
+    "c5_sweep10": ("scale sweep point: 10 cuboids, 1048576 variations/GPU",
+                   lambda n: __import__("paper_2512_16896_b200.scenes", fromlist=["x"]).scale_sweep(n, 10), 1 << 20),
 }
 
 

@@ -350,59 +350,16 @@ struct CheckCounters {
   uint32_t nodes;   // BVH node-pair box tests
 };
 
-// One candidate of CollisionWorld::check_batch (collision.cpp:433-449): candidate box,
-// inverse pose, then every enabled object in ascending id order, AABB broad phase, BVH
-// narrow phase; returns the first colliding object or -1.
-__device__ __forceinline__ int check_candidate(const WorldView& w, int32_t geom, const M34& pose,
-                                               uint64_t inst, CheckCounters& cnt) {
-  const SbGeom g = w.geoms[geom];
-  double cmn[3], cmx[3];
-  xform_aabb(pose, g.box_c, g.box_h, cmn, cmx);
-  M34 inv;
-  inverse_rigid(pose, inv);
-  const SbNode* nA = w.nodes + g.node_offset;
-  const SbTri* tA = w.tris + g.tri_offset;
-  for (int ob0 = 0; ob0 < w.n_objects; ob0 += 32) {
-    uint32_t bits = w.enabled[(uint64_t)(ob0 >> 5) * w.n + inst];
-    while (bits) {
-      const int ob = ob0 + __ffs(bits) - 1;
-      bits &= bits - 1u;
-      ++cnt.broad;
-      const double2* bp = reinterpret_cast<const double2*>(w.box + ((uint64_t)ob * w.n + inst) * 6);
-      double2 b0 = bp[0], b1 = bp[1], b2 = bp[2];
-      double omn[3] = {b0.x, b0.y, b1.x}, omx[3] = {b1.y, b2.x, b2.y};
-      if (!overlaps(cmn, cmx, omn, omx)) continue;
-      ++cnt.narrow;
-      const double2* pp =
-          reinterpret_cast<const double2*>(w.pose + ((uint64_t)ob * w.n + inst) * 12);
-      M34 P;
-#pragma unroll
-      for (int k = 0; k < 6; ++k) {
-        double2 v = pp[k];
-        P.m[2 * k] = v.x;
-        P.m[2 * k + 1] = v.y;
-      }
-      M34 rel;
-      mul34(inv, P, rel);
-      const SbGeom gb = w.geoms[w.obj_geom[ob]];
-      if (collide(nA, g.n_nodes, w.nodes + gb.node_offset, tA, w.tris + gb.tri_offset, rel,
-                  cnt.nodes, cnt.pairs))
-        return ob;
-    }
-  }
-  return -1;
-}
-
 // Store an accepted pose: record + world box (update_transform, collision.cpp:408-412).
 __device__ __forceinline__ void store_pose(const WorldView& w, int32_t obj, uint64_t inst,
                                            const M34& P) {
-  double2* pp = reinterpret_cast<double2*>(w.pose + ((uint64_t)obj * w.n + inst) * 12);
+  double2* pp = reinterpret_cast<double2*>(w.pose + sb_pose_off(w, obj, inst));
 #pragma unroll
   for (int k = 0; k < 6; ++k) pp[k] = make_double2(P.m[2 * k], P.m[2 * k + 1]);
   const SbGeom g = w.geoms[w.obj_geom[obj]];
   double mn[3], mx[3];
   xform_aabb(P, g.box_c, g.box_h, mn, mx);
-  double2* bp = reinterpret_cast<double2*>(w.box + ((uint64_t)obj * w.n + inst) * 6);
+  double2* bp = reinterpret_cast<double2*>(w.box + sb_box_off(w, obj, inst));
   bp[0] = make_double2(mn[0], mn[1]);
   bp[1] = make_double2(mn[2], mx[0]);
   bp[2] = make_double2(mx[1], mx[2]);

@@ -40,14 +40,14 @@ __device__ __forceinline__ void identity34(M34& P) {
 __device__ __forceinline__ void store_identity(const WorldView& w, int32_t obj, uint64_t i) {
   M34 P;
   identity34(P);
-  double2* pp = reinterpret_cast<double2*>(w.pose + ((uint64_t)obj * w.n + i) * 12);
+  double2* pp = reinterpret_cast<double2*>(w.pose + sb_pose_off(w, obj, i));
 #pragma unroll
   for (int k = 0; k < 6; ++k) pp[k] = make_double2(P.m[2 * k], P.m[2 * k + 1]);
 }
 
 __device__ __forceinline__ void store_local_box(const WorldView& w, int32_t obj, uint64_t i) {
   const SbGeom g = w.geoms[w.obj_geom[obj]];
-  double2* bp = reinterpret_cast<double2*>(w.box + ((uint64_t)obj * w.n + i) * 6);
+  double2* bp = reinterpret_cast<double2*>(w.box + sb_box_off(w, obj, i));
   bp[0] = make_double2(g.box_min[0], g.box_min[1]);
   bp[1] = make_double2(g.box_min[2], g.box_max[0]);
   bp[2] = make_double2(g.box_max[1], g.box_max[2]);
@@ -59,7 +59,7 @@ __global__ void k_init_object(WorldView w, int32_t obj) {
   if (i >= w.n) return;
   store_identity(w, obj, i);
   store_local_box(w, obj, i);
-  w.enabled[(uint64_t)(obj >> 5) * w.n + i] &= ~(1u << (obj & 31));
+  w.enabled[sb_word_off(w, obj >> 5, i)] &= ~(1u << (obj & 31));
 }
 
 // set_enabled (collision.cpp:386-389); atomics because `instances` may repeat.
@@ -67,7 +67,7 @@ __global__ void k_set_enabled_list(WorldView w, int32_t obj, const uint32_t* ins
                                    int enabled) {
   uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (j >= n) return;
-  uint32_t* word = w.enabled + (uint64_t)(obj >> 5) * w.n + inst[j];
+  uint32_t* word = w.enabled + sb_word_off(w, obj >> 5, inst[j]);
   uint32_t bit = 1u << (obj & 31);
   if (enabled) atomicOr(word, bit);
   else atomicAnd(word, ~bit);
@@ -76,7 +76,7 @@ __global__ void k_set_enabled_list(WorldView w, int32_t obj, const uint32_t* ins
 __global__ void k_set_enabled_all(WorldView w, int32_t obj, int enabled) {
   uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i >= w.n) return;
-  uint32_t* word = w.enabled + (uint64_t)(obj >> 5) * w.n + i;
+  uint32_t* word = w.enabled + sb_word_off(w, obj >> 5, i);
   uint32_t bit = 1u << (obj & 31);
   *word = enabled ? (*word | bit) : (*word & ~bit);
 }
@@ -133,7 +133,7 @@ __global__ void k_engine_reset(WorldView w, int32_t first_obj, int32_t n_obj, ui
     uint32_t clear = 0u;
     for (int32_t o = first_obj; o < first_obj + n_obj; ++o)
       if ((o >> 5) == wd) clear |= 1u << (o & 31);
-    if (clear) w.enabled[(uint64_t)wd * w.n + i] &= ~clear;
+    if (clear) w.enabled[sb_word_off(w, wd, i)] &= ~clear;
   }
   valid[i] = 1;
   for (int32_t p = 0; p < n_place; ++p) accepted[(uint64_t)p * w.n + i] = -1;
@@ -144,7 +144,7 @@ __global__ void k_engine_reset(WorldView w, int32_t first_obj, int32_t n_obj, ui
 __global__ void k_anchor_states(WorldView w, int32_t anchor_obj, M34 inv_support, double* out) {
   uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i >= w.n) return;
-  const double* pp = w.pose + ((uint64_t)anchor_obj * w.n + i) * 12;
+  const double* pp = w.pose + sb_pose_off(w, anchor_obj, i);
   M34 P, rel;
 #pragma unroll
   for (int k = 0; k < 12; ++k) P.m[k] = pp[k];
@@ -157,7 +157,7 @@ __global__ void k_anchor_states(WorldView w, int32_t anchor_obj, M34 inv_support
 __global__ void k_pose_colmajor(WorldView w, int32_t obj, double* out16) {
   uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i >= w.n) return;
-  const double* pp = w.pose + ((uint64_t)obj * w.n + i) * 12;
+  const double* pp = w.pose + sb_pose_off(w, obj, i);
   double* o = out16 + 16 * i;
 #pragma unroll
   for (int r = 0; r < 3; ++r)

@@ -51,18 +51,38 @@ struct SbPlacementDev {
 };
 
 // Device view of a collision world (plain pointers; built by the host World class).
+// Per-instance state is INSTANCE-major: one instance's objects are contiguous, so a warp
+// checking one candidate against its placed objects (lanes over objects) reads one
+// contiguous burst (32 boxes = 1.5 KB), and accepting writes one record.
 struct SbWorldView {
   uint64_t n;                // instances held on this device
   int32_t n_objects;
-  int32_t n_words;           // enable-bit words per instance = ceil(n_objects / 32)
+  int32_t n_words;           // enable-bit words in use = ceil(n_objects / 32)
+  int32_t obj_stride;        // object capacity per instance (record stride)
+  int32_t word_stride;       // enable-word capacity per instance
   const int32_t* obj_geom;   // [n_objects]
-  double* pose;              // [object][n][12]  row-major 3x4 [R | t]
-  double* box;               // [object][n][6]   world AABB min xyz, max xyz
-  uint32_t* enabled;         // [word][n]        bit (object & 31) of word (object >> 5)
+  double* pose;              // [n][obj_stride][12]  row-major 3x4 [R | t]
+  double* box;               // [n][obj_stride][6]   world AABB min xyz, max xyz
+  uint32_t* enabled;         // [n][word_stride]     bit (object & 31) of word (object >> 5)
   const SbGeom* geoms;
   const SbNode* nodes;
   const SbTri* tris;
 };
+
+#ifdef __CUDACC__
+#define SB_HDI __host__ __device__ __forceinline__
+#else
+#define SB_HDI inline
+#endif
+SB_HDI uint64_t sb_pose_off(const SbWorldView& w, int32_t ob, uint64_t inst) {
+  return (inst * (uint64_t)w.obj_stride + (uint64_t)ob) * 12u;
+}
+SB_HDI uint64_t sb_box_off(const SbWorldView& w, int32_t ob, uint64_t inst) {
+  return (inst * (uint64_t)w.obj_stride + (uint64_t)ob) * 6u;
+}
+SB_HDI uint64_t sb_word_off(const SbWorldView& w, int32_t word, uint64_t inst) {
+  return inst * (uint64_t)w.word_stride + (uint64_t)word;
+}
 
 #define SB_MAX_NODES_PER_GEOM 32   // effective DAG nodes (bitmask traversal width)
 #define SB_MAX_EFF_TRIS 32         // reachable triangles per geometry (pooled narrow phase)

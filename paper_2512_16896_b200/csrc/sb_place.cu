@@ -27,8 +27,17 @@ constexpr uint8_t kSlotVoid = 0, kSlotChecked = 1, kSlotUnplaceable = 2;
 
 enum Ctrl { kM = 0, kPairs = 1, kRounds = 2, kErr = 3, kCur = 4 };
 
+// Phase A tile (one slot per thread) and phase B warp scratch share the same bytes.
+struct TileA {
+  double box[kB][6];   // candidate world AABB per slot of the tile
+  uint32_t inst[kB];
+  uint8_t ok[kB];      // slot holds a placeable candidate
+};
 struct Shared {
-  WarpScratch ws[kWarps];
+  union {
+    WarpScratch ws[kWarps];
+    TileA ta;
+  } u;
   GeomCache gc;
 };
 
@@ -140,130 +149,171 @@ __device__ void compact_scatter(const PlaceParams& p, uint64_t m, Flag flag, Src
 }
 
 // ------------------------------------------------------------------ phase A
-// Warp per virtual slot v = e * W + s (instance act[e], attempt `attempt + s`):
-// sample -> yaw -> compose -> candidate box / inverse -> broad phase -> pair queue.
+// Tiles of kB virtual slots per block; slot v = e * W + s is instance act[e] at attempt
+// `attempt + s`.
+// A1 (thread per slot): sample -> yaw -> compose -> candidate AABB + inverse; pose and
+//    inverse to global, AABB to shared memory.
+// A2 (thread per (slot, object) item): AABB broad phase (collision.cpp:439-443) over the
+//    enabled objects; consecutive threads read consecutive object records of one instance
+//    (instance-major layout), so the loads are contiguous and independent. Overlaps set
+//    the slot's ovmask bit and append (slot, object) to the pair queue.
 __device__ void phase_a(const PlaceParams& p, const Sampling& S, const SbGeom& gA,
-                        const uint32_t* act, uint64_t m, int W, uint64_t draw_base,
-                        int32_t attempt, Local& L) {
+                        Shared& sh, const uint32_t* act, uint64_t m, int W,
+                        uint64_t draw_base, int32_t attempt, Local& L) {
   const int lane = threadIdx.x & 31;
-  const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
   const SbPlacementDev& pl = p.pl;
   const WorldView& w = p.w;
+  TileA& ta = sh.u.ta;
   const uint64_t nslots = m * (uint64_t)W;
-  for (uint64_t v = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); v < nslots; v += nwarps) {
-    const uint64_t e = v / W;
-    const int32_t at = attempt + (int32_t)(v - e * W);
-    const uint32_t inst = act[e];
-    const uint64_t gid = p.global_begin + inst;
-    bool placeable = true;
-    double lx = 0.0, ly = 0.0;
-    if (S.fast) {
-      if (S.n == 0) {
-        placeable = false;
-      } else {
-        Pcg r{p.fast_state0};
-        r.advance(6ull * (draw_base + e));  // j-th drained point = j-th draw (sampler.cpp:30-43)
-        double u = r.next_double(), r1 = r.next_double(), r2 = r.next_double();
-        sbp::draw_point(S.tris, S.cum, S.n, u, r1, r2, lx, ly);
-      }
-    } else {
-      const int nt = p.inst_n[inst];
-      if (nt == 0) {
-        placeable = false;
-      } else {  // make_stream(run_seed, {salt, "fall", inst, attempt}) (sampler.cpp:117)
-        Pcg r = Pcg::seeded(stream_seed4(p.run_seed, pl.salt, kFallbackSalt, gid,
-                                         static_cast<uint64_t>(at)));
-        double u = r.next_double(), r1 = r.next_double(), r2 = r.next_double();
-        const uint64_t off = (uint64_t)inst * p.inst_cap;
-        sbp::draw_point(p.inst_tris + off, p.inst_cum + off, nt, u, r1, r2, lx, ly);
-      }
-    }
-    if (!placeable) {
-      if (lane == 0) {
-        p.cflag[v] = kSlotUnplaceable;
-        p.contact[v] = kFree;
-      }
-      continue;
-    }
-    M34 S;
-#pragma unroll
-    for (int k = 0; k < 12; ++k) S.m[k] = pl.support[k];
-    double px, py, pz;
-    xform(S, lx, ly, 0.0, px, py, pz);  // transform_point(support_world, (x, y, 0))
-    double yaw = 0.0;
-    if (pl.orientation == SB_ORIENT_UNIFORM_YAW) {  // sampler.cpp:140-141
-      Pcg r = Pcg::seeded(
-          stream_seed4(p.run_seed, pl.salt, kYawSalt, gid, static_cast<uint64_t>(at)));
-      const double two_pi = 2.0 * 3.14159265358979323846;
-      yaw = 0.0 + (two_pi - 0.0) * r.next_double();
-    } else if (pl.orientation == SB_ORIENT_FACE_TO) {  // relationships.cpp:232-239
-      const double* tp = w.pose + ((uint64_t)pl.face_object * w.n + inst) * 12;
-      double dx = tp[3] - px, dy = tp[7] - py;
-      yaw = sqrt(dx * dx + dy * dy) < 1e-12 ? 0.0 : sbm::atan2_cr(dy, dx);
-    }
-    double c, s;
-    sbm::sincos_cr(yaw, &s, &c);  // rotation_z: std::cos / std::sin (transform.hpp:47)
-    M34 T, Rz, pose;  // translation(p + z_off z) * rotation_z(yaw)
-#pragma unroll
-    for (int k = 0; k < 12; ++k) T.m[k] = Rz.m[k] = 0.0;
-    T.m[0] = T.m[5] = T.m[10] = 1.0;
-    Rz.m[10] = 1.0;
-    T.m[3] = px + 0.0;
-    T.m[7] = py + 0.0;
-    T.m[11] = pz + pl.z_off;
-    Rz.m[0] = c;
-    Rz.m[1] = -s;
-    Rz.m[4] = s;
-    Rz.m[5] = c;
-    mul34(T, Rz, pose);
-    double cmn[3], cmx[3];
-    xform_aabb(pose, gA.box_c, gA.box_h, cmn, cmx);
-    M34 inv;
-    inverse_rigid(pose, inv);
-    if (lane < 12) {
-      double pv = 0.0, iv = 0.0;
-#pragma unroll
-      for (int k = 0; k < 12; ++k)
-        if (lane == k) {
-          pv = pose.m[k];
-          iv = inv.m[k];
+  const int nobj = w.n_objects;
+  // tile size: kB slots, or fewer so that small rounds still spread over every block
+  uint64_t T = (nslots + gridDim.x - 1) / gridDim.x;
+  T = T < 32 ? 32 : ((T + 31) / 32) * 32;
+  if (T > (uint64_t)kB) T = kB;
+  for (uint64_t t0 = (uint64_t)blockIdx.x * T; t0 < nslots; t0 += (uint64_t)gridDim.x * T) {
+    // ---------------- A1
+    const uint64_t v = t0 + threadIdx.x;
+    bool ok = false;
+    uint32_t inst = 0;
+    if (threadIdx.x < T && v < nslots) {
+      const uint64_t e = v / W;
+      const int32_t at = attempt + (int32_t)(v - e * W);
+      inst = act[e];
+      const uint64_t gid = p.global_begin + inst;
+      bool placeable = true;
+      double lx = 0.0, ly = 0.0;
+      if (S.fast) {
+        if (S.n == 0) {
+          placeable = false;
+        } else {
+          Pcg r{p.fast_state0};
+          r.advance(6ull * (draw_base + e));  // j-th drained point = j-th draw (sampler.cpp:30-43)
+          double u = r.next_double(), r1 = r.next_double(), r2 = r.next_double();
+          sbp::draw_point(S.tris, S.cum, S.n, u, r1, r2, lx, ly);
         }
-      p.cpose[v * 12 + lane] = pv;
-      p.cinv[v * 12 + lane] = iv;
-    }
-    if (lane == 0) {
-      p.cflag[v] = kSlotChecked;
+      } else {
+        const int nt = p.inst_n[inst];
+        if (nt == 0) {
+          placeable = false;
+        } else {  // make_stream(run_seed, {salt, "fall", inst, attempt}) (sampler.cpp:117)
+          Pcg r = Pcg::seeded(stream_seed4(p.run_seed, pl.salt, kFallbackSalt, gid,
+                                           static_cast<uint64_t>(at)));
+          double u = r.next_double(), r1 = r.next_double(), r2 = r.next_double();
+          const uint64_t off = (uint64_t)inst * p.inst_cap;
+          sbp::draw_point(p.inst_tris + off, p.inst_cum + off, nt, u, r1, r2, lx, ly);
+        }
+      }
       p.contact[v] = kFree;
+      for (int wd = 0; wd < w.n_words; ++wd) p.ovmask[(uint64_t)wd * p.slot_cap + v] = 0u;
+      if (!placeable) {
+        p.cflag[v] = kSlotUnplaceable;
+      } else {
+        M34 Sp;
+#pragma unroll
+        for (int k = 0; k < 12; ++k) Sp.m[k] = pl.support[k];
+        double px, py, pz;
+        xform(Sp, lx, ly, 0.0, px, py, pz);  // transform_point(support_world, (x, y, 0))
+        double yaw = 0.0;
+        if (pl.orientation == SB_ORIENT_UNIFORM_YAW) {  // sampler.cpp:140-141
+          Pcg r = Pcg::seeded(
+              stream_seed4(p.run_seed, pl.salt, kYawSalt, gid, static_cast<uint64_t>(at)));
+          const double two_pi = 2.0 * 3.14159265358979323846;
+          yaw = 0.0 + (two_pi - 0.0) * r.next_double();
+        } else if (pl.orientation == SB_ORIENT_FACE_TO) {  // relationships.cpp:232-239
+          const double* tp = w.pose + sb_pose_off(w, pl.face_object, inst);
+          double dx = tp[3] - px, dy = tp[7] - py;
+          yaw = sqrt(dx * dx + dy * dy) < 1e-12 ? 0.0 : sbm::atan2_cr(dy, dx);
+        }
+        double c, s;
+        sbm::sincos_cr(yaw, &s, &c);  // rotation_z: std::cos / std::sin (transform.hpp:47)
+        M34 T, Rz, pose;  // translation(p + z_off z) * rotation_z(yaw)
+#pragma unroll
+        for (int k = 0; k < 12; ++k) T.m[k] = Rz.m[k] = 0.0;
+        T.m[0] = T.m[5] = T.m[10] = 1.0;
+        Rz.m[10] = 1.0;
+        T.m[3] = px + 0.0;
+        T.m[7] = py + 0.0;
+        T.m[11] = pz + pl.z_off;
+        Rz.m[0] = c;
+        Rz.m[1] = -s;
+        Rz.m[4] = s;
+        Rz.m[5] = c;
+        mul34(T, Rz, pose);
+        double cmn[3], cmx[3];
+        xform_aabb(pose, gA.box_c, gA.box_h, cmn, cmx);
+        M34 inv;
+        inverse_rigid(pose, inv);
+        double2* cp = reinterpret_cast<double2*>(p.cpose + v * 12);
+        double2* ci = reinterpret_cast<double2*>(p.cinv + v * 12);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+          cp[k] = make_double2(pose.m[2 * k], pose.m[2 * k + 1]);
+          ci[k] = make_double2(inv.m[2 * k], inv.m[2 * k + 1]);
+        }
+        p.cflag[v] = kSlotChecked;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          ta.box[threadIdx.x][k] = cmn[k];
+          ta.box[threadIdx.x][3 + k] = cmx[k];
+        }
+        ok = true;
+      }
     }
-    // broad phase (collision.cpp:439-443): lanes over objects, ascending chunks of 32
-    for (int ob0 = 0; ob0 < w.n_objects; ob0 += 32) {
-      const int ob = ob0 + lane;
-      const uint32_t bits = w.enabled[(uint64_t)(ob0 >> 5) * w.n + inst];
-      const bool en = ob < w.n_objects && ((bits >> lane) & 1u);
-      bool ov = false;
-      if (en) {
-        const double2* bp =
-            reinterpret_cast<const double2*>(w.box + ((uint64_t)ob * w.n + inst) * 6);
-        double2 b0 = bp[0], b1 = bp[1], b2 = bp[2];
-        double omn[3] = {b0.x, b0.y, b1.x}, omx[3] = {b1.y, b2.x, b2.y};
-        ov = overlaps(cmn, cmx, omn, omx);
+    ta.inst[threadIdx.x] = inst;
+    ta.ok[threadIdx.x] = ok ? 1 : 0;
+    __syncthreads();
+    // ---------------- A2 (4 items per thread in flight: loads first, then ballots)
+    const uint64_t tile_n = (nslots - t0) < T ? (nslots - t0) : T;
+    const uint64_t items = tile_n * (uint64_t)nobj;
+    constexpr int U = 4;
+    for (uint64_t it0 = 0; it0 < items; it0 += (uint64_t)kB * U) {
+      bool ov[U];
+      uint32_t tt[U];
+      int obs[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint64_t it = it0 + (uint64_t)u * kB + threadIdx.x;
+        ov[u] = false;
+        tt[u] = 0;
+        obs[u] = 0;
+        if (it < items) {
+          const uint32_t t = (uint32_t)(it / nobj);
+          const int ob = (int)(it - (uint64_t)t * nobj);
+          tt[u] = t;
+          obs[u] = ob;
+          if (ta.ok[t]) {
+            const uint32_t in = ta.inst[t];
+            const uint32_t bits = w.enabled[sb_word_off(w, ob >> 5, in)];
+            if ((bits >> (ob & 31)) & 1u) {
+              ++L.cnt.broad;
+              const double2* bp =
+                  reinterpret_cast<const double2*>(w.box + sb_box_off(w, ob, in));
+              const double2 b0 = bp[0], b1 = bp[1], b2 = bp[2];
+              const double* cb = ta.box[t];
+              ov[u] = cb[0] <= b1.y && b0.x <= cb[3] && cb[1] <= b2.x && b0.y <= cb[4] &&
+                      cb[2] <= b2.y && b1.x <= cb[5];
+            }
+          }
+        }
       }
-      const uint32_t mask = __ballot_sync(kFull, ov);
-      if (lane == 0) {
-        p.ovmask[(uint64_t)(ob0 >> 5) * p.slot_cap + v] = mask;
-        L.cnt.broad += __popc(bits);
-      }
-      if (mask) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t mask = __ballot_sync(kFull, ov[u]);
+        if (!mask) continue;
         uint32_t base = 0;
         if (lane == 0) base = atomicAdd(p.ctrl + kPairs, (uint32_t)__popc(mask));
         base = __shfl_sync(kFull, base, 0);
-        if (ov) {
+        if (ov[u]) {
+          const uint64_t vv = t0 + tt[u];
+          const int ob = obs[u];
+          atomicOr(p.ovmask + (uint64_t)(ob >> 5) * p.slot_cap + vv, 1u << (ob & 31));
           const uint64_t idx = base + __popc(mask & ((1u << lane) - 1u));
-          if (idx < p.pair_cap) p.pairs[idx] = (v << 32) | (uint32_t)ob;
+          if (idx < p.pair_cap) p.pairs[idx] = (vv << 32) | (uint32_t)ob;
           else atomicOr(p.ctrl + kErr, 1u);
         }
       }
     }
+    __syncthreads();  // tile buffers are reused by the next tile
   }
 }
 
@@ -274,7 +324,7 @@ __device__ void phase_b(const PlaceParams& p, Shared& sh, const uint32_t* act, i
   const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
   uint64_t np = __ldcg(p.ctrl + kPairs);
   if (np > p.pair_cap) np = p.pair_cap;
-  WarpScratch& ws = sh.ws[threadIdx.x >> 5];
+  WarpScratch& ws = sh.u.ws[threadIdx.x >> 5];
   for (uint64_t q = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); q < np; q += nwarps) {
     const uint64_t pr = p.pairs[q];
     const uint64_t v = pr >> 32;
@@ -317,7 +367,7 @@ __device__ void phase_c(const PlaceParams& p, const uint32_t* act, uint64_t m, i
 #pragma unroll
         for (int k = 0; k < 12; ++k) P.m[k] = p.cpose[v * 12 + k];
         store_pose(w, p.pl.object, inst, P);
-        w.enabled[(uint64_t)(p.pl.object >> 5) * w.n + inst] |= 1u << (p.pl.object & 31);
+        w.enabled[sb_word_off(w, p.pl.object >> 5, inst)] |= 1u << (p.pl.object & 31);
         p.accepted[inst] = (int16_t)(attempt + s);
         ++L.accepted;
         ok = true;
@@ -384,7 +434,7 @@ __global__ void __launch_bounds__(kB) k_place(PlaceParams p) {
     if (m == 0) break;
     const int W = spec_width(p, S.fast, m, a);
     const uint32_t* act = act_list(p, cur);
-    phase_a(p, S, gA, act, m, W, draws, a, L);
+    phase_a(p, S, gA, sh, act, m, W, draws, a, L);
     grid.sync();
     clk.lap(1);
     phase_b(p, sh, act, W, L);
@@ -421,9 +471,10 @@ __global__ void __launch_bounds__(kB) k_init_scatter(PlaceParams p) {
 __global__ void __launch_bounds__(kB) k_phase_a(PlaceParams p, int32_t attempt, int cur) {
   SbGeom gA = p.w.geoms[p.pl.geom];
   const uint64_t m = __ldcg(p.ctrl + kM);
+  __shared__ Shared sh;
   Local L;
   const Sampling S = resolve_sampling(p);
-  phase_a(p, S, gA, act_list(p, cur), m, p.spec_width, p.draw_base, attempt, L);
+  phase_a(p, S, gA, sh, act_list(p, cur), m, p.spec_width, p.draw_base, attempt, L);
   flush(p, L);
 }
 __global__ void __launch_bounds__(kB) k_phase_b(PlaceParams p, int cur) {

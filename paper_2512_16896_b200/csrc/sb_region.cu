@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(kRB) k_relation_regions(RelationRegionParams p
   // the positions agree (relationships.cpp:180-181), so atan2 is skipped otherwise.
   const bool yaw_used = p.pl.direction != SB_DIR_NONE && p.pl.frame == SB_FRAME_LOCAL;
   auto rel_of = [&](uint64_t inst, M34& rel) {
-    const double* pp = p.w.pose + ((uint64_t)p.anchor_object * p.w.n + inst) * 12;
+    const double* pp = p.w.pose + sb_pose_off(p.w, p.anchor_object, inst);
     M34 P;
 #pragma unroll
     for (int k = 0; k < 12; ++k) P.m[k] = pp[k];

@@ -182,6 +182,8 @@ struct sb_world {
     v.n = n;
     v.n_objects = static_cast<int32_t>(obj_geom.size());
     v.n_words = (v.n_objects + 31) / 32;
+    v.obj_stride = cap_objects;
+    v.word_stride = cap_words;
     v.obj_geom = d_obj_geom.p;
     v.pose = d_pose.p;
     v.box = d_box.p;
@@ -267,10 +269,13 @@ struct sb_world {
     nb.alloc(static_cast<size_t>(cap) * n * 6);
     ne.alloc(static_cast<size_t>(words) * n);
     cuda_check(cudaMemset(ne.p, 0, ne.count * sizeof(uint32_t)), "memset enabled");
-    if (cap_objects > 0) {
-      cuda_check(cudaMemcpy(np.p, d_pose.p, sizeof(double) * cap_objects * n * 12, cudaMemcpyDeviceToDevice), "D2D");
-      cuda_check(cudaMemcpy(nb.p, d_box.p, sizeof(double) * cap_objects * n * 6, cudaMemcpyDeviceToDevice), "D2D");
-      cuda_check(cudaMemcpy(ne.p, d_enabled.p, sizeof(uint32_t) * cap_words * n, cudaMemcpyDeviceToDevice), "D2D");
+    if (cap_objects > 0) {  // instance-major records: re-pitch every instance row
+      cuda_check(cudaMemcpy2D(np.p, sizeof(double) * 12 * cap, d_pose.p, sizeof(double) * 12 * cap_objects,
+                              sizeof(double) * 12 * cap_objects, n, cudaMemcpyDeviceToDevice), "D2D pose");
+      cuda_check(cudaMemcpy2D(nb.p, sizeof(double) * 6 * cap, d_box.p, sizeof(double) * 6 * cap_objects,
+                              sizeof(double) * 6 * cap_objects, n, cudaMemcpyDeviceToDevice), "D2D box");
+      cuda_check(cudaMemcpy2D(ne.p, sizeof(uint32_t) * words, d_enabled.p, sizeof(uint32_t) * cap_words,
+                              sizeof(uint32_t) * cap_words, n, cudaMemcpyDeviceToDevice), "D2D enabled");
     }
     std::swap(d_pose.p, np.p);
     std::swap(d_pose.count, np.count);
@@ -338,7 +343,7 @@ struct sb_world {
     instance_check(inst);
     activate();
     double rec[12];
-    cuda_check(cudaMemcpyAsync(rec, d_pose.p + (static_cast<size_t>(obj) * n + inst) * 12, sizeof rec, cudaMemcpyDeviceToHost, stream), "D2H");
+    cuda_check(cudaMemcpyAsync(rec, d_pose.p + sb_pose_off(view(), obj, inst), sizeof rec, cudaMemcpyDeviceToHost, stream), "D2H");
     cuda_check(cudaStreamSynchronize(stream), "sync");
     for (int i = 0; i < 3; ++i)
       for (int j = 0; j < 4; ++j) out16[4 * j + i] = rec[4 * i + j];
@@ -350,7 +355,7 @@ struct sb_world {
     instance_check(inst);
     activate();
     uint32_t w = 0;
-    cuda_check(cudaMemcpyAsync(&w, d_enabled.p + static_cast<size_t>(obj >> 5) * n + inst, 4, cudaMemcpyDeviceToHost, stream), "D2H");
+    cuda_check(cudaMemcpyAsync(&w, d_enabled.p + sb_word_off(view(), obj >> 5, inst), 4, cudaMemcpyDeviceToHost, stream), "D2H");
     cuda_check(cudaStreamSynchronize(stream), "sync");
     return (w >> (obj & 31)) & 1u;
   }

@@ -82,7 +82,7 @@ __device__ __forceinline__ bool warp_collide(const WorldView& w, const GeomCache
                                              WarpScratch& ws, CheckCounters& cnt) {
   const int lane = threadIdx.x & 31;
   const SbGeom gB = w.geoms[w.obj_geom[ob]];
-  const double* P = w.pose + ((uint64_t)ob * w.n + inst) * 12;
+  const double* P = w.pose + sb_pose_off(w, ob, inst);
   if (lane < 12) {  // other_in_cand = inv(cand) * pose(ob), one entry per lane (shim order)
     const int i = lane >> 2, j = lane & 3;
 
@@ -204,13 +204,13 @@ __device__ __forceinline__ int warp_check(const WorldView& w, const SbGeom& gA,
   for (int ob0 = 0; ob0 < w.n_objects; ob0 += 32) {
     uint32_t ovm = 0;
     if (!done) {
-      uint32_t bits = w.enabled[(uint64_t)(ob0 >> 5) * w.n + inst];
+      uint32_t bits = w.enabled[sb_word_off(w, ob0 >> 5, inst)];
       while (bits) {
         const int b = __ffs(bits) - 1;
         bits &= bits - 1u;
         ++cnt.broad;
         const double2* bp =
-            reinterpret_cast<const double2*>(w.box + ((uint64_t)(ob0 + b) * w.n + inst) * 6);
+            reinterpret_cast<const double2*>(w.box + sb_box_off(w, ob0 + b, inst));
         double2 b0 = bp[0], b1 = bp[1], b2 = bp[2];
         double omn[3] = {b0.x, b0.y, b1.x}, omx[3] = {b1.y, b2.x, b2.y};
         if (overlaps(cmn, cmx, omn, omx)) ovm |= 1u << b;
