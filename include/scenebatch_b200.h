@@ -267,6 +267,10 @@ sb_status sb_engine_phase_profile(const sb_engine* e, double out[8]);
  * polygon.cpp:151, relationships.cpp:184,238) on n inputs on device 0.
  * fn 0: out[i] = sin(in[i]); 1: cos(in[i]); 2: atan2(in[2i], in[2i+1]). */
 sb_status sb_device_math(int fn, const double* in, uint64_t n, double* out);
+/* Diagnostics: narrow-phase cycle breakdown accumulated since the last call (all zeros
+ * unless the library was built with -DSB_NARROW_PROF): pose+M, node tests, triangle
+ * transform, DAG walk, triangle tests, pairs. */
+sb_status sb_debug_narrow_profile(uint64_t out[8]);
 
 #ifdef __cplusplus
 }

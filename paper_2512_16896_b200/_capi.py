@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libscenebatch_b200.so")
+LIB_PATH = os.environ.get("SB_LIB_PATH", os.path.join(_HERE, "libscenebatch_b200.so"))
 
 SB_OK = 0
 SB_ERR_INVALID_ARGUMENT = 1
@@ -126,6 +126,7 @@ SIGNATURES = {
     "sb_engine_last_timing": (C.c_int, [_P, _D, _D, C.POINTER(C.c_uint64)]),
     "sb_engine_phase_profile": (C.c_int, [_P, _D]),
     "sb_device_math": (C.c_int, [C.c_int, _D, C.c_uint64, _D]),
+    "sb_debug_narrow_profile": (C.c_int, [C.POINTER(C.c_uint64)]),
 }
 
 _lib = None

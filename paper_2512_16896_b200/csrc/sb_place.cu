@@ -410,7 +410,7 @@ struct PhaseClock {
   }
 };
 
-__global__ void __launch_bounds__(kB) k_place(PlaceParams p) {
+__global__ void __launch_bounds__(kB, 2) k_place(PlaceParams p) {
   __shared__ Shared sh;
   cg::grid_group grid = cg::this_grid();
   PhaseClock clk(p.prof);
@@ -523,6 +523,14 @@ unsigned host_grid() {
 }
 
 }  // namespace
+
+void narrow_profile(unsigned long long out[8], bool reset) {
+  check(cudaMemcpyFromSymbol(out, g_nprof, 8 * sizeof(unsigned long long)), "narrow_profile");
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    check(cudaMemcpyToSymbol(g_nprof, z, sizeof z), "narrow_profile reset");
+  }
+}
 
 int place_grid_warps(int num_sms) {
   if (g_coop_blocks < 0) {

@@ -78,6 +78,8 @@ constexpr int kPlaceBlock = 256;
 bool place_persistent(const PlaceParams& p, int num_sms, sb_stream_t s);
 // Warps of the co-resident persistent grid (sizes the speculative-attempt budget).
 int place_grid_warps(int num_sms);
+// Cycle breakdown of the narrow phase (zeros unless built with -DSB_NARROW_PROF).
+void narrow_profile(unsigned long long out[8], bool reset);
 // Host loop building blocks (sharded runs): init active list, then per round
 // phase_abcd(draw_base) with the count read back in between.
 void place_init(const PlaceParams& p, sb_stream_t s);

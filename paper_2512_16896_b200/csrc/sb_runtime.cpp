@@ -1130,6 +1130,14 @@ sb_status sb_engine_download(sb_engine* e, sb_result* out) {
 sb_world* sb_engine_world(sb_engine* e) { return e->world.get(); }
 uint64_t sb_engine_local_instances(const sb_engine* e) { return e->n; }
 uint64_t sb_engine_last_launches(const sb_engine* e) { return e->last_launches; }
+sb_status sb_debug_narrow_profile(uint64_t out[8]) {
+  return guard([&] {
+    unsigned long long v[8];
+    sbk::narrow_profile(v, true);
+    for (int k = 0; k < 8; ++k) out[k] = v[k];
+  });
+}
+
 sb_status sb_device_math(int fn, const double* in, uint64_t n, double* out) {
   return guard([&] {
     if (fn < 0 || fn > 2) throw std::invalid_argument("sb_device_math: fn must be 0, 1 or 2");

@@ -25,18 +25,31 @@
 namespace sbd {
 
 constexpr unsigned kFull = 0xffffffffu;
+
+// Optional cycle breakdown of the narrow phase (build with -DSB_NARROW_PROF):
+// [0] pose load + M, [1] triangle transform + all triangle pairs, [2] node transform +
+// node-pair tests (hits only), [3] DAG walk, [4] reached-hit check, [5] pairs.
+static __device__ unsigned long long g_nprof[8];
+#ifdef SB_NARROW_PROF
+#define SB_NP_MARK(var) const long long var = clock64()
+#define SB_NP_ADD(k, a, b) \
+  if ((threadIdx.x & 31) == 0) atomicAdd(&g_nprof[k], (unsigned long long)((b) - (a)))
+#else
+#define SB_NP_MARK(var)
+#define SB_NP_ADD(k, a, b)
+#endif
 constexpr int kMaxEffTris = SB_MAX_EFF_TRIS;  // host-checked at registration
 constexpr int kMaxNodes = SB_MAX_NODES_PER_GEOM;
 
 struct WarpScratch {
   double M[12];                // other_in_self of the pair under test
   double qb[kMaxEffTris][9];   // B's effective triangles moved into A's frame
-  uint32_t pass[kMaxNodes];    // pass[a] bit b: A node a overlaps B node b (in A's frame)
-  uint32_t desc[kMaxNodes];    // desc[a] bit b: descend A at pair (a, b)
+  double bb[kMaxNodes][6];     // B's effective node boxes in A's frame
+  double e2b[kMaxNodes];       // their squared extents
+  uint32_t cm[kMaxNodes];      // B node -> mask of its effective children (0 for leaves)
   uint32_t allowed[kMaxNodes]; // allowed[a] bit b: leaf pair reached by the traversal
-  uint32_t pend[kMaxNodes];
-  int8_t c0b[kMaxNodes], c1b[kMaxNodes];
   int8_t tleafb[kMaxEffTris];
+  uint32_t hitw[kMaxEffTris * kMaxEffTris / 32];  // intersecting triangle pairs (bitset)
 };
 
 // Candidate geometry (uniform per launch), staged in shared memory once per block.
@@ -81,6 +94,7 @@ __device__ __forceinline__ bool warp_collide(const WorldView& w, const GeomCache
                                              int32_t ob, uint64_t inst, const double* I,
                                              WarpScratch& ws, CheckCounters& cnt) {
   const int lane = threadIdx.x & 31;
+  SB_NP_MARK(np0);
   const SbGeom gB = w.geoms[w.obj_geom[ob]];
   const double* P = w.pose + sb_pose_off(w, ob, inst);
   if (lane < 12) {  // other_in_cand = inv(cand) * pose(ob), one entry per lane (shim order)
@@ -96,38 +110,19 @@ __device__ __forceinline__ bool warp_collide(const WorldView& w, const GeomCache
   M34 M;
 #pragma unroll
   for (int k = 0; k < 12; ++k) M.m[k] = ws.M[k];
+  SB_NP_MARK(np1);
+  SB_NP_ADD(0, np0, np1);
 
-  // 1-2: node pair box tests and descend decisions
-  const int nA = gc.n_nodes, nB = gB.n_nodes;
-  const SbNode* nodesB = w.nodes + gB.node_offset;
-  bool lb = false;
-  double bmn[3] = {0, 0, 0}, bmx[3] = {0, 0, 0}, ext2b = 0.0;
-  if (lane < nB) {
-    const SbNode& nb = nodesB[lane];
-    xform_aabb(M, nb.c, nb.h, bmn, bmx);
-    const double e0 = bmx[0] - bmn[0], e1 = bmx[1] - bmn[1], e2 = bmx[2] - bmn[2];
-    ext2b = (e0 * e0 + e1 * e1) + e2 * e2;
-    lb = nb.child0 < 0;
-    ws.c0b[lane] = (int8_t)nb.child0;
-    ws.c1b[lane] = (int8_t)nb.child1;
-  }
-  const uint32_t leafB = __ballot_sync(kFull, lb);
-  for (int a = 0; a < nA; ++a) {
-    const bool la = (gc.leafmask >> a) & 1u;
-    const bool p = lane < nB && gc.bmin[a][0] <= bmx[0] && bmn[0] <= gc.bmax[a][0] &&
-                   gc.bmin[a][1] <= bmx[1] && bmn[1] <= gc.bmax[a][1] &&
-                   gc.bmin[a][2] <= bmx[2] && bmn[2] <= gc.bmax[a][2];
-    const bool d = lb || (!la && gc.ext2[a] >= ext2b);
-    const uint32_t pm = __ballot_sync(kFull, p);
-    const uint32_t dm = __ballot_sync(kFull, d);
-    if (lane == 0) {
-      ws.pass[a] = pm;
-      ws.desc[a] = dm;
-    }
-  }
-  // B's effective triangles into A's frame (transform_point per vertex, collision.cpp:308-310)
+  // 1: B's effective triangles into A's frame (transform_point, collision.cpp:308-310).
+  // Then, when the node-pair grid is large (deep effective DAGs, e.g. sphere sets), test
+  // every effective triangle pair first: no intersecting pair in Eff(A) x Eff(B) means the
+  // reference cannot report a hit (it only tests pairs of reachable leaves), so node tests
+  // and the DAG walk run only when some pair intersects. Small grids (box-box: 4 x 4) cull
+  // first and test only the reached leaf pairs.
   const SbTri* tB = w.tris + gB.tri_offset;
   const int nTB = gB.n_tris, nTA = gc.n_tris;
+  const int nA = gc.n_nodes, nB = gB.n_nodes;
+  const bool tri_first = nA * nB > 16;
   for (int v = lane; v < nTB * 3; v += 32) {
     const double* p = tB[v / 3].v + 3 * (v % 3);
     double* q = ws.qb[v / 3] + 3 * (v % 3);
@@ -135,52 +130,136 @@ __device__ __forceinline__ bool warp_collide(const WorldView& w, const GeomCache
   }
   for (int k = lane; k < nTB; k += 32) ws.tleafb[k] = (int8_t)tB[k].leaf;
   __syncwarp();
-
-  // 3: walk the pair DAG (lexicographic order is topological: children ids > parent ids)
-  if (lane == 0) {
-    for (int a = 0; a < nA; ++a) {
-      ws.pend[a] = 0u;
-      ws.allowed[a] = 0u;
+  const int ntp = nTA * nTB;
+  if (tri_first) {
+    bool any_hit = false;
+    for (int k0 = 0; k0 < ntp; k0 += 32) {
+      const int idx = k0 + lane;
+      bool hit = false;
+      if (idx < ntp) {
+        const int ia = idx / nTB, ib = idx - ia * nTB;
+        hit = tri_tri_intersect(gc.ta[ia], ws.qb[ib]);
+      }
+      const uint32_t hm = __ballot_sync(kFull, hit);
+      if (lane == 0) ws.hitw[k0 >> 5] = hm;
+      any_hit = any_hit || hm != 0u;
     }
-    ws.pend[0] = 1u;
-    uint32_t visited = 0;
+    if (lane == 0) cnt.pairs += ntp;
+    if (!any_hit) {
+      SB_NP_MARK(npx);
+      SB_NP_ADD(1, np1, npx);
+      return false;
+    }
+    __syncwarp();
+  }
+  SB_NP_MARK(np2);
+  SB_NP_ADD(1, np1, np2);
+
+  // 2a: lane b moves B's node b into A's frame (independent of the A node it meets)
+  const SbNode* nodesB = w.nodes + gB.node_offset;
+  bool lb = false;
+  if (lane < nB) {
+    const SbNode& nb = nodesB[lane];
+    double bmn[3], bmx[3];
+    xform_aabb(M, nb.c, nb.h, bmn, bmx);
+    const double e0 = bmx[0] - bmn[0], e1 = bmx[1] - bmn[1], e2 = bmx[2] - bmn[2];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      ws.bb[lane][c] = bmn[c];
+      ws.bb[lane][3 + c] = bmx[c];
+    }
+    ws.e2b[lane] = (e0 * e0 + e1 * e1) + e2 * e2;
+    lb = nb.child0 < 0;
+    ws.cm[lane] = lb ? 0u : ((1u << nb.child0) | (1u << nb.child1));
+  }
+  const uint32_t leafB = __ballot_sync(kFull, lb);
+  __syncwarp();
+
+  // 2: pass(a,b) = na.box.overlaps(nb_in_a) and the descend rule
+  // desc(a,b) = leaf(nb) || (!leaf(na) && ext2(na) >= ext2(nb_in_a)) for all (a, b),
+  // 32 pairs per ballot; lane a collects row a (pair k = a * nB + b).
+  uint32_t rpass = 0u, rdesc = 0u;
+  const int np = nA * nB;
+  for (int k0 = 0; k0 < np; k0 += 32) {
+    const int k = k0 + lane;
+    bool pb = false, db = false;
+    if (k < np) {
+      const int a = k / nB, bi = k - a * nB;
+      const double* bb = ws.bb[bi];
+      pb = gc.bmin[a][0] <= bb[3] && bb[0] <= gc.bmax[a][0] && gc.bmin[a][1] <= bb[4] &&
+           bb[1] <= gc.bmax[a][1] && gc.bmin[a][2] <= bb[5] && bb[2] <= gc.bmax[a][2];
+      db = ((leafB >> bi) & 1u) || (!((gc.leafmask >> a) & 1u) && gc.ext2[a] >= ws.e2b[bi]);
+    }
+    const uint32_t P = __ballot_sync(kFull, pb), D = __ballot_sync(kFull, db);
+    if (lane < nA) {
+      const int lo = lane * nB;
+      const int s0 = lo > k0 ? lo : k0;
+      const int e0 = (lo + nB) < (k0 + 32) ? (lo + nB) : (k0 + 32);
+      if (s0 < e0) {
+        const int len = e0 - s0;
+        const uint32_t mk = len >= 32 ? 0xffffffffu : ((1u << len) - 1u);
+        rpass |= ((P >> (s0 - k0)) & mk) << (s0 - lo);
+        rdesc |= ((D >> (s0 - k0)) & mk) << (s0 - lo);
+      }
+    }
+  }
+  SB_NP_MARK(np3);
+  SB_NP_ADD(2, np2, np3);
+
+  // 3: walk the pair DAG from (0,0) in lexicographic order (a topological order: every
+  // child id exceeds its parent's). Lane a owns the pending row of A node a; descending A
+  // forwards the row's bits to the lanes of A's effective children.
+  {
+    uint32_t pend = lane == 0 ? 1u : 0u, allowed = 0u;
+    const bool la = lane < nA && ((gc.leafmask >> lane) & 1u);
+    const int c0 = lane < nA ? gc.c0[lane] : -1, c1 = lane < nA ? gc.c1[lane] : -1;
+    unsigned visited = 0;
     for (int a = 0; a < nA; ++a) {
-      uint32_t pend = ws.pend[a];
-      const uint32_t pass = ws.pass[a], desc = ws.desc[a];
-      const bool la = (gc.leafmask >> a) & 1u;
-      uint32_t allowed = 0u;
-      while (pend) {
-        const int b = __ffs(pend) - 1;
-        pend &= pend - 1u;
-        ++visited;
-        if (!((pass >> b) & 1u)) continue;
-        if (la && ((leafB >> b) & 1u)) {
-          allowed |= 1u << b;
-        } else if ((desc >> b) & 1u) {
-          ws.pend[gc.c0[a]] |= 1u << b;
-          ws.pend[gc.c1[a]] |= 1u << b;
-        } else {
-          pend |= (1u << ws.c0b[b]) | (1u << ws.c1b[b]);
+      uint32_t down = 0u;
+      if (lane == a) {
+        while (pend) {
+          const int bi = __ffs(pend) - 1;
+          pend &= pend - 1u;
+          ++visited;
+          if (!((rpass >> bi) & 1u)) continue;
+          if (la && ((leafB >> bi) & 1u)) allowed |= 1u << bi;
+          else if ((rdesc >> bi) & 1u) down |= 1u << bi;
+          else pend |= ws.cm[bi];
         }
       }
-      ws.allowed[a] = allowed;
+      down = __shfl_sync(kFull, down, a);
+      const int d0 = __shfl_sync(kFull, c0, a), d1 = __shfl_sync(kFull, c1, a);
+      if (down && (lane == d0 || lane == d1)) pend |= down;
     }
+    if (lane < nA) ws.allowed[lane] = allowed;
     cnt.nodes += visited;
   }
   __syncwarp();
+  SB_NP_MARK(np4);
+  SB_NP_ADD(3, np3, np4);
 
-  // 4: triangle pairs of the reached leaf pairs
-  bool hit = false;
+  // 4: tri-first: does some intersecting pair lie in a reached leaf pair? Cull-first:
+  // test the triangle pairs of the reached leaf pairs.
+  bool ok = false;
   unsigned tests = 0;
-  for (int idx = lane; idx < nTA * nTB; idx += 32) {
+  for (int k0 = 0; k0 < ntp; k0 += 32) {
+    const int idx = k0 + lane;
+    if (idx >= ntp) continue;
     const int ia = idx / nTB, ib = idx - ia * nTB;
-    if ((ws.allowed[gc.tleaf[ia]] >> ws.tleafb[ib]) & 1u) {
+    const bool reached = (ws.allowed[gc.tleaf[ia]] >> ws.tleafb[ib]) & 1u;
+    if (tri_first) {
+      ok = ok || (reached && ((ws.hitw[k0 >> 5] >> lane) & 1u));
+    } else if (reached) {
       ++tests;
-      hit = hit || tri_tri_intersect(gc.ta[ia], ws.qb[ib]);
+      ok = ok || tri_tri_intersect(gc.ta[ia], ws.qb[ib]);
     }
   }
   cnt.pairs += tests;
-  return __any_sync(kFull, hit);
+  const bool res = __any_sync(kFull, ok);
+  SB_NP_MARK(np5);
+  SB_NP_ADD(4, np4, np5);
+  SB_NP_ADD(5, 0, 1);
+  return res;
 }
 
 // Pooled check of the warp's 32 candidates (inactive lanes pass active = false but must
