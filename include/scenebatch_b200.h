@@ -255,12 +255,13 @@ uint64_t sb_engine_last_launches(const sb_engine* e);
  * its check kernels alone (the dominant kernel; roofline numerator). */
 sb_status sb_engine_last_timing(const sb_engine* e, double* total_ms, double* check_ms,
                                 uint64_t* check_launches);
-/* Breakdown of the last generate call: out[0..4] = ms spent (device globaltimer, block 0)
- * in the placement kernel's init / broad (A) / narrow (B) / accept (C) / compaction (D)
- * phases summed over placements, out[5] = persistent rounds executed, out[6] = ms in
- * relation-region preparation (anchor states, variation test, region build), out[7] =
- * total ms (CUDA events). */
-sb_status sb_engine_phase_profile(const sb_engine* e, double out[8]);
+/* Breakdown of the last generate call, summed over placements (device globaltimer of the
+ * placement kernel's block 0, ms): out[0] setup + tile init, out[1] fast-path prefix
+ * scans, out[2] A1 sample/compose, out[3] A2+B broad/narrow phase, out[4] C accept +
+ * compaction, out[5] grid-barrier waits, out[6] per-instance placements (whole), out[7] =
+ * fast-path rounds, out[8] = ms in relation-region preparation (CUDA events), out[9] =
+ * total ms (CUDA events), out[10..15] reserved (0). */
+sb_status sb_engine_phase_profile(const sb_engine* e, double out[16]);
 
 /* Diagnostics: evaluate the device libm used on the hot path (correctly rounded
  * double-double sin/cos/atan2, replacing glibc's std::sin/cos/atan2 in transform.hpp:47,

@@ -236,36 +236,49 @@ static __device__ __noinline__ bool coplanar_tri_tri(const double n[3], const do
   return false;
 }
 
-// tri_tri_intersect (collision.cpp:87-130). p, q: 9 doubles each (three xyz vertices).
-__device__ __forceinline__ bool tri_tri_intersect(const double* p, const double* q) {
-  double e1x = q[3] - q[0], e1y = q[4] - q[1], e1z = q[5] - q[2];
-  double e2x = q[6] - q[0], e2y = q[7] - q[1], e2z = q[8] - q[2];
-  double n2[3] = {e1y * e2z - e1z * e2y, e1z * e2x - e1x * e2z, e1x * e2y - e1y * e2x};
-  double d2c = -((n2[0] * q[0] + n2[1] * q[1]) + n2[2] * q[2]);
-  double dp0 = ((n2[0] * p[0] + n2[1] * p[1]) + n2[2] * p[2]) + d2c;
-  double dp1 = ((n2[0] * p[3] + n2[1] * p[4]) + n2[2] * p[5]) + d2c;
-  double dp2 = ((n2[0] * p[6] + n2[1] * p[7]) + n2[2] * p[8]) + d2c;
-  double scale2 = sqrt((n2[0] * n2[0] + n2[1] * n2[1]) + n2[2] * n2[2]);
-  double tol2 = kEps * dmax(1.0, scale2);
-  if (fabs(dp0) < tol2) dp0 = 0.0;
-  if (fabs(dp1) < tol2) dp1 = 0.0;
-  if (fabs(dp2) < tol2) dp2 = 0.0;
-  if ((dp0 > 0 && dp1 > 0 && dp2 > 0) || (dp0 < 0 && dp1 < 0 && dp2 < 0)) return false;
+// tri_tri_intersect (collision.cpp:87-130), split into the stages the warp narrow phase
+// runs as separate filter passes. Every quantity is computed with the reference's
+// operations in the reference's order, so the staged and the monolithic forms agree bit
+// for bit; only *when* a pure function of one triangle is evaluated changes.
+struct TriPlane {
+  double n[3];  // cross(v1 - v0, v2 - v0)
+  double dc;    // -dot(n, v0)
+  double tol;   // kEps * max(1, |n|)  (collision.cpp:95-98 / 108-110)
+};
 
-  double f1x = p[3] - p[0], f1y = p[4] - p[1], f1z = p[5] - p[2];
-  double f2x = p[6] - p[0], f2y = p[7] - p[1], f2z = p[8] - p[2];
-  double n1[3] = {f1y * f2z - f1z * f2y, f1z * f2x - f1x * f2z, f1x * f2y - f1y * f2x};
-  double d1c = -((n1[0] * p[0] + n1[1] * p[1]) + n1[2] * p[2]);
-  double dq0 = ((n1[0] * q[0] + n1[1] * q[1]) + n1[2] * q[2]) + d1c;
-  double dq1 = ((n1[0] * q[3] + n1[1] * q[4]) + n1[2] * q[5]) + d1c;
-  double dq2 = ((n1[0] * q[6] + n1[1] * q[7]) + n1[2] * q[8]) + d1c;
-  double scale1 = sqrt((n1[0] * n1[0] + n1[1] * n1[1]) + n1[2] * n1[2]);
-  double tol1 = kEps * dmax(1.0, scale1);
-  if (fabs(dq0) < tol1) dq0 = 0.0;
-  if (fabs(dq1) < tol1) dq1 = 0.0;
-  if (fabs(dq2) < tol1) dq2 = 0.0;
-  if ((dq0 > 0 && dq1 > 0 && dq2 > 0) || (dq0 < 0 && dq1 < 0 && dq2 < 0)) return false;
+__device__ __forceinline__ TriPlane tri_plane(const double* t) {
+  TriPlane P;
+  double e1x = t[3] - t[0], e1y = t[4] - t[1], e1z = t[5] - t[2];
+  double e2x = t[6] - t[0], e2y = t[7] - t[1], e2z = t[8] - t[2];
+  P.n[0] = e1y * e2z - e1z * e2y;
+  P.n[1] = e1z * e2x - e1x * e2z;
+  P.n[2] = e1x * e2y - e1y * e2x;
+  P.dc = -((P.n[0] * t[0] + P.n[1] * t[1]) + P.n[2] * t[2]);
+  double scale = sqrt((P.n[0] * P.n[0] + P.n[1] * P.n[1]) + P.n[2] * P.n[2]);
+  P.tol = kEps * dmax(1.0, scale);
+  return P;
+}
 
+// Signed distances of t's vertices to plane (n, dc), snapped to 0 below tol.
+__device__ __forceinline__ void plane_dists(const double* n, double dc, double tol, const double* t,
+                                            double& d0, double& d1, double& d2) {
+  d0 = ((n[0] * t[0] + n[1] * t[1]) + n[2] * t[2]) + dc;
+  d1 = ((n[0] * t[3] + n[1] * t[4]) + n[2] * t[5]) + dc;
+  d2 = ((n[0] * t[6] + n[1] * t[7]) + n[2] * t[8]) + dc;
+  if (fabs(d0) < tol) d0 = 0.0;
+  if (fabs(d1) < tol) d1 = 0.0;
+  if (fabs(d2) < tol) d2 = 0.0;
+}
+
+// false = all three strictly on one side (the early-outs of collision.cpp:99,111)
+__device__ __forceinline__ bool straddles(double d0, double d1, double d2) {
+  return !((d0 > 0 && d1 > 0 && d2 > 0) || (d0 < 0 && d1 < 0 && d2 < 0));
+}
+
+// Rest of the test once both plane tests passed (collision.cpp:113-129).
+__device__ __forceinline__ bool tri_tri_finish(const double* p, const double* q, const double n1[3],
+                                               const double n2[3], double dp0, double dp1,
+                                               double dp2, double dq0, double dq1, double dq2) {
   if (dp0 == 0 && dp1 == 0 && dp2 == 0) return coplanar_tri_tri(n1, p, q);
 
   double dir0 = n1[1] * n2[2] - n1[2] * n2[1];
@@ -282,6 +295,19 @@ __device__ __forceinline__ bool tri_tri_intersect(const double* p, const double*
   if (!compute_interval(q[axis], q[3 + axis], q[6 + axis], dq0, dq1, dq2, lo2, hi2))
     return coplanar_tri_tri(n1, p, q);
   return hi1 > lo2 + kEps && hi2 > lo1 + kEps;
+}
+
+// tri_tri_intersect (collision.cpp:87-130). p, q: 9 doubles each (three xyz vertices).
+__device__ __forceinline__ bool tri_tri_intersect(const double* p, const double* q) {
+  const TriPlane P2 = tri_plane(q);
+  double dp0, dp1, dp2;
+  plane_dists(P2.n, P2.dc, P2.tol, p, dp0, dp1, dp2);
+  if (!straddles(dp0, dp1, dp2)) return false;
+  const TriPlane P1 = tri_plane(p);
+  double dq0, dq1, dq2;
+  plane_dists(P1.n, P1.dc, P1.tol, q, dq0, dq1, dq2);
+  if (!straddles(dq0, dq1, dq2)) return false;
+  return tri_tri_finish(p, q, P1.n, P2.n, dp0, dp1, dp2, dq0, dq1, dq2);
 }
 
 // ---------------------------------------------------------- BVH-vs-BVH collide

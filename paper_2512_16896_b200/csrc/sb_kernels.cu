@@ -97,8 +97,9 @@ __global__ void __launch_bounds__(kBlock) k_check_batch(WorldView w, int32_t geo
                                                         const uint32_t* active, uint64_t m,
                                                         uint8_t* free_out, int32_t* contact_out,
                                                         unsigned long long* counters) {
-  __shared__ WarpScratch ws[kBlock / 32];
+  extern __shared__ __align__(16) unsigned char ws_dyn[];  // [kBlock / 32] WarpScratch
   __shared__ double invs[kBlock / 32][32][12];
+  WarpScratch* ws = reinterpret_cast<WarpScratch*>(ws_dyn);
   __shared__ GeomCache gc;
   const SbGeom gA = w.geoms[geom];
   load_geom_cache(w, gA, gc);
@@ -215,8 +216,16 @@ void check_batch(const SbWorldView& w, int32_t geom, const double* poses16,
                  const uint32_t* active, uint64_t m, uint8_t* free_out, int32_t* contact_out,
                  unsigned long long* counters, sb_stream_t s) {
   if (m == 0) return;
-  k_check_batch<<<grid_for(m), kBlock, 0, s>>>(w, geom, poses16, active, m, free_out,
-                                                contact_out, counters);
+  const size_t smem = (kBlock / 32) * sizeof(WarpScratch);
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute((const void*)k_check_batch, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+      throw std::runtime_error("check_batch: cudaFuncSetAttribute failed");
+    attr = true;
+  }
+  k_check_batch<<<grid_for(m), kBlock, smem, s>>>(w, geom, poses16, active, m, free_out,
+                                                  contact_out, counters);
   check_launch("check_batch");
 }
 void engine_reset(const SbWorldView& w, int32_t first_obj, int32_t n_obj, uint8_t* valid,

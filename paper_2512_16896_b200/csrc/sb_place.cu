@@ -1,6 +1,5 @@
-// Phased placement engine (see sb_place.h). sm_100a, -fmad=false.
+// Tiled placement engine (see sb_place.h). sm_100a, -fmad=false.
 #include <cooperative_groups.h>
-#include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
 
 #include <climits>
@@ -23,23 +22,61 @@ namespace {
 constexpr int kB = kPlaceBlock;
 constexpr int kWarps = kB / 32;
 constexpr int32_t kFree = INT32_MAX;
-constexpr uint8_t kSlotVoid = 0, kSlotChecked = 1, kSlotUnplaceable = 2;
+constexpr int kQueue = 2048;  // shared-memory narrow-phase queue (slot << 24 | object)
+constexpr int kU = 4;         // broad-phase items per thread per batch (loads in flight)
+constexpr uint8_t kSlotChecked = 1, kSlotUnplaceable = 2;
+constexpr int kPrefixItems = 8;  // tile counts per thread per prefix-scan chunk
 
-enum Ctrl { kM = 0, kPairs = 1, kRounds = 2, kErr = 3, kCur = 4 };
+enum Ctrl { kRounds = 2, kErr = 3, kTileCtr = 4 /* kTotal0 = 5, kTotal1 = 6 */ };
 
-// Phase A tile (one slot per thread) and phase B warp scratch share the same bytes.
-struct TileA {
-  double box[kB][6];   // candidate world AABB per slot of the tile
-  uint32_t inst[kB];
-  uint8_t ok[kB];      // slot holds a placeable candidate
+using BlockScan = cub::BlockScan<uint32_t, kB>;
+
+// Per-round candidate state of the CTA's tile (dynamic shared memory).
+struct Tile {
+  double* pose;      // [kB][12] candidate pose per slot
+  double* inv;       // [kB][12] inverse pose per slot
+  double* box;       // [kB][6]  candidate world AABB per slot
+  uint32_t* ovm;     // [words][kB] broad-phase overlap bits per slot
+  uint32_t* enw;     // [words][kB] enable words per tile entry
+  uint32_t* list;    // [kB] tile's active instances (ascending)
+  uint32_t* queue;   // [kQueue]
+  int32_t* contact;  // [kB] min colliding object per slot
+  uint8_t* sflag;    // [kB]
+  unsigned char* ws; // [kWarps][ws_bytes]
 };
-struct Shared {
-  union {
-    WarpScratch ws[kWarps];
-    TileA ta;
-  } u;
+
+struct Fixed {  // static shared memory
   GeomCache gc;
+  typename BlockScan::TempStorage scan;
+  uint32_t prefix[kPlaceMaxOwnedTiles];  // fast path: draw offset of each owned tile
+  uint32_t cnt[kPlaceMaxOwnedTiles];     // fast path: its survivors entering this round
+  uint32_t qn;
+  uint32_t total;
+  uint32_t tile;
+  unsigned long long tclk;  // block 0 / thread 0 phase clock
+  unsigned long long acc[8];  // its per-slot sums, written to p.prof once at the end
+  unsigned long long ta, tb, t0;  // every block: A1 / A2+B ns of the current round (debug)
 };
+
+__device__ __forceinline__ Tile carve(unsigned char* d, int words, int ws_bytes) {
+  Tile t;
+  t.pose = reinterpret_cast<double*>(d);
+  t.inv = t.pose + 12 * kB;
+  t.box = t.inv + 12 * kB;
+  t.ovm = reinterpret_cast<uint32_t*>(t.box + 6 * kB);
+  t.enw = t.ovm + words * kB;
+  t.list = t.enw + words * kB;
+  t.queue = t.list + kB;
+  t.contact = reinterpret_cast<int32_t*>(t.queue + kQueue);
+  t.sflag = reinterpret_cast<uint8_t*>(t.contact + kB);
+  t.ws = t.sflag + kB;
+  return t;
+}
+
+__host__ __device__ constexpr size_t tile_bytes(int words) {
+  return (12 + 12 + 6) * 8 * (size_t)kB + 2 * (size_t)words * kB * 4 + (size_t)kB * 4 +
+         (size_t)kQueue * 4 + (size_t)kB * 4 + kB;
+}
 
 struct Local {  // per-thread counters, flushed once at kernel end
   unsigned checked = 0, sampled = 0, accepted = 0;
@@ -58,10 +95,6 @@ __device__ __forceinline__ void flush(const PlaceParams& p, const Local& l) {
   add(4, l.cnt.broad);
   add(5, l.cnt.nodes);
   add(6, l.accepted);
-}
-
-__device__ __forceinline__ uint32_t* act_list(const PlaceParams& p, int which) {
-  return which ? p.act1 : p.act0;
 }
 
 // Sampling source of the placement, resolved on the device when the host left the
@@ -87,273 +120,236 @@ __device__ __forceinline__ Sampling resolve_sampling(const PlaceParams& p) {
   return s;
 }
 
-// Attempts evaluated per remaining instance this round (1 on the FIFO fast path).
-__device__ __forceinline__ int spec_width(const PlaceParams& p, int fast, uint64_t m,
-                                          int32_t attempt) {
-  if (fast || m == 0) return 1;
-  uint64_t w = p.spec_budget / m;
-  const uint64_t cap = p.slot_cap / m;
-  if (w > cap) w = cap;
-  if (w > (uint64_t)(p.attempts - attempt)) w = (uint64_t)(p.attempts - attempt);
-  return w < 1 ? 1 : (int)w;
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
 
-// ------------------------------------------------------------------ compaction
-// Stable compaction in chunks of kB entries: count pass, then (after a grid barrier) a
-// scatter pass that derives each chunk's output offset from the chunk counts.
-template <class Flag>
-__device__ void compact_count(const PlaceParams& p, uint64_t m, Flag flag) {
-  const uint64_t nc = (m + kB - 1) / kB;
-  for (uint64_t ch = blockIdx.x; ch < nc; ch += gridDim.x) {
-    const uint64_t e = ch * kB + threadIdx.x;
-    const int f = e < m ? flag(e) : 0;
-    const int c = __syncthreads_count(f);
-    if (threadIdx.x == 0) p.chunk_cnt[ch] = (uint32_t)c;
+// Phase clock (block 0, thread 0; device globaltimer) into p.prof[slot] (ns):
+// 0 setup + tile init, 1 fast-path prefix scan, 2 A1 sample/compose, 3 A2+B broad/narrow,
+// 4 C accept + compaction, 5 grid barrier, 6 per-instance path (whole), 7 fast rounds.
+__device__ __forceinline__ void dbg_mark(const PlaceParams& p, Fixed& F, unsigned long long& acc) {
+  if (p.dbg && threadIdx.x == 0) {
+    const unsigned long long now = global_ns();
+    acc += now - F.t0;
+    F.t0 = now;
   }
 }
 
-template <class Flag, class Src>
-__device__ void compact_scatter(const PlaceParams& p, uint64_t m, Flag flag, Src src,
-                                uint32_t* dst) {
-  using BR = cub::BlockReduce<uint32_t, kB>;
-  using BS = cub::BlockScan<uint32_t, kB>;
-  __shared__ union {
-    typename BR::TempStorage r;
-    typename BS::TempStorage s;
-  } tmp;
-  __shared__ uint32_t s_off;
-  const uint64_t nc = (m + kB - 1) / kB;
-  uint64_t done = 0;  // chunks [0, done) already summed into off
-  uint32_t off = 0;
-  for (uint64_t ch = blockIdx.x; ch < nc; ch += gridDim.x) {
-    uint32_t part = 0;
-    for (uint64_t c = done + threadIdx.x; c < ch; c += kB) part += __ldcg(p.chunk_cnt + c);
-    uint32_t sum = BR(tmp.r).Sum(part);
-    if (threadIdx.x == 0) s_off = off + sum;
-    __syncthreads();
-    off = s_off;
-    done = ch;
-    const uint64_t e = ch * kB + threadIdx.x;
-    const uint32_t f = e < m ? (uint32_t)flag(e) : 0u;
-    uint32_t rank;
-    BS(tmp.s).ExclusiveSum(f, rank);
-    if (f) dst[off + rank] = src(e);
-    __syncthreads();
-  }
-  if (blockIdx.x == 0) {  // total -> next M
-    uint32_t part = 0;
-    for (uint64_t c = threadIdx.x; c < nc; c += kB) part += __ldcg(p.chunk_cnt + c);
-    uint32_t sum = BR(tmp.r).Sum(part);
-    if (threadIdx.x == 0) p.ctrl[kM] = sum;
+__device__ __forceinline__ void lap(const PlaceParams& p, Fixed& F, int slot) {
+  if (p.prof && blockIdx.x == 0 && threadIdx.x == 0) {
+    const unsigned long long now = global_ns();
+    F.acc[slot] += now - F.tclk;
+    F.tclk = now;
   }
 }
 
-// ------------------------------------------------------------------ phase A
-// Tiles of kB virtual slots per block; slot v = e * W + s is instance act[e] at attempt
-// `attempt + s`.
-// A1 (thread per slot): sample -> yaw -> compose -> candidate AABB + inverse; pose and
-//    inverse to global, AABB to shared memory.
-// A2 (thread per (slot, object) item): AABB broad phase (collision.cpp:439-443) over the
-//    enabled objects; consecutive threads read consecutive object records of one instance
-//    (instance-major layout), so the loads are contiguous and independent. Overlaps set
-//    the slot's ovmask bit and append (slot, object) to the pair queue.
-__device__ void phase_a(const PlaceParams& p, const Sampling& S, const SbGeom& gA,
-                        Shared& sh, const uint32_t* act, uint64_t m, int W,
-                        uint64_t draw_base, int32_t attempt, Local& L) {
-  const int lane = threadIdx.x & 31;
+// ------------------------------------------------------------------ one tile round
+// Evaluates attempts [a, a + W) of the tile's nt active instances (T.list) and compacts the
+// survivors in place. Returns the survivor count. All threads of the CTA call it.
+__device__ uint32_t tile_round(const PlaceParams& p, const Sampling& S, const SbGeom& gA,
+                               Tile& T, Fixed& F, uint32_t nt, int32_t a, int W,
+                               uint64_t draw_base, Local& L) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const WorldView& w = p.w;
   const SbPlacementDev& pl = p.pl;
-  const WorldView& w = p.w;
-  TileA& ta = sh.u.ta;
-  const uint64_t nslots = m * (uint64_t)W;
-  const int nobj = w.n_objects;
-  // tile size: kB slots, or fewer so that small rounds still spread over every block
-  uint64_t T = (nslots + gridDim.x - 1) / gridDim.x;
-  T = T < 32 ? 32 : ((T + 31) / 32) * 32;
-  if (T > (uint64_t)kB) T = kB;
-  for (uint64_t t0 = (uint64_t)blockIdx.x * T; t0 < nslots; t0 += (uint64_t)gridDim.x * T) {
-    // ---------------- A1
-    const uint64_t v = t0 + threadIdx.x;
-    bool ok = false;
-    uint32_t inst = 0;
-    if (threadIdx.x < T && v < nslots) {
-      const uint64_t e = v / W;
-      const int32_t at = attempt + (int32_t)(v - e * W);
-      inst = act[e];
-      const uint64_t gid = p.global_begin + inst;
-      bool placeable = true;
-      double lx = 0.0, ly = 0.0;
-      if (S.fast) {
-        if (S.n == 0) {
-          placeable = false;
-        } else {
-          Pcg r{p.fast_state0};
-          r.advance(6ull * (draw_base + e));  // j-th drained point = j-th draw (sampler.cpp:30-43)
-          double u = r.next_double(), r1 = r.next_double(), r2 = r.next_double();
-          sbp::draw_point(S.tris, S.cum, S.n, u, r1, r2, lx, ly);
-        }
+  const int words = w.n_words, nobj = w.n_objects;
+  const int nslots = (int)nt * W;
+
+  // enable words of the tile's instances (independent loads, consumed in A2)
+  for (int i = tid; i < (int)nt * words; i += kB) {
+    const int wd = i / (int)nt, e = i - wd * (int)nt;
+    T.enw[wd * kB + e] = __ldcg(w.enabled + sb_word_off(w, wd, T.list[e]));
+  }
+  // ---------------- A1: thread per slot
+  if (tid < nslots) {
+    const int v = tid;
+    const int e = v / W;
+    const int32_t at = a + (v - e * W);
+    const uint32_t inst = T.list[e];
+    const uint64_t gid = p.global_begin + inst;
+    bool placeable = true;
+    double lx = 0.0, ly = 0.0;
+    if (S.fast) {
+      if (S.n == 0) {
+        placeable = false;
       } else {
-        const int nt = p.inst_n[inst];
-        if (nt == 0) {
-          placeable = false;
-        } else {  // make_stream(run_seed, {salt, "fall", inst, attempt}) (sampler.cpp:117)
-          Pcg r = Pcg::seeded(stream_seed4(p.run_seed, pl.salt, kFallbackSalt, gid,
-                                           static_cast<uint64_t>(at)));
-          double u = r.next_double(), r1 = r.next_double(), r2 = r.next_double();
-          const uint64_t off = (uint64_t)inst * p.inst_cap;
-          sbp::draw_point(p.inst_tris + off, p.inst_cum + off, nt, u, r1, r2, lx, ly);
-        }
+        Pcg r{p.fast_state0};
+        r.advance(6ull * (draw_base + (uint64_t)e));  // j-th drained point = j-th draw (sampler.cpp:30-43)
+        double u = r.next_double(), r1 = r.next_double(), r2 = r.next_double();
+        sbp::draw_point(S.tris, S.cum, S.n, u, r1, r2, lx, ly);
       }
-      p.contact[v] = kFree;
-      for (int wd = 0; wd < w.n_words; ++wd) p.ovmask[(uint64_t)wd * p.slot_cap + v] = 0u;
-      if (!placeable) {
-        p.cflag[v] = kSlotUnplaceable;
-      } else {
-        M34 Sp;
-#pragma unroll
-        for (int k = 0; k < 12; ++k) Sp.m[k] = pl.support[k];
-        double px, py, pz;
-        xform(Sp, lx, ly, 0.0, px, py, pz);  // transform_point(support_world, (x, y, 0))
-        double yaw = 0.0;
-        if (pl.orientation == SB_ORIENT_UNIFORM_YAW) {  // sampler.cpp:140-141
-          Pcg r = Pcg::seeded(
-              stream_seed4(p.run_seed, pl.salt, kYawSalt, gid, static_cast<uint64_t>(at)));
-          const double two_pi = 2.0 * 3.14159265358979323846;
-          yaw = 0.0 + (two_pi - 0.0) * r.next_double();
-        } else if (pl.orientation == SB_ORIENT_FACE_TO) {  // relationships.cpp:232-239
-          const double* tp = w.pose + sb_pose_off(w, pl.face_object, inst);
-          double dx = tp[3] - px, dy = tp[7] - py;
-          yaw = sqrt(dx * dx + dy * dy) < 1e-12 ? 0.0 : sbm::atan2_cr(dy, dx);
-        }
-        double c, s;
-        sbm::sincos_cr(yaw, &s, &c);  // rotation_z: std::cos / std::sin (transform.hpp:47)
-        M34 T, Rz, pose;  // translation(p + z_off z) * rotation_z(yaw)
-#pragma unroll
-        for (int k = 0; k < 12; ++k) T.m[k] = Rz.m[k] = 0.0;
-        T.m[0] = T.m[5] = T.m[10] = 1.0;
-        Rz.m[10] = 1.0;
-        T.m[3] = px + 0.0;
-        T.m[7] = py + 0.0;
-        T.m[11] = pz + pl.z_off;
-        Rz.m[0] = c;
-        Rz.m[1] = -s;
-        Rz.m[4] = s;
-        Rz.m[5] = c;
-        mul34(T, Rz, pose);
-        double cmn[3], cmx[3];
-        xform_aabb(pose, gA.box_c, gA.box_h, cmn, cmx);
-        M34 inv;
-        inverse_rigid(pose, inv);
-        double2* cp = reinterpret_cast<double2*>(p.cpose + v * 12);
-        double2* ci = reinterpret_cast<double2*>(p.cinv + v * 12);
-#pragma unroll
-        for (int k = 0; k < 6; ++k) {
-          cp[k] = make_double2(pose.m[2 * k], pose.m[2 * k + 1]);
-          ci[k] = make_double2(inv.m[2 * k], inv.m[2 * k + 1]);
-        }
-        p.cflag[v] = kSlotChecked;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          ta.box[threadIdx.x][k] = cmn[k];
-          ta.box[threadIdx.x][3 + k] = cmx[k];
-        }
-        ok = true;
+    } else {
+      const int nti = __ldg(p.inst_n + inst);
+      if (nti == 0) {
+        placeable = false;
+      } else {  // make_stream(run_seed, {salt, "fall", inst, attempt}) (sampler.cpp:117)
+        Pcg r = Pcg::seeded(stream_seed4(p.run_seed, pl.salt, kFallbackSalt, gid,
+                                         static_cast<uint64_t>(at)));
+        double u = r.next_double(), r1 = r.next_double(), r2 = r.next_double();
+        const uint64_t off = (uint64_t)inst * p.inst_cap;
+        sbp::draw_point(p.inst_tris + off, p.inst_cum + off, nti, u, r1, r2, lx, ly);
       }
     }
-    ta.inst[threadIdx.x] = inst;
-    ta.ok[threadIdx.x] = ok ? 1 : 0;
+    T.contact[v] = kFree;
+    for (int wd = 0; wd < words; ++wd) T.ovm[wd * kB + v] = 0u;
+    if (!placeable) {
+      T.sflag[v] = kSlotUnplaceable;
+    } else {
+      M34 Sp;
+#pragma unroll
+      for (int k = 0; k < 12; ++k) Sp.m[k] = pl.support[k];
+      double px, py, pz;
+      xform(Sp, lx, ly, 0.0, px, py, pz);  // transform_point(support_world, (x, y, 0))
+      double yaw = 0.0;
+      if (pl.orientation == SB_ORIENT_UNIFORM_YAW) {  // sampler.cpp:140-141
+        Pcg r = Pcg::seeded(
+            stream_seed4(p.run_seed, pl.salt, kYawSalt, gid, static_cast<uint64_t>(at)));
+        const double two_pi = 2.0 * 3.14159265358979323846;
+        yaw = 0.0 + (two_pi - 0.0) * r.next_double();
+      } else if (pl.orientation == SB_ORIENT_FACE_TO) {  // relationships.cpp:232-239
+        const double* tp = w.pose + sb_pose_off(w, pl.face_object, inst);
+        double dx = tp[3] - px, dy = tp[7] - py;
+        yaw = sqrt(dx * dx + dy * dy) < 1e-12 ? 0.0 : sbm::atan2_cr(dy, dx);
+      }
+      double c, s;
+      sbm::sincos_cr(yaw, &s, &c);  // rotation_z: std::cos / std::sin (transform.hpp:47)
+      M34 Tr, Rz, pose;  // translation(p + z_off z) * rotation_z(yaw)
+#pragma unroll
+      for (int k = 0; k < 12; ++k) Tr.m[k] = Rz.m[k] = 0.0;
+      Tr.m[0] = Tr.m[5] = Tr.m[10] = 1.0;
+      Rz.m[10] = 1.0;
+      Tr.m[3] = px + 0.0;
+      Tr.m[7] = py + 0.0;
+      Tr.m[11] = pz + pl.z_off;
+      Rz.m[0] = c;
+      Rz.m[1] = -s;
+      Rz.m[4] = s;
+      Rz.m[5] = c;
+      mul34(Tr, Rz, pose);
+      double cmn[3], cmx[3];
+      xform_aabb(pose, gA.box_c, gA.box_h, cmn, cmx);
+      M34 inv;
+      inverse_rigid(pose, inv);
+#pragma unroll
+      for (int k = 0; k < 12; ++k) {
+        T.pose[12 * v + k] = pose.m[k];
+        T.inv[12 * v + k] = inv.m[k];
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        T.box[6 * v + k] = cmn[k];
+        T.box[6 * v + 3 + k] = cmx[k];
+      }
+      T.sflag[v] = kSlotChecked;
+    }
+  }
+  if (tid == 0) F.qn = 0;
+  __syncthreads();
+  lap(p, F, 2);
+  dbg_mark(p, F, F.ta);
+
+  // ---------------- A2 (broad phase) interleaved with B (narrow phase) in queue batches
+  const int items = nslots * nobj;
+  for (int it0 = 0; it0 < items; it0 += kB * kU) {
+    bool ov[kU];
+    int vs[kU], obs[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int it = it0 + u * kB + tid;
+      ov[u] = false;
+      vs[u] = 0;
+      obs[u] = 0;
+      if (it < items) {
+        const int v = it / nobj;
+        const int ob = it - v * nobj;
+        vs[u] = v;
+        obs[u] = ob;
+        if (T.sflag[v] == kSlotChecked &&
+            ((T.enw[(ob >> 5) * kB + v / W] >> (ob & 31)) & 1u)) {
+          ++L.cnt.broad;
+          const double2* bp = reinterpret_cast<const double2*>(w.box + sb_box_off(w, ob, T.list[v / W]));
+          const double2 b0 = __ldcg(bp), b1 = __ldcg(bp + 1), b2 = __ldcg(bp + 2);
+          const double* cb = T.box + 6 * v;
+          ov[u] = cb[0] <= b1.y && b0.x <= cb[3] && cb[1] <= b2.x && b0.y <= cb[4] &&
+                  cb[2] <= b2.y && b1.x <= cb[5];
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint32_t mask = __ballot_sync(kFull, ov[u]);
+      if (!mask) continue;
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(&F.qn, (uint32_t)__popc(mask));
+      base = __shfl_sync(kFull, base, 0);
+      if (ov[u]) {
+        atomicOr(T.ovm + (obs[u] >> 5) * kB + vs[u], 1u << (obs[u] & 31));
+        T.queue[base + __popc(mask & ((1u << lane) - 1u))] = ((uint32_t)vs[u] << 24) | (uint32_t)obs[u];
+      }
+    }
     __syncthreads();
-    // ---------------- A2 (4 items per thread in flight: loads first, then ballots)
-    const uint64_t tile_n = (nslots - t0) < T ? (nslots - t0) : T;
-    const uint64_t items = tile_n * (uint64_t)nobj;
-    constexpr int U = 4;
-    for (uint64_t it0 = 0; it0 < items; it0 += (uint64_t)kB * U) {
-      bool ov[U];
-      uint32_t tt[U];
-      int obs[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint64_t it = it0 + (uint64_t)u * kB + threadIdx.x;
-        ov[u] = false;
-        tt[u] = 0;
-        obs[u] = 0;
-        if (it < items) {
-          const uint32_t t = (uint32_t)(it / nobj);
-          const int ob = (int)(it - (uint64_t)t * nobj);
-          tt[u] = t;
-          obs[u] = ob;
-          if (ta.ok[t]) {
-            const uint32_t in = ta.inst[t];
-            const uint32_t bits = w.enabled[sb_word_off(w, ob >> 5, in)];
-            if ((bits >> (ob & 31)) & 1u) {
-              ++L.cnt.broad;
-              const double2* bp =
-                  reinterpret_cast<const double2*>(w.box + sb_box_off(w, ob, in));
-              const double2 b0 = bp[0], b1 = bp[1], b2 = bp[2];
-              const double* cb = ta.box[t];
-              ov[u] = cb[0] <= b1.y && b0.x <= cb[3] && cb[1] <= b2.x && b0.y <= cb[4] &&
-                      cb[2] <= b2.y && b1.x <= cb[5];
-            }
-          }
+    const uint32_t qn = F.qn;
+    if (it0 + kB * kU >= items || qn > (uint32_t)(kQueue - kB * kU)) {
+      // ---------------- B: warp per queued pair; skip pairs behind a lower hit
+      const WarpScratchView ws = carve_scratch(T.ws + warp * p.ws_bytes, p.max_tris, p.max_nodes);
+      // software-pipelined: the next pair's pose entries and geometry are in flight while
+      // the current pair is tested
+      uint32_t q = warp;
+      int v = 0, ob = 0;
+      double Pn = 0.0;
+      int4 gB = make_int4(0, 0, 0, 0);
+      auto fetch = [&](uint32_t qq, int& v_, int& ob_, double& Pn_, int4& g_) {
+        const uint32_t ent = T.queue[qq];
+        v_ = (int)(ent >> 24);
+        ob_ = (int)(ent & 0xffffffu);
+        Pn_ = pose_entry(w, ob_, T.list[v_ / W]);
+        g_ = geom_ref(w, ob_);
+      };
+      if (q < qn) fetch(q, v, ob, Pn, gB);
+      while (q < qn) {
+        const uint32_t qn2 = q + kWarps;
+        int v2 = 0, ob2 = 0;
+        double Pn2 = 0.0;
+        int4 gB2 = make_int4(0, 0, 0, 0);
+        if (qn2 < qn) fetch(qn2, v2, ob2, Pn2, gB2);
+        if (*((volatile int32_t*)T.contact + v) >= ob) {  // skip pairs behind a lower hit
+          const bool hit = warp_collide(w, F.gc, gB, Pn, T.inv + 12 * v, ws, L.cnt);
+          if (hit && lane == 0) atomicMin(T.contact + v, ob);
         }
+        __syncwarp();
+        q = qn2;
+        v = v2;
+        ob = ob2;
+        Pn = Pn2;
+        gB = gB2;
       }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint32_t mask = __ballot_sync(kFull, ov[u]);
-        if (!mask) continue;
-        uint32_t base = 0;
-        if (lane == 0) base = atomicAdd(p.ctrl + kPairs, (uint32_t)__popc(mask));
-        base = __shfl_sync(kFull, base, 0);
-        if (ov[u]) {
-          const uint64_t vv = t0 + tt[u];
-          const int ob = obs[u];
-          atomicOr(p.ovmask + (uint64_t)(ob >> 5) * p.slot_cap + vv, 1u << (ob & 31));
-          const uint64_t idx = base + __popc(mask & ((1u << lane) - 1u));
-          if (idx < p.pair_cap) p.pairs[idx] = (vv << 32) | (uint32_t)ob;
-          else atomicOr(p.ctrl + kErr, 1u);
-        }
-      }
+      __syncthreads();
+      if (tid == 0) F.qn = 0;
+      __syncthreads();
     }
-    __syncthreads();  // tile buffers are reused by the next tile
   }
-}
+  if (items == 0) __syncthreads();
+  lap(p, F, 3);
+  dbg_mark(p, F, F.tb);
 
-// ------------------------------------------------------------------ phase B
-__device__ void phase_b(const PlaceParams& p, Shared& sh, const uint32_t* act, int W,
-                        Local& L) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
-  uint64_t np = __ldcg(p.ctrl + kPairs);
-  if (np > p.pair_cap) np = p.pair_cap;
-  WarpScratch& ws = sh.u.ws[threadIdx.x >> 5];
-  for (uint64_t q = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); q < np; q += nwarps) {
-    const uint64_t pr = p.pairs[q];
-    const uint64_t v = pr >> 32;
-    const int32_t ob = (int32_t)(pr & 0xffffffffu);
-    const bool hit = warp_collide(p.w, sh.gc, ob, act[v / W], p.cinv + 12 * v, ws, L.cnt);
-    if (hit && lane == 0) atomicMin(p.contact + v, ob);
-    __syncwarp();
-  }
-}
-
-// ------------------------------------------------------------------ phase C
-// Thread per remaining instance: first free attempt among its W slots is accepted
-// (update_transform + set_enabled, Appendix C.5); counters follow the sequential loop.
-__device__ void phase_c(const PlaceParams& p, const uint32_t* act, uint64_t m, int W,
-                        int32_t attempt, Local& L) {
-  const WorldView& w = p.w;
-  const int words = w.n_words;
-  compact_count(p, m, [&](uint64_t e) -> int {
-    int32_t last = attempt;  // last attempt this instance made in the sequential loop
+  // ---------------- C: thread per instance; first free slot is accepted (Appendix C.5)
+  uint32_t keep = 0, inst = 0;
+  if (tid < (int)nt) {
+    const int e = tid;
+    inst = T.list[e];
+    int32_t last = a;  // last attempt this instance made in the sequential loop
     bool ok = false;
     for (int s = 0; s < W && !ok; ++s) {
-      const uint64_t v = e * W + s;
-      last = attempt + s;
+      const int v = e * W + s;
+      last = a + s;
       ++L.sampled;
-      if (p.cflag[v] != kSlotChecked) continue;  // placeable == 0 -> failed attempt
+      if (T.sflag[v] != kSlotChecked) continue;  // placeable == 0 -> failed attempt
       ++L.checked;
-      const int32_t c = __ldcg(p.contact + v);
+      const int32_t c = T.contact[v];
       for (int wd = 0; wd < words; ++wd) {  // narrow tests up to the first hit
-        uint32_t mk = p.ovmask[(uint64_t)wd * p.slot_cap + v];
+        uint32_t mk = T.ovm[wd * kB + v];
         if (c != kFree) {
           const int lim = c - 32 * wd;  // keep objects <= c
           if (lim < 0) mk = 0;
@@ -361,168 +357,272 @@ __device__ void phase_c(const PlaceParams& p, const uint32_t* act, uint64_t m, i
         }
         L.cnt.narrow += __popc(mk);
       }
-      if (c == kFree) {
-        const uint32_t inst = act[e];
-        M34 P;
+      if (c == kFree) {  // update_transform (collision.cpp:408-412) + set_enabled
+        double2* pp = reinterpret_cast<double2*>(w.pose + sb_pose_off(w, pl.object, inst));
 #pragma unroll
-        for (int k = 0; k < 12; ++k) P.m[k] = p.cpose[v * 12 + k];
-        store_pose(w, p.pl.object, inst, P);
-        w.enabled[sb_word_off(w, p.pl.object >> 5, inst)] |= 1u << (p.pl.object & 31);
-        p.accepted[inst] = (int16_t)(attempt + s);
+        for (int k = 0; k < 6; ++k) pp[k] = make_double2(T.pose[12 * v + 2 * k], T.pose[12 * v + 2 * k + 1]);
+        double2* bp = reinterpret_cast<double2*>(w.box + sb_box_off(w, pl.object, inst));
+#pragma unroll
+        for (int k = 0; k < 3; ++k) bp[k] = make_double2(T.box[6 * v + 2 * k], T.box[6 * v + 2 * k + 1]);
+        w.enabled[sb_word_off(w, pl.object >> 5, inst)] |= 1u << (pl.object & 31);
+        p.accepted[inst] = (int16_t)(a + s);
         ++L.accepted;
         ok = true;
       }
     }
     atomicMax(p.ctrl + kRounds, (uint32_t)(last + 1));  // reference round count
-    p.failflag[e] = ok ? 0 : 1;
-    return ok ? 0 : 1;
-  });
-  if (blockIdx.x == 0 && threadIdx.x == 0) p.ctrl[kPairs] = 0;  // phase B is done reading it
+    keep = ok ? 0u : 1u;
+  }
+  uint32_t rank, total;
+  BlockScan(F.scan).ExclusiveSum(keep, rank, total);
+  __syncthreads();  // every thread has read T.list[tid]
+  if (keep) T.list[rank] = inst;
+  __syncthreads();
+  lap(p, F, 4);
+  return total;
 }
 
-// ------------------------------------------------------------------ kernels
-__device__ __forceinline__ void block_setup(const PlaceParams& p, Shared& sh, SbGeom& gA) {
-  gA = p.w.geoms[p.pl.geom];
-  load_geom_cache(p.w, gA, sh.gc);
+// Stable compaction of the valid instances of tile t into T.list; returns the count.
+__device__ uint32_t tile_load_valid(const PlaceParams& p, Tile& T, Fixed& F, uint32_t t) {
+  const uint64_t i = (uint64_t)t * p.tile_inst + threadIdx.x;
+  const uint32_t f = (threadIdx.x < p.tile_inst && i < p.w.n && p.valid[i] != 0) ? 1u : 0u;
+  uint32_t rank, total;
+  BlockScan(F.scan).ExclusiveSum(f, rank, total);
+  if (f) T.list[rank] = (uint32_t)i;
+  __syncthreads();
+  return total;
+}
+
+__device__ __forceinline__ void mark_invalid(const PlaceParams& p, const Tile& T, uint32_t nt) {
+  for (uint32_t e = threadIdx.x; e < nt; e += kB) p.valid[T.list[e]] = 0;  // mark_invalid
+}
+
+// Fast path: exclusive prefix of the per-tile survivor counts for the CTA's tiles
+// (t = blockIdx.x + k * gridDim.x) into F.prefix / F.cnt; returns the round total.
+__device__ uint64_t tile_prefix(const PlaceParams& p, const uint32_t* cnt, Fixed& F) {
+  const uint32_t G = gridDim.x, b = blockIdx.x, nt = p.ntiles;
+  uint64_t running = 0;
+  for (uint32_t c0 = 0; c0 < nt; c0 += kB * kPrefixItems) {
+    uint32_t x[kPrefixItems], ex[kPrefixItems], agg;
+#pragma unroll
+    for (int j = 0; j < kPrefixItems; ++j) {
+      const uint32_t idx = c0 + threadIdx.x * kPrefixItems + j;
+      x[j] = idx < nt ? __ldcg(cnt + idx) : 0u;
+    }
+    BlockScan(F.scan).ExclusiveSum(x, ex, agg);
+#pragma unroll
+    for (int j = 0; j < kPrefixItems; ++j) {
+      const uint32_t idx = c0 + threadIdx.x * kPrefixItems + j;
+      if (idx < nt && idx % G == b) {
+        F.prefix[idx / G] = (uint32_t)running + ex[j];
+        F.cnt[idx / G] = x[j];
+      }
+    }
+    running += agg;
+    __syncthreads();
+  }
+  return running;
+}
+
+__device__ __forceinline__ void load_list(const PlaceParams& p, Tile& T, uint32_t t, uint32_t n) {
+  const uint32_t* src = p.tile_list + (uint64_t)t * p.tile_inst;
+  for (uint32_t e = threadIdx.x; e < n; e += kB) T.list[e] = __ldcg(src + e);
   __syncthreads();
 }
 
-__device__ __forceinline__ uint64_t global_ns() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
+__device__ __forceinline__ void store_list(const PlaceParams& p, const Tile& T, uint32_t t,
+                                           uint32_t n, uint32_t* cnt_out) {
+  uint32_t* dst = p.tile_list + (uint64_t)t * p.tile_inst;
+  for (uint32_t e = threadIdx.x; e < n; e += kB) dst[e] = T.list[e];
+  if (threadIdx.x == 0) cnt_out[t] = n;
 }
 
-// Phase timer: block 0 / thread 0 accumulates wall time between grid barriers into
-// p.prof[slot] (ns): 0 init, 1 A, 2 B, 3 C, 4 D; prof[5] counts rounds.
-struct PhaseClock {
-  uint64_t* prof;
-  uint64_t t;
-  __device__ PhaseClock(uint64_t* pr) : prof(pr), t(0) {
-    if (prof && blockIdx.x == 0 && threadIdx.x == 0) t = global_ns();
-  }
-  __device__ void lap(int slot) {
-    if (prof && blockIdx.x == 0 && threadIdx.x == 0) {
-      uint64_t now = global_ns();
-      prof[slot] += now - t;
-      t = now;
+// One fast-path round over the CTA's tiles: survivors of round a -> counts of round a+1.
+__device__ uint64_t fast_round(const PlaceParams& p, const Sampling& S, const SbGeom& gA,
+                               Tile& T, Fixed& F, int32_t a, uint64_t draws, Local& L,
+                               uint32_t* total_word) {
+  const uint32_t* cin = p.tile_cnt + (size_t)(a & 1) * p.cnt_stride;
+  uint32_t* cout = p.tile_cnt + (size_t)((a + 1) & 1) * p.cnt_stride;
+  const uint64_t total = tile_prefix(p, cin, F);
+  lap(p, F, 1);
+  if (total == 0) return 0;
+  uint32_t k = 0, mine = 0;
+  for (uint32_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++k) {
+    const uint32_t n = F.cnt[k];
+    if (n == 0) {
+      if (threadIdx.x == 0) cout[t] = 0;
+      continue;
     }
+    load_list(p, T, t, n);
+    lap(p, F, 1);
+    if (p.dbg && threadIdx.x == 0) F.t0 = global_ns();
+    const uint32_t ns = tile_round(p, S, gA, T, F, n, a, 1, draws + F.prefix[k], L);
+    store_list(p, T, t, ns, cout);
+    mine += ns;
+    __syncthreads();
   }
-};
+  if (total_word && threadIdx.x == 0 && mine) atomicAdd(total_word, mine);
+  return total;
+}
+
+// Per-instance path: tiles are independent; each is run to completion by one CTA.
+__device__ void instance_tiles(const PlaceParams& p, const Sampling& S, const SbGeom& gA,
+                               Tile& T, Fixed& F, Local& L) {
+  for (;;) {
+    if (threadIdx.x == 0) F.tile = atomicAdd(p.ctrl + kTileCtr, 1u);
+    __syncthreads();
+    const uint32_t t = F.tile;
+    __syncthreads();
+    if (t >= p.ntiles) break;
+    uint32_t nt = tile_load_valid(p, T, F, t);
+    int32_t a = 0;
+    while (nt > 0 && a < p.attempts) {
+      int W = p.spec_target / (int)nt;
+      if (W < 1) W = 1;
+      if (W > kB / (int)nt) W = kB / (int)nt;
+      if (W > p.attempts - a) W = p.attempts - a;
+      nt = tile_round(p, S, gA, T, F, nt, a, W, 0, L);
+      a += W;
+    }
+    mark_invalid(p, T, nt);
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ void block_setup(const PlaceParams& p, Fixed& F, SbGeom& gA) {
+  gA = p.w.geoms[p.pl.geom];
+  load_geom_cache(p.w, gA, F.gc);
+  __syncthreads();
+}
+
+extern __shared__ __align__(16) unsigned char g_dsm[];
 
 __global__ void __launch_bounds__(kB, 2) k_place(PlaceParams p) {
-  __shared__ Shared sh;
-  cg::grid_group grid = cg::this_grid();
-  PhaseClock clk(p.prof);
-  SbGeom gA;
-  block_setup(p, sh, gA);
-  Local L;
-  const uint64_t n = p.w.n;
-  compact_count(p, n, [&](uint64_t i) -> int { return p.valid[i] != 0; });
-  grid.sync();
-  compact_scatter(p, n, [&](uint64_t i) -> int { return p.valid[i] != 0; },
-                  [&](uint64_t i) -> uint32_t { return (uint32_t)i; }, p.act0);
-  grid.sync();
-  clk.lap(0);
-  const Sampling S = resolve_sampling(p);
-  if (p.vary_flag && !S.fast && blockIdx.x == 0 && threadIdx.x == 0)
-    atomicAdd(p.counters + 7, 1ull);  // per-instance placement
-  uint64_t draws = 0;
-  int cur = 0;
-  for (int32_t a = 0; a < p.attempts;) {
-    const uint64_t m = __ldcg(p.ctrl + kM);
-    if (m == 0) break;
-    const int W = spec_width(p, S.fast, m, a);
-    const uint32_t* act = act_list(p, cur);
-    phase_a(p, S, gA, sh, act, m, W, draws, a, L);
-    grid.sync();
-    clk.lap(1);
-    phase_b(p, sh, act, W, L);
-    grid.sync();
-    clk.lap(2);
-    phase_c(p, act, m, W, a, L);
-    grid.sync();
-    clk.lap(3);
-    compact_scatter(p, m, [&](uint64_t e) -> int { return p.failflag[e]; },
-                    [&](uint64_t e) -> uint32_t { return act[e]; }, act_list(p, cur ^ 1));
-    grid.sync();
-    clk.lap(4);
-    if (p.prof && blockIdx.x == 0 && threadIdx.x == 0) p.prof[5] += 1;
-    if (S.fast) draws += m;
-    cur ^= 1;
-    a += W;
+  __shared__ Fixed F;
+  Tile T = carve(g_dsm, p.w.n_words, p.ws_bytes);
+  const bool timer = p.prof && blockIdx.x == 0 && threadIdx.x == 0;
+  if (timer) {
+    for (int k = 0; k < 8; ++k) F.acc[k] = 0;
+    F.tclk = global_ns();
   }
-  const uint64_t m = __ldcg(p.ctrl + kM);
-  const uint32_t* act = act_list(p, cur);
-  for (uint64_t e = blockIdx.x * (uint64_t)kB + threadIdx.x; e < m; e += (uint64_t)gridDim.x * kB)
-    p.valid[act[e]] = 0;  // K attempts exhausted: mark_invalid
-  if (blockIdx.x == 0 && threadIdx.x == 0) p.ctrl[kCur] = cur;
-  flush(p, L);
-}
-
-// Host-loop variants (sharded runs: the rank exchange happens between rounds).
-__global__ void __launch_bounds__(kB) k_init_count(PlaceParams p) {
-  compact_count(p, p.w.n, [&](uint64_t i) -> int { return p.valid[i] != 0; });
-}
-__global__ void __launch_bounds__(kB) k_init_scatter(PlaceParams p) {
-  compact_scatter(p, p.w.n, [&](uint64_t i) -> int { return p.valid[i] != 0; },
-                  [&](uint64_t i) -> uint32_t { return (uint32_t)i; }, p.act0);
-}
-__global__ void __launch_bounds__(kB) k_phase_a(PlaceParams p, int32_t attempt, int cur) {
-  SbGeom gA = p.w.geoms[p.pl.geom];
-  const uint64_t m = __ldcg(p.ctrl + kM);
-  __shared__ Shared sh;
+  SbGeom gA;
+  block_setup(p, F, gA);
   Local L;
   const Sampling S = resolve_sampling(p);
-  phase_a(p, S, gA, sh, act_list(p, cur), m, p.spec_width, p.draw_base, attempt, L);
+  if (!S.fast) {
+    if (p.vary_flag && blockIdx.x == 0 && threadIdx.x == 0)
+      atomicAdd(p.counters + 7, 1ull);  // per-instance placement
+    const unsigned long long t6 = timer ? global_ns() : 0;
+    instance_tiles(p, S, gA, T, F, L);
+    if (timer) F.acc[6] += global_ns() - t6;
+  } else {
+    cg::grid_group grid = cg::this_grid();
+    for (uint32_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+      const uint32_t n = tile_load_valid(p, T, F, t);
+      store_list(p, T, t, n, p.tile_cnt);
+      __syncthreads();
+    }
+    lap(p, F, 0);
+    grid.sync();
+    lap(p, F, 5);
+    uint64_t draws = 0;
+    int32_t a = 0;
+    for (; a < p.attempts; ++a) {
+      unsigned long long r0 = 0;
+      if (p.dbg && threadIdx.x == 0) {
+        r0 = global_ns();
+        F.ta = F.tb = 0;
+      }
+      const uint64_t total = fast_round(p, S, gA, T, F, a, draws, L, nullptr);
+      if (total == 0) break;
+      draws += total;
+      if (p.dbg && threadIdx.x == 0) {  // per-round maxima over CTAs: work, A1, A2+B
+        atomicMax(p.dbg + 3 * a, (unsigned)(global_ns() - r0));
+        atomicMax(p.dbg + 3 * a + 1, (unsigned)F.ta);
+        atomicMax(p.dbg + 3 * a + 2, (unsigned)F.tb);
+      }
+      lap(p, F, 1);
+      grid.sync();
+      lap(p, F, 5);
+      if (timer) F.acc[7] += 1;
+    }
+    if (a == p.attempts) {  // K attempts exhausted: survivors are invalid
+      const uint32_t* cin = p.tile_cnt + (size_t)(a & 1) * p.cnt_stride;
+      for (uint32_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+        const uint32_t n = __ldcg(cin + t);
+        if (n == 0) continue;
+        load_list(p, T, t, n);
+        mark_invalid(p, T, n);
+        __syncthreads();
+      }
+    }
+  }
+  if (timer)
+    for (int k = 0; k < 8; ++k) p.prof[k] += F.acc[k];
   flush(p, L);
-}
-__global__ void __launch_bounds__(kB) k_phase_b(PlaceParams p, int cur) {
-  __shared__ Shared sh;
-  SbGeom gA;
-  block_setup(p, sh, gA);
-  Local L;
-  phase_b(p, sh, act_list(p, cur), p.spec_width, L);
-  flush(p, L);
-}
-__global__ void __launch_bounds__(kB) k_phase_c(PlaceParams p, int32_t attempt, int cur) {
-  Local L;
-  const uint64_t m = __ldcg(p.ctrl + kM);
-  phase_c(p, act_list(p, cur), m, p.spec_width, attempt, L);
-  flush(p, L);
-}
-__global__ void __launch_bounds__(kB) k_phase_d(PlaceParams p, int cur) {
-  const uint64_t m = __ldcg(p.ctrl + kM);
-  const uint32_t* act = act_list(p, cur);
-  compact_scatter(p, m, [&](uint64_t e) -> int { return p.failflag[e]; },
-                  [&](uint64_t e) -> uint32_t { return act[e]; }, act_list(p, cur ^ 1));
-}
-__global__ void __launch_bounds__(kB) k_finish(PlaceParams p, int cur) {
-  const uint64_t m = __ldcg(p.ctrl + kM);
-  const uint32_t* act = act_list(p, cur);
-  for (uint64_t e = blockIdx.x * (uint64_t)kB + threadIdx.x; e < m; e += (uint64_t)gridDim.x * kB)
-    p.valid[act[e]] = 0;
 }
 
-int g_coop_blocks = -1;
+// Sharded building blocks (no grid barrier inside a launch).
+__global__ void __launch_bounds__(kB, 2) k_place_instances(PlaceParams p) {
+  __shared__ Fixed F;
+  Tile T = carve(g_dsm, p.w.n_words, p.ws_bytes);
+  SbGeom gA;
+  block_setup(p, F, gA);
+  Local L;
+  Sampling S{0, nullptr, nullptr, 0};
+  instance_tiles(p, S, gA, T, F, L);
+  flush(p, L);
+}
+
+__global__ void __launch_bounds__(kB, 2) k_fast_init(PlaceParams p) {
+  __shared__ Fixed F;
+  Tile T = carve(g_dsm, p.w.n_words, p.ws_bytes);
+  uint32_t mine = 0;
+  for (uint32_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+    const uint32_t n = tile_load_valid(p, T, F, t);
+    store_list(p, T, t, n, p.tile_cnt);
+    mine += n;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && mine) atomicAdd(p.ctrl + place_total_word(0), mine);
+}
+
+__global__ void __launch_bounds__(kB, 2) k_fast_round(PlaceParams p, int32_t a) {
+  __shared__ Fixed F;
+  Tile T = carve(g_dsm, p.w.n_words, p.ws_bytes);
+  SbGeom gA;
+  block_setup(p, F, gA);
+  Local L;
+  Sampling S{1, p.canon_tris, p.canon_cum, p.canon_n};
+  fast_round(p, S, gA, T, F, a, p.draw_base, L, p.ctrl + place_total_word(a + 1));
+  flush(p, L);
+}
+
+__global__ void __launch_bounds__(kB) k_fast_finish(PlaceParams p, int32_t a) {
+  const uint32_t* cin = p.tile_cnt + (size_t)(a & 1) * p.cnt_stride;
+  for (uint32_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+    const uint32_t n = __ldcg(cin + t);
+    const uint32_t* src = p.tile_list + (uint64_t)t * p.tile_inst;
+    for (uint32_t e = threadIdx.x; e < n; e += kB) p.valid[src[e]] = 0;
+  }
+}
 
 void check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-unsigned host_grid() {
-  static unsigned g = 0;
-  if (g == 0) {
-    int dev = 0, sms = 0, per = 0;
-    check(cudaGetDevice(&dev), "cudaGetDevice");
-    check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
-    check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_phase_b, kB, 0), "occupancy");
-    g = (unsigned)(sms * (per > 0 ? per : 1));
-  }
-  return g;
+void set_smem(const void* fn, size_t smem) {
+  check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+        "cudaFuncSetAttribute(smem)");
 }
 
 }  // namespace
+
+int place_ws_bytes(int max_tris, int max_nodes) { return warp_scratch_bytes(max_tris, max_nodes); }
+
+size_t place_smem_bytes(int n_words, int ws_bytes) {
+  return tile_bytes(n_words) + (size_t)kWarps * ws_bytes;
+}
 
 void narrow_profile(unsigned long long out[8], bool reset) {
   check(cudaMemcpyFromSymbol(out, g_nprof, 8 * sizeof(unsigned long long)), "narrow_profile");
@@ -532,45 +632,45 @@ void narrow_profile(unsigned long long out[8], bool reset) {
   }
 }
 
-int place_grid_warps(int num_sms) {
-  if (g_coop_blocks < 0) {
-    int per = 0;
-    check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_place, kB, 0), "occupancy");
-    g_coop_blocks = per * num_sms;
-  }
-  return g_coop_blocks * kWarps;
+int place_grid(int num_sms, size_t smem) {
+  set_smem((const void*)k_place, smem);
+  int per = 0;
+  check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_place, kB, smem), "occupancy");
+  return per * num_sms;
 }
 
-bool place_persistent(const PlaceParams& p, int num_sms, sb_stream_t s) {
-  if (place_grid_warps(num_sms) <= 0) return false;
-  unsigned grid = (unsigned)g_coop_blocks;
+bool place_persistent(const PlaceParams& p, unsigned grid, size_t smem, sb_stream_t s) {
+  if (grid == 0) return false;
   PlaceParams q = p;
   void* args[] = {&q};
-  check(cudaLaunchCooperativeKernel((void*)k_place, dim3(grid), dim3(kB), args, 0,
+  check(cudaLaunchCooperativeKernel((void*)k_place, dim3(grid), dim3(kB), args, smem,
                                     reinterpret_cast<cudaStream_t>(s)),
         "cudaLaunchCooperativeKernel(k_place)");
   return true;
 }
 
-void place_init(const PlaceParams& p, sb_stream_t s) {
-  unsigned g = host_grid();
-  k_init_count<<<g, kB, 0, s>>>(p);
-  k_init_scatter<<<g, kB, 0, s>>>(p);
-  check(cudaGetLastError(), "place_init");
+void place_instances(const PlaceParams& p, unsigned grid, size_t smem, sb_stream_t s) {
+  set_smem((const void*)k_place_instances, smem);
+  k_place_instances<<<grid, kB, smem, s>>>(p);
+  check(cudaGetLastError(), "k_place_instances");
 }
 
-void place_round(const PlaceParams& p, int32_t attempt, int cur, sb_stream_t s) {
-  unsigned g = host_grid();
-  k_phase_a<<<g, kB, 0, s>>>(p, attempt, cur);
-  k_phase_b<<<g, kB, 0, s>>>(p, cur);
-  k_phase_c<<<g, kB, 0, s>>>(p, attempt, cur);
-  k_phase_d<<<g, kB, 0, s>>>(p, cur);
-  check(cudaGetLastError(), "place_round");
+void place_fast_init(const PlaceParams& p, unsigned grid, size_t smem, sb_stream_t s) {
+  set_smem((const void*)k_fast_init, smem);
+  k_fast_init<<<grid, kB, smem, s>>>(p);
+  check(cudaGetLastError(), "k_fast_init");
 }
 
-void place_finish(const PlaceParams& p, int cur, sb_stream_t s) {
-  k_finish<<<host_grid(), kB, 0, s>>>(p, cur);
-  check(cudaGetLastError(), "place_finish");
+void place_fast_round(const PlaceParams& p, int32_t attempt, unsigned grid, size_t smem,
+                      sb_stream_t s) {
+  set_smem((const void*)k_fast_round, smem);
+  k_fast_round<<<grid, kB, smem, s>>>(p, attempt);
+  check(cudaGetLastError(), "k_fast_round");
+}
+
+void place_fast_finish(const PlaceParams& p, int32_t attempt, unsigned grid, sb_stream_t s) {
+  k_fast_finish<<<grid, kB, 0, s>>>(p, attempt);
+  check(cudaGetLastError(), "k_fast_finish");
 }
 
 }  // namespace sbk

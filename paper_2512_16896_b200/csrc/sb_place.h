@@ -1,25 +1,32 @@
-// Phased placement engine: one placement's whole attempt loop on the device.
+// Tiled placement engine: one placement's whole attempt loop on the device.
 //
-// A round (= one attempt over the still-failing instances) runs as four
-// grid-wide phases:
-//   A  warp per active slot: sample (FIFO jump-ahead or counter stream), yaw, pose compose,
-//      candidate AABB + inverse pose, AABB broad phase with lanes over objects; overlapping
-//      (slot, object) pairs are appended to a pair queue
-//   B  warp per pair: exact MeshBvh::collide (sb_warp.cuh) -> atomicMin(contact[slot], obj)
-//   C  thread per slot: first-valid accept (update_transform + set_enabled) or fail flag;
-//      reference-equivalent narrow-phase count; per-chunk failure counts
-//   D  stable compaction of the failing slots into the next round's active list
-// Per-instance (counter-stream) regions: attempt a of instance i depends only on
-// make_stream(run_seed, {salt, tag, i, a}) and on instance i's world, which is unchanged
-// until i accepts. A round may therefore evaluate W consecutive attempts of every remaining
-// instance at once ("virtual slots") and accept the lowest free one -- the sequential
-// first-valid result; counters are reported as the sequential loop would have counted
-// them. The FIFO fast path couples instances through the draw index, so W = 1 there.
-// Every (candidate, object) pair of a round is evaluated in parallel; contact_object is the
-// minimum colliding object id, i.e. the reference's first hit in ascending order
-// (collision.cpp:439-448). Single GPU: one cooperative kernel loops over all rounds with
-// grid.sync() between phases. Sharded: the host launches the phases per round and
-// exchanges the per-rank counts between rounds.
+// The instances of a shard are cut into `ntiles` contiguous ranges ("tiles") of at most
+// `tile_inst` (<= kPlaceBlock) instances. A tile is owned by one CTA for a round, and
+// everything one attempt round does to it stays in that CTA's shared memory:
+//   A1  thread per slot: sample (FIFO jump-ahead or counter stream), yaw, pose compose,
+//       candidate AABB + inverse pose (sampler.cpp:70-156, transform.hpp:40-69)
+//   A2  thread per (slot, object): AABB broad phase (collision.cpp:439-443); overlapping
+//       pairs go to a shared-memory queue
+//   B   warp per queued pair: exact MeshBvh::collide (sb_warp.cuh) -> atomicMin on the
+//       slot's contact object (the reference's first hit in ascending object order)
+//   C   thread per instance: first-valid accept (update_transform + set_enabled) or keep
+//       the instance for the next attempt; survivors are compacted in place
+// so a round has no grid-wide phase barrier. Tiles keep their own survivors, which makes
+// the global active order (tile order, then ascending instance inside a tile) the
+// reference's ascending `active` order at every attempt.
+//
+// FIFO fast path (canonical region, sampler.cpp:78-99): instance i at attempt a takes draw
+// j = sum_{a'<a} |active_a'| + rank_a(i), so tiles advance in lockstep: per round every CTA
+// scans the per-tile survivor counts once (its tiles' draw offsets + the round total) and
+// the round ends with ONE grid barrier. Per-instance regions (counter streams
+// make_stream(run_seed, {salt, "fall"|"yaw!", inst, attempt}), sampler.cpp:101-156): tiles
+// are independent, so a CTA runs a tile to completion with no grid barrier at all, and
+// evaluates W consecutive attempts of each survivor at once ("speculative slots"; W grows
+// as the tile empties) -- attempt a of instance i depends only on its stream and on
+// instance i's world, which is unchanged until i accepts, so accepting the lowest free
+// slot is exactly the sequential first-valid result.
+// Single GPU: one cooperative launch per placement. Sharded (multi-GPU): the fast path runs
+// one launch per round with the per-rank counts exchanged on the host in between.
 #pragma once
 
 #include <cstddef>
@@ -47,24 +54,19 @@ struct PlaceParams {
   const int32_t* inst_n;
   uint8_t* valid;               // [n]
   int16_t* accepted;            // [n] of this placement
-  uint32_t* act0;               // active lists (ping-pong), slot -> local instance
-  uint32_t* act1;
-  double* cpose;                // [n][12] candidate pose per slot
-  double* cinv;                 // [n][12] candidate inverse pose per slot
-  uint8_t* cflag;               // [n] 1 = placeable (checked)
-  int32_t* contact;             // [n] min colliding object, INT32_MAX = free
-  uint32_t* ovmask;             // [words][n] overlap bits per slot
-  uint8_t* failflag;            // [n]
-  uint64_t* pairs;              // pair queue (slot << 32 | object)
-  uint64_t pair_cap;
-  uint32_t* chunk_cnt;          // [ceil(n / 256)]
-  uint32_t* ctrl;               // [0] M, [1] pair count, [2] rounds, [3] error, [4] cur list
+  uint32_t* tile_list;          // [ntiles * tile_inst] survivors of each tile
+  uint32_t* tile_cnt;           // [2][cnt_stride] survivors per tile, ping-pong by round
+  uint32_t cnt_stride;
+  uint32_t ntiles;
+  int32_t tile_inst;            // instances per tile (<= kPlaceBlock)
+  int32_t spec_target;          // per-instance path: target slots per tile round
+  int32_t ws_bytes;             // narrow-phase scratch per warp (sb_warp.cuh)
+  int32_t max_tris, max_nodes;  // scratch geometry bounds over the world's geometries
+  uint32_t* ctrl;               // [8] per placement: see Ctrl in sb_place.cu
   unsigned long long* counters; // [8]
-  uint64_t draw_base;           // sharded host loop: this rank's first draw index
-  uint64_t slot_cap;            // capacity of the per-slot candidate arrays
-  uint64_t spec_budget;         // target candidates per round for speculative attempts
-  int32_t spec_width;           // host loop: attempts per instance this round (1 = none)
-  uint64_t* prof;               // optional phase timers (ns) [init, A, B, C, D, rounds]
+  uint64_t draw_base;           // sharded fast path: draws before this rank this round
+  unsigned* dbg;                // optional [attempts][3] per-round CTA maxima (ns), fast path
+  uint64_t* prof;               // optional timers (ns) [init, rounds, -, -, -, rounds]
   // Relation placements on one GPU: the path is chosen on the device. When non-null,
   // *vary_flag != 0 selects the per-instance tables, else the FIFO fast path samples the
   // canonical region_for(0) = local instance 0's table (relationships.cpp:188-190).
@@ -72,18 +74,30 @@ struct PlaceParams {
 };
 
 constexpr int kPlaceBlock = 256;
+constexpr int kPlaceMaxOwnedTiles = 64;  // tiles per CTA on the fast path
 
-// Single GPU: whole placement in one cooperative launch. Returns false if the device
-// cannot co-schedule the grid (caller falls back to the host loop).
-bool place_persistent(const PlaceParams& p, int num_sms, sb_stream_t s);
-// Warps of the co-resident persistent grid (sizes the speculative-attempt budget).
-int place_grid_warps(int num_sms);
+// Dynamic shared memory of one placement CTA for a world with `n_words` enable words.
+size_t place_smem_bytes(int n_words, int ws_bytes);
+// Narrow-phase scratch bytes per warp for the given geometry bounds.
+int place_ws_bytes(int max_tris, int max_nodes);
+// Co-resident CTAs of the persistent placement kernel (0 if it cannot be launched).
+int place_grid(int num_sms, size_t smem);
+// Single GPU: whole placement in one cooperative launch.
+bool place_persistent(const PlaceParams& p, unsigned grid, size_t smem, sb_stream_t s);
 // Cycle breakdown of the narrow phase (zeros unless built with -DSB_NARROW_PROF).
 void narrow_profile(unsigned long long out[8], bool reset);
-// Host loop building blocks (sharded runs): init active list, then per round
-// phase_abcd(draw_base) with the count read back in between.
-void place_init(const PlaceParams& p, sb_stream_t s);
-void place_round(const PlaceParams& p, int32_t attempt, int cur, sb_stream_t s);
-void place_finish(const PlaceParams& p, int cur, sb_stream_t s);
+// Sharded runs. Per-instance path: one launch, no exchange (place_instances). Fast path:
+// place_fast_init, then per round place_fast_round (ctrl[kTotal + (a+1)&1] receives the
+// survivors; the host zeroes it before the launch), then place_fast_finish.
+void place_instances(const PlaceParams& p, unsigned grid, size_t smem, sb_stream_t s);
+void place_fast_init(const PlaceParams& p, unsigned grid, size_t smem, sb_stream_t s);
+void place_fast_round(const PlaceParams& p, int32_t attempt, unsigned grid, size_t smem,
+                      sb_stream_t s);
+void place_fast_finish(const PlaceParams& p, int32_t attempt, unsigned grid, sb_stream_t s);
+// ctrl word receiving the survivor total of round `attempt` (fast path, sharded)
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+constexpr int place_total_word(int32_t attempt) { return 5 + (attempt & 1); }
 
 }  // namespace sbk

@@ -29,20 +29,39 @@ constexpr unsigned kFull = 0xffffffffu;
 struct RegionScratch {
   double x[2][kCap], y[2][kCap];
   double area[kCap];
+  double cum[kCap];
 };
 
-__device__ __forceinline__ double ring_area_seq(const double* x, const double* y, int n) {
-  double s = 0.0;
-  for (int i = 0; i < n; ++i) {
-    const int j = (i + 1) % n;
-    s += x[i] * y[j] - x[j] * y[i];
+// ring_area (polygon.cpp:58-66): the shoelace terms in parallel, their sum on lane 0 in
+// the reference's left-to-right order (bit-identical to sbp::ring_area). All lanes call;
+// every lane gets the result.
+__device__ __noinline__ double warp_ring_area(const double* x, const double* y, int n, double* tmp) {
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < n; i += 32) {
+    const int j = i + 1 == n ? 0 : i + 1;
+    tmp[i] = x[i] * y[j] - x[j] * y[i];
   }
+  __syncwarp();
+  double s = 0.0;
+  if (lane == 0) {
+#pragma unroll 8
+    for (int i = 0; i < n; ++i) s += tmp[i];
+  }
+  s = __shfl_sync(kFull, s, 0);
+  __syncwarp();
   return 0.5 * s;
+}
+
+// Exclusive warp prefix count of `flag` over lanes; returns this lane's offset.
+__device__ __forceinline__ int lane_rank(bool flag, int& total) {
+  const unsigned m = __ballot_sync(kFull, flag);
+  total = __popc(m);
+  return __popc(m & ((1u << (threadIdx.x & 31)) - 1u));
 }
 
 // One Sutherland-Hodgman pass (same arithmetic and output order as sbp::clip_half);
 // returns the output size, or -1 on overflow.
-__device__ int warp_clip(const double* ix, const double* iy, int n, double* ox, double* oy,
+__device__ __noinline__ int warp_clip(const double* ix, const double* iy, int n, double* ox, double* oy,
                          int axis, double bound, bool keep_ge) {
   const int lane = threadIdx.x & 31;
   int base = 0;
@@ -207,9 +226,7 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
 
   // ---- intersect with the support rect (oracle Boost stand-in): correct() orientation
   if (n < 3) return {sbp::kRegionEmpty, 0};
-  double ar = 0.0;
-  if (lane == 0) ar = ring_area_seq(X, Y, n);
-  ar = __shfl_sync(kFull, ar, 0);
+  const double ar = warp_ring_area(X, Y, n, sc.area);
   if (ar < 0.0) {  // reverse the closed ring: p0 stays first
     for (int i = 1 + lane; i < n - i; i += 32) {
       const int j = n - i;
@@ -228,58 +245,93 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
   if (n >= 0) n = warp_clip(sc.x[0], sc.y[0], n, sc.x[1], sc.y[1], 1, y0, true);
   if (n >= 0) n = warp_clip(sc.x[1], sc.y[1], n, sc.x[0], sc.y[0], 1, y1, false);
   if (n < 0) return {sbp::kRegionOverflow, 0};
-  // drop consecutive exact duplicates (keep the first of each run), then trailing copies
-  // of vertex 0 -- lane 0, sequential like the stand-in
+  // drop consecutive exact duplicates (keep the first of each run; == is transitive, so
+  // comparing with the previous vertex equals comparing with the last kept one), then
+  // trailing copies of vertex 0. Out of place: buffer 0 -> buffer 1.
+  double* X1 = sc.x[1];
+  double* Y1 = sc.y[1];
   int m = 0;
-  if (lane == 0) {
-    for (int i = 0; i < n; ++i) {
-      if (m == 0 || X[i] != X[m - 1] || Y[i] != Y[m - 1]) {
-        X[m] = X[i];
-        Y[m] = Y[i];
-        ++m;
-      }
+  for (int i0 = 0; i0 < n; i0 += 32) {
+    const int i = i0 + lane;
+    bool keep = false;
+    double xi = 0.0, yi = 0.0;
+    if (i < n) {
+      xi = X[i];
+      yi = Y[i];
+      keep = i == 0 || xi != X[i - 1] || yi != Y[i - 1];
     }
-    while (m > 1 && X[0] == X[m - 1] && Y[0] == Y[m - 1]) --m;
-    if (m >= 3 && ring_area_seq(X, Y, m) == 0.0) m = 0;
+    int tot;
+    const int r = lane_rank(keep, tot);
+    if (keep) {
+      X1[m + r] = xi;
+      Y1[m + r] = yi;
+    }
+    m += tot;
   }
-  m = __shfl_sync(kFull, m, 0);
   __syncwarp();
+  if (lane == 0)
+    while (m > 1 && X1[0] == X1[m - 1] && Y1[0] == Y1[m - 1]) --m;
+  m = __shfl_sync(kFull, m, 0);
+  double area1 = 0.0;
+  if (m >= 3) {
+    area1 = warp_ring_area(X1, Y1, m, sc.area);
+    if (area1 == 0.0) m = 0;
+  }
   if (m < 3) return {sbp::kRegionEmpty, 0};
 
-  // ---- triangulate (polygon.cpp:344-368) + ear_clip_ring (:260-340): orientation,
-  // tolerance-based duplicate drop (lane 0, order-dependent), then the fan fast path
-  int k = 0;
+  // ---- triangulate (polygon.cpp:344-368) + ear_clip_ring (:260-340): orientation (same
+  // ring, same area), tolerance-based duplicate drop, then the fan fast path
+  if (area1 < 0.0) {
+    for (int i = lane; i < m - 1 - i; i += 32) {
+      const int j = m - 1 - i;
+      const double tx = X1[i], ty = Y1[i];
+      X1[i] = X1[j];
+      Y1[i] = Y1[j];
+      X1[j] = tx;
+      Y1[j] = ty;
+    }
+    __syncwarp();
+  }
+  // The drop compares each vertex with the last KEPT one (not transitive): if no
+  // consecutive pair is within tolerance nothing is dropped; otherwise lane 0 runs the
+  // sequential loop.
+  bool close = false;
+  for (int i = 1 + lane; i < m; i += 32) {
+    const double dx = X1[i] - X1[i - 1], dy = Y1[i] - Y1[i - 1];
+    if (!(dx * dx + dy * dy > 1e-24)) close = true;
+  }
+  int k = m;
+  if (__any_sync(kFull, close)) {
+    if (lane == 0) {
+      k = 0;
+      for (int i = 0; i < m; ++i) {
+        if (k > 0) {
+          const double dx = X1[i] - X1[k - 1], dy = Y1[i] - Y1[k - 1];
+          if (!(dx * dx + dy * dy > 1e-24)) continue;
+        }
+        X1[k] = X1[i];
+        Y1[k] = Y1[i];
+        ++k;
+      }
+    }
+    k = __shfl_sync(kFull, k, 0);
+    __syncwarp();
+  }
   if (lane == 0) {
-    if (ring_area_seq(X, Y, m) < 0.0) {
-      for (int i = 0, j = m - 1; i < j; ++i, --j) {
-        double tx = X[i], ty = Y[i];
-        X[i] = X[j];
-        Y[i] = Y[j];
-        X[j] = tx;
-        Y[j] = ty;
-      }
-    }
-    for (int i = 0; i < m; ++i) {
-      if (k > 0) {
-        const double dx = X[i] - X[k - 1], dy = Y[i] - Y[k - 1];
-        if (!(dx * dx + dy * dy > 1e-24)) continue;
-      }
-      X[k] = X[i];
-      Y[k] = Y[i];
-      ++k;
-    }
     while (k > 1) {
-      const double dx = X[0] - X[k - 1], dy = Y[0] - Y[k - 1];
+      const double dx = X1[0] - X1[k - 1], dy = Y1[0] - Y1[k - 1];
       if (dx * dx + dy * dy <= 1e-24) --k;
       else break;
     }
   }
   k = __shfl_sync(kFull, k, 0);
   __syncwarp();
+  X = X1;
+  Y = Y1;
   if (k < 3) return {sbp::kRegionOk, 0};  // valid() == false -> placeable = 0
   bool ok = true;
   for (int i = lane; i < k; i += 32) {
-    const int a = (i + k - 1) % k, c = (i + 1) % k;
+    const int a = i == 0 ? k - 1 : i - 1, c = i + 1 == k ? 0 : i + 1;
     if (sbp::cross2(X[a], Y[a], X[i], Y[i], X[c], Y[c]) < 0.0) ok = false;
     if (i + 3 < k) {
       const double cr = sbp::cross2(X[k - 1], Y[k - 1], X[i], Y[i], X[i + 1], Y[i + 1]);
@@ -289,36 +341,46 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
   const bool fan = __all_sync(kFull, ok);
   int ntri = 0;
   if (fan) {
-    // triangle i = (k-1, i, i+1); keep area > 0 (PolygonSampler ctor, polygon.cpp:374-375)
-    for (int i = lane; i + 2 < k; i += 32)
-      sc.area[i] = 0.5 * fabs(sbp::cross2(X[k - 1], Y[k - 1], X[i], Y[i], X[i + 1], Y[i + 1]));
+    // triangle i = (k-1, i, i+1); keep area > 0 (PolygonSampler ctor, polygon.cpp:374-375):
+    // areas and output slots in parallel, the running total on lane 0 in order, the
+    // normalisation (polygon.cpp:381-387) in parallel again.
+    const int nt = k - 2;
+    int slot[(kCap + 31) / 32];
+    for (int i0 = 0, c = 0; i0 < nt; i0 += 32, ++c) {
+      const int i = i0 + lane;
+      double a = 0.0;
+      if (i < nt) a = 0.5 * fabs(sbp::cross2(X[k - 1], Y[k - 1], X[i], Y[i], X[i + 1], Y[i + 1]));
+      int tot;
+      const int r = lane_rank(a > 0.0, tot);
+      slot[c] = a > 0.0 ? ntri + r : -1;
+      if (a > 0.0) sc.area[ntri + r] = a;
+      ntri += tot;
+    }
     __syncwarp();
+    if (ntri > cap) return {sbp::kRegionOverflow, 0};
+    double total = 0.0;
     if (lane == 0) {
-      double total = 0.0;
-      for (int i = 0; i + 2 < k; ++i) {
-        const double a = sc.area[i];
-        if (a <= 0.0) continue;
-        if (ntri >= cap) {
-          ntri = -1;
-          break;
-        }
-        SbRegionTri& t = tris[ntri];
+#pragma unroll 8
+      for (int j = 0; j < ntri; ++j) {
+        total += sc.area[j];
+        sc.cum[j] = total;
+      }
+    }
+    total = __shfl_sync(kFull, total, 0);
+    __syncwarp();
+    if (ntri > 0 && !(total > 0.0)) ntri = 0;
+    for (int i0 = 0, c = 0; i0 < nt; i0 += 32, ++c) {
+      const int i = i0 + lane;
+      const int j = slot[c];
+      if (i < nt && j >= 0 && ntri > 0) {
+        SbRegionTri& t = tris[j];
         t.a[0] = X[k - 1];
         t.a[1] = Y[k - 1];
         t.b[0] = X[i];
         t.b[1] = Y[i];
         t.c[0] = X[i + 1];
         t.c[1] = Y[i + 1];
-        total += a;
-        cum[ntri++] = total;
-      }
-      if (ntri > 0) {  // polygon.cpp:381-387
-        if (total > 0.0) {
-          for (int j = 0; j < ntri; ++j) cum[j] /= total;
-          cum[ntri - 1] = 1.0;
-        } else {
-          ntri = 0;
-        }
+        cum[j] = j == ntri - 1 ? 1.0 : sc.cum[j] / total;
       }
     }
   } else if (lane == 0) {  // general ear clipping (reflex or sliver corners): restatement

@@ -411,21 +411,23 @@ struct sb_engine {
 
   DevArray<uint8_t> d_valid;
   DevArray<int16_t> d_accepted;
-  DevArray<uint32_t> d_act[2];
-  DevArray<uint8_t> d_fail;
-  DevArray<double> d_cpose, d_cinv;
-  DevArray<uint8_t> d_cflag;
-  DevArray<int32_t> d_contact;
-  DevArray<uint32_t> d_ovmask;
-  DevArray<uint64_t> d_pairs;
-  DevArray<uint32_t> d_chunk;
+  DevArray<uint32_t> d_tile_list;   // [ntiles * tile_inst] survivors per tile
+  DevArray<uint32_t> d_tile_cnt;    // [2][ntiles]
   DevArray<uint32_t> d_ctrl;
   DevArray<uint64_t> d_prof;
+  DevArray<unsigned> d_dbg;        // SB_ROUND_DEBUG=1: per-round CTA maxima (fast path)
+  bool round_debug = false;
+  double last_dbg[3] = {0, 0, 0};
   DevArray<int32_t> d_rflags;
   std::vector<cudaEvent_t> ev_place;
-  double last_prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  double last_prof[16] = {};
   int num_sms = 0;
-  uint64_t spec_budget = 0, slot_cap = 0;
+  // tile decomposition of the shard (sb_place.h) and launch shape of the placement kernel
+  uint32_t ntiles = 0;
+  int tile_inst = 0, max_tris = 1, max_nodes = 1, ws_bytes = 0;
+  int spec_target = 64;
+  unsigned grid = 0;
+  size_t smem = 0;
   DevArray<unsigned long long> d_counters;
   DevArray<double> d_anchor;
   DevArray<double> d_s0;
@@ -596,26 +598,31 @@ struct sb_engine {
     d_flags.alloc(2);
     d_valid.alloc(n);
     d_accepted.alloc(std::max<size_t>(1, P) * n);
-    d_act[0].alloc(n);
-    d_act[1].alloc(n);
-    d_fail.alloc(n);
     cuda_check(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, world->device), "attr");
-    spec_budget = 2ull * static_cast<uint64_t>(sbk::place_grid_warps(num_sms));
-    slot_cap = std::max<uint64_t>(n, spec_budget);
-    d_cpose.alloc(12 * slot_cap);
-    d_cinv.alloc(12 * slot_cap);
-    d_cflag.alloc(slot_cap);
-    d_contact.alloc(slot_cap);
-    {
-      const size_t words = (world->obj_geom.size() + 31) / 32;
-      d_ovmask.alloc(std::max<size_t>(1, words) * slot_cap);
-      const size_t per = std::min<size_t>(world->obj_geom.size(), 32);
-      d_pairs.alloc(std::max<size_t>(1, per) * slot_cap);
+    for (const auto& g : world->geoms) {
+      max_tris = std::max(max_tris, static_cast<int>(g.g.n_tris));
+      max_nodes = std::max(max_nodes, static_cast<int>(g.g.n_nodes));
     }
-    d_chunk.alloc(n / 256 + 2);
+    ws_bytes = sbk::place_ws_bytes(max_tris, max_nodes);
+    smem = sbk::place_smem_bytes(world->view().n_words, ws_bytes);
+    grid = static_cast<unsigned>(sbk::place_grid(num_sms, smem));
+    if (grid == 0) throw CudaError("placement kernel does not fit on the device (shared memory)");
+    {  // tiles: a multiple of the grid, at most kPlaceBlock instances each
+      const uint64_t per_wave = static_cast<uint64_t>(grid) * sbk::kPlaceBlock;
+      const uint64_t waves = (n + per_wave - 1) / per_wave;
+      const uint64_t want = static_cast<uint64_t>(grid) * waves;
+      tile_inst = static_cast<int>((n + want - 1) / want);
+      ntiles = static_cast<uint32_t>((n + tile_inst - 1) / tile_inst);
+      if ((ntiles + grid - 1) / grid > static_cast<uint32_t>(sbk::kPlaceMaxOwnedTiles))
+        throw std::invalid_argument("shard too large for one device: " + std::to_string(n) + " instances");
+    }
+    d_tile_list.alloc(static_cast<size_t>(ntiles) * tile_inst);
+    d_tile_cnt.alloc(2 * static_cast<size_t>(ntiles));
     d_ctrl.alloc(8 * std::max<size_t>(1, places.size()));
     d_rflags.alloc(2 * std::max<size_t>(1, places.size()));
     d_prof.alloc(8);
+    round_debug = std::getenv("SB_ROUND_DEBUG") != nullptr;
+    if (round_debug) d_dbg.alloc(3 * static_cast<size_t>(attempts) * std::max<size_t>(1, places.size()));
     d_counters.alloc(8);
     cuda_check(cudaEventCreate(&ev_start), "event");
     cuda_check(cudaEventCreate(&ev_stop), "event");
@@ -713,6 +720,7 @@ struct sb_engine {
     const size_t P = places.size();
     uint64_t launches = 0, rounds_host = 0, per_inst_host = 0, round_launches = 0;
     double sharded_check_ms = 0.0;
+    std::vector<char> device_rounds(places.size(), world_size == 1 ? 1 : 0);
     while (ev_place.size() < 2 * P + 2) {
       cudaEvent_t e;
       cuda_check(cudaEventCreate(&e), "event");
@@ -721,6 +729,7 @@ struct sb_engine {
     cuda_check(cudaEventRecord(ev_start, stream), "event");
     cuda_check(cudaMemsetAsync(d_counters.p, 0, 8 * sizeof(unsigned long long), stream), "memset");
     cuda_check(cudaMemsetAsync(d_prof.p, 0, 8 * sizeof(uint64_t), stream), "memset");
+    if (round_debug) cuda_check(cudaMemsetAsync(d_dbg.p, 0, d_dbg.count * sizeof(unsigned), stream), "memset");
     cuda_check(cudaMemsetAsync(d_ctrl.p, 0, d_ctrl.count * sizeof(uint32_t), stream), "memset");
     cuda_check(cudaMemsetAsync(d_rflags.p, 0, d_rflags.count * sizeof(int32_t), stream), "memset");
     sbk::engine_reset(wv, first_place_obj, static_cast<int32_t>(P), d_valid.p, d_accepted.p,
@@ -770,42 +779,51 @@ struct sb_engine {
       pp.inst_n = d_inst_n.p;
       pp.valid = d_valid.p;
       pp.accepted = d_accepted.p + p * n;
-      pp.act0 = d_act[0].p;
-      pp.act1 = d_act[1].p;
-      pp.cpose = d_cpose.p;
-      pp.cinv = d_cinv.p;
-      pp.cflag = d_cflag.p;
-      pp.contact = d_contact.p;
-      pp.ovmask = d_ovmask.p;
-      pp.failflag = d_fail.p;
-      pp.pairs = d_pairs.p;
-      pp.pair_cap = d_pairs.count;
-      pp.chunk_cnt = d_chunk.p;
+      pp.tile_list = d_tile_list.p;
+      pp.tile_cnt = d_tile_cnt.p;
+      pp.cnt_stride = ntiles;
+      pp.ntiles = ntiles;
+      pp.tile_inst = tile_inst;
+      pp.spec_target = spec_target;
+      pp.ws_bytes = ws_bytes;
+      pp.max_tris = max_tris;
+      pp.max_nodes = max_nodes;
       pp.ctrl = d_ctrl.p + 8 * p;
       pp.counters = d_counters.p;
-      pp.slot_cap = slot_cap;
-      pp.spec_budget = spec_budget;
-      pp.spec_width = 1;
       pp.prof = d_prof.p;
+      pp.dbg = round_debug ? d_dbg.p + 3 * static_cast<size_t>(attempts) * p : nullptr;
       pp.vary_flag = (relation && world_size == 1) ? d_rflags.p + 2 * p : nullptr;
       if (world_size == 1) {
-        if (!sbk::place_persistent(pp, num_sms, s))
+        if (!sbk::place_persistent(pp, grid, smem, s))
           throw CudaError("cooperative launch of the placement kernel is not possible");
         ++launches;
         ++round_launches;
+      } else if (!fast) {
+        // per-instance regions: tiles are independent, no exchange
+        device_rounds[p] = 1;
+        cuda_check(cudaEventRecord(ev_r0, stream), "event");
+        sbk::place_instances(pp, grid, smem, s);
+        cuda_check(cudaEventRecord(ev_r1, stream), "event");
+        ++launches;
+        ++round_launches;
+        cuda_check(cudaEventSynchronize(ev_r1), "sync");
+        float ms = 0.f;
+        cuda_check(cudaEventElapsedTime(&ms, ev_r0, ev_r1), "elapsed");
+        sharded_check_ms += ms;
       } else {
-        // sharded: same phases, one launch each, with the per-round count exchange
-        uint32_t ctrl[8];
-        sbk::place_init(pp, s);
-        launches += 2;
-        auto read_ctrl = [&]() {
-          cuda_check(cudaMemcpyAsync(ctrl, pp.ctrl, sizeof ctrl, cudaMemcpyDeviceToHost, stream), "D2H ctrl");
+        // FIFO fast path: one launch per round, per-rank survivor counts exchanged between
+        uint32_t* tot = pp.ctrl;
+        auto read_total = [&](int32_t a) {
+          uint32_t v = 0;
+          cuda_check(cudaMemcpyAsync(&v, tot + sbk::place_total_word(a), 4, cudaMemcpyDeviceToHost, stream), "D2H total");
           cuda_check(cudaStreamSynchronize(stream), "sync");
+          return static_cast<uint64_t>(v);
         };
-        read_ctrl();
-        uint64_t m = ctrl[0], draws = 0;
-        int cur = 0;
-        for (int a = 0; a < attempts; ++a) {
+        sbk::place_fast_init(pp, grid, smem, s);
+        ++launches;
+        uint64_t m = read_total(0), draws = 0;
+        int32_t a = 0;
+        for (; a < attempts; ++a) {
           std::vector<uint64_t> counts = exchange({m});
           uint64_t total = 0, before = 0;
           for (int r = 0; r < world_size; ++r) {
@@ -814,24 +832,27 @@ struct sb_engine {
           }
           if (total == 0) break;
           ++rounds_host;
+          cuda_check(cudaMemsetAsync(tot + sbk::place_total_word(a + 1), 0, 4, stream), "memset");
           if (m > 0) {
             pp.draw_base = draws + before;
             cuda_check(cudaEventRecord(ev_r0, stream), "event");
-            sbk::place_round(pp, a, cur, s);
+            sbk::place_fast_round(pp, a, grid, smem, s);
             cuda_check(cudaEventRecord(ev_r1, stream), "event");
-            launches += 4;
-            round_launches += 4;
-            cur ^= 1;
-            read_ctrl();
-            m = ctrl[0];
+            launches += 1;
+            round_launches += 1;
+            m = read_total(a + 1);
             float ms = 0.f;
             cuda_check(cudaEventElapsedTime(&ms, ev_r0, ev_r1), "elapsed");
             sharded_check_ms += ms;
+          } else {
+            m = 0;
           }
-          if (fast && canon_n > 0) draws += total;
+          if (canon_n > 0) draws += total;
         }
-        sbk::place_finish(pp, cur, s);
-        ++launches;
+        if (a == attempts && m > 0) {
+          sbk::place_fast_finish(pp, a, grid, s);
+          ++launches;
+        }
       }
     }
     cuda_check(cudaEventRecord(ev_place[2 * P], stream), "event");
@@ -850,9 +871,6 @@ struct sb_engine {
         throw std::runtime_error("constraint region build failed for placement " + std::to_string(p) +
                                  " (status " + std::to_string(rflags[2 * p + 1]) +
                                  ": capacity overflow or unsupported annulus)");
-      if (ctrl_all[8 * p + 3] != 0)
-        throw std::runtime_error("narrow-phase pair queue overflow (more than " +
-                                 std::to_string(d_pairs.count) + " overlapping pairs in a round)");
     }
     float total_ms = 0.f;
     cuda_check(cudaEventElapsedTime(&total_ms, ev_start, ev_stop), "elapsed");
@@ -865,16 +883,22 @@ struct sb_engine {
       place_ms += b;
     }
     uint64_t rounds = rounds_host;
-    if (world_size == 1)
-      for (size_t p = 0; p < P; ++p) rounds += ctrl_all[8 * p + 2];
+    for (size_t p = 0; p < P; ++p)
+      if (device_rounds[p]) rounds += ctrl_all[8 * p + 2];
     last_total_ms = total_ms;
     last_check_ms = world_size == 1 ? place_ms : sharded_check_ms;
     last_check_launches = round_launches;
     last_launches = launches;
-    for (int k = 0; k < 5; ++k) last_prof[k] = prof[k] * 1e-6;
-    last_prof[5] = static_cast<double>(prof[5]);
-    last_prof[6] = regions_ms;
-    last_prof[7] = total_ms;
+    for (int k = 0; k < 7; ++k) last_prof[k] = prof[k] * 1e-6;
+    last_prof[7] = static_cast<double>(prof[7]);
+    if (round_debug) {
+      std::vector<unsigned> dbg(d_dbg.count);
+      cuda_check(cudaMemcpy(dbg.data(), d_dbg.p, dbg.size() * sizeof(unsigned), cudaMemcpyDeviceToHost), "D2H dbg");
+      for (int k = 0; k < 3; ++k) last_prof[10 + k] = 0;
+      for (size_t i = 0; i < dbg.size(); ++i) last_prof[10 + i % 3] += dbg[i] * 1e-6;
+    }
+    last_prof[8] = regions_ms;
+    last_prof[9] = total_ms;
     world->stats.check_calls += round_launches;
     world->stats.checked_instances += c[0];
     world->stats.narrow_phase_tests += c[1];
@@ -1152,9 +1176,9 @@ sb_status sb_device_math(int fn, const double* in, uint64_t n, double* out) {
   });
 }
 
-sb_status sb_engine_phase_profile(const sb_engine* e, double out[8]) {
+sb_status sb_engine_phase_profile(const sb_engine* e, double out[16]) {
   return guard([&] {
-    for (int k = 0; k < 8; ++k) out[k] = e->last_prof[k];
+    for (int k = 0; k < 16; ++k) out[k] = e->last_prof[k];
   });
 }
 sb_status sb_engine_last_timing(const sb_engine* e, double* total_ms, double* check_ms,

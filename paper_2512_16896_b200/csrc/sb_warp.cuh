@@ -27,8 +27,8 @@ namespace sbd {
 constexpr unsigned kFull = 0xffffffffu;
 
 // Optional cycle breakdown of the narrow phase (build with -DSB_NARROW_PROF):
-// [0] pose load + M, [1] triangle transform + all triangle pairs, [2] node transform +
-// node-pair tests (hits only), [3] DAG walk, [4] reached-hit check, [5] pairs.
+// [0] M, [1] B triangle transform + planes, [2] node transform + node-pair tests (hits
+// only), [3] DAG walk, [4] reached-hit check, [5] pairs, [6] filter 1, [7] filter 2 + rest.
 static __device__ unsigned long long g_nprof[8];
 #ifdef SB_NARROW_PROF
 #define SB_NP_MARK(var) const long long var = clock64()
@@ -41,34 +41,88 @@ static __device__ unsigned long long g_nprof[8];
 constexpr int kMaxEffTris = SB_MAX_EFF_TRIS;  // host-checked at registration
 constexpr int kMaxNodes = SB_MAX_NODES_PER_GEOM;
 
-struct WarpScratch {
-  double M[12];                // other_in_self of the pair under test
-  double qb[kMaxEffTris][9];   // B's effective triangles moved into A's frame
-  double bb[kMaxNodes][6];     // B's effective node boxes in A's frame
-  double e2b[kMaxNodes];       // their squared extents
-  uint32_t cm[kMaxNodes];      // B node -> mask of its effective children (0 for leaves)
-  uint32_t allowed[kMaxNodes]; // allowed[a] bit b: leaf pair reached by the traversal
-  int8_t tleafb[kMaxEffTris];
-  uint32_t hitw[kMaxEffTris * kMaxEffTris / 32];  // intersecting triangle pairs (bitset)
+// Per-warp narrow-phase scratch, as pointers into shared memory so a kernel can size it
+// by the world's largest effective geometry (place_ws_bytes) or use the fixed-size
+// WarpScratch below.
+struct WarpScratchView {
+  double* M;           // [12] other_in_self of the pair under test
+  double* qb;          // [maxT][9] B's effective triangles moved into A's frame
+  double* pb;          // [maxT][5] their planes: n xyz, dc, tol (TriPlane)
+  double* bb;          // [maxN][6] B's effective node boxes in A's frame
+  double* e2b;         // [maxN] their squared extents
+  uint32_t* cm;        // [maxN] B node -> mask of its effective children (0 for leaves)
+  uint32_t* allowed;   // [maxN] allowed[a] bit b: leaf pair reached by the traversal
+  uint32_t* hitw;      // [ceil(maxT^2 / 32)] intersecting triangle pairs (bitset)
+  uint16_t* l1;        // [maxT^2] triangle pairs past filter 1
+  uint16_t* l2;        // [maxT^2] triangle pairs past filter 2
+  int8_t* tleafb;      // [maxT]
+  int8_t* leafb;       // [maxN] B's leaf node ids, ascending
 };
 
-// Candidate geometry (uniform per launch), staged in shared memory once per block.
+__host__ __device__ __forceinline__ int warp_scratch_bytes(int maxT, int maxN) {
+  int b = (12 + maxT * 14 + maxN * 7) * 8;
+  b += (2 * maxN + (maxT * maxT + 31) / 32) * 4 + 2 * maxT * maxT * 2 + maxT + maxN;
+  return (b + 15) & ~15;
+}
+
+__device__ __forceinline__ WarpScratchView carve_scratch(unsigned char* base, int maxT, int maxN) {
+  WarpScratchView v;
+  double* d = reinterpret_cast<double*>(base);
+  v.M = d;
+  v.qb = d + 12;
+  v.pb = v.qb + 9 * maxT;
+  v.bb = v.pb + 5 * maxT;
+  v.e2b = v.bb + 6 * maxN;
+  uint32_t* u = reinterpret_cast<uint32_t*>(v.e2b + maxN);
+  v.cm = u;
+  v.allowed = u + maxN;
+  v.hitw = u + 2 * maxN;
+  v.l1 = reinterpret_cast<uint16_t*>(v.hitw + (maxT * maxT + 31) / 32);
+  v.l2 = v.l1 + maxT * maxT;
+  v.tleafb = reinterpret_cast<int8_t*>(v.l2 + maxT * maxT);
+  v.leafb = v.tleafb + maxT;
+  return v;
+}
+
+struct alignas(16) WarpScratch {  // fixed-size variant (world API check_batch)
+  unsigned char bytes[(12 + kMaxEffTris * 14 + kMaxNodes * 7) * 8 +
+                      (2 * kMaxNodes + kMaxEffTris * kMaxEffTris / 32) * 4 +
+                      4 * kMaxEffTris * kMaxEffTris + kMaxEffTris + kMaxNodes + 16];
+  __device__ __forceinline__ WarpScratchView view() {
+    return carve_scratch(bytes, kMaxEffTris, kMaxNodes);
+  }
+};
+
+// Candidate geometry (uniform per launch), staged in shared memory once per block, with
+// the planes of its triangles (pure functions of the A triangles in A's own frame).
 struct GeomCache {
   double ta[kMaxEffTris][9];
+  double pa[kMaxEffTris][5];  // TriPlane: n xyz, dc, tol
   double bmin[kMaxNodes][3], bmax[kMaxNodes][3];
   double ext2[kMaxNodes];
   int8_t c0[kMaxNodes], c1[kMaxNodes];
   int8_t tleaf[kMaxEffTris];
   uint32_t leafmask;
-  int n_tris, n_nodes;
+  int8_t leaves[kMaxNodes];  // leaf node ids, ascending
+  int n_tris, n_nodes, n_leaves;
 };
 
 __device__ __forceinline__ void load_geom_cache(const WorldView& w, const SbGeom& gA,
                                                 GeomCache& gc) {
   const SbTri* t = w.tris + gA.tri_offset;
   const SbNode* nd = w.nodes + gA.node_offset;
-  for (int k = threadIdx.x; k < gA.n_tris * 9; k += blockDim.x) gc.ta[k / 9][k % 9] = t[k / 9].v[k % 9];
-  for (int k = threadIdx.x; k < gA.n_tris; k += blockDim.x) gc.tleaf[k] = (int8_t)t[k].leaf;
+  for (int k = threadIdx.x; k < gA.n_tris; k += blockDim.x) {
+    double v[9];
+#pragma unroll
+    for (int c = 0; c < 9; ++c) gc.ta[k][c] = v[c] = t[k].v[c];
+    const TriPlane P = tri_plane(v);
+    gc.pa[k][0] = P.n[0];
+    gc.pa[k][1] = P.n[1];
+    gc.pa[k][2] = P.n[2];
+    gc.pa[k][3] = P.dc;
+    gc.pa[k][4] = P.tol;
+    gc.tleaf[k] = (int8_t)t[k].leaf;
+  }
   for (int k = threadIdx.x; k < gA.n_nodes; k += blockDim.x) {
     for (int c = 0; c < 3; ++c) {
       gc.bmin[k][c] = nd[k].bmin[c];
@@ -83,29 +137,50 @@ __device__ __forceinline__ void load_geom_cache(const WorldView& w, const SbGeom
     for (int k = 0; k < gA.n_nodes; ++k)
       if (nd[k].child0 < 0) lm |= 1u << k;
     gc.leafmask = lm;
+    int nl = 0;
+    for (int k = 0; k < gA.n_nodes; ++k)
+      if ((lm >> k) & 1u) gc.leaves[nl++] = (int8_t)k;
+    gc.n_leaves = nl;
     gc.n_tris = gA.n_tris;
     gc.n_nodes = gA.n_nodes;
   }
 }
 
+// Appends the lanes with `pass` to list[n..] in lane order; returns the new length.
+__device__ __forceinline__ int warp_append(bool pass, uint16_t value, uint16_t* list, int n) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t m = __ballot_sync(kFull, pass);
+  if (pass) list[n + __popc(m & ((1u << lane) - 1u))] = value;
+  return n + __popc(m);
+}
+
 // Warp-cooperative MeshBvh::collide for one (candidate, object) pair. All 32 lanes call
-// it with identical arguments.
+// it with identical arguments. `Pn` (lanes < 12) holds the placed object's pose entries,
+// loaded by the caller (software-pipelined one pair ahead).
+//  1. M = other_in_cand (lanes < 12), B's effective triangles into A's frame and their
+//     planes (one lane per triangle; A's planes are cached per launch);
+//  2. every triangle pair of Eff(A) x Eff(B) runs through tri_tri_intersect as three
+//     compacted filter passes -- B's plane vs A's vertices, A's plane vs B's vertices, the
+//     interval / coplanar rest -- so the long FP64 tail runs only for the few pairs that
+//     survive both plane tests. No intersecting pair => the reference cannot report a hit;
+//  3. otherwise the node-pair tests and the pair-DAG walk decide which leaf pairs the
+//     reference traversal reaches; hit = some reached leaf pair holds an intersecting pair.
 __device__ __forceinline__ bool warp_collide(const WorldView& w, const GeomCache& gc,
-                                             int32_t ob, uint64_t inst, const double* I,
-                                             WarpScratch& ws, CheckCounters& cnt) {
+                                             const int4 gB, double Pn, const double* I,
+                                             const WarpScratchView& ws, CheckCounters& cnt) {
   const int lane = threadIdx.x & 31;
   SB_NP_MARK(np0);
-  const SbGeom gB = w.geoms[w.obj_geom[ob]];
-  const double* P = w.pose + sb_pose_off(w, ob, inst);
   if (lane < 12) {  // other_in_cand = inv(cand) * pose(ob), one entry per lane (shim order)
     const int i = lane >> 2, j = lane & 3;
-
-    double s = I[4 * i + 0] * P[j];
-    s = s + I[4 * i + 1] * P[4 + j];
-    s = s + I[4 * i + 2] * P[8 + j];
+    const double P0 = __shfl_sync(0xfffu, Pn, j), P1 = __shfl_sync(0xfffu, Pn, 4 + j),
+                 P2 = __shfl_sync(0xfffu, Pn, 8 + j);
+    double s = I[4 * i + 0] * P0;
+    s = s + I[4 * i + 1] * P1;
+    s = s + I[4 * i + 2] * P2;
     s = s + I[4 * i + 3] * (j == 3 ? 1.0 : 0.0);
     ws.M[lane] = s;
   }
+  if (lane < gc.n_nodes) ws.allowed[lane] = 0u;  // leaf-pair candidates (step 2)
   __syncwarp();
   M34 M;
 #pragma unroll
@@ -113,50 +188,13 @@ __device__ __forceinline__ bool warp_collide(const WorldView& w, const GeomCache
   SB_NP_MARK(np1);
   SB_NP_ADD(0, np0, np1);
 
-  // 1: B's effective triangles into A's frame (transform_point, collision.cpp:308-310).
-  // Then, when the node-pair grid is large (deep effective DAGs, e.g. sphere sets), test
-  // every effective triangle pair first: no intersecting pair in Eff(A) x Eff(B) means the
-  // reference cannot report a hit (it only tests pairs of reachable leaves), so node tests
-  // and the DAG walk run only when some pair intersects. Small grids (box-box: 4 x 4) cull
-  // first and test only the reached leaf pairs.
-  const SbTri* tB = w.tris + gB.tri_offset;
-  const int nTB = gB.n_tris, nTA = gc.n_tris;
-  const int nA = gc.n_nodes, nB = gB.n_nodes;
-  const bool tri_first = nA * nB > 16;
-  for (int v = lane; v < nTB * 3; v += 32) {
-    const double* p = tB[v / 3].v + 3 * (v % 3);
-    double* q = ws.qb[v / 3] + 3 * (v % 3);
-    xform(M, p[0], p[1], p[2], q[0], q[1], q[2]);
-  }
-  for (int k = lane; k < nTB; k += 32) ws.tleafb[k] = (int8_t)tB[k].leaf;
-  __syncwarp();
-  const int ntp = nTA * nTB;
-  if (tri_first) {
-    bool any_hit = false;
-    for (int k0 = 0; k0 < ntp; k0 += 32) {
-      const int idx = k0 + lane;
-      bool hit = false;
-      if (idx < ntp) {
-        const int ia = idx / nTB, ib = idx - ia * nTB;
-        hit = tri_tri_intersect(gc.ta[ia], ws.qb[ib]);
-      }
-      const uint32_t hm = __ballot_sync(kFull, hit);
-      if (lane == 0) ws.hitw[k0 >> 5] = hm;
-      any_hit = any_hit || hm != 0u;
-    }
-    if (lane == 0) cnt.pairs += ntp;
-    if (!any_hit) {
-      SB_NP_MARK(npx);
-      SB_NP_ADD(1, np1, npx);
-      return false;
-    }
-    __syncwarp();
-  }
-  SB_NP_MARK(np2);
-  SB_NP_ADD(1, np1, np2);
+  const SbTri* tB = w.tris + gB.z;  // gB = {node_offset, n_nodes, tri_offset, n_tris}
+  const int nTB = gB.w, nTA = gc.n_tris;
+  const int nA = gc.n_nodes, nB = gB.y;
 
-  // 2a: lane b moves B's node b into A's frame (independent of the A node it meets)
-  const SbNode* nodesB = w.nodes + gB.node_offset;
+  // 1: lane b moves B's node b into A's frame (transform_aabb, collision.cpp:297-300; it
+  // does not depend on the A node it meets)
+  const SbNode* nodesB = w.nodes + gB.x;
   bool lb = false;
   if (lane < nB) {
     const SbNode& nb = nodesB[lane];
@@ -165,17 +203,128 @@ __device__ __forceinline__ bool warp_collide(const WorldView& w, const GeomCache
     const double e0 = bmx[0] - bmn[0], e1 = bmx[1] - bmn[1], e2 = bmx[2] - bmn[2];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      ws.bb[lane][c] = bmn[c];
-      ws.bb[lane][3 + c] = bmx[c];
+      ws.bb[6 * lane + c] = bmn[c];
+      ws.bb[6 * lane + 3 + c] = bmx[c];
     }
     ws.e2b[lane] = (e0 * e0 + e1 * e1) + e2 * e2;
     lb = nb.child0 < 0;
     ws.cm[lane] = lb ? 0u : ((1u << nb.child0) | (1u << nb.child1));
   }
   const uint32_t leafB = __ballot_sync(kFull, lb);
+  if (lb) ws.leafb[__popc(leafB & ((1u << lane) - 1u))] = (int8_t)lane;
+  const int nLB = __popc(leafB), nLA = gc.n_leaves;
   __syncwarp();
 
-  // 2: pass(a,b) = na.box.overlaps(nb_in_a) and the descend rule
+  // 2: leaf-box filter. The traversal tests triangles of a leaf pair only after that
+  // pair's own box test passed, so a triangle pair whose leaf boxes are disjoint can never
+  // be reported: collect the leaf pairs whose boxes overlap (ws.allowed[a] bit b).
+  uint32_t anyc = 0u;
+  {
+    const int nlp = nLA * nLB;
+    for (int k0 = 0; k0 < nlp; k0 += 32) {
+      const int k = k0 + lane;
+      bool ov = false;
+      if (k < nlp) {
+        const int a = gc.leaves[k / nLB], b = ws.leafb[k - (k / nLB) * nLB];
+        const double* bb = ws.bb + 6 * b;
+        ov = gc.bmin[a][0] <= bb[3] && bb[0] <= gc.bmax[a][0] && gc.bmin[a][1] <= bb[4] &&
+             bb[1] <= gc.bmax[a][1] && gc.bmin[a][2] <= bb[5] && bb[2] <= gc.bmax[a][2];
+      }
+      if (__any_sync(kFull, ov)) {
+        const uint32_t m = __ballot_sync(kFull, ov);
+        anyc |= m;
+        if (ov) atomicOr(ws.allowed + gc.leaves[k / nLB], 1u << ws.leafb[k - (k / nLB) * nLB]);
+      }
+    }
+  }
+  SB_NP_MARK(np1a);
+  SB_NP_ADD(1, np1, np1a);
+  if (!anyc) return false;
+  __syncwarp();
+
+  // 3: B's effective triangles into A's frame (transform_point, collision.cpp:308-310) and
+  // their planes; A's planes are cached per launch.
+  for (int v = lane; v < nTB * 3; v += 32) {
+    const double* p = tB[v / 3].v + 3 * (v % 3);
+    double* q = ws.qb + 9 * (v / 3) + 3 * (v % 3);
+    xform(M, __ldg(p), __ldg(p + 1), __ldg(p + 2), q[0], q[1], q[2]);
+  }
+  for (int k = lane; k < nTB; k += 32) ws.tleafb[k] = (int8_t)tB[k].leaf;
+  __syncwarp();
+  for (int k = lane; k < nTB; k += 32) {
+    const TriPlane P = tri_plane(ws.qb + 9 * k);
+    double* pb = ws.pb + 5 * k;
+    pb[0] = P.n[0];
+    pb[1] = P.n[1];
+    pb[2] = P.n[2];
+    pb[3] = P.dc;
+    pb[4] = P.tol;
+  }
+  const int ntp = nTA * nTB;
+  for (int k = lane; k < (ntp + 31) / 32; k += 32) ws.hitw[k] = 0u;
+  __syncwarp();
+
+  // 4: staged tri_tri_intersect over the triangle pairs k = ia * nTB + ib of candidate
+  // leaf pairs: filter 1 (B's plane vs A's vertices), filter 2 (A's plane vs B's
+  // vertices), then the interval / coplanar rest.
+  int n1 = 0;
+  for (int k0 = 0; k0 < ntp; k0 += 32) {
+    const int k = k0 + lane;
+    bool pass = false;
+    if (k < ntp) {
+      const int ia = k / nTB, ib = k - ia * nTB;
+      if ((ws.allowed[gc.tleaf[ia]] >> ws.tleafb[ib]) & 1u) {
+        const double* pb = ws.pb + 5 * ib;
+        double d0, d1, d2;
+        plane_dists(pb, pb[3], pb[4], gc.ta[ia], d0, d1, d2);
+        pass = straddles(d0, d1, d2);
+        ++cnt.pairs;
+      }
+    }
+    n1 = warp_append(pass, (uint16_t)k, ws.l1, n1);
+  }
+  __syncwarp();
+  SB_NP_MARK(np1b);
+  SB_NP_ADD(6, np1a, np1b);
+  int n2 = 0;
+  for (int j0 = 0; j0 < n1; j0 += 32) {
+    const int j = j0 + lane;
+    bool pass = false;
+    int k = 0;
+    if (j < n1) {
+      k = ws.l1[j];
+      const int ia = k / nTB, ib = k - ia * nTB;
+      double d0, d1, d2;
+      plane_dists(gc.pa[ia], gc.pa[ia][3], gc.pa[ia][4], ws.qb + 9 * ib, d0, d1, d2);
+      pass = straddles(d0, d1, d2);
+    }
+    n2 = warp_append(pass, (uint16_t)k, ws.l2, n2);
+  }
+  __syncwarp();
+  bool any = false;
+  for (int j0 = 0; j0 < n2; j0 += 32) {
+    const int j = j0 + lane;
+    bool hit = false;
+    int k = 0;
+    if (j < n2) {
+      k = ws.l2[j];
+      const int ia = k / nTB, ib = k - ia * nTB;
+      const double* pb = ws.pb + 5 * ib;
+      const double* q = ws.qb + 9 * ib;
+      double dp0, dp1, dp2, dq0, dq1, dq2;
+      plane_dists(pb, pb[3], pb[4], gc.ta[ia], dp0, dp1, dp2);
+      plane_dists(gc.pa[ia], gc.pa[ia][3], gc.pa[ia][4], q, dq0, dq1, dq2);
+      hit = tri_tri_finish(gc.ta[ia], q, gc.pa[ia], pb, dp0, dp1, dp2, dq0, dq1, dq2);
+    }
+    if (hit) atomicOr(ws.hitw + (k >> 5), 1u << (k & 31));
+    any = __any_sync(kFull, hit) || any;
+  }
+  SB_NP_MARK(np2);
+  SB_NP_ADD(7, np1b, np2);
+  if (!any) return false;
+  __syncwarp();
+
+  // 5a: pass(a,b) = na.box.overlaps(nb_in_a) and the descend rule
   // desc(a,b) = leaf(nb) || (!leaf(na) && ext2(na) >= ext2(nb_in_a)) for all (a, b),
   // 32 pairs per ballot; lane a collects row a (pair k = a * nB + b).
   uint32_t rpass = 0u, rdesc = 0u;
@@ -185,7 +334,7 @@ __device__ __forceinline__ bool warp_collide(const WorldView& w, const GeomCache
     bool pb = false, db = false;
     if (k < np) {
       const int a = k / nB, bi = k - a * nB;
-      const double* bb = ws.bb[bi];
+      const double* bb = ws.bb + 6 * bi;
       pb = gc.bmin[a][0] <= bb[3] && bb[0] <= gc.bmax[a][0] && gc.bmin[a][1] <= bb[4] &&
            bb[1] <= gc.bmax[a][1] && gc.bmin[a][2] <= bb[5] && bb[2] <= gc.bmax[a][2];
       db = ((leafB >> bi) & 1u) || (!((gc.leafmask >> a) & 1u) && gc.ext2[a] >= ws.e2b[bi]);
@@ -206,7 +355,7 @@ __device__ __forceinline__ bool warp_collide(const WorldView& w, const GeomCache
   SB_NP_MARK(np3);
   SB_NP_ADD(2, np2, np3);
 
-  // 3: walk the pair DAG from (0,0) in lexicographic order (a topological order: every
+  // 3c: walk the pair DAG from (0,0) in lexicographic order (a topological order: every
   // child id exceeds its parent's). Lane a owns the pending row of A node a; descending A
   // forwards the row's bits to the lanes of A's effective children.
   {
@@ -238,23 +387,15 @@ __device__ __forceinline__ bool warp_collide(const WorldView& w, const GeomCache
   SB_NP_MARK(np4);
   SB_NP_ADD(3, np3, np4);
 
-  // 4: tri-first: does some intersecting pair lie in a reached leaf pair? Cull-first:
-  // test the triangle pairs of the reached leaf pairs.
+  // 3d: does some intersecting pair lie in a reached leaf pair?
   bool ok = false;
-  unsigned tests = 0;
   for (int k0 = 0; k0 < ntp; k0 += 32) {
     const int idx = k0 + lane;
     if (idx >= ntp) continue;
     const int ia = idx / nTB, ib = idx - ia * nTB;
     const bool reached = (ws.allowed[gc.tleaf[ia]] >> ws.tleafb[ib]) & 1u;
-    if (tri_first) {
-      ok = ok || (reached && ((ws.hitw[k0 >> 5] >> lane) & 1u));
-    } else if (reached) {
-      ++tests;
-      ok = ok || tri_tri_intersect(gc.ta[ia], ws.qb[ib]);
-    }
+    ok = ok || (reached && ((ws.hitw[k0 >> 5] >> lane) & 1u));
   }
-  cnt.pairs += tests;
   const bool res = __any_sync(kFull, ok);
   SB_NP_MARK(np5);
   SB_NP_ADD(4, np4, np5);
@@ -262,13 +403,25 @@ __device__ __forceinline__ bool warp_collide(const WorldView& w, const GeomCache
   return res;
 }
 
+// {node_offset, n_nodes, tri_offset, n_tris} of object ob's geometry (SbGeom's first 16 B).
+__device__ __forceinline__ int4 geom_ref(const WorldView& w, int32_t ob) {
+  return __ldg(reinterpret_cast<const int4*>(w.geoms + __ldg(w.obj_geom + ob)));
+}
+
+// Placed object's pose entry for lane < 12 (row-major 3x4), the narrow phase's `Pn`.
+__device__ __forceinline__ double pose_entry(const WorldView& w, int32_t ob, uint64_t inst) {
+  const int lane = threadIdx.x & 31;
+  return lane < 12 ? __ldcg(w.pose + sb_pose_off(w, ob, inst) + lane) : 0.0;
+}
+
 // Pooled check of the warp's 32 candidates (inactive lanes pass active = false but must
 // still call). Returns the first colliding object id for this lane's candidate, or -1.
 __device__ __forceinline__ int warp_check(const WorldView& w, const SbGeom& gA,
                                           const GeomCache& gc, bool active, const M34& pose,
-                                          uint64_t inst, WarpScratch& ws, double (*invs)[12],
+                                          uint64_t inst, WarpScratch& wsf, double (*invs)[12],
                                           CheckCounters& cnt) {
   const int lane = threadIdx.x & 31;
+  const WarpScratchView ws = wsf.view();
   double cmn[3] = {0, 0, 0}, cmx[3] = {0, 0, 0};
   if (active) {
     xform_aabb(pose, gA.box_c, gA.box_h, cmn, cmx);
@@ -304,7 +457,7 @@ __device__ __forceinline__ int warp_check(const WorldView& w, const SbGeom& gA,
         const uint32_t ovL = __shfl_sync(kFull, ovm, L);
         const uint64_t instL = __shfl_sync(kFull, inst, L);
         const int ob = ob0 + __ffs(ovL) - 1;
-        const bool hit = warp_collide(w, gc, ob, instL, invs[L], ws, cnt);
+        const bool hit = warp_collide(w, gc, geom_ref(w, ob), pose_entry(w, ob, instL), invs[L], ws, cnt);
         if (lane == L) {
           ++cnt.narrow;
           ovm &= ovm - 1u;

@@ -367,10 +367,12 @@ class Engine:
         return t.value, c.value, n.value
 
     def phase_profile(self) -> dict:
-        out = (C.c_double * 8)()
+        out = (C.c_double * 16)()
         A.check(A.lib().sb_engine_phase_profile(self._h, out))
-        keys = ("init_ms", "broad_ms", "narrow_ms", "accept_ms", "compact_ms", "rounds",
-                "regions_ms", "total_ms")
+        # block 0's device clock inside the placement kernels (see the C header)
+        keys = ("init_ms", "prefix_ms", "sample_ms", "broad_narrow_ms", "accept_ms",
+                "grid_sync_ms", "per_instance_ms", "fast_rounds", "regions_ms", "total_ms",
+                "dbg_round_max_ms", "dbg_a1_max_ms", "dbg_a2b_max_ms")
         return dict(zip(keys, list(out)))
 
     def last_launches(self) -> int:
