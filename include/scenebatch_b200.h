@@ -260,7 +260,8 @@ sb_status sb_engine_last_timing(const sb_engine* e, double* total_ms, double* ch
  * scans, out[2] A1 sample/compose, out[3] A2+B broad/narrow phase, out[4] C accept +
  * compaction, out[5] grid-barrier waits, out[6] per-instance placements (whole), out[7] =
  * fast-path rounds, out[8] = ms in relation-region preparation (CUDA events), out[9] =
- * total ms (CUDA events), out[10..15] reserved (0). */
+ * total ms (CUDA events), out[10] / out[11] = placement-kernel ms (CUDA events) of the
+ * per-instance / fast-path placements, out[12..14] = debug maxima (SB_ROUND_DEBUG). */
 sb_status sb_engine_phase_profile(const sb_engine* e, double out[16]);
 
 /* Diagnostics: evaluate the device libm used on the hot path (correctly rounded

@@ -265,6 +265,12 @@ EffectiveBvh build_effective_bvh(const Mesh& mesh) {
       }
     }
   }
+  // leaves_below: effective leaves under each node (children ids exceed their parent's)
+  for (int i = static_cast<int>(out.nodes.size()) - 1; i >= 0; --i) {
+    SbNode& d = out.nodes[i];
+    d.leaves_below = d.child0 < 0 ? (1u << i)
+                                  : (out.nodes[d.child0].leaves_below | out.nodes[d.child1].leaves_below);
+  }
   out.reachable_tris = static_cast<int>(out.tris.size());
   return out;
 }

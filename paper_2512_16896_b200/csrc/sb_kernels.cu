@@ -228,6 +228,15 @@ void check_batch(const SbWorldView& w, int32_t geom, const double* poses16,
                                                   contact_out, counters);
   check_launch("check_batch");
 }
+void narrow_profile_check(unsigned long long out[8], bool reset) {
+  if (cudaMemcpyFromSymbol(out, g_nprof, 8 * sizeof(unsigned long long)) != cudaSuccess)
+    throw std::runtime_error("narrow_profile_check");
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (cudaMemcpyToSymbol(g_nprof, z, sizeof z) != cudaSuccess)
+      throw std::runtime_error("narrow_profile_check reset");
+  }
+}
 void engine_reset(const SbWorldView& w, int32_t first_obj, int32_t n_obj, uint8_t* valid,
                   int16_t* accepted, int32_t n_place, sb_stream_t s) {
   k_engine_reset<<<grid_for(w.n), kBlock, 0, s>>>(w, first_obj, n_obj, valid, accepted, n_place);

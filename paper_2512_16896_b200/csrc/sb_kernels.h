@@ -1,4 +1,7 @@
 // Kernel launch wrappers for CollisionWorld maintenance, the world-API check_batch and
+// narrow-phase cycle profile of check_batch (zeros unless built with -DSB_NARROW_PROF)
+void narrow_profile_check(unsigned long long out[8], bool reset);
+
 // engine bookkeeping (implemented in sb_kernels.cu). Plain C++ signatures so the host
 // runtime (sb_runtime.cpp, g++) can call them without CUDA types in its interfaces.
 // The placement engine proper lives in sb_place.h, the relation regions in sb_region.h.
@@ -26,6 +29,9 @@ void update_transforms(const SbWorldView& w, int32_t obj, const double* poses16,
 void check_batch(const SbWorldView& w, int32_t geom, const double* poses16,
                  const uint32_t* active, uint64_t m, uint8_t* free_out, int32_t* contact_out,
                  unsigned long long* counters, sb_stream_t s);
+
+// narrow-phase cycle profile of check_batch (zeros unless built with -DSB_NARROW_PROF)
+void narrow_profile_check(unsigned long long out[8], bool reset);
 
 // engine bookkeeping
 void engine_reset(const SbWorldView& w, int32_t first_obj, int32_t n_obj, uint8_t* valid,

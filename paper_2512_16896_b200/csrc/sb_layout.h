@@ -11,7 +11,8 @@ struct SbNode {
   double ext2;              // box.extent().squaredNorm(): descent rule (collision.cpp:320)
   int32_t child0, child1;   // compact child ids, -1 for a leaf
   int32_t tri_start, tri_count;
-  int32_t pad[2];
+  uint32_t leaves_below;    // bit k: effective leaf k lies under this node (or is it)
+  int32_t pad;
 };
 
 struct SbTri {
@@ -67,7 +68,25 @@ struct SbWorldView {
   const SbGeom* geoms;
   const SbNode* nodes;
   const SbTri* tris;
+  // Compact B-side narrow-phase record per geometry (sb_brec_* below), staged into shared
+  // memory with cp.async one pair ahead: grec[g] = {offset, length} in 16-byte units,
+  // n_nodes, n_tris.
+  const int32_t* grec;        // [n_geoms][4]
+  const void* brec;           // 16-byte aligned records
 };
+
+// Narrow-phase record of one geometry, 16-byte aligned, byte offsets:
+//   [0, 48 nN)                 node boxes: c xyz, h xyz (double)
+//   [48 nN, 56 nN)             node info: u32 child0 | child1 << 8 (0xff = none),
+//                                         u32 leaves_below
+//   [56 nN, 56 nN + 72 nT)     effective triangles: 9 doubles
+//   [56 nN + 72 nT, + nT)      leaf id of each triangle (int8)
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline constexpr int sb_brec_bytes(int n_nodes, int n_tris) {
+  return (56 * n_nodes + 73 * n_tris + 15) & ~15;
+}
 
 #ifdef __CUDACC__
 #define SB_HDI __host__ __device__ __forceinline__

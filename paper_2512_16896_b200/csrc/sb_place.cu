@@ -33,7 +33,6 @@ using BlockScan = cub::BlockScan<uint32_t, kB>;
 
 // Per-round candidate state of the CTA's tile (dynamic shared memory).
 struct Tile {
-  double* pose;      // [kB][12] candidate pose per slot
   double* inv;       // [kB][12] inverse pose per slot
   double* box;       // [kB][6]  candidate world AABB per slot
   uint32_t* ovm;     // [words][kB] broad-phase overlap bits per slot
@@ -41,8 +40,11 @@ struct Tile {
   uint32_t* list;    // [kB] tile's active instances (ascending)
   uint32_t* queue;   // [kQueue]
   int32_t* contact;  // [kB] min colliding object per slot
+  uint32_t* rem;     // [kB] queued, not yet tested pairs per slot
+  int32_t* minfree;  // [kB] per tile entry: lowest slot (attempt offset) confirmed free, W = none
   uint8_t* sflag;    // [kB]
   unsigned char* ws; // [kWarps][ws_bytes]
+  int4* ogeo;        // [n_objects] narrow-record descriptor of each object's geometry
 };
 
 struct Fixed {  // static shared memory
@@ -51,6 +53,7 @@ struct Fixed {  // static shared memory
   uint32_t prefix[kPlaceMaxOwnedTiles];  // fast path: draw offset of each owned tile
   uint32_t cnt[kPlaceMaxOwnedTiles];     // fast path: its survivors entering this round
   uint32_t qn;
+  uint32_t vdone;  // slots whose broad-phase items are all enumerated
   uint32_t total;
   uint32_t tile;
   unsigned long long tclk;  // block 0 / thread 0 phase clock
@@ -60,22 +63,24 @@ struct Fixed {  // static shared memory
 
 __device__ __forceinline__ Tile carve(unsigned char* d, int words, int ws_bytes) {
   Tile t;
-  t.pose = reinterpret_cast<double*>(d);
-  t.inv = t.pose + 12 * kB;
+  t.inv = reinterpret_cast<double*>(d);
   t.box = t.inv + 12 * kB;
   t.ovm = reinterpret_cast<uint32_t*>(t.box + 6 * kB);
   t.enw = t.ovm + words * kB;
   t.list = t.enw + words * kB;
   t.queue = t.list + kB;
   t.contact = reinterpret_cast<int32_t*>(t.queue + kQueue);
-  t.sflag = reinterpret_cast<uint8_t*>(t.contact + kB);
+  t.rem = reinterpret_cast<uint32_t*>(t.contact + kB);
+  t.minfree = reinterpret_cast<int32_t*>(t.rem + kB);
+  t.sflag = reinterpret_cast<uint8_t*>(t.minfree + kB);
   t.ws = t.sflag + kB;
+  t.ogeo = reinterpret_cast<int4*>(t.ws + kWarps * ws_bytes);
   return t;
 }
 
 __host__ __device__ constexpr size_t tile_bytes(int words) {
-  return (12 + 12 + 6) * 8 * (size_t)kB + 2 * (size_t)words * kB * 4 + (size_t)kB * 4 +
-         (size_t)kQueue * 4 + (size_t)kB * 4 + kB;
+  return (12 + 6) * 8 * (size_t)kB + 2 * (size_t)words * kB * 4 + (size_t)kB * 4 +
+         (size_t)kQueue * 4 + 3 * (size_t)kB * 4 + kB;
 }
 
 struct Local {  // per-thread counters, flushed once at kernel end
@@ -130,7 +135,7 @@ __device__ __forceinline__ uint64_t global_ns() {
 // 0 setup + tile init, 1 fast-path prefix scan, 2 A1 sample/compose, 3 A2+B broad/narrow,
 // 4 C accept + compaction, 5 grid barrier, 6 per-instance path (whole), 7 fast rounds.
 __device__ __forceinline__ void dbg_mark(const PlaceParams& p, Fixed& F, unsigned long long& acc) {
-  if (p.dbg && threadIdx.x == 0) {
+  if ((p.dbg || p.dbg_inst) && threadIdx.x == 0) {
     const unsigned long long now = global_ns();
     acc += now - F.t0;
     F.t0 = now;
@@ -193,6 +198,8 @@ __device__ uint32_t tile_round(const PlaceParams& p, const Sampling& S, const Sb
       }
     }
     T.contact[v] = kFree;
+    T.rem[v] = 0u;
+    if (v - e * W == 0) T.minfree[e] = W;
     for (int wd = 0; wd < words; ++wd) T.ovm[wd * kB + v] = 0u;
     if (!placeable) {
       T.sflag[v] = kSlotUnplaceable;
@@ -232,11 +239,11 @@ __device__ uint32_t tile_round(const PlaceParams& p, const Sampling& S, const Sb
       xform_aabb(pose, gA.box_c, gA.box_h, cmn, cmx);
       M34 inv;
       inverse_rigid(pose, inv);
+      double2* cp = reinterpret_cast<double2*>(p.cpose + ((size_t)blockIdx.x * kB + v) * 12);
 #pragma unroll
-      for (int k = 0; k < 12; ++k) {
-        T.pose[12 * v + k] = pose.m[k];
-        T.inv[12 * v + k] = inv.m[k];
-      }
+      for (int k = 0; k < 6; ++k) cp[k] = make_double2(pose.m[2 * k], pose.m[2 * k + 1]);
+#pragma unroll
+      for (int k = 0; k < 12; ++k) T.inv[12 * v + k] = inv.m[k];
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
         T.box[6 * v + k] = cmn[k];
@@ -245,7 +252,10 @@ __device__ uint32_t tile_round(const PlaceParams& p, const Sampling& S, const Sb
       T.sflag[v] = kSlotChecked;
     }
   }
-  if (tid == 0) F.qn = 0;
+  if (tid == 0) {
+    F.qn = 0;
+    F.vdone = 0;
+  }
   __syncthreads();
   lap(p, F, 2);
   dbg_mark(p, F, F.ta);
@@ -286,44 +296,71 @@ __device__ uint32_t tile_round(const PlaceParams& p, const Sampling& S, const Sb
       base = __shfl_sync(kFull, base, 0);
       if (ov[u]) {
         atomicOr(T.ovm + (obs[u] >> 5) * kB + vs[u], 1u << (obs[u] & 31));
+        atomicAdd(T.rem + vs[u], 1u);
         T.queue[base + __popc(mask & ((1u << lane) - 1u))] = ((uint32_t)vs[u] << 24) | (uint32_t)obs[u];
       }
     }
     __syncthreads();
+    // Slots whose items are now all enumerated and whose queued pairs are all tested
+    // without a hit are free: the instance's lowest such attempt bounds the useful work.
+    const int vdone_old = (int)F.vdone;
+    int vdone = (it0 + kB * kU >= items) ? nslots : (it0 + kB * kU) / nobj;
+    for (int v = vdone_old + tid; v < vdone; v += kB)
+      if (T.sflag[v] == kSlotChecked && T.rem[v] == 0u && T.contact[v] == kFree)
+        atomicMin(T.minfree + v / W, v - (v / W) * W);
+    __syncthreads();
+    if (tid == 0) F.vdone = (uint32_t)vdone;
     const uint32_t qn = F.qn;
     if (it0 + kB * kU >= items || qn > (uint32_t)(kQueue - kB * kU)) {
       // ---------------- B: warp per queued pair; skip pairs behind a lower hit
       const WarpScratchView ws = carve_scratch(T.ws + warp * p.ws_bytes, p.max_tris, p.max_nodes);
-      // software-pipelined: the next pair's pose entries and geometry are in flight while
-      // the current pair is tested
+      // software-pipelined: the next pair's pose and geometry record are copied into the
+      // warp's other staging buffer (cp.async) while the current pair is tested
+      unsigned char* wsb = T.ws + warp * p.ws_bytes;
       uint32_t q = warp;
-      int v = 0, ob = 0;
-      double Pn = 0.0;
-      int4 gB = make_int4(0, 0, 0, 0);
-      auto fetch = [&](uint32_t qq, int& v_, int& ob_, double& Pn_, int4& g_) {
+      int v = 0, ob = 0, cur = 0;
+      int4 gr = make_int4(0, 0, 0, 0);
+      auto fetch = [&](uint32_t qq, int& v_, int& ob_, int4& g_, int buf) {
         const uint32_t ent = T.queue[qq];
         v_ = (int)(ent >> 24);
         ob_ = (int)(ent & 0xffffffu);
-        Pn_ = pose_entry(w, ob_, T.list[v_ / W]);
-        g_ = geom_ref(w, ob_);
+        g_ = T.ogeo[ob_];
+        warp_stage(w, g_, ob_, T.list[v_ / W], stage_buf(wsb, p.max_tris, p.max_nodes, buf));
       };
-      if (q < qn) fetch(q, v, ob, Pn, gB);
+      if (q < qn) fetch(q, v, ob, gr, 0);
       while (q < qn) {
         const uint32_t qn2 = q + kWarps;
         int v2 = 0, ob2 = 0;
-        double Pn2 = 0.0;
-        int4 gB2 = make_int4(0, 0, 0, 0);
-        if (qn2 < qn) fetch(qn2, v2, ob2, Pn2, gB2);
-        if (*((volatile int32_t*)T.contact + v) >= ob) {  // skip pairs behind a lower hit
-          const bool hit = warp_collide(w, F.gc, gB, Pn, T.inv + 12 * v, ws, L.cnt);
-          if (hit && lane == 0) atomicMin(T.contact + v, ob);
+        int4 gr2 = make_int4(0, 0, 0, 0);
+        if (qn2 < qn) {
+          fetch(qn2, v2, ob2, gr2, cur ^ 1);
+          cp_async_wait<1>();
+        } else {
+          cp_async_wait<0>();
+        }
+        __syncwarp();
+        // skip pairs behind a lower hit of their slot, or of a slot beyond the instance's
+        // lowest confirmed-free attempt (neither can change the first-valid result)
+        const int e = v / W;
+        if (*((volatile int32_t*)T.contact + v) >= ob &&
+            v - e * W <= *((volatile int32_t*)T.minfree + e)) {
+          const bool hit = warp_collide(F.gc, stage_buf(wsb, p.max_tris, p.max_nodes, cur), gr.z,
+                                        gr.w, T.inv + 12 * v, ws, L.cnt);
+          if (lane == 0) {
+            if (hit) {
+              atomicMin(T.contact + v, ob);
+            } else if (atomicSub(T.rem + v, 1u) == 1u && v < vdone &&
+                       *((volatile int32_t*)T.contact + v) == kFree) {
+              atomicMin(T.minfree + e, v - e * W);
+            }
+          }
         }
         __syncwarp();
         q = qn2;
         v = v2;
         ob = ob2;
-        Pn = Pn2;
-        gB = gB2;
+        gr = gr2;
+        cur ^= 1;
       }
       __syncthreads();
       if (tid == 0) F.qn = 0;
@@ -360,7 +397,7 @@ __device__ uint32_t tile_round(const PlaceParams& p, const Sampling& S, const Sb
       if (c == kFree) {  // update_transform (collision.cpp:408-412) + set_enabled
         double2* pp = reinterpret_cast<double2*>(w.pose + sb_pose_off(w, pl.object, inst));
 #pragma unroll
-        for (int k = 0; k < 6; ++k) pp[k] = make_double2(T.pose[12 * v + 2 * k], T.pose[12 * v + 2 * k + 1]);
+        for (int k = 0; k < 6; ++k) pp[k] = __ldcg(reinterpret_cast<const double2*>(p.cpose + ((size_t)blockIdx.x * kB + v) * 12) + k);
         double2* bp = reinterpret_cast<double2*>(w.box + sb_box_off(w, pl.object, inst));
 #pragma unroll
         for (int k = 0; k < 3; ++k) bp[k] = make_double2(T.box[6 * v + 2 * k], T.box[6 * v + 2 * k + 1]);
@@ -476,22 +513,46 @@ __device__ void instance_tiles(const PlaceParams& p, const Sampling& S, const Sb
     if (t >= p.ntiles) break;
     uint32_t nt = tile_load_valid(p, T, F, t);
     int32_t a = 0;
+    unsigned rounds = 0;
+    const unsigned long long tt0 = p.dbg_inst && threadIdx.x == 0 ? global_ns() : 0;
     while (nt > 0 && a < p.attempts) {
+      ++rounds;
       int W = p.spec_target / (int)nt;
       if (W < 1) W = 1;
       if (W > kB / (int)nt) W = kB / (int)nt;
       if (W > p.attempts - a) W = p.attempts - a;
+      if (p.dbg_inst && threadIdx.x == 0) {
+        F.ta = F.tb = 0;
+        F.t0 = global_ns();
+      }
+      const unsigned nslots_dbg = nt * W;
       nt = tile_round(p, S, gA, T, F, nt, a, W, 0, L);
       a += W;
+      if (p.dbg_inst && threadIdx.x == 0) {  // A1 / A2+B / C sums (us) and A2+B max (ns)
+        atomicAdd(p.dbg_inst + 5, (unsigned)(F.ta / 1000));
+        atomicAdd(p.dbg_inst + 6, (unsigned)(F.tb / 1000));
+        atomicAdd(p.dbg_inst + 7, (unsigned)((global_ns() - F.t0) / 1000));
+        atomicMax(p.dbg_inst + 8, (unsigned)F.tb);
+        atomicAdd(p.dbg_inst + 9, nslots_dbg);
+      }
     }
     mark_invalid(p, T, nt);
+    if (p.dbg_inst && threadIdx.x == 0) {  // per-tile debug: max / sum of ns and rounds
+      const unsigned dt = (unsigned)(global_ns() - tt0);
+      atomicMax(p.dbg_inst + 0, dt);
+      atomicAdd(p.dbg_inst + 1, dt / 1000u);
+      atomicMax(p.dbg_inst + 2, rounds);
+      atomicAdd(p.dbg_inst + 3, rounds);
+      atomicAdd(p.dbg_inst + 4, 1u);
+    }
     __syncthreads();
   }
 }
 
-__device__ __forceinline__ void block_setup(const PlaceParams& p, Fixed& F, SbGeom& gA) {
+__device__ __forceinline__ void block_setup(const PlaceParams& p, Fixed& F, Tile& T, SbGeom& gA) {
   gA = p.w.geoms[p.pl.geom];
   load_geom_cache(p.w, gA, F.gc);
+  for (int ob = threadIdx.x; ob < p.w.n_objects; ob += kB) T.ogeo[ob] = obj_grec(p.w, ob);
   __syncthreads();
 }
 
@@ -506,7 +567,7 @@ __global__ void __launch_bounds__(kB, 2) k_place(PlaceParams p) {
     F.tclk = global_ns();
   }
   SbGeom gA;
-  block_setup(p, F, gA);
+  block_setup(p, F, T, gA);
   Local L;
   const Sampling S = resolve_sampling(p);
   if (!S.fast) {
@@ -567,7 +628,7 @@ __global__ void __launch_bounds__(kB, 2) k_place_instances(PlaceParams p) {
   __shared__ Fixed F;
   Tile T = carve(g_dsm, p.w.n_words, p.ws_bytes);
   SbGeom gA;
-  block_setup(p, F, gA);
+  block_setup(p, F, T, gA);
   Local L;
   Sampling S{0, nullptr, nullptr, 0};
   instance_tiles(p, S, gA, T, F, L);
@@ -591,7 +652,7 @@ __global__ void __launch_bounds__(kB, 2) k_fast_round(PlaceParams p, int32_t a) 
   __shared__ Fixed F;
   Tile T = carve(g_dsm, p.w.n_words, p.ws_bytes);
   SbGeom gA;
-  block_setup(p, F, gA);
+  block_setup(p, F, T, gA);
   Local L;
   Sampling S{1, p.canon_tris, p.canon_cum, p.canon_n};
   fast_round(p, S, gA, T, F, a, p.draw_base, L, p.ctrl + place_total_word(a + 1));
@@ -620,8 +681,8 @@ void set_smem(const void* fn, size_t smem) {
 
 int place_ws_bytes(int max_tris, int max_nodes) { return warp_scratch_bytes(max_tris, max_nodes); }
 
-size_t place_smem_bytes(int n_words, int ws_bytes) {
-  return tile_bytes(n_words) + (size_t)kWarps * ws_bytes;
+size_t place_smem_bytes(int n_words, int ws_bytes, int n_objects) {
+  return tile_bytes(n_words) + (size_t)kWarps * ws_bytes + 16 * (size_t)n_objects;
 }
 
 void narrow_profile(unsigned long long out[8], bool reset) {

@@ -62,10 +62,12 @@ struct PlaceParams {
   int32_t spec_target;          // per-instance path: target slots per tile round
   int32_t ws_bytes;             // narrow-phase scratch per warp (sb_warp.cuh)
   int32_t max_tris, max_nodes;  // scratch geometry bounds over the world's geometries
+  double* cpose;                // [grid][kPlaceBlock][12] candidate pose per CTA slot
   uint32_t* ctrl;               // [8] per placement: see Ctrl in sb_place.cu
   unsigned long long* counters; // [8]
   uint64_t draw_base;           // sharded fast path: draws before this rank this round
   unsigned* dbg;                // optional [attempts][3] per-round CTA maxima (ns), fast path
+  unsigned* dbg_inst;           // optional [5] per-instance tiles: max ns, sum us, max/sum rounds, n
   uint64_t* prof;               // optional timers (ns) [init, rounds, -, -, -, rounds]
   // Relation placements on one GPU: the path is chosen on the device. When non-null,
   // *vary_flag != 0 selects the per-instance tables, else the FIFO fast path samples the
@@ -77,7 +79,7 @@ constexpr int kPlaceBlock = 256;
 constexpr int kPlaceMaxOwnedTiles = 64;  // tiles per CTA on the fast path
 
 // Dynamic shared memory of one placement CTA for a world with `n_words` enable words.
-size_t place_smem_bytes(int n_words, int ws_bytes);
+size_t place_smem_bytes(int n_words, int ws_bytes, int n_objects);
 // Narrow-phase scratch bytes per warp for the given geometry bounds.
 int place_ws_bytes(int max_tris, int max_nodes);
 // Co-resident CTAs of the persistent placement kernel (0 if it cannot be launched).

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -144,6 +145,8 @@ struct sb_world {
   DevArray<SbGeom> d_geoms;
   DevArray<SbNode> d_nodes;
   DevArray<SbTri> d_tris;
+  DevArray<int32_t> d_grec;      // per geometry: record offset / length (16 B units), nN, nT
+  DevArray<uint8_t> d_brec;      // compact narrow-phase records (sb_layout.h)
   DevArray<int32_t> d_obj_geom;
   DevArray<double> d_pose;
   DevArray<double> d_box;
@@ -191,6 +194,8 @@ struct sb_world {
     v.geoms = d_geoms.p;
     v.nodes = d_nodes.p;
     v.tris = d_tris.p;
+    v.grec = d_grec.p;
+    v.brec = d_brec.p;
     return v;
   }
 
@@ -252,9 +257,45 @@ struct sb_world {
     cuda_check(cudaMemcpy(d_geoms.p, gs.data(), gs.size() * sizeof(SbGeom), cudaMemcpyHostToDevice), "H2D geoms");
     cuda_check(cudaMemcpy(d_nodes.p, nodes.data(), nodes.size() * sizeof(SbNode), cudaMemcpyHostToDevice), "H2D nodes");
     cuda_check(cudaMemcpy(d_tris.p, tris.data(), tris.size() * sizeof(SbTri), cudaMemcpyHostToDevice), "H2D tris");
+    upload_narrow_records();
     ++stats.geometry_registrations;
     ++stats.bvh_builds;
     return static_cast<int>(geoms.size() - 1);
+  }
+
+  // Compact B-side narrow-phase records (layout in sb_layout.h), rebuilt per registration.
+  void upload_narrow_records() {
+    std::vector<int32_t> grec;
+    std::vector<uint8_t> brec;
+    for (const auto& g : geoms) {
+      const int nN = g.g.n_nodes, nT = g.g.n_tris;
+      const size_t off = brec.size(), len = static_cast<size_t>(sb_brec_bytes(nN, nT));
+      brec.resize(off + len, 0);
+      uint8_t* r = brec.data() + off;
+      for (int k = 0; k < nN; ++k) {
+        const SbNode& nd = nodes[g.g.node_offset + k];
+        double box[6] = {nd.c[0], nd.c[1], nd.c[2], nd.h[0], nd.h[1], nd.h[2]};
+        std::memcpy(r + 48 * k, box, sizeof box);
+        uint32_t info[2];
+        info[0] = static_cast<uint32_t>(nd.child0 < 0 ? 0xff : nd.child0) |
+                  (static_cast<uint32_t>(nd.child1 < 0 ? 0xff : nd.child1) << 8);
+        info[1] = nd.leaves_below;
+        std::memcpy(r + 48 * nN + 8 * k, info, sizeof info);
+      }
+      for (int k = 0; k < nT; ++k) {
+        const SbTri& t = tris[g.g.tri_offset + k];
+        std::memcpy(r + 56 * nN + 72 * k, t.v, 72);
+        r[56 * nN + 72 * nT + k] = static_cast<uint8_t>(t.leaf - 0);
+      }
+      grec.push_back(static_cast<int32_t>(off / 16));
+      grec.push_back(static_cast<int32_t>(len / 16));
+      grec.push_back(nN);
+      grec.push_back(nT);
+    }
+    d_grec.alloc(grec.size());
+    d_brec.alloc(brec.size());
+    cuda_check(cudaMemcpy(d_grec.p, grec.data(), grec.size() * 4, cudaMemcpyHostToDevice), "H2D grec");
+    cuda_check(cudaMemcpy(d_brec.p, brec.data(), brec.size(), cudaMemcpyHostToDevice), "H2D brec");
   }
 
   void grow_objects(int need) {
@@ -413,6 +454,7 @@ struct sb_engine {
   DevArray<int16_t> d_accepted;
   DevArray<uint32_t> d_tile_list;   // [ntiles * tile_inst] survivors per tile
   DevArray<uint32_t> d_tile_cnt;    // [2][ntiles]
+  DevArray<double> d_cpose;         // [grid][kPlaceBlock][12] candidate poses
   DevArray<uint32_t> d_ctrl;
   DevArray<uint64_t> d_prof;
   DevArray<unsigned> d_dbg;        // SB_ROUND_DEBUG=1: per-round CTA maxima (fast path)
@@ -604,7 +646,7 @@ struct sb_engine {
       max_nodes = std::max(max_nodes, static_cast<int>(g.g.n_nodes));
     }
     ws_bytes = sbk::place_ws_bytes(max_tris, max_nodes);
-    smem = sbk::place_smem_bytes(world->view().n_words, ws_bytes);
+    smem = sbk::place_smem_bytes(world->view().n_words, ws_bytes, world->view().n_objects);
     grid = static_cast<unsigned>(sbk::place_grid(num_sms, smem));
     if (grid == 0) throw CudaError("placement kernel does not fit on the device (shared memory)");
     {  // tiles: a multiple of the grid, at most kPlaceBlock instances each
@@ -618,11 +660,13 @@ struct sb_engine {
     }
     d_tile_list.alloc(static_cast<size_t>(ntiles) * tile_inst);
     d_tile_cnt.alloc(2 * static_cast<size_t>(ntiles));
+    d_cpose.alloc(static_cast<size_t>(grid) * sbk::kPlaceBlock * 12);
     d_ctrl.alloc(8 * std::max<size_t>(1, places.size()));
     d_rflags.alloc(2 * std::max<size_t>(1, places.size()));
     d_prof.alloc(8);
     round_debug = std::getenv("SB_ROUND_DEBUG") != nullptr;
-    if (round_debug) d_dbg.alloc(3 * static_cast<size_t>(attempts) * std::max<size_t>(1, places.size()));
+    if (const char* st = std::getenv("SB_SPEC_TARGET")) spec_target = std::max(1, std::atoi(st));
+    if (round_debug) d_dbg.alloc(3 * static_cast<size_t>(attempts) * std::max<size_t>(1, places.size()) + 16);
     d_counters.alloc(8);
     cuda_check(cudaEventCreate(&ev_start), "event");
     cuda_check(cudaEventCreate(&ev_stop), "event");
@@ -781,6 +825,7 @@ struct sb_engine {
       pp.accepted = d_accepted.p + p * n;
       pp.tile_list = d_tile_list.p;
       pp.tile_cnt = d_tile_cnt.p;
+      pp.cpose = d_cpose.p;
       pp.cnt_stride = ntiles;
       pp.ntiles = ntiles;
       pp.tile_inst = tile_inst;
@@ -792,6 +837,7 @@ struct sb_engine {
       pp.counters = d_counters.p;
       pp.prof = d_prof.p;
       pp.dbg = round_debug ? d_dbg.p + 3 * static_cast<size_t>(attempts) * p : nullptr;
+      pp.dbg_inst = round_debug ? d_dbg.p + d_dbg.count - 16 : nullptr;
       pp.vary_flag = (relation && world_size == 1) ? d_rflags.p + 2 * p : nullptr;
       if (world_size == 1) {
         if (!sbk::place_persistent(pp, grid, smem, s))
@@ -874,14 +920,18 @@ struct sb_engine {
     }
     float total_ms = 0.f;
     cuda_check(cudaEventElapsedTime(&total_ms, ev_start, ev_stop), "elapsed");
-    double regions_ms = 0.0, place_ms = 0.0;
+    double regions_ms = 0.0, place_ms = 0.0, inst_ms = 0.0, fast_ms = 0.0;
     for (size_t p = 0; p < P; ++p) {
       float a = 0.f, b = 0.f;
       cuda_check(cudaEventElapsedTime(&a, ev_place[2 * p], ev_place[2 * p + 1]), "elapsed");
       cuda_check(cudaEventElapsedTime(&b, ev_place[2 * p + 1], ev_place[2 * p + 2]), "elapsed");
       regions_ms += a;
       place_ms += b;
+      const bool per_inst = places[p].dev.anchor_object >= 0 && rflags[2 * p] != 0;
+      (per_inst ? inst_ms : fast_ms) += b;
     }
+    last_prof[10] = inst_ms;
+    last_prof[11] = fast_ms;
     uint64_t rounds = rounds_host;
     for (size_t p = 0; p < P; ++p)
       if (device_rounds[p]) rounds += ctrl_all[8 * p + 2];
@@ -894,8 +944,14 @@ struct sb_engine {
     if (round_debug) {
       std::vector<unsigned> dbg(d_dbg.count);
       cuda_check(cudaMemcpy(dbg.data(), d_dbg.p, dbg.size() * sizeof(unsigned), cudaMemcpyDeviceToHost), "D2H dbg");
-      for (int k = 0; k < 3; ++k) last_prof[10 + k] = 0;
-      for (size_t i = 0; i < dbg.size(); ++i) last_prof[10 + i % 3] += dbg[i] * 1e-6;
+      for (int k = 0; k < 3; ++k) last_prof[12 + k] = 0;
+      for (size_t i = 0; i + 16 < dbg.size(); ++i) last_prof[12 + i % 3] += dbg[i] * 1e-6;
+      const unsigned* di = dbg.data() + dbg.size() - 16;
+      std::fprintf(stderr, "[round debug] per-instance tiles: %u, max %.1f us, mean %.1f us, max rounds %u, mean rounds %.2f; "
+                   "per tile-round: A1 %.1f us, A2+B %.1f us, total %.1f us, max A2+B %.1f us, slots %.1f\n",
+                   di[4], di[0] * 1e-3, di[4] ? double(di[1]) / di[4] : 0.0, di[2], di[4] ? double(di[3]) / di[4] : 0.0,
+                   di[3] ? double(di[5]) / di[3] : 0.0, di[3] ? double(di[6]) / di[3] : 0.0,
+                   di[3] ? double(di[7]) / di[3] : 0.0, di[8] * 1e-3, di[3] ? double(di[9]) / di[3] : 0.0);
     }
     last_prof[8] = regions_ms;
     last_prof[9] = total_ms;
@@ -1156,9 +1212,10 @@ uint64_t sb_engine_local_instances(const sb_engine* e) { return e->n; }
 uint64_t sb_engine_last_launches(const sb_engine* e) { return e->last_launches; }
 sb_status sb_debug_narrow_profile(uint64_t out[8]) {
   return guard([&] {
-    unsigned long long v[8];
-    sbk::narrow_profile(v, true);
-    for (int k = 0; k < 8; ++k) out[k] = v[k];
+    unsigned long long v[8], u[8];
+    sbk::narrow_profile(v, true);        // placement kernels (sb_place.cu)
+    sbk::narrow_profile_check(u, true);  // world API check_batch (sb_kernels.cu)
+    for (int k = 0; k < 8; ++k) out[k] = v[k] + u[k];
   });
 }
 

@@ -41,6 +41,42 @@ static __device__ unsigned long long g_nprof[8];
 constexpr int kMaxEffTris = SB_MAX_EFF_TRIS;  // host-checked at registration
 constexpr int kMaxNodes = SB_MAX_NODES_PER_GEOM;
 
+// ---------------------------------------------------------------- async staging
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Bytes of one pair's staging buffer: the placed object's pose (row-major 3x4, 96 B) and
+// the compact record of its geometry (sb_layout.h).
+__host__ __device__ constexpr int stage_bytes(int maxT, int maxN) {
+  return 96 + sb_brec_bytes(maxN, maxT);
+}
+
+// The whole warp issues the asynchronous copies of pair (ob, inst) into `dst` (one commit
+// group per lane); gr = grec[geometry of ob].
+__device__ __forceinline__ void warp_stage(const WorldView& w, const int4 gr, int32_t ob,
+                                           uint64_t inst, unsigned char* dst) {
+  const int lane = threadIdx.x & 31;
+  const unsigned char* pose = reinterpret_cast<const unsigned char*>(w.pose + sb_pose_off(w, ob, inst));
+  const unsigned char* rec = reinterpret_cast<const unsigned char*>(w.brec) + 16 * (size_t)gr.x;
+  for (int c = lane; c < 6 + gr.y; c += 32) {
+    if (c < 6) cp_async16(dst + 16 * c, pose + 16 * c);
+    else cp_async16(dst + 16 * c, rec + 16 * (c - 6));
+  }
+  cp_async_commit();
+}
+
+// {record offset, record length (16 B units), n_nodes, n_tris} of object ob's geometry.
+__device__ __forceinline__ int4 obj_grec(const WorldView& w, int32_t ob) {
+  return __ldg(reinterpret_cast<const int4*>(w.grec) + __ldg(w.obj_geom + ob));
+}
+
 // Per-warp narrow-phase scratch, as pointers into shared memory so a kernel can size it
 // by the world's largest effective geometry (place_ws_bytes) or use the fixed-size
 // WarpScratch below.
@@ -51,18 +87,29 @@ struct WarpScratchView {
   double* bb;          // [maxN][6] B's effective node boxes in A's frame
   double* e2b;         // [maxN] their squared extents
   uint32_t* cm;        // [maxN] B node -> mask of its effective children (0 for leaves)
-  uint32_t* allowed;   // [maxN] allowed[a] bit b: leaf pair reached by the traversal
-  uint32_t* hitw;      // [ceil(maxT^2 / 32)] intersecting triangle pairs (bitset)
-  uint16_t* l1;        // [maxT^2] triangle pairs past filter 1
-  uint16_t* l2;        // [maxT^2] triangle pairs past filter 2
+  uint32_t* allowed;   // [maxN] A leaf -> B leaves whose boxes overlap; later the walk rows
+  uint32_t* H;         // [maxN] A leaf -> B leaves holding an intersecting triangle pair
+  uint32_t* lbb;       // [maxN] B node -> effective leaves below it
+  uint32_t* pend;      // [maxN] pair-DAG walk: visited B nodes per A node
+  uint16_t* l1;        // [max(maxT^2, maxN^2)] triangle pairs past filter 1 / walk frontier
+  uint16_t* l2;        // [max(maxT^2, maxN^2)] triangle pairs past filter 2 / walk frontier
   int8_t* tleafb;      // [maxT]
   int8_t* leafb;       // [maxN] B's leaf node ids, ascending
 };
 
-__host__ __device__ __forceinline__ int warp_scratch_bytes(int maxT, int maxN) {
-  int b = (12 + maxT * 14 + maxN * 7) * 8;
-  b += (2 * maxN + (maxT * maxT + 31) / 32) * 4 + 2 * maxT * maxT * 2 + maxT + maxN;
-  return (b + 15) & ~15;
+__host__ __device__ constexpr int scratch_list_len(int maxT, int maxN) {
+  return maxT * maxT > maxN * maxN ? maxT * maxT : maxN * maxN;
+}
+
+__host__ __device__ constexpr int warp_scratch_bytes(int maxT, int maxN) {
+  return ((((12 + maxT * 14 + maxN * 7) * 8 + 5 * maxN * 4 + 2 * scratch_list_len(maxT, maxN) * 2 +
+            maxT + maxN) + 15) & ~15) +
+         2 * stage_bytes(maxT, maxN);  // + double-buffered staging
+}
+
+// The two staging buffers of a warp's scratch (16-byte aligned, after the scratch arrays).
+__device__ __forceinline__ unsigned char* stage_buf(unsigned char* ws_base, int maxT, int maxN, int k) {
+  return ws_base + warp_scratch_bytes(maxT, maxN) - (2 - k) * stage_bytes(maxT, maxN);
 }
 
 __device__ __forceinline__ WarpScratchView carve_scratch(unsigned char* base, int maxT, int maxN) {
@@ -76,18 +123,18 @@ __device__ __forceinline__ WarpScratchView carve_scratch(unsigned char* base, in
   uint32_t* u = reinterpret_cast<uint32_t*>(v.e2b + maxN);
   v.cm = u;
   v.allowed = u + maxN;
-  v.hitw = u + 2 * maxN;
-  v.l1 = reinterpret_cast<uint16_t*>(v.hitw + (maxT * maxT + 31) / 32);
-  v.l2 = v.l1 + maxT * maxT;
-  v.tleafb = reinterpret_cast<int8_t*>(v.l2 + maxT * maxT);
+  v.H = u + 2 * maxN;
+  v.lbb = u + 3 * maxN;
+  v.pend = u + 4 * maxN;
+  v.l1 = reinterpret_cast<uint16_t*>(u + 5 * maxN);
+  v.l2 = v.l1 + scratch_list_len(maxT, maxN);
+  v.tleafb = reinterpret_cast<int8_t*>(v.l2 + scratch_list_len(maxT, maxN));
   v.leafb = v.tleafb + maxT;
   return v;
 }
 
 struct alignas(16) WarpScratch {  // fixed-size variant (world API check_batch)
-  unsigned char bytes[(12 + kMaxEffTris * 14 + kMaxNodes * 7) * 8 +
-                      (2 * kMaxNodes + kMaxEffTris * kMaxEffTris / 32) * 4 +
-                      4 * kMaxEffTris * kMaxEffTris + kMaxEffTris + kMaxNodes + 16];
+  unsigned char bytes[warp_scratch_bytes(kMaxEffTris, kMaxNodes)];
   __device__ __forceinline__ WarpScratchView view() {
     return carve_scratch(bytes, kMaxEffTris, kMaxNodes);
   }
@@ -104,6 +151,7 @@ struct GeomCache {
   int8_t tleaf[kMaxEffTris];
   uint32_t leafmask;
   int8_t leaves[kMaxNodes];  // leaf node ids, ascending
+  uint32_t lbelow[kMaxNodes];  // effective leaves under each node
   int n_tris, n_nodes, n_leaves;
 };
 
@@ -131,6 +179,7 @@ __device__ __forceinline__ void load_geom_cache(const WorldView& w, const SbGeom
     gc.ext2[k] = nd[k].ext2;
     gc.c0[k] = (int8_t)nd[k].child0;
     gc.c1[k] = (int8_t)nd[k].child1;
+    gc.lbelow[k] = nd[k].leaves_below;
   }
   if (threadIdx.x == 0) {
     uint32_t lm = 0;
@@ -165,22 +214,30 @@ __device__ __forceinline__ int warp_append(bool pass, uint16_t value, uint16_t* 
 //     survive both plane tests. No intersecting pair => the reference cannot report a hit;
 //  3. otherwise the node-pair tests and the pair-DAG walk decide which leaf pairs the
 //     reference traversal reaches; hit = some reached leaf pair holds an intersecting pair.
-__device__ __forceinline__ bool warp_collide(const WorldView& w, const GeomCache& gc,
-                                             const int4 gB, double Pn, const double* I,
+// `stage` = the pair's staged pose + geometry record (warp_stage, copies complete and
+// visible to the warp), nB / nTB = that geometry's node / triangle counts.
+__device__ __forceinline__ bool warp_collide(const GeomCache& gc, const unsigned char* stage,
+                                             int nB, int nTB, const double* I,
                                              const WarpScratchView& ws, CheckCounters& cnt) {
   const int lane = threadIdx.x & 31;
   SB_NP_MARK(np0);
+  const double* P = reinterpret_cast<const double*>(stage);
+  const double* recbox = reinterpret_cast<const double*>(stage + 96);
+  const uint32_t* recinfo = reinterpret_cast<const uint32_t*>(stage + 96 + 48 * nB);
+  const double* rectri = reinterpret_cast<const double*>(stage + 96 + 56 * nB);
+  const int8_t* recleaf = reinterpret_cast<const int8_t*>(stage + 96 + 56 * nB + 72 * nTB);
   if (lane < 12) {  // other_in_cand = inv(cand) * pose(ob), one entry per lane (shim order)
     const int i = lane >> 2, j = lane & 3;
-    const double P0 = __shfl_sync(0xfffu, Pn, j), P1 = __shfl_sync(0xfffu, Pn, 4 + j),
-                 P2 = __shfl_sync(0xfffu, Pn, 8 + j);
-    double s = I[4 * i + 0] * P0;
-    s = s + I[4 * i + 1] * P1;
-    s = s + I[4 * i + 2] * P2;
+    double s = I[4 * i + 0] * P[j];
+    s = s + I[4 * i + 1] * P[4 + j];
+    s = s + I[4 * i + 2] * P[8 + j];
     s = s + I[4 * i + 3] * (j == 3 ? 1.0 : 0.0);
     ws.M[lane] = s;
   }
-  if (lane < gc.n_nodes) ws.allowed[lane] = 0u;  // leaf-pair candidates (step 2)
+  if (lane < gc.n_nodes) {
+    ws.allowed[lane] = 0u;  // leaf-pair candidates (step 2)
+    ws.H[lane] = 0u;        // intersecting leaf pairs (step 4)
+  }
   __syncwarp();
   M34 M;
 #pragma unroll
@@ -188,18 +245,16 @@ __device__ __forceinline__ bool warp_collide(const WorldView& w, const GeomCache
   SB_NP_MARK(np1);
   SB_NP_ADD(0, np0, np1);
 
-  const SbTri* tB = w.tris + gB.z;  // gB = {node_offset, n_nodes, tri_offset, n_tris}
-  const int nTB = gB.w, nTA = gc.n_tris;
-  const int nA = gc.n_nodes, nB = gB.y;
+  const int nTA = gc.n_tris, nA = gc.n_nodes;
 
   // 1: lane b moves B's node b into A's frame (transform_aabb, collision.cpp:297-300; it
   // does not depend on the A node it meets)
-  const SbNode* nodesB = w.nodes + gB.x;
   bool lb = false;
   if (lane < nB) {
-    const SbNode& nb = nodesB[lane];
+    const double* nbox = recbox + 6 * lane;
+    const uint32_t info = recinfo[2 * lane];
     double bmn[3], bmx[3];
-    xform_aabb(M, nb.c, nb.h, bmn, bmx);
+    xform_aabb(M, nbox, nbox + 3, bmn, bmx);
     const double e0 = bmx[0] - bmn[0], e1 = bmx[1] - bmn[1], e2 = bmx[2] - bmn[2];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
@@ -207,8 +262,9 @@ __device__ __forceinline__ bool warp_collide(const WorldView& w, const GeomCache
       ws.bb[6 * lane + 3 + c] = bmx[c];
     }
     ws.e2b[lane] = (e0 * e0 + e1 * e1) + e2 * e2;
-    lb = nb.child0 < 0;
-    ws.cm[lane] = lb ? 0u : ((1u << nb.child0) | (1u << nb.child1));
+    lb = (info & 0xffu) == 0xffu;
+    ws.cm[lane] = lb ? 0u : ((1u << (info & 0xffu)) | (1u << ((info >> 8) & 0xffu)));
+    ws.lbb[lane] = recinfo[2 * lane + 1];
   }
   const uint32_t leafB = __ballot_sync(kFull, lb);
   if (lb) ws.leafb[__popc(leafB & ((1u << lane) - 1u))] = (int8_t)lane;
@@ -245,11 +301,11 @@ __device__ __forceinline__ bool warp_collide(const WorldView& w, const GeomCache
   // 3: B's effective triangles into A's frame (transform_point, collision.cpp:308-310) and
   // their planes; A's planes are cached per launch.
   for (int v = lane; v < nTB * 3; v += 32) {
-    const double* p = tB[v / 3].v + 3 * (v % 3);
-    double* q = ws.qb + 9 * (v / 3) + 3 * (v % 3);
-    xform(M, __ldg(p), __ldg(p + 1), __ldg(p + 2), q[0], q[1], q[2]);
+    const double* p = rectri + 3 * v;
+    double* q = ws.qb + 3 * v;
+    xform(M, p[0], p[1], p[2], q[0], q[1], q[2]);
   }
-  for (int k = lane; k < nTB; k += 32) ws.tleafb[k] = (int8_t)tB[k].leaf;
+  for (int k = lane; k < nTB; k += 32) ws.tleafb[k] = recleaf[k];
   __syncwarp();
   for (int k = lane; k < nTB; k += 32) {
     const TriPlane P = tri_plane(ws.qb + 9 * k);
@@ -261,7 +317,6 @@ __device__ __forceinline__ bool warp_collide(const WorldView& w, const GeomCache
     pb[4] = P.tol;
   }
   const int ntp = nTA * nTB;
-  for (int k = lane; k < (ntp + 31) / 32; k += 32) ws.hitw[k] = 0u;
   __syncwarp();
 
   // 4: staged tri_tri_intersect over the triangle pairs k = ia * nTB + ib of candidate
@@ -316,7 +371,7 @@ __device__ __forceinline__ bool warp_collide(const WorldView& w, const GeomCache
       plane_dists(gc.pa[ia], gc.pa[ia][3], gc.pa[ia][4], q, dq0, dq1, dq2);
       hit = tri_tri_finish(gc.ta[ia], q, gc.pa[ia], pb, dp0, dp1, dp2, dq0, dq1, dq2);
     }
-    if (hit) atomicOr(ws.hitw + (k >> 5), 1u << (k & 31));
+    if (hit) atomicOr(ws.H + gc.tleaf[k / nTB], 1u << ws.tleafb[k - (k / nTB) * nTB]);
     any = __any_sync(kFull, hit) || any;
   }
   SB_NP_MARK(np2);
@@ -324,94 +379,119 @@ __device__ __forceinline__ bool warp_collide(const WorldView& w, const GeomCache
   if (!any) return false;
   __syncwarp();
 
-  // 5a: pass(a,b) = na.box.overlaps(nb_in_a) and the descend rule
-  // desc(a,b) = leaf(nb) || (!leaf(na) && ext2(na) >= ext2(nb_in_a)) for all (a, b),
-  // 32 pairs per ballot; lane a collects row a (pair k = a * nB + b).
-  uint32_t rpass = 0u, rdesc = 0u;
-  const int np = nA * nB;
-  for (int k0 = 0; k0 < np; k0 += 32) {
-    const int k = k0 + lane;
-    bool pb = false, db = false;
-    if (k < np) {
-      const int a = k / nB, bi = k - a * nB;
-      const double* bb = ws.bb + 6 * bi;
-      pb = gc.bmin[a][0] <= bb[3] && bb[0] <= gc.bmax[a][0] && gc.bmin[a][1] <= bb[4] &&
-           bb[1] <= gc.bmax[a][1] && gc.bmin[a][2] <= bb[5] && bb[2] <= gc.bmax[a][2];
-      db = ((leafB >> bi) & 1u) || (!((gc.leafmask >> a) & 1u) && gc.ext2[a] >= ws.e2b[bi]);
+  // 5: walk the pair DAG from (0,0) -- the reference's stack traversal with children read
+  // as {left, left+1} (collision.cpp:285-329) -- level by level (one lane per frontier
+  // pair; each node pair enters the frontier once), pruned to the node pairs whose
+  // subtrees hold an intersecting leaf pair: rows[a] = { b : leaves_below(a) x
+  // leaves_below(b) meets H }. Every path to such a leaf pair runs through these pairs
+  // only, and an existential does not depend on the visiting order, so the verdict --
+  // some intersecting leaf pair is reached with every box test on the way passing -- is
+  // the reference's. Box tests and the descend rule are evaluated at visited pairs only.
+  if (lane < nA) {
+    uint32_t la = gc.lbelow[lane], RA = 0u;
+    while (la) {
+      RA |= ws.H[__ffs(la) - 1];
+      la &= la - 1u;
     }
-    const uint32_t P = __ballot_sync(kFull, pb), D = __ballot_sync(kFull, db);
-    if (lane < nA) {
-      const int lo = lane * nB;
-      const int s0 = lo > k0 ? lo : k0;
-      const int e0 = (lo + nB) < (k0 + 32) ? (lo + nB) : (k0 + 32);
-      if (s0 < e0) {
-        const int len = e0 - s0;
-        const uint32_t mk = len >= 32 ? 0xffffffffu : ((1u << len) - 1u);
-        rpass |= ((P >> (s0 - k0)) & mk) << (s0 - lo);
-        rdesc |= ((D >> (s0 - k0)) & mk) << (s0 - lo);
-      }
-    }
-  }
-  SB_NP_MARK(np3);
-  SB_NP_ADD(2, np2, np3);
-
-  // 3c: walk the pair DAG from (0,0) in lexicographic order (a topological order: every
-  // child id exceeds its parent's). Lane a owns the pending row of A node a; descending A
-  // forwards the row's bits to the lanes of A's effective children.
-  {
-    uint32_t pend = lane == 0 ? 1u : 0u, allowed = 0u;
-    const bool la = lane < nA && ((gc.leafmask >> lane) & 1u);
-    const int c0 = lane < nA ? gc.c0[lane] : -1, c1 = lane < nA ? gc.c1[lane] : -1;
-    unsigned visited = 0;
-    for (int a = 0; a < nA; ++a) {
-      uint32_t down = 0u;
-      if (lane == a) {
-        while (pend) {
-          const int bi = __ffs(pend) - 1;
-          pend &= pend - 1u;
-          ++visited;
-          if (!((rpass >> bi) & 1u)) continue;
-          if (la && ((leafB >> bi) & 1u)) allowed |= 1u << bi;
-          else if ((rdesc >> bi) & 1u) down |= 1u << bi;
-          else pend |= ws.cm[bi];
-        }
-      }
-      down = __shfl_sync(kFull, down, a);
-      const int d0 = __shfl_sync(kFull, c0, a), d1 = __shfl_sync(kFull, c1, a);
-      if (down && (lane == d0 || lane == d1)) pend |= down;
-    }
-    if (lane < nA) ws.allowed[lane] = allowed;
-    cnt.nodes += visited;
+    uint32_t row = 0u;
+    if (RA)
+      for (int b = 0; b < nB; ++b)
+        if (ws.lbb[b] & RA) row |= 1u << b;
+    ws.allowed[lane] = row;
+    ws.pend[lane] = lane == 0 ? 1u : 0u;  // visited
   }
   __syncwarp();
+  SB_NP_MARK(np3);
+  SB_NP_ADD(2, np2, np3);
+  // Certificate: every path from (0,0) to an intersecting leaf pair runs through relevant
+  // pairs only, and from any relevant pair the descend rule always continues towards one
+  // (leaves_below of a node is the union of its children's). So if EVERY relevant pair
+  // passes its box test, every intersecting leaf pair is reached: hit. Node boxes contain
+  // their descendants', so this is the common case; a failing test (boxes that only touch
+  // after rounding) falls back to the exact walk below.
+  {
+    bool all = true;
+    const int np = nA * nB;
+    for (int k0 = 0; k0 < np; k0 += 32) {
+      const int k = k0 + lane;
+      if (k < np) {
+        const int a = k / nB, b = k - a * nB;
+        if ((ws.allowed[a] >> b) & 1u) {
+          const double* bb = ws.bb + 6 * b;
+          ++cnt.nodes;
+          all = all && gc.bmin[a][0] <= bb[3] && bb[0] <= gc.bmax[a][0] &&
+                gc.bmin[a][1] <= bb[4] && bb[1] <= gc.bmax[a][1] && gc.bmin[a][2] <= bb[5] &&
+                bb[2] <= gc.bmax[a][2];
+        }
+      }
+    }
+    if (__all_sync(kFull, all)) {
+      SB_NP_MARK(np4c);
+      SB_NP_ADD(3, np3, np4c);
+      SB_NP_ADD(5, 0, 1);
+      return true;
+    }
+  }
+  bool res = false;
+  if (ws.allowed[0] & 1u) {
+    uint16_t* F = ws.l1;
+    uint16_t* G = ws.l2;
+    if (lane == 0) F[0] = 0;
+    int nf = 1;
+    __syncwarp();
+    while (nf > 0) {
+      int ng = 0;
+      bool hit = false;
+      for (int i0 = 0; i0 < nf; i0 += 32) {
+        const int i = i0 + lane;
+        int ch0 = -1, ch1 = -1;  // children (a << 5 | b) entering the next level
+        if (i < nf) {
+          const int e = F[i];
+          const int a = e >> 5, b = e & 31;
+          ++cnt.nodes;
+          const double* bb = ws.bb + 6 * b;
+          if (gc.bmin[a][0] <= bb[3] && bb[0] <= gc.bmax[a][0] && gc.bmin[a][1] <= bb[4] &&
+              bb[1] <= gc.bmax[a][1] && gc.bmin[a][2] <= bb[5] && bb[2] <= gc.bmax[a][2]) {
+            const bool la = (gc.leafmask >> a) & 1u, lb = (leafB >> b) & 1u;
+            if (la && lb) {
+              hit = (ws.H[a] >> b) & 1u;
+            } else if (lb || (!la && gc.ext2[a] >= ws.e2b[b])) {  // descend A (collision.cpp:320)
+              ch0 = (gc.c0[a] << 5) | b;
+              ch1 = (gc.c1[a] << 5) | b;
+            } else {
+              const uint32_t cm = ws.cm[b];
+              ch0 = (a << 5) | (__ffs(cm) - 1);
+              ch1 = (a << 5) | (__ffs(cm & (cm - 1u)) - 1);
+            }
+            auto admit = [&](int c) {
+              if (c < 0) return -1;
+              const uint32_t bit = 1u << (c & 31);
+              if (!(ws.allowed[c >> 5] & bit)) return -1;
+              return (atomicOr(ws.pend + (c >> 5), bit) & bit) ? -1 : c;
+            };
+            ch0 = admit(ch0);
+            ch1 = admit(ch1);
+          }
+        }
+        if (__any_sync(kFull, hit)) {
+          res = true;
+          break;
+        }
+        ng = warp_append(ch0 >= 0, (uint16_t)ch0, G, ng);
+        ng = warp_append(ch1 >= 0, (uint16_t)ch1, G, ng);
+      }
+      if (res) break;
+      __syncwarp();
+      uint16_t* t = F;
+      F = G;
+      G = t;
+      nf = ng;
+    }
+  }
   SB_NP_MARK(np4);
   SB_NP_ADD(3, np3, np4);
-
-  // 3d: does some intersecting pair lie in a reached leaf pair?
-  bool ok = false;
-  for (int k0 = 0; k0 < ntp; k0 += 32) {
-    const int idx = k0 + lane;
-    if (idx >= ntp) continue;
-    const int ia = idx / nTB, ib = idx - ia * nTB;
-    const bool reached = (ws.allowed[gc.tleaf[ia]] >> ws.tleafb[ib]) & 1u;
-    ok = ok || (reached && ((ws.hitw[k0 >> 5] >> lane) & 1u));
-  }
-  const bool res = __any_sync(kFull, ok);
-  SB_NP_MARK(np5);
-  SB_NP_ADD(4, np4, np5);
   SB_NP_ADD(5, 0, 1);
   return res;
-}
-
-// {node_offset, n_nodes, tri_offset, n_tris} of object ob's geometry (SbGeom's first 16 B).
-__device__ __forceinline__ int4 geom_ref(const WorldView& w, int32_t ob) {
-  return __ldg(reinterpret_cast<const int4*>(w.geoms + __ldg(w.obj_geom + ob)));
-}
-
-// Placed object's pose entry for lane < 12 (row-major 3x4), the narrow phase's `Pn`.
-__device__ __forceinline__ double pose_entry(const WorldView& w, int32_t ob, uint64_t inst) {
-  const int lane = threadIdx.x & 31;
-  return lane < 12 ? __ldcg(w.pose + sb_pose_off(w, ob, inst) + lane) : 0.0;
 }
 
 // Pooled check of the warp's 32 candidates (inactive lanes pass active = false but must
@@ -457,7 +537,12 @@ __device__ __forceinline__ int warp_check(const WorldView& w, const SbGeom& gA,
         const uint32_t ovL = __shfl_sync(kFull, ovm, L);
         const uint64_t instL = __shfl_sync(kFull, inst, L);
         const int ob = ob0 + __ffs(ovL) - 1;
-        const bool hit = warp_collide(w, gc, geom_ref(w, ob), pose_entry(w, ob, instL), invs[L], ws, cnt);
+        const int4 gr = obj_grec(w, ob);
+        unsigned char* st = stage_buf(wsf.bytes, kMaxEffTris, kMaxNodes, 0);
+        warp_stage(w, gr, ob, instL, st);
+        cp_async_wait<0>();
+        __syncwarp();
+        const bool hit = warp_collide(gc, st, gr.z, gr.w, invs[L], ws, cnt);
         if (lane == L) {
           ++cnt.narrow;
           ovm &= ovm - 1u;

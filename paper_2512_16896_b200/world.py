@@ -372,7 +372,8 @@ class Engine:
         # block 0's device clock inside the placement kernels (see the C header)
         keys = ("init_ms", "prefix_ms", "sample_ms", "broad_narrow_ms", "accept_ms",
                 "grid_sync_ms", "per_instance_ms", "fast_rounds", "regions_ms", "total_ms",
-                "dbg_round_max_ms", "dbg_a1_max_ms", "dbg_a2b_max_ms")
+                "ev_per_instance_ms", "ev_fast_ms", "dbg_round_max_ms", "dbg_a1_max_ms",
+                "dbg_a2b_max_ms")
         return dict(zip(keys, list(out)))
 
     def last_launches(self) -> int:

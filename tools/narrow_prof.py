@@ -12,5 +12,5 @@ A.check(A.lib().sb_debug_narrow_profile(out))
 eng.generate(1, with_poses=False, download=False)
 A.check(A.lib().sb_debug_narrow_profile(out))
 v = list(out); pairs = max(1, v[5])
-names = ["M", "B tris+planes", "node tests", "DAG walk", "hit check", "-", "filter1", "filter2+rest"]
+names = ["M", "B nodes+leaf", "walk rows", "walk", "-", "-", "filter1", "filter2+rest"]
 print(cfg, "pairs", pairs, {n: round(v[i] / pairs) for i, n in enumerate(names) if n != "-"})
