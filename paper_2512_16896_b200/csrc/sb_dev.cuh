@@ -366,6 +366,32 @@ __device__ __forceinline__ bool collide(const SbNode* __restrict__ A, int nA,
   return false;
 }
 
+// ------------------------------------------------------------------ occupancy grid
+__device__ __forceinline__ int cell_of(double v, double v0, double inv, int g) {
+  const double f = floor((v - v0) * inv);
+  if (!(f >= 0.0)) return 0;  // also NaN
+  return f >= (double)g ? g - 1 : (int)f;
+}
+
+// Cell range [cx0, cx1] x [cy0, cy1] of a world box (min xyz, max xyz).
+__device__ __forceinline__ void cell_range(const SbCellGrid& G, const double* mn, const double* mx,
+                                           int& cx0, int& cx1, int& cy0, int& cy1) {
+  cx0 = cell_of(mn[0], G.x0, G.inv_x, G.g);
+  cx1 = cell_of(mx[0], G.x0, G.inv_x, G.g);
+  cy0 = cell_of(mn[1], G.y0, G.inv_y, G.g);
+  cy1 = cell_of(mx[1], G.y0, G.inv_y, G.g);
+}
+
+// Set object `obj`'s bit in the cells its world box (min xyz, max xyz) meets.
+__device__ __forceinline__ void cell_insert(const SbCellGrid& G, uint64_t inst, int32_t obj,
+                                            const double* mn, const double* mx) {
+  int cx0, cx1, cy0, cy1;
+  cell_range(G, mn, mx, cx0, cx1, cy0, cy1);
+  uint32_t* base = G.cells + inst * (uint64_t)(G.g * G.g) * G.words + (obj >> 5);
+  for (int cy = cy0; cy <= cy1; ++cy)
+    for (int cx = cx0; cx <= cx1; ++cx) base[(uint64_t)(cy * G.g + cx) * G.words] |= 1u << (obj & 31);
+}
+
 // ------------------------------------------------------------------ world view
 using WorldView = SbWorldView;
 

@@ -140,6 +140,20 @@ __global__ void k_engine_reset(WorldView w, int32_t first_obj, int32_t n_obj, ui
   for (int32_t p = 0; p < n_place; ++p) accepted[(uint64_t)p * w.n + i] = -1;
 }
 
+// Occupancy grid at generate() start: cells cleared, then the enabled fixed objects
+// (ids < first_obj) inserted from their world boxes. Thread per instance.
+__global__ void k_cells_reset(WorldView w, SbCellGrid G, int32_t first_obj) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= w.n) return;
+  uint32_t* c = G.cells + i * (uint64_t)(G.g * G.g) * G.words;
+  for (int k = 0; k < G.g * G.g * G.words; ++k) c[k] = 0u;
+  for (int32_t o = 0; o < first_obj; ++o) {
+    if (!((w.enabled[sb_word_off(w, o >> 5, i)] >> (o & 31)) & 1u)) continue;
+    const double* b = w.box + sb_box_off(w, o, i);
+    cell_insert(G, i, o, b, b + 3);
+  }
+}
+
 // AnchorState in the support frame: inverse_rigid(support) * anchor pose; position is the
 // translation, yaw = yaw_of (transform.hpp:77).
 __global__ void k_anchor_states(WorldView w, int32_t anchor_obj, M34 inv_support, double* out) {
@@ -241,6 +255,10 @@ void engine_reset(const SbWorldView& w, int32_t first_obj, int32_t n_obj, uint8_
                   int16_t* accepted, int32_t n_place, sb_stream_t s) {
   k_engine_reset<<<grid_for(w.n), kBlock, 0, s>>>(w, first_obj, n_obj, valid, accepted, n_place);
   check_launch("engine_reset");
+}
+void cells_reset(const SbWorldView& w, const SbCellGrid& g, int32_t first_obj, sb_stream_t s) {
+  k_cells_reset<<<grid_for(w.n), kBlock, 0, s>>>(w, g, first_obj);
+  check_launch("cells_reset");
 }
 void anchor_states(const SbWorldView& w, int32_t anchor_obj, const double inv_support[12],
                    double* out, sb_stream_t s) {

@@ -36,6 +36,8 @@ void narrow_profile_check(unsigned long long out[8], bool reset);
 // engine bookkeeping
 void engine_reset(const SbWorldView& w, int32_t first_obj, int32_t n_obj, uint8_t* valid,
                   int16_t* accepted, int32_t n_place, sb_stream_t s);
+// broad-phase occupancy grid: clear, then insert the enabled fixed objects (ids < first_obj)
+void cells_reset(const SbWorldView& w, const SbCellGrid& g, int32_t first_obj, sb_stream_t s);
 // AnchorState per instance (support frame): out[3i..3i+2] = x, y, yaw
 void anchor_states(const SbWorldView& w, int32_t anchor_obj, const double inv_support[12],
                    double* out, sb_stream_t s);

@@ -75,6 +75,17 @@ struct SbWorldView {
   const void* brec;           // 16-byte aligned records
 };
 
+// Per-instance XY occupancy grid of the engine's broad phase: cell (cx, cy) of instance i
+// holds the enabled objects whose world AABB meets the cell (bit o of word o >> 5).
+// Cell index = clamp(floor((x - x0) * inv_x), 0, g - 1) -- monotone in x, so a candidate box
+// and an object box that overlap always share a cell; the exact AABB test then decides.
+struct SbCellGrid {
+  double x0, y0, inv_x, inv_y;
+  int32_t g;        // cells per side (0 = no grid)
+  int32_t words;    // words per cell (= enable words)
+  uint32_t* cells;  // [n][g * g][words]
+};
+
 // Narrow-phase record of one geometry, 16-byte aligned, byte offsets:
 //   [0, 48 nN)                 node boxes: c xyz, h xyz (double)
 //   [48 nN, 56 nN)             node info: u32 child0 | child1 << 8 (0xff = none),

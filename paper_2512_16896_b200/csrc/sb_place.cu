@@ -22,9 +22,10 @@ namespace {
 constexpr int kB = kPlaceBlock;
 constexpr int kWarps = kB / 32;
 constexpr int32_t kFree = INT32_MAX;
-constexpr int kQueue = 2048;  // shared-memory narrow-phase queue (slot << 24 | object)
-constexpr int kU = 4;         // broad-phase items per thread per batch (loads in flight)
-constexpr uint8_t kSlotChecked = 1, kSlotUnplaceable = 2;
+constexpr int kCand = 1024;   // broad-phase items per chunk
+constexpr int kQueue = kCand; // narrow pairs per chunk (at most one per item)
+constexpr uint8_t kSlotChecked = 1, kSlotUnplaceable = 2, kSlotEnumerated = 4;
+constexpr int kGW = 8;  // enable words the broad phase keeps in registers (<= 256 objects)
 constexpr int kPrefixItems = 8;  // tile counts per thread per prefix-scan chunk
 
 enum Ctrl { kRounds = 2, kErr = 3, kTileCtr = 4 /* kTotal0 = 5, kTotal1 = 6 */ };
@@ -38,7 +39,8 @@ struct Tile {
   uint32_t* ovm;     // [words][kB] broad-phase overlap bits per slot
   uint32_t* enw;     // [words][kB] enable words per tile entry
   uint32_t* list;    // [kB] tile's active instances (ascending)
-  uint32_t* queue;   // [kQueue]
+  uint32_t* queue;   // [kQueue] narrow pairs (slot << 24 | object)
+  uint32_t* cand;    // [kCand] broad-phase items (slot << 24 | object)
   int32_t* contact;  // [kB] min colliding object per slot
   uint32_t* rem;     // [kB] queued, not yet tested pairs per slot
   int32_t* minfree;  // [kB] per tile entry: lowest slot (attempt offset) confirmed free, W = none
@@ -53,7 +55,8 @@ struct Fixed {  // static shared memory
   uint32_t prefix[kPlaceMaxOwnedTiles];  // fast path: draw offset of each owned tile
   uint32_t cnt[kPlaceMaxOwnedTiles];     // fast path: its survivors entering this round
   uint32_t qn;
-  uint32_t vdone;  // slots whose broad-phase items are all enumerated
+  uint32_t dq, dt;  // debug: pairs queued / tested this tile round
+  uint32_t qhead;   // narrow-phase claim counter
   uint32_t total;
   uint32_t tile;
   unsigned long long tclk;  // block 0 / thread 0 phase clock
@@ -69,7 +72,8 @@ __device__ __forceinline__ Tile carve(unsigned char* d, int words, int ws_bytes)
   t.enw = t.ovm + words * kB;
   t.list = t.enw + words * kB;
   t.queue = t.list + kB;
-  t.contact = reinterpret_cast<int32_t*>(t.queue + kQueue);
+  t.cand = t.queue + kQueue;
+  t.contact = reinterpret_cast<int32_t*>(t.cand + kCand);
   t.rem = reinterpret_cast<uint32_t*>(t.contact + kB);
   t.minfree = reinterpret_cast<int32_t*>(t.rem + kB);
   t.sflag = reinterpret_cast<uint8_t*>(t.minfree + kB);
@@ -80,7 +84,7 @@ __device__ __forceinline__ Tile carve(unsigned char* d, int words, int ws_bytes)
 
 __host__ __device__ constexpr size_t tile_bytes(int words) {
   return (12 + 6) * 8 * (size_t)kB + 2 * (size_t)words * kB * 4 + (size_t)kB * 4 +
-         (size_t)kQueue * 4 + 3 * (size_t)kB * 4 + kB;
+         (size_t)(kQueue + kCand) * 4 + 3 * (size_t)kB * 4 + kB;
 }
 
 struct Local {  // per-thread counters, flushed once at kernel end
@@ -150,9 +154,74 @@ __device__ __forceinline__ void lap(const PlaceParams& p, Fixed& F, int slot) {
   }
 }
 
+// ---------------- B: warp per queued pair (warp w takes entries w, w + 8, ...). Pairs
+// behind a lower hit of their slot, or of a slot beyond their instance's lowest
+// confirmed-free attempt, are skipped before any data is staged; the next eligible pair's
+// pose and geometry record are copied into the warp's other staging buffer (cp.async)
+// while the current one is tested. All threads of the CTA call it.
+__device__ __forceinline__ void narrow_drain(const PlaceParams& p, Tile& T, Fixed& F, uint32_t nt, uint32_t qn,
+                             Local& L) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const WorldView& w = p.w;
+  const WarpScratchView ws = carve_scratch(T.ws + warp * p.ws_bytes, p.max_tris, p.max_nodes);
+  unsigned char* wsb = T.ws + warp * p.ws_bytes;
+  auto skippable = [&](int v, int ob) {
+    return *((volatile int32_t*)T.contact + v) < ob ||
+           v / (int)nt > *((volatile int32_t*)T.minfree + v % (int)nt);
+  };
+  auto next_eligible = [&](uint32_t q) {  // first non-skippable entry at q, q + 8, ...
+    for (; q < qn; q += kWarps) {
+      const uint32_t ent = T.queue[q];
+      if (!skippable((int)(ent >> 24), (int)(ent & 0xffffffu))) break;
+    }
+    return q;
+  };
+  auto stage = [&](uint32_t ent, int buf) {
+    const int v = (int)(ent >> 24), ob = (int)(ent & 0xffffffu);
+    warp_stage(w, T.ogeo[ob], ob, T.list[v % (int)nt], stage_buf(wsb, p.max_tris, p.max_nodes, buf));
+  };
+  int cur = 0;
+  uint32_t q = next_eligible(warp);
+  if (q < qn) stage(T.queue[q], cur);
+  while (q < qn) {
+    const uint32_t ent_cur = T.queue[q];
+    const uint32_t q2 = next_eligible(q + kWarps);
+    if (q2 < qn) {
+      stage(T.queue[q2], cur ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncwarp();
+    const int v = (int)(ent_cur >> 24), ob = (int)(ent_cur & 0xffffffu);
+    if (!skippable(v, ob)) {
+      const int e = v % (int)nt, sl = v / (int)nt;
+      const bool hit = warp_collide(F.gc, stage_buf(wsb, p.max_tris, p.max_nodes, cur),
+                                    T.ogeo[ob].z, T.ogeo[ob].w, T.inv + 12 * v, ws, L.cnt);
+      if (p.dbg_inst && lane == 0) atomicAdd(&F.dt, 1u);
+      if (lane == 0) {
+        if (hit) {
+          atomicMin(T.contact + v, ob);
+        } else if (atomicSub(T.rem + v, 1u) == 1u &&
+                   (*((volatile uint8_t*)T.sflag + v) & kSlotEnumerated) &&
+                   *((volatile int32_t*)T.contact + v) == kFree) {
+          atomicMin(T.minfree + e, sl);
+        }
+      }
+    }
+    __syncwarp();
+    q = q2;
+    cur ^= 1;
+  }
+}
+
 // ------------------------------------------------------------------ one tile round
 // Evaluates attempts [a, a + W) of the tile's nt active instances (T.list) and compacts the
-// survivors in place. Returns the survivor count. All threads of the CTA call it.
+// survivors in place. Slots are attempt-major (slot v = s * nt + e is attempt a + s of entry
+// e), so the narrow queue lists every instance's first attempt before any second one and
+// an instance's later attempts are mostly skipped once a lower one is confirmed free.
+// Returns the survivor count. All threads of the CTA call it.
+template <bool kGrid>
 __device__ uint32_t tile_round(const PlaceParams& p, const Sampling& S, const SbGeom& gA,
                                Tile& T, Fixed& F, uint32_t nt, int32_t a, int W,
                                uint64_t draw_base, Local& L) {
@@ -170,8 +239,8 @@ __device__ uint32_t tile_round(const PlaceParams& p, const Sampling& S, const Sb
   // ---------------- A1: thread per slot
   if (tid < nslots) {
     const int v = tid;
-    const int e = v / W;
-    const int32_t at = a + (v - e * W);
+    const int e = v % (int)nt;  // attempt-major slots: v = s * nt + e
+    const int32_t at = a + v / (int)nt;
     const uint32_t inst = T.list[e];
     const uint64_t gid = p.global_begin + inst;
     bool placeable = true;
@@ -199,7 +268,7 @@ __device__ uint32_t tile_round(const PlaceParams& p, const Sampling& S, const Sb
     }
     T.contact[v] = kFree;
     T.rem[v] = 0u;
-    if (v - e * W == 0) T.minfree[e] = W;
+    if (v < (int)nt) T.minfree[e] = W;
     for (int wd = 0; wd < words; ++wd) T.ovm[wd * kB + v] = 0u;
     if (!placeable) {
       T.sflag[v] = kSlotUnplaceable;
@@ -254,120 +323,189 @@ __device__ uint32_t tile_round(const PlaceParams& p, const Sampling& S, const Sb
   }
   if (tid == 0) {
     F.qn = 0;
-    F.vdone = 0;
+    F.dq = F.dt = 0;
   }
   __syncthreads();
   lap(p, F, 2);
   dbg_mark(p, F, F.ta);
 
-  // ---------------- A2 (broad phase) interleaved with B (narrow phase) in queue batches
-  const int items = nslots * nobj;
-  for (int it0 = 0; it0 < items; it0 += kB * kU) {
-    bool ov[kU];
-    int vs[kU], obs[kU];
+  if constexpr (!kGrid) {
+    // ---------------- A2 (broad phase) + B, few objects: item per (slot, enabled object),
+    // four box loads in flight per thread (aabb.hpp:29-33, collision.cpp:439-443); the
+    // queue (queue + cand storage, kQueue + kCand entries) is drained when nearly full.
+    constexpr int kU = 4;
+    constexpr uint32_t kQD = kQueue + kCand;
+    const int items = nslots * nobj;
+    for (int it0 = 0; it0 < items; it0 += kB * kU) {
+      bool ov[kU];
+      int vs[kU], obs[kU];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int it = it0 + u * kB + tid;
-      ov[u] = false;
-      vs[u] = 0;
-      obs[u] = 0;
-      if (it < items) {
-        const int v = it / nobj;
-        const int ob = it - v * nobj;
-        vs[u] = v;
-        obs[u] = ob;
-        if (T.sflag[v] == kSlotChecked &&
-            ((T.enw[(ob >> 5) * kB + v / W] >> (ob & 31)) & 1u)) {
-          ++L.cnt.broad;
-          const double2* bp = reinterpret_cast<const double2*>(w.box + sb_box_off(w, ob, T.list[v / W]));
-          const double2 b0 = __ldcg(bp), b1 = __ldcg(bp + 1), b2 = __ldcg(bp + 2);
-          const double* cb = T.box + 6 * v;
-          ov[u] = cb[0] <= b1.y && b0.x <= cb[3] && cb[1] <= b2.x && b0.y <= cb[4] &&
-                  cb[2] <= b2.y && b1.x <= cb[5];
-        }
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const uint32_t mask = __ballot_sync(kFull, ov[u]);
-      if (!mask) continue;
-      uint32_t base = 0;
-      if (lane == 0) base = atomicAdd(&F.qn, (uint32_t)__popc(mask));
-      base = __shfl_sync(kFull, base, 0);
-      if (ov[u]) {
-        atomicOr(T.ovm + (obs[u] >> 5) * kB + vs[u], 1u << (obs[u] & 31));
-        atomicAdd(T.rem + vs[u], 1u);
-        T.queue[base + __popc(mask & ((1u << lane) - 1u))] = ((uint32_t)vs[u] << 24) | (uint32_t)obs[u];
-      }
-    }
-    __syncthreads();
-    // Slots whose items are now all enumerated and whose queued pairs are all tested
-    // without a hit are free: the instance's lowest such attempt bounds the useful work.
-    const int vdone_old = (int)F.vdone;
-    int vdone = (it0 + kB * kU >= items) ? nslots : (it0 + kB * kU) / nobj;
-    for (int v = vdone_old + tid; v < vdone; v += kB)
-      if (T.sflag[v] == kSlotChecked && T.rem[v] == 0u && T.contact[v] == kFree)
-        atomicMin(T.minfree + v / W, v - (v / W) * W);
-    __syncthreads();
-    if (tid == 0) F.vdone = (uint32_t)vdone;
-    const uint32_t qn = F.qn;
-    if (it0 + kB * kU >= items || qn > (uint32_t)(kQueue - kB * kU)) {
-      // ---------------- B: warp per queued pair; skip pairs behind a lower hit
-      const WarpScratchView ws = carve_scratch(T.ws + warp * p.ws_bytes, p.max_tris, p.max_nodes);
-      // software-pipelined: the next pair's pose and geometry record are copied into the
-      // warp's other staging buffer (cp.async) while the current pair is tested
-      unsigned char* wsb = T.ws + warp * p.ws_bytes;
-      uint32_t q = warp;
-      int v = 0, ob = 0, cur = 0;
-      int4 gr = make_int4(0, 0, 0, 0);
-      auto fetch = [&](uint32_t qq, int& v_, int& ob_, int4& g_, int buf) {
-        const uint32_t ent = T.queue[qq];
-        v_ = (int)(ent >> 24);
-        ob_ = (int)(ent & 0xffffffu);
-        g_ = T.ogeo[ob_];
-        warp_stage(w, g_, ob_, T.list[v_ / W], stage_buf(wsb, p.max_tris, p.max_nodes, buf));
-      };
-      if (q < qn) fetch(q, v, ob, gr, 0);
-      while (q < qn) {
-        const uint32_t qn2 = q + kWarps;
-        int v2 = 0, ob2 = 0;
-        int4 gr2 = make_int4(0, 0, 0, 0);
-        if (qn2 < qn) {
-          fetch(qn2, v2, ob2, gr2, cur ^ 1);
-          cp_async_wait<1>();
-        } else {
-          cp_async_wait<0>();
-        }
-        __syncwarp();
-        // skip pairs behind a lower hit of their slot, or of a slot beyond the instance's
-        // lowest confirmed-free attempt (neither can change the first-valid result)
-        const int e = v / W;
-        if (*((volatile int32_t*)T.contact + v) >= ob &&
-            v - e * W <= *((volatile int32_t*)T.minfree + e)) {
-          const bool hit = warp_collide(F.gc, stage_buf(wsb, p.max_tris, p.max_nodes, cur), gr.z,
-                                        gr.w, T.inv + 12 * v, ws, L.cnt);
-          if (lane == 0) {
-            if (hit) {
-              atomicMin(T.contact + v, ob);
-            } else if (atomicSub(T.rem + v, 1u) == 1u && v < vdone &&
-                       *((volatile int32_t*)T.contact + v) == kFree) {
-              atomicMin(T.minfree + e, v - e * W);
-            }
+      for (int u = 0; u < kU; ++u) {
+        const int it = it0 + u * kB + tid;
+        ov[u] = false;
+        vs[u] = 0;
+        obs[u] = 0;
+        if (it < items) {
+          const int v = it / nobj;
+          const int ob = it - v * nobj;
+          vs[u] = v;
+          obs[u] = ob;
+          if (T.sflag[v] == kSlotChecked &&
+              ((T.enw[(ob >> 5) * kB + v % (int)nt] >> (ob & 31)) & 1u)) {
+            ++L.cnt.broad;
+            const double2* bp =
+                reinterpret_cast<const double2*>(w.box + sb_box_off(w, ob, T.list[v % (int)nt]));
+            const double2 b0 = __ldcg(bp), b1 = __ldcg(bp + 1), b2 = __ldcg(bp + 2);
+            const double* cb = T.box + 6 * v;
+            ov[u] = cb[0] <= b1.y && b0.x <= cb[3] && cb[1] <= b2.x && b0.y <= cb[4] &&
+                    cb[2] <= b2.y && b1.x <= cb[5];
           }
         }
-        __syncwarp();
-        q = qn2;
-        v = v2;
-        ob = ob2;
-        gr = gr2;
-        cur ^= 1;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const uint32_t mask = __ballot_sync(kFull, ov[u]);
+        if (!mask) continue;
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(&F.qn, (uint32_t)__popc(mask));
+        base = __shfl_sync(kFull, base, 0);
+        if (ov[u]) {
+          atomicOr(T.ovm + (obs[u] >> 5) * kB + vs[u], 1u << (obs[u] & 31));
+          atomicAdd(T.rem + vs[u], 1u);
+          T.queue[base + __popc(mask & ((1u << lane) - 1u))] = ((uint32_t)vs[u] << 24) | (uint32_t)obs[u];
+        }
       }
       __syncthreads();
-      if (tid == 0) F.qn = 0;
+      // slots whose items are now all enumerated: free if no queued pair is pending
+      const bool last = it0 + kB * kU >= items;
+      const int vdone = last ? nslots : (it0 + kB * kU) / nobj;
+      const int vprev = it0 / nobj;
+      for (int v = vprev + tid; v < vdone; v += kB)
+        if (T.sflag[v] == kSlotChecked) {
+          T.sflag[v] = kSlotChecked | kSlotEnumerated;
+          if (T.rem[v] == 0u && T.contact[v] == kFree) atomicMin(T.minfree + v % (int)nt, v / (int)nt);
+        }
       __syncthreads();
+      const uint32_t qn = F.qn;
+      if (last || qn > kQD - kB * kU) {
+        if (p.dbg_inst && tid == 0) F.dq += qn;
+        narrow_drain(p, T, F, nt, qn, L);
+        __syncthreads();
+        if (tid == 0) F.qn = 0;
+        __syncthreads();
+      }
+    }
+    if (items == 0) __syncthreads();
+  } else {
+  // ---------------- A2 (broad phase) + B (narrow phase). The candidate objects of a slot are
+  // the OR of the occupancy-grid cells its box meets (only enabled objects are ever in a
+  // cell). Slots' candidates are expanded into a shared item list (block scan), then
+  // tested item-parallel against the world AABBs (aabb.hpp:29-33, collision.cpp:439-443),
+  // kCand items per chunk; the chunk's overlapping pairs go to the queue, which B drains.
+  uint32_t pend[kGW];
+  uint32_t cnt = 0;
+  {
+    const bool mine = tid < nslots && T.sflag[tid] == kSlotChecked;
+#pragma unroll
+    for (int wd = 0; wd < kGW; ++wd) pend[wd] = 0u;
+    if (mine) {
+      const SbCellGrid& G = p.grid;
+      int cx0, cx1, cy0, cy1;
+      cell_range(G, T.box + 6 * tid, T.box + 6 * tid + 3, cx0, cx1, cy0, cy1);
+      const uint32_t* cb = G.cells + (uint64_t)T.list[tid % (int)nt] * (uint64_t)(G.g * G.g) * words;
+      for (int cy = cy0; cy <= cy1; ++cy)
+        for (int cx = cx0; cx <= cx1; ++cx) {
+          const uint32_t* c = cb + (uint64_t)(cy * G.g + cx) * words;
+#pragma unroll
+          for (int wd = 0; wd < kGW; ++wd)
+            if (wd < words) pend[wd] |= __ldcg(c + wd);
+        }
+#pragma unroll
+      for (int wd = 0; wd < kGW; ++wd) cnt += __popc(pend[wd]);
     }
   }
-  if (items == 0) __syncthreads();
+  uint32_t off, ncand;
+  BlockScan(F.scan).ExclusiveSum(cnt, off, ncand);
+  __syncthreads();
+  for (uint32_t c0 = 0; c0 < ncand || c0 == 0; c0 += kCand) {
+    const uint32_t nitems = ncand - c0 < (uint32_t)kCand ? ncand - c0 : (uint32_t)kCand;
+    if (cnt && off < c0 + nitems && off + cnt > c0) {  // this slot's items in the chunk
+      uint32_t idx = off;
+#pragma unroll
+      for (int wd = 0; wd < kGW; ++wd) {
+        uint32_t m = pend[wd];
+        while (m) {
+          const int ob = 32 * wd + __ffs(m) - 1;
+          m &= m - 1u;
+          if (idx >= c0 && idx < c0 + nitems) T.cand[idx - c0] = ((uint32_t)tid << 24) | (uint32_t)ob;
+          ++idx;
+        }
+      }
+    }
+    if (tid == 0) F.qn = 0;
+    __syncthreads();
+    {  // item-parallel AABB tests, two box loads in flight per thread
+      constexpr int kI = kCand / kB;
+#pragma unroll 1
+      for (int u0 = 0; u0 < kI; u0 += 2) {
+        double2 bx[2][3];
+        uint32_t ent[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const uint32_t i = (u0 + u) * kB + tid;
+          ent[u] = i < nitems ? T.cand[i] : 0xffffffffu;
+          if (i < nitems) {
+            const int v = (int)(ent[u] >> 24), ob = (int)(ent[u] & 0xffffffu);
+            const double2* bp =
+                reinterpret_cast<const double2*>(w.box + sb_box_off(w, ob, T.list[v % (int)nt]));
+            bx[u][0] = __ldcg(bp);
+            bx[u][1] = __ldcg(bp + 1);
+            bx[u][2] = __ldcg(bp + 2);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          bool ov = false;
+          int v = 0, ob = 0;
+          if (ent[u] != 0xffffffffu) {
+            v = (int)(ent[u] >> 24);
+            ob = (int)(ent[u] & 0xffffffu);
+            ++L.cnt.broad;
+            const double* cb = T.box + 6 * v;
+            const double2 b0 = bx[u][0], b1 = bx[u][1], b2 = bx[u][2];
+            ov = cb[0] <= b1.y && b0.x <= cb[3] && cb[1] <= b2.x && b0.y <= cb[4] &&
+                 cb[2] <= b2.y && b1.x <= cb[5];
+          }
+          const uint32_t mask = __ballot_sync(kFull, ov);
+          if (!mask) continue;
+          uint32_t base = 0;
+          if (lane == 0) base = atomicAdd(&F.qn, (uint32_t)__popc(mask));
+          base = __shfl_sync(kFull, base, 0);
+          if (ov) {
+            atomicOr(T.ovm + (ob >> 5) * kB + v, 1u << (ob & 31));
+            atomicAdd(T.rem + v, 1u);
+            T.queue[base + __popc(mask & ((1u << lane) - 1u))] = ((uint32_t)v << 24) | (uint32_t)ob;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // slots whose candidates are now all enumerated: free if no queued pair is pending
+    if (tid < nslots && T.sflag[tid] == kSlotChecked && off + cnt <= c0 + nitems) {
+      T.sflag[tid] = kSlotChecked | kSlotEnumerated;
+      if (T.rem[tid] == 0u && T.contact[tid] == kFree)
+        atomicMin(T.minfree + tid % (int)nt, tid / (int)nt);
+    }
+    __syncthreads();
+    const uint32_t qn = F.qn;
+    if (p.dbg_inst && tid == 0) F.dq += qn;
+    if (qn > 0) {
+      narrow_drain(p, T, F, nt, qn, L);
+    }
+    __syncthreads();
+    if (ncand == 0) break;
+  }
+  }
   lap(p, F, 3);
   dbg_mark(p, F, F.tb);
 
@@ -379,10 +517,10 @@ __device__ uint32_t tile_round(const PlaceParams& p, const Sampling& S, const Sb
     int32_t last = a;  // last attempt this instance made in the sequential loop
     bool ok = false;
     for (int s = 0; s < W && !ok; ++s) {
-      const int v = e * W + s;
+      const int v = s * (int)nt + e;
       last = a + s;
       ++L.sampled;
-      if (T.sflag[v] != kSlotChecked) continue;  // placeable == 0 -> failed attempt
+      if (!(T.sflag[v] & kSlotChecked)) continue;  // placeable == 0 -> failed attempt
       ++L.checked;
       const int32_t c = T.contact[v];
       for (int wd = 0; wd < words; ++wd) {  // narrow tests up to the first hit
@@ -402,6 +540,7 @@ __device__ uint32_t tile_round(const PlaceParams& p, const Sampling& S, const Sb
 #pragma unroll
         for (int k = 0; k < 3; ++k) bp[k] = make_double2(T.box[6 * v + 2 * k], T.box[6 * v + 2 * k + 1]);
         w.enabled[sb_word_off(w, pl.object >> 5, inst)] |= 1u << (pl.object & 31);
+        if (kGrid) cell_insert(p.grid, inst, pl.object, T.box + 6 * v, T.box + 6 * v + 3);
         p.accepted[inst] = (int16_t)(a + s);
         ++L.accepted;
         ok = true;
@@ -475,6 +614,7 @@ __device__ __forceinline__ void store_list(const PlaceParams& p, const Tile& T, 
 }
 
 // One fast-path round over the CTA's tiles: survivors of round a -> counts of round a+1.
+template <bool kGrid>
 __device__ uint64_t fast_round(const PlaceParams& p, const Sampling& S, const SbGeom& gA,
                                Tile& T, Fixed& F, int32_t a, uint64_t draws, Local& L,
                                uint32_t* total_word) {
@@ -493,7 +633,7 @@ __device__ uint64_t fast_round(const PlaceParams& p, const Sampling& S, const Sb
     load_list(p, T, t, n);
     lap(p, F, 1);
     if (p.dbg && threadIdx.x == 0) F.t0 = global_ns();
-    const uint32_t ns = tile_round(p, S, gA, T, F, n, a, 1, draws + F.prefix[k], L);
+    const uint32_t ns = tile_round<kGrid>(p, S, gA, T, F, n, a, 1, draws + F.prefix[k], L);
     store_list(p, T, t, ns, cout);
     mine += ns;
     __syncthreads();
@@ -503,6 +643,7 @@ __device__ uint64_t fast_round(const PlaceParams& p, const Sampling& S, const Sb
 }
 
 // Per-instance path: tiles are independent; each is run to completion by one CTA.
+template <bool kGrid>
 __device__ void instance_tiles(const PlaceParams& p, const Sampling& S, const SbGeom& gA,
                                Tile& T, Fixed& F, Local& L) {
   for (;;) {
@@ -526,7 +667,7 @@ __device__ void instance_tiles(const PlaceParams& p, const Sampling& S, const Sb
         F.t0 = global_ns();
       }
       const unsigned nslots_dbg = nt * W;
-      nt = tile_round(p, S, gA, T, F, nt, a, W, 0, L);
+      nt = tile_round<kGrid>(p, S, gA, T, F, nt, a, W, 0, L);
       a += W;
       if (p.dbg_inst && threadIdx.x == 0) {  // A1 / A2+B / C sums (us) and A2+B max (ns)
         atomicAdd(p.dbg_inst + 5, (unsigned)(F.ta / 1000));
@@ -534,6 +675,10 @@ __device__ void instance_tiles(const PlaceParams& p, const Sampling& S, const Sb
         atomicAdd(p.dbg_inst + 7, (unsigned)((global_ns() - F.t0) / 1000));
         atomicMax(p.dbg_inst + 8, (unsigned)F.tb);
         atomicAdd(p.dbg_inst + 9, nslots_dbg);
+        atomicAdd(p.dbg_inst + 10, F.dq);
+        atomicAdd(p.dbg_inst + 11, F.dt);
+        atomicMax(p.dbg_inst + 12, F.dq);
+        atomicMax(p.dbg_inst + 13, F.dt);
       }
     }
     mark_invalid(p, T, nt);
@@ -558,6 +703,7 @@ __device__ __forceinline__ void block_setup(const PlaceParams& p, Fixed& F, Tile
 
 extern __shared__ __align__(16) unsigned char g_dsm[];
 
+template <bool kGrid>
 __global__ void __launch_bounds__(kB, 2) k_place(PlaceParams p) {
   __shared__ Fixed F;
   Tile T = carve(g_dsm, p.w.n_words, p.ws_bytes);
@@ -574,7 +720,7 @@ __global__ void __launch_bounds__(kB, 2) k_place(PlaceParams p) {
     if (p.vary_flag && blockIdx.x == 0 && threadIdx.x == 0)
       atomicAdd(p.counters + 7, 1ull);  // per-instance placement
     const unsigned long long t6 = timer ? global_ns() : 0;
-    instance_tiles(p, S, gA, T, F, L);
+    instance_tiles<kGrid>(p, S, gA, T, F, L);
     if (timer) F.acc[6] += global_ns() - t6;
   } else {
     cg::grid_group grid = cg::this_grid();
@@ -594,13 +740,15 @@ __global__ void __launch_bounds__(kB, 2) k_place(PlaceParams p) {
         r0 = global_ns();
         F.ta = F.tb = 0;
       }
-      const uint64_t total = fast_round(p, S, gA, T, F, a, draws, L, nullptr);
+      const uint64_t total = fast_round<kGrid>(p, S, gA, T, F, a, draws, L, nullptr);
       if (total == 0) break;
       draws += total;
       if (p.dbg && threadIdx.x == 0) {  // per-round maxima over CTAs: work, A1, A2+B
         atomicMax(p.dbg + 3 * a, (unsigned)(global_ns() - r0));
         atomicMax(p.dbg + 3 * a + 1, (unsigned)F.ta);
         atomicMax(p.dbg + 3 * a + 2, (unsigned)F.tb);
+        atomicAdd(p.dbg_inst + 14, (unsigned)((global_ns() - r0) / 1000));  // sum of work (us)
+        atomicAdd(p.dbg_inst + 15, (unsigned)(F.tb / 1000));                // sum of A2+B (us)
       }
       lap(p, F, 1);
       grid.sync();
@@ -624,6 +772,7 @@ __global__ void __launch_bounds__(kB, 2) k_place(PlaceParams p) {
 }
 
 // Sharded building blocks (no grid barrier inside a launch).
+template <bool kGrid>
 __global__ void __launch_bounds__(kB, 2) k_place_instances(PlaceParams p) {
   __shared__ Fixed F;
   Tile T = carve(g_dsm, p.w.n_words, p.ws_bytes);
@@ -631,7 +780,7 @@ __global__ void __launch_bounds__(kB, 2) k_place_instances(PlaceParams p) {
   block_setup(p, F, T, gA);
   Local L;
   Sampling S{0, nullptr, nullptr, 0};
-  instance_tiles(p, S, gA, T, F, L);
+  instance_tiles<kGrid>(p, S, gA, T, F, L);
   flush(p, L);
 }
 
@@ -648,6 +797,7 @@ __global__ void __launch_bounds__(kB, 2) k_fast_init(PlaceParams p) {
   if (threadIdx.x == 0 && mine) atomicAdd(p.ctrl + place_total_word(0), mine);
 }
 
+template <bool kGrid>
 __global__ void __launch_bounds__(kB, 2) k_fast_round(PlaceParams p, int32_t a) {
   __shared__ Fixed F;
   Tile T = carve(g_dsm, p.w.n_words, p.ws_bytes);
@@ -655,7 +805,7 @@ __global__ void __launch_bounds__(kB, 2) k_fast_round(PlaceParams p, int32_t a) 
   block_setup(p, F, T, gA);
   Local L;
   Sampling S{1, p.canon_tris, p.canon_cum, p.canon_n};
-  fast_round(p, S, gA, T, F, a, p.draw_base, L, p.ctrl + place_total_word(a + 1));
+  fast_round<kGrid>(p, S, gA, T, F, a, p.draw_base, L, p.ctrl + place_total_word(a + 1));
   flush(p, L);
 }
 
@@ -694,9 +844,12 @@ void narrow_profile(unsigned long long out[8], bool reset) {
 }
 
 int place_grid(int num_sms, size_t smem) {
-  set_smem((const void*)k_place, smem);
-  int per = 0;
-  check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_place, kB, smem), "occupancy");
+  set_smem((const void*)k_place<false>, smem);
+  set_smem((const void*)k_place<true>, smem);
+  int per = 0, per2 = 0;
+  check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_place<false>, kB, smem), "occupancy");
+  check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, k_place<true>, kB, smem), "occupancy");
+  if (per2 < per) per = per2;
   return per * num_sms;
 }
 
@@ -704,15 +857,21 @@ bool place_persistent(const PlaceParams& p, unsigned grid, size_t smem, sb_strea
   if (grid == 0) return false;
   PlaceParams q = p;
   void* args[] = {&q};
-  check(cudaLaunchCooperativeKernel((void*)k_place, dim3(grid), dim3(kB), args, smem,
+  const void* fn = p.grid.g ? (const void*)k_place<true> : (const void*)k_place<false>;
+  check(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kB), args, smem,
                                     reinterpret_cast<cudaStream_t>(s)),
         "cudaLaunchCooperativeKernel(k_place)");
   return true;
 }
 
 void place_instances(const PlaceParams& p, unsigned grid, size_t smem, sb_stream_t s) {
-  set_smem((const void*)k_place_instances, smem);
-  k_place_instances<<<grid, kB, smem, s>>>(p);
+  if (p.grid.g) {
+    set_smem((const void*)k_place_instances<true>, smem);
+    k_place_instances<true><<<grid, kB, smem, s>>>(p);
+  } else {
+    set_smem((const void*)k_place_instances<false>, smem);
+    k_place_instances<false><<<grid, kB, smem, s>>>(p);
+  }
   check(cudaGetLastError(), "k_place_instances");
 }
 
@@ -724,8 +883,13 @@ void place_fast_init(const PlaceParams& p, unsigned grid, size_t smem, sb_stream
 
 void place_fast_round(const PlaceParams& p, int32_t attempt, unsigned grid, size_t smem,
                       sb_stream_t s) {
-  set_smem((const void*)k_fast_round, smem);
-  k_fast_round<<<grid, kB, smem, s>>>(p, attempt);
+  if (p.grid.g) {
+    set_smem((const void*)k_fast_round<true>, smem);
+    k_fast_round<true><<<grid, kB, smem, s>>>(p, attempt);
+  } else {
+    set_smem((const void*)k_fast_round<false>, smem);
+    k_fast_round<false><<<grid, kB, smem, s>>>(p, attempt);
+  }
   check(cudaGetLastError(), "k_fast_round");
 }
 

@@ -455,6 +455,8 @@ struct sb_engine {
   DevArray<uint32_t> d_tile_list;   // [ntiles * tile_inst] survivors per tile
   DevArray<uint32_t> d_tile_cnt;    // [2][ntiles]
   DevArray<double> d_cpose;         // [grid][kPlaceBlock][12] candidate poses
+  DevArray<uint32_t> d_cells;       // broad-phase occupancy grid [n][g * g][words]
+  SbCellGrid cell_grid{};
   DevArray<uint32_t> d_ctrl;
   DevArray<uint64_t> d_prof;
   DevArray<unsigned> d_dbg;        // SB_ROUND_DEBUG=1: per-round CTA maxima (fast path)
@@ -661,6 +663,52 @@ struct sb_engine {
     d_tile_list.alloc(static_cast<size_t>(ntiles) * tile_inst);
     d_tile_cnt.alloc(2 * static_cast<size_t>(ntiles));
     d_cpose.alloc(static_cast<size_t>(grid) * sbk::kPlaceBlock * 12);
+    {  // occupancy grid over the supports' XY extent, widened by the largest object radius
+      double bx0 = HUGE_VAL, by0 = HUGE_VAL, bx1 = -HUGE_VAL, by1 = -HUGE_VAL, rad = 0.0;
+      for (uint32_t k = 0; k < sc->n_supports; ++k) {
+        const sb_support& su = sc->supports[k];
+        const double xs[2] = {su.rect[0], su.rect[2]}, ys[2] = {su.rect[1], su.rect[3]};
+        for (double x : xs)
+          for (double y : ys) {
+            const double wx = su.pose[0] * x + su.pose[4] * y + su.pose[12];
+            const double wy = su.pose[1] * x + su.pose[5] * y + su.pose[13];
+            bx0 = std::min(bx0, wx);
+            bx1 = std::max(bx1, wx);
+            by0 = std::min(by0, wy);
+            by1 = std::max(by1, wy);
+          }
+      }
+      for (const Placement& pl : places) {  // candidates only: fixed objects just clamp
+        const SbGeom& g = world->geom_at(pl.dev.geom).g;
+        const double ex = std::max(std::fabs(g.box_min[0]), std::fabs(g.box_max[0]));
+        const double ey = std::max(std::fabs(g.box_min[1]), std::fabs(g.box_max[1]));
+        rad = std::max(rad, std::sqrt(ex * ex + ey * ey));
+      }
+      const int words = world->view().n_words;
+      if (words > 8) throw std::invalid_argument("engine: more than 256 objects per scene");
+      // Few objects: the broad phase reads every enabled object's box (one round trip);
+      // many: the grid narrows the candidates first (SB_CELL_GRID=0/1 forces either).
+      int g = world->view().n_objects > 32 ? 16 : 0;
+      if (const char* e = std::getenv("SB_CELL_GRID")) g = std::atoi(e) ? 16 : 0;
+      while (g > 1 && static_cast<double>(n) * g * g * words * 4.0 > 8.0e9) g /= 2;
+      if (g == 1) g = 0;
+      if (!(bx0 <= bx1) || !(by0 <= by1)) {
+        bx0 = by0 = -1.0;
+        bx1 = by1 = 1.0;
+      }
+      bx0 -= rad;
+      by0 -= rad;
+      bx1 += rad;
+      by1 += rad;
+      cell_grid.x0 = bx0;
+      cell_grid.y0 = by0;
+      cell_grid.inv_x = g / std::max(bx1 - bx0, 1e-9);
+      cell_grid.inv_y = g / std::max(by1 - by0, 1e-9);
+      cell_grid.g = g;
+      cell_grid.words = words;
+      if (g) d_cells.alloc(static_cast<size_t>(n) * g * g * words);
+      cell_grid.cells = d_cells.p;
+    }
     d_ctrl.alloc(8 * std::max<size_t>(1, places.size()));
     d_rflags.alloc(2 * std::max<size_t>(1, places.size()));
     d_prof.alloc(8);
@@ -778,7 +826,11 @@ struct sb_engine {
     cuda_check(cudaMemsetAsync(d_rflags.p, 0, d_rflags.count * sizeof(int32_t), stream), "memset");
     sbk::engine_reset(wv, first_place_obj, static_cast<int32_t>(P), d_valid.p, d_accepted.p,
                       static_cast<int32_t>(P), s);
-    ++launches;
+    launches += 1;
+    if (cell_grid.g) {
+      sbk::cells_reset(wv, cell_grid, first_place_obj, s);
+      ++launches;
+    }
     for (size_t p = 0; p < P; ++p) {
       Placement& pl = places[p];
       bool fast = true;
@@ -826,6 +878,7 @@ struct sb_engine {
       pp.tile_list = d_tile_list.p;
       pp.tile_cnt = d_tile_cnt.p;
       pp.cpose = d_cpose.p;
+      pp.grid = cell_grid;
       pp.cnt_stride = ntiles;
       pp.ntiles = ntiles;
       pp.tile_inst = tile_inst;
@@ -948,10 +1001,15 @@ struct sb_engine {
       for (size_t i = 0; i + 16 < dbg.size(); ++i) last_prof[12 + i % 3] += dbg[i] * 1e-6;
       const unsigned* di = dbg.data() + dbg.size() - 16;
       std::fprintf(stderr, "[round debug] per-instance tiles: %u, max %.1f us, mean %.1f us, max rounds %u, mean rounds %.2f; "
-                   "per tile-round: A1 %.1f us, A2+B %.1f us, total %.1f us, max A2+B %.1f us, slots %.1f\n",
+                   "per tile-round: A1 %.1f us, A2+B %.1f us, C %.1f us, max A2+B %.1f us, slots %.1f, "
+                   "pairs queued %.1f (max %u) tested %.1f (max %u)\n",
                    di[4], di[0] * 1e-3, di[4] ? double(di[1]) / di[4] : 0.0, di[2], di[4] ? double(di[3]) / di[4] : 0.0,
                    di[3] ? double(di[5]) / di[3] : 0.0, di[3] ? double(di[6]) / di[3] : 0.0,
-                   di[3] ? double(di[7]) / di[3] : 0.0, di[8] * 1e-3, di[3] ? double(di[9]) / di[3] : 0.0);
+                   di[3] ? double(di[7]) / di[3] : 0.0, di[8] * 1e-3, di[3] ? double(di[9]) / di[3] : 0.0,
+                   di[3] ? double(di[10]) / di[3] : 0.0, di[12], di[3] ? double(di[11]) / di[3] : 0.0, di[13]);
+      std::fprintf(stderr, "[round debug] fast path: sum over rounds of max CTA work %.3f ms (A1 %.3f, A2+B %.3f); "
+                   "mean CTA work %.3f ms, mean A2+B %.3f ms (grid %u)\n", last_prof[12], last_prof[13], last_prof[14],
+                   di[14] * 1e-3 / grid, di[15] * 1e-3 / grid, grid);
     }
     last_prof[8] = regions_ms;
     last_prof[9] = total_ms;
