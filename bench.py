@@ -127,10 +127,6 @@ FLOPS = {
     "nodes": 36,      # transform_aabb of the B node box (30) + 6 overlap comparisons
     "pairs": 46,      # first-plane test of tri_tri_intersect (the cost every pair pays)
 }
-# Algorithmic HBM bytes (results resident): per checked candidate the active id (4) +
-# fail flag (1) + enable word (4); per broad-phase object the world box (48); per narrow
-# pair the placed pose (96); per accepted candidate pose + box + enable + accepted (150).
-BYTES = {"checked": 9, "broad": 48, "narrow": 96, "accepted": 150}
 
 
 def run_ours(args, rank, world, local_rank):
@@ -226,7 +222,12 @@ def run_ours(args, rank, world, local_rank):
     ms_step = time_ms / K
     value = valid_sum / (ms_step * 1e-3)
 
-    # roofline of the dominant kernel (the fused round kernel k_round)
+    # Roofline of the dominant kernel, k_place (one cooperative launch per placement: every
+    # attempt round's sample + compose + broad + narrow + accept). Algorithmic units are
+    # SURVEY.md 8(d)'s: bytes = every placed object's pose (96 B) + world box (48 B) + enable
+    # bit (1 B) read once per (instance, placement) + 150 B written per accepted candidate;
+    # FP64 ops from the kernel's own work counters (FLOPS above). The binding roofline
+    # (larger time at peak) is reported as `roofline`, the other as `roofline_secondary`.
     per = {k: agg.get(v, 0) / K for k, v in (("checked", "candidate_checks"),
                                               ("broad", "broad_phase_tests"),
                                               ("narrow", "narrow_phase_tests"),
@@ -234,15 +235,37 @@ def run_ours(args, rank, world, local_rank):
                                               ("pairs", "triangle_pair_tests"),
                                               ("accepted", "accepted_candidates"))}
     flops = sum(FLOPS[k] * per[k] for k in FLOPS)
-    bytes_ = sum(BYTES[k] * per[k] for k in BYTES)
+    n_fixed = len(scene.fixed)
+    bytes_ = n_per * sum((n_fixed + k) * 145 for k in range(P)) + 150 * per["accepted"]
     k_ms = sum(check_ms) / K
     n_launch = sum(check_launches) / K
     peaks = fp64_peak(device)
     fp64_peak_tf = peaks["dadd"] / 1e3  # no-FMA build: one flop per FP64 instruction
-    measured = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
+    mp_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    measured = json.load(open(mp_path)) if os.path.exists(mp_path) else None
+    hbm_peak = measured["hbm_gbs"] if measured else 6650.0
+    hbm_src = "of measured (MEASURED_PEAKS.json hbm_gbs)" if measured else "of fallback (B200_PROFILING.md)"
     achieved_tf = flops / (k_ms * 1e-3) / 1e12 if k_ms > 0 else 0.0
     achieved_gbs = bytes_ / (k_ms * 1e-3) / 1e9 if k_ms > 0 else 0.0
+    traffic = None  # dram__bytes_read.sum + dram__bytes_write.sum per launch, ncu --set full
+    prof_json = os.path.join(ROOT, "profiles", f"ncu_k_place_{args.config}.json")
+    if os.path.exists(prof_json):
+        traffic = json.load(open(prof_json)).get("dram_bytes_per_launch")
+    hbm = {"bound": "hbm", "achieved": round(achieved_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+           "frac": round(achieved_gbs / hbm_peak, 5), "traffic": traffic,
+           "peak_source": hbm_src, "algorithmic_bytes_per_launch": round(bytes_ / max(n_launch, 1)),
+           "traffic_source": f"profiles/ncu_k_place_{args.config}.json" if traffic else None}
+    fp64 = {"bound": "fp64", "achieved": round(achieved_tf, 3), "peak": round(fp64_peak_tf, 3),
+            "unit": "TFLOP/s", "frac": round(achieved_tf / fp64_peak_tf, 5) if fp64_peak_tf > 0 else None,
+            "peak_source": "measured in this run: DADD rate, tools/fp64_peak.cu (no-FMA build)",
+            "algorithmic_flops_per_launch": round(flops / max(n_launch, 1))}
+    t_hbm = bytes_ / (hbm_peak * 1e9)
+    t_fp64 = flops / (fp64_peak_tf * 1e12) if fp64_peak_tf > 0 else 0.0
+    primary, secondary = (hbm, fp64) if t_hbm >= t_fp64 else (fp64, hbm)
+    for r in (primary, secondary):
+        r.update({"kernel": "k_place (persistent per placement: sample+compose+broad+narrow+accept)",
+                  "kernel_ms_per_step": round(k_ms, 4), "launches_per_step": n_launch,
+                  "share_of_step": round(k_ms / ms_step, 4)})
     line = {
         "metric": METRIC,
         "value": round(value, 1),
@@ -259,18 +282,8 @@ def run_ours(args, rank, world, local_rank):
                    "l2": "flushed (256 MiB write) between timed steps",
                    "valid_fraction": round(valid_sum / n_total, 4)},
         "cold_start_s": round(cold_s, 3),
-        "roofline": {"bound": "fp64", "achieved": round(achieved_tf, 3),
-                     "peak": round(fp64_peak_tf, 3), "unit": "TFLOP/s",
-                     "frac": round(achieved_tf / fp64_peak_tf, 4) if fp64_peak_tf > 0 else None,
-                     "traffic": None, "kernel": "k_round (fused sample+compose+check+accept)",
-                     "kernel_ms_per_step": round(k_ms, 4), "launches_per_step": n_launch,
-                     "peak_source": "measured DADD rate, tools/fp64_peak.cu, this run",
-                     "algorithmic_flops_per_step": round(flops),
-                     "share_of_step": round(k_ms / ms_step, 4)},
-        "roofline_hbm": {"bound": "hbm", "achieved": round(achieved_gbs, 1),
-                         "peak": measured.get("hbm_gbs"), "unit": "GB/s",
-                         "frac": round(achieved_gbs / measured.get("hbm_gbs", 6650.0), 5),
-                         "algorithmic_bytes_per_step": round(bytes_)},
+        "roofline": primary,
+        "roofline_secondary": secondary,
         "fp64_peaks_gflops": {k: round(v, 1) for k, v in peaks.items()},
         "work_per_step": {k: round(v) for k, v in per.items()},
         "e2e": {"value": round(valid_sum / (e2e * 1e-3), 1), "unit": "collision-free scenes/s",
