@@ -103,8 +103,10 @@ typedef struct sb_stats {          /* CollisionStats, collision.hpp:65-72 */
   uint64_t triangle_pair_tests;
 } sb_stats;
 
-/* CollisionWorld(batch_size, margin): collision.cpp:334-337. margin must be 0 (the only
- * value the reference's configs use; margin > 0 = tri_tri_distance path, not built yet). */
+/* CollisionWorld(batch_size, margin): collision.cpp:334-337. Any finite margin: box tests
+ * use Aabb3::overlaps(., margin) and, for margin > 0, a triangle pair collides when
+ * tri_tri_distance < margin (collision.cpp:136-212,312-313). The generation engine uses the
+ * reference driver's margin 0 (Appendix C.7). */
 sb_status sb_world_create(uint64_t batch_size, double margin, int device, sb_world** out);
 void sb_world_destroy(sb_world* w);
 /* register_geometry: collision.cpp:339-355 (fingerprint dedupe, drop_degenerate, MeshBvh). */

@@ -310,6 +310,103 @@ __device__ __forceinline__ bool tri_tri_intersect(const double* p, const double*
   return tri_tri_finish(p, q, P1.n, P2.n, dp0, dp1, dp2, dq0, dq1, dq2);
 }
 
+// ------------------------------------------------ triangle distance (margin > 0)
+// collision.cpp:136-212 with the shim's vector arithmetic (dot = ((x x' + y y') + z z'),
+// element-wise +, -, scalar *). Only used when the world's margin is > 0.
+struct V3 {
+  double x, y, z;
+};
+__device__ __forceinline__ V3 v3(const double* p) { return {p[0], p[1], p[2]}; }
+__device__ __forceinline__ V3 vsub(V3 a, V3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ V3 vadd(V3 a, V3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+__device__ __forceinline__ V3 vmul(V3 a, double s) { return {a.x * s, a.y * s, a.z * s}; }
+__device__ __forceinline__ double vdot(V3 a, V3 b) { return (a.x * b.x + a.y * b.y) + a.z * b.z; }
+__device__ __forceinline__ double vnorm(V3 a) { return sqrt(vdot(a, a)); }
+__device__ __forceinline__ double clamp01(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
+
+static __device__ __noinline__ double seg_seg_distance(V3 p0, V3 p1, V3 q0, V3 q1) {
+  const V3 d1 = vsub(p1, p0), d2 = vsub(q1, q0), r = vsub(p0, q0);
+  const double a = vdot(d1, d1), e = vdot(d2, d2), f = vdot(d2, r);
+  double s, t;
+  if (a <= kEps && e <= kEps) return vnorm(r);
+  if (a <= kEps) {
+    s = 0.0;
+    t = clamp01(f / e);
+  } else {
+    const double c = vdot(d1, r);
+    if (e <= kEps) {
+      t = 0.0;
+      s = clamp01(-c / a);
+    } else {
+      const double b = vdot(d1, d2);
+      const double denom = a * e - b * b;
+      s = denom > kEps ? clamp01((b * f - c * e) / denom) : 0.0;
+      t = (b * s + f) / e;
+      if (t < 0.0) {
+        t = 0.0;
+        s = clamp01(-c / a);
+      } else if (t > 1.0) {
+        t = 1.0;
+        s = clamp01((b - c) / a);
+      }
+    }
+  }
+  return vnorm(vsub(vadd(p0, vmul(d1, s)), vadd(q0, vmul(d2, t))));
+}
+
+static __device__ __noinline__ double point_tri_distance(V3 p, V3 a, V3 b, V3 c) {
+  const V3 ab = vsub(b, a), ac = vsub(c, a), ap = vsub(p, a);
+  const double d1 = vdot(ab, ap), d2 = vdot(ac, ap);
+  if (d1 <= 0 && d2 <= 0) return vnorm(ap);
+  const V3 bp = vsub(p, b);
+  const double d3 = vdot(ab, bp), d4 = vdot(ac, bp);
+  if (d3 >= 0 && d4 <= d3) return vnorm(bp);
+  const double vc = d1 * d4 - d3 * d2;
+  if (vc <= 0 && d1 >= 0 && d3 <= 0) {
+    const double v = d1 / (d1 - d3);
+    return vnorm(vsub(p, vadd(a, vmul(ab, v))));
+  }
+  const V3 cp = vsub(p, c);
+  const double d5 = vdot(ab, cp), d6 = vdot(ac, cp);
+  if (d6 >= 0 && d5 <= d6) return vnorm(cp);
+  const double vb = d5 * d2 - d1 * d6;
+  if (vb <= 0 && d2 >= 0 && d6 <= 0) {
+    const double w = d2 / (d2 - d6);
+    return vnorm(vsub(p, vadd(a, vmul(ac, w))));
+  }
+  const double va = d3 * d6 - d5 * d4;
+  if (va <= 0 && (d4 - d3) >= 0 && (d5 - d6) >= 0) {
+    const double w = (d4 - d3) / ((d4 - d3) + (d5 - d6));
+    return vnorm(vsub(p, vadd(b, vmul(vsub(c, b), w))));
+  }
+  const double denom = 1.0 / (va + vb + vc);
+  const double v = vb * denom, w = vc * denom;
+  return vnorm(vsub(p, vadd(vadd(a, vmul(ab, v)), vmul(ac, w))));
+}
+
+// tri_tri_distance (collision.cpp:198-212); p, q: 9 doubles each.
+static __device__ __noinline__ double tri_tri_distance(const double* p, const double* q) {
+  if (tri_tri_intersect(p, q)) return 0.0;
+  const V3 pa[3] = {v3(p), v3(p + 3), v3(p + 6)};
+  const V3 qa[3] = {v3(q), v3(q + 3), v3(q + 6)};
+  double best = __longlong_as_double(0x7ff0000000000000LL);
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      best = dmin(best, seg_seg_distance(pa[i], pa[(i + 1) % 3], qa[j], qa[(j + 1) % 3]));
+  for (int i = 0; i < 3; ++i) {
+    best = dmin(best, point_tri_distance(pa[i], qa[0], qa[1], qa[2]));
+    best = dmin(best, point_tri_distance(qa[i], pa[0], pa[1], pa[2]));
+  }
+  return best;
+}
+
+// Aabb3::overlaps with margin (aabb.hpp:29-33): a.min <= b.max + m && b.min <= a.max + m.
+__device__ __forceinline__ bool overlaps_m(const double amn[3], const double amx[3],
+                                           const double bmn[3], const double bmx[3], double m) {
+  return amn[0] <= bmx[0] + m && bmn[0] <= amx[0] + m && amn[1] <= bmx[1] + m &&
+         bmn[1] <= amx[1] + m && amn[2] <= bmx[2] + m && bmn[2] <= amx[2] + m;
+}
+
 // ---------------------------------------------------------- BVH-vs-BVH collide
 // MeshBvh::collide (collision.cpp:285-329) over the effective DAGs of A (candidate, frame
 // of reference) and B (placed object, posed by M = other_in_self). Each node pair is

@@ -61,6 +61,7 @@ struct SbWorldView {
   int32_t n_words;           // enable-bit words in use = ceil(n_objects / 32)
   int32_t obj_stride;        // object capacity per instance (record stride)
   int32_t word_stride;       // enable-word capacity per instance
+  double margin;             // CollisionWorld margin (collision.hpp:78)
   const int32_t* obj_geom;   // [n_objects]
   double* pose;              // [n][obj_stride][12]  row-major 3x4 [R | t]
   double* box;               // [n][obj_stride][6]   world AABB min xyz, max xyz

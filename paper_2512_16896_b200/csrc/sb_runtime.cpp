@@ -160,10 +160,10 @@ struct sb_world {
   DevArray<int32_t> d_contact;
   DevArray<unsigned long long> d_counters;
 
-  sb_world(uint64_t batch, double margin, int dev) : n(batch), device(dev) {
+  double margin = 0.0;
+  sb_world(uint64_t batch, double margin_, int dev) : n(batch), device(dev), margin(margin_) {
     if (batch == 0) throw std::invalid_argument("CollisionWorld: batch_size must be >= 1");
-    if (margin != 0.0)
-      throw std::invalid_argument("CollisionWorld: margin > 0 (tri_tri_distance path) is not built");
+    if (!std::isfinite(margin)) throw std::invalid_argument("CollisionWorld: margin must be finite");
     if (batch > 0xffffffffull) throw std::invalid_argument("CollisionWorld: batch_size > 2^32-1");
     current_device_checked(dev);
     cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -187,6 +187,7 @@ struct sb_world {
     v.n_words = (v.n_objects + 31) / 32;
     v.obj_stride = cap_objects;
     v.word_stride = cap_words;
+    v.margin = margin;
     v.obj_geom = d_obj_geom.p;
     v.pose = d_pose.p;
     v.box = d_box.p;

@@ -216,9 +216,13 @@ __device__ __forceinline__ int warp_append(bool pass, uint16_t value, uint16_t* 
 //     reference traversal reaches; hit = some reached leaf pair holds an intersecting pair.
 // `stage` = the pair's staged pose + geometry record (warp_stage, copies complete and
 // visible to the warp), nB / nTB = that geometry's node / triangle counts.
+// `margin` = the world's margin (collision.hpp:78): box tests use Aabb3::overlaps(., margin)
+// and, when margin > 0, a triangle pair counts when tri_tri_distance < margin
+// (collision.cpp:312-313) instead of the staged intersection filters.
 __device__ __forceinline__ bool warp_collide(const GeomCache& gc, const unsigned char* stage,
                                              int nB, int nTB, const double* I,
-                                             const WarpScratchView& ws, CheckCounters& cnt) {
+                                             const WarpScratchView& ws, CheckCounters& cnt,
+                                             double mg = 0.0) {
   const int lane = threadIdx.x & 31;
   SB_NP_MARK(np0);
   const double* P = reinterpret_cast<const double*>(stage);
@@ -283,8 +287,9 @@ __device__ __forceinline__ bool warp_collide(const GeomCache& gc, const unsigned
       if (k < nlp) {
         const int a = gc.leaves[k / nLB], b = ws.leafb[k - (k / nLB) * nLB];
         const double* bb = ws.bb + 6 * b;
-        ov = gc.bmin[a][0] <= bb[3] && bb[0] <= gc.bmax[a][0] && gc.bmin[a][1] <= bb[4] &&
-             bb[1] <= gc.bmax[a][1] && gc.bmin[a][2] <= bb[5] && bb[2] <= gc.bmax[a][2];
+        ov = gc.bmin[a][0] <= bb[3] + mg && bb[0] <= gc.bmax[a][0] + mg &&
+             gc.bmin[a][1] <= bb[4] + mg && bb[1] <= gc.bmax[a][1] + mg &&
+             gc.bmin[a][2] <= bb[5] + mg && bb[2] <= gc.bmax[a][2] + mg;
       }
       if (__any_sync(kFull, ov)) {
         const uint32_t m = __ballot_sync(kFull, ov);
@@ -319,6 +324,22 @@ __device__ __forceinline__ bool warp_collide(const GeomCache& gc, const unsigned
   const int ntp = nTA * nTB;
   __syncwarp();
 
+  bool any = false;
+  if (mg > 0.0) {  // 4': tri_tri_distance < margin over the candidate leaf pairs' triangles
+    for (int k0 = 0; k0 < ntp; k0 += 32) {
+      const int k = k0 + lane;
+      bool hit = false;
+      if (k < ntp) {
+        const int ia = k / nTB, ib = k - ia * nTB;
+        if ((ws.allowed[gc.tleaf[ia]] >> ws.tleafb[ib]) & 1u) {
+          ++cnt.pairs;
+          hit = tri_tri_distance(gc.ta[ia], ws.qb + 9 * ib) < mg;
+        }
+      }
+      if (hit) atomicOr(ws.H + gc.tleaf[k / nTB], 1u << ws.tleafb[k - (k / nTB) * nTB]);
+      any = __any_sync(kFull, hit) || any;
+    }
+  } else {
   // 4: staged tri_tri_intersect over the triangle pairs k = ia * nTB + ib of candidate
   // leaf pairs: filter 1 (B's plane vs A's vertices), filter 2 (A's plane vs B's
   // vertices), then the interval / coplanar rest.
@@ -356,7 +377,6 @@ __device__ __forceinline__ bool warp_collide(const GeomCache& gc, const unsigned
     n2 = warp_append(pass, (uint16_t)k, ws.l2, n2);
   }
   __syncwarp();
-  bool any = false;
   for (int j0 = 0; j0 < n2; j0 += 32) {
     const int j = j0 + lane;
     bool hit = false;
@@ -374,6 +394,7 @@ __device__ __forceinline__ bool warp_collide(const GeomCache& gc, const unsigned
     if (hit) atomicOr(ws.H + gc.tleaf[k / nTB], 1u << ws.tleafb[k - (k / nTB) * nTB]);
     any = __any_sync(kFull, hit) || any;
   }
+  }  // margin == 0
   SB_NP_MARK(np2);
   SB_NP_ADD(7, np1b, np2);
   if (!any) return false;
@@ -419,9 +440,9 @@ __device__ __forceinline__ bool warp_collide(const GeomCache& gc, const unsigned
         if ((ws.allowed[a] >> b) & 1u) {
           const double* bb = ws.bb + 6 * b;
           ++cnt.nodes;
-          all = all && gc.bmin[a][0] <= bb[3] && bb[0] <= gc.bmax[a][0] &&
-                gc.bmin[a][1] <= bb[4] && bb[1] <= gc.bmax[a][1] && gc.bmin[a][2] <= bb[5] &&
-                bb[2] <= gc.bmax[a][2];
+          all = all && gc.bmin[a][0] <= bb[3] + mg && bb[0] <= gc.bmax[a][0] + mg &&
+                gc.bmin[a][1] <= bb[4] + mg && bb[1] <= gc.bmax[a][1] + mg &&
+                gc.bmin[a][2] <= bb[5] + mg && bb[2] <= gc.bmax[a][2] + mg;
         }
       }
     }
@@ -450,8 +471,9 @@ __device__ __forceinline__ bool warp_collide(const GeomCache& gc, const unsigned
           const int a = e >> 5, b = e & 31;
           ++cnt.nodes;
           const double* bb = ws.bb + 6 * b;
-          if (gc.bmin[a][0] <= bb[3] && bb[0] <= gc.bmax[a][0] && gc.bmin[a][1] <= bb[4] &&
-              bb[1] <= gc.bmax[a][1] && gc.bmin[a][2] <= bb[5] && bb[2] <= gc.bmax[a][2]) {
+          if (gc.bmin[a][0] <= bb[3] + mg && bb[0] <= gc.bmax[a][0] + mg &&
+              gc.bmin[a][1] <= bb[4] + mg && bb[1] <= gc.bmax[a][1] + mg &&
+              gc.bmin[a][2] <= bb[5] + mg && bb[2] <= gc.bmax[a][2] + mg) {
             const bool la = (gc.leafmask >> a) & 1u, lb = (leafB >> b) & 1u;
             if (la && lb) {
               hit = (ws.H[a] >> b) & 1u;
@@ -525,7 +547,7 @@ __device__ __forceinline__ int warp_check(const WorldView& w, const SbGeom& gA,
             reinterpret_cast<const double2*>(w.box + sb_box_off(w, ob0 + b, inst));
         double2 b0 = bp[0], b1 = bp[1], b2 = bp[2];
         double omn[3] = {b0.x, b0.y, b1.x}, omx[3] = {b1.y, b2.x, b2.y};
-        if (overlaps(cmn, cmx, omn, omx)) ovm |= 1u << b;
+        if (overlaps_m(cmn, cmx, omn, omx, w.margin)) ovm |= 1u << b;
       }
     }
     for (;;) {
@@ -542,7 +564,7 @@ __device__ __forceinline__ int warp_check(const WorldView& w, const SbGeom& gA,
         warp_stage(w, gr, ob, instL, st);
         cp_async_wait<0>();
         __syncwarp();
-        const bool hit = warp_collide(gc, st, gr.z, gr.w, invs[L], ws, cnt);
+        const bool hit = warp_collide(gc, st, gr.z, gr.w, invs[L], ws, cnt, w.margin);
         if (lane == L) {
           ++cnt.narrow;
           ovm &= ovm - 1u;

@@ -45,9 +45,9 @@ def assert_poses(got, ref_colmajor, pkg):
     assert not bad.any(), f"{bad.sum()} pose entries outside tolerance"
 
 
-def world_pair(pkg, ref, n, meshes):
-    W = pkg.CollisionWorld(n)
-    R = ref.RefWorld(n)
+def world_pair(pkg, ref, n, meshes, margin=0.0):
+    W = pkg.CollisionWorld(n, margin)
+    R = ref.RefWorld(n, margin)
     gids = []
     for m in meshes:
         g1 = W.register_geometry(m)
@@ -64,14 +64,17 @@ def mesh_zoo(pkg):
             scenes.sphere_set(rng), scenes.open_container(0.3, 0.25, 0.15, 0.01)]
 
 
-@pytest.mark.parametrize("upright", [True, False])
-@pytest.mark.parametrize("seed", [0, 1, 2])
-def test_check_batch_random_worlds(gpu, ref, upright, seed):
+@pytest.mark.parametrize("upright,seed,margin", [(True, 0, 0.0), (True, 1, 0.0), (True, 2, 0.0),
+                                                 (False, 0, 0.0), (False, 1, 0.0), (False, 2, 0.0),
+                                                 # margin > 0: tri_tri_distance path (collision.cpp:136-212)
+                                                 (True, 3, 0.004), (False, 4, 0.004),
+                                                 (True, 5, 0.02), (False, 6, 0.02)])
+def test_check_batch_random_worlds(gpu, ref, upright, seed, margin):
     pkg = gpu
     rng = np.random.default_rng(seed)
     n = 512
     meshes = mesh_zoo(pkg)
-    W, R, gids = world_pair(pkg, ref, n, meshes)
+    W, R, gids = world_pair(pkg, ref, n, meshes, margin)
     n_obj = 8
     for k in range(n_obj):
         g = gids[rng.integers(len(gids))]
