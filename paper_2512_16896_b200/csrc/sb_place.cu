@@ -13,6 +13,10 @@
 #include "sb_poly.h"
 #include "sb_warp.cuh"
 
+#ifndef SB_PLACE_MIN_BLOCKS
+#define SB_PLACE_MIN_BLOCKS 2  // CTAs per SM the register budget is sized for
+#endif
+
 namespace cg = cooperative_groups;
 using namespace sbd;
 
@@ -22,8 +26,8 @@ namespace {
 constexpr int kB = kPlaceBlock;
 constexpr int kWarps = kB / 32;
 constexpr int32_t kFree = INT32_MAX;
-constexpr int kCand = 1024;   // broad-phase items per chunk
-constexpr int kQueue = kCand; // narrow pairs per chunk (at most one per item)
+constexpr int kCand = 512;    // broad-phase items per chunk (grid mode)
+constexpr int kQueue = 1024;  // narrow pairs (grid mode: <= one per item of a chunk)
 constexpr uint8_t kSlotChecked = 1, kSlotUnplaceable = 2, kSlotEnumerated = 4;
 constexpr int kGW = 8;  // enable words the broad phase keeps in registers (<= 256 objects)
 constexpr int kPrefixItems = 8;  // tile counts per thread per prefix-scan chunk
@@ -34,7 +38,6 @@ using BlockScan = cub::BlockScan<uint32_t, kB>;
 
 // Per-round candidate state of the CTA's tile (dynamic shared memory).
 struct Tile {
-  double* inv;       // [kB][12] inverse pose per slot
   double* box;       // [kB][6]  candidate world AABB per slot
   uint32_t* ovm;     // [words][kB] broad-phase overlap bits per slot
   uint32_t* enw;     // [words][kB] enable words per tile entry
@@ -50,7 +53,7 @@ struct Tile {
 };
 
 struct Fixed {  // static shared memory
-  GeomCache gc;
+  PlaceGeomCache gc;
   typename BlockScan::TempStorage scan;
   uint32_t prefix[kPlaceMaxOwnedTiles];  // fast path: draw offset of each owned tile
   uint32_t cnt[kPlaceMaxOwnedTiles];     // fast path: its survivors entering this round
@@ -66,8 +69,7 @@ struct Fixed {  // static shared memory
 
 __device__ __forceinline__ Tile carve(unsigned char* d, int words, int ws_bytes) {
   Tile t;
-  t.inv = reinterpret_cast<double*>(d);
-  t.box = t.inv + 12 * kB;
+  t.box = reinterpret_cast<double*>(d);
   t.ovm = reinterpret_cast<uint32_t*>(t.box + 6 * kB);
   t.enw = t.ovm + words * kB;
   t.list = t.enw + words * kB;
@@ -83,7 +85,7 @@ __device__ __forceinline__ Tile carve(unsigned char* d, int words, int ws_bytes)
 }
 
 __host__ __device__ constexpr size_t tile_bytes(int words) {
-  return (12 + 6) * 8 * (size_t)kB + 2 * (size_t)words * kB * 4 + (size_t)kB * 4 +
+  return 6 * 8 * (size_t)kB + 2 * (size_t)words * kB * 4 + (size_t)kB * 4 +
          (size_t)(kQueue + kCand) * 4 + 3 * (size_t)kB * 4 + kB;
 }
 
@@ -178,7 +180,8 @@ __device__ __forceinline__ void narrow_drain(const PlaceParams& p, Tile& T, Fixe
   };
   auto stage = [&](uint32_t ent, int buf) {
     const int v = (int)(ent >> 24), ob = (int)(ent & 0xffffffu);
-    warp_stage(w, T.ogeo[ob], ob, T.list[v % (int)nt], stage_buf(wsb, p.max_tris, p.max_nodes, buf));
+    warp_stage(w, T.ogeo[ob], ob, T.list[v % (int)nt], p.cinv + ((size_t)blockIdx.x * kB + v) * 12,
+               stage_buf(wsb, p.max_tris, p.max_nodes, buf));
   };
   int cur = 0;
   uint32_t q = next_eligible(warp);
@@ -197,7 +200,7 @@ __device__ __forceinline__ void narrow_drain(const PlaceParams& p, Tile& T, Fixe
     if (!skippable(v, ob)) {
       const int e = v % (int)nt, sl = v / (int)nt;
       const bool hit = warp_collide(F.gc, stage_buf(wsb, p.max_tris, p.max_nodes, cur),
-                                    T.ogeo[ob].z, T.ogeo[ob].w, T.inv + 12 * v, ws, L.cnt);
+                                    T.ogeo[ob].z, T.ogeo[ob].w, ws, L.cnt);
       if (p.dbg_inst && lane == 0) atomicAdd(&F.dt, 1u);
       if (lane == 0) {
         if (hit) {
@@ -312,7 +315,9 @@ __device__ uint32_t tile_round(const PlaceParams& p, const Sampling& S, const Sb
 #pragma unroll
       for (int k = 0; k < 6; ++k) cp[k] = make_double2(pose.m[2 * k], pose.m[2 * k + 1]);
 #pragma unroll
-      for (int k = 0; k < 12; ++k) T.inv[12 * v + k] = inv.m[k];
+      for (int k = 0; k < 6; ++k)
+        reinterpret_cast<double2*>(p.cinv + ((size_t)blockIdx.x * kB + v) * 12)[k] =
+            make_double2(inv.m[2 * k], inv.m[2 * k + 1]);
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
         T.box[6 * v + k] = cmn[k];
@@ -704,7 +709,7 @@ __device__ __forceinline__ void block_setup(const PlaceParams& p, Fixed& F, Tile
 extern __shared__ __align__(16) unsigned char g_dsm[];
 
 template <bool kGrid>
-__global__ void __launch_bounds__(kB, 2) k_place(PlaceParams p) {
+__global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_place(PlaceParams p) {
   __shared__ Fixed F;
   Tile T = carve(g_dsm, p.w.n_words, p.ws_bytes);
   const bool timer = p.prof && blockIdx.x == 0 && threadIdx.x == 0;
@@ -773,7 +778,7 @@ __global__ void __launch_bounds__(kB, 2) k_place(PlaceParams p) {
 
 // Sharded building blocks (no grid barrier inside a launch).
 template <bool kGrid>
-__global__ void __launch_bounds__(kB, 2) k_place_instances(PlaceParams p) {
+__global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_place_instances(PlaceParams p) {
   __shared__ Fixed F;
   Tile T = carve(g_dsm, p.w.n_words, p.ws_bytes);
   SbGeom gA;
@@ -784,7 +789,7 @@ __global__ void __launch_bounds__(kB, 2) k_place_instances(PlaceParams p) {
   flush(p, L);
 }
 
-__global__ void __launch_bounds__(kB, 2) k_fast_init(PlaceParams p) {
+__global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_fast_init(PlaceParams p) {
   __shared__ Fixed F;
   Tile T = carve(g_dsm, p.w.n_words, p.ws_bytes);
   uint32_t mine = 0;
@@ -798,7 +803,7 @@ __global__ void __launch_bounds__(kB, 2) k_fast_init(PlaceParams p) {
 }
 
 template <bool kGrid>
-__global__ void __launch_bounds__(kB, 2) k_fast_round(PlaceParams p, int32_t a) {
+__global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_fast_round(PlaceParams p, int32_t a) {
   __shared__ Fixed F;
   Tile T = carve(g_dsm, p.w.n_words, p.ws_bytes);
   SbGeom gA;

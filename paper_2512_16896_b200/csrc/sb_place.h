@@ -63,6 +63,7 @@ struct PlaceParams {
   int32_t ws_bytes;             // narrow-phase scratch per warp (sb_warp.cuh)
   int32_t max_tris, max_nodes;  // scratch geometry bounds over the world's geometries
   double* cpose;                // [grid][kPlaceBlock][12] candidate pose per CTA slot
+  double* cinv;                 // [grid][kPlaceBlock][12] its inverse (narrow phase, cp.async)
   SbCellGrid grid;              // broad-phase occupancy grid
   uint32_t* ctrl;               // [8] per placement: see Ctrl in sb_place.cu
   unsigned long long* counters; // [8]

@@ -456,6 +456,7 @@ struct sb_engine {
   DevArray<uint32_t> d_tile_list;   // [ntiles * tile_inst] survivors per tile
   DevArray<uint32_t> d_tile_cnt;    // [2][ntiles]
   DevArray<double> d_cpose;         // [grid][kPlaceBlock][12] candidate poses
+  DevArray<double> d_cinv;          // [grid][kPlaceBlock][12] their inverses
   DevArray<uint32_t> d_cells;       // broad-phase occupancy grid [n][g * g][words]
   SbCellGrid cell_grid{};
   DevArray<uint32_t> d_ctrl;
@@ -648,6 +649,8 @@ struct sb_engine {
       max_tris = std::max(max_tris, static_cast<int>(g.g.n_tris));
       max_nodes = std::max(max_nodes, static_cast<int>(g.g.n_nodes));
     }
+    if (max_tris > 16 || max_nodes > 16)
+      throw std::invalid_argument("engine: a geometry's effective BVH exceeds 16 nodes / 16 triangles");
     ws_bytes = sbk::place_ws_bytes(max_tris, max_nodes);
     smem = sbk::place_smem_bytes(world->view().n_words, ws_bytes, world->view().n_objects);
     grid = static_cast<unsigned>(sbk::place_grid(num_sms, smem));
@@ -664,6 +667,7 @@ struct sb_engine {
     d_tile_list.alloc(static_cast<size_t>(ntiles) * tile_inst);
     d_tile_cnt.alloc(2 * static_cast<size_t>(ntiles));
     d_cpose.alloc(static_cast<size_t>(grid) * sbk::kPlaceBlock * 12);
+    d_cinv.alloc(static_cast<size_t>(grid) * sbk::kPlaceBlock * 12);
     {  // occupancy grid over the supports' XY extent, widened by the largest object radius
       double bx0 = HUGE_VAL, by0 = HUGE_VAL, bx1 = -HUGE_VAL, by1 = -HUGE_VAL, rad = 0.0;
       for (uint32_t k = 0; k < sc->n_supports; ++k) {
@@ -879,6 +883,7 @@ struct sb_engine {
       pp.tile_list = d_tile_list.p;
       pp.tile_cnt = d_tile_cnt.p;
       pp.cpose = d_cpose.p;
+      pp.cinv = d_cinv.p;
       pp.grid = cell_grid;
       pp.cnt_stride = ntiles;
       pp.ntiles = ntiles;

@@ -46,28 +46,36 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
 }
+// L2-only variant for data written earlier in the same kernel (no stale L1 line).
+__device__ __forceinline__ void cp_async16_cg(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// Bytes of one pair's staging buffer: the placed object's pose (row-major 3x4, 96 B) and
-// the compact record of its geometry (sb_layout.h).
+// Bytes of one pair's staging buffer: the placed object's pose (row-major 3x4, 96 B), the
+// candidate's inverse pose (96 B) and the compact record of its geometry (sb_layout.h).
 __host__ __device__ constexpr int stage_bytes(int maxT, int maxN) {
-  return 96 + sb_brec_bytes(maxN, maxT);
+  return 192 + sb_brec_bytes(maxN, maxT);
 }
 
 // The whole warp issues the asynchronous copies of pair (ob, inst) into `dst` (one commit
-// group per lane); gr = grec[geometry of ob].
+// group per lane); gr = grec[geometry of ob]; inv = the candidate's inverse pose in global
+// memory (12 doubles, 16-byte aligned) or null when the caller fills dst + 96 itself.
 __device__ __forceinline__ void warp_stage(const WorldView& w, const int4 gr, int32_t ob,
-                                           uint64_t inst, unsigned char* dst) {
+                                           uint64_t inst, const double* inv, unsigned char* dst) {
   const int lane = threadIdx.x & 31;
   const unsigned char* pose = reinterpret_cast<const unsigned char*>(w.pose + sb_pose_off(w, ob, inst));
   const unsigned char* rec = reinterpret_cast<const unsigned char*>(w.brec) + 16 * (size_t)gr.x;
-  for (int c = lane; c < 6 + gr.y; c += 32) {
-    if (c < 6) cp_async16(dst + 16 * c, pose + 16 * c);
-    else cp_async16(dst + 16 * c, rec + 16 * (c - 6));
+  for (int c = lane; c < 12 + gr.y; c += 32) {
+    if (c < 6) cp_async16_cg(dst + 16 * c, pose + 16 * c);
+    else if (c < 12) {
+      if (inv) cp_async16_cg(dst + 16 * c, reinterpret_cast<const unsigned char*>(inv) + 16 * (c - 6));
+    } else cp_async16(dst + 16 * c, rec + 16 * (c - 12));
   }
   cp_async_commit();
 }
@@ -142,21 +150,27 @@ struct alignas(16) WarpScratch {  // fixed-size variant (world API check_batch)
 
 // Candidate geometry (uniform per launch), staged in shared memory once per block, with
 // the planes of its triangles (pure functions of the A triangles in A's own frame).
-struct GeomCache {
-  double ta[kMaxEffTris][9];
-  double pa[kMaxEffTris][5];  // TriPlane: n xyz, dc, tol
-  double bmin[kMaxNodes][3], bmax[kMaxNodes][3];
-  double ext2[kMaxNodes];
-  int8_t c0[kMaxNodes], c1[kMaxNodes];
-  int8_t tleaf[kMaxEffTris];
+template <int NT, int NN>
+struct GeomCacheT {
+  double ta[NT][9];
+  double pa[NT][5];  // TriPlane: n xyz, dc, tol
+  double bmin[NN][3], bmax[NN][3];
+  double ext2[NN];
+  int8_t c0[NN], c1[NN];
+  int8_t tleaf[NT];
   uint32_t leafmask;
-  int8_t leaves[kMaxNodes];  // leaf node ids, ascending
-  uint32_t lbelow[kMaxNodes];  // effective leaves under each node
+  int8_t leaves[NN];  // leaf node ids, ascending
+  uint32_t lbelow[NN];  // effective leaves under each node
   int n_tris, n_nodes, n_leaves;
 };
 
-__device__ __forceinline__ void load_geom_cache(const WorldView& w, const SbGeom& gA,
-                                                GeomCache& gc) {
+// world API check_batch: any registrable geometry; placement engine: <= 16 / 16 (host-checked)
+using GeomCache = GeomCacheT<kMaxEffTris, kMaxNodes>;
+constexpr int kPlaceCacheTris = 16, kPlaceCacheNodes = 16;
+using PlaceGeomCache = GeomCacheT<kPlaceCacheTris, kPlaceCacheNodes>;
+
+template <class GC>
+__device__ __forceinline__ void load_geom_cache(const WorldView& w, const SbGeom& gA, GC& gc) {
   const SbTri* t = w.tris + gA.tri_offset;
   const SbNode* nd = w.nodes + gA.node_offset;
   for (int k = threadIdx.x; k < gA.n_tris; k += blockDim.x) {
@@ -219,17 +233,18 @@ __device__ __forceinline__ int warp_append(bool pass, uint16_t value, uint16_t* 
 // `margin` = the world's margin (collision.hpp:78): box tests use Aabb3::overlaps(., margin)
 // and, when margin > 0, a triangle pair counts when tri_tri_distance < margin
 // (collision.cpp:312-313) instead of the staged intersection filters.
-__device__ __forceinline__ bool warp_collide(const GeomCache& gc, const unsigned char* stage,
-                                             int nB, int nTB, const double* I,
-                                             const WarpScratchView& ws, CheckCounters& cnt,
-                                             double mg = 0.0) {
+template <class GC>
+__device__ __forceinline__ bool warp_collide(const GC& gc, const unsigned char* stage,
+                                             int nB, int nTB, const WarpScratchView& ws,
+                                             CheckCounters& cnt, double mg = 0.0) {
   const int lane = threadIdx.x & 31;
   SB_NP_MARK(np0);
   const double* P = reinterpret_cast<const double*>(stage);
-  const double* recbox = reinterpret_cast<const double*>(stage + 96);
-  const uint32_t* recinfo = reinterpret_cast<const uint32_t*>(stage + 96 + 48 * nB);
-  const double* rectri = reinterpret_cast<const double*>(stage + 96 + 56 * nB);
-  const int8_t* recleaf = reinterpret_cast<const int8_t*>(stage + 96 + 56 * nB + 72 * nTB);
+  const double* I = reinterpret_cast<const double*>(stage + 96);
+  const double* recbox = reinterpret_cast<const double*>(stage + 192);
+  const uint32_t* recinfo = reinterpret_cast<const uint32_t*>(stage + 192 + 48 * nB);
+  const double* rectri = reinterpret_cast<const double*>(stage + 192 + 56 * nB);
+  const int8_t* recleaf = reinterpret_cast<const int8_t*>(stage + 192 + 56 * nB + 72 * nTB);
   if (lane < 12) {  // other_in_cand = inv(cand) * pose(ob), one entry per lane (shim order)
     const int i = lane >> 2, j = lane & 3;
     double s = I[4 * i + 0] * P[j];
@@ -561,10 +576,11 @@ __device__ __forceinline__ int warp_check(const WorldView& w, const SbGeom& gA,
         const int ob = ob0 + __ffs(ovL) - 1;
         const int4 gr = obj_grec(w, ob);
         unsigned char* st = stage_buf(wsf.bytes, kMaxEffTris, kMaxNodes, 0);
-        warp_stage(w, gr, ob, instL, st);
+        warp_stage(w, gr, ob, instL, nullptr, st);
+        if (lane < 12) reinterpret_cast<double*>(st + 96)[lane] = invs[L][lane];
         cp_async_wait<0>();
         __syncwarp();
-        const bool hit = warp_collide(gc, st, gr.z, gr.w, invs[L], ws, cnt, w.margin);
+        const bool hit = warp_collide(gc, st, gr.z, gr.w, ws, cnt, w.margin);
         if (lane == L) {
           ++cnt.narrow;
           ovm &= ovm - 1u;
