@@ -14,7 +14,7 @@
 #include "sb_warp.cuh"
 
 #ifndef SB_PLACE_MIN_BLOCKS
-#define SB_PLACE_MIN_BLOCKS 2  // CTAs per SM the register budget is sized for
+#define SB_PLACE_MIN_BLOCKS (512 / SB_PLACE_BLOCK)  // CTAs per SM the register budget is sized for
 #endif
 
 namespace cg = cooperative_groups;

@@ -77,7 +77,10 @@ struct PlaceParams {
   const int32_t* vary_flag;
 };
 
-constexpr int kPlaceBlock = 256;
+#ifndef SB_PLACE_BLOCK
+#define SB_PLACE_BLOCK 256
+#endif
+constexpr int kPlaceBlock = SB_PLACE_BLOCK;  // threads per placement CTA = max tile slots
 constexpr int kPlaceMaxOwnedTiles = 64;  // tiles per CTA on the fast path
 
 // Dynamic shared memory of one placement CTA for a world with `n_words` enable words.
