@@ -203,7 +203,12 @@ SB_HD bool sink_tri(TableSink& s, double ax, double ay, double bx, double by, do
 
 // triangulate() of a hole-free polygon (polygon.cpp:344-368) feeding ear_clip_ring
 // (polygon.cpp:260-340) straight into the sampler table. `r` is consumed.
-SB_HD bool ear_clip_into(Ring& r, TableSink& sink) {
+#ifdef __CUDACC__
+static __host__ __device__ __noinline__
+#else
+inline
+#endif
+bool ear_clip_into(Ring& r, TableSink& sink) {
   if (r.n < 3) return true;
   if (ring_area(r) < 0.0) reverse_ring(r);
   // drop consecutive duplicates (squared distance <= 1e-24)
