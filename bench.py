@@ -145,12 +145,9 @@ def run_ours(args, rank, world, local_rank):
 
     shard = None
     if world > 1:
-        def allgather(vals):
-            t = torch.tensor(vals, dtype=torch.int64)
-            out = [torch.zeros_like(t) for _ in range(world)]
-            dist.all_gather(out, t)
-            return [int(v) for o in out for v in o.tolist()]
-        shard = pkg.Shard(rank * n_per, (rank + 1) * n_per, rank, world, allgather)
+        from paper_2512_16896_b200.dist import torch_allgather
+
+        shard = pkg.Shard(rank * n_per, (rank + 1) * n_per, rank, world, torch_allgather(world))
     t0 = time.time()
     eng = pkg.Engine(scene, shard, device=device)
     cold_s = time.time() - t0
