@@ -620,9 +620,11 @@ __device__ __forceinline__ void store_list(const PlaceParams& p, const Tile& T, 
 
 // One fast-path round over the CTA's tiles: survivors of round a -> counts of round a+1.
 template <bool kGrid>
+// `resident`: the CTA owns at most one tile and T.list still holds its survivors from the
+// previous round (persistent kernel), so the list is not reloaded.
 __device__ uint64_t fast_round(const PlaceParams& p, const Sampling& S, const SbGeom& gA,
                                Tile& T, Fixed& F, int32_t a, uint64_t draws, Local& L,
-                               uint32_t* total_word) {
+                               uint32_t* total_word, bool resident) {
   const uint32_t* cin = p.tile_cnt + (size_t)(a & 1) * p.cnt_stride;
   uint32_t* cout = p.tile_cnt + (size_t)((a + 1) & 1) * p.cnt_stride;
   const uint64_t total = tile_prefix(p, cin, F);
@@ -635,7 +637,7 @@ __device__ uint64_t fast_round(const PlaceParams& p, const Sampling& S, const Sb
       if (threadIdx.x == 0) cout[t] = 0;
       continue;
     }
-    load_list(p, T, t, n);
+    if (!resident) load_list(p, T, t, n);
     lap(p, F, 1);
     if (p.dbg && threadIdx.x == 0) F.t0 = global_ns();
     const uint32_t ns = tile_round<kGrid>(p, S, gA, T, F, n, a, 1, draws + F.prefix[k], L);
@@ -745,7 +747,8 @@ __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_place(PlaceParams p
         r0 = global_ns();
         F.ta = F.tb = 0;
       }
-      const uint64_t total = fast_round<kGrid>(p, S, gA, T, F, a, draws, L, nullptr);
+      const uint64_t total =
+          fast_round<kGrid>(p, S, gA, T, F, a, draws, L, nullptr, p.ntiles <= gridDim.x);
       if (total == 0) break;
       draws += total;
       if (p.dbg && threadIdx.x == 0) {  // per-round maxima over CTAs: work, A1, A2+B
@@ -810,7 +813,7 @@ __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_fast_round(PlacePar
   block_setup(p, F, T, gA);
   Local L;
   Sampling S{1, p.canon_tris, p.canon_cum, p.canon_n};
-  fast_round<kGrid>(p, S, gA, T, F, a, p.draw_base, L, p.ctrl + place_total_word(a + 1));
+  fast_round<kGrid>(p, S, gA, T, F, a, p.draw_base, L, p.ctrl + place_total_word(a + 1), false);
   flush(p, L);
 }
 
