@@ -564,9 +564,10 @@ __device__ uint32_t tile_round(const PlaceParams& p, const Sampling& S, const Sb
 }
 
 // Stable compaction of the valid instances of tile t into T.list; returns the count.
-__device__ uint32_t tile_load_valid(const PlaceParams& p, Tile& T, Fixed& F, uint32_t t) {
-  const uint64_t i = (uint64_t)t * p.tile_inst + threadIdx.x;
-  const uint32_t f = (threadIdx.x < p.tile_inst && i < p.w.n && p.valid[i] != 0) ? 1u : 0u;
+__device__ uint32_t tile_load_valid(const PlaceParams& p, Tile& T, Fixed& F, uint32_t t,
+                                    uint32_t ti) {
+  const uint64_t i = (uint64_t)t * ti + threadIdx.x;
+  const uint32_t f = (threadIdx.x < ti && i < p.w.n && p.valid[i] != 0) ? 1u : 0u;
   uint32_t rank, total;
   BlockScan(F.scan).ExclusiveSum(f, rank, total);
   if (f) T.list[rank] = (uint32_t)i;
@@ -658,8 +659,8 @@ __device__ void instance_tiles(const PlaceParams& p, const Sampling& S, const Sb
     __syncthreads();
     const uint32_t t = F.tile;
     __syncthreads();
-    if (t >= p.ntiles) break;
-    uint32_t nt = tile_load_valid(p, T, F, t);
+    if (t >= p.ntiles_pi) break;
+    uint32_t nt = tile_load_valid(p, T, F, t, p.tile_inst_pi);
     int32_t a = 0;
     unsigned rounds = 0;
     const unsigned long long tt0 = p.dbg_inst && threadIdx.x == 0 ? global_ns() : 0;
@@ -732,7 +733,7 @@ __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_place(PlaceParams p
   } else {
     cg::grid_group grid = cg::this_grid();
     for (uint32_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
-      const uint32_t n = tile_load_valid(p, T, F, t);
+      const uint32_t n = tile_load_valid(p, T, F, t, p.tile_inst);
       store_list(p, T, t, n, p.tile_cnt);
       __syncthreads();
     }
@@ -797,7 +798,7 @@ __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_fast_init(PlacePara
   Tile T = carve(g_dsm, p.w.n_words, p.ws_bytes);
   uint32_t mine = 0;
   for (uint32_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
-    const uint32_t n = tile_load_valid(p, T, F, t);
+    const uint32_t n = tile_load_valid(p, T, F, t, p.tile_inst);
     store_list(p, T, t, n, p.tile_cnt);
     mine += n;
     __syncthreads();

@@ -59,6 +59,8 @@ struct PlaceParams {
   uint32_t cnt_stride;
   uint32_t ntiles;
   int32_t tile_inst;            // instances per tile (<= kPlaceBlock)
+  uint32_t ntiles_pi;           // per-instance path: smaller tiles taken dynamically
+  int32_t tile_inst_pi;
   int32_t spec_target;          // per-instance path: target slots per tile round
   int32_t ws_bytes;             // narrow-phase scratch per warp (sb_warp.cuh)
   int32_t max_tris, max_nodes;  // scratch geometry bounds over the world's geometries

@@ -470,7 +470,7 @@ struct sb_engine {
   int num_sms = 0;
   // tile decomposition of the shard (sb_place.h) and launch shape of the placement kernel
   uint32_t ntiles = 0;
-  int tile_inst = 0, max_tris = 1, max_nodes = 1, ws_bytes = 0;
+  int tile_inst = 0, tile_inst_pi = 0, max_tris = 1, max_nodes = 1, ws_bytes = 0;
   int spec_target = 64;
   unsigned grid = 0;
   size_t smem = 0;
@@ -486,6 +486,8 @@ struct sb_engine {
   DevArray<int32_t> d_inst_n;
   DevArray<double> d_pose16;
   PinnedArray<uint64_t> h_count;
+  cudaStream_t copy_stream = nullptr;  // pipelined result download
+  std::vector<cudaEvent_t> ev_pose;
   cudaEvent_t ev_start = nullptr, ev_stop = nullptr, ev_r0 = nullptr, ev_r1 = nullptr;
 
   uint64_t last_launches = 0;
@@ -660,6 +662,11 @@ struct sb_engine {
       const uint64_t waves = (n + per_wave - 1) / per_wave;
       const uint64_t want = static_cast<uint64_t>(grid) * waves;
       tile_inst = static_cast<int>((n + want - 1) / want);
+      // per-instance placements: smaller tiles, taken dynamically, so a dense tile's heavy
+      // narrow phase does not hold the whole placement (SB_PI_SPLIT; measured best: 1)
+      int split = 1;
+      if (const char* e = std::getenv("SB_PI_SPLIT")) split = std::max(1, std::atoi(e));
+      tile_inst_pi = std::max(1, (tile_inst + split - 1) / split);
       ntiles = static_cast<uint32_t>((n + tile_inst - 1) / tile_inst);
       if ((ntiles + grid - 1) / grid > static_cast<uint32_t>(sbk::kPlaceMaxOwnedTiles))
         throw std::invalid_argument("shard too large for one device: " + std::to_string(n) + " instances");
@@ -733,6 +740,11 @@ struct sb_engine {
     for (cudaEvent_t e : {ev_start, ev_stop, ev_r0, ev_r1})
       if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : ev_place) cudaEventDestroy(e);
+    for (cudaEvent_t e : ev_pose) cudaEventDestroy(e);
+    if (copy_stream) {
+      cudaStreamSynchronize(copy_stream);
+      cudaStreamDestroy(copy_stream);
+    }
   }
 
 
@@ -809,8 +821,22 @@ struct sb_engine {
     return vary;
   }
 
-  void generate(uint64_t run_seed, sb_run_stats* st) {
+  // Results requested with the call (sb_engine_generate with an sb_result) are downloaded
+  // while later placements compute: placement p's poses are final once its kernel ends, so
+  // a copy stream converts them (k_pose_colmajor) and copies them to the host behind an event.
+  void generate(uint64_t run_seed, sb_run_stats* st, sb_result* out = nullptr) {
     world->activate();
+    const bool pipe = out && out->poses && !places.empty();
+    if (pipe) {
+      if (!copy_stream)
+        cuda_check(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+      while (ev_pose.size() < places.size()) {
+        cudaEvent_t e;
+        cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+        ev_pose.push_back(e);
+      }
+      d_pose16.ensure(2 * 16 * n);
+    }
     cudaStream_t stream = world->stream;
     sb_stream_t s = world->s();
     const SbWorldView wv = world->view();
@@ -888,6 +914,8 @@ struct sb_engine {
       pp.cnt_stride = ntiles;
       pp.ntiles = ntiles;
       pp.tile_inst = tile_inst;
+      pp.tile_inst_pi = tile_inst_pi;
+      pp.ntiles_pi = static_cast<uint32_t>((n + tile_inst_pi - 1) / tile_inst_pi);
       pp.spec_target = spec_target;
       pp.ws_bytes = ws_bytes;
       pp.max_tris = max_tris;
@@ -959,6 +987,20 @@ struct sb_engine {
           ++launches;
         }
       }
+      if (pipe) {  // placement p is final: convert + copy its poses behind an event
+        double* buf = d_pose16.p + (p & 1) * 16 * n;
+        cuda_check(cudaEventRecord(ev_pose[p], stream), "event");
+        cuda_check(cudaStreamWaitEvent(copy_stream, ev_pose[p], 0), "wait");
+        sbk::download_poses(wv, pl.dev.object, buf, reinterpret_cast<sb_stream_t>(copy_stream));
+        cuda_check(cudaMemcpyAsync(out->poses + 16 * n * p, buf, 16 * n * sizeof(double),
+                                   cudaMemcpyDeviceToHost, copy_stream), "D2H poses");
+      }
+    }
+    if (out) {
+      if (out->accepted && P)
+        cuda_check(cudaMemcpyAsync(out->accepted, d_accepted.p, P * n * sizeof(int16_t), cudaMemcpyDeviceToHost, stream), "D2H accepted");
+      if (out->valid)
+        cuda_check(cudaMemcpyAsync(out->valid, d_valid.p, n, cudaMemcpyDeviceToHost, stream), "D2H valid");
     }
     cuda_check(cudaEventRecord(ev_place[2 * P], stream), "event");
     cuda_check(cudaEventRecord(ev_stop, stream), "event");
@@ -1040,6 +1082,7 @@ struct sb_engine {
       for (uint8_t x : v) nv += x;
       st->valid_instances = nv;
     }
+    if (pipe) cuda_check(cudaStreamSynchronize(copy_stream), "sync copy stream");
   }
 
   void download(sb_result* out) {
@@ -1264,8 +1307,7 @@ sb_status sb_engine_create(const sb_scene* sc, const sb_shard* shard, int device
 void sb_engine_destroy(sb_engine* e) { delete e; }
 sb_status sb_engine_generate(sb_engine* e, uint64_t run_seed, sb_result* out, sb_run_stats* st) {
   return guard([&] {
-    e->generate(run_seed, st);
-    e->download(out);
+    e->generate(run_seed, st, out);  // results (if requested) are downloaded by generate
   });
 }
 sb_status sb_engine_download(sb_engine* e, sb_result* out) {
