@@ -31,6 +31,7 @@ constexpr int kQueue = 1024;  // narrow pairs (grid mode: <= one per item of a c
 constexpr uint8_t kSlotChecked = 1, kSlotUnplaceable = 2, kSlotEnumerated = 4;
 constexpr int kGW = 8;  // enable words the broad phase keeps in registers (<= 256 objects)
 constexpr int kPrefixItems = 8;  // tile counts per thread per prefix-scan chunk
+constexpr uint64_t kSoloFlag = 1ull << 63;
 
 enum Ctrl { kRounds = 2, kErr = 3, kTileCtr = 4 /* kTotal0 = 5, kTotal1 = 6 */ };
 
@@ -631,6 +632,7 @@ __device__ uint64_t fast_round(const PlaceParams& p, const Sampling& S, const Sb
   const uint64_t total = tile_prefix(p, cin, F);
   lap(p, F, 1);
   if (total == 0) return 0;
+  if (total <= (uint64_t)p.solo_max) return total | kSoloFlag;  // caller runs solo rounds
   uint32_t k = 0, mine = 0;
   for (uint32_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++k) {
     const uint32_t n = F.cnt[k];
@@ -648,6 +650,34 @@ __device__ uint64_t fast_round(const PlaceParams& p, const Sampling& S, const Sb
   }
   if (total_word && threadIdx.x == 0 && mine) atomicAdd(total_word, mine);
   return total;
+}
+
+// Fast path tail: once at most p.solo_max instances remain, CTA 0 gathers them in global
+// active order (tile order, then position) and runs the remaining rounds alone -- no grid
+// barrier, no prefix scan; draw j of round a is draws + position, as in the grid rounds.
+template <bool kGrid>
+__device__ void solo_rounds(const PlaceParams& p, const Sampling& S, const SbGeom& gA, Tile& T,
+                            Fixed& F, int32_t a, uint64_t draws, Local& L) {
+  const uint32_t* cin = p.tile_cnt + (size_t)(a & 1) * p.cnt_stride;
+  uint32_t base = 0;
+  for (uint32_t t0 = 0; t0 < p.ntiles; t0 += kB) {
+    const uint32_t t = t0 + threadIdx.x;
+    const uint32_t c = t < p.ntiles ? __ldcg(cin + t) : 0u;
+    uint32_t off, tot;
+    BlockScan(F.scan).ExclusiveSum(c, off, tot);
+    const uint32_t* src = p.tile_list + (uint64_t)t * p.tile_inst;
+    for (uint32_t e = 0; e < c; ++e) T.list[base + off + e] = __ldcg(src + e);
+    base += tot;
+    __syncthreads();
+  }
+  uint32_t nt = base;
+  while (nt > 0 && a < p.attempts) {
+    const uint32_t ns = tile_round<kGrid>(p, S, gA, T, F, nt, a, 1, draws, L);
+    draws += nt;
+    nt = ns;
+    ++a;
+  }
+  if (a == p.attempts) mark_invalid(p, T, nt);
 }
 
 // Per-instance path: tiles are independent; each is run to completion by one CTA.
@@ -748,8 +778,13 @@ __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_place(PlaceParams p
         r0 = global_ns();
         F.ta = F.tb = 0;
       }
-      const uint64_t total =
+      uint64_t total =
           fast_round<kGrid>(p, S, gA, T, F, a, draws, L, nullptr, p.ntiles <= gridDim.x);
+      if (total & kSoloFlag) {
+        if (blockIdx.x == 0) solo_rounds<kGrid>(p, S, gA, T, F, a, draws, L);
+        a = -1;  // tail done by CTA 0
+        break;
+      }
       if (total == 0) break;
       draws += total;
       if (p.dbg && threadIdx.x == 0) {  // per-round maxima over CTAs: work, A1, A2+B

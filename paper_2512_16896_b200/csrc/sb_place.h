@@ -62,6 +62,7 @@ struct PlaceParams {
   uint32_t ntiles_pi;           // per-instance path: smaller tiles taken dynamically
   int32_t tile_inst_pi;
   int32_t spec_target;          // per-instance path: target slots per tile round
+  int32_t solo_max;             // fast path: at most this many survivors -> CTA 0 alone
   int32_t ws_bytes;             // narrow-phase scratch per warp (sb_warp.cuh)
   int32_t max_tris, max_nodes;  // scratch geometry bounds over the world's geometries
   double* cpose;                // [grid][kPlaceBlock][12] candidate pose per CTA slot
