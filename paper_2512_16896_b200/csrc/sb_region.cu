@@ -1,11 +1,12 @@
 // Warp-cooperative per-instance constraint regions (relationships.cpp:161-218 with
 // polygon.cpp:136-176 annulus_sector, the rect-clip stand-in for Boost intersect, and
-// polygon.cpp:260-388 triangulate + PolygonSampler), one warp per instance, all on device.
+// polygon.cpp:260-388 triangulate + PolygonSampler), one 16-lane group per instance (two
+// instances per warp), all on device.
 //
 // Lanes compute the arc points, the Sutherland-Hodgman passes (prefix-sum compaction
 // preserves the sequential output order) and the fan triangles in parallel; every step
 // whose rounding depends on evaluation order (ring areas, the tolerance-based duplicate
-// drop, the cumulative-area table) runs on lane 0 in the reference's order, so tables are
+// drop, the cumulative-area table) runs on g.gl 0 in the reference's order, so tables are
 // bit-identical to sbp::* (the single-thread restatement) and to the reference.
 #include <stdexcept>
 #include <string>
@@ -22,9 +23,27 @@ namespace sbk {
 namespace {
 
 constexpr int kRB = 128;            // threads per block
-constexpr int kRW = kRB / 32;       // warps per block
+constexpr int kG = 16;              // lanes per instance group: two instances per warp
+constexpr int kRW = kRB / kG;       // groups per block
 constexpr int kCap = sbp::kCap;
-constexpr unsigned kFull = 0xffffffffu;
+
+// The lanes of one instance group and its collectives (kG-wide shuffles, ballots, votes).
+struct Grp {
+  int gl;          // g.gl within the group
+  int base;        // the group's first lane in the warp
+  unsigned mask;   // the group's lanes
+  __device__ __forceinline__ Grp()
+      : gl(threadIdx.x & (kG - 1)), base((threadIdx.x & 31) & ~(kG - 1)),
+        mask((kG == 32 ? 0xffffffffu : ((1u << kG) - 1u)) << ((threadIdx.x & 31) & ~(kG - 1))) {}
+  __device__ __forceinline__ unsigned ballot(bool p) const {
+    return (__ballot_sync(mask, p) >> base) & (kG == 32 ? 0xffffffffu : ((1u << kG) - 1u));
+  }
+  template <class T>
+  __device__ __forceinline__ T bcast(T v, int src) const { return __shfl_sync(mask, v, src, kG); }
+  __device__ __forceinline__ bool any(bool p) const { return __any_sync(mask, p); }
+  __device__ __forceinline__ bool all(bool p) const { return __all_sync(mask, p); }
+  __device__ __forceinline__ void sync() const { __syncwarp(mask); }
+};
 
 struct RegionScratch {
   double x[2][kCap], y[2][kCap];
@@ -32,41 +51,41 @@ struct RegionScratch {
   double cum[kCap];
 };
 
-// ring_area (polygon.cpp:58-66): the shoelace terms in parallel, their sum on lane 0 in
+// ring_area (polygon.cpp:58-66): the shoelace terms in parallel, their sum on g.gl 0 in
 // the reference's left-to-right order (bit-identical to sbp::ring_area). All lanes call;
-// every lane gets the result.
+// every g.gl gets the result.
 __device__ __noinline__ double warp_ring_area(const double* x, const double* y, int n, double* tmp) {
-  const int lane = threadIdx.x & 31;
-  for (int i = lane; i < n; i += 32) {
+  const Grp g;
+  for (int i = g.gl; i < n; i += kG) {
     const int j = i + 1 == n ? 0 : i + 1;
     tmp[i] = x[i] * y[j] - x[j] * y[i];
   }
-  __syncwarp();
+  g.sync();
   double s = 0.0;
-  if (lane == 0) {
+  if (g.gl == 0) {
 #pragma unroll 8
     for (int i = 0; i < n; ++i) s += tmp[i];
   }
-  s = __shfl_sync(kFull, s, 0);
-  __syncwarp();
+  s = g.bcast(s, 0);
+  g.sync();
   return 0.5 * s;
 }
 
-// Exclusive warp prefix count of `flag` over lanes; returns this lane's offset.
-__device__ __forceinline__ int lane_rank(bool flag, int& total) {
-  const unsigned m = __ballot_sync(kFull, flag);
+// Exclusive group prefix count of `flag` over lanes; returns this lane's offset.
+__device__ __forceinline__ int lane_rank(const Grp& g, bool flag, int& total) {
+  const unsigned m = g.ballot(flag);
   total = __popc(m);
-  return __popc(m & ((1u << (threadIdx.x & 31)) - 1u));
+  return __popc(m & ((1u << g.gl) - 1u));
 }
 
 // One Sutherland-Hodgman pass (same arithmetic and output order as sbp::clip_half);
 // returns the output size, or -1 on overflow.
 __device__ __noinline__ int warp_clip(const double* ix, const double* iy, int n, double* ox, double* oy,
                          int axis, double bound, bool keep_ge) {
-  const int lane = threadIdx.x & 31;
+  const Grp g;
   int base = 0;
-  for (int i0 = 0; i0 < n; i0 += 32) {
-    const int i = i0 + lane;
+  for (int i0 = 0; i0 < n; i0 += kG) {
+    const int i = i0 + g.gl;
     int cnt = 0;
     bool ci = false, pi = false;
     double cx = 0, cy = 0, qx = 0, qy = 0;
@@ -94,11 +113,11 @@ __device__ __noinline__ int warp_clip(const double* ix, const double* iy, int n,
     // exclusive prefix of cnt across the warp
     int incl = cnt;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const int v = __shfl_up_sync(kFull, incl, d);
-      if (lane >= d) incl += v;
+    for (int d = 1; d < kG; d <<= 1) {
+      const int v = __shfl_up_sync(g.mask, incl, d, kG);
+      if (g.gl >= d) incl += v;
     }
-    const int total = __shfl_sync(kFull, incl, 31);
+    const int total = g.bcast(incl, kG - 1);
     int pos = base + incl - cnt;
     if (base + total <= kCap && i < n) {
       if (ci != pi) {
@@ -113,7 +132,7 @@ __device__ __noinline__ int warp_clip(const double* ix, const double* iy, int n,
     }
     base += total;
   }
-  __syncwarp();
+  g.sync();
   return base <= kCap ? base : -1;
 }
 
@@ -125,7 +144,7 @@ struct RegionStats {
 // Region for one anchor state into (tris, cum) with capacity `cap`. All lanes call.
 __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double ay, double ayaw,
                                    SbRegionTri* tris, double* cum, int cap, RegionScratch& sc) {
-  const int lane = threadIdx.x & 31;
+  const Grp g;
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
   double min_r = 0.0, max_r = inf;  // distance_band (relationships.cpp:101-122)
   if (pl.distance_type == SB_DIST_GREATER) {
@@ -193,7 +212,7 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
   auto arc = [&](double radius, double a0, double a1, int off) -> int {
     const int na = arc_n(a0, a1);
     if (off + na + 1 > kCap) return -1;
-    for (int i = lane; i <= na; i += 32) {
+    for (int i = g.gl; i <= na; i += kG) {
       const double a = a0 + (a1 - a0) * (double)i / (double)na;
       double sa, ca;
       sbm::sincos_cr(a, &sa, &ca);
@@ -215,20 +234,20 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
       if (n < 0) return {sbp::kRegionOverflow, 0};
     } else {
       if (n + 1 > kCap) return {sbp::kRegionOverflow, 0};
-      if (lane == 0) {
+      if (g.gl == 0) {
         X[n] = ax;
         Y[n] = ay;
       }
       ++n;
     }
   }
-  __syncwarp();
+  g.sync();
 
   // ---- intersect with the support rect (oracle Boost stand-in): correct() orientation
   if (n < 3) return {sbp::kRegionEmpty, 0};
   const double ar = warp_ring_area(X, Y, n, sc.area);
   if (ar < 0.0) {  // reverse the closed ring: p0 stays first
-    for (int i = 1 + lane; i < n - i; i += 32) {
+    for (int i = 1 + g.gl; i < n - i; i += kG) {
       const int j = n - i;
       const double tx = X[i], ty = Y[i];
       X[i] = X[j];
@@ -236,7 +255,7 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
       X[j] = tx;
       Y[j] = ty;
     }
-    __syncwarp();
+    g.sync();
   }
   const double x0 = fmin(rc[0], rc[2]), x1 = fmax(rc[0], rc[2]);
   const double y0 = fmin(rc[1], rc[3]), y1 = fmax(rc[1], rc[3]);
@@ -251,8 +270,8 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
   double* X1 = sc.x[1];
   double* Y1 = sc.y[1];
   int m = 0;
-  for (int i0 = 0; i0 < n; i0 += 32) {
-    const int i = i0 + lane;
+  for (int i0 = 0; i0 < n; i0 += kG) {
+    const int i = i0 + g.gl;
     bool keep = false;
     double xi = 0.0, yi = 0.0;
     if (i < n) {
@@ -261,17 +280,17 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
       keep = i == 0 || xi != X[i - 1] || yi != Y[i - 1];
     }
     int tot;
-    const int r = lane_rank(keep, tot);
+    const int r = lane_rank(g, keep, tot);
     if (keep) {
       X1[m + r] = xi;
       Y1[m + r] = yi;
     }
     m += tot;
   }
-  __syncwarp();
-  if (lane == 0)
+  g.sync();
+  if (g.gl == 0)
     while (m > 1 && X1[0] == X1[m - 1] && Y1[0] == Y1[m - 1]) --m;
-  m = __shfl_sync(kFull, m, 0);
+  m = g.bcast(m, 0);
   double area1 = 0.0;
   if (m >= 3) {
     area1 = warp_ring_area(X1, Y1, m, sc.area);
@@ -282,7 +301,7 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
   // ---- triangulate (polygon.cpp:344-368) + ear_clip_ring (:260-340): orientation (same
   // ring, same area), tolerance-based duplicate drop, then the fan fast path
   if (area1 < 0.0) {
-    for (int i = lane; i < m - 1 - i; i += 32) {
+    for (int i = g.gl; i < m - 1 - i; i += kG) {
       const int j = m - 1 - i;
       const double tx = X1[i], ty = Y1[i];
       X1[i] = X1[j];
@@ -290,19 +309,19 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
       X1[j] = tx;
       Y1[j] = ty;
     }
-    __syncwarp();
+    g.sync();
   }
   // The drop compares each vertex with the last KEPT one (not transitive): if no
-  // consecutive pair is within tolerance nothing is dropped; otherwise lane 0 runs the
+  // consecutive pair is within tolerance nothing is dropped; otherwise g.gl 0 runs the
   // sequential loop.
   bool close = false;
-  for (int i = 1 + lane; i < m; i += 32) {
+  for (int i = 1 + g.gl; i < m; i += kG) {
     const double dx = X1[i] - X1[i - 1], dy = Y1[i] - Y1[i - 1];
     if (!(dx * dx + dy * dy > 1e-24)) close = true;
   }
   int k = m;
-  if (__any_sync(kFull, close)) {
-    if (lane == 0) {
+  if (g.any(close)) {
+    if (g.gl == 0) {
       k = 0;
       for (int i = 0; i < m; ++i) {
         if (k > 0) {
@@ -314,23 +333,23 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
         ++k;
       }
     }
-    k = __shfl_sync(kFull, k, 0);
-    __syncwarp();
+    k = g.bcast(k, 0);
+    g.sync();
   }
-  if (lane == 0) {
+  if (g.gl == 0) {
     while (k > 1) {
       const double dx = X1[0] - X1[k - 1], dy = Y1[0] - Y1[k - 1];
       if (dx * dx + dy * dy <= 1e-24) --k;
       else break;
     }
   }
-  k = __shfl_sync(kFull, k, 0);
-  __syncwarp();
+  k = g.bcast(k, 0);
+  g.sync();
   X = X1;
   Y = Y1;
   if (k < 3) return {sbp::kRegionOk, 0};  // valid() == false -> placeable = 0
   bool ok = true;
-  for (int i = lane; i < k; i += 32) {
+  for (int i = g.gl; i < k; i += kG) {
     const int a = i == 0 ? k - 1 : i - 1, c = i + 1 == k ? 0 : i + 1;
     if (sbp::cross2(X[a], Y[a], X[i], Y[i], X[c], Y[c]) < 0.0) ok = false;
     if (i + 3 < k) {
@@ -338,39 +357,39 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
       if (cr < 0.0 || fabs(cr) < 1e-18) ok = false;
     }
   }
-  const bool fan = __all_sync(kFull, ok);
+  const bool fan = g.all(ok);
   int ntri = 0;
   if (fan) {
     // triangle i = (k-1, i, i+1); keep area > 0 (PolygonSampler ctor, polygon.cpp:374-375):
-    // areas and output slots in parallel, the running total on lane 0 in order, the
+    // areas and output slots in parallel, the running total on g.gl 0 in order, the
     // normalisation (polygon.cpp:381-387) in parallel again.
     const int nt = k - 2;
-    int slot[(kCap + 31) / 32];
-    for (int i0 = 0, c = 0; i0 < nt; i0 += 32, ++c) {
-      const int i = i0 + lane;
+    int slot[(kCap + kG - 1) / kG];
+    for (int i0 = 0, c = 0; i0 < nt; i0 += kG, ++c) {
+      const int i = i0 + g.gl;
       double a = 0.0;
       if (i < nt) a = 0.5 * fabs(sbp::cross2(X[k - 1], Y[k - 1], X[i], Y[i], X[i + 1], Y[i + 1]));
       int tot;
-      const int r = lane_rank(a > 0.0, tot);
+      const int r = lane_rank(g, a > 0.0, tot);
       slot[c] = a > 0.0 ? ntri + r : -1;
       if (a > 0.0) sc.area[ntri + r] = a;
       ntri += tot;
     }
-    __syncwarp();
+    g.sync();
     if (ntri > cap) return {sbp::kRegionOverflow, 0};
     double total = 0.0;
-    if (lane == 0) {
+    if (g.gl == 0) {
 #pragma unroll 8
       for (int j = 0; j < ntri; ++j) {
         total += sc.area[j];
         sc.cum[j] = total;
       }
     }
-    total = __shfl_sync(kFull, total, 0);
-    __syncwarp();
+    total = g.bcast(total, 0);
+    g.sync();
     if (ntri > 0 && !(total > 0.0)) ntri = 0;
-    for (int i0 = 0, c = 0; i0 < nt; i0 += 32, ++c) {
-      const int i = i0 + lane;
+    for (int i0 = 0, c = 0; i0 < nt; i0 += kG, ++c) {
+      const int i = i0 + g.gl;
       const int j = slot[c];
       if (i < nt && j >= 0 && ntri > 0) {
         SbRegionTri& t = tris[j];
@@ -383,7 +402,7 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
         cum[j] = j == ntri - 1 ? 1.0 : sc.cum[j] / total;
       }
     }
-  } else if (lane == 0) {  // general ear clipping (reflex or sliver corners): restatement
+  } else if (g.gl == 0) {  // general ear clipping (reflex or sliver corners): restatement
     sbp::Ring r;
     r.n = k;
     for (int i = 0; i < k; ++i) {
@@ -394,8 +413,8 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
     if (!sbp::ear_clip_into(r, sink)) ntri = -1;
     else ntri = sbp::finish_table(sink);
   }
-  ntri = __shfl_sync(kFull, ntri, 0);
-  __syncwarp();
+  ntri = g.bcast(ntri, 0);
+  g.sync();
   if (ntri < 0) return {sbp::kRegionOverflow, 0};
   return {sbp::kRegionOk, ntri};
 }
@@ -406,10 +425,10 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
 // shard owns global instance 0, is recomputed per warp from local instance 0.
 __global__ void __launch_bounds__(kRB) k_relation_regions(RelationRegionParams p) {
   __shared__ RegionScratch scratch[kRW];
-  const int lane = threadIdx.x & 31;
-  const uint64_t warp = (blockIdx.x * (uint64_t)kRB + threadIdx.x) >> 5;
+  const Grp g;
+  const uint64_t warp = (blockIdx.x * (uint64_t)kRB + threadIdx.x) / kG;  // instance group
   const uint64_t nwarps = (uint64_t)gridDim.x * kRW;
-  RegionScratch& sc = scratch[threadIdx.x >> 5];
+  RegionScratch& sc = scratch[threadIdx.x / kG];
   M34 inv;
 #pragma unroll
   for (int k = 0; k < 12; ++k) inv.m[k] = p.inv_support[k];
@@ -428,7 +447,7 @@ __global__ void __launch_bounds__(kRB) k_relation_regions(RelationRegionParams p
   if (p.from_s0) {  // canonical region_for(0) from the exchanged instance-0 state
     if (warp == 0) {
       const RegionStats r = warp_region(p.pl, p.s0[0], p.s0[1], p.s0[2], p.tris, p.cum, p.cap, sc);
-      if (lane == 0) {
+      if (g.gl == 0) {
         const bool good = r.status == sbp::kRegionOk || r.status == sbp::kRegionEmpty;
         p.ntri[0] = good ? r.ntri : 0;
         if (!good) atomicMax(p.flags + 1, r.status);
@@ -463,13 +482,13 @@ __global__ void __launch_bounds__(kRB) k_relation_regions(RelationRegionParams p
     vary = vary || pos_vary;
     const RegionStats r = warp_region(p.pl, ax, ay, ayaw, p.tris + i * p.cap, p.cum + i * p.cap,
                                       p.cap, sc);
-    if (lane == 0) {
+    if (g.gl == 0) {
       p.ntri[i] = r.status == sbp::kRegionOk || r.status == sbp::kRegionEmpty ? r.ntri : 0;
       if (r.status != sbp::kRegionOk && r.status != sbp::kRegionEmpty && r.status > worst)
         worst = r.status;
     }
   }
-  if (lane == 0) {
+  if (g.gl == 0) {
     if (vary) atomicOr(p.flags + 0, 1);
     if (worst) atomicMax(p.flags + 1, worst);
   }
