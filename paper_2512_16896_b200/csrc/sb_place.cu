@@ -172,12 +172,17 @@ __device__ __forceinline__ void narrow_drain(const PlaceParams& p, Tile& T, Fixe
     return *((volatile int32_t*)T.contact + v) < ob ||
            v / (int)nt > *((volatile int32_t*)T.minfree + v % (int)nt);
   };
-  auto next_eligible = [&](uint32_t q) {  // first non-skippable entry at q, q + 8, ...
-    for (; q < qn; q += kWarps) {
+  // Pairs are claimed one at a time from a shared counter (F.qhead, zeroed by the caller),
+  // so a warp that drew cheap pairs (skips, early exits) takes more of them.
+  auto claim = [&]() -> uint32_t {  // next non-skippable queue index, or qn
+    for (;;) {
+      uint32_t q = 0;
+      if (lane == 0) q = atomicAdd(&F.qhead, 1u);
+      q = __shfl_sync(kFull, q, 0);
+      if (q >= qn) return qn;
       const uint32_t ent = T.queue[q];
-      if (!skippable((int)(ent >> 24), (int)(ent & 0xffffffu))) break;
+      if (!skippable((int)(ent >> 24), (int)(ent & 0xffffffu))) return q;
     }
-    return q;
   };
   auto stage = [&](uint32_t ent, int buf) {
     const int v = (int)(ent >> 24), ob = (int)(ent & 0xffffffu);
@@ -185,11 +190,11 @@ __device__ __forceinline__ void narrow_drain(const PlaceParams& p, Tile& T, Fixe
                stage_buf(wsb, p.max_tris, p.max_nodes, buf));
   };
   int cur = 0;
-  uint32_t q = next_eligible(warp);
+  uint32_t q = claim();
   if (q < qn) stage(T.queue[q], cur);
   while (q < qn) {
     const uint32_t ent_cur = T.queue[q];
-    const uint32_t q2 = next_eligible(q + kWarps);
+    const uint32_t q2 = claim();
     if (q2 < qn) {
       stage(T.queue[q2], cur ^ 1);
       cp_async_wait<1>();
@@ -329,6 +334,7 @@ __device__ uint32_t tile_round(const PlaceParams& p, const Sampling& S, const Sb
   }
   if (tid == 0) {
     F.qn = 0;
+    F.qhead = 0;
     F.dq = F.dt = 0;
   }
   __syncthreads();
@@ -397,7 +403,10 @@ __device__ uint32_t tile_round(const PlaceParams& p, const Sampling& S, const Sb
         if (p.dbg_inst && tid == 0) F.dq += qn;
         narrow_drain(p, T, F, nt, qn, L);
         __syncthreads();
-        if (tid == 0) F.qn = 0;
+        if (tid == 0) {
+          F.qn = 0;
+          F.qhead = 0;
+        }
         __syncthreads();
       }
     }
@@ -448,7 +457,10 @@ __device__ uint32_t tile_round(const PlaceParams& p, const Sampling& S, const Sb
         }
       }
     }
-    if (tid == 0) F.qn = 0;
+    if (tid == 0) {
+          F.qn = 0;
+          F.qhead = 0;
+        }
     __syncthreads();
     {  // item-parallel AABB tests, two box loads in flight per thread
       constexpr int kI = kCand / kB;
