@@ -275,6 +275,9 @@ sb_status sb_device_math(int fn, const double* in, uint64_t n, double* out);
  * unless the library was built with -DSB_NARROW_PROF): pose+M, node tests, triangle
  * transform, DAG walk, triangle tests, pairs. */
 sb_status sb_debug_narrow_profile(uint64_t out[8]);
+/* Diagnostics: stage cycle profile of the relation-region kernel (sb_region.cu; zeros
+ * unless the library is built with -DSB_REGION_PROF); read and reset. */
+sb_status sb_debug_region_profile(uint64_t out[8]);
 
 #ifdef __cplusplus
 }

@@ -125,6 +125,7 @@ SIGNATURES = {
     "sb_engine_last_launches": (C.c_uint64, [_P]),
     "sb_engine_last_timing": (C.c_int, [_P, _D, _D, C.POINTER(C.c_uint64)]),
     "sb_engine_phase_profile": (C.c_int, [_P, _D]),
+    "sb_debug_region_profile": (C.c_int, [C.POINTER(C.c_uint64)]),
     "sb_device_math": (C.c_int, [C.c_int, _D, C.c_uint64, _D]),
     "sb_debug_narrow_profile": (C.c_int, [C.POINTER(C.c_uint64)]),
 }

@@ -45,6 +45,19 @@ struct Grp {
   __device__ __forceinline__ void sync() const { __syncwarp(mask); }
 };
 
+// Optional stage cycle profile (build with -DSB_REGION_PROF): [0] anchor state, [1] band /
+// direction / bounds, [2] arc points, [3] orientation + 4 clips, [4] dedupe + area,
+// [5] triangulate + fan test, [6] sampler table, [7] instances.
+__device__ unsigned long long g_rprof[8];
+#ifdef SB_REGION_PROF
+#define SB_RP_MARK(var) const long long var = clock64()
+#define SB_RP_ADD(k, a, b) \
+  if (g.gl == 0) atomicAdd(&g_rprof[k], (unsigned long long)((b) - (a)))
+#else
+#define SB_RP_MARK(var)
+#define SB_RP_ADD(k, a, b)
+#endif
+
 struct RegionScratch {
   double x[2][kCap], y[2][kCap];
   double area[kCap];
@@ -110,7 +123,7 @@ __device__ __noinline__ int warp_clip(const double* ix, const double* iy, int n,
         ++cnt;
       }
     }
-    // exclusive prefix of cnt across the warp
+    // exclusive prefix of cnt across the group
     int incl = cnt;
 #pragma unroll
     for (int d = 1; d < kG; d <<= 1) {
@@ -145,6 +158,7 @@ struct RegionStats {
 __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double ay, double ayaw,
                                    SbRegionTri* tris, double* cum, int cap, RegionScratch& sc) {
   const Grp g;
+  SB_RP_MARK(rp0);
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
   double min_r = 0.0, max_r = inf;  // distance_band (relationships.cpp:101-122)
   if (pl.distance_type == SB_DIST_GREATER) {
@@ -195,6 +209,8 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
   const double ddx = bx1 - bx0, ddy = by1 - by0;
   const double diag = bx0 > bx1 ? 0.0 : sqrt(ddx * ddx + ddy * ddy);
 
+  SB_RP_MARK(rp1);
+  SB_RP_ADD(1, rp0, rp1);
   // ---- annulus_sector (polygon.cpp:136-176), arc points in parallel
   if (!(theta > 0.0) || theta > pi + 1e-12) return {sbp::kRegionBadArg, 0};
   if (isinf(max_r)) max_r = fmax(diag, min_r + 1e-6);
@@ -243,6 +259,8 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
   }
   g.sync();
 
+  SB_RP_MARK(rp2);
+  SB_RP_ADD(2, rp1, rp2);
   // ---- intersect with the support rect (oracle Boost stand-in): correct() orientation
   if (n < 3) return {sbp::kRegionEmpty, 0};
   const double ar = warp_ring_area(X, Y, n, sc.area);
@@ -264,6 +282,8 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
   if (n >= 0) n = warp_clip(sc.x[0], sc.y[0], n, sc.x[1], sc.y[1], 1, y0, true);
   if (n >= 0) n = warp_clip(sc.x[1], sc.y[1], n, sc.x[0], sc.y[0], 1, y1, false);
   if (n < 0) return {sbp::kRegionOverflow, 0};
+  SB_RP_MARK(rp3);
+  SB_RP_ADD(3, rp2, rp3);
   // drop consecutive exact duplicates (keep the first of each run; == is transitive, so
   // comparing with the previous vertex equals comparing with the last kept one), then
   // trailing copies of vertex 0. Out of place: buffer 0 -> buffer 1.
@@ -298,6 +318,8 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
   }
   if (m < 3) return {sbp::kRegionEmpty, 0};
 
+  SB_RP_MARK(rp4);
+  SB_RP_ADD(4, rp3, rp4);
   // ---- triangulate (polygon.cpp:344-368) + ear_clip_ring (:260-340): orientation (same
   // ring, same area), tolerance-based duplicate drop, then the fan fast path
   if (area1 < 0.0) {
@@ -358,6 +380,8 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
     }
   }
   const bool fan = g.all(ok);
+  SB_RP_MARK(rp5);
+  SB_RP_ADD(5, rp4, rp5);
   int ntri = 0;
   if (fan) {
     // triangle i = (k-1, i, i+1); keep area > 0 (PolygonSampler ctor, polygon.cpp:374-375):
@@ -416,6 +440,9 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
   ntri = g.bcast(ntri, 0);
   g.sync();
   if (ntri < 0) return {sbp::kRegionOverflow, 0};
+  SB_RP_MARK(rp6);
+  SB_RP_ADD(6, rp5, rp6);
+  SB_RP_ADD(7, 0, 1);
   return {sbp::kRegionOk, ntri};
 }
 
@@ -468,6 +495,7 @@ __global__ void __launch_bounds__(kRB) k_relation_regions(RelationRegionParams p
   bool vary = false;
   int worst = 0;
   for (uint64_t i = warp; i < p.w.n; i += nwarps) {
+    SB_RP_MARK(ra0);
     M34 rel;
     rel_of(i, rel);
     const double ax = rel.m[3], ay = rel.m[7];
@@ -480,6 +508,8 @@ __global__ void __launch_bounds__(kRB) k_relation_regions(RelationRegionParams p
       vary = vary || fabs(ayaw - yaw0) > 1e-12;
     }
     vary = vary || pos_vary;
+    SB_RP_MARK(ra1);
+    SB_RP_ADD(0, ra0, ra1);
     const RegionStats r = warp_region(p.pl, ax, ay, ayaw, p.tris + i * p.cap, p.cum + i * p.cap,
                                       p.cap, sc);
     if (g.gl == 0) {
@@ -495,6 +525,15 @@ __global__ void __launch_bounds__(kRB) k_relation_regions(RelationRegionParams p
 }
 
 }  // namespace
+
+void region_profile(unsigned long long out[8], bool reset) {
+  if (cudaMemcpyFromSymbol(out, g_rprof, 8 * sizeof(unsigned long long)) != cudaSuccess)
+    throw std::runtime_error("region_profile");
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (cudaMemcpyToSymbol(g_rprof, z, sizeof z) != cudaSuccess) throw std::runtime_error("region_profile reset");
+  }
+}
 
 void relation_regions(const RelationRegionParams& p, int num_sms, sb_stream_t s) {
   unsigned blocks = (unsigned)((p.w.n + kRW - 1) / kRW);

@@ -23,6 +23,8 @@ struct RelationRegionParams {
   int32_t* flags;          // [0] |= anchors vary, [1] = max region error status
 };
 
+// Stage cycle profile of the region kernel (zeros unless built with -DSB_REGION_PROF).
+void region_profile(unsigned long long out[8], bool reset);
 void relation_regions(const RelationRegionParams& p, int num_sms, sb_stream_t s);
 
 }  // namespace sbk

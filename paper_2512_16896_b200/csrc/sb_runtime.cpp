@@ -1328,6 +1328,14 @@ sb_status sb_debug_narrow_profile(uint64_t out[8]) {
   });
 }
 
+sb_status sb_debug_region_profile(uint64_t out[8]) {
+  return guard([&] {
+    unsigned long long v[8];
+    sbk::region_profile(v, true);
+    for (int k = 0; k < 8; ++k) out[k] = v[k];
+  });
+}
+
 sb_status sb_device_math(int fn, const double* in, uint64_t n, double* out) {
   return guard([&] {
     if (fn < 0 || fn > 2) throw std::invalid_argument("sb_device_math: fn must be 0, 1 or 2");

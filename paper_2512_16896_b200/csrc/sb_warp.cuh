@@ -375,8 +375,8 @@ __device__ __forceinline__ bool warp_collide(const GC& gc, const unsigned char* 
     n1 = warp_append(pass, (uint16_t)k, ws.l1, n1);
   }
   __syncwarp();
-  SB_NP_MARK(np1b);
-  SB_NP_ADD(6, np1a, np1b);
+  SB_NP_MARK(np1b_);
+  SB_NP_ADD(6, np1a, np1b_);
   int n2 = 0;
   for (int j0 = 0; j0 < n1; j0 += 32) {
     const int j = j0 + lane;
@@ -411,7 +411,7 @@ __device__ __forceinline__ bool warp_collide(const GC& gc, const unsigned char* 
   }
   }  // margin == 0
   SB_NP_MARK(np2);
-  SB_NP_ADD(7, np1b, np2);
+  SB_NP_ADD(7, np1a, np2);  // filter 1 + filter 2 + rest (filter 1 alone in slot 6)
   if (!any) return false;
   __syncwarp();
 
