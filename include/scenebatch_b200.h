@@ -266,6 +266,41 @@ sb_status sb_engine_last_timing(const sb_engine* e, double* total_ms, double* ch
  * per-instance / fast-path placements, out[12..14] = debug maxima (SB_ROUND_DEBUG). */
 sb_status sb_engine_phase_profile(const sb_engine* e, double out[16]);
 
+/* ------------------------------------------------------------------------------------
+ * PositionSampler (sampler.hpp:66-96) and sample_orientations (sampler.hpp:98-104) as
+ * standalone device-backed calls, for callers that drive their own attempt loop.
+ * Regions are given as hole-free rings (x,y pairs; ring r = vertices
+ * [ring_offsets[r], ring_offsets[r+1]), at most 96 vertices). instance_rings == NULL:
+ * canonical region (ConstraintRegion::region = all rings, the FIFO-cache fast path);
+ * else per-instance regions (instance i = rings [instance_rings[i], instance_rings[i+1]),
+ * batch_size + 1 entries; sampler.cpp:101-126). Host buffers in and out.
+ * ---------------------------------------------------------------------------------- */
+typedef struct sb_sampler sb_sampler;
+/* PositionSampler(placement_salt) (sampler.hpp:73) on `device`. */
+sb_status sb_sampler_create(uint64_t placement_salt, int device, sb_sampler** out);
+void sb_sampler_destroy(sb_sampler* s);
+/* prepare(constraint, batch_size, run_seed) (sampler.cpp:54-67): rebinds the cache to the
+ * stream of run_seed (the queue survives a re-prepare with the same seed) and restarts
+ * the cache rng. n_rings == 0 is an empty region (every sample is not placeable). */
+sb_status sb_sampler_prepare(sb_sampler* s, const double* ring_xy, const uint32_t* ring_offsets,
+                             uint32_t n_rings, const uint32_t* instance_rings,
+                             uint64_t batch_size, uint64_t run_seed);
+/* sample(support_world, active, attempt, positions, placeable) (sampler.cpp:69-127):
+ * support_world = batch_size column-major Mat4 (16 doubles each); positions_xyz = 3 doubles
+ * per active entry. A canonical region with zero area is SB_ERR_INVALID_ARGUMENT (the
+ * reference draws from an empty table there). */
+sb_status sb_sampler_sample(sb_sampler* s, const double* support_colmajor16xN,
+                            const uint32_t* active, uint64_t m, uint64_t attempt,
+                            double* positions_xyz, uint8_t* placeable);
+/* SampleCache state (sampler.hpp:18-36): points queued, refills so far. */
+sb_status sb_sampler_cache_info(const sb_sampler* s, uint64_t* queue_size, uint64_t* refill_count);
+/* sample_orientations (sampler.cpp:129-156): kind = SB_ORIENT_*; face_targets_xy = one
+ * (x, y) per instance (n_targets of them, SB_ORIENT_FACE_TO only, else NULL). */
+sb_status sb_sample_orientations(int kind, const uint32_t* active, uint64_t m,
+                                 const double* positions_xyz, const double* face_targets_xy,
+                                 uint64_t n_targets, uint64_t run_seed, uint64_t placement_salt,
+                                 uint64_t attempt, double* yaws, int device);
+
 /* Diagnostics: evaluate the device libm used on the hot path (correctly rounded
  * double-double sin/cos/atan2, replacing glibc's std::sin/cos/atan2 in transform.hpp:47,
  * polygon.cpp:151, relationships.cpp:184,238) on n inputs on device 0.

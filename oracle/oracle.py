@@ -84,6 +84,15 @@ def lib():
         L.ref_get_stats.argtypes = [C.c_void_p, C.c_void_p]
         L.ref_generate.argtypes = [C.c_void_p, C.c_void_p, u64, C.c_int, C.c_void_p, C.c_void_p,
                                    C.c_void_p, C.c_void_p]
+        L.ref_sampler_create.restype = C.c_void_p
+        L.ref_sampler_create.argtypes = [u64]
+        L.ref_sampler_destroy.argtypes = [C.c_void_p]
+        L.ref_sampler_prepare.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32,
+                                          C.c_void_p, u64, u64]
+        L.ref_sampler_sample.argtypes = [C.c_void_p, C.c_void_p, u64, C.c_void_p, u64, u64,
+                                         C.c_void_p, C.c_void_p, C.c_void_p]
+        L.ref_sample_orientations.argtypes = [C.c_int, C.c_void_p, u64, C.c_void_p, C.c_void_p,
+                                              u64, u64, u64, u64, C.c_void_p]
         _lib = L
     return _lib
 
@@ -260,3 +269,54 @@ def generate(scene, run_seed: int, threads: int = 1, shard=None, with_poses: boo
     check(rc)
     stats = {k: getattr(st, k) for k, _ in A.sb_run_stats._fields_}
     return {"accepted": acc, "valid": valid, "poses": poses, "stats": stats}
+
+
+def _rings(rings):
+    """List of rings ((k, 2) xy arrays) -> flat xy (float64) and offsets (uint32)."""
+    xy = np.ascontiguousarray(np.concatenate([np.asarray(r, np.float64).reshape(-1, 2) for r in rings])
+                              if rings else np.zeros((0, 2)), dtype=np.float64)
+    off = np.zeros(len(rings) + 1, np.uint32)
+    for i, r in enumerate(rings):
+        off[i + 1] = off[i] + len(r)
+    return xy, off
+
+
+class RefSampler:
+    """The reference's PositionSampler (sampler.hpp:71-96) over a region given as rings."""
+
+    def __init__(self, salt: int):
+        self.h = lib().ref_sampler_create(salt)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().ref_sampler_destroy(self.h)
+            self.h = None
+
+    def prepare(self, rings, n: int, run_seed: int, instance_rings=None):
+        self._xy, self._off = _rings(rings)
+        self._inst = None if instance_rings is None else np.ascontiguousarray(instance_rings, np.uint32)
+        check(lib().ref_sampler_prepare(self.h, _p(self._xy), _p(self._off), len(rings),
+                                        None if self._inst is None else _p(self._inst), n, run_seed))
+
+    def sample(self, support16: np.ndarray, active, attempt: int):
+        sw = np.ascontiguousarray(support16, np.float64)
+        act = np.ascontiguousarray(active, np.uint32)
+        pos = np.zeros((len(act), 3))
+        pl = np.zeros(len(act), np.uint8)
+        rc = C.c_uint64()
+        check(lib().ref_sampler_sample(self.h, _p(sw), sw.shape[0], _p(act), len(act), attempt,
+                                       _p(pos), _p(pl), C.byref(rc)))
+        return pos, pl, rc.value
+
+
+def sample_orientations(kind: int, active, positions, face_xy, run_seed: int, salt: int,
+                        attempt: int) -> np.ndarray:
+    act = np.ascontiguousarray(active, np.uint32)
+    pos = np.ascontiguousarray(positions, np.float64)
+    fx = None if face_xy is None else np.ascontiguousarray(face_xy, np.float64)
+    y = np.zeros(len(act))
+    check(lib().ref_sample_orientations(kind, _p(act), len(act), _p(pos),
+                                        None if fx is None else _p(fx),
+                                        0 if fx is None else fx.shape[0], run_seed, salt, attempt,
+                                        _p(y)))
+    return y

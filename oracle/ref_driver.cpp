@@ -218,6 +218,84 @@ int ref_relation_region(const sb_relation* rel, const double* rect, double ax, d
   });
 }
 
+
+// ---------------------------------------------------------------- PositionSampler (sampler.hpp:71-96)
+// Region input: n_rings outer rings (xy, ring_offsets[n_rings + 1] in points); canonical
+// region = all rings; per_instance: instance i's region = rings [inst_rings[i], inst_rings[i+1]).
+struct RefSampler {
+  PositionSampler sampler;
+  ConstraintRegion region;
+  explicit RefSampler(uint64_t salt) : sampler(salt) {}
+};
+static MultiPolygon2D rings_to_region(const double* xy, const uint32_t* off, uint32_t r0, uint32_t r1) {
+  MultiPolygon2D m;
+  for (uint32_t r = r0; r < r1; ++r) {
+    Polygon2D poly;
+    for (uint32_t k = off[r]; k < off[r + 1]; ++k) poly.exterior.emplace_back(xy[2 * k], xy[2 * k + 1]);
+    m.parts.push_back(std::move(poly));
+  }
+  return m;
+}
+void* ref_sampler_create(uint64_t salt) { return new RefSampler(salt); }
+void ref_sampler_destroy(void* h) { delete static_cast<RefSampler*>(h); }
+int ref_sampler_prepare(void* h, const double* xy, const uint32_t* ring_offsets, uint32_t n_rings,
+                        const uint32_t* inst_rings, uint64_t n, uint64_t run_seed) {
+  REF_TRY({
+    RefSampler& s = *static_cast<RefSampler*>(h);
+    s.region = ConstraintRegion();
+    if (inst_rings) {
+      s.region.per_instance = true;
+      for (uint64_t i = 0; i < n; ++i)
+        s.region.regions_by_instance.push_back(rings_to_region(xy, ring_offsets, inst_rings[i], inst_rings[i + 1]));
+      s.region.region = s.region.regions_by_instance.empty() ? MultiPolygon2D() : s.region.regions_by_instance[0];
+    } else {
+      s.region.region = rings_to_region(xy, ring_offsets, 0, n_rings);
+    }
+    s.sampler.prepare(&s.region, n, run_seed);
+  });
+}
+// support16: N column-major Mat4; positions: 3 per active entry
+int ref_sampler_sample(void* h, const double* support16, uint64_t n, const uint32_t* active,
+                       uint64_t m, uint64_t attempt, double* positions, uint8_t* placeable,
+                       uint64_t* refill_count) {
+  REF_TRY({
+    RefSampler& s = *static_cast<RefSampler*>(h);
+    TransformBatch sw(n);
+    for (uint64_t i = 0; i < n; ++i)
+      for (int c = 0; c < 4; ++c)
+        for (int r = 0; r < 4; ++r) sw[i](r, c) = support16[16 * i + 4 * c + r];
+    std::vector<Vec3> pos;
+    std::vector<uint8_t> pl;
+    s.sampler.sample(sw, std::span<const uint32_t>(active, m), attempt, pos, pl);
+    for (uint64_t j = 0; j < m; ++j) {
+      positions[3 * j] = pos[j].x();
+      positions[3 * j + 1] = pos[j].y();
+      positions[3 * j + 2] = pos[j].z();
+      placeable[j] = pl[j];
+    }
+    if (refill_count) *refill_count = s.sampler.cache().refill_count;
+  });
+}
+// sample_orientations (sampler.cpp:129-156); kind 0 fixed, 1 uniform_yaw, 2 face_to;
+// face_xy: N targets (face_to only)
+int ref_sample_orientations(int kind, const uint32_t* active, uint64_t m, const double* positions,
+                            const double* face_xy, uint64_t n, uint64_t run_seed, uint64_t salt,
+                            uint64_t attempt, double* yaws) {
+  REF_TRY({
+    OrientationRule rule;
+    rule.kind = kind == 1 ? OrientationRule::Kind::uniform_yaw
+                          : (kind == 2 ? OrientationRule::Kind::face_to : OrientationRule::Kind::fixed);
+    std::vector<Vec3> pos(m);
+    for (uint64_t j = 0; j < m; ++j) pos[j] = Vec3(positions[3 * j], positions[3 * j + 1], positions[3 * j + 2]);
+    std::vector<Vec2> targets;
+    if (face_xy)
+      for (uint64_t i = 0; i < n; ++i) targets.emplace_back(face_xy[2 * i], face_xy[2 * i + 1]);
+    auto y = sample_orientations(rule, std::span<const uint32_t>(active, m), pos,
+                                 face_xy ? &targets : nullptr, run_seed, salt, attempt);
+    for (uint64_t j = 0; j < m; ++j) yaws[j] = y[j];
+  });
+}
+
 // ---------------------------------------------------------------- CollisionWorld
 void* ref_world_create(uint64_t n, double margin, int threads) {
   try {

@@ -14,6 +14,7 @@ Slow by design (pure Python loops): use small N and few objects.
 from __future__ import annotations
 
 import math
+import struct
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence, Tuple
 
@@ -697,6 +698,94 @@ class PolygonSampler:  # polygon.cpp:370-400
         s = math.sqrt(r1)
         wa, wb, wc = 1.0 - s, s * (1.0 - r2), s * r2
         return ((a[0] * wa + b[0] * wb) + c[0] * wc, (a[1] * wa + b[1] * wb) + c[1] * wc)
+
+
+def region_fingerprint(parts) -> int:  # polygon.cpp:422-444 (hole-free parts)
+    h = 0x9E3779B97F4A7C15
+    for ring in parts:
+        h = mix64(h ^ len(ring))
+        for x, y in ring:
+            h = mix64(h ^ struct.unpack("<Q", struct.pack("<d", x))[0])
+            h = mix64(h ^ struct.unpack("<Q", struct.pack("<d", y))[0])
+    return h
+
+
+class SampleCache:  # sampler.hpp:18-36, refill_cache / drain_cache (sampler.cpp:14-43)
+    def __init__(self):
+        self.refill_factor, self.fingerprint, self.stream = 4.0, 0, 0
+        self.sampler, self.queue, self.refill_count = None, [], 0
+
+    def bind_stream(self, key: int):
+        if self.stream != key:
+            self.queue = []
+            self.stream = key
+
+    def refill(self, parts, n: int, rng: Pcg32):
+        fp = region_fingerprint(parts)
+        if fp != self.fingerprint:
+            self.queue = []
+            self.sampler = PolygonSampler(parts)
+            self.fingerprint = fp
+        target = max(int(self.refill_factor * float(n)), n)
+        if len(self.queue) >= target:
+            return
+        for _ in range(target - len(self.queue)):
+            self.queue.append(self.sampler.draw(rng))
+        self.refill_count += 1
+
+    def drain(self, parts, k: int, rng: Pcg32):
+        if region_fingerprint(parts) != self.fingerprint or len(self.queue) < k:
+            self.refill(parts, max(k, 1), rng)
+        out, self.queue = self.queue[:k], self.queue[k:]
+        return out
+
+
+class PositionSampler:  # sampler.cpp:54-127; region: list of rings or per-instance lists
+    def __init__(self, salt: int):
+        self.salt, self.cache = salt, SampleCache()
+
+    def prepare(self, region, n: int, run_seed: int, per_instance: bool = False):
+        self.region, self.per_instance, self.n, self.run_seed = region, per_instance, n, run_seed
+        self.cache.bind_stream(stream_key([run_seed, self.salt, CACHE_SALT]))
+        self.rng = make_stream(run_seed, [self.salt, CACHE_SALT])
+        self.fallback = [None] * n if per_instance else []
+
+    def sample(self, support_rows, active, attempt: int):
+        """support_rows[i]: 3x4 row-major support pose of instance i."""
+        pos, placeable = [(0.0, 0.0, 0.0)] * len(active), [1] * len(active)
+        if not self.per_instance:
+            if not self.region:
+                return pos, [0] * len(active)
+            pts = self.cache.drain(self.region, len(active), self.rng)
+            for j, inst in enumerate(active):
+                pos[j] = xform(support_rows[inst], (pts[j][0], pts[j][1], 0.0))
+            return pos, placeable
+        for j, inst in enumerate(active):
+            reg = self.region[inst]
+            if not reg:
+                placeable[j] = 0
+                continue
+            if self.fallback[inst] is None:
+                self.fallback[inst] = PolygonSampler(reg)
+            if not self.fallback[inst].valid():
+                placeable[j] = 0
+                continue
+            p = self.fallback[inst].draw(make_stream(self.run_seed, [self.salt, FALL_SALT, inst, attempt]))
+            pos[j] = xform(support_rows[inst], (p[0], p[1], 0.0))
+        return pos, placeable
+
+
+def sample_orientations(kind: int, active, positions, face_targets, run_seed: int, salt: int,
+                        attempt: int):  # sampler.cpp:129-156; kind 0 fixed, 1 uniform, 2 face_to
+    yaws = [0.0] * len(active)
+    for j, inst in enumerate(active):
+        if kind == 1:
+            yaws[j] = make_stream(run_seed, [salt, YAW_SALT, inst, attempt]).uniform(0.0, 2.0 * math.pi)
+        elif kind == 2:  # face_to_yaw (relationships.cpp:232-239)
+            dx = face_targets[inst][0] - positions[j][0]
+            dy = face_targets[inst][1] - positions[j][1]
+            yaws[j] = 0.0 if math.sqrt(dx * dx + dy * dy) < 1e-12 else math.atan2(dy, dx)
+    return yaws
 
 
 def rect_ring(x0, y0, x1, y1):  # make_rect (polygon.cpp:84-88)

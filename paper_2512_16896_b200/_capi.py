@@ -128,6 +128,14 @@ SIGNATURES = {
     "sb_debug_region_profile": (C.c_int, [C.POINTER(C.c_uint64)]),
     "sb_device_math": (C.c_int, [C.c_int, _D, C.c_uint64, _D]),
     "sb_debug_narrow_profile": (C.c_int, [C.POINTER(C.c_uint64)]),
+    "sb_sampler_create": (C.c_int, [C.c_uint64, C.c_int, C.POINTER(_P)]),
+    "sb_sampler_destroy": (None, [_P]),
+    "sb_sampler_prepare": (C.c_int, [_P, _D, _U32, C.c_uint32, _U32, C.c_uint64, C.c_uint64]),
+    "sb_sampler_sample": (C.c_int, [_P, _D, _U32, C.c_uint64, C.c_uint64, _D,
+                                    C.POINTER(C.c_uint8)]),
+    "sb_sampler_cache_info": (C.c_int, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "sb_sample_orientations": (C.c_int, [C.c_int, _U32, C.c_uint64, _D, _D, C.c_uint64,
+                                         C.c_uint64, C.c_uint64, C.c_uint64, _D, C.c_int]),
 }
 
 _lib = None

@@ -8,6 +8,7 @@
 #include "sb_crmath.cuh"
 #include "sb_dev.cuh"
 #include "sb_kernels.h"
+#include "sb_poly.h"
 #include "sb_warp.cuh"
 
 using namespace sbd;
@@ -196,6 +197,85 @@ __global__ void k_debug_math(int fn, const double* in, uint64_t n, double* out) 
   }
 }
 
+// ------------------------------------------------------------ standalone PositionSampler
+// Fast path (sampler.cpp:78-97): the j-th active entry takes FIFO point j, which is draw
+// number seg_draw[s] + (j - seg_first[s]) of the cache stream (the host keeps the queue as
+// draw-index ranges, SampleCache semantics). Draw d = 6d PCG steps in (polygon.cpp:390-400).
+__global__ void k_sampler_fifo(const double* sup34, uint64_t m, const uint64_t* seg_first,
+                               const uint64_t* seg_draw, int nseg, uint64_t state0,
+                               const SbRegionTri* tris, const double* cum, int nt, double* pos) {
+  const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  int lo = 0, hi = nseg - 1;  // last segment with seg_first <= j
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(seg_first + mid) <= j) lo = mid;
+    else hi = mid - 1;
+  }
+  Pcg r{state0};
+  r.advance(6ull * (__ldg(seg_draw + lo) + (j - __ldg(seg_first + lo))));
+  const double u = r.next_double(), r1 = r.next_double(), r2 = r.next_double();
+  double lx, ly;
+  sbp::draw_point(tris, cum, nt, u, r1, r2, lx, ly);
+  M34 S;
+#pragma unroll
+  for (int k = 0; k < 12; ++k) S.m[k] = __ldg(sup34 + 12 * j + k);
+  double px, py, pz;
+  xform(S, lx, ly, 0.0, px, py, pz);  // transform_point(support_world[inst], (x, y, 0))
+  pos[3 * j] = px;
+  pos[3 * j + 1] = py;
+  pos[3 * j + 2] = pz;
+}
+
+// Per-instance regions (sampler.cpp:101-126): one draw from instance inst's own table on
+// make_stream(run_seed, {salt, "fall", inst, attempt}); an empty table -> not placeable.
+__global__ void k_sampler_fallback(const double* sup34, const uint32_t* active, uint64_t m,
+                                   uint64_t run_seed, uint64_t salt, uint64_t attempt,
+                                   const uint32_t* inst_tab, const SbRegionTri* tris,
+                                   const double* cum, double* pos, uint8_t* placeable) {
+  const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  const uint32_t inst = __ldg(active + j);
+  const uint32_t o0 = __ldg(inst_tab + 2 * inst), nt = __ldg(inst_tab + 2 * inst + 1);
+  double px = 0.0, py = 0.0, pz = 0.0;
+  if (nt > 0) {
+    Pcg r = Pcg::seeded(stream_seed4(run_seed, salt, kFallbackSalt, inst, attempt));
+    const double u = r.next_double(), r1 = r.next_double(), r2 = r.next_double();
+    double lx, ly;
+    sbp::draw_point(tris + o0, cum + o0, (int)nt, u, r1, r2, lx, ly);
+    M34 S;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) S.m[k] = __ldg(sup34 + 12 * j + k);
+    xform(S, lx, ly, 0.0, px, py, pz);
+  }
+  pos[3 * j] = px;
+  pos[3 * j + 1] = py;
+  pos[3 * j + 2] = pz;
+  placeable[j] = nt > 0 ? 1 : 0;
+}
+
+// sample_orientations (sampler.cpp:129-156): kind 1 = uniform_yaw on
+// make_stream(run_seed, {salt, "yaw!", inst, attempt}); kind 2 = face_to_yaw
+// (relationships.cpp:232-239) toward face_xy[inst] with the correctly rounded atan2.
+__global__ void k_orientations(int kind, const uint32_t* active, uint64_t m, const double* pos,
+                               const double* face_xy, uint64_t run_seed, uint64_t salt,
+                               uint64_t attempt, double* yaws) {
+  const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  const uint32_t inst = __ldg(active + j);
+  double yaw = 0.0;
+  if (kind == SB_ORIENT_UNIFORM_YAW) {
+    Pcg r = Pcg::seeded(stream_seed4(run_seed, salt, kYawSalt, inst, attempt));
+    const double two_pi = 2.0 * 3.14159265358979323846;
+    yaw = 0.0 + (two_pi - 0.0) * r.next_double();
+  } else if (kind == SB_ORIENT_FACE_TO) {
+    const double dx = __ldg(face_xy + 2 * inst) - __ldg(pos + 3 * j);
+    const double dy = __ldg(face_xy + 2 * inst + 1) - __ldg(pos + 3 * j + 1);
+    yaw = sqrt(dx * dx + dy * dy) < 1e-12 ? 0.0 : sbm::atan2_cr(dy, dx);
+  }
+  yaws[j] = yaw;
+}
+
 }  // namespace
 
 namespace sbk {
@@ -270,6 +350,32 @@ void anchor_states(const SbWorldView& w, int32_t anchor_obj, const double inv_su
 void download_poses(const SbWorldView& w, int32_t obj, double* out16, sb_stream_t s) {
   k_pose_colmajor<<<grid_for(w.n), kBlock, 0, s>>>(w, obj, out16);
   check_launch("download_poses");
+}
+
+void sampler_fifo(const double* sup34, uint64_t m, const uint64_t* seg_first,
+                  const uint64_t* seg_draw, int nseg, uint64_t state0, const SbRegionTri* tris,
+                  const double* cum, int nt, double* pos, sb_stream_t s) {
+  if (m == 0) return;
+  k_sampler_fifo<<<grid_for(m, 256), 256, 0, s>>>(sup34, m, seg_first, seg_draw, nseg, state0,
+                                                  tris, cum, nt, pos);
+  check_launch("sampler_fifo");
+}
+void sampler_fallback(const double* sup34, const uint32_t* active, uint64_t m, uint64_t run_seed,
+                      uint64_t salt, uint64_t attempt, const uint32_t* inst_tab,
+                      const SbRegionTri* tris, const double* cum, double* pos, uint8_t* placeable,
+                      sb_stream_t s) {
+  if (m == 0) return;
+  k_sampler_fallback<<<grid_for(m, 256), 256, 0, s>>>(sup34, active, m, run_seed, salt, attempt,
+                                                      inst_tab, tris, cum, pos, placeable);
+  check_launch("sampler_fallback");
+}
+void orientations(int kind, const uint32_t* active, uint64_t m, const double* pos,
+                  const double* face_xy, uint64_t run_seed, uint64_t salt, uint64_t attempt,
+                  double* yaws, sb_stream_t s) {
+  if (m == 0) return;
+  k_orientations<<<grid_for(m, 256), 256, 0, s>>>(kind, active, m, pos, face_xy, run_seed, salt,
+                                                  attempt, yaws);
+  check_launch("orientations");
 }
 
 }  // namespace sbk

@@ -46,4 +46,18 @@ void debug_math(int fn, const double* in, uint64_t n, double* out, sb_stream_t s
 // accepted poses of one object as column-major Mat4 (N x 16 doubles)
 void download_poses(const SbWorldView& w, int32_t obj, double* out16, sb_stream_t s);
 
+// standalone PositionSampler / sample_orientations (sampler.cpp:54-156). sup34: one
+// row-major 3x4 support pose per active entry (host-gathered); inst_tab: per instance
+// (first table row, rows) into tris/cum.
+void sampler_fifo(const double* sup34, uint64_t m, const uint64_t* seg_first,
+                  const uint64_t* seg_draw, int nseg, uint64_t state0, const SbRegionTri* tris,
+                  const double* cum, int nt, double* pos, sb_stream_t s);
+void sampler_fallback(const double* sup34, const uint32_t* active, uint64_t m, uint64_t run_seed,
+                      uint64_t salt, uint64_t attempt, const uint32_t* inst_tab,
+                      const SbRegionTri* tris, const double* cum, double* pos, uint8_t* placeable,
+                      sb_stream_t s);
+void orientations(int kind, const uint32_t* active, uint64_t m, const double* pos,
+                  const double* face_xy, uint64_t run_seed, uint64_t salt, uint64_t attempt,
+                  double* yaws, sb_stream_t s);
+
 }  // namespace sbk
