@@ -3,6 +3,7 @@
 //   g++ -std=c++20 -Iinclude examples/cpp_dropin.cpp -Lpaper_2512_16896_b200
 //       -lscenebatch_b200 -Wl,-rpath,$PWD/paper_2512_16896_b200 -o cpp_dropin
 // Prints the box fingerprint; with a GPU also runs SPEC.md:394-395's unit-cube checks.
+#include <cmath>
 #include <cstdio>
 #include <vector>
 
@@ -27,7 +28,20 @@ int main() {
     std::vector<uint32_t> active = {0, 1, 2, 3};
     CollisionMask m = world.check_batch(g, cand, active);
     std::printf("free: %d %d %d %d\n", m.free[0], m.free[1], m.free[2], m.free[3]);
-    return (m.free[0] == 0 && m.free[1] == 0 && m.free[2] == 1 && m.free[3] == 0) ? 0 : 1;
+    // PositionSampler (sampler.hpp:66-96): 4 points of the rect under identity supports
+    PositionSampler ps(/*placement_salt*/ 1);
+    ps.prepare({{{-0.6, -0.4}, {0.6, -0.4}, {0.6, 0.4}, {-0.6, 0.4}}}, 4, /*run_seed*/ 7);
+    std::vector<Pose> sup(4, Pose{1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0, 0, 0, 0.75, 1});
+    std::vector<std::array<double, 3>> pos;
+    std::vector<uint8_t> placeable;
+    ps.sample(sup[0].data(), active, 0, pos, placeable);
+    bool inside = true;
+    for (const auto& p : pos) inside = inside && std::abs(p[0]) <= 0.6 && std::abs(p[1]) <= 0.4 && p[2] == 0.75;
+    std::printf("sampled: inside %d refills %llu\n", inside ? 1 : 0,
+                (unsigned long long)ps.refill_count());
+    auto yaws = sample_orientations(SB_ORIENT_UNIFORM_YAW, active, pos, nullptr, 7, 1, 0);
+    std::printf("yaw0 %.17g\n", yaws[0]);
+    return (m.free[0] == 0 && m.free[1] == 0 && m.free[2] == 1 && m.free[3] == 0 && inside) ? 0 : 1;
   } catch (const cuda_error& e) {
     std::printf("no device: %s\n", e.what());
     return 2;

@@ -1,6 +1,6 @@
 // scenebatch_b200.hpp -- the reference's C++ class API on top of the C ABI.
 //
-// Drop-in shape of /root/reference/proj/include/scenebatch/{collision,trimesh}.hpp plus
+// Drop-in shape of /root/reference/proj/include/scenebatch/{collision,trimesh,sampler}.hpp plus
 // the generation engine the reference specifies but does not ship.
 // Header-only; link libscenebatch_b200.so. Errors are rethrown as the reference's
 // exception types (std::invalid_argument, std::out_of_range, std::logic_error,
@@ -189,5 +189,87 @@ class Engine {
  private:
   sb_engine* e_ = nullptr;
 };
+
+// Polygon2D / MultiPolygon2D (polygon.hpp:12-24), hole-free parts as xy rings.
+using Ring = std::vector<std::array<double, 2>>;
+using MultiPolygon2D = std::vector<Ring>;
+
+// PositionSampler (sampler.hpp:66-96) on one B200. prepare() takes the canonical region
+// (ConstraintRegion::region) or, via prepare_per_instance, regions_by_instance.
+class PositionSampler {
+ public:
+  explicit PositionSampler(uint64_t placement_salt, int device = 0) {
+    check(sb_sampler_create(placement_salt, device, &s_));
+  }
+  ~PositionSampler() { sb_sampler_destroy(s_); }
+  PositionSampler(const PositionSampler&) = delete;
+  PositionSampler& operator=(const PositionSampler&) = delete;
+
+  void prepare(const MultiPolygon2D& region, std::size_t batch_size, uint64_t run_seed) {
+    std::vector<double> xy;
+    std::vector<uint32_t> off;
+    flatten(region, xy, off);
+    n_ = batch_size;
+    check(sb_sampler_prepare(s_, xy.data(), off.data(), static_cast<uint32_t>(region.size()),
+                             nullptr, batch_size, run_seed));
+  }
+  void prepare_per_instance(const std::vector<MultiPolygon2D>& regions, uint64_t run_seed) {
+    MultiPolygon2D all;
+    std::vector<uint32_t> inst{0};
+    for (const auto& r : regions) {
+      all.insert(all.end(), r.begin(), r.end());
+      inst.push_back(static_cast<uint32_t>(all.size()));
+    }
+    std::vector<double> xy;
+    std::vector<uint32_t> off;
+    flatten(all, xy, off);
+    n_ = regions.size();
+    check(sb_sampler_prepare(s_, xy.data(), off.data(), static_cast<uint32_t>(all.size()),
+                             inst.data(), regions.size(), run_seed));
+  }
+  // support_world: batch_size column-major Mat4 (TransformBatch::data memory)
+  void sample(const double* support_world, std::span<const uint32_t> active, uint64_t attempt,
+              std::vector<std::array<double, 3>>& positions, std::vector<uint8_t>& placeable) {
+    positions.assign(active.size(), {0.0, 0.0, 0.0});
+    placeable.assign(active.size(), 1);
+    check(sb_sampler_sample(s_, support_world, active.data(), active.size(), attempt,
+                            positions.empty() ? nullptr : positions[0].data(), placeable.data()));
+  }
+  uint64_t refill_count() const {
+    uint64_t q = 0, r = 0;
+    check(sb_sampler_cache_info(s_, &q, &r));
+    return r;
+  }
+
+ private:
+  static void flatten(const MultiPolygon2D& region, std::vector<double>& xy,
+                      std::vector<uint32_t>& off) {
+    off.assign(1, 0);
+    for (const auto& ring : region) {
+      for (const auto& p : ring) {
+        xy.push_back(p[0]);
+        xy.push_back(p[1]);
+      }
+      off.push_back(static_cast<uint32_t>(xy.size() / 2));
+    }
+  }
+  sb_sampler* s_ = nullptr;
+  std::size_t n_ = 0;
+};
+
+// sample_orientations (sampler.hpp:98-104); kind = SB_ORIENT_*.
+inline std::vector<double> sample_orientations(int kind, std::span<const uint32_t> active,
+                                               std::span<const std::array<double, 3>> positions,
+                                               const std::vector<std::array<double, 2>>* face_targets,
+                                               uint64_t run_seed, uint64_t placement_salt,
+                                               uint64_t attempt, int device = 0) {
+  std::vector<double> yaws(active.size(), 0.0);
+  check(sb_sample_orientations(kind, active.data(), active.size(),
+                               positions.empty() ? nullptr : positions[0].data(),
+                               face_targets ? (*face_targets)[0].data() : nullptr,
+                               face_targets ? face_targets->size() : 0, run_seed, placement_salt,
+                               attempt, yaws.data(), device));
+  return yaws;
+}
 
 }  // namespace scenebatch_b200

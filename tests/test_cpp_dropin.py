@@ -26,7 +26,10 @@ def test_cpp_header_builds_and_fails_loudly_without_gpu(tmp_path, pkg):
 
 
 @pytest.mark.gpu
-def test_cpp_header_unit_cubes_on_gpu(tmp_path, gpu):
+def test_cpp_header_unit_cubes_on_gpu(tmp_path, gpu, ref):
     r = subprocess.run([build(tmp_path)], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "free: 0 0 1 0" in r.stdout
+    assert "sampled: inside 1 refills 1" in r.stdout
+    yaw0 = ref.sample_orientations(1, [0, 1, 2, 3], None, None, 7, 1, 0)[0]
+    assert f"yaw0 {yaw0!r}" in r.stdout or f"yaw0 {yaw0:.17g}" in r.stdout
