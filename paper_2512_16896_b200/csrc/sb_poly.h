@@ -24,11 +24,18 @@ namespace sbp {
 constexpr double kPi = 3.14159265358979323846;  // M_PI
 constexpr int kCap = SB_REGION_MAX_VERTS;
 
-struct Ring {
-  double x[kCap];
-  double y[kCap];
+template <int Cap>
+struct RingT {
+  static constexpr int cap = Cap;
+  double x[Cap];
+  double y[Cap];
   int n;
 };
+using Ring = RingT<kCap>;
+// Merged ring of an annulus clipped to a rect with its hole bridged in
+// (bridge_hole, polygon.cpp:197-258): outer + hole + 2 bridge vertices.
+constexpr int kHoleCap = 2 * kCap + 2;
+using HoleRing = RingT<kHoleCap>;
 
 enum RegionStatus { kRegionOk = 0, kRegionEmpty = 1, kRegionOverflow = 2, kRegionBadArg = 3 };
 
@@ -38,7 +45,8 @@ SB_HD double cross2(double ox, double oy, double ax, double ay, double bx, doubl
 }
 
 // ring_area (polygon.cpp:58-66); shoelace, left to right.
-SB_HD double ring_area(const Ring& r) {
+template <int Cap>
+SB_HD double ring_area(const RingT<Cap>& r) {
   double s = 0.0;
   for (int i = 0; i < r.n; ++i) {
     int j = (i + 1) % r.n;
@@ -47,7 +55,8 @@ SB_HD double ring_area(const Ring& r) {
   return 0.5 * s;
 }
 
-SB_HD void reverse_ring(Ring& r) {
+template <int Cap>
+SB_HD void reverse_ring(RingT<Cap>& r) {
   for (int i = 0, j = r.n - 1; i < j; ++i, --j) {
     double tx = r.x[i], ty = r.y[i];
     r.x[i] = r.x[j];
@@ -57,8 +66,9 @@ SB_HD void reverse_ring(Ring& r) {
   }
 }
 
-SB_HD bool push(Ring& r, double x, double y) {
-  if (r.n >= kCap) return false;
+template <int Cap>
+SB_HD bool push(RingT<Cap>& r, double x, double y) {
+  if (r.n >= Cap) return false;
   r.x[r.n] = x;
   r.y[r.n] = y;
   ++r.n;
@@ -103,7 +113,8 @@ SB_HD int annulus_sector(double cx, double cy, double vx, double vy, double thet
 
 // One Sutherland-Hodgman pass against an axis-aligned half plane; the stand-in for
 // Boost intersection documented in oracle/shim/boost/geometry.hpp (same operation order).
-SB_HD bool clip_half(const Ring& in, Ring& out, int axis, double bound, bool keep_ge) {
+template <int Cap>
+SB_HD bool clip_half(const RingT<Cap>& in, RingT<Cap>& out, int axis, double bound, bool keep_ge) {
   out.n = 0;
   int n = in.n;
   for (int i = 0; i < n; ++i) {
@@ -128,11 +139,13 @@ SB_HD bool clip_half(const Ring& in, Ring& out, int axis, double bound, bool kee
 // intersect(ring, rect) as the oracle stand-in defines it: correct() orientation,
 // 4 half-plane passes (x>=x0, x<=x1, y>=y0, y<=y1), drop consecutive exact duplicates,
 // discard < 3 vertices or zero area. Result in `r` (open ring). Uses `tmp` as scratch.
-SB_HD int intersect_rect(Ring& r, Ring& tmp, const double rect[4]) {
+// hole: correct() orients holes clockwise instead of counter-clockwise.
+template <int Cap>
+SB_HD int intersect_rect(RingT<Cap>& r, RingT<Cap>& tmp, const double rect[4], bool hole = false) {
   if (r.n < 3) return kRegionEmpty;
   // bg::correct (via to_boost, polygon.cpp:27-36) reverses the CLOSED ring, which keeps
   // vertex 0 first: [p0, p(n-1), ..., p1].
-  if (ring_area(r) < 0.0) {
+  if (hole ? ring_area(r) > 0.0 : ring_area(r) < 0.0) {
     for (int i = 1, j = r.n - 1; i < j; ++i, --j) {
       double tx = r.x[i], ty = r.y[i];
       r.x[i] = r.x[j];
@@ -202,15 +215,17 @@ SB_HD bool sink_tri(TableSink& s, double ax, double ay, double bx, double by, do
 }
 
 // triangulate() of a hole-free polygon (polygon.cpp:344-368) feeding ear_clip_ring
-// (polygon.cpp:260-340) straight into the sampler table. `r` is consumed.
+// (polygon.cpp:260-340) straight into the sampler table. `r` is consumed. orient = false:
+// ear_clip_ring alone (a ring triangulate() already oriented and bridged).
+template <int Cap>
 #ifdef __CUDACC__
 static __host__ __device__ __noinline__
 #else
 inline
 #endif
-bool ear_clip_into(Ring& r, TableSink& sink) {
+bool ear_clip_into(RingT<Cap>& r, TableSink& sink, bool orient = true) {
   if (r.n < 3) return true;
-  if (ring_area(r) < 0.0) reverse_ring(r);
+  if (orient && ring_area(r) < 0.0) reverse_ring(r);
   // drop consecutive duplicates (squared distance <= 1e-24)
   int n = 0;
   for (int i = 0; i < r.n; ++i) {
@@ -249,8 +264,8 @@ bool ear_clip_into(Ring& r, TableSink& sink) {
       return true;
     }
   }
-  int prv[kCap], nxt[kCap];
-  bool reflex[kCap];
+  int prv[Cap], nxt[Cap];
+  bool reflex[Cap];
   for (int i = 0; i < n; ++i) {
     prv[i] = (i + n - 1) % n;
     nxt[i] = (i + 1) % n;
@@ -312,6 +327,127 @@ bool ear_clip_into(Ring& r, TableSink& sink) {
     if (!sink_tri(sink, r.x[p], r.y[p], r.x[cur], r.y[cur], r.x[q], r.y[q])) return false;
   }
   return true;
+}
+
+// ------------------------------------------------------------ annulus with a hole
+// libm policy for the hole path: glibc on the host (the reference's), the correctly
+// rounded device functions in sb_region.cu.
+struct HostMath {
+  static inline void sincos(double a, double* s, double* c) {
+    *s = ::sin(a);
+    *c = ::cos(a);
+  }
+  static inline double atan2(double y, double x) { return ::atan2(y, x); }
+};
+
+// bridge_hole (polygon.cpp:197-258): merge the CW hole into the CCW outer ring at the
+// hole's max-x vertex; a reflex outer vertex inside the bridge triangle takes over as
+// the bridge end (the candidate and its triangle update as the scan proceeds).
+template <class M>
+SB_HD bool bridge_hole(const Ring& outer, const Ring& hole, HoleRing& out) {
+  int mi = 0;
+  for (int i = 1; i < hole.n; ++i)
+    if (hole.x[i] > hole.x[mi]) mi = i;
+  const double mx = hole.x[mi], my = hole.y[mi];
+  const int n = outer.n;
+  double best_x = INFINITY, hx = 0.0, hy = 0.0;
+  int best_edge = n;
+  for (int i = 0; i < n; ++i) {
+    const int j = (i + 1) % n;
+    const double ax = outer.x[i], ay = outer.y[i], bx = outer.x[j], by = outer.y[j];
+    if ((ay > my) == (by > my)) continue;
+    const double t = (my - ay) / (by - ay);
+    const double x = ax + t * (bx - ax);
+    if (x >= mx - 1e-12 && x < best_x) {
+      best_x = x;
+      best_edge = i;
+      hx = x;
+      hy = my;
+    }
+  }
+  out.n = 0;
+  if (best_edge == n) {  // degenerate: the hole is dropped (polygon.cpp:219-222)
+    for (int i = 0; i < n; ++i)
+      if (!push(out, outer.x[i], outer.y[i])) return false;
+    return true;
+  }
+  const int eb = (best_edge + 1) % n;
+  int cand = outer.x[best_edge] > outer.x[eb] ? best_edge : eb;
+  double cx = outer.x[cand], cy = outer.y[cand];
+  double best_metric = INFINITY;
+  for (int i = 0; i < n; ++i) {
+    if (i == cand) continue;
+    const int ip = (i + n - 1) % n, in = (i + 1) % n;
+    const bool reflex =
+        cross2(outer.x[ip], outer.y[ip], outer.x[i], outer.y[i], outer.x[in], outer.y[in]) < 0.0;
+    if (!reflex) continue;
+    if (point_in_tri_strict(outer.x[i], outer.y[i], mx, my, hx, hy, cx, cy) ||
+        point_in_tri_strict(outer.x[i], outer.y[i], mx, my, cx, cy, hx, hy)) {
+      const double dx = outer.x[i] - mx, dy = outer.y[i] - my;
+      const double metric = fabs(M::atan2(dy, dx));
+      if (metric < best_metric) {
+        best_metric = metric;
+        cand = i;
+        cx = outer.x[i];
+        cy = outer.y[i];
+      }
+    }
+  }
+  for (int i = 0; i <= cand; ++i)
+    if (!push(out, outer.x[i], outer.y[i])) return false;
+  for (int k = 0; k <= hole.n; ++k)
+    if (!push(out, hole.x[(mi + k) % hole.n], hole.y[(mi + k) % hole.n])) return false;
+  if (!push(out, outer.x[cand], outer.y[cand])) return false;
+  for (int i = cand + 1; i < n; ++i)
+    if (!push(out, outer.x[i], outer.y[i])) return false;
+  return true;
+}
+
+struct HoleScratch {
+  Ring o, h, tmp;
+  HoleRing mg;
+};
+
+// region_for(i) of a full annulus with a hole (theta = pi, min_r > 0;
+// relationships.cpp:197-209): annulus_sector's full branch (polygon.cpp:157-167, outer
+// circle + CW inner circle), the shim intersection (outer and hole each clipped to the
+// rect; a hole that clips away is dropped), from_boost, then triangulate (orientation,
+// bridge_hole) and ear_clip_ring into the sampler table. max_r must be finite.
+template <class M>
+SB_HD int hole_annulus_table(double cx, double cy, double min_r, double max_r,
+                             const double rect[4], HoleScratch& sc, TableSink& sink) {
+  const double step = 5.0 * kPi / 180.0;
+  auto arc = [&](Ring& out, double radius, double a0, double a1) -> bool {
+    int na = (int)ceil(fabs(a1 - a0) / step);
+    if (na < 1) na = 1;
+    for (int i = 0; i <= na; ++i) {
+      const double a = a0 + (a1 - a0) * (double)i / (double)na;
+      double sa, ca;
+      M::sincos(a, &sa, &ca);
+      if (!push(out, cx + radius * ca, cy + radius * sa)) return false;
+    }
+    out.n -= 1;  // closing vertex
+    return true;
+  };
+  sc.o.n = 0;
+  sc.h.n = 0;
+  if (!arc(sc.o, max_r, 0.0, 2.0 * kPi) || !arc(sc.h, min_r, 2.0 * kPi, 0.0))
+    return kRegionOverflow;
+  const int so = intersect_rect(sc.o, sc.tmp, rect, false);
+  if (so == kRegionOverflow) return so;
+  if (so != kRegionOk) return kRegionEmpty;
+  const int sh = intersect_rect(sc.h, sc.tmp, rect, true);
+  if (sh == kRegionOverflow) return sh;
+  if (ring_area(sc.o) < 0.0) reverse_ring(sc.o);  // triangulate (polygon.cpp:348-354)
+  if (sh == kRegionOk) {
+    if (ring_area(sc.h) > 0.0) reverse_ring(sc.h);
+    if (!bridge_hole<M>(sc.o, sc.h, sc.mg)) return kRegionOverflow;
+  } else {
+    sc.mg.n = 0;
+    for (int i = 0; i < sc.o.n; ++i) push(sc.mg, sc.o.x[i], sc.o.y[i]);
+  }
+  if (!ear_clip_into(sc.mg, sink, false)) return kRegionOverflow;
+  return kRegionOk;
 }
 
 // Normalise the cumulative table (polygon.cpp:381-387). Returns the triangle count

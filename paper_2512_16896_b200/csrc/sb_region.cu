@@ -446,10 +446,70 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
   return {sbp::kRegionOk, ntri};
 }
 
+// libm policy of the hole path on the device: the correctly rounded sin/cos/atan2.
+struct DevMath {
+  __device__ static void sincos(double a, double* s, double* c) { sbm::sincos_cr(a, s, c); }
+  __device__ static double atan2(double y, double x) { return sbm::atan2_cr(y, x); }
+};
+
+// Full annulus with a hole (theta = pi, min_r > 0): one lane per instance runs the
+// restated pipeline (sbp::hole_annulus_table) in local memory -- outer + hole rings up to
+// 2 * kCap + 2 vertices do not fit the group's shared scratch, and bridged rings are
+// never convex, so the lane-parallel fan path would not apply anyway.
+__device__ __noinline__ RegionStats hole_region_lane(const SbPlacementDev& pl, double ax, double ay,
+                                                     SbRegionTri* tris, double* cum, int cap) {
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  double min_r = 0.0, max_r = inf;  // distance_band (relationships.cpp:101-122)
+  if (pl.distance_type == SB_DIST_GREATER) {
+    min_r = pl.distance;
+  } else if (pl.distance_type == SB_DIST_EQUAL) {
+    const double half = dmax(0.05 * pl.distance, 0.01);
+    min_r = dmax(0.0, pl.distance - half);
+    max_r = pl.distance + half;
+  }
+  const double* rc = pl.rect;
+  double bx0 = inf, by0 = inf, bx1 = -inf, by1 = -inf;
+  const double vxs[5] = {rc[0], rc[2], rc[2], rc[0], ax};
+  const double vys[5] = {rc[1], rc[1], rc[3], rc[3], ay};
+  for (int k = 0; k < 5; ++k) {
+    bx0 = dmin(bx0, vxs[k]);
+    by0 = dmin(by0, vys[k]);
+    bx1 = dmax(bx1, vxs[k]);
+    by1 = dmax(by1, vys[k]);
+  }
+  const double ddx = bx1 - bx0, ddy = by1 - by0;
+  const double diag = bx0 > bx1 ? 0.0 : sqrt(ddx * ddx + ddy * ddy);
+  if (isinf(max_r)) max_r = fmax(diag, min_r + 1e-6);
+  if (!(min_r < max_r)) return {sbp::kRegionBadArg, 0};
+  sbp::HoleScratch sc;
+  sbp::TableSink sink{tris, cum, 0, cap, 0.0};
+  const int st = sbp::hole_annulus_table<DevMath>(ax, ay, min_r, max_r, rc, sc, sink);
+  if (st != sbp::kRegionOk) return {st, 0};
+  return {sbp::kRegionOk, sbp::finish_table(sink)};
+}
+
+// Group-level dispatch: the hole path on lane 0, broadcast to the group.
+template <bool kHole>
+__device__ __forceinline__ RegionStats group_region(const SbPlacementDev& pl, double ax, double ay,
+                                                    double ayaw, SbRegionTri* tris, double* cum,
+                                                    int cap, RegionScratch& sc) {
+  if constexpr (kHole) {
+    const Grp g;
+    RegionStats r{0, 0};
+    if (g.gl == 0) r = hole_region_lane(pl, ax, ay, tris, cum, cap);
+    r.status = g.bcast(r.status, 0);
+    r.ntri = g.bcast(r.ntri, 0);
+    return r;
+  } else {
+    return warp_region(pl, ax, ay, ayaw, tris, cum, cap, sc);
+  }
+}
+
 // Warp per local instance: anchor state in the support frame (inverse_rigid(support) *
 // anchor pose, yaw_of), the variation test against instance 0 (relationships.cpp:178-186)
 // and the region table. Instance 0's state comes from `s0` (sharded runs) or, when this
 // shard owns global instance 0, is recomputed per warp from local instance 0.
+template <bool kHole>
 __global__ void __launch_bounds__(kRB) k_relation_regions(RelationRegionParams p) {
   __shared__ RegionScratch scratch[kRW];
   const Grp g;
@@ -473,7 +533,8 @@ __global__ void __launch_bounds__(kRB) k_relation_regions(RelationRegionParams p
   auto yaw_of = [](const M34& rel) { return sbm::atan2_cr(rel.m[4], rel.m[0]); };  // transform.hpp:77
   if (p.from_s0) {  // canonical region_for(0) from the exchanged instance-0 state
     if (warp == 0) {
-      const RegionStats r = warp_region(p.pl, p.s0[0], p.s0[1], p.s0[2], p.tris, p.cum, p.cap, sc);
+      const RegionStats r =
+          group_region<kHole>(p.pl, p.s0[0], p.s0[1], p.s0[2], p.tris, p.cum, p.cap, sc);
       if (g.gl == 0) {
         const bool good = r.status == sbp::kRegionOk || r.status == sbp::kRegionEmpty;
         p.ntri[0] = good ? r.ntri : 0;
@@ -510,8 +571,8 @@ __global__ void __launch_bounds__(kRB) k_relation_regions(RelationRegionParams p
     vary = vary || pos_vary;
     SB_RP_MARK(ra1);
     SB_RP_ADD(0, ra0, ra1);
-    const RegionStats r = warp_region(p.pl, ax, ay, ayaw, p.tris + i * p.cap, p.cum + i * p.cap,
-                                      p.cap, sc);
+    const RegionStats r = group_region<kHole>(p.pl, ax, ay, ayaw, p.tris + i * p.cap,
+                                              p.cum + i * p.cap, p.cap, sc);
     if (g.gl == 0) {
       p.ntri[i] = r.status == sbp::kRegionOk || r.status == sbp::kRegionEmpty ? r.ntri : 0;
       if (r.status != sbp::kRegionOk && r.status != sbp::kRegionEmpty && r.status > worst)
@@ -540,7 +601,8 @@ void relation_regions(const RelationRegionParams& p, int num_sms, sb_stream_t s)
   const unsigned cap_blocks = (unsigned)(num_sms * 16);
   if (blocks > cap_blocks) blocks = cap_blocks;
   if (blocks == 0) blocks = 1;
-  k_relation_regions<<<blocks, kRB, 0, s>>>(p);
+  if (p.hole) k_relation_regions<true><<<blocks, kRB, 0, s>>>(p);
+  else k_relation_regions<false><<<blocks, kRB, 0, s>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("relation_regions: ") + cudaGetErrorString(e));
 }

@@ -17,6 +17,7 @@ struct RelationRegionParams {
   const double* s0;        // instance 0's anchor state when !owns_instance0 (device)
   int32_t from_s0;         // 1: build a single region from s0 (canonical, sharded runs)
   int32_t cap;
+  int32_t hole;            // full annulus with a hole: bridged-hole path (sbp::hole_annulus_table)
   SbRegionTri* tris;       // [n][cap] (or [1][cap] when from_s0)
   double* cum;
   int32_t* ntri;           // [n]

@@ -20,6 +20,7 @@
 #include "sb_host.hpp"
 #include "sb_kernels.h"
 #include "sb_place.h"
+#include "sb_poly.h"
 #include "sb_region.h"
 #include "sb_layout.h"
 
@@ -447,10 +448,11 @@ struct sb_engine {
     double support16[16];
     double inv_support[12];
     int canon_n = 0;  // host-built canonical table size (no anchor)
+    bool hole = false;  // full annulus with a hole (theta = pi, min_r > 0)
   };
   std::vector<Placement> places;
   int32_t first_place_obj = 0;
-  int inst_cap = 0;
+  int inst_cap = 0;  // region table stride (canonical and per instance)
 
   DevArray<uint8_t> d_valid;
   DevArray<int16_t> d_accepted;
@@ -558,7 +560,7 @@ struct sb_engine {
       world->set_enabled_all(obj, true);
     }
     first_place_obj = static_cast<int32_t>(sc->n_fixed);
-    bool any_anchor = false;
+    bool any_anchor = false, any_hole = false;
     for (uint32_t p = 0; p < sc->n_placements; ++p) {
       const sb_placement& sp = sc->placements[p];
       int obj = world->add_object("p" + std::to_string(p), mesh_geom(sp.mesh));
@@ -614,8 +616,12 @@ struct sb_engine {
       if (r.anchor >= 0) {
         any_anchor = true;
         double theta = r.angle_threshold > 0 ? r.angle_threshold : (r.direction == SB_DIR_NONE ? M_PI : M_PI / 4);
-        if (theta >= M_PI - 1e-12 && (r.distance_type == SB_DIST_GREATER || r.distance_type == SB_DIST_EQUAL))
-          throw std::invalid_argument("full annulus with a hole is not supported on the device path");
+        double min_r = 0.0;  // distance_band (relationships.cpp:101-122)
+        if (r.distance_type == SB_DIST_GREATER) min_r = r.distance;
+        if (r.distance_type == SB_DIST_EQUAL)
+          min_r = std::max(0.0, r.distance - std::max(0.05 * r.distance, 0.01));
+        pl.hole = theta >= M_PI - 1e-12 && min_r > 0.0;
+        any_hole = any_hole || pl.hole;
       }
       places.push_back(pl);
     }
@@ -623,8 +629,9 @@ struct sb_engine {
 
     // canonical sampler tables (no-anchor placements: the support rect itself)
     const size_t P = places.size();
-    d_canon_tris.alloc(std::max<size_t>(1, P) * SB_REGION_MAX_VERTS);
-    d_canon_cum.alloc(std::max<size_t>(1, P) * SB_REGION_MAX_VERTS);
+    inst_cap = any_hole ? sbp::kHoleCap : SB_REGION_MAX_VERTS;
+    d_canon_tris.alloc(std::max<size_t>(1, P) * inst_cap);
+    d_canon_cum.alloc(std::max<size_t>(1, P) * inst_cap);
     d_canon_n.alloc(std::max<size_t>(1, P));
     for (size_t p = 0; p < P; ++p) {
       if (places[p].dev.anchor_object >= 0) continue;
@@ -633,11 +640,10 @@ struct sb_engine {
       sbh::SamplerTable t = sbh::sampler_table({ring});
       places[p].canon_n = static_cast<int>(t.tris.size());
       if (!t.tris.empty()) {
-        cuda_check(cudaMemcpy(d_canon_tris.p + p * SB_REGION_MAX_VERTS, t.tris.data(), t.tris.size() * sizeof(SbRegionTri), cudaMemcpyHostToDevice), "H2D canon");
-        cuda_check(cudaMemcpy(d_canon_cum.p + p * SB_REGION_MAX_VERTS, t.cum.data(), t.cum.size() * sizeof(double), cudaMemcpyHostToDevice), "H2D canon");
+        cuda_check(cudaMemcpy(d_canon_tris.p + p * inst_cap, t.tris.data(), t.tris.size() * sizeof(SbRegionTri), cudaMemcpyHostToDevice), "H2D canon");
+        cuda_check(cudaMemcpy(d_canon_cum.p + p * inst_cap, t.cum.data(), t.cum.size() * sizeof(double), cudaMemcpyHostToDevice), "H2D canon");
       }
     }
-    inst_cap = SB_REGION_MAX_VERTS;
     if (any_anchor) {
       d_inst_tris.alloc(n * inst_cap);
       d_inst_cum.alloc(n * inst_cap);
@@ -761,6 +767,7 @@ struct sb_engine {
     rp.owns_instance0 = 1;
     std::memcpy(rp.inv_support, pl.inv_support, sizeof rp.inv_support);
     rp.cap = inst_cap;
+    rp.hole = pl.hole ? 1 : 0;
     rp.tris = d_inst_tris.p;
     rp.cum = d_inst_cum.p;
     rp.ntri = d_inst_n.p;
@@ -798,6 +805,7 @@ struct sb_engine {
     std::memcpy(rp.inv_support, pl.inv_support, sizeof rp.inv_support);
     rp.s0 = d_s0.p;
     rp.cap = inst_cap;
+    rp.hole = pl.hole ? 1 : 0;
     rp.tris = d_inst_tris.p;
     rp.cum = d_inst_cum.p;
     rp.ntri = d_inst_n.p;
@@ -813,8 +821,8 @@ struct sb_engine {
     for (uint64_t x : f) vary = vary || x != 0;
     if (!vary) {
       rp.from_s0 = 1;
-      rp.tris = d_canon_tris.p + p * SB_REGION_MAX_VERTS;
-      rp.cum = d_canon_cum.p + p * SB_REGION_MAX_VERTS;
+      rp.tris = d_canon_tris.p + p * inst_cap;
+      rp.cum = d_canon_cum.p + p * inst_cap;
       rp.ntri = d_canon_n.p + p;
       sbk::relation_regions(rp, num_sms, s);
       ++launches;
@@ -869,8 +877,8 @@ struct sb_engine {
       Placement& pl = places[p];
       bool fast = true;
       int canon_n = pl.canon_n;
-      const SbRegionTri* canon_tris = d_canon_tris.p + p * SB_REGION_MAX_VERTS;
-      const double* canon_cum = d_canon_cum.p + p * SB_REGION_MAX_VERTS;
+      const SbRegionTri* canon_tris = d_canon_tris.p + p * inst_cap;
+      const double* canon_cum = d_canon_cum.p + p * inst_cap;
       const bool relation = pl.dev.anchor_object >= 0;
       cuda_check(cudaEventRecord(ev_place[2 * p], stream), "event");
       if (relation) {

@@ -311,3 +311,25 @@ def test_sharded_generate_equals_single(gpu, ref, world):
     assert np.array_equal(acc, whole.accepted)
     assert np.array_equal(valid, whole.valid)
     assert np.array_equal(poses, whole.poses)
+
+
+def _hole_scene(pkg, n):
+    """Full annuli with a hole (direction none, theta = pi, min_r > 0): 'greater' keeps
+    a hole that may clip against the table edge, 'equal' a band ring; the region is
+    triangulated through bridge_hole (polygon.cpp:197-258)."""
+    base = scenes.tabletop_boxes(n, n_objects=7, table=(1.6, 1.2))
+    base.placements[2].relation = pkg.Relation(anchor=0, distance_type=A.SB_DIST_GREATER,
+                                               distance=0.25)
+    base.placements[4].relation = pkg.Relation(anchor=1, distance_type=A.SB_DIST_EQUAL,
+                                               distance=0.3)
+    base.placements[6].relation = pkg.Relation(anchor=3, distance_type=A.SB_DIST_GREATER,
+                                               distance=0.5)
+    return base
+
+
+@pytest.mark.parametrize("n,seed", [(1024, 3), (1, 2)])
+def test_generate_annulus_with_hole(gpu, ref, n, seed):
+    eng, got, want = run_generate_pair(gpu, ref, _hole_scene(gpu, n), seed=seed)
+    assert_same(gpu, got, want)
+    if n > 1:
+        assert got.stats["per_instance_placements"] == 3
