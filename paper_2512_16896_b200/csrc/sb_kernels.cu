@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(kBlock) k_check_batch(WorldView w, int32_t geo
 
 // generate() start: placement objects back to add_object state; valid = 1; accepted = -1.
 __global__ void k_engine_reset(WorldView w, int32_t first_obj, int32_t n_obj, uint8_t* valid,
-                               int16_t* accepted, int32_t n_place) {
+                               int16_t* accepted, int32_t n_place, double* out16) {
   uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i >= w.n) return;
   for (int32_t o = first_obj; o < first_obj + n_obj; ++o) {
@@ -139,6 +139,14 @@ __global__ void k_engine_reset(WorldView w, int32_t first_obj, int32_t n_obj, ui
   }
   valid[i] = 1;
   for (int32_t p = 0; p < n_place; ++p) accepted[(uint64_t)p * w.n + i] = -1;
+  if (out16) {  // result poses start as the identity an unaccepted object keeps
+    for (int32_t p = 0; p < n_place; ++p) {
+      double2* o = reinterpret_cast<double2*>(out16 + ((uint64_t)p * w.n + i) * 16);
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        o[k] = make_double2((2 * k) % 5 == 0 ? 1.0 : 0.0, (2 * k + 1) % 5 == 0 ? 1.0 : 0.0);
+    }
+  }
 }
 
 // Occupancy grid at generate() start: cells cleared, then the enabled fixed objects
@@ -332,8 +340,9 @@ void narrow_profile_check(unsigned long long out[8], bool reset) {
   }
 }
 void engine_reset(const SbWorldView& w, int32_t first_obj, int32_t n_obj, uint8_t* valid,
-                  int16_t* accepted, int32_t n_place, sb_stream_t s) {
-  k_engine_reset<<<grid_for(w.n), kBlock, 0, s>>>(w, first_obj, n_obj, valid, accepted, n_place);
+                  int16_t* accepted, int32_t n_place, double* out16, sb_stream_t s) {
+  k_engine_reset<<<grid_for(w.n), kBlock, 0, s>>>(w, first_obj, n_obj, valid, accepted, n_place,
+                                                  out16);
   check_launch("engine_reset");
 }
 void cells_reset(const SbWorldView& w, const SbCellGrid& g, int32_t first_obj, sb_stream_t s) {

@@ -552,8 +552,24 @@ __device__ uint32_t tile_round(const PlaceParams& p, const Sampling& S, const Sb
       }
       if (c == kFree) {  // update_transform (collision.cpp:408-412) + set_enabled
         double2* pp = reinterpret_cast<double2*>(w.pose + sb_pose_off(w, pl.object, inst));
+        double2 q[6];
 #pragma unroll
-        for (int k = 0; k < 6; ++k) pp[k] = __ldcg(reinterpret_cast<const double2*>(p.cpose + ((size_t)blockIdx.x * kB + v) * 12) + k);
+        for (int k = 0; k < 6; ++k) {
+          q[k] = __ldcg(reinterpret_cast<const double2*>(p.cpose + ((size_t)blockIdx.x * kB + v) * 12) + k);
+          pp[k] = q[k];
+        }
+        if (p.out16) {  // the result pose, column-major Mat4 (k_pose_colmajor layout)
+          const double* m = reinterpret_cast<const double*>(q);
+          double2* o = reinterpret_cast<double2*>(p.out16 + (size_t)inst * 16);
+          o[0] = make_double2(m[0], m[4]);
+          o[1] = make_double2(m[8], 0.0);
+          o[2] = make_double2(m[1], m[5]);
+          o[3] = make_double2(m[9], 0.0);
+          o[4] = make_double2(m[2], m[6]);
+          o[5] = make_double2(m[10], 0.0);
+          o[6] = make_double2(m[3], m[7]);
+          o[7] = make_double2(m[11], 1.0);
+        }
         double2* bp = reinterpret_cast<double2*>(w.box + sb_box_off(w, pl.object, inst));
 #pragma unroll
         for (int k = 0; k < 3; ++k) bp[k] = make_double2(T.box[6 * v + 2 * k], T.box[6 * v + 2 * k + 1]);

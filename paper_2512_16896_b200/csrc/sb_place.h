@@ -54,6 +54,7 @@ struct PlaceParams {
   const int32_t* inst_n;
   uint8_t* valid;               // [n]
   int16_t* accepted;            // [n] of this placement
+  double* out16;                // optional [n][16]: accepted poses, column-major (result download)
   uint32_t* tile_list;          // [ntiles * tile_inst] survivors of each tile
   uint32_t* tile_cnt;           // [2][cnt_stride] survivors per tile, ping-pong by round
   uint32_t cnt_stride;

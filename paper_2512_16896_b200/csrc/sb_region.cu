@@ -26,6 +26,10 @@ constexpr int kRB = 128;            // threads per block
 constexpr int kG = 16;              // lanes per instance group: two instances per warp
 constexpr int kRW = kRB / kG;       // groups per block
 constexpr int kCap = sbp::kCap;
+#ifndef SB_REGION_MIN_BLOCKS
+#define SB_REGION_MIN_BLOCKS 8
+#endif
+constexpr int kRegionMinBlocks = SB_REGION_MIN_BLOCKS;  // resident blocks per SM (register cap)
 
 // The lanes of one instance group and its collectives (kG-wide shuffles, ballots, votes).
 struct Grp {
@@ -58,10 +62,10 @@ __device__ unsigned long long g_rprof[8];
 #define SB_RP_ADD(k, a, b)
 #endif
 
+// Two ring buffers per instance group; the triangle areas / cumulative sums of the fan
+// reuse whichever buffer the final ring is not in (24.6 KB of shared memory per block).
 struct RegionScratch {
   double x[2][kCap], y[2][kCap];
-  double area[kCap];
-  double cum[kCap];
 };
 
 // ring_area (polygon.cpp:58-66): the shoelace terms in parallel, their sum on g.gl 0 in
@@ -263,7 +267,7 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
   SB_RP_ADD(2, rp1, rp2);
   // ---- intersect with the support rect (oracle Boost stand-in): correct() orientation
   if (n < 3) return {sbp::kRegionEmpty, 0};
-  const double ar = warp_ring_area(X, Y, n, sc.area);
+  const double ar = warp_ring_area(X, Y, n, sc.x[1]);
   if (ar < 0.0) {  // reverse the closed ring: p0 stays first
     for (int i = 1 + g.gl; i < n - i; i += kG) {
       const int j = n - i;
@@ -277,18 +281,37 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
   }
   const double x0 = fmin(rc[0], rc[2]), x1 = fmax(rc[0], rc[2]);
   const double y0 = fmin(rc[1], rc[3]), y1 = fmax(rc[1], rc[3]);
-  n = warp_clip(sc.x[0], sc.y[0], n, sc.x[1], sc.y[1], 0, x0, true);
-  if (n >= 0) n = warp_clip(sc.x[1], sc.y[1], n, sc.x[0], sc.y[0], 0, x1, false);
-  if (n >= 0) n = warp_clip(sc.x[0], sc.y[0], n, sc.x[1], sc.y[1], 1, y0, true);
-  if (n >= 0) n = warp_clip(sc.x[1], sc.y[1], n, sc.x[0], sc.y[0], 1, y1, false);
+  // Sutherland-Hodgman passes x >= x0, x <= x1, y >= y0, y <= y1. A pass that keeps every
+  // vertex outputs its input unchanged (no crossings, same order), so it is skipped; the
+  // ring stays in buffer cb.
+  int cb = 0;
+  auto pass = [&](int axis, double bound, bool keep_ge) {
+    if (n < 0) return;
+    bool inside = true;
+    for (int i = g.gl; i < n; i += kG) {
+      const double a = axis == 0 ? sc.x[cb][i] : sc.y[cb][i];
+      if (!(keep_ge ? a >= bound : a <= bound)) inside = false;
+    }
+    if (g.all(inside)) return;
+    n = warp_clip(sc.x[cb], sc.y[cb], n, sc.x[cb ^ 1], sc.y[cb ^ 1], axis, bound, keep_ge);
+    cb ^= 1;
+  };
+  pass(0, x0, true);
+  pass(0, x1, false);
+  pass(1, y0, true);
+  pass(1, y1, false);
   if (n < 0) return {sbp::kRegionOverflow, 0};
+  X = sc.x[cb];
+  Y = sc.y[cb];
   SB_RP_MARK(rp3);
   SB_RP_ADD(3, rp2, rp3);
   // drop consecutive exact duplicates (keep the first of each run; == is transitive, so
   // comparing with the previous vertex equals comparing with the last kept one), then
-  // trailing copies of vertex 0. Out of place: buffer 0 -> buffer 1.
-  double* X1 = sc.x[1];
-  double* Y1 = sc.y[1];
+  // trailing copies of vertex 0. Out of place: buffer cb -> buffer cb ^ 1.
+  double* X1 = sc.x[cb ^ 1];
+  double* Y1 = sc.y[cb ^ 1];
+  double* const FA = sc.x[cb];  // free once the ring is copied out: fan areas
+  double* const FC = sc.y[cb];  // and cumulative sums
   int m = 0;
   for (int i0 = 0; i0 < n; i0 += kG) {
     const int i = i0 + g.gl;
@@ -313,7 +336,7 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
   m = g.bcast(m, 0);
   double area1 = 0.0;
   if (m >= 3) {
-    area1 = warp_ring_area(X1, Y1, m, sc.area);
+    area1 = warp_ring_area(X1, Y1, m, FA);
     if (area1 == 0.0) m = 0;
   }
   if (m < 3) return {sbp::kRegionEmpty, 0};
@@ -396,7 +419,7 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
       int tot;
       const int r = lane_rank(g, a > 0.0, tot);
       slot[c] = a > 0.0 ? ntri + r : -1;
-      if (a > 0.0) sc.area[ntri + r] = a;
+      if (a > 0.0) FA[ntri + r] = a;
       ntri += tot;
     }
     g.sync();
@@ -405,8 +428,8 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
     if (g.gl == 0) {
 #pragma unroll 8
       for (int j = 0; j < ntri; ++j) {
-        total += sc.area[j];
-        sc.cum[j] = total;
+        total += FA[j];
+        FC[j] = total;
       }
     }
     total = g.bcast(total, 0);
@@ -423,7 +446,7 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
         t.b[1] = Y[i];
         t.c[0] = X[i + 1];
         t.c[1] = Y[i + 1];
-        cum[j] = j == ntri - 1 ? 1.0 : sc.cum[j] / total;
+        cum[j] = j == ntri - 1 ? 1.0 : FC[j] / total;
       }
     }
   } else if (g.gl == 0) {  // general ear clipping (reflex or sliver corners): restatement
@@ -510,7 +533,7 @@ __device__ __forceinline__ RegionStats group_region(const SbPlacementDev& pl, do
 // and the region table. Instance 0's state comes from `s0` (sharded runs) or, when this
 // shard owns global instance 0, is recomputed per warp from local instance 0.
 template <bool kHole>
-__global__ void __launch_bounds__(kRB) k_relation_regions(RelationRegionParams p) {
+__global__ void __launch_bounds__(kRB, kRegionMinBlocks) k_relation_regions(RelationRegionParams p) {
   __shared__ RegionScratch scratch[kRW];
   const Grp g;
   const uint64_t warp = (blockIdx.x * (uint64_t)kRB + threadIdx.x) / kG;  // instance group

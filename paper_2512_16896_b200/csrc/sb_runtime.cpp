@@ -470,6 +470,7 @@ struct sb_engine {
   DevArray<int32_t> d_rflags;
   std::vector<cudaEvent_t> ev_place;
   double last_prof[16] = {};
+  bool place_times = false;  // SB_PLACE_TIMES=1: per-placement event times to stderr
   int num_sms = 0;
   // tile decomposition of the shard (sb_place.h) and launch shape of the placement kernel
   uint32_t ntiles = 0;
@@ -489,6 +490,8 @@ struct sb_engine {
   DevArray<double> d_inst_cum;
   DevArray<int32_t> d_inst_n;
   DevArray<double> d_pose16;
+  DevArray<double> d_out16;
+  PinnedArray<uint8_t> h_stat;  // end-of-run counters / ctrl words / region flags / timers  // [P][n][16] result poses written at accept (pipelined download)
   PinnedArray<uint64_t> h_count;
   cudaStream_t copy_stream = nullptr;  // pipelined result download
   std::vector<cudaEvent_t> ev_pose;
@@ -733,6 +736,7 @@ struct sb_engine {
     d_rflags.alloc(2 * std::max<size_t>(1, places.size()));
     d_prof.alloc(8);
     round_debug = std::getenv("SB_ROUND_DEBUG") != nullptr;
+    place_times = std::getenv("SB_PLACE_TIMES") != nullptr;
     if (const char* st = std::getenv("SB_SPEC_TARGET")) spec_target = std::max(1, std::atoi(st));
     if (const char* so = std::getenv("SB_SOLO")) solo_max = std::max(0, std::min(sbk::kPlaceBlock, std::atoi(so)));
     if (round_debug) d_dbg.alloc(3 * static_cast<size_t>(attempts) * std::max<size_t>(1, places.size()) + 16);
@@ -846,7 +850,7 @@ struct sb_engine {
         cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
         ev_pose.push_back(e);
       }
-      d_pose16.ensure(2 * 16 * n);
+      d_out16.ensure(16 * n * places.size());
     }
     cudaStream_t stream = world->stream;
     sb_stream_t s = world->s();
@@ -867,7 +871,7 @@ struct sb_engine {
     cuda_check(cudaMemsetAsync(d_ctrl.p, 0, d_ctrl.count * sizeof(uint32_t), stream), "memset");
     cuda_check(cudaMemsetAsync(d_rflags.p, 0, d_rflags.count * sizeof(int32_t), stream), "memset");
     sbk::engine_reset(wv, first_place_obj, static_cast<int32_t>(P), d_valid.p, d_accepted.p,
-                      static_cast<int32_t>(P), s);
+                      static_cast<int32_t>(P), pipe ? d_out16.p : nullptr, s);
     launches += 1;
     if (cell_grid.g) {
       sbk::cells_reset(wv, cell_grid, first_place_obj, s);
@@ -917,6 +921,7 @@ struct sb_engine {
       pp.inst_n = d_inst_n.p;
       pp.valid = d_valid.p;
       pp.accepted = d_accepted.p + p * n;
+      pp.out16 = pipe ? d_out16.p + p * 16 * n : nullptr;
       pp.tile_list = d_tile_list.p;
       pp.tile_cnt = d_tile_cnt.p;
       pp.cpose = d_cpose.p;
@@ -1000,12 +1005,12 @@ struct sb_engine {
         }
       }
       if (pipe) {  // placement p is final: convert + copy its poses behind an event
-        double* buf = d_pose16.p + (p & 1) * 16 * n;
+        // (k_place wrote them at accept: a DMA only, no SM work beside the next placement)
         cuda_check(cudaEventRecord(ev_pose[p], stream), "event");
         cuda_check(cudaStreamWaitEvent(copy_stream, ev_pose[p], 0), "wait");
-        sbk::download_poses(wv, pl.dev.object, buf, reinterpret_cast<sb_stream_t>(copy_stream));
-        cuda_check(cudaMemcpyAsync(out->poses + 16 * n * p, buf, 16 * n * sizeof(double),
-                                   cudaMemcpyDeviceToHost, copy_stream), "D2H poses");
+        cuda_check(cudaMemcpyAsync(out->poses + 16 * n * p, d_out16.p + 16 * n * p,
+                                   16 * n * sizeof(double), cudaMemcpyDeviceToHost, copy_stream),
+                   "D2H poses");
       }
     }
     if (out) {
@@ -1016,14 +1021,17 @@ struct sb_engine {
     }
     cuda_check(cudaEventRecord(ev_place[2 * P], stream), "event");
     cuda_check(cudaEventRecord(ev_stop, stream), "event");
-    unsigned long long c[8];
-    cuda_check(cudaMemcpyAsync(c, d_counters.p, sizeof c, cudaMemcpyDeviceToHost, stream), "D2H counters");
-    std::vector<uint32_t> ctrl_all(8 * std::max<size_t>(1, P));
-    cuda_check(cudaMemcpyAsync(ctrl_all.data(), d_ctrl.p, ctrl_all.size() * 4, cudaMemcpyDeviceToHost, stream), "D2H ctrl");
-    std::vector<int32_t> rflags(2 * std::max<size_t>(1, P));
-    cuda_check(cudaMemcpyAsync(rflags.data(), d_rflags.p, rflags.size() * 4, cudaMemcpyDeviceToHost, stream), "D2H flags");
-    uint64_t prof[8];
-    cuda_check(cudaMemcpyAsync(prof, d_prof.p, sizeof prof, cudaMemcpyDeviceToHost, stream), "D2H prof");
+    // run statistics: small async copies into one pinned block, one synchronisation
+    const size_t P1 = std::max<size_t>(1, P);
+    h_stat.ensure(128 + 40 * P1);
+    unsigned long long* c = reinterpret_cast<unsigned long long*>(h_stat.p);
+    uint64_t* prof = reinterpret_cast<uint64_t*>(h_stat.p + 64);
+    uint32_t* ctrl_all = reinterpret_cast<uint32_t*>(h_stat.p + 128);
+    int32_t* rflags = reinterpret_cast<int32_t*>(h_stat.p + 128 + 32 * P1);
+    cuda_check(cudaMemcpyAsync(c, d_counters.p, 64, cudaMemcpyDeviceToHost, stream), "D2H counters");
+    cuda_check(cudaMemcpyAsync(prof, d_prof.p, 64, cudaMemcpyDeviceToHost, stream), "D2H prof");
+    cuda_check(cudaMemcpyAsync(ctrl_all, d_ctrl.p, 32 * P1, cudaMemcpyDeviceToHost, stream), "D2H ctrl");
+    cuda_check(cudaMemcpyAsync(rflags, d_rflags.p, 8 * P1, cudaMemcpyDeviceToHost, stream), "D2H flags");
     cuda_check(cudaStreamSynchronize(stream), "sync");
     for (size_t p = 0; p < P; ++p) {
       if (rflags[2 * p + 1] != 0)
@@ -1042,6 +1050,10 @@ struct sb_engine {
       place_ms += b;
       const bool per_inst = places[p].dev.anchor_object >= 0 && rflags[2 * p] != 0;
       (per_inst ? inst_ms : fast_ms) += b;
+      if (place_times)
+        std::fprintf(stderr, "[place %2zu] %s regions %.1f us, placement %.1f us, rounds %u\n", p,
+                     per_inst ? "per-instance" : "fifo        ", a * 1e3, b * 1e3,
+                     device_rounds[p] ? ctrl_all[8 * p + 2] : 0u);
     }
     last_prof[10] = inst_ms;
     last_prof[11] = fast_ms;
