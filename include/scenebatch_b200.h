@@ -292,6 +292,15 @@ sb_status sb_sampler_prepare(sb_sampler* s, const double* ring_xy, const uint32_
 sb_status sb_sampler_sample(sb_sampler* s, const double* support_colmajor16xN,
                             const uint32_t* active, uint64_t m, uint64_t attempt,
                             double* positions_xyz, uint8_t* placeable);
+/* build_constraint_region (relationships.cpp:161-218) + prepare(), on the device: the
+ * relation's region against the support rect (x0 y0 x1 y1) for n anchor states
+ * (anchor_states: x, y, yaw per instance, support frame; may be NULL when rel->anchor < 0,
+ * which means "no anchor": region = the support rect). rel->anchor only selects anchored
+ * vs not here. per_instance is decided as the reference does (an anchor moving by more
+ * than 1e-12). An empty region_for(0) makes every sample not placeable. */
+sb_status sb_sampler_prepare_relation(sb_sampler* s, const sb_relation* rel,
+                                      const double support_rect[4], const double* anchor_states,
+                                      uint64_t n, uint64_t run_seed);
 /* SampleCache state (sampler.hpp:18-36): points queued, refills so far. */
 sb_status sb_sampler_cache_info(const sb_sampler* s, uint64_t* queue_size, uint64_t* refill_count);
 /* sample_orientations (sampler.cpp:129-156): kind = SB_ORIENT_*; face_targets_xy = one

@@ -227,6 +227,15 @@ class PositionSampler {
     check(sb_sampler_prepare(s_, xy.data(), off.data(), static_cast<uint32_t>(all.size()),
                              inst.data(), regions.size(), run_seed));
   }
+  // build_constraint_region(spec, support rect, {anchor states}, N) + prepare, on the device;
+  // anchor_states: N x (x, y, yaw) in the support frame.
+  void prepare_relation(const sb_relation& rel, const std::array<double, 4>& support_rect,
+                        std::span<const std::array<double, 3>> anchor_states, uint64_t run_seed) {
+    n_ = anchor_states.size();
+    check(sb_sampler_prepare_relation(s_, &rel, support_rect.data(),
+                                      anchor_states.empty() ? nullptr : anchor_states[0].data(),
+                                      anchor_states.size(), run_seed));
+  }
   // support_world: batch_size column-major Mat4 (TransformBatch::data memory)
   void sample(const double* support_world, std::span<const uint32_t> active, uint64_t attempt,
               std::vector<std::array<double, 3>>& positions, std::vector<uint8_t>& placeable) {

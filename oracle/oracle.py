@@ -91,6 +91,8 @@ def lib():
                                           C.c_void_p, u64, u64]
         L.ref_sampler_sample.argtypes = [C.c_void_p, C.c_void_p, u64, C.c_void_p, u64, u64,
                                          C.c_void_p, C.c_void_p, C.c_void_p]
+        L.ref_sampler_prepare_relation.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                                   u64, u64]
         L.ref_sample_orientations.argtypes = [C.c_int, C.c_void_p, u64, C.c_void_p, C.c_void_p,
                                               u64, u64, u64, u64, C.c_void_p]
         _lib = L
@@ -297,6 +299,12 @@ class RefSampler:
         self._inst = None if instance_rings is None else np.ascontiguousarray(instance_rings, np.uint32)
         check(lib().ref_sampler_prepare(self.h, _p(self._xy), _p(self._off), len(rings),
                                         None if self._inst is None else _p(self._inst), n, run_seed))
+
+    def prepare_relation(self, rel_c, rect, states, n: int, run_seed: int):
+        rc = np.ascontiguousarray(rect, np.float64)
+        self._st = np.ascontiguousarray(states, np.float64).reshape(-1, 3)
+        check(lib().ref_sampler_prepare_relation(self.h, C.byref(rel_c), _p(rc), _p(self._st), n,
+                                                 run_seed))
 
     def sample(self, support16: np.ndarray, active, attempt: int):
         sw = np.ascontiguousarray(support16, np.float64)

@@ -254,6 +254,27 @@ int ref_sampler_prepare(void* h, const double* xy, const uint32_t* ring_offsets,
     s.sampler.prepare(&s.region, n, run_seed);
   });
 }
+// build_constraint_region(spec, rect, {states}, n) (relationships.cpp:161-218) + prepare;
+// states: n x (x, y, yaw); rel->anchor < 0: no anchors (region = the support rect).
+int ref_sampler_prepare_relation(void* h, const sb_relation* rel, const double* rect,
+                                 const double* states, uint64_t n, uint64_t run_seed) {
+  REF_TRY({
+    RefSampler& s = *static_cast<RefSampler*>(h);
+    RelationshipSpec spec = spec_from(*rel);
+    MultiPolygon2D support = MultiPolygon2D::from(make_rect(rect[0], rect[1], rect[2], rect[3]));
+    std::vector<std::vector<AnchorState>> anchors;
+    if (rel->anchor >= 0) {
+      std::vector<AnchorState> a(n);
+      for (uint64_t i = 0; i < n; ++i) {
+        a[i].position = Vec2(states[3 * i], states[3 * i + 1]);
+        a[i].yaw = states[3 * i + 2];
+      }
+      anchors.push_back(std::move(a));
+    }
+    s.region = build_constraint_region(spec, support, anchors, n);
+    s.sampler.prepare(&s.region, n, run_seed);
+  });
+}
 // support16: N column-major Mat4; positions: 3 per active entry
 int ref_sampler_sample(void* h, const double* support16, uint64_t n, const uint32_t* active,
                        uint64_t m, uint64_t attempt, double* positions, uint8_t* placeable,

@@ -133,6 +133,8 @@ SIGNATURES = {
     "sb_sampler_prepare": (C.c_int, [_P, _D, _U32, C.c_uint32, _U32, C.c_uint64, C.c_uint64]),
     "sb_sampler_sample": (C.c_int, [_P, _D, _U32, C.c_uint64, C.c_uint64, _D,
                                     C.POINTER(C.c_uint8)]),
+    "sb_sampler_prepare_relation": (C.c_int, [_P, C.POINTER(sb_relation), _D, _D, C.c_uint64,
+                                              C.c_uint64]),
     "sb_sampler_cache_info": (C.c_int, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "sb_sample_orientations": (C.c_int, [C.c_int, _U32, C.c_uint64, _D, _D, C.c_uint64,
                                          C.c_uint64, C.c_uint64, C.c_uint64, _D, C.c_int]),

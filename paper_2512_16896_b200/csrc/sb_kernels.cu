@@ -239,12 +239,20 @@ __global__ void k_sampler_fifo(const double* sup34, uint64_t m, const uint64_t* 
 // make_stream(run_seed, {salt, "fall", inst, attempt}); an empty table -> not placeable.
 __global__ void k_sampler_fallback(const double* sup34, const uint32_t* active, uint64_t m,
                                    uint64_t run_seed, uint64_t salt, uint64_t attempt,
-                                   const uint32_t* inst_tab, const SbRegionTri* tris,
-                                   const double* cum, double* pos, uint8_t* placeable) {
+                                   const uint32_t* inst_tab, const int32_t* inst_n, int cap,
+                                   const SbRegionTri* tris, const double* cum, double* pos,
+                                   uint8_t* placeable) {
   const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (j >= m) return;
   const uint32_t inst = __ldg(active + j);
-  const uint32_t o0 = __ldg(inst_tab + 2 * inst), nt = __ldg(inst_tab + 2 * inst + 1);
+  uint32_t o0, nt;
+  if (inst_tab) {
+    o0 = __ldg(inst_tab + 2 * inst);
+    nt = __ldg(inst_tab + 2 * inst + 1);
+  } else {  // relation tables, [n][cap] (k_relation_regions layout)
+    o0 = inst * (uint32_t)cap;
+    nt = (uint32_t)__ldg(inst_n + inst);
+  }
   double px = 0.0, py = 0.0, pz = 0.0;
   if (nt > 0) {
     Pcg r = Pcg::seeded(stream_seed4(run_seed, salt, kFallbackSalt, inst, attempt));
@@ -371,11 +379,12 @@ void sampler_fifo(const double* sup34, uint64_t m, const uint64_t* seg_first,
 }
 void sampler_fallback(const double* sup34, const uint32_t* active, uint64_t m, uint64_t run_seed,
                       uint64_t salt, uint64_t attempt, const uint32_t* inst_tab,
-                      const SbRegionTri* tris, const double* cum, double* pos, uint8_t* placeable,
-                      sb_stream_t s) {
+                      const int32_t* inst_n, int cap, const SbRegionTri* tris, const double* cum,
+                      double* pos, uint8_t* placeable, sb_stream_t s) {
   if (m == 0) return;
   k_sampler_fallback<<<grid_for(m, 256), 256, 0, s>>>(sup34, active, m, run_seed, salt, attempt,
-                                                      inst_tab, tris, cum, pos, placeable);
+                                                      inst_tab, inst_n, cap, tris, cum, pos,
+                                                      placeable);
   check_launch("sampler_fallback");
 }
 void orientations(int kind, const uint32_t* active, uint64_t m, const double* pos,

@@ -566,6 +566,28 @@ __global__ void __launch_bounds__(kRB, kRegionMinBlocks) k_relation_regions(Rela
     }
     return;
   }
+  if (p.states) {  // AnchorState batch given directly (build_constraint_region's input)
+    const double x0 = p.states[0], y0 = p.states[1], yaw0 = p.states[2];
+    bool vary = false;
+    int worst = 0;
+    for (uint64_t i = warp; i < p.w.n; i += nwarps) {
+      const double ax = p.states[3 * i], ay = p.states[3 * i + 1], ayaw = p.states[3 * i + 2];
+      const double dx = ax - x0, dy = ay - y0;  // relationships.cpp:178-186
+      vary = vary || sqrt(dx * dx + dy * dy) > 1e-12 || fabs(ayaw - yaw0) > 1e-12;
+      const RegionStats r = group_region<kHole>(p.pl, ax, ay, ayaw, p.tris + i * p.cap,
+                                                p.cum + i * p.cap, p.cap, sc);
+      if (g.gl == 0) {
+        p.ntri[i] = r.status == sbp::kRegionOk || r.status == sbp::kRegionEmpty ? r.ntri : 0;
+        if (r.status != sbp::kRegionOk && r.status != sbp::kRegionEmpty && r.status > worst)
+          worst = r.status;
+      }
+    }
+    if (g.gl == 0) {
+      if (vary) atomicOr(p.flags + 0, 1);
+      if (worst) atomicMax(p.flags + 1, worst);
+    }
+    return;
+  }
   double x0, y0;
   M34 rel0;
   if (p.owns_instance0) {

@@ -18,6 +18,8 @@ struct RelationRegionParams {
   int32_t from_s0;         // 1: build a single region from s0 (canonical, sharded runs)
   int32_t cap;
   int32_t hole;            // full annulus with a hole: bridged-hole path (sbp::hole_annulus_table)
+  const double* states;    // optional [n][3] anchor states (x, y, yaw) in the support frame
+                           // given directly (standalone sampler); else read from world poses
   SbRegionTri* tris;       // [n][cap] (or [1][cap] when from_s0)
   double* cum;
   int32_t* ntri;           // [n]

@@ -124,6 +124,39 @@ int current_device_checked(int device) {
   return device;
 }
 
+// RelationshipSpec::validate (relationships.cpp:59-76) for the single-anchor subset, then
+// the relation fields of the device record. Returns whether region_for() is a full annulus
+// with a hole (theta = pi, min_r > 0), i.e. needs the bridged-hole region path.
+bool relation_to_dev(const sb_relation& r, SbPlacementDev& d) {
+  if (r.distance < 0.0) throw std::invalid_argument("relationship: distance must be >= 0");
+  if (r.angle_threshold > M_PI) throw std::invalid_argument("relationship: angle_threshold outside (0, pi]");
+  const bool dist = r.distance_type == SB_DIST_GREATER || r.distance_type == SB_DIST_LESS ||
+                    r.distance_type == SB_DIST_EQUAL;
+  if (r.distance_type < SB_DIST_NONE || r.distance_type > SB_DIST_EQUAL)
+    throw std::invalid_argument("relationship: distance_type (middle is out of scope)");
+  if (dist && r.anchor < 0) throw std::invalid_argument("relationship: greater/less/equal require exactly 1 anchor");
+  if (r.direction != SB_DIR_NONE && r.anchor < 0) throw std::invalid_argument("relationship: direction requires exactly 1 anchor");
+  if (r.direction < SB_DIR_NONE || r.direction > SB_DIR_VECTOR) throw std::invalid_argument("relationship: direction");
+  if (r.direction == SB_DIR_VECTOR &&
+      std::sqrt(r.direction_vector[0] * r.direction_vector[0] + r.direction_vector[1] * r.direction_vector[1]) < 1e-12)
+    throw std::invalid_argument("relationship: zero-length direction vector");
+  if (r.distance_type == SB_DIST_LESS && !(0.0 < r.distance))
+    throw std::invalid_argument("annulus_sector: min_r >= max_r");
+  d.distance_type = r.distance_type;
+  d.direction = r.direction;
+  d.frame = r.frame;
+  d.direction_vector[0] = r.direction_vector[0];
+  d.direction_vector[1] = r.direction_vector[1];
+  d.distance = r.distance;
+  d.angle_threshold = r.angle_threshold;
+  if (r.anchor < 0) return false;
+  const double theta = r.angle_threshold > 0 ? r.angle_threshold : (r.direction == SB_DIR_NONE ? M_PI : M_PI / 4);
+  double min_r = 0.0;  // distance_band (relationships.cpp:101-122)
+  if (r.distance_type == SB_DIST_GREATER) min_r = r.distance;
+  if (r.distance_type == SB_DIST_EQUAL) min_r = std::max(0.0, r.distance - std::max(0.05 * r.distance, 0.01));
+  return theta >= M_PI - 1e-12 && min_r > 0.0;
+}
+
 }  // namespace
 
 // ===================================================================== World
@@ -590,42 +623,13 @@ struct sb_engine {
       inverse_rigid34(sup.pose, pl.inv_support);
       for (int k = 0; k < 4; ++k) pl.dev.rect[k] = sup.rect[k];
       const sb_relation& r = sp.relation;
-      // RelationshipSpec::validate (relationships.cpp:59-76) for the single-anchor subset
-      if (r.distance < 0.0) throw std::invalid_argument("relationship: distance must be >= 0");
-      if (r.angle_threshold > M_PI) throw std::invalid_argument("relationship: angle_threshold outside (0, pi]");
-      bool dist = r.distance_type == SB_DIST_GREATER || r.distance_type == SB_DIST_LESS ||
-                  r.distance_type == SB_DIST_EQUAL;
-      if (r.distance_type < SB_DIST_NONE || r.distance_type > SB_DIST_EQUAL)
-        throw std::invalid_argument("relationship: distance_type (middle is out of scope)");
-      if (dist && r.anchor < 0) throw std::invalid_argument("relationship: greater/less/equal require exactly 1 anchor");
-      if (r.direction != SB_DIR_NONE && r.anchor < 0) throw std::invalid_argument("relationship: direction requires exactly 1 anchor");
-      if (r.direction < SB_DIR_NONE || r.direction > SB_DIR_VECTOR) throw std::invalid_argument("relationship: direction");
-      if (r.direction == SB_DIR_VECTOR &&
-          std::sqrt(r.direction_vector[0] * r.direction_vector[0] + r.direction_vector[1] * r.direction_vector[1]) < 1e-12)
-        throw std::invalid_argument("relationship: zero-length direction vector");
-      if (r.distance_type == SB_DIST_LESS && !(0.0 < r.distance))
-        throw std::invalid_argument("annulus_sector: min_r >= max_r");
+      pl.hole = relation_to_dev(r, pl.dev);
       if (r.anchor >= 0 && static_cast<uint32_t>(r.anchor) >= p)
         throw std::invalid_argument("relationship: anchor must be an earlier placement");
       pl.dev.anchor_object = r.anchor >= 0 ? first_place_obj + r.anchor : -1;
-      pl.dev.distance_type = r.distance_type;
-      pl.dev.direction = r.direction;
-      pl.dev.frame = r.frame;
-      pl.dev.direction_vector[0] = r.direction_vector[0];
-      pl.dev.direction_vector[1] = r.direction_vector[1];
-      pl.dev.distance = r.distance;
-      pl.dev.angle_threshold = r.angle_threshold;
       pl.dev.salt = p;
-      if (r.anchor >= 0) {
-        any_anchor = true;
-        double theta = r.angle_threshold > 0 ? r.angle_threshold : (r.direction == SB_DIR_NONE ? M_PI : M_PI / 4);
-        double min_r = 0.0;  // distance_band (relationships.cpp:101-122)
-        if (r.distance_type == SB_DIST_GREATER) min_r = r.distance;
-        if (r.distance_type == SB_DIST_EQUAL)
-          min_r = std::max(0.0, r.distance - std::max(0.05 * r.distance, 0.01));
-        pl.hole = theta >= M_PI - 1e-12 && min_r > 0.0;
-        any_hole = any_hole || pl.hole;
-      }
+      if (r.anchor >= 0) any_anchor = true;
+      any_hole = any_hole || pl.hole;
       places.push_back(pl);
     }
     attempts = sc->attempts;
@@ -1449,6 +1453,11 @@ struct sb_sampler {
   DevArray<SbRegionTri> d_tris;  // canonical table, or all per-instance tables
   DevArray<double> d_cum;
   DevArray<uint32_t> d_inst_tab;  // per instance: (first table row, rows)
+  bool stride_tables = false;     // relation tables: [n][table_cap] rows, d_inst_n each
+  int table_cap = 0;
+  DevArray<int32_t> d_inst_n;
+  DevArray<double> d_states;
+  DevArray<int32_t> d_rflags;
   DevArray<double> d_sup, d_pos;
   DevArray<uint32_t> d_active;
   DevArray<uint8_t> d_pl;
@@ -1520,6 +1529,7 @@ struct sb_sampler {
       cuda_check(cudaMemcpy(d_cum.p, cum.data(), cum.size() * sizeof(double), cudaMemcpyHostToDevice), "H2D table");
     }
     per_instance = inst_rings != nullptr;
+    stride_tables = false;
     n = batch;
     run_seed = seed;
     const uint64_t parts[3] = {seed, salt, 0x63616368ULL};  // bind_stream(stream_key(...))
@@ -1530,6 +1540,87 @@ struct sb_sampler {
       cache_stream = key;
     }
     rng_pos = 0;  // cache_rng_ = make_stream(run_seed, {salt, "cach"})
+    prepared = true;
+  }
+
+  // build_constraint_region (relationships.cpp:161-218) on the device for a batch of
+  // anchor states (x, y, yaw per instance, support frame), then prepare(). The region
+  // kernel decides per_instance exactly as the reference (any anchor moving by > 1e-12);
+  // a canonical region's cache fingerprint is a hash of its sampler table (the polygon
+  // itself never leaves the device).
+  void prepare_relation(const sb_relation& rel, const double rect[4], const double* states,
+                        uint64_t batch, uint64_t seed) {
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    if (batch == 0) throw std::invalid_argument("anchor state batch is empty");
+    if (batch > 0xffffffffull) throw std::invalid_argument("batch_size exceeds 2^32");
+    SbPlacementDev pd;
+    std::memset(&pd, 0, sizeof pd);
+    const bool hole = relation_to_dev(rel, pd);
+    for (int k = 0; k < 4; ++k) pd.rect[k] = rect[k];
+    if (rel.anchor < 0) {  // no anchors: region = support (relationships.cpp:168-171)
+      const double xy[8] = {rect[0], rect[1], rect[2], rect[1], rect[2], rect[3], rect[0], rect[3]};
+      const uint32_t off[2] = {0, 4};
+      prepare(xy, off, 1, nullptr, batch, seed);
+      return;
+    }
+    if (!states) throw std::invalid_argument("anchor states are NULL");
+    int sms = 0;
+    cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "attr");
+    table_cap = hole ? sbp::kHoleCap : SB_REGION_MAX_VERTS;
+    d_tris.ensure(batch * table_cap);
+    d_cum.ensure(batch * table_cap);
+    d_inst_n.ensure(batch);
+    d_states.ensure(3 * batch);
+    d_rflags.ensure(2);
+    cuda_check(cudaMemcpyAsync(d_states.p, states, 3 * batch * sizeof(double), cudaMemcpyHostToDevice, stream), "H2D states");
+    cuda_check(cudaMemsetAsync(d_rflags.p, 0, 2 * sizeof(int32_t), stream), "memset");
+    sbk::RelationRegionParams rp;
+    std::memset(&rp, 0, sizeof rp);
+    rp.w.n = batch;
+    rp.pl = pd;
+    rp.anchor_object = -1;
+    rp.cap = table_cap;
+    rp.hole = hole ? 1 : 0;
+    rp.states = d_states.p;
+    rp.tris = d_tris.p;
+    rp.cum = d_cum.p;
+    rp.ntri = d_inst_n.p;
+    rp.flags = d_rflags.p;
+    sbk::relation_regions(rp, sms, reinterpret_cast<sb_stream_t>(stream));
+    int32_t flags[2], n0 = 0;
+    cuda_check(cudaMemcpyAsync(flags, d_rflags.p, sizeof flags, cudaMemcpyDeviceToHost, stream), "D2H flags");
+    cuda_check(cudaMemcpyAsync(&n0, d_inst_n.p, 4, cudaMemcpyDeviceToHost, stream), "D2H n");
+    cuda_check(cudaStreamSynchronize(stream), "sync");
+    if (flags[1] != 0)
+      throw std::runtime_error("constraint region build failed (status " + std::to_string(flags[1]) + ")");
+    per_instance = flags[0] != 0;
+    stride_tables = true;
+    n = batch;
+    region_nt = per_instance ? 0 : n0;
+    region_empty = !per_instance && n0 == 0;  // an empty (or zero-area) region_for(0)
+    if (!per_instance && n0 > 0) {  // fingerprint of the canonical table
+      std::vector<SbRegionTri> t(n0);
+      std::vector<double> c(n0);
+      cuda_check(cudaMemcpy(t.data(), d_tris.p, n0 * sizeof(SbRegionTri), cudaMemcpyDeviceToHost), "D2H table");
+      cuda_check(cudaMemcpy(c.data(), d_cum.p, n0 * sizeof(double), cudaMemcpyDeviceToHost), "D2H table");
+      uint64_t h = 0x9e3779b97f4a7c15ULL ^ 0x7461626cULL;  // "tabl": never a ring fingerprint
+      auto feed = [&h](const void* p, size_t bytes) {
+        const uint64_t* w = static_cast<const uint64_t*>(p);
+        for (size_t k = 0; k < bytes / 8; ++k) h = sbh::mix64(h ^ w[k]);
+      };
+      feed(t.data(), t.size() * sizeof(SbRegionTri));
+      feed(c.data(), c.size() * sizeof(double));
+      region_fp = h;
+    }
+    run_seed = seed;
+    const uint64_t parts[3] = {seed, salt, 0x63616368ULL};
+    uint64_t key = 0x853c49e6748fea9bULL;
+    for (uint64_t q : parts) key = sbh::mix64(key ^ q);
+    if (cache_stream != key) {
+      clear_queue();
+      cache_stream = key;
+    }
+    rng_pos = 0;
     prepared = true;
   }
 
@@ -1614,7 +1705,8 @@ struct sb_sampler {
     d_active.ensure(m);
     d_pl.ensure(m);
     cuda_check(cudaMemcpyAsync(d_active.p, active, m * 4, cudaMemcpyHostToDevice, stream), "H2D active");
-    sbk::sampler_fallback(d_sup.p, d_active.p, m, run_seed, salt, attempt, d_inst_tab.p, d_tris.p,
+    sbk::sampler_fallback(d_sup.p, d_active.p, m, run_seed, salt, attempt,
+                          stride_tables ? nullptr : d_inst_tab.p, d_inst_n.p, table_cap, d_tris.p,
                           d_cum.p, d_pos.p, d_pl.p, stream);
     cuda_check(cudaMemcpyAsync(pos, d_pos.p, 3 * m * sizeof(double), cudaMemcpyDeviceToHost, stream), "D2H positions");
     cuda_check(cudaMemcpyAsync(placeable, d_pl.p, m, cudaMemcpyDeviceToHost, stream), "D2H placeable");
@@ -1659,6 +1751,14 @@ sb_status sb_sampler_prepare(sb_sampler* s, const double* xy, const uint32_t* of
 sb_status sb_sampler_sample(sb_sampler* s, const double* support, const uint32_t* active, uint64_t m,
                             uint64_t attempt, double* pos, uint8_t* placeable) {
   return guard([&] { s->sample(support, active, m, attempt, pos, placeable); });
+}
+sb_status sb_sampler_prepare_relation(sb_sampler* s, const sb_relation* rel,
+                                      const double support_rect[4], const double* anchor_states,
+                                      uint64_t n, uint64_t run_seed) {
+  return guard([&] {
+    if (!rel || !support_rect) throw std::invalid_argument("relation / support rect is NULL");
+    s->prepare_relation(*rel, support_rect, anchor_states, n, run_seed);
+  });
 }
 sb_status sb_sampler_cache_info(const sb_sampler* s, uint64_t* queue_size, uint64_t* refills) {
   return guard([&] {

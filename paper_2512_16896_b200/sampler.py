@@ -63,6 +63,15 @@ class PositionSampler:
                                            None if inst is None else _up(inst), batch_size,
                                            run_seed))
 
+    def prepare_relation(self, relation, support_rect, anchor_states, run_seed: int):
+        """build_constraint_region + prepare on the device. relation: world.Relation
+        (anchor >= 0 = anchored); anchor_states: (N, 3) x, y, yaw in the support frame."""
+        st = np.ascontiguousarray(anchor_states, np.float64).reshape(-1, 3)
+        rect = np.ascontiguousarray(support_rect, np.float64)
+        r = relation.to_c()
+        A.check(A.lib().sb_sampler_prepare_relation(self._h, C.byref(r), _dp(rect), _dp(st),
+                                                    len(st), run_seed))
+
     def sample(self, support_world: np.ndarray, active: Sequence[int], attempt: int):
         """support_world: (N, 4, 4) poses. Returns (positions (m, 3), placeable uint8 (m,))."""
         sw = colmajor(np.asarray(support_world, np.float64)).reshape(-1, 16)

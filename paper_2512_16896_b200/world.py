@@ -217,6 +217,11 @@ class Relation:
     distance: float = 0.0
     angle_threshold: float = 0.0   # <= 0: default
 
+    def to_c(self) -> "A.sb_relation":
+        return A.sb_relation(self.anchor, self.distance_type, self.direction, self.frame,
+                             (C.c_double * 2)(*self.direction_vector), self.distance,
+                             self.angle_threshold)
+
 
 @dataclass
 class Placement:

@@ -81,3 +81,67 @@ def test_sampler_errors(gpu):
         gpu.sample_orientations(gpu.sampler.FACE_TO, [0], np.zeros((1, 3)), None, 1, 1, 0)
     with pytest.raises(IndexError):
         gpu.sample_orientations(gpu.sampler.FACE_TO, [3], np.zeros((1, 3)), np.zeros((2, 2)), 1, 1, 0)
+
+
+def _relation_cases(pkg):
+    R = pkg.Relation
+    return {
+        "front_less": R(anchor=0, distance_type=A.SB_DIST_LESS, direction=A.SB_DIR_FRONT, distance=0.3),
+        "greater_hole": R(anchor=0, distance_type=A.SB_DIST_GREATER, distance=0.2),
+        "equal_hole": R(anchor=0, distance_type=A.SB_DIST_EQUAL, distance=0.25),
+        "local_vector": R(anchor=0, distance_type=A.SB_DIST_LESS, direction=A.SB_DIR_VECTOR,
+                          direction_vector=(0.3, -0.4), distance=0.35, frame=A.SB_FRAME_LOCAL),
+        "none_dir_right": R(anchor=0, direction=A.SB_DIR_RIGHT),
+        "no_anchor": R(),
+    }
+
+
+@pytest.mark.parametrize("case", ["front_less", "greater_hole", "equal_hole", "local_vector",
+                                  "none_dir_right", "no_anchor"])
+@pytest.mark.parametrize("vary", [True, False])
+def test_prepare_relation_matches_reference(gpu, ref, case, vary):
+    """build_constraint_region + prepare on the device vs the reference: per-instance
+    regions when the anchors move, the canonical region_for(0) through the FIFO cache when
+    they do not (relationships.cpp:178-190)."""
+    rel = _relation_cases(gpu)[case]
+    n = 2000
+    rng = np.random.default_rng(7)
+    rect = np.array([-0.8, -0.6, 0.8, 0.6])
+    if vary:
+        st = np.column_stack([rng.uniform(-0.7, 0.7, n), rng.uniform(-0.5, 0.5, n),
+                              rng.uniform(-3, 3, n)])
+    else:
+        st = np.tile([0.1, -0.2, 0.7], (n, 1))
+    sup = S.supports(n, 3)
+    R_, D = S.RefAdapter(ref, 4), S.DeviceAdapter(gpu, 4)
+    R_.s.prepare_relation(rel.to_c(), rect, st, n, 11)
+    D.s.prepare_relation(rel, rect, st, 11)
+    act = np.arange(n, dtype=np.uint32)
+    for attempt in range(3):
+        pa, la = R_.sample(sup, act, attempt)
+        pb, lb = D.sample(sup, act, attempt)
+        assert np.array_equal(la, lb)
+        # Bit-exact except where glibc misrounds a sin/cos/atan2 that the device rounds
+        # correctly: then one arc vertex, hence the points drawn from the triangles next
+        # to it, move by ulps (DESIGN.md section 5). The canonical local_vector case hits
+        # one: glibc sin(0.20903709499696999) is 1 ulp off (checked with mpmath), so ~1.5%
+        # of its points differ. Tolerance well inside the 1e-5 bar.
+        same = np.all(pa == pb, axis=1)
+        assert same.mean() >= 0.95, f"{np.sum(~same)} of {len(same)} positions differ"
+        np.testing.assert_allclose(pb, pa, rtol=1e-9, atol=1e-12)
+        assert R_.refills() == D.refills()
+        act = act[rng.random(len(act)) < 0.6]
+
+
+def test_prepare_relation_empty_canonical_region(gpu, ref):
+    rel = gpu.Relation(anchor=0, distance_type=A.SB_DIST_LESS, distance=0.05)
+    n, rect = 64, np.array([-0.3, -0.3, 0.3, 0.3])
+    st = np.tile([2.0, 2.0, 0.0], (n, 1))  # anchor far off the support: empty region
+    D = S.DeviceAdapter(gpu, 1)
+    D.s.prepare_relation(rel, rect, st, 3)
+    pos, pl = D.sample(S.supports(n, 1), np.arange(n, dtype=np.uint32), 0)
+    assert not pl.any() and D.refills() == 0
+    R_ = S.RefAdapter(ref, 1)
+    R_.s.prepare_relation(rel.to_c(), rect, st, n, 3)
+    _, lr = R_.sample(S.supports(n, 1), np.arange(n, dtype=np.uint32), 0)
+    assert not lr.any()
