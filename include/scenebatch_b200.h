@@ -310,6 +310,55 @@ sb_status sb_sample_orientations(int kind, const uint32_t* active, uint64_t m,
                                  uint64_t n_targets, uint64_t run_seed, uint64_t placement_salt,
                                  uint64_t attempt, double* yaws, int device);
 
+/* ------------------------------------------------------------------------------------
+ * BatchedSceneGraph (scene_graph.hpp:33-94) with every edge batch resident on one B200:
+ * N transforms per edge, articulated nodes (edge = base * joint motion), batched forward
+ * kinematics (world_poses) on the device, validity mask. Poses cross as column-major
+ * double[16] per instance (TransformBatch memory). Node ids are dense (root = 0).
+ * ---------------------------------------------------------------------------------- */
+typedef struct sb_graph sb_graph;
+typedef struct sb_joint {  /* JointSpec (scene_graph.hpp:19-30) */
+  int32_t kind;            /* 0 revolute, 1 prismatic */
+  double axis[3];          /* normalised by add_node when |axis| != 1 (scene_graph.cpp:9-17) */
+  double lo, hi;
+} sb_joint;
+sb_status sb_graph_create(uint64_t batch_size, int device, sb_graph** out);
+void sb_graph_destroy(sb_graph* g);
+/* add_node(parent, name, geometry_id, joint or NULL) (scene_graph.cpp:54-71) */
+sb_status sb_graph_add_node(sb_graph* g, uint32_t parent, const char* name, int64_t geometry_id,
+                            const sb_joint* joint, uint32_t* id);
+sb_status sb_graph_set_edge_batch(sb_graph* g, uint32_t parent, uint32_t child,
+                                  const double* poses_colmajor16xN);
+sb_status sb_graph_set_edge(sb_graph* g, uint32_t child, uint64_t instance, const double pose[16]);
+sb_status sb_graph_edge_batch(const sb_graph* g, uint32_t child, double* poses_colmajor16xN);
+sb_status sb_graph_set_joint_states(sb_graph* g, uint32_t node, const double* values_N);
+sb_status sb_graph_joint_states(const sb_graph* g, uint32_t node, double* values_N);
+/* world_poses(node) (scene_graph.cpp:131-151): batched FK on the device */
+sb_status sb_graph_world_poses(const sb_graph* g, uint32_t node, double* poses_colmajor16xN);
+/* world_pose(node, instance) (scene_graph.cpp:153-158) */
+sb_status sb_graph_world_pose(const sb_graph* g, uint32_t node, uint64_t instance, double pose[16]);
+/* find(name): *id = -1 when absent */
+sb_status sb_graph_find(const sb_graph* g, const char* name, int64_t* id);
+/* name / parent / geometry / articulated / joint of a node; joint_out may be NULL */
+sb_status sb_graph_node_info(const sb_graph* g, uint32_t node, const char** name,
+                             uint32_t* parent, int64_t* geometry_id, int* articulated,
+                             sb_joint* joint_out);
+uint64_t sb_graph_node_count(const sb_graph* g);
+/* children(node) in ascending id order: up to cap ids into out, the count into *count */
+sb_status sb_graph_children(const sb_graph* g, uint32_t node, uint32_t* out, uint32_t cap,
+                            uint32_t* count);
+sb_status sb_graph_is_tree(const sb_graph* g, int* is_tree);
+sb_status sb_graph_valid_mask(const sb_graph* g, uint8_t* mask_N);
+sb_status sb_graph_mark_invalid(sb_graph* g, uint64_t instance);
+sb_status sb_graph_reset_validity(sb_graph* g);
+sb_status sb_graph_valid_count(const sb_graph* g, uint64_t* count);
+/* Accepted-pose write-back: the engine's last run, placement
+ * `placement`, into `node` (a child of the root: its edge is the world pose; an
+ * articulated node receives it as its base) for the engine's local instances, and every
+ * instance the run left invalid is marked invalid in the graph. Device to device; the
+ * graph must live on the engine's GPU and have its local batch size. */
+sb_status sb_engine_write_back(sb_engine* e, uint32_t placement, sb_graph* g, uint32_t node);
+
 /* Diagnostics: evaluate the device libm used on the hot path (correctly rounded
  * double-double sin/cos/atan2, replacing glibc's std::sin/cos/atan2 in transform.hpp:47,
  * polygon.cpp:151, relationships.cpp:184,238) on n inputs on device 0.

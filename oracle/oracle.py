@@ -95,6 +95,22 @@ def lib():
                                                    u64, u64]
         L.ref_sample_orientations.argtypes = [C.c_int, C.c_void_p, u64, C.c_void_p, C.c_void_p,
                                               u64, u64, u64, u64, C.c_void_p]
+        L.ref_graph_create.restype = C.c_void_p
+        L.ref_graph_create.argtypes = [u64]
+        L.ref_graph_destroy.argtypes = [C.c_void_p]
+        L.ref_graph_add_node.argtypes = [C.c_void_p, C.c_uint32, C.c_char_p, C.c_int64, C.c_int,
+                                         C.c_int, C.c_void_p, C.c_double, C.c_double, C.c_void_p]
+        L.ref_graph_set_edge_batch.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p]
+        L.ref_graph_set_edge.argtypes = [C.c_void_p, C.c_uint32, u64, C.c_void_p]
+        L.ref_graph_edge_batch.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p]
+        L.ref_graph_set_joint_states.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p, u64]
+        L.ref_graph_joint_states.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p]
+        L.ref_graph_world_poses.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p]
+        L.ref_graph_world_pose.argtypes = [C.c_void_p, C.c_uint32, u64, C.c_void_p]
+        L.ref_graph_is_tree.argtypes = [C.c_void_p]
+        L.ref_graph_mark_invalid.argtypes = [C.c_void_p, u64]
+        L.ref_graph_valid_count.restype = u64
+        L.ref_graph_valid_count.argtypes = [C.c_void_p]
         _lib = L
     return _lib
 
@@ -328,3 +344,80 @@ def sample_orientations(kind: int, active, positions, face_xy, run_seed: int, sa
                                         0 if fx is None else fx.shape[0], run_seed, salt, attempt,
                                         _p(y)))
     return y
+
+
+def _cm(poses):  # (..., 4, 4) -> column-major (..., 16)
+    p = np.asarray(poses, np.float64)
+    return np.ascontiguousarray(np.swapaxes(p, -1, -2)).reshape(p.shape[:-2] + (16,))
+
+
+def _uncm(flat):
+    f = np.asarray(flat, np.float64)
+    return np.swapaxes(f.reshape(f.shape[:-1] + (4, 4)), -1, -2).copy()
+
+
+class RefGraph:
+    """The reference's BatchedSceneGraph (scene_graph.cpp) with the package's Python API."""
+
+    def __init__(self, n: int):
+        self.h = lib().ref_graph_create(n)
+        if not self.h:
+            raise ValueError(lib().ref_last_error().decode())
+        self.n = n
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().ref_graph_destroy(self.h)
+            self.h = None
+
+    def add_node(self, parent, name, geometry_id=-1, joint=None):
+        out = C.c_uint32()
+        ax = np.ascontiguousarray(joint.axis if joint is not None else (0, 0, 1), np.float64)
+        check(lib().ref_graph_add_node(self.h, parent, name.encode(), geometry_id,
+                                       1 if joint is not None else 0,
+                                       joint.kind if joint is not None else 0, _p(ax),
+                                       joint.lo if joint is not None else 0.0,
+                                       joint.hi if joint is not None else 0.0, C.byref(out)))
+        return out.value
+
+    def set_edge_batch(self, parent, child, transforms):
+        t = _cm(transforms).reshape(-1, 16)
+        check(lib().ref_graph_set_edge_batch(self.h, parent, child, _p(t)))
+
+    def set_edge(self, child, instance, transform):
+        t = _cm(transform).reshape(16)
+        check(lib().ref_graph_set_edge(self.h, child, instance, _p(t)))
+
+    def _batch(self, fn, node):
+        out = np.empty((self.n, 16))
+        check(fn(self.h, node, _p(out)))
+        return _uncm(out)
+
+    def edge_batch(self, child):
+        return self._batch(lib().ref_graph_edge_batch, child)
+
+    def world_poses(self, node):
+        return self._batch(lib().ref_graph_world_poses, node)
+
+    def world_pose(self, node, instance):
+        out = np.empty(16)
+        check(lib().ref_graph_world_pose(self.h, node, instance, _p(out)))
+        return _uncm(out)
+
+    def set_joint_states(self, node, values):
+        v = np.ascontiguousarray(values, np.float64)
+        check(lib().ref_graph_set_joint_states(self.h, node, _p(v), len(v)))
+
+    def joint_states(self, node):
+        out = np.empty(self.n)
+        check(lib().ref_graph_joint_states(self.h, node, _p(out)))
+        return out
+
+    def is_tree(self):
+        return bool(lib().ref_graph_is_tree(self.h))
+
+    def mark_invalid(self, i):
+        lib().ref_graph_mark_invalid(self.h, i)
+
+    def valid_count(self):
+        return lib().ref_graph_valid_count(self.h)

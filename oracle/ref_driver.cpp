@@ -27,6 +27,7 @@
 #include "scenebatch/relationships.hpp"
 #include "scenebatch/rng.hpp"
 #include "scenebatch/sampler.hpp"
+#include "scenebatch/scene_graph.hpp"
 #include "scenebatch/trimesh.hpp"
 #include "scenebatch_b200.h"
 
@@ -316,6 +317,76 @@ int ref_sample_orientations(int kind, const uint32_t* active, uint64_t m, const 
     for (uint64_t j = 0; j < m; ++j) yaws[j] = y[j];
   });
 }
+
+// ---------------------------------------------------------------- BatchedSceneGraph
+// scene_graph.hpp:33-94 over column-major double[16] batches.
+static Mat4 mat_from16(const double* c) {
+  Mat4 m;
+  for (int col = 0; col < 4; ++col)
+    for (int r = 0; r < 4; ++r) m(r, col) = c[4 * col + r];
+  return m;
+}
+static void mat_to16(const Mat4& m, double* c) {
+  for (int col = 0; col < 4; ++col)
+    for (int r = 0; r < 4; ++r) c[4 * col + r] = m(r, col);
+}
+void* ref_graph_create(uint64_t n) {
+  try {
+    return new BatchedSceneGraph(n);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+void ref_graph_destroy(void* h) { delete static_cast<BatchedSceneGraph*>(h); }
+int ref_graph_add_node(void* h, uint32_t parent, const char* name, int64_t geom, int has_joint,
+                       int kind, const double* axis, double lo, double hi, uint32_t* id) {
+  REF_TRY({
+    std::optional<JointSpec> j;
+    if (has_joint)
+      j = JointSpec(kind == 1 ? JointSpec::Kind::prismatic : JointSpec::Kind::revolute,
+                    Vec3(axis[0], axis[1], axis[2]), lo, hi);
+    *id = static_cast<BatchedSceneGraph*>(h)->add_node(NodeId{parent}, name, geom, j).index;
+  });
+}
+int ref_graph_set_edge_batch(void* h, uint32_t parent, uint32_t child, const double* t16) {
+  REF_TRY({
+    auto& g = *static_cast<BatchedSceneGraph*>(h);
+    TransformBatch t(g.batch_size());
+    for (std::size_t i = 0; i < g.batch_size(); ++i) t[i] = mat_from16(t16 + 16 * i);
+    g.set_edge_batch(NodeId{parent}, NodeId{child}, t);
+  });
+}
+int ref_graph_set_edge(void* h, uint32_t child, uint64_t i, const double* m16) {
+  REF_TRY(static_cast<BatchedSceneGraph*>(h)->set_edge(NodeId{child}, i, mat_from16(m16)));
+}
+int ref_graph_edge_batch(void* h, uint32_t child, double* out16) {
+  REF_TRY({
+    const auto& t = static_cast<BatchedSceneGraph*>(h)->edge_batch(NodeId{child});
+    for (std::size_t i = 0; i < t.size(); ++i) mat_to16(t[i], out16 + 16 * i);
+  });
+}
+int ref_graph_set_joint_states(void* h, uint32_t node, const double* v, uint64_t n) {
+  REF_TRY(static_cast<BatchedSceneGraph*>(h)->set_joint_states(NodeId{node}, std::span<const double>(v, n)));
+}
+int ref_graph_joint_states(void* h, uint32_t node, double* out) {
+  REF_TRY({
+    const auto& v = static_cast<BatchedSceneGraph*>(h)->joint_states(NodeId{node});
+    for (std::size_t i = 0; i < v.size(); ++i) out[i] = v[i];
+  });
+}
+int ref_graph_world_poses(void* h, uint32_t node, double* out16) {
+  REF_TRY({
+    TransformBatch t = static_cast<BatchedSceneGraph*>(h)->world_poses(NodeId{node});
+    for (std::size_t i = 0; i < t.size(); ++i) mat_to16(t[i], out16 + 16 * i);
+  });
+}
+int ref_graph_world_pose(void* h, uint32_t node, uint64_t i, double* out16) {
+  REF_TRY(mat_to16(static_cast<BatchedSceneGraph*>(h)->world_pose(NodeId{node}, i), out16));
+}
+int ref_graph_is_tree(void* h) { return static_cast<BatchedSceneGraph*>(h)->is_tree() ? 1 : 0; }
+void ref_graph_mark_invalid(void* h, uint64_t i) { static_cast<BatchedSceneGraph*>(h)->mark_invalid(i); }
+uint64_t ref_graph_valid_count(void* h) { return static_cast<BatchedSceneGraph*>(h)->valid_count(); }
 
 // ---------------------------------------------------------------- CollisionWorld
 void* ref_world_create(uint64_t n, double margin, int threads) {

@@ -43,6 +43,11 @@ class sb_support(C.Structure):
     _fields_ = [("pose", C.c_double * 16), ("rect", C.c_double * 4)]
 
 
+class sb_joint(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("axis", C.c_double * 3), ("lo", C.c_double),
+                ("hi", C.c_double)]
+
+
 class sb_relation(C.Structure):
     _fields_ = [("anchor", C.c_int32), ("distance_type", C.c_int32), ("direction", C.c_int32),
                 ("frame", C.c_int32), ("direction_vector", C.c_double * 2),
@@ -135,6 +140,28 @@ SIGNATURES = {
                                     C.POINTER(C.c_uint8)]),
     "sb_sampler_prepare_relation": (C.c_int, [_P, C.POINTER(sb_relation), _D, _D, C.c_uint64,
                                               C.c_uint64]),
+    "sb_graph_create": (C.c_int, [C.c_uint64, C.c_int, C.POINTER(_P)]),
+    "sb_graph_destroy": (None, [_P]),
+    "sb_graph_add_node": (C.c_int, [_P, C.c_uint32, C.c_char_p, C.c_int64, C.POINTER(sb_joint),
+                                    C.POINTER(C.c_uint32)]),
+    "sb_graph_set_edge_batch": (C.c_int, [_P, C.c_uint32, C.c_uint32, _D]),
+    "sb_graph_set_edge": (C.c_int, [_P, C.c_uint32, C.c_uint64, _D]),
+    "sb_graph_edge_batch": (C.c_int, [_P, C.c_uint32, _D]),
+    "sb_graph_set_joint_states": (C.c_int, [_P, C.c_uint32, _D]),
+    "sb_graph_joint_states": (C.c_int, [_P, C.c_uint32, _D]),
+    "sb_graph_world_poses": (C.c_int, [_P, C.c_uint32, _D]),
+    "sb_graph_world_pose": (C.c_int, [_P, C.c_uint32, C.c_uint64, _D]),
+    "sb_graph_find": (C.c_int, [_P, C.c_char_p, C.POINTER(C.c_int64)]),
+    "sb_graph_node_info": (C.c_int, [_P, C.c_uint32, C.POINTER(C.c_char_p), C.POINTER(C.c_uint32),
+                                     C.POINTER(C.c_int64), C.POINTER(C.c_int), C.POINTER(sb_joint)]),
+    "sb_graph_node_count": (C.c_uint64, [_P]),
+    "sb_graph_children": (C.c_int, [_P, C.c_uint32, _U32, C.c_uint32, C.POINTER(C.c_uint32)]),
+    "sb_graph_is_tree": (C.c_int, [_P, C.POINTER(C.c_int)]),
+    "sb_graph_valid_mask": (C.c_int, [_P, C.POINTER(C.c_uint8)]),
+    "sb_graph_mark_invalid": (C.c_int, [_P, C.c_uint64]),
+    "sb_graph_reset_validity": (C.c_int, [_P]),
+    "sb_graph_valid_count": (C.c_int, [_P, C.POINTER(C.c_uint64)]),
+    "sb_engine_write_back": (C.c_int, [_P, C.c_uint32, _P, C.c_uint32]),
     "sb_sampler_cache_info": (C.c_int, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "sb_sample_orientations": (C.c_int, [C.c_int, _U32, C.c_uint64, _D, _D, C.c_uint64,
                                          C.c_uint64, C.c_uint64, C.c_uint64, _D, C.c_int]),

@@ -1,0 +1,220 @@
+// BatchedSceneGraph on the device (scene_graph.hpp:33-94, scene_graph.cpp:9-196): per-node
+// edge batches stay in HBM as row-major 3x4 records (bottom row (0,0,0,1) by the
+// is_homogeneous contract), articulated nodes add a base batch and joint values, and the
+// batched forward kinematics is one thread per instance walking the root -> node chain.
+// Products use the reference's (shim) operation order (mul34), joint motions the Rodrigues
+// form of Eigen::AngleAxis::toRotationMatrix with the correctly rounded sin/cos.
+#include <stdexcept>
+#include <string>
+
+#include "sb_crmath.cuh"
+#include "sb_dev.cuh"
+#include "sb_graph.h"
+
+using namespace sbd;
+
+namespace {
+
+constexpr int kBlock = 256;
+
+inline unsigned grid_for(uint64_t n) { return static_cast<unsigned>((n + kBlock - 1) / kBlock); }
+
+inline void check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+__device__ __forceinline__ void load34(const double* p, M34& M) {
+  const double2* q = reinterpret_cast<const double2*>(p);
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    const double2 v = __ldg(q + k);
+    M.m[2 * k] = v.x;
+    M.m[2 * k + 1] = v.y;
+  }
+}
+__device__ __forceinline__ void store34(double* p, const M34& M) {
+  double2* q = reinterpret_cast<double2*>(p);
+#pragma unroll
+  for (int k = 0; k < 6; ++k) q[k] = make_double2(M.m[2 * k], M.m[2 * k + 1]);
+}
+__device__ __forceinline__ void store_colmajor(double* o, const M34& M) {
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) o[4 * c + r] = M.m[4 * r + c];
+  o[3] = o[7] = o[11] = 0.0;
+  o[15] = 1.0;
+}
+
+// JointSpec::motion (scene_graph.cpp:19-27): prismatic = translation(axis * v); revolute =
+// AngleAxisd(v, axis).toRotationMatrix() (Rodrigues, Eigen's operation order).
+__device__ __forceinline__ void joint_motion(const sbk::GraphJoint& j, double v, M34& m) {
+#pragma unroll
+  for (int k = 0; k < 12; ++k) m.m[k] = 0.0;
+  m.m[0] = m.m[5] = m.m[10] = 1.0;
+  const double ax = j.axis[0], ay = j.axis[1], az = j.axis[2];
+  if (j.kind == 1) {
+    m.m[3] = ax * v;
+    m.m[7] = ay * v;
+    m.m[11] = az * v;
+    return;
+  }
+  double s, c;
+  sbm::sincos_cr(v, &s, &c);
+  const double sx = ax * s, sy = ay * s, sz = az * s;
+  const double c1 = 1.0 - c;
+  const double cx = ax * c1, cy = ay * c1, cz = az * c1;
+  double t = cx * ay;
+  m.m[1] = t - sz;
+  m.m[4] = t + sz;
+  t = cx * az;
+  m.m[2] = t + sy;
+  m.m[8] = t - sy;
+  t = cy * az;
+  m.m[6] = t - sx;
+  m.m[9] = t + sx;
+  m.m[0] = cx * ax + c;
+  m.m[5] = cy * ay + c;
+  m.m[10] = cz * az + c;
+}
+
+__global__ void k_colmajor_to_34(const double* in16, uint64_t n, double* out12) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* c = in16 + 16 * i;
+  M34 M;
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) M.m[4 * r + k] = c[4 * k + r];
+  store34(out12 + 12 * i, M);
+}
+
+__global__ void k_34_to_colmajor(const double* in12, uint64_t n, double* out16) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  M34 M;
+  load34(in12 + 12 * i, M);
+  store_colmajor(out16 + 16 * i, M);
+}
+
+// edge[i] = base[i] * motion(value[i]) for instances [i0, i0 + n); base == NULL: the
+// add_node initialisation edge[i] = motion(value[i]) (scene_graph.cpp:63-67).
+__global__ void k_joint_compose(const double* base, const double* values, uint64_t i0, uint64_t n,
+                                sbk::GraphJoint j, double* edge) {
+  const uint64_t i = i0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= i0 + n) return;
+  M34 B, J, E;
+  joint_motion(j, values[i], J);
+  if (base) {
+    load34(base + 12 * i, B);
+    mul34(B, J, E);
+    store34(edge + 12 * i, E);
+  } else {
+    store34(edge + 12 * i, J);
+  }
+}
+
+// world_poses (scene_graph.cpp:131-151): acc = edge[chain[d-1]]; acc = acc * edge[chain[k]]
+// for k = d-2 .. 0 (chain[0] = the node). Output column-major Mat4 per instance.
+__global__ void k_world_poses(const double* const* chain, int depth, uint64_t n, double* out16) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  M34 acc, E, T;
+  load34(chain[depth - 1] + 12 * i, acc);
+  for (int k = depth - 2; k >= 0; --k) {
+    load34(chain[k] + 12 * i, E);
+    mul34(acc, E, T);
+    acc = T;
+  }
+  store_colmajor(out16 + 16 * i, acc);
+}
+
+// world_pose (scene_graph.cpp:153-158): acc = Identity; acc = edge[cur] * acc walking up.
+__global__ void k_world_pose_one(const double* const* chain, int depth, uint64_t i, double* out16) {
+  M34 acc, E, T;
+#pragma unroll
+  for (int k = 0; k < 12; ++k) acc.m[k] = 0.0;
+  acc.m[0] = acc.m[5] = acc.m[10] = 1.0;
+  for (int k = 0; k < depth; ++k) {
+    load34(chain[k] + 12 * i, E);
+    mul34(E, acc, T);
+    acc = T;
+  }
+  store_colmajor(out16, acc);
+}
+
+__global__ void k_count_valid(const uint8_t* v, uint64_t n, unsigned long long* out) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const unsigned c = i < n && v[i] != 0 ? 1u : 0u;
+  const unsigned s = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, (unsigned long long)s);
+}
+
+// Engine write-back: the accepted world pose of `obj` per instance (instance-major world
+// records) into a node's edge (or base) batch.
+__global__ void k_gather_object_poses(const double* pose, uint64_t obj_stride, uint64_t inst_stride,
+                                      uint64_t n, double* out12) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  M34 M;
+  load34(pose + i * inst_stride + obj_stride, M);
+  store34(out12 + 12 * i, M);
+}
+
+__global__ void k_and_mask(uint8_t* dst, const uint8_t* src, uint64_t n) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i < n && src[i] == 0) dst[i] = 0;
+}
+
+}  // namespace
+
+namespace sbk {
+
+void graph_and_valid(uint8_t* dst, const uint8_t* src, uint64_t n, sb_stream_t s) {
+  if (!n) return;
+  k_and_mask<<<grid_for(n), kBlock, 0, s>>>(dst, src, n);
+  check_launch("graph_and_valid");
+}
+
+void graph_colmajor_to_34(const double* in16, uint64_t n, double* out12, sb_stream_t s) {
+  if (!n) return;
+  k_colmajor_to_34<<<grid_for(n), kBlock, 0, s>>>(in16, n, out12);
+  check_launch("graph_colmajor_to_34");
+}
+void graph_34_to_colmajor(const double* in12, uint64_t n, double* out16, sb_stream_t s) {
+  if (!n) return;
+  k_34_to_colmajor<<<grid_for(n), kBlock, 0, s>>>(in12, n, out16);
+  check_launch("graph_34_to_colmajor");
+}
+void graph_joint_compose(const double* base, const double* values, uint64_t i0, uint64_t n,
+                         const GraphJoint& j, double* edge, sb_stream_t s) {
+  if (!n) return;
+  k_joint_compose<<<grid_for(n), kBlock, 0, s>>>(base, values, i0, n, j, edge);
+  check_launch("graph_joint_compose");
+}
+void graph_world_poses(const double* const* chain, int depth, uint64_t n, double* out16,
+                       sb_stream_t s) {
+  if (!n) return;
+  k_world_poses<<<grid_for(n), kBlock, 0, s>>>(chain, depth, n, out16);
+  check_launch("graph_world_poses");
+}
+void graph_world_pose_one(const double* const* chain, int depth, uint64_t i, double* out16,
+                          sb_stream_t s) {
+  k_world_pose_one<<<1, 1, 0, s>>>(chain, depth, i, out16);
+  check_launch("graph_world_pose_one");
+}
+void graph_count_valid(const uint8_t* v, uint64_t n, unsigned long long* out, sb_stream_t s) {
+  if (!n) return;
+  k_count_valid<<<grid_for(n), kBlock, 0, s>>>(v, n, out);
+  check_launch("graph_count_valid");
+}
+void graph_gather_object_poses(const double* pose, uint64_t obj_stride, uint64_t inst_stride,
+                               uint64_t n, double* out12, sb_stream_t s) {
+  if (!n) return;
+  k_gather_object_poses<<<grid_for(n), kBlock, 0, s>>>(pose, obj_stride, inst_stride, n, out12);
+  check_launch("graph_gather_object_poses");
+}
+
+}  // namespace sbk

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "../../include/scenebatch_b200.h"
+#include "sb_graph.h"
 #include "sb_host.hpp"
 #include "sb_kernels.h"
 #include "sb_place.h"
@@ -470,6 +471,7 @@ struct sb_world {
 // ===================================================================== Engine
 struct sb_engine {
   std::unique_ptr<sb_world> world;
+  void write_back(uint32_t placement, sb_graph& g, uint32_t node);  // defined after sb_graph
   uint64_t n_total = 0, begin = 0, end = 0, n = 0;
   int rank = 0, world_size = 1;
   sb_allgather_fn allgather = nullptr;
@@ -1799,6 +1801,373 @@ sb_status sb_sample_orientations(int kind, const uint32_t* active, uint64_t m, c
     cuda_check(cudaMemcpyAsync(yaws, o.yaws.p, m * sizeof(double), cudaMemcpyDeviceToHost, o.stream), "D2H yaws");
     cuda_check(cudaStreamSynchronize(o.stream), "sync");
   });
+}
+
+}  // extern "C"
+
+// ===================================================================== BatchedSceneGraph
+// scene_graph.hpp:33-94. Names, parents and joint specs are host metadata; every per-
+// instance batch (edges, bases, joint values, validity) lives in HBM (sb_graph.cu).
+namespace {
+bool homogeneous16(const double* m) {  // is_homogeneous (transform.hpp:28-30)
+  return m[3] == 0.0 && m[7] == 0.0 && m[11] == 0.0 && m[15] == 1.0;
+}
+}  // namespace
+
+struct sb_graph {
+  uint64_t n;
+  int device;
+  cudaStream_t stream = nullptr;
+  struct Node {
+    std::string name;
+    uint32_t parent = 0;
+    int64_t geometry = -1;
+    bool joint = false;
+    sb_joint spec{};
+    std::unique_ptr<DevArray<double>> edge, base, values;
+  };
+  std::vector<Node> nodes;
+  std::unordered_map<std::string, uint32_t> by_name;
+  DevArray<uint8_t> d_valid;
+  mutable DevArray<double> d_tmp16;
+  mutable DevArray<const double*> d_chain;
+  mutable DevArray<unsigned long long> d_count;
+
+  sb_graph(uint64_t batch, int dev) : n(batch), device(current_device_checked(dev)) {
+    if (batch == 0) throw std::invalid_argument("batch_size must be >= 1");
+    cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    d_valid.alloc(n);
+    cuda_check(cudaMemsetAsync(d_valid.p, 1, n, stream), "memset");
+    Node world;
+    world.name = "world";
+    world.edge = std::make_unique<DevArray<double>>();
+    identity_batch(*world.edge);
+    by_name.emplace("world", 0);
+    nodes.push_back(std::move(world));
+    sync();
+  }
+  ~sb_graph() {
+    if (stream) {
+      cudaSetDevice(device);
+      cudaStreamSynchronize(stream);
+      cudaStreamDestroy(stream);
+    }
+  }
+  sb_stream_t s() const { return reinterpret_cast<sb_stream_t>(stream); }
+  void activate() const { cuda_check(cudaSetDevice(device), "cudaSetDevice"); }
+  void sync() const { cuda_check(cudaStreamSynchronize(stream), "sync"); }
+
+  void identity_batch(DevArray<double>& a) {
+    a.alloc(12 * n);
+    std::vector<double> one(16, 0.0);
+    one[0] = one[5] = one[10] = one[15] = 1.0;
+    d_tmp16.ensure(16 * n);
+    std::vector<double> host(16 * n);
+    for (uint64_t i = 0; i < n; ++i) std::memcpy(&host[16 * i], one.data(), sizeof(double) * 16);
+    cuda_check(cudaMemcpyAsync(d_tmp16.p, host.data(), 16 * n * sizeof(double), cudaMemcpyHostToDevice, stream), "H2D");
+    sbk::graph_colmajor_to_34(d_tmp16.p, n, a.p, s());
+    sync();
+  }
+  const Node& at(uint32_t id) const {
+    if (id >= nodes.size()) throw std::out_of_range("unknown node");
+    return nodes[id];
+  }
+  Node& at(uint32_t id) {
+    if (id >= nodes.size()) throw std::out_of_range("unknown node");
+    return nodes[id];
+  }
+  static sbk::GraphJoint gj(const sb_joint& j) {
+    sbk::GraphJoint g;
+    g.kind = j.kind;
+    for (int k = 0; k < 3; ++k) g.axis[k] = j.axis[k];
+    return g;
+  }
+  // edge = base * motion(values) over all instances (or motion alone when base == NULL)
+  void compose(Node& nd, bool with_base) {
+    sbk::graph_joint_compose(with_base ? nd.base->p : nullptr, nd.values->p, 0, n, gj(nd.spec),
+                             nd.edge->p, s());
+  }
+
+  uint32_t add_node(uint32_t parent, const char* name_c, int64_t geometry, const sb_joint* joint) {
+    activate();
+    at(parent);
+    if (!name_c) throw std::invalid_argument("node name is NULL");
+    const std::string name(name_c);
+    if (by_name.count(name)) throw std::invalid_argument("duplicate node name: " + name);
+    Node nd;
+    nd.name = name;
+    nd.parent = parent;
+    nd.geometry = geometry;
+    nd.edge = std::make_unique<DevArray<double>>();
+    if (joint) {  // JointSpec ctor (scene_graph.cpp:9-17)
+      sb_joint j = *joint;
+      if (j.kind != 0 && j.kind != 1) throw std::invalid_argument("JointSpec: unknown kind");
+      if (j.lo > j.hi) throw std::invalid_argument("JointSpec: lo > hi");
+      const double nrm = std::sqrt((j.axis[0] * j.axis[0] + j.axis[1] * j.axis[1]) + j.axis[2] * j.axis[2]);
+      if (std::abs(nrm - 1.0) > 1e-9) {
+        if (nrm < 1e-12) throw std::invalid_argument("JointSpec: zero axis");
+        for (int k = 0; k < 3; ++k) j.axis[k] = j.axis[k] / nrm;
+      }
+      nd.joint = true;
+      nd.spec = j;
+      nd.base = std::make_unique<DevArray<double>>();
+      identity_batch(*nd.base);
+      nd.values = std::make_unique<DevArray<double>>();
+      nd.values->alloc(n);
+      std::vector<double> lo(n, j.lo);
+      cuda_check(cudaMemcpyAsync(nd.values->p, lo.data(), n * sizeof(double), cudaMemcpyHostToDevice, stream), "H2D");
+      nd.edge->alloc(12 * n);
+      compose(nd, false);  // every edge = motion(lo)
+      sync();
+    } else {
+      identity_batch(*nd.edge);
+    }
+    const uint32_t id = static_cast<uint32_t>(nodes.size());
+    by_name.emplace(name, id);
+    nodes.push_back(std::move(nd));
+    return id;
+  }
+
+  void set_edge_batch(uint32_t parent, uint32_t child, const double* t16) {
+    activate();
+    Node& nd = at(child);
+    if (nd.parent != parent || child == 0)
+      throw std::invalid_argument("no such edge: " + at(parent).name + " -> " + nd.name);
+    if (!t16) throw std::invalid_argument("transform batch is NULL");
+    for (uint64_t i = 0; i < n; ++i)
+      if (!homogeneous16(t16 + 16 * i)) throw std::invalid_argument("non-homogeneous matrix in batch");
+    d_tmp16.ensure(16 * n);
+    cuda_check(cudaMemcpyAsync(d_tmp16.p, t16, 16 * n * sizeof(double), cudaMemcpyHostToDevice, stream), "H2D");
+    sbk::graph_colmajor_to_34(d_tmp16.p, n, nd.joint ? nd.base->p : nd.edge->p, s());
+    if (nd.joint) compose(nd, true);
+    sync();
+  }
+
+  void set_edge(uint32_t child, uint64_t i, const double* m16) {
+    activate();
+    Node& nd = at(child);
+    if (child == 0) throw std::invalid_argument("cannot set edge on root");
+    if (i >= n) throw std::out_of_range("instance out of range");
+    if (!m16 || !homogeneous16(m16)) throw std::invalid_argument("non-homogeneous matrix");
+    double r[12];
+    colmajor_to_34(m16, r);
+    double* dst = (nd.joint ? nd.base->p : nd.edge->p) + 12 * i;
+    cuda_check(cudaMemcpyAsync(dst, r, sizeof r, cudaMemcpyHostToDevice, stream), "H2D");
+    if (nd.joint)
+      sbk::graph_joint_compose(nd.base->p, nd.values->p, i, 1, gj(nd.spec), nd.edge->p, s());
+    sync();
+  }
+
+  void edge_batch(uint32_t child, double* out16) const {
+    activate();
+    const Node& nd = at(child);
+    download16(nd.edge->p, out16);
+  }
+  void download16(const double* d12, double* out16) const {
+    d_tmp16.ensure(16 * n);
+    sbk::graph_34_to_colmajor(d12, n, d_tmp16.p, s());
+    cuda_check(cudaMemcpyAsync(out16, d_tmp16.p, 16 * n * sizeof(double), cudaMemcpyDeviceToHost, stream), "D2H");
+    sync();
+  }
+
+  void set_joint_states(uint32_t node, const double* v) {
+    activate();
+    Node& nd = at(node);
+    if (!nd.joint) throw std::invalid_argument("node is not articulated: " + nd.name);
+    if (!v) throw std::invalid_argument("joint values are NULL");
+    for (uint64_t i = 0; i < n; ++i)
+      if (v[i] < nd.spec.lo - 1e-12 || v[i] > nd.spec.hi + 1e-12)
+        throw std::invalid_argument("joint value out of limits for " + nd.name);
+    cuda_check(cudaMemcpyAsync(nd.values->p, v, n * sizeof(double), cudaMemcpyHostToDevice, stream), "H2D");
+    compose(nd, true);
+    sync();
+  }
+  void joint_states(uint32_t node, double* out) const {
+    activate();
+    const Node& nd = at(node);
+    if (!nd.joint) throw std::invalid_argument("node is not articulated: " + nd.name);
+    cuda_check(cudaMemcpyAsync(out, nd.values->p, n * sizeof(double), cudaMemcpyDeviceToHost, stream), "D2H");
+    sync();
+  }
+
+  // root -> node chain as device pointers, chain[0] = node
+  int upload_chain(uint32_t node) const {
+    std::vector<const double*> chain;
+    for (uint32_t cur = node; cur != 0; cur = nodes[cur].parent) {
+      chain.push_back(nodes[cur].edge->p);
+      if (chain.size() > nodes.size()) throw std::logic_error("scene graph is not a tree");
+    }
+    if (!chain.empty()) {
+      d_chain.ensure(chain.size());
+      cuda_check(cudaMemcpyAsync(d_chain.p, chain.data(), chain.size() * sizeof(void*), cudaMemcpyHostToDevice, stream), "H2D chain");
+    }
+    return static_cast<int>(chain.size());
+  }
+  void world_poses(uint32_t node, double* out16) const {
+    activate();
+    at(node);
+    const int depth = upload_chain(node);
+    if (depth == 0) {  // the root: N identities
+      download16(nodes[0].edge->p, out16);
+      return;
+    }
+    d_tmp16.ensure(16 * n);
+    sbk::graph_world_poses(d_chain.p, depth, n, d_tmp16.p, s());
+    cuda_check(cudaMemcpyAsync(out16, d_tmp16.p, 16 * n * sizeof(double), cudaMemcpyDeviceToHost, stream), "D2H");
+    sync();
+  }
+  void world_pose(uint32_t node, uint64_t i, double* out16) const {
+    activate();
+    if (i >= n) throw std::out_of_range("instance out of range");
+    at(node);
+    const int depth = upload_chain(node);
+    d_tmp16.ensure(16);
+    sbk::graph_world_pose_one(d_chain.p, depth, i, d_tmp16.p, s());
+    cuda_check(cudaMemcpyAsync(out16, d_tmp16.p, 16 * sizeof(double), cudaMemcpyDeviceToHost, stream), "D2H");
+    sync();
+  }
+  bool is_tree() const {  // scene_graph.cpp:174-187
+    for (uint32_t i = 1; i < nodes.size(); ++i) {
+      std::vector<bool> seen(nodes.size(), false);
+      uint32_t cur = i;
+      while (cur != 0) {
+        if (seen[cur]) return false;
+        seen[cur] = true;
+        cur = nodes[cur].parent;
+      }
+    }
+    return true;
+  }
+  uint64_t valid_count() const {
+    activate();
+    d_count.ensure(1);
+    cuda_check(cudaMemsetAsync(d_count.p, 0, sizeof(unsigned long long), stream), "memset");
+    sbk::graph_count_valid(d_valid.p, n, d_count.p, s());
+    unsigned long long c = 0;
+    cuda_check(cudaMemcpyAsync(&c, d_count.p, sizeof c, cudaMemcpyDeviceToHost, stream), "D2H");
+    sync();
+    return c;
+  }
+};
+
+void sb_engine::write_back(uint32_t p, sb_graph& g, uint32_t node) {
+  if (p >= places.size()) throw std::out_of_range("placement index out of range");
+  if (g.n != n) throw std::invalid_argument("write_back: graph batch size != engine local instances");
+  if (g.device != world->device) throw std::invalid_argument("write_back: graph and engine on different devices");
+  sb_graph::Node& nd = g.at(node);
+  if (node == 0 || nd.parent != 0)
+    throw std::invalid_argument("write_back: node must be a child of the root (world-frame edge)");
+  world->activate();
+  cuda_check(cudaStreamSynchronize(world->stream), "sync");  // the last run is complete
+  const SbWorldView wv = world->view();
+  sbk::graph_gather_object_poses(wv.pose, 12ull * static_cast<uint64_t>(places[p].dev.object),
+                                 12ull * static_cast<uint64_t>(wv.obj_stride), n,
+                                 nd.joint ? nd.base->p : nd.edge->p, g.s());
+  if (nd.joint) g.compose(nd, true);
+  sbk::graph_and_valid(g.d_valid.p, d_valid.p, n, g.s());
+  g.sync();
+}
+
+extern "C" {
+
+sb_status sb_graph_create(uint64_t batch, int device, sb_graph** out) {
+  return guard([&] {
+    if (!out) throw std::invalid_argument("out is NULL");
+    *out = new sb_graph(batch, device);
+  });
+}
+void sb_graph_destroy(sb_graph* g) { delete g; }
+sb_status sb_graph_add_node(sb_graph* g, uint32_t parent, const char* name, int64_t geometry,
+                            const sb_joint* joint, uint32_t* id) {
+  return guard([&] {
+    const uint32_t v = g->add_node(parent, name, geometry, joint);
+    if (id) *id = v;
+  });
+}
+sb_status sb_graph_set_edge_batch(sb_graph* g, uint32_t parent, uint32_t child, const double* t16) {
+  return guard([&] { g->set_edge_batch(parent, child, t16); });
+}
+sb_status sb_graph_set_edge(sb_graph* g, uint32_t child, uint64_t i, const double pose[16]) {
+  return guard([&] { g->set_edge(child, i, pose); });
+}
+sb_status sb_graph_edge_batch(const sb_graph* g, uint32_t child, double* out16) {
+  return guard([&] { g->edge_batch(child, out16); });
+}
+sb_status sb_graph_set_joint_states(sb_graph* g, uint32_t node, const double* v) {
+  return guard([&] { g->set_joint_states(node, v); });
+}
+sb_status sb_graph_joint_states(const sb_graph* g, uint32_t node, double* out) {
+  return guard([&] { g->joint_states(node, out); });
+}
+sb_status sb_graph_world_poses(const sb_graph* g, uint32_t node, double* out16) {
+  return guard([&] { g->world_poses(node, out16); });
+}
+sb_status sb_graph_world_pose(const sb_graph* g, uint32_t node, uint64_t i, double pose[16]) {
+  return guard([&] { g->world_pose(node, i, pose); });
+}
+sb_status sb_graph_find(const sb_graph* g, const char* name, int64_t* id) {
+  return guard([&] {
+    if (!name || !id) throw std::invalid_argument("NULL argument");
+    auto it = g->by_name.find(name);
+    *id = it == g->by_name.end() ? -1 : static_cast<int64_t>(it->second);
+  });
+}
+sb_status sb_graph_node_info(const sb_graph* g, uint32_t node, const char** name, uint32_t* parent,
+                             int64_t* geometry, int* articulated, sb_joint* joint) {
+  return guard([&] {
+    const sb_graph::Node& nd = g->at(node);
+    if (name) *name = nd.name.c_str();
+    if (parent) *parent = nd.parent;
+    if (geometry) *geometry = nd.geometry;
+    if (articulated) *articulated = nd.joint ? 1 : 0;
+    if (joint && nd.joint) *joint = nd.spec;
+  });
+}
+uint64_t sb_graph_node_count(const sb_graph* g) { return g->nodes.size(); }
+sb_status sb_graph_children(const sb_graph* g, uint32_t node, uint32_t* out, uint32_t cap,
+                            uint32_t* count) {
+  return guard([&] {
+    g->at(node);
+    uint32_t c = 0;
+    for (uint32_t i = 1; i < g->nodes.size(); ++i)
+      if (g->nodes[i].parent == node) {
+        if (out && c < cap) out[c] = i;
+        ++c;
+      }
+    if (count) *count = c;
+  });
+}
+sb_status sb_graph_is_tree(const sb_graph* g, int* t) {
+  return guard([&] { *t = g->is_tree() ? 1 : 0; });
+}
+sb_status sb_graph_valid_mask(const sb_graph* g, uint8_t* mask) {
+  return guard([&] {
+    g->activate();
+    cuda_check(cudaMemcpyAsync(mask, g->d_valid.p, g->n, cudaMemcpyDeviceToHost, g->stream), "D2H");
+    g->sync();
+  });
+}
+sb_status sb_graph_mark_invalid(sb_graph* g, uint64_t i) {
+  return guard([&] {
+    if (i >= g->n) throw std::out_of_range("instance out of range");
+    g->activate();
+    cuda_check(cudaMemsetAsync(g->d_valid.p + i, 0, 1, g->stream), "memset");
+    g->sync();
+  });
+}
+sb_status sb_graph_reset_validity(sb_graph* g) {
+  return guard([&] {
+    g->activate();
+    cuda_check(cudaMemsetAsync(g->d_valid.p, 1, g->n, g->stream), "memset");
+    g->sync();
+  });
+}
+sb_status sb_graph_valid_count(const sb_graph* g, uint64_t* count) {
+  return guard([&] { *count = g->valid_count(); });
+}
+
+sb_status sb_engine_write_back(sb_engine* e, uint32_t placement, sb_graph* g, uint32_t node) {
+  return guard([&] { e->write_back(placement, *g, node); });
 }
 
 }  // extern "C"

@@ -366,6 +366,11 @@ class Engine:
         A.check(A.lib().sb_engine_generate(self._h, run_seed, C.byref(res), C.byref(st)))
         return {k: getattr(st, k) for k, _ in A.sb_run_stats._fields_}
 
+    def write_back(self, placement: int, graph, node: int) -> None:
+        """Accepted poses of `placement` from the last run into graph node `node` (a child
+        of the root); instances the run left invalid are marked invalid in the graph."""
+        A.check(A.lib().sb_engine_write_back(self._h, placement, graph._h, node))
+
     def last_timing(self):
         t, c, n = C.c_double(), C.c_double(), C.c_uint64()
         A.check(A.lib().sb_engine_last_timing(self._h, C.byref(t), C.byref(c), C.byref(n)))
