@@ -359,6 +359,44 @@ sb_status sb_graph_valid_count(const sb_graph* g, uint64_t* count);
  * graph must live on the engine's GPU and have its local batch size. */
 sb_status sb_engine_write_back(sb_engine* e, uint32_t placement, sb_graph* g, uint32_t node);
 
+/* ------------------------------------------------------------------------------------
+ * ReachMap4D (reachability.hpp:14-94) on the device: FK-sampled (r, z, psi) occupancy
+ * build, batched queries, placement_filter, and the "SBRM" v1 binary file (byte-compatible
+ * with ReachMap4D::save / load).
+ * ---------------------------------------------------------------------------------- */
+typedef struct sb_chain_link {  /* ChainLink (reachability.hpp:15-18) */
+  double origin[16];            /* column-major fixed transform to the joint frame */
+  sb_joint joint;
+} sb_chain_link;
+typedef struct sb_reach_map sb_reach_map;
+typedef struct sb_reach_info {
+  uint64_t samples;
+  double resolution, psi_resolution, max_radius, z_min, z_max;
+  uint64_t nr, nz, npsi, cell_count, occupied_cells;
+} sb_reach_info;
+/* ReachMap4D::build(chain, samples, resolution, psi_resolution, seed) */
+sb_status sb_reach_build(const sb_chain_link* links, uint32_t n_links, const double ee_offset[16],
+                         uint64_t samples, double resolution, double psi_resolution,
+                         uint64_t seed, int device, sb_reach_map** out);
+sb_status sb_reach_load(const char* path, int device, sb_reach_map** out);
+sb_status sb_reach_save(const sb_reach_map* m, const char* path);
+void sb_reach_destroy(sb_reach_map* m);
+sb_status sb_reach_get_info(const sb_reach_map* m, sb_reach_info* out);
+/* FK samples recorded in a cell (0 after load) */
+sb_status sb_reach_cell_samples(const sb_reach_map* m, uint64_t ir, uint64_t iz, uint64_t ipsi,
+                                uint32_t* count);
+/* query_batch(base_poses, targets, inclination) (reachability.cpp:143-162): has_inclination
+ * = 0 ignores `inclination` (any psi). */
+sb_status sb_reach_query_batch(const sb_reach_map* m, const double* base_colmajor16xN,
+                               const double* targets_xyz, uint64_t n, int has_inclination,
+                               double inclination, uint8_t* out);
+/* placement_filter(map, robot_base, frames, active) (reachability.cpp:164-190): frames =
+ * n_frames pointers to N column-major poses each (NULL entries skipped). */
+sb_status sb_reach_placement_filter(const sb_reach_map* m, const double* robot_base16xN,
+                                    uint64_t n, const double* const* frames16xN,
+                                    uint32_t n_frames, const uint32_t* active, uint64_t m_active,
+                                    uint8_t* out);
+
 /* Diagnostics: evaluate the device libm used on the hot path (correctly rounded
  * double-double sin/cos/atan2, replacing glibc's std::sin/cos/atan2 in transform.hpp:47,
  * polygon.cpp:151, relationships.cpp:184,238) on n inputs on device 0.

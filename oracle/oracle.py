@@ -111,6 +111,21 @@ def lib():
         L.ref_graph_mark_invalid.argtypes = [C.c_void_p, u64]
         L.ref_graph_valid_count.restype = u64
         L.ref_graph_valid_count.argtypes = [C.c_void_p]
+        L.ref_reach_build.restype = C.c_void_p
+        L.ref_reach_build.argtypes = [C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p, u64,
+                                      C.c_double, C.c_double, u64, C.c_int]
+        L.ref_reach_destroy.argtypes = [C.c_void_p]
+        L.ref_reach_save.argtypes = [C.c_void_p, C.c_char_p]
+        L.ref_reach_load.restype = C.c_void_p
+        L.ref_reach_load.argtypes = [C.c_char_p]
+        L.ref_reach_info.argtypes = [C.c_void_p, C.c_void_p]
+        L.ref_reach_cell_samples.restype = C.c_uint32
+        L.ref_reach_cell_samples.argtypes = [C.c_void_p, u64, u64, u64]
+        L.ref_reach_query_batch.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, u64, C.c_int,
+                                            C.c_double, C.c_void_p]
+        L.ref_reach_placement_filter.argtypes = [C.c_void_p, C.c_void_p, u64, C.c_void_p,
+                                                 C.c_void_p, C.c_uint32, C.c_void_p, u64,
+                                                 C.c_void_p]
         _lib = L
     return _lib
 
@@ -421,3 +436,65 @@ class RefGraph:
 
     def valid_count(self):
         return lib().ref_graph_valid_count(self.h)
+
+
+class RefReachMap:
+    """The reference's ReachMap4D (reachability.cpp) built / loaded through oracle/_ref."""
+
+    def __init__(self, h):
+        if not h:
+            raise RuntimeError(lib().ref_last_error().decode())
+        self.h = h
+
+    @classmethod
+    def build(cls, chain, samples, resolution, psi_resolution, seed, threads=1):
+        n = len(chain.links)
+        org = np.ascontiguousarray(np.concatenate([_cm(l.origin).reshape(1, 16) for l in chain.links]))
+        jt = np.ascontiguousarray([[float(l.joint.kind), *map(float, l.joint.axis), l.joint.lo,
+                                    l.joint.hi] for l in chain.links], np.float64)
+        ee = _cm(chain.ee_offset).reshape(16)
+        return cls(lib().ref_reach_build(n, _p(org), _p(jt), _p(ee), samples, resolution,
+                                         psi_resolution, seed, threads))
+
+    @classmethod
+    def load(cls, path):
+        return cls(lib().ref_reach_load(path.encode()))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().ref_reach_destroy(self.h)
+            self.h = None
+
+    def save(self, path):
+        check(lib().ref_reach_save(self.h, path.encode()))
+
+    def info(self):
+        o = np.zeros(6)
+        lib().ref_reach_info(self.h, _p(o))
+        return dict(zip(("samples", "resolution", "psi_resolution", "max_radius", "cell_count",
+                         "occupied_cells"), o.tolist()))
+
+    def cell_samples(self, ir, iz, ip):
+        return lib().ref_reach_cell_samples(self.h, ir, iz, ip)
+
+    def query_batch(self, base_poses, targets, inclination=None):
+        b = _cm(base_poses).reshape(-1, 16)
+        t = np.ascontiguousarray(targets, np.float64).reshape(-1, 3)
+        out = np.zeros(len(t), np.uint8)
+        check(lib().ref_reach_query_batch(self.h, _p(b), _p(t), len(t),
+                                          0 if inclination is None else 1,
+                                          0.0 if inclination is None else inclination, _p(out)))
+        return out
+
+    def placement_filter(self, robot_base, frames, active):
+        b = _cm(robot_base).reshape(-1, 16)
+        n = len(b)
+        pres = np.array([f is not None for f in frames], np.uint8)
+        fr = np.ascontiguousarray(np.concatenate(
+            [(_cm(f).reshape(-1, 16) if f is not None else np.zeros((n, 16))) for f in frames])
+            if frames else np.zeros((0, 16)))
+        act = np.ascontiguousarray(active, np.uint32)
+        out = np.zeros(len(act), np.uint8)
+        check(lib().ref_reach_placement_filter(self.h, _p(b), n, _p(fr), _p(pres), len(frames),
+                                               _p(act), len(act), _p(out)))
+        return out

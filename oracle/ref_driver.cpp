@@ -24,6 +24,7 @@
 #include "scenebatch/collision.hpp"
 #include "scenebatch/parallel.hpp"
 #include "scenebatch/polygon.hpp"
+#include "scenebatch/reachability.hpp"
 #include "scenebatch/relationships.hpp"
 #include "scenebatch/rng.hpp"
 #include "scenebatch/sampler.hpp"
@@ -387,6 +388,87 @@ int ref_graph_world_pose(void* h, uint32_t node, uint64_t i, double* out16) {
 int ref_graph_is_tree(void* h) { return static_cast<BatchedSceneGraph*>(h)->is_tree() ? 1 : 0; }
 void ref_graph_mark_invalid(void* h, uint64_t i) { static_cast<BatchedSceneGraph*>(h)->mark_invalid(i); }
 uint64_t ref_graph_valid_count(void* h) { return static_cast<BatchedSceneGraph*>(h)->valid_count(); }
+
+// ---------------------------------------------------------------- ReachMap4D
+// reachability.hpp:14-94; joints: n x (kind, ax, ay, az, lo, hi)
+void* ref_reach_build(uint32_t n_links, const double* origins16, const double* joints,
+                      const double* ee16, uint64_t samples, double res, double psi_res,
+                      uint64_t seed, int threads) {
+  try {
+    KinematicChain chain;
+    for (uint32_t l = 0; l < n_links; ++l) {
+      ChainLink link;
+      link.origin = mat_from16(origins16 + 16 * l);
+      const double* j = joints + 6 * l;
+      link.joint = JointSpec(j[0] == 1.0 ? JointSpec::Kind::prismatic : JointSpec::Kind::revolute,
+                             Vec3(j[1], j[2], j[3]), j[4], j[5]);
+      chain.links.push_back(link);
+    }
+    if (ee16) chain.ee_offset = mat_from16(ee16);
+    std::unique_ptr<ThreadPool> pool;
+    if (threads != 1) pool = std::make_unique<ThreadPool>(threads);
+    return new ReachMap4D(ReachMap4D::build(chain, samples, res, psi_res, seed, pool.get()));
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+void ref_reach_destroy(void* h) { delete static_cast<ReachMap4D*>(h); }
+int ref_reach_save(void* h, const char* path) { REF_TRY(static_cast<ReachMap4D*>(h)->save(path)); }
+void* ref_reach_load(const char* path) {
+  try {
+    return new ReachMap4D(ReachMap4D::load(path));
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+// out: samples, resolution, psi_resolution, max_radius, cell_count, occupied_cells
+void ref_reach_info(void* h, double* out) {
+  const ReachMap4D& m = *static_cast<ReachMap4D*>(h);
+  out[0] = static_cast<double>(m.sample_count());
+  out[1] = m.resolution();
+  out[2] = m.psi_resolution();
+  out[3] = m.max_radius();
+  out[4] = static_cast<double>(m.cell_count());
+  out[5] = static_cast<double>(m.occupied_cells());
+}
+uint32_t ref_reach_cell_samples(void* h, uint64_t ir, uint64_t iz, uint64_t ip) {
+  return static_cast<ReachMap4D*>(h)->cell_samples(ir, iz, ip);
+}
+int ref_reach_query_batch(void* h, const double* base16, const double* targets, uint64_t n,
+                          int has_incl, double incl, uint8_t* out) {
+  REF_TRY({
+    TransformBatch b(n);
+    std::vector<Vec3> t(n);
+    for (uint64_t i = 0; i < n; ++i) {
+      b[i] = mat_from16(base16 + 16 * i);
+      t[i] = Vec3(targets[3 * i], targets[3 * i + 1], targets[3 * i + 2]);
+    }
+    std::optional<double> inc;
+    if (has_incl) inc = incl;
+    auto r = static_cast<ReachMap4D*>(h)->query_batch(b, t, inc);
+    for (uint64_t i = 0; i < n; ++i) out[i] = r[i];
+  });
+}
+// frames16: n_frames x N x 16 (contiguous); present[f] = 0 -> a null frame
+int ref_reach_placement_filter(void* h, const double* base16, uint64_t n, const double* frames16,
+                               const uint8_t* present, uint32_t n_frames, const uint32_t* active,
+                               uint64_t m, uint8_t* out) {
+  REF_TRY({
+    TransformBatch b(n);
+    for (uint64_t i = 0; i < n; ++i) b[i] = mat_from16(base16 + 16 * i);
+    std::vector<TransformBatch> fr(n_frames, TransformBatch(n));
+    std::vector<const TransformBatch*> ptr(n_frames, nullptr);
+    for (uint32_t f = 0; f < n_frames; ++f) {
+      if (!present[f]) continue;
+      for (uint64_t i = 0; i < n; ++i) fr[f][i] = mat_from16(frames16 + 16 * (f * n + i));
+      ptr[f] = &fr[f];
+    }
+    auto r = placement_filter(*static_cast<ReachMap4D*>(h), b, ptr, std::span<const uint32_t>(active, m));
+    for (uint64_t j = 0; j < m; ++j) out[j] = r[j];
+  });
+}
 
 // ---------------------------------------------------------------- CollisionWorld
 void* ref_world_create(uint64_t n, double margin, int threads) {

@@ -5,6 +5,7 @@ bench.py; the product is libscenebatch_b200.so (sm_100a CUDA + C++ host runtime)
 """
 from ._capi import LIB_PATH, SbCudaError, SbError, lib  # noqa: F401
 from .graph import BatchedSceneGraph, JointSpec  # noqa: F401
+from .reach import ChainLink, KinematicChain, ReachMap4D, placement_filter  # noqa: F401
 from .sampler import PositionSampler, sample_orientations  # noqa: F401
 from .world import (CollisionWorld, Engine, Fixed, GenerationResult, Placement, Relation,  # noqa: F401
                     Scene, Shard, Support, TriMesh, colmajor, from_colmajor, make_box,

@@ -48,6 +48,18 @@ class sb_joint(C.Structure):
                 ("hi", C.c_double)]
 
 
+class sb_chain_link(C.Structure):
+    _fields_ = [("origin", C.c_double * 16), ("joint", sb_joint)]
+
+
+class sb_reach_info(C.Structure):
+    _fields_ = [("samples", C.c_uint64), ("resolution", C.c_double),
+                ("psi_resolution", C.c_double), ("max_radius", C.c_double),
+                ("z_min", C.c_double), ("z_max", C.c_double), ("nr", C.c_uint64),
+                ("nz", C.c_uint64), ("npsi", C.c_uint64), ("cell_count", C.c_uint64),
+                ("occupied_cells", C.c_uint64)]
+
+
 class sb_relation(C.Structure):
     _fields_ = [("anchor", C.c_int32), ("distance_type", C.c_int32), ("direction", C.c_int32),
                 ("frame", C.c_int32), ("direction_vector", C.c_double * 2),
@@ -162,6 +174,18 @@ SIGNATURES = {
     "sb_graph_reset_validity": (C.c_int, [_P]),
     "sb_graph_valid_count": (C.c_int, [_P, C.POINTER(C.c_uint64)]),
     "sb_engine_write_back": (C.c_int, [_P, C.c_uint32, _P, C.c_uint32]),
+    "sb_reach_build": (C.c_int, [C.POINTER(sb_chain_link), C.c_uint32, _D, C.c_uint64, C.c_double,
+                                 C.c_double, C.c_uint64, C.c_int, C.POINTER(_P)]),
+    "sb_reach_load": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(_P)]),
+    "sb_reach_save": (C.c_int, [_P, C.c_char_p]),
+    "sb_reach_destroy": (None, [_P]),
+    "sb_reach_get_info": (C.c_int, [_P, C.POINTER(sb_reach_info)]),
+    "sb_reach_cell_samples": (C.c_int, [_P, C.c_uint64, C.c_uint64, C.c_uint64,
+                                        C.POINTER(C.c_uint32)]),
+    "sb_reach_query_batch": (C.c_int, [_P, _D, _D, C.c_uint64, C.c_int, C.c_double,
+                                       C.POINTER(C.c_uint8)]),
+    "sb_reach_placement_filter": (C.c_int, [_P, _D, C.c_uint64, C.POINTER(_D), C.c_uint32, _U32,
+                                            C.c_uint64, C.POINTER(C.c_uint8)]),
     "sb_sampler_cache_info": (C.c_int, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "sb_sample_orientations": (C.c_int, [C.c_int, _U32, C.c_uint64, _D, _D, C.c_uint64,
                                          C.c_uint64, C.c_uint64, C.c_uint64, _D, C.c_int]),

@@ -10,6 +10,7 @@
 #include "sb_crmath.cuh"
 #include "sb_dev.cuh"
 #include "sb_graph.h"
+#include "sb_joint.cuh"
 
 using namespace sbd;
 
@@ -45,38 +46,6 @@ __device__ __forceinline__ void store_colmajor(double* o, const M34& M) {
     for (int c = 0; c < 4; ++c) o[4 * c + r] = M.m[4 * r + c];
   o[3] = o[7] = o[11] = 0.0;
   o[15] = 1.0;
-}
-
-// JointSpec::motion (scene_graph.cpp:19-27): prismatic = translation(axis * v); revolute =
-// AngleAxisd(v, axis).toRotationMatrix() (Rodrigues, Eigen's operation order).
-__device__ __forceinline__ void joint_motion(const sbk::GraphJoint& j, double v, M34& m) {
-#pragma unroll
-  for (int k = 0; k < 12; ++k) m.m[k] = 0.0;
-  m.m[0] = m.m[5] = m.m[10] = 1.0;
-  const double ax = j.axis[0], ay = j.axis[1], az = j.axis[2];
-  if (j.kind == 1) {
-    m.m[3] = ax * v;
-    m.m[7] = ay * v;
-    m.m[11] = az * v;
-    return;
-  }
-  double s, c;
-  sbm::sincos_cr(v, &s, &c);
-  const double sx = ax * s, sy = ay * s, sz = az * s;
-  const double c1 = 1.0 - c;
-  const double cx = ax * c1, cy = ay * c1, cz = az * c1;
-  double t = cx * ay;
-  m.m[1] = t - sz;
-  m.m[4] = t + sz;
-  t = cx * az;
-  m.m[2] = t + sy;
-  m.m[8] = t - sy;
-  t = cy * az;
-  m.m[6] = t - sx;
-  m.m[9] = t + sx;
-  m.m[0] = cx * ax + c;
-  m.m[5] = cy * ay + c;
-  m.m[10] = cz * az + c;
 }
 
 __global__ void k_colmajor_to_34(const double* in16, uint64_t n, double* out12) {
