@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
@@ -507,6 +508,10 @@ struct sb_engine {
   std::vector<cudaEvent_t> ev_place;
   double last_prof[16] = {};
   bool place_times = false;  // SB_PLACE_TIMES=1: per-placement event times to stderr
+  bool timing_pending = false;
+  std::vector<char> pending_per_inst;
+  std::vector<uint32_t> pending_rounds;
+  double pending_sharded_ms = 0.0;
   int num_sms = 0;
   // tile decomposition of the shard (sb_place.h) and launch shape of the placement kernel
   uint32_t ntiles = 0;
@@ -527,7 +532,9 @@ struct sb_engine {
   DevArray<int32_t> d_inst_n;
   DevArray<double> d_pose16;
   DevArray<double> d_out16;
-  PinnedArray<uint8_t> h_stat;  // end-of-run counters / ctrl words / region flags / timers  // [P][n][16] result poses written at accept (pipelined download)
+  PinnedArray<uint8_t> h_stat;
+  DevArray<unsigned long long> d_nvalid;
+  bool host_times = std::getenv("SB_HOST_TIMES") != nullptr;  // end-of-run counters / ctrl words / region flags / timers  // [P][n][16] result poses written at accept (pipelined download)
   PinnedArray<uint64_t> h_count;
   cudaStream_t copy_stream = nullptr;  // pipelined result download
   std::vector<cudaEvent_t> ev_pose;
@@ -847,6 +854,7 @@ struct sb_engine {
   // while later placements compute: placement p's poses are final once its kernel ends, so
   // a copy stream converts them (k_pose_colmajor) and copies them to the host behind an event.
   void generate(uint64_t run_seed, sb_run_stats* st, sb_result* out = nullptr) {
+    const auto th0 = std::chrono::steady_clock::now();
     world->activate();
     const bool pipe = out && out->poses && !places.empty();
     if (pipe) {
@@ -1030,7 +1038,7 @@ struct sb_engine {
     cuda_check(cudaEventRecord(ev_stop, stream), "event");
     // run statistics: small async copies into one pinned block, one synchronisation
     const size_t P1 = std::max<size_t>(1, P);
-    h_stat.ensure(128 + 40 * P1);
+    h_stat.ensure(136 + 40 * P1);
     unsigned long long* c = reinterpret_cast<unsigned long long*>(h_stat.p);
     uint64_t* prof = reinterpret_cast<uint64_t*>(h_stat.p + 64);
     uint32_t* ctrl_all = reinterpret_cast<uint32_t*>(h_stat.p + 128);
@@ -1039,36 +1047,35 @@ struct sb_engine {
     cuda_check(cudaMemcpyAsync(prof, d_prof.p, 64, cudaMemcpyDeviceToHost, stream), "D2H prof");
     cuda_check(cudaMemcpyAsync(ctrl_all, d_ctrl.p, 32 * P1, cudaMemcpyDeviceToHost, stream), "D2H ctrl");
     cuda_check(cudaMemcpyAsync(rflags, d_rflags.p, 8 * P1, cudaMemcpyDeviceToHost, stream), "D2H flags");
+    unsigned long long* nvalid = reinterpret_cast<unsigned long long*>(h_stat.p + 128 + 40 * P1);
+    if (st) {  // valid instances counted on the device (no N-byte readback)
+      d_nvalid.ensure(1);
+      cuda_check(cudaMemsetAsync(d_nvalid.p, 0, 8, stream), "memset");
+      sbk::graph_count_valid(d_valid.p, n, d_nvalid.p, s);
+      cuda_check(cudaMemcpyAsync(nvalid, d_nvalid.p, 8, cudaMemcpyDeviceToHost, stream), "D2H nvalid");
+    }
+    const auto th1 = std::chrono::steady_clock::now();
     cuda_check(cudaStreamSynchronize(stream), "sync");
+    const auto th2 = std::chrono::steady_clock::now();
     for (size_t p = 0; p < P; ++p) {
       if (rflags[2 * p + 1] != 0)
         throw std::runtime_error("constraint region build failed for placement " + std::to_string(p) +
                                  " (status " + std::to_string(rflags[2 * p + 1]) +
                                  ": capacity overflow or unsupported annulus)");
     }
-    float total_ms = 0.f;
-    cuda_check(cudaEventElapsedTime(&total_ms, ev_start, ev_stop), "elapsed");
-    double regions_ms = 0.0, place_ms = 0.0, inst_ms = 0.0, fast_ms = 0.0;
-    for (size_t p = 0; p < P; ++p) {
-      float a = 0.f, b = 0.f;
-      cuda_check(cudaEventElapsedTime(&a, ev_place[2 * p], ev_place[2 * p + 1]), "elapsed");
-      cuda_check(cudaEventElapsedTime(&b, ev_place[2 * p + 1], ev_place[2 * p + 2]), "elapsed");
-      regions_ms += a;
-      place_ms += b;
-      const bool per_inst = places[p].dev.anchor_object >= 0 && rflags[2 * p] != 0;
-      (per_inst ? inst_ms : fast_ms) += b;
-      if (place_times)
-        std::fprintf(stderr, "[place %2zu] %s regions %.1f us, placement %.1f us, rounds %u\n", p,
-                     per_inst ? "per-instance" : "fifo        ", a * 1e3, b * 1e3,
-                     device_rounds[p] ? ctrl_all[8 * p + 2] : 0u);
-    }
-    last_prof[10] = inst_ms;
-    last_prof[11] = fast_ms;
+    // CUDA-event timings are resolved lazily (resolve_timing: ~2.5 us per
+    // cudaEventElapsedTime, 2 per placement) -- only phase_profile / last_timing need them.
+    pending_per_inst.assign(P, 0);
+    for (size_t p = 0; p < P; ++p)
+      pending_per_inst[p] = places[p].dev.anchor_object >= 0 && rflags[2 * p] != 0;
+    pending_rounds.assign(P, 0);
+    for (size_t p = 0; p < P; ++p) pending_rounds[p] = device_rounds[p] ? ctrl_all[8 * p + 2] : 0u;
+    pending_sharded_ms = sharded_check_ms;
+    timing_pending = true;
+    const auto th2a = std::chrono::steady_clock::now();
     uint64_t rounds = rounds_host;
     for (size_t p = 0; p < P; ++p)
       if (device_rounds[p]) rounds += ctrl_all[8 * p + 2];
-    last_total_ms = total_ms;
-    last_check_ms = world_size == 1 ? place_ms : sharded_check_ms;
     last_check_launches = round_launches;
     last_launches = launches;
     for (int k = 0; k < 7; ++k) last_prof[k] = prof[k] * 1e-6;
@@ -1090,8 +1097,8 @@ struct sb_engine {
                    "mean CTA work %.3f ms, mean A2+B %.3f ms (grid %u)\n", last_prof[12], last_prof[13], last_prof[14],
                    di[14] * 1e-3 / grid, di[15] * 1e-3 / grid, grid);
     }
-    last_prof[8] = regions_ms;
-    last_prof[9] = total_ms;
+    if (place_times) resolve_timing();
+    const auto th2b = std::chrono::steady_clock::now();
     world->stats.check_calls += round_launches;
     world->stats.checked_instances += c[0];
     world->stats.narrow_phase_tests += c[1];
@@ -1107,13 +1114,46 @@ struct sb_engine {
       st->broad_phase_tests = c[4];
       st->node_pair_tests = c[5];
       st->accepted_candidates = c[6];
-      std::vector<uint8_t> v(n);
-      cuda_check(cudaMemcpy(v.data(), d_valid.p, n, cudaMemcpyDeviceToHost), "D2H valid");
-      uint64_t nv = 0;
-      for (uint8_t x : v) nv += x;
-      st->valid_instances = nv;
+      st->valid_instances = *nvalid;
     }
     if (pipe) cuda_check(cudaStreamSynchronize(copy_stream), "sync copy stream");
+    if (host_times) {
+      const auto th3 = std::chrono::steady_clock::now();
+      auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+      resolve_timing();
+      std::fprintf(stderr, "[host] enqueue %.1f us, wait %.1f us, after %.1f us (%.1f / %.1f / %.1f) (device %.1f us) t0 %.1f t3 %.1f\n",
+                   us(th0, th1), us(th1, th2), us(th2, th3), us(th2, th2a), us(th2a, th2b), us(th2b, th3),
+                   last_total_ms * 1e3,
+                   std::chrono::duration<double, std::micro>(th0.time_since_epoch()).count(),
+                   std::chrono::duration<double, std::micro>(th3.time_since_epoch()).count());
+    }
+  }
+
+  void resolve_timing() {
+    if (!timing_pending) return;
+    timing_pending = false;
+    const size_t P = pending_per_inst.size();
+    float total_ms = 0.f;
+    cuda_check(cudaEventElapsedTime(&total_ms, ev_start, ev_stop), "elapsed");
+    double regions_ms = 0.0, place_ms = 0.0, inst_ms = 0.0, fast_ms = 0.0;
+    for (size_t p = 0; p < P; ++p) {
+      float a = 0.f, b = 0.f;
+      cuda_check(cudaEventElapsedTime(&a, ev_place[2 * p], ev_place[2 * p + 1]), "elapsed");
+      cuda_check(cudaEventElapsedTime(&b, ev_place[2 * p + 1], ev_place[2 * p + 2]), "elapsed");
+      regions_ms += a;
+      place_ms += b;
+      (pending_per_inst[p] ? inst_ms : fast_ms) += b;
+      if (place_times)
+        std::fprintf(stderr, "[place %2zu] %s regions %.1f us, placement %.1f us, rounds %u\n", p,
+                     pending_per_inst[p] ? "per-instance" : "fifo        ", a * 1e3, b * 1e3,
+                     pending_rounds[p]);
+    }
+    last_prof[8] = regions_ms;
+    last_prof[9] = total_ms;
+    last_prof[10] = inst_ms;
+    last_prof[11] = fast_ms;
+    last_total_ms = total_ms;
+    last_check_ms = world_size == 1 ? place_ms : pending_sharded_ms;
   }
 
   void download(sb_result* out) {
@@ -1380,12 +1420,14 @@ sb_status sb_device_math(int fn, const double* in, uint64_t n, double* out) {
 
 sb_status sb_engine_phase_profile(const sb_engine* e, double out[16]) {
   return guard([&] {
+    const_cast<sb_engine*>(e)->resolve_timing();
     for (int k = 0; k < 16; ++k) out[k] = e->last_prof[k];
   });
 }
 sb_status sb_engine_last_timing(const sb_engine* e, double* total_ms, double* check_ms,
                                 uint64_t* check_launches) {
   return guard([&] {
+    const_cast<sb_engine*>(e)->resolve_timing();
     if (total_ms) *total_ms = e->last_total_ms;
     if (check_ms) *check_ms = e->last_check_ms;
     if (check_launches) *check_launches = e->last_check_launches;
