@@ -333,3 +333,22 @@ def test_generate_annulus_with_hole(gpu, ref, n, seed):
     assert_same(gpu, got, want)
     if n > 1:
         assert got.stats["per_instance_placements"] == 3
+
+
+@pytest.mark.parametrize("name,factory", [
+    ("c2_full_16384x25", lambda: scenes.tabletop_mixed(16384)),
+    ("c3_full_65536x50_k256", lambda: scenes.kitchen(65536)),
+    ("c4_full_262144x100_sphere_sets", lambda: scenes.dense_clutter(262144)),
+    ("c5_1M_x10", lambda: scenes.scale_sweep(1 << 20, 10)),
+])
+def test_generate_matches_reference_at_scale(gpu, ref, name, factory):
+    """BASELINE sizes (C2, C3, C4 in full, C5's 2^20 x 10 point): the device
+    engine against the reference on the box's host cores -- accepted indices and valid
+    masks bit-exact, poses within 1e-5, work counters equal."""
+    import os
+
+    scene = factory()
+    eng = gpu.Engine(scene)
+    got = eng.generate(1)
+    want = ref.generate(scene, 1, threads=os.cpu_count() or 8)
+    assert_same(gpu, got, want)
