@@ -63,6 +63,7 @@ struct Fixed {  // static shared memory
   uint32_t qhead;   // narrow-phase claim counter
   uint32_t total;
   uint32_t tile;
+  int32_t used;     // rounds a tile round consumed (FIFO speculation, phase C)
   unsigned long long tclk;  // block 0 / thread 0 phase clock
   unsigned long long acc[8];  // its per-slot sums, written to p.prof once at the end
   unsigned long long ta, tb, t0;  // every block: A1 / A2+B ns of the current round (debug)
@@ -259,7 +260,10 @@ __device__ uint32_t tile_round(const PlaceParams& p, const Sampling& S, const Sb
         placeable = false;
       } else {
         Pcg r{p.fast_state0};
-        r.advance(6ull * (draw_base + (uint64_t)e));  // j-th drained point = j-th draw (sampler.cpp:30-43)
+        // j-th drained point = j-th draw (sampler.cpp:30-43). Slot v = s * nt + e is round
+        // a + s, rank e: draw draw_base + s * nt + e = draw_base + v while nobody accepts
+        // before round a + s (FIFO speculation, resolved in phase C).
+        r.advance(6ull * (draw_base + (uint64_t)v));
         double u = r.next_double(), r1 = r.next_double(), r2 = r.next_double();
         sbp::draw_point(S.tris, S.cum, S.n, u, r1, r2, lx, ly);
       }
@@ -528,13 +532,28 @@ __device__ uint32_t tile_round(const PlaceParams& p, const Sampling& S, const Sb
   dbg_mark(p, F, F.tb);
 
   // ---------------- C: thread per instance; first free slot is accepted (Appendix C.5)
+  // FIFO speculation (S.fast, W > 1): rounds a .. a + slim are exact, where slim = the first
+  // round in which any instance is free (ranks shift after an accept); later slots are
+  // discarded and F.used = rounds consumed. Per-instance streams: every slot is exact.
+  int lim = W - 1;
+  if (S.fast && W > 1) {
+    if (tid == 0) F.used = W;
+    __syncthreads();
+    if (tid < (int)nt && T.minfree[tid] < W) atomicMin(&F.used, T.minfree[tid]);
+    __syncthreads();
+    if (F.used < W) lim = F.used;
+    __syncthreads();
+    if (tid == 0) F.used = lim + 1;
+  } else if (tid == 0) {
+    F.used = W;
+  }
   uint32_t keep = 0, inst = 0;
   if (tid < (int)nt) {
     const int e = tid;
     inst = T.list[e];
     int32_t last = a;  // last attempt this instance made in the sequential loop
     bool ok = false;
-    for (int s = 0; s < W && !ok; ++s) {
+    for (int s = 0; s <= lim && !ok; ++s) {
       const int v = s * (int)nt + e;
       last = a + s;
       ++L.sampled;
@@ -700,10 +719,17 @@ __device__ void solo_rounds(const PlaceParams& p, const Sampling& S, const SbGeo
   }
   uint32_t nt = base;
   while (nt > 0 && a < p.attempts) {
-    const uint32_t ns = tile_round<kGrid>(p, S, gA, T, F, nt, a, 1, draws, L);
-    draws += nt;
+    // W speculative rounds at once (see tile_round phase C): round a + s of rank e is
+    // draw draws + s * nt + e as long as nobody accepts before it
+    int W = p.solo_spec / (int)nt;
+    if (W < 1) W = 1;
+    if (W > kB / (int)nt) W = kB / (int)nt;
+    if (W > p.attempts - a) W = p.attempts - a;
+    const uint32_t ns = tile_round<kGrid>(p, S, gA, T, F, nt, a, W, draws, L);
+    const int used = F.used;
+    draws += (uint64_t)used * nt;
+    a += used;
     nt = ns;
-    ++a;
   }
   if (a == p.attempts) mark_invalid(p, T, nt);
 }

@@ -64,6 +64,7 @@ struct PlaceParams {
   int32_t tile_inst_pi;
   int32_t spec_target;          // per-instance path: target slots per tile round
   int32_t solo_max;             // fast path: at most this many survivors -> CTA 0 alone
+  int32_t solo_spec;            // fast path solo tail: target speculative slots per round
   int32_t ws_bytes;             // narrow-phase scratch per warp (sb_warp.cuh)
   int32_t max_tris, max_nodes;  // scratch geometry bounds over the world's geometries
   double* cpose;                // [grid][kPlaceBlock][12] candidate pose per CTA slot

@@ -518,6 +518,7 @@ struct sb_engine {
   int tile_inst = 0, tile_inst_pi = 0, max_tris = 1, max_nodes = 1, ws_bytes = 0;
   int spec_target = 64;
   int solo_max = 16;
+  int solo_spec = 0;  // SB_SOLO_SPEC: speculative slots per solo round (0/1: one round at a time)
   unsigned grid = 0;
   size_t smem = 0;
   DevArray<unsigned long long> d_counters;
@@ -753,6 +754,7 @@ struct sb_engine {
     place_times = std::getenv("SB_PLACE_TIMES") != nullptr;
     if (const char* st = std::getenv("SB_SPEC_TARGET")) spec_target = std::max(1, std::atoi(st));
     if (const char* so = std::getenv("SB_SOLO")) solo_max = std::max(0, std::min(sbk::kPlaceBlock, std::atoi(so)));
+    if (const char* ss = std::getenv("SB_SOLO_SPEC")) solo_spec = std::max(0, std::min(sbk::kPlaceBlock, std::atoi(ss)));
     if (round_debug) d_dbg.alloc(3 * static_cast<size_t>(attempts) * std::max<size_t>(1, places.size()) + 16);
     d_counters.alloc(8);
     cuda_check(cudaEventCreate(&ev_start), "event");
@@ -949,6 +951,7 @@ struct sb_engine {
       pp.ntiles_pi = static_cast<uint32_t>((n + tile_inst_pi - 1) / tile_inst_pi);
       pp.spec_target = spec_target;
       pp.solo_max = world_size == 1 ? solo_max : 0;
+      pp.solo_spec = solo_spec;
       pp.ws_bytes = ws_bytes;
       pp.max_tris = max_tris;
       pp.max_nodes = max_nodes;

@@ -352,3 +352,15 @@ def test_generate_matches_reference_at_scale(gpu, ref, name, factory):
     got = eng.generate(1)
     want = ref.generate(scene, 1, threads=os.cpu_count() or 8)
     assert_same(gpu, got, want)
+
+
+@pytest.mark.parametrize("spec", [8, 64])
+def test_fifo_speculative_solo_tail(gpu, ref, spec, monkeypatch):
+    """SB_SOLO_SPEC > 0: the FIFO solo tail evaluates several rounds at once (draw of round
+    a + s, rank e = draws + s * nt + e) and keeps only the rounds up to the first accept;
+    results must equal the sequential reference (off by default: not faster on C2)."""
+    monkeypatch.setenv("SB_SOLO_SPEC", str(spec))
+    monkeypatch.setenv("SB_SOLO", "32")
+    for scene in (scenes.tabletop_mixed(2048), scenes.kitchen(1024, attempts=128)):
+        eng, got, want = run_generate_pair(gpu, ref, scene, seed=7)
+        assert_same(gpu, got, want)
