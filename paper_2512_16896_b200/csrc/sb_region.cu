@@ -158,13 +158,11 @@ struct RegionStats {
   int ntri;
 };
 
-// Region for one anchor state into (tris, cum) with capacity `cap`. All lanes call.
-__device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double ay, double ayaw,
-                                   SbRegionTri* tris, double* cum, int cap, RegionScratch& sc) {
-  const Grp g;
-  SB_RP_MARK(rp0);
+// distance_band (relationships.cpp:101-122)
+__device__ __forceinline__ void distance_band(const SbPlacementDev& pl, double& min_r, double& max_r) {
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
-  double min_r = 0.0, max_r = inf;  // distance_band (relationships.cpp:101-122)
+  min_r = 0.0;
+  max_r = inf;
   if (pl.distance_type == SB_DIST_GREATER) {
     min_r = pl.distance;
   } else if (pl.distance_type == SB_DIST_LESS) {
@@ -174,31 +172,82 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
     min_r = dmax(0.0, pl.distance - half);
     max_r = pl.distance + half;
   }
+}
+// RelationshipSpec::effective_angle_threshold
+__device__ __forceinline__ double region_theta(const SbPlacementDev& pl) {
   const double pi = 3.14159265358979323846;
-  const double theta = pl.angle_threshold > 0.0 ? pl.angle_threshold
-                                                : (pl.direction == SB_DIR_NONE ? pi : pi / 4.0);
-  double vx = 1.0, vy = 0.0;  // resolve_direction (relationships.cpp:78-99)
-  if (pl.direction != SB_DIR_NONE) {
-    switch (pl.direction) {
-      case SB_DIR_LEFT: vx = -1; vy = 0; break;
-      case SB_DIR_RIGHT: vx = 1; vy = 0; break;
-      case SB_DIR_FRONT: vx = 0; vy = -1; break;
-      case SB_DIR_BACK: vx = 0; vy = 1; break;
-      default: {
-        const double nrm = sqrt(pl.direction_vector[0] * pl.direction_vector[0] +
-                                pl.direction_vector[1] * pl.direction_vector[1]);
-        vx = pl.direction_vector[0] / nrm;
-        vy = pl.direction_vector[1] / nrm;
-      }
-    }
-    if (pl.frame == SB_FRAME_LOCAL) {
-      double c, s;
-      sbm::sincos_cr(ayaw, &s, &c);
-      const double nx = c * vx - s * vy, ny = s * vx + c * vy;
-      vx = nx;
-      vy = ny;
+  return pl.angle_threshold > 0.0 ? pl.angle_threshold
+                                  : (pl.direction == SB_DIR_NONE ? pi : pi / 4.0);
+}
+// resolve_direction (relationships.cpp:78-99); (1, 0) without a direction
+__device__ __forceinline__ void resolve_direction(const SbPlacementDev& pl, double ayaw, double& vx,
+                                                  double& vy) {
+  vx = 1.0;
+  vy = 0.0;
+  if (pl.direction == SB_DIR_NONE) return;
+  switch (pl.direction) {
+    case SB_DIR_LEFT: vx = -1; vy = 0; break;
+    case SB_DIR_RIGHT: vx = 1; vy = 0; break;
+    case SB_DIR_FRONT: vx = 0; vy = -1; break;
+    case SB_DIR_BACK: vx = 0; vy = 1; break;
+    default: {
+      const double nrm = sqrt(pl.direction_vector[0] * pl.direction_vector[0] +
+                              pl.direction_vector[1] * pl.direction_vector[1]);
+      vx = pl.direction_vector[0] / nrm;
+      vy = pl.direction_vector[1] / nrm;
     }
   }
+  if (pl.frame == SB_FRAME_LOCAL) {
+    double c, s;
+    sbm::sincos_cr(ayaw, &s, &c);
+    const double nx = c * vx - s * vy, ny = s * vx + c * vy;
+    vx = nx;
+    vy = ny;
+  }
+}
+
+__device__ __forceinline__ int arc_count(double a0, double a1) {
+  const double step = 5.0 * 3.14159265358979323846 / 180.0;
+  const int n = (int)ceil(fabs(a1 - a0) / step);
+  return n < 1 ? 1 : n;
+}
+// arc k's endpoints for direction (vx, vy); false if there is no arc k
+__device__ __forceinline__ bool arc_ends(const SbPlacementDev& pl, double vx, double vy, int k,
+                                         double& a0, double& a1) {
+  const double pi = 3.14159265358979323846;
+  const double theta = region_theta(pl);
+  double min_r, max_r;
+  distance_band(pl, min_r, max_r);
+  if (theta >= pi - 1e-12) {  // full: one circle (the hole case has its own kernel)
+    a0 = 0.0;
+    a1 = 2.0 * pi;
+    return k == 0;
+  }
+  const double base = sbm::atan2_cr(vy, vx);
+  if (k == 0) {
+    a0 = base - theta;
+    a1 = base + theta;
+    return true;
+  }
+  a0 = base + theta;
+  a1 = base - theta;
+  return min_r > 0.0;
+}
+// Region for one anchor state into (tris, cum) with capacity `cap`. All lanes call.
+// arcs: the placement's shared arc table (arc_table_host), or NULL when the arcs depend on
+// the anchor yaw.
+__device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double ay, double ayaw,
+                                   SbRegionTri* tris, double* cum, int cap, RegionScratch& sc,
+                                   const SbArcTable* arcs) {
+  const Grp g;
+  SB_RP_MARK(rp0);
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  double min_r, max_r;
+  distance_band(pl, min_r, max_r);
+  const double pi = 3.14159265358979323846;
+  const double theta = region_theta(pl);
+  double vx, vy;
+  if (!arcs) resolve_direction(pl, ayaw, vx, vy);  // only the arcs need the direction
   // clip bound = bounds(support) expanded by the anchor; only used for infinite max_r
   const double* rc = pl.rect;
   double bx0 = inf, by0 = inf, bx1 = -inf, by1 = -inf;
@@ -219,38 +268,44 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
   if (!(theta > 0.0) || theta > pi + 1e-12) return {sbp::kRegionBadArg, 0};
   if (isinf(max_r)) max_r = fmax(diag, min_r + 1e-6);
   if (!(min_r < max_r)) return {sbp::kRegionBadArg, 0};
-  const double base = sbm::atan2_cr(vy, vx);
   const bool full = theta >= pi - 1e-12;
-  const double step = 5.0 * pi / 180.0;
-  auto arc_n = [&](double a0, double a1) {
-    int n = (int)ceil(fabs(a1 - a0) / step);
-    return n < 1 ? 1 : n;
-  };
+  if (full && min_r > 0.0) return {sbp::kRegionBadArg, 0};  // hole: k_relation_regions<true>
   double* X = sc.x[0];
   double* Y = sc.y[0];
   int n = 0;
-  auto arc = [&](double radius, double a0, double a1, int off) -> int {
-    const int na = arc_n(a0, a1);
+  auto arc = [&](int k, double radius, int off) -> int {
+    double a0 = 0.0, a1 = 0.0;
+    int na;
+    if (arcs) {
+      na = __ldg(&arcs->na[k]);
+    } else {
+      arc_ends(pl, vx, vy, k, a0, a1);
+      na = arc_count(a0, a1);
+    }
     if (off + na + 1 > kCap) return -1;
     for (int i = g.gl; i <= na; i += kG) {
-      const double a = a0 + (a1 - a0) * (double)i / (double)na;
       double sa, ca;
-      sbm::sincos_cr(a, &sa, &ca);
+      if (arcs) {
+        ca = __ldg(&arcs->c[k][i]);
+        sa = __ldg(&arcs->s[k][i]);
+      } else {
+        const double a = a0 + (a1 - a0) * (double)i / (double)na;
+        sbm::sincos_cr(a, &sa, &ca);
+      }
       X[off + i] = ax + radius * ca;
       Y[off + i] = ay + radius * sa;
     }
     return off + na + 1;
   };
   if (full) {
-    if (min_r > 0.0) return {sbp::kRegionBadArg, 0};
-    n = arc(max_r, 0.0, 2.0 * pi, 0);
+    n = arc(0, max_r, 0);
     if (n < 0) return {sbp::kRegionOverflow, 0};
     n -= 1;
   } else {
-    n = arc(max_r, base - theta, base + theta, 0);
+    n = arc(0, max_r, 0);
     if (n < 0) return {sbp::kRegionOverflow, 0};
     if (min_r > 0.0) {
-      n = arc(min_r, base + theta, base - theta, n);
+      n = arc(1, min_r, n);
       if (n < 0) return {sbp::kRegionOverflow, 0};
     } else {
       if (n + 1 > kCap) return {sbp::kRegionOverflow, 0};
@@ -515,7 +570,8 @@ __device__ __noinline__ RegionStats hole_region_lane(const SbPlacementDev& pl, d
 template <bool kHole>
 __device__ __forceinline__ RegionStats group_region(const SbPlacementDev& pl, double ax, double ay,
                                                     double ayaw, SbRegionTri* tris, double* cum,
-                                                    int cap, RegionScratch& sc) {
+                                                    int cap, RegionScratch& sc,
+                                                    const SbArcTable* arcs) {
   if constexpr (kHole) {
     const Grp g;
     RegionStats r{0, 0};
@@ -524,7 +580,7 @@ __device__ __forceinline__ RegionStats group_region(const SbPlacementDev& pl, do
     r.ntri = g.bcast(r.ntri, 0);
     return r;
   } else {
-    return warp_region(pl, ax, ay, ayaw, tris, cum, cap, sc);
+    return warp_region(pl, ax, ay, ayaw, tris, cum, cap, sc, arcs);
   }
 }
 
@@ -535,6 +591,7 @@ __device__ __forceinline__ RegionStats group_region(const SbPlacementDev& pl, do
 template <bool kHole>
 __global__ void __launch_bounds__(kRB, kRegionMinBlocks) k_relation_regions(RelationRegionParams p) {
   __shared__ RegionScratch scratch[kRW];
+  const SbArcTable* arcs = kHole ? nullptr : p.arcs;
   const Grp g;
   const uint64_t warp = (blockIdx.x * (uint64_t)kRB + threadIdx.x) / kG;  // instance group
   const uint64_t nwarps = (uint64_t)gridDim.x * kRW;
@@ -557,7 +614,7 @@ __global__ void __launch_bounds__(kRB, kRegionMinBlocks) k_relation_regions(Rela
   if (p.from_s0) {  // canonical region_for(0) from the exchanged instance-0 state
     if (warp == 0) {
       const RegionStats r =
-          group_region<kHole>(p.pl, p.s0[0], p.s0[1], p.s0[2], p.tris, p.cum, p.cap, sc);
+          group_region<kHole>(p.pl, p.s0[0], p.s0[1], p.s0[2], p.tris, p.cum, p.cap, sc, arcs);
       if (g.gl == 0) {
         const bool good = r.status == sbp::kRegionOk || r.status == sbp::kRegionEmpty;
         p.ntri[0] = good ? r.ntri : 0;
@@ -575,7 +632,7 @@ __global__ void __launch_bounds__(kRB, kRegionMinBlocks) k_relation_regions(Rela
       const double dx = ax - x0, dy = ay - y0;  // relationships.cpp:178-186
       vary = vary || sqrt(dx * dx + dy * dy) > 1e-12 || fabs(ayaw - yaw0) > 1e-12;
       const RegionStats r = group_region<kHole>(p.pl, ax, ay, ayaw, p.tris + i * p.cap,
-                                                p.cum + i * p.cap, p.cap, sc);
+                                                p.cum + i * p.cap, p.cap, sc, arcs);
       if (g.gl == 0) {
         p.ntri[i] = r.status == sbp::kRegionOk || r.status == sbp::kRegionEmpty ? r.ntri : 0;
         if (r.status != sbp::kRegionOk && r.status != sbp::kRegionEmpty && r.status > worst)
@@ -617,7 +674,7 @@ __global__ void __launch_bounds__(kRB, kRegionMinBlocks) k_relation_regions(Rela
     SB_RP_MARK(ra1);
     SB_RP_ADD(0, ra0, ra1);
     const RegionStats r = group_region<kHole>(p.pl, ax, ay, ayaw, p.tris + i * p.cap,
-                                              p.cum + i * p.cap, p.cap, sc);
+                                              p.cum + i * p.cap, p.cap, sc, arcs);
     if (g.gl == 0) {
       p.ntri[i] = r.status == sbp::kRegionOk || r.status == sbp::kRegionEmpty ? r.ntri : 0;
       if (r.status != sbp::kRegionOk && r.status != sbp::kRegionEmpty && r.status > worst)

@@ -8,6 +8,18 @@
 
 namespace sbk {
 
+// cos / sin of annulus_sector's arc points (polygon.cpp:146-153) when they do not depend on
+// the anchor (no local-frame direction): computed once per placement on the host with the
+// reference's own libm (std::atan2 / std::cos / std::sin), read by every instance.
+constexpr int kArcCap = 80;  // a full circle is 72 segments at the 5 degree step
+struct SbArcTable {
+  double c[2][kArcCap], s[2][kArcCap];  // arc 0 = outer arc / full circle, arc 1 = inner arc
+  int32_t na[2];                         // segments of arc k (points = na + 1), 0 = none
+};
+// Fills `t` for placement `pl`; false when the arcs depend on the anchor yaw (local frame)
+// or do not fit the table.
+bool arc_table_host(const SbPlacementDev& pl, SbArcTable& t);
+
 struct RelationRegionParams {
   SbWorldView w;
   SbPlacementDev pl;
@@ -18,6 +30,7 @@ struct RelationRegionParams {
   int32_t from_s0;         // 1: build a single region from s0 (canonical, sharded runs)
   int32_t cap;
   int32_t hole;            // full annulus with a hole: bridged-hole path (sbp::hole_annulus_table)
+  const SbArcTable* arcs;  // optional device copy of arc_table_host (shared arcs)
   const double* states;    // optional [n][3] anchor states (x, y, yaw) in the support frame
                            // given directly (standalone sampler); else read from world poses
   SbRegionTri* tris;       // [n][cap] (or [1][cap] when from_s0)

@@ -162,6 +162,62 @@ bool relation_to_dev(const sb_relation& r, SbPlacementDev& d) {
 
 }  // namespace
 
+// annulus_sector's arc points (polygon.cpp:136-176) with the host libm, shared by every
+// instance when the direction is not in the anchor's local frame (sb_region.h).
+bool sbk::arc_table_host(const SbPlacementDev& pl, SbArcTable& t) {
+  std::memset(&t, 0, sizeof t);
+  if (pl.direction != SB_DIR_NONE && pl.frame == SB_FRAME_LOCAL) return false;
+  const double pi = M_PI;
+  const double theta = pl.angle_threshold > 0.0 ? pl.angle_threshold
+                                                : (pl.direction == SB_DIR_NONE ? pi : pi / 4.0);
+  double min_r = 0.0;  // distance_band (relationships.cpp:101-122)
+  if (pl.distance_type == SB_DIST_GREATER) min_r = pl.distance;
+  if (pl.distance_type == SB_DIST_EQUAL)
+    min_r = std::max(0.0, pl.distance - std::max(0.05 * pl.distance, 0.01));
+  double vx = 1.0, vy = 0.0;  // resolve_direction (relationships.cpp:78-99), global frame
+  switch (pl.direction) {
+    case SB_DIR_LEFT: vx = -1; vy = 0; break;
+    case SB_DIR_RIGHT: vx = 1; vy = 0; break;
+    case SB_DIR_FRONT: vx = 0; vy = -1; break;
+    case SB_DIR_BACK: vx = 0; vy = 1; break;
+    case SB_DIR_VECTOR: {
+      const double nrm = std::sqrt(pl.direction_vector[0] * pl.direction_vector[0] +
+                                   pl.direction_vector[1] * pl.direction_vector[1]);
+      vx = pl.direction_vector[0] / nrm;
+      vy = pl.direction_vector[1] / nrm;
+      break;
+    }
+    default: break;
+  }
+  const double step = 5.0 * pi / 180.0;
+  const bool full = theta >= pi - 1e-12;
+  double ends[2][2];
+  int narcs = 1;
+  if (full) {
+    ends[0][0] = 0.0;
+    ends[0][1] = 2.0 * pi;
+  } else {
+    const double base = std::atan2(vy, vx);
+    ends[0][0] = base - theta;
+    ends[0][1] = base + theta;
+    ends[1][0] = base + theta;
+    ends[1][1] = base - theta;
+    if (min_r > 0.0) narcs = 2;
+  }
+  for (int k = 0; k < narcs; ++k) {
+    const double a0 = ends[k][0], a1 = ends[k][1];
+    const int na = std::max(1, static_cast<int>(std::ceil(std::abs(a1 - a0) / step)));
+    if (na + 1 > kArcCap) return false;
+    t.na[k] = na;
+    for (int i = 0; i <= na; ++i) {
+      const double a = a0 + (a1 - a0) * static_cast<double>(i) / na;
+      t.c[k][i] = std::cos(a);
+      t.s[k][i] = std::sin(a);
+    }
+  }
+  return true;
+}
+
 // ===================================================================== World
 struct sb_world {
   uint64_t n;
@@ -486,6 +542,7 @@ struct sb_engine {
     double inv_support[12];
     int canon_n = 0;  // host-built canonical table size (no anchor)
     bool hole = false;  // full annulus with a hole (theta = pi, min_r > 0)
+    bool shared_arcs = false;  // arc table in d_arcs[p] (no local-frame direction)
   };
   std::vector<Placement> places;
   int32_t first_place_obj = 0;
@@ -528,6 +585,7 @@ struct sb_engine {
   DevArray<SbRegionTri> d_canon_tris;
   DevArray<double> d_canon_cum;
   DevArray<int32_t> d_canon_n;
+  DevArray<sbk::SbArcTable> d_arcs;  // per placement: shared annulus arc points
   DevArray<SbRegionTri> d_inst_tris;
   DevArray<double> d_inst_cum;
   DevArray<int32_t> d_inst_n;
@@ -647,6 +705,14 @@ struct sb_engine {
 
     // canonical sampler tables (no-anchor placements: the support rect itself)
     const size_t P = places.size();
+    {  // annulus arc points shared by all instances (host libm, sb_region.h)
+      std::vector<sbk::SbArcTable> arcs(std::max<size_t>(1, P));
+      for (size_t p = 0; p < P; ++p)
+        places[p].shared_arcs = places[p].dev.anchor_object >= 0 && !places[p].hole &&
+                                sbk::arc_table_host(places[p].dev, arcs[p]);
+      d_arcs.alloc(arcs.size());
+      cuda_check(cudaMemcpy(d_arcs.p, arcs.data(), arcs.size() * sizeof(sbk::SbArcTable), cudaMemcpyHostToDevice), "H2D arcs");
+    }
     inst_cap = any_hole ? sbp::kHoleCap : SB_REGION_MAX_VERTS;
     d_canon_tris.alloc(std::max<size_t>(1, P) * inst_cap);
     d_canon_cum.alloc(std::max<size_t>(1, P) * inst_cap);
@@ -788,6 +854,7 @@ struct sb_engine {
     std::memcpy(rp.inv_support, pl.inv_support, sizeof rp.inv_support);
     rp.cap = inst_cap;
     rp.hole = pl.hole ? 1 : 0;
+    rp.arcs = pl.shared_arcs ? d_arcs.p + p : nullptr;
     rp.tris = d_inst_tris.p;
     rp.cum = d_inst_cum.p;
     rp.ntri = d_inst_n.p;
@@ -826,6 +893,7 @@ struct sb_engine {
     rp.s0 = d_s0.p;
     rp.cap = inst_cap;
     rp.hole = pl.hole ? 1 : 0;
+    rp.arcs = pl.shared_arcs ? d_arcs.p + p : nullptr;
     rp.tris = d_inst_tris.p;
     rp.cum = d_inst_cum.p;
     rp.ntri = d_inst_n.p;
@@ -1506,6 +1574,7 @@ struct sb_sampler {
   DevArray<int32_t> d_inst_n;
   DevArray<double> d_states;
   DevArray<int32_t> d_rflags;
+  DevArray<sbk::SbArcTable> d_arcs;
   DevArray<double> d_sup, d_pos;
   DevArray<uint32_t> d_active;
   DevArray<uint8_t> d_pl;
@@ -1629,6 +1698,12 @@ struct sb_sampler {
     rp.anchor_object = -1;
     rp.cap = table_cap;
     rp.hole = hole ? 1 : 0;
+    sbk::SbArcTable arc_tab;
+    if (!hole && sbk::arc_table_host(pd, arc_tab)) {
+      d_arcs.ensure(1);
+      cuda_check(cudaMemcpyAsync(d_arcs.p, &arc_tab, sizeof arc_tab, cudaMemcpyHostToDevice, stream), "H2D arcs");
+      rp.arcs = d_arcs.p;
+    }
     rp.states = d_states.p;
     rp.tris = d_tris.p;
     rp.cum = d_cum.p;
