@@ -147,7 +147,8 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         from paper_2512_16896_b200.dist import torch_allgather
 
-        shard = pkg.Shard(rank * n_per, (rank + 1) * n_per, rank, world, torch_allgather(world))
+        shard = pkg.Shard(rank * n_per, (rank + 1) * n_per, rank, world,
+                          torch_allgather(world, getattr(args, "xdev", None)))
     t0 = time.time()
     eng = pkg.Engine(scene, shard, device=device)
     cold_s = time.time() - t0
@@ -370,10 +371,11 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     rank, world, local_rank = dist_env()
+    args.xdev = None
     if world > 1:
-        import torch.distributed as dist
+        from paper_2512_16896_b200.dist import init_group
 
-        dist.init_process_group("gloo")
+        args.xdev = init_group(local_rank)
     if args.impl == "reference":
         line = run_reference(args, rank, world)
     else:

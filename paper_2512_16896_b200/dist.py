@@ -1,7 +1,8 @@
 """Multi-GPU plumbing: one process per GPU, instances sharded into
 contiguous variation ranges; the only exchange is the FIFO fast path's per-round survivor
 counts and a relation placement's instance-0 anchor state (a few u64 per rank), done with
-torch.distributed all_gather on the host values the engine already reads back."""
+torch.distributed all_gather: over NCCL (NVLink / NVSwitch) when the process group has a
+CUDA backend and a device is given, else over the CPU backend (gloo)."""
 from __future__ import annotations
 
 from typing import Callable, List
@@ -12,16 +13,43 @@ def shard_bounds(n_total: int, world: int) -> List[int]:
     return [n_total * r // world for r in range(world + 1)]
 
 
-def torch_allgather(world: int) -> Callable[[List[int]], List[int]]:
+def torch_allgather(world: int, device=None) -> Callable[[List[int]], List[int]]:
     """sb_shard.allgather callback over the initialised torch.distributed group: every
-    rank contributes the same number of u64 values; returns them rank-major."""
+    rank contributes the same number of u64 values; returns them rank-major. With `device`
+    (a CUDA device of a group whose CUDA backend is NCCL) the values travel as one NCCL
+    all_gather_into_tensor; otherwise as CPU tensors (gloo)."""
     import torch
     import torch.distributed as dist
 
     def allgather(vals: List[int]) -> List[int]:
         t = torch.tensor([v & 0xFFFFFFFFFFFFFFFF for v in vals], dtype=torch.uint64).view(torch.int64)
+        if device is not None:
+            src = t.to(device, non_blocking=False)
+            out = torch.empty(world * len(vals), dtype=torch.int64, device=device)
+            dist.all_gather_into_tensor(out, src)
+            return [int(v) & 0xFFFFFFFFFFFFFFFF for v in out.cpu().tolist()]
         out = [torch.zeros_like(t) for _ in range(world)]
         dist.all_gather(out, t)
         return [int(v) & 0xFFFFFFFFFFFFFFFF for o in out for v in o.tolist()]
 
     return allgather
+
+
+def init_group(local_rank: int):
+    """One process per GPU: CPU tensors over gloo (timing reductions), CUDA tensors over
+    NCCL (the engine's count exchange). Returns the CUDA device for torch_allgather, or None
+    when only gloo could be initialised."""
+    import torch
+    import torch.distributed as dist
+
+    if torch.cuda.is_available():
+        try:
+            dev = torch.device("cuda", local_rank)
+            torch.cuda.set_device(dev)
+            dist.init_process_group("cpu:gloo,cuda:nccl", device_id=dev)
+            return dev
+        except Exception:  # noqa: BLE001 -- fall back to the CPU backend alone
+            if dist.is_initialized():
+                dist.destroy_process_group()
+    dist.init_process_group("gloo")
+    return None
