@@ -397,6 +397,15 @@ sb_status sb_reach_placement_filter(const sb_reach_map* m, const double* robot_b
                                     uint32_t n_frames, const uint32_t* active, uint64_t m_active,
                                     uint8_t* out);
 
+/* Fused reachability filter: from the next generate
+ * on, placement `placement` accepts a candidate only if its frame origin, expressed in the
+ * instance's robot base frame, falls in an occupied (r, z) cell of `map`
+ * (placement_filter, reachability.cpp:164-190); an unreachable candidate is a failed
+ * attempt and is not collision-checked. robot_base: the engine's local instances'
+ * column-major poses. map == NULL clears the filter. The map must outlive the engine's use. */
+sb_status sb_engine_set_reach_filter(sb_engine* e, uint32_t placement, const sb_reach_map* map,
+                                     const double* robot_base_colmajor16xN);
+
 /* Diagnostics: evaluate the device libm used on the hot path (correctly rounded
  * double-double sin/cos/atan2, replacing glibc's std::sin/cos/atan2 in transform.hpp:47,
  * polygon.cpp:151, relationships.cpp:184,238) on n inputs on device 0.

@@ -126,6 +126,8 @@ def lib():
         L.ref_reach_placement_filter.argtypes = [C.c_void_p, C.c_void_p, u64, C.c_void_p,
                                                  C.c_void_p, C.c_uint32, C.c_void_p, u64,
                                                  C.c_void_p]
+        L.ref_set_reach_filter.argtypes = [C.c_uint32, C.c_void_p, C.c_void_p, u64]
+        L.ref_clear_reach_filters.argtypes = []
         _lib = L
     return _lib
 
@@ -498,3 +500,17 @@ class RefReachMap:
         check(lib().ref_reach_placement_filter(self.h, _p(b), n, _p(fr), _p(pres), len(frames),
                                                _p(act), len(act), _p(out)))
         return out
+
+
+def set_reach_filter(placement: int, refmap, robot_base):
+    """Appendix C item 8 for ref generate: refmap = RefReachMap (kept alive by the caller),
+    robot_base = (N_total, 4, 4); None clears it."""
+    if refmap is None:
+        check(lib().ref_set_reach_filter(placement, None, None, 0))
+        return
+    b = _cm(robot_base).reshape(-1, 16)
+    check(lib().ref_set_reach_filter(placement, refmap.h, _p(b), len(b)))
+
+
+def clear_reach_filters():
+    lib().ref_clear_reach_filters()

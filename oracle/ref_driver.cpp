@@ -12,10 +12,14 @@
 //      invalid and later placements skip it.
 //   6. placeable == 0 (empty region) counts as a failed attempt (not checked).
 //   7. margin 0.
+//   8. reachability filter (optional, per placement; "and reachability, if
+//      flagged"): placement_filter(map, robot_base, {candidate pose}) before collision;
+//      an unreachable candidate is a failed attempt and is not checked.
 // Exposes a C ABI (prefix ref_) for ctypes; data layouts come from include/scenebatch_b200.h.
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -530,6 +534,27 @@ void ref_get_stats(void* h, uint64_t* out) {
 // ---------------------------------------------------------------- generation driver
 // Optional per-round trace (debugging parity): global instance ids, candidate poses,
 // placeable flags, free flags per active slot.
+// ---------------------------------------------------------------- fused reachability filter
+// Appendix C item 8 (driver contract): placement -> (map, robot base per GLOBAL instance).
+struct RefReach {
+  const ReachMap4D* map;
+  std::vector<Mat4> base;
+};
+static std::map<uint32_t, RefReach> g_reach;
+extern "C" int ref_set_reach_filter(uint32_t placement, void* map, const double* base16,
+                                    uint64_t n_total) {
+  REF_TRY({
+    if (!map) {
+      g_reach.erase(placement);
+      return 0;
+    }
+    RefReach r{static_cast<ReachMap4D*>(map), std::vector<Mat4>(n_total)};
+    for (uint64_t i = 0; i < n_total; ++i) r.base[i] = mat_from16(base16 + 16 * i);
+    g_reach[placement] = std::move(r);
+  });
+}
+extern "C" void ref_clear_reach_filters() { g_reach.clear(); }
+
 typedef void (*ref_trace_fn)(void* ctx, int32_t placement, int32_t attempt, uint64_t m,
                              const uint32_t* active_global, const double* poses16,
                              const uint8_t* placeable, const uint8_t* free_by_slot);
@@ -698,8 +723,25 @@ int ref_generate(const sb_scene* sc, const sb_shard* shard, uint64_t run_seed, i
         std::vector<Mat4> poses(active.size());
         std::vector<Mat4> chk_poses;
         std::vector<uint32_t> chk_local;
-        for (std::size_t j = 0; j < active.size(); ++j) {
+        for (std::size_t j = 0; j < active.size(); ++j)
           poses[j] = translation(pos[j] + Vec3(0, 0, z_off)) * rotation_z(yaws[j]);
+        // 8. reachability (if set for this placement): placement_filter on the candidate
+        //    frame before collision; unreachable = failed attempt, not checked.
+        auto rit = g_reach.find(p);
+        if (rit != g_reach.end()) {
+          TransformBatch rb(active.size()), fr(active.size());
+          std::vector<uint32_t> idx(active.size());
+          for (std::size_t j = 0; j < active.size(); ++j) {
+            rb[j] = rit->second.base[active[j]];
+            fr[j] = poses[j];
+            idx[j] = static_cast<uint32_t>(j);
+          }
+          std::vector<const TransformBatch*> frames{&fr};
+          auto ok = placement_filter(*rit->second.map, rb, frames, idx);
+          for (std::size_t j = 0; j < active.size(); ++j)
+            if (!ok[j]) placeable[j] = 0;
+        }
+        for (std::size_t j = 0; j < active.size(); ++j) {
           if (placeable[j]) {
             chk_poses.push_back(poses[j]);
             chk_local.push_back(static_cast<uint32_t>(active[j] - begin));

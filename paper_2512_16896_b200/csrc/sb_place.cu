@@ -10,6 +10,7 @@
 #include "sb_crmath.cuh"
 #include "sb_dev.cuh"
 #include "sb_place.h"
+#include "sb_reachdev.cuh"
 #include "sb_poly.h"
 #include "sb_warp.cuh"
 
@@ -231,7 +232,7 @@ __device__ __forceinline__ void narrow_drain(const PlaceParams& p, Tile& T, Fixe
 // e), so the narrow queue lists every instance's first attempt before any second one and
 // an instance's later attempts are mostly skipped once a lower one is confirmed free.
 // Returns the survivor count. All threads of the CTA call it.
-template <bool kGrid>
+template <bool kGrid, bool kReach>
 __device__ uint32_t tile_round(const PlaceParams& p, const Sampling& S, const SbGeom& gA,
                                Tile& T, Fixed& F, uint32_t nt, int32_t a, int W,
                                uint64_t draw_base, Local& L) {
@@ -334,6 +335,21 @@ __device__ uint32_t tile_round(const PlaceParams& p, const Sampling& S, const Sb
         T.box[6 * v + 3 + k] = cmx[k];
       }
       T.sflag[v] = kSlotChecked;
+      if constexpr (kReach) {  // fused placement_filter (reachability.cpp:164-190): the
+        // candidate frame's origin in the instance's robot base frame must hit occ_any;
+        // an unreachable candidate is a failed attempt that is not collision-checked
+        M34 Bs, Bi;
+        const double* bp = p.reach_base + (size_t)inst * 12;
+#pragma unroll
+        for (int k = 0; k < 12; ++k) Bs.m[k] = __ldg(bp + k);
+        inverse_rigid(Bs, Bi);
+        double rx, ry, rz;
+        xform(Bi, pose.m[3], pose.m[7], pose.m[11], rx, ry, rz);
+        uint64_t ir, iz;
+        const bool reach = reach_bin(p.reach_grid, rx, ry, rz, ir, iz) &&
+                           reach_bit(p.reach_any, ir * p.reach_grid.nz + iz);
+        if (!reach) T.sflag[v] = kSlotUnplaceable;
+      }
     }
   }
   if (tid == 0) {
@@ -668,7 +684,7 @@ __device__ __forceinline__ void store_list(const PlaceParams& p, const Tile& T, 
 }
 
 // One fast-path round over the CTA's tiles: survivors of round a -> counts of round a+1.
-template <bool kGrid>
+template <bool kGrid, bool kReach>
 // `resident`: the CTA owns at most one tile and T.list still holds its survivors from the
 // previous round (persistent kernel), so the list is not reloaded.
 __device__ uint64_t fast_round(const PlaceParams& p, const Sampling& S, const SbGeom& gA,
@@ -690,7 +706,7 @@ __device__ uint64_t fast_round(const PlaceParams& p, const Sampling& S, const Sb
     if (!resident) load_list(p, T, t, n);
     lap(p, F, 1);
     if (p.dbg && threadIdx.x == 0) F.t0 = global_ns();
-    const uint32_t ns = tile_round<kGrid>(p, S, gA, T, F, n, a, 1, draws + F.prefix[k], L);
+    const uint32_t ns = tile_round<kGrid, kReach>(p, S, gA, T, F, n, a, 1, draws + F.prefix[k], L);
     store_list(p, T, t, ns, cout);
     mine += ns;
     __syncthreads();
@@ -702,7 +718,7 @@ __device__ uint64_t fast_round(const PlaceParams& p, const Sampling& S, const Sb
 // Fast path tail: once at most p.solo_max instances remain, CTA 0 gathers them in global
 // active order (tile order, then position) and runs the remaining rounds alone -- no grid
 // barrier, no prefix scan; draw j of round a is draws + position, as in the grid rounds.
-template <bool kGrid>
+template <bool kGrid, bool kReach>
 __device__ void solo_rounds(const PlaceParams& p, const Sampling& S, const SbGeom& gA, Tile& T,
                             Fixed& F, int32_t a, uint64_t draws, Local& L) {
   const uint32_t* cin = p.tile_cnt + (size_t)(a & 1) * p.cnt_stride;
@@ -725,7 +741,7 @@ __device__ void solo_rounds(const PlaceParams& p, const Sampling& S, const SbGeo
     if (W < 1) W = 1;
     if (W > kB / (int)nt) W = kB / (int)nt;
     if (W > p.attempts - a) W = p.attempts - a;
-    const uint32_t ns = tile_round<kGrid>(p, S, gA, T, F, nt, a, W, draws, L);
+    const uint32_t ns = tile_round<kGrid, kReach>(p, S, gA, T, F, nt, a, W, draws, L);
     const int used = F.used;
     draws += (uint64_t)used * nt;
     a += used;
@@ -735,7 +751,7 @@ __device__ void solo_rounds(const PlaceParams& p, const Sampling& S, const SbGeo
 }
 
 // Per-instance path: tiles are independent; each is run to completion by one CTA.
-template <bool kGrid>
+template <bool kGrid, bool kReach>
 __device__ void instance_tiles(const PlaceParams& p, const Sampling& S, const SbGeom& gA,
                                Tile& T, Fixed& F, Local& L) {
   for (;;) {
@@ -759,7 +775,7 @@ __device__ void instance_tiles(const PlaceParams& p, const Sampling& S, const Sb
         F.t0 = global_ns();
       }
       const unsigned nslots_dbg = nt * W;
-      nt = tile_round<kGrid>(p, S, gA, T, F, nt, a, W, 0, L);
+      nt = tile_round<kGrid, kReach>(p, S, gA, T, F, nt, a, W, 0, L);
       a += W;
       if (p.dbg_inst && threadIdx.x == 0) {  // A1 / A2+B / C sums (us) and A2+B max (ns)
         atomicAdd(p.dbg_inst + 5, (unsigned)(F.ta / 1000));
@@ -795,7 +811,7 @@ __device__ __forceinline__ void block_setup(const PlaceParams& p, Fixed& F, Tile
 
 extern __shared__ __align__(16) unsigned char g_dsm[];
 
-template <bool kGrid>
+template <bool kGrid, bool kReach>
 __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_place(PlaceParams p) {
   __shared__ Fixed F;
   Tile T = carve(g_dsm, p.w.n_words, p.ws_bytes);
@@ -812,7 +828,7 @@ __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_place(PlaceParams p
     if (p.vary_flag && blockIdx.x == 0 && threadIdx.x == 0)
       atomicAdd(p.counters + 7, 1ull);  // per-instance placement
     const unsigned long long t6 = timer ? global_ns() : 0;
-    instance_tiles<kGrid>(p, S, gA, T, F, L);
+    instance_tiles<kGrid, kReach>(p, S, gA, T, F, L);
     if (timer) F.acc[6] += global_ns() - t6;
   } else {
     cg::grid_group grid = cg::this_grid();
@@ -833,9 +849,9 @@ __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_place(PlaceParams p
         F.ta = F.tb = 0;
       }
       uint64_t total =
-          fast_round<kGrid>(p, S, gA, T, F, a, draws, L, nullptr, p.ntiles <= gridDim.x);
+          fast_round<kGrid, kReach>(p, S, gA, T, F, a, draws, L, nullptr, p.ntiles <= gridDim.x);
       if (total & kSoloFlag) {
-        if (blockIdx.x == 0) solo_rounds<kGrid>(p, S, gA, T, F, a, draws, L);
+        if (blockIdx.x == 0) solo_rounds<kGrid, kReach>(p, S, gA, T, F, a, draws, L);
         a = -1;  // tail done by CTA 0
         break;
       }
@@ -870,7 +886,7 @@ __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_place(PlaceParams p
 }
 
 // Sharded building blocks (no grid barrier inside a launch).
-template <bool kGrid>
+template <bool kGrid, bool kReach>
 __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_place_instances(PlaceParams p) {
   __shared__ Fixed F;
   Tile T = carve(g_dsm, p.w.n_words, p.ws_bytes);
@@ -878,7 +894,7 @@ __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_place_instances(Pla
   block_setup(p, F, T, gA);
   Local L;
   Sampling S{0, nullptr, nullptr, 0};
-  instance_tiles<kGrid>(p, S, gA, T, F, L);
+  instance_tiles<kGrid, kReach>(p, S, gA, T, F, L);
   flush(p, L);
 }
 
@@ -895,7 +911,7 @@ __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_fast_init(PlacePara
   if (threadIdx.x == 0 && mine) atomicAdd(p.ctrl + place_total_word(0), mine);
 }
 
-template <bool kGrid>
+template <bool kGrid, bool kReach>
 __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_fast_round(PlaceParams p, int32_t a) {
   __shared__ Fixed F;
   Tile T = carve(g_dsm, p.w.n_words, p.ws_bytes);
@@ -903,7 +919,7 @@ __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_fast_round(PlacePar
   block_setup(p, F, T, gA);
   Local L;
   Sampling S{1, p.canon_tris, p.canon_cum, p.canon_n};
-  fast_round<kGrid>(p, S, gA, T, F, a, p.draw_base, L, p.ctrl + place_total_word(a + 1), false);
+  fast_round<kGrid, kReach>(p, S, gA, T, F, a, p.draw_base, L, p.ctrl + place_total_word(a + 1), false);
   flush(p, L);
 }
 
@@ -941,13 +957,25 @@ void narrow_profile(unsigned long long out[8], bool reset) {
   }
 }
 
+namespace {
+// kernel variant by (occupancy grid, fused reachability filter)
+const void* place_fn(const PlaceParams& p) {
+  const bool g = p.grid.g != 0, r = p.reach_any != nullptr;
+  return g ? (r ? (const void*)k_place<true, true> : (const void*)k_place<true, false>)
+           : (r ? (const void*)k_place<false, true> : (const void*)k_place<false, false>);
+}
+}  // namespace
+
 int place_grid(int num_sms, size_t smem) {
-  set_smem((const void*)k_place<false>, smem);
-  set_smem((const void*)k_place<true>, smem);
-  int per = 0, per2 = 0;
-  check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_place<false>, kB, smem), "occupancy");
-  check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, k_place<true>, kB, smem), "occupancy");
-  if (per2 < per) per = per2;
+  const void* fns[4] = {(const void*)k_place<false, false>, (const void*)k_place<true, false>,
+                        (const void*)k_place<false, true>, (const void*)k_place<true, true>};
+  int per = 1 << 30;
+  for (const void* fn : fns) {
+    set_smem(fn, smem);
+    int v = 0;
+    check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, fn, kB, smem), "occupancy");
+    if (v < per) per = v;
+  }
   return per * num_sms;
 }
 
@@ -955,21 +983,22 @@ bool place_persistent(const PlaceParams& p, unsigned grid, size_t smem, sb_strea
   if (grid == 0) return false;
   PlaceParams q = p;
   void* args[] = {&q};
-  const void* fn = p.grid.g ? (const void*)k_place<true> : (const void*)k_place<false>;
-  check(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kB), args, smem,
+  check(cudaLaunchCooperativeKernel(place_fn(p), dim3(grid), dim3(kB), args, smem,
                                     reinterpret_cast<cudaStream_t>(s)),
         "cudaLaunchCooperativeKernel(k_place)");
   return true;
 }
 
+template <bool kGrid, bool kReach>
+void launch_instances(const PlaceParams& p, unsigned grid, size_t smem, sb_stream_t s) {
+  set_smem((const void*)k_place_instances<kGrid, kReach>, smem);
+  k_place_instances<kGrid, kReach><<<grid, kB, smem, s>>>(p);
+}
+
 void place_instances(const PlaceParams& p, unsigned grid, size_t smem, sb_stream_t s) {
-  if (p.grid.g) {
-    set_smem((const void*)k_place_instances<true>, smem);
-    k_place_instances<true><<<grid, kB, smem, s>>>(p);
-  } else {
-    set_smem((const void*)k_place_instances<false>, smem);
-    k_place_instances<false><<<grid, kB, smem, s>>>(p);
-  }
+  const bool r = p.reach_any != nullptr;
+  if (p.grid.g) r ? launch_instances<true, true>(p, grid, smem, s) : launch_instances<true, false>(p, grid, smem, s);
+  else r ? launch_instances<false, true>(p, grid, smem, s) : launch_instances<false, false>(p, grid, smem, s);
   check(cudaGetLastError(), "k_place_instances");
 }
 
@@ -979,15 +1008,18 @@ void place_fast_init(const PlaceParams& p, unsigned grid, size_t smem, sb_stream
   check(cudaGetLastError(), "k_fast_init");
 }
 
+template <bool kGrid, bool kReach>
+void launch_fast_round(const PlaceParams& p, int32_t attempt, unsigned grid, size_t smem,
+                       sb_stream_t s) {
+  set_smem((const void*)k_fast_round<kGrid, kReach>, smem);
+  k_fast_round<kGrid, kReach><<<grid, kB, smem, s>>>(p, attempt);
+}
+
 void place_fast_round(const PlaceParams& p, int32_t attempt, unsigned grid, size_t smem,
                       sb_stream_t s) {
-  if (p.grid.g) {
-    set_smem((const void*)k_fast_round<true>, smem);
-    k_fast_round<true><<<grid, kB, smem, s>>>(p, attempt);
-  } else {
-    set_smem((const void*)k_fast_round<false>, smem);
-    k_fast_round<false><<<grid, kB, smem, s>>>(p, attempt);
-  }
+  const bool r = p.reach_any != nullptr;
+  if (p.grid.g) r ? launch_fast_round<true, true>(p, attempt, grid, smem, s) : launch_fast_round<true, false>(p, attempt, grid, smem, s);
+  else r ? launch_fast_round<false, true>(p, attempt, grid, smem, s) : launch_fast_round<false, false>(p, attempt, grid, smem, s);
   check(cudaGetLastError(), "k_fast_round");
 }
 

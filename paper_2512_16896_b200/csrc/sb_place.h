@@ -34,6 +34,7 @@
 
 #include "sb_kernels.h"
 #include "sb_layout.h"
+#include "sb_reach.h"
 
 namespace sbk {
 
@@ -80,6 +81,12 @@ struct PlaceParams {
   // *vary_flag != 0 selects the per-instance tables, else the FIFO fast path samples the
   // canonical region_for(0) = local instance 0's table (relationships.cpp:188-190).
   const int32_t* vary_flag;
+  // Optional fused reachability filter: a candidate whose frame origin,
+  // in its instance's robot base frame, misses the map's (r, z) occupancy is a failed
+  // attempt that is not collision-checked (Appendix C item 8).
+  const unsigned long long* reach_any;  // occ_any bitset of the map, NULL = no filter
+  ReachGrid reach_grid;
+  const double* reach_base;             // [n][12] robot base per local instance (row-major)
 };
 
 #ifndef SB_PLACE_BLOCK

@@ -12,6 +12,7 @@
 #include "sb_dev.cuh"
 #include "sb_joint.cuh"
 #include "sb_reach.h"
+#include "sb_reachdev.cuh"
 
 using namespace sbd;
 
@@ -24,34 +25,6 @@ inline unsigned grid_for(uint64_t n) { return static_cast<unsigned>((n + kBlock 
 inline void check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
-}
-
-// std::hypot, correctly rounded (glibc's is: 0 misroundings in 20k random checks): x^2 + y^2
-// in double-double, then one Newton correction of the square root.
-__device__ __forceinline__ double hypot_cr(double x, double y) {
-  x = fabs(x);
-  y = fabs(y);
-  const double big = fmax(x, y), small = fmin(x, y);
-  if (!isfinite(big) || big > 1e150 || (small != 0.0 && small < 1e-150)) return hypot(x, y);
-  if (big == 0.0) return 0.0;
-  const sbm::dd s = sbm::dd_add(sbm::two_prod(x, x), sbm::two_prod(y, y));
-  const double r = sqrt(s.hi);
-  const sbm::dd e = sbm::dd_add(s, sbm::dd_neg(sbm::two_prod(r, r)));
-  return r + e.hi / (2.0 * r);
-}
-
-// ReachMap4D::bin (reachability.cpp:113-119)
-__device__ __forceinline__ bool bin(const sbk::ReachGrid& g, double x, double y, double z,
-                                    uint64_t& ir, uint64_t& iz) {
-  const double r = hypot_cr(x, y);
-  if (r >= g.r_max || z < g.z_min || z >= g.z_max) return false;
-  ir = (uint64_t)(r / g.res);
-  iz = (uint64_t)((z - g.z_min) / g.res);
-  return ir < g.nr && iz < g.nz;
-}
-
-__device__ __forceinline__ bool bit(const unsigned long long* w, uint64_t idx) {
-  return (__ldg(w + (idx >> 6)) >> (idx & 63)) & 1ull;
 }
 
 __device__ __forceinline__ void load_colmajor(const double* c, M34& M) {
@@ -88,7 +61,7 @@ __global__ void k_reach_build(const double* links, int n_links, sbk::ReachGrid g
   }
   mul34(t, ee, b);
   uint64_t ir, iz;
-  if (!bin(g, b.m[3], b.m[7], b.m[11], ir, iz)) return;
+  if (!reach_bin(g, b.m[3], b.m[7], b.m[11], ir, iz)) return;
   // tool_inclination: axis = R * (0,0,1) (shim order), psi = acos(clamp(-axis.z, -1, 1))
   const double axz = (b.m[8] * 0.0 + b.m[9] * 0.0) + b.m[10] * 1.0;
   const double c = fmin(fmax(-axz, -1.0), 1.0);
@@ -105,7 +78,7 @@ __global__ void k_reach_any(sbk::ReachGrid g, const unsigned long long* occ,
   const uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;  // (ir, iz) cell
   if (c >= g.nr * g.nz) return;
   bool any = false;
-  for (uint64_t ip = 0; ip < g.npsi && !any; ++ip) any = bit(occ, c * g.npsi + ip);
+  for (uint64_t ip = 0; ip < g.npsi && !any; ++ip) any = reach_bit(occ, c * g.npsi + ip);
   if (any) atomicOr(occ_any + (c >> 6), 1ull << (c & 63));
 }
 
@@ -114,12 +87,12 @@ __device__ __forceinline__ bool query(const sbk::ReachGrid& g, const unsigned lo
                                       const unsigned long long* occ_any, double x, double y,
                                       double z, double incl) {
   uint64_t ir, iz;
-  if (!bin(g, x, y, z, ir, iz)) return false;
-  if (isnan(incl)) return bit(occ_any, ir * g.nz + iz);  // no inclination: any psi
+  if (!reach_bin(g, x, y, z, ir, iz)) return false;
+  if (isnan(incl)) return reach_bit(occ_any, ir * g.nz + iz);  // no inclination: any psi
   const double psi = fmin(fmax(incl, 0.0), 3.14159265358979323846);
   uint64_t ipsi = (uint64_t)(psi / g.psi_res);
   if (ipsi > g.npsi - 1) ipsi = g.npsi - 1;
-  return bit(occ, (ir * g.nz + iz) * g.npsi + ipsi);
+  return reach_bit(occ, (ir * g.nz + iz) * g.npsi + ipsi);
 }
 
 __global__ void k_reach_query(sbk::ReachGrid g, const unsigned long long* occ,

@@ -530,6 +530,12 @@ struct sb_world {
 struct sb_engine {
   std::unique_ptr<sb_world> world;
   void write_back(uint32_t placement, sb_graph& g, uint32_t node);  // defined after sb_graph
+  struct ReachFilter {  // fused reachability filter of one placement (sb_engine_set_reach_filter)
+    const unsigned long long* any = nullptr;
+    sbk::ReachGrid grid{};
+    std::unique_ptr<DevArray<double>> base;
+  };
+  std::vector<ReachFilter> reach;
   uint64_t n_total = 0, begin = 0, end = 0, n = 0;
   int rank = 0, world_size = 1;
   sb_allgather_fn allgather = nullptr;
@@ -1029,6 +1035,11 @@ struct sb_engine {
       pp.dbg = round_debug ? d_dbg.p + 3 * static_cast<size_t>(attempts) * p : nullptr;
       pp.dbg_inst = round_debug ? d_dbg.p + d_dbg.count - 16 : nullptr;
       pp.vary_flag = (relation && world_size == 1) ? d_rflags.p + 2 * p : nullptr;
+      if (p < reach.size() && reach[p].any) {
+        pp.reach_any = reach[p].any;
+        pp.reach_grid = reach[p].grid;
+        pp.reach_base = reach[p].base->p;
+      }
       if (world_size == 1) {
         if (!sbk::place_persistent(pp, grid, smem, s))
           throw CudaError("cooperative launch of the placement kernel is not possible");
@@ -2579,3 +2590,29 @@ sb_status sb_reach_placement_filter(const sb_reach_map* m, const double* base16,
 }
 
 }  // extern "C"
+
+extern "C" sb_status sb_engine_set_reach_filter(sb_engine* e, uint32_t placement,
+                                                const sb_reach_map* m, const double* base16) {
+  return guard([&] {
+    if (placement >= e->places.size()) throw std::out_of_range("placement index out of range");
+    e->reach.resize(e->places.size());
+    sb_engine::ReachFilter& f = e->reach[placement];
+    if (!m) {  // clear
+      f = sb_engine::ReachFilter();
+      return;
+    }
+    if (!base16) throw std::invalid_argument("robot base poses are NULL");
+    if (m->device != e->world->device) throw std::invalid_argument("reach map on another device");
+    std::vector<double> rows(12 * e->n);
+    for (uint64_t i = 0; i < e->n; ++i) {
+      if (!homogeneous16(base16 + 16 * i)) throw std::invalid_argument("non-homogeneous robot base pose");
+      colmajor_to_34(base16 + 16 * i, &rows[12 * i]);
+    }
+    e->world->activate();
+    f.base = std::make_unique<DevArray<double>>();
+    f.base->alloc(rows.size());
+    cuda_check(cudaMemcpy(f.base->p, rows.data(), rows.size() * sizeof(double), cudaMemcpyHostToDevice), "H2D base");
+    f.any = m->d_any.p;
+    f.grid = m->g;
+  });
+}

@@ -366,6 +366,17 @@ class Engine:
         A.check(A.lib().sb_engine_generate(self._h, run_seed, C.byref(res), C.byref(st)))
         return {k: getattr(st, k) for k, _ in A.sb_run_stats._fields_}
 
+    def set_reach_filter(self, placement: int, reach_map, robot_base=None) -> None:
+        """Fused reachability filter for `placement` (Appendix C item 8): candidates whose
+        frame origin is unreachable from the instance's robot base ((N, 4, 4)) fail."""
+        if reach_map is None:
+            A.check(A.lib().sb_engine_set_reach_filter(self._h, placement, None, None))
+            return
+        b = colmajor(np.asarray(robot_base, np.float64)).reshape(-1, 16)
+        self._reach_keep = getattr(self, "_reach_keep", {})
+        self._reach_keep[placement] = reach_map  # the map must outlive the engine's use
+        A.check(A.lib().sb_engine_set_reach_filter(self._h, placement, reach_map._h, _dp(b)))
+
     def write_back(self, placement: int, graph, node: int) -> None:
         """Accepted poses of `placement` from the last run into graph node `node` (a child
         of the root); instances the run left invalid are marked invalid in the graph."""
