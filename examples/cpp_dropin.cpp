@@ -41,6 +41,24 @@ int main() {
                 (unsigned long long)ps.refill_count());
     auto yaws = sample_orientations(SB_ORIENT_UNIFORM_YAW, active, pos, nullptr, 7, 1, 0);
     std::printf("yaw0 %.17g\n", yaws[0]);
+    // BatchedSceneGraph (scene_graph.hpp:33-94): table -> drawer (prismatic) -> apple
+    BatchedSceneGraph sg(4);
+    uint32_t table = sg.add_node(sg.root(), "table");
+    JointSpec slide{1, {1, 0, 0}, 0.0, 0.3};
+    uint32_t drawer = sg.add_node(table, "drawer", -1, &slide);
+    uint32_t apple = sg.add_node(drawer, "apple", 3);
+    const double js[4] = {0.0, 0.1, 0.2, 0.3};
+    sg.set_joint_states(drawer, js);
+    const std::vector<Pose> wp = sg.world_poses(apple);
+    std::printf("apple x: %.2f %.2f %.2f %.2f\n", wp[0][12], wp[1][12], wp[2][12], wp[3][12]);
+    // ReachMap4D (reachability.hpp:34-94): 1-joint planar arm, 1 m link -> a ring of radius 1
+    sb_chain_link link{{1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1}, {0, {0, 0, 1}, -3.14159, 3.14159}};
+    const Pose ee{1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0, 1.0, 0, 0, 1};
+    ReachMap4D rm = ReachMap4D::build(std::span<const sb_chain_link>(&link, 1), ee, 20000, 0.05, 0.5, 3);
+    const std::vector<Pose> bases(2, Pose{1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1});
+    const std::vector<std::array<double, 3>> tg = {{0.0, 1.0, 0.0}, {0.5, 0.0, 0.0}};
+    const std::vector<uint8_t> q = rm.query_batch(bases, tg);
+    std::printf("reach ring: %d %d\n", q[0], q[1]);
     return (m.free[0] == 0 && m.free[1] == 0 && m.free[2] == 1 && m.free[3] == 0 && inside) ? 0 : 1;
   } catch (const cuda_error& e) {
     std::printf("no device: %s\n", e.what());

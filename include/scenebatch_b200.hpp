@@ -1,6 +1,7 @@
 // scenebatch_b200.hpp -- the reference's C++ class API on top of the C ABI.
 //
-// Drop-in shape of /root/reference/proj/include/scenebatch/{collision,trimesh,sampler}.hpp plus
+// Drop-in shape of /root/reference/proj/include/scenebatch/{collision,trimesh,sampler,
+// scene_graph,reachability}.hpp plus
 // the generation engine the reference specifies but does not ship.
 // Header-only; link libscenebatch_b200.so. Errors are rethrown as the reference's
 // exception types (std::invalid_argument, std::out_of_range, std::logic_error,
@@ -11,6 +12,7 @@
 #pragma once
 
 #include <array>
+#include <optional>
 #include <cstdint>
 #include <span>
 #include <stdexcept>
@@ -279,6 +281,147 @@ inline std::vector<double> sample_orientations(int kind, std::span<const uint32_
                                face_targets ? face_targets->size() : 0, run_seed, placement_salt,
                                attempt, yaws.data(), device));
   return yaws;
+}
+
+// JointSpec / BatchedSceneGraph (scene_graph.hpp:19-94), edge batches resident on one B200.
+using JointSpec = sb_joint;  // {kind 0 revolute / 1 prismatic, axis, lo, hi}
+
+class BatchedSceneGraph {
+ public:
+  explicit BatchedSceneGraph(std::size_t batch_size, int device = 0) : n_(batch_size) {
+    check(sb_graph_create(batch_size, device, &g_));
+  }
+  ~BatchedSceneGraph() { sb_graph_destroy(g_); }
+  BatchedSceneGraph(const BatchedSceneGraph&) = delete;
+  BatchedSceneGraph& operator=(const BatchedSceneGraph&) = delete;
+
+  std::size_t batch_size() const { return n_; }
+  uint32_t root() const { return 0; }
+  uint32_t add_node(uint32_t parent, const std::string& name, int64_t geometry_id = -1,
+                    const JointSpec* joint = nullptr) {
+    uint32_t id = 0;
+    check(sb_graph_add_node(g_, parent, name.c_str(), geometry_id, joint, &id));
+    return id;
+  }
+  // transforms: batch_size column-major Mat4 (TransformBatch::data memory)
+  void set_edge_batch(uint32_t parent, uint32_t child, const double* transforms) {
+    check(sb_graph_set_edge_batch(g_, parent, child, transforms));
+  }
+  void set_edge(uint32_t child, std::size_t instance, const Pose& m) {
+    check(sb_graph_set_edge(g_, child, instance, m.data()));
+  }
+  std::vector<Pose> edge_batch(uint32_t child) const { return batch(sb_graph_edge_batch, child); }
+  void set_joint_states(uint32_t node, std::span<const double> values) {
+    if (values.size() != n_) throw std::invalid_argument("joint value batch size mismatch");
+    check(sb_graph_set_joint_states(g_, node, values.data()));
+  }
+  std::vector<double> joint_states(uint32_t node) const {
+    std::vector<double> v(n_);
+    check(sb_graph_joint_states(g_, node, v.data()));
+    return v;
+  }
+  std::vector<Pose> world_poses(uint32_t node) const { return batch(sb_graph_world_poses, node); }
+  Pose world_pose(uint32_t node, std::size_t instance) const {
+    Pose p{};
+    check(sb_graph_world_pose(g_, node, instance, p.data()));
+    return p;
+  }
+  std::optional<uint32_t> find(const std::string& name) const {
+    int64_t id = -1;
+    check(sb_graph_find(g_, name.c_str(), &id));
+    if (id < 0) return std::nullopt;
+    return static_cast<uint32_t>(id);
+  }
+  std::size_t node_count() const { return sb_graph_node_count(g_); }
+  bool is_tree() const {
+    int t = 0;
+    check(sb_graph_is_tree(g_, &t));
+    return t != 0;
+  }
+  std::vector<uint8_t> valid_mask() const {
+    std::vector<uint8_t> m(n_);
+    check(sb_graph_valid_mask(g_, m.data()));
+    return m;
+  }
+  void mark_invalid(std::size_t instance) { check(sb_graph_mark_invalid(g_, instance)); }
+  void reset_validity() { check(sb_graph_reset_validity(g_)); }
+  std::size_t valid_count() const {
+    uint64_t c = 0;
+    check(sb_graph_valid_count(g_, &c));
+    return c;
+  }
+  sb_graph* handle() const { return g_; }
+
+ private:
+  template <class F>
+  std::vector<Pose> batch(F f, uint32_t node) const {
+    std::vector<Pose> out(n_);
+    check(f(g_, node, out[0].data()));
+    return out;
+  }
+  sb_graph* g_ = nullptr;
+  std::size_t n_ = 0;
+};
+
+// ReachMap4D (reachability.hpp:34-94) built and queried on one B200; SBRM v1 files.
+class ReachMap4D {
+ public:
+  static ReachMap4D build(std::span<const sb_chain_link> chain, const Pose& ee_offset,
+                          std::size_t samples, double resolution, double psi_resolution,
+                          uint64_t seed, int device = 0) {
+    ReachMap4D m;
+    check(sb_reach_build(chain.data(), static_cast<uint32_t>(chain.size()), ee_offset.data(),
+                         samples, resolution, psi_resolution, seed, device, &m.m_));
+    return m;
+  }
+  static ReachMap4D load(const std::string& path, int device = 0) {
+    ReachMap4D m;
+    check(sb_reach_load(path.c_str(), device, &m.m_));
+    return m;
+  }
+  ReachMap4D(ReachMap4D&& o) noexcept : m_(o.m_) { o.m_ = nullptr; }
+  ReachMap4D& operator=(ReachMap4D&& o) noexcept {
+    std::swap(m_, o.m_);
+    return *this;
+  }
+  ~ReachMap4D() {
+    if (m_) sb_reach_destroy(m_);
+  }
+  void save(const std::string& path) const { check(sb_reach_save(m_, path.c_str())); }
+  sb_reach_info info() const {
+    sb_reach_info i{};
+    check(sb_reach_get_info(m_, &i));
+    return i;
+  }
+  // targets[i] is a world point checked against base_poses[i]
+  std::vector<uint8_t> query_batch(std::span<const Pose> base_poses,
+                                   std::span<const std::array<double, 3>> targets,
+                                   std::optional<double> inclination = std::nullopt) const {
+    if (base_poses.size() != targets.size()) throw std::invalid_argument("query_batch: size mismatch");
+    std::vector<uint8_t> out(targets.size());
+    if (targets.empty()) return out;
+    check(sb_reach_query_batch(m_, base_poses[0].data(), targets[0].data(), targets.size(),
+                               inclination ? 1 : 0, inclination.value_or(0.0), out.data()));
+    return out;
+  }
+  sb_reach_map* handle() const { return m_; }
+
+ private:
+  ReachMap4D() = default;
+  sb_reach_map* m_ = nullptr;
+};
+
+// placement_filter(map, robot_base, frames, active) (reachability.cpp:164-190); frames:
+// column-major pose batches of robot_base's size, nullptr entries skipped.
+inline std::vector<uint8_t> placement_filter(const ReachMap4D& map, std::span<const Pose> robot_base,
+                                             std::span<const double* const> frames,
+                                             std::span<const uint32_t> active) {
+  std::vector<uint8_t> out(active.size());
+  if (active.empty()) return out;
+  check(sb_reach_placement_filter(map.handle(), robot_base[0].data(), robot_base.size(),
+                                  frames.data(), static_cast<uint32_t>(frames.size()),
+                                  active.data(), active.size(), out.data()));
+  return out;
 }
 
 }  // namespace scenebatch_b200

@@ -31,5 +31,7 @@ def test_cpp_header_unit_cubes_on_gpu(tmp_path, gpu, ref):
     assert r.returncode == 0, r.stdout + r.stderr
     assert "free: 0 0 1 0" in r.stdout
     assert "sampled: inside 1 refills 1" in r.stdout
+    assert "apple x: 0.00 0.10 0.20 0.30" in r.stdout
+    assert "reach ring: 1 0" in r.stdout
     yaw0 = ref.sample_orientations(1, [0, 1, 2, 3], None, None, 7, 1, 0)[0]
     assert f"yaw0 {yaw0!r}" in r.stdout or f"yaw0 {yaw0:.17g}" in r.stdout
