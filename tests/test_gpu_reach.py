@@ -107,3 +107,46 @@ def test_engine_fused_reach_filter(gpu, ref, tmp_path, seed):
     # the filter bites: many sampled candidates are never collision-checked
     assert got.stats["candidates_sampled"] > 2 * got.stats["candidate_checks"]
     eng.set_reach_filter(1, None)  # cleared: back to plain collision placement for 1
+
+
+def test_sharded_engine_with_reach_filter(gpu, tmp_path):
+    """The fused filter in the sharded kernels (k_fast_round / k_place_instances kReach
+    variants): 2 shards with the per-round count exchange equal the single engine."""
+    import threading
+
+    from paper_2512_16896_b200 import scenes
+    from tests.test_gpu_parity import ThreadAllgather
+
+    n, world = 1500, 2
+    scene = scenes.tabletop_mixed(n, n_objects=8)
+    R = O.RefReachMap.build(RC.arm(), 100000, 0.04, math.pi / 6, seed=3, threads=8)
+    p = str(tmp_path / "arm.sbrm")
+    R.save(p)
+    D = gpu.ReachMap4D.load(p)
+    base = RC.bases(n, 5)
+    ang = np.random.default_rng(5).uniform(0, 2 * math.pi, n)
+    base[:, 0, 3], base[:, 1, 3], base[:, 2, 3] = 1.15 * np.cos(ang), 1.15 * np.sin(ang), 0.5
+    whole_eng = gpu.Engine(scene)
+    for pl in (1, 2, 5):
+        whole_eng.set_reach_filter(pl, D, base)
+    whole = whole_eng.generate(4)
+    ag = ThreadAllgather(world)
+    bounds = [n * r // world for r in range(world + 1)]
+    engines = [gpu.Engine(scene, gpu.Shard(bounds[r], bounds[r + 1], r, world, ag.fn(r)))
+               for r in range(world)]
+    for r, e in enumerate(engines):
+        for pl in (1, 2, 5):
+            e.set_reach_filter(pl, D, base[bounds[r]:bounds[r + 1]])
+    results = [None] * world
+
+    def run(r):
+        results[r] = engines[r].generate(4)
+
+    ts = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert np.array_equal(np.concatenate([r.accepted for r in results], axis=1), whole.accepted)
+    assert np.array_equal(np.concatenate([r.valid for r in results]), whole.valid)
+    assert whole.stats["candidates_sampled"] > 2 * whole.stats["candidate_checks"]
