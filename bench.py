@@ -147,8 +147,11 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         from paper_2512_16896_b200.dist import torch_allgather
 
+        xdev = getattr(args, "xdev", None)
+        from paper_2512_16896_b200.dist import nccl_allgather_dev
         shard = pkg.Shard(rank * n_per, (rank + 1) * n_per, rank, world,
-                          torch_allgather(world, getattr(args, "xdev", None)))
+                          torch_allgather(world, xdev),
+                          nccl_allgather_dev(world, xdev) if xdev is not None else None)
     t0 = time.time()
     eng = pkg.Engine(scene, shard, device=device)
     cold_s = time.time() - t0

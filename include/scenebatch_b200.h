@@ -228,11 +228,19 @@ typedef struct sb_run_stats {
  * must return every rank's values in rank order (recv has n * world_size slots). */
 typedef int (*sb_allgather_fn)(void* ctx, const uint64_t* send, uint32_t n, uint64_t* recv);
 
+/* Optional device-side variant: enqueue, on `cuda_stream` (a cudaStream_t), an all-gather of
+ * n u64 from device memory `d_send` of every rank into `d_recv` (rank-major, world * n),
+ * e.g. ncclAllGather; returns 0 on success. With it, FIFO placements chain their rounds on
+ * the device (the host only checks for completion every few rounds). */
+typedef int (*sb_allgather_dev_fn)(void* ctx, const uint64_t* d_send, uint32_t n,
+                                   uint64_t* d_recv, void* cuda_stream);
 typedef struct sb_shard {
   uint64_t begin, end;     /* this rank owns global instances [begin, end) */
   int32_t rank, world_size;
   sb_allgather_fn allgather; /* required when world_size > 1 */
   void* ctx;
+  sb_allgather_dev_fn allgather_dev; /* optional (NULL: host exchange per round) */
+  void* ctx_dev;
 } sb_shard;
 
 typedef struct sb_engine sb_engine;

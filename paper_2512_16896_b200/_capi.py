@@ -95,9 +95,15 @@ ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_uint64), C.c_uint3
                            C.POINTER(C.c_uint64))
 
 
+# (ctx, d_send, n, d_recv, cuda_stream) -> status: device-side all-gather
+ALLGATHER_DEV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p,
+                               C.c_void_p)
+
+
 class sb_shard(C.Structure):
     _fields_ = [("begin", C.c_uint64), ("end", C.c_uint64), ("rank", C.c_int32),
-                ("world_size", C.c_int32), ("allgather", ALLGATHER_FN), ("ctx", C.c_void_p)]
+                ("world_size", C.c_int32), ("allgather", ALLGATHER_FN), ("ctx", C.c_void_p),
+                ("allgather_dev", ALLGATHER_DEV_FN), ("ctx_dev", C.c_void_p)]
 
 
 # Every symbol the header declares, with (restype, argtypes).

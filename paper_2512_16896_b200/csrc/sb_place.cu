@@ -689,7 +689,8 @@ template <bool kGrid, bool kReach>
 // previous round (persistent kernel), so the list is not reloaded.
 __device__ uint64_t fast_round(const PlaceParams& p, const Sampling& S, const SbGeom& gA,
                                Tile& T, Fixed& F, int32_t a, uint64_t draws, Local& L,
-                               uint32_t* total_word, bool resident) {
+                               uint32_t* total_word, bool resident,
+                               unsigned long long* total_word64 = nullptr) {
   const uint32_t* cin = p.tile_cnt + (size_t)(a & 1) * p.cnt_stride;
   uint32_t* cout = p.tile_cnt + (size_t)((a + 1) & 1) * p.cnt_stride;
   const uint64_t total = tile_prefix(p, cin, F);
@@ -712,6 +713,7 @@ __device__ uint64_t fast_round(const PlaceParams& p, const Sampling& S, const Sb
     __syncthreads();
   }
   if (total_word && threadIdx.x == 0 && mine) atomicAdd(total_word, mine);
+  if (total_word64 && threadIdx.x == 0 && mine) atomicAdd(total_word64, (unsigned long long)mine);
   return total;
 }
 
@@ -908,7 +910,10 @@ __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_fast_init(PlacePara
     mine += n;
     __syncthreads();
   }
-  if (threadIdx.x == 0 && mine) atomicAdd(p.ctrl + place_total_word(0), mine);
+  if (threadIdx.x == 0 && mine) {
+    if (p.xcount) atomicAdd(p.xcount, (unsigned long long)mine);
+    else atomicAdd(p.ctrl + place_total_word(0), mine);
+  }
 }
 
 template <bool kGrid, bool kReach>
@@ -919,7 +924,25 @@ __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_fast_round(PlacePar
   block_setup(p, F, T, gA);
   Local L;
   Sampling S{1, p.canon_tris, p.canon_cum, p.canon_n};
-  fast_round<kGrid, kReach>(p, S, gA, T, F, a, p.draw_base, L, p.ctrl + place_total_word(a + 1), false);
+  if (p.xrecv) {  // device-side exchange: this round's offsets from the gathered counts
+    unsigned long long tot = 0, before = 0;
+    for (int r = 0; r < p.xworld; ++r) {
+      const unsigned long long v = __ldcg(p.xrecv + (size_t)a * p.xworld + r);
+      tot += v;
+      if (r < p.xrank) before += v;
+    }
+    if (tot == 0) return;  // every rank is done: a no-op round
+    const unsigned long long draws = __ldcg(p.xdraws + a);
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+      p.xdraws[a + 1] = draws + (p.canon_n > 0 ? tot : 0ull);  // cache drained only if sampled
+    // this rank has no survivors left (its tile counts are no longer maintained): idle
+    if (__ldcg(p.xrecv + (size_t)a * p.xworld + p.xrank) == 0) return;
+    fast_round<kGrid, kReach>(p, S, gA, T, F, a, draws + before, L, nullptr, false,
+                              p.xcount + a + 1);
+  } else {
+    fast_round<kGrid, kReach>(p, S, gA, T, F, a, p.draw_base, L, p.ctrl + place_total_word(a + 1),
+                              false);
+  }
   flush(p, L);
 }
 

@@ -74,6 +74,14 @@ struct PlaceParams {
   uint32_t* ctrl;               // [8] per placement: see Ctrl in sb_place.cu
   unsigned long long* counters; // [8]
   uint64_t draw_base;           // sharded fast path: draws before this rank this round
+  // Sharded fast path with a device-side count exchange (sb_shard.allgather_dev): round a
+  // reads the gathered counts xrecv[a][world] and the draws before it xdraws[a] on the
+  // device (no host round trip), adds its survivors into xcount[a + 1] and writes
+  // xdraws[a + 1]; a round whose gathered total is 0 returns at once.
+  const unsigned long long* xrecv;
+  unsigned long long* xdraws;
+  unsigned long long* xcount;
+  int32_t xrank, xworld;
   unsigned* dbg;                // optional [attempts][3] per-round CTA maxima (ns), fast path
   unsigned* dbg_inst;           // optional [5] per-instance tiles: max ns, sum us, max/sum rounds, n
   uint64_t* prof;               // optional timers (ns) [init, rounds, -, -, -, rounds]

@@ -540,6 +540,10 @@ struct sb_engine {
   int rank = 0, world_size = 1;
   sb_allgather_fn allgather = nullptr;
   void* allgather_ctx = nullptr;
+  sb_allgather_dev_fn allgather_dev = nullptr;  // device-side count exchange (optional)
+  void* allgather_dev_ctx = nullptr;
+  DevArray<unsigned long long> d_xcount, d_xrecv, d_xdraws;
+  PinnedArray<unsigned long long> h_xrecv;
   int attempts = 0;
 
   struct Placement {
@@ -629,6 +633,8 @@ struct sb_engine {
       world_size = shard->world_size;
       allgather = shard->allgather;
       allgather_ctx = shard->ctx;
+      allgather_dev = shard->allgather_dev;
+      allgather_dev_ctx = shard->ctx_dev;
       if (world_size < 1 || rank < 0 || rank >= world_size) throw std::invalid_argument("bad shard rank");
       if (world_size > 1 && !allgather) throw std::invalid_argument("sharded engine needs an allgather callback");
     }
@@ -1054,6 +1060,63 @@ struct sb_engine {
         ++launches;
         ++round_launches;
         cuda_check(cudaEventSynchronize(ev_r1), "sync");
+        float ms = 0.f;
+        cuda_check(cudaEventElapsedTime(&ms, ev_r0, ev_r1), "elapsed");
+        sharded_check_ms += ms;
+      } else if (allgather_dev) {
+        // FIFO fast path, device-side exchange: round a's kernel reads the gathered counts
+        // and the draws before it from device memory, the all-gather of its survivors is
+        // enqueued behind it; the host only checks for completion every kChunk rounds.
+        constexpr int kChunk = 4;
+        const size_t K1 = static_cast<size_t>(attempts) + 1, W = static_cast<size_t>(world_size);
+        d_xcount.ensure(K1);
+        d_xrecv.ensure(K1 * W);
+        d_xdraws.ensure(K1);
+        h_xrecv.ensure(K1 * W);
+        cuda_check(cudaMemsetAsync(d_xcount.p, 0, K1 * 8, stream), "memset");
+        cuda_check(cudaMemsetAsync(d_xdraws.p, 0, K1 * 8, stream), "memset");
+        pp.xcount = d_xcount.p;
+        pp.xrecv = d_xrecv.p;
+        pp.xdraws = d_xdraws.p;
+        pp.xrank = rank;
+        pp.xworld = world_size;
+        auto gather = [&](int32_t a) {
+          if (allgather_dev(allgather_dev_ctx, reinterpret_cast<const uint64_t*>(d_xcount.p + a), 1,
+                            reinterpret_cast<uint64_t*>(d_xrecv.p + a * W), stream) != 0)
+            throw std::runtime_error("sb_shard.allgather_dev failed");
+        };
+        cuda_check(cudaEventRecord(ev_r0, stream), "event");
+        sbk::place_fast_init(pp, grid, smem, s);
+        ++launches;
+        gather(0);
+        int32_t a = 0;
+        uint64_t last_total = 1;
+        while (a < attempts && last_total > 0) {
+          const int32_t stop = std::min<int32_t>(attempts, a + kChunk);
+          for (; a < stop; ++a) {
+            sbk::place_fast_round(pp, a, grid, smem, s);
+            launches += 1;
+            round_launches += 1;
+            gather(a + 1);
+          }
+          cuda_check(cudaMemcpyAsync(h_xrecv.p + a * W, d_xrecv.p + a * W, W * 8, cudaMemcpyDeviceToHost, stream), "D2H counts");
+          cuda_check(cudaStreamSynchronize(stream), "sync");
+          last_total = 0;
+          for (size_t r = 0; r < W; ++r) last_total += h_xrecv.p[a * W + r];
+        }
+        cuda_check(cudaEventRecord(ev_r1, stream), "event");
+        cuda_check(cudaMemcpyAsync(h_xrecv.p, d_xrecv.p, K1 * W * 8, cudaMemcpyDeviceToHost, stream), "D2H counts");
+        cuda_check(cudaStreamSynchronize(stream), "sync");
+        for (int32_t r = 0; r < a; ++r) {  // rounds the reference runs: total > 0
+          uint64_t t = 0;
+          for (size_t k = 0; k < W; ++k) t += h_xrecv.p[r * W + k];
+          if (t > 0) ++rounds_host;
+        }
+        if (a == attempts && last_total > 0) {
+          pp.xrecv = nullptr;  // mark the K-attempt survivors invalid
+          sbk::place_fast_finish(pp, a, grid, s);
+          ++launches;
+        }
         float ms = 0.f;
         cuda_check(cudaEventElapsedTime(&ms, ev_r0, ev_r1), "elapsed");
         sharded_check_ms += ms;

@@ -53,3 +53,26 @@ def init_group(local_rank: int):
                 dist.destroy_process_group()
     dist.init_process_group("gloo")
     return None
+
+
+class _DevArray:
+    """Zero-copy view of n u64 at a raw device pointer (__cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<u8", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def nccl_allgather_dev(world: int, device):
+    """sb_shard.allgather_dev over the NCCL backend of the initialised group: the engine's
+    device count words are gathered in place on the engine's stream (no host round trip)."""
+    import torch
+    import torch.distributed as dist
+
+    def allgather_dev(send_ptr: int, n: int, recv_ptr: int, stream_ptr: int) -> None:
+        src = torch.as_tensor(_DevArray(send_ptr, n), device=device).view(torch.int64)
+        dst = torch.as_tensor(_DevArray(recv_ptr, world * n), device=device).view(torch.int64)
+        with torch.cuda.stream(torch.cuda.ExternalStream(stream_ptr, device=device)):
+            dist.all_gather_into_tensor(dst, src)
+
+    return allgather_dev

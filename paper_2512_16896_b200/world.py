@@ -294,11 +294,17 @@ class GenerationResult:
 
 
 class Shard:
-    """Instance range [begin, end) of one rank plus the allgather used by the fast path."""
+    """Instance range [begin, end) of one rank plus the allgather used by the fast path.
+    `allgather(vals) -> list` exchanges host u64 values; the optional
+    `allgather_dev(send_ptr, n, recv_ptr, stream_ptr)` enqueues a device-side all-gather of
+    n u64 (device pointers) on the engine's CUDA stream (e.g. NCCL), which lets FIFO
+    placements chain their rounds on the device."""
 
-    def __init__(self, begin: int, end: int, rank: int, world_size: int, allgather=None):
+    def __init__(self, begin: int, end: int, rank: int, world_size: int, allgather=None,
+                 allgather_dev=None):
         self.begin, self.end, self.rank, self.world_size = begin, end, rank, world_size
         self._py = allgather
+        self._pydev = allgather_dev
 
         def _cb(ctx, send, n, recv):
             try:
@@ -312,10 +318,21 @@ class Shard:
                 traceback.print_exc()
                 return 1
 
+        def _cbdev(ctx, send, n, recv, stream):
+            try:
+                self._pydev(send, n, recv, stream)
+                return 0
+            except Exception:  # pragma: no cover - surfaced as an engine error
+                import traceback
+                traceback.print_exc()
+                return 1
+
         self._cb = A.ALLGATHER_FN(_cb) if allgather is not None else A.ALLGATHER_FN()
+        self._cbdev = A.ALLGATHER_DEV_FN(_cbdev) if allgather_dev is not None else A.ALLGATHER_DEV_FN()
 
     def to_c(self):
-        return A.sb_shard(self.begin, self.end, self.rank, self.world_size, self._cb, None)
+        return A.sb_shard(self.begin, self.end, self.rank, self.world_size, self._cb, None,
+                          self._cbdev, None)
 
 
 class Engine:

@@ -284,6 +284,64 @@ class ThreadAllgather:
         return allgather
 
 
+class ThreadDevAllgather:
+    """In-process stand-in for NCCL all_gather on the engines' streams (shards on one GPU):
+    each rank records an event behind its send word, every rank's stream waits for all the
+    events and copies the words into its receive buffer (device to device)."""
+
+    def __init__(self, world):
+        self.world = world
+        self.barrier = threading.Barrier(world)
+        self.slots = [None] * world
+
+    def fn(self, rank):
+        import torch
+
+        from paper_2512_16896_b200.dist import _DevArray
+
+        def allgather_dev(send, n, recv, stream):
+            ext = torch.cuda.ExternalStream(stream)
+            ev = torch.cuda.Event()
+            ev.record(ext)
+            self.slots[rank] = (send, ev)
+            self.barrier.wait()
+            dst = torch.as_tensor(_DevArray(recv, self.world * n), device="cuda")
+            with torch.cuda.stream(ext):
+                for r, (sp, evr) in enumerate(self.slots):
+                    ext.wait_event(evr)
+                    dst[r * n:(r + 1) * n].copy_(torch.as_tensor(_DevArray(sp, n), device="cuda"))
+            self.barrier.wait()
+        return allgather_dev
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_device_exchange_equals_single(gpu, ref, world):
+    """FIFO placements with the device-side count exchange (sb_shard.allgather_dev: rounds
+    chained on the device, host checks every few rounds) equal the single-shard run."""
+    pkg = gpu
+    scene = scenes.tabletop_mixed(1500, n_objects=10)
+    whole = pkg.Engine(scene).generate(4)
+    ag, agd = ThreadAllgather(world), ThreadDevAllgather(world)
+    bounds = [scene.n_instances * r // world for r in range(world + 1)]
+    engines = [pkg.Engine(scene, pkg.Shard(bounds[r], bounds[r + 1], r, world, ag.fn(r),
+                                           agd.fn(r))) for r in range(world)]
+    results = [None] * world
+
+    def run(r):
+        results[r] = engines[r].generate(4)
+
+    ts = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert all(r is not None for r in results)
+    assert np.array_equal(np.concatenate([r.accepted for r in results], axis=1), whole.accepted)
+    assert np.array_equal(np.concatenate([r.valid for r in results]), whole.valid)
+    assert np.array_equal(np.concatenate([r.poses for r in results], axis=1), whole.poses)
+    assert sum(r.stats["rounds"] for r in results) >= whole.stats["rounds"]
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_sharded_generate_equals_single(gpu, ref, world):
     """Variation-batch sharding: G shards with the per-round count exchange
