@@ -309,6 +309,14 @@ sb_status sb_sampler_sample(sb_sampler* s, const double* support_colmajor16xN,
 sb_status sb_sampler_prepare_relation(sb_sampler* s, const sb_relation* rel,
                                       const double support_rect[4], const double* anchor_states,
                                       uint64_t n, uint64_t run_seed);
+/* Device-resident sample(): support_world (batch_size column-major Mat4), active,
+ * positions and placeable are DEVICE pointers; the work is enqueued on cuda_stream (a
+ * cudaStream_t) -- only the SampleCache bookkeeping runs on the host. Active indices must
+ * be < batch_size (not checked on the device). */
+sb_status sb_sampler_sample_device(sb_sampler* s, const double* d_support_colmajor16xN,
+                                   const uint32_t* d_active, uint64_t m, uint64_t attempt,
+                                   double* d_positions_xyz, uint8_t* d_placeable,
+                                   void* cuda_stream);
 /* SampleCache state (sampler.hpp:18-36): points queued, refills so far. */
 sb_status sb_sampler_cache_info(const sb_sampler* s, uint64_t* queue_size, uint64_t* refill_count);
 /* sample_orientations (sampler.cpp:129-156): kind = SB_ORIENT_*; face_targets_xy = one
@@ -343,6 +351,9 @@ sb_status sb_graph_set_joint_states(sb_graph* g, uint32_t node, const double* va
 sb_status sb_graph_joint_states(const sb_graph* g, uint32_t node, double* values_N);
 /* world_poses(node) (scene_graph.cpp:131-151): batched FK on the device */
 sb_status sb_graph_world_poses(const sb_graph* g, uint32_t node, double* poses_colmajor16xN);
+/* world_poses into device memory (N column-major Mat4), enqueued on cuda_stream */
+sb_status sb_graph_world_poses_device(const sb_graph* g, uint32_t node, double* d_poses16xN,
+                                      void* cuda_stream);
 /* world_pose(node, instance) (scene_graph.cpp:153-158) */
 sb_status sb_graph_world_pose(const sb_graph* g, uint32_t node, uint64_t instance, double pose[16]);
 /* find(name): *id = -1 when absent */
@@ -398,6 +409,11 @@ sb_status sb_reach_cell_samples(const sb_reach_map* m, uint64_t ir, uint64_t iz,
 sb_status sb_reach_query_batch(const sb_reach_map* m, const double* base_colmajor16xN,
                                const double* targets_xyz, uint64_t n, int has_inclination,
                                double inclination, uint8_t* out);
+/* query_batch with device pointers (base poses, targets, out), enqueued on cuda_stream */
+sb_status sb_reach_query_batch_device(const sb_reach_map* m, const double* d_base_colmajor16xN,
+                                      const double* d_targets_xyz, uint64_t n,
+                                      int has_inclination, double inclination, uint8_t* d_out,
+                                      void* cuda_stream);
 /* placement_filter(map, robot_base, frames, active) (reachability.cpp:164-190): frames =
  * n_frames pointers to N column-major poses each (NULL entries skipped). */
 sb_status sb_reach_placement_filter(const sb_reach_map* m, const double* robot_base16xN,

@@ -323,9 +323,12 @@ class RefSampler:
         self.h = lib().ref_sampler_create(salt)
 
     def __del__(self):
-        if getattr(self, "h", None):
-            lib().ref_sampler_destroy(self.h)
-            self.h = None
+        try:
+            if getattr(self, "h", None):
+                lib().ref_sampler_destroy(self.h)
+                self.h = None
+        except Exception:  # interpreter shutdown
+            pass
 
     def prepare(self, rings, n: int, run_seed: int, instance_rings=None):
         self._xy, self._off = _rings(rings)
@@ -383,9 +386,12 @@ class RefGraph:
         self.n = n
 
     def __del__(self):
-        if getattr(self, "h", None):
-            lib().ref_graph_destroy(self.h)
-            self.h = None
+        try:
+            if getattr(self, "h", None):
+                lib().ref_graph_destroy(self.h)
+                self.h = None
+        except Exception:  # interpreter shutdown
+            pass
 
     def add_node(self, parent, name, geometry_id=-1, joint=None):
         out = C.c_uint32()
@@ -463,9 +469,12 @@ class RefReachMap:
         return cls(lib().ref_reach_load(path.encode()))
 
     def __del__(self):
-        if getattr(self, "h", None):
-            lib().ref_reach_destroy(self.h)
-            self.h = None
+        try:
+            if getattr(self, "h", None):
+                lib().ref_reach_destroy(self.h)
+                self.h = None
+        except Exception:  # interpreter shutdown
+            pass
 
     def save(self, path):
         check(lib().ref_reach_save(self.h, path.encode()))

@@ -193,6 +193,10 @@ SIGNATURES = {
     "sb_reach_placement_filter": (C.c_int, [_P, _D, C.c_uint64, C.POINTER(_D), C.c_uint32, _U32,
                                             C.c_uint64, C.POINTER(C.c_uint8)]),
     "sb_engine_set_reach_filter": (C.c_int, [_P, C.c_uint32, _P, _D]),
+    "sb_sampler_sample_device": (C.c_int, [_P, _P, _P, C.c_uint64, C.c_uint64, _P, _P, _P]),
+    "sb_graph_world_poses_device": (C.c_int, [_P, C.c_uint32, _P, _P]),
+    "sb_reach_query_batch_device": (C.c_int, [_P, _P, _P, C.c_uint64, C.c_int, C.c_double, _P,
+                                              _P]),
     "sb_sampler_cache_info": (C.c_int, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "sb_sample_orientations": (C.c_int, [C.c_int, _U32, C.c_uint64, _D, _D, C.c_uint64,
                                          C.c_uint64, C.c_uint64, C.c_uint64, _D, C.c_int]),

@@ -209,7 +209,24 @@ __global__ void k_debug_math(int fn, const double* in, uint64_t n, double* out) 
 // Fast path (sampler.cpp:78-97): the j-th active entry takes FIFO point j, which is draw
 // number seg_draw[s] + (j - seg_first[s]) of the cache stream (the host keeps the queue as
 // draw-index ranges, SampleCache semantics). Draw d = 6d PCG steps in (polygon.cpp:390-400).
-__global__ void k_sampler_fifo(const double* sup34, uint64_t m, const uint64_t* seg_first,
+// Support pose of active entry j: host-gathered row-major 3x4 (sup34), or column-major Mat4
+// of instance active[j] read in place (device-resident API).
+__device__ __forceinline__ void support_of(const double* sup34, const double* sup16,
+                                           const uint32_t* active, uint64_t j, M34& S) {
+  if (sup34) {
+#pragma unroll
+    for (int k = 0; k < 12; ++k) S.m[k] = __ldg(sup34 + 12 * j + k);
+  } else {
+    const double* c = sup16 + 16 * (uint64_t)__ldg(active + j);
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) S.m[4 * r + k] = __ldg(c + 4 * k + r);
+  }
+}
+
+__global__ void k_sampler_fifo(const double* sup34, const double* sup16, const uint32_t* active,
+                               uint64_t m, const uint64_t* seg_first,
                                const uint64_t* seg_draw, int nseg, uint64_t state0,
                                const SbRegionTri* tris, const double* cum, int nt, double* pos) {
   const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -226,8 +243,7 @@ __global__ void k_sampler_fifo(const double* sup34, uint64_t m, const uint64_t* 
   double lx, ly;
   sbp::draw_point(tris, cum, nt, u, r1, r2, lx, ly);
   M34 S;
-#pragma unroll
-  for (int k = 0; k < 12; ++k) S.m[k] = __ldg(sup34 + 12 * j + k);
+  support_of(sup34, sup16, active, j, S);
   double px, py, pz;
   xform(S, lx, ly, 0.0, px, py, pz);  // transform_point(support_world[inst], (x, y, 0))
   pos[3 * j] = px;
@@ -237,7 +253,8 @@ __global__ void k_sampler_fifo(const double* sup34, uint64_t m, const uint64_t* 
 
 // Per-instance regions (sampler.cpp:101-126): one draw from instance inst's own table on
 // make_stream(run_seed, {salt, "fall", inst, attempt}); an empty table -> not placeable.
-__global__ void k_sampler_fallback(const double* sup34, const uint32_t* active, uint64_t m,
+__global__ void k_sampler_fallback(const double* sup34, const double* sup16,
+                                   const uint32_t* active, uint64_t m,
                                    uint64_t run_seed, uint64_t salt, uint64_t attempt,
                                    const uint32_t* inst_tab, const int32_t* inst_n, int cap,
                                    const SbRegionTri* tris, const double* cum, double* pos,
@@ -260,8 +277,7 @@ __global__ void k_sampler_fallback(const double* sup34, const uint32_t* active, 
     double lx, ly;
     sbp::draw_point(tris + o0, cum + o0, (int)nt, u, r1, r2, lx, ly);
     M34 S;
-#pragma unroll
-    for (int k = 0; k < 12; ++k) S.m[k] = __ldg(sup34 + 12 * j + k);
+    support_of(sup34, sup16, active, j, S);
     xform(S, lx, ly, 0.0, px, py, pz);
   }
   pos[3 * j] = px;
@@ -369,20 +385,22 @@ void download_poses(const SbWorldView& w, int32_t obj, double* out16, sb_stream_
   check_launch("download_poses");
 }
 
-void sampler_fifo(const double* sup34, uint64_t m, const uint64_t* seg_first,
-                  const uint64_t* seg_draw, int nseg, uint64_t state0, const SbRegionTri* tris,
-                  const double* cum, int nt, double* pos, sb_stream_t s) {
+void sampler_fifo(const double* sup34, const double* sup16, const uint32_t* active, uint64_t m,
+                  const uint64_t* seg_first, const uint64_t* seg_draw, int nseg, uint64_t state0,
+                  const SbRegionTri* tris, const double* cum, int nt, double* pos, sb_stream_t s) {
   if (m == 0) return;
-  k_sampler_fifo<<<grid_for(m, 256), 256, 0, s>>>(sup34, m, seg_first, seg_draw, nseg, state0,
-                                                  tris, cum, nt, pos);
+  k_sampler_fifo<<<grid_for(m, 256), 256, 0, s>>>(sup34, sup16, active, m, seg_first, seg_draw,
+                                                  nseg, state0, tris, cum, nt, pos);
   check_launch("sampler_fifo");
 }
-void sampler_fallback(const double* sup34, const uint32_t* active, uint64_t m, uint64_t run_seed,
+void sampler_fallback(const double* sup34, const double* sup16, const uint32_t* active,
+                      uint64_t m, uint64_t run_seed,
                       uint64_t salt, uint64_t attempt, const uint32_t* inst_tab,
                       const int32_t* inst_n, int cap, const SbRegionTri* tris, const double* cum,
                       double* pos, uint8_t* placeable, sb_stream_t s) {
   if (m == 0) return;
-  k_sampler_fallback<<<grid_for(m, 256), 256, 0, s>>>(sup34, active, m, run_seed, salt, attempt,
+  k_sampler_fallback<<<grid_for(m, 256), 256, 0, s>>>(sup34, sup16, active, m, run_seed, salt,
+                                                      attempt,
                                                       inst_tab, inst_n, cap, tris, cum, pos,
                                                       placeable);
   check_launch("sampler_fallback");

@@ -50,10 +50,12 @@ void download_poses(const SbWorldView& w, int32_t obj, double* out16, sb_stream_
 // standalone PositionSampler / sample_orientations (sampler.cpp:54-156). sup34: one
 // row-major 3x4 support pose per active entry (host-gathered); inst_tab: per instance
 // (first table row, rows) into tris/cum, or NULL: [n][cap] tables with inst_n rows each.
-void sampler_fifo(const double* sup34, uint64_t m, const uint64_t* seg_first,
-                  const uint64_t* seg_draw, int nseg, uint64_t state0, const SbRegionTri* tris,
-                  const double* cum, int nt, double* pos, sb_stream_t s);
-void sampler_fallback(const double* sup34, const uint32_t* active, uint64_t m, uint64_t run_seed,
+// sup34 == NULL: supports read in place from sup16 (N column-major Mat4) at active[j]
+void sampler_fifo(const double* sup34, const double* sup16, const uint32_t* active, uint64_t m,
+                  const uint64_t* seg_first, const uint64_t* seg_draw, int nseg, uint64_t state0,
+                  const SbRegionTri* tris, const double* cum, int nt, double* pos, sb_stream_t s);
+void sampler_fallback(const double* sup34, const double* sup16, const uint32_t* active,
+                      uint64_t m, uint64_t run_seed,
                       uint64_t salt, uint64_t attempt, const uint32_t* inst_tab,
                       const int32_t* inst_n, int cap, const SbRegionTri* tris, const double* cum,
                       double* pos, uint8_t* placeable, sb_stream_t s);

@@ -1660,6 +1660,7 @@ struct sb_sampler {
     cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
   }
   ~sb_sampler() {
+    if (ev_seg) cudaEventDestroy(ev_seg);
     if (stream) {
       cudaSetDevice(device);
       cudaStreamSynchronize(stream);
@@ -1892,7 +1893,8 @@ struct sb_sampler {
       const int nseg = drain(m);
       d_seg.ensure(2 * nseg);
       cuda_check(cudaMemcpyAsync(d_seg.p, h_seg.p, 2 * nseg * sizeof(uint64_t), cudaMemcpyHostToDevice, stream), "H2D segments");
-      sbk::sampler_fifo(d_sup.p, m, d_seg.p, d_seg.p + nseg, nseg, cache_state0(run_seed, salt),
+      sbk::sampler_fifo(d_sup.p, nullptr, nullptr, m, d_seg.p, d_seg.p + nseg, nseg,
+                        cache_state0(run_seed, salt),
                         d_tris.p, d_cum.p, region_nt, d_pos.p, stream);
       cuda_check(cudaMemcpyAsync(pos, d_pos.p, 3 * m * sizeof(double), cudaMemcpyDeviceToHost, stream), "D2H positions");
       cuda_check(cudaStreamSynchronize(stream), "sync");
@@ -1902,12 +1904,51 @@ struct sb_sampler {
     d_active.ensure(m);
     d_pl.ensure(m);
     cuda_check(cudaMemcpyAsync(d_active.p, active, m * 4, cudaMemcpyHostToDevice, stream), "H2D active");
-    sbk::sampler_fallback(d_sup.p, d_active.p, m, run_seed, salt, attempt,
+    sbk::sampler_fallback(d_sup.p, nullptr, d_active.p, m, run_seed, salt, attempt,
                           stride_tables ? nullptr : d_inst_tab.p, d_inst_n.p, table_cap, d_tris.p,
                           d_cum.p, d_pos.p, d_pl.p, stream);
     cuda_check(cudaMemcpyAsync(pos, d_pos.p, 3 * m * sizeof(double), cudaMemcpyDeviceToHost, stream), "D2H positions");
     cuda_check(cudaMemcpyAsync(placeable, d_pl.p, m, cudaMemcpyDeviceToHost, stream), "D2H placeable");
     cuda_check(cudaStreamSynchronize(stream), "sync");
+  }
+
+  // Device-resident variant: supports (N column-major Mat4), active, positions and
+  // placeable are device pointers; everything is enqueued on `st` (no host round trip but
+  // the SampleCache bookkeeping, which stays on the host).
+  cudaEvent_t ev_seg = nullptr;
+  void sample_device(const double* d_sup16, const uint32_t* d_act, uint64_t m, uint64_t attempt,
+                     double* d_out, uint8_t* d_placeable, cudaStream_t st) {
+    if (!prepared) throw std::logic_error("PositionSampler: prepare() not called");
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    if (m && (!d_sup16 || !d_act || !d_out || !d_placeable))
+      throw std::invalid_argument("sample_device: NULL array");
+    if (!per_instance && region_empty) {
+      if (m) {
+        cuda_check(cudaMemsetAsync(d_out, 0, 3 * m * sizeof(double), st), "memset");
+        cuda_check(cudaMemsetAsync(d_placeable, 0, m, st), "memset");
+      }
+      return;
+    }
+    if (!per_instance && region_nt == 0)
+      throw std::invalid_argument("sample: canonical region has zero area");
+    if (!per_instance) {
+      if (!ev_seg) cuda_check(cudaEventCreateWithFlags(&ev_seg, cudaEventDisableTiming), "event");
+      cuda_check(cudaEventSynchronize(ev_seg), "sync segments");  // h_seg reusable
+      const int nseg = drain(m);
+      if (m == 0) return;
+      d_seg.ensure(2 * nseg);
+      cuda_check(cudaMemcpyAsync(d_seg.p, h_seg.p, 2 * nseg * sizeof(uint64_t), cudaMemcpyHostToDevice, st), "H2D segments");
+      cuda_check(cudaEventRecord(ev_seg, st), "event");
+      sbk::sampler_fifo(nullptr, d_sup16, d_act, m, d_seg.p, d_seg.p + nseg, nseg,
+                        cache_state0(run_seed, salt), d_tris.p, d_cum.p, region_nt, d_out,
+                        reinterpret_cast<sb_stream_t>(st));
+      cuda_check(cudaMemsetAsync(d_placeable, 1, m, st), "memset");
+      return;
+    }
+    if (m == 0) return;
+    sbk::sampler_fallback(nullptr, d_sup16, d_act, m, run_seed, salt, attempt,
+                          stride_tables ? nullptr : d_inst_tab.p, d_inst_n.p, table_cap, d_tris.p,
+                          d_cum.p, d_out, d_placeable, reinterpret_cast<sb_stream_t>(st));
   }
 };
 
@@ -1955,6 +1996,14 @@ sb_status sb_sampler_prepare_relation(sb_sampler* s, const sb_relation* rel,
   return guard([&] {
     if (!rel || !support_rect) throw std::invalid_argument("relation / support rect is NULL");
     s->prepare_relation(*rel, support_rect, anchor_states, n, run_seed);
+  });
+}
+sb_status sb_sampler_sample_device(sb_sampler* s, const double* d_support16, const uint32_t* d_active,
+                                   uint64_t m, uint64_t attempt, double* d_positions,
+                                   uint8_t* d_placeable, void* cuda_stream) {
+  return guard([&] {
+    s->sample_device(d_support16, d_active, m, attempt, d_positions, d_placeable,
+                     static_cast<cudaStream_t>(cuda_stream));
   });
 }
 sb_status sb_sampler_cache_info(const sb_sampler* s, uint64_t* queue_size, uint64_t* refills) {
@@ -2042,6 +2091,7 @@ struct sb_graph {
     sync();
   }
   ~sb_graph() {
+    if (ev_chain) cudaEventDestroy(ev_chain);
     if (stream) {
       cudaSetDevice(device);
       cudaStreamSynchronize(stream);
@@ -2211,6 +2261,29 @@ struct sb_graph {
     cuda_check(cudaMemcpyAsync(out16, d_tmp16.p, 16 * n * sizeof(double), cudaMemcpyDeviceToHost, stream), "D2H");
     sync();
   }
+  // batched FK into device memory on the caller's stream
+  void world_poses_device(uint32_t node, double* d_out16, cudaStream_t st) const {
+    activate();
+    at(node);
+    cuda_check(cudaStreamSynchronize(stream), "sync");  // the graph's own updates are done
+    std::vector<const double*> chain;
+    for (uint32_t cur = node; cur != 0; cur = nodes[cur].parent) chain.push_back(nodes[cur].edge->p);
+    if (chain.empty()) {
+      sbk::graph_34_to_colmajor(nodes[0].edge->p, n, d_out16, reinterpret_cast<sb_stream_t>(st));
+      return;
+    }
+    if (!ev_chain) cuda_check(cudaEventCreateWithFlags(&ev_chain, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventSynchronize(ev_chain), "sync");  // the previous chain upload is consumed
+    d_chain.ensure(chain.size());
+    h_chain.ensure(chain.size());
+    std::copy(chain.begin(), chain.end(), h_chain.p);
+    cuda_check(cudaMemcpyAsync(d_chain.p, h_chain.p, chain.size() * sizeof(void*), cudaMemcpyHostToDevice, st), "H2D chain");
+    sbk::graph_world_poses(d_chain.p, static_cast<int>(chain.size()), n, d_out16,
+                           reinterpret_cast<sb_stream_t>(st));
+    cuda_check(cudaEventRecord(ev_chain, st), "event");
+  }
+  mutable cudaEvent_t ev_chain = nullptr;
+  mutable PinnedArray<const double*> h_chain;
   void world_pose(uint32_t node, uint64_t i, double* out16) const {
     activate();
     if (i >= n) throw std::out_of_range("instance out of range");
@@ -2299,6 +2372,10 @@ sb_status sb_graph_world_poses(const sb_graph* g, uint32_t node, double* out16) 
 }
 sb_status sb_graph_world_pose(const sb_graph* g, uint32_t node, uint64_t i, double pose[16]) {
   return guard([&] { g->world_pose(node, i, pose); });
+}
+sb_status sb_graph_world_poses_device(const sb_graph* g, uint32_t node, double* d_out16,
+                                      void* cuda_stream) {
+  return guard([&] { g->world_poses_device(node, d_out16, static_cast<cudaStream_t>(cuda_stream)); });
 }
 sb_status sb_graph_find(const sb_graph* g, const char* name, int64_t* id) {
   return guard([&] {
@@ -2642,6 +2719,18 @@ sb_status sb_reach_query_batch(const sb_reach_map* m, const double* base16, cons
                                uint64_t n, int has_incl, double incl, uint8_t* out) {
   return guard([&] {
     const_cast<sb_reach_map*>(m)->query_batch(base16, targets, n, has_incl != 0, incl, out);
+  });
+}
+sb_status sb_reach_query_batch_device(const sb_reach_map* m, const double* d_base16,
+                                      const double* d_targets, uint64_t n, int has_incl,
+                                      double incl, uint8_t* d_out, void* cuda_stream) {
+  return guard([&] {
+    if (!n) return;
+    if (!d_base16 || !d_targets || !d_out) throw std::invalid_argument("query_batch: NULL array");
+    cuda_check(cudaSetDevice(m->device), "cudaSetDevice");
+    sbk::reach_query_batch(m->g, m->d_occ.p, m->d_any.p, d_base16, d_targets, n,
+                           has_incl ? incl : std::nan(""), d_out,
+                           reinterpret_cast<sb_stream_t>(static_cast<cudaStream_t>(cuda_stream)));
   });
 }
 sb_status sb_reach_placement_filter(const sb_reach_map* m, const double* base16, uint64_t n,

@@ -81,6 +81,10 @@ class BatchedSceneGraph:
     def world_poses(self, node: int) -> np.ndarray:
         return self._batch(A.lib().sb_graph_world_poses, node)
 
+    def world_poses_device(self, node: int, d_out16: int, stream: int = 0) -> None:
+        """Batched FK into device memory (N column-major Mat4 at d_out16), on `stream`."""
+        A.check(A.lib().sb_graph_world_poses_device(self._h, node, d_out16, stream or None))
+
     def world_pose(self, node: int, instance: int) -> np.ndarray:
         out = np.empty(16)
         A.check(A.lib().sb_graph_world_pose(self._h, node, instance, _dp(out)))

@@ -89,6 +89,13 @@ class ReachMap4D:
                                              out.ctypes.data_as(C.POINTER(C.c_uint8))))
         return out
 
+    def query_batch_device(self, d_base16: int, d_targets: int, n: int, d_out: int,
+                           inclination: Optional[float] = None, stream: int = 0) -> None:
+        """query_batch on device pointers (N column-major Mat4, N x 3 f64, N u8)."""
+        A.check(A.lib().sb_reach_query_batch_device(
+            self._h, d_base16, d_targets, n, 0 if inclination is None else 1,
+            0.0 if inclination is None else inclination, d_out, stream or None))
+
     def query(self, target_in_base, inclination: Optional[float] = None) -> bool:
         return bool(self.query_batch(np.eye(4)[None], np.asarray(target_in_base)[None],
                                      inclination)[0])

@@ -82,6 +82,14 @@ class PositionSampler:
                                           pl.ctypes.data_as(C.POINTER(C.c_uint8))))
         return pos, pl
 
+    def sample_device(self, d_support16: int, d_active: int, m: int, attempt: int,
+                      d_positions: int, d_placeable: int, stream: int = 0) -> None:
+        """Device-resident sample (raw device pointers, e.g. torch .data_ptr()): supports
+        (N column-major Mat4), active (u32), positions (m x 3 f64), placeable (u8); enqueued
+        on `stream` (a cudaStream_t as int)."""
+        A.check(A.lib().sb_sampler_sample_device(self._h, d_support16, d_active, m, attempt,
+                                                 d_positions, d_placeable, stream or None))
+
     def cache_info(self):
         q, r = C.c_uint64(), C.c_uint64()
         A.check(A.lib().sb_sampler_cache_info(self._h, C.byref(q), C.byref(r)))
