@@ -187,6 +187,9 @@ typedef struct sb_placement {
   int32_t orientation;     /* SB_ORIENT_* */
   int32_t face_target;     /* placement index for SB_ORIENT_FACE_TO, else -1 */
   sb_relation relation;
+  /* apply_ratio_on_support (relationships.cpp:220-230): the region is eroded by
+   * ratio * min(mesh AABB x, y extents) / 2; in [0, 1]; > 0 only without a relation */
+  double ratio_on_support;
 } sb_placement;
 
 typedef struct sb_scene {

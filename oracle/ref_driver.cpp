@@ -670,6 +670,11 @@ int ref_generate(const sb_scene* sc, const sb_shard* shard, uint64_t run_seed, i
         anchors.push_back(std::move(all));
       }
       ConstraintRegion cr = build_constraint_region(spec, support_region, anchors, n_total);
+      if (pl.ratio_on_support != 0.0) {  // footprint = the mesh AABB's x / y extents
+        const Aabb3 fb = meshes.at(pl.mesh).aabb();
+        apply_ratio_on_support(cr, fb.max.x() - fb.min.x(), fb.max.y() - fb.min.y(),
+                               pl.ratio_on_support);
+      }
       if (cr.per_instance) ++per_inst;
       PositionSampler sampler(p);
       sampler.prepare(&cr, n_total, run_seed);

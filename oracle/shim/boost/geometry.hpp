@@ -12,8 +12,9 @@
 //     exact duplicates are dropped; rings with < 3 vertices or zero area are discarded.
 //     This is a DEFINED stand-in: the product restates exactly this algorithm, and parity
 //     against an upstream Boost build of the reference is unpinned.
-// Everything else (buffer/erode, union_, distance, is_valid, convex_hull) throws: those
-// paths (ratio_on_support > 0, support-surface extraction, `middle`) are out of scope.
+// buffer: erosion (negative distance) of convex hole-free polygons (see below).
+// Everything else (union_, distance, is_valid, convex_hull) throws: those paths
+// (support-surface extraction, `middle`) are out of scope.
 #pragma once
 
 #include <cmath>
@@ -187,7 +188,8 @@ namespace strategy {
 namespace buffer {
 template <class T>
 struct distance_symmetric {
-  explicit distance_symmetric(T) {}
+  T value;
+  explicit distance_symmetric(T v) : value(v) {}
 };
 struct side_straight {};
 struct join_round {
@@ -202,9 +204,51 @@ struct point_circle {
 }  // namespace buffer
 }  // namespace strategy
 
-template <class... A>
-void buffer(A&&...) {
-  throw std::runtime_error("boost shim: buffer (erode) is out of scope");
+// buffer with a negative distance on convex, hole-free polygons: the DEFINED stand-in for
+// erode() (polygon.cpp:101-113) -- every edge moves inward by r along its unit normal and
+// vertex i becomes the intersection of the offset edges i-1 and i (same order as the input
+// ring); a polygon whose offset edges reverse (eroded away) is dropped. The product
+// restates exactly this (sbh::erode_convex). Concave or holed input throws.
+template <class Poly, class D, class... Rest>
+void buffer(const model::multi_polygon<Poly>& in, model::multi_polygon<Poly>& out,
+            const strategy::buffer::distance_symmetric<D>& dist, Rest&&...) {
+  const double r = -static_cast<double>(dist.value);
+  if (!(r > 0.0)) throw std::runtime_error("boost shim: buffer supports erosion only");
+  for (const auto& poly : in) {
+    if (!poly.inners().empty()) throw std::runtime_error("boost shim: erosion of a holed polygon");
+    auto ring = shim_detail::open_ring(poly.outer());
+    const std::size_t n = ring.size();
+    if (n < 3) continue;
+    std::vector<double> ax(n), ay(n), dx(n), dy(n);
+    for (std::size_t i = 0; i < n; ++i) {
+      const auto& p = ring[i];
+      const auto& q = ring[(i + 1) % n];
+      const auto& o = ring[(i + n - 1) % n];
+      const double cr = (p.v[0] - o.v[0]) * (q.v[1] - o.v[1]) - (p.v[1] - o.v[1]) * (q.v[0] - o.v[0]);
+      if (cr < 0.0) throw std::runtime_error("boost shim: erosion of a concave polygon");
+      dx[i] = q.v[0] - p.v[0];
+      dy[i] = q.v[1] - p.v[1];
+      const double len = std::sqrt(dx[i] * dx[i] + dy[i] * dy[i]);
+      ax[i] = p.v[0] + (-dy[i] / len) * r;
+      ay[i] = p.v[1] + (dx[i] / len) * r;
+    }
+    Poly res;
+    for (std::size_t i = 0; i < n; ++i) {
+      const std::size_t h = (i + n - 1) % n;
+      const double den = dx[h] * dy[i] - dy[h] * dx[i];
+      const double t = ((ax[i] - ax[h]) * dy[i] - (ay[i] - ay[h]) * dx[i]) / den;
+      res.outer().push_back(typename Poly::ring_type::value_type(ax[h] + t * dx[h], ay[h] + t * dy[h]));
+    }
+    bool alive = true;
+    for (std::size_t i = 0; i < n; ++i) {
+      const auto& p = res.outer()[i];
+      const auto& q = res.outer()[(i + 1) % n];
+      if (!((q.v[0] - p.v[0]) * dx[i] + (q.v[1] - p.v[1]) * dy[i] > 0.0)) alive = false;
+    }
+    if (!alive) continue;
+    shim_detail::close_ring(res.outer());
+    out.push_back(res);
+  }
 }
 template <class... A>
 void union_(A&&...) {

@@ -68,7 +68,8 @@ class sb_relation(C.Structure):
 
 class sb_placement(C.Structure):
     _fields_ = [("mesh", C.c_int32), ("support", C.c_int32), ("orientation", C.c_int32),
-                ("face_target", C.c_int32), ("relation", sb_relation)]
+                ("face_target", C.c_int32), ("relation", sb_relation),
+                ("ratio_on_support", C.c_double)]
 
 
 class sb_scene(C.Structure):

@@ -322,4 +322,35 @@ SamplerTable sampler_table(const std::vector<std::vector<V2>>& part_rings) {
   return out;
 }
 
+std::vector<V2> erode_convex(const std::vector<V2>& ring, double r) {
+  const std::size_t n = ring.size();
+  if (n < 3) return {};
+  std::vector<double> ax(n), ay(n), dx(n), dy(n);
+  for (std::size_t i = 0; i < n; ++i) {
+    const V2& p = ring[i];
+    const V2& q = ring[(i + 1) % n];
+    const V2& o = ring[(i + n - 1) % n];
+    const double cr = (p[0] - o[0]) * (q[1] - o[1]) - (p[1] - o[1]) * (q[0] - o[0]);
+    if (cr < 0.0) throw std::invalid_argument("erode: concave support polygon");
+    dx[i] = q[0] - p[0];
+    dy[i] = q[1] - p[1];
+    const double len = std::sqrt(dx[i] * dx[i] + dy[i] * dy[i]);
+    ax[i] = p[0] + (-dy[i] / len) * r;
+    ay[i] = p[1] + (dx[i] / len) * r;
+  }
+  std::vector<V2> out(n);
+  for (std::size_t i = 0; i < n; ++i) {
+    const std::size_t h = (i + n - 1) % n;
+    const double den = dx[h] * dy[i] - dy[h] * dx[i];
+    const double t = ((ax[i] - ax[h]) * dy[i] - (ay[i] - ay[h]) * dx[i]) / den;
+    out[i] = {ax[h] + t * dx[h], ay[h] + t * dy[h]};
+  }
+  for (std::size_t i = 0; i < n; ++i) {
+    const V2& p = out[i];
+    const V2& q = out[(i + 1) % n];
+    if (!((q[0] - p[0]) * dx[i] + (q[1] - p[1]) * dy[i] > 0.0)) return {};  // eroded away
+  }
+  return out;
+}
+
 }  // namespace sbh

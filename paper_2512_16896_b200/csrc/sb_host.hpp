@@ -55,6 +55,11 @@ struct SamplerTable {
 };
 SamplerTable sampler_table(const std::vector<std::vector<V2>>& part_rings);
 
+// erode() (polygon.cpp:101-113) of a convex counter-clockwise ring by r, as the oracle's
+// Boost stand-in defines buffer(-r): edges move inward by r along their unit normals,
+// vertex i = intersection of offset edges i-1 and i; empty when eroded away.
+std::vector<V2> erode_convex(const std::vector<V2>& ring, double r);
+
 // splitmix64 / make_stream seed derivation (rng.hpp:9-21,63-67)
 uint64_t mix64(uint64_t x);
 

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -553,6 +554,8 @@ struct sb_engine {
     int canon_n = 0;  // host-built canonical table size (no anchor)
     bool hole = false;  // full annulus with a hole (theta = pi, min_r > 0)
     bool shared_arcs = false;  // arc table in d_arcs[p] (no local-frame direction)
+    double ratio = 0.0;        // ratio_on_support (no-relation placements)
+    int mesh = 0;
   };
   std::vector<Placement> places;
   int32_t first_place_obj = 0;
@@ -646,6 +649,7 @@ struct sb_engine {
 
     std::vector<int> geom_of_mesh;
     std::vector<double> z_off;
+    std::vector<std::array<double, 2>> footprint;  // mesh AABB x / y extents
     for (uint32_t i = 0; i < sc->n_meshes; ++i) {
       const sb_mesh& m = sc->meshes[i];
       if (!m.vertices || !m.triangles) throw std::invalid_argument("mesh arrays are NULL");
@@ -658,6 +662,7 @@ struct sb_engine {
         h.t[k] = {m.triangles[3 * k], m.triangles[3 * k + 1], m.triangles[3 * k + 2]};
       double box[6];
       sbh::mesh_aabb(h, box);  // rest_pose uses the mesh as given (sampler.cpp:45-52)
+      footprint.push_back({box[3] - box[0], box[4] - box[1]});
       if (!(box[2] <= box[5]) || !std::isfinite(box[2]) || !std::isfinite(box[5]))
         throw std::invalid_argument("rest_pose: degenerate bounding box");
       z_off.push_back(-box[2] + 1e-3);
@@ -705,6 +710,16 @@ struct sb_engine {
       for (int k = 0; k < 4; ++k) pl.dev.rect[k] = sup.rect[k];
       const sb_relation& r = sp.relation;
       pl.hole = relation_to_dev(r, pl.dev);
+      if (sp.ratio_on_support != 0.0) {  // apply_ratio_on_support's checks (relationships.cpp:222-227)
+        if (sp.ratio_on_support < 0.0 || sp.ratio_on_support > 1.0)
+          throw std::invalid_argument("apply_ratio_on_support: ratio outside [0,1]");
+        if (!(footprint[sp.mesh][0] > 0.0) || !(footprint[sp.mesh][1] > 0.0))
+          throw std::invalid_argument("apply_ratio_on_support: footprint edges must be positive");
+        if (r.anchor >= 0)
+          throw std::invalid_argument("ratio_on_support with a relation (erosion of relation regions) is out of scope");
+      }
+      pl.ratio = sp.ratio_on_support;
+      pl.mesh = sp.mesh;
       if (r.anchor >= 0 && static_cast<uint32_t>(r.anchor) >= p)
         throw std::invalid_argument("relationship: anchor must be an earlier placement");
       pl.dev.anchor_object = r.anchor >= 0 ? first_place_obj + r.anchor : -1;
@@ -733,6 +748,11 @@ struct sb_engine {
       if (places[p].dev.anchor_object >= 0) continue;
       const double* rc = places[p].dev.rect;
       std::vector<sbh::V2> ring = {{rc[0], rc[1]}, {rc[2], rc[1]}, {rc[2], rc[3]}, {rc[0], rc[3]}};
+      if (places[p].ratio > 0.0) {  // apply_ratio_on_support (relationships.cpp:220-230)
+        const auto& fp = footprint[places[p].mesh];
+        const double r = places[p].ratio * std::min(fp[0], fp[1]) / 2.0;
+        if (r > 0.0) ring = sbh::erode_convex(ring, r);
+      }
       sbh::SamplerTable t = sbh::sampler_table({ring});
       places[p].canon_n = static_cast<int>(t.tris.size());
       if (!t.tris.empty()) {

@@ -230,6 +230,7 @@ class Placement:
     orientation: int = A.SB_ORIENT_UNIFORM_YAW
     face_target: int = -1
     relation: Relation = field(default_factory=Relation)
+    ratio_on_support: float = 0.0  # apply_ratio_on_support (relationships.cpp:220-230)
 
 
 @dataclass
@@ -277,7 +278,7 @@ class Scene:
                 p.mesh, p.support, p.orientation, p.face_target,
                 A.sb_relation(r.anchor, r.distance_type, r.direction, r.frame,
                               (C.c_double * 2)(*r.direction_vector), r.distance,
-                              r.angle_threshold))
+                              r.angle_threshold), p.ratio_on_support)
         sc = A.sb_scene(self.n_instances, self.attempts, 0,
                         len(self.meshes), meshes, len(self.fixed), fixed,
                         len(self.supports), sups, len(self.placements), pls)

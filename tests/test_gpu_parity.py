@@ -422,3 +422,35 @@ def test_fifo_speculative_solo_tail(gpu, ref, spec, monkeypatch):
     for scene in (scenes.tabletop_mixed(2048), scenes.kitchen(1024, attempts=128)):
         eng, got, want = run_generate_pair(gpu, ref, scene, seed=7)
         assert_same(gpu, got, want)
+
+
+def test_generate_ratio_on_support(gpu, ref):
+    """apply_ratio_on_support (relationships.cpp:220-230) on rect supports: the region is
+    eroded by ratio * min(footprint) / 2 (Boost buffer stand-in, oracle/shim); a support
+    too small for the erosion leaves the placement impossible."""
+    pkg = gpu
+    scene = scenes.tabletop_boxes(1024, n_objects=6)
+    scene.placements[1].ratio_on_support = 1.0
+    scene.placements[3].ratio_on_support = 0.5
+    eng, got, want = run_generate_pair(pkg, ref, scene, seed=5)
+    assert_same(pkg, got, want)
+    assert got.valid.sum() > 0
+    small = pkg.Support(pkg.translation(0.0, 0.0, 0.75), (-0.03, -0.03, 0.03, 0.03))
+    scene.supports.append(small)
+    scene.placements[5].support = len(scene.supports) - 1
+    scene.placements[5].ratio_on_support = 1.0  # boxes >= 0.08 wide: eroded away
+    eng, got, want = run_generate_pair(pkg, ref, scene, seed=5)
+    assert_same(pkg, got, want)
+    assert (got.accepted[5] == -1).all() and got.valid.sum() == 0
+
+
+def test_ratio_on_support_validation(gpu):
+    pkg = gpu
+    scene = scenes.tabletop_boxes(16, n_objects=3)
+    scene.placements[1].ratio_on_support = 1.5
+    with pytest.raises(ValueError):
+        pkg.Engine(scene)
+    scene.placements[1].ratio_on_support = 0.5
+    scene.placements[1].relation = pkg.Relation(anchor=0, distance_type=A.SB_DIST_LESS, distance=0.3)
+    with pytest.raises(ValueError):
+        pkg.Engine(scene)
