@@ -49,6 +49,7 @@ struct SbPlacementDev {
   double distance;
   double angle_threshold;  // <= 0: default
   uint64_t salt;           // placement index (Appendix C)
+  double erode_r;          // apply_ratio_on_support radius of relation regions, 0 = none
 };
 
 // Device view of a collision world (plain pointers; built by the host World class).

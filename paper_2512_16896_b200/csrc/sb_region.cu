@@ -395,6 +395,42 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
     if (area1 == 0.0) m = 0;
   }
   if (m < 3) return {sbp::kRegionEmpty, 0};
+  if (pl.erode_r > 0.0) {
+    // apply_ratio_on_support -> erode (relationships.cpp:220-230, polygon.cpp:101-113) as the
+    // oracle's Boost stand-in defines buffer(-r) on a convex ring (sbh::erode_convex): lane i
+    // rebuilds the offset lines of edges i-1 and i and intersects them.
+    const double r = pl.erode_r;
+    bool convex = true;
+    for (int i = g.gl; i < m; i += kG) {
+      const int h = i == 0 ? m - 1 : i - 1, q = i + 1 == m ? 0 : i + 1;
+      const double ox = X1[h], oy = Y1[h], px = X1[i], py = Y1[i], qx = X1[q], qy = Y1[q];
+      if ((px - ox) * (qy - oy) - (py - oy) * (qx - ox) < 0.0) convex = false;
+      const double dxh = px - ox, dyh = py - oy, dxi = qx - px, dyi = qy - py;
+      const double lh = sqrt(dxh * dxh + dyh * dyh), li = sqrt(dxi * dxi + dyi * dyi);
+      const double axh = ox + (-dyh / lh) * r, ayh = oy + (dxh / lh) * r;
+      const double axi = px + (-dyi / li) * r, ayi = py + (dxi / li) * r;
+      const double den = dxh * dyi - dyh * dxi;
+      const double t = ((axi - axh) * dyi - (ayi - ayh) * dxi) / den;
+      FA[i] = axh + t * dxh;
+      FC[i] = ayh + t * dyh;
+    }
+    if (!g.all(convex)) return {sbp::kRegionBadArg, 0};  // concave region: out of scope
+    g.sync();
+    bool alive = true;  // every offset edge keeps its direction, else eroded away
+    for (int i = g.gl; i < m; i += kG) {
+      const int q = i + 1 == m ? 0 : i + 1;
+      if (!((FA[q] - FA[i]) * (X1[q] - X1[i]) + (FC[q] - FC[i]) * (Y1[q] - Y1[i]) > 0.0))
+        alive = false;
+    }
+    if (!g.all(alive)) return {sbp::kRegionEmpty, 0};
+    g.sync();
+    for (int i = g.gl; i < m; i += kG) {
+      X1[i] = FA[i];
+      Y1[i] = FC[i];
+    }
+    g.sync();
+    area1 = warp_ring_area(X1, Y1, m, FA);
+  }
 
   SB_RP_MARK(rp4);
   SB_RP_ADD(4, rp3, rp4);

@@ -715,11 +715,13 @@ struct sb_engine {
           throw std::invalid_argument("apply_ratio_on_support: ratio outside [0,1]");
         if (!(footprint[sp.mesh][0] > 0.0) || !(footprint[sp.mesh][1] > 0.0))
           throw std::invalid_argument("apply_ratio_on_support: footprint edges must be positive");
-        if (r.anchor >= 0)
-          throw std::invalid_argument("ratio_on_support with a relation (erosion of relation regions) is out of scope");
+        if (pl.hole)
+          throw std::invalid_argument("ratio_on_support on an annulus with a hole (not convex) is out of scope");
       }
       pl.ratio = sp.ratio_on_support;
       pl.mesh = sp.mesh;
+      if (r.anchor >= 0 && sp.ratio_on_support > 0.0)  // relation regions erode on the device
+        pl.dev.erode_r = sp.ratio_on_support * std::min(footprint[sp.mesh][0], footprint[sp.mesh][1]) / 2.0;
       if (r.anchor >= 0 && static_cast<uint32_t>(r.anchor) >= p)
         throw std::invalid_argument("relationship: anchor must be an earlier placement");
       pl.dev.anchor_object = r.anchor >= 0 ? first_place_obj + r.anchor : -1;

@@ -444,13 +444,31 @@ def test_generate_ratio_on_support(gpu, ref):
     assert (got.accepted[5] == -1).all() and got.valid.sum() == 0
 
 
+def test_generate_ratio_on_support_relations(gpu, ref):
+    """Erosion of (convex) relation regions on the device: a disc clipped to the table and
+    90-degree sectors, eroded per instance by the region kernel."""
+    pkg = gpu
+    scene = scenes.tabletop_boxes(1024, n_objects=8, table=(1.6, 1.2))
+    scene.placements[2].relation = pkg.Relation(anchor=1, distance_type=A.SB_DIST_LESS,
+                                                distance=0.35)
+    scene.placements[4].relation = pkg.Relation(anchor=3, direction=A.SB_DIR_RIGHT)
+    scene.placements[6].relation = pkg.Relation(anchor=5, distance_type=A.SB_DIST_LESS,
+                                                direction=A.SB_DIR_FRONT, distance=0.4)
+    for k, ratio in ((2, 0.6), (4, 1.0), (6, 0.4), (7, 0.8)):
+        scene.placements[k].ratio_on_support = ratio
+    eng, got, want = run_generate_pair(pkg, ref, scene, seed=2)
+    assert_same(pkg, got, want)
+    assert got.stats["per_instance_placements"] >= 3
+
+
 def test_ratio_on_support_validation(gpu):
     pkg = gpu
     scene = scenes.tabletop_boxes(16, n_objects=3)
     scene.placements[1].ratio_on_support = 1.5
     with pytest.raises(ValueError):
         pkg.Engine(scene)
-    scene.placements[1].ratio_on_support = 0.5
-    scene.placements[1].relation = pkg.Relation(anchor=0, distance_type=A.SB_DIST_LESS, distance=0.3)
+    scene.placements[1].ratio_on_support = 0.5  # an annulus with a hole is not convex
+    scene.placements[1].relation = pkg.Relation(anchor=0, distance_type=A.SB_DIST_GREATER,
+                                                distance=0.3)
     with pytest.raises(ValueError):
         pkg.Engine(scene)
