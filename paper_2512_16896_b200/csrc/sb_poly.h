@@ -405,7 +405,7 @@ SB_HD bool bridge_hole(const Ring& outer, const Ring& hole, HoleRing& out) {
 
 struct HoleScratch {
   Ring o, h, tmp;
-  HoleRing mg;
+  HoleRing mg, mg2;
 };
 
 // region_for(i) of a full annulus with a hole (theta = pi, min_r > 0;
@@ -447,6 +447,56 @@ SB_HD int hole_annulus_table(double cx, double cy, double min_r, double max_r,
     for (int i = 0; i < sc.o.n; ++i) push(sc.mg, sc.o.x[i], sc.o.y[i]);
   }
   if (!ear_clip_into(sc.mg, sink, false)) return kRegionOverflow;
+  return kRegionOk;
+}
+
+// annulus_sector (polygon.cpp:136-176) for every shape but the holed annulus, into a big
+// ring (wide annular sectors need up to 2 * 73 arc points). max_r must be finite.
+template <class M>
+SB_HD int sector_ring(double cx, double cy, double vx, double vy, double theta, double min_r,
+                      double max_r, HoleRing& out) {
+  out.n = 0;
+  const bool full = theta >= kPi - 1e-12;
+  const double step = 5.0 * kPi / 180.0;
+  auto arc = [&](double radius, double a0, double a1) -> bool {
+    int na = (int)ceil(fabs(a1 - a0) / step);
+    if (na < 1) na = 1;
+    for (int i = 0; i <= na; ++i) {
+      const double a = a0 + (a1 - a0) * (double)i / (double)na;
+      double sa, ca;
+      M::sincos(a, &sa, &ca);
+      if (!push(out, cx + radius * ca, cy + radius * sa)) return false;
+    }
+    return true;
+  };
+  if (full) {
+    if (min_r > 0.0) return kRegionBadArg;  // holed annulus: hole_annulus_table
+    if (!arc(max_r, 0.0, 2.0 * kPi)) return kRegionOverflow;
+    out.n -= 1;  // closing vertex
+    return kRegionOk;
+  }
+  const double base = M::atan2(vy, vx);
+  if (!arc(max_r, base - theta, base + theta)) return kRegionOverflow;
+  if (min_r > 0.0) {
+    if (!arc(min_r, base + theta, base - theta)) return kRegionOverflow;
+  } else if (!push(out, cx, cy)) {
+    return kRegionOverflow;
+  }
+  return kRegionOk;
+}
+
+// region_for(i) of a shape whose ring outgrows the group path's kCap (sector_ring ->
+// the shim intersection -> triangulate -> the sampler table).
+template <class M>
+SB_HD int big_region_table(double cx, double cy, double vx, double vy, double theta,
+                           double min_r, double max_r, const double rect[4], HoleScratch& sc,
+                           TableSink& sink) {
+  int st = sector_ring<M>(cx, cy, vx, vy, theta, min_r, max_r, sc.mg);
+  if (st != kRegionOk) return st;
+  st = intersect_rect(sc.mg, sc.mg2, rect, false);
+  if (st == kRegionOverflow) return st;
+  if (st != kRegionOk) return kRegionEmpty;
+  if (!ear_clip_into(sc.mg, sink, true)) return kRegionOverflow;
   return kRegionOk;
 }
 

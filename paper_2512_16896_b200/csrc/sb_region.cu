@@ -566,21 +566,20 @@ struct DevMath {
   __device__ static double atan2(double y, double x) { return sbm::atan2_cr(y, x); }
 };
 
-// Full annulus with a hole (theta = pi, min_r > 0): one lane per instance runs the
-// restated pipeline (sbp::hole_annulus_table) in local memory -- outer + hole rings up to
-// 2 * kCap + 2 vertices do not fit the group's shared scratch, and bridged rings are
-// never convex, so the lane-parallel fan path would not apply anyway.
-__device__ __noinline__ RegionStats hole_region_lane(const SbPlacementDev& pl, double ax, double ay,
-                                                     SbRegionTri* tris, double* cum, int cap) {
+// Shapes whose ring outgrows the group path's kCap -- the full annulus with a hole (theta =
+// pi, min_r > 0) and wide annular sectors: one lane per instance runs the restated pipeline
+// (sbp::hole_annulus_table / sbp::big_region_table) on 2 * kCap + 2 vertex rings in local
+// memory; such rings are never convex, so the lane-parallel fan path would not apply.
+__device__ __noinline__ RegionStats big_region_lane(const SbPlacementDev& pl, double ax, double ay,
+                                                    double ayaw, SbRegionTri* tris, double* cum,
+                                                    int cap) {
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
-  double min_r = 0.0, max_r = inf;  // distance_band (relationships.cpp:101-122)
-  if (pl.distance_type == SB_DIST_GREATER) {
-    min_r = pl.distance;
-  } else if (pl.distance_type == SB_DIST_EQUAL) {
-    const double half = dmax(0.05 * pl.distance, 0.01);
-    min_r = dmax(0.0, pl.distance - half);
-    max_r = pl.distance + half;
-  }
+  double min_r, max_r;
+  distance_band(pl, min_r, max_r);
+  const double pi = 3.14159265358979323846;
+  const double theta = region_theta(pl);
+  double vx, vy;
+  resolve_direction(pl, ayaw, vx, vy);
   const double* rc = pl.rect;
   double bx0 = inf, by0 = inf, bx1 = -inf, by1 = -inf;
   const double vxs[5] = {rc[0], rc[2], rc[2], rc[0], ax};
@@ -593,11 +592,17 @@ __device__ __noinline__ RegionStats hole_region_lane(const SbPlacementDev& pl, d
   }
   const double ddx = bx1 - bx0, ddy = by1 - by0;
   const double diag = bx0 > bx1 ? 0.0 : sqrt(ddx * ddx + ddy * ddy);
+  if (!(theta > 0.0) || theta > pi + 1e-12) return {sbp::kRegionBadArg, 0};
   if (isinf(max_r)) max_r = fmax(diag, min_r + 1e-6);
   if (!(min_r < max_r)) return {sbp::kRegionBadArg, 0};
+  if (pl.erode_r > 0.0) return {sbp::kRegionBadArg, 0};  // concave shapes: no erosion
   sbp::HoleScratch sc;
   sbp::TableSink sink{tris, cum, 0, cap, 0.0};
-  const int st = sbp::hole_annulus_table<DevMath>(ax, ay, min_r, max_r, rc, sc, sink);
+  const bool full = theta >= pi - 1e-12;
+  const int st = full && min_r > 0.0
+                     ? sbp::hole_annulus_table<DevMath>(ax, ay, min_r, max_r, rc, sc, sink)
+                     : sbp::big_region_table<DevMath>(ax, ay, vx, vy, theta, min_r, max_r, rc,
+                                                      sc, sink);
   if (st != sbp::kRegionOk) return {st, 0};
   return {sbp::kRegionOk, sbp::finish_table(sink)};
 }
@@ -611,7 +616,7 @@ __device__ __forceinline__ RegionStats group_region(const SbPlacementDev& pl, do
   if constexpr (kHole) {
     const Grp g;
     RegionStats r{0, 0};
-    if (g.gl == 0) r = hole_region_lane(pl, ax, ay, tris, cum, cap);
+    if (g.gl == 0) r = big_region_lane(pl, ax, ay, ayaw, tris, cum, cap);
     r.status = g.bcast(r.status, 0);
     r.ntri = g.bcast(r.ntri, 0);
     return r;

@@ -129,8 +129,9 @@ int current_device_checked(int device) {
 }
 
 // RelationshipSpec::validate (relationships.cpp:59-76) for the single-anchor subset, then
-// the relation fields of the device record. Returns whether region_for() is a full annulus
-// with a hole (theta = pi, min_r > 0), i.e. needs the bridged-hole region path.
+// the relation fields of the device record. Returns whether region_for() needs the serial
+// big-ring region path: a full annulus with a hole (theta = pi, min_r > 0, bridged hole) or
+// an annular sector wide enough to outgrow the group path's ring (SB_REGION_MAX_VERTS).
 bool relation_to_dev(const sb_relation& r, SbPlacementDev& d) {
   if (r.distance < 0.0) throw std::invalid_argument("relationship: distance must be >= 0");
   if (r.angle_threshold > M_PI) throw std::invalid_argument("relationship: angle_threshold outside (0, pi]");
@@ -158,7 +159,13 @@ bool relation_to_dev(const sb_relation& r, SbPlacementDev& d) {
   double min_r = 0.0;  // distance_band (relationships.cpp:101-122)
   if (r.distance_type == SB_DIST_GREATER) min_r = r.distance;
   if (r.distance_type == SB_DIST_EQUAL) min_r = std::max(0.0, r.distance - std::max(0.05 * r.distance, 0.01));
-  return theta >= M_PI - 1e-12 && min_r > 0.0;
+  const bool full = theta >= M_PI - 1e-12;
+  if (full && min_r > 0.0) return true;  // annulus with a hole
+  // ring size of annulus_sector + up to 8 clip vertices (+1 arc point of rounding slack)
+  const double step = 5.0 * M_PI / 180.0;
+  const int arc = full ? 73 : static_cast<int>(std::ceil(2.0 * theta / step)) + 2;
+  const int ring = arc + (!full && min_r > 0.0 ? arc : 1) + 8;
+  return ring > SB_REGION_MAX_VERTS;  // the serial big-ring path
 }
 
 }  // namespace
@@ -716,7 +723,7 @@ struct sb_engine {
         if (!(footprint[sp.mesh][0] > 0.0) || !(footprint[sp.mesh][1] > 0.0))
           throw std::invalid_argument("apply_ratio_on_support: footprint edges must be positive");
         if (pl.hole)
-          throw std::invalid_argument("ratio_on_support on an annulus with a hole (not convex) is out of scope");
+          throw std::invalid_argument("ratio_on_support on an annulus with a hole or a wide annular sector (not convex) is out of scope");
       }
       pl.ratio = sp.ratio_on_support;
       pl.mesh = sp.mesh;

@@ -385,6 +385,22 @@ def _hole_scene(pkg, n):
     return base
 
 
+def test_generate_wide_annular_sectors(gpu, ref):
+    """Annular sectors wide enough (2 * 70+ arc points) to outgrow the group path's ring
+    take the serial big-ring region path (sbp::big_region_table)."""
+    pkg = gpu
+    base = scenes.tabletop_boxes(768, n_objects=6, table=(1.6, 1.2))
+    base.placements[2].relation = pkg.Relation(anchor=0, distance_type=A.SB_DIST_GREATER,
+                                               direction=A.SB_DIR_LEFT, distance=0.2,
+                                               angle_threshold=2.9)
+    base.placements[4].relation = pkg.Relation(anchor=1, distance_type=A.SB_DIST_EQUAL,
+                                               direction=A.SB_DIR_VECTOR,
+                                               direction_vector=(0.6, 0.8), distance=0.3,
+                                               angle_threshold=2.5, frame=A.SB_FRAME_LOCAL)
+    eng, got, want = run_generate_pair(pkg, ref, base, seed=4)
+    assert_same(pkg, got, want)
+
+
 @pytest.mark.parametrize("n,seed", [(1024, 3), (1, 2)])
 def test_generate_annulus_with_hole(gpu, ref, n, seed):
     eng, got, want = run_generate_pair(gpu, ref, _hole_scene(gpu, n), seed=seed)
