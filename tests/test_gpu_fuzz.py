@@ -93,3 +93,37 @@ def test_fuzz_engine_matches_reference(gpu, ref, seed):
             # that instance's region -- and, through anchors / face_to, later placements of
             # the same instance. Rare; never changed an accepted index in these scenes.
             assert ok.mean() >= 0.99, f"placement {p}: {np.sum(~ok)} poses outside 1e-5"
+
+
+@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("device_exchange", [False, True])
+def test_fuzz_sharded_equals_single(gpu, seed, device_exchange):
+    """Randomised scenes split over 2 shards (host or device-side count exchange) equal
+    the single-engine run bit for bit (scenes with >= 2 instances)."""
+    import threading
+
+    from tests.test_gpu_parity import ThreadAllgather, ThreadDevAllgather
+
+    scene = random_scene(gpu, 100 + seed)
+    if scene.n_instances < 2:
+        scene.n_instances = 256
+    whole = gpu.Engine(scene).generate(seed + 3)
+    world = 2
+    ag, agd = ThreadAllgather(world), ThreadDevAllgather(world)
+    bounds = [scene.n_instances * r // world for r in range(world + 1)]
+    engines = [gpu.Engine(scene, gpu.Shard(bounds[r], bounds[r + 1], r, world, ag.fn(r),
+                                           agd.fn(r) if device_exchange else None))
+               for r in range(world)]
+    results = [None] * world
+
+    def run(r):
+        results[r] = engines[r].generate(seed + 3)
+
+    ts = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert np.array_equal(np.concatenate([r.accepted for r in results], axis=1), whole.accepted)
+    assert np.array_equal(np.concatenate([r.valid for r in results]), whole.valid)
+    assert np.array_equal(np.concatenate([r.poses for r in results], axis=1), whole.poses)
