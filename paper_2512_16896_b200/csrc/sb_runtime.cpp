@@ -3,172 +3,10 @@
 // World  = CollisionWorld (collision.hpp:76-127) with all per-instance state in HBM.
 // Engine = the reference's absent rejection loop (contract frozen in
 //          DESIGN.md) driving the fused per-round kernel; one engine per GPU / shard.
-#include <cuda_runtime.h>
+#include "sb_rt.hpp"
+#include "sb_graph_rt.hpp"
+#include "sb_reach_rt.hpp"
 
-#include <algorithm>
-#include <array>
-#include <chrono>
-#include <cstdio>
-#include <cstdlib>
-#include <cmath>
-#include <cstring>
-#include <memory>
-#include <stdexcept>
-#include <string>
-#include <unordered_map>
-#include <vector>
-
-#include "../../include/scenebatch_b200.h"
-#include "sb_graph.h"
-#include "sb_host.hpp"
-#include "sb_reach.h"
-#include "sb_kernels.h"
-#include "sb_place.h"
-#include "sb_poly.h"
-#include "sb_region.h"
-#include "sb_layout.h"
-
-namespace {
-
-thread_local std::string g_error;
-
-void cuda_check(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    throw std::runtime_error(std::string("CUDA: ") + what + ": " + cudaGetErrorString(e));
-  }
-}
-
-struct CudaError : std::runtime_error {
-  using std::runtime_error::runtime_error;
-};
-
-template <class T>
-struct DevArray {
-  T* p = nullptr;
-  size_t count = 0;
-  DevArray() = default;
-  DevArray(const DevArray&) = delete;
-  DevArray& operator=(const DevArray&) = delete;
-  ~DevArray() { release(); }
-  void release() {
-    if (p) cudaFree(p);
-    p = nullptr;
-    count = 0;
-  }
-  void alloc(size_t n) {
-    release();
-    if (n == 0) return;
-    cuda_check(cudaMalloc(&p, n * sizeof(T)), "cudaMalloc");
-    count = n;
-  }
-  void ensure(size_t n) {
-    if (n > count) alloc(n);
-  }
-};
-
-template <class T>
-struct PinnedArray {
-  T* p = nullptr;
-  size_t count = 0;
-  ~PinnedArray() {
-    if (p) cudaFreeHost(p);
-  }
-  void ensure(size_t n) {
-    if (n <= count) return;
-    if (p) cudaFreeHost(p);
-    p = nullptr;
-    cuda_check(cudaMallocHost(&p, n * sizeof(T)), "cudaMallocHost");
-    count = n;
-  }
-};
-
-void require_homogeneous(const double* p) {
-  if (p[3] != 0.0 || p[7] != 0.0 || p[11] != 0.0 || p[15] != 1.0)
-    throw std::invalid_argument("pose bottom row must be exactly (0,0,0,1)");
-  for (int k = 0; k < 16; ++k)
-    if (!std::isfinite(p[k])) throw std::invalid_argument("pose must be finite");
-}
-
-// inverse_rigid (transform.hpp:63-69) on the host, same operation order as the device.
-void inverse_rigid34(const double* colmajor16, double out[12]) {
-  double R[3][3], t[3];
-  for (int i = 0; i < 3; ++i) {
-    for (int j = 0; j < 3; ++j) R[i][j] = colmajor16[4 * j + i];
-    t[i] = colmajor16[12 + i];
-  }
-  for (int i = 0; i < 3; ++i) {
-    for (int k = 0; k < 3; ++k) out[4 * i + k] = R[k][i];
-    double s = (-R[0][i]) * t[0];
-    s = s + (-R[1][i]) * t[1];
-    s = s + (-R[2][i]) * t[2];
-    out[4 * i + 3] = s;
-  }
-}
-
-void colmajor_to_34(const double* c, double out[12]) {
-  for (int i = 0; i < 3; ++i)
-    for (int j = 0; j < 4; ++j) out[4 * i + j] = c[4 * j + i];
-}
-
-int current_device_checked(int device) {
-  int count = 0;
-  cudaError_t e = cudaGetDeviceCount(&count);
-  if (e != cudaSuccess || count == 0) {
-    cudaGetLastError();
-    throw CudaError("no CUDA device available (this build has no CPU fallback)");
-  }
-  if (device < 0 || device >= count) throw std::out_of_range("device index out of range");
-  cudaDeviceProp prop;
-  cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
-  if (prop.major != 10)
-    throw CudaError("device " + std::to_string(device) + " is sm_" + std::to_string(prop.major) +
-                    std::to_string(prop.minor) + "; this build targets sm_100a only");
-  cuda_check(cudaSetDevice(device), "cudaSetDevice");
-  return device;
-}
-
-// RelationshipSpec::validate (relationships.cpp:59-76) for the single-anchor subset, then
-// the relation fields of the device record. Returns whether region_for() needs the serial
-// big-ring region path: a full annulus with a hole (theta = pi, min_r > 0, bridged hole) or
-// an annular sector wide enough to outgrow the group path's ring (SB_REGION_MAX_VERTS).
-bool relation_to_dev(const sb_relation& r, SbPlacementDev& d) {
-  if (r.distance < 0.0) throw std::invalid_argument("relationship: distance must be >= 0");
-  if (r.angle_threshold > M_PI) throw std::invalid_argument("relationship: angle_threshold outside (0, pi]");
-  const bool dist = r.distance_type == SB_DIST_GREATER || r.distance_type == SB_DIST_LESS ||
-                    r.distance_type == SB_DIST_EQUAL;
-  if (r.distance_type < SB_DIST_NONE || r.distance_type > SB_DIST_EQUAL)
-    throw std::invalid_argument("relationship: distance_type (middle is out of scope)");
-  if (dist && r.anchor < 0) throw std::invalid_argument("relationship: greater/less/equal require exactly 1 anchor");
-  if (r.direction != SB_DIR_NONE && r.anchor < 0) throw std::invalid_argument("relationship: direction requires exactly 1 anchor");
-  if (r.direction < SB_DIR_NONE || r.direction > SB_DIR_VECTOR) throw std::invalid_argument("relationship: direction");
-  if (r.direction == SB_DIR_VECTOR &&
-      std::sqrt(r.direction_vector[0] * r.direction_vector[0] + r.direction_vector[1] * r.direction_vector[1]) < 1e-12)
-    throw std::invalid_argument("relationship: zero-length direction vector");
-  if (r.distance_type == SB_DIST_LESS && !(0.0 < r.distance))
-    throw std::invalid_argument("annulus_sector: min_r >= max_r");
-  d.distance_type = r.distance_type;
-  d.direction = r.direction;
-  d.frame = r.frame;
-  d.direction_vector[0] = r.direction_vector[0];
-  d.direction_vector[1] = r.direction_vector[1];
-  d.distance = r.distance;
-  d.angle_threshold = r.angle_threshold;
-  if (r.anchor < 0) return false;
-  const double theta = r.angle_threshold > 0 ? r.angle_threshold : (r.direction == SB_DIR_NONE ? M_PI : M_PI / 4);
-  double min_r = 0.0;  // distance_band (relationships.cpp:101-122)
-  if (r.distance_type == SB_DIST_GREATER) min_r = r.distance;
-  if (r.distance_type == SB_DIST_EQUAL) min_r = std::max(0.0, r.distance - std::max(0.05 * r.distance, 0.01));
-  const bool full = theta >= M_PI - 1e-12;
-  if (full && min_r > 0.0) return true;  // annulus with a hole
-  // ring size of annulus_sector + up to 8 clip vertices (+1 arc point of rounding slack)
-  const double step = 5.0 * M_PI / 180.0;
-  const int arc = full ? 73 : static_cast<int>(std::ceil(2.0 * theta / step)) + 2;
-  const int ring = arc + (!full && min_r > 0.0 ? arc : 1) + 8;
-  return ring > SB_REGION_MAX_VERTS;  // the serial big-ring path
-}
-
-}  // namespace
 
 // annulus_sector's arc points (polygon.cpp:136-176) with the host libm, shared by every
 // instance when the direction is not in the anchor's local frame (sb_region.h).
@@ -1352,30 +1190,6 @@ struct sb_engine {
 
 // ===================================================================== C ABI
 namespace {
-template <class F>
-sb_status guard(F&& f) {
-  try {
-    f();
-    return SB_OK;
-  } catch (const std::invalid_argument& e) {
-    g_error = e.what();
-    return SB_ERR_INVALID_ARGUMENT;
-  } catch (const std::out_of_range& e) {
-    g_error = e.what();
-    return SB_ERR_OUT_OF_RANGE;
-  } catch (const std::logic_error& e) {
-    g_error = e.what();
-    return SB_ERR_LOGIC;
-  } catch (const CudaError& e) {
-    g_error = e.what();
-    return SB_ERR_CUDA;
-  } catch (const std::exception& e) {
-    g_error = e.what();
-    std::string w = e.what();
-    return w.rfind("CUDA", 0) == 0 ? SB_ERR_CUDA : SB_ERR_RUNTIME;
-  }
-}
-
 sb_status mesh_out(const sbh::Mesh& m, double* v, uint32_t* nv, uint32_t* t, uint32_t* nt) {
   if (nv) *nv = static_cast<uint32_t>(m.v.size());
   if (nt) *nt = static_cast<uint32_t>(m.t.size());
@@ -1397,6 +1211,7 @@ sbh::Mesh mesh_in(const double* v, uint32_t nv, const uint32_t* t, uint32_t nt) 
   for (uint32_t i = 0; i < nt; ++i) m.t[i] = {t[3 * i], t[3 * i + 1], t[3 * i + 2]};
   return m;
 }
+
 }  // namespace
 
 extern "C" {
@@ -1610,743 +1425,6 @@ sb_status sb_engine_last_timing(const sb_engine* e, double* total_ms, double* ch
 
 }  // extern "C"
 
-// ===================================================================== PositionSampler
-// The reference's PositionSampler (sampler.hpp:66-96, sampler.cpp:54-127) as a standalone
-// device-backed object. The SampleCache (sampler.hpp:18-36) is kept on the host as FIFO
-// ranges of draw indices of the cache stream -- a queued point is fully determined by its
-// draw index (polygon.cpp:390-391: 3 doubles = 6 PCG steps per point) and by the region
-// table, which only changes together with the fingerprint (and then clears the queue).
-// So refill / drain / bind_stream are index bookkeeping, and the points themselves are
-// drawn on the device by jump-ahead (k_sampler_fifo), one thread per active entry.
-namespace {
-
-// region_fingerprint (polygon.cpp:422-444) of hole-free parts.
-uint64_t rings_fingerprint(const double* xy, const uint32_t* off, uint32_t r0, uint32_t r1) {
-  uint64_t h = 0x9e3779b97f4a7c15ULL;
-  auto feed = [&h](double v) {
-    uint64_t bits;
-    std::memcpy(&bits, &v, sizeof bits);
-    h = sbh::mix64(h ^ bits);
-  };
-  for (uint32_t r = r0; r < r1; ++r) {
-    h = sbh::mix64(h ^ static_cast<uint64_t>(off[r + 1] - off[r]));
-    for (uint32_t k = off[r]; k < off[r + 1]; ++k) {
-      feed(xy[2 * k]);
-      feed(xy[2 * k + 1]);
-    }
-  }
-  return h;
-}
-
-sbh::SamplerTable rings_table(const double* xy, const uint32_t* off, uint32_t r0, uint32_t r1) {
-  std::vector<std::vector<sbh::V2>> parts;
-  for (uint32_t r = r0; r < r1; ++r) {
-    std::vector<sbh::V2> ring;
-    for (uint32_t k = off[r]; k < off[r + 1]; ++k) ring.push_back({xy[2 * k], xy[2 * k + 1]});
-    parts.push_back(std::move(ring));
-  }
-  return sbh::sampler_table(parts);
-}
-
-uint64_t cache_state0(uint64_t run_seed, uint64_t salt) {  // Pcg32(make_stream(seed, {salt, "cach"}))
-  const uint64_t h = sbh::mix64(sbh::mix64(sbh::mix64(run_seed) ^ salt) ^ 0x63616368ULL);
-  const uint64_t mult = 6364136223846793005ULL, inc = (0xda3e39cb94b95bdbULL << 1u) | 1u;
-  uint64_t st = inc;
-  st += h;
-  return st * mult + inc;
-}
-
-}  // namespace
-
-struct sb_sampler {
-  uint64_t salt;
-  int device;
-  cudaStream_t stream = nullptr;
-  bool prepared = false, per_instance = false, region_empty = true;
-  uint64_t n = 0, run_seed = 0, region_fp = 0;
-  int region_nt = 0;
-  // SampleCache (sampler.hpp:18-36): queue of [first, end) draw-index ranges
-  uint64_t cache_fp = 0, cache_stream = 0, refill_count = 0, queue_size = 0, rng_pos = 0;
-  std::vector<std::pair<uint64_t, uint64_t>> queue;  // front at queue_head
-  size_t queue_head = 0;
-  DevArray<SbRegionTri> d_tris;  // canonical table, or all per-instance tables
-  DevArray<double> d_cum;
-  DevArray<uint32_t> d_inst_tab;  // per instance: (first table row, rows)
-  bool stride_tables = false;     // relation tables: [n][table_cap] rows, d_inst_n each
-  int table_cap = 0;
-  DevArray<int32_t> d_inst_n;
-  DevArray<double> d_states;
-  DevArray<int32_t> d_rflags;
-  DevArray<sbk::SbArcTable> d_arcs;
-  DevArray<double> d_sup, d_pos;
-  DevArray<uint32_t> d_active;
-  DevArray<uint8_t> d_pl;
-  DevArray<uint64_t> d_seg;
-  PinnedArray<double> h_sup;
-  PinnedArray<uint64_t> h_seg;
-
-  sb_sampler(uint64_t salt_, int dev) : salt(salt_), device(current_device_checked(dev)) {
-    cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
-  }
-  ~sb_sampler() {
-    if (ev_seg) cudaEventDestroy(ev_seg);
-    if (stream) {
-      cudaSetDevice(device);
-      cudaStreamSynchronize(stream);
-      cudaStreamDestroy(stream);
-    }
-  }
-
-  void clear_queue() {
-    queue.clear();
-    queue_head = 0;
-    queue_size = 0;
-  }
-
-  // PositionSampler::prepare (sampler.cpp:54-67) + the region tables PolygonSampler builds.
-  void prepare(const double* xy, const uint32_t* off, uint32_t n_rings, const uint32_t* inst_rings,
-               uint64_t batch, uint64_t seed) {
-    cuda_check(cudaSetDevice(device), "cudaSetDevice");
-    if (n_rings && (!xy || !off)) throw std::invalid_argument("ring arrays are NULL");
-    for (uint32_t r = 0; r < n_rings; ++r)
-      if (off[r + 1] < off[r]) throw std::invalid_argument("ring_offsets must be non-decreasing");
-    if (batch > 0xffffffffull) throw std::invalid_argument("batch_size exceeds 2^32");
-    std::vector<SbRegionTri> tris;
-    std::vector<double> cum;
-    if (inst_rings) {
-      std::vector<uint32_t> tab(2 * batch);
-      std::unordered_map<uint64_t, uint64_t> seen;  // ring range -> first instance using it
-      for (uint64_t i = 0; i < batch; ++i) {
-        const uint32_t r0 = inst_rings[i], r1 = inst_rings[i + 1];
-        if (r1 < r0 || r1 > n_rings) throw std::invalid_argument("instance_rings out of range");
-        auto ins = seen.emplace((static_cast<uint64_t>(r0) << 32) | r1, i);
-        if (!ins.second) {  // same rings as an earlier instance: share its table
-          tab[2 * i] = tab[2 * ins.first->second];
-          tab[2 * i + 1] = tab[2 * ins.first->second + 1];
-          continue;
-        }
-        auto t = rings_table(xy, off, r0, r1);
-        tab[2 * i] = static_cast<uint32_t>(tris.size());
-        tab[2 * i + 1] = static_cast<uint32_t>(t.tris.size());
-        tris.insert(tris.end(), t.tris.begin(), t.tris.end());
-        cum.insert(cum.end(), t.cum.begin(), t.cum.end());
-      }
-      d_inst_tab.ensure(std::max<uint64_t>(1, 2 * batch));
-      if (batch)
-        cuda_check(cudaMemcpy(d_inst_tab.p, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice),
-                   "H2D instance tables");
-    } else {
-      region_empty = n_rings == 0;
-      region_fp = rings_fingerprint(xy, off, 0, n_rings);
-      auto t = rings_table(xy, off, 0, n_rings);
-      tris = std::move(t.tris);
-      cum = std::move(t.cum);
-      region_nt = static_cast<int>(tris.size());
-    }
-    d_tris.ensure(std::max<size_t>(1, tris.size()));
-    d_cum.ensure(std::max<size_t>(1, cum.size()));
-    if (!tris.empty()) {
-      cuda_check(cudaMemcpy(d_tris.p, tris.data(), tris.size() * sizeof(SbRegionTri), cudaMemcpyHostToDevice), "H2D table");
-      cuda_check(cudaMemcpy(d_cum.p, cum.data(), cum.size() * sizeof(double), cudaMemcpyHostToDevice), "H2D table");
-    }
-    per_instance = inst_rings != nullptr;
-    stride_tables = false;
-    n = batch;
-    run_seed = seed;
-    const uint64_t parts[3] = {seed, salt, 0x63616368ULL};  // bind_stream(stream_key(...))
-    uint64_t key = 0x853c49e6748fea9bULL;
-    for (uint64_t p : parts) key = sbh::mix64(key ^ p);
-    if (cache_stream != key) {
-      clear_queue();
-      cache_stream = key;
-    }
-    rng_pos = 0;  // cache_rng_ = make_stream(run_seed, {salt, "cach"})
-    prepared = true;
-  }
-
-  // build_constraint_region (relationships.cpp:161-218) on the device for a batch of
-  // anchor states (x, y, yaw per instance, support frame), then prepare(). The region
-  // kernel decides per_instance exactly as the reference (any anchor moving by > 1e-12);
-  // a canonical region's cache fingerprint is a hash of its sampler table (the polygon
-  // itself never leaves the device).
-  void prepare_relation(const sb_relation& rel, const double rect[4], const double* states,
-                        uint64_t batch, uint64_t seed) {
-    cuda_check(cudaSetDevice(device), "cudaSetDevice");
-    if (batch == 0) throw std::invalid_argument("anchor state batch is empty");
-    if (batch > 0xffffffffull) throw std::invalid_argument("batch_size exceeds 2^32");
-    SbPlacementDev pd;
-    std::memset(&pd, 0, sizeof pd);
-    const bool hole = relation_to_dev(rel, pd);
-    for (int k = 0; k < 4; ++k) pd.rect[k] = rect[k];
-    if (rel.anchor < 0) {  // no anchors: region = support (relationships.cpp:168-171)
-      const double xy[8] = {rect[0], rect[1], rect[2], rect[1], rect[2], rect[3], rect[0], rect[3]};
-      const uint32_t off[2] = {0, 4};
-      prepare(xy, off, 1, nullptr, batch, seed);
-      return;
-    }
-    if (!states) throw std::invalid_argument("anchor states are NULL");
-    int sms = 0;
-    cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "attr");
-    table_cap = hole ? sbp::kHoleCap : SB_REGION_MAX_VERTS;
-    d_tris.ensure(batch * table_cap);
-    d_cum.ensure(batch * table_cap);
-    d_inst_n.ensure(batch);
-    d_states.ensure(3 * batch);
-    d_rflags.ensure(2);
-    cuda_check(cudaMemcpyAsync(d_states.p, states, 3 * batch * sizeof(double), cudaMemcpyHostToDevice, stream), "H2D states");
-    cuda_check(cudaMemsetAsync(d_rflags.p, 0, 2 * sizeof(int32_t), stream), "memset");
-    sbk::RelationRegionParams rp;
-    std::memset(&rp, 0, sizeof rp);
-    rp.w.n = batch;
-    rp.pl = pd;
-    rp.anchor_object = -1;
-    rp.cap = table_cap;
-    rp.hole = hole ? 1 : 0;
-    sbk::SbArcTable arc_tab;
-    if (!hole && sbk::arc_table_host(pd, arc_tab)) {
-      d_arcs.ensure(1);
-      cuda_check(cudaMemcpyAsync(d_arcs.p, &arc_tab, sizeof arc_tab, cudaMemcpyHostToDevice, stream), "H2D arcs");
-      rp.arcs = d_arcs.p;
-    }
-    rp.states = d_states.p;
-    rp.tris = d_tris.p;
-    rp.cum = d_cum.p;
-    rp.ntri = d_inst_n.p;
-    rp.flags = d_rflags.p;
-    sbk::relation_regions(rp, sms, reinterpret_cast<sb_stream_t>(stream));
-    int32_t flags[2], n0 = 0;
-    cuda_check(cudaMemcpyAsync(flags, d_rflags.p, sizeof flags, cudaMemcpyDeviceToHost, stream), "D2H flags");
-    cuda_check(cudaMemcpyAsync(&n0, d_inst_n.p, 4, cudaMemcpyDeviceToHost, stream), "D2H n");
-    cuda_check(cudaStreamSynchronize(stream), "sync");
-    if (flags[1] != 0)
-      throw std::runtime_error("constraint region build failed (status " + std::to_string(flags[1]) + ")");
-    per_instance = flags[0] != 0;
-    stride_tables = true;
-    n = batch;
-    region_nt = per_instance ? 0 : n0;
-    region_empty = !per_instance && n0 == 0;  // an empty (or zero-area) region_for(0)
-    if (!per_instance && n0 > 0) {  // fingerprint of the canonical table
-      std::vector<SbRegionTri> t(n0);
-      std::vector<double> c(n0);
-      cuda_check(cudaMemcpy(t.data(), d_tris.p, n0 * sizeof(SbRegionTri), cudaMemcpyDeviceToHost), "D2H table");
-      cuda_check(cudaMemcpy(c.data(), d_cum.p, n0 * sizeof(double), cudaMemcpyDeviceToHost), "D2H table");
-      uint64_t h = 0x9e3779b97f4a7c15ULL ^ 0x7461626cULL;  // "tabl": never a ring fingerprint
-      auto feed = [&h](const void* p, size_t bytes) {
-        const uint64_t* w = static_cast<const uint64_t*>(p);
-        for (size_t k = 0; k < bytes / 8; ++k) h = sbh::mix64(h ^ w[k]);
-      };
-      feed(t.data(), t.size() * sizeof(SbRegionTri));
-      feed(c.data(), c.size() * sizeof(double));
-      region_fp = h;
-    }
-    run_seed = seed;
-    const uint64_t parts[3] = {seed, salt, 0x63616368ULL};
-    uint64_t key = 0x853c49e6748fea9bULL;
-    for (uint64_t q : parts) key = sbh::mix64(key ^ q);
-    if (cache_stream != key) {
-      clear_queue();
-      cache_stream = key;
-    }
-    rng_pos = 0;
-    prepared = true;
-  }
-
-  // refill_cache (sampler.cpp:14-28) on draw indices
-  void refill(uint64_t k) {
-    if (region_fp != cache_fp) {
-      clear_queue();
-      cache_fp = region_fp;
-    }
-    uint64_t target = static_cast<uint64_t>(4.0 * static_cast<double>(k));
-    if (target < k) target = k;
-    if (queue_size >= target) return;
-    const uint64_t need = target - queue_size;
-    queue.push_back({rng_pos, rng_pos + need});
-    rng_pos += need;
-    queue_size += need;
-    ++refill_count;
-  }
-
-  // drain_cache (sampler.cpp:30-43): pops k points as segments (first entry, first draw).
-  int drain(uint64_t k) {
-    if (region_fp != cache_fp || queue_size < k) refill(std::max<uint64_t>(k, 1));
-    std::vector<uint64_t> first, draw;
-    uint64_t j = 0;
-    while (j < k) {
-      auto& r = queue[queue_head];
-      const uint64_t take = std::min(k - j, r.second - r.first);
-      first.push_back(j);
-      draw.push_back(r.first);
-      r.first += take;
-      j += take;
-      if (r.first == r.second) ++queue_head;
-    }
-    queue_size -= k;
-    if (queue_head > 64 && queue_head * 2 > queue.size()) {
-      queue.erase(queue.begin(), queue.begin() + queue_head);
-      queue_head = 0;
-    }
-    const int nseg = static_cast<int>(first.size());
-    h_seg.ensure(std::max(2, 2 * nseg));
-    std::copy(first.begin(), first.end(), h_seg.p);
-    std::copy(draw.begin(), draw.end(), h_seg.p + nseg);
-    return nseg;
-  }
-
-  void sample(const double* support, const uint32_t* active, uint64_t m, uint64_t attempt,
-              double* pos, uint8_t* placeable) {
-    if (!prepared) throw std::logic_error("PositionSampler: prepare() not called");
-    if (m && (!active || !pos || !placeable || !support))
-      throw std::invalid_argument("sample: NULL array");
-    cuda_check(cudaSetDevice(device), "cudaSetDevice");
-    if (!per_instance && region_empty) {  // sampler.cpp:81-84
-      std::memset(pos, 0, 3 * m * sizeof(double));
-      std::memset(placeable, 0, m);
-      return;
-    }
-    if (!per_instance && region_nt == 0)
-      throw std::invalid_argument("sample: canonical region has zero area");
-    if (m == 0) {
-      if (!per_instance) drain(0);
-      return;
-    }
-    h_sup.ensure(12 * m);
-    for (uint64_t j = 0; j < m; ++j) {
-      if (active[j] >= n) throw std::out_of_range("sample: active index >= batch_size");
-      colmajor_to_34(support + 16 * static_cast<uint64_t>(active[j]), h_sup.p + 12 * j);
-    }
-    d_sup.ensure(12 * m);
-    d_pos.ensure(3 * m);
-    cuda_check(cudaMemcpyAsync(d_sup.p, h_sup.p, 12 * m * sizeof(double), cudaMemcpyHostToDevice, stream), "H2D support");
-    if (!per_instance) {
-      const int nseg = drain(m);
-      d_seg.ensure(2 * nseg);
-      cuda_check(cudaMemcpyAsync(d_seg.p, h_seg.p, 2 * nseg * sizeof(uint64_t), cudaMemcpyHostToDevice, stream), "H2D segments");
-      sbk::sampler_fifo(d_sup.p, nullptr, nullptr, m, d_seg.p, d_seg.p + nseg, nseg,
-                        cache_state0(run_seed, salt),
-                        d_tris.p, d_cum.p, region_nt, d_pos.p, stream);
-      cuda_check(cudaMemcpyAsync(pos, d_pos.p, 3 * m * sizeof(double), cudaMemcpyDeviceToHost, stream), "D2H positions");
-      cuda_check(cudaStreamSynchronize(stream), "sync");
-      std::memset(placeable, 1, m);
-      return;
-    }
-    d_active.ensure(m);
-    d_pl.ensure(m);
-    cuda_check(cudaMemcpyAsync(d_active.p, active, m * 4, cudaMemcpyHostToDevice, stream), "H2D active");
-    sbk::sampler_fallback(d_sup.p, nullptr, d_active.p, m, run_seed, salt, attempt,
-                          stride_tables ? nullptr : d_inst_tab.p, d_inst_n.p, table_cap, d_tris.p,
-                          d_cum.p, d_pos.p, d_pl.p, stream);
-    cuda_check(cudaMemcpyAsync(pos, d_pos.p, 3 * m * sizeof(double), cudaMemcpyDeviceToHost, stream), "D2H positions");
-    cuda_check(cudaMemcpyAsync(placeable, d_pl.p, m, cudaMemcpyDeviceToHost, stream), "D2H placeable");
-    cuda_check(cudaStreamSynchronize(stream), "sync");
-  }
-
-  // Device-resident variant: supports (N column-major Mat4), active, positions and
-  // placeable are device pointers; everything is enqueued on `st` (no host round trip but
-  // the SampleCache bookkeeping, which stays on the host).
-  cudaEvent_t ev_seg = nullptr;
-  void sample_device(const double* d_sup16, const uint32_t* d_act, uint64_t m, uint64_t attempt,
-                     double* d_out, uint8_t* d_placeable, cudaStream_t st) {
-    if (!prepared) throw std::logic_error("PositionSampler: prepare() not called");
-    cuda_check(cudaSetDevice(device), "cudaSetDevice");
-    if (m && (!d_sup16 || !d_act || !d_out || !d_placeable))
-      throw std::invalid_argument("sample_device: NULL array");
-    if (!per_instance && region_empty) {
-      if (m) {
-        cuda_check(cudaMemsetAsync(d_out, 0, 3 * m * sizeof(double), st), "memset");
-        cuda_check(cudaMemsetAsync(d_placeable, 0, m, st), "memset");
-      }
-      return;
-    }
-    if (!per_instance && region_nt == 0)
-      throw std::invalid_argument("sample: canonical region has zero area");
-    if (!per_instance) {
-      if (!ev_seg) cuda_check(cudaEventCreateWithFlags(&ev_seg, cudaEventDisableTiming), "event");
-      cuda_check(cudaEventSynchronize(ev_seg), "sync segments");  // h_seg reusable
-      const int nseg = drain(m);
-      if (m == 0) return;
-      d_seg.ensure(2 * nseg);
-      cuda_check(cudaMemcpyAsync(d_seg.p, h_seg.p, 2 * nseg * sizeof(uint64_t), cudaMemcpyHostToDevice, st), "H2D segments");
-      cuda_check(cudaEventRecord(ev_seg, st), "event");
-      sbk::sampler_fifo(nullptr, d_sup16, d_act, m, d_seg.p, d_seg.p + nseg, nseg,
-                        cache_state0(run_seed, salt), d_tris.p, d_cum.p, region_nt, d_out,
-                        reinterpret_cast<sb_stream_t>(st));
-      cuda_check(cudaMemsetAsync(d_placeable, 1, m, st), "memset");
-      return;
-    }
-    if (m == 0) return;
-    sbk::sampler_fallback(nullptr, d_sup16, d_act, m, run_seed, salt, attempt,
-                          stride_tables ? nullptr : d_inst_tab.p, d_inst_n.p, table_cap, d_tris.p,
-                          d_cum.p, d_out, d_placeable, reinterpret_cast<sb_stream_t>(st));
-  }
-};
-
-namespace {
-struct OrientScratch {  // per host thread: reused device buffers of sb_sample_orientations
-  int device = -1;
-  cudaStream_t stream = nullptr;
-  DevArray<uint32_t> active;
-  DevArray<double> pos, face, yaws;
-  void bind(int dev) {
-    if (device == dev) return;
-    active.release();
-    pos.release();
-    face.release();
-    yaws.release();
-    if (stream) cudaStreamDestroy(stream);
-    stream = nullptr;
-    device = dev;
-    cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
-  }
-};
-thread_local OrientScratch g_orient;
-}  // namespace
-
-extern "C" {
-
-sb_status sb_sampler_create(uint64_t salt, int device, sb_sampler** out) {
-  return guard([&] {
-    if (!out) throw std::invalid_argument("out is NULL");
-    *out = new sb_sampler(salt, device);
-  });
-}
-void sb_sampler_destroy(sb_sampler* s) { delete s; }
-sb_status sb_sampler_prepare(sb_sampler* s, const double* xy, const uint32_t* off, uint32_t n_rings,
-                             const uint32_t* inst_rings, uint64_t n, uint64_t run_seed) {
-  return guard([&] { s->prepare(xy, off, n_rings, inst_rings, n, run_seed); });
-}
-sb_status sb_sampler_sample(sb_sampler* s, const double* support, const uint32_t* active, uint64_t m,
-                            uint64_t attempt, double* pos, uint8_t* placeable) {
-  return guard([&] { s->sample(support, active, m, attempt, pos, placeable); });
-}
-sb_status sb_sampler_prepare_relation(sb_sampler* s, const sb_relation* rel,
-                                      const double support_rect[4], const double* anchor_states,
-                                      uint64_t n, uint64_t run_seed) {
-  return guard([&] {
-    if (!rel || !support_rect) throw std::invalid_argument("relation / support rect is NULL");
-    s->prepare_relation(*rel, support_rect, anchor_states, n, run_seed);
-  });
-}
-sb_status sb_sampler_sample_device(sb_sampler* s, const double* d_support16, const uint32_t* d_active,
-                                   uint64_t m, uint64_t attempt, double* d_positions,
-                                   uint8_t* d_placeable, void* cuda_stream) {
-  return guard([&] {
-    s->sample_device(d_support16, d_active, m, attempt, d_positions, d_placeable,
-                     static_cast<cudaStream_t>(cuda_stream));
-  });
-}
-sb_status sb_sampler_cache_info(const sb_sampler* s, uint64_t* queue_size, uint64_t* refills) {
-  return guard([&] {
-    if (queue_size) *queue_size = s->queue_size;
-    if (refills) *refills = s->refill_count;
-  });
-}
-
-// sample_orientations (sampler.cpp:129-156)
-sb_status sb_sample_orientations(int kind, const uint32_t* active, uint64_t m, const double* pos,
-                                 const double* face_xy, uint64_t n_targets, uint64_t run_seed,
-                                 uint64_t salt, uint64_t attempt, double* yaws, int device) {
-  return guard([&] {
-    if (kind < SB_ORIENT_FIXED || kind > SB_ORIENT_FACE_TO)
-      throw std::invalid_argument("sample_orientations: unknown orientation kind");
-    if (kind == SB_ORIENT_FACE_TO && !face_xy)
-      throw std::invalid_argument("sample_orientations: face_to target positions missing");
-    if (m && (!active || !yaws || (kind == SB_ORIENT_FACE_TO && !pos)))
-      throw std::invalid_argument("sample_orientations: NULL array");
-    if (kind == SB_ORIENT_FACE_TO)
-      for (uint64_t j = 0; j < m; ++j)
-        if (active[j] >= n_targets)
-          throw std::out_of_range("sample_orientations: active index >= n_targets");
-    current_device_checked(device);
-    if (m == 0) return;
-    OrientScratch& o = g_orient;
-    o.bind(device);
-    o.active.ensure(m);
-    o.yaws.ensure(m);
-    cuda_check(cudaMemcpyAsync(o.active.p, active, m * 4, cudaMemcpyHostToDevice, o.stream), "H2D active");
-    if (kind == SB_ORIENT_FACE_TO) {
-      o.pos.ensure(3 * m);
-      o.face.ensure(std::max<uint64_t>(1, 2 * n_targets));
-      cuda_check(cudaMemcpyAsync(o.pos.p, pos, 3 * m * sizeof(double), cudaMemcpyHostToDevice, o.stream), "H2D positions");
-      cuda_check(cudaMemcpyAsync(o.face.p, face_xy, 2 * n_targets * sizeof(double), cudaMemcpyHostToDevice, o.stream), "H2D targets");
-    }
-    sbk::orientations(kind, o.active.p, m, o.pos.p, o.face.p, run_seed, salt, attempt, o.yaws.p, o.stream);
-    cuda_check(cudaMemcpyAsync(yaws, o.yaws.p, m * sizeof(double), cudaMemcpyDeviceToHost, o.stream), "D2H yaws");
-    cuda_check(cudaStreamSynchronize(o.stream), "sync");
-  });
-}
-
-}  // extern "C"
-
-// ===================================================================== BatchedSceneGraph
-// scene_graph.hpp:33-94. Names, parents and joint specs are host metadata; every per-
-// instance batch (edges, bases, joint values, validity) lives in HBM (sb_graph.cu).
-namespace {
-bool homogeneous16(const double* m) {  // is_homogeneous (transform.hpp:28-30)
-  return m[3] == 0.0 && m[7] == 0.0 && m[11] == 0.0 && m[15] == 1.0;
-}
-}  // namespace
-
-struct sb_graph {
-  uint64_t n;
-  int device;
-  cudaStream_t stream = nullptr;
-  struct Node {
-    std::string name;
-    uint32_t parent = 0;
-    int64_t geometry = -1;
-    bool joint = false;
-    sb_joint spec{};
-    std::unique_ptr<DevArray<double>> edge, base, values;
-  };
-  std::vector<Node> nodes;
-  std::unordered_map<std::string, uint32_t> by_name;
-  DevArray<uint8_t> d_valid;
-  mutable DevArray<double> d_tmp16;
-  mutable DevArray<const double*> d_chain;
-  mutable DevArray<unsigned long long> d_count;
-
-  sb_graph(uint64_t batch, int dev) : n(batch), device(current_device_checked(dev)) {
-    if (batch == 0) throw std::invalid_argument("batch_size must be >= 1");
-    cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
-    d_valid.alloc(n);
-    cuda_check(cudaMemsetAsync(d_valid.p, 1, n, stream), "memset");
-    Node world;
-    world.name = "world";
-    world.edge = std::make_unique<DevArray<double>>();
-    identity_batch(*world.edge);
-    by_name.emplace("world", 0);
-    nodes.push_back(std::move(world));
-    sync();
-  }
-  ~sb_graph() {
-    if (ev_chain) cudaEventDestroy(ev_chain);
-    if (stream) {
-      cudaSetDevice(device);
-      cudaStreamSynchronize(stream);
-      cudaStreamDestroy(stream);
-    }
-  }
-  sb_stream_t s() const { return reinterpret_cast<sb_stream_t>(stream); }
-  void activate() const { cuda_check(cudaSetDevice(device), "cudaSetDevice"); }
-  void sync() const { cuda_check(cudaStreamSynchronize(stream), "sync"); }
-
-  void identity_batch(DevArray<double>& a) {
-    a.alloc(12 * n);
-    std::vector<double> one(16, 0.0);
-    one[0] = one[5] = one[10] = one[15] = 1.0;
-    d_tmp16.ensure(16 * n);
-    std::vector<double> host(16 * n);
-    for (uint64_t i = 0; i < n; ++i) std::memcpy(&host[16 * i], one.data(), sizeof(double) * 16);
-    cuda_check(cudaMemcpyAsync(d_tmp16.p, host.data(), 16 * n * sizeof(double), cudaMemcpyHostToDevice, stream), "H2D");
-    sbk::graph_colmajor_to_34(d_tmp16.p, n, a.p, s());
-    sync();
-  }
-  const Node& at(uint32_t id) const {
-    if (id >= nodes.size()) throw std::out_of_range("unknown node");
-    return nodes[id];
-  }
-  Node& at(uint32_t id) {
-    if (id >= nodes.size()) throw std::out_of_range("unknown node");
-    return nodes[id];
-  }
-  static sbk::GraphJoint gj(const sb_joint& j) {
-    sbk::GraphJoint g;
-    g.kind = j.kind;
-    for (int k = 0; k < 3; ++k) g.axis[k] = j.axis[k];
-    return g;
-  }
-  // edge = base * motion(values) over all instances (or motion alone when base == NULL)
-  void compose(Node& nd, bool with_base) {
-    sbk::graph_joint_compose(with_base ? nd.base->p : nullptr, nd.values->p, 0, n, gj(nd.spec),
-                             nd.edge->p, s());
-  }
-
-  uint32_t add_node(uint32_t parent, const char* name_c, int64_t geometry, const sb_joint* joint) {
-    activate();
-    at(parent);
-    if (!name_c) throw std::invalid_argument("node name is NULL");
-    const std::string name(name_c);
-    if (by_name.count(name)) throw std::invalid_argument("duplicate node name: " + name);
-    Node nd;
-    nd.name = name;
-    nd.parent = parent;
-    nd.geometry = geometry;
-    nd.edge = std::make_unique<DevArray<double>>();
-    if (joint) {  // JointSpec ctor (scene_graph.cpp:9-17)
-      sb_joint j = *joint;
-      if (j.kind != 0 && j.kind != 1) throw std::invalid_argument("JointSpec: unknown kind");
-      if (j.lo > j.hi) throw std::invalid_argument("JointSpec: lo > hi");
-      const double nrm = std::sqrt((j.axis[0] * j.axis[0] + j.axis[1] * j.axis[1]) + j.axis[2] * j.axis[2]);
-      if (std::abs(nrm - 1.0) > 1e-9) {
-        if (nrm < 1e-12) throw std::invalid_argument("JointSpec: zero axis");
-        for (int k = 0; k < 3; ++k) j.axis[k] = j.axis[k] / nrm;
-      }
-      nd.joint = true;
-      nd.spec = j;
-      nd.base = std::make_unique<DevArray<double>>();
-      identity_batch(*nd.base);
-      nd.values = std::make_unique<DevArray<double>>();
-      nd.values->alloc(n);
-      std::vector<double> lo(n, j.lo);
-      cuda_check(cudaMemcpyAsync(nd.values->p, lo.data(), n * sizeof(double), cudaMemcpyHostToDevice, stream), "H2D");
-      nd.edge->alloc(12 * n);
-      compose(nd, false);  // every edge = motion(lo)
-      sync();
-    } else {
-      identity_batch(*nd.edge);
-    }
-    const uint32_t id = static_cast<uint32_t>(nodes.size());
-    by_name.emplace(name, id);
-    nodes.push_back(std::move(nd));
-    return id;
-  }
-
-  void set_edge_batch(uint32_t parent, uint32_t child, const double* t16) {
-    activate();
-    Node& nd = at(child);
-    if (nd.parent != parent || child == 0)
-      throw std::invalid_argument("no such edge: " + at(parent).name + " -> " + nd.name);
-    if (!t16) throw std::invalid_argument("transform batch is NULL");
-    for (uint64_t i = 0; i < n; ++i)
-      if (!homogeneous16(t16 + 16 * i)) throw std::invalid_argument("non-homogeneous matrix in batch");
-    d_tmp16.ensure(16 * n);
-    cuda_check(cudaMemcpyAsync(d_tmp16.p, t16, 16 * n * sizeof(double), cudaMemcpyHostToDevice, stream), "H2D");
-    sbk::graph_colmajor_to_34(d_tmp16.p, n, nd.joint ? nd.base->p : nd.edge->p, s());
-    if (nd.joint) compose(nd, true);
-    sync();
-  }
-
-  void set_edge(uint32_t child, uint64_t i, const double* m16) {
-    activate();
-    Node& nd = at(child);
-    if (child == 0) throw std::invalid_argument("cannot set edge on root");
-    if (i >= n) throw std::out_of_range("instance out of range");
-    if (!m16 || !homogeneous16(m16)) throw std::invalid_argument("non-homogeneous matrix");
-    double r[12];
-    colmajor_to_34(m16, r);
-    double* dst = (nd.joint ? nd.base->p : nd.edge->p) + 12 * i;
-    cuda_check(cudaMemcpyAsync(dst, r, sizeof r, cudaMemcpyHostToDevice, stream), "H2D");
-    if (nd.joint)
-      sbk::graph_joint_compose(nd.base->p, nd.values->p, i, 1, gj(nd.spec), nd.edge->p, s());
-    sync();
-  }
-
-  void edge_batch(uint32_t child, double* out16) const {
-    activate();
-    const Node& nd = at(child);
-    download16(nd.edge->p, out16);
-  }
-  void download16(const double* d12, double* out16) const {
-    d_tmp16.ensure(16 * n);
-    sbk::graph_34_to_colmajor(d12, n, d_tmp16.p, s());
-    cuda_check(cudaMemcpyAsync(out16, d_tmp16.p, 16 * n * sizeof(double), cudaMemcpyDeviceToHost, stream), "D2H");
-    sync();
-  }
-
-  void set_joint_states(uint32_t node, const double* v) {
-    activate();
-    Node& nd = at(node);
-    if (!nd.joint) throw std::invalid_argument("node is not articulated: " + nd.name);
-    if (!v) throw std::invalid_argument("joint values are NULL");
-    for (uint64_t i = 0; i < n; ++i)
-      if (v[i] < nd.spec.lo - 1e-12 || v[i] > nd.spec.hi + 1e-12)
-        throw std::invalid_argument("joint value out of limits for " + nd.name);
-    cuda_check(cudaMemcpyAsync(nd.values->p, v, n * sizeof(double), cudaMemcpyHostToDevice, stream), "H2D");
-    compose(nd, true);
-    sync();
-  }
-  void joint_states(uint32_t node, double* out) const {
-    activate();
-    const Node& nd = at(node);
-    if (!nd.joint) throw std::invalid_argument("node is not articulated: " + nd.name);
-    cuda_check(cudaMemcpyAsync(out, nd.values->p, n * sizeof(double), cudaMemcpyDeviceToHost, stream), "D2H");
-    sync();
-  }
-
-  // root -> node chain as device pointers, chain[0] = node
-  int upload_chain(uint32_t node) const {
-    std::vector<const double*> chain;
-    for (uint32_t cur = node; cur != 0; cur = nodes[cur].parent) {
-      chain.push_back(nodes[cur].edge->p);
-      if (chain.size() > nodes.size()) throw std::logic_error("scene graph is not a tree");
-    }
-    if (!chain.empty()) {
-      d_chain.ensure(chain.size());
-      cuda_check(cudaMemcpyAsync(d_chain.p, chain.data(), chain.size() * sizeof(void*), cudaMemcpyHostToDevice, stream), "H2D chain");
-    }
-    return static_cast<int>(chain.size());
-  }
-  void world_poses(uint32_t node, double* out16) const {
-    activate();
-    at(node);
-    const int depth = upload_chain(node);
-    if (depth == 0) {  // the root: N identities
-      download16(nodes[0].edge->p, out16);
-      return;
-    }
-    d_tmp16.ensure(16 * n);
-    sbk::graph_world_poses(d_chain.p, depth, n, d_tmp16.p, s());
-    cuda_check(cudaMemcpyAsync(out16, d_tmp16.p, 16 * n * sizeof(double), cudaMemcpyDeviceToHost, stream), "D2H");
-    sync();
-  }
-  // batched FK into device memory on the caller's stream
-  void world_poses_device(uint32_t node, double* d_out16, cudaStream_t st) const {
-    activate();
-    at(node);
-    cuda_check(cudaStreamSynchronize(stream), "sync");  // the graph's own updates are done
-    std::vector<const double*> chain;
-    for (uint32_t cur = node; cur != 0; cur = nodes[cur].parent) chain.push_back(nodes[cur].edge->p);
-    if (chain.empty()) {
-      sbk::graph_34_to_colmajor(nodes[0].edge->p, n, d_out16, reinterpret_cast<sb_stream_t>(st));
-      return;
-    }
-    if (!ev_chain) cuda_check(cudaEventCreateWithFlags(&ev_chain, cudaEventDisableTiming), "event");
-    cuda_check(cudaEventSynchronize(ev_chain), "sync");  // the previous chain upload is consumed
-    d_chain.ensure(chain.size());
-    h_chain.ensure(chain.size());
-    std::copy(chain.begin(), chain.end(), h_chain.p);
-    cuda_check(cudaMemcpyAsync(d_chain.p, h_chain.p, chain.size() * sizeof(void*), cudaMemcpyHostToDevice, st), "H2D chain");
-    sbk::graph_world_poses(d_chain.p, static_cast<int>(chain.size()), n, d_out16,
-                           reinterpret_cast<sb_stream_t>(st));
-    cuda_check(cudaEventRecord(ev_chain, st), "event");
-  }
-  mutable cudaEvent_t ev_chain = nullptr;
-  mutable PinnedArray<const double*> h_chain;
-  void world_pose(uint32_t node, uint64_t i, double* out16) const {
-    activate();
-    if (i >= n) throw std::out_of_range("instance out of range");
-    at(node);
-    const int depth = upload_chain(node);
-    d_tmp16.ensure(16);
-    sbk::graph_world_pose_one(d_chain.p, depth, i, d_tmp16.p, s());
-    cuda_check(cudaMemcpyAsync(out16, d_tmp16.p, 16 * sizeof(double), cudaMemcpyDeviceToHost, stream), "D2H");
-    sync();
-  }
-  bool is_tree() const {  // scene_graph.cpp:174-187
-    for (uint32_t i = 1; i < nodes.size(); ++i) {
-      std::vector<bool> seen(nodes.size(), false);
-      uint32_t cur = i;
-      while (cur != 0) {
-        if (seen[cur]) return false;
-        seen[cur] = true;
-        cur = nodes[cur].parent;
-      }
-    }
-    return true;
-  }
-  uint64_t valid_count() const {
-    activate();
-    d_count.ensure(1);
-    cuda_check(cudaMemsetAsync(d_count.p, 0, sizeof(unsigned long long), stream), "memset");
-    sbk::graph_count_valid(d_valid.p, n, d_count.p, s());
-    unsigned long long c = 0;
-    cuda_check(cudaMemcpyAsync(&c, d_count.p, sizeof c, cudaMemcpyDeviceToHost, stream), "D2H");
-    sync();
-    return c;
-  }
-};
-
 void sb_engine::write_back(uint32_t p, sb_graph& g, uint32_t node) {
   if (p >= places.size()) throw std::out_of_range("placement index out of range");
   if (g.n != n) throw std::invalid_argument("write_back: graph batch size != engine local instances");
@@ -2365,412 +1443,9 @@ void sb_engine::write_back(uint32_t p, sb_graph& g, uint32_t node) {
   g.sync();
 }
 
-extern "C" {
-
-sb_status sb_graph_create(uint64_t batch, int device, sb_graph** out) {
-  return guard([&] {
-    if (!out) throw std::invalid_argument("out is NULL");
-    *out = new sb_graph(batch, device);
-  });
-}
-void sb_graph_destroy(sb_graph* g) { delete g; }
-sb_status sb_graph_add_node(sb_graph* g, uint32_t parent, const char* name, int64_t geometry,
-                            const sb_joint* joint, uint32_t* id) {
-  return guard([&] {
-    const uint32_t v = g->add_node(parent, name, geometry, joint);
-    if (id) *id = v;
-  });
-}
-sb_status sb_graph_set_edge_batch(sb_graph* g, uint32_t parent, uint32_t child, const double* t16) {
-  return guard([&] { g->set_edge_batch(parent, child, t16); });
-}
-sb_status sb_graph_set_edge(sb_graph* g, uint32_t child, uint64_t i, const double pose[16]) {
-  return guard([&] { g->set_edge(child, i, pose); });
-}
-sb_status sb_graph_edge_batch(const sb_graph* g, uint32_t child, double* out16) {
-  return guard([&] { g->edge_batch(child, out16); });
-}
-sb_status sb_graph_set_joint_states(sb_graph* g, uint32_t node, const double* v) {
-  return guard([&] { g->set_joint_states(node, v); });
-}
-sb_status sb_graph_joint_states(const sb_graph* g, uint32_t node, double* out) {
-  return guard([&] { g->joint_states(node, out); });
-}
-sb_status sb_graph_world_poses(const sb_graph* g, uint32_t node, double* out16) {
-  return guard([&] { g->world_poses(node, out16); });
-}
-sb_status sb_graph_world_pose(const sb_graph* g, uint32_t node, uint64_t i, double pose[16]) {
-  return guard([&] { g->world_pose(node, i, pose); });
-}
-sb_status sb_graph_world_poses_device(const sb_graph* g, uint32_t node, double* d_out16,
-                                      void* cuda_stream) {
-  return guard([&] { g->world_poses_device(node, d_out16, static_cast<cudaStream_t>(cuda_stream)); });
-}
-sb_status sb_graph_find(const sb_graph* g, const char* name, int64_t* id) {
-  return guard([&] {
-    if (!name || !id) throw std::invalid_argument("NULL argument");
-    auto it = g->by_name.find(name);
-    *id = it == g->by_name.end() ? -1 : static_cast<int64_t>(it->second);
-  });
-}
-sb_status sb_graph_node_info(const sb_graph* g, uint32_t node, const char** name, uint32_t* parent,
-                             int64_t* geometry, int* articulated, sb_joint* joint) {
-  return guard([&] {
-    const sb_graph::Node& nd = g->at(node);
-    if (name) *name = nd.name.c_str();
-    if (parent) *parent = nd.parent;
-    if (geometry) *geometry = nd.geometry;
-    if (articulated) *articulated = nd.joint ? 1 : 0;
-    if (joint && nd.joint) *joint = nd.spec;
-  });
-}
-uint64_t sb_graph_node_count(const sb_graph* g) { return g->nodes.size(); }
-sb_status sb_graph_children(const sb_graph* g, uint32_t node, uint32_t* out, uint32_t cap,
-                            uint32_t* count) {
-  return guard([&] {
-    g->at(node);
-    uint32_t c = 0;
-    for (uint32_t i = 1; i < g->nodes.size(); ++i)
-      if (g->nodes[i].parent == node) {
-        if (out && c < cap) out[c] = i;
-        ++c;
-      }
-    if (count) *count = c;
-  });
-}
-sb_status sb_graph_is_tree(const sb_graph* g, int* t) {
-  return guard([&] { *t = g->is_tree() ? 1 : 0; });
-}
-sb_status sb_graph_valid_mask(const sb_graph* g, uint8_t* mask) {
-  return guard([&] {
-    g->activate();
-    cuda_check(cudaMemcpyAsync(mask, g->d_valid.p, g->n, cudaMemcpyDeviceToHost, g->stream), "D2H");
-    g->sync();
-  });
-}
-sb_status sb_graph_mark_invalid(sb_graph* g, uint64_t i) {
-  return guard([&] {
-    if (i >= g->n) throw std::out_of_range("instance out of range");
-    g->activate();
-    cuda_check(cudaMemsetAsync(g->d_valid.p + i, 0, 1, g->stream), "memset");
-    g->sync();
-  });
-}
-sb_status sb_graph_reset_validity(sb_graph* g) {
-  return guard([&] {
-    g->activate();
-    cuda_check(cudaMemsetAsync(g->d_valid.p, 1, g->n, g->stream), "memset");
-    g->sync();
-  });
-}
-sb_status sb_graph_valid_count(const sb_graph* g, uint64_t* count) {
-  return guard([&] { *count = g->valid_count(); });
-}
-
-sb_status sb_engine_write_back(sb_engine* e, uint32_t placement, sb_graph* g, uint32_t node) {
+extern "C" sb_status sb_engine_write_back(sb_engine* e, uint32_t placement, sb_graph* g, uint32_t node) {
   return guard([&] { e->write_back(placement, *g, node); });
 }
-
-}  // extern "C"
-
-// ===================================================================== ReachMap4D
-// reachability.cpp:10-273. Grid metadata on the host (same arithmetic as the reference),
-// occupancy bitsets and sample counts in HBM (sb_reach.cu), SBRM v1 files on the host.
-struct sb_reach_map {
-  int device;
-  cudaStream_t stream = nullptr;
-  uint64_t samples = 0;
-  sbk::ReachGrid g{};
-  uint64_t words = 0;
-  DevArray<unsigned long long> d_occ, d_any, d_count;
-  DevArray<unsigned> d_counts;  // empty after load
-  DevArray<double> d_base, d_targets, d_frames;
-  DevArray<const double*> d_frame_ptrs;
-  DevArray<uint32_t> d_active;
-  DevArray<uint8_t> d_out;
-
-  explicit sb_reach_map(int dev) : device(current_device_checked(dev)) {
-    cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
-  }
-  ~sb_reach_map() {
-    if (stream) {
-      cudaSetDevice(device);
-      cudaStreamSynchronize(stream);
-      cudaStreamDestroy(stream);
-    }
-  }
-  sb_stream_t s() const { return reinterpret_cast<sb_stream_t>(stream); }
-  void sync() const { cuda_check(cudaStreamSynchronize(stream), "sync"); }
-  uint64_t cells() const { return g.nr * g.nz * g.npsi; }
-
-  // occ_any from occ (build and load)
-  void finish_any() {
-    d_any.alloc(std::max<uint64_t>(1, (g.nr * g.nz + 63) / 64));
-    cuda_check(cudaMemsetAsync(d_any.p, 0, d_any.count * 8, stream), "memset");
-    sbk::reach_any(g, d_occ.p, d_any.p, s());
-  }
-
-  void build(const sb_chain_link* links, uint32_t n_links, const double* ee16, uint64_t n_samples,
-             double res, double psi_res, uint64_t seed) {
-    if (n_links == 0 || !links) throw std::invalid_argument("build: chain has no joints");
-    if (n_samples < 1) throw std::invalid_argument("build: need at least one sample");
-    if (res <= 0.0 || psi_res <= 0.0) throw std::invalid_argument("build: resolution must be positive");
-    std::vector<double> L(18 * n_links);
-    double ee[12];
-    if (ee16) {
-      if (!homogeneous16(ee16)) throw std::invalid_argument("build: non-homogeneous ee_offset");
-      colmajor_to_34(ee16, ee);
-    } else {
-      for (int k = 0; k < 12; ++k) ee[k] = (k % 5 == 0) ? 1.0 : 0.0;
-    }
-    auto norm3 = [](double x, double y, double z) { return std::sqrt((x * x + y * y) + z * z); };
-    double reach = norm3(ee[3], ee[7], ee[11]);  // KinematicChain::max_reach (:20-28)
-    for (uint32_t l = 0; l < n_links; ++l) {
-      const sb_chain_link& k = links[l];
-      if (!homogeneous16(k.origin)) throw std::invalid_argument("build: non-homogeneous link origin");
-      sb_joint j = k.joint;  // JointSpec ctor (scene_graph.cpp:9-17)
-      if (j.kind != 0 && j.kind != 1) throw std::invalid_argument("JointSpec: unknown kind");
-      if (j.lo > j.hi) throw std::invalid_argument("JointSpec: lo > hi");
-      const double nrm = norm3(j.axis[0], j.axis[1], j.axis[2]);
-      if (std::abs(nrm - 1.0) > 1e-9) {
-        if (nrm < 1e-12) throw std::invalid_argument("JointSpec: zero axis");
-        for (int c = 0; c < 3; ++c) j.axis[c] = j.axis[c] / nrm;
-      }
-      colmajor_to_34(k.origin, &L[18 * l]);
-      L[18 * l + 12] = j.kind;
-      for (int c = 0; c < 3; ++c) L[18 * l + 13 + c] = j.axis[c];
-      L[18 * l + 16] = j.lo;
-      L[18 * l + 17] = j.hi;
-      reach += norm3(k.origin[12], k.origin[13], k.origin[14]);
-      if (j.kind == 1) reach += std::max(std::abs(j.lo), std::abs(j.hi));
-    }
-    samples = n_samples;
-    g.res = res;
-    g.psi_res = psi_res;
-    g.r_max = reach + res;
-    g.z_min = -reach - res;
-    g.z_max = reach + res;
-    g.nr = static_cast<uint64_t>(std::ceil(g.r_max / res));
-    g.nz = static_cast<uint64_t>(std::ceil((g.z_max - g.z_min) / res));
-    g.npsi = static_cast<uint64_t>(std::ceil(M_PI / psi_res));
-    if (cells() > (1ull << 34)) throw std::invalid_argument("build: grid too fine");
-    words = (cells() + 63) / 64;
-    cuda_check(cudaSetDevice(device), "cudaSetDevice");
-    d_occ.alloc(std::max<uint64_t>(1, words));
-    d_counts.alloc(std::max<uint64_t>(1, cells()));
-    cuda_check(cudaMemsetAsync(d_occ.p, 0, d_occ.count * 8, stream), "memset");
-    cuda_check(cudaMemsetAsync(d_counts.p, 0, d_counts.count * 4, stream), "memset");
-    DevArray<double> d_links;
-    d_links.alloc(L.size());
-    cuda_check(cudaMemcpyAsync(d_links.p, L.data(), L.size() * 8, cudaMemcpyHostToDevice, stream), "H2D");
-    sbk::reach_build(d_links.p, static_cast<int>(n_links), ee, samples, seed, g, d_occ.p,
-                     d_counts.p, s());
-    finish_any();
-    sync();
-  }
-
-  uint64_t occupied() const {
-    cuda_check(cudaSetDevice(device), "cudaSetDevice");
-    auto& self = const_cast<sb_reach_map&>(*this);
-    self.d_count.ensure(1);
-    cuda_check(cudaMemsetAsync(self.d_count.p, 0, 8, stream), "memset");
-    sbk::reach_popcount(d_occ.p, words, self.d_count.p, s());
-    unsigned long long c = 0;
-    cuda_check(cudaMemcpyAsync(&c, self.d_count.p, 8, cudaMemcpyDeviceToHost, stream), "D2H");
-    sync();
-    return c;
-  }
-
-  // SBRM v1 (reachability.cpp:192-273)
-  void save(const char* path) const {
-    if (!path) throw std::invalid_argument("path is NULL");
-    std::vector<unsigned long long> occ(words);
-    cuda_check(cudaSetDevice(device), "cudaSetDevice");
-    if (words)
-      cuda_check(cudaMemcpy(occ.data(), d_occ.p, words * 8, cudaMemcpyDeviceToHost), "D2H occ");
-    FILE* f = std::fopen(path, "wb");
-    if (!f) throw std::runtime_error(std::string("cannot open for write: ") + path);
-    const uint32_t version = 1;
-    const uint64_t hdr[1] = {samples};
-    bool ok = std::fwrite("SBRM", 1, 4, f) == 4;
-    ok = ok && std::fwrite(&version, 4, 1, f) == 1 && std::fwrite(hdr, 8, 1, f) == 1;
-    const double dv[5] = {g.res, g.psi_res, g.r_max, g.z_min, g.z_max};
-    ok = ok && std::fwrite(dv, 8, 5, f) == 5;
-    const uint64_t nv[4] = {g.nr, g.nz, g.npsi, words};
-    ok = ok && std::fwrite(nv, 8, 4, f) == 4;
-    ok = ok && (words == 0 || std::fwrite(occ.data(), 8, words, f) == words);
-    ok = (std::fclose(f) == 0) && ok;
-    if (!ok) throw std::runtime_error(std::string("write failed: ") + path);
-  }
-  void load(const char* path) {
-    if (!path) throw std::invalid_argument("path is NULL");
-    FILE* f = std::fopen(path, "rb");
-    if (!f) throw std::runtime_error(std::string("cannot open reach map: ") + path);
-    char magic[4];
-    uint32_t version = 0;
-    double dv[5];
-    uint64_t nv[4];
-    const bool head = std::fread(magic, 1, 4, f) == 4;
-    if (!head || std::memcmp(magic, "SBRM", 4) != 0) {
-      std::fclose(f);
-      throw std::runtime_error(std::string("not a reach map file: ") + path);
-    }
-    if (std::fread(&version, 4, 1, f) != 1 || version != 1) {
-      std::fclose(f);
-      throw std::runtime_error("unsupported reach map version");
-    }
-    bool ok = std::fread(&samples, 8, 1, f) == 1 && std::fread(dv, 8, 5, f) == 5 &&
-              std::fread(nv, 8, 4, f) == 4;
-    std::vector<unsigned long long> occ;
-    if (ok) {
-      occ.resize(nv[3]);
-      ok = nv[3] == 0 || std::fread(occ.data(), 8, nv[3], f) == nv[3];
-    }
-    std::fclose(f);
-    if (!ok) throw std::runtime_error(std::string("truncated reach map: ") + path);
-    g.res = dv[0];
-    g.psi_res = dv[1];
-    g.r_max = dv[2];
-    g.z_min = dv[3];
-    g.z_max = dv[4];
-    g.nr = nv[0];
-    g.nz = nv[1];
-    g.npsi = nv[2];
-    words = nv[3];
-    if (words * 64 < cells()) throw std::runtime_error("reach map bitset shorter than its grid");
-    cuda_check(cudaSetDevice(device), "cudaSetDevice");
-    d_occ.alloc(std::max<uint64_t>(1, words));
-    if (words)
-      cuda_check(cudaMemcpyAsync(d_occ.p, occ.data(), words * 8, cudaMemcpyHostToDevice, stream), "H2D occ");
-    d_counts.release();
-    finish_any();
-    sync();
-  }
-
-  void query_batch(const double* base16, const double* targets, uint64_t n, bool has_incl,
-                   double incl, uint8_t* out) {
-    if (n && (!base16 || !targets || !out)) throw std::invalid_argument("query_batch: NULL array");
-    if (!n) return;
-    cuda_check(cudaSetDevice(device), "cudaSetDevice");
-    d_base.ensure(16 * n);
-    d_targets.ensure(3 * n);
-    d_out.ensure(n);
-    cuda_check(cudaMemcpyAsync(d_base.p, base16, 16 * n * 8, cudaMemcpyHostToDevice, stream), "H2D");
-    cuda_check(cudaMemcpyAsync(d_targets.p, targets, 3 * n * 8, cudaMemcpyHostToDevice, stream), "H2D");
-    sbk::reach_query_batch(g, d_occ.p, d_any.p, d_base.p, d_targets.p, n,
-                           has_incl ? incl : std::nan(""), d_out.p, s());
-    cuda_check(cudaMemcpyAsync(out, d_out.p, n, cudaMemcpyDeviceToHost, stream), "D2H");
-    sync();
-  }
-
-  void placement_filter(const double* base16, uint64_t n, const double* const* frames,
-                        uint32_t n_frames, const uint32_t* active, uint64_t m, uint8_t* out) {
-    if (m && (!base16 || !active || !out)) throw std::invalid_argument("placement_filter: NULL array");
-    if (!m) return;
-    for (uint64_t j = 0; j < m; ++j)
-      if (active[j] >= n) throw std::out_of_range("placement_filter: active index >= N");
-    cuda_check(cudaSetDevice(device), "cudaSetDevice");
-    d_base.ensure(16 * n);
-    cuda_check(cudaMemcpyAsync(d_base.p, base16, 16 * n * 8, cudaMemcpyHostToDevice, stream), "H2D");
-    uint32_t present = 0;
-    for (uint32_t f = 0; f < n_frames; ++f) present += frames && frames[f] ? 1 : 0;
-    d_frames.ensure(std::max<uint64_t>(1, 16 * n * present));
-    std::vector<const double*> ptrs(std::max<uint32_t>(1, n_frames), nullptr);
-    for (uint32_t f = 0, k = 0; f < n_frames; ++f) {
-      if (!frames || !frames[f]) continue;
-      double* dst = d_frames.p + 16 * n * k++;
-      cuda_check(cudaMemcpyAsync(dst, frames[f], 16 * n * 8, cudaMemcpyHostToDevice, stream), "H2D frames");
-      ptrs[f] = dst;
-    }
-    d_frame_ptrs.ensure(ptrs.size());
-    cuda_check(cudaMemcpyAsync(d_frame_ptrs.p, ptrs.data(), ptrs.size() * sizeof(void*), cudaMemcpyHostToDevice, stream), "H2D");
-    d_active.ensure(m);
-    d_out.ensure(m);
-    cuda_check(cudaMemcpyAsync(d_active.p, active, m * 4, cudaMemcpyHostToDevice, stream), "H2D");
-    sbk::reach_placement_filter(g, d_any.p, d_base.p, d_frame_ptrs.p, static_cast<int>(n_frames),
-                                d_active.p, m, d_out.p, s());
-    cuda_check(cudaMemcpyAsync(out, d_out.p, m, cudaMemcpyDeviceToHost, stream), "D2H");
-    sync();
-  }
-};
-
-extern "C" {
-
-sb_status sb_reach_build(const sb_chain_link* links, uint32_t n_links, const double ee[16],
-                         uint64_t samples, double res, double psi_res, uint64_t seed, int device,
-                         sb_reach_map** out) {
-  return guard([&] {
-    if (!out) throw std::invalid_argument("out is NULL");
-    std::unique_ptr<sb_reach_map> m(new sb_reach_map(device));
-    m->build(links, n_links, ee, samples, res, psi_res, seed);
-    *out = m.release();
-  });
-}
-sb_status sb_reach_load(const char* path, int device, sb_reach_map** out) {
-  return guard([&] {
-    if (!out) throw std::invalid_argument("out is NULL");
-    std::unique_ptr<sb_reach_map> m(new sb_reach_map(device));
-    m->load(path);
-    *out = m.release();
-  });
-}
-sb_status sb_reach_save(const sb_reach_map* m, const char* path) {
-  return guard([&] { m->save(path); });
-}
-void sb_reach_destroy(sb_reach_map* m) { delete m; }
-sb_status sb_reach_get_info(const sb_reach_map* m, sb_reach_info* o) {
-  return guard([&] {
-    o->samples = m->samples;
-    o->resolution = m->g.res;
-    o->psi_resolution = m->g.psi_res;
-    o->max_radius = m->g.r_max;
-    o->z_min = m->g.z_min;
-    o->z_max = m->g.z_max;
-    o->nr = m->g.nr;
-    o->nz = m->g.nz;
-    o->npsi = m->g.npsi;
-    o->cell_count = m->cells();
-    o->occupied_cells = m->occupied();
-  });
-}
-sb_status sb_reach_cell_samples(const sb_reach_map* m, uint64_t ir, uint64_t iz, uint64_t ip,
-                                uint32_t* count) {
-  return guard([&] {
-    *count = 0;
-    if (m->d_counts.count == 0) return;
-    if (ir >= m->g.nr || iz >= m->g.nz || ip >= m->g.npsi) throw std::out_of_range("cell out of range");
-    cuda_check(cudaSetDevice(m->device), "cudaSetDevice");
-    const uint64_t idx = (ir * m->g.nz + iz) * m->g.npsi + ip;
-    cuda_check(cudaMemcpy(count, m->d_counts.p + idx, 4, cudaMemcpyDeviceToHost), "D2H");
-  });
-}
-sb_status sb_reach_query_batch(const sb_reach_map* m, const double* base16, const double* targets,
-                               uint64_t n, int has_incl, double incl, uint8_t* out) {
-  return guard([&] {
-    const_cast<sb_reach_map*>(m)->query_batch(base16, targets, n, has_incl != 0, incl, out);
-  });
-}
-sb_status sb_reach_query_batch_device(const sb_reach_map* m, const double* d_base16,
-                                      const double* d_targets, uint64_t n, int has_incl,
-                                      double incl, uint8_t* d_out, void* cuda_stream) {
-  return guard([&] {
-    if (!n) return;
-    if (!d_base16 || !d_targets || !d_out) throw std::invalid_argument("query_batch: NULL array");
-    cuda_check(cudaSetDevice(m->device), "cudaSetDevice");
-    sbk::reach_query_batch(m->g, m->d_occ.p, m->d_any.p, d_base16, d_targets, n,
-                           has_incl ? incl : std::nan(""), d_out,
-                           reinterpret_cast<sb_stream_t>(static_cast<cudaStream_t>(cuda_stream)));
-  });
-}
-sb_status sb_reach_placement_filter(const sb_reach_map* m, const double* base16, uint64_t n,
-                                    const double* const* frames, uint32_t n_frames,
-                                    const uint32_t* active, uint64_t m_active, uint8_t* out) {
-  return guard([&] {
-    const_cast<sb_reach_map*>(m)->placement_filter(base16, n, frames, n_frames, active, m_active, out);
-  });
-}
-
-}  // extern "C"
 
 extern "C" sb_status sb_engine_set_reach_filter(sb_engine* e, uint32_t placement,
                                                 const sb_reach_map* m, const double* base16) {
@@ -2797,3 +1472,4 @@ extern "C" sb_status sb_engine_set_reach_filter(sb_engine* e, uint32_t placement
     f.grid = m->g;
   });
 }
+
