@@ -433,6 +433,14 @@ sb_status sb_reach_placement_filter(const sb_reach_map* m, const double* robot_b
 sb_status sb_engine_set_reach_filter(sb_engine* e, uint32_t placement, const sb_reach_map* map,
                                      const double* robot_base_colmajor16xN);
 
+/* sample_orientations on device pointers (active, positions_xyz, face_targets_xy, yaws),
+ * enqueued on cuda_stream (a cudaStream_t). */
+sb_status sb_sample_orientations_device(int kind, const uint32_t* d_active, uint64_t m,
+                                        const double* d_positions_xyz,
+                                        const double* d_face_targets_xy, uint64_t run_seed,
+                                        uint64_t placement_salt, uint64_t attempt, double* d_yaws,
+                                        void* cuda_stream);
+
 /* Diagnostics: evaluate the device libm used on the hot path (correctly rounded
  * double-double sin/cos/atan2, replacing glibc's std::sin/cos/atan2 in transform.hpp:47,
  * polygon.cpp:151, relationships.cpp:184,238) on n inputs on device 0.

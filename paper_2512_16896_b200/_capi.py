@@ -198,6 +198,8 @@ SIGNATURES = {
     "sb_graph_world_poses_device": (C.c_int, [_P, C.c_uint32, _P, _P]),
     "sb_reach_query_batch_device": (C.c_int, [_P, _P, _P, C.c_uint64, C.c_int, C.c_double, _P,
                                               _P]),
+    "sb_sample_orientations_device": (C.c_int, [C.c_int, _P, C.c_uint64, _P, _P, C.c_uint64,
+                                                C.c_uint64, C.c_uint64, _P, _P]),
     "sb_sampler_cache_info": (C.c_int, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "sb_sample_orientations": (C.c_int, [C.c_int, _U32, C.c_uint64, _D, _D, C.c_uint64,
                                          C.c_uint64, C.c_uint64, C.c_uint64, _D, C.c_int]),

@@ -468,4 +468,22 @@ sb_status sb_sample_orientations(int kind, const uint32_t* active, uint64_t m, c
   });
 }
 
+// sample_orientations on device pointers (active, positions, face targets, yaws), enqueued
+// on cuda_stream; face targets must cover every active index (not checked on the device).
+sb_status sb_sample_orientations_device(int kind, const uint32_t* d_active, uint64_t m,
+                                        const double* d_positions, const double* d_face_xy,
+                                        uint64_t run_seed, uint64_t salt, uint64_t attempt,
+                                        double* d_yaws, void* cuda_stream) {
+  return guard([&] {
+    if (kind < SB_ORIENT_FIXED || kind > SB_ORIENT_FACE_TO)
+      throw std::invalid_argument("sample_orientations: unknown orientation kind");
+    if (kind == SB_ORIENT_FACE_TO && !d_face_xy)
+      throw std::invalid_argument("sample_orientations: face_to target positions missing");
+    if (m && (!d_active || !d_yaws || (kind == SB_ORIENT_FACE_TO && !d_positions)))
+      throw std::invalid_argument("sample_orientations: NULL array");
+    sbk::orientations(kind, d_active, m, d_positions, d_face_xy, run_seed, salt, attempt, d_yaws,
+                      reinterpret_cast<sb_stream_t>(static_cast<cudaStream_t>(cuda_stream)));
+  });
+}
+
 }  // extern "C"

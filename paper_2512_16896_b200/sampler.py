@@ -110,3 +110,13 @@ def sample_orientations(kind: int, active: Sequence[int], positions: Optional[np
                                            0 if ft is None else len(ft), run_seed, placement_salt,
                                            attempt, _dp(y), device))
     return y
+
+
+def sample_orientations_device(kind: int, d_active: int, m: int, d_positions: int,
+                               d_face_targets: int, run_seed: int, placement_salt: int,
+                               attempt: int, d_yaws: int, stream: int = 0) -> None:
+    """sample_orientations on device pointers (e.g. torch .data_ptr()), on `stream`."""
+    A.check(A.lib().sb_sample_orientations_device(kind, d_active, m, d_positions or None,
+                                                  d_face_targets or None, run_seed,
+                                                  placement_salt, attempt, d_yaws,
+                                                  stream or None))

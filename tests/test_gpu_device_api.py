@@ -63,3 +63,25 @@ def test_graph_and_reach_device_equal_host(gpu, tmp_path):
         m.query_batch_device(db.data_ptr(), dt.data_ptr(), n, out.data_ptr(), inc, st.cuda_stream)
         st.synchronize()
         assert np.array_equal(out.cpu().numpy(), m.query_batch(B, T, inc))
+
+
+def test_orientations_device_equals_host(gpu):
+    import torch
+
+    from paper_2512_16896_b200.sampler import FACE_TO, UNIFORM_YAW, sample_orientations_device
+
+    rng = np.random.default_rng(3)
+    n = 3000
+    act = np.sort(rng.choice(n, 2000, replace=False)).astype(np.uint32)
+    pos = rng.uniform(-2, 2, (len(act), 3))
+    face = rng.uniform(-2, 2, (n, 2))
+    da = torch.tensor(act.astype(np.int32), device="cuda")
+    dp, df = torch.tensor(pos, device="cuda"), torch.tensor(face, device="cuda")
+    st = torch.cuda.Stream()
+    for kind in (UNIFORM_YAW, FACE_TO):
+        dy = torch.empty(len(act), dtype=torch.float64, device="cuda")
+        sample_orientations_device(kind, da.data_ptr(), len(act), dp.data_ptr(), df.data_ptr(),
+                                   77, 5, 2, dy.data_ptr(), st.cuda_stream)
+        st.synchronize()
+        want = gpu.sample_orientations(kind, act, pos, face, 77, 5, 2)
+        assert np.array_equal(dy.cpu().numpy(), want)
