@@ -65,6 +65,8 @@ struct Fixed {  // static shared memory
   uint32_t total;
   uint32_t tile;
   int32_t used;     // rounds a tile round consumed (FIFO speculation, phase C)
+  uint64_t seed;    // run seed (from p.seed_dev when set: graph-replayable launches)
+  uint64_t state0;  // Pcg32(make_stream(seed, {salt, "cach"})) after its constructor
   unsigned long long tclk;  // block 0 / thread 0 phase clock
   unsigned long long acc[8];  // its per-slot sums, written to p.prof once at the end
   unsigned long long ta, tb, t0;  // every block: A1 / A2+B ns of the current round (debug)
@@ -260,7 +262,7 @@ __device__ uint32_t tile_round(const PlaceParams& p, const Sampling& S, const Sb
       if (S.n == 0) {
         placeable = false;
       } else {
-        Pcg r{p.fast_state0};
+        Pcg r{F.state0};
         // j-th drained point = j-th draw (sampler.cpp:30-43). Slot v = s * nt + e is round
         // a + s, rank e: draw draw_base + s * nt + e = draw_base + v while nobody accepts
         // before round a + s (FIFO speculation, resolved in phase C).
@@ -273,7 +275,7 @@ __device__ uint32_t tile_round(const PlaceParams& p, const Sampling& S, const Sb
       if (nti == 0) {
         placeable = false;
       } else {  // make_stream(run_seed, {salt, "fall", inst, attempt}) (sampler.cpp:117)
-        Pcg r = Pcg::seeded(stream_seed4(p.run_seed, pl.salt, kFallbackSalt, gid,
+        Pcg r = Pcg::seeded(stream_seed4(F.seed, pl.salt, kFallbackSalt, gid,
                                          static_cast<uint64_t>(at)));
         double u = r.next_double(), r1 = r.next_double(), r2 = r.next_double();
         const uint64_t off = (uint64_t)inst * p.inst_cap;
@@ -295,7 +297,7 @@ __device__ uint32_t tile_round(const PlaceParams& p, const Sampling& S, const Sb
       double yaw = 0.0;
       if (pl.orientation == SB_ORIENT_UNIFORM_YAW) {  // sampler.cpp:140-141
         Pcg r = Pcg::seeded(
-            stream_seed4(p.run_seed, pl.salt, kYawSalt, gid, static_cast<uint64_t>(at)));
+            stream_seed4(F.seed, pl.salt, kYawSalt, gid, static_cast<uint64_t>(at)));
         const double two_pi = 2.0 * 3.14159265358979323846;
         yaw = 0.0 + (two_pi - 0.0) * r.next_double();
       } else if (pl.orientation == SB_ORIENT_FACE_TO) {  // relationships.cpp:232-239
@@ -805,6 +807,12 @@ __device__ void instance_tiles(const PlaceParams& p, const Sampling& S, const Sb
 }
 
 __device__ __forceinline__ void block_setup(const PlaceParams& p, Fixed& F, Tile& T, SbGeom& gA) {
+  if (threadIdx.x == 0) {  // the run seed from device memory (CUDA-graph replays) or the params
+    const uint64_t seed = p.seed_dev ? *p.seed_dev : p.run_seed;
+    F.seed = seed;
+    F.state0 = p.seed_dev ? Pcg::seeded(stream_seed2(seed, p.pl.salt, kCacheSalt)).state
+                          : p.fast_state0;
+  }
   gA = p.w.geoms[p.pl.geom];
   load_geom_cache(p.w, gA, F.gc);
   for (int ob = threadIdx.x; ob < p.w.n_objects; ob += kB) T.ogeo[ob] = obj_grec(p.w, ob);

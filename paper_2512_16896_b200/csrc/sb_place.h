@@ -44,6 +44,7 @@ struct PlaceParams {
   int32_t attempts;             // K
   int32_t fast;                 // canonical region (FIFO stream) vs per-instance regions
   uint64_t run_seed;
+  const uint64_t* seed_dev;     // optional: run_seed read on the device (graph replays)
   uint64_t global_begin;
   uint64_t fast_state0;
   const SbRegionTri* canon_tris;

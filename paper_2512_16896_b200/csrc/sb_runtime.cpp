@@ -450,6 +450,16 @@ struct sb_engine {
   DevArray<double> d_pose16;
   DevArray<double> d_out16;
   PinnedArray<uint8_t> h_stat;
+  DevArray<uint64_t> d_seed;  // run seed read by the placement kernels (graph replays)
+  PinnedArray<uint64_t> h_seed;
+  struct GraphSlot {  // one captured run per result mode (poses piped or not)
+    cudaGraphExec_t exec = nullptr;
+    uint64_t launches = 0, round_launches = 0, gen = 0;
+    SbWorldView view{};
+  };
+  GraphSlot graphs[2];
+  uint64_t graph_gen = 0;  // bumped when a placement's launch parameters change
+  bool use_graphs = std::getenv("SB_GRAPH") != nullptr;  // measured: no faster
   DevArray<unsigned long long> d_nvalid;
   bool host_times = std::getenv("SB_HOST_TIMES") != nullptr;  // end-of-run counters / ctrl words / region flags / timers  // [P][n][16] result poses written at accept (pipelined download)
   PinnedArray<uint64_t> h_count;
@@ -711,6 +721,8 @@ struct sb_engine {
 
   ~sb_engine() {
     if (world) cudaSetDevice(world->device);
+    for (GraphSlot& g : graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
     for (cudaEvent_t e : {ev_start, ev_stop, ev_r0, ev_r1})
       if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : ev_place) cudaEventDestroy(e);
@@ -828,217 +840,275 @@ struct sb_engine {
       cuda_check(cudaEventCreate(&e), "event");
       ev_place.push_back(e);
     }
-    cuda_check(cudaEventRecord(ev_start, stream), "event");
-    cuda_check(cudaMemsetAsync(d_counters.p, 0, 8 * sizeof(unsigned long long), stream), "memset");
-    cuda_check(cudaMemsetAsync(d_prof.p, 0, 8 * sizeof(uint64_t), stream), "memset");
-    if (round_debug) cuda_check(cudaMemsetAsync(d_dbg.p, 0, d_dbg.count * sizeof(unsigned), stream), "memset");
-    cuda_check(cudaMemsetAsync(d_ctrl.p, 0, d_ctrl.count * sizeof(uint32_t), stream), "memset");
-    cuda_check(cudaMemsetAsync(d_rflags.p, 0, d_rflags.count * sizeof(int32_t), stream), "memset");
-    sbk::engine_reset(wv, first_place_obj, static_cast<int32_t>(P), d_valid.p, d_accepted.p,
-                      static_cast<int32_t>(P), pipe ? d_out16.p : nullptr, s);
-    launches += 1;
-    if (cell_grid.g) {
-      sbk::cells_reset(wv, cell_grid, first_place_obj, s);
-      ++launches;
-    }
-    for (size_t p = 0; p < P; ++p) {
-      Placement& pl = places[p];
-      bool fast = true;
-      int canon_n = pl.canon_n;
-      const SbRegionTri* canon_tris = d_canon_tris.p + p * inst_cap;
-      const double* canon_cum = d_canon_cum.p + p * inst_cap;
-      const bool relation = pl.dev.anchor_object >= 0;
-      cuda_check(cudaEventRecord(ev_place[2 * p], stream), "event");
-      if (relation) {
-        if (world_size == 1) {
-          relation_prep_device(p, pl, wv, launches);
-        } else {
-          fast = !relation_prep_sharded(p, pl, wv, launches, canon_n);
-          if (!fast) ++per_inst_host;
-        }
+    // The device work of one run. capturing: recorded into a CUDA graph (single GPU, replayed
+    // by later calls; the run seed is read from d_seed on the device), so copies to the
+    // caller's buffers stay outside and events are external event nodes.
+    auto rec = [&](cudaEvent_t e, bool capturing) {
+      cuda_check(capturing ? cudaEventRecordWithFlags(e, stream, cudaEventRecordExternal)
+                           : cudaEventRecord(e, stream),
+                 "event");
+    };
+    h_seed.ensure(1);
+    h_seed.p[0] = run_seed;
+    d_seed.ensure(1);
+    cuda_check(cudaMemcpyAsync(d_seed.p, h_seed.p, 8, cudaMemcpyHostToDevice, stream), "H2D seed");
+    auto enqueue = [&](bool capturing) {
+      rec(ev_start, capturing);
+      cuda_check(cudaMemsetAsync(d_counters.p, 0, 8 * sizeof(unsigned long long), stream), "memset");
+      cuda_check(cudaMemsetAsync(d_prof.p, 0, 8 * sizeof(uint64_t), stream), "memset");
+      if (round_debug) cuda_check(cudaMemsetAsync(d_dbg.p, 0, d_dbg.count * sizeof(unsigned), stream), "memset");
+      cuda_check(cudaMemsetAsync(d_ctrl.p, 0, d_ctrl.count * sizeof(uint32_t), stream), "memset");
+      cuda_check(cudaMemsetAsync(d_rflags.p, 0, d_rflags.count * sizeof(int32_t), stream), "memset");
+      sbk::engine_reset(wv, first_place_obj, static_cast<int32_t>(P), d_valid.p, d_accepted.p,
+                        static_cast<int32_t>(P), pipe ? d_out16.p : nullptr, s);
+      launches += 1;
+      if (cell_grid.g) {
+        sbk::cells_reset(wv, cell_grid, first_place_obj, s);
+        ++launches;
       }
-      cuda_check(cudaEventRecord(ev_place[2 * p + 1], stream), "event");
-      uint64_t fast_state0 = 0;
-      {  // Pcg32(make_stream(run_seed, {salt, "cach"})) state after the constructor
-        uint64_t h = sbh::mix64(sbh::mix64(sbh::mix64(run_seed) ^ pl.dev.salt) ^ 0x63616368ULL);
-        const uint64_t mult = 6364136223846793005ULL, inc = (0xda3e39cb94b95bdbULL << 1u) | 1u;
-        uint64_t st0 = inc;
-        st0 += h;
-        st0 = st0 * mult + inc;
-        fast_state0 = st0;
-      }
-      sbk::PlaceParams pp;
-      std::memset(&pp, 0, sizeof pp);
-      pp.w = wv;
-      pp.pl = pl.dev;
-      pp.attempts = attempts;
-      pp.fast = fast ? 1 : 0;
-      pp.run_seed = run_seed;
-      pp.global_begin = begin;
-      pp.fast_state0 = fast_state0;
-      pp.canon_tris = canon_tris;
-      pp.canon_cum = canon_cum;
-      pp.canon_n = canon_n;
-      pp.inst_cap = inst_cap;
-      pp.inst_tris = d_inst_tris.p;
-      pp.inst_cum = d_inst_cum.p;
-      pp.inst_n = d_inst_n.p;
-      pp.valid = d_valid.p;
-      pp.accepted = d_accepted.p + p * n;
-      pp.out16 = pipe ? d_out16.p + p * 16 * n : nullptr;
-      pp.tile_list = d_tile_list.p;
-      pp.tile_cnt = d_tile_cnt.p;
-      pp.cpose = d_cpose.p;
-      pp.cinv = d_cinv.p;
-      pp.grid = cell_grid;
-      pp.cnt_stride = ntiles;
-      pp.ntiles = ntiles;
-      pp.tile_inst = tile_inst;
-      pp.tile_inst_pi = tile_inst_pi;
-      pp.ntiles_pi = static_cast<uint32_t>((n + tile_inst_pi - 1) / tile_inst_pi);
-      pp.spec_target = spec_target;
-      pp.solo_max = world_size == 1 ? solo_max : 0;
-      pp.solo_spec = solo_spec;
-      pp.ws_bytes = ws_bytes;
-      pp.max_tris = max_tris;
-      pp.max_nodes = max_nodes;
-      pp.ctrl = d_ctrl.p + 8 * p;
-      pp.counters = d_counters.p;
-      pp.prof = d_prof.p;
-      pp.dbg = round_debug ? d_dbg.p + 3 * static_cast<size_t>(attempts) * p : nullptr;
-      pp.dbg_inst = round_debug ? d_dbg.p + d_dbg.count - 16 : nullptr;
-      pp.vary_flag = (relation && world_size == 1) ? d_rflags.p + 2 * p : nullptr;
-      if (p < reach.size() && reach[p].any) {
-        pp.reach_any = reach[p].any;
-        pp.reach_grid = reach[p].grid;
-        pp.reach_base = reach[p].base->p;
-      }
-      if (world_size == 1) {
-        if (!sbk::place_persistent(pp, grid, smem, s))
-          throw CudaError("cooperative launch of the placement kernel is not possible");
-        ++launches;
-        ++round_launches;
-      } else if (!fast) {
-        // per-instance regions: tiles are independent, no exchange
-        device_rounds[p] = 1;
-        cuda_check(cudaEventRecord(ev_r0, stream), "event");
-        sbk::place_instances(pp, grid, smem, s);
-        cuda_check(cudaEventRecord(ev_r1, stream), "event");
-        ++launches;
-        ++round_launches;
-        cuda_check(cudaEventSynchronize(ev_r1), "sync");
-        float ms = 0.f;
-        cuda_check(cudaEventElapsedTime(&ms, ev_r0, ev_r1), "elapsed");
-        sharded_check_ms += ms;
-      } else if (allgather_dev) {
-        // FIFO fast path, device-side exchange: round a's kernel reads the gathered counts
-        // and the draws before it from device memory, the all-gather of its survivors is
-        // enqueued behind it; the host only checks for completion every kChunk rounds.
-        constexpr int kChunk = 4;
-        const size_t K1 = static_cast<size_t>(attempts) + 1, W = static_cast<size_t>(world_size);
-        d_xcount.ensure(K1);
-        d_xrecv.ensure(K1 * W);
-        d_xdraws.ensure(K1);
-        h_xrecv.ensure(K1 * W);
-        cuda_check(cudaMemsetAsync(d_xcount.p, 0, K1 * 8, stream), "memset");
-        cuda_check(cudaMemsetAsync(d_xdraws.p, 0, K1 * 8, stream), "memset");
-        pp.xcount = d_xcount.p;
-        pp.xrecv = d_xrecv.p;
-        pp.xdraws = d_xdraws.p;
-        pp.xrank = rank;
-        pp.xworld = world_size;
-        auto gather = [&](int32_t a) {
-          if (allgather_dev(allgather_dev_ctx, reinterpret_cast<const uint64_t*>(d_xcount.p + a), 1,
-                            reinterpret_cast<uint64_t*>(d_xrecv.p + a * W), stream) != 0)
-            throw std::runtime_error("sb_shard.allgather_dev failed");
-        };
-        cuda_check(cudaEventRecord(ev_r0, stream), "event");
-        sbk::place_fast_init(pp, grid, smem, s);
-        ++launches;
-        gather(0);
-        int32_t a = 0;
-        uint64_t last_total = 1;
-        while (a < attempts && last_total > 0) {
-          const int32_t stop = std::min<int32_t>(attempts, a + kChunk);
-          for (; a < stop; ++a) {
-            sbk::place_fast_round(pp, a, grid, smem, s);
-            launches += 1;
-            round_launches += 1;
-            gather(a + 1);
-          }
-          cuda_check(cudaMemcpyAsync(h_xrecv.p + a * W, d_xrecv.p + a * W, W * 8, cudaMemcpyDeviceToHost, stream), "D2H counts");
-          cuda_check(cudaStreamSynchronize(stream), "sync");
-          last_total = 0;
-          for (size_t r = 0; r < W; ++r) last_total += h_xrecv.p[a * W + r];
-        }
-        cuda_check(cudaEventRecord(ev_r1, stream), "event");
-        cuda_check(cudaMemcpyAsync(h_xrecv.p, d_xrecv.p, K1 * W * 8, cudaMemcpyDeviceToHost, stream), "D2H counts");
-        cuda_check(cudaStreamSynchronize(stream), "sync");
-        for (int32_t r = 0; r < a; ++r) {  // rounds the reference runs: total > 0
-          uint64_t t = 0;
-          for (size_t k = 0; k < W; ++k) t += h_xrecv.p[r * W + k];
-          if (t > 0) ++rounds_host;
-        }
-        if (a == attempts && last_total > 0) {
-          pp.xrecv = nullptr;  // mark the K-attempt survivors invalid
-          sbk::place_fast_finish(pp, a, grid, s);
-          ++launches;
-        }
-        float ms = 0.f;
-        cuda_check(cudaEventElapsedTime(&ms, ev_r0, ev_r1), "elapsed");
-        sharded_check_ms += ms;
-      } else {
-        // FIFO fast path: one launch per round, per-rank survivor counts exchanged between
-        uint32_t* tot = pp.ctrl;
-        auto read_total = [&](int32_t a) {
-          uint32_t v = 0;
-          cuda_check(cudaMemcpyAsync(&v, tot + sbk::place_total_word(a), 4, cudaMemcpyDeviceToHost, stream), "D2H total");
-          cuda_check(cudaStreamSynchronize(stream), "sync");
-          return static_cast<uint64_t>(v);
-        };
-        sbk::place_fast_init(pp, grid, smem, s);
-        ++launches;
-        uint64_t m = read_total(0), draws = 0;
-        int32_t a = 0;
-        for (; a < attempts; ++a) {
-          std::vector<uint64_t> counts = exchange({m});
-          uint64_t total = 0, before = 0;
-          for (int r = 0; r < world_size; ++r) {
-            if (r < rank) before += counts[r];
-            total += counts[r];
-          }
-          if (total == 0) break;
-          ++rounds_host;
-          cuda_check(cudaMemsetAsync(tot + sbk::place_total_word(a + 1), 0, 4, stream), "memset");
-          if (m > 0) {
-            pp.draw_base = draws + before;
-            cuda_check(cudaEventRecord(ev_r0, stream), "event");
-            sbk::place_fast_round(pp, a, grid, smem, s);
-            cuda_check(cudaEventRecord(ev_r1, stream), "event");
-            launches += 1;
-            round_launches += 1;
-            m = read_total(a + 1);
-            float ms = 0.f;
-            cuda_check(cudaEventElapsedTime(&ms, ev_r0, ev_r1), "elapsed");
-            sharded_check_ms += ms;
+      for (size_t p = 0; p < P; ++p) {
+        Placement& pl = places[p];
+        bool fast = true;
+        int canon_n = pl.canon_n;
+        const SbRegionTri* canon_tris = d_canon_tris.p + p * inst_cap;
+        const double* canon_cum = d_canon_cum.p + p * inst_cap;
+        const bool relation = pl.dev.anchor_object >= 0;
+        rec(ev_place[2 * p], capturing);
+        if (relation) {
+          if (world_size == 1) {
+            relation_prep_device(p, pl, wv, launches);
           } else {
-            m = 0;
+            fast = !relation_prep_sharded(p, pl, wv, launches, canon_n);
+            if (!fast) ++per_inst_host;
           }
-          if (canon_n > 0) draws += total;
         }
-        if (a == attempts && m > 0) {
-          sbk::place_fast_finish(pp, a, grid, s);
+        rec(ev_place[2 * p + 1], capturing);
+        uint64_t fast_state0 = 0;
+        {  // Pcg32(make_stream(run_seed, {salt, "cach"})) state after the constructor
+          uint64_t h = sbh::mix64(sbh::mix64(sbh::mix64(run_seed) ^ pl.dev.salt) ^ 0x63616368ULL);
+          const uint64_t mult = 6364136223846793005ULL, inc = (0xda3e39cb94b95bdbULL << 1u) | 1u;
+          uint64_t st0 = inc;
+          st0 += h;
+          st0 = st0 * mult + inc;
+          fast_state0 = st0;
+        }
+        sbk::PlaceParams pp;
+        std::memset(&pp, 0, sizeof pp);
+        pp.w = wv;
+        pp.pl = pl.dev;
+        pp.attempts = attempts;
+        pp.fast = fast ? 1 : 0;
+        pp.run_seed = run_seed;
+        pp.seed_dev = d_seed.p;
+        pp.global_begin = begin;
+        pp.fast_state0 = fast_state0;
+        pp.canon_tris = canon_tris;
+        pp.canon_cum = canon_cum;
+        pp.canon_n = canon_n;
+        pp.inst_cap = inst_cap;
+        pp.inst_tris = d_inst_tris.p;
+        pp.inst_cum = d_inst_cum.p;
+        pp.inst_n = d_inst_n.p;
+        pp.valid = d_valid.p;
+        pp.accepted = d_accepted.p + p * n;
+        pp.out16 = pipe ? d_out16.p + p * 16 * n : nullptr;
+        pp.tile_list = d_tile_list.p;
+        pp.tile_cnt = d_tile_cnt.p;
+        pp.cpose = d_cpose.p;
+        pp.cinv = d_cinv.p;
+        pp.grid = cell_grid;
+        pp.cnt_stride = ntiles;
+        pp.ntiles = ntiles;
+        pp.tile_inst = tile_inst;
+        pp.tile_inst_pi = tile_inst_pi;
+        pp.ntiles_pi = static_cast<uint32_t>((n + tile_inst_pi - 1) / tile_inst_pi);
+        pp.spec_target = spec_target;
+        pp.solo_max = world_size == 1 ? solo_max : 0;
+        pp.solo_spec = solo_spec;
+        pp.ws_bytes = ws_bytes;
+        pp.max_tris = max_tris;
+        pp.max_nodes = max_nodes;
+        pp.ctrl = d_ctrl.p + 8 * p;
+        pp.counters = d_counters.p;
+        pp.prof = d_prof.p;
+        pp.dbg = round_debug ? d_dbg.p + 3 * static_cast<size_t>(attempts) * p : nullptr;
+        pp.dbg_inst = round_debug ? d_dbg.p + d_dbg.count - 16 : nullptr;
+        pp.vary_flag = (relation && world_size == 1) ? d_rflags.p + 2 * p : nullptr;
+        if (p < reach.size() && reach[p].any) {
+          pp.reach_any = reach[p].any;
+          pp.reach_grid = reach[p].grid;
+          pp.reach_base = reach[p].base->p;
+        }
+        if (world_size == 1) {
+          if (!sbk::place_persistent(pp, grid, smem, s))
+            throw CudaError("cooperative launch of the placement kernel is not possible");
           ++launches;
+          ++round_launches;
+        } else if (!fast) {
+          // per-instance regions: tiles are independent, no exchange
+          device_rounds[p] = 1;
+          cuda_check(cudaEventRecord(ev_r0, stream), "event");
+          sbk::place_instances(pp, grid, smem, s);
+          cuda_check(cudaEventRecord(ev_r1, stream), "event");
+          ++launches;
+          ++round_launches;
+          cuda_check(cudaEventSynchronize(ev_r1), "sync");
+          float ms = 0.f;
+          cuda_check(cudaEventElapsedTime(&ms, ev_r0, ev_r1), "elapsed");
+          sharded_check_ms += ms;
+        } else if (allgather_dev) {
+          // FIFO fast path, device-side exchange: round a's kernel reads the gathered counts
+          // and the draws before it from device memory, the all-gather of its survivors is
+          // enqueued behind it; the host only checks for completion every kChunk rounds.
+          constexpr int kChunk = 4;
+          const size_t K1 = static_cast<size_t>(attempts) + 1, W = static_cast<size_t>(world_size);
+          d_xcount.ensure(K1);
+          d_xrecv.ensure(K1 * W);
+          d_xdraws.ensure(K1);
+          h_xrecv.ensure(K1 * W);
+          cuda_check(cudaMemsetAsync(d_xcount.p, 0, K1 * 8, stream), "memset");
+          cuda_check(cudaMemsetAsync(d_xdraws.p, 0, K1 * 8, stream), "memset");
+          pp.xcount = d_xcount.p;
+          pp.xrecv = d_xrecv.p;
+          pp.xdraws = d_xdraws.p;
+          pp.xrank = rank;
+          pp.xworld = world_size;
+          auto gather = [&](int32_t a) {
+            if (allgather_dev(allgather_dev_ctx, reinterpret_cast<const uint64_t*>(d_xcount.p + a), 1,
+                              reinterpret_cast<uint64_t*>(d_xrecv.p + a * W), stream) != 0)
+              throw std::runtime_error("sb_shard.allgather_dev failed");
+          };
+          cuda_check(cudaEventRecord(ev_r0, stream), "event");
+          sbk::place_fast_init(pp, grid, smem, s);
+          ++launches;
+          gather(0);
+          int32_t a = 0;
+          uint64_t last_total = 1;
+          while (a < attempts && last_total > 0) {
+            const int32_t stop = std::min<int32_t>(attempts, a + kChunk);
+            for (; a < stop; ++a) {
+              sbk::place_fast_round(pp, a, grid, smem, s);
+              launches += 1;
+              round_launches += 1;
+              gather(a + 1);
+            }
+            cuda_check(cudaMemcpyAsync(h_xrecv.p + a * W, d_xrecv.p + a * W, W * 8, cudaMemcpyDeviceToHost, stream), "D2H counts");
+            cuda_check(cudaStreamSynchronize(stream), "sync");
+            last_total = 0;
+            for (size_t r = 0; r < W; ++r) last_total += h_xrecv.p[a * W + r];
+          }
+          cuda_check(cudaEventRecord(ev_r1, stream), "event");
+          cuda_check(cudaMemcpyAsync(h_xrecv.p, d_xrecv.p, K1 * W * 8, cudaMemcpyDeviceToHost, stream), "D2H counts");
+          cuda_check(cudaStreamSynchronize(stream), "sync");
+          for (int32_t r = 0; r < a; ++r) {  // rounds the reference runs: total > 0
+            uint64_t t = 0;
+            for (size_t k = 0; k < W; ++k) t += h_xrecv.p[r * W + k];
+            if (t > 0) ++rounds_host;
+          }
+          if (a == attempts && last_total > 0) {
+            pp.xrecv = nullptr;  // mark the K-attempt survivors invalid
+            sbk::place_fast_finish(pp, a, grid, s);
+            ++launches;
+          }
+          float ms = 0.f;
+          cuda_check(cudaEventElapsedTime(&ms, ev_r0, ev_r1), "elapsed");
+          sharded_check_ms += ms;
+        } else {
+          // FIFO fast path: one launch per round, per-rank survivor counts exchanged between
+          uint32_t* tot = pp.ctrl;
+          auto read_total = [&](int32_t a) {
+            uint32_t v = 0;
+            cuda_check(cudaMemcpyAsync(&v, tot + sbk::place_total_word(a), 4, cudaMemcpyDeviceToHost, stream), "D2H total");
+            cuda_check(cudaStreamSynchronize(stream), "sync");
+            return static_cast<uint64_t>(v);
+          };
+          sbk::place_fast_init(pp, grid, smem, s);
+          ++launches;
+          uint64_t m = read_total(0), draws = 0;
+          int32_t a = 0;
+          for (; a < attempts; ++a) {
+            std::vector<uint64_t> counts = exchange({m});
+            uint64_t total = 0, before = 0;
+            for (int r = 0; r < world_size; ++r) {
+              if (r < rank) before += counts[r];
+              total += counts[r];
+            }
+            if (total == 0) break;
+            ++rounds_host;
+            cuda_check(cudaMemsetAsync(tot + sbk::place_total_word(a + 1), 0, 4, stream), "memset");
+            if (m > 0) {
+              pp.draw_base = draws + before;
+              cuda_check(cudaEventRecord(ev_r0, stream), "event");
+              sbk::place_fast_round(pp, a, grid, smem, s);
+              cuda_check(cudaEventRecord(ev_r1, stream), "event");
+              launches += 1;
+              round_launches += 1;
+              m = read_total(a + 1);
+              float ms = 0.f;
+              cuda_check(cudaEventElapsedTime(&ms, ev_r0, ev_r1), "elapsed");
+              sharded_check_ms += ms;
+            } else {
+              m = 0;
+            }
+            if (canon_n > 0) draws += total;
+          }
+          if (a == attempts && m > 0) {
+            sbk::place_fast_finish(pp, a, grid, s);
+            ++launches;
+          }
+        }
+        if (pipe && capturing) {  // graph: the copy follows the launch (graph_copies)
+          rec(ev_pose[p], true);
+        } else if (pipe) {  // placement p is final: copy its poses behind an event
+          // (k_place wrote them at accept: a DMA only, no SM work beside the next placement)
+          cuda_check(cudaEventRecord(ev_pose[p], stream), "event");
+          cuda_check(cudaStreamWaitEvent(copy_stream, ev_pose[p], 0), "wait");
+          cuda_check(cudaMemcpyAsync(out->poses + 16 * n * p, d_out16.p + 16 * n * p,
+                                     16 * n * sizeof(double), cudaMemcpyDeviceToHost, copy_stream),
+                     "D2H poses");
         }
       }
-      if (pipe) {  // placement p is final: convert + copy its poses behind an event
-        // (k_place wrote them at accept: a DMA only, no SM work beside the next placement)
-        cuda_check(cudaEventRecord(ev_pose[p], stream), "event");
-        cuda_check(cudaStreamWaitEvent(copy_stream, ev_pose[p], 0), "wait");
-        cuda_check(cudaMemcpyAsync(out->poses + 16 * n * p, d_out16.p + 16 * n * p,
-                                   16 * n * sizeof(double), cudaMemcpyDeviceToHost, copy_stream),
-                   "D2H poses");
+    };
+    const bool graphable = world_size == 1 && !round_debug && !place_times && use_graphs;
+    if (graphable) {
+      GraphSlot& gs = graphs[pipe ? 1 : 0];
+      const SbWorldView now = world->view();
+      if (!gs.exec || gs.gen != graph_gen || std::memcmp(&now, &gs.view, sizeof now) != 0) {
+        if (gs.exec) cudaGraphExecDestroy(gs.exec);
+        gs.exec = nullptr;
+        const uint64_t l0 = launches, r0 = round_launches;
+        cuda_check(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+        try {
+          enqueue(true);
+        } catch (...) {
+          cudaGraph_t gbad = nullptr;
+          cudaStreamEndCapture(stream, &gbad);
+          if (gbad) cudaGraphDestroy(gbad);
+          throw;
+        }
+        cudaGraph_t gr = nullptr;
+        cuda_check(cudaStreamEndCapture(stream, &gr), "end capture");
+        const cudaError_t ie = cudaGraphInstantiate(&gs.exec, gr, 0);
+        cudaGraphDestroy(gr);
+        cuda_check(ie, "graph instantiate");
+        gs.launches = launches - l0;
+        gs.round_launches = round_launches - r0;
+        gs.view = now;
+        gs.gen = graph_gen;
+      } else {
+        launches += gs.launches;
+        round_launches += gs.round_launches;
       }
+      cuda_check(cudaGraphLaunch(gs.exec, stream), "graph launch");
+      if (pipe)  // graph_copies: each placement's poses behind its event, on the copy stream
+        for (size_t p = 0; p < P; ++p) {
+          cuda_check(cudaStreamWaitEvent(copy_stream, ev_pose[p], 0), "wait");
+          cuda_check(cudaMemcpyAsync(out->poses + 16 * n * p, d_out16.p + 16 * n * p,
+                                     16 * n * sizeof(double), cudaMemcpyDeviceToHost, copy_stream),
+                     "D2H poses");
+        }
+    } else {
+      enqueue(false);
     }
     if (out) {
       if (out->accepted && P)
@@ -1452,6 +1522,7 @@ extern "C" sb_status sb_engine_set_reach_filter(sb_engine* e, uint32_t placement
   return guard([&] {
     if (placement >= e->places.size()) throw std::out_of_range("placement index out of range");
     e->reach.resize(e->places.size());
+    ++e->graph_gen;  // the captured launches carry the filter parameters
     sb_engine::ReachFilter& f = e->reach[placement];
     if (!m) {  // clear
       f = sb_engine::ReachFilter();

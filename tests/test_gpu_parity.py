@@ -488,3 +488,14 @@ def test_ratio_on_support_validation(gpu):
                                                 distance=0.3)
     with pytest.raises(ValueError):
         pkg.Engine(scene)
+
+
+def test_graph_replay_equals_direct(gpu, ref, monkeypatch):
+    """SB_GRAPH=1: the run captured once into a CUDA graph and replayed (seed read on the
+    device) gives the same results as direct launches, for several seeds."""
+    monkeypatch.setenv("SB_GRAPH", "1")
+    scene = scenes.tabletop_mixed(1024, n_objects=9)
+    eng = gpu.Engine(scene)
+    for seed in (1, 2, 1):
+        got = eng.generate(seed)
+        assert_same(gpu, got, ref.generate(scene, seed, threads=8))
