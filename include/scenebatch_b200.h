@@ -15,7 +15,8 @@
  *    memory of the reference's Eigen::Matrix4d / TransformBatch (transform.hpp:10-27),
  *    so a TransformBatch's data() can be passed without conversion. The bottom row must
  *    be (0,0,0,1) exactly (SPEC TransformBatch invariant); other poses are rejected.
- *  - All buffers are caller-owned host memory, copied in and out. No torch types.
+ *  - Buffers are caller-owned host memory, copied in and out, except the *_device entry
+ *    points, which take device pointers and a cudaStream_t (as void*). No torch types.
  *  - A handle is single-writer; calls on one handle are serialized on its CUDA stream.
  *  - There is no CPU fallback: without a usable sm_100 device every compute entry point
  *    fails with SB_ERR_CUDA.
