@@ -1134,6 +1134,7 @@ struct sb_engine {
       d_nvalid.ensure(1);
       cuda_check(cudaMemsetAsync(d_nvalid.p, 0, 8, stream), "memset");
       sbk::graph_count_valid(d_valid.p, n, d_nvalid.p, s);
+      ++launches;
       cuda_check(cudaMemcpyAsync(nvalid, d_nvalid.p, 8, cudaMemcpyDeviceToHost, stream), "D2H nvalid");
     }
     const auto th1 = std::chrono::steady_clock::now();
