@@ -70,7 +70,7 @@ struct sb_sampler {
   DevArray<double> d_states;
   DevArray<int32_t> d_rflags;
   DevArray<sbk::SbArcTable> d_arcs;
-  DevArray<double> d_sup, d_pos;
+  DevArray<double> d_sup, d_pos, d_sup16;
   DevArray<uint32_t> d_active;
   DevArray<uint8_t> d_pl;
   DevArray<uint64_t> d_seg;
@@ -302,19 +302,33 @@ struct sb_sampler {
       if (!per_instance) drain(0);
       return;
     }
-    h_sup.ensure(12 * m);
-    for (uint64_t j = 0; j < m; ++j) {
+    for (uint64_t j = 0; j < m; ++j)
       if (active[j] >= n) throw std::out_of_range("sample: active index >= batch_size");
-      colmajor_to_34(support + 16 * static_cast<uint64_t>(active[j]), h_sup.p + 12 * j);
+    // Dense active sets: the whole TransformBatch goes up as is and the kernels read each
+    // support in place; sparse ones: the active rows are gathered on the host first.
+    const bool dense = 4 * m >= n;
+    const double* ksup34 = nullptr;
+    const double* ksup16 = nullptr;
+    d_active.ensure(m);
+    cuda_check(cudaMemcpyAsync(d_active.p, active, m * 4, cudaMemcpyHostToDevice, stream), "H2D active");
+    if (dense) {
+      d_sup16.ensure(16 * n);
+      cuda_check(cudaMemcpyAsync(d_sup16.p, support, 16 * n * sizeof(double), cudaMemcpyHostToDevice, stream), "H2D support");
+      ksup16 = d_sup16.p;
+    } else {
+      h_sup.ensure(12 * m);
+      for (uint64_t j = 0; j < m; ++j)
+        colmajor_to_34(support + 16 * static_cast<uint64_t>(active[j]), h_sup.p + 12 * j);
+      d_sup.ensure(12 * m);
+      cuda_check(cudaMemcpyAsync(d_sup.p, h_sup.p, 12 * m * sizeof(double), cudaMemcpyHostToDevice, stream), "H2D support");
+      ksup34 = d_sup.p;
     }
-    d_sup.ensure(12 * m);
     d_pos.ensure(3 * m);
-    cuda_check(cudaMemcpyAsync(d_sup.p, h_sup.p, 12 * m * sizeof(double), cudaMemcpyHostToDevice, stream), "H2D support");
     if (!per_instance) {
       const int nseg = drain(m);
       d_seg.ensure(2 * nseg);
       cuda_check(cudaMemcpyAsync(d_seg.p, h_seg.p, 2 * nseg * sizeof(uint64_t), cudaMemcpyHostToDevice, stream), "H2D segments");
-      sbk::sampler_fifo(d_sup.p, nullptr, nullptr, m, d_seg.p, d_seg.p + nseg, nseg,
+      sbk::sampler_fifo(ksup34, ksup16, d_active.p, m, d_seg.p, d_seg.p + nseg, nseg,
                         cache_state0(run_seed, salt),
                         d_tris.p, d_cum.p, region_nt, d_pos.p, stream);
       cuda_check(cudaMemcpyAsync(pos, d_pos.p, 3 * m * sizeof(double), cudaMemcpyDeviceToHost, stream), "D2H positions");
@@ -322,10 +336,8 @@ struct sb_sampler {
       std::memset(placeable, 1, m);
       return;
     }
-    d_active.ensure(m);
     d_pl.ensure(m);
-    cuda_check(cudaMemcpyAsync(d_active.p, active, m * 4, cudaMemcpyHostToDevice, stream), "H2D active");
-    sbk::sampler_fallback(d_sup.p, nullptr, d_active.p, m, run_seed, salt, attempt,
+    sbk::sampler_fallback(ksup34, ksup16, d_active.p, m, run_seed, salt, attempt,
                           stride_tables ? nullptr : d_inst_tab.p, d_inst_n.p, table_cap, d_tris.p,
                           d_cum.p, d_pos.p, d_pl.p, stream);
     cuda_check(cudaMemcpyAsync(pos, d_pos.p, 3 * m * sizeof(double), cudaMemcpyDeviceToHost, stream), "D2H positions");
