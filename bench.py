@@ -4,13 +4,18 @@
 A step is one full generation pass (every placement, every attempt round) over the
 config's N variations per GPU, through the C ABI (libscenebatch_b200.so).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2_mixed] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4_clutter] [--impl ours|reference]
 
+Default workload: C4 (262,144 variations x 100 sphere-set objects), the largest
+single-GPU configuration BASELINE.json names (its `metric` is not quoted on any config).
 N>1 runs under torchrun (one rank per GPU): instances are sharded by contiguous
 variation ranges (weak scaling: N_per_gpu fixed); the only exchange is the fast-path
-per-round count allgather (4-8 bytes per rank per round, torch.distributed gloo).
+per-round count all-gather (8 bytes per rank per round).
 `value` times results resident in HBM (CUDA events on the engine stream, L2 flushed
 between steps); `e2e` times the same call with the results copied to pinned host memory.
+--impl reference times the reference itself (oracle/_ref/libsbref.so: its own sources
+compiled in place + the Appendix-C driver) on the host cores; that process builds its
+scene with the reference's own mesh constructors and never maps this package's library.
 """
 from __future__ import annotations
 
@@ -277,11 +282,9 @@ def run_ours(args, rank, world, local_rank):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic scene of the named shape, seeded (no assets/network); run_seed 1",
-        "config": {"workload": f"{args.config}: {desc}", "n_instances_per_gpu": n_per,
-                   "n_instances_total": n_total, "placements": P,
-                   "candidates_per_object": scene.attempts, "parallelism": f"dp{world} (variation shards)",
-                   "l2": "flushed (256 MiB write) between timed steps",
-                   "valid_fraction": round(valid_sum / n_total, 4)},
+        "config": workload_config(args, world, scene),
+        "valid_fraction": round(valid_sum / n_total, 4),
+        "l2": "flushed (256 MiB write) between timed steps",
         "cold_start_s": round(cold_s, 3),
         "roofline": primary,
         "roofline_secondary": secondary,
@@ -296,66 +299,106 @@ def run_ours(args, rank, world, local_rank):
         "clocks": clk,
     }
     if not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args, scene_factory=factory, n_default=n_default)
+        line["cpu_baseline"] = cpu_baseline(args)
     return line
 
 
-def cpu_baseline(args, scene_factory, n_default, budget_s=12.0):
-    """Reference (oracle/_ref: the reference's own sources + driver) on the host cores."""
+def workload_config(args, world, scene):
+    """The `config` object, identical in both arms (--impl ours / reference)."""
+    desc, _, n_default = WORKLOADS[args.config]
+    n_per = args.n or n_default
+    return {"workload": f"{args.config}: {desc}", "n_instances_per_gpu": n_per,
+            "n_instances_total": n_per * world, "placements": len(scene.placements),
+            "candidates_per_object": scene.attempts,
+            "parallelism": f"dp{world} (variation shards)"}
+
+
+# Variations per reference step: a bounded sample of the workload (the same scene, fewer
+# variations), so `--steps K --warmup W` of the CPU reference ends within minutes. Per-
+# variation CPU work does not depend on N (the fast path's shared stream only orders the
+# draws), so scenes/s over the sample is the reference's rate on the workload.
+REF_SAMPLE = {"c1_tabletop": 1024, "c2_mixed": 16384, "c3_kitchen": 8192, "c4_clutter": 8192,
+              "c5_sweep100": 32768, "c5_sweep10": 262144}
+
+
+def reference_scene(args, n):
+    """The workload's scene built with the reference's own mesh constructors
+    (oracle/_ref: trimesh.cpp make_box / make_cylinder / make_sphere, transform_point)."""
+    from oracle import oracle as O
+    from paper_2512_16896_b200 import scenes
+    from paper_2512_16896_b200.world import TriMesh
+
+    prims = {"make_box": lambda sx, sy, sz: TriMesh(*O.make_box(sx, sy, sz)),
+             "make_cylinder": lambda r, h, seg=32: TriMesh(*O.make_cylinder(r, h, seg)),
+             "make_sphere": lambda r, st=12, sl=16: TriMesh(*O.make_sphere(r, st, sl)),
+             "transformed": lambda m, pose: TriMesh(O.transformed_vertices(m.vertices, pose),
+                                                    m.triangles.copy())}
+    with scenes.mesh_source(**prims):
+        return WORKLOADS[args.config][1](n)
+
+
+def time_reference(scene, steps, warmup, threads):
+    """Warm generation passes of the reference (RefEngine: cold part outside the timer)."""
     from oracle import oracle as O
 
-    threads = os.cpu_count() or 1
-    n = args.cpu_n or min(n_default, 4096)
-    scene = scene_factory(n)
-    t0 = time.perf_counter()
-    passes = valid = checks = 0
-    while True:
-        r = O.generate(scene, 1, threads=threads, with_poses=False)
-        passes += 1
+    eng = O.RefEngine(scene, threads)
+    for _ in range(warmup):
+        eng.generate(1)
+    times, valid, checks = [], 0, 0
+    for _ in range(steps):
+        t = time.perf_counter()
+        r = eng.generate(1)
+        times.append(time.perf_counter() - t)
         valid += r["stats"]["valid_instances"]
         checks += r["stats"]["candidate_checks"]
-        if time.perf_counter() - t0 > budget_s or passes >= 50:
-            break
-    dt = time.perf_counter() - t0
-    return {"value": round(valid / dt, 1), "unit": "collision-free scenes/s",
-            "checks_per_s": round(checks / dt, 1), "cores": threads, "kind": "reference",
-            "sample": f"{passes} generation pass(es) of the same scene shape at N={n} "
-                      f"({dt:.1f} s, ThreadPool({threads}))"}
+    eng.close()
+    return sum(times), valid, checks
+
+
+def cpu_baseline(args, budget_s=12.0):
+    """The reference (oracle/_ref) on the host cores, rank 0 at N=1: warm passes over a
+    bounded sample of the workload for about `budget_s` seconds."""
+    threads = os.cpu_count() or 1
+    n = args.cpu_n or min(REF_SAMPLE[args.config], WORKLOADS[args.config][2], 4096)
+    scene = reference_scene(args, n)
+    total = valid = checks = passes = 0
+    while total < budget_s and passes < 50:
+        dt, v, c = time_reference(scene, 1, 1 if passes == 0 else 0, threads)
+        total += dt
+        valid += v
+        checks += c
+        passes += 1
+    return {"value": round(valid / total, 1), "unit": "collision-free scenes/s",
+            "checks_per_s": round(checks / total, 1), "cores": threads, "kind": "reference",
+            "sample": f"{passes} warm generation pass(es) of the workload's scene at {n} "
+                      f"variations ({total:.1f} s timed, ThreadPool({threads}))"}
 
 
 def run_reference(args, rank, world):
     """--impl reference: the reference's CPU path on this host (rank 0 only)."""
     if rank != 0:
         return None
-    from oracle import oracle as O
-
-    desc, factory, n_default = WORKLOADS[args.config]
-    n = args.n or n_default
-    scene = factory(n)
+    desc, _, n_default = WORKLOADS[args.config]
+    n_cfg = args.n or n_default
+    n = min(n_cfg, args.ref_n or REF_SAMPLE[args.config])
+    scene = reference_scene(args, n)
     threads = os.cpu_count() or 1
-    for _ in range(args.warmup):
-        O.generate(scene, 1, threads=threads, with_poses=False)
-    times, valid, checks = [], 0, 0
-    for _ in range(args.steps):
-        t = time.perf_counter()
-        r = O.generate(scene, 1, threads=threads, with_poses=False)
-        times.append(time.perf_counter() - t)
-        valid += r["stats"]["valid_instances"]
-        checks += r["stats"]["candidate_checks"]
-    total = sum(times)
+    total, valid, checks = time_reference(scene, args.steps, args.warmup, threads)
     value = valid / total
+    sample = (f"each step: one warm generation pass of the workload's scene over {n} of its "
+              f"{n_cfg} variations per GPU (bounded sample; ThreadPool({threads}))")
     return {
         "impl": "reference", "metric": METRIC, "value": round(value, 1),
         "unit": "collision-free scenes/s", "checks_per_s": round(checks / total, 1),
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(total / args.steps * 1e3, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic scene of the named shape, seeded; run_seed 1",
-        "config": {"workload": f"{args.config}: {desc}", "n_instances": n,
-                   "placements": len(scene.placements), "candidates_per_object": scene.attempts},
+        "data": "synthetic scene of the named shape, seeded (no assets/network); run_seed 1",
+        "config": workload_config(args, world, scene),
+        "valid_fraction": round(valid / (n * args.steps), 4),
+        "sample": sample,
         "cpu_baseline": {"value": round(value, 1), "unit": "collision-free scenes/s",
-                         "cores": threads, "kind": "reference",
-                         "sample": f"{args.steps} full generation passes at N={n}"},
+                         "cores": threads, "kind": "reference", "sample": sample},
         "e2e": {"value": round(value, 1), "unit": "collision-free scenes/s",
                 "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -366,23 +409,29 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2_mixed", choices=sorted(WORKLOADS))
+    ap.add_argument("--config", default="c4_clutter", choices=sorted(WORKLOADS))
     ap.add_argument("--n", type=int, default=0, help="variations per GPU (default: config's)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-n", type=int, default=0)
+    ap.add_argument("--ref-n", type=int, default=0,
+                    help="--impl reference: variations per step (default: REF_SAMPLE)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     rank, world, local_rank = dist_env()
     args.xdev = None
+    if args.impl == "reference":
+        # rank 0 alone times the reference; no process group, nothing of this package's
+        # library is loaded in this process
+        line = run_reference(args, rank, world)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
     if world > 1:
         from paper_2512_16896_b200.dist import init_group
 
         args.xdev = init_group(local_rank)
-    if args.impl == "reference":
-        line = run_reference(args, rank, world)
-    else:
-        line = run_ours(args, rank, world, local_rank)
+    line = run_ours(args, rank, world, local_rank)
     if line is not None:
         print(json.dumps(line), flush=True)
     if world > 1:

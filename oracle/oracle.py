@@ -84,6 +84,10 @@ def lib():
         L.ref_get_stats.argtypes = [C.c_void_p, C.c_void_p]
         L.ref_generate.argtypes = [C.c_void_p, C.c_void_p, u64, C.c_int, C.c_void_p, C.c_void_p,
                                    C.c_void_p, C.c_void_p]
+        L.ref_engine_create.restype = C.c_void_p
+        L.ref_engine_create.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
+        L.ref_engine_destroy.argtypes = [C.c_void_p]
+        L.ref_engine_generate.argtypes = [C.c_void_p, u64, C.c_void_p, C.c_void_p]
         L.ref_sampler_create.restype = C.c_void_p
         L.ref_sampler_create.argtypes = [u64]
         L.ref_sampler_destroy.argtypes = [C.c_void_p]
@@ -304,6 +308,57 @@ def generate(scene, run_seed: int, threads: int = 1, shard=None, with_poses: boo
     check(rc)
     stats = {k: getattr(st, k) for k, _ in A.sb_run_stats._fields_}
     return {"accepted": acc, "valid": valid, "poses": poses, "stats": stats}
+
+
+class RefEngine:
+    """The rejection loop split into its cold part (constructor: RefWorld + ThreadPool,
+    geometry registration / BVH builds, objects) and warm runs (generate), so a timer can
+    bracket only the generation loop (warm time)."""
+
+    def __init__(self, scene, threads: int = 1):
+        self.scene = scene
+        self._sc, self._keep = scene.to_c()
+        self.h = lib().ref_engine_create(C.byref(self._sc), None, threads)
+        if not self.h:
+            raise ValueError(lib().ref_last_error().decode())
+        self.n = scene.n_instances
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().ref_engine_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown
+            pass
+
+    def generate(self, run_seed: int, with_poses: bool = False):
+        from paper_2512_16896_b200 import _capi as A  # data layout only
+
+        P = len(self.scene.placements)
+        acc = np.empty((P, self.n), np.int16)
+        valid = np.empty(self.n, np.uint8)
+        poses = np.empty((P, self.n, 16)) if with_poses else None
+        res = A.sb_result(acc.ctypes.data_as(C.POINTER(C.c_int16)),
+                          poses.ctypes.data_as(C.POINTER(C.c_double)) if with_poses else None,
+                          valid.ctypes.data_as(C.POINTER(C.c_uint8)))
+        st = A.sb_run_stats()
+        check(lib().ref_engine_generate(self.h, C.c_uint64(run_seed), C.byref(res), C.byref(st)))
+        stats = {k: getattr(st, k) for k, _ in A.sb_run_stats._fields_}
+        return {"accepted": acc, "valid": valid, "poses": poses, "stats": stats}
+
+
+def transformed_vertices(v, pose):
+    """trimesh.cpp:112-118 (transform_point per vertex, transform.hpp:71-73) in the Eigen
+    shim's order: ((r0 x + r1 y) + r2 z) + t, rounded once per operation."""
+    v = np.asarray(v, np.float64)
+    m = np.asarray(pose, np.float64)
+    out = np.empty_like(v)
+    for r in range(3):
+        out[:, r] = ((m[r, 0] * v[:, 0] + m[r, 1] * v[:, 1]) + m[r, 2] * v[:, 2]) + m[r, 3]
+    return out
 
 
 def _rings(rings):

@@ -559,54 +559,93 @@ typedef void (*ref_trace_fn)(void* ctx, int32_t placement, int32_t attempt, uint
                              const uint32_t* active_global, const double* poses16,
                              const uint8_t* placeable, const uint8_t* free_by_slot);
 
-// Runs the rejection loop. shard may be NULL (whole batch). threads: ThreadPool size
-// (0 = hardware concurrency, 1 = serial). Outputs follow sb_result (local instances).
-int ref_generate(const sb_scene* sc, const sb_shard* shard, uint64_t run_seed, int threads,
-                 sb_result* out, sb_run_stats* st, ref_trace_fn trace, void* trace_ctx) {
-  REF_TRY({
-    const uint64_t n_total = sc->n_instances;
-    uint64_t begin = 0, end = n_total;
-    int rank = 0, world_size = 1;
+// The rejection loop, split as the reference's SPEC splits it:
+// RefEngine's constructor is the cold part (RefWorld + ThreadPool, geometry registration
+// with its BVH builds, object creation); generate() is one warm run -- the only part
+// bench.py times. shard may be NULL (whole batch). threads: ThreadPool size (0 = hardware
+// concurrency, 1 = serial). Outputs follow sb_result (local instances).
+struct RefEngine {
+  uint64_t n_total = 0, begin = 0, end = 0;
+  int rank = 0, world_size = 1;
+  sb_allgather_fn ag = nullptr;
+  void* ag_ctx = nullptr;
+  std::size_t n_local = 0;
+  int K = 0;
+  std::vector<sb_fixed_object> fixed;
+  std::vector<sb_support> supports;
+  std::vector<sb_placement> placements;
+  RefWorld w;
+  std::vector<TriMesh> meshes;
+  std::vector<int> geom_of_mesh;
+  std::vector<int> obj_of_placement;
+
+  static std::size_t local_size(const sb_scene* sc, const sb_shard* shard) {
+    if (!sc) throw std::invalid_argument("scene is NULL");
+    const uint64_t b = shard ? shard->begin : 0, e = shard ? shard->end : sc->n_instances;
+    if (b > e || e > sc->n_instances) throw std::invalid_argument("bad shard range");
+    if (e == b) throw std::invalid_argument("empty shard");
+    return e - b;
+  }
+
+  RefEngine(const sb_scene* sc, const sb_shard* shard, int threads)
+      : w(local_size(sc, shard), 0.0, threads) {
+    n_total = sc->n_instances;
+    begin = 0;
+    end = n_total;
     if (shard) {
       begin = shard->begin;
       end = shard->end;
       rank = shard->rank;
       world_size = shard->world_size;
+      ag = shard->allgather;
+      ag_ctx = shard->ctx;
     }
-    if (begin > end || end > n_total) throw std::invalid_argument("bad shard range");
-    const std::size_t n_local = end - begin;
-    if (n_local == 0) throw std::invalid_argument("empty shard");
-    if (world_size > 1 && (!shard || !shard->allgather))
-      throw std::invalid_argument("sharded run needs an allgather callback");
-    auto allgather = [&](std::vector<uint64_t> send) {
-      std::vector<uint64_t> recv(send.size() * world_size);
-      if (world_size == 1) return send;
-      if (shard->allgather(shard->ctx, send.data(), static_cast<uint32_t>(send.size()),
-                           recv.data()) != 0)
-        throw std::runtime_error("allgather callback failed");
-      return recv;
-    };
-
-    RefWorld w(n_local, 0.0, threads);
-    std::vector<TriMesh> meshes;
-    std::vector<int> geom_of_mesh;
+    n_local = end - begin;
+    if (world_size > 1 && !ag) throw std::invalid_argument("sharded run needs an allgather callback");
+    K = sc->attempts;
+    fixed.assign(sc->fixed, sc->fixed + sc->n_fixed);
+    supports.assign(sc->supports, sc->supports + sc->n_supports);
+    placements.assign(sc->placements, sc->placements + sc->n_placements);
     for (uint32_t i = 0; i < sc->n_meshes; ++i) {
       const sb_mesh& m = sc->meshes[i];
       meshes.push_back(mesh_from(m.vertices, m.n_vertices, m.triangles, m.n_triangles));
       geom_of_mesh.push_back(w.world.register_geometry(meshes.back()));
     }
-    for (uint32_t f = 0; f < sc->n_fixed; ++f) {
-      int obj = w.world.add_object("fixed", geom_of_mesh.at(sc->fixed[f].mesh));
-      w.world.update_transforms(obj, TransformBatch(n_local, mat_from(sc->fixed[f].pose)));
+    for (const sb_fixed_object& f : fixed) {
+      int obj = w.world.add_object("fixed", geom_of_mesh.at(f.mesh));
+      w.world.update_transforms(obj, TransformBatch(n_local, mat_from(f.pose)));
       w.world.set_enabled_all(obj, true);
     }
-    std::vector<int> obj_of_placement;
-    for (uint32_t p = 0; p < sc->n_placements; ++p)
+    for (uint32_t p = 0; p < placements.size(); ++p)
       obj_of_placement.push_back(
-          w.world.add_object("p" + std::to_string(p), geom_of_mesh.at(sc->placements[p].mesh)));
+          w.world.add_object("p" + std::to_string(p), geom_of_mesh.at(placements[p].mesh)));
+  }
 
+  std::vector<uint64_t> allgather(std::vector<uint64_t> send) {
+    if (world_size == 1) return send;
+    std::vector<uint64_t> recv(send.size() * world_size);
+    if (ag(ag_ctx, send.data(), static_cast<uint32_t>(send.size()), recv.data()) != 0)
+      throw std::runtime_error("allgather callback failed");
+    return recv;
+  }
+
+  void generate(uint64_t run_seed, sb_result* out, sb_run_stats* st, ref_trace_fn trace,
+                void* trace_ctx);
+};
+
+void RefEngine::generate(uint64_t run_seed, sb_result* out, sb_run_stats* st,
+                         ref_trace_fn trace, void* trace_ctx) {
+    // warm reset: every placed object leaves the world, counters restart
+    for (int obj : obj_of_placement) w.world.set_enabled_all(obj, false);
+    w.world.reset_stats();
+    struct {
+      uint32_t n_placements;
+      const sb_placement* placements;
+      const sb_support* supports;
+    } scv{static_cast<uint32_t>(placements.size()), placements.data(), supports.data()};
+    const auto* sc = &scv;
     std::vector<uint8_t> valid(n_local, 1);
-    const int K = sc->attempts;
+    // K: attempts per placement (member)
     uint64_t rounds = 0, sampled = 0, per_inst = 0;
     if (out && out->accepted)
       for (std::size_t k = 0; k < sc->n_placements * n_local; ++k) out->accepted[k] = -1;
@@ -799,7 +838,27 @@ int ref_generate(const sb_scene* sc, const sb_shard* shard, uint64_t run_seed, i
       st->rounds = rounds;
       st->per_instance_placements = per_inst;
     }
+}
+
+int ref_generate(const sb_scene* sc, const sb_shard* shard, uint64_t run_seed, int threads,
+                 sb_result* out, sb_run_stats* st, ref_trace_fn trace, void* trace_ctx) {
+  REF_TRY({
+    RefEngine e(sc, shard, threads);
+    e.generate(run_seed, out, st, trace, trace_ctx);
   });
+}
+
+extern "C" void* ref_engine_create(const sb_scene* sc, const sb_shard* shard, int threads) {
+  try {
+    return new RefEngine(sc, shard, threads);
+  } catch (const std::exception& e) {
+    fail(e, SB_ERR_INVALID_ARGUMENT);
+    return nullptr;
+  }
+}
+extern "C" void ref_engine_destroy(void* h) { delete static_cast<RefEngine*>(h); }
+extern "C" int ref_engine_generate(void* h, uint64_t run_seed, sb_result* out, sb_run_stats* st) {
+  REF_TRY(static_cast<RefEngine*>(h)->generate(run_seed, out, st, nullptr, nullptr));
 }
 
 }  // extern "C"

@@ -943,8 +943,13 @@ __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_fast_round(PlacePar
     const unsigned long long draws = __ldcg(p.xdraws + a);
     if (blockIdx.x == 0 && threadIdx.x == 0)
       p.xdraws[a + 1] = draws + (p.canon_n > 0 ? tot : 0ull);  // cache drained only if sampled
-    // this rank has no survivors left (its tile counts are no longer maintained): idle
-    if (__ldcg(p.xrecv + (size_t)a * p.xworld + p.xrank) == 0) return;
+    // this rank has no survivors left: idle, but keep its tile counts maintained (the
+    // round-(a+1) buffer still holds round a-1's counts, which k_fast_finish would read)
+    if (__ldcg(p.xrecv + (size_t)a * p.xworld + p.xrank) == 0) {
+      uint32_t* cout = p.tile_cnt + (size_t)((a + 1) & 1) * p.cnt_stride;
+      for (uint32_t t = blockIdx.x * kB + threadIdx.x; t < p.ntiles; t += gridDim.x * kB) cout[t] = 0;
+      return;
+    }
     fast_round<kGrid, kReach>(p, S, gA, T, F, a, draws + before, L, nullptr, false,
                               p.xcount + a + 1);
   } else {

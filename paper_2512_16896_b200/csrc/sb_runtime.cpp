@@ -1005,8 +1005,8 @@ struct sb_engine {
             for (size_t k = 0; k < W; ++k) t += h_xrecv.p[r * W + k];
             if (t > 0) ++rounds_host;
           }
-          if (a == attempts && last_total > 0) {
-            pp.xrecv = nullptr;  // mark the K-attempt survivors invalid
+          if (a == attempts && h_xrecv.p[static_cast<size_t>(a) * W + rank] > 0) {
+            pp.xrecv = nullptr;  // mark this rank's K-attempt survivors invalid
             sbk::place_fast_finish(pp, a, grid, s);
             ++launches;
           }

@@ -4,18 +4,52 @@ There is no network and the reference ships no assets, so every scene is generat
 a fixed seed: object sizes come from the reference's own PCG32 (rng.hpp:24-60) seeded
 with ``config_seed`` and are identical across variations. Meshes are built through the
 C ABI's primitives (bit-identical to trimesh.cpp), so the reference oracle and the GPU
-engine consume byte-identical inputs.
+engine consume byte-identical inputs. ``mesh_source`` swaps the primitive constructors
+(bench.py's reference arm builds the same scenes with the reference's own make_box /
+make_cylinder / make_sphere, so that process never maps this package's library).
 """
 from __future__ import annotations
 
+import contextlib
 import math
 from typing import List
 
 import numpy as np
 
 from . import _capi as A
-from .world import (Fixed, Placement, Relation, Scene, Support, TriMesh, make_box,
-                    make_cylinder, make_sphere, merge, transformed, translation)
+from . import world as _world
+from .world import Fixed, Placement, Relation, Scene, Support, TriMesh, merge, translation
+
+_PRIMS = {"make_box": _world.make_box, "make_cylinder": _world.make_cylinder,
+          "make_sphere": _world.make_sphere, "transformed": _world.transformed}
+
+
+@contextlib.contextmanager
+def mesh_source(**prims):
+    """Temporarily build scenes with other primitive constructors (same signatures as
+    world.make_box / make_cylinder / make_sphere / transformed)."""
+    old = dict(_PRIMS)
+    _PRIMS.update(prims)
+    try:
+        yield
+    finally:
+        _PRIMS.update(old)
+
+
+def make_box(sx, sy, sz) -> TriMesh:
+    return _PRIMS["make_box"](sx, sy, sz)
+
+
+def make_cylinder(radius, height, segments=32) -> TriMesh:
+    return _PRIMS["make_cylinder"](radius, height, segments)
+
+
+def make_sphere(radius, stacks=12, slices=16) -> TriMesh:
+    return _PRIMS["make_sphere"](radius, stacks, slices)
+
+
+def transformed(mesh: TriMesh, pose) -> TriMesh:
+    return _PRIMS["transformed"](mesh, pose)
 
 M64 = (1 << 64) - 1
 
