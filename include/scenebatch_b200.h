@@ -442,11 +442,16 @@ sb_status sb_sample_orientations_device(int kind, const uint32_t* d_active, uint
                                         uint64_t placement_salt, uint64_t attempt, double* d_yaws,
                                         void* cuda_stream);
 
-/* Diagnostics: evaluate the device libm used on the hot path (correctly rounded
- * double-double sin/cos/atan2, replacing glibc's std::sin/cos/atan2 in transform.hpp:47,
- * polygon.cpp:151, relationships.cpp:184,238) on n inputs on device 0.
- * fn 0: out[i] = sin(in[i]); 1: cos(in[i]); 2: atan2(in[2i], in[2i+1]). */
+/* Diagnostics: evaluate the device libm used on the hot path (sb_glibcm.cuh: glibc
+ * 2.39's sincos / sin / cos / atan2 restated bit for bit, replacing the reference's
+ * std::sin/cos/atan2 in transform.hpp:47,77, polygon.cpp:151, relationships.cpp:95,202,238)
+ * on n inputs on device 0. fn 0 / 1: the sine / cosine of sincos(in[i]) (what GCC makes of
+ * the reference's adjacent std::cos + std::sin); 2: atan2(in[2i], in[2i+1]); 3 / 4: sin /
+ * cos(in[i]). */
 sb_status sb_device_math(int fn, const double* in, uint64_t n, double* out);
+/* The same functions (same fn codes) evaluated by the host build of sb_glibcm.cuh: no
+ * device needed; the CPU tests pin the restatement to the host's glibc with it. */
+sb_status sb_host_math(int fn, const double* in, uint64_t n, double* out);
 /* Diagnostics: narrow-phase cycle breakdown accumulated since the last call (all zeros
  * unless the library was built with -DSB_NARROW_PROF): pose+M, node tests, triangle
  * transform, DAG walk, triangle tests, pairs. */

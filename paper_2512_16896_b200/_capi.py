@@ -151,6 +151,7 @@ SIGNATURES = {
     "sb_engine_phase_profile": (C.c_int, [_P, _D]),
     "sb_debug_region_profile": (C.c_int, [C.POINTER(C.c_uint64)]),
     "sb_device_math": (C.c_int, [C.c_int, _D, C.c_uint64, _D]),
+    "sb_host_math": (C.c_int, [C.c_int, _D, C.c_uint64, _D]),
     "sb_debug_narrow_profile": (C.c_int, [C.POINTER(C.c_uint64)]),
     "sb_sampler_create": (C.c_int, [C.c_uint64, C.c_int, C.POINTER(_P)]),
     "sb_sampler_destroy": (None, [_P]),

@@ -8,6 +8,7 @@
 #include <string>
 
 #include "sb_crmath.cuh"
+#include "sb_glibcm.cuh"
 #include "sb_dev.cuh"
 #include "sb_graph.h"
 #include "sb_joint.cuh"

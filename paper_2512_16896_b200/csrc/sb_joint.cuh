@@ -3,6 +3,7 @@
 #pragma once
 
 #include "sb_crmath.cuh"
+#include "sb_glibcm.cuh"
 #include "sb_dev.cuh"
 #include "sb_graph.h"
 
@@ -22,7 +23,7 @@ __device__ __forceinline__ void joint_motion(const sbk::GraphJoint& j, double v,
     return;
   }
   double s, c;
-  sbm::sincos_cr(v, &s, &c);
+  sbg::sincos(v, &s, &c);
   const double sx = ax * s, sy = ay * s, sz = az * s;
   const double c1 = 1.0 - c;
   const double cx = ax * c1, cy = ay * c1, cz = az * c1;

@@ -6,6 +6,7 @@
 
 #include "../../include/scenebatch_b200.h"
 #include "sb_crmath.cuh"
+#include "sb_glibcm.cuh"
 #include "sb_dev.cuh"
 #include "sb_kernels.h"
 #include "sb_poly.h"
@@ -175,7 +176,7 @@ __global__ void k_anchor_states(WorldView w, int32_t anchor_obj, M34 inv_support
   mul34(inv_support, P, rel);
   out[3 * i + 0] = rel.m[3];
   out[3 * i + 1] = rel.m[7];
-  out[3 * i + 2] = sbm::atan2_cr(rel.m[4], rel.m[0]);
+  out[3 * i + 2] = sbg::atan2(rel.m[4], rel.m[0]);
 }
 
 __global__ void k_pose_colmajor(WorldView w, int32_t obj, double* out16) {
@@ -191,16 +192,21 @@ __global__ void k_pose_colmajor(WorldView w, int32_t obj, double* out16) {
   o[15] = 1.0;
 }
 
-// Test hook: fn 0 = sin, 1 = cos, 2 = atan2(in[2i], in[2i+1]) with the device functions the
-// hot path uses (sb_crmath.cuh).
+// Test hook with the device functions the hot path uses (sb_glibcm.cuh): fn 0 / 1 = the
+// sine / cosine of glibc's sincos (what the reference's merged std::sin + std::cos calls
+// run), 2 = atan2(in[2i], in[2i+1]), 3 / 4 = glibc's sin / cos on their own.
 __global__ void k_debug_math(int fn, const double* in, uint64_t n, double* out) {
   uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (fn == 2) {
-    out[i] = sbm::atan2_cr(in[2 * i], in[2 * i + 1]);
+    out[i] = sbg::atan2(in[2 * i], in[2 * i + 1]);
+  } else if (fn == 3) {
+    out[i] = sbg::sin(in[i]);
+  } else if (fn == 4) {
+    out[i] = sbg::cos(in[i]);
   } else {
     double s, c;
-    sbm::sincos_cr(in[i], &s, &c);
+    sbg::sincos(in[i], &s, &c);
     out[i] = fn == 0 ? s : c;
   }
 }
@@ -303,7 +309,7 @@ __global__ void k_orientations(int kind, const uint32_t* active, uint64_t m, con
   } else if (kind == SB_ORIENT_FACE_TO) {
     const double dx = __ldg(face_xy + 2 * inst) - __ldg(pos + 3 * j);
     const double dy = __ldg(face_xy + 2 * inst + 1) - __ldg(pos + 3 * j + 1);
-    yaw = sqrt(dx * dx + dy * dy) < 1e-12 ? 0.0 : sbm::atan2_cr(dy, dx);
+    yaw = sqrt(dx * dx + dy * dy) < 1e-12 ? 0.0 : sbg::atan2(dy, dx);
   }
   yaws[j] = yaw;
 }

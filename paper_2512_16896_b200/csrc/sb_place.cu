@@ -8,6 +8,7 @@
 
 #include "../../include/scenebatch_b200.h"
 #include "sb_crmath.cuh"
+#include "sb_glibcm.cuh"
 #include "sb_dev.cuh"
 #include "sb_place.h"
 #include "sb_reachdev.cuh"
@@ -303,10 +304,10 @@ __device__ uint32_t tile_round(const PlaceParams& p, const Sampling& S, const Sb
       } else if (pl.orientation == SB_ORIENT_FACE_TO) {  // relationships.cpp:232-239
         const double* tp = w.pose + sb_pose_off(w, pl.face_object, inst);
         double dx = tp[3] - px, dy = tp[7] - py;
-        yaw = sqrt(dx * dx + dy * dy) < 1e-12 ? 0.0 : sbm::atan2_cr(dy, dx);
+        yaw = sqrt(dx * dx + dy * dy) < 1e-12 ? 0.0 : sbg::atan2(dy, dx);
       }
       double c, s;
-      sbm::sincos_cr(yaw, &s, &c);  // rotation_z: std::cos / std::sin (transform.hpp:47)
+      sbg::sincos(yaw, &s, &c);  // rotation_z: std::cos / std::sin (transform.hpp:47)
       M34 Tr, Rz, pose;  // translation(p + z_off z) * rotation_z(yaw)
 #pragma unroll
       for (int k = 0; k < 12; ++k) Tr.m[k] = Rz.m[k] = 0.0;

@@ -13,6 +13,7 @@
 
 #include "../../include/scenebatch_b200.h"
 #include "sb_crmath.cuh"
+#include "sb_glibcm.cuh"
 #include "sb_dev.cuh"
 #include "sb_poly.h"
 #include "sb_region.h"
@@ -199,7 +200,7 @@ __device__ __forceinline__ void resolve_direction(const SbPlacementDev& pl, doub
   }
   if (pl.frame == SB_FRAME_LOCAL) {
     double c, s;
-    sbm::sincos_cr(ayaw, &s, &c);
+    sbg::sincos(ayaw, &s, &c);
     const double nx = c * vx - s * vy, ny = s * vx + c * vy;
     vx = nx;
     vy = ny;
@@ -223,7 +224,7 @@ __device__ __forceinline__ bool arc_ends(const SbPlacementDev& pl, double vx, do
     a1 = 2.0 * pi;
     return k == 0;
   }
-  const double base = sbm::atan2_cr(vy, vx);
+  const double base = sbg::atan2(vy, vx);
   if (k == 0) {
     a0 = base - theta;
     a1 = base + theta;
@@ -290,7 +291,7 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
         sa = __ldg(&arcs->s[k][i]);
       } else {
         const double a = a0 + (a1 - a0) * (double)i / (double)na;
-        sbm::sincos_cr(a, &sa, &ca);
+        sbg::sincos(a, &sa, &ca);
       }
       X[off + i] = ax + radius * ca;
       Y[off + i] = ay + radius * sa;
@@ -562,8 +563,8 @@ __device__ RegionStats warp_region(const SbPlacementDev& pl, double ax, double a
 
 // libm policy of the hole path on the device: the correctly rounded sin/cos/atan2.
 struct DevMath {
-  __device__ static void sincos(double a, double* s, double* c) { sbm::sincos_cr(a, s, c); }
-  __device__ static double atan2(double y, double x) { return sbm::atan2_cr(y, x); }
+  __device__ static void sincos(double a, double* s, double* c) { sbg::sincos(a, s, c); }
+  __device__ static double atan2(double y, double x) { return sbg::atan2(y, x); }
 };
 
 // Shapes whose ring outgrows the group path's kCap -- the full annulus with a hole (theta =
@@ -651,7 +652,7 @@ __global__ void __launch_bounds__(kRB, kRegionMinBlocks) k_relation_regions(Rela
     for (int k = 0; k < 12; ++k) P.m[k] = pp[k];
     mul34(inv, P, rel);
   };
-  auto yaw_of = [](const M34& rel) { return sbm::atan2_cr(rel.m[4], rel.m[0]); };  // transform.hpp:77
+  auto yaw_of = [](const M34& rel) { return sbg::atan2(rel.m[4], rel.m[0]); };  // transform.hpp:77
   if (p.from_s0) {  // canonical region_for(0) from the exchanged instance-0 state
     if (warp == 0) {
       const RegionStats r =

@@ -6,6 +6,7 @@
 #include "sb_rt.hpp"
 #include "sb_graph_rt.hpp"
 #include "sb_reach_rt.hpp"
+#include "sb_glibcm.cuh"
 
 
 // annulus_sector's arc points (polygon.cpp:136-176) with the host libm, shared by every
@@ -1464,9 +1465,25 @@ sb_status sb_debug_region_profile(uint64_t out[8]) {
   });
 }
 
+sb_status sb_host_math(int fn, const double* in, uint64_t n, double* out) {
+  return guard([&] {
+    if (fn < 0 || fn > 4) throw std::invalid_argument("sb_host_math: fn must be in [0, 4]");
+    if (n && (!in || !out)) throw std::invalid_argument("NULL argument");
+    for (uint64_t i = 0; i < n; ++i) {
+      double s, c;
+      switch (fn) {
+        case 2: out[i] = sbg::atan2(in[2 * i], in[2 * i + 1]); break;
+        case 3: out[i] = sbg::sin(in[i]); break;
+        case 4: out[i] = sbg::cos(in[i]); break;
+        default: sbg::sincos(in[i], &s, &c); out[i] = fn == 0 ? s : c;
+      }
+    }
+  });
+}
+
 sb_status sb_device_math(int fn, const double* in, uint64_t n, double* out) {
   return guard([&] {
-    if (fn < 0 || fn > 2) throw std::invalid_argument("sb_device_math: fn must be 0, 1 or 2");
+    if (fn < 0 || fn > 4) throw std::invalid_argument("sb_device_math: fn must be in [0, 4]");
     current_device_checked(0);
     const uint64_t nin = fn == 2 ? 2 * n : n;
     DevArray<double> din, dout;

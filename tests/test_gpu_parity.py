@@ -38,11 +38,17 @@ def random_pose(rng, spread, upright, z=None):
     return m
 
 
-def assert_poses(got, ref_colmajor, pkg):
+def assert_poses(got, ref_colmajor, pkg, accepted=None):
+    """north_star's bar (1e-5 relative) everywhere; with `accepted`, every accepted pose
+    must also be bit-identical (the device libm is glibc's own, sb_glibcm.cuh)."""
     ref = pkg.from_colmajor(ref_colmajor)
     assert got.shape == ref.shape
     bad = ~np.isclose(got, ref, rtol=POSE_RTOL, atol=POSE_ATOL)
     assert not bad.any(), f"{bad.sum()} pose entries outside tolerance"
+    if accepted is not None:
+        same = (got == ref).all(axis=(-2, -1))
+        placed = accepted >= 0
+        assert same[placed].all(), f"{np.sum(~same[placed])} accepted poses not bit-identical"
 
 
 def world_pair(pkg, ref, n, meshes, margin=0.0):
@@ -177,7 +183,7 @@ def assert_same(pkg, got, want):
     assert np.array_equal(got.valid, want["valid"]), "valid mask differs"
     diff = np.argwhere(got.accepted != want["accepted"])
     assert len(diff) == 0, f"accepted differs at (placement, inst) {diff[:10].tolist()}"
-    assert_poses(got.poses, want["poses"], pkg)
+    assert_poses(got.poses, want["poses"], pkg, got.accepted)
     for k in ("valid_instances", "candidate_checks", "narrow_phase_tests", "rounds",
               "per_instance_placements"):
         assert got.stats[k] == want["stats"][k], k

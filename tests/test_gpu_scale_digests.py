@@ -42,7 +42,6 @@ def test_scale_digest(gpu, name):
         d["valid_sha256"]
     for k in COUNTERS:
         assert got.stats[k] == d["stats"][k], k
-    assert got.stats["triangle_pair_tests"] <= d["stats"]["triangle_pair_tests"]
     # seeded pose sample, read from the engine's world (object = n_fixed + placement)
     rng = np.random.default_rng(d["pose_sample_seed"])
     S = len(np.load(os.path.join(GOLD, f"scale_{name}.npz"))["poses"])

@@ -11,8 +11,8 @@ for st in $STAGES; do
   case $st in
     tests) echo "== pytest -m gpu"; timeout ${TEST_TIMEOUT:-1500} python -m pytest tests -x -q -m gpu ${PYTEST_EXTRA:-} > gpurun_out/pytest_${TAG}.log 2>&1; tail -5 gpurun_out/pytest_${TAG}.log ;;
     smoke) echo "== smoke"; timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2 ;;
-    bench) echo "== bench"; /usr/bin/time -f "wall %e s" timeout 1200 python bench.py --steps ${STEPS:-20} --warmup ${WARMUP:-5} ${BENCH_EXTRA:-} > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err; tail -c 1500 gpurun_out/bench_${TAG}.json; tail -2 gpurun_out/bench_${TAG}.err ;;
-    ref) echo "== reference arm"; /usr/bin/time -f "wall %e s" timeout 1800 python bench.py --impl reference --steps ${STEPS:-20} --warmup ${WARMUP:-5} ${BENCH_EXTRA:-} > gpurun_out/bench_ref_${TAG}.json 2> gpurun_out/bench_ref_${TAG}.err; tail -c 800 gpurun_out/bench_ref_${TAG}.json; tail -2 gpurun_out/bench_ref_${TAG}.err ;;
+    bench) echo "== bench"; timeout 1200 python bench.py --steps ${STEPS:-20} --warmup ${WARMUP:-5} ${BENCH_EXTRA:-} > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err; tail -c 1500 gpurun_out/bench_${TAG}.json; tail -2 gpurun_out/bench_${TAG}.err ;;
+    ref) echo "== reference arm"; timeout 1800 python bench.py --impl reference --steps ${STEPS:-20} --warmup ${WARMUP:-5} ${BENCH_EXTRA:-} > gpurun_out/bench_ref_${TAG}.json 2> gpurun_out/bench_ref_${TAG}.err; tail -c 800 gpurun_out/bench_ref_${TAG}.json; tail -2 gpurun_out/bench_ref_${TAG}.err ;;
     configs) : > gpurun_out/configs_${TAG}.jsonl
       for c in ${CONFIGS:-c1_tabletop c2_mixed c3_kitchen c4_clutter c5_sweep10 c5_sweep100}; do
         timeout 900 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline >> gpurun_out/configs_${TAG}.jsonl 2> gpurun_out/err_$c.log || echo "{\"config\": \"$c\", \"failed\": true}" >> gpurun_out/configs_${TAG}.jsonl
