@@ -162,6 +162,115 @@ __device__ __forceinline__ void lap(const PlaceParams& p, Fixed& F, int slot) {
   }
 }
 
+// A1 core for one slot (sampler.cpp:70-156 + the driver's pose compose): the position
+// (FIFO draw `draw`, or the counter stream make_stream(run_seed, {salt, "fall", inst, at}))
+// mapped through the support frame, the yaw, and pose = translation(p + z_off z) *
+// rotation_z(yaw) in the shim's operation order. Returns false when the region is empty
+// (placeable = 0: a failed attempt).
+__device__ __forceinline__ bool compose_candidate(const PlaceParams& p, const Sampling& S,
+                                                  uint64_t seed, uint64_t state0, uint32_t inst,
+                                                  int32_t at, uint64_t draw, M34& pose) {
+  const WorldView& w = p.w;
+  const SbPlacementDev& pl = p.pl;
+  const uint64_t gid = p.global_begin + inst;
+  double lx = 0.0, ly = 0.0;
+  if (S.fast) {
+    if (S.n == 0) return false;
+    Pcg r{state0};
+    // j-th drained point = j-th draw (sampler.cpp:30-43): 6j PCG steps in
+    r.advance(6ull * draw);
+    double u = r.next_double(), r1 = r.next_double(), r2 = r.next_double();
+    sbp::draw_point(S.tris, S.cum, S.n, u, r1, r2, lx, ly);
+  } else {
+    const int nti = __ldg(p.inst_n + inst);
+    if (nti == 0) return false;
+    // make_stream(run_seed, {salt, "fall", inst, attempt}) (sampler.cpp:117)
+    Pcg r = Pcg::seeded(stream_seed4(seed, pl.salt, kFallbackSalt, gid, static_cast<uint64_t>(at)));
+    double u = r.next_double(), r1 = r.next_double(), r2 = r.next_double();
+    const uint64_t off = (uint64_t)inst * p.inst_cap;
+    sbp::draw_point(p.inst_tris + off, p.inst_cum + off, nti, u, r1, r2, lx, ly);
+  }
+  M34 Sp;
+#pragma unroll
+  for (int k = 0; k < 12; ++k) Sp.m[k] = pl.support[k];
+  double px, py, pz;
+  xform(Sp, lx, ly, 0.0, px, py, pz);  // transform_point(support_world, (x, y, 0))
+  double yaw = 0.0;
+  if (pl.orientation == SB_ORIENT_UNIFORM_YAW) {  // sampler.cpp:140-141
+    Pcg r = Pcg::seeded(stream_seed4(seed, pl.salt, kYawSalt, gid, static_cast<uint64_t>(at)));
+    const double two_pi = 2.0 * 3.14159265358979323846;
+    yaw = 0.0 + (two_pi - 0.0) * r.next_double();
+  } else if (pl.orientation == SB_ORIENT_FACE_TO) {  // relationships.cpp:232-239
+    const double* tp = w.pose + sb_pose_off(w, pl.face_object, inst);
+    double dx = tp[3] - px, dy = tp[7] - py;
+    yaw = sqrt(dx * dx + dy * dy) < 1e-12 ? 0.0 : sbg::atan2(dy, dx);
+  }
+  double c, s;
+  sbg::sincos(yaw, &s, &c);  // rotation_z: std::cos / std::sin (transform.hpp:47)
+  M34 Tr, Rz;  // translation(p + z_off z) * rotation_z(yaw)
+#pragma unroll
+  for (int k = 0; k < 12; ++k) Tr.m[k] = Rz.m[k] = 0.0;
+  Tr.m[0] = Tr.m[5] = Tr.m[10] = 1.0;
+  Rz.m[10] = 1.0;
+  Tr.m[3] = px + 0.0;
+  Tr.m[7] = py + 0.0;
+  Tr.m[11] = pz + pl.z_off;
+  Rz.m[0] = c;
+  Rz.m[1] = -s;
+  Rz.m[4] = s;
+  Rz.m[5] = c;
+  mul34(Tr, Rz, pose);
+  return true;
+}
+
+// Fused placement_filter (reachability.cpp:164-190): the candidate frame's origin in the
+// instance's robot base frame must hit occ_any; an unreachable candidate is a failed
+// attempt that is not collision-checked (Appendix C item 8).
+__device__ __forceinline__ bool reach_ok(const PlaceParams& p, uint32_t inst, const M34& pose) {
+  M34 Bs, Bi;
+  const double* bp = p.reach_base + (size_t)inst * 12;
+#pragma unroll
+  for (int k = 0; k < 12; ++k) Bs.m[k] = __ldg(bp + k);
+  inverse_rigid(Bs, Bi);
+  double rx, ry, rz;
+  xform(Bi, pose.m[3], pose.m[7], pose.m[11], rx, ry, rz);
+  uint64_t ir, iz;
+  return reach_bin(p.reach_grid, rx, ry, rz, ir, iz) &&
+         reach_bit(p.reach_any, ir * p.reach_grid.nz + iz);
+}
+
+// Accept (update_transform, collision.cpp:408-412, + set_enabled): the candidate pose q
+// (row-major 3x4 as 6 double2) and its world box (min xyz, max xyz) become instance inst's
+// record of the placement's object; the attempt index and (optionally) the column-major
+// result pose are written.
+template <bool kGrid>
+__device__ __forceinline__ void accept_candidate(const PlaceParams& p, uint32_t inst, const double2 q[6],
+                                                 const double* box, int32_t attempt) {
+  const WorldView& w = p.w;
+  const SbPlacementDev& pl = p.pl;
+  double2* pp = reinterpret_cast<double2*>(w.pose + sb_pose_off(w, pl.object, inst));
+#pragma unroll
+  for (int k = 0; k < 6; ++k) pp[k] = q[k];
+  if (p.out16) {  // the result pose, column-major Mat4 (k_pose_colmajor layout)
+    const double* m = reinterpret_cast<const double*>(q);
+    double2* o = reinterpret_cast<double2*>(p.out16 + (size_t)inst * 16);
+    o[0] = make_double2(m[0], m[4]);
+    o[1] = make_double2(m[8], 0.0);
+    o[2] = make_double2(m[1], m[5]);
+    o[3] = make_double2(m[9], 0.0);
+    o[4] = make_double2(m[2], m[6]);
+    o[5] = make_double2(m[10], 0.0);
+    o[6] = make_double2(m[3], m[7]);
+    o[7] = make_double2(m[11], 1.0);
+  }
+  double2* bp = reinterpret_cast<double2*>(w.box + sb_box_off(w, pl.object, inst));
+#pragma unroll
+  for (int k = 0; k < 3; ++k) bp[k] = make_double2(box[2 * k], box[2 * k + 1]);
+  w.enabled[sb_word_off(w, pl.object >> 5, inst)] |= 1u << (pl.object & 31);
+  if (kGrid) cell_insert(p.grid, inst, pl.object, box, box + 3);
+  p.accepted[inst] = (int16_t)attempt;
+}
+
 // ---------------- B: warp per queued pair (warp w takes entries w, w + 8, ...). Pairs
 // behind a lower hit of their slot, or of a slot beyond their instance's lowest
 // confirmed-free attempt, are skipped before any data is staged; the next eligible pair's
@@ -256,33 +365,11 @@ __device__ uint32_t tile_round(const PlaceParams& p, const Sampling& S, const Sb
     const int e = v % (int)nt;  // attempt-major slots: v = s * nt + e
     const int32_t at = a + v / (int)nt;
     const uint32_t inst = T.list[e];
-    const uint64_t gid = p.global_begin + inst;
-    bool placeable = true;
-    double lx = 0.0, ly = 0.0;
-    if (S.fast) {
-      if (S.n == 0) {
-        placeable = false;
-      } else {
-        Pcg r{F.state0};
-        // j-th drained point = j-th draw (sampler.cpp:30-43). Slot v = s * nt + e is round
-        // a + s, rank e: draw draw_base + s * nt + e = draw_base + v while nobody accepts
-        // before round a + s (FIFO speculation, resolved in phase C).
-        r.advance(6ull * (draw_base + (uint64_t)v));
-        double u = r.next_double(), r1 = r.next_double(), r2 = r.next_double();
-        sbp::draw_point(S.tris, S.cum, S.n, u, r1, r2, lx, ly);
-      }
-    } else {
-      const int nti = __ldg(p.inst_n + inst);
-      if (nti == 0) {
-        placeable = false;
-      } else {  // make_stream(run_seed, {salt, "fall", inst, attempt}) (sampler.cpp:117)
-        Pcg r = Pcg::seeded(stream_seed4(F.seed, pl.salt, kFallbackSalt, gid,
-                                         static_cast<uint64_t>(at)));
-        double u = r.next_double(), r1 = r.next_double(), r2 = r.next_double();
-        const uint64_t off = (uint64_t)inst * p.inst_cap;
-        sbp::draw_point(p.inst_tris + off, p.inst_cum + off, nti, u, r1, r2, lx, ly);
-      }
-    }
+    // slot v = s * nt + e is round a + s, rank e: FIFO draw draw_base + s * nt + e =
+    // draw_base + v while nobody accepts before round a + s (speculation, resolved in C)
+    M34 pose;
+    const bool placeable = compose_candidate(p, S, F.seed, F.state0, inst, at,
+                                             draw_base + (uint64_t)v, pose);
     T.contact[v] = kFree;
     T.rem[v] = 0u;
     if (v < (int)nt) T.minfree[e] = W;
@@ -290,37 +377,6 @@ __device__ uint32_t tile_round(const PlaceParams& p, const Sampling& S, const Sb
     if (!placeable) {
       T.sflag[v] = kSlotUnplaceable;
     } else {
-      M34 Sp;
-#pragma unroll
-      for (int k = 0; k < 12; ++k) Sp.m[k] = pl.support[k];
-      double px, py, pz;
-      xform(Sp, lx, ly, 0.0, px, py, pz);  // transform_point(support_world, (x, y, 0))
-      double yaw = 0.0;
-      if (pl.orientation == SB_ORIENT_UNIFORM_YAW) {  // sampler.cpp:140-141
-        Pcg r = Pcg::seeded(
-            stream_seed4(F.seed, pl.salt, kYawSalt, gid, static_cast<uint64_t>(at)));
-        const double two_pi = 2.0 * 3.14159265358979323846;
-        yaw = 0.0 + (two_pi - 0.0) * r.next_double();
-      } else if (pl.orientation == SB_ORIENT_FACE_TO) {  // relationships.cpp:232-239
-        const double* tp = w.pose + sb_pose_off(w, pl.face_object, inst);
-        double dx = tp[3] - px, dy = tp[7] - py;
-        yaw = sqrt(dx * dx + dy * dy) < 1e-12 ? 0.0 : sbg::atan2(dy, dx);
-      }
-      double c, s;
-      sbg::sincos(yaw, &s, &c);  // rotation_z: std::cos / std::sin (transform.hpp:47)
-      M34 Tr, Rz, pose;  // translation(p + z_off z) * rotation_z(yaw)
-#pragma unroll
-      for (int k = 0; k < 12; ++k) Tr.m[k] = Rz.m[k] = 0.0;
-      Tr.m[0] = Tr.m[5] = Tr.m[10] = 1.0;
-      Rz.m[10] = 1.0;
-      Tr.m[3] = px + 0.0;
-      Tr.m[7] = py + 0.0;
-      Tr.m[11] = pz + pl.z_off;
-      Rz.m[0] = c;
-      Rz.m[1] = -s;
-      Rz.m[4] = s;
-      Rz.m[5] = c;
-      mul34(Tr, Rz, pose);
       double cmn[3], cmx[3];
       xform_aabb(pose, gA.box_c, gA.box_h, cmn, cmx);
       M34 inv;
@@ -338,20 +394,8 @@ __device__ uint32_t tile_round(const PlaceParams& p, const Sampling& S, const Sb
         T.box[6 * v + 3 + k] = cmx[k];
       }
       T.sflag[v] = kSlotChecked;
-      if constexpr (kReach) {  // fused placement_filter (reachability.cpp:164-190): the
-        // candidate frame's origin in the instance's robot base frame must hit occ_any;
-        // an unreachable candidate is a failed attempt that is not collision-checked
-        M34 Bs, Bi;
-        const double* bp = p.reach_base + (size_t)inst * 12;
-#pragma unroll
-        for (int k = 0; k < 12; ++k) Bs.m[k] = __ldg(bp + k);
-        inverse_rigid(Bs, Bi);
-        double rx, ry, rz;
-        xform(Bi, pose.m[3], pose.m[7], pose.m[11], rx, ry, rz);
-        uint64_t ir, iz;
-        const bool reach = reach_bin(p.reach_grid, rx, ry, rz, ir, iz) &&
-                           reach_bit(p.reach_any, ir * p.reach_grid.nz + iz);
-        if (!reach) T.sflag[v] = kSlotUnplaceable;
+      if constexpr (kReach) {
+        if (!reach_ok(p, inst, pose)) T.sflag[v] = kSlotUnplaceable;
       }
     }
   }
@@ -589,31 +633,11 @@ __device__ uint32_t tile_round(const PlaceParams& p, const Sampling& S, const Sb
         L.cnt.narrow += __popc(mk);
       }
       if (c == kFree) {  // update_transform (collision.cpp:408-412) + set_enabled
-        double2* pp = reinterpret_cast<double2*>(w.pose + sb_pose_off(w, pl.object, inst));
         double2 q[6];
 #pragma unroll
-        for (int k = 0; k < 6; ++k) {
+        for (int k = 0; k < 6; ++k)
           q[k] = __ldcg(reinterpret_cast<const double2*>(p.cpose + ((size_t)blockIdx.x * kB + v) * 12) + k);
-          pp[k] = q[k];
-        }
-        if (p.out16) {  // the result pose, column-major Mat4 (k_pose_colmajor layout)
-          const double* m = reinterpret_cast<const double*>(q);
-          double2* o = reinterpret_cast<double2*>(p.out16 + (size_t)inst * 16);
-          o[0] = make_double2(m[0], m[4]);
-          o[1] = make_double2(m[8], 0.0);
-          o[2] = make_double2(m[1], m[5]);
-          o[3] = make_double2(m[9], 0.0);
-          o[4] = make_double2(m[2], m[6]);
-          o[5] = make_double2(m[10], 0.0);
-          o[6] = make_double2(m[3], m[7]);
-          o[7] = make_double2(m[11], 1.0);
-        }
-        double2* bp = reinterpret_cast<double2*>(w.box + sb_box_off(w, pl.object, inst));
-#pragma unroll
-        for (int k = 0; k < 3; ++k) bp[k] = make_double2(T.box[6 * v + 2 * k], T.box[6 * v + 2 * k + 1]);
-        w.enabled[sb_word_off(w, pl.object >> 5, inst)] |= 1u << (pl.object & 31);
-        if (kGrid) cell_insert(p.grid, inst, pl.object, T.box + 6 * v, T.box + 6 * v + 3);
-        p.accepted[inst] = (int16_t)(a + s);
+        accept_candidate<kGrid>(p, inst, q, T.box + 6 * v, a + s);
         ++L.accepted;
         ok = true;
       }
@@ -843,24 +867,29 @@ __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_place(PlaceParams p
     if (timer) F.acc[6] += global_ns() - t6;
   } else {
     cg::grid_group grid = cg::this_grid();
-    for (uint32_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
-      const uint32_t n = tile_load_valid(p, T, F, t, p.tile_inst);
-      store_list(p, T, t, n, p.tile_cnt);
-      __syncthreads();
-    }
-    lap(p, F, 0);
-    grid.sync();
-    lap(p, F, 5);
     uint64_t draws = 0;
     int32_t a = 0;
+    if (p.start_round == 0) {
+      for (uint32_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+        const uint32_t n = tile_load_valid(p, T, F, t, p.tile_inst);
+        store_list(p, T, t, n, p.tile_cnt);
+        __syncthreads();
+      }
+      lap(p, F, 0);
+      grid.sync();
+      lap(p, F, 5);
+    } else {  // rounds < start_round ran in k_wide_*: their draws precede this round's
+      a = p.start_round;
+      draws = tile_prefix(p, p.tile_cnt, F);  // round 0's count (tile_cnt buffer 0)
+    }
     for (; a < p.attempts; ++a) {
       unsigned long long r0 = 0;
       if (p.dbg && threadIdx.x == 0) {
         r0 = global_ns();
         F.ta = F.tb = 0;
       }
-      uint64_t total =
-          fast_round<kGrid, kReach>(p, S, gA, T, F, a, draws, L, nullptr, p.ntiles <= gridDim.x);
+      uint64_t total = fast_round<kGrid, kReach>(p, S, gA, T, F, a, draws, L, nullptr,
+                                                 p.ntiles <= gridDim.x && a > p.start_round);
       if (total & kSoloFlag) {
         if (blockIdx.x == 0) solo_rounds<kGrid, kReach>(p, S, gA, T, F, a, draws, L);
         a = -1;  // tail done by CTA 0
@@ -969,6 +998,297 @@ __global__ void __launch_bounds__(kB) k_fast_finish(PlaceParams p, int32_t a) {
   }
 }
 
+// ---------------------------------------------------------------- wide round 0
+// The first attempt round of a FIFO placement carries every valid instance (C4: 262,144),
+// and nearly all of them accept there. It runs as three grid-wide kernels with no CTA
+// barrier between the phases and no grid barrier at all; the persistent kernel then takes
+// the survivors from round 1 on (k_place with start_round = 1). Slot of a round-0 entry:
+// tile * kB + position in the tile's (ascending) list, the tiles of k_fast_init.
+constexpr uint8_t kWideDone = 8;  // accepted in k_wide_sample: no object overlaps its box
+constexpr int kWideChunk = 8;     // narrow pairs a warp claims at a time
+
+// Exclusive prefix of the round-0 tile counts = each tile's first FIFO draw; resets the
+// pair counters. One block of kWideScanThreads.
+constexpr int kWideScanThreads = 1024;
+__global__ void __launch_bounds__(kWideScanThreads) k_wide_scan(PlaceParams p) {
+  using Scan = cub::BlockScan<uint32_t, kWideScanThreads>;
+  __shared__ typename Scan::TempStorage scan;
+  uint32_t running = 0;
+  for (uint32_t c0 = 0; c0 < p.ntiles; c0 += kWideScanThreads) {
+    const uint32_t t = c0 + threadIdx.x;
+    const uint32_t x = t < p.ntiles ? __ldcg(p.tile_cnt + t) : 0u;
+    uint32_t ex, agg;
+    Scan(scan).ExclusiveSum(x, ex, agg);
+    if (t < p.ntiles) p.w_toff[t] = running + ex;
+    running += agg;
+    __syncthreads();
+  }
+  if (threadIdx.x < 2) p.w_ctl[threadIdx.x] = 0ull;
+}
+
+// Thread per round-0 entry: sample + compose (A1), candidate box, broad phase over the
+// instance's enabled objects (the occupancy grid narrows them when kGrid). A candidate
+// that overlaps no object is free (collision.cpp:439-448 finds nothing) and is accepted
+// here; the others keep their pose / inverse / box / overlap bits in the slot scratch and
+// append one (slot, object) pair per overlap, ascending objects, for k_wide_narrow.
+template <bool kGrid, bool kReach>
+__global__ void __launch_bounds__(kB, 2) k_wide_sample(PlaceParams p) {
+  const uint32_t t = blockIdx.x;
+  const int e = threadIdx.x, lane = e & 31;
+  const WorldView& w = p.w;
+  const uint32_t n = __ldcg(p.tile_cnt + t);
+  const uint64_t seed = p.seed_dev ? __ldg(p.seed_dev) : p.run_seed;
+  const uint64_t state0 =
+      p.seed_dev ? Pcg::seeded(stream_seed2(seed, p.pl.salt, kCacheSalt)).state : p.fast_state0;
+  const Sampling S = resolve_sampling(p);
+  const int words = w.n_words;
+  Local L;
+  uint32_t ov[kGW];
+#pragma unroll
+  for (int wd = 0; wd < kGW; ++wd) ov[wd] = 0u;
+  uint32_t npairs = 0;
+  const size_t slot = (size_t)t * kB + e;
+  if (e < (int)n) {
+    const uint32_t inst = __ldcg(p.tile_list + (uint64_t)t * p.tile_inst + e);
+    M34 pose;
+    bool placeable = compose_candidate(p, S, seed, state0, inst, 0,
+                                       (uint64_t)__ldcg(p.w_toff + t) + (uint64_t)e, pose);
+    if constexpr (kReach) {
+      if (placeable) placeable = reach_ok(p, inst, pose);
+    }
+    ++L.sampled;
+    uint8_t flag = kSlotUnplaceable;
+    if (placeable) {
+      ++L.checked;
+      const SbGeom* gA = p.w.geoms + p.pl.geom;
+      double box[6];
+      {
+        double c[3], h[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          c[k] = __ldg(gA->box_c + k);
+          h[k] = __ldg(gA->box_h + k);
+        }
+        xform_aabb(pose, c, h, box, box + 3);
+      }
+      uint32_t cand[kGW];
+      if constexpr (kGrid) {  // OR of the cells the candidate box meets
+        const SbCellGrid& G = p.grid;
+#pragma unroll
+        for (int wd = 0; wd < kGW; ++wd) cand[wd] = 0u;
+        int cx0, cx1, cy0, cy1;
+        cell_range(G, box, box + 3, cx0, cx1, cy0, cy1);
+        const uint32_t* cb = G.cells + (uint64_t)inst * (uint64_t)(G.g * G.g) * words;
+        for (int cy = cy0; cy <= cy1; ++cy)
+          for (int cx = cx0; cx <= cx1; ++cx) {
+            const uint32_t* c = cb + (uint64_t)(cy * G.g + cx) * words;
+#pragma unroll
+            for (int wd = 0; wd < kGW; ++wd)
+              if (wd < words) cand[wd] |= __ldcg(c + wd);
+          }
+      } else {  // every enabled object
+#pragma unroll
+        for (int wd = 0; wd < kGW; ++wd)
+          cand[wd] = wd < words ? __ldcg(w.enabled + sb_word_off(w, wd, inst)) : 0u;
+      }
+      // AABB tests (aabb.hpp:29-33, margin 0), two box loads in flight
+#pragma unroll
+      for (int wd = 0; wd < kGW; ++wd) {
+        uint32_t m = cand[wd];
+        while (m) {
+          const int ob0 = 32 * wd + __ffs(m) - 1;
+          m &= m - 1u;
+          const int ob1 = m ? 32 * wd + __ffs(m) - 1 : -1;
+          if (m) m &= m - 1u;
+          const double2* b0p = reinterpret_cast<const double2*>(w.box + sb_box_off(w, ob0, inst));
+          const double2 a0 = __ldcg(b0p), a1 = __ldcg(b0p + 1), a2 = __ldcg(b0p + 2);
+          double2 c0 = a0, c1 = a1, c2 = a2;
+          if (ob1 >= 0) {
+            const double2* b1p = reinterpret_cast<const double2*>(w.box + sb_box_off(w, ob1, inst));
+            c0 = __ldcg(b1p);
+            c1 = __ldcg(b1p + 1);
+            c2 = __ldcg(b1p + 2);
+          }
+          ++L.cnt.broad;
+          if (box[0] <= a1.y && a0.x <= box[3] && box[1] <= a2.x && a0.y <= box[4] &&
+              box[2] <= a2.y && a1.x <= box[5])
+            ov[wd] |= 1u << (ob0 & 31);
+          if (ob1 >= 0) {
+            ++L.cnt.broad;
+            if (box[0] <= c1.y && c0.x <= box[3] && box[1] <= c2.x && c0.y <= box[4] &&
+                box[2] <= c2.y && c1.x <= box[5])
+              ov[wd] |= 1u << (ob1 & 31);
+          }
+        }
+      }
+#pragma unroll
+      for (int wd = 0; wd < kGW; ++wd) npairs += __popc(ov[wd]);
+      double2 q[6];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) q[k] = make_double2(pose.m[2 * k], pose.m[2 * k + 1]);
+      if (npairs == 0) {  // free: accept now
+        accept_candidate<kGrid>(p, inst, q, box, 0);
+        ++L.accepted;
+        flag = kWideDone;
+      } else {
+        M34 inv;
+        inverse_rigid(pose, inv);
+        double2* cp = reinterpret_cast<double2*>(p.w_pose + slot * 12);
+        double2* ci = reinterpret_cast<double2*>(p.w_inv + slot * 12);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+          cp[k] = q[k];
+          ci[k] = make_double2(inv.m[2 * k], inv.m[2 * k + 1]);
+        }
+        double2* bx = reinterpret_cast<double2*>(p.w_box + slot * 6);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) bx[k] = make_double2(box[2 * k], box[2 * k + 1]);
+        for (int wd = 0; wd < words; ++wd) p.w_ovm[slot * kGW + wd] = ov[wd];
+        p.w_contact[slot] = kFree;
+        flag = kSlotChecked;
+      }
+    }
+    p.w_flag[slot] = flag;
+  }
+  // warp-aggregated append of the pairs (slot << 8 | object), each entry's in ascending order
+  uint32_t incl = npairs;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, incl, d);
+    if (lane >= d) incl += y;
+  }
+  const uint32_t wtotal = __shfl_sync(kFull, incl, 31);
+  unsigned long long base = 0;
+  if (lane == 31 && wtotal) base = atomicAdd(p.w_ctl, (unsigned long long)wtotal);
+  base = __shfl_sync(kFull, base, 31);
+  if (npairs) {
+    uint64_t q = base + incl - npairs;
+#pragma unroll
+    for (int wd = 0; wd < kGW; ++wd) {
+      uint32_t m = ov[wd];
+      while (m) {
+        const int ob = 32 * wd + __ffs(m) - 1;
+        m &= m - 1u;
+        p.w_pairs[q++] = ((uint32_t)slot << 8) | (uint32_t)ob;
+      }
+    }
+  }
+  if (threadIdx.x == 0 && n) atomicMax(p.ctrl + kRounds, 1u);  // reference round count
+  flush(p, L);
+}
+
+// Warp per (slot, object) pair over the whole grid: the exact narrow phase (sb_warp.cuh)
+// with the pair's pose + geometry record staged one pair ahead; a pair behind a lower
+// hit of its slot is skipped (the reference stops at the first colliding object).
+__global__ void __launch_bounds__(kB) k_wide_narrow(PlaceParams p) {
+  __shared__ PlaceGeomCache gc;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const WorldView& w = p.w;
+  load_geom_cache(w, p.w.geoms[p.pl.geom], gc);
+  __syncthreads();
+  unsigned char* wsb = g_dsm + warp * p.ws_bytes;
+  const WarpScratchView ws = carve_scratch(wsb, p.max_tris, p.max_nodes);
+  const uint64_t np = __ldcg(p.w_ctl);
+  Local L;
+  auto skippable = [&](uint32_t ent) {
+    return *((volatile int32_t*)p.w_contact + (ent >> 8)) < (int32_t)(ent & 0xffu);
+  };
+  auto stage = [&](uint32_t ent, int buf) {
+    const uint32_t sl = ent >> 8, ob = ent & 0xffu;
+    const uint32_t inst = __ldcg(p.tile_list + (uint64_t)(sl / kB) * p.tile_inst + sl % kB);
+    warp_stage(w, obj_grec(w, (int32_t)ob), (int32_t)ob, inst, p.w_inv + (size_t)sl * 12,
+               stage_buf(wsb, p.max_tris, p.max_nodes, buf));
+  };
+  for (;;) {
+    unsigned long long q0 = 0;
+    if (lane == 0) q0 = atomicAdd(p.w_ctl + 1, (unsigned long long)kWideChunk);
+    q0 = __shfl_sync(kFull, q0, 0);
+    if (q0 >= np) break;
+    const uint64_t q1 = q0 + kWideChunk < np ? q0 + kWideChunk : np;
+    // next non-skippable pair of the chunk at or after q
+    auto next = [&](uint64_t q) {
+      while (q < q1 && skippable(__ldcg(p.w_pairs + q))) ++q;
+      return q;
+    };
+    int cur = 0;
+    uint64_t q = next(q0);
+    if (q < q1) stage(__ldcg(p.w_pairs + q), cur);
+    while (q < q1) {
+      const uint32_t ent = __ldcg(p.w_pairs + q);
+      const uint64_t q2 = next(q + 1);
+      if (q2 < q1) {
+        stage(__ldcg(p.w_pairs + q2), cur ^ 1);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncwarp();
+      if (!skippable(ent)) {
+        const int32_t ob = (int32_t)(ent & 0xffu);
+        const int4 gr = obj_grec(w, ob);
+        const bool hit = warp_collide(gc, stage_buf(wsb, p.max_tris, p.max_nodes, cur), gr.z, gr.w,
+                                      ws, L.cnt);
+        if (hit && lane == 0) atomicMin(p.w_contact + (ent >> 8), ob);
+      }
+      __syncwarp();
+      q = q2;
+      cur ^= 1;
+    }
+  }
+  flush(p, L);
+}
+
+// Thread per round-0 entry: first-valid accept of the slots that had pairs (contact still
+// free), the reference's narrow-test count up to the first hit, and the survivors
+// compacted in place into the tile's list with round 1's count (tile_cnt buffer 1).
+template <bool kGrid>
+__global__ void __launch_bounds__(kB) k_wide_accept(PlaceParams p) {
+  __shared__ typename BlockScan::TempStorage scan;
+  const uint32_t t = blockIdx.x;
+  const int e = threadIdx.x;
+  const uint32_t n = __ldcg(p.tile_cnt + t);
+  const int words = p.w.n_words;
+  Local L;
+  uint32_t keep = 0, inst = 0;
+  if (e < (int)n) {
+    const size_t slot = (size_t)t * kB + e;
+    inst = __ldcg(p.tile_list + (uint64_t)t * p.tile_inst + e);
+    const uint8_t flag = __ldcg(p.w_flag + slot);
+    if (flag == kSlotUnplaceable) {
+      keep = 1;
+    } else if (flag == kSlotChecked) {
+      const int32_t c = __ldcg(p.w_contact + slot);
+      for (int wd = 0; wd < words; ++wd) {  // narrow tests up to the first hit
+        uint32_t mk = __ldcg(p.w_ovm + slot * kGW + wd);
+        if (c != kFree) {
+          const int lim = c - 32 * wd;  // keep objects <= c
+          if (lim < 0) mk = 0;
+          else if (lim < 31) mk &= (2u << lim) - 1u;
+        }
+        L.cnt.narrow += __popc(mk);
+      }
+      if (c == kFree) {
+        double2 q[6];
+        double box[6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) q[k] = __ldcg(reinterpret_cast<const double2*>(p.w_pose + slot * 12) + k);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) box[k] = __ldcg(p.w_box + slot * 6 + k);
+        accept_candidate<kGrid>(p, inst, q, box, 0);
+        ++L.accepted;
+      } else {
+        keep = 1;
+      }
+    }
+  }
+  uint32_t rank, total;
+  BlockScan(scan).ExclusiveSum(keep, rank, total);
+  __syncthreads();  // every entry of the list has been read
+  if (keep) p.tile_list[(uint64_t)t * p.tile_inst + rank] = inst;
+  if (e == 0) p.tile_cnt[p.cnt_stride + t] = total;
+  flush(p, L);
+}
+
 void check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
 }
@@ -1058,6 +1378,30 @@ void place_fast_round(const PlaceParams& p, int32_t attempt, unsigned grid, size
   if (p.grid.g) r ? launch_fast_round<true, true>(p, attempt, grid, smem, s) : launch_fast_round<true, false>(p, attempt, grid, smem, s);
   else r ? launch_fast_round<false, true>(p, attempt, grid, smem, s) : launch_fast_round<false, false>(p, attempt, grid, smem, s);
   check(cudaGetLastError(), "k_fast_round");
+}
+
+size_t wide_narrow_smem(int ws_bytes) { return (size_t)kWarps * ws_bytes; }
+
+int place_wide_round0(const PlaceParams& p, unsigned init_grid, size_t init_smem, int num_sms,
+                      sb_stream_t s) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
+  place_fast_init(p, init_grid, init_smem, s);
+  k_wide_scan<<<1, kWideScanThreads, 0, st>>>(p);
+  check(cudaGetLastError(), "k_wide_scan");
+  const bool g = p.grid.g != 0, r = p.reach_any != nullptr;
+  if (g) r ? k_wide_sample<true, true><<<p.ntiles, kB, 0, st>>>(p) : k_wide_sample<true, false><<<p.ntiles, kB, 0, st>>>(p);
+  else r ? k_wide_sample<false, true><<<p.ntiles, kB, 0, st>>>(p) : k_wide_sample<false, false><<<p.ntiles, kB, 0, st>>>(p);
+  check(cudaGetLastError(), "k_wide_sample");
+  const size_t smem = wide_narrow_smem(p.ws_bytes);
+  set_smem((const void*)k_wide_narrow, smem);
+  int per = 0;
+  check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void*)k_wide_narrow, kB, smem), "occupancy");
+  k_wide_narrow<<<(unsigned)(per > 0 ? per : 1) * num_sms, kB, smem, st>>>(p);
+  check(cudaGetLastError(), "k_wide_narrow");
+  if (g) k_wide_accept<true><<<p.ntiles, kB, 0, st>>>(p);
+  else k_wide_accept<false><<<p.ntiles, kB, 0, st>>>(p);
+  check(cudaGetLastError(), "k_wide_accept");
+  return 5;
 }
 
 void place_fast_finish(const PlaceParams& p, int32_t attempt, unsigned grid, sb_stream_t s) {

@@ -96,6 +96,18 @@ struct PlaceParams {
   const unsigned long long* reach_any;  // occ_any bitset of the map, NULL = no filter
   ReachGrid reach_grid;
   const double* reach_base;             // [n][12] robot base per local instance (row-major)
+  // Wide round 0 (FIFO placements, place_wide_round0): k_place then starts at round
+  // start_round = 1 from the survivors k_wide_accept left in tile_cnt buffer 1.
+  int32_t start_round;
+  double* w_pose;                // [ntiles * kPlaceBlock][12] candidate pose per round-0 slot
+  double* w_inv;                 // [..][12] its inverse (narrow staging)
+  double* w_box;                 // [..][6]  its world AABB
+  int32_t* w_contact;            // [..] lowest colliding object, INT32_MAX = free
+  uint32_t* w_ovm;               // [..][8]  broad-phase overlap bits
+  uint8_t* w_flag;               // [..]     slot state
+  uint32_t* w_pairs;             // [<= n * n_objects] (slot << 8 | object)
+  uint32_t* w_toff;              // [ntiles] first FIFO draw of each tile
+  unsigned long long* w_ctl;     // [2] pairs appended / claimed
 };
 
 #ifndef SB_PLACE_BLOCK
@@ -122,6 +134,13 @@ void place_fast_init(const PlaceParams& p, unsigned grid, size_t smem, sb_stream
 void place_fast_round(const PlaceParams& p, int32_t attempt, unsigned grid, size_t smem,
                       sb_stream_t s);
 void place_fast_finish(const PlaceParams& p, int32_t attempt, unsigned grid, sb_stream_t s);
+// Single GPU, FIFO placement: round 0 as k_fast_init + k_wide_scan + k_wide_sample +
+// k_wide_narrow + k_wide_accept (no grid barrier); the caller then launches
+// place_persistent with p.start_round = 1. Returns the number of launches.
+int place_wide_round0(const PlaceParams& p, unsigned init_grid, size_t init_smem, int num_sms,
+                      sb_stream_t s);
+// Narrow-kernel dynamic shared memory (per-warp scratch) for the given ws_bytes.
+size_t wide_narrow_smem(int ws_bytes);
 // ctrl word receiving the survivor total of round `attempt` (fast path, sharded)
 #ifdef __CUDACC__
 __host__ __device__

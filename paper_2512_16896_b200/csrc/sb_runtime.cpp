@@ -411,6 +411,13 @@ struct sb_engine {
   DevArray<int16_t> d_accepted;
   DevArray<uint32_t> d_tile_list;   // [ntiles * tile_inst] survivors per tile
   DevArray<uint32_t> d_tile_cnt;    // [2][ntiles]
+  // wide round 0 (sbk::place_wide_round0) scratch, per round-0 slot (tile * kPlaceBlock + e)
+  bool use_wide = false;
+  DevArray<double> d_wpose, d_winv, d_wbox;
+  DevArray<int32_t> d_wcontact;
+  DevArray<uint32_t> d_wovm, d_wpairs, d_wtoff;
+  DevArray<uint8_t> d_wflag;
+  DevArray<unsigned long long> d_wctl;
   DevArray<double> d_cpose;         // [grid][kPlaceBlock][12] candidate poses
   DevArray<double> d_cinv;          // [grid][kPlaceBlock][12] their inverses
   DevArray<uint32_t> d_cells;       // broad-phase occupancy grid [n][g * g][words]
@@ -655,6 +662,24 @@ struct sb_engine {
     }
     d_tile_list.alloc(static_cast<size_t>(ntiles) * tile_inst);
     d_tile_cnt.alloc(2 * static_cast<size_t>(ntiles));
+    {  // wide round 0: single GPU, FIFO placements (no relation), enough instances
+      bool any_fifo = false;
+      for (const Placement& pl : places) any_fifo = any_fifo || pl.dev.anchor_object < 0;
+      use_wide = world_size == 1 && any_fifo && n >= 4096;
+      if (const char* e = std::getenv("SB_WIDE")) use_wide = world_size == 1 && any_fifo && std::atoi(e) != 0;
+      if (use_wide) {
+        const size_t slots = static_cast<size_t>(ntiles) * sbk::kPlaceBlock;
+        d_wpose.alloc(slots * 12);
+        d_winv.alloc(slots * 12);
+        d_wbox.alloc(slots * 6);
+        d_wcontact.alloc(slots);
+        d_wovm.alloc(slots * 8);
+        d_wflag.alloc(slots);
+        d_wpairs.alloc(std::max<size_t>(1, static_cast<size_t>(n) * world->view().n_objects));
+        d_wtoff.alloc(ntiles);
+        d_wctl.alloc(2);
+      }
+    }
     d_cpose.alloc(static_cast<size_t>(grid) * sbk::kPlaceBlock * 12);
     d_cinv.alloc(static_cast<size_t>(grid) * sbk::kPlaceBlock * 12);
     {  // occupancy grid over the supports' XY extent, widened by the largest object radius
@@ -941,6 +966,19 @@ struct sb_engine {
           pp.reach_base = reach[p].base->p;
         }
         if (world_size == 1) {
+          if (use_wide && !relation) {  // round 0 grid-wide, then the persistent kernel
+            pp.w_pose = d_wpose.p;
+            pp.w_inv = d_winv.p;
+            pp.w_box = d_wbox.p;
+            pp.w_contact = d_wcontact.p;
+            pp.w_ovm = d_wovm.p;
+            pp.w_flag = d_wflag.p;
+            pp.w_pairs = d_wpairs.p;
+            pp.w_toff = d_wtoff.p;
+            pp.w_ctl = d_wctl.p;
+            launches += sbk::place_wide_round0(pp, grid, smem, num_sms, s);
+            pp.start_round = 1;
+          }
           if (!sbk::place_persistent(pp, grid, smem, s))
             throw CudaError("cooperative launch of the placement kernel is not possible");
           ++launches;
