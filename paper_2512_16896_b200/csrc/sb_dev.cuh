@@ -77,6 +77,23 @@ struct Pcg {
   }
 };
 
+// LCG jump by whole fast-path draws (6 steps each) from a table of powers: entry
+// [k][d] = {mult, plus} of the map "advance 6 * d * 256^k steps"; the jumps commute, so
+// state(draw) = J3[b3] J2[b2] J1[b1] J0[b0] state0 for the bytes b of `draw` -- the same
+// state advance(6 * draw) reaches (modular arithmetic, bit-exact), in 4 multiply-adds
+// instead of ~21 squaring rounds. Built by pcg_jump_table_host; draws < 2^32.
+__device__ __forceinline__ uint64_t pcg_jump_draws(const uint64_t* table, uint64_t state, uint64_t draw) {
+#pragma unroll
+  for (int k = 0; k < SB_PCG_JUMP_LEVELS; ++k) {
+    const uint32_t d = static_cast<uint32_t>(draw >> (8 * k)) & 0xffu;
+    if (d) {
+      const ulonglong2 e = __ldg(reinterpret_cast<const ulonglong2*>(table) + (k * 256 + d));
+      state = e.x * state + e.y;
+    }
+  }
+  return state;
+}
+
 // make_stream(seed, {c0, c1, ...}) (rng.hpp:63-67)
 __host__ __device__ __forceinline__ uint64_t stream_seed2(uint64_t seed, uint64_t c0, uint64_t c1) {
   return mix64(mix64(mix64(seed) ^ c0) ^ c1);

@@ -124,14 +124,14 @@ __global__ void __launch_bounds__(kBlock) k_check_batch(WorldView w, int32_t geo
 }
 
 // generate() start: placement objects back to add_object state; valid = 1; accepted = -1.
+// generate() start: placement objects leave the world (enable bits), every instance is
+// valid, no attempt accepted. Poses / boxes of placement objects are left as they are:
+// a disabled object is never read by the collision check, and k_unaccepted_fixup gives
+// the objects a run leaves unaccepted the identity pose / local box at the end.
 __global__ void k_engine_reset(WorldView w, int32_t first_obj, int32_t n_obj, uint8_t* valid,
-                               int16_t* accepted, int32_t n_place, double* out16) {
+                               int16_t* accepted, int32_t n_place) {
   uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i >= w.n) return;
-  for (int32_t o = first_obj; o < first_obj + n_obj; ++o) {
-    store_identity(w, o, i);
-    store_local_box(w, o, i);
-  }
   for (int32_t wd = 0; wd < w.n_words; ++wd) {
     uint32_t clear = 0u;
     for (int32_t o = first_obj; o < first_obj + n_obj; ++o)
@@ -140,23 +140,37 @@ __global__ void k_engine_reset(WorldView w, int32_t first_obj, int32_t n_obj, ui
   }
   valid[i] = 1;
   for (int32_t p = 0; p < n_place; ++p) accepted[(uint64_t)p * w.n + i] = -1;
-  if (out16) {  // result poses start as the identity an unaccepted object keeps
-    for (int32_t p = 0; p < n_place; ++p) {
-      double2* o = reinterpret_cast<double2*>(out16 + ((uint64_t)p * w.n + i) * 16);
-#pragma unroll
-      for (int k = 0; k < 8; ++k)
-        o[k] = make_double2((2 * k) % 5 == 0 ? 1.0 : 0.0, (2 * k + 1) % 5 == 0 ? 1.0 : 0.0);
+}
+
+// generate() end: an object whose placement accepted nothing for instance i keeps the
+// state add_object gave it (collision.cpp:365-376): identity pose, local box.
+__global__ void k_unaccepted_fixup(WorldView w, int32_t first_obj, int32_t n_place,
+                                   const int16_t* accepted) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= w.n) return;
+  for (int32_t p = 0; p < n_place; ++p)
+    if (accepted[(uint64_t)p * w.n + i] < 0) {
+      store_identity(w, first_obj + p, i);
+      store_local_box(w, first_obj + p, i);
     }
-  }
+}
+
+// Result poses of one placement (column-major Mat4): the identity where nothing was
+// accepted (k_place writes the accepted ones at accept time).
+__global__ void k_out16_fixup(uint64_t n, const int16_t* accepted, double* out16) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= n || accepted[i] >= 0) return;
+  double2* o = reinterpret_cast<double2*>(out16 + i * 16);
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    o[k] = make_double2((2 * k) % 5 == 0 ? 1.0 : 0.0, (2 * k + 1) % 5 == 0 ? 1.0 : 0.0);
 }
 
 // Occupancy grid at generate() start: cells cleared, then the enabled fixed objects
 // (ids < first_obj) inserted from their world boxes. Thread per instance.
-__global__ void k_cells_reset(WorldView w, SbCellGrid G, int32_t first_obj) {
+__global__ void k_cells_insert_fixed(WorldView w, SbCellGrid G, int32_t first_obj) {
   const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i >= w.n) return;
-  uint32_t* c = G.cells + i * (uint64_t)(G.g * G.g) * G.words;
-  for (int k = 0; k < G.g * G.g * G.words; ++k) c[k] = 0u;
   for (int32_t o = 0; o < first_obj; ++o) {
     if (!((w.enabled[sb_word_off(w, o >> 5, i)] >> (o & 31)) & 1u)) continue;
     const double* b = w.box + sb_box_off(w, o, i);
@@ -370,13 +384,24 @@ void narrow_profile_check(unsigned long long out[8], bool reset) {
   }
 }
 void engine_reset(const SbWorldView& w, int32_t first_obj, int32_t n_obj, uint8_t* valid,
-                  int16_t* accepted, int32_t n_place, double* out16, sb_stream_t s) {
-  k_engine_reset<<<grid_for(w.n), kBlock, 0, s>>>(w, first_obj, n_obj, valid, accepted, n_place,
-                                                  out16);
+                  int16_t* accepted, int32_t n_place, sb_stream_t s) {
+  k_engine_reset<<<grid_for(w.n), kBlock, 0, s>>>(w, first_obj, n_obj, valid, accepted, n_place);
   check_launch("engine_reset");
 }
+void unaccepted_fixup(const SbWorldView& w, int32_t first_obj, int32_t n_place,
+                      const int16_t* accepted, sb_stream_t s) {
+  k_unaccepted_fixup<<<grid_for(w.n), kBlock, 0, s>>>(w, first_obj, n_place, accepted);
+  check_launch("unaccepted_fixup");
+}
+void out16_fixup(uint64_t n, const int16_t* accepted, double* out16, sb_stream_t s) {
+  k_out16_fixup<<<grid_for(n), kBlock, 0, s>>>(n, accepted, out16);
+  check_launch("out16_fixup");
+}
 void cells_reset(const SbWorldView& w, const SbCellGrid& g, int32_t first_obj, sb_stream_t s) {
-  k_cells_reset<<<grid_for(w.n), kBlock, 0, s>>>(w, g, first_obj);
+  const cudaError_t e = cudaMemsetAsync(g.cells, 0, w.n * (uint64_t)(g.g * g.g) * g.words * sizeof(uint32_t),
+                                        reinterpret_cast<cudaStream_t>(s));
+  if (e != cudaSuccess) throw std::runtime_error(std::string("cells memset: ") + cudaGetErrorString(e));
+  k_cells_insert_fixed<<<grid_for(w.n), kBlock, 0, s>>>(w, g, first_obj);
   check_launch("cells_reset");
 }
 void anchor_states(const SbWorldView& w, int32_t anchor_obj, const double inv_support[12],

@@ -34,9 +34,14 @@ void check_batch(const SbWorldView& w, int32_t geom, const double* poses16,
 void narrow_profile_check(unsigned long long out[8], bool reset);
 
 // engine bookkeeping
-// out16 (nullable): [n_place][n][16] result poses, set to the identity
 void engine_reset(const SbWorldView& w, int32_t first_obj, int32_t n_obj, uint8_t* valid,
-                  int16_t* accepted, int32_t n_place, double* out16, sb_stream_t s);
+                  int16_t* accepted, int32_t n_place, sb_stream_t s);
+// end of a run: identity pose + local box for every (placement object, instance) left
+// unaccepted (accepted: [n_place][n])
+void unaccepted_fixup(const SbWorldView& w, int32_t first_obj, int32_t n_place,
+                      const int16_t* accepted, sb_stream_t s);
+// one placement's column-major result poses [n][16]: identity where accepted[i] < 0
+void out16_fixup(uint64_t n, const int16_t* accepted, double* out16, sb_stream_t s);
 // broad-phase occupancy grid: clear, then insert the enabled fixed objects (ids < first_obj)
 void cells_reset(const SbWorldView& w, const SbCellGrid& g, int32_t first_obj, sb_stream_t s);
 // AnchorState per instance (support frame): out[3i..3i+2] = x, y, yaw

@@ -119,3 +119,28 @@ SB_HDI uint64_t sb_word_off(const SbWorldView& w, int32_t word, uint64_t inst) {
 #define SB_MAX_NODES_PER_GEOM 32   // effective DAG nodes (bitmask traversal width)
 #define SB_MAX_EFF_TRIS 32         // reachable triangles per geometry (pooled narrow phase)
 #define SB_REGION_MAX_VERTS 96     // per-instance constraint region ring capacity
+
+// PCG32 jump table of the FIFO fast path (sbd::pcg_jump_draws): entry [k][d] = {mult, plus}
+// of the LCG map "advance 6 * d * 256^k steps" (6 steps per polygon draw, rng.hpp:24-60;
+// Brown's arbitrary-stride jump), table[(k * 256 + d) * 2 + {0, 1}].
+#define SB_PCG_JUMP_LEVELS 4
+SB_HDI void sb_pcg_jump_entry(uint64_t delta, uint64_t* mult, uint64_t* plus) {
+  const uint64_t kMult = 6364136223846793005ULL, kInc = (0xda3e39cb94b95bdbULL << 1u) | 1u;
+  uint64_t cur_mult = kMult, cur_plus = kInc, acc_mult = 1u, acc_plus = 0u;
+  while (delta > 0) {
+    if (delta & 1u) {
+      acc_mult *= cur_mult;
+      acc_plus = acc_plus * cur_mult + cur_plus;
+    }
+    cur_plus = (cur_mult + 1u) * cur_plus;
+    cur_mult *= cur_mult;
+    delta >>= 1u;
+  }
+  *mult = acc_mult;
+  *plus = acc_plus;
+}
+inline void sb_pcg_jump_table_host(uint64_t* table) {
+  for (int k = 0; k < SB_PCG_JUMP_LEVELS; ++k)
+    for (uint64_t d = 0; d < 256; ++d)
+      sb_pcg_jump_entry(6u * (d << (8 * k)), &table[(k * 256 + d) * 2], &table[(k * 256 + d) * 2 + 1]);
+}

@@ -15,6 +15,12 @@
 #include "sb_poly.h"
 #include "sb_warp.cuh"
 
+#ifndef SB_WIDE_SAMPLE_MINB
+#define SB_WIDE_SAMPLE_MINB 3  // CTAs per SM k_wide_sample's register budget is sized for
+#endif
+#ifndef SB_WIDE_NARROW_MINB
+#define SB_WIDE_NARROW_MINB 3  // same for k_wide_narrow
+#endif
 #ifndef SB_PLACE_MIN_BLOCKS
 #define SB_PLACE_MIN_BLOCKS (512 / SB_PLACE_BLOCK)  // CTAs per SM the register budget is sized for
 #endif
@@ -176,9 +182,8 @@ __device__ __forceinline__ bool compose_candidate(const PlaceParams& p, const Sa
   double lx = 0.0, ly = 0.0;
   if (S.fast) {
     if (S.n == 0) return false;
-    Pcg r{state0};
     // j-th drained point = j-th draw (sampler.cpp:30-43): 6j PCG steps in
-    r.advance(6ull * draw);
+    Pcg r{pcg_jump_draws(p.jump, state0, draw)};
     double u = r.next_double(), r1 = r.next_double(), r2 = r.next_double();
     sbp::draw_point(S.tris, S.cum, S.n, u, r1, r2, lx, ly);
   } else {
@@ -1032,7 +1037,7 @@ __global__ void __launch_bounds__(kWideScanThreads) k_wide_scan(PlaceParams p) {
 // here; the others keep their pose / inverse / box / overlap bits in the slot scratch and
 // append one (slot, object) pair per overlap, ascending objects, for k_wide_narrow.
 template <bool kGrid, bool kReach>
-__global__ void __launch_bounds__(kB, 2) k_wide_sample(PlaceParams p) {
+__global__ void __launch_bounds__(kB, SB_WIDE_SAMPLE_MINB) k_wide_sample(PlaceParams p) {
   const uint32_t t = blockIdx.x;
   const int e = threadIdx.x, lane = e & 31;
   const WorldView& w = p.w;
@@ -1180,7 +1185,7 @@ __global__ void __launch_bounds__(kB, 2) k_wide_sample(PlaceParams p) {
 // Warp per (slot, object) pair over the whole grid: the exact narrow phase (sb_warp.cuh)
 // with the pair's pose + geometry record staged one pair ahead; a pair behind a lower
 // hit of its slot is skipped (the reference stops at the first colliding object).
-__global__ void __launch_bounds__(kB) k_wide_narrow(PlaceParams p) {
+__global__ void __launch_bounds__(kB, SB_WIDE_NARROW_MINB) k_wide_narrow(PlaceParams p) {
   __shared__ PlaceGeomCache gc;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const WorldView& w = p.w;

@@ -47,6 +47,7 @@ struct PlaceParams {
   const uint64_t* seed_dev;     // optional: run_seed read on the device (graph replays)
   uint64_t global_begin;
   uint64_t fast_state0;
+  const uint64_t* jump;         // pcg_jump_table_host: FIFO draw -> PCG state (draws < 2^32)
   const SbRegionTri* canon_tris;
   const double* canon_cum;
   int32_t canon_n;

@@ -418,6 +418,7 @@ struct sb_engine {
   DevArray<uint32_t> d_wovm, d_wpairs, d_wtoff;
   DevArray<uint8_t> d_wflag;
   DevArray<unsigned long long> d_wctl;
+  DevArray<uint64_t> d_jump;        // FIFO draw jump table (sbd::pcg_jump_table_host)
   DevArray<double> d_cpose;         // [grid][kPlaceBlock][12] candidate poses
   DevArray<double> d_cinv;          // [grid][kPlaceBlock][12] their inverses
   DevArray<uint32_t> d_cells;       // broad-phase occupancy grid [n][g * g][words]
@@ -680,6 +681,14 @@ struct sb_engine {
         d_wctl.alloc(2);
       }
     }
+    {
+      std::vector<uint64_t> jt(SB_PCG_JUMP_LEVELS * 256 * 2);
+      sb_pcg_jump_table_host(jt.data());
+      d_jump.alloc(jt.size());
+      cuda_check(cudaMemcpy(d_jump.p, jt.data(), jt.size() * 8, cudaMemcpyHostToDevice), "H2D jump");
+    }
+    if (static_cast<uint64_t>(n) * static_cast<uint64_t>(attempts) >= (1ull << 32))
+      throw std::invalid_argument("engine: variations x attempts per shard must stay below 2^32 draws");
     d_cpose.alloc(static_cast<size_t>(grid) * sbk::kPlaceBlock * 12);
     d_cinv.alloc(static_cast<size_t>(grid) * sbk::kPlaceBlock * 12);
     {  // occupancy grid over the supports' XY extent, widened by the largest object radius
@@ -886,7 +895,7 @@ struct sb_engine {
       cuda_check(cudaMemsetAsync(d_ctrl.p, 0, d_ctrl.count * sizeof(uint32_t), stream), "memset");
       cuda_check(cudaMemsetAsync(d_rflags.p, 0, d_rflags.count * sizeof(int32_t), stream), "memset");
       sbk::engine_reset(wv, first_place_obj, static_cast<int32_t>(P), d_valid.p, d_accepted.p,
-                        static_cast<int32_t>(P), pipe ? d_out16.p : nullptr, s);
+                        static_cast<int32_t>(P), s);
       launches += 1;
       if (cell_grid.g) {
         sbk::cells_reset(wv, cell_grid, first_place_obj, s);
@@ -928,6 +937,7 @@ struct sb_engine {
         pp.seed_dev = d_seed.p;
         pp.global_begin = begin;
         pp.fast_state0 = fast_state0;
+        pp.jump = d_jump.p;
         pp.canon_tris = canon_tris;
         pp.canon_cum = canon_cum;
         pp.canon_n = canon_n;
@@ -1096,6 +1106,10 @@ struct sb_engine {
             ++launches;
           }
         }
+        if (pipe) {  // identity result poses where placement p accepted nothing
+          sbk::out16_fixup(n, d_accepted.p + p * n, d_out16.p + p * 16 * n, s);
+          ++launches;
+        }
         if (pipe && capturing) {  // graph: the copy follows the launch (graph_copies)
           rec(ev_pose[p], true);
         } else if (pipe) {  // placement p is final: copy its poses behind an event
@@ -1107,6 +1121,9 @@ struct sb_engine {
                      "D2H poses");
         }
       }
+      // objects left unaccepted keep add_object's identity pose / local box
+      sbk::unaccepted_fixup(wv, first_place_obj, static_cast<int32_t>(P), d_accepted.p, s);
+      ++launches;
     };
     const bool graphable = world_size == 1 && !round_debug && !place_times && use_graphs;
     if (graphable) {
