@@ -1028,7 +1028,7 @@ __global__ void __launch_bounds__(kWideScanThreads) k_wide_scan(PlaceParams p) {
     running += agg;
     __syncthreads();
   }
-  if (threadIdx.x < 2) p.w_ctl[threadIdx.x] = 0ull;
+  if (threadIdx.x < 4) p.w_ctl[threadIdx.x] = 0ull;
 }
 
 // Thread per round-0 entry: sample + compose (A1), candidate box, broad phase over the
@@ -1182,6 +1182,98 @@ __global__ void __launch_bounds__(kB, SB_WIDE_SAMPLE_MINB) k_wide_sample(PlacePa
   flush(p, L);
 }
 
+// Thread per (slot, object) pair: the leaf-box filter of the narrow phase (warp_collide
+// step 2) on its own. other_in_cand = inv(cand) * pose(ob) and B's leaf boxes moved into
+// A's frame are computed with the very operations warp_collide uses, so "no leaf pair's
+// boxes overlap" here is exactly the case in which warp_collide returns false at step 2
+// -- such pairs never reach k_wide_narrow. Survivors are appended to the second list.
+// Pairs behind a lower hit of their slot cannot matter and are dropped as well.
+__global__ void __launch_bounds__(kB) k_wide_filter(PlaceParams p) {
+  __shared__ double abox[32][6];  // A's leaf boxes: min xyz, max xyz
+  __shared__ int nla;
+  const WorldView& w = p.w;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    const SbGeom gA = w.geoms[p.pl.geom];
+    int k = 0;
+    for (int nd = 0; nd < gA.n_nodes; ++nd) {
+      const SbNode& N = w.nodes[gA.node_offset + nd];
+      if (N.child0 >= 0) continue;
+      for (int c = 0; c < 3; ++c) {
+        abox[k][c] = N.bmin[c];
+        abox[k][3 + c] = N.bmax[c];
+      }
+      ++k;
+    }
+    nla = k;
+  }
+  __syncthreads();
+  const uint64_t np = __ldcg(p.w_ctl);
+  const int nA = nla;
+  Local L;
+  for (uint64_t q0 = (uint64_t)blockIdx.x * kB; q0 < np; q0 += (uint64_t)gridDim.x * kB) {
+    const uint64_t q = q0 + threadIdx.x;
+    bool pass = false;
+    uint32_t ent = 0;
+    if (q < np) {
+      ent = __ldcg(p.w_pairs + q);
+      const uint32_t sl = ent >> 8;
+      const int32_t ob = (int32_t)(ent & 0xffu);
+      if (*((volatile int32_t*)p.w_contact + sl) >= ob) {
+        const uint32_t inst = __ldcg(p.tile_list + (uint64_t)(sl / kB) * p.tile_inst + sl % kB);
+        double I[12], P[12];
+        const double2* ip = reinterpret_cast<const double2*>(p.w_inv + (size_t)sl * 12);
+        const double2* pp = reinterpret_cast<const double2*>(w.pose + sb_pose_off(w, ob, inst));
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+          const double2 a = __ldcg(ip + k), b = __ldcg(pp + k);
+          I[2 * k] = a.x;
+          I[2 * k + 1] = a.y;
+          P[2 * k] = b.x;
+          P[2 * k + 1] = b.y;
+        }
+        M34 M;  // warp_collide's other_in_cand, entry by entry (shim order)
+#pragma unroll
+        for (int e = 0; e < 12; ++e) {
+          const int i = e >> 2, j = e & 3;
+          double s = I[4 * i + 0] * P[j];
+          s = s + I[4 * i + 1] * P[4 + j];
+          s = s + I[4 * i + 2] * P[8 + j];
+          s = s + I[4 * i + 3] * (j == 3 ? 1.0 : 0.0);
+          M.m[e] = s;
+        }
+        const int4 gr = obj_grec(w, ob);
+        const unsigned char* rec = reinterpret_cast<const unsigned char*>(w.brec) + 16 * (size_t)gr.x;
+        const int nB = gr.z;
+        const uint32_t* info = reinterpret_cast<const uint32_t*>(rec + 48 * nB);
+        for (int b = 0; b < nB && !pass; ++b) {
+          if ((__ldg(info + 2 * b) & 0xffu) != 0xffu) continue;  // B leaf nodes only
+          const double* nbox = reinterpret_cast<const double*>(rec) + 6 * b;
+          double c[3], h[3], bmn[3], bmx[3];
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            c[k] = __ldg(nbox + k);
+            h[k] = __ldg(nbox + 3 + k);
+          }
+          xform_aabb(M, c, h, bmn, bmx);
+          for (int a = 0; a < nA && !pass; ++a)
+            pass = abox[a][0] <= bmx[0] && bmn[0] <= abox[a][3] && abox[a][1] <= bmx[1] &&
+                   bmn[1] <= abox[a][4] && abox[a][2] <= bmx[2] && bmn[2] <= abox[a][5];
+        }
+        ++L.cnt.nodes;
+      }
+    }
+    // warp-aggregated append of the survivors (order within the list is free: the narrow
+    // verdict is a min over objects)
+    const uint32_t m = __ballot_sync(kFull, pass);
+    unsigned long long base = 0;
+    if (lane == 0 && m) base = atomicAdd(p.w_ctl + 2, (unsigned long long)__popc(m));
+    base = __shfl_sync(kFull, base, 0);
+    if (pass) p.w_pairs2[base + __popc(m & ((1u << lane) - 1u))] = ent;
+  }
+  flush(p, L);
+}
+
 // Warp per (slot, object) pair over the whole grid: the exact narrow phase (sb_warp.cuh)
 // with the pair's pose + geometry record staged one pair ahead; a pair behind a lower
 // hit of its slot is skipped (the reference stops at the first colliding object).
@@ -1193,7 +1285,7 @@ __global__ void __launch_bounds__(kB, SB_WIDE_NARROW_MINB) k_wide_narrow(PlacePa
   __syncthreads();
   unsigned char* wsb = g_dsm + warp * p.ws_bytes;
   const WarpScratchView ws = carve_scratch(wsb, p.max_tris, p.max_nodes);
-  const uint64_t np = __ldcg(p.w_ctl);
+  const uint64_t np = __ldcg(p.w_ctl + 2);  // pairs past k_wide_filter
   Local L;
   auto skippable = [&](uint32_t ent) {
     return *((volatile int32_t*)p.w_contact + (ent >> 8)) < (int32_t)(ent & 0xffu);
@@ -1206,23 +1298,23 @@ __global__ void __launch_bounds__(kB, SB_WIDE_NARROW_MINB) k_wide_narrow(PlacePa
   };
   for (;;) {
     unsigned long long q0 = 0;
-    if (lane == 0) q0 = atomicAdd(p.w_ctl + 1, (unsigned long long)kWideChunk);
+    if (lane == 0) q0 = atomicAdd(p.w_ctl + 3, (unsigned long long)kWideChunk);
     q0 = __shfl_sync(kFull, q0, 0);
     if (q0 >= np) break;
     const uint64_t q1 = q0 + kWideChunk < np ? q0 + kWideChunk : np;
     // next non-skippable pair of the chunk at or after q
     auto next = [&](uint64_t q) {
-      while (q < q1 && skippable(__ldcg(p.w_pairs + q))) ++q;
+      while (q < q1 && skippable(__ldcg(p.w_pairs2 + q))) ++q;
       return q;
     };
     int cur = 0;
     uint64_t q = next(q0);
-    if (q < q1) stage(__ldcg(p.w_pairs + q), cur);
+    if (q < q1) stage(__ldcg(p.w_pairs2 + q), cur);
     while (q < q1) {
-      const uint32_t ent = __ldcg(p.w_pairs + q);
+      const uint32_t ent = __ldcg(p.w_pairs2 + q);
       const uint64_t q2 = next(q + 1);
       if (q2 < q1) {
-        stage(__ldcg(p.w_pairs + q2), cur ^ 1);
+        stage(__ldcg(p.w_pairs2 + q2), cur ^ 1);
         cp_async_wait<1>();
       } else {
         cp_async_wait<0>();
@@ -1397,6 +1489,12 @@ int place_wide_round0(const PlaceParams& p, unsigned init_grid, size_t init_smem
   if (g) r ? k_wide_sample<true, true><<<p.ntiles, kB, 0, st>>>(p) : k_wide_sample<true, false><<<p.ntiles, kB, 0, st>>>(p);
   else r ? k_wide_sample<false, true><<<p.ntiles, kB, 0, st>>>(p) : k_wide_sample<false, false><<<p.ntiles, kB, 0, st>>>(p);
   check(cudaGetLastError(), "k_wide_sample");
+  {
+    int per = 0;
+    check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void*)k_wide_filter, kB, 0), "occupancy");
+    k_wide_filter<<<(unsigned)(per > 0 ? per : 1) * num_sms, kB, 0, st>>>(p);
+    check(cudaGetLastError(), "k_wide_filter");
+  }
   const size_t smem = wide_narrow_smem(p.ws_bytes);
   set_smem((const void*)k_wide_narrow, smem);
   int per = 0;
@@ -1406,7 +1504,7 @@ int place_wide_round0(const PlaceParams& p, unsigned init_grid, size_t init_smem
   if (g) k_wide_accept<true><<<p.ntiles, kB, 0, st>>>(p);
   else k_wide_accept<false><<<p.ntiles, kB, 0, st>>>(p);
   check(cudaGetLastError(), "k_wide_accept");
-  return 5;
+  return 6;
 }
 
 void place_fast_finish(const PlaceParams& p, int32_t attempt, unsigned grid, sb_stream_t s) {

@@ -107,8 +107,9 @@ struct PlaceParams {
   uint32_t* w_ovm;               // [..][8]  broad-phase overlap bits
   uint8_t* w_flag;               // [..]     slot state
   uint32_t* w_pairs;             // [<= n * n_objects] (slot << 8 | object)
+  uint32_t* w_pairs2;            // [same] the pairs past the leaf-box filter
   uint32_t* w_toff;              // [ntiles] first FIFO draw of each tile
-  unsigned long long* w_ctl;     // [2] pairs appended / claimed
+  unsigned long long* w_ctl;     // [4] pairs appended, -, filtered pairs appended / claimed
 };
 
 #ifndef SB_PLACE_BLOCK

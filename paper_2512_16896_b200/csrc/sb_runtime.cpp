@@ -415,7 +415,7 @@ struct sb_engine {
   bool use_wide = false;
   DevArray<double> d_wpose, d_winv, d_wbox;
   DevArray<int32_t> d_wcontact;
-  DevArray<uint32_t> d_wovm, d_wpairs, d_wtoff;
+  DevArray<uint32_t> d_wovm, d_wpairs, d_wpairs2, d_wtoff;
   DevArray<uint8_t> d_wflag;
   DevArray<unsigned long long> d_wctl;
   DevArray<uint64_t> d_jump;        // FIFO draw jump table (sbd::pcg_jump_table_host)
@@ -677,8 +677,9 @@ struct sb_engine {
         d_wovm.alloc(slots * 8);
         d_wflag.alloc(slots);
         d_wpairs.alloc(std::max<size_t>(1, static_cast<size_t>(n) * world->view().n_objects));
+        d_wpairs2.alloc(d_wpairs.count);
         d_wtoff.alloc(ntiles);
-        d_wctl.alloc(2);
+        d_wctl.alloc(4);
       }
     }
     {
@@ -984,6 +985,7 @@ struct sb_engine {
             pp.w_ovm = d_wovm.p;
             pp.w_flag = d_wflag.p;
             pp.w_pairs = d_wpairs.p;
+            pp.w_pairs2 = d_wpairs2.p;
             pp.w_toff = d_wtoff.p;
             pp.w_ctl = d_wctl.p;
             launches += sbk::place_wide_round0(pp, grid, smem, num_sms, s);
