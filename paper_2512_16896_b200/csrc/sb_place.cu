@@ -1077,53 +1077,70 @@ __global__ void __launch_bounds__(kB, SB_WIDE_SAMPLE_MINB) k_wide_sample(PlacePa
         xform_aabb(pose, c, h, box, box + 3);
       }
       uint32_t cand[kGW];
-      if constexpr (kGrid) {  // OR of the cells the candidate box meets
-        const SbCellGrid& G = p.grid;
 #pragma unroll
-        for (int wd = 0; wd < kGW; ++wd) cand[wd] = 0u;
+      for (int wd = 0; wd < kGW; ++wd) cand[wd] = 0u;
+      if constexpr (kGrid) {  // OR of the cells the candidate box meets, 4 cells' loads at once
+        const SbCellGrid& G = p.grid;
         int cx0, cx1, cy0, cy1;
         cell_range(G, box, box + 3, cx0, cx1, cy0, cy1);
+        const int nx = cx1 - cx0 + 1, ncell = nx * (cy1 - cy0 + 1);
         const uint32_t* cb = G.cells + (uint64_t)inst * (uint64_t)(G.g * G.g) * words;
-        for (int cy = cy0; cy <= cy1; ++cy)
-          for (int cx = cx0; cx <= cx1; ++cx) {
-            const uint32_t* c = cb + (uint64_t)(cy * G.g + cx) * words;
+        for (int c0 = 0; c0 < ncell; c0 += 4)
 #pragma unroll
-            for (int wd = 0; wd < kGW; ++wd)
-              if (wd < words) cand[wd] |= __ldcg(c + wd);
+          for (int wg = 0; wg < kGW; wg += 4) {  // words [wg, wg + 4) of 4 cells
+            if (wg >= words) break;
+            uint32_t v[4][4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int ci = c0 + u;
+              const int cy = cy0 + ci / nx, cx = cx0 + ci % nx;
+              const uint32_t* c = cb + (uint64_t)(cy * G.g + cx) * words + wg;
+#pragma unroll
+              for (int j = 0; j < 4; ++j) v[u][j] = (ci < ncell && wg + j < words) ? __ldcg(c + j) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+              for (int j = 0; j < 4; ++j) cand[wg + j] |= v[u][j];
           }
       } else {  // every enabled object
 #pragma unroll
         for (int wd = 0; wd < kGW; ++wd)
           cand[wd] = wd < words ? __ldcg(w.enabled + sb_word_off(w, wd, inst)) : 0u;
       }
-      // AABB tests (aabb.hpp:29-33, margin 0), two box loads in flight
+      // AABB tests (aabb.hpp:29-33, margin 0), four box loads in flight
+      {
+        int wd = 0;
+        uint32_t m = cand[0];
+        for (;;) {
+          int obs[4];
+          int k = 0;
+          while (k < 4) {
+            while (!m && wd + 1 < kGW) m = cand[++wd];
+            if (!m) break;
+            obs[k++] = 32 * wd + __ffs(m) - 1;
+            m &= m - 1u;
+          }
+          if (k == 0) break;
+          double2 bx[4][3];
 #pragma unroll
-      for (int wd = 0; wd < kGW; ++wd) {
-        uint32_t m = cand[wd];
-        while (m) {
-          const int ob0 = 32 * wd + __ffs(m) - 1;
-          m &= m - 1u;
-          const int ob1 = m ? 32 * wd + __ffs(m) - 1 : -1;
-          if (m) m &= m - 1u;
-          const double2* b0p = reinterpret_cast<const double2*>(w.box + sb_box_off(w, ob0, inst));
-          const double2 a0 = __ldcg(b0p), a1 = __ldcg(b0p + 1), a2 = __ldcg(b0p + 2);
-          double2 c0 = a0, c1 = a1, c2 = a2;
-          if (ob1 >= 0) {
-            const double2* b1p = reinterpret_cast<const double2*>(w.box + sb_box_off(w, ob1, inst));
-            c0 = __ldcg(b1p);
-            c1 = __ldcg(b1p + 1);
-            c2 = __ldcg(b1p + 2);
-          }
-          ++L.cnt.broad;
-          if (box[0] <= a1.y && a0.x <= box[3] && box[1] <= a2.x && a0.y <= box[4] &&
-              box[2] <= a2.y && a1.x <= box[5])
-            ov[wd] |= 1u << (ob0 & 31);
-          if (ob1 >= 0) {
-            ++L.cnt.broad;
-            if (box[0] <= c1.y && c0.x <= box[3] && box[1] <= c2.x && c0.y <= box[4] &&
-                box[2] <= c2.y && c1.x <= box[5])
-              ov[wd] |= 1u << (ob1 & 31);
-          }
+          for (int u = 0; u < 4; ++u)
+            if (u < k) {
+              const double2* bp = reinterpret_cast<const double2*>(w.box + sb_box_off(w, obs[u], inst));
+              bx[u][0] = __ldcg(bp);
+              bx[u][1] = __ldcg(bp + 1);
+              bx[u][2] = __ldcg(bp + 2);
+            }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (u < k) {
+              ++L.cnt.broad;
+              const double2 a0 = bx[u][0], a1 = bx[u][1], a2 = bx[u][2];
+              if (box[0] <= a1.y && a0.x <= box[3] && box[1] <= a2.x && a0.y <= box[4] &&
+                  box[2] <= a2.y && a1.x <= box[5])
+                ov[obs[u] >> 5] |= 1u << (obs[u] & 31);
+            }
+          if (k < 4) break;
         }
       }
 #pragma unroll
@@ -1260,7 +1277,6 @@ __global__ void __launch_bounds__(kB) k_wide_filter(PlaceParams p) {
             pass = abox[a][0] <= bmx[0] && bmn[0] <= abox[a][3] && abox[a][1] <= bmx[1] &&
                    bmn[1] <= abox[a][4] && abox[a][2] <= bmx[2] && bmn[2] <= abox[a][5];
         }
-        ++L.cnt.nodes;
       }
     }
     // warp-aggregated append of the survivors (order within the list is free: the narrow

@@ -28,6 +28,7 @@ for cub in sorted(os.listdir(tmp)):
     dis = subprocess.run(["nvdisasm", "-gi", os.path.join(tmp, cub)], capture_output=True, text=True).stdout
     sec = None
     cur_inner = cur_outer = None
+    in_block = False
     for ln in dis.splitlines():
         m = re.match(r"\s*\.section\s+\.text\.(\S+),", ln)
         if m:
@@ -36,12 +37,16 @@ for cub in sorted(os.listdir(tmp)):
         if sec is None or kname not in sec:
             continue
         m = re.match(r'\s*//## File "([^"]+)", line (\d+)(?: inlined at "([^"]+)", line (\d+))?', ln)
-        if m:
-            cur_inner = f"{os.path.basename(m.group(1))}:{m.group(2)}"
-            cur_outer = f"{os.path.basename(m.group(3))}:{m.group(4)}" if m.group(3) else cur_inner
+        if m:  # the first annotation of a block is the innermost frame, the last the kernel's
+            here = f"{os.path.basename(m.group(1))}:{m.group(2)}"
+            if not in_block:
+                cur_inner = here
+                in_block = True
+            cur_outer = here if not m.group(3) else f"{os.path.basename(m.group(3))}:{m.group(4)}"
             continue
         m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", ln)
         if m and cur_inner:
+            in_block = False
             lines_of[int(m.group(1), 16)] = (cur_inner, cur_outer)
     if lines_of:
         break
