@@ -3,6 +3,7 @@
 #include <cub/block/block_scan.cuh>
 
 #include <climits>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -885,7 +886,7 @@ __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_place(PlaceParams p
       lap(p, F, 5);
     } else {  // rounds < start_round ran in k_wide_*: their draws precede this round's
       a = p.start_round;
-      draws = tile_prefix(p, p.tile_cnt, F);  // round 0's count (tile_cnt buffer 0)
+      draws = __ldcg(p.start_draws);
     }
     for (; a < p.attempts; ++a) {
       unsigned long long r0 = 0;
@@ -1015,20 +1016,27 @@ constexpr int kWideChunk = 8;     // narrow pairs a warp claims at a time
 // Exclusive prefix of the round-0 tile counts = each tile's first FIFO draw; resets the
 // pair counters. One block of kWideScanThreads.
 constexpr int kWideScanThreads = 1024;
-__global__ void __launch_bounds__(kWideScanThreads) k_wide_scan(PlaceParams p) {
+// buf 0: round 0's counts (draw offsets, pair counters reset); buf 1: round 1's survivors
+// (offsets for k_wide_spread, total S into w_ctl[5]).
+__global__ void __launch_bounds__(kWideScanThreads) k_wide_scan(PlaceParams p, int buf) {
   using Scan = cub::BlockScan<uint32_t, kWideScanThreads>;
   __shared__ typename Scan::TempStorage scan;
   uint32_t running = 0;
   for (uint32_t c0 = 0; c0 < p.ntiles; c0 += kWideScanThreads) {
     const uint32_t t = c0 + threadIdx.x;
-    const uint32_t x = t < p.ntiles ? __ldcg(p.tile_cnt + t) : 0u;
+    const uint32_t x = t < p.ntiles ? __ldcg(p.tile_cnt + (size_t)buf * p.cnt_stride + t) : 0u;
     uint32_t ex, agg;
     Scan(scan).ExclusiveSum(x, ex, agg);
     if (t < p.ntiles) p.w_toff[t] = running + ex;
     running += agg;
     __syncthreads();
   }
-  if (threadIdx.x < 4) p.w_ctl[threadIdx.x] = 0ull;
+  if (buf == 0) {
+    if (threadIdx.x < 4) p.w_ctl[threadIdx.x] = 0ull;
+    if (threadIdx.x == 0) p.w_ctl[4] = running;  // round 0's draws (k_place: start_draws)
+  } else if (threadIdx.x == 0) {
+    p.w_ctl[5] = running;  // round 1's active instances
+  }
 }
 
 // Thread per round-0 entry: sample + compose (A1), candidate box, broad phase over the
@@ -1402,6 +1410,30 @@ __global__ void __launch_bounds__(kB) k_wide_accept(PlaceParams p) {
   flush(p, L);
 }
 
+// Round 1's survivors (S, ascending in tile order) re-dealt over `gridDim` tiles of
+// q = min(ceil(S / min(grid, ntiles)), tile_inst) consecutive entries each, so every CTA of the persistent kernel
+// gets a share (rounds >= 1 are few instances; one CTA's narrow phase is serial per warp):
+// survivor of old tile t at position e has global rank toff[t] + e and goes to tile
+// rank / q, entry rank % q (tile_list2, tile_cnt2 buffer 1). Block per old tile; the
+// counts of all new tiles are written by a grid-stride loop.
+__global__ void __launch_bounds__(kB) k_wide_spread(PlaceParams p, unsigned grid) {
+  const unsigned long long S = __ldcg(p.w_ctl + 5);
+  if (grid > p.ntiles) grid = p.ntiles;  // S / q tiles must exist
+  unsigned long long q = S ? (S + grid - 1) / grid : 1;  // at most one tile's capacity
+  if (q > (unsigned long long)p.tile_inst) q = p.tile_inst;
+  const uint32_t t = blockIdx.x;
+  const uint32_t n = __ldcg(p.tile_cnt + p.cnt_stride + t);
+  const unsigned long long off = __ldcg(p.w_toff + t);
+  for (uint32_t e = threadIdx.x; e < n; e += kB) {
+    const unsigned long long r = off + e;
+    p.w_list2[(r / q) * p.tile_inst + r % q] = __ldcg(p.tile_list + (uint64_t)t * p.tile_inst + e);
+  }
+  for (uint32_t k = blockIdx.x * kB + threadIdx.x; k < p.ntiles; k += gridDim.x * kB) {
+    const unsigned long long lo = (unsigned long long)k * q;
+    p.w_cnt2[p.cnt_stride + k] = S > lo ? (uint32_t)(S - lo < q ? S - lo : q) : 0u;
+  }
+}
+
 void check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
 }
@@ -1499,7 +1531,7 @@ int place_wide_round0(const PlaceParams& p, unsigned init_grid, size_t init_smem
                       sb_stream_t s) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
   place_fast_init(p, init_grid, init_smem, s);
-  k_wide_scan<<<1, kWideScanThreads, 0, st>>>(p);
+  k_wide_scan<<<1, kWideScanThreads, 0, st>>>(p, 0);
   check(cudaGetLastError(), "k_wide_scan");
   const bool g = p.grid.g != 0, r = p.reach_any != nullptr;
   if (g) r ? k_wide_sample<true, true><<<p.ntiles, kB, 0, st>>>(p) : k_wide_sample<true, false><<<p.ntiles, kB, 0, st>>>(p);
@@ -1520,7 +1552,13 @@ int place_wide_round0(const PlaceParams& p, unsigned init_grid, size_t init_smem
   if (g) k_wide_accept<true><<<p.ntiles, kB, 0, st>>>(p);
   else k_wide_accept<false><<<p.ntiles, kB, 0, st>>>(p);
   check(cudaGetLastError(), "k_wide_accept");
-  return 6;
+  k_wide_scan<<<1, kWideScanThreads, 0, st>>>(p, 1);
+  check(cudaGetLastError(), "k_wide_scan");
+  unsigned spread = init_grid;  // SB_SPREAD=0: pack round 1 into full tiles instead
+  if (const char* e = std::getenv("SB_SPREAD")) spread = std::atoi(e) ? init_grid : 1u;
+  k_wide_spread<<<p.ntiles, kB, 0, st>>>(p, spread);
+  check(cudaGetLastError(), "k_wide_spread");
+  return 8;
 }
 
 void place_fast_finish(const PlaceParams& p, int32_t attempt, unsigned grid, sb_stream_t s) {

@@ -100,6 +100,7 @@ struct PlaceParams {
   // Wide round 0 (FIFO placements, place_wide_round0): k_place then starts at round
   // start_round = 1 from the survivors k_wide_accept left in tile_cnt buffer 1.
   int32_t start_round;
+  const unsigned long long* start_draws;  // draws of the rounds before start_round
   double* w_pose;                // [ntiles * kPlaceBlock][12] candidate pose per round-0 slot
   double* w_inv;                 // [..][12] its inverse (narrow staging)
   double* w_box;                 // [..][6]  its world AABB
@@ -109,7 +110,10 @@ struct PlaceParams {
   uint32_t* w_pairs;             // [<= n * n_objects] (slot << 8 | object)
   uint32_t* w_pairs2;            // [same] the pairs past the leaf-box filter
   uint32_t* w_toff;              // [ntiles] first FIFO draw of each tile
-  unsigned long long* w_ctl;     // [4] pairs appended, -, filtered pairs appended / claimed
+  unsigned long long* w_ctl;     // [6] pairs appended, -, filtered pairs appended / claimed,
+                                 // round-0 draws, round-1 active instances
+  uint32_t* w_list2;             // [ntiles * tile_inst] round 1's active list, re-dealt
+  uint32_t* w_cnt2;              // [2][cnt_stride] its tile counts (buffer 1 = round 1)
 };
 
 #ifndef SB_PLACE_BLOCK

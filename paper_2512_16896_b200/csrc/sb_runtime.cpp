@@ -415,7 +415,8 @@ struct sb_engine {
   bool use_wide = false;
   DevArray<double> d_wpose, d_winv, d_wbox;
   DevArray<int32_t> d_wcontact;
-  DevArray<uint32_t> d_wovm, d_wpairs, d_wpairs2, d_wtoff;
+  DevArray<uint32_t> d_wovm, d_wpairs, d_wpairs2, d_wtoff, d_wlist2;
+  DevArray<uint32_t> d_wcnt2;
   DevArray<uint8_t> d_wflag;
   DevArray<unsigned long long> d_wctl;
   DevArray<uint64_t> d_jump;        // FIFO draw jump table (sbd::pcg_jump_table_host)
@@ -666,7 +667,7 @@ struct sb_engine {
     {  // wide round 0: single GPU, FIFO placements (no relation), enough instances
       bool any_fifo = false;
       for (const Placement& pl : places) any_fifo = any_fifo || pl.dev.anchor_object < 0;
-      use_wide = world_size == 1 && any_fifo && n >= 4096;
+      use_wide = world_size == 1 && any_fifo && n >= 131072;  // measured: slower below (C2, C3)
       if (const char* e = std::getenv("SB_WIDE")) use_wide = world_size == 1 && any_fifo && std::atoi(e) != 0;
       if (use_wide) {
         const size_t slots = static_cast<size_t>(ntiles) * sbk::kPlaceBlock;
@@ -679,7 +680,9 @@ struct sb_engine {
         d_wpairs.alloc(std::max<size_t>(1, static_cast<size_t>(n) * world->view().n_objects));
         d_wpairs2.alloc(d_wpairs.count);
         d_wtoff.alloc(ntiles);
-        d_wctl.alloc(4);
+        d_wctl.alloc(8);
+        d_wcnt2.alloc(2 * static_cast<size_t>(ntiles));
+        d_wlist2.alloc(static_cast<size_t>(ntiles) * tile_inst);
       }
     }
     {
@@ -988,8 +991,13 @@ struct sb_engine {
             pp.w_pairs2 = d_wpairs2.p;
             pp.w_toff = d_wtoff.p;
             pp.w_ctl = d_wctl.p;
+            pp.w_list2 = d_wlist2.p;
+            pp.w_cnt2 = d_wcnt2.p;
             launches += sbk::place_wide_round0(pp, grid, smem, num_sms, s);
-            pp.start_round = 1;
+            pp.start_round = 1;  // rounds 1.. on the re-dealt survivor list
+            pp.start_draws = d_wctl.p + 4;
+            pp.tile_list = d_wlist2.p;
+            pp.tile_cnt = d_wcnt2.p;
           }
           if (!sbk::place_persistent(pp, grid, smem, s))
             throw CudaError("cooperative launch of the placement kernel is not possible");
