@@ -277,6 +277,58 @@ __device__ __forceinline__ void accept_candidate(const PlaceParams& p, uint32_t 
   p.accepted[inst] = (int16_t)attempt;
 }
 
+// Leaf-box filter of one (candidate, object) pair, thread-level: warp_collide's step 2 on
+// its own. other_in_cand = inv(cand) * pose(ob) and B's leaf boxes moved into A's frame
+// are computed with the very operations warp_collide uses, so "no leaf pair's boxes
+// overlap" here is exactly warp_collide returning false at step 2 (a miss). inv / pose:
+// row-major 3x4 (global memory); gr = obj_grec of the object.
+__device__ __forceinline__ bool leaf_filter(const WorldView& w, const PlaceGeomCache& gc,
+                                            const double* inv, const double* pose, int4 gr) {
+  double I[12], P[12];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    const double2 a = __ldcg(reinterpret_cast<const double2*>(inv) + k);
+    const double2 b = __ldcg(reinterpret_cast<const double2*>(pose) + k);
+    I[2 * k] = a.x;
+    I[2 * k + 1] = a.y;
+    P[2 * k] = b.x;
+    P[2 * k + 1] = b.y;
+  }
+  M34 M;  // warp_collide's other_in_cand, entry by entry (shim order)
+#pragma unroll
+  for (int e = 0; e < 12; ++e) {
+    const int i = e >> 2, j = e & 3;
+    double s = I[4 * i + 0] * P[j];
+    s = s + I[4 * i + 1] * P[4 + j];
+    s = s + I[4 * i + 2] * P[8 + j];
+    s = s + I[4 * i + 3] * (j == 3 ? 1.0 : 0.0);
+    M.m[e] = s;
+  }
+  const unsigned char* rec = reinterpret_cast<const unsigned char*>(w.brec) + 16 * (size_t)gr.x;
+  const int nB = gr.z, nA = gc.n_leaves;
+  const uint32_t* info = reinterpret_cast<const uint32_t*>(rec + 48 * nB);
+  for (int b = 0; b < nB; ++b) {
+    if ((__ldg(info + 2 * b) & 0xffu) != 0xffu) continue;  // B leaf nodes only
+    const double* nbox = reinterpret_cast<const double*>(rec) + 6 * b;
+    double c[3], h[3], bmn[3], bmx[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      c[k] = __ldg(nbox + k);
+      h[k] = __ldg(nbox + 3 + k);
+    }
+    xform_aabb(M, c, h, bmn, bmx);
+    for (int l = 0; l < nA; ++l) {
+      const int a = gc.leaves[l];
+      if (gc.bmin[a][0] <= bmx[0] && bmn[0] <= gc.bmax[a][0] && gc.bmin[a][1] <= bmx[1] &&
+          bmn[1] <= gc.bmax[a][1] && gc.bmin[a][2] <= bmx[2] && bmn[2] <= gc.bmax[a][2])
+        return true;
+    }
+  }
+  return false;
+}
+
+constexpr uint32_t kQueueDone = 0xffffffffu;  // queue entry settled by the leaf filter
+
 // ---------------- B: warp per queued pair (warp w takes entries w, w + 8, ...). Pairs
 // behind a lower hit of their slot, or of a slot beyond their instance's lowest
 // confirmed-free attempt, are skipped before any data is staged; the next eligible pair's
@@ -294,6 +346,22 @@ __device__ __forceinline__ void narrow_drain(const PlaceParams& p, Tile& T, Fixe
   };
   // Pairs are claimed one at a time from a shared counter (F.qhead, zeroed by the caller),
   // so a warp that drew cheap pairs (skips, early exits) takes more of them.
+  // Thread per queued pair: the leaf-box filter settles most pairs as misses (the same
+  // bookkeeping as a warp-tested miss below) before any warp stages one.
+  for (uint32_t q = threadIdx.x; q < qn; q += kB) {
+    const uint32_t ent = T.queue[q];
+    const int v = (int)(ent >> 24), ob = (int)(ent & 0xffffffu);
+    if (skippable(v, ob)) continue;
+    if (!leaf_filter(w, F.gc, p.cinv + ((size_t)blockIdx.x * kB + v) * 12,
+                     w.pose + sb_pose_off(w, ob, T.list[v % (int)nt]), T.ogeo[ob])) {
+      T.queue[q] = kQueueDone;
+      if (atomicSub(T.rem + v, 1u) == 1u &&
+          (*((volatile uint8_t*)T.sflag + v) & kSlotEnumerated) &&
+          *((volatile int32_t*)T.contact + v) == kFree)
+        atomicMin(T.minfree + v % (int)nt, v / (int)nt);
+    }
+  }
+  __syncthreads();
   auto claim = [&]() -> uint32_t {  // next non-skippable queue index, or qn
     for (;;) {
       uint32_t q = 0;
@@ -301,7 +369,7 @@ __device__ __forceinline__ void narrow_drain(const PlaceParams& p, Tile& T, Fixe
       q = __shfl_sync(kFull, q, 0);
       if (q >= qn) return qn;
       const uint32_t ent = T.queue[q];
-      if (!skippable((int)(ent >> 24), (int)(ent & 0xffffffu))) return q;
+      if (ent != kQueueDone && !skippable((int)(ent >> 24), (int)(ent & 0xffffffu))) return q;
     }
   };
   auto stage = [&](uint32_t ent, int buf) {
@@ -1214,27 +1282,12 @@ __global__ void __launch_bounds__(kB, SB_WIDE_SAMPLE_MINB) k_wide_sample(PlacePa
 // -- such pairs never reach k_wide_narrow. Survivors are appended to the second list.
 // Pairs behind a lower hit of their slot cannot matter and are dropped as well.
 __global__ void __launch_bounds__(kB) k_wide_filter(PlaceParams p) {
-  __shared__ double abox[32][6];  // A's leaf boxes: min xyz, max xyz
-  __shared__ int nla;
+  __shared__ PlaceGeomCache gc;
   const WorldView& w = p.w;
   const int lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    const SbGeom gA = w.geoms[p.pl.geom];
-    int k = 0;
-    for (int nd = 0; nd < gA.n_nodes; ++nd) {
-      const SbNode& N = w.nodes[gA.node_offset + nd];
-      if (N.child0 >= 0) continue;
-      for (int c = 0; c < 3; ++c) {
-        abox[k][c] = N.bmin[c];
-        abox[k][3 + c] = N.bmax[c];
-      }
-      ++k;
-    }
-    nla = k;
-  }
+  load_geom_cache(w, p.w.geoms[p.pl.geom], gc);
   __syncthreads();
   const uint64_t np = __ldcg(p.w_ctl);
-  const int nA = nla;
   Local L;
   for (uint64_t q0 = (uint64_t)blockIdx.x * kB; q0 < np; q0 += (uint64_t)gridDim.x * kB) {
     const uint64_t q = q0 + threadIdx.x;
@@ -1246,45 +1299,8 @@ __global__ void __launch_bounds__(kB) k_wide_filter(PlaceParams p) {
       const int32_t ob = (int32_t)(ent & 0xffu);
       if (*((volatile int32_t*)p.w_contact + sl) >= ob) {
         const uint32_t inst = __ldcg(p.tile_list + (uint64_t)(sl / kB) * p.tile_inst + sl % kB);
-        double I[12], P[12];
-        const double2* ip = reinterpret_cast<const double2*>(p.w_inv + (size_t)sl * 12);
-        const double2* pp = reinterpret_cast<const double2*>(w.pose + sb_pose_off(w, ob, inst));
-#pragma unroll
-        for (int k = 0; k < 6; ++k) {
-          const double2 a = __ldcg(ip + k), b = __ldcg(pp + k);
-          I[2 * k] = a.x;
-          I[2 * k + 1] = a.y;
-          P[2 * k] = b.x;
-          P[2 * k + 1] = b.y;
-        }
-        M34 M;  // warp_collide's other_in_cand, entry by entry (shim order)
-#pragma unroll
-        for (int e = 0; e < 12; ++e) {
-          const int i = e >> 2, j = e & 3;
-          double s = I[4 * i + 0] * P[j];
-          s = s + I[4 * i + 1] * P[4 + j];
-          s = s + I[4 * i + 2] * P[8 + j];
-          s = s + I[4 * i + 3] * (j == 3 ? 1.0 : 0.0);
-          M.m[e] = s;
-        }
-        const int4 gr = obj_grec(w, ob);
-        const unsigned char* rec = reinterpret_cast<const unsigned char*>(w.brec) + 16 * (size_t)gr.x;
-        const int nB = gr.z;
-        const uint32_t* info = reinterpret_cast<const uint32_t*>(rec + 48 * nB);
-        for (int b = 0; b < nB && !pass; ++b) {
-          if ((__ldg(info + 2 * b) & 0xffu) != 0xffu) continue;  // B leaf nodes only
-          const double* nbox = reinterpret_cast<const double*>(rec) + 6 * b;
-          double c[3], h[3], bmn[3], bmx[3];
-#pragma unroll
-          for (int k = 0; k < 3; ++k) {
-            c[k] = __ldg(nbox + k);
-            h[k] = __ldg(nbox + 3 + k);
-          }
-          xform_aabb(M, c, h, bmn, bmx);
-          for (int a = 0; a < nA && !pass; ++a)
-            pass = abox[a][0] <= bmx[0] && bmn[0] <= abox[a][3] && abox[a][1] <= bmx[1] &&
-                   bmn[1] <= abox[a][4] && abox[a][2] <= bmx[2] && bmn[2] <= abox[a][5];
-        }
+        pass = leaf_filter(w, gc, p.w_inv + (size_t)sl * 12, w.pose + sb_pose_off(w, ob, inst),
+                           obj_grec(w, ob));
       }
     }
     // warp-aggregated append of the survivors (order within the list is free: the narrow
