@@ -161,13 +161,28 @@ typedef struct sb_mesh {
 typedef struct sb_fixed_object {
   int32_t mesh;
   double pose[16];
+  /* Optional per-instance poses (a TransformBatch, CollisionWorld::update_transforms,
+   * collision.hpp:95): n_instances column-major Mat4 in GLOBAL instance order (a shard
+   * reads its own range); NULL = `pose` for every instance. */
+  const double* poses16;
 } sb_fixed_object;
 
-/* A support surface: axis-aligned rect [x0,x1]x[y0,y1] in the z=0 plane of `pose`
- * (SupportSurface, surface.hpp:15-20, given directly: surface extraction is out of scope). */
+/* A support surface: axis-aligned rect [x0,x1]x[y0,y1] in the z=0 plane of its frame
+ * (SupportSurface, surface.hpp:15-20, given directly or from sb_extract_support_surfaces).
+ * The frame per instance is the reference's support_world[inst] (sampler.hpp:78-80,
+ * sampler.cpp:90,119; built by the driver from BatchedSceneGraph::world_poses,
+ * scene_graph.cpp:126-147, times the surface frame):
+ *   on_placement >= 0: (accepted pose of placement on_placement) * pose -- a surface of an
+ *                      earlier placed object (stacking), evaluated per instance and run;
+ *   else poses16 != NULL: poses16[inst] (n_instances column-major Mat4, global order),
+ *                      e.g. a drawer floor at per-instance joint values (FK);
+ *   else: `pose` for every instance. */
 typedef struct sb_support {
   double pose[16];
   double rect[4]; /* x0, y0, x1, y1 */
+  const double* poses16;
+  int32_t on_placement;
+  int32_t reserved;
 } sb_support;
 
 /* RelationshipSpec (relationships.hpp:18-38) restricted to zero or one anchor. */

@@ -578,6 +578,7 @@ struct RefEngine {
   std::vector<TriMesh> meshes;
   std::vector<int> geom_of_mesh;
   std::vector<int> obj_of_placement;
+  std::vector<std::vector<double>> support_batches;
 
   static std::size_t local_size(const sb_scene* sc, const sb_shard* shard) {
     if (!sc) throw std::invalid_argument("scene is NULL");
@@ -613,9 +614,21 @@ struct RefEngine {
     }
     for (const sb_fixed_object& f : fixed) {
       int obj = w.world.add_object("fixed", geom_of_mesh.at(f.mesh));
-      w.world.update_transforms(obj, TransformBatch(n_local, mat_from(f.pose)));
+      if (f.poses16) {  // per-instance TransformBatch (GLOBAL order; this shard's range)
+        TransformBatch b(n_local);
+        for (std::size_t i = 0; i < n_local; ++i) b[i] = mat_from(f.poses16 + 16 * (begin + i));
+        w.world.update_transforms(obj, b);
+      } else {
+        w.world.update_transforms(obj, TransformBatch(n_local, mat_from(f.pose)));
+      }
       w.world.set_enabled_all(obj, true);
     }
+    support_batches.resize(supports.size());
+    for (std::size_t k = 0; k < supports.size(); ++k)
+      if (supports[k].poses16) {  // keep the caller's support_world batch (global order)
+        support_batches[k].assign(supports[k].poses16, supports[k].poses16 + 16 * n_total);
+        supports[k].poses16 = support_batches[k].data();
+      }
     for (uint32_t p = 0; p < placements.size(); ++p)
       obj_of_placement.push_back(
           w.world.add_object("p" + std::to_string(p), geom_of_mesh.at(placements[p].mesh)));
@@ -661,14 +674,24 @@ void RefEngine::generate(uint64_t run_seed, sb_result* out, sb_run_stats* st,
           MultiPolygon2D::from(make_rect(sup.rect[0], sup.rect[1], sup.rect[2], sup.rect[3]));
       RelationshipSpec spec = spec_from(pl.relation);
 
+      // support_world (sampler.hpp:78-80), GLOBAL instance order: the surface of an earlier
+      // placed object (its accepted pose * the surface frame), a given batch (e.g. FK world
+      // poses of a drawer times the surface frame), or one pose for all
+      TransformBatch support_world(n_total, sup_pose);
+      if (sup.on_placement >= 0) {
+        const int sobj = obj_of_placement.at(sup.on_placement);
+        for (std::size_t i = 0; i < n_local; ++i)
+          support_world[begin + i] = w.world.object_pose(sobj, i) * sup_pose;
+      } else if (sup.poses16) {
+        for (std::size_t i = 0; i < n_total; ++i) support_world[i] = mat_from(sup.poses16 + 16 * i);
+      }
       // Anchor states in the support frame, indexed by GLOBAL instance id.
       std::vector<std::vector<AnchorState>> anchors;
       if (pl.relation.anchor >= 0) {
         const int aobj = obj_of_placement.at(pl.relation.anchor);
-        Mat4 inv_sup = inverse_rigid(sup_pose);
         std::vector<AnchorState> local(n_local);
         for (std::size_t i = 0; i < n_local; ++i) {
-          Mat4 rel = inv_sup * w.world.object_pose(aobj, i);
+          Mat4 rel = inverse_rigid(support_world[begin + i]) * w.world.object_pose(aobj, i);
           local[i].position = Vec2(rel(0, 3), rel(1, 3));
           local[i].yaw = yaw_of(rel);
         }
@@ -717,7 +740,6 @@ void RefEngine::generate(uint64_t run_seed, sb_result* out, sb_run_stats* st,
       if (cr.per_instance) ++per_inst;
       PositionSampler sampler(p);
       sampler.prepare(&cr, n_total, run_seed);
-      TransformBatch support_world(n_total, sup_pose);
       OrientationRule rule;
       rule.kind = static_cast<OrientationRule::Kind>(pl.orientation);
       std::vector<Vec2> face_targets;

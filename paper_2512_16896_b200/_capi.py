@@ -36,11 +36,13 @@ class sb_mesh(C.Structure):
 
 
 class sb_fixed_object(C.Structure):
-    _fields_ = [("mesh", C.c_int32), ("pose", C.c_double * 16)]
+    _fields_ = [("mesh", C.c_int32), ("pose", C.c_double * 16), ("poses16", C.POINTER(C.c_double))]
 
 
 class sb_support(C.Structure):
-    _fields_ = [("pose", C.c_double * 16), ("rect", C.c_double * 4)]
+    _fields_ = [("pose", C.c_double * 16), ("rect", C.c_double * 4),
+                ("poses16", C.POINTER(C.c_double)), ("on_placement", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 class sb_joint(C.Structure):

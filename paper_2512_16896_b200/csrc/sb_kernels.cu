@@ -142,6 +142,30 @@ __global__ void k_engine_reset(WorldView w, int32_t first_obj, int32_t n_obj, ui
   for (int32_t p = 0; p < n_place; ++p) accepted[(uint64_t)p * w.n + i] = -1;
 }
 
+// Per-instance support frames of a placement (sampler.hpp:78-80): S[i] = pose(obj, i) *
+// frame when obj >= 0 (a surface of a placed object, Mat4 product in the shim's order),
+// else S[i] as given; inv[i] = inverse_rigid(S[i]) (transform.hpp:63-69).
+__global__ void k_support_frames(WorldView w, int32_t obj, M34 frame, double* S, double* inv) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= w.n) return;
+  M34 F, I;
+  if (obj >= 0) {
+    const double* pp = w.pose + sb_pose_off(w, obj, i);
+    M34 P;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) P.m[k] = pp[k];
+    mul34(P, frame, F);
+#pragma unroll
+    for (int k = 0; k < 12; ++k) S[i * 12 + k] = F.m[k];
+  } else {
+#pragma unroll
+    for (int k = 0; k < 12; ++k) F.m[k] = S[i * 12 + k];
+  }
+  inverse_rigid(F, I);
+#pragma unroll
+  for (int k = 0; k < 12; ++k) inv[i * 12 + k] = I.m[k];
+}
+
 // generate() end: an object whose placement accepted nothing for instance i keeps the
 // state add_object gave it (collision.cpp:365-376): identity pose, local box.
 __global__ void k_unaccepted_fixup(WorldView w, int32_t first_obj, int32_t n_place,
@@ -180,13 +204,18 @@ __global__ void k_cells_insert_fixed(WorldView w, SbCellGrid G, int32_t first_ob
 
 // AnchorState in the support frame: inverse_rigid(support) * anchor pose; position is the
 // translation, yaw = yaw_of (transform.hpp:77).
-__global__ void k_anchor_states(WorldView w, int32_t anchor_obj, M34 inv_support, double* out) {
+__global__ void k_anchor_states(WorldView w, int32_t anchor_obj, M34 inv_support,
+                                const double* inv_inst, double* out) {
   uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i >= w.n) return;
   const double* pp = w.pose + sb_pose_off(w, anchor_obj, i);
   M34 P, rel;
 #pragma unroll
   for (int k = 0; k < 12; ++k) P.m[k] = pp[k];
+  if (inv_inst) {  // per-instance support frames
+#pragma unroll
+    for (int k = 0; k < 12; ++k) inv_support.m[k] = inv_inst[i * 12 + k];
+  }
   mul34(inv_support, P, rel);
   out[3 * i + 0] = rel.m[3];
   out[3 * i + 1] = rel.m[7];
@@ -393,6 +422,13 @@ void unaccepted_fixup(const SbWorldView& w, int32_t first_obj, int32_t n_place,
   k_unaccepted_fixup<<<grid_for(w.n), kBlock, 0, s>>>(w, first_obj, n_place, accepted);
   check_launch("unaccepted_fixup");
 }
+void support_frames(const SbWorldView& w, int32_t obj, const double frame[12], double* S,
+                    double* inv, sb_stream_t s) {
+  M34 F;
+  for (int k = 0; k < 12; ++k) F.m[k] = frame[k];
+  k_support_frames<<<grid_for(w.n), kBlock, 0, s>>>(w, obj, F, S, inv);
+  check_launch("support_frames");
+}
 void out16_fixup(uint64_t n, const int16_t* accepted, double* out16, sb_stream_t s) {
   k_out16_fixup<<<grid_for(n), kBlock, 0, s>>>(n, accepted, out16);
   check_launch("out16_fixup");
@@ -405,10 +441,10 @@ void cells_reset(const SbWorldView& w, const SbCellGrid& g, int32_t first_obj, s
   check_launch("cells_reset");
 }
 void anchor_states(const SbWorldView& w, int32_t anchor_obj, const double inv_support[12],
-                   double* out, sb_stream_t s) {
+                   const double* inv_inst, double* out, sb_stream_t s) {
   M34 inv;
   for (int k = 0; k < 12; ++k) inv.m[k] = inv_support[k];
-  k_anchor_states<<<grid_for(w.n), kBlock, 0, s>>>(w, anchor_obj, inv, out);
+  k_anchor_states<<<grid_for(w.n), kBlock, 0, s>>>(w, anchor_obj, inv, inv_inst, out);
   check_launch("anchor_states");
 }
 void download_poses(const SbWorldView& w, int32_t obj, double* out16, sb_stream_t s) {

@@ -46,7 +46,11 @@ void out16_fixup(uint64_t n, const int16_t* accepted, double* out16, sb_stream_t
 void cells_reset(const SbWorldView& w, const SbCellGrid& g, int32_t first_obj, sb_stream_t s);
 // AnchorState per instance (support frame): out[3i..3i+2] = x, y, yaw
 void anchor_states(const SbWorldView& w, int32_t anchor_obj, const double inv_support[12],
-                   double* out, sb_stream_t s);
+                   const double* inv_inst, double* out, sb_stream_t s);
+// per-instance support frames: S[i] = pose(obj, i) * frame (obj >= 0) or as given,
+// inv[i] = inverse_rigid(S[i]); row-major 3x4, [n][12]
+void support_frames(const SbWorldView& w, int32_t obj, const double frame[12], double* S,
+                    double* inv, sb_stream_t s);
 // test hook for the device libm (sb_crmath.cuh): fn 0 sin, 1 cos, 2 atan2 (pairs y, x)
 void debug_math(int fn, const double* in, uint64_t n, double* out, sb_stream_t s);
 // accepted poses of one object as column-major Mat4 (N x 16 doubles)

@@ -50,6 +50,14 @@ struct SbPlacementDev {
   double angle_threshold;  // <= 0: default
   uint64_t salt;           // placement index (Appendix C)
   double erode_r;          // apply_ratio_on_support radius of relation regions, 0 = none
+  // support_world per instance (sampler.hpp:78-80): when non-null the frame of instance i
+  // is support_inst[i] (row-major 3x4), else `support`; inv_support_inst[i] = its
+  // inverse_rigid (anchor states in the support frame). support_object >= 0: the frames
+  // are (pose of that world object) * support, refreshed per run (k_support_frames).
+  const double* support_inst;
+  const double* inv_support_inst;
+  int32_t support_object;
+  int32_t pad_;
 };
 
 // Device view of a collision world (plain pointers; built by the host World class).

@@ -196,9 +196,19 @@ __device__ __forceinline__ bool compose_candidate(const PlaceParams& p, const Sa
     const uint64_t off = (uint64_t)inst * p.inst_cap;
     sbp::draw_point(p.inst_tris + off, p.inst_cum + off, nti, u, r1, r2, lx, ly);
   }
-  M34 Sp;
+  M34 Sp;  // support_world[inst]
+  if (pl.support_inst) {
+    const double2* sp = reinterpret_cast<const double2*>(pl.support_inst + (size_t)inst * 12);
 #pragma unroll
-  for (int k = 0; k < 12; ++k) Sp.m[k] = pl.support[k];
+    for (int k = 0; k < 6; ++k) {
+      const double2 v = __ldcg(sp + k);
+      Sp.m[2 * k] = v.x;
+      Sp.m[2 * k + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 12; ++k) Sp.m[k] = pl.support[k];
+  }
   double px, py, pz;
   xform(Sp, lx, ly, 0.0, px, py, pz);  // transform_point(support_world, (x, y, 0))
   double yaw = 0.0;

@@ -645,12 +645,19 @@ __global__ void __launch_bounds__(kRB, kRegionMinBlocks) k_relation_regions(Rela
   // feeds a local-frame direction and the variation test; the latter only needs it when
   // the positions agree (relationships.cpp:180-181), so atan2 is skipped otherwise.
   const bool yaw_used = p.pl.direction != SB_DIR_NONE && p.pl.frame == SB_FRAME_LOCAL;
-  auto rel_of = [&](uint64_t inst, M34& rel) {
+  auto rel_of = [&](uint64_t inst, M34& rel) {  // inverse_rigid(support_world[i]) * anchor pose
     const double* pp = p.w.pose + sb_pose_off(p.w, p.anchor_object, inst);
     M34 P;
 #pragma unroll
     for (int k = 0; k < 12; ++k) P.m[k] = pp[k];
-    mul34(inv, P, rel);
+    if (p.pl.inv_support_inst) {
+      M34 Ii;
+#pragma unroll
+      for (int k = 0; k < 12; ++k) Ii.m[k] = p.pl.inv_support_inst[inst * 12 + k];
+      mul34(Ii, P, rel);
+    } else {
+      mul34(inv, P, rel);
+    }
   };
   auto yaw_of = [](const M34& rel) { return sbg::atan2(rel.m[4], rel.m[0]); };  // transform.hpp:77
   if (p.from_s0) {  // canonical region_for(0) from the exchanged instance-0 state

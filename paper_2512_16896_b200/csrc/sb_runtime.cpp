@@ -404,6 +404,7 @@ struct sb_engine {
     int mesh = 0;
   };
   std::vector<Placement> places;
+  std::vector<std::unique_ptr<DevArray<double>>> sup_frames;  // per-instance support frames
   int32_t first_place_obj = 0;
   int inst_cap = 0;  // region table stride (canonical and per instance)
 
@@ -539,10 +540,15 @@ struct sb_engine {
     };
     for (uint32_t f = 0; f < sc->n_fixed; ++f) {
       int obj = world->add_object("fixed" + std::to_string(f), mesh_geom(sc->fixed[f].mesh));
-      require_homogeneous(sc->fixed[f].pose);
-      world->upload_poses(sc->fixed[f].pose, 1);
-      // broadcast one pose to every instance (stride 0)
-      sbk::update_transforms(world->view(), obj, world->d_scratch_poses.p, nullptr, n, 0, world->s());
+      if (sc->fixed[f].poses16) {  // a TransformBatch (update_transforms): this shard's range
+        world->upload_poses(sc->fixed[f].poses16 + 16 * begin, n);
+        sbk::update_transforms(world->view(), obj, world->d_scratch_poses.p, nullptr, n, 16, world->s());
+      } else {
+        require_homogeneous(sc->fixed[f].pose);
+        world->upload_poses(sc->fixed[f].pose, 1);
+        // broadcast one pose to every instance (stride 0)
+        sbk::update_transforms(world->view(), obj, world->d_scratch_poses.p, nullptr, n, 0, world->s());
+      }
       cuda_check(cudaStreamSynchronize(world->stream), "sync");
       world->set_enabled_all(obj, true);
     }
@@ -572,6 +578,28 @@ struct sb_engine {
       std::memcpy(pl.support16, sup.pose, sizeof pl.support16);
       colmajor_to_34(sup.pose, pl.dev.support);
       inverse_rigid34(sup.pose, pl.inv_support);
+      pl.dev.support_object = -1;
+      if (sup.on_placement >= 0 || sup.poses16) {  // support_world per instance
+        if (sup.on_placement >= 0 && static_cast<uint32_t>(sup.on_placement) >= p)
+          throw std::invalid_argument("support on_placement must be an earlier placement");
+        auto S = std::make_unique<DevArray<double>>();
+        auto I = std::make_unique<DevArray<double>>();
+        S->alloc(12 * n);
+        I->alloc(12 * n);
+        if (sup.on_placement >= 0) {
+          pl.dev.support_object = first_place_obj + sup.on_placement;
+        } else {
+          for (uint64_t i = 0; i < n; ++i) require_homogeneous(sup.poses16 + 16 * (begin + i));
+          world->upload_poses(sup.poses16 + 16 * begin, n);
+          sbk::graph_colmajor_to_34(world->d_scratch_poses.p, n, S->p, world->s());
+          sbk::support_frames(world->view(), -1, pl.dev.support, S->p, I->p, world->s());
+          cuda_check(cudaStreamSynchronize(world->stream), "sync");
+        }
+        pl.dev.support_inst = S->p;
+        pl.dev.inv_support_inst = I->p;
+        sup_frames.push_back(std::move(S));
+        sup_frames.push_back(std::move(I));
+      }
       for (int k = 0; k < 4; ++k) pl.dev.rect[k] = sup.rect[k];
       const sb_relation& r = sp.relation;
       pl.hole = relation_to_dev(r, pl.dev);
@@ -801,7 +829,8 @@ struct sb_engine {
     sb_stream_t s = world->s();
     double s0[3] = {0, 0, 0};
     if (begin == 0) {
-      sbk::anchor_states(wv, pl.dev.anchor_object, pl.inv_support, d_anchor.p, s);
+      sbk::anchor_states(wv, pl.dev.anchor_object, pl.inv_support, pl.dev.inv_support_inst,
+                         d_anchor.p, s);
       ++launches;
       cuda_check(cudaMemcpyAsync(s0, d_anchor.p, sizeof s0, cudaMemcpyDeviceToHost, stream), "D2H s0");
       cuda_check(cudaStreamSynchronize(stream), "sync");
@@ -913,6 +942,12 @@ struct sb_engine {
         const double* canon_cum = d_canon_cum.p + p * inst_cap;
         const bool relation = pl.dev.anchor_object >= 0;
         rec(ev_place[2 * p], capturing);
+        if (pl.dev.support_object >= 0) {  // surface of a placed object: this run's poses
+          sbk::support_frames(wv, pl.dev.support_object, pl.dev.support,
+                              const_cast<double*>(pl.dev.support_inst),
+                              const_cast<double*>(pl.dev.inv_support_inst), s);
+          ++launches;
+        }
         if (relation) {
           if (world_size == 1) {
             relation_prep_device(p, pl, wv, launches);

@@ -235,14 +235,22 @@ class Placement:
 
 @dataclass
 class Support:
+    """A support surface (sb_support): rect in the z = 0 plane of its frame. The frame is
+    `pose`, or per instance `poses` ((N, 4, 4), e.g. FK world poses of a drawer times the
+    surface frame), or -- with on_placement >= 0 -- the accepted pose of that earlier
+    placement times `pose` (a surface on a placed object)."""
     pose: np.ndarray
     rect: tuple  # x0, y0, x1, y1 in the support frame
+    poses: Optional[np.ndarray] = None
+    on_placement: int = -1
 
 
 @dataclass
 class Fixed:
+    """A fixed object: one pose, or per-instance `poses` ((N, 4, 4), a TransformBatch)."""
     mesh: int
     pose: np.ndarray
+    poses: Optional[np.ndarray] = None
 
 
 @dataclass
@@ -263,14 +271,26 @@ class Scene:
             meshes[i] = A.sb_mesh(_dp(m.vertices), len(m.vertices), _up(m.triangles),
                                   len(m.triangles))
             keep.append(m)
+        def batch(poses):
+            if poses is None:
+                return None
+            b = colmajor(poses).reshape(-1, 16)
+            if len(b) != self.n_instances:
+                raise ValueError("per-instance poses must have n_instances entries")
+            keep.append(b)
+            return _dp(b)
+
         fixed = (A.sb_fixed_object * max(1, len(self.fixed)))()
         for i, f in enumerate(self.fixed):
             fixed[i].mesh = f.mesh
             fixed[i].pose[:] = list(colmajor(f.pose))
+            fixed[i].poses16 = batch(f.poses)
         sups = (A.sb_support * max(1, len(self.supports)))()
         for i, s in enumerate(self.supports):
             sups[i].pose[:] = list(colmajor(s.pose))
             sups[i].rect[:] = list(map(float, s.rect))
+            sups[i].poses16 = batch(s.poses)
+            sups[i].on_placement = s.on_placement
         pls = (A.sb_placement * max(1, len(self.placements)))()
         for i, p in enumerate(self.placements):
             r = p.relation
