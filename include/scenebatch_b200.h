@@ -262,6 +262,31 @@ typedef struct sb_shard {
   void* ctx_dev;
 } sb_shard;
 
+/* ------------------------------------------------------------------------------------
+ * Native shard communicator: one process per GPU, no PyTorch.
+ * Bootstrap and the host exchange go through a TCP star via rank 0 (host:port; under
+ * torchrun e.g. MASTER_ADDR and MASTER_PORT + 1); with device >= 0 every rank also exposes
+ * a count board in HBM that each peer maps through CUDA IPC, and sb_shard.allgather_dev
+ * becomes remote stores over NVLink / NVSwitch + per-rank epoch flags the consuming stream
+ * waits on (cuStreamWaitValue64; no host round trip). The reference has no multi-GPU layer;
+ * this replaces the count exchange SURVEY 8(e)(i) describes. */
+typedef struct sb_comm sb_comm;
+/* Blocks until all world_size ranks have connected (timeout_s <= 0: 300 s). device < 0:
+ * host exchange only (no allgather_dev). Ranks must be separate processes. */
+sb_status sb_comm_create(int32_t rank, int32_t world_size, int device, const char* host,
+                         int32_t port, double timeout_s, sb_comm** out);
+void sb_comm_destroy(sb_comm* c);
+/* Contiguous variation shard of n_total for this rank + the comm's exchange callbacks
+ * (valid while the comm lives). */
+sb_status sb_comm_shard(sb_comm* c, uint64_t n_total, sb_shard* out);
+sb_status sb_comm_allgather(sb_comm* c, const uint64_t* send, uint32_t n, uint64_t* recv);
+/* n <= 15 u64 of device memory per rank, enqueued on cuda_stream (a cudaStream_t). */
+sb_status sb_comm_allgather_dev(sb_comm* c, const uint64_t* d_send, uint32_t n, uint64_t* d_recv,
+                                void* cuda_stream);
+sb_status sb_comm_barrier(sb_comm* c);
+/* 1 if the device exchange waits with stream memory operations, 0 if it spins a kernel. */
+int32_t sb_comm_uses_stream_waits(const sb_comm* c);
+
 typedef struct sb_engine sb_engine;
 
 /* initialize: registers meshes, adds fixed + placement objects, uploads

@@ -4,6 +4,7 @@ against placed geometry and first-valid acceptance, behind a C-ABI drop-in
 bench.py; the product is libscenebatch_b200.so (sm_100a CUDA + C++ host runtime).
 """
 from ._capi import LIB_PATH, SbCudaError, SbError, lib  # noqa: F401
+from .comm import Comm, CommShard  # noqa: F401
 from .graph import BatchedSceneGraph, JointSpec  # noqa: F401
 from .reach import ChainLink, KinematicChain, ReachMap4D, placement_filter  # noqa: F401
 from .sampler import PositionSampler, sample_orientations  # noqa: F401

@@ -142,6 +142,14 @@ SIGNATURES = {
                                  C.POINTER(C.c_int32)]),
     "sb_get_stats": (C.c_int, [_P, C.POINTER(sb_stats)]),
     "sb_reset_stats": (C.c_int, [_P]),
+    "sb_comm_create": (C.c_int, [C.c_int32, C.c_int32, C.c_int, C.c_char_p, C.c_int32, C.c_double,
+                                 C.POINTER(_P)]),
+    "sb_comm_destroy": (None, [_P]),
+    "sb_comm_shard": (C.c_int, [_P, C.c_uint64, C.POINTER(sb_shard)]),
+    "sb_comm_allgather": (C.c_int, [_P, C.POINTER(C.c_uint64), C.c_uint32, C.POINTER(C.c_uint64)]),
+    "sb_comm_allgather_dev": (C.c_int, [_P, _P, C.c_uint32, _P, _P]),
+    "sb_comm_barrier": (C.c_int, [_P]),
+    "sb_comm_uses_stream_waits": (C.c_int32, [_P]),
     "sb_engine_create": (C.c_int, [C.POINTER(sb_scene), C.POINTER(sb_shard), C.c_int, C.POINTER(_P)]),
     "sb_engine_destroy": (None, [_P]),
     "sb_engine_generate": (C.c_int, [_P, C.c_uint64, C.POINTER(sb_result), C.POINTER(sb_run_stats)]),

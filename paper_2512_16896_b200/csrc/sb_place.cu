@@ -1015,6 +1015,7 @@ __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_place_instances(Pla
   __shared__ Fixed F;
   Tile T = carve(g_dsm, p.w.n_words, p.ws_bytes);
   SbGeom gA;
+  if (p.shard_vary && __ldcg(p.shard_vary) == 0) return;  // canonical: the FIFO rounds place it
   block_setup(p, F, T, gA);
   Local L;
   Sampling S{0, nullptr, nullptr, 0};
@@ -1025,6 +1026,7 @@ __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_place_instances(Pla
 __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_fast_init(PlaceParams p) {
   __shared__ Fixed F;
   Tile T = carve(g_dsm, p.w.n_words, p.ws_bytes);
+  if (p.shard_vary && __ldcg(p.shard_vary) != 0) return;  // per-instance: no FIFO rounds
   uint32_t mine = 0;
   for (uint32_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
     const uint32_t n = tile_load_valid(p, T, F, t, p.tile_inst);
@@ -1045,7 +1047,8 @@ __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_fast_round(PlacePar
   SbGeom gA;
   block_setup(p, F, T, gA);
   Local L;
-  Sampling S{1, p.canon_tris, p.canon_cum, p.canon_n};
+  const int32_t canon_n = p.canon_n_dev ? __ldcg(p.canon_n_dev) : p.canon_n;
+  Sampling S{1, p.canon_tris, p.canon_cum, canon_n};
   if (p.xrecv) {  // device-side exchange: this round's offsets from the gathered counts
     unsigned long long tot = 0, before = 0;
     for (int r = 0; r < p.xworld; ++r) {
@@ -1056,7 +1059,7 @@ __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_fast_round(PlacePar
     if (tot == 0) return;  // every rank is done: a no-op round
     const unsigned long long draws = __ldcg(p.xdraws + a);
     if (blockIdx.x == 0 && threadIdx.x == 0)
-      p.xdraws[a + 1] = draws + (p.canon_n > 0 ? tot : 0ull);  // cache drained only if sampled
+      p.xdraws[a + 1] = draws + (canon_n > 0 ? tot : 0ull);  // cache drained only if sampled
     // this rank has no survivors left: idle, but keep its tile counts maintained (the
     // round-(a+1) buffer still holds round a-1's counts, which k_fast_finish would read)
     if (__ldcg(p.xrecv + (size_t)a * p.xworld + p.xrank) == 0) {

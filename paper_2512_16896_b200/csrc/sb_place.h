@@ -91,6 +91,12 @@ struct PlaceParams {
   // *vary_flag != 0 selects the per-instance tables, else the FIFO fast path samples the
   // canonical region_for(0) = local instance 0's table (relationships.cpp:188-190).
   const int32_t* vary_flag;
+  // Sharded relation placements with the device exchange: both paths are enqueued and the
+  // OR-gathered flag picks one on the device -- k_place_instances runs iff *shard_vary != 0,
+  // k_fast_init (and so the FIFO rounds) iff *shard_vary == 0; the FIFO rounds then read
+  // the canonical table size from canon_n_dev.
+  const int32_t* shard_vary;
+  const int32_t* canon_n_dev;
   // Optional fused reachability filter: a candidate whose frame origin,
   // in its instance's robot base frame, misses the map's (r, z) occupancy is a failed
   // attempt that is not collision-checked (Appendix C item 8).

@@ -3,6 +3,7 @@
 // World  = CollisionWorld (collision.hpp:76-127) with all per-instance state in HBM.
 // Engine = the reference's absent rejection loop (contract frozen in
 //          DESIGN.md) driving the fused per-round kernel; one engine per GPU / shard.
+#include "sb_comm.h"
 #include "sb_rt.hpp"
 #include "sb_graph_rt.hpp"
 #include "sb_reach_rt.hpp"
@@ -390,6 +391,7 @@ struct sb_engine {
   sb_allgather_dev_fn allgather_dev = nullptr;  // device-side count exchange (optional)
   void* allgather_dev_ctx = nullptr;
   DevArray<unsigned long long> d_xcount, d_xrecv, d_xdraws;
+  DevArray<uint64_t> d_xsend, d_xgather;  // relation exchange: [4] out, [world][4] in
   PinnedArray<unsigned long long> h_xrecv;
   int attempts = 0;
 
@@ -437,7 +439,6 @@ struct sb_engine {
   bool timing_pending = false;
   std::vector<char> pending_per_inst;
   std::vector<uint32_t> pending_rounds;
-  double pending_sharded_ms = 0.0;
   int num_sms = 0;
   // tile decomposition of the shard (sb_place.h) and launch shape of the placement kernel
   uint32_t ntiles = 0;
@@ -476,7 +477,8 @@ struct sb_engine {
   PinnedArray<uint64_t> h_count;
   cudaStream_t copy_stream = nullptr;  // pipelined result download
   std::vector<cudaEvent_t> ev_pose;
-  cudaEvent_t ev_start = nullptr, ev_stop = nullptr, ev_r0 = nullptr, ev_r1 = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
+  cudaEvent_t ev_chunk[2] = {nullptr, nullptr};  // sharded FIFO rounds: chunk completion (no timing)
 
   uint64_t last_launches = 0;
   double last_total_ms = 0.0, last_check_ms = 0.0;
@@ -781,8 +783,7 @@ struct sb_engine {
     d_counters.alloc(8);
     cuda_check(cudaEventCreate(&ev_start), "event");
     cuda_check(cudaEventCreate(&ev_stop), "event");
-    cuda_check(cudaEventCreate(&ev_r0), "event");
-    cuda_check(cudaEventCreate(&ev_r1), "event");
+    for (cudaEvent_t& e : ev_chunk) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     cuda_check(cudaDeviceSynchronize(), "sync");
   }
 
@@ -790,7 +791,7 @@ struct sb_engine {
     if (world) cudaSetDevice(world->device);
     for (GraphSlot& g : graphs)
       if (g.exec) cudaGraphExecDestroy(g.exec);
-    for (cudaEvent_t e : {ev_start, ev_stop, ev_r0, ev_r1})
+    for (cudaEvent_t e : {ev_start, ev_stop, ev_chunk[0], ev_chunk[1]})
       if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : ev_place) cudaEventDestroy(e);
     for (cudaEvent_t e : ev_pose) cudaEventDestroy(e);
@@ -879,6 +880,61 @@ struct sb_engine {
     return vary;
   }
 
+  // Sharded relation placement with the device exchange (sb_shard.allgather_dev): instance
+  // 0's anchor state and the "anchors vary" flag travel through the device all-gather, and
+  // both region sets are built -- this rank's per-instance tables and the canonical
+  // region_for(0) from the exchanged state (relationships.cpp:178-190) -- so the path is
+  // picked on the device (PlaceParams::shard_vary) with no host round trip.
+  void relation_prep_sharded_dev(size_t p, Placement& pl, const SbWorldView& wv, uint64_t& launches) {
+    sb_stream_t s = world->s();
+    cudaStream_t stream = world->stream;
+    const size_t W = static_cast<size_t>(world_size);
+    // send words are unique per (placement, exchange): an all-gather may still read them
+    // after this stream has moved on (the sb_shard contract allows a lazy reader)
+    d_xsend.ensure(8 * places.size());
+    d_xgather.ensure(4 * W);
+    uint64_t* send_anchor = d_xsend.p + 8 * p;
+    uint64_t* send_flag = send_anchor + 4;
+    auto gather = [&](const uint64_t* send, uint32_t k) {
+      if (allgather_dev(allgather_dev_ctx, send, k, d_xgather.p, stream) != 0)
+        throw std::runtime_error("sb_shard.allgather_dev failed");
+    };
+    if (begin == 0) {
+      sbk::anchor_states(wv, pl.dev.anchor_object, pl.inv_support, pl.dev.inv_support_inst,
+                         d_anchor.p, s);
+      ++launches;
+    }
+    sbk::shard_anchor_pack(begin == 0 ? d_anchor.p : nullptr, send_anchor, s);
+    gather(send_anchor, 4);
+    sbk::shard_anchor_pick(d_xgather.p, world_size, d_s0.p, s);
+    launches += 2;
+    sbk::RelationRegionParams rp;
+    std::memset(&rp, 0, sizeof rp);
+    rp.w = wv;
+    rp.pl = pl.dev;
+    rp.anchor_object = pl.dev.anchor_object;
+    rp.owns_instance0 = 0;
+    std::memcpy(rp.inv_support, pl.inv_support, sizeof rp.inv_support);
+    rp.s0 = d_s0.p;
+    rp.cap = inst_cap;
+    rp.hole = pl.hole ? 1 : 0;
+    rp.arcs = pl.shared_arcs ? d_arcs.p + p : nullptr;
+    rp.tris = d_inst_tris.p;
+    rp.cum = d_inst_cum.p;
+    rp.ntri = d_inst_n.p;
+    rp.flags = d_rflags.p + 2 * p;
+    sbk::relation_regions(rp, num_sms, s);
+    sbk::shard_flag_pack(rp.flags, send_flag, s);
+    gather(send_flag, 1);
+    sbk::shard_flag_or(d_xgather.p, world_size, rp.flags, s);  // flags[0] = OR over ranks
+    rp.from_s0 = 1;
+    rp.tris = d_canon_tris.p + p * inst_cap;
+    rp.cum = d_canon_cum.p + p * inst_cap;
+    rp.ntri = d_canon_n.p + p;
+    sbk::relation_regions(rp, num_sms, s);
+    launches += 4;
+  }
+
   // Results requested with the call (sb_engine_generate with an sb_result) are downloaded
   // while later placements compute: placement p's poses are final once its kernel ends, so
   // a copy stream converts them (k_pose_colmajor) and copies them to the host behind an event.
@@ -901,7 +957,7 @@ struct sb_engine {
     const SbWorldView wv = world->view();
     const size_t P = places.size();
     uint64_t launches = 0, rounds_host = 0, per_inst_host = 0, round_launches = 0;
-    double sharded_check_ms = 0.0;
+    std::vector<char> shard_dev_relation(places.size(), 0);
     std::vector<char> device_rounds(places.size(), world_size == 1 ? 1 : 0);
     while (ev_place.size() < 2 * P + 2) {
       cudaEvent_t e;
@@ -948,9 +1004,14 @@ struct sb_engine {
                               const_cast<double*>(pl.dev.inv_support_inst), s);
           ++launches;
         }
+        bool dev_relation = false;  // sharded, path picked on the device
         if (relation) {
           if (world_size == 1) {
             relation_prep_device(p, pl, wv, launches);
+          } else if (allgather_dev) {
+            relation_prep_sharded_dev(p, pl, wv, launches);
+            dev_relation = true;
+            shard_dev_relation[p] = 1;
           } else {
             fast = !relation_prep_sharded(p, pl, wv, launches, canon_n);
             if (!fast) ++per_inst_host;
@@ -1041,19 +1102,21 @@ struct sb_engine {
         } else if (!fast) {
           // per-instance regions: tiles are independent, no exchange
           device_rounds[p] = 1;
-          cuda_check(cudaEventRecord(ev_r0, stream), "event");
           sbk::place_instances(pp, grid, smem, s);
-          cuda_check(cudaEventRecord(ev_r1, stream), "event");
           ++launches;
           ++round_launches;
-          cuda_check(cudaEventSynchronize(ev_r1), "sync");
-          float ms = 0.f;
-          cuda_check(cudaEventElapsedTime(&ms, ev_r0, ev_r1), "elapsed");
-          sharded_check_ms += ms;
         } else if (allgather_dev) {
+          if (dev_relation) {  // per-instance kernel first; each side no-ops on the other path
+            device_rounds[p] = 1;
+            pp.shard_vary = d_rflags.p + 2 * p;
+            pp.canon_n_dev = d_canon_n.p + p;
+            sbk::place_instances(pp, grid, smem, s);
+            ++launches;
+            ++round_launches;
+          }
           // FIFO fast path, device-side exchange: round a's kernel reads the gathered counts
           // and the draws before it from device memory, the all-gather of its survivors is
-          // enqueued behind it; the host only checks for completion every kChunk rounds.
+          // enqueued behind it; the host checks for completion once per kChunk rounds.
           constexpr int kChunk = 4;
           const size_t K1 = static_cast<size_t>(attempts) + 1, W = static_cast<size_t>(world_size);
           d_xcount.ensure(K1);
@@ -1072,13 +1135,17 @@ struct sb_engine {
                               reinterpret_cast<uint64_t*>(d_xrecv.p + a * W), stream) != 0)
               throw std::runtime_error("sb_shard.allgather_dev failed");
           };
-          cuda_check(cudaEventRecord(ev_r0, stream), "event");
           sbk::place_fast_init(pp, grid, smem, s);
           ++launches;
           gather(0);
+          // The host stays one chunk of rounds ahead of the device: after enqueuing chunk
+          // c it reads the gathered total at the end of chunk c-1 (copied behind an event,
+          // normally complete by then), so the device never idles on the host; rounds
+          // enqueued past the last one with survivors return at once.
           int32_t a = 0;
-          uint64_t last_total = 1;
-          while (a < attempts && last_total > 0) {
+          int pending = -1;  // ev_chunk slot whose total is in flight
+          int32_t pending_round = 0;
+          for (;;) {
             const int32_t stop = std::min<int32_t>(attempts, a + kChunk);
             for (; a < stop; ++a) {
               sbk::place_fast_round(pp, a, grid, smem, s);
@@ -1086,12 +1153,20 @@ struct sb_engine {
               round_launches += 1;
               gather(a + 1);
             }
+            const int slot = pending == 0 ? 1 : 0;
             cuda_check(cudaMemcpyAsync(h_xrecv.p + a * W, d_xrecv.p + a * W, W * 8, cudaMemcpyDeviceToHost, stream), "D2H counts");
-            cuda_check(cudaStreamSynchronize(stream), "sync");
-            last_total = 0;
-            for (size_t r = 0; r < W; ++r) last_total += h_xrecv.p[a * W + r];
+            cuda_check(cudaEventRecord(ev_chunk[slot], stream), "event");
+            bool done = a >= attempts;
+            if (pending >= 0) {
+              cuda_check(cudaEventSynchronize(ev_chunk[pending]), "sync chunk");
+              uint64_t t = 0;
+              for (size_t r = 0; r < W; ++r) t += h_xrecv.p[static_cast<size_t>(pending_round) * W + r];
+              done = done || t == 0;
+            }
+            pending = slot;
+            pending_round = a;
+            if (done) break;
           }
-          cuda_check(cudaEventRecord(ev_r1, stream), "event");
           cuda_check(cudaMemcpyAsync(h_xrecv.p, d_xrecv.p, K1 * W * 8, cudaMemcpyDeviceToHost, stream), "D2H counts");
           cuda_check(cudaStreamSynchronize(stream), "sync");
           for (int32_t r = 0; r < a; ++r) {  // rounds the reference runs: total > 0
@@ -1104,9 +1179,6 @@ struct sb_engine {
             sbk::place_fast_finish(pp, a, grid, s);
             ++launches;
           }
-          float ms = 0.f;
-          cuda_check(cudaEventElapsedTime(&ms, ev_r0, ev_r1), "elapsed");
-          sharded_check_ms += ms;
         } else {
           // FIFO fast path: one launch per round, per-rank survivor counts exchanged between
           uint32_t* tot = pp.ctrl;
@@ -1132,15 +1204,10 @@ struct sb_engine {
             cuda_check(cudaMemsetAsync(tot + sbk::place_total_word(a + 1), 0, 4, stream), "memset");
             if (m > 0) {
               pp.draw_base = draws + before;
-              cuda_check(cudaEventRecord(ev_r0, stream), "event");
               sbk::place_fast_round(pp, a, grid, smem, s);
-              cuda_check(cudaEventRecord(ev_r1, stream), "event");
               launches += 1;
               round_launches += 1;
               m = read_total(a + 1);
-              float ms = 0.f;
-              cuda_check(cudaEventElapsedTime(&ms, ev_r0, ev_r1), "elapsed");
-              sharded_check_ms += ms;
             } else {
               m = 0;
             }
@@ -1254,7 +1321,6 @@ struct sb_engine {
       pending_per_inst[p] = places[p].dev.anchor_object >= 0 && rflags[2 * p] != 0;
     pending_rounds.assign(P, 0);
     for (size_t p = 0; p < P; ++p) pending_rounds[p] = device_rounds[p] ? ctrl_all[8 * p + 2] : 0u;
-    pending_sharded_ms = sharded_check_ms;
     timing_pending = true;
     const auto th2a = std::chrono::steady_clock::now();
     uint64_t rounds = rounds_host;
@@ -1294,7 +1360,9 @@ struct sb_engine {
       st->triangle_pair_tests = c[2];
       st->candidates_sampled = c[3];
       st->rounds = rounds;
-      st->per_instance_placements = c[7] + per_inst_host;
+      uint64_t per_inst_dev = 0;  // sharded relation placements decided on the device
+      for (size_t p = 0; p < P; ++p) per_inst_dev += shard_dev_relation[p] && rflags[2 * p] != 0;
+      st->per_instance_placements = c[7] + per_inst_host + per_inst_dev;
       st->broad_phase_tests = c[4];
       st->node_pair_tests = c[5];
       st->accepted_candidates = c[6];
@@ -1337,7 +1405,7 @@ struct sb_engine {
     last_prof[10] = inst_ms;
     last_prof[11] = fast_ms;
     last_total_ms = total_ms;
-    last_check_ms = world_size == 1 ? place_ms : pending_sharded_ms;
+    last_check_ms = place_ms;  // placement intervals (sharded: incl. exchange waits)
   }
 
   void download(sb_result* out) {

@@ -81,12 +81,28 @@ struct sb_sampler {
     cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
   }
   ~sb_sampler() {
-    if (ev_seg) cudaEventDestroy(ev_seg);
+    if (ev_busy) {
+      cudaEventSynchronize(ev_busy);
+      cudaEventDestroy(ev_busy);
+    }
     if (stream) {
       cudaSetDevice(device);
       cudaStreamSynchronize(stream);
       cudaStreamDestroy(stream);
     }
+  }
+
+  // Every kernel that reads the sampler's device tables or segment buffer is followed by
+  // ev_busy (on whichever stream it ran: the internal one or a caller's). Host code that
+  // rewrites h_seg / d_seg / the region tables first waits for it, so a later prepare() or
+  // sample() cannot overwrite buffers an earlier, still running sample_device kernel reads.
+  cudaEvent_t ev_busy = nullptr;
+  void quiesce() {
+    if (ev_busy) cuda_check(cudaEventSynchronize(ev_busy), "sync sampler kernels");
+  }
+  void mark_busy(cudaStream_t st) {
+    if (!ev_busy) cuda_check(cudaEventCreateWithFlags(&ev_busy, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventRecord(ev_busy, st), "event");
   }
 
   void clear_queue() {
@@ -99,6 +115,7 @@ struct sb_sampler {
   void prepare(const double* xy, const uint32_t* off, uint32_t n_rings, const uint32_t* inst_rings,
                uint64_t batch, uint64_t seed) {
     cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    quiesce();
     if (n_rings && (!xy || !off)) throw std::invalid_argument("ring arrays are NULL");
     for (uint32_t r = 0; r < n_rings; ++r)
       if (off[r + 1] < off[r]) throw std::invalid_argument("ring_offsets must be non-decreasing");
@@ -164,6 +181,7 @@ struct sb_sampler {
   void prepare_relation(const sb_relation& rel, const double rect[4], const double* states,
                         uint64_t batch, uint64_t seed) {
     cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    quiesce();
     if (batch == 0) throw std::invalid_argument("anchor state batch is empty");
     if (batch > 0xffffffffull) throw std::invalid_argument("batch_size exceeds 2^32");
     SbPlacementDev pd;
@@ -291,6 +309,7 @@ struct sb_sampler {
     if (m && (!active || !pos || !placeable || !support))
       throw std::invalid_argument("sample: NULL array");
     cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    quiesce();
     if (!per_instance && region_empty) {  // sampler.cpp:81-84
       std::memset(pos, 0, 3 * m * sizeof(double));
       std::memset(placeable, 0, m);
@@ -348,7 +367,6 @@ struct sb_sampler {
   // Device-resident variant: supports (N column-major Mat4), active, positions and
   // placeable are device pointers; everything is enqueued on `st` (no host round trip but
   // the SampleCache bookkeeping, which stays on the host).
-  cudaEvent_t ev_seg = nullptr;
   void sample_device(const double* d_sup16, const uint32_t* d_act, uint64_t m, uint64_t attempt,
                      double* d_out, uint8_t* d_placeable, cudaStream_t st) {
     if (!prepared) throw std::logic_error("PositionSampler: prepare() not called");
@@ -365,16 +383,15 @@ struct sb_sampler {
     if (!per_instance && region_nt == 0)
       throw std::invalid_argument("sample: canonical region has zero area");
     if (!per_instance) {
-      if (!ev_seg) cuda_check(cudaEventCreateWithFlags(&ev_seg, cudaEventDisableTiming), "event");
-      cuda_check(cudaEventSynchronize(ev_seg), "sync segments");  // h_seg reusable
+      quiesce();  // h_seg / d_seg are rewritten below
       const int nseg = drain(m);
       if (m == 0) return;
       d_seg.ensure(2 * nseg);
       cuda_check(cudaMemcpyAsync(d_seg.p, h_seg.p, 2 * nseg * sizeof(uint64_t), cudaMemcpyHostToDevice, st), "H2D segments");
-      cuda_check(cudaEventRecord(ev_seg, st), "event");
       sbk::sampler_fifo(nullptr, d_sup16, d_act, m, d_seg.p, d_seg.p + nseg, nseg,
                         cache_state0(run_seed, salt), d_tris.p, d_cum.p, region_nt, d_out,
                         reinterpret_cast<sb_stream_t>(st));
+      mark_busy(st);
       cuda_check(cudaMemsetAsync(d_placeable, 1, m, st), "memset");
       return;
     }
@@ -382,6 +399,7 @@ struct sb_sampler {
     sbk::sampler_fallback(nullptr, d_sup16, d_act, m, run_seed, salt, attempt,
                           stride_tables ? nullptr : d_inst_tab.p, d_inst_n.p, table_cap, d_tris.p,
                           d_cum.p, d_out, d_placeable, reinterpret_cast<sb_stream_t>(st));
+    mark_busy(st);
   }
 };
 
