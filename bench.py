@@ -10,7 +10,9 @@ Default workload: C4 (262,144 variations x 100 sphere-set objects), the largest
 single-GPU configuration BASELINE.json names (its `metric` is not quoted on any config).
 N>1 runs under torchrun (one rank per GPU): instances are sharded by contiguous
 variation ranges (weak scaling: N_per_gpu fixed); the only exchange is the fast-path
-per-round count all-gather (8 bytes per rank per round).
+per-round count all-gather (8 bytes per rank per round) and a relation placement's
+instance-0 anchor state, both through the library's native communicator (sb_comm: no
+torch.distributed, no NCCL on the data path).
 `value` times results resident in HBM (CUDA events on the engine stream, L2 flushed
 between steps); `e2e` times the same call with the results copied to pinned host memory.
 --impl reference times the reference itself (oracle/_ref/libsbref.so: its own sources
@@ -25,6 +27,7 @@ import json
 import math
 import os
 import statistics
+import struct
 import subprocess
 import sys
 import threading
@@ -135,9 +138,7 @@ FLOPS = {
 
 
 def run_ours(args, rank, world, local_rank):
-    import numpy as np
     import torch
-    import torch.distributed as dist
 
     import paper_2512_16896_b200 as pkg
 
@@ -145,18 +146,18 @@ def run_ours(args, rank, world, local_rank):
     n_per = args.n or n_default
     n_total = n_per * world
     scene = factory(n_total)
-    device = local_rank
+    # one process per GPU (local_rank modulo the visible devices, so a 2-rank run can also be
+    # exercised on a single GPU)
+    device = local_rank % max(1, torch.cuda.device_count())
     torch.cuda.set_device(device)
 
-    shard = None
+    shard = comm = None
     if world > 1:
-        from paper_2512_16896_b200.dist import torch_allgather
-
-        xdev = getattr(args, "xdev", None)
-        from paper_2512_16896_b200.dist import nccl_allgather_dev
-        shard = pkg.Shard(rank * n_per, (rank + 1) * n_per, rank, world,
-                          torch_allgather(world, xdev),
-                          nccl_allgather_dev(world, xdev) if xdev is not None else None)
+        # the engine's exchange is native (sb_comm: TCP bootstrap at MASTER_ADDR /
+        # MASTER_PORT + 1, count boards mapped over NVLink / NVSwitch by CUDA IPC); the same
+        # communicator provides the timing barrier and the max-over-ranks reduction
+        comm = pkg.Comm(rank, world, device=device)
+        shard = comm.shard(n_total)
     t0 = time.time()
     eng = pkg.Engine(scene, shard, device=device)
     cold_s = time.time() - t0
@@ -173,9 +174,9 @@ def run_ours(args, rank, world, local_rank):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{device}")
 
     def barrier():
-        if world > 1:
-            dist.barrier()
         torch.cuda.synchronize()
+        if world > 1:
+            comm.barrier()
 
     seed = 1
     for _ in range(args.warmup):
@@ -214,12 +215,14 @@ def run_ours(args, rank, world, local_rank):
     mine = {"time_ms": sum(step_ms), "e2e_ms": statistics.median(e2e_ms),
             "valid": agg["valid_instances"] / K, "checks": agg["candidate_checks"] / K}
     if world > 1:
-        t = torch.tensor([mine["time_ms"], mine["e2e_ms"]], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        s = torch.tensor([mine["valid"], mine["checks"]], dtype=torch.float64)
-        dist.all_reduce(s, op=dist.ReduceOp.SUM)
-        time_ms, e2e = t.tolist()
-        valid_sum, checks_sum = s.tolist()
+        keys = ("time_ms", "e2e_ms", "valid", "checks")
+        bits = comm.allgather([struct.unpack("<Q", struct.pack("<d", float(mine[k])))[0] for k in keys])
+        vals = [struct.unpack("<d", struct.pack("<Q", b))[0] for b in bits]
+        per_rank = [dict(zip(keys, vals[4 * r:4 * r + 4])) for r in range(world)]
+        time_ms = max(d["time_ms"] for d in per_rank)  # device time, max over ranks
+        e2e = max(d["e2e_ms"] for d in per_rank)
+        valid_sum = sum(d["valid"] for d in per_rank)
+        checks_sum = sum(d["checks"] for d in per_rank)
     else:
         time_ms, e2e, valid_sum, checks_sum = (mine["time_ms"], mine["e2e_ms"], mine["valid"],
                                                mine["checks"])
@@ -298,7 +301,7 @@ def run_ours(args, rank, world, local_rank):
         "phase_profile_per_step": {k: round(v, 4) for k, v in phases.items()},
         "clocks": clk,
     }
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:  # rank 0 at N=1 only
         line["cpu_baseline"] = cpu_baseline(args)
     return line
 
@@ -419,7 +422,6 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     rank, world, local_rank = dist_env()
-    args.xdev = None
     if args.impl == "reference":
         # rank 0 alone times the reference; no process group, nothing of this package's
         # library is loaded in this process
@@ -427,18 +429,9 @@ def main():
         if line is not None:
             print(json.dumps(line), flush=True)
         return
-    if world > 1:
-        from paper_2512_16896_b200.dist import init_group
-
-        args.xdev = init_group(local_rank)
     line = run_ours(args, rank, world, local_rank)
     if line is not None:
         print(json.dumps(line), flush=True)
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.barrier()
-        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

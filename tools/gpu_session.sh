@@ -9,10 +9,16 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gp
 lscpu | head -20 > gpurun_out/cpu_${TAG}.txt
 for st in $STAGES; do
   case $st in
-    tests) echo "== pytest -m gpu"; timeout ${TEST_TIMEOUT:-1500} python -m pytest tests -x -q -m gpu ${PYTEST_EXTRA:-} > gpurun_out/pytest_${TAG}.log 2>&1; tail -5 gpurun_out/pytest_${TAG}.log ;;
+    tests) echo "== pytest -m gpu"; timeout ${TEST_TIMEOUT:-1500} python -m pytest tests -x -q -m gpu ${PYTEST_K:+-k "$PYTEST_K"} ${PYTEST_EXTRA:-} > gpurun_out/pytest_${TAG}.log 2>&1; tail -5 gpurun_out/pytest_${TAG}.log ;;
     smoke) echo "== smoke"; timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2 ;;
     bench) echo "== bench"; timeout 1200 python bench.py --steps ${STEPS:-20} --warmup ${WARMUP:-5} ${BENCH_EXTRA:-} > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err; tail -c 1500 gpurun_out/bench_${TAG}.json; tail -2 gpurun_out/bench_${TAG}.err ;;
     ref) echo "== reference arm"; timeout 1800 python bench.py --impl reference --steps ${STEPS:-20} --warmup ${WARMUP:-5} ${BENCH_EXTRA:-} > gpurun_out/bench_ref_${TAG}.json 2> gpurun_out/bench_ref_${TAG}.err; tail -c 800 gpurun_out/bench_ref_${TAG}.json; tail -2 gpurun_out/bench_ref_${TAG}.err ;;
+    multi) echo "== 2-rank bench on this box (both ranks share the visible GPUs)"
+      for c in ${MULTI_CONFIGS:-c2_mixed c4_clutter}; do
+        timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29611 \
+          bench.py --gpus 2 --steps ${STEPS:-5} --warmup 3 --config $c --no-cpu-baseline > gpurun_out/multi_${TAG}_$c.json 2> gpurun_out/multi_${TAG}_$c.err
+        echo "$c rc=$?"; tail -c 400 gpurun_out/multi_${TAG}_$c.json; tail -3 gpurun_out/multi_${TAG}_$c.err
+      done ;;
     configs) : > gpurun_out/configs_${TAG}.jsonl
       for c in ${CONFIGS:-c1_tabletop c2_mixed c3_kitchen c4_clutter c5_sweep10 c5_sweep100}; do
         timeout 900 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline >> gpurun_out/configs_${TAG}.jsonl 2> gpurun_out/err_$c.log || echo "{\"config\": \"$c\", \"failed\": true}" >> gpurun_out/configs_${TAG}.jsonl
