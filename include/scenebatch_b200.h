@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define SB_ABI_VERSION 1
+#define SB_ABI_VERSION 2
 
 typedef enum sb_status {
   SB_OK = 0,
@@ -144,7 +144,10 @@ sb_status sb_reset_stats(sb_world* w);
  * compose (transform.hpp:40-54), build_constraint_region (relationships.cpp:161-218) and
  * CollisionWorld::check_batch into one on-device pipeline.
  * ---------------------------------------------------------------------------------- */
-enum { SB_DIST_NONE = 0, SB_DIST_GREATER = 1, SB_DIST_LESS = 2, SB_DIST_EQUAL = 3 };
+enum { SB_DIST_NONE = 0, SB_DIST_GREATER = 1, SB_DIST_LESS = 2, SB_DIST_EQUAL = 3,
+       SB_DIST_MIDDLE = 4 };                                  /* relationships.hpp:12 */
+#define SB_MAX_ANCHORS 8          /* anchors per relation (RelationshipSpec::anchors) */
+#define SB_MAX_SUPPORT_VERTS 16   /* vertices of a convex polygon support */
 enum { SB_DIR_NONE = 0, SB_DIR_LEFT = 1, SB_DIR_RIGHT = 2, SB_DIR_FRONT = 3, SB_DIR_BACK = 4,
        SB_DIR_VECTOR = 5 };                                   /* relationships.hpp:12-14 */
 enum { SB_FRAME_GLOBAL = 0, SB_FRAME_LOCAL = 1 };
@@ -167,8 +170,12 @@ typedef struct sb_fixed_object {
   const double* poses16;
 } sb_fixed_object;
 
-/* A support surface: axis-aligned rect [x0,x1]x[y0,y1] in the z=0 plane of its frame
- * (SupportSurface, surface.hpp:15-20, given directly or from sb_extract_support_surfaces).
+/* A support surface in the z=0 plane of its frame (SupportSurface, surface.hpp:15-20,
+ * given directly or from sb_extract_support_surfaces): the axis-aligned rect
+ * [x0,x1]x[y0,y1] (make_rect order), or, when n_polygon >= 3, the convex polygon
+ * polygon_xy[0..2*n_polygon) (SupportSurface::polygon as given: its vertex order and start
+ * feed the sampler triangulation; clipping uses it corrected to counter-clockwise). A
+ * polygon that is an axis-aligned rectangle clips exactly as a rect does.
  * The frame per instance is the reference's support_world[inst] (sampler.hpp:78-80,
  * sampler.cpp:90,119; built by the driver from BatchedSceneGraph::world_poses,
  * scene_graph.cpp:126-147, times the surface frame):
@@ -179,21 +186,27 @@ typedef struct sb_fixed_object {
  *   else: `pose` for every instance. */
 typedef struct sb_support {
   double pose[16];
-  double rect[4]; /* x0, y0, x1, y1 */
+  double rect[4]; /* x0, y0, x1, y1 (ignored when n_polygon >= 3) */
   const double* poses16;
   int32_t on_placement;
-  int32_t reserved;
+  uint32_t n_polygon;        /* 0 = rect, else 3..SB_MAX_SUPPORT_VERTS */
+  const double* polygon_xy;  /* n_polygon (x, y) pairs, convex */
 } sb_support;
 
-/* RelationshipSpec (relationships.hpp:18-38) restricted to zero or one anchor. */
+/* RelationshipSpec (relationships.hpp:18-38). anchors = {anchor, extra_anchors[0..n)}
+ * (placement indices, each < this placement); greater/less/equal and a direction take
+ * exactly one anchor, `middle` two or more (RelationshipSpec::validate,
+ * relationships.cpp:59-76); the per-instance test covers every anchor (:178-186). */
 typedef struct sb_relation {
-  int32_t anchor;          /* placement index of the anchor (< this placement), -1 = none */
+  int32_t anchor;          /* placement index of the first anchor, -1 = none */
   int32_t distance_type;   /* SB_DIST_* */
   int32_t direction;       /* SB_DIR_* */
   int32_t frame;           /* SB_FRAME_* */
   double direction_vector[2];
   double distance;
   double angle_threshold;  /* <= 0: default (pi/4 with a direction, pi without) */
+  int32_t n_extra_anchors; /* further anchors, 0..SB_MAX_ANCHORS-1 */
+  int32_t extra_anchors[SB_MAX_ANCHORS - 1];
 } sb_relation;
 
 /* PlacementSpec (config.hpp:45-54) subset on the hot path. */
@@ -280,12 +293,22 @@ void sb_comm_destroy(sb_comm* c);
  * (valid while the comm lives). */
 sb_status sb_comm_shard(sb_comm* c, uint64_t n_total, sb_shard* out);
 sb_status sb_comm_allgather(sb_comm* c, const uint64_t* send, uint32_t n, uint64_t* recv);
-/* n <= 15 u64 of device memory per rank, enqueued on cuda_stream (a cudaStream_t). */
+/* n <= 31 u64 of device memory per rank, enqueued on cuda_stream (a cudaStream_t). */
 sb_status sb_comm_allgather_dev(sb_comm* c, const uint64_t* d_send, uint32_t n, uint64_t* d_recv,
                                 void* cuda_stream);
 sb_status sb_comm_barrier(sb_comm* c);
 /* 1 if the device exchange waits with stream memory operations, 0 if it spins a kernel. */
 int32_t sb_comm_uses_stream_waits(const sb_comm* c);
+
+/* Test hook (host, no GPU): region_for(0) of build_constraint_region + apply_ratio_on_support
+ * (relationships.cpp:161-230) restated on the host with the serial region path's code
+ * (sb_poly.h) and glibc as libm -- states: (x, y, yaw) per anchor in the support frame --
+ * then n PolygonSampler::draw points from Pcg32(make_stream(seed, c)) (polygon.cpp:390-400).
+ * *n_tris = 0: empty region (no draws). */
+sb_status sb_region_draws_host(const sb_relation* rel, const sb_support* support,
+                               const double* states, double erode_r, uint64_t seed,
+                               const uint64_t* c, uint32_t nc, double* out_xy, uint32_t n,
+                               int32_t* n_tris);
 
 typedef struct sb_engine sb_engine;
 

@@ -66,6 +66,10 @@ def lib():
         L.ref_polygon_draws.argtypes = [C.c_void_p, C.c_uint32, u64, C.c_void_p, C.c_uint32,
                                         C.c_void_p, C.c_uint32]
         L.ref_triangulate.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint32, C.c_void_p]
+        L.ref_region_draws.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_double,
+                                       C.c_double, u64, C.c_void_p, C.c_uint32, C.c_void_p,
+                                       C.c_uint32, C.c_void_p]
+        L.ref_middle_polygon.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint32, C.c_void_p]
         L.ref_relation_region.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_double,
                                           C.c_double, C.c_void_p, C.c_uint32, C.c_void_p,
                                           C.c_void_p]
@@ -201,6 +205,27 @@ def triangulate(ring) -> np.ndarray:
     nt = C.c_uint32()
     check(lib().ref_triangulate(_p(r), len(r), _p(out), 512, C.byref(nt)))
     return out[: nt.value].reshape(-1, 3, 2)
+
+
+def region_draws(rel_c, sup_c, states, ratio, fx, fy, seed, c, n):
+    """region_for(0) of build_constraint_region (+ apply_ratio_on_support) for one instance's
+    anchor states ((na, 3): x, y, yaw) -> (n draws (n, 2), sampler triangle count)."""
+    st = np.ascontiguousarray(np.asarray(states, np.float64).reshape(-1))
+    cc = np.ascontiguousarray(np.asarray(c, np.uint64))
+    out = np.zeros((max(n, 1), 2))
+    nt = C.c_int32()
+    check(lib().ref_region_draws(C.byref(rel_c), C.byref(sup_c), _p(st) if st.size else None,
+                                 ratio, fx, fy, seed, _p(cc), len(cc), _p(out), n, C.byref(nt)))
+    return out[:n].copy(), nt.value
+
+
+def middle_polygon(points):
+    """middle_polygon (relationships.cpp:124-157) -> exterior ring (k, 2)."""
+    xy = np.ascontiguousarray(np.asarray(points, np.float64).reshape(-1, 2))
+    out = np.zeros((256, 2))
+    k = C.c_uint32()
+    check(lib().ref_middle_polygon(_p(xy), len(xy), _p(out), 256, C.byref(k)))
+    return out[: k.value].copy()
 
 
 def relation_region(rel_c, rect, ax, ay, ayaw):

@@ -97,10 +97,32 @@ struct RefWorld {
   }
 };
 
+// RelationshipSpec::anchors of an sb_relation: {anchor, extra_anchors...}
+std::vector<int32_t> anchors_of(const sb_relation& r) {
+  std::vector<int32_t> out;
+  if (r.anchor < 0) return out;
+  out.push_back(r.anchor);
+  if (r.n_extra_anchors < 0 || r.n_extra_anchors > SB_MAX_ANCHORS - 1)
+    throw std::invalid_argument("relationship: n_extra_anchors outside [0, 7]");
+  for (int k = 0; k < r.n_extra_anchors; ++k) out.push_back(r.extra_anchors[k]);
+  return out;
+}
+
+// the support polygon of an sb_support: the rect (make_rect order) or the given ring
+MultiPolygon2D support_region_of(const sb_support& sup) {
+  if (sup.n_polygon == 0)
+    return MultiPolygon2D::from(make_rect(sup.rect[0], sup.rect[1], sup.rect[2], sup.rect[3]));
+  if (sup.n_polygon < 3 || !sup.polygon_xy) throw std::invalid_argument("support polygon needs >= 3 vertices");
+  Polygon2D p;
+  for (uint32_t k = 0; k < sup.n_polygon; ++k)
+    p.exterior.emplace_back(sup.polygon_xy[2 * k], sup.polygon_xy[2 * k + 1]);
+  return MultiPolygon2D::from(p);
+}
+
 RelationshipSpec spec_from(const sb_relation& r) {
   RelationshipSpec s;
   s.kind = SurfaceMode::on;
-  if (r.anchor >= 0) s.anchors.push_back("p" + std::to_string(r.anchor));
+  for (int32_t a : anchors_of(r)) s.anchors.push_back("p" + std::to_string(a));
   s.distance_type = static_cast<DistanceType>(r.distance_type);
   s.direction = static_cast<DirectionKind>(r.direction);
   s.frame = static_cast<DirectionFrame>(r.frame);
@@ -194,6 +216,51 @@ int ref_triangulate(const double* ring, uint32_t nring, double* out, uint32_t ma
 }
 uint64_t ref_region_fingerprint_rect(double x0, double y0, double x1, double y1) {
   return region_fingerprint(MultiPolygon2D::from(make_rect(x0, y0, x1, y1)));
+}
+// region_for(0): build_constraint_region(spec, support, {anchor states}, 1) +
+// apply_ratio_on_support(ratio, footprint fx x fy) (relationships.cpp:161-230), then n draws
+// of PolygonSampler(region) from Pcg32(make_stream(seed, c)). states: (x, y, yaw) per
+// anchor. *ntri = triangle count of the region's sampler (0: empty region).
+int ref_region_draws(const sb_relation* rel, const sb_support* sup, const double* states,
+                     double ratio, double fx, double fy, uint64_t seed, const uint64_t* c,
+                     uint32_t nc, double* out, uint32_t n, int32_t* ntri) {
+  REF_TRY({
+    RelationshipSpec spec = spec_from(*rel);
+    MultiPolygon2D support = support_region_of(*sup);
+    std::vector<std::vector<AnchorState>> anchors;
+    const std::size_t na = anchors_of(*rel).size();
+    for (std::size_t a = 0; a < na; ++a) {
+      AnchorState s;
+      s.position = Vec2(states[3 * a], states[3 * a + 1]);
+      s.yaw = states[3 * a + 2];
+      anchors.push_back({s});
+    }
+    ConstraintRegion cr = build_constraint_region(spec, support, anchors, 1);
+    if (ratio != 0.0) apply_ratio_on_support(cr, fx, fy, ratio);
+    PolygonSampler ps(cr.region);
+    *ntri = static_cast<int32_t>(ps.triangle_count());
+    uint64_t h = mix64(seed);
+    for (uint32_t i = 0; i < nc; ++i) h = mix64(h ^ c[i]);
+    Pcg32 r(h);
+    for (uint32_t i = 0; i < n && ps.valid(); ++i) {
+      Vec2 q = ps.draw(r);
+      out[2 * i] = q.x();
+      out[2 * i + 1] = q.y();
+    }
+  });
+}
+// middle_polygon (relationships.cpp:124-157) of n points -> exterior ring.
+int ref_middle_polygon(const double* xy, uint32_t n, double* out, uint32_t cap, uint32_t* nout) {
+  REF_TRY({
+    std::vector<Vec2> pts;
+    for (uint32_t i = 0; i < n; ++i) pts.emplace_back(xy[2 * i], xy[2 * i + 1]);
+    Polygon2D p = middle_polygon(pts);
+    *nout = static_cast<uint32_t>(p.exterior.size());
+    for (std::size_t i = 0; i < p.exterior.size() && i < cap; ++i) {
+      out[2 * i] = p.exterior[i].x();
+      out[2 * i + 1] = p.exterior[i].y();
+    }
+  });
 }
 // build_constraint_region for one anchor state, return the region's exterior ring(s).
 // out: flattened xy of part 0 exterior (max_pts), *npts, *nparts.
@@ -670,8 +737,7 @@ void RefEngine::generate(uint64_t run_seed, sb_result* out, sb_run_stats* st,
       const int geom = geom_of_mesh.at(pl.mesh);
       const double z_off = rest_pose(meshes.at(pl.mesh)).z_offset;
       Mat4 sup_pose = mat_from(sup.pose);
-      MultiPolygon2D support_region =
-          MultiPolygon2D::from(make_rect(sup.rect[0], sup.rect[1], sup.rect[2], sup.rect[3]));
+      MultiPolygon2D support_region = support_region_of(sup);
       RelationshipSpec spec = spec_from(pl.relation);
 
       // support_world (sampler.hpp:78-80), GLOBAL instance order: the surface of an earlier
@@ -687,49 +753,58 @@ void RefEngine::generate(uint64_t run_seed, sb_result* out, sb_run_stats* st,
       }
       // Anchor states in the support frame, indexed by GLOBAL instance id.
       std::vector<std::vector<AnchorState>> anchors;
-      if (pl.relation.anchor >= 0) {
-        const int aobj = obj_of_placement.at(pl.relation.anchor);
-        std::vector<AnchorState> local(n_local);
-        for (std::size_t i = 0; i < n_local; ++i) {
-          Mat4 rel = inverse_rigid(support_world[begin + i]) * w.world.object_pose(aobj, i);
-          local[i].position = Vec2(rel(0, 3), rel(1, 3));
-          local[i].yaw = yaw_of(rel);
+      const std::vector<int32_t> anchor_ids = anchors_of(pl.relation);
+      if (!anchor_ids.empty()) {
+        const std::size_t na = anchor_ids.size();
+        std::vector<std::vector<AnchorState>> local(na, std::vector<AnchorState>(n_local));
+        for (std::size_t a = 0; a < na; ++a) {
+          const int aobj = obj_of_placement.at(anchor_ids[a]);
+          for (std::size_t i = 0; i < n_local; ++i) {
+            Mat4 rel = inverse_rigid(support_world[begin + i]) * w.world.object_pose(aobj, i);
+            local[a][i].position = Vec2(rel(0, 3), rel(1, 3));
+            local[a][i].yaw = yaw_of(rel);
+          }
         }
-        std::vector<AnchorState> all(n_total);
+        std::vector<std::vector<AnchorState>> all(na, std::vector<AnchorState>(n_total));
         if (world_size == 1) {
           all = local;
         } else {
-          // instance 0 lives on rank 0; exchange its state and each rank's vary flag
-          // (relationships.cpp:178-186 compares every instance against instance 0).
-          std::vector<uint64_t> send(4, 0);
-          if (begin == 0) {
-            std::memcpy(&send[0], &local[0].position.x(), 8);
-            std::memcpy(&send[1], &local[0].position.y(), 8);
-            std::memcpy(&send[2], &local[0].yaw, 8);
-          }
-          std::vector<uint64_t> recv = allgather(send);
-          AnchorState s0;
-          double tmp[3];
-          std::memcpy(tmp, &recv[0], 24);  // rank 0's slots
-          s0.position = Vec2(tmp[0], tmp[1]);
-          s0.yaw = tmp[2];
+          // instance 0 lives on rank 0; exchange its anchor states and each rank's vary
+          // flag (relationships.cpp:178-186 compares every instance against instance 0).
+          std::vector<uint64_t> send(3 * na, 0);
+          if (begin == 0)
+            for (std::size_t a = 0; a < na; ++a) {
+              std::memcpy(&send[3 * a + 0], &local[a][0].position.x(), 8);
+              std::memcpy(&send[3 * a + 1], &local[a][0].position.y(), 8);
+              std::memcpy(&send[3 * a + 2], &local[a][0].yaw, 8);
+            }
+          std::vector<uint64_t> recv = allgather(send);  // rank 0's slots first
+          std::vector<AnchorState> s0(na);
           bool local_vary = false;
-          for (std::size_t i = 0; i < n_local; ++i)
-            if ((local[i].position - s0.position).norm() > 1e-12 ||
-                std::abs(local[i].yaw - s0.yaw) > 1e-12)
-              local_vary = true;
+          for (std::size_t a = 0; a < na; ++a) {
+            double tmp[3];
+            std::memcpy(tmp, &recv[3 * a], 24);
+            s0[a].position = Vec2(tmp[0], tmp[1]);
+            s0[a].yaw = tmp[2];
+            for (std::size_t i = 0; i < n_local; ++i)
+              if ((local[a][i].position - s0[a].position).norm() > 1e-12 ||
+                  std::abs(local[a][i].yaw - s0[a].yaw) > 1e-12)
+                local_vary = true;
+          }
           std::vector<uint64_t> flags = allgather({local_vary ? 1ull : 0ull});
           bool global_vary = false;
           for (uint64_t f : flags) global_vary = global_vary || f != 0;
-          for (std::size_t i = 0; i < n_total; ++i) all[i] = s0;
-          for (std::size_t i = 0; i < n_local; ++i) all[begin + i] = local[i];
+          for (std::size_t a = 0; a < na; ++a) {
+            for (std::size_t i = 0; i < n_total; ++i) all[a][i] = s0[a];
+            for (std::size_t i = 0; i < n_local; ++i) all[a][begin + i] = local[a][i];
+          }
           if (global_vary && !local_vary) {
             // force the per-instance path through a non-local slot (never sampled here)
             std::size_t slot = begin == 0 ? n_total - 1 : 0;
-            all[slot].position = s0.position + Vec2(1.0, 0.0);
+            all[0][slot].position = s0[0].position + Vec2(1.0, 0.0);
           }
         }
-        anchors.push_back(std::move(all));
+        for (auto& a : all) anchors.push_back(std::move(a));
       }
       ConstraintRegion cr = build_constraint_region(spec, support_region, anchors, n_total);
       if (pl.ratio_on_support != 0.0) {  // footprint = the mesh AABB's x / y extents

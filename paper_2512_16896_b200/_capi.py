@@ -18,7 +18,9 @@ SB_ERR_LOGIC = 3
 SB_ERR_RUNTIME = 4
 SB_ERR_CUDA = 5
 
-SB_DIST_NONE, SB_DIST_GREATER, SB_DIST_LESS, SB_DIST_EQUAL = 0, 1, 2, 3
+SB_DIST_NONE, SB_DIST_GREATER, SB_DIST_LESS, SB_DIST_EQUAL, SB_DIST_MIDDLE = 0, 1, 2, 3, 4
+SB_MAX_ANCHORS = 8
+SB_MAX_SUPPORT_VERTS = 16
 SB_DIR_NONE, SB_DIR_LEFT, SB_DIR_RIGHT, SB_DIR_FRONT, SB_DIR_BACK, SB_DIR_VECTOR = range(6)
 SB_FRAME_GLOBAL, SB_FRAME_LOCAL = 0, 1
 SB_ORIENT_FIXED, SB_ORIENT_UNIFORM_YAW, SB_ORIENT_FACE_TO = 0, 1, 2
@@ -42,7 +44,7 @@ class sb_fixed_object(C.Structure):
 class sb_support(C.Structure):
     _fields_ = [("pose", C.c_double * 16), ("rect", C.c_double * 4),
                 ("poses16", C.POINTER(C.c_double)), ("on_placement", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("n_polygon", C.c_uint32), ("polygon_xy", C.POINTER(C.c_double))]
 
 
 class sb_joint(C.Structure):
@@ -65,7 +67,8 @@ class sb_reach_info(C.Structure):
 class sb_relation(C.Structure):
     _fields_ = [("anchor", C.c_int32), ("distance_type", C.c_int32), ("direction", C.c_int32),
                 ("frame", C.c_int32), ("direction_vector", C.c_double * 2),
-                ("distance", C.c_double), ("angle_threshold", C.c_double)]
+                ("distance", C.c_double), ("angle_threshold", C.c_double),
+                ("n_extra_anchors", C.c_int32), ("extra_anchors", C.c_int32 * (SB_MAX_ANCHORS - 1))]
 
 
 class sb_placement(C.Structure):
@@ -142,6 +145,9 @@ SIGNATURES = {
                                  C.POINTER(C.c_int32)]),
     "sb_get_stats": (C.c_int, [_P, C.POINTER(sb_stats)]),
     "sb_reset_stats": (C.c_int, [_P]),
+    "sb_region_draws_host": (C.c_int, [C.POINTER(sb_relation), C.POINTER(sb_support), _D, C.c_double,
+                                       C.c_uint64, C.POINTER(C.c_uint64), C.c_uint32, _D, C.c_uint32,
+                                       C.POINTER(C.c_int32)]),
     "sb_comm_create": (C.c_int, [C.c_int32, C.c_int32, C.c_int, C.c_char_p, C.c_int32, C.c_double,
                                  C.POINTER(_P)]),
     "sb_comm_destroy": (None, [_P]),

@@ -65,17 +65,18 @@ __global__ void k_comm_collect(const uint64_t* board, int world, int slot, uint6
   }
 }
 
-__global__ void k_anchor_pack(const double* s0, uint64_t* send) {
-  const int t = threadIdx.x;
-  if (t < 3) send[t] = s0 ? __double_as_longlong(s0[t]) : 0ull;
-  if (t == 3) send[3] = s0 ? 1ull : 0ull;
+__global__ void k_anchor_pack(const double* s0, int na, uint64_t* send) {
+  const int t = threadIdx.x, m = 3 * na;
+  if (t < m) send[t] = s0 ? __double_as_longlong(s0[t]) : 0ull;
+  if (t == m) send[m] = s0 ? 1ull : 0ull;
 }
 
-__global__ void k_anchor_pick(const uint64_t* recv, int world, double* s0) {
+__global__ void k_anchor_pick(const uint64_t* recv, int world, int na, double* s0) {
   if (threadIdx.x != 0) return;
+  const int m = 3 * na, stride = m + 1;
   for (int r = 0; r < world; ++r)
-    if (recv[4 * r + 3]) {
-      for (int k = 0; k < 3; ++k) s0[k] = __longlong_as_double(recv[4 * r + k]);
+    if (recv[stride * r + m]) {
+      for (int k = 0; k < m; ++k) s0[k] = __longlong_as_double(recv[stride * r + k]);
       return;
     }
 }
@@ -114,12 +115,12 @@ void comm_collect(const uint64_t* board, int world_size, int slot, uint64_t epoc
   check_launch("k_comm_collect");
 }
 
-void shard_anchor_pack(const double* s0, uint64_t* send4, sb_stream_t s) {
-  k_anchor_pack<<<1, 32, 0, reinterpret_cast<cudaStream_t>(s)>>>(s0, send4);
+void shard_anchor_pack(const double* s0, int na, uint64_t* send, sb_stream_t s) {
+  k_anchor_pack<<<1, 32, 0, reinterpret_cast<cudaStream_t>(s)>>>(s0, na, send);
   check_launch("k_anchor_pack");
 }
-void shard_anchor_pick(const uint64_t* recv, int world_size, double* s0, sb_stream_t s) {
-  k_anchor_pick<<<1, 32, 0, reinterpret_cast<cudaStream_t>(s)>>>(recv, world_size, s0);
+void shard_anchor_pick(const uint64_t* recv, int world_size, int na, double* s0, sb_stream_t s) {
+  k_anchor_pick<<<1, 32, 0, reinterpret_cast<cudaStream_t>(s)>>>(recv, world_size, na, s0);
   check_launch("k_anchor_pick");
 }
 void shard_flag_pack(const int32_t* flag, uint64_t* send1, sb_stream_t s) {

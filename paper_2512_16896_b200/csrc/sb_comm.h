@@ -15,7 +15,7 @@ typedef struct CUstream_st* sb_stream_t;
 namespace sbk {
 
 constexpr int kCommSlots = 64;      // exchanges in flight before a slot is reused
-constexpr int kCommStride = 16;     // u64 words per (slot, source rank): flag + 15 values
+constexpr int kCommStride = 32;     // u64 words per (slot, source rank): flag + 31 values
 constexpr int kCommMaxValues = kCommStride - 1;
 constexpr int kCommMaxRanks = 64;
 
@@ -30,12 +30,12 @@ void comm_collect(const uint64_t* board, int world_size, int slot, uint64_t epoc
                   uint32_t n, uint64_t* d_recv, int spin, sb_stream_t s);
 
 // Sharded relation placements, exchanged on the device (sb_runtime.cpp):
-//   anchor_pack: send[0..2] = bits of instance 0's anchor state s0 (if this rank owns global
-//     instance 0, s0 != NULL), send[3] = owner flag;
-//   anchor_pick: s0 = the owner's entry of the gathered recv[world][4];
+//   anchor_pack: send[0..3na) = bits of instance 0's anchor states s0 (x, y, yaw per anchor;
+//     s0 != NULL iff this rank owns global instance 0), send[3na] = owner flag;
+//   anchor_pick: s0 = the owner's entry of the gathered recv[world][3na + 1];
 //   flag_pack / flag_or: the local "anchors vary" flag out, the OR over ranks back in.
-void shard_anchor_pack(const double* s0, uint64_t* send4, sb_stream_t s);
-void shard_anchor_pick(const uint64_t* recv, int world_size, double* s0, sb_stream_t s);
+void shard_anchor_pack(const double* s0, int na, uint64_t* send, sb_stream_t s);
+void shard_anchor_pick(const uint64_t* recv, int world_size, int na, double* s0, sb_stream_t s);
 void shard_flag_pack(const int32_t* flag, uint64_t* send1, sb_stream_t s);
 void shard_flag_or(const uint64_t* recv, int world_size, int32_t* flag, sb_stream_t s);
 

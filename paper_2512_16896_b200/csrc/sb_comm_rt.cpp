@@ -232,7 +232,7 @@ struct sb_comm {
 
   void allgather_dev(const uint64_t* d_send, uint32_t n, uint64_t* d_recv, cudaStream_t st) {
     if (device < 0) throw std::logic_error("sb_comm: created without a device (host exchange only)");
-    if (n > static_cast<uint32_t>(sbk::kCommMaxValues)) throw std::invalid_argument("sb_comm: more than 15 values per device exchange");
+    if (n > static_cast<uint32_t>(sbk::kCommMaxValues)) throw std::invalid_argument("sb_comm: more than 31 values per device exchange");
     cuda_check(cudaSetDevice(device), "cudaSetDevice");
     const uint64_t e = ++epoch;
     const int slot = static_cast<int>(e % sbk::kCommSlots);

@@ -33,6 +33,13 @@ struct SbRegionTri {
   double a[2], b[2], c[2];
 };
 
+#ifndef SB_MAX_ANCHORS
+#define SB_MAX_ANCHORS 8          // include/scenebatch_b200.h
+#endif
+#ifndef SB_MAX_SUPPORT_VERTS
+#define SB_MAX_SUPPORT_VERTS 16
+#endif
+
 // Placement descriptor consumed by the generation kernels.
 struct SbPlacementDev {
   int32_t geom;            // candidate geometry
@@ -57,7 +64,17 @@ struct SbPlacementDev {
   const double* support_inst;
   const double* inv_support_inst;
   int32_t support_object;
-  int32_t pad_;
+  // every anchor of the relation (anchor_objects[0] == anchor_object): `middle` uses all
+  // positions, the per-instance test all states (relationships.cpp:178-196)
+  int32_t n_anchors;
+  int32_t anchor_objects[SB_MAX_ANCHORS];
+  // support polygon: bounds = bounds(support) (x0 y0 x1 y1 over its vertices); poly_n > 0:
+  // the convex clip operand (counter-clockwise, vertex 0 first), else `rect`
+  double bounds[4];
+  int32_t poly_n;
+  int32_t serial;          // region built by the serial per-instance path (big_region_lane)
+  double poly_x[SB_MAX_SUPPORT_VERTS];
+  double poly_y[SB_MAX_SUPPORT_VERTS];
 };
 
 // Device view of a collision world (plain pointers; built by the host World class).

@@ -176,6 +176,290 @@ SB_HD int intersect_rect(RingT<Cap>& r, RingT<Cap>& tmp, const double rect[4], b
   return kRegionOk;
 }
 
+// One Sutherland-Hodgman pass against the half plane left of the clip edge a->b (convex
+// support polygon; oracle shim clip_edge): side(p) = (b-a) x (p-a), inside iff >= 0,
+// crossing point prev + t (cur - prev), t = side(prev) / (side(prev) - side(cur)).
+template <int Cap>
+SB_HD bool clip_edge(const RingT<Cap>& in, RingT<Cap>& out, double ax, double ay, double bx,
+                     double by) {
+  out.n = 0;
+  const int n = in.n;
+  const double ex = bx - ax, ey = by - ay;
+  for (int i = 0; i < n; ++i) {
+    const int ip = (i + n - 1) % n;
+    const double sc = ex * (in.y[i] - ay) - ey * (in.x[i] - ax);
+    const double sp = ex * (in.y[ip] - ay) - ey * (in.x[ip] - ax);
+    const bool ci = sc >= 0.0, pi = sp >= 0.0;
+    if (ci != pi) {
+      const double t = sp / (sp - sc);
+      if (!push(out, in.x[ip] + t * (in.x[i] - in.x[ip]), in.y[ip] + t * (in.y[i] - in.y[ip])))
+        return false;
+    }
+    if (ci && !push(out, in.x[i], in.y[i])) return false;
+  }
+  return true;
+}
+
+// The support polygon as the intersection's clip operand (oracle shim `intersection`):
+// n == 0: the axis-aligned rect `rect`; else a convex counter-clockwise ring (x, y).
+struct SupportClip {
+  const double* rect;
+  int n;
+  const double* x;
+  const double* y;
+};
+
+// intersect(ring, support) as the oracle stand-in defines it (rect: intersect_rect; convex
+// polygon: correct() orientation, one clip_edge pass per support edge in ring order, the
+// same duplicate / area filter). Result in `r`.
+template <int Cap>
+SB_HD int intersect_support(RingT<Cap>& r, RingT<Cap>& tmp, const SupportClip& c, bool hole = false) {
+  if (c.n == 0) return intersect_rect(r, tmp, c.rect, hole);
+  if (r.n < 3) return kRegionEmpty;
+  if (hole ? ring_area(r) > 0.0 : ring_area(r) < 0.0) {  // bg::correct keeps vertex 0 first
+    for (int i = 1, j = r.n - 1; i < j; ++i, --j) {
+      double tx = r.x[i], ty = r.y[i];
+      r.x[i] = r.x[j];
+      r.y[i] = r.y[j];
+      r.x[j] = tx;
+      r.y[j] = ty;
+    }
+  }
+  for (int e = 0; e < c.n; ++e) {
+    const int f = e + 1 == c.n ? 0 : e + 1;
+    if (!clip_edge(r, tmp, c.x[e], c.y[e], c.x[f], c.y[f])) return kRegionOverflow;
+    r.n = tmp.n;
+    for (int i = 0; i < tmp.n; ++i) {
+      r.x[i] = tmp.x[i];
+      r.y[i] = tmp.y[i];
+    }
+  }
+  int m = 0;
+  for (int i = 0; i < r.n; ++i) {
+    if (m == 0 || r.x[i] != r.x[m - 1] || r.y[i] != r.y[m - 1]) {
+      r.x[m] = r.x[i];
+      r.y[m] = r.y[i];
+      ++m;
+    }
+  }
+  while (m > 1 && r.x[0] == r.x[m - 1] && r.y[0] == r.y[m - 1]) --m;
+  r.n = m;
+  if (r.n < 3 || ring_area(r) == 0.0) return kRegionEmpty;
+  return kRegionOk;
+}
+
+// erode() of a convex counter-clockwise ring by r (the oracle shim's buffer(-r), restated by
+// sbh::erode_convex): in place; kRegionBadArg if concave, kRegionEmpty if eroded away.
+template <int Cap>
+SB_HD int erode_convex_ring(RingT<Cap>& ring, RingT<Cap>& tmp, double r) {
+  const int n = ring.n;
+  if (n < 3) return kRegionEmpty;
+  for (int i = 0; i < n; ++i) {
+    const int h = (i + n - 1) % n, q = (i + 1) % n;
+    const double ox = ring.x[h], oy = ring.y[h], px = ring.x[i], py = ring.y[i];
+    const double qx = ring.x[q], qy = ring.y[q];
+    if ((px - ox) * (qy - oy) - (py - oy) * (qx - ox) < 0.0) return kRegionBadArg;
+    const double dxh = px - ox, dyh = py - oy, dxi = qx - px, dyi = qy - py;
+    const double lh = sqrt(dxh * dxh + dyh * dyh), li = sqrt(dxi * dxi + dyi * dyi);
+    const double axh = ox + (-dyh / lh) * r, ayh = oy + (dxh / lh) * r;
+    const double axi = px + (-dyi / li) * r, ayi = py + (dxi / li) * r;
+    const double den = dxh * dyi - dyh * dxi;
+    const double t = ((axi - axh) * dyi - (ayi - ayh) * dxi) / den;
+    tmp.x[i] = axh + t * dxh;
+    tmp.y[i] = ayh + t * dyh;
+  }
+  tmp.n = n;
+  for (int i = 0; i < n; ++i) {
+    const int q = (i + 1) % n;
+    if (!((tmp.x[q] - tmp.x[i]) * (ring.x[q] - ring.x[i]) + (tmp.y[q] - tmp.y[i]) * (ring.y[q] - ring.y[i]) > 0.0))
+      return kRegionEmpty;
+  }
+  for (int i = 0; i < n; ++i) {
+    ring.x[i] = tmp.x[i];
+    ring.y[i] = tmp.y[i];
+  }
+  return kRegionOk;
+}
+
+// ------------------------------------------------------------ middle (multi-anchor)
+// is_valid_polygon (polygon.cpp:407-410) as the oracle shim defines bg::is_valid: a simple
+// ring -- >= 3 vertices after dropping consecutive exact duplicates, finite, non-zero
+// area, no two non-adjacent edges meeting (closed segments, exact orientation signs).
+SB_HD int orient_sign(double ax, double ay, double bx, double by, double cx, double cy) {
+  const double c = (bx - ax) * (cy - ay) - (by - ay) * (cx - ax);
+  return c > 0.0 ? 1 : (c < 0.0 ? -1 : 0);
+}
+SB_HD bool on_box(double ax, double ay, double bx, double by, double cx, double cy) {
+  return fmin(ax, bx) <= cx && cx <= fmax(ax, bx) && fmin(ay, by) <= cy && cy <= fmax(ay, by);
+}
+SB_HD bool segments_meet(double px, double py, double qx, double qy, double rx, double ry,
+                         double sx, double sy) {
+  const int o1 = orient_sign(px, py, qx, qy, rx, ry), o2 = orient_sign(px, py, qx, qy, sx, sy);
+  const int o3 = orient_sign(rx, ry, sx, sy, px, py), o4 = orient_sign(rx, ry, sx, sy, qx, qy);
+  if (o1 != o2 && o3 != o4) return true;
+  if (o1 == 0 && on_box(px, py, qx, qy, rx, ry)) return true;
+  if (o2 == 0 && on_box(px, py, qx, qy, sx, sy)) return true;
+  if (o3 == 0 && on_box(rx, ry, sx, sy, px, py)) return true;
+  if (o4 == 0 && on_box(rx, ry, sx, sy, qx, qy)) return true;
+  return false;
+}
+template <int Cap>
+SB_HD bool simple_ring(const RingT<Cap>& in, RingT<Cap>& r) {
+  // to_boost: correct() (orientation only -- irrelevant to simplicity) then the open ring
+  r.n = 0;
+  for (int i = 0; i < in.n; ++i)
+    if (r.n == 0 || in.x[i] != r.x[r.n - 1] || in.y[i] != r.y[r.n - 1]) push(r, in.x[i], in.y[i]);
+  while (r.n > 1 && r.x[0] == r.x[r.n - 1] && r.y[0] == r.y[r.n - 1]) --r.n;
+  const int n = r.n;
+  if (n < 3) return false;
+  for (int i = 0; i < n; ++i)
+    if (!isfinite(r.x[i]) || !isfinite(r.y[i])) return false;
+  if (ring_area(r) == 0.0) return false;
+  for (int i = 0; i < n; ++i)
+    for (int j = i + 1; j < n; ++j) {
+      if (j == i + 1 || (i == 0 && j == n - 1)) continue;
+      const int i1 = (i + 1) % n, j1 = (j + 1) % n;
+      if (segments_meet(r.x[i], r.y[i], r.x[i1], r.y[i1], r.x[j], r.y[j], r.x[j1], r.y[j1]))
+        return false;
+    }
+  return true;
+}
+
+// convex_hull (polygon.cpp:412-420) as the oracle shim defines bg::convex_hull: Andrew's
+// monotone chain over the points sorted by (x, y) (stable insertion sort; equal points
+// are interchangeable), collinear and duplicate points dropped, counter-clockwise from the
+// lowest (x, y); ring_to_vec drops the closing vertex.
+template <int Cap>
+SB_HD void convex_hull_ring(const double* px, const double* py, int m, RingT<Cap>& out) {
+  double sx[SB_MAX_ANCHORS], sy[SB_MAX_ANCHORS];
+  for (int i = 0; i < m; ++i) {
+    double x = px[i], y = py[i];
+    int j = i;
+    while (j > 0 && (x < sx[j - 1] || (x == sx[j - 1] && y < sy[j - 1]))) {
+      sx[j] = sx[j - 1];
+      sy[j] = sy[j - 1];
+      --j;
+    }
+    sx[j] = x;
+    sy[j] = y;
+  }
+  auto turn = [](double ox, double oy, double ax, double ay, double bx, double by) {
+    return (ax - ox) * (by - oy) - (ay - oy) * (bx - ox);
+  };
+  out.n = 0;
+  for (int i = 0; i < m; ++i) {
+    while (out.n >= 2 && turn(out.x[out.n - 2], out.y[out.n - 2], out.x[out.n - 1], out.y[out.n - 1], sx[i], sy[i]) <= 0.0)
+      --out.n;
+    push(out, sx[i], sy[i]);
+  }
+  const int lower = out.n + 1;
+  for (int i = m - 1; i >= 0; --i) {
+    while (out.n >= lower && turn(out.x[out.n - 2], out.y[out.n - 2], out.x[out.n - 1], out.y[out.n - 1], sx[i], sy[i]) <= 0.0)
+      --out.n;
+    push(out, sx[i], sy[i]);
+  }
+  if (out.n > 1) --out.n;  // the start point again
+  // close_ring + ring_to_vec: the closing copy is dropped again; a 1-point hull keeps its
+  // point (ring_to_vec drops only a distinct-looking closing vertex within 1e-15)
+}
+
+// stadium (relationships.cpp:17-40): the capsule of radius `radius` around segment a-b
+// (a disc of 72 points if a == b), cap at b then cap at a, 37 points each.
+template <class M, int Cap>
+SB_HD bool stadium_ring(double ax, double ay, double bx, double by, double radius, RingT<Cap>& out) {
+  out.n = 0;
+  const double dx = bx - ax, dy = by - ay;
+  const double len = sqrt(dx * dx + dy * dy);
+  if (len < 1e-12) {
+    for (int i = 0; i < 72; ++i) {
+      const double ang = 2.0 * kPi * (double)i / 72;
+      double sa, ca;
+      M::sincos(ang, &sa, &ca);
+      if (!push(out, ax + radius * ca, ay + radius * sa)) return false;
+    }
+    return true;
+  }
+  const double ux = dx / len, uy = dy / len;
+  const double base = M::atan2(uy, ux);
+  auto cap = [&](double cx, double cy, double a0, double a1) -> bool {
+    const int steps = 36;
+    for (int i = 0; i <= steps; ++i) {
+      const double ang = a0 + (a1 - a0) * (double)i / (double)steps;
+      double sa, ca;
+      M::sincos(ang, &sa, &ca);
+      if (!push(out, cx + radius * ca, cy + radius * sa)) return false;
+    }
+    return true;
+  };
+  if (!cap(bx, by, base - kPi / 2, base + kPi / 2)) return false;
+  return cap(ax, ay, base + kPi / 2, base + 3 * kPi / 2);
+}
+
+// middle_polygon (relationships.cpp:124-157) of m >= 2 anchor positions.
+template <class M, int Cap>
+SB_HD int middle_ring(const double* px, const double* py, int m, RingT<Cap>& out, RingT<Cap>& tmp) {
+  if (m < 2 || m > SB_MAX_ANCHORS) return kRegionBadArg;
+  const double inf = INFINITY;
+  double bx0 = inf, by0 = inf, bx1 = -inf, by1 = -inf;
+  for (int i = 0; i < m; ++i) {
+    bx0 = fmin(bx0, px[i]);
+    by0 = fmin(by0, py[i]);
+    bx1 = fmax(bx1, px[i]);
+    by1 = fmax(by1, py[i]);
+  }
+  double diag = 0.0;
+  if (!(bx0 > bx1)) {
+    const double ddx = bx1 - bx0, ddy = by1 - by0;
+    diag = sqrt(ddx * ddx + ddy * ddy);
+  }
+  const double scale = fmax(1e-9, diag);
+  bool collinear = true;  // relationships.cpp:42-50
+  if (m >= 3) {
+    const double ex = px[1] - px[0], ey = py[1] - py[0];
+    for (int i = 2; i < m && collinear; ++i) {
+      const double c = ex * (py[i] - py[0]) - ey * (px[i] - px[0]);
+      if (fabs(c) > 1e-9 * scale * scale) collinear = false;
+    }
+  }
+  if (m == 2 || collinear) {  // inflated extreme segment (lexicographic lo / hi)
+    int lo = 0, hi = 0;
+    for (int i = 0; i < m; ++i) {
+      if (px[i] < px[lo] || (px[i] == px[lo] && py[i] < py[lo])) lo = i;
+      if (px[i] > px[hi] || (px[i] == px[hi] && py[i] > py[hi])) hi = i;
+    }
+    const double sx = px[hi] - px[lo], sy = py[hi] - py[lo];
+    const double sep = sqrt(sx * sx + sy * sy);
+    return stadium_ring<M>(px[lo], py[lo], px[hi], py[hi], fmax(1e-6, 0.1 * sep), out) ? kRegionOk
+                                                                                      : kRegionOverflow;
+  }
+  double cx = 0.0, cy = 0.0;
+  for (int i = 0; i < m; ++i) {
+    cx = cx + px[i];
+    cy = cy + py[i];
+  }
+  cx = cx / (double)m;
+  cy = cy / (double)m;
+  // std::sort of <= 16 elements is libstdc++'s insertion sort: stable on equal angles
+  double key[SB_MAX_ANCHORS];
+  out.n = 0;
+  for (int i = 0; i < m; ++i) {
+    const double k = M::atan2(py[i] - cy, px[i] - cx);
+    int j = out.n;
+    push(out, 0.0, 0.0);
+    while (j > 0 && k < key[j - 1]) {
+      key[j] = key[j - 1];
+      out.x[j] = out.x[j - 1];
+      out.y[j] = out.y[j - 1];
+      --j;
+    }
+    key[j] = k;
+    out.x[j] = px[i];
+    out.y[j] = py[i];
+  }
+  if (!simple_ring(out, tmp)) convex_hull_ring(px, py, m, out);  // equal-angle ties
+  return kRegionOk;
+}
+
 // point_in_tri_strict (polygon.cpp:189-195)
 SB_HD bool point_in_tri_strict(double px, double py, double ax, double ay, double bx, double by,
                                double cx, double cy) {
@@ -415,7 +699,8 @@ struct HoleScratch {
 // bridge_hole) and ear_clip_ring into the sampler table. max_r must be finite.
 template <class M>
 SB_HD int hole_annulus_table(double cx, double cy, double min_r, double max_r,
-                             const double rect[4], HoleScratch& sc, TableSink& sink) {
+                             const SupportClip& clip, double erode_r, HoleScratch& sc,
+                             TableSink& sink) {
   const double step = 5.0 * kPi / 180.0;
   auto arc = [&](Ring& out, double radius, double a0, double a1) -> bool {
     int na = (int)ceil(fabs(a1 - a0) / step);
@@ -433,11 +718,16 @@ SB_HD int hole_annulus_table(double cx, double cy, double min_r, double max_r,
   sc.h.n = 0;
   if (!arc(sc.o, max_r, 0.0, 2.0 * kPi) || !arc(sc.h, min_r, 2.0 * kPi, 0.0))
     return kRegionOverflow;
-  const int so = intersect_rect(sc.o, sc.tmp, rect, false);
+  const int so = intersect_support(sc.o, sc.tmp, clip, false);
   if (so == kRegionOverflow) return so;
   if (so != kRegionOk) return kRegionEmpty;
-  const int sh = intersect_rect(sc.h, sc.tmp, rect, true);
+  const int sh = intersect_support(sc.h, sc.tmp, clip, true);
   if (sh == kRegionOverflow) return sh;
+  if (erode_r > 0.0) {  // apply_ratio_on_support: the shim's buffer takes hole-free rings only
+    if (sh == kRegionOk) return kRegionBadArg;
+    const int se = erode_convex_ring(sc.o, sc.tmp, erode_r);
+    if (se != kRegionOk) return se;
+  }
   if (ring_area(sc.o) < 0.0) reverse_ring(sc.o);  // triangulate (polygon.cpp:348-354)
   if (sh == kRegionOk) {
     if (ring_area(sc.h) > 0.0) reverse_ring(sc.h);
@@ -485,18 +775,41 @@ SB_HD int sector_ring(double cx, double cy, double vx, double vy, double theta, 
   return kRegionOk;
 }
 
-// region_for(i) of a shape whose ring outgrows the group path's kCap (sector_ring ->
-// the shim intersection -> triangulate -> the sampler table).
+// region_for(i) on the serial path: shapes whose ring outgrows the group path's kCap, and
+// every shape on a polygon support (sector_ring -> the shim intersection -> optional
+// erosion -> triangulate -> the sampler table).
 template <class M>
 SB_HD int big_region_table(double cx, double cy, double vx, double vy, double theta,
-                           double min_r, double max_r, const double rect[4], HoleScratch& sc,
-                           TableSink& sink) {
+                           double min_r, double max_r, const SupportClip& clip, double erode_r,
+                           HoleScratch& sc, TableSink& sink) {
   int st = sector_ring<M>(cx, cy, vx, vy, theta, min_r, max_r, sc.mg);
   if (st != kRegionOk) return st;
-  st = intersect_rect(sc.mg, sc.mg2, rect, false);
+  st = intersect_support(sc.mg, sc.mg2, clip, false);
   if (st == kRegionOverflow) return st;
   if (st != kRegionOk) return kRegionEmpty;
+  if (erode_r > 0.0) {  // apply_ratio_on_support: convex rings only (the shim's buffer)
+    st = erode_convex_ring(sc.mg, sc.mg2, erode_r);
+    if (st != kRegionOk) return st;
+  }
   if (!ear_clip_into(sc.mg, sink, true)) return kRegionOverflow;
+  return kRegionOk;
+}
+
+// region_for(i) of a `middle` relation (relationships.cpp:192-196): middle_polygon ->
+// the shim intersection with the support -> optional erosion (apply_ratio_on_support) ->
+// triangulate -> the sampler table.
+template <class M>
+SB_HD int middle_region_table(const double* px, const double* py, int m, const SupportClip& clip,
+                              double erode_r, Ring& r, Ring& tmp, TableSink& sink) {
+  int st = middle_ring<M>(px, py, m, r, tmp);
+  if (st != kRegionOk) return st;
+  st = intersect_support(r, tmp, clip, false);
+  if (st != kRegionOk) return st;
+  if (erode_r > 0.0) {
+    st = erode_convex_ring(r, tmp, erode_r);
+    if (st != kRegionOk) return st;
+  }
+  if (!ear_clip_into(r, sink, true)) return kRegionOverflow;
   return kRegionOk;
 }
 

@@ -572,8 +572,16 @@ struct DevMath {
 // (sbp::hole_annulus_table / sbp::big_region_table) on 2 * kCap + 2 vertex rings in local
 // memory; such rings are never convex, so the lane-parallel fan path would not apply.
 __device__ __noinline__ RegionStats big_region_lane(const SbPlacementDev& pl, double ax, double ay,
-                                                    double ayaw, SbRegionTri* tris, double* cum,
-                                                    int cap) {
+                                                    double ayaw, const double* mx, const double* my,
+                                                    SbRegionTri* tris, double* cum, int cap) {
+  const sbp::SupportClip clip{pl.rect, pl.poly_n, pl.poly_x, pl.poly_y};
+  sbp::TableSink sink{tris, cum, 0, cap, 0.0};
+  if (pl.distance_type == SB_DIST_MIDDLE) {  // relationships.cpp:192-196
+    sbp::Ring r, tmp;
+    const int st = sbp::middle_region_table<DevMath>(mx, my, pl.n_anchors, clip, pl.erode_r, r, tmp, sink);
+    if (st != sbp::kRegionOk) return {st, 0};
+    return {sbp::kRegionOk, sbp::finish_table(sink)};
+  }
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
   double min_r, max_r;
   distance_band(pl, min_r, max_r);
@@ -581,29 +589,25 @@ __device__ __noinline__ RegionStats big_region_lane(const SbPlacementDev& pl, do
   const double theta = region_theta(pl);
   double vx, vy;
   resolve_direction(pl, ayaw, vx, vy);
-  const double* rc = pl.rect;
-  double bx0 = inf, by0 = inf, bx1 = -inf, by1 = -inf;
-  const double vxs[5] = {rc[0], rc[2], rc[2], rc[0], ax};
-  const double vys[5] = {rc[1], rc[1], rc[3], rc[3], ay};
-  for (int k = 0; k < 5; ++k) {
-    bx0 = dmin(bx0, vxs[k]);
-    by0 = dmin(by0, vys[k]);
-    bx1 = dmax(bx1, vxs[k]);
-    by1 = dmax(by1, vys[k]);
-  }
+  // clip bound = bounds(support) expanded by the anchor (relationships.cpp:188-203)
+  const double* bd = pl.bounds;
+  const double bx0 = dmin(bd[0], ax), by0 = dmin(bd[1], ay);
+  const double bx1 = dmax(bd[2], ax), by1 = dmax(bd[3], ay);
   const double ddx = bx1 - bx0, ddy = by1 - by0;
   const double diag = bx0 > bx1 ? 0.0 : sqrt(ddx * ddx + ddy * ddy);
+  (void)inf;
   if (!(theta > 0.0) || theta > pi + 1e-12) return {sbp::kRegionBadArg, 0};
   if (isinf(max_r)) max_r = fmax(diag, min_r + 1e-6);
   if (!(min_r < max_r)) return {sbp::kRegionBadArg, 0};
-  if (pl.erode_r > 0.0) return {sbp::kRegionBadArg, 0};  // concave shapes: no erosion
   sbp::HoleScratch sc;
-  sbp::TableSink sink{tris, cum, 0, cap, 0.0};
   const bool full = theta >= pi - 1e-12;
-  const int st = full && min_r > 0.0
-                     ? sbp::hole_annulus_table<DevMath>(ax, ay, min_r, max_r, rc, sc, sink)
-                     : sbp::big_region_table<DevMath>(ax, ay, vx, vy, theta, min_r, max_r, rc,
-                                                      sc, sink);
+  int st;
+  if (full && min_r > 0.0) {
+    st = sbp::hole_annulus_table<DevMath>(ax, ay, min_r, max_r, clip, pl.erode_r, sc, sink);
+  } else {
+    st = sbp::big_region_table<DevMath>(ax, ay, vx, vy, theta, min_r, max_r, clip, pl.erode_r,
+                                        sc, sink);
+  }
   if (st != sbp::kRegionOk) return {st, 0};
   return {sbp::kRegionOk, sbp::finish_table(sink)};
 }
@@ -613,11 +617,13 @@ template <bool kHole>
 __device__ __forceinline__ RegionStats group_region(const SbPlacementDev& pl, double ax, double ay,
                                                     double ayaw, SbRegionTri* tris, double* cum,
                                                     int cap, RegionScratch& sc,
-                                                    const SbArcTable* arcs) {
+                                                    const SbArcTable* arcs,
+                                                    const double* mx = nullptr,
+                                                    const double* my = nullptr) {
   if constexpr (kHole) {
     const Grp g;
     RegionStats r{0, 0};
-    if (g.gl == 0) r = big_region_lane(pl, ax, ay, ayaw, tris, cum, cap);
+    if (g.gl == 0) r = big_region_lane(pl, ax, ay, ayaw, mx, my, tris, cum, cap);
     r.status = g.bcast(r.status, 0);
     r.ntri = g.bcast(r.ntri, 0);
     return r;
@@ -645,8 +651,8 @@ __global__ void __launch_bounds__(kRB, kRegionMinBlocks) k_relation_regions(Rela
   // feeds a local-frame direction and the variation test; the latter only needs it when
   // the positions agree (relationships.cpp:180-181), so atan2 is skipped otherwise.
   const bool yaw_used = p.pl.direction != SB_DIR_NONE && p.pl.frame == SB_FRAME_LOCAL;
-  auto rel_of = [&](uint64_t inst, M34& rel) {  // inverse_rigid(support_world[i]) * anchor pose
-    const double* pp = p.w.pose + sb_pose_off(p.w, p.anchor_object, inst);
+  auto rel_of = [&](int32_t obj, uint64_t inst, M34& rel) {  // inverse_rigid(support_world[i]) * anchor pose
+    const double* pp = p.w.pose + sb_pose_off(p.w, obj, inst);
     M34 P;
 #pragma unroll
     for (int k = 0; k < 12; ++k) P.m[k] = pp[k];
@@ -660,10 +666,17 @@ __global__ void __launch_bounds__(kRB, kRegionMinBlocks) k_relation_regions(Rela
     }
   };
   auto yaw_of = [](const M34& rel) { return sbg::atan2(rel.m[4], rel.m[0]); };  // transform.hpp:77
-  if (p.from_s0) {  // canonical region_for(0) from the exchanged instance-0 state
+  // several anchors (middle, or the multi-anchor variation test) take the serial path
+  const int na = kHole && p.pl.n_anchors > 1 ? p.pl.n_anchors : 1;
+  if (p.from_s0) {  // canonical region_for(0) from the exchanged instance-0 states
     if (warp == 0) {
-      const RegionStats r =
-          group_region<kHole>(p.pl, p.s0[0], p.s0[1], p.s0[2], p.tris, p.cum, p.cap, sc, arcs);
+      double mx[SB_MAX_ANCHORS], my[SB_MAX_ANCHORS];
+      for (int k = 0; k < na; ++k) {
+        mx[k] = p.s0[3 * k];
+        my[k] = p.s0[3 * k + 1];
+      }
+      const RegionStats r = group_region<kHole>(p.pl, p.s0[0], p.s0[1], p.s0[2], p.tris, p.cum,
+                                                p.cap, sc, arcs, mx, my);
       if (g.gl == 0) {
         const bool good = r.status == sbp::kRegionOk || r.status == sbp::kRegionEmpty;
         p.ntri[0] = good ? r.ntri : 0;
@@ -694,36 +707,53 @@ __global__ void __launch_bounds__(kRB, kRegionMinBlocks) k_relation_regions(Rela
     }
     return;
   }
-  double x0, y0;
+  // instance 0's anchor states: recomputed from local instance 0, or exchanged (s0)
+  double x0[SB_MAX_ANCHORS], y0[SB_MAX_ANCHORS];
   M34 rel0;
-  if (p.owns_instance0) {
-    rel_of(0, rel0);
-    x0 = rel0.m[3];
-    y0 = rel0.m[7];
-  } else {
-    x0 = p.s0[0];
-    y0 = p.s0[1];
+  for (int k = 0; k < na; ++k) {
+    if (p.owns_instance0) {
+      rel_of(p.pl.anchor_objects[k], 0, rel0);
+      x0[k] = rel0.m[3];
+      y0[k] = rel0.m[7];
+    } else {
+      x0[k] = p.s0[3 * k];
+      y0[k] = p.s0[3 * k + 1];
+    }
   }
+  auto yaw0_of = [&](int k) {
+    if (!p.owns_instance0) return p.s0[3 * k + 2];
+    M34 r0;
+    rel_of(p.pl.anchor_objects[k], 0, r0);
+    return yaw_of(r0);
+  };
   bool vary = false;
   int worst = 0;
   for (uint64_t i = warp; i < p.w.n; i += nwarps) {
     SB_RP_MARK(ra0);
-    M34 rel;
-    rel_of(i, rel);
-    const double ax = rel.m[3], ay = rel.m[7];
-    const double dx = ax - x0, dy = ay - y0;
-    const bool pos_vary = sqrt(dx * dx + dy * dy) > 1e-12;
-    double ayaw = 0.0;
-    if (yaw_used || !pos_vary) ayaw = yaw_of(rel);
-    if (!pos_vary) {
-      const double yaw0 = p.owns_instance0 ? yaw_of(rel0) : p.s0[2];
-      vary = vary || fabs(ayaw - yaw0) > 1e-12;
+    double ax = 0.0, ay = 0.0, ayaw = 0.0;
+    double mx[SB_MAX_ANCHORS], my[SB_MAX_ANCHORS];
+    for (int k = 0; k < na; ++k) {  // relationships.cpp:178-186, every anchor
+      M34 rel;
+      rel_of(p.pl.anchor_objects[k], i, rel);
+      const double kx = rel.m[3], ky = rel.m[7];
+      const double dx = kx - x0[k], dy = ky - y0[k];
+      const bool pos_vary = sqrt(dx * dx + dy * dy) > 1e-12;
+      double kyaw = 0.0;
+      if ((k == 0 && yaw_used) || !pos_vary) kyaw = yaw_of(rel);
+      if (!pos_vary && !vary) vary = fabs(kyaw - yaw0_of(k)) > 1e-12;
+      vary = vary || pos_vary;
+      mx[k] = kx;
+      my[k] = ky;
+      if (k == 0) {
+        ax = kx;
+        ay = ky;
+        ayaw = kyaw;
+      }
     }
-    vary = vary || pos_vary;
     SB_RP_MARK(ra1);
     SB_RP_ADD(0, ra0, ra1);
     const RegionStats r = group_region<kHole>(p.pl, ax, ay, ayaw, p.tris + i * p.cap,
-                                              p.cum + i * p.cap, p.cap, sc, arcs);
+                                              p.cum + i * p.cap, p.cap, sc, arcs, mx, my);
     if (g.gl == 0) {
       p.ntri[i] = r.status == sbp::kRegionOk || r.status == sbp::kRegionEmpty ? r.ntri : 0;
       if (r.status != sbp::kRegionOk && r.status != sbp::kRegionEmpty && r.status > worst)

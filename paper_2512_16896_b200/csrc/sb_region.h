@@ -26,7 +26,8 @@ struct RelationRegionParams {
   int32_t anchor_object;
   int32_t owns_instance0;  // 1: global instance 0 is local instance 0 (compute s0 in-kernel)
   double inv_support[12];  // inverse_rigid(support pose), row-major 3x4 (host-computed)
-  const double* s0;        // instance 0's anchor state when !owns_instance0 (device)
+  const double* s0;        // instance 0's anchor states (x, y, yaw per anchor) when
+                           // !owns_instance0 (device)
   int32_t from_s0;         // 1: build a single region from s0 (canonical, sharded runs)
   int32_t cap;
   int32_t hole;            // full annulus with a hole: bridged-hole path (sbp::hole_annulus_table)

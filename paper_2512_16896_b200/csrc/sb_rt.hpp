@@ -128,19 +128,33 @@ inline int current_device_checked(int device) {
   return device;
 }
 
-// RelationshipSpec::validate (relationships.cpp:59-76) for the single-anchor subset, then
-// the relation fields of the device record. Returns whether region_for() needs the serial
-// big-ring region path: a full annulus with a hole (theta = pi, min_r > 0, bridged hole) or
-// an annular sector wide enough to outgrow the group path's ring (SB_REGION_MAX_VERTS).
+// Anchor count of an sb_relation (RelationshipSpec::anchors = {anchor, extra_anchors...}).
+inline int relation_anchor_count(const sb_relation& r) {
+  if (r.anchor < 0) return 0;
+  if (r.n_extra_anchors < 0 || r.n_extra_anchors > SB_MAX_ANCHORS - 1)
+    throw std::invalid_argument("relationship: n_extra_anchors outside [0, 7]");
+  return 1 + r.n_extra_anchors;
+}
+
+// RelationshipSpec::validate (relationships.cpp:59-76), then the relation fields of the
+// device record (anchor objects are filled by the caller). Returns whether region_for()
+// needs the serial big-ring region path for its SHAPE: a full annulus with a hole (theta =
+// pi, min_r > 0, bridged hole) or an annular sector wide enough to outgrow the group path's
+// ring (SB_REGION_MAX_VERTS).
 inline bool relation_to_dev(const sb_relation& r, SbPlacementDev& d) {
+  const int na = relation_anchor_count(r);
   if (r.distance < 0.0) throw std::invalid_argument("relationship: distance must be >= 0");
   if (r.angle_threshold > M_PI) throw std::invalid_argument("relationship: angle_threshold outside (0, pi]");
+  if (r.distance_type < SB_DIST_NONE || r.distance_type > SB_DIST_MIDDLE)
+    throw std::invalid_argument("relationship: distance_type");
   const bool dist = r.distance_type == SB_DIST_GREATER || r.distance_type == SB_DIST_LESS ||
                     r.distance_type == SB_DIST_EQUAL;
-  if (r.distance_type < SB_DIST_NONE || r.distance_type > SB_DIST_EQUAL)
-    throw std::invalid_argument("relationship: distance_type (middle is out of scope)");
-  if (dist && r.anchor < 0) throw std::invalid_argument("relationship: greater/less/equal require exactly 1 anchor");
-  if (r.direction != SB_DIR_NONE && r.anchor < 0) throw std::invalid_argument("relationship: direction requires exactly 1 anchor");
+  if (r.distance_type == SB_DIST_MIDDLE) {
+    if (na < 2) throw std::invalid_argument("relationship: middle requires at least 2 anchors");
+  } else if (dist && na != 1) {
+    throw std::invalid_argument("relationship: greater/less/equal require exactly 1 anchor");
+  }
+  if (r.direction != SB_DIR_NONE && na != 1) throw std::invalid_argument("relationship: direction requires exactly 1 anchor");
   if (r.direction < SB_DIR_NONE || r.direction > SB_DIR_VECTOR) throw std::invalid_argument("relationship: direction");
   if (r.direction == SB_DIR_VECTOR &&
       std::sqrt(r.direction_vector[0] * r.direction_vector[0] + r.direction_vector[1] * r.direction_vector[1]) < 1e-12)
@@ -154,7 +168,8 @@ inline bool relation_to_dev(const sb_relation& r, SbPlacementDev& d) {
   d.direction_vector[1] = r.direction_vector[1];
   d.distance = r.distance;
   d.angle_threshold = r.angle_threshold;
-  if (r.anchor < 0) return false;
+  d.n_anchors = na;
+  if (na == 0 || r.distance_type == SB_DIST_MIDDLE) return false;
   const double theta = r.angle_threshold > 0 ? r.angle_threshold : (r.direction == SB_DIR_NONE ? M_PI : M_PI / 4);
   double min_r = 0.0;  // distance_band (relationships.cpp:101-122)
   if (r.distance_type == SB_DIST_GREATER) min_r = r.distance;
@@ -166,6 +181,76 @@ inline bool relation_to_dev(const sb_relation& r, SbPlacementDev& d) {
   const int arc = full ? 73 : static_cast<int>(std::ceil(2.0 * theta / step)) + 2;
   const int ring = arc + (!full && min_r > 0.0 ? arc : 1) + 8;
   return ring > SB_REGION_MAX_VERTS;  // the serial big-ring path
+}
+
+// The support polygon of an sb_support into the device record: bounds(support) over its
+// vertices, and the clip operand -- the rect (poly_n = 0) when the polygon is an
+// axis-aligned rectangle (the shim clips those exactly as a rect), else the convex ring
+// corrected to counter-clockwise with vertex 0 first (bg::correct). Returns the ring as
+// given (the canonical sampler triangulates it as is).
+inline std::vector<std::array<double, 2>> support_to_dev(const sb_support& sup, SbPlacementDev& d) {
+  std::vector<std::array<double, 2>> ring;
+  if (sup.n_polygon == 0) {
+    const double* rc = sup.rect;
+    ring = {{rc[0], rc[1]}, {rc[2], rc[1]}, {rc[2], rc[3]}, {rc[0], rc[3]}};
+  } else {
+    if (sup.n_polygon < 3 || sup.n_polygon > SB_MAX_SUPPORT_VERTS || !sup.polygon_xy)
+      throw std::invalid_argument("support polygon needs 3..16 vertices");
+    for (uint32_t k = 0; k < sup.n_polygon; ++k) {
+      const double x = sup.polygon_xy[2 * k], y = sup.polygon_xy[2 * k + 1];
+      if (!std::isfinite(x) || !std::isfinite(y)) throw std::invalid_argument("support polygon must be finite");
+      ring.push_back({x, y});
+    }
+  }
+  const size_t k = ring.size();
+  double x0 = ring[0][0], x1 = ring[0][0], y0 = ring[0][1], y1 = ring[0][1];
+  double bx0 = HUGE_VAL, by0 = HUGE_VAL, bx1 = -HUGE_VAL, by1 = -HUGE_VAL;  // Aabb2::expand
+  for (const auto& v : ring) {
+    x0 = std::fmin(x0, v[0]);
+    x1 = std::fmax(x1, v[0]);
+    y0 = std::fmin(y0, v[1]);
+    y1 = std::fmax(y1, v[1]);
+    bx0 = std::min(bx0, v[0]);
+    by0 = std::min(by0, v[1]);
+    bx1 = std::max(bx1, v[0]);
+    by1 = std::max(by1, v[1]);
+  }
+  d.bounds[0] = bx0;
+  d.bounds[1] = by0;
+  d.bounds[2] = bx1;
+  d.bounds[3] = by1;
+  bool is_rect = k == 4;
+  for (const auto& v : ring)
+    if (!((v[0] == x0 || v[0] == x1) && (v[1] == y0 || v[1] == y1))) is_rect = false;
+  d.poly_n = 0;
+  if (is_rect) {
+    d.rect[0] = x0;  // intersect_rect takes min / max again
+    d.rect[1] = y0;
+    d.rect[2] = x1;
+    d.rect[3] = y1;
+    return ring;
+  }
+  std::vector<std::array<double, 2>> c = ring;  // bg::correct: counter-clockwise, v0 first
+  double a = 0.0;
+  for (size_t i = 0; i < k; ++i) a += c[i][0] * c[(i + 1) % k][1] - c[(i + 1) % k][0] * c[i][1];
+  if (0.5 * a < 0.0) std::reverse(c.begin() + 1, c.end());
+  for (size_t i = 0; i < k; ++i) {
+    const auto& o = c[(i + k - 1) % k];
+    const auto& p = c[i];
+    const auto& q = c[(i + 1) % k];
+    if ((p[0] - o[0]) * (q[1] - o[1]) - (p[1] - o[1]) * (q[0] - o[0]) < 0.0)
+      throw std::invalid_argument("support polygon must be convex (non-convex supports are out of scope)");
+  }
+  d.poly_n = static_cast<int32_t>(k);
+  for (size_t i = 0; i < k; ++i) {
+    d.poly_x[i] = c[i][0];
+    d.poly_y[i] = c[i][1];
+  }
+  d.rect[0] = x0;
+  d.rect[1] = y0;
+  d.rect[2] = x1;
+  d.rect[3] = y1;
+  return ring;
 }
 
 

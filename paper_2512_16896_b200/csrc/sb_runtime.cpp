@@ -400,7 +400,9 @@ struct sb_engine {
     double support16[16];
     double inv_support[12];
     int canon_n = 0;  // host-built canonical table size (no anchor)
-    bool hole = false;  // full annulus with a hole (theta = pi, min_r > 0)
+    bool hole = false;  // serial region path (holed annulus, wide sector, polygon support,
+                        // middle / multi-anchor relation): k_relation_regions<true>
+    std::vector<std::array<double, 2>> support_ring;  // the support polygon as given
     bool shared_arcs = false;  // arc table in d_arcs[p] (no local-frame direction)
     double ratio = 0.0;        // ratio_on_support (no-relation placements)
     int mesh = 0;
@@ -602,24 +604,33 @@ struct sb_engine {
         sup_frames.push_back(std::move(S));
         sup_frames.push_back(std::move(I));
       }
-      for (int k = 0; k < 4; ++k) pl.dev.rect[k] = sup.rect[k];
+      pl.support_ring = support_to_dev(sup, pl.dev);
       const sb_relation& r = sp.relation;
-      pl.hole = relation_to_dev(r, pl.dev);
+      // holed annulus / wide sector (erosion of those: only where the clipped ring is convex
+      // and hole-free, else a region-build error as the reference's buffer throws)
+      const bool big = relation_to_dev(r, pl.dev);
       if (sp.ratio_on_support != 0.0) {  // apply_ratio_on_support's checks (relationships.cpp:222-227)
         if (sp.ratio_on_support < 0.0 || sp.ratio_on_support > 1.0)
           throw std::invalid_argument("apply_ratio_on_support: ratio outside [0,1]");
         if (!(footprint[sp.mesh][0] > 0.0) || !(footprint[sp.mesh][1] > 0.0))
           throw std::invalid_argument("apply_ratio_on_support: footprint edges must be positive");
-        if (pl.hole)
-          throw std::invalid_argument("ratio_on_support on an annulus with a hole or a wide annular sector (not convex) is out of scope");
       }
       pl.ratio = sp.ratio_on_support;
       pl.mesh = sp.mesh;
-      if (r.anchor >= 0 && sp.ratio_on_support > 0.0)  // relation regions erode on the device
+      const int na = pl.dev.n_anchors;
+      if (na > 0 && sp.ratio_on_support > 0.0)  // relation regions erode on the device
         pl.dev.erode_r = sp.ratio_on_support * std::min(footprint[sp.mesh][0], footprint[sp.mesh][1]) / 2.0;
-      if (r.anchor >= 0 && static_cast<uint32_t>(r.anchor) >= p)
-        throw std::invalid_argument("relationship: anchor must be an earlier placement");
-      pl.dev.anchor_object = r.anchor >= 0 ? first_place_obj + r.anchor : -1;
+      for (int k = 0; k < na; ++k) {
+        const int32_t a = k == 0 ? r.anchor : r.extra_anchors[k - 1];
+        if (a < 0 || static_cast<uint32_t>(a) >= p)
+          throw std::invalid_argument("relationship: anchor must be an earlier placement");
+        pl.dev.anchor_objects[k] = first_place_obj + a;
+      }
+      pl.dev.anchor_object = na > 0 ? pl.dev.anchor_objects[0] : -1;
+      // serial per-instance region path (big_region_lane): ring shapes past the group
+      // path's capacity, polygon supports, `middle` and multi-anchor relations
+      pl.hole = big || (na > 0 && (pl.dev.poly_n > 0 || na > 1 || r.distance_type == SB_DIST_MIDDLE));
+      pl.dev.serial = pl.hole ? 1 : 0;
       pl.dev.salt = p;
       if (r.anchor >= 0) any_anchor = true;
       any_hole = any_hole || pl.hole;
@@ -643,12 +654,19 @@ struct sb_engine {
     d_canon_n.alloc(std::max<size_t>(1, P));
     for (size_t p = 0; p < P; ++p) {
       if (places[p].dev.anchor_object >= 0) continue;
-      const double* rc = places[p].dev.rect;
-      std::vector<sbh::V2> ring = {{rc[0], rc[1]}, {rc[2], rc[1]}, {rc[2], rc[3]}, {rc[0], rc[3]}};
+      // region = the support polygon as given (relationships.cpp:168-171)
+      std::vector<sbh::V2> ring;
+      for (const auto& v : places[p].support_ring) ring.push_back({v[0], v[1]});
       if (places[p].ratio > 0.0) {  // apply_ratio_on_support (relationships.cpp:220-230)
         const auto& fp = footprint[places[p].mesh];
         const double r = places[p].ratio * std::min(fp[0], fp[1]) / 2.0;
-        if (r > 0.0) ring = sbh::erode_convex(ring, r);
+        if (r > 0.0) {  // erode -> to_boost: bg::correct (counter-clockwise, vertex 0 first)
+          double a = 0.0;
+          for (size_t i = 0; i < ring.size(); ++i)
+            a += ring[i][0] * ring[(i + 1) % ring.size()][1] - ring[(i + 1) % ring.size()][0] * ring[i][1];
+          if (0.5 * a < 0.0) std::reverse(ring.begin() + 1, ring.end());
+          ring = sbh::erode_convex(ring, r);
+        }
       }
       sbh::SamplerTable t = sbh::sampler_table({ring});
       places[p].canon_n = static_cast<int>(t.tris.size());
@@ -661,9 +679,9 @@ struct sb_engine {
       d_inst_tris.alloc(n * inst_cap);
       d_inst_cum.alloc(n * inst_cap);
       d_inst_n.alloc(n);
-      d_anchor.alloc(3 * n);
+      d_anchor.alloc(3 * SB_MAX_ANCHORS);  // instance 0's anchor states (sharded runs)
     }
-    d_s0.alloc(3);
+    d_s0.alloc(3 * SB_MAX_ANCHORS);
     d_flags.alloc(2);
     d_valid.alloc(n);
     d_accepted.alloc(std::max<size_t>(1, P) * n);
@@ -729,16 +747,20 @@ struct sb_engine {
       double bx0 = HUGE_VAL, by0 = HUGE_VAL, bx1 = -HUGE_VAL, by1 = -HUGE_VAL, rad = 0.0;
       for (uint32_t k = 0; k < sc->n_supports; ++k) {
         const sb_support& su = sc->supports[k];
-        const double xs[2] = {su.rect[0], su.rect[2]}, ys[2] = {su.rect[1], su.rect[3]};
-        for (double x : xs)
-          for (double y : ys) {
-            const double wx = su.pose[0] * x + su.pose[4] * y + su.pose[12];
-            const double wy = su.pose[1] * x + su.pose[5] * y + su.pose[13];
-            bx0 = std::min(bx0, wx);
-            bx1 = std::max(bx1, wx);
-            by0 = std::min(by0, wy);
-            by1 = std::max(by1, wy);
-          }
+        std::vector<std::array<double, 2>> pts;
+        if (su.n_polygon >= 3 && su.polygon_xy) {
+          for (uint32_t v = 0; v < su.n_polygon; ++v) pts.push_back({su.polygon_xy[2 * v], su.polygon_xy[2 * v + 1]});
+        } else {
+          pts = {{su.rect[0], su.rect[1]}, {su.rect[2], su.rect[1]}, {su.rect[2], su.rect[3]}, {su.rect[0], su.rect[3]}};
+        }
+        for (const auto& q : pts) {
+          const double wx = su.pose[0] * q[0] + su.pose[4] * q[1] + su.pose[12];
+          const double wy = su.pose[1] * q[0] + su.pose[5] * q[1] + su.pose[13];
+          bx0 = std::min(bx0, wx);
+          bx1 = std::max(bx1, wx);
+          by0 = std::min(by0, wy);
+          by1 = std::max(by1, wy);
+        }
       }
       for (const Placement& pl : places) {  // candidates only: fixed objects just clamp
         const SbGeom& g = world->geom_at(pl.dev.geom).g;
@@ -822,27 +844,37 @@ struct sb_engine {
     ++launches;
   }
 
+  // Instance 0's anchor states (x, y, yaw in the support frame) of every anchor into d_anchor.
+  void anchor_states0(const Placement& pl, const SbWorldView& wv, uint64_t& launches) {
+    SbWorldView w1 = wv;
+    w1.n = 1;
+    for (int k = 0; k < std::max(1, pl.dev.n_anchors); ++k) {
+      sbk::anchor_states(w1, pl.dev.anchor_objects[k], pl.inv_support, pl.dev.inv_support_inst,
+                         d_anchor.p + 3 * k, world->s());
+      ++launches;
+    }
+  }
+
   // Sharded runs: instance 0's anchor state and the variation flag are exchanged.
   // Returns true if the anchors vary (per-instance path); else fills the canonical slot.
   bool relation_prep_sharded(size_t p, Placement& pl, const SbWorldView& wv, uint64_t& launches,
                              int& canon_n) {
     cudaStream_t stream = world->stream;
     sb_stream_t s = world->s();
-    double s0[3] = {0, 0, 0};
+    const int na = std::max(1, pl.dev.n_anchors);
+    double s0[3 * SB_MAX_ANCHORS] = {};
     if (begin == 0) {
-      sbk::anchor_states(wv, pl.dev.anchor_object, pl.inv_support, pl.dev.inv_support_inst,
-                         d_anchor.p, s);
-      ++launches;
-      cuda_check(cudaMemcpyAsync(s0, d_anchor.p, sizeof s0, cudaMemcpyDeviceToHost, stream), "D2H s0");
+      anchor_states0(pl, wv, launches);
+      cuda_check(cudaMemcpyAsync(s0, d_anchor.p, 3 * na * sizeof(double), cudaMemcpyDeviceToHost, stream), "D2H s0");
       cuda_check(cudaStreamSynchronize(stream), "sync");
     }
-    std::vector<uint64_t> send(4, 0);
-    std::memcpy(send.data(), s0, sizeof s0);
-    send[3] = begin == 0 ? 1 : 0;
+    std::vector<uint64_t> send(3 * na + 1, 0);
+    std::memcpy(send.data(), s0, 3 * na * sizeof(double));
+    send[3 * na] = begin == 0 ? 1 : 0;
     std::vector<uint64_t> recv = exchange(send);
     for (int r = 0; r < world_size; ++r)
-      if (recv[4 * r + 3]) std::memcpy(s0, &recv[4 * r], sizeof s0);
-    cuda_check(cudaMemcpyAsync(d_s0.p, s0, sizeof s0, cudaMemcpyHostToDevice, stream), "H2D s0");
+      if (recv[(3 * na + 1) * r + 3 * na]) std::memcpy(s0, &recv[(3 * na + 1) * r], 3 * na * sizeof(double));
+    cuda_check(cudaMemcpyAsync(d_s0.p, s0, 3 * na * sizeof(double), cudaMemcpyHostToDevice, stream), "H2D s0");
     sbk::RelationRegionParams rp;
     std::memset(&rp, 0, sizeof rp);
     rp.w = wv;
@@ -891,22 +923,20 @@ struct sb_engine {
     const size_t W = static_cast<size_t>(world_size);
     // send words are unique per (placement, exchange): an all-gather may still read them
     // after this stream has moved on (the sb_shard contract allows a lazy reader)
-    d_xsend.ensure(8 * places.size());
-    d_xgather.ensure(4 * W);
-    uint64_t* send_anchor = d_xsend.p + 8 * p;
-    uint64_t* send_flag = send_anchor + 4;
+    const int na = std::max(1, pl.dev.n_anchors);
+    const uint32_t nsend = 3 * na + 1;
+    d_xsend.ensure(32 * places.size());
+    d_xgather.ensure((3 * SB_MAX_ANCHORS + 1) * W);
+    uint64_t* send_anchor = d_xsend.p + 32 * p;
+    uint64_t* send_flag = send_anchor + nsend;
     auto gather = [&](const uint64_t* send, uint32_t k) {
       if (allgather_dev(allgather_dev_ctx, send, k, d_xgather.p, stream) != 0)
         throw std::runtime_error("sb_shard.allgather_dev failed");
     };
-    if (begin == 0) {
-      sbk::anchor_states(wv, pl.dev.anchor_object, pl.inv_support, pl.dev.inv_support_inst,
-                         d_anchor.p, s);
-      ++launches;
-    }
-    sbk::shard_anchor_pack(begin == 0 ? d_anchor.p : nullptr, send_anchor, s);
-    gather(send_anchor, 4);
-    sbk::shard_anchor_pick(d_xgather.p, world_size, d_s0.p, s);
+    if (begin == 0) anchor_states0(pl, wv, launches);
+    sbk::shard_anchor_pack(begin == 0 ? d_anchor.p : nullptr, na, send_anchor, s);
+    gather(send_anchor, nsend);
+    sbk::shard_anchor_pick(d_xgather.p, world_size, na, d_s0.p, s);
     launches += 2;
     sbk::RelationRegionParams rp;
     std::memset(&rp, 0, sizeof rp);
@@ -1523,6 +1553,108 @@ sb_status sb_triangulate_ring(const double* ring_xy, uint32_t n, double* tris_ou
         tris_out[6 * i + 2 * k] = t[i][k][0];
         tris_out[6 * i + 2 * k + 1] = t[i][k][1];
       }
+  });
+}
+
+// Host restatement of region_for(0) (relationships.cpp:161-230, the serial path of
+// k_relation_regions with glibc as libm) + n PolygonSampler draws from
+// Pcg32(make_stream(seed, c)); test hook for the region pipeline on CPU.
+sb_status sb_region_draws_host(const sb_relation* rel, const sb_support* sup,
+                               const double* states, double erode_r, uint64_t seed,
+                               const uint64_t* c, uint32_t nc, double* out_xy, uint32_t n,
+                               int32_t* n_tris) {
+  return guard([&] {
+    if (!rel || !sup || !n_tris || (n && !out_xy)) throw std::invalid_argument("NULL argument");
+    SbPlacementDev pd;
+    std::memset(&pd, 0, sizeof pd);
+    const std::vector<std::array<double, 2>> given = support_to_dev(*sup, pd);
+    relation_to_dev(*rel, pd);
+    const int na = pd.n_anchors;
+    if (na > 0 && !states) throw std::invalid_argument("anchor states are NULL");
+    std::vector<SbRegionTri> tris(sbp::kHoleCap);
+    std::vector<double> cum(sbp::kHoleCap);
+    sbp::TableSink sink{tris.data(), cum.data(), 0, sbp::kHoleCap, 0.0};
+    const sbp::SupportClip clip{pd.rect, pd.poly_n, pd.poly_x, pd.poly_y};
+    int st = sbp::kRegionOk;
+    if (na == 0) {  // region = the support as given (+ erode of its corrected ring)
+      std::vector<sbh::V2> ring;
+      for (const auto& v : given) ring.push_back({v[0], v[1]});
+      if (erode_r > 0.0) {
+        double a = 0.0;
+        for (size_t i = 0; i < ring.size(); ++i)
+          a += ring[i][0] * ring[(i + 1) % ring.size()][1] - ring[(i + 1) % ring.size()][0] * ring[i][1];
+        if (0.5 * a < 0.0) std::reverse(ring.begin() + 1, ring.end());
+        ring = sbh::erode_convex(ring, erode_r);
+      }
+      sbh::SamplerTable t = sbh::sampler_table({ring});
+      sink.n = static_cast<int>(t.tris.size());
+      for (int k = 0; k < sink.n; ++k) {
+        tris[k] = t.tris[k];
+        cum[k] = t.cum[k];
+      }
+    } else if (pd.distance_type == SB_DIST_MIDDLE) {
+      double mx[SB_MAX_ANCHORS], my[SB_MAX_ANCHORS];
+      for (int k = 0; k < na; ++k) {
+        mx[k] = states[3 * k];
+        my[k] = states[3 * k + 1];
+      }
+      sbp::Ring r, tmp;
+      st = sbp::middle_region_table<sbp::HostMath>(mx, my, na, clip, erode_r, r, tmp, sink);
+      if (st == sbp::kRegionOk) sbp::finish_table(sink);
+    } else {
+      const double ax = states[0], ay = states[1], ayaw = states[2];
+      double min_r = 0.0, max_r = HUGE_VAL;  // distance_band (relationships.cpp:101-122)
+      if (pd.distance_type == SB_DIST_GREATER) min_r = pd.distance;
+      if (pd.distance_type == SB_DIST_LESS) max_r = pd.distance;
+      if (pd.distance_type == SB_DIST_EQUAL) {
+        const double half = std::max(0.05 * pd.distance, 0.01);
+        min_r = std::max(0.0, pd.distance - half);
+        max_r = pd.distance + half;
+      }
+      const double theta = pd.angle_threshold > 0 ? pd.angle_threshold : (pd.direction == SB_DIR_NONE ? M_PI : M_PI / 4.0);
+      double vx = 1.0, vy = 0.0;  // resolve_direction (relationships.cpp:78-99)
+      switch (pd.direction) {
+        case SB_DIR_LEFT: vx = -1.0; vy = 0.0; break;
+        case SB_DIR_RIGHT: vx = 1.0; vy = 0.0; break;
+        case SB_DIR_FRONT: vx = 0.0; vy = -1.0; break;
+        case SB_DIR_BACK: vx = 0.0; vy = 1.0; break;
+        case SB_DIR_VECTOR: {
+          const double nrm = std::sqrt(pd.direction_vector[0] * pd.direction_vector[0] +
+                                       pd.direction_vector[1] * pd.direction_vector[1]);
+          vx = pd.direction_vector[0] / nrm;
+          vy = pd.direction_vector[1] / nrm;
+          break;
+        }
+        default: break;
+      }
+      if (pd.direction != SB_DIR_NONE && pd.frame == SB_FRAME_LOCAL) {
+        const double cs = std::cos(ayaw), sn = std::sin(ayaw);
+        const double rx = cs * vx - sn * vy, ry = sn * vx + cs * vy;
+        vx = rx;
+        vy = ry;
+      }
+      const double bx0 = std::min(pd.bounds[0], ax), by0 = std::min(pd.bounds[1], ay);
+      const double bx1 = std::max(pd.bounds[2], ax), by1 = std::max(pd.bounds[3], ay);
+      const double ddx = bx1 - bx0, ddy = by1 - by0;
+      const double diag = bx0 > bx1 ? 0.0 : std::sqrt(ddx * ddx + ddy * ddy);
+      if (std::isinf(max_r)) max_r = std::fmax(diag, min_r + 1e-6);
+      sbp::HoleScratch sc;
+      if (theta >= M_PI - 1e-12 && min_r > 0.0)
+        st = sbp::hole_annulus_table<sbp::HostMath>(ax, ay, min_r, max_r, clip, erode_r, sc, sink);
+      else
+        st = sbp::big_region_table<sbp::HostMath>(ax, ay, vx, vy, theta, min_r, max_r, clip, erode_r, sc, sink);
+      if (st == sbp::kRegionOk) sbp::finish_table(sink);
+    }
+    if (st != sbp::kRegionOk && st != sbp::kRegionEmpty)
+      throw std::invalid_argument("region build failed (status " + std::to_string(st) + ")");
+    const int nt = st == sbp::kRegionOk ? sink.n : 0;
+    *n_tris = nt;
+    if (nt == 0 || n == 0) return;
+    std::vector<double> d(3 * static_cast<size_t>(n));
+    if (sb_stream_doubles(seed, c, nc, d.data(), 3 * n) != SB_OK) throw std::runtime_error(g_error);
+    for (uint32_t k = 0; k < n; ++k)
+      sbp::draw_point(tris.data(), cum.data(), nt, d[3 * k], d[3 * k + 1], d[3 * k + 2],
+                      out_xy[2 * k], out_xy[2 * k + 1]);
   });
 }
 

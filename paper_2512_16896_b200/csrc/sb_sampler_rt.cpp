@@ -186,8 +186,13 @@ struct sb_sampler {
     if (batch > 0xffffffffull) throw std::invalid_argument("batch_size exceeds 2^32");
     SbPlacementDev pd;
     std::memset(&pd, 0, sizeof pd);
+    if (relation_anchor_count(rel) > 1)
+      throw std::invalid_argument("prepare_relation: the anchor state batch holds one anchor");
     const bool hole = relation_to_dev(rel, pd);
-    for (int k = 0; k < 4; ++k) pd.rect[k] = rect[k];
+    sb_support sup;
+    std::memset(&sup, 0, sizeof sup);
+    for (int k = 0; k < 4; ++k) sup.rect[k] = rect[k];
+    support_to_dev(sup, pd);  // rect + bounds
     if (rel.anchor < 0) {  // no anchors: region = support (relationships.cpp:168-171)
       const double xy[8] = {rect[0], rect[1], rect[2], rect[1], rect[2], rect[3], rect[0], rect[3]};
       const uint32_t off[2] = {0, 4};

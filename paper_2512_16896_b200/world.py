@@ -208,7 +208,9 @@ class CollisionWorld:
 # ------------------------------------------------------------------------ scene spec
 @dataclass
 class Relation:
-    """RelationshipSpec (relationships.hpp:18-38), zero or one anchor."""
+    """RelationshipSpec (relationships.hpp:18-38): anchors = [anchor] + extra_anchors
+    (placement indices); `middle` takes two or more, the other distance types and a
+    direction exactly one."""
     anchor: int = -1
     distance_type: int = A.SB_DIST_NONE
     direction: int = A.SB_DIR_NONE
@@ -216,11 +218,16 @@ class Relation:
     direction_vector: tuple = (0.0, 0.0)
     distance: float = 0.0
     angle_threshold: float = 0.0   # <= 0: default
+    extra_anchors: tuple = ()
 
     def to_c(self) -> "A.sb_relation":
+        if len(self.extra_anchors) > A.SB_MAX_ANCHORS - 1:
+            raise ValueError(f"at most {A.SB_MAX_ANCHORS} anchors per relation")
+        extra = list(self.extra_anchors) + [-1] * (A.SB_MAX_ANCHORS - 1 - len(self.extra_anchors))
         return A.sb_relation(self.anchor, self.distance_type, self.direction, self.frame,
                              (C.c_double * 2)(*self.direction_vector), self.distance,
-                             self.angle_threshold)
+                             self.angle_threshold, len(self.extra_anchors),
+                             (C.c_int32 * (A.SB_MAX_ANCHORS - 1))(*extra))
 
 
 @dataclass
@@ -235,14 +242,48 @@ class Placement:
 
 @dataclass
 class Support:
-    """A support surface (sb_support): rect in the z = 0 plane of its frame. The frame is
+    """A support surface (sb_support) in the z = 0 plane of its frame: `rect`, or the
+    convex `polygon` ((k, 2), k <= 16; SupportSurface::polygon) when given. The frame is
     `pose`, or per instance `poses` ((N, 4, 4), e.g. FK world poses of a drawer times the
     surface frame), or -- with on_placement >= 0 -- the accepted pose of that earlier
     placement times `pose` (a surface on a placed object)."""
     pose: np.ndarray
-    rect: tuple  # x0, y0, x1, y1 in the support frame
+    rect: tuple = (0.0, 0.0, 0.0, 0.0)  # x0, y0, x1, y1 in the support frame
     poses: Optional[np.ndarray] = None
     on_placement: int = -1
+    polygon: Optional[np.ndarray] = None
+
+
+def support_to_c(s: "Support", keep: list) -> "A.sb_support":
+    """sb_support of a Support (keep: keepalive list for the arrays it points to)."""
+    out = A.sb_support()
+    out.pose[:] = list(colmajor(s.pose))
+    out.rect[:] = list(map(float, s.rect))
+    out.on_placement = s.on_placement
+    if s.polygon is not None:
+        poly = np.ascontiguousarray(np.asarray(s.polygon, np.float64).reshape(-1, 2))
+        keep.append(poly)
+        out.n_polygon = len(poly)
+        out.polygon_xy = _dp(poly)
+    return out
+
+
+def region_draws_host(relation: "Relation", support: "Support", states, erode_r: float,
+                      seed: int, c, n: int):
+    """sb_region_draws_host: region_for(0) restated on the host (the serial region path's
+    code) + n sampler draws; returns ((n, 2) points, triangle count). states: (na, 3)."""
+    keep = []
+    sup = support_to_c(support, keep)
+    rel = relation.to_c()
+    st = np.ascontiguousarray(np.asarray(states, np.float64).reshape(-1))
+    cc = np.ascontiguousarray(np.asarray(c, np.uint64))
+    out = np.zeros((max(n, 1), 2))
+    nt = C.c_int32()
+    A.check(A.lib().sb_region_draws_host(C.byref(rel), C.byref(sup), _dp(st) if st.size else None,
+                                         erode_r, seed,
+                                         cc.ctypes.data_as(C.POINTER(C.c_uint64)), len(cc),
+                                         _dp(out), n, C.byref(nt)))
+    return out[:n].copy(), nt.value
 
 
 @dataclass
@@ -287,18 +328,13 @@ class Scene:
             fixed[i].poses16 = batch(f.poses)
         sups = (A.sb_support * max(1, len(self.supports)))()
         for i, s in enumerate(self.supports):
-            sups[i].pose[:] = list(colmajor(s.pose))
-            sups[i].rect[:] = list(map(float, s.rect))
+            sups[i] = support_to_c(s, keep)
             sups[i].poses16 = batch(s.poses)
-            sups[i].on_placement = s.on_placement
         pls = (A.sb_placement * max(1, len(self.placements)))()
         for i, p in enumerate(self.placements):
             r = p.relation
-            pls[i] = A.sb_placement(
-                p.mesh, p.support, p.orientation, p.face_target,
-                A.sb_relation(r.anchor, r.distance_type, r.direction, r.frame,
-                              (C.c_double * 2)(*r.direction_vector), r.distance,
-                              r.angle_threshold), p.ratio_on_support)
+            pls[i] = A.sb_placement(p.mesh, p.support, p.orientation, p.face_target, r.to_c(),
+                                    p.ratio_on_support)
         sc = A.sb_scene(self.n_instances, self.attempts, 0,
                         len(self.meshes), meshes, len(self.fixed), fixed,
                         len(self.supports), sups, len(self.placements), pls)

@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol():
     for s in syms:
         assert hasattr(L, s), s
     assert set(A.SIGNATURES) >= syms  # every symbol is bound with a signature
-    assert L.sb_abi_version() == 1
+    assert L.sb_abi_version() == 2
 
 
 def test_no_device_fails_loudly():
