@@ -325,13 +325,17 @@ REF_SAMPLE = {"c1_tabletop": 1024, "c2_mixed": 16384, "c3_kitchen": 8192, "c4_cl
 
 
 def reference_scene(args, n):
-    """The workload's scene built with the reference's own mesh constructors
-    (oracle/_ref: trimesh.cpp make_box / make_cylinder / make_sphere, transform_point)."""
+    """The workload's scene built with the reference's own mesh constructors and
+    support-surface extraction (oracle/_ref: trimesh.cpp make_box / make_cylinder /
+    make_sphere, transform_point; surface.cpp extract_support_surfaces)."""
     from oracle import oracle as O
     from paper_2512_16896_b200 import scenes
     from paper_2512_16896_b200.world import TriMesh
 
-    prims = {"make_box": lambda sx, sy, sz: TriMesh(*O.make_box(sx, sy, sz)),
+    prims = {"extract_support_surfaces": lambda m, mode: [
+                 (poly, frame.reshape(4, 4).T)
+                 for poly, frame, _, _ in O.extract_support_surfaces(m.vertices, m.triangles, mode)],
+             "make_box": lambda sx, sy, sz: TriMesh(*O.make_box(sx, sy, sz)),
              "make_cylinder": lambda r, h, seg=32: TriMesh(*O.make_cylinder(r, h, seg)),
              "make_sphere": lambda r, st=12, sl=16: TriMesh(*O.make_sphere(r, st, sl)),
              "transformed": lambda m, pose: TriMesh(O.transformed_vertices(m.vertices, pose),

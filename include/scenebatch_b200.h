@@ -300,6 +300,29 @@ sb_status sb_comm_barrier(sb_comm* c);
 /* 1 if the device exchange waits with stream memory operations, 0 if it spins a kernel. */
 int32_t sb_comm_uses_stream_waits(const sb_comm* c);
 
+/* ------------------------------------------------------------------------------------
+ * Support-surface extraction (surface.cpp:53-153; host, cold start):
+ * upward facets within 5 degrees of +z clustered by shared edges, each cluster's xy
+ * projection merged with union_of (the oracle's Boost stand-in semantics: edge splicing),
+ * parts below 1e-4 m^2 dropped, roofed by a majority of 16 upward ray casts from sampler
+ * draws, sorted by area (largest first). mode: SB_SURFACE_ON (open to the sky),
+ * SB_SURFACE_INSIDE (roofed cavity floors), SB_SURFACE_ALL (extract_all_support_surfaces).
+ * A surface's `frame` is translation(0, 0, z_top) (column-major); polygons with more than
+ * SB_MAX_SURFACE_VERTS vertices are an error. */
+enum { SB_SURFACE_ON = 0, SB_SURFACE_INSIDE = 1, SB_SURFACE_ALL = -1 };
+#define SB_MAX_SURFACE_VERTS 96
+typedef struct sb_surface {
+  double frame[16];
+  double area;
+  int32_t roofed;
+  uint32_t n_polygon;
+  double polygon_xy[2 * SB_MAX_SURFACE_VERTS];
+} sb_surface;
+sb_status sb_extract_support_surfaces(const double* vertices, uint32_t n_vertices,
+                                      const uint32_t* triangles, uint32_t n_triangles,
+                                      int32_t mode, sb_surface* out, uint32_t cap,
+                                      uint32_t* n_out);
+
 /* Test hook (host, no GPU): region_for(0) of build_constraint_region + apply_ratio_on_support
  * (relationships.cpp:161-230) restated on the host with the serial region path's code
  * (sb_poly.h) and glibc as libm -- states: (x, y, yaw) per anchor in the support frame --

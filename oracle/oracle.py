@@ -69,6 +69,8 @@ def lib():
         L.ref_region_draws.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_double,
                                        C.c_double, u64, C.c_void_p, C.c_uint32, C.c_void_p,
                                        C.c_uint32, C.c_void_p]
+        L.ref_extract_support_surfaces.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint32,
+                                                   C.c_int32, C.c_void_p, C.c_uint32, C.c_void_p]
         L.ref_middle_polygon.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint32, C.c_void_p]
         L.ref_relation_region.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_double,
                                           C.c_double, C.c_void_p, C.c_uint32, C.c_void_p,
@@ -217,6 +219,28 @@ def region_draws(rel_c, sup_c, states, ratio, fx, fy, seed, c, n):
     check(lib().ref_region_draws(C.byref(rel_c), C.byref(sup_c), _p(st) if st.size else None,
                                  ratio, fx, fy, seed, _p(cc), len(cc), _p(out), n, C.byref(nt)))
     return out[:n].copy(), nt.value
+
+
+def extract_support_surfaces(vertices, triangles, mode=0):
+    """extract_support_surfaces (mode 0 on / 1 inside) or extract_all_support_surfaces
+    (mode -1) of the reference -> list of (polygon (k, 2), frame colmajor 16, roofed, area)."""
+    class sb_surface(C.Structure):  # include/scenebatch_b200.h
+        _fields_ = [("frame", C.c_double * 16), ("area", C.c_double), ("roofed", C.c_int32),
+                    ("n_polygon", C.c_uint32), ("polygon_xy", C.c_double * 192)]
+
+    v = np.ascontiguousarray(vertices, np.float64)
+    t = np.ascontiguousarray(triangles, np.uint32)
+    cap = 256
+    arr = (sb_surface * cap)()
+    n = C.c_uint32()
+    check(lib().ref_extract_support_surfaces(_p(v), len(v), _p(t), len(t), mode, arr, cap,
+                                             C.byref(n)))
+    out = []
+    for k in range(min(n.value, cap)):
+        s = arr[k]
+        out.append((np.array(s.polygon_xy[: 2 * s.n_polygon]).reshape(-1, 2), np.array(s.frame),
+                    bool(s.roofed), s.area))
+    return out
 
 
 def middle_polygon(points):

@@ -249,6 +249,33 @@ int ref_region_draws(const sb_relation* rel, const sb_support* sup, const double
     }
   });
 }
+// extract_support_surfaces / extract_all_support_surfaces (surface.cpp:53-153) into
+// sb_surface records (mode: SB_SURFACE_*).
+int ref_extract_support_surfaces(const double* v, uint32_t nv, const uint32_t* t, uint32_t nt,
+                                 int32_t mode, sb_surface* out, uint32_t cap, uint32_t* n_out) {
+  REF_TRY({
+    TriMesh m = mesh_from(v, nv, t, nt);
+    std::vector<SupportSurface> ss = mode == SB_SURFACE_ALL
+                                         ? extract_all_support_surfaces(m)
+                                         : extract_support_surfaces(m, static_cast<SurfaceMode>(mode));
+    *n_out = static_cast<uint32_t>(ss.size());
+    for (std::size_t k = 0; k < ss.size() && k < cap; ++k) {
+      sb_surface& o = out[k];
+      std::memset(&o, 0, sizeof o);
+      for (int c = 0; c < 4; ++c)
+        for (int r = 0; r < 4; ++r) o.frame[4 * c + r] = ss[k].frame(r, c);
+      o.area = ss[k].area;
+      o.roofed = ss[k].roofed ? 1 : 0;
+      const auto& ext = ss[k].polygon.exterior;
+      if (ext.size() > SB_MAX_SURFACE_VERTS) throw std::invalid_argument("surface polygon too large");
+      o.n_polygon = static_cast<uint32_t>(ext.size());
+      for (std::size_t i = 0; i < ext.size(); ++i) {
+        o.polygon_xy[2 * i] = ext[i].x();
+        o.polygon_xy[2 * i + 1] = ext[i].y();
+      }
+    }
+  });
+}
 // middle_polygon (relationships.cpp:124-157) of n points -> exterior ring.
 int ref_middle_polygon(const double* xy, uint32_t n, double* out, uint32_t cap, uint32_t* nout) {
   REF_TRY({

@@ -924,10 +924,20 @@ def generate(scene, run_seed: int):
         sup = scene.supports[pl.support]
         S = _rows(colmajor(sup.pose))
         rect = tuple(map(float, sup.rect))
+        canon = rect_ring(*rect)
+        if getattr(sup, "polygon", None) is not None:
+            # a polygon support (e.g. from extract_support_surfaces): the ring as given feeds
+            # the sampler; this restatement clips only axis-aligned rectangles (convex
+            # polygons are covered by the compiled reference, tests/test_region_widening.py)
+            canon = [(float(x), float(y)) for x, y in sup.polygon]
+            xs, ys = [q[0] for q in canon], [q[1] for q in canon]
+            rect = (min(xs), min(ys), max(xs), max(ys))
+            if len(canon) != 4 or any(x not in (rect[0], rect[2]) or y not in (rect[1], rect[3])
+                                      for x, y in canon):
+                raise NotImplementedError("restate: non-rectangular polygon support")
         z_off = -aabb_of(meshes[pl.mesh].v)[0][2] + 1e-3  # rest_pose (sampler.cpp:45-52)
         r = pl.relation
         regions = None
-        canon = rect_ring(*rect)
         if r.anchor >= 0:
             inv_s = inverse_rigid(S)
             states = []

@@ -9,8 +9,9 @@ from .graph import BatchedSceneGraph, JointSpec  # noqa: F401
 from .reach import ChainLink, KinematicChain, ReachMap4D, placement_filter  # noqa: F401
 from .sampler import PositionSampler, sample_orientations  # noqa: F401
 from .world import (CollisionWorld, Engine, Fixed, GenerationResult, Placement, Relation,  # noqa: F401
-                    Scene, Shard, Support, TriMesh, colmajor, from_colmajor, make_box,
-                    make_cylinder, make_sphere, merge, transformed, translation)
+                    Scene, Shard, Support, SupportSurface, TriMesh, colmajor,
+                    extract_support_surfaces, from_colmajor, make_box, make_cylinder,
+                    make_sphere, merge, transformed, translation)
 
 
 def device_available() -> bool:

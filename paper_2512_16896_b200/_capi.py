@@ -47,6 +47,15 @@ class sb_support(C.Structure):
                 ("n_polygon", C.c_uint32), ("polygon_xy", C.POINTER(C.c_double))]
 
 
+SB_SURFACE_ON, SB_SURFACE_INSIDE, SB_SURFACE_ALL = 0, 1, -1
+SB_MAX_SURFACE_VERTS = 96
+
+
+class sb_surface(C.Structure):
+    _fields_ = [("frame", C.c_double * 16), ("area", C.c_double), ("roofed", C.c_int32),
+                ("n_polygon", C.c_uint32), ("polygon_xy", C.c_double * (2 * SB_MAX_SURFACE_VERTS))]
+
+
 class sb_joint(C.Structure):
     _fields_ = [("kind", C.c_int32), ("axis", C.c_double * 3), ("lo", C.c_double),
                 ("hi", C.c_double)]
@@ -145,6 +154,8 @@ SIGNATURES = {
                                  C.POINTER(C.c_int32)]),
     "sb_get_stats": (C.c_int, [_P, C.POINTER(sb_stats)]),
     "sb_reset_stats": (C.c_int, [_P]),
+    "sb_extract_support_surfaces": (C.c_int, [_D, C.c_uint32, _U32, C.c_uint32, C.c_int32,
+                                              C.POINTER(sb_surface), C.c_uint32, _U32]),
     "sb_region_draws_host": (C.c_int, [C.POINTER(sb_relation), C.POINTER(sb_support), _D, C.c_double,
                                        C.c_uint64, C.POINTER(C.c_uint64), C.c_uint32, _D, C.c_uint32,
                                        C.POINTER(C.c_int32)]),

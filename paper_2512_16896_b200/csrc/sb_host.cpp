@@ -5,6 +5,8 @@
 #include <cmath>
 #include <cstring>
 #include <limits>
+#include <map>
+#include <numeric>
 #include <stdexcept>
 
 #include "sb_poly.h"
@@ -350,6 +352,228 @@ std::vector<V2> erode_convex(const std::vector<V2>& ring, double r) {
     const V2& q = out[(i + 1) % n];
     if (!((q[0] - p[0]) * dx[i] + (q[1] - p[1]) * dy[i] > 0.0)) return {};  // eroded away
   }
+  return out;
+}
+
+
+// ------------------------------------------------------------ support-surface extraction
+namespace {
+
+struct Pcg32H {  // rng.hpp:24-60
+  uint64_t state = 0, inc;
+  explicit Pcg32H(uint64_t seed, uint64_t seq = 0xda3e39cb94b95bdbULL) : inc((seq << 1u) | 1u) {
+    next_u32();
+    state += seed;
+    next_u32();
+  }
+  uint32_t next_u32() {
+    const uint64_t old = state;
+    state = old * 6364136223846793005ULL + inc;
+    const uint32_t xs = static_cast<uint32_t>(((old >> 18u) ^ old) >> 27u);
+    const uint32_t rot = static_cast<uint32_t>(old >> 59u);
+    return (xs >> rot) | (xs << ((32u - rot) & 31u));
+  }
+  double next_double() {
+    const uint64_t hi = next_u32();  // GCC evaluates the left operand first
+    const uint64_t w = (hi << 32) | next_u32();
+    return static_cast<double>(w >> 11) * 0x1.0p-53;
+  }
+};
+
+// the shim's ring helpers (oracle/shim/boost/geometry.hpp): exact duplicates only
+double shim_signed_area(const std::vector<V2>& r) {
+  double s = 0.0;
+  const std::size_t n = r.size();
+  for (std::size_t i = 0; i < n; ++i) {
+    const V2& a = r[i];
+    const V2& b = r[(i + 1) % n];
+    s += a[0] * b[1] - b[0] * a[1];
+  }
+  return 0.5 * s;
+}
+std::vector<V2> shim_dedupe(const std::vector<V2>& r) {
+  std::vector<V2> o;
+  for (const V2& p : r)
+    if (o.empty() || p[0] != o.back()[0] || p[1] != o.back()[1]) o.push_back(p);
+  while (o.size() > 1 && o.front()[0] == o.back()[0] && o.front()[1] == o.back()[1]) o.pop_back();
+  return o;
+}
+// to_boost's bg::correct of an open exterior: counter-clockwise, vertex 0 first
+std::vector<V2> shim_correct(std::vector<V2> r) {
+  std::vector<V2> closed = r;
+  if (!closed.empty()) closed.push_back(closed.front());
+  if (shim_signed_area(closed) < 0.0) std::reverse(r.begin() + (r.empty() ? 0 : 1), r.end());
+  return r;
+}
+// splice ring b into ring a along one shared edge (a: u->v, b: v->u)
+bool shim_splice(std::vector<V2>& a, const std::vector<V2>& b) {
+  const std::size_t na = a.size(), nb = b.size();
+  for (std::size_t i = 0; i < na; ++i) {
+    const V2& u = a[i];
+    const V2& v = a[(i + 1) % na];
+    for (std::size_t j = 0; j < nb; ++j) {
+      const V2& p = b[j];
+      const V2& q = b[(j + 1) % nb];
+      if (p[0] == v[0] && p[1] == v[1] && q[0] == u[0] && q[1] == u[1]) {
+        std::vector<V2> out;
+        for (std::size_t k = 0; k <= i; ++k) out.push_back(a[k]);
+        for (std::size_t k = 2; k < nb; ++k) out.push_back(b[(j + k) % nb]);
+        for (std::size_t k = i + 1; k < na; ++k) out.push_back(a[k]);
+        a = shim_dedupe(out);
+        return true;
+      }
+    }
+  }
+  return false;
+}
+// union_of(a, b) (polygon.cpp:121-125): to_boost both, the shim's union_, from_boost
+std::vector<std::vector<V2>> shim_union(const std::vector<std::vector<V2>>& a,
+                                        const std::vector<std::vector<V2>>& b) {
+  std::vector<std::vector<V2>> parts;
+  for (const auto& p : a) parts.push_back(shim_correct(p));
+  for (const auto& q : b) {
+    std::vector<V2> ring = shim_correct(q);
+    std::size_t host = parts.size();
+    for (std::size_t k = 0; k < parts.size() && host == parts.size(); ++k)
+      if (shim_splice(parts[k], ring)) host = k;
+    if (host == parts.size()) {
+      parts.push_back(ring);
+      continue;
+    }
+    for (bool again = true; again;) {
+      again = false;
+      for (std::size_t k = 0; k < parts.size(); ++k) {
+        if (k == host) continue;
+        if (shim_splice(parts[host], parts[k])) {
+          parts.erase(parts.begin() + static_cast<std::ptrdiff_t>(k));
+          if (k < host) --host;
+          again = true;
+          break;
+        }
+      }
+    }
+  }
+  std::vector<std::vector<V2>> out;  // from_boost: closed ring -> ring_to_vec, >= 3 points
+  for (auto& r : parts) {
+    std::vector<V2> v = r;
+    if (!v.empty()) v.push_back(v.front());  // close_ring
+    if (v.size() > 1) {
+      const double dx = v.front()[0] - v.back()[0], dy = v.front()[1] - v.back()[1];
+      if (std::sqrt(dx * dx + dy * dy) < 1e-15) v.pop_back();
+    }
+    if (v.size() >= 3) out.push_back(std::move(v));
+  }
+  return out;
+}
+
+// Moller-Trumbore with a +z ray (surface.cpp:20-37)
+double ray_up_hit(const Mesh& m, std::size_t t, const V3& o) {
+  const auto& tri = m.t[t];
+  const V3& v0 = m.v[tri[0]];
+  const V3 e1 = {m.v[tri[1]][0] - v0[0], m.v[tri[1]][1] - v0[1], m.v[tri[1]][2] - v0[2]};
+  const V3 e2 = {m.v[tri[2]][0] - v0[0], m.v[tri[2]][1] - v0[1], m.v[tri[2]][2] - v0[2]};
+  const V3 pvec = {-e2[1], e2[0], 0.0};
+  const double det = e1[0] * pvec[0] + e1[1] * pvec[1] + e1[2] * pvec[2];
+  if (std::abs(det) < 1e-14) return -1.0;
+  const double inv = 1.0 / det;
+  const V3 tv = {o[0] - v0[0], o[1] - v0[1], o[2] - v0[2]};
+  const double u = (tv[0] * pvec[0] + tv[1] * pvec[1] + tv[2] * pvec[2]) * inv;
+  if (u < -1e-12 || u > 1.0 + 1e-12) return -1.0;
+  const V3 q = {tv[1] * e1[2] - tv[2] * e1[1], tv[2] * e1[0] - tv[0] * e1[2],
+                tv[0] * e1[1] - tv[1] * e1[0]};
+  const double v = q[2] * inv;
+  if (v < -1e-12 || u + v > 1.0 + 1e-12) return -1.0;
+  return (e2[0] * q[0] + e2[1] * q[1] + e2[2] * q[2]) * inv;
+}
+
+}  // namespace
+
+std::vector<Surface> extract_all_support_surfaces(const Mesh& mesh) {
+  std::vector<Surface> out;
+  if (mesh.t.empty()) return out;
+  const double cos_tol = std::cos(5.0 * M_PI / 180.0);
+  std::vector<std::size_t> up;
+  for (std::size_t t = 0; t < mesh.t.size(); ++t) {  // triangle_normal (trimesh.cpp:31-36)
+    const auto& tri = mesh.t[t];
+    const V3& a = mesh.v[tri[0]];
+    const V3 b = {mesh.v[tri[1]][0] - a[0], mesh.v[tri[1]][1] - a[1], mesh.v[tri[1]][2] - a[2]};
+    const V3 c = {mesh.v[tri[2]][0] - a[0], mesh.v[tri[2]][1] - a[1], mesh.v[tri[2]][2] - a[2]};
+    const V3 n = {b[1] * c[2] - b[2] * c[1], b[2] * c[0] - b[0] * c[2], b[0] * c[1] - b[1] * c[0]};
+    const double len = std::sqrt(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]);
+    const double nz = len > 0.0 ? n[2] / len : 0.0;
+    if (nz >= cos_tol) up.push_back(t);
+  }
+  if (up.empty()) return out;
+  std::vector<int> parent(up.size());  // DisjointSet with path halving
+  std::iota(parent.begin(), parent.end(), 0);
+  auto find = [&](int x) {
+    while (parent[x] != x) x = parent[x] = parent[parent[x]];
+    return x;
+  };
+  using EdgeKey = std::array<int64_t, 6>;
+  std::map<EdgeKey, int> edge_owner;
+  auto quantize = [](double v) { return static_cast<int64_t>(std::llround(v * 1e9)); };
+  for (std::size_t i = 0; i < up.size(); ++i) {
+    const auto& tri = mesh.t[up[i]];
+    for (int e = 0; e < 3; ++e) {
+      const V3& a = mesh.v[tri[e]];
+      const V3& b = mesh.v[tri[(e + 1) % 3]];
+      const EdgeKey ka{quantize(a[0]), quantize(a[1]), quantize(a[2]),
+                       quantize(b[0]), quantize(b[1]), quantize(b[2])};
+      const EdgeKey kb{ka[3], ka[4], ka[5], ka[0], ka[1], ka[2]};
+      auto [it, inserted] = edge_owner.try_emplace(std::min(ka, kb), static_cast<int>(i));
+      if (!inserted) parent[find(it->second)] = find(static_cast<int>(i));
+    }
+  }
+  std::map<int, std::vector<std::size_t>> clusters;
+  for (std::size_t i = 0; i < up.size(); ++i) clusters[find(static_cast<int>(i))].push_back(up[i]);
+  int cluster_index = 0;
+  for (const auto& [root, tris] : clusters) {
+    (void)root;
+    double z_top = -std::numeric_limits<double>::infinity();
+    for (std::size_t t : tris)
+      for (uint32_t vi : mesh.t[t]) z_top = std::max(z_top, mesh.v[vi][2]);
+    std::vector<std::vector<V2>> merged;
+    for (std::size_t t : tris) {
+      const auto& tri = mesh.t[t];
+      std::vector<V2> p;
+      for (int k = 0; k < 3; ++k) p.push_back({mesh.v[tri[k]][0], mesh.v[tri[k]][1]});
+      const double a2 = (p[1][0] - p[0][0]) * (p[2][1] - p[0][1]) - (p[1][1] - p[0][1]) * (p[2][0] - p[0][0]);
+      if (std::abs(a2) < 1e-14) continue;
+      if (a2 < 0.0) std::reverse(p.begin(), p.end());
+      merged = merged.empty() ? std::vector<std::vector<V2>>{p} : shim_union(merged, {p});
+    }
+    for (auto& part : merged) {
+      std::vector<V2> closed = shim_correct(part);  // area(MultiPolygon) via to_boost
+      closed.push_back(closed.front());
+      const double a = std::abs(shim_signed_area(closed));
+      if (a < 1e-4) continue;
+      Surface s;
+      s.z_top = z_top;
+      s.area = a;
+      const SamplerTable tab = sampler_table({part});  // PolygonSampler(one)
+      Pcg32H rng(mix64(mix64(0x853c49e6748fea9bULL ^ 0x726f6f66ULL) ^ static_cast<uint64_t>(cluster_index)));
+      int hits = 0, cast = 0;
+      for (int i = 0; i < 16 && !tab.tris.empty(); ++i) {
+        const double u = rng.next_double(), r1 = rng.next_double(), r2 = rng.next_double();
+        double px, py;
+        sbp::draw_point(tab.tris.data(), tab.cum.data(), static_cast<int>(tab.tris.size()), u, r1,
+                        r2, px, py);
+        const V3 origin = {px, py, z_top};
+        ++cast;
+        for (std::size_t t = 0; t < mesh.t.size(); ++t)
+          if (ray_up_hit(mesh, t, origin) > 1e-4) {
+            ++hits;
+            break;
+          }
+      }
+      s.roofed = cast > 0 && hits * 2 >= cast;
+      s.polygon = part;
+      out.push_back(std::move(s));
+      ++cluster_index;
+    }
+  }
+  std::stable_sort(out.begin(), out.end(), [](const Surface& a, const Surface& b) { return a.area > b.area; });
   return out;
 }
 

@@ -63,4 +63,17 @@ std::vector<V2> erode_convex(const std::vector<V2>& ring, double r);
 // splitmix64 / make_stream seed derivation (rng.hpp:9-21,63-67)
 uint64_t mix64(uint64_t x);
 
+// extract_all_support_surfaces (surface.cpp:53-142): upward facets (normal within 5 deg of
+// +z) clustered by shared edges (quantized 1e-9 positions), each cluster's xy projection
+// merged with the union stand-in (union_of, polygon.cpp:121-125, as oracle/shim defines
+// bg::union_), parts below 1e-4 m^2 dropped, the roof flag by a majority vote of 16 upward
+// ray casts from sampler draws; stable-sorted by area, largest first.
+struct Surface {
+  std::vector<V2> polygon;  // exterior ring in the z = z_top plane
+  double z_top = 0.0;
+  double area = 0.0;
+  bool roofed = false;
+};
+std::vector<Surface> extract_all_support_surfaces(const Mesh& m);
+
 }  // namespace sbh

@@ -1556,6 +1556,48 @@ sb_status sb_triangulate_ring(const double* ring_xy, uint32_t n, double* tris_ou
   });
 }
 
+sb_status sb_extract_support_surfaces(const double* vertices, uint32_t n_vertices,
+                                      const uint32_t* triangles, uint32_t n_triangles,
+                                      int32_t mode, sb_surface* out, uint32_t cap,
+                                      uint32_t* n_out) {
+  return guard([&] {
+    if (!n_out || (cap && !out)) throw std::invalid_argument("NULL argument");
+    if (mode < SB_SURFACE_ALL || mode > SB_SURFACE_INSIDE) throw std::invalid_argument("surface mode");
+    sbh::Mesh m;
+    if ((n_vertices && !vertices) || (n_triangles && !triangles)) throw std::invalid_argument("mesh arrays are NULL");
+    m.v.resize(n_vertices);
+    m.t.resize(n_triangles);
+    for (uint32_t k = 0; k < n_vertices; ++k) m.v[k] = {vertices[3 * k], vertices[3 * k + 1], vertices[3 * k + 2]};
+    for (uint32_t k = 0; k < n_triangles; ++k) {
+      m.t[k] = {triangles[3 * k], triangles[3 * k + 1], triangles[3 * k + 2]};
+      for (int c = 0; c < 3; ++c)
+        if (m.t[k][c] >= n_vertices) throw std::out_of_range("triangle vertex index");
+    }
+    std::vector<sbh::Surface> all = sbh::extract_all_support_surfaces(m);
+    uint32_t k = 0;
+    for (const sbh::Surface& sf : all) {  // extract_support_surfaces (surface.cpp:145-153)
+      if (mode != SB_SURFACE_ALL && (mode == SB_SURFACE_INSIDE) != sf.roofed) continue;
+      if (k < cap) {
+        sb_surface& o = out[k];
+        std::memset(&o, 0, sizeof o);
+        o.frame[0] = o.frame[5] = o.frame[10] = o.frame[15] = 1.0;
+        o.frame[14] = sf.z_top;
+        o.area = sf.area;
+        o.roofed = sf.roofed ? 1 : 0;
+        if (sf.polygon.size() > SB_MAX_SURFACE_VERTS)
+          throw std::invalid_argument("support surface polygon exceeds SB_MAX_SURFACE_VERTS");
+        o.n_polygon = static_cast<uint32_t>(sf.polygon.size());
+        for (size_t v = 0; v < sf.polygon.size(); ++v) {
+          o.polygon_xy[2 * v] = sf.polygon[v][0];
+          o.polygon_xy[2 * v + 1] = sf.polygon[v][1];
+        }
+      }
+      ++k;
+    }
+    *n_out = k;
+  });
+}
+
 // Host restatement of region_for(0) (relationships.cpp:161-230, the serial path of
 // k_relation_regions with glibc as libm) + n PolygonSampler draws from
 // Pcg32(make_stream(seed, c)); test hook for the region pipeline on CPU.

@@ -20,14 +20,21 @@ from . import _capi as A
 from . import world as _world
 from .world import Fixed, Placement, Relation, Scene, Support, TriMesh, merge, translation
 
+def _extract(mesh: TriMesh, mode: int):
+    """(polygon (k, 2), frame (4, 4)) of each support surface (sb_extract_support_surfaces)."""
+    return [(s.polygon, s.frame) for s in _world.extract_support_surfaces(mesh, mode)]
+
+
 _PRIMS = {"make_box": _world.make_box, "make_cylinder": _world.make_cylinder,
-          "make_sphere": _world.make_sphere, "transformed": _world.transformed}
+          "make_sphere": _world.make_sphere, "transformed": _world.transformed,
+          "extract_support_surfaces": _extract}
 
 
 @contextlib.contextmanager
 def mesh_source(**prims):
     """Temporarily build scenes with other primitive constructors (same signatures as
-    world.make_box / make_cylinder / make_sphere / transformed)."""
+    world.make_box / make_cylinder / make_sphere / transformed, and
+    extract_support_surfaces(mesh, mode) -> [(polygon, frame)])."""
     old = dict(_PRIMS)
     _PRIMS.update(prims)
     try:
@@ -149,17 +156,26 @@ def open_container(sx=0.6, sy=0.5, sz=0.3, wall=0.02) -> TriMesh:
     return merge(parts)
 
 
+def surface_support(mesh: TriMesh, pose, mode: int = A.SB_SURFACE_ON, k: int = 0) -> Support:
+    """The k-th largest support surface of `mesh` placed at `pose`
+    (extract_support_surfaces, surface.cpp:145-153) as a polygon Support."""
+    polygon, frame = _PRIMS["extract_support_surfaces"](mesh, mode)[k]
+    return Support(np.asarray(pose) @ np.asarray(frame), polygon=np.asarray(polygon))
+
+
 def kitchen(n_instances=65536, n_objects=50, attempts=256, config_seed=23) -> Scene:
-    """C3: counter + table + the interior floor of an open container ("inside");
-    boxes, cylinders and sphere sets; every 7th object is next-to the previous object on
-    its support."""
+    """C3: counter + table + the floor of an open container, all three supports extracted
+    from the fixed meshes (extract_support_surfaces, mode `on`: the bin is open to the sky,
+    so its floor is not roofed); boxes, cylinders and sphere sets; every 7th object is
+    next-to the previous object on its support."""
     rng = Pcg32(config_seed)
-    counter, cpose, csup = _table(2.0, 0.7, 0.9, at=(0.0, 0.0))
-    table, tpose, tsup = _table(1.2, 1.2, 0.75, at=(0.0, 1.6))
+    counter, cpose, _ = _table(2.0, 0.7, 0.9, at=(0.0, 0.0))
+    table, tpose, _ = _table(1.2, 1.2, 0.75, at=(0.0, 1.6))
     bin_mesh = open_container()
     bin_pose = translation(-1.8, 0.0, 0.0)
-    wall = 0.02
-    bsup = Support(translation(-1.8, 0.0, wall), (-0.28, -0.23, 0.28, 0.23))
+    csup = surface_support(counter, cpose)
+    tsup = surface_support(table, tpose)
+    bsup = surface_support(bin_mesh, bin_pose)  # the floor slab's top (largest area)
     meshes = [counter, table, bin_mesh]
     fixed = [Fixed(0, cpose), Fixed(1, tpose), Fixed(2, bin_pose)]
     supports = [csup, tsup, bsup]

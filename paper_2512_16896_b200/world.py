@@ -254,6 +254,45 @@ class Support:
     polygon: Optional[np.ndarray] = None
 
 
+@dataclass
+class SupportSurface:
+    """SupportSurface (surface.hpp:15-20): polygon in the z = 0 plane of `frame` (the
+    mesh frame translated to the cluster's top), roof flag and area."""
+    polygon: np.ndarray  # (k, 2)
+    frame: np.ndarray    # (4, 4)
+    roofed: bool
+    area: float
+
+    def support(self, object_pose=None) -> "Support":
+        """A Support on this surface of a mesh placed at object_pose (default identity)."""
+        pose = self.frame if object_pose is None else np.asarray(object_pose) @ self.frame
+        return Support(pose, polygon=self.polygon.copy())
+
+
+def _surfaces_from(arr, n) -> List["SupportSurface"]:
+    out = []
+    for k in range(n):
+        s = arr[k]
+        poly = np.array(s.polygon_xy[: 2 * s.n_polygon]).reshape(-1, 2)
+        out.append(SupportSurface(poly, from_colmajor(np.array(s.frame)), bool(s.roofed), s.area))
+    return out
+
+
+def extract_support_surfaces(mesh: "TriMesh", mode: int = A.SB_SURFACE_ON) -> List["SupportSurface"]:
+    """extract_support_surfaces / extract_all_support_surfaces (surface.cpp:53-153); mode
+    SB_SURFACE_ON, SB_SURFACE_INSIDE or SB_SURFACE_ALL."""
+    cap = 64
+    while True:
+        arr = (A.sb_surface * cap)()
+        n = C.c_uint32()
+        A.check(A.lib().sb_extract_support_surfaces(_dp(mesh.vertices), len(mesh.vertices),
+                                                    _up(mesh.triangles), len(mesh.triangles),
+                                                    mode, arr, cap, C.byref(n)))
+        if n.value <= cap:
+            return _surfaces_from(arr, n.value)
+        cap = n.value
+
+
 def support_to_c(s: "Support", keep: list) -> "A.sb_support":
     """sb_support of a Support (keep: keepalive list for the arrays it points to)."""
     out = A.sb_support()
