@@ -176,7 +176,8 @@ __device__ __forceinline__ void lap(const PlaceParams& p, Fixed& F, int slot) {
 // (placeable = 0: a failed attempt).
 __device__ __forceinline__ bool compose_candidate(const PlaceParams& p, const Sampling& S,
                                                   uint64_t seed, uint64_t state0, uint32_t inst,
-                                                  int32_t at, uint64_t draw, M34& pose) {
+                                                  int32_t at, uint64_t draw, M34& pose,
+                                                  double* rec = nullptr) {
   const WorldView& w = p.w;
   const SbPlacementDev& pl = p.pl;
   const uint64_t gid = p.global_begin + inst;
@@ -236,7 +237,42 @@ __device__ __forceinline__ bool compose_candidate(const PlaceParams& p, const Sa
   Rz.m[4] = s;
   Rz.m[5] = c;
   mul34(Tr, Rz, pose);
+  if (rec) {
+    rec[0] = Tr.m[3];
+    rec[1] = Tr.m[7];
+    rec[2] = Tr.m[11];
+    rec[3] = c;
+    rec[4] = s;
+    rec[5] = 0.0;
+  }
   return true;
+}
+
+// The candidate pose from its compact record {tx, ty, tz, cos, sin, 0} (48 B, what
+// compose_candidate wrote): translation * rotation_z rebuilt and multiplied with the same
+// operations, so the result is bit-identical to compose_candidate's pose.
+__device__ __forceinline__ void pose_from_rec(const double* rec, M34& pose) {
+  M34 Tr, Rz;
+#pragma unroll
+  for (int k = 0; k < 12; ++k) Tr.m[k] = Rz.m[k] = 0.0;
+  Tr.m[0] = Tr.m[5] = Tr.m[10] = 1.0;
+  Rz.m[10] = 1.0;
+  Tr.m[3] = rec[0];
+  Tr.m[7] = rec[1];
+  Tr.m[11] = rec[2];
+  Rz.m[0] = rec[3];
+  Rz.m[1] = -rec[4];
+  Rz.m[4] = rec[4];
+  Rz.m[5] = rec[3];
+  mul34(Tr, Rz, pose);
+}
+__device__ __forceinline__ void load_rec(const double* g, double rec[6]) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double2 v = __ldcg(reinterpret_cast<const double2*>(g) + k);
+    rec[2 * k] = v.x;
+    rec[2 * k + 1] = v.y;
+  }
 }
 
 // Fused placement_filter (reachability.cpp:164-190): the candidate frame's origin in the
@@ -292,17 +328,31 @@ __device__ __forceinline__ void accept_candidate(const PlaceParams& p, uint32_t 
 // are computed with the very operations warp_collide uses, so "no leaf pair's boxes
 // overlap" here is exactly warp_collide returning false at step 2 (a miss). inv / pose:
 // row-major 3x4 (global memory); gr = obj_grec of the object.
+template <bool kCandRec = false>
 __device__ __forceinline__ bool leaf_filter(const WorldView& w, const PlaceGeomCache& gc,
                                             const double* inv, const double* pose, int4 gr) {
   double I[12], P[12];
 #pragma unroll
   for (int k = 0; k < 6; ++k) {
-    const double2 a = __ldcg(reinterpret_cast<const double2*>(inv) + k);
     const double2 b = __ldcg(reinterpret_cast<const double2*>(pose) + k);
-    I[2 * k] = a.x;
-    I[2 * k + 1] = a.y;
     P[2 * k] = b.x;
     P[2 * k + 1] = b.y;
+  }
+  if constexpr (kCandRec) {  // `inv` is the candidate's compact record: pose, then inverse
+    double rec[6];
+    load_rec(inv, rec);
+    M34 C, Ci;
+    pose_from_rec(rec, C);
+    inverse_rigid(C, Ci);
+#pragma unroll
+    for (int k = 0; k < 12; ++k) I[k] = Ci.m[k];
+  } else {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      const double2 a = __ldcg(reinterpret_cast<const double2*>(inv) + k);
+      I[2 * k] = a.x;
+      I[2 * k + 1] = a.y;
+    }
   }
   M34 M;  // warp_collide's other_in_cand, entry by entry (shim order)
 #pragma unroll
@@ -1093,6 +1143,46 @@ __global__ void __launch_bounds__(kB) k_fast_finish(PlaceParams p, int32_t a) {
 // tile * kB + position in the tile's (ascending) list, the tiles of k_fast_init.
 constexpr uint8_t kWideDone = 8;  // accepted in k_wide_sample: no object overlaps its box
 constexpr int kWideChunk = 8;     // narrow pairs a warp claims at a time
+static_assert(kWideRec == 6, "compact candidate record: tx, ty, tz, cos, sin, pad");
+
+// A set of object ids < 32 * kW held in 64-bit registers with explicit members (no
+// dynamically indexed array, which nvcc places in local memory).
+template <int kW>
+struct ObjSet {
+  static constexpr int kQ = (kW + 1) / 2;  // 64-bit quads
+  static_assert(kQ >= 1 && kQ <= 4, "at most 256 objects");
+  unsigned long long q0 = 0, q1 = 0, q2 = 0, q3 = 0;
+  __device__ __forceinline__ unsigned long long& quad(int k) {  // k compile-time after unrolling
+    return k == 0 ? q0 : k == 1 ? q1 : k == 2 ? q2 : q3;
+  }
+  __device__ __forceinline__ unsigned long long quad_c(int k) const {
+    return k == 0 ? q0 : k == 1 ? q1 : k == 2 ? q2 : q3;
+  }
+  __device__ __forceinline__ void or_word(int wd, uint32_t v) {  // wd compile-time
+    quad(wd >> 1) |= (unsigned long long)v << (32 * (wd & 1));
+  }
+  __device__ __forceinline__ uint32_t word(int wd) const {  // wd compile-time
+    return (uint32_t)(quad_c(wd >> 1) >> (32 * (wd & 1)));
+  }
+  __device__ __forceinline__ void set(int ob) {  // ob at run time: branches, no indexing
+    const unsigned long long b = 1ull << (ob & 63);
+    if (kQ == 1 || ob < 64) q0 |= b;
+    else if (kQ == 2 || ob < 128) q1 |= b;
+    else if (kQ == 3 || ob < 192) q2 |= b;
+    else q3 |= b;
+  }
+  __device__ __forceinline__ int pop_lowest() {  // lowest id, removed; -1 when empty
+    if (q0) { const int i = __ffsll(q0) - 1; q0 &= q0 - 1ull; return i; }
+    if (kQ > 1 && q1) { const int i = __ffsll(q1) - 1; q1 &= q1 - 1ull; return 64 + i; }
+    if (kQ > 2 && q2) { const int i = __ffsll(q2) - 1; q2 &= q2 - 1ull; return 128 + i; }
+    if (kQ > 3 && q3) { const int i = __ffsll(q3) - 1; q3 &= q3 - 1ull; return 192 + i; }
+    return -1;
+  }
+  __device__ __forceinline__ int count() const {
+    return __popcll(q0) + (kQ > 1 ? __popcll(q1) : 0) + (kQ > 2 ? __popcll(q2) : 0) +
+           (kQ > 3 ? __popcll(q3) : 0);
+  }
+};
 
 // Exclusive prefix of the round-0 tile counts = each tile's first FIFO draw; resets the
 // pair counters. One block of kWideScanThreads.
@@ -1125,8 +1215,10 @@ __global__ void __launch_bounds__(kWideScanThreads) k_wide_scan(PlaceParams p, i
 // that overlaps no object is free (collision.cpp:439-448 finds nothing) and is accepted
 // here; the others keep their pose / inverse / box / overlap bits in the slot scratch and
 // append one (slot, object) pair per overlap, ascending objects, for k_wide_narrow.
-template <bool kGrid, bool kReach>
+template <bool kGrid, bool kReach, int kW>
 __global__ void __launch_bounds__(kB, SB_WIDE_SAMPLE_MINB) k_wide_sample(PlaceParams p) {
+  static_assert(kW <= kGW && kGW % kW == 0, "enable words");
+  constexpr int kWC = kW < 4 ? kW : 4;  // words of a cell loaded per batch
   const uint32_t t = blockIdx.x;
   const int e = threadIdx.x, lane = e & 31;
   const WorldView& w = p.w;
@@ -1137,16 +1229,15 @@ __global__ void __launch_bounds__(kB, SB_WIDE_SAMPLE_MINB) k_wide_sample(PlacePa
   const Sampling S = resolve_sampling(p);
   const int words = w.n_words;
   Local L;
-  uint32_t ov[kGW];
-#pragma unroll
-  for (int wd = 0; wd < kGW; ++wd) ov[wd] = 0u;
+  ObjSet<kW> ov;
   uint32_t npairs = 0;
   const size_t slot = (size_t)t * kB + e;
   if (e < (int)n) {
     const uint32_t inst = __ldcg(p.tile_list + (uint64_t)t * p.tile_inst + e);
     M34 pose;
+    double rec[6];
     bool placeable = compose_candidate(p, S, seed, state0, inst, 0,
-                                       (uint64_t)__ldcg(p.w_toff + t) + (uint64_t)e, pose);
+                                       (uint64_t)__ldcg(p.w_toff + t) + (uint64_t)e, pose, rec);
     if constexpr (kReach) {
       if (placeable) placeable = reach_ok(p, inst, pose);
     }
@@ -1165,9 +1256,7 @@ __global__ void __launch_bounds__(kB, SB_WIDE_SAMPLE_MINB) k_wide_sample(PlacePa
         }
         xform_aabb(pose, c, h, box, box + 3);
       }
-      uint32_t cand[kGW];
-#pragma unroll
-      for (int wd = 0; wd < kGW; ++wd) cand[wd] = 0u;
+      ObjSet<kW> cand;
       if constexpr (kGrid) {  // OR of the cells the candidate box meets, 4 cells' loads at once
         const SbCellGrid& G = p.grid;
         int cx0, cx1, cy0, cy1;
@@ -1176,39 +1265,38 @@ __global__ void __launch_bounds__(kB, SB_WIDE_SAMPLE_MINB) k_wide_sample(PlacePa
         const uint32_t* cb = G.cells + (uint64_t)inst * (uint64_t)(G.g * G.g) * words;
         for (int c0 = 0; c0 < ncell; c0 += 4)
 #pragma unroll
-          for (int wg = 0; wg < kGW; wg += 4) {  // words [wg, wg + 4) of 4 cells
+          for (int wg = 0; wg < kW; wg += kWC) {  // words [wg, wg + kWC) of 4 cells
             if (wg >= words) break;
-            uint32_t v[4][4];
+            uint32_t v[4][kWC];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               const int ci = c0 + u;
               const int cy = cy0 + ci / nx, cx = cx0 + ci % nx;
               const uint32_t* c = cb + (uint64_t)(cy * G.g + cx) * words + wg;
 #pragma unroll
-              for (int j = 0; j < 4; ++j) v[u][j] = (ci < ncell && wg + j < words) ? __ldcg(c + j) : 0u;
+              for (int j = 0; j < kWC; ++j) v[u][j] = (ci < ncell && wg + j < words) ? __ldcg(c + j) : 0u;
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u)
 #pragma unroll
-              for (int j = 0; j < 4; ++j) cand[wg + j] |= v[u][j];
+              for (int j = 0; j < kWC; ++j) cand.or_word(wg + j, v[u][j]);
           }
       } else {  // every enabled object
 #pragma unroll
-        for (int wd = 0; wd < kGW; ++wd)
-          cand[wd] = wd < words ? __ldcg(w.enabled + sb_word_off(w, wd, inst)) : 0u;
+        for (int wd = 0; wd < kW; ++wd)
+          if (wd < words) cand.or_word(wd, __ldcg(w.enabled + sb_word_off(w, wd, inst)));
       }
-      // AABB tests (aabb.hpp:29-33, margin 0), four box loads in flight
+      // AABB tests (aabb.hpp:29-33, margin 0), four box loads in flight. The next set bit is
+      // found by a select chain over the (unrolled) words, so cand[] / ov[] stay in
+      // registers (no dynamically indexed local arrays).
       {
-        int wd = 0;
-        uint32_t m = cand[0];
         for (;;) {
           int obs[4];
           int k = 0;
-          while (k < 4) {
-            while (!m && wd + 1 < kGW) m = cand[++wd];
-            if (!m) break;
-            obs[k++] = 32 * wd + __ffs(m) - 1;
-            m &= m - 1u;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            obs[u] = cand.pop_lowest();
+            k += obs[u] >= 0;
           }
           if (k == 0) break;
           double2 bx[4][3];
@@ -1227,34 +1315,31 @@ __global__ void __launch_bounds__(kB, SB_WIDE_SAMPLE_MINB) k_wide_sample(PlacePa
               const double2 a0 = bx[u][0], a1 = bx[u][1], a2 = bx[u][2];
               if (box[0] <= a1.y && a0.x <= box[3] && box[1] <= a2.x && a0.y <= box[4] &&
                   box[2] <= a2.y && a1.x <= box[5])
-                ov[obs[u] >> 5] |= 1u << (obs[u] & 31);
+                ov.set(obs[u]);
             }
           if (k < 4) break;
         }
       }
+      npairs = ov.count();
+      if (npairs == 0) {  // free: accept now (the pose rebuilt from the record, bit-identical)
+        M34 P;
+        pose_from_rec(rec, P);
+        double2 q[6];
 #pragma unroll
-      for (int wd = 0; wd < kGW; ++wd) npairs += __popc(ov[wd]);
-      double2 q[6];
-#pragma unroll
-      for (int k = 0; k < 6; ++k) q[k] = make_double2(pose.m[2 * k], pose.m[2 * k + 1]);
-      if (npairs == 0) {  // free: accept now
+        for (int k = 0; k < 6; ++k) q[k] = make_double2(P.m[2 * k], P.m[2 * k + 1]);
         accept_candidate<kGrid>(p, inst, q, box, 0);
         ++L.accepted;
         flag = kWideDone;
       } else {
-        M34 inv;
-        inverse_rigid(pose, inv);
-        double2* cp = reinterpret_cast<double2*>(p.w_pose + slot * 12);
-        double2* ci = reinterpret_cast<double2*>(p.w_inv + slot * 12);
+        // only the compact record (translation, cos, sin: 48 B) is kept; the pose, its
+        // inverse (k_wide_filter / k_wide_narrow) and the world box (k_wide_accept) are
+        // recomputed from it with the same operations, bit for bit
+        double2* cp = reinterpret_cast<double2*>(p.w_pose + slot * kWideRec);
 #pragma unroll
-        for (int k = 0; k < 6; ++k) {
-          cp[k] = q[k];
-          ci[k] = make_double2(inv.m[2 * k], inv.m[2 * k + 1]);
-        }
-        double2* bx = reinterpret_cast<double2*>(p.w_box + slot * 6);
+        for (int k = 0; k < 3; ++k) cp[k] = make_double2(rec[2 * k], rec[2 * k + 1]);
 #pragma unroll
-        for (int k = 0; k < 3; ++k) bx[k] = make_double2(box[2 * k], box[2 * k + 1]);
-        for (int wd = 0; wd < words; ++wd) p.w_ovm[slot * kGW + wd] = ov[wd];
+        for (int wd = 0; wd < kW; ++wd)
+          if (wd < words) p.w_ovm[slot * kGW + wd] = ov.word(wd);
         p.w_contact[slot] = kFree;
         flag = kSlotChecked;
       }
@@ -1275,14 +1360,8 @@ __global__ void __launch_bounds__(kB, SB_WIDE_SAMPLE_MINB) k_wide_sample(PlacePa
   if (npairs) {
     uint64_t q = base + incl - npairs;
 #pragma unroll
-    for (int wd = 0; wd < kGW; ++wd) {
-      uint32_t m = ov[wd];
-      while (m) {
-        const int ob = 32 * wd + __ffs(m) - 1;
-        m &= m - 1u;
-        p.w_pairs[q++] = ((uint32_t)slot << 8) | (uint32_t)ob;
-      }
-    }
+    for (int ob = ov.pop_lowest(); ob >= 0; ob = ov.pop_lowest())
+      p.w_pairs[q++] = ((uint32_t)slot << 8) | (uint32_t)ob;
   }
   if (threadIdx.x == 0 && n) atomicMax(p.ctrl + kRounds, 1u);  // reference round count
   flush(p, L);
@@ -1312,8 +1391,8 @@ __global__ void __launch_bounds__(kB) k_wide_filter(PlaceParams p) {
       const int32_t ob = (int32_t)(ent & 0xffu);
       if (*((volatile int32_t*)p.w_contact + sl) >= ob) {
         const uint32_t inst = __ldcg(p.tile_list + (uint64_t)(sl / kB) * p.tile_inst + sl % kB);
-        pass = leaf_filter(w, gc, p.w_inv + (size_t)sl * 12, w.pose + sb_pose_off(w, ob, inst),
-                           obj_grec(w, ob));
+        pass = leaf_filter<true>(w, gc, p.w_pose + (size_t)sl * kWideRec, w.pose + sb_pose_off(w, ob, inst),
+                                 obj_grec(w, ob));
       }
     }
     // warp-aggregated append of the survivors (order within the list is free: the narrow
@@ -1346,8 +1425,8 @@ __global__ void __launch_bounds__(kB, SB_WIDE_NARROW_MINB) k_wide_narrow(PlacePa
   auto stage = [&](uint32_t ent, int buf) {
     const uint32_t sl = ent >> 8, ob = ent & 0xffu;
     const uint32_t inst = __ldcg(p.tile_list + (uint64_t)(sl / kB) * p.tile_inst + sl % kB);
-    warp_stage(w, obj_grec(w, (int32_t)ob), (int32_t)ob, inst, p.w_inv + (size_t)sl * 12,
-               stage_buf(wsb, p.max_tris, p.max_nodes, buf));
+    warp_stage(w, obj_grec(w, (int32_t)ob), (int32_t)ob, inst, p.w_pose + (size_t)sl * kWideRec,
+               stage_buf(wsb, p.max_tris, p.max_nodes, buf), 3);  // candidate RECORD at +96
   };
   for (;;) {
     unsigned long long q0 = 0;
@@ -1373,11 +1452,30 @@ __global__ void __launch_bounds__(kB, SB_WIDE_NARROW_MINB) k_wide_narrow(PlacePa
         cp_async_wait<0>();
       }
       __syncwarp();
-      if (!skippable(ent)) {
+      if (__shfl_sync(kFull, (int)!skippable(ent), 0)) {  // one verdict for the whole warp
         const int32_t ob = (int32_t)(ent & 0xffu);
         const int4 gr = obj_grec(w, ob);
-        const bool hit = warp_collide(gc, stage_buf(wsb, p.max_tris, p.max_nodes, cur), gr.z, gr.w,
-                                      ws, L.cnt);
+        unsigned char* st = stage_buf(wsb, p.max_tris, p.max_nodes, cur);
+        {  // the staged record -> the candidate's inverse pose, lane per entry
+          double* R = reinterpret_cast<double*>(st + 96);
+          double v = 0.0;
+          if (lane < 12) {
+            double rec[6];
+#pragma unroll
+            for (int k = 0; k < 6; ++k) rec[k] = R[k];
+            M34 C, Ci;
+            pose_from_rec(rec, C);
+            inverse_rigid(C, Ci);
+            v = Ci.m[0];
+#pragma unroll
+            for (int k = 1; k < 12; ++k)
+              if (lane == k) v = Ci.m[k];
+          }
+          __syncwarp();
+          if (lane < 12) R[lane] = v;
+          __syncwarp();
+        }
+        const bool hit = warp_collide(gc, st, gr.z, gr.w, ws, L.cnt);
         if (hit && lane == 0) atomicMin(p.w_contact + (ent >> 8), ob);
       }
       __syncwarp();
@@ -1420,10 +1518,22 @@ __global__ void __launch_bounds__(kB) k_wide_accept(PlaceParams p) {
       if (c == kFree) {
         double2 q[6];
         double box[6];
+        {  // the candidate's pose and world box, as k_wide_sample computed them
+          double rec[6];
+          load_rec(p.w_pose + slot * kWideRec, rec);
+          M34 pose;
+          pose_from_rec(rec, pose);
 #pragma unroll
-        for (int k = 0; k < 6; ++k) q[k] = __ldcg(reinterpret_cast<const double2*>(p.w_pose + slot * 12) + k);
+          for (int k = 0; k < 6; ++k) q[k] = make_double2(pose.m[2 * k], pose.m[2 * k + 1]);
+          const SbGeom* gA = p.w.geoms + p.pl.geom;
+          double c[3], h[3];
 #pragma unroll
-        for (int k = 0; k < 6; ++k) box[k] = __ldcg(p.w_box + slot * 6 + k);
+          for (int k = 0; k < 3; ++k) {
+            c[k] = __ldg(gA->box_c + k);
+            h[k] = __ldg(gA->box_h + k);
+          }
+          xform_aabb(pose, c, h, box, box + 3);
+        }
         accept_candidate<kGrid>(p, inst, q, box, 0);
         ++L.accepted;
       } else {
@@ -1554,6 +1664,14 @@ void place_fast_round(const PlaceParams& p, int32_t attempt, unsigned grid, size
   check(cudaGetLastError(), "k_fast_round");
 }
 
+template <bool kGrid, bool kReach>
+void launch_wide_sample(const PlaceParams& p, int nw, cudaStream_t st) {
+  if (nw <= 1) k_wide_sample<kGrid, kReach, 1><<<p.ntiles, kB, 0, st>>>(p);
+  else if (nw <= 2) k_wide_sample<kGrid, kReach, 2><<<p.ntiles, kB, 0, st>>>(p);
+  else if (nw <= 4) k_wide_sample<kGrid, kReach, 4><<<p.ntiles, kB, 0, st>>>(p);
+  else k_wide_sample<kGrid, kReach, kGW><<<p.ntiles, kB, 0, st>>>(p);
+}
+
 size_t wide_narrow_smem(int ws_bytes) { return (size_t)kWarps * ws_bytes; }
 
 int place_wide_round0(const PlaceParams& p, unsigned init_grid, size_t init_smem, int num_sms,
@@ -1563,8 +1681,10 @@ int place_wide_round0(const PlaceParams& p, unsigned init_grid, size_t init_smem
   k_wide_scan<<<1, kWideScanThreads, 0, st>>>(p, 0);
   check(cudaGetLastError(), "k_wide_scan");
   const bool g = p.grid.g != 0, r = p.reach_any != nullptr;
-  if (g) r ? k_wide_sample<true, true><<<p.ntiles, kB, 0, st>>>(p) : k_wide_sample<true, false><<<p.ntiles, kB, 0, st>>>(p);
-  else r ? k_wide_sample<false, true><<<p.ntiles, kB, 0, st>>>(p) : k_wide_sample<false, false><<<p.ntiles, kB, 0, st>>>(p);
+  // register footprint sized by the enable words in use (cand / ov stay in registers)
+  const int nw = p.w.n_words;
+  if (g) r ? launch_wide_sample<true, true>(p, nw, st) : launch_wide_sample<true, false>(p, nw, st);
+  else r ? launch_wide_sample<false, true>(p, nw, st) : launch_wide_sample<false, false>(p, nw, st);
   check(cudaGetLastError(), "k_wide_sample");
   {
     int per = 0;

@@ -107,9 +107,8 @@ struct PlaceParams {
   // start_round = 1 from the survivors k_wide_accept left in tile_cnt buffer 1.
   int32_t start_round;
   const unsigned long long* start_draws;  // draws of the rounds before start_round
-  double* w_pose;                // [ntiles * kPlaceBlock][12] candidate pose per round-0 slot
-  double* w_inv;                 // [..][12] its inverse (narrow staging)
-  double* w_box;                 // [..][6]  its world AABB
+  double* w_pose;                // [ntiles * kPlaceBlock][kWideRec] compact candidate record
+                                 // per round-0 slot: tx, ty, tz, cos, sin, 0
   int32_t* w_contact;            // [..] lowest colliding object, INT32_MAX = free
   uint32_t* w_ovm;               // [..][8]  broad-phase overlap bits
   uint8_t* w_flag;               // [..]     slot state
@@ -127,6 +126,7 @@ struct PlaceParams {
 #endif
 constexpr int kPlaceBlock = SB_PLACE_BLOCK;  // threads per placement CTA = max tile slots
 constexpr int kPlaceMaxOwnedTiles = 64;  // tiles per CTA on the fast path
+constexpr int kWideRec = 6;  // doubles per round-0 candidate record (w_pose)
 
 // Dynamic shared memory of one placement CTA for a world with `n_words` enable words.
 size_t place_smem_bytes(int n_words, int ws_bytes, int n_objects);

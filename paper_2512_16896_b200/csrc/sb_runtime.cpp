@@ -418,7 +418,7 @@ struct sb_engine {
   DevArray<uint32_t> d_tile_cnt;    // [2][ntiles]
   // wide round 0 (sbk::place_wide_round0) scratch, per round-0 slot (tile * kPlaceBlock + e)
   bool use_wide = false;
-  DevArray<double> d_wpose, d_winv, d_wbox;
+  DevArray<double> d_wpose;
   DevArray<int32_t> d_wcontact;
   DevArray<uint32_t> d_wovm, d_wpairs, d_wpairs2, d_wtoff, d_wlist2;
   DevArray<uint32_t> d_wcnt2;
@@ -719,9 +719,7 @@ struct sb_engine {
       if (const char* e = std::getenv("SB_WIDE")) use_wide = world_size == 1 && any_fifo && std::atoi(e) != 0;
       if (use_wide) {
         const size_t slots = static_cast<size_t>(ntiles) * sbk::kPlaceBlock;
-        d_wpose.alloc(slots * 12);
-        d_winv.alloc(slots * 12);
-        d_wbox.alloc(slots * 6);
+        d_wpose.alloc(slots * sbk::kWideRec);
         d_wcontact.alloc(slots);
         d_wovm.alloc(slots * 8);
         d_wflag.alloc(slots);
@@ -1108,8 +1106,6 @@ struct sb_engine {
         if (world_size == 1) {
           if (use_wide && !relation) {  // round 0 grid-wide, then the persistent kernel
             pp.w_pose = d_wpose.p;
-            pp.w_inv = d_winv.p;
-            pp.w_box = d_wbox.p;
             pp.w_contact = d_wcontact.p;
             pp.w_ovm = d_wovm.p;
             pp.w_flag = d_wflag.p;

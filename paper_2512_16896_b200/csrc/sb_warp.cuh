@@ -67,14 +67,16 @@ __host__ __device__ constexpr int stage_bytes(int maxT, int maxN) {
 // group per lane); gr = grec[geometry of ob]; inv = the candidate's inverse pose in global
 // memory (12 doubles, 16-byte aligned) or null when the caller fills dst + 96 itself.
 __device__ __forceinline__ void warp_stage(const WorldView& w, const int4 gr, int32_t ob,
-                                           uint64_t inst, const double* inv, unsigned char* dst) {
+                                           uint64_t inst, const double* inv, unsigned char* dst,
+                                           int inv_chunks = 6) {
   const int lane = threadIdx.x & 31;
   const unsigned char* pose = reinterpret_cast<const unsigned char*>(w.pose + sb_pose_off(w, ob, inst));
   const unsigned char* rec = reinterpret_cast<const unsigned char*>(w.brec) + 16 * (size_t)gr.x;
   for (int c = lane; c < 12 + gr.y; c += 32) {
     if (c < 6) cp_async16_cg(dst + 16 * c, pose + 16 * c);
     else if (c < 12) {
-      if (inv) cp_async16_cg(dst + 16 * c, reinterpret_cast<const unsigned char*>(inv) + 16 * (c - 6));
+      if (inv && c - 6 < inv_chunks)
+        cp_async16_cg(dst + 16 * c, reinterpret_cast<const unsigned char*>(inv) + 16 * (c - 6));
     } else cp_async16(dst + 16 * c, rec + 16 * (c - 12));
   }
   cp_async_commit();
