@@ -62,18 +62,41 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed region: NVML every 20 ms in a
+    thread (nvidia-smi -lms 200 as the fallback when pynvml is unavailable)."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, device: int):
+    def __init__(self, device: int, period_s: float = 0.02):
         self.device = device
+        self.period = period_s
         self.proc = None
+        self.nvml = None
         self.lines = []
+        self.samples = []  # (sm_mhz, max_mhz, set of reasons)
+        self._stop = threading.Event()
 
     def start(self):
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            idx = self.device
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            if vis:
+                try:
+                    idx = int(vis.split(",")[self.device])
+                except (ValueError, IndexError):
+                    pass
+            self.nvml = (N, N.nvmlDeviceGetHandleByIndex(idx))
+        except Exception:
+            self.nvml = None
+        if self.nvml is not None:
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
@@ -84,35 +107,56 @@ class ClockSampler:
         except FileNotFoundError:
             self.proc = None
 
+    def _poll(self):
+        N, h = self.nvml
+        bits = {"hw_slowdown": N.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": N.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": N.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": N.nvmlClocksEventReasonSwPowerCap}
+        mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+        while not self._stop.is_set():
+            try:
+                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((float(sm), float(mx), {k for k, b in bits.items() if r & b}))
+            except Exception:
+                pass
+            self._stop.wait(self.period)
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 6:
-                continue
+        self._stop.set()
+        if self.nvml is None and self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
+        if self.nvml is not None:
+            self.t.join(timeout=2)
+            src = "nvml, every 20 ms"
+        else:
+            self.proc.terminate()
             try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[2:6]):
-                if v.lower() in ("active", "1"):
-                    reasons.add(n)
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            src = "nvidia-smi -lms 200"
+            for ln in self.lines:
+                parts = [p.strip() for p in ln.split(",")]
+                if len(parts) < 6:
+                    continue
+                try:
+                    rs = {n for n, v in zip(self.NAMES, parts[2:6]) if v.lower() in ("active", "1")}
+                    self.samples.append((float(parts[0]), float(parts[1]), rs))
+                except ValueError:
+                    continue
+        sm = [a for a, _, _ in self.samples]
+        mx = [b for _, b, _ in self.samples]
+        reasons = set().union(*[r for _, _, r in self.samples]) if self.samples else set()
         return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_min_mhz": min(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": src}
 
 
 def fp64_peak(device: int):
@@ -256,14 +300,16 @@ def run_ours(args, rank, world, local_rank):
     hbm_src = "of measured (MEASURED_PEAKS.json hbm_gbs)" if measured else "of fallback (B200_PROFILING.md)"
     achieved_tf = flops / (k_ms * 1e-3) / 1e12 if k_ms > 0 else 0.0
     achieved_gbs = bytes_ / (k_ms * 1e-3) / 1e9 if k_ms > 0 else 0.0
-    traffic = None  # dram__bytes_read.sum + dram__bytes_write.sum per launch, ncu --set full
-    prof_json = os.path.join(ROOT, "profiles", f"ncu_k_place_{args.config}.json")
+    # dram__bytes_read.sum + dram__bytes_write.sum per launch (= per placement chain) from
+    # the committed ncu capture of one warm generation (tools/gpu_traffic.sh)
+    traffic = None
+    prof_json = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(prof_json):
         traffic = json.load(open(prof_json)).get("dram_bytes_per_launch")
     hbm = {"bound": "hbm", "achieved": round(achieved_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
            "frac": round(achieved_gbs / hbm_peak, 5), "traffic": traffic,
            "peak_source": hbm_src, "algorithmic_bytes_per_launch": round(bytes_ / max(n_launch, 1)),
-           "traffic_source": f"profiles/ncu_k_place_{args.config}.json" if traffic else None}
+           "traffic_source": f"profiles/traffic_{args.config}.json" if traffic else None}
     fp64 = {"bound": "fp64", "achieved": round(achieved_tf, 3), "peak": round(fp64_peak_tf, 3),
             "unit": "TFLOP/s", "frac": round(achieved_tf / fp64_peak_tf, 5) if fp64_peak_tf > 0 else None,
             "peak_source": "measured in this run: DADD rate, tools/fp64_peak.cu (no-FMA build)",
@@ -271,8 +317,15 @@ def run_ours(args, rank, world, local_rank):
     t_hbm = bytes_ / (hbm_peak * 1e9)
     t_fp64 = flops / (fp64_peak_tf * 1e12) if fp64_peak_tf > 0 else 0.0
     primary, secondary = (hbm, fp64) if t_hbm >= t_fp64 else (fp64, hbm)
+    # One "launch" here is one placement's kernel chain on the engine stream, timed by CUDA
+    # events around it: FIFO placements of large batches run round 0 as k_fast_init +
+    # k_wide_scan + k_wide_sample + k_wide_filter + k_wide_narrow + k_wide_accept +
+    # k_wide_scan + k_wide_spread and later rounds in the persistent k_place; other
+    # placements are one k_place (or k_place_instances). Per-kernel shares: the committed
+    # ncu launch list (profiles/).
     for r in (primary, secondary):
-        r.update({"kernel": "k_place (persistent per placement: sample+compose+broad+narrow+accept)",
+        r.update({"kernel": "placement kernel chain (k_wide_* round 0 + persistent k_place; "
+                            "per-kernel shares in profiles/ launch lists)",
                   "kernel_ms_per_step": round(k_ms, 4), "launches_per_step": n_launch,
                   "share_of_step": round(k_ms / ms_step, 4)})
     line = {

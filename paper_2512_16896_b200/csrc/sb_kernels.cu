@@ -1,6 +1,7 @@
 // sm_100a kernels for CollisionWorld maintenance, the world-API check_batch and engine
 // bookkeeping. Build: -gencode arch=compute_100a,code=sm_100a -fmad=false (see sb_dev.cuh
 // for why every FP64 op must round exactly once).
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -192,6 +193,40 @@ __global__ void k_out16_fixup(uint64_t n, const int16_t* accepted, double* out16
 
 // Occupancy grid at generate() start: cells cleared, then the enabled fixed objects
 // (ids < first_obj) inserted from their world boxes. Thread per instance.
+// The occupancy grid of every instance written in one coalesced pass (replaces a memset
+// of the grid + k_cells_insert_fixed): thread per (instance, cell); a cell's words are the
+// bits of the enabled fixed objects (ids < first_obj) whose world box meets the cell, with
+// cell_range's rounding. The fixed objects' boxes of an instance are read by the 32 lanes
+// of its cells at once (broadcast loads).
+__global__ void __launch_bounds__(256) k_cells_init(WorldView w, SbCellGrid G, int32_t first_obj) {
+  const uint64_t cells = (uint64_t)G.g * G.g;
+  const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (k >= w.n * cells) return;
+  const uint64_t i = k / cells;
+  const int c = (int)(k - i * cells), cy = c / G.g, cx = c - cy * G.g;
+  uint32_t word[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // G.words <= 8 (256 objects)
+  for (int32_t o = 0; o < first_obj; ++o) {
+    if (!((__ldg(w.enabled + sb_word_off(w, o >> 5, i)) >> (o & 31)) & 1u)) continue;
+    const double* b = w.box + sb_box_off(w, o, i);
+    double mn[3] = {__ldg(b), __ldg(b + 1), __ldg(b + 2)}, mx[3] = {__ldg(b + 3), __ldg(b + 4), __ldg(b + 5)};
+    int cx0, cx1, cy0, cy1;
+    cell_range(G, mn, mx, cx0, cx1, cy0, cy1);
+    if (cx >= cx0 && cx <= cx1 && cy >= cy0 && cy <= cy1) {
+#pragma unroll
+      for (int wd = 0; wd < 8; ++wd)
+        if ((o >> 5) == wd) word[wd] |= 1u << (o & 31);
+    }
+  }
+  uint32_t* out = G.cells + k * G.words;
+  if (G.words == 4) {
+    *reinterpret_cast<uint4*>(out) = make_uint4(word[0], word[1], word[2], word[3]);
+  } else {
+#pragma unroll
+    for (int wd = 0; wd < 8; ++wd)
+      if (wd < G.words) out[wd] = word[wd];
+  }
+}
+
 __global__ void k_cells_insert_fixed(WorldView w, SbCellGrid G, int32_t first_obj) {
   const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i >= w.n) return;
@@ -434,6 +469,12 @@ void out16_fixup(uint64_t n, const int16_t* accepted, double* out16, sb_stream_t
   check_launch("out16_fixup");
 }
 void cells_reset(const SbWorldView& w, const SbCellGrid& g, int32_t first_obj, sb_stream_t s) {
+  if (g.words <= 8 && std::getenv("SB_CELLS_MEMSET") == nullptr) {
+    const uint64_t total = w.n * (uint64_t)(g.g * g.g);
+    k_cells_init<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(w, g, first_obj);
+    check_launch("cells_init");
+    return;
+  }
   const cudaError_t e = cudaMemsetAsync(g.cells, 0, w.n * (uint64_t)(g.g * g.g) * g.words * sizeof(uint32_t),
                                         reinterpret_cast<cudaStream_t>(s));
   if (e != cudaSuccess) throw std::runtime_error(std::string("cells memset: ") + cudaGetErrorString(e));
