@@ -344,6 +344,18 @@ void sb_engine_destroy(sb_engine* e);
  * placement. Results stay in HBM; `out` (optional) is filled from them afterwards. */
 sb_status sb_engine_generate(sb_engine* e, uint64_t run_seed, sb_result* out,
                              sb_run_stats* stats);
+/* One run driven placement by placement (the per-placement step of the reference's
+ * generation loop, SPEC.md:525-528 / Appendix C: prepare the sampler, K attempts of
+ * sample -> sample_orientations -> check_batch -> accept, on the device as in
+ * sb_engine_generate). first == 0 starts a run (the world's placed objects, counters and
+ * grid are reset); a later call continues the open run at placement `first` == the end of
+ * the previous call, with the same run_seed (else SB_ERR_LOGIC). Between calls the caller
+ * may read or use the world (sb_engine_world: sb_object_pose, sb_enabled, sb_check_batch).
+ * `out` is accepted only by the call that completes the run (first + count == number of
+ * placements; else SB_ERR_INVALID_ARGUMENT); `stats` are cumulative over the run so far.
+ * Any split of [0, P) gives results bit-identical to one sb_engine_generate call. */
+sb_status sb_engine_place(sb_engine* e, uint64_t run_seed, uint32_t first, uint32_t count,
+                          sb_result* out, sb_run_stats* stats);
 /* Copy the last run's results to host buffers (D2H). */
 sb_status sb_engine_download(sb_engine* e, sb_result* out);
 /* The engine's collision world (for check_batch-level access); owned by the engine. */

@@ -185,6 +185,14 @@ class Engine {
     check(sb_engine_generate(e_, run_seed, out, &st));
     return st;
   }
+  // Placement-stepped run (sb_engine_place): placements [first, first + count) of the run
+  // with run_seed; `out` only on the call that completes it. Stats cumulative.
+  sb_run_stats place(uint64_t run_seed, uint32_t first, uint32_t count = 1,
+                     sb_result* out = nullptr) {
+    sb_run_stats st{};
+    check(sb_engine_place(e_, run_seed, first, count, out, &st));
+    return st;
+  }
   void download(sb_result& out) { check(sb_engine_download(e_, &out)); }
   CollisionWorld world() { return CollisionWorld(sb_engine_world(e_), local_instances()); }
 

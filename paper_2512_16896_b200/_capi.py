@@ -171,6 +171,8 @@ SIGNATURES = {
     "sb_engine_destroy": (None, [_P]),
     "sb_engine_generate": (C.c_int, [_P, C.c_uint64, C.POINTER(sb_result), C.POINTER(sb_run_stats)]),
     "sb_engine_download": (C.c_int, [_P, C.POINTER(sb_result)]),
+    "sb_engine_place": (C.c_int, [_P, C.c_uint64, C.c_uint32, C.c_uint32, C.POINTER(sb_result),
+                                  C.POINTER(sb_run_stats)]),
     "sb_engine_world": (_P, [_P]),
     "sb_engine_local_instances": (C.c_uint64, [_P]),
     "sb_engine_last_launches": (C.c_uint64, [_P]),

@@ -966,10 +966,38 @@ struct sb_engine {
   // Results requested with the call (sb_engine_generate with an sb_result) are downloaded
   // while later placements compute: placement p's poses are final once its kernel ends, so
   // a copy stream converts them (k_pose_colmajor) and copies them to the host behind an event.
+  // Placement-stepped runs (sb_engine_place): [run_lo, run_hi) of the last call; a run
+  // is open while placements remain; counters that span calls accumulate in run_acc_*.
+  size_t run_lo = 0, run_hi = 0;
+  bool run_open = false;
+  uint64_t run_seed_open = 0;
+  uint64_t run_acc_rounds_host = 0, run_acc_per_inst = 0;
+  std::vector<char> device_rounds_run;
+
   void generate(uint64_t run_seed, sb_run_stats* st, sb_result* out = nullptr) {
+    generate_range(run_seed, 0, places.size(), st, out);
+  }
+
+  // Placements [lo, hi) of a run: lo == 0 starts a run (reset), lo > 0 continues the open
+  // run at its next placement with the same seed; hi == P completes it (fixups, `out`).
+  void generate_range(uint64_t run_seed, size_t lo, size_t hi, sb_run_stats* st,
+                      sb_result* out = nullptr) {
+    const size_t P_all = places.size();
+    if (hi > P_all || lo > hi || (lo == hi && P_all != 0))
+      throw std::invalid_argument("placement range out of bounds");
+    if (lo > 0 && (!run_open || lo != run_hi || run_seed != run_seed_open))
+      throw std::logic_error("sb_engine_place: continue the open run at its next placement with its seed");
+    if (out && hi != P_all)
+      throw std::invalid_argument("sb_engine_place: results are available when the run completes");
+    const bool full = lo == 0 && hi == P_all;
+    if (lo == 0) run_acc_rounds_host = run_acc_per_inst = 0;
+    run_lo = lo;
+    run_hi = hi;
+    run_open = hi < P_all;
+    run_seed_open = run_seed;
     const auto th0 = std::chrono::steady_clock::now();
     world->activate();
-    const bool pipe = out && out->poses && !places.empty();
+    const bool pipe = full && out && out->poses && !places.empty();
     if (pipe) {
       if (!copy_stream)
         cuda_check(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -1001,24 +1029,28 @@ struct sb_engine {
                  "event");
     };
     h_seed.ensure(1);
-    h_seed.p[0] = run_seed;
     d_seed.ensure(1);
-    cuda_check(cudaMemcpyAsync(d_seed.p, h_seed.p, 8, cudaMemcpyHostToDevice, stream), "H2D seed");
+    if (lo == 0) {
+      h_seed.p[0] = run_seed;
+      cuda_check(cudaMemcpyAsync(d_seed.p, h_seed.p, 8, cudaMemcpyHostToDevice, stream), "H2D seed");
+    }
     auto enqueue = [&](bool capturing) {
       rec(ev_start, capturing);
-      cuda_check(cudaMemsetAsync(d_counters.p, 0, 8 * sizeof(unsigned long long), stream), "memset");
-      cuda_check(cudaMemsetAsync(d_prof.p, 0, 8 * sizeof(uint64_t), stream), "memset");
-      if (round_debug) cuda_check(cudaMemsetAsync(d_dbg.p, 0, d_dbg.count * sizeof(unsigned), stream), "memset");
-      cuda_check(cudaMemsetAsync(d_ctrl.p, 0, d_ctrl.count * sizeof(uint32_t), stream), "memset");
-      cuda_check(cudaMemsetAsync(d_rflags.p, 0, d_rflags.count * sizeof(int32_t), stream), "memset");
-      sbk::engine_reset(wv, first_place_obj, static_cast<int32_t>(P), d_valid.p, d_accepted.p,
-                        static_cast<int32_t>(P), s);
-      launches += 1;
-      if (cell_grid.g) {
-        sbk::cells_reset(wv, cell_grid, first_place_obj, s);
-        ++launches;
+      if (lo == 0) {  // a new run: reset the world's placed objects, counters, grid
+        cuda_check(cudaMemsetAsync(d_counters.p, 0, 8 * sizeof(unsigned long long), stream), "memset");
+        cuda_check(cudaMemsetAsync(d_prof.p, 0, 8 * sizeof(uint64_t), stream), "memset");
+        if (round_debug) cuda_check(cudaMemsetAsync(d_dbg.p, 0, d_dbg.count * sizeof(unsigned), stream), "memset");
+        cuda_check(cudaMemsetAsync(d_ctrl.p, 0, d_ctrl.count * sizeof(uint32_t), stream), "memset");
+        cuda_check(cudaMemsetAsync(d_rflags.p, 0, d_rflags.count * sizeof(int32_t), stream), "memset");
+        sbk::engine_reset(wv, first_place_obj, static_cast<int32_t>(P), d_valid.p, d_accepted.p,
+                          static_cast<int32_t>(P), s);
+        launches += 1;
+        if (cell_grid.g) {
+          sbk::cells_reset(wv, cell_grid, first_place_obj, s);
+          ++launches;
+        }
       }
-      for (size_t p = 0; p < P; ++p) {
+      for (size_t p = lo; p < hi; ++p) {
         Placement& pl = places[p];
         bool fast = true;
         int canon_n = pl.canon_n;
@@ -1259,11 +1291,12 @@ struct sb_engine {
                      "D2H poses");
         }
       }
-      // objects left unaccepted keep add_object's identity pose / local box
-      sbk::unaccepted_fixup(wv, first_place_obj, static_cast<int32_t>(P), d_accepted.p, s);
-      ++launches;
+      if (hi == P) {  // objects left unaccepted keep add_object's identity pose / local box
+        sbk::unaccepted_fixup(wv, first_place_obj, static_cast<int32_t>(P), d_accepted.p, s);
+        ++launches;
+      }
     };
-    const bool graphable = world_size == 1 && !round_debug && !place_times && use_graphs;
+    const bool graphable = full && world_size == 1 && !round_debug && !place_times && use_graphs;
     if (graphable) {
       GraphSlot& gs = graphs[pipe ? 1 : 0];
       const SbWorldView now = world->view();
@@ -1305,12 +1338,21 @@ struct sb_engine {
       enqueue(false);
     }
     if (out) {
+      if (out->poses && !pipe && P) {  // a stepped run's last call: poses from the world
+        d_pose16.ensure(16 * n);
+        for (size_t p = 0; p < P; ++p) {
+          sbk::download_poses(world->view(), places[p].dev.object, d_pose16.p, s);
+          ++launches;
+          cuda_check(cudaMemcpyAsync(out->poses + 16 * n * p, d_pose16.p, 16 * n * sizeof(double),
+                                     cudaMemcpyDeviceToHost, stream), "D2H poses");
+        }
+      }
       if (out->accepted && P)
         cuda_check(cudaMemcpyAsync(out->accepted, d_accepted.p, P * n * sizeof(int16_t), cudaMemcpyDeviceToHost, stream), "D2H accepted");
       if (out->valid)
         cuda_check(cudaMemcpyAsync(out->valid, d_valid.p, n, cudaMemcpyDeviceToHost, stream), "D2H valid");
     }
-    cuda_check(cudaEventRecord(ev_place[2 * P], stream), "event");
+    cuda_check(cudaEventRecord(ev_place[2 * hi], stream), "event");
     cuda_check(cudaEventRecord(ev_stop, stream), "event");
     // run statistics: small async copies into one pinned block, one synchronisation
     const size_t P1 = std::max<size_t>(1, P);
@@ -1334,7 +1376,7 @@ struct sb_engine {
     const auto th1 = std::chrono::steady_clock::now();
     cuda_check(cudaStreamSynchronize(stream), "sync");
     const auto th2 = std::chrono::steady_clock::now();
-    for (size_t p = 0; p < P; ++p) {
+    for (size_t p = lo; p < hi; ++p) {
       if (rflags[2 * p + 1] != 0)
         throw std::runtime_error("constraint region build failed for placement " + std::to_string(p) +
                                  " (status " + std::to_string(rflags[2 * p + 1]) +
@@ -1343,15 +1385,18 @@ struct sb_engine {
     // CUDA-event timings are resolved lazily (resolve_timing: ~2.5 us per
     // cudaEventElapsedTime, 2 per placement) -- only phase_profile / last_timing need them.
     pending_per_inst.assign(P, 0);
-    for (size_t p = 0; p < P; ++p)
+    for (size_t p = lo; p < hi; ++p)
       pending_per_inst[p] = places[p].dev.anchor_object >= 0 && rflags[2 * p] != 0;
     pending_rounds.assign(P, 0);
-    for (size_t p = 0; p < P; ++p) pending_rounds[p] = device_rounds[p] ? ctrl_all[8 * p + 2] : 0u;
+    for (size_t p = lo; p < hi; ++p) pending_rounds[p] = device_rounds[p] ? ctrl_all[8 * p + 2] : 0u;
     timing_pending = true;
     const auto th2a = std::chrono::steady_clock::now();
-    uint64_t rounds = rounds_host;
-    for (size_t p = 0; p < P; ++p)
-      if (device_rounds[p]) rounds += ctrl_all[8 * p + 2];
+    if (lo == 0) device_rounds_run.assign(P, 0);
+    for (size_t p = lo; p < hi; ++p) device_rounds_run[p] = device_rounds[p];
+    run_acc_rounds_host += rounds_host;
+    uint64_t rounds = run_acc_rounds_host;  // the run so far (placements [0, hi))
+    for (size_t p = 0; p < hi; ++p)
+      if (device_rounds_run[p]) rounds += ctrl_all[8 * p + 2];
     last_check_launches = round_launches;
     last_launches = launches;
     for (int k = 0; k < 7; ++k) last_prof[k] = prof[k] * 1e-6;
@@ -1387,8 +1432,9 @@ struct sb_engine {
       st->candidates_sampled = c[3];
       st->rounds = rounds;
       uint64_t per_inst_dev = 0;  // sharded relation placements decided on the device
-      for (size_t p = 0; p < P; ++p) per_inst_dev += shard_dev_relation[p] && rflags[2 * p] != 0;
-      st->per_instance_placements = c[7] + per_inst_host + per_inst_dev;
+      for (size_t p = lo; p < hi; ++p) per_inst_dev += shard_dev_relation[p] && rflags[2 * p] != 0;
+      run_acc_per_inst += per_inst_host + per_inst_dev;
+      st->per_instance_placements = c[7] + run_acc_per_inst;
       st->broad_phase_tests = c[4];
       st->node_pair_tests = c[5];
       st->accepted_candidates = c[6];
@@ -1414,7 +1460,7 @@ struct sb_engine {
     float total_ms = 0.f;
     cuda_check(cudaEventElapsedTime(&total_ms, ev_start, ev_stop), "elapsed");
     double regions_ms = 0.0, place_ms = 0.0, inst_ms = 0.0, fast_ms = 0.0;
-    for (size_t p = 0; p < P; ++p) {
+    for (size_t p = run_lo; p < run_hi && p < P; ++p) {
       float a = 0.f, b = 0.f;
       cuda_check(cudaEventElapsedTime(&a, ev_place[2 * p], ev_place[2 * p + 1]), "elapsed");
       cuda_check(cudaEventElapsedTime(&b, ev_place[2 * p + 1], ev_place[2 * p + 2]), "elapsed");
@@ -1778,6 +1824,12 @@ void sb_engine_destroy(sb_engine* e) { delete e; }
 sb_status sb_engine_generate(sb_engine* e, uint64_t run_seed, sb_result* out, sb_run_stats* st) {
   return guard([&] {
     e->generate(run_seed, st, out);  // results (if requested) are downloaded by generate
+  });
+}
+sb_status sb_engine_place(sb_engine* e, uint64_t run_seed, uint32_t first, uint32_t count,
+                          sb_result* out, sb_run_stats* st) {
+  return guard([&] {
+    e->generate_range(run_seed, first, static_cast<size_t>(first) + count, st, out);
   });
 }
 sb_status sb_engine_download(sb_engine* e, sb_result* out) {

@@ -473,6 +473,28 @@ class Engine:
         stats = {k: getattr(st, k) for k, _ in A.sb_run_stats._fields_}
         return GenerationResult(acc, valid, from_colmajor(poses) if with_poses else None, stats)
 
+    def place(self, run_seed: int, first: int, count: int = 1, with_poses: bool = True):
+        """Placements [first, first + count) of a run (sb_engine_place): first == 0 starts
+        the run, later calls continue it in order with the same seed. Returns the run's
+        cumulative stats, plus the GenerationResult when the call completes the run."""
+        P = len(self.scene.placements)
+        st = A.sb_run_stats()
+        done = first + count == P
+        res, out = None, None
+        if done:
+            acc = np.empty((P, self.n), np.int16)
+            valid = np.empty(self.n, np.uint8)
+            poses = np.empty((P, self.n, 16), np.float64) if with_poses else None
+            res = A.sb_result(acc.ctypes.data_as(C.POINTER(C.c_int16)),
+                              poses.ctypes.data_as(C.POINTER(C.c_double)) if with_poses else None,
+                              valid.ctypes.data_as(C.POINTER(C.c_uint8)))
+        A.check(A.lib().sb_engine_place(self._h, run_seed, first, count,
+                                        C.byref(res) if done else None, C.byref(st)))
+        stats = {k: getattr(st, k) for k, _ in A.sb_run_stats._fields_}
+        if done:
+            out = GenerationResult(acc, valid, from_colmajor(poses) if with_poses else None, stats)
+        return stats, out
+
     def generate_into(self, run_seed: int, res: "A.sb_result") -> dict:
         """generate + D2H into caller-owned (pinned) buffers already wrapped in sb_result."""
         st = A.sb_run_stats()
