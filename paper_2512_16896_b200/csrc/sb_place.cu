@@ -1095,6 +1095,11 @@ __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_fast_round(PlacePar
   __shared__ Fixed F;
   Tile T = carve(g_dsm, p.w.n_words, p.ws_bytes);
   SbGeom gA;
+  if (p.xrecv) {  // rounds enqueued past the placement's last one: return before any setup
+    unsigned long long tot = 0;
+    for (int r = 0; r < p.xworld; ++r) tot += __ldcg(p.xrecv + (size_t)a * p.xworld + r);
+    if (tot == 0) return;
+  }
   block_setup(p, F, T, gA);
   Local L;
   const int32_t canon_n = p.canon_n_dev ? __ldcg(p.canon_n_dev) : p.canon_n;
@@ -1207,6 +1212,7 @@ __global__ void __launch_bounds__(kWideScanThreads) k_wide_scan(PlaceParams p, i
     if (threadIdx.x == 0) p.w_ctl[4] = running;  // round 0's draws (k_place: start_draws)
   } else if (threadIdx.x == 0) {
     p.w_ctl[5] = running;  // round 1's active instances
+    if (p.xcount) p.xcount[1] = running;  // sharded: this rank's count for the exchange
   }
 }
 
@@ -1228,6 +1234,19 @@ __global__ void __launch_bounds__(kB, SB_WIDE_SAMPLE_MINB) k_wide_sample(PlacePa
       p.seed_dev ? Pcg::seeded(stream_seed2(seed, p.pl.salt, kCacheSalt)).state : p.fast_state0;
   const Sampling S = resolve_sampling(p);
   const int words = w.n_words;
+  // sharded (device exchange): round 0's draws start after the lower ranks' instances,
+  // and round 1's draw offset is published as k_fast_round does for its rounds
+  uint64_t draw_base = 0;
+  if (p.xrecv) {
+    unsigned long long tot = 0;
+    for (int r = 0; r < p.xworld; ++r) {
+      const unsigned long long v = __ldcg(p.xrecv + r);
+      tot += v;
+      if (r < p.xrank) draw_base += v;
+    }
+    draw_base += __ldcg(p.xdraws);
+    if (t == 0 && threadIdx.x == 0) p.xdraws[1] = __ldcg(p.xdraws) + (S.n > 0 ? tot : 0ull);
+  }
   Local L;
   ObjSet<kW> ov;
   uint32_t npairs = 0;
@@ -1237,7 +1256,8 @@ __global__ void __launch_bounds__(kB, SB_WIDE_SAMPLE_MINB) k_wide_sample(PlacePa
     M34 pose;
     double rec[6];
     bool placeable = compose_candidate(p, S, seed, state0, inst, 0,
-                                       (uint64_t)__ldcg(p.w_toff + t) + (uint64_t)e, pose, rec);
+                                       draw_base + (uint64_t)__ldcg(p.w_toff + t) + (uint64_t)e,
+                                       pose, rec);
     if constexpr (kReach) {
       if (placeable) placeable = reach_ok(p, inst, pose);
     }
@@ -1675,9 +1695,14 @@ void launch_wide_sample(const PlaceParams& p, int nw, cudaStream_t st) {
 size_t wide_narrow_smem(int ws_bytes) { return (size_t)kWarps * ws_bytes; }
 
 int place_wide_round0(const PlaceParams& p, unsigned init_grid, size_t init_smem, int num_sms,
-                      sb_stream_t s) {
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
+                      sb_stream_t s, unsigned spread_grid) {
   place_fast_init(p, init_grid, init_smem, s);
+  return 1 + place_wide_round0_rest(p, init_grid, num_sms, s, spread_grid, true);
+}
+
+int place_wide_round0_rest(const PlaceParams& p, unsigned init_grid, int num_sms, sb_stream_t s,
+                           unsigned spread_grid, bool spread) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
   k_wide_scan<<<1, kWideScanThreads, 0, st>>>(p, 0);
   check(cudaGetLastError(), "k_wide_scan");
   const bool g = p.grid.g != 0, r = p.reach_any != nullptr;
@@ -1703,11 +1728,13 @@ int place_wide_round0(const PlaceParams& p, unsigned init_grid, size_t init_smem
   check(cudaGetLastError(), "k_wide_accept");
   k_wide_scan<<<1, kWideScanThreads, 0, st>>>(p, 1);
   check(cudaGetLastError(), "k_wide_scan");
-  unsigned spread = init_grid;  // SB_SPREAD=0: pack round 1 into full tiles instead
-  if (const char* e = std::getenv("SB_SPREAD")) spread = std::atoi(e) ? init_grid : 1u;
-  k_wide_spread<<<p.ntiles, kB, 0, st>>>(p, spread);
+  if (!spread) return 6;  // sharded: rounds >= 1 read the compacted tiles in place
+  // round 1's survivors over the persistent kernel's grid (SB_SPREAD=0: full tiles instead)
+  unsigned sg = spread_grid ? spread_grid : init_grid;
+  if (const char* e = std::getenv("SB_SPREAD")) sg = std::atoi(e) ? sg : 1u;
+  k_wide_spread<<<p.ntiles, kB, 0, st>>>(p, sg);
   check(cudaGetLastError(), "k_wide_spread");
-  return 8;
+  return 7;
 }
 
 void place_fast_finish(const PlaceParams& p, int32_t attempt, unsigned grid, sb_stream_t s) {

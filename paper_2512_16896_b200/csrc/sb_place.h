@@ -150,7 +150,13 @@ void place_fast_finish(const PlaceParams& p, int32_t attempt, unsigned grid, sb_
 // k_wide_narrow + k_wide_accept (no grid barrier); the caller then launches
 // place_persistent with p.start_round = 1. Returns the number of launches.
 int place_wide_round0(const PlaceParams& p, unsigned init_grid, size_t init_smem, int num_sms,
-                      sb_stream_t s);
+                      sb_stream_t s, unsigned spread_grid = 0);
+// The same after k_fast_init (sharded runs exchange the round-0 counts in between: the
+// sample kernel takes its draw base from p.xrecv / p.xdraws, the final scan writes the
+// rank's round-1 count into p.xcount[1]); spread = false leaves the survivors compacted in
+// their tiles (tile_cnt buffer 1) for k_fast_round. Returns the number of launches.
+int place_wide_round0_rest(const PlaceParams& p, unsigned init_grid, int num_sms, sb_stream_t s,
+                           unsigned spread_grid, bool spread);
 // Narrow-kernel dynamic shared memory (per-warp scratch) for the given ws_bytes.
 size_t wide_narrow_smem(int ws_bytes);
 // ctrl word receiving the survivor total of round `attempt` (fast path, sharded)

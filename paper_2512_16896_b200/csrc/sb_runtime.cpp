@@ -418,6 +418,7 @@ struct sb_engine {
   DevArray<uint32_t> d_tile_cnt;    // [2][ntiles]
   // wide round 0 (sbk::place_wide_round0) scratch, per round-0 slot (tile * kPlaceBlock + e)
   bool use_wide = false;
+  unsigned wide_pgrid = 0;
   DevArray<double> d_wpose;
   DevArray<int32_t> d_wcontact;
   DevArray<uint32_t> d_wovm, d_wpairs, d_wpairs2, d_wtoff, d_wlist2;
@@ -715,8 +716,16 @@ struct sb_engine {
     {  // wide round 0: single GPU, FIFO placements (no relation), enough instances
       bool any_fifo = false;
       for (const Placement& pl : places) any_fifo = any_fifo || pl.dev.anchor_object < 0;
-      use_wide = world_size == 1 && any_fifo && n >= 131072;  // measured: slower below (C2, C3)
-      if (const char* e = std::getenv("SB_WIDE")) use_wide = world_size == 1 && any_fifo && std::atoi(e) != 0;
+      // single GPU, or sharded with the device-side exchange (round 0's counts gathered
+      // between k_fast_init and the wide kernels); measured slower below 131072 (C2, C3)
+      use_wide = (world_size == 1 || allgather_dev) && any_fifo && n >= 131072;
+      wide_pgrid = grid;  // persistent grid for rounds >= 1 (SB_WIDE_PGRID: fewer CTAs)
+      if (const char* e = std::getenv("SB_WIDE_PGRID"))
+        wide_pgrid = std::max<unsigned>(
+            (ntiles + sbk::kPlaceMaxOwnedTiles - 1) / sbk::kPlaceMaxOwnedTiles,  // owned-tile cap
+            std::min<unsigned>(grid, static_cast<unsigned>(std::max(1, std::atoi(e)))));
+      if (const char* e = std::getenv("SB_WIDE"))
+        use_wide = (world_size == 1 || allgather_dev) && any_fifo && std::atoi(e) != 0;
       if (use_wide) {
         const size_t slots = static_cast<size_t>(ntiles) * sbk::kPlaceBlock;
         d_wpose.alloc(slots * sbk::kWideRec);
@@ -1147,13 +1156,13 @@ struct sb_engine {
             pp.w_ctl = d_wctl.p;
             pp.w_list2 = d_wlist2.p;
             pp.w_cnt2 = d_wcnt2.p;
-            launches += sbk::place_wide_round0(pp, grid, smem, num_sms, s);
+            launches += sbk::place_wide_round0(pp, grid, smem, num_sms, s, wide_pgrid);
             pp.start_round = 1;  // rounds 1.. on the re-dealt survivor list
             pp.start_draws = d_wctl.p + 4;
             pp.tile_list = d_wlist2.p;
             pp.tile_cnt = d_wcnt2.p;
           }
-          if (!sbk::place_persistent(pp, grid, smem, s))
+          if (!sbk::place_persistent(pp, use_wide && !relation ? wide_pgrid : grid, smem, s))
             throw CudaError("cooperative launch of the placement kernel is not possible");
           ++launches;
           ++round_launches;
@@ -1196,11 +1205,27 @@ struct sb_engine {
           sbk::place_fast_init(pp, grid, smem, s);
           ++launches;
           gather(0);
+          int32_t a = 0;
+          if (use_wide && !relation) {
+            // round 0 grid-wide (draw base from the gathered counts), survivors left in
+            // their tiles for the per-round kernels, this rank's count gathered for round 1
+            pp.w_pose = d_wpose.p;
+            pp.w_contact = d_wcontact.p;
+            pp.w_ovm = d_wovm.p;
+            pp.w_flag = d_wflag.p;
+            pp.w_pairs = d_wpairs.p;
+            pp.w_pairs2 = d_wpairs2.p;
+            pp.w_toff = d_wtoff.p;
+            pp.w_ctl = d_wctl.p;
+            launches += sbk::place_wide_round0_rest(pp, grid, num_sms, s, 0, false);
+            ++round_launches;
+            gather(1);
+            a = 1;
+          }
           // The host stays one chunk of rounds ahead of the device: after enqueuing chunk
           // c it reads the gathered total at the end of chunk c-1 (copied behind an event,
           // normally complete by then), so the device never idles on the host; rounds
           // enqueued past the last one with survivors return at once.
-          int32_t a = 0;
           int pending = -1;  // ev_chunk slot whose total is in flight
           int32_t pending_round = 0;
           for (;;) {

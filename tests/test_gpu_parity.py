@@ -348,6 +348,48 @@ def test_sharded_device_exchange_equals_single(gpu, ref, world):
     assert sum(r.stats["rounds"] for r in results) >= whole.stats["rounds"]
 
 
+def _run_shards(pkg, scene, world, seed, device_exchange=True):
+    ag, agd = ThreadAllgather(world), ThreadDevAllgather(world)
+    bounds = [scene.n_instances * r // world for r in range(world + 1)]
+    engines = [pkg.Engine(scene, pkg.Shard(bounds[r], bounds[r + 1], r, world, ag.fn(r),
+                                           agd.fn(r) if device_exchange else None))
+               for r in range(world)]
+    results = [None] * world
+
+    def run(r):
+        results[r] = engines[r].generate(seed)
+
+    ts = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert all(r is not None for r in results)
+    return results
+
+
+@pytest.mark.parametrize("name,world,factory,force", [
+    ("mixed_relations_forced", 2, lambda: scenes.tabletop_mixed(1500, n_objects=10), True),
+    ("mixed_relations_forced", 3, lambda: scenes.tabletop_mixed(1500, n_objects=10), True),
+    ("clutter40_full_size", 2, lambda: scenes.dense_clutter(262144, n_objects=40), False),
+])
+def test_sharded_wide_round0_equals_single(gpu, monkeypatch, name, world, factory, force):
+    """Sharded runs with the device exchange take round 0 grid-wide too (k_wide_* with the
+    draw base from the gathered round-0 counts, survivors left in their tiles for the
+    per-round kernels): bit-identical to the single-GPU run. `force`: SB_WIDE=1 below the
+    131,072-instance threshold (relation placements keep the per-round path)."""
+    pkg = gpu
+    scene = factory()
+    whole = pkg.Engine(scene).generate(6)
+    if force:
+        monkeypatch.setenv("SB_WIDE", "1")
+    results = _run_shards(pkg, scene, world, 6)
+    assert np.array_equal(np.concatenate([r.accepted for r in results], axis=1), whole.accepted)
+    assert np.array_equal(np.concatenate([r.valid for r in results]), whole.valid)
+    assert np.array_equal(np.concatenate([r.poses for r in results], axis=1), whole.poses)
+    assert sum(r.stats["candidate_checks"] for r in results) == whole.stats["candidate_checks"]
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_sharded_generate_equals_single(gpu, ref, world):
     """Variation-batch sharding: G shards with the per-round count exchange
