@@ -1429,11 +1429,24 @@ __global__ void __launch_bounds__(kB) k_wide_filter(PlaceParams p) {
 // Warp per (slot, object) pair over the whole grid: the exact narrow phase (sb_warp.cuh)
 // with the pair's pose + geometry record staged one pair ahead; a pair behind a lower
 // hit of its slot is skipped (the reference stops at the first colliding object).
+// kBulk: pairs staged by cp.async.bulk + an mbarrier per staging buffer (one lane issues
+// three copies) instead of per-lane 16-byte cp.async (default; SB_BULK_STAGE=0 for the
+// cp.async variant; DESIGN 3.3).
+template <bool kBulk>
 __global__ void __launch_bounds__(kB, SB_WIDE_NARROW_MINB) k_wide_narrow(PlaceParams p) {
   __shared__ PlaceGeomCache gc;
+  __shared__ __align__(8) uint64_t bars[kWarps][2];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const WorldView& w = p.w;
   load_geom_cache(w, p.w.geoms[p.pl.geom], gc);
+  if constexpr (kBulk) {
+    if (lane == 0) {
+      mbar_init(&bars[warp][0], 1);
+      mbar_init(&bars[warp][1], 1);
+      mbar_init_fence();
+    }
+  }
+  unsigned phase_bits = 0u;  // bit b: the parity staging buffer b's barrier completes next
   __syncthreads();
   unsigned char* wsb = g_dsm + warp * p.ws_bytes;
   const WarpScratchView ws = carve_scratch(wsb, p.max_tris, p.max_nodes);
@@ -1445,8 +1458,22 @@ __global__ void __launch_bounds__(kB, SB_WIDE_NARROW_MINB) k_wide_narrow(PlacePa
   auto stage = [&](uint32_t ent, int buf) {
     const uint32_t sl = ent >> 8, ob = ent & 0xffu;
     const uint32_t inst = __ldcg(p.tile_list + (uint64_t)(sl / kB) * p.tile_inst + sl % kB);
-    warp_stage(w, obj_grec(w, (int32_t)ob), (int32_t)ob, inst, p.w_pose + (size_t)sl * kWideRec,
-               stage_buf(wsb, p.max_tris, p.max_nodes, buf), 3);  // candidate RECORD at +96
+    if constexpr (kBulk)
+      warp_stage_bulk(w, obj_grec(w, (int32_t)ob), (int32_t)ob, inst, p.w_pose + (size_t)sl * kWideRec,
+                      8u * kWideRec, stage_buf(wsb, p.max_tris, p.max_nodes, buf), &bars[warp][buf]);
+    else
+      warp_stage(w, obj_grec(w, (int32_t)ob), (int32_t)ob, inst, p.w_pose + (size_t)sl * kWideRec,
+                 stage_buf(wsb, p.max_tris, p.max_nodes, buf), 3);  // candidate RECORD at +96
+  };
+  auto wait_stage = [&](int buf, int pending) {  // buffer `buf` staged and visible
+    if constexpr (kBulk) {
+      while (!mbar_try_wait(&bars[warp][buf], (phase_bits >> buf) & 1u)) {
+      }
+      phase_bits ^= 1u << buf;
+    } else {
+      if (pending) cp_async_wait<1>();
+      else cp_async_wait<0>();
+    }
   };
   for (;;) {
     unsigned long long q0 = 0;
@@ -1465,12 +1492,8 @@ __global__ void __launch_bounds__(kB, SB_WIDE_NARROW_MINB) k_wide_narrow(PlacePa
     while (q < q1) {
       const uint32_t ent = __ldcg(p.w_pairs2 + q);
       const uint64_t q2 = next(q + 1);
-      if (q2 < q1) {
-        stage(__ldcg(p.w_pairs2 + q2), cur ^ 1);
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
-      }
+      if (q2 < q1) stage(__ldcg(p.w_pairs2 + q2), cur ^ 1);
+      wait_stage(cur, q2 < q1);
       __syncwarp();
       if (__shfl_sync(kFull, (int)!skippable(ent), 0)) {  // one verdict for the whole warp
         const int32_t ob = (int32_t)(ent & 0xffu);
@@ -1718,10 +1741,17 @@ int place_wide_round0_rest(const PlaceParams& p, unsigned init_grid, int num_sms
     check(cudaGetLastError(), "k_wide_filter");
   }
   const size_t smem = wide_narrow_smem(p.ws_bytes);
-  set_smem((const void*)k_wide_narrow, smem);
+  static const bool bulk = [] {  // measured: C4 37.41 -> 37.28 ms (SB_BULK_STAGE=0: cp.async)
+    const char* e = std::getenv("SB_BULK_STAGE");
+    return !e || std::atoi(e) != 0;
+  }();
+  const void* nfn = bulk ? (const void*)k_wide_narrow<true> : (const void*)k_wide_narrow<false>;
+  set_smem(nfn, smem);
   int per = 0;
-  check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void*)k_wide_narrow, kB, smem), "occupancy");
-  k_wide_narrow<<<(unsigned)(per > 0 ? per : 1) * num_sms, kB, smem, st>>>(p);
+  check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, nfn, kB, smem), "occupancy");
+  const unsigned ngrid = (unsigned)(per > 0 ? per : 1) * num_sms;
+  if (bulk) k_wide_narrow<true><<<ngrid, kB, smem, st>>>(p);
+  else k_wide_narrow<false><<<ngrid, kB, smem, st>>>(p);
   check(cudaGetLastError(), "k_wide_narrow");
   if (g) k_wide_accept<true><<<p.ntiles, kB, 0, st>>>(p);
   else k_wide_accept<false><<<p.ntiles, kB, 0, st>>>(p);

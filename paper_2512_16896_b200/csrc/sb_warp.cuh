@@ -82,6 +82,61 @@ __device__ __forceinline__ void warp_stage(const WorldView& w, const int4 gr, in
   cp_async_commit();
 }
 
+// ---------------------------------------------------------------- bulk-copy staging
+// The same staging with the Blackwell copy engine: one lane arms an mbarrier with the byte
+// count and issues cp.async.bulk (global -> shared, no register or LSU round trip per 16 B;
+// SASS UBLKCP + SYNCS), the warp waits on the barrier's phase.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, unsigned phase) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// generic-proxy writes to shared memory before later async-proxy (bulk) writes to it
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// Lane 0 stages pair (ob, inst) into dst with bulk copies completing on `bar`: the placed
+// pose (96 B), `cand_bytes` of candidate data at +96, the geometry record at +192.
+__device__ __forceinline__ void warp_stage_bulk(const WorldView& w, const int4 gr, int32_t ob,
+                                                uint64_t inst, const double* cand,
+                                                unsigned cand_bytes, unsigned char* dst,
+                                                uint64_t* bar) {
+  if ((threadIdx.x & 31) == 0) {
+    fence_proxy_async_smem();
+    const unsigned rec_bytes = 16u * (unsigned)gr.y;
+    mbar_expect_tx(bar, 96u + cand_bytes + rec_bytes);
+    bulk_g2s(dst, w.pose + sb_pose_off(w, ob, inst), 96u, bar);
+    bulk_g2s(dst + 96, cand, cand_bytes, bar);
+    bulk_g2s(dst + 192, reinterpret_cast<const unsigned char*>(w.brec) + 16 * (size_t)gr.x, rec_bytes, bar);
+  }
+}
+
 // {record offset, record length (16 B units), n_nodes, n_tris} of object ob's geometry.
 __device__ __forceinline__ int4 obj_grec(const WorldView& w, int32_t ob) {
   return __ldg(reinterpret_cast<const int4*>(w.grec) + __ldg(w.obj_geom + ob));
