@@ -496,14 +496,29 @@ __device__ __forceinline__ void cell_range(const SbCellGrid& G, const double* mn
   cy1 = cell_of(mx[1], G.y0, G.inv_y, G.g);
 }
 
-// Set object `obj`'s bit in the cells its world box (min xyz, max xyz) meets.
+// Set object `obj`'s bit in the cells its world box (min xyz, max xyz) meets. The words of
+// up to 8 cells are loaded before any is stored (a plain load -> or -> store per cell
+// would serialise on the possible aliasing; RED atomics measured slower: C4 +14 %).
 __device__ __forceinline__ void cell_insert(const SbCellGrid& G, uint64_t inst, int32_t obj,
                                             const double* mn, const double* mx) {
   int cx0, cx1, cy0, cy1;
   cell_range(G, mn, mx, cx0, cx1, cy0, cy1);
   uint32_t* base = G.cells + inst * (uint64_t)(G.g * G.g) * G.words + (obj >> 5);
-  for (int cy = cy0; cy <= cy1; ++cy)
-    for (int cx = cx0; cx <= cx1; ++cx) base[(uint64_t)(cy * G.g + cx) * G.words] |= 1u << (obj & 31);
+  const uint32_t bit = 1u << (obj & 31);
+  const int nx = cx1 - cx0 + 1, nc = nx * (cy1 - cy0 + 1);
+  for (int c0 = 0; c0 < nc; c0 += 8) {
+    uint32_t v[8];
+    uint32_t* a[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int ci = c0 + u;
+      a[u] = base + (uint64_t)((cy0 + ci / nx) * G.g + cx0 + ci % nx) * G.words;
+      v[u] = ci < nc ? *a[u] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (c0 + u < nc) *a[u] = v[u] | bit;
+  }
 }
 
 // ------------------------------------------------------------------ world view

@@ -11,7 +11,7 @@ from collections import Counter
 obj = sys.argv[1] if len(sys.argv) > 1 else "paper_2512_16896_b200/csrc/build/sb_place.o"
 sass = subprocess.run(["cuobjdump", "-sass", obj], capture_output=True, text=True, check=True).stdout
 KEYS = ["LDGSTS", "UBLKCP", "UTMALDG", "SYNCS", "LDG", "STG", "LDS", "STS", "LDL", "STL",
-        "DADD", "DMUL", "DFMA", "BAR", "ATOMG", "RED", "SHFL"]
+        "DADD", "DMUL", "DFMA", "BAR", "ATOMG", "REDG", "SHFL"]
 funcs = {}
 cur = None
 for line in sass.splitlines():
