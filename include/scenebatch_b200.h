@@ -54,6 +54,12 @@ int sb_device_available(void);
  * ---------------------------------------------------------------------------------- */
 sb_status sb_make_box(double sx, double sy, double sz, double* vertices, uint32_t* n_vertices,
                       uint32_t* triangles, uint32_t* n_triangles);
+/* load_obj (config.hpp:88-90; declared, not defined, by the reference): Wavefront OBJ
+ * subset -- v / f records (f: i, i/j, i//k, i/j/k; negative = relative), polygon faces
+ * fan-triangulated, other records ignored; errors are SB_ERR_RUNTIME with
+ * "path:line: ..." in sb_last_error(). Same size-query convention as sb_make_box. */
+sb_status sb_load_obj(const char* path, double* vertices, uint32_t* n_vertices,
+                      uint32_t* triangles, uint32_t* n_triangles);
 sb_status sb_make_cylinder(double radius, double height, int segments, double* vertices,
                            uint32_t* n_vertices, uint32_t* triangles, uint32_t* n_triangles);
 sb_status sb_make_sphere(double radius, int stacks, int slices, double* vertices,

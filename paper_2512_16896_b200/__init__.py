@@ -10,7 +10,7 @@ from .reach import ChainLink, KinematicChain, ReachMap4D, placement_filter  # no
 from .sampler import PositionSampler, sample_orientations  # noqa: F401
 from .world import (CollisionWorld, Engine, Fixed, GenerationResult, Placement, Relation,  # noqa: F401
                     Scene, Shard, Support, SupportSurface, TriMesh, colmajor,
-                    extract_support_surfaces, from_colmajor, make_box, make_cylinder,
+                    extract_support_surfaces, from_colmajor, load_obj, make_box, make_cylinder,
                     make_sphere, merge, transformed, translation)
 
 

@@ -130,6 +130,7 @@ SIGNATURES = {
     "sb_abi_version": (C.c_int, []),
     "sb_device_available": (C.c_int, []),
     "sb_make_box": (C.c_int, [C.c_double, C.c_double, C.c_double, _D, _U32, _U32, _U32]),
+    "sb_load_obj": (C.c_int, [C.c_char_p, _D, _U32, _U32, _U32]),
     "sb_make_cylinder": (C.c_int, [C.c_double, C.c_double, C.c_int, _D, _U32, _U32, _U32]),
     "sb_make_sphere": (C.c_int, [C.c_double, C.c_int, C.c_int, _D, _U32, _U32, _U32]),
     "sb_transform_vertices": (C.c_int, [_D, _D, C.c_uint32]),

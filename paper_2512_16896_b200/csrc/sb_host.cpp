@@ -1,4 +1,7 @@
 // Host-side geometry preparation. See sb_host.hpp.
+#include <fstream>
+#include <sstream>
+#include <cstdlib>
 #include "sb_host.hpp"
 
 #include <algorithm>
@@ -28,6 +31,69 @@ Mesh make_box(double sx, double sy, double sz) {  // trimesh.cpp:40-53
   m.t = {{0, 2, 1}, {0, 3, 2}, {4, 5, 6}, {4, 6, 7}, {0, 1, 5}, {0, 5, 4},
          {2, 3, 7}, {2, 7, 6}, {1, 2, 6}, {1, 6, 5}, {3, 0, 4}, {3, 4, 7}};
   return m;
+}
+
+// ---------------------------------------------------------------- Wavefront OBJ subset
+Mesh parse_obj(const std::string& text, const std::string& name) {
+  Mesh m;
+  size_t pos = 0;
+  int line_no = 0;
+  auto fail = [&](const std::string& what) {
+    throw std::runtime_error(name + ":" + std::to_string(line_no) + ": " + what);
+  };
+  while (pos <= text.size()) {
+    size_t end = text.find('\n', pos);
+    if (end == std::string::npos) end = text.size();
+    std::string line = text.substr(pos, end - pos);
+    pos = end + 1;
+    ++line_no;
+    if (!line.empty() && line.back() == '\r') line.pop_back();
+    const size_t hash = line.find('#');
+    if (hash != std::string::npos) line.resize(hash);
+    std::istringstream in(line);
+    std::string tag;
+    if (!(in >> tag)) {
+      if (end == text.size()) break;
+      continue;
+    }
+    if (tag == "v") {
+      V3 p{};
+      for (int c = 0; c < 3; ++c) {
+        std::string tok;
+        if (!(in >> tok)) fail("vertex needs 3 coordinates");
+        char* e = nullptr;
+        p[c] = std::strtod(tok.c_str(), &e);
+        if (e == tok.c_str() || *e != '\0' || !std::isfinite(p[c])) fail("bad coordinate '" + tok + "'");
+      }
+      m.v.push_back(p);
+    } else if (tag == "f") {
+      std::vector<uint32_t> idx;
+      std::string tok;
+      while (in >> tok) {
+        const std::string head = tok.substr(0, tok.find('/'));
+        char* e = nullptr;
+        const long long k = std::strtoll(head.c_str(), &e, 10);
+        if (head.empty() || *e != '\0' || k == 0) fail("bad face index '" + tok + "'");
+        const long long nv = static_cast<long long>(m.v.size());
+        const long long i = k > 0 ? k - 1 : nv + k;  // negative: relative to the end
+        if (i < 0 || i >= nv) fail("face index " + std::to_string(k) + " out of range");
+        idx.push_back(static_cast<uint32_t>(i));
+      }
+      if (idx.size() < 3) fail("face needs at least 3 vertices");
+      for (size_t j = 1; j + 1 < idx.size(); ++j) m.t.push_back({idx[0], idx[j], idx[j + 1]});
+    }
+    if (end == text.size()) break;
+  }
+  if (m.t.empty()) throw std::runtime_error(name + ": no faces");
+  return m;
+}
+
+Mesh load_obj(const std::string& path) {
+  std::ifstream f(path, std::ios::binary);
+  if (!f) throw std::runtime_error(path + ": cannot open");
+  std::ostringstream ss;
+  ss << f.rdbuf();
+  return parse_obj(ss.str(), path);
 }
 
 Mesh make_cylinder(double radius, double height, int segments) {  // trimesh.cpp:55-76

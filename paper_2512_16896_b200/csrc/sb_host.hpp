@@ -27,6 +27,12 @@ struct Mesh {
 Mesh make_box(double sx, double sy, double sz);
 Mesh make_cylinder(double radius, double height, int segments);
 Mesh make_sphere(double radius, int stacks, int slices);
+// load_obj (config.hpp:88-90, declared by the reference, defined here): the Wavefront OBJ
+// subset -- `v x y z [w]` and `f a b c ...` records (a = i, i/j, i//k or i/j/k, 1-based,
+// negative = relative to the end), polygon faces fan-triangulated (a, b, c), (a, c, d), ...;
+// every other record ignored. Errors (std::runtime_error) carry "path:line:".
+Mesh load_obj(const std::string& path);
+Mesh parse_obj(const std::string& text, const std::string& name);
 // trimesh.cpp:120-135
 uint64_t mesh_fingerprint(const Mesh& m);
 // trimesh.cpp:16-29 (returns number removed)

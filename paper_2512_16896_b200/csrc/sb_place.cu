@@ -1432,8 +1432,8 @@ __global__ void __launch_bounds__(kB) k_wide_filter(PlaceParams p) {
 // kBulk: pairs staged by cp.async.bulk + an mbarrier per staging buffer (one lane issues
 // three copies) instead of per-lane 16-byte cp.async (default; SB_BULK_STAGE=0 for the
 // cp.async variant; DESIGN 3.3).
-template <bool kBulk>
-__global__ void __launch_bounds__(kB, SB_WIDE_NARROW_MINB) k_wide_narrow(PlaceParams p) {
+template <bool kBulk, int kMinB = SB_WIDE_NARROW_MINB>
+__global__ void __launch_bounds__(kB, kMinB) k_wide_narrow(PlaceParams p) {
   __shared__ PlaceGeomCache gc;
   __shared__ __align__(8) uint64_t bars[kWarps][2];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1745,13 +1745,19 @@ int place_wide_round0_rest(const PlaceParams& p, unsigned init_grid, int num_sms
     const char* e = std::getenv("SB_BULK_STAGE");
     return !e || std::atoi(e) != 0;
   }();
-  const void* nfn = bulk ? (const void*)k_wide_narrow<true> : (const void*)k_wide_narrow<false>;
+  static const int minb = [] {  // experiment: SB_NARROW_MINB=4 (64-register cap)
+    const char* e = std::getenv("SB_NARROW_MINB");
+    return e && std::atoi(e) == 4 ? 4 : SB_WIDE_NARROW_MINB;
+  }();
+  const void* nfn = !bulk ? (const void*)k_wide_narrow<false>
+                    : minb == 4 ? (const void*)k_wide_narrow<true, 4> : (const void*)k_wide_narrow<true>;
   set_smem(nfn, smem);
   int per = 0;
   check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, nfn, kB, smem), "occupancy");
   const unsigned ngrid = (unsigned)(per > 0 ? per : 1) * num_sms;
-  if (bulk) k_wide_narrow<true><<<ngrid, kB, smem, st>>>(p);
-  else k_wide_narrow<false><<<ngrid, kB, smem, st>>>(p);
+  if (!bulk) k_wide_narrow<false><<<ngrid, kB, smem, st>>>(p);
+  else if (minb == 4) k_wide_narrow<true, 4><<<ngrid, kB, smem, st>>>(p);
+  else k_wide_narrow<true><<<ngrid, kB, smem, st>>>(p);
   check(cudaGetLastError(), "k_wide_narrow");
   if (g) k_wide_accept<true><<<p.ntiles, kB, 0, st>>>(p);
   else k_wide_accept<false><<<p.ntiles, kB, 0, st>>>(p);

@@ -1571,6 +1571,12 @@ sb_status sb_make_sphere(double r, int st, int sl, double* v, uint32_t* nv, uint
                          uint32_t* nt) {
   return guard([&] { mesh_out(sbh::make_sphere(r, st, sl), v, nv, t, nt); });
 }
+sb_status sb_load_obj(const char* path, double* v, uint32_t* nv, uint32_t* t, uint32_t* nt) {
+  return guard([&] {
+    if (!path) throw std::invalid_argument("path is NULL");
+    mesh_out(sbh::load_obj(path), v, nv, t, nt);
+  });
+}
 sb_status sb_transform_vertices(const double pose[16], double* v, uint32_t nv) {
   return guard([&] {
     if (!pose || (nv && !v)) throw std::invalid_argument("NULL argument");

@@ -90,6 +90,12 @@ def make_box(sx: float, sy: float, sz: float) -> TriMesh:
     return _make(A.lib().sb_make_box, C.c_double(sx), C.c_double(sy), C.c_double(sz))
 
 
+def load_obj(path: str) -> TriMesh:
+    """config.hpp:88-90 -- Wavefront OBJ subset (v / f, polygon faces fan-triangulated);
+    parse errors raise with "path:line:" in the message."""
+    return _make(A.lib().sb_load_obj, str(path).encode())
+
+
 def make_cylinder(radius: float, height: float, segments: int = 32) -> TriMesh:
     """trimesh.hpp:30 -- capped cylinder along z (4 * segments triangles)."""
     return _make(A.lib().sb_make_cylinder, C.c_double(radius), C.c_double(height),
