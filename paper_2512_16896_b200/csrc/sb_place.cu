@@ -806,8 +806,13 @@ __device__ __forceinline__ void mark_invalid(const PlaceParams& p, const Tile& T
 
 // Fast path: exclusive prefix of the per-tile survivor counts for the CTA's tiles
 // (t = blockIdx.x + k * gridDim.x) into F.prefix / F.cnt; returns the round total.
+// Tiles of the fast path's current lists: all of them, or those k_wide_spread filled.
+__device__ __forceinline__ uint32_t tiles_in_use(const PlaceParams& p) {
+  return p.ntiles_dev ? (uint32_t)__ldcg(p.ntiles_dev) : p.ntiles;
+}
+
 __device__ uint64_t tile_prefix(const PlaceParams& p, const uint32_t* cnt, Fixed& F) {
-  const uint32_t G = gridDim.x, b = blockIdx.x, nt = p.ntiles;
+  const uint32_t G = gridDim.x, b = blockIdx.x, nt = tiles_in_use(p);
   uint64_t running = 0;
   for (uint32_t c0 = 0; c0 < nt; c0 += kB * kPrefixItems) {
     uint32_t x[kPrefixItems], ex[kPrefixItems], agg;
@@ -859,7 +864,8 @@ __device__ uint64_t fast_round(const PlaceParams& p, const Sampling& S, const Sb
   if (total == 0) return 0;
   if (total <= (uint64_t)p.solo_max) return total | kSoloFlag;  // caller runs solo rounds
   uint32_t k = 0, mine = 0;
-  for (uint32_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++k) {
+  const uint32_t ntu = tiles_in_use(p);
+  for (uint32_t t = blockIdx.x; t < ntu; t += gridDim.x, ++k) {
     const uint32_t n = F.cnt[k];
     if (n == 0) {
       if (threadIdx.x == 0) cout[t] = 0;
@@ -886,9 +892,10 @@ __device__ void solo_rounds(const PlaceParams& p, const Sampling& S, const SbGeo
                             Fixed& F, int32_t a, uint64_t draws, Local& L) {
   const uint32_t* cin = p.tile_cnt + (size_t)(a & 1) * p.cnt_stride;
   uint32_t base = 0;
-  for (uint32_t t0 = 0; t0 < p.ntiles; t0 += kB) {
+  const uint32_t ntu = tiles_in_use(p);
+  for (uint32_t t0 = 0; t0 < ntu; t0 += kB) {
     const uint32_t t = t0 + threadIdx.x;
-    const uint32_t c = t < p.ntiles ? __ldcg(cin + t) : 0u;
+    const uint32_t c = t < ntu ? __ldcg(cin + t) : 0u;
     uint32_t off, tot;
     BlockScan(F.scan).ExclusiveSum(c, off, tot);
     const uint32_t* src = p.tile_list + (uint64_t)t * p.tile_inst;
@@ -1023,7 +1030,7 @@ __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_place(PlaceParams p
         F.ta = F.tb = 0;
       }
       uint64_t total = fast_round<kGrid, kReach>(p, S, gA, T, F, a, draws, L, nullptr,
-                                                 p.ntiles <= gridDim.x && a > p.start_round);
+                                                 tiles_in_use(p) <= gridDim.x && a > p.start_round);
       if (total & kSoloFlag) {
         if (blockIdx.x == 0) solo_rounds<kGrid, kReach>(p, S, gA, T, F, a, draws, L);
         a = -1;  // tail done by CTA 0
@@ -1045,7 +1052,8 @@ __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_place(PlaceParams p
     }
     if (a == p.attempts) {  // K attempts exhausted: survivors are invalid
       const uint32_t* cin = p.tile_cnt + (size_t)(a & 1) * p.cnt_stride;
-      for (uint32_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+      const uint32_t ntu = tiles_in_use(p);
+      for (uint32_t t = blockIdx.x; t < ntu; t += gridDim.x) {
         const uint32_t n = __ldcg(cin + t);
         if (n == 0) continue;
         load_list(p, T, t, n);
@@ -1614,6 +1622,7 @@ __global__ void __launch_bounds__(kB) k_wide_spread(PlaceParams p, unsigned grid
     const unsigned long long lo = (unsigned long long)k * q;
     p.w_cnt2[p.cnt_stride + k] = S > lo ? (uint32_t)(S - lo < q ? S - lo : q) : 0u;
   }
+  if (blockIdx.x == 0 && threadIdx.x == 0) p.w_ctl[6] = (S + q - 1) / q;  // tiles in use
 }
 
 void check(cudaError_t e, const char* what) {

@@ -115,8 +115,11 @@ struct PlaceParams {
   uint32_t* w_pairs;             // [<= n * n_objects] (slot << 8 | object)
   uint32_t* w_pairs2;            // [same] the pairs past the leaf-box filter
   uint32_t* w_toff;              // [ntiles] first FIFO draw of each tile
-  unsigned long long* w_ctl;     // [6] pairs appended, -, filtered pairs appended / claimed,
-                                 // round-0 draws, round-1 active instances
+  unsigned long long* w_ctl;     // [7] pairs appended, -, filtered pairs appended / claimed,
+                                 // round-0 draws, round-1 active instances, tiles in use
+  // Tiles holding survivors (k_wide_spread's w_ctl[6]); null = ntiles. The persistent
+  // kernel's rounds >= 1 then scan / own only those (and keep them resident).
+  const unsigned long long* ntiles_dev;
   uint32_t* w_list2;             // [ntiles * tile_inst] round 1's active list, re-dealt
   uint32_t* w_cnt2;              // [2][cnt_stride] its tile counts (buffer 1 = round 1)
 };

@@ -1161,6 +1161,7 @@ struct sb_engine {
             pp.start_draws = d_wctl.p + 4;
             pp.tile_list = d_wlist2.p;
             pp.tile_cnt = d_wcnt2.p;
+            pp.ntiles_dev = d_wctl.p + 6;
           }
           if (!sbk::place_persistent(pp, use_wide && !relation ? wide_pgrid : grid, smem, s))
             throw CudaError("cooperative launch of the placement kernel is not possible");
