@@ -390,6 +390,47 @@ def test_sharded_wide_round0_equals_single(gpu, monkeypatch, name, world, factor
     assert sum(r.stats["candidate_checks"] for r in results) == whole.stats["candidate_checks"]
 
 
+def _run_bounds(pkg, scene, bounds, seed, device_exchange=True):
+    world = len(bounds) - 1
+    ag, agd = ThreadAllgather(world), ThreadDevAllgather(world)
+    engines = [pkg.Engine(scene, pkg.Shard(bounds[r], bounds[r + 1], r, world, ag.fn(r),
+                                           agd.fn(r) if device_exchange else None))
+               for r in range(world)]
+    results = [None] * world
+
+    def run(r):
+        results[r] = engines[r].generate(seed)
+
+    ts = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert all(r is not None for r in results)
+    return results
+
+
+@pytest.mark.parametrize("attempts", [8, 9])
+@pytest.mark.parametrize("wide", [False, True])
+def test_sharded_early_finisher_and_exhausted_shard(gpu, monkeypatch, attempts, wide):
+    """a tiny shard runs out of survivors at some round r0 while the
+    other exhausts all K attempts; with both parities of K - r0 (K = 8, 9) the idle shard's
+    tile counts must not let the final invalidation clear instances it already placed."""
+    pkg = gpu
+    scene = scenes.tabletop_boxes(700, n_objects=40, attempts=attempts)  # ~half end invalid
+    whole = pkg.Engine(scene).generate(3)
+    assert (whole.valid == 0).any(), "the scene must exhaust K for some instances"
+    if wide:
+        monkeypatch.setenv("SB_WIDE", "1")
+        single = pkg.Engine(scene).generate(3)  # single-GPU wide round 0 + persistent rounds
+        assert np.array_equal(single.valid, whole.valid)
+        assert np.array_equal(single.accepted, whole.accepted)
+    for bounds in ([0, 3, 700], [0, 697, 700], [0, 1, 2, 700]):
+        results = _run_bounds(pkg, scene, bounds, 3)
+        assert np.array_equal(np.concatenate([r.valid for r in results]), whole.valid), bounds
+        assert np.array_equal(np.concatenate([r.accepted for r in results], axis=1), whole.accepted), bounds
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_sharded_generate_equals_single(gpu, ref, world):
     """Variation-batch sharding: G shards with the per-round count exchange
