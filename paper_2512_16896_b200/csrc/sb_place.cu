@@ -1155,7 +1155,7 @@ __global__ void __launch_bounds__(kB) k_fast_finish(PlaceParams p, int32_t a) {
 // the survivors from round 1 on (k_place with start_round = 1). Slot of a round-0 entry:
 // tile * kB + position in the tile's (ascending) list, the tiles of k_fast_init.
 constexpr uint8_t kWideDone = 8;  // accepted in k_wide_sample: no object overlaps its box
-constexpr int kWideChunk = 8;     // narrow pairs a warp claims at a time
+constexpr int kWideChunk = 1;  // narrow pairs a warp claims at a time (C4: 1 / 2 / 4 / 8 = 31.0 / 31.2 / 32.5 / 35.6 ms)
 static_assert(kWideRec == 6, "compact candidate record: tx, ty, tz, cos, sin, pad");
 
 // A set of object ids < 32 * kW held in 64-bit registers with explicit members (no
@@ -1412,13 +1412,13 @@ __global__ void __launch_bounds__(kB) k_wide_filter(PlaceParams p) {
   for (uint64_t q0 = (uint64_t)blockIdx.x * kB; q0 < np; q0 += (uint64_t)gridDim.x * kB) {
     const uint64_t q = q0 + threadIdx.x;
     bool pass = false;
-    uint32_t ent = 0;
+    uint32_t ent = 0, inst = 0;
     if (q < np) {
       ent = __ldcg(p.w_pairs + q);
       const uint32_t sl = ent >> 8;
       const int32_t ob = (int32_t)(ent & 0xffu);
       if (*((volatile int32_t*)p.w_contact + sl) >= ob) {
-        const uint32_t inst = __ldcg(p.tile_list + (uint64_t)(sl / kB) * p.tile_inst + sl % kB);
+        inst = __ldcg(p.tile_list + (uint64_t)(sl / kB) * p.tile_inst + sl % kB);
         pass = leaf_filter<true>(w, gc, p.w_pose + (size_t)sl * kWideRec, w.pose + sb_pose_off(w, ob, inst),
                                  obj_grec(w, ob));
       }
@@ -1429,7 +1429,11 @@ __global__ void __launch_bounds__(kB) k_wide_filter(PlaceParams p) {
     unsigned long long base = 0;
     if (lane == 0 && m) base = atomicAdd(p.w_ctl + 2, (unsigned long long)__popc(m));
     base = __shfl_sync(kFull, base, 0);
-    if (pass) p.w_pairs2[base + __popc(m & ((1u << lane) - 1u))] = ent;
+    if (pass) {
+      const unsigned long long k = base + __popc(m & ((1u << lane) - 1u));
+      p.w_pairs2[k] = ent;
+      p.w_pinst2[k] = inst;
+    }
   }
   flush(p, L);
 }
@@ -1441,12 +1445,14 @@ __global__ void __launch_bounds__(kB) k_wide_filter(PlaceParams p) {
 // three copies) instead of per-lane 16-byte cp.async (default; SB_BULK_STAGE=0 for the
 // cp.async variant; DESIGN 3.3).
 template <bool kBulk, int kMinB = SB_WIDE_NARROW_MINB>
-__global__ void __launch_bounds__(kB, kMinB) k_wide_narrow(PlaceParams p) {
+__global__ void __launch_bounds__(kB, kMinB) k_wide_narrow(PlaceParams p, int chunk, int claim_ahead) {
   __shared__ PlaceGeomCache gc;
   __shared__ __align__(8) uint64_t bars[kWarps][2];
+  __shared__ int4 ogeo[kGW * 32];  // obj_grec of every object (no dependent load per pair)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const WorldView& w = p.w;
   load_geom_cache(w, p.w.geoms[p.pl.geom], gc);
+  for (int ob = threadIdx.x; ob < w.n_objects; ob += kB) ogeo[ob] = obj_grec(w, ob);
   if constexpr (kBulk) {
     if (lane == 0) {
       mbar_init(&bars[warp][0], 1);
@@ -1463,14 +1469,14 @@ __global__ void __launch_bounds__(kB, kMinB) k_wide_narrow(PlaceParams p) {
   auto skippable = [&](uint32_t ent) {
     return *((volatile int32_t*)p.w_contact + (ent >> 8)) < (int32_t)(ent & 0xffu);
   };
-  auto stage = [&](uint32_t ent, int buf) {
+  auto stage = [&](uint64_t q, int buf) {  // pair q's records into staging buffer `buf`
+    const uint32_t ent = __ldcg(p.w_pairs2 + q), inst = __ldcg(p.w_pinst2 + q);
     const uint32_t sl = ent >> 8, ob = ent & 0xffu;
-    const uint32_t inst = __ldcg(p.tile_list + (uint64_t)(sl / kB) * p.tile_inst + sl % kB);
     if constexpr (kBulk)
-      warp_stage_bulk(w, obj_grec(w, (int32_t)ob), (int32_t)ob, inst, p.w_pose + (size_t)sl * kWideRec,
+      warp_stage_bulk(w, ogeo[ob], (int32_t)ob, inst, p.w_pose + (size_t)sl * kWideRec,
                       8u * kWideRec, stage_buf(wsb, p.max_tris, p.max_nodes, buf), &bars[warp][buf]);
     else
-      warp_stage(w, obj_grec(w, (int32_t)ob), (int32_t)ob, inst, p.w_pose + (size_t)sl * kWideRec,
+      warp_stage(w, ogeo[ob], (int32_t)ob, inst, p.w_pose + (size_t)sl * kWideRec,
                  stage_buf(wsb, p.max_tris, p.max_nodes, buf), 3);  // candidate RECORD at +96
   };
   auto wait_stage = [&](int buf, int pending) {  // buffer `buf` staged and visible
@@ -1483,56 +1489,64 @@ __global__ void __launch_bounds__(kB, kMinB) k_wide_narrow(PlaceParams p) {
       else cp_async_wait<0>();
     }
   };
-  for (;;) {
-    unsigned long long q0 = 0;
-    if (lane == 0) q0 = atomicAdd(p.w_ctl + 3, (unsigned long long)kWideChunk);
-    q0 = __shfl_sync(kFull, q0, 0);
-    if (q0 >= np) break;
-    const uint64_t q1 = q0 + kWideChunk < np ? q0 + kWideChunk : np;
-    // next non-skippable pair of the chunk at or after q
-    auto next = [&](uint64_t q) {
-      while (q < q1 && skippable(__ldcg(p.w_pairs2 + q))) ++q;
-      return q;
-    };
-    int cur = 0;
-    uint64_t q = next(q0);
-    if (q < q1) stage(__ldcg(p.w_pairs2 + q), cur);
-    while (q < q1) {
-      const uint32_t ent = __ldcg(p.w_pairs2 + q);
-      const uint64_t q2 = next(q + 1);
-      if (q2 < q1) stage(__ldcg(p.w_pairs2 + q2), cur ^ 1);
-      wait_stage(cur, q2 < q1);
-      __syncwarp();
-      if (__shfl_sync(kFull, (int)!skippable(ent), 0)) {  // one verdict for the whole warp
-        const int32_t ob = (int32_t)(ent & 0xffu);
-        const int4 gr = obj_grec(w, ob);
-        unsigned char* st = stage_buf(wsb, p.max_tris, p.max_nodes, cur);
-        {  // the staged record -> the candidate's inverse pose, lane per entry
-          double* R = reinterpret_cast<double*>(st + 96);
-          double v = 0.0;
-          if (lane < 12) {
-            double rec[6];
-#pragma unroll
-            for (int k = 0; k < 6; ++k) rec[k] = R[k];
-            M34 C, Ci;
-            pose_from_rec(rec, C);
-            inverse_rigid(C, Ci);
-            v = Ci.m[0];
-#pragma unroll
-            for (int k = 1; k < 12; ++k)
-              if (lane == k) v = Ci.m[k];
-          }
-          __syncwarp();
-          if (lane < 12) R[lane] = v;
-          __syncwarp();
-        }
-        const bool hit = warp_collide(gc, st, gr.z, gr.w, ws, L.cnt);
-        if (hit && lane == 0) atomicMin(p.w_contact + (ent >> 8), ob);
-      }
-      __syncwarp();
-      q = q2;
-      cur ^= 1;
+  // One continuous stream of pairs per warp: chunks of kWideChunk claimed dynamically, the
+  // next chunk claimed one chunk ahead (lane 0's atomic is only waited for at the chunk
+  // boundary), so staging stays one pair ahead across chunk boundaries.
+  constexpr uint64_t kEnd = ~0ull;
+  const unsigned long long ck = (unsigned long long)chunk;
+  unsigned long long ahead = 0;  // lane 0: start of the chunk claimed ahead (in flight)
+  if (lane == 0 && claim_ahead) ahead = atomicAdd(p.w_ctl + 3, ck);
+  uint64_t qe = 0;  // end of the current chunk
+  auto advance = [&](uint64_t q) -> uint64_t {  // next non-skippable pair at or after q
+    for (;;) {
+      while (q < qe && skippable(__ldcg(p.w_pairs2 + q))) ++q;
+      if (q < qe) return q;
+      if (lane == 0 && !claim_ahead) ahead = atomicAdd(p.w_ctl + 3, ck);
+      const unsigned long long c = __shfl_sync(kFull, ahead, 0);
+      if (c >= np) return kEnd;
+      if (lane == 0 && claim_ahead) ahead = atomicAdd(p.w_ctl + 3, ck);
+      q = c;
+      qe = c + ck < np ? c + ck : np;
     }
+  };
+  int cur = 0;
+  uint64_t q = advance(0);
+  if (q != kEnd) stage(q, cur);
+  while (q != kEnd) {
+    const uint32_t ent = __ldcg(p.w_pairs2 + q);
+    const uint64_t q2 = advance(q + 1);
+    if (q2 != kEnd) stage(q2, cur ^ 1);
+    wait_stage(cur, q2 != kEnd);
+    __syncwarp();
+    if (__shfl_sync(kFull, (int)!skippable(ent), 0)) {  // one verdict for the whole warp
+      const int32_t ob = (int32_t)(ent & 0xffu);
+      const int4 gr = ogeo[ob];
+      unsigned char* st = stage_buf(wsb, p.max_tris, p.max_nodes, cur);
+      {  // the staged record -> the candidate's inverse pose, lane per entry
+        double* R = reinterpret_cast<double*>(st + 96);
+        double v = 0.0;
+        if (lane < 12) {
+          double rec[6];
+#pragma unroll
+          for (int k = 0; k < 6; ++k) rec[k] = R[k];
+          M34 C, Ci;
+          pose_from_rec(rec, C);
+          inverse_rigid(C, Ci);
+          v = Ci.m[0];
+#pragma unroll
+          for (int k = 1; k < 12; ++k)
+            if (lane == k) v = Ci.m[k];
+        }
+        __syncwarp();
+        if (lane < 12) R[lane] = v;
+        __syncwarp();
+      }
+      const bool hit = warp_collide(gc, st, gr.z, gr.w, ws, L.cnt);
+      if (hit && lane == 0) atomicMin(p.w_contact + (ent >> 8), ob);
+    }
+    __syncwarp();
+    q = q2;
+    cur ^= 1;
   }
   flush(p, L);
 }
@@ -1764,9 +1778,17 @@ int place_wide_round0_rest(const PlaceParams& p, unsigned init_grid, int num_sms
   int per = 0;
   check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, nfn, kB, smem), "occupancy");
   const unsigned ngrid = (unsigned)(per > 0 ? per : 1) * num_sms;
-  if (!bulk) k_wide_narrow<false><<<ngrid, kB, smem, st>>>(p);
-  else if (minb == 4) k_wide_narrow<true, 4><<<ngrid, kB, smem, st>>>(p);
-  else k_wide_narrow<true><<<ngrid, kB, smem, st>>>(p);
+  static const int chunk = [] {  // pairs a warp claims at a time (SB_NARROW_CHUNK)
+    const char* e = std::getenv("SB_NARROW_CHUNK");
+    return e && std::atoi(e) > 0 ? std::atoi(e) : kWideChunk;
+  }();
+  static const int ahead = [] {  // claim the next chunk one chunk ahead (SB_NARROW_AHEAD)
+    const char* e = std::getenv("SB_NARROW_AHEAD");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (!bulk) k_wide_narrow<false><<<ngrid, kB, smem, st>>>(p, chunk, ahead);
+  else if (minb == 4) k_wide_narrow<true, 4><<<ngrid, kB, smem, st>>>(p, chunk, ahead);
+  else k_wide_narrow<true><<<ngrid, kB, smem, st>>>(p, chunk, ahead);
   check(cudaGetLastError(), "k_wide_narrow");
   if (g) k_wide_accept<true><<<p.ntiles, kB, 0, st>>>(p);
   else k_wide_accept<false><<<p.ntiles, kB, 0, st>>>(p);

@@ -114,6 +114,7 @@ struct PlaceParams {
   uint8_t* w_flag;               // [..]     slot state
   uint32_t* w_pairs;             // [<= n * n_objects] (slot << 8 | object)
   uint32_t* w_pairs2;            // [same] the pairs past the leaf-box filter
+  uint32_t* w_pinst2;            // [same] their instance ids (no tile-list lookup to stage)
   uint32_t* w_toff;              // [ntiles] first FIFO draw of each tile
   unsigned long long* w_ctl;     // [7] pairs appended, -, filtered pairs appended / claimed,
                                  // round-0 draws, round-1 active instances, tiles in use

@@ -421,7 +421,7 @@ struct sb_engine {
   unsigned wide_pgrid = 0;
   DevArray<double> d_wpose;
   DevArray<int32_t> d_wcontact;
-  DevArray<uint32_t> d_wovm, d_wpairs, d_wpairs2, d_wtoff, d_wlist2;
+  DevArray<uint32_t> d_wovm, d_wpairs, d_wpairs2, d_wpinst2, d_wtoff, d_wlist2;
   DevArray<uint32_t> d_wcnt2;
   DevArray<uint8_t> d_wflag;
   DevArray<unsigned long long> d_wctl;
@@ -734,6 +734,7 @@ struct sb_engine {
         d_wflag.alloc(slots);
         d_wpairs.alloc(std::max<size_t>(1, static_cast<size_t>(n) * world->view().n_objects));
         d_wpairs2.alloc(d_wpairs.count);
+        d_wpinst2.alloc(d_wpairs.count);
         d_wtoff.alloc(ntiles);
         d_wctl.alloc(8);
         d_wcnt2.alloc(2 * static_cast<size_t>(ntiles));
@@ -1152,6 +1153,7 @@ struct sb_engine {
             pp.w_flag = d_wflag.p;
             pp.w_pairs = d_wpairs.p;
             pp.w_pairs2 = d_wpairs2.p;
+            pp.w_pinst2 = d_wpinst2.p;
             pp.w_toff = d_wtoff.p;
             pp.w_ctl = d_wctl.p;
             pp.w_list2 = d_wlist2.p;
@@ -1216,6 +1218,7 @@ struct sb_engine {
             pp.w_flag = d_wflag.p;
             pp.w_pairs = d_wpairs.p;
             pp.w_pairs2 = d_wpairs2.p;
+            pp.w_pinst2 = d_wpinst2.p;
             pp.w_toff = d_wtoff.p;
             pp.w_ctl = d_wctl.p;
             launches += sbk::place_wide_round0_rest(pp, grid, num_sms, s, 0, false);
