@@ -505,15 +505,19 @@ __device__ __forceinline__ void cell_insert(const SbCellGrid& G, uint64_t inst, 
   cell_range(G, mn, mx, cx0, cx1, cy0, cy1);
   uint32_t* base = G.cells + inst * (uint64_t)(G.g * G.g) * G.words + (obj >> 5);
   const uint32_t bit = 1u << (obj & 31);
-  const int nx = cx1 - cx0 + 1, nc = nx * (cy1 - cy0 + 1);
+  const int nc = (cx1 - cx0 + 1) * (cy1 - cy0 + 1);
+  int cx = cx0, cy = cy0;  // walked row by row (no division per cell)
   for (int c0 = 0; c0 < nc; c0 += 8) {
     uint32_t v[8];
     uint32_t* a[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const int ci = c0 + u;
-      a[u] = base + (uint64_t)((cy0 + ci / nx) * G.g + cx0 + ci % nx) * G.words;
-      v[u] = ci < nc ? *a[u] : 0u;
+      a[u] = base + (uint64_t)(cy * G.g + cx) * G.words;
+      v[u] = c0 + u < nc ? *a[u] : 0u;
+      if (++cx > cx1) {
+        cx = cx0;
+        ++cy;
+      }
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u)

@@ -1289,26 +1289,34 @@ __global__ void __launch_bounds__(kB, SB_WIDE_SAMPLE_MINB) k_wide_sample(PlacePa
         const SbCellGrid& G = p.grid;
         int cx0, cx1, cy0, cy1;
         cell_range(G, box, box + 3, cx0, cx1, cy0, cy1);
-        const int nx = cx1 - cx0 + 1, ncell = nx * (cy1 - cy0 + 1);
+        const int ncell = (cx1 - cx0 + 1) * (cy1 - cy0 + 1);
         const uint32_t* cb = G.cells + (uint64_t)inst * (uint64_t)(G.g * G.g) * words;
-        for (int c0 = 0; c0 < ncell; c0 += 4)
+        int wx = cx0, wy = cy0;  // cells walked row by row (no division per cell)
+        for (int c0 = 0; c0 < ncell; c0 += 4) {
+          const uint32_t* cp[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            cp[u] = cb + (uint64_t)(wy * G.g + wx) * words;
+            if (++wx > cx1) {
+              wx = cx0;
+              ++wy;
+            }
+          }
 #pragma unroll
           for (int wg = 0; wg < kW; wg += kWC) {  // words [wg, wg + kWC) of 4 cells
             if (wg >= words) break;
             uint32_t v[4][kWC];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int ci = c0 + u;
-              const int cy = cy0 + ci / nx, cx = cx0 + ci % nx;
-              const uint32_t* c = cb + (uint64_t)(cy * G.g + cx) * words + wg;
+            for (int u = 0; u < 4; ++u)
 #pragma unroll
-              for (int j = 0; j < kWC; ++j) v[u][j] = (ci < ncell && wg + j < words) ? __ldcg(c + j) : 0u;
-            }
+              for (int j = 0; j < kWC; ++j)
+                v[u][j] = (c0 + u < ncell && wg + j < words) ? __ldcg(cp[u] + wg + j) : 0u;
 #pragma unroll
             for (int u = 0; u < 4; ++u)
 #pragma unroll
               for (int j = 0; j < kWC; ++j) cand.or_word(wg + j, v[u][j]);
           }
+        }
       } else {  // every enabled object
 #pragma unroll
         for (int wd = 0; wd < kW; ++wd)

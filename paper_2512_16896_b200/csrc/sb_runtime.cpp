@@ -697,11 +697,27 @@ struct sb_engine {
     smem = sbk::place_smem_bytes(world->view().n_words, ws_bytes, world->view().n_objects);
     grid = static_cast<unsigned>(sbk::place_grid(num_sms, smem));
     if (grid == 0) throw CudaError("placement kernel does not fit on the device (shared memory)");
+    bool any_fifo = false;
+    for (const Placement& pl : places) any_fifo = any_fifo || pl.dev.anchor_object < 0;
+    // wide round 0: single GPU, or sharded with the device-side exchange (round 0's counts
+    // gathered between k_fast_init and the wide kernels); measured slower below 131072 (C2, C3)
+    use_wide = (world_size == 1 || allgather_dev) && any_fifo && n >= 131072;
+    if (const char* e = std::getenv("SB_WIDE"))
+      use_wide = (world_size == 1 || allgather_dev) && any_fifo && std::atoi(e) != 0;
     {  // tiles: a multiple of the grid, at most kPlaceBlock instances each
       const uint64_t per_wave = static_cast<uint64_t>(grid) * sbk::kPlaceBlock;
       const uint64_t waves = (n + per_wave - 1) / per_wave;
       const uint64_t want = static_cast<uint64_t>(grid) * waves;
       tile_inst = static_cast<int>((n + want - 1) / want);
+      // Wide engines: full 256-instance tiles. Round 0's grid-wide kernels launch a CTA per
+      // tile (no idle threads), and the persistent rounds work on the re-dealt survivor list,
+      // so the tile count need not be a multiple of the persistent grid (SB_WIDE_FULL_TILES=0:
+      // the balanced size).
+      static const bool full_tiles = [] {
+        const char* e = std::getenv("SB_WIDE_FULL_TILES");
+        return !e || std::atoi(e) != 0;
+      }();
+      if (use_wide && full_tiles) tile_inst = sbk::kPlaceBlock;
       // per-instance placements: smaller tiles, taken dynamically, so a dense tile's heavy
       // narrow phase does not hold the whole placement (SB_PI_SPLIT; measured best: 1)
       int split = 1;
@@ -713,19 +729,12 @@ struct sb_engine {
     }
     d_tile_list.alloc(static_cast<size_t>(ntiles) * tile_inst);
     d_tile_cnt.alloc(2 * static_cast<size_t>(ntiles));
-    {  // wide round 0: single GPU, FIFO placements (no relation), enough instances
-      bool any_fifo = false;
-      for (const Placement& pl : places) any_fifo = any_fifo || pl.dev.anchor_object < 0;
-      // single GPU, or sharded with the device-side exchange (round 0's counts gathered
-      // between k_fast_init and the wide kernels); measured slower below 131072 (C2, C3)
-      use_wide = (world_size == 1 || allgather_dev) && any_fifo && n >= 131072;
+    {  // wide round 0 scratch (use_wide decided above)
       wide_pgrid = grid;  // persistent grid for rounds >= 1 (SB_WIDE_PGRID: fewer CTAs)
       if (const char* e = std::getenv("SB_WIDE_PGRID"))
         wide_pgrid = std::max<unsigned>(
             (ntiles + sbk::kPlaceMaxOwnedTiles - 1) / sbk::kPlaceMaxOwnedTiles,  // owned-tile cap
             std::min<unsigned>(grid, static_cast<unsigned>(std::max(1, std::atoi(e)))));
-      if (const char* e = std::getenv("SB_WIDE"))
-        use_wide = (world_size == 1 || allgather_dev) && any_fifo && std::atoi(e) != 0;
       if (use_wide) {
         const size_t slots = static_cast<size_t>(ntiles) * sbk::kPlaceBlock;
         d_wpose.alloc(slots * sbk::kWideRec);

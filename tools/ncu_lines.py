@@ -63,6 +63,10 @@ print(f"{tot} samples; mapped offsets {len(lines_of)}")
 print("-- by innermost line")
 for k, v in agg_in.most_common(top):
     print(f"{v:7d} {v / max(tot, 1):6.1%}  exec {exe[k]:10d}  {k}")
+tot_e = sum(exe.values())
+print(f"-- by executed instructions (innermost line), {tot_e} total")
+for k, v in exe.most_common(top):
+    print(f"{v:10d} {v / max(tot_e, 1):6.1%}  samples {agg_in[k]:6d}  {k}")
 print("-- by outermost (kernel-file) line")
 for k, v in agg_out.most_common(top // 2):
     print(f"{v:7d} {v / max(tot, 1):6.1%}  {k}")
