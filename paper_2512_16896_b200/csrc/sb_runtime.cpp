@@ -447,7 +447,7 @@ struct sb_engine {
   uint32_t ntiles = 0;
   int tile_inst = 0, tile_inst_pi = 0, max_tris = 1, max_nodes = 1, ws_bytes = 0;
   int spec_target = 64;
-  int solo_max = 16;
+  int solo_max = 0;  // SB_SOLO: CTA 0 alone below this many survivors (r02: off measured best, C2 +0.9 %, C4 -2.7 %)
   int solo_spec = 0;  // SB_SOLO_SPEC: speculative slots per solo round (0/1: one round at a time)
   unsigned grid = 0;
   size_t smem = 0;
