@@ -632,6 +632,14 @@ __device__ uint32_t tile_round(const PlaceParams& p, const Sampling& S, const Sb
       for (int cy = cy0; cy <= cy1; ++cy)
         for (int cx = cx0; cx <= cx1; ++cx) {
           const uint32_t* c = cb + (uint64_t)(cy * G.g + cx) * words;
+          if (words == 4) {  // the cell's words in one 16-byte load
+            const uint4 v = __ldcg(reinterpret_cast<const uint4*>(c));
+            pend[0] |= v.x;
+            pend[1] |= v.y;
+            pend[2] |= v.z;
+            pend[3] |= v.w;
+            continue;
+          }
 #pragma unroll
           for (int wd = 0; wd < kGW; ++wd)
             if (wd < words) pend[wd] |= __ldcg(c + wd);
@@ -1301,6 +1309,20 @@ __global__ void __launch_bounds__(kB, SB_WIDE_SAMPLE_MINB) k_wide_sample(PlacePa
               wx = cx0;
               ++wy;
             }
+          }
+          if (kW == 4 && words == 4) {  // a cell's 4 words in one 16-byte load
+            uint4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              v[u] = c0 + u < ncell ? __ldcg(reinterpret_cast<const uint4*>(cp[u])) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              cand.or_word(0, v[u].x);
+              cand.or_word(1, v[u].y);
+              cand.or_word(2, v[u].z);
+              cand.or_word(3, v[u].w);
+            }
+            continue;
           }
 #pragma unroll
           for (int wg = 0; wg < kW; wg += kWC) {  // words [wg, wg + kWC) of 4 cells
