@@ -1395,9 +1395,14 @@ __global__ void __launch_bounds__(kB, SB_WIDE_SAMPLE_MINB) k_wide_sample(PlacePa
         double2* cp = reinterpret_cast<double2*>(p.w_pose + slot * kWideRec);
 #pragma unroll
         for (int k = 0; k < 3; ++k) cp[k] = make_double2(rec[2 * k], rec[2 * k + 1]);
+        if (kW == 4 && words == 4) {
+          *reinterpret_cast<uint4*>(p.w_ovm + slot * kGW) =
+              make_uint4(ov.word(0), ov.word(1), ov.word(2), ov.word(3));
+        } else {
 #pragma unroll
-        for (int wd = 0; wd < kW; ++wd)
-          if (wd < words) p.w_ovm[slot * kGW + wd] = ov.word(wd);
+          for (int wd = 0; wd < kW; ++wd)
+            if (wd < words) p.w_ovm[slot * kGW + wd] = ov.word(wd);
+        }
         p.w_contact[slot] = kFree;
         flag = kSlotChecked;
       }
@@ -1601,8 +1606,11 @@ __global__ void __launch_bounds__(kB) k_wide_accept(PlaceParams p) {
       keep = 1;
     } else if (flag == kSlotChecked) {
       const int32_t c = __ldcg(p.w_contact + slot);
+      uint4 m4 = make_uint4(0, 0, 0, 0);
+      if (words == 4) m4 = __ldcg(reinterpret_cast<const uint4*>(p.w_ovm + slot * kGW));
       for (int wd = 0; wd < words; ++wd) {  // narrow tests up to the first hit
-        uint32_t mk = __ldcg(p.w_ovm + slot * kGW + wd);
+        uint32_t mk = words == 4 ? (wd == 0 ? m4.x : wd == 1 ? m4.y : wd == 2 ? m4.z : m4.w)
+                                 : __ldcg(p.w_ovm + slot * kGW + wd);
         if (c != kFree) {
           const int lim = c - 32 * wd;  // keep objects <= c
           if (lim < 0) mk = 0;
