@@ -88,6 +88,17 @@ def test_fuzz_engine_matches_reference(gpu, ref, seed):
     eng, got, want = run_generate_pair(gpu, ref, scene, seed=seed + 1)
     check_against_reference(gpu, scene, got, want)
 
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("SB_FUZZ_WIDE_SEEDS", "16"))))
+def test_fuzz_wide_round0_matches_reference(gpu, ref, seed, monkeypatch):
+    """The grid-wide round 0 (k_wide_*; normally from 131,072 instances) forced onto the
+    random scenes: every FIFO placement without a relation takes it, the rest keep the
+    persistent path -- bit-exact against the reference like the default path."""
+    monkeypatch.setenv("SB_WIDE", "1")
+    scene = random_scene(gpu, 1000 + seed)
+    eng, got, want = run_generate_pair(gpu, ref, scene, seed=seed + 7)
+    check_against_reference(gpu, scene, got, want)
+
+
 @pytest.mark.parametrize("seed", range(8))
 @pytest.mark.parametrize("device_exchange", [False, True])
 def test_fuzz_sharded_equals_single(gpu, seed, device_exchange):
