@@ -1210,9 +1210,15 @@ struct ObjSet {
 constexpr int kWideScanThreads = 1024;
 // buf 0: round 0's counts (draw offsets, pair counters reset); buf 1: round 1's survivors
 // (offsets for k_wide_spread, total S into w_ctl[5]).
-__global__ void __launch_bounds__(kWideScanThreads) k_wide_scan(PlaceParams p, int buf) {
+// post = 0, before round a's sample: offsets of the round's actives (count buffer a & 1),
+// pair counters reset, w_ctl[9] = D_a (draws before round a), w_ctl[4] = D_a + actives.
+// post = 1, after its accept: offsets of the survivors (buffer (a + 1) & 1) for k_wide_spread,
+// their total into w_ctl[5] (and w_surv[a] when the engine records it).
+__global__ void __launch_bounds__(kWideScanThreads) k_wide_scan(PlaceParams p, int post) {
   using Scan = cub::BlockScan<uint32_t, kWideScanThreads>;
   __shared__ typename Scan::TempStorage scan;
+  const int32_t a = p.wide_round;
+  const int buf = (a + post) & 1;
   uint32_t running = 0;
   for (uint32_t c0 = 0; c0 < p.ntiles; c0 += kWideScanThreads) {
     const uint32_t t = c0 + threadIdx.x;
@@ -1223,11 +1229,16 @@ __global__ void __launch_bounds__(kWideScanThreads) k_wide_scan(PlaceParams p, i
     running += agg;
     __syncthreads();
   }
-  if (buf == 0) {
+  if (!post) {
     if (threadIdx.x < 4) p.w_ctl[threadIdx.x] = 0ull;
-    if (threadIdx.x == 0) p.w_ctl[4] = running;  // round 0's draws (k_place: start_draws)
+    if (threadIdx.x == 0) {
+      const unsigned long long d_a = a ? p.w_ctl[4] : 0ull;
+      p.w_ctl[9] = d_a;
+      p.w_ctl[4] = d_a + running;  // draws before round a + 1 (k_place: start_draws)
+    }
   } else if (threadIdx.x == 0) {
-    p.w_ctl[5] = running;  // round 1's active instances
+    p.w_ctl[5] = running;  // round a + 1's active instances
+    if (p.w_surv && a < kWideSurvRounds) p.w_surv[a] = running;
     if (p.xcount) p.xcount[1] = running;  // sharded: this rank's count for the exchange
   }
 }
@@ -1244,7 +1255,8 @@ __global__ void __launch_bounds__(kB, SB_WIDE_SAMPLE_MINB) k_wide_sample(PlacePa
   const uint32_t t = blockIdx.x;
   const int e = threadIdx.x, lane = e & 31;
   const WorldView& w = p.w;
-  const uint32_t n = __ldcg(p.tile_cnt + t);
+  const int32_t a = p.wide_round;  // this wide round's attempt (0, or later dense rounds)
+  const uint32_t n = __ldcg(p.tile_cnt + (size_t)(a & 1) * p.cnt_stride + t);
   const uint64_t seed = p.seed_dev ? __ldg(p.seed_dev) : p.run_seed;
   const uint64_t state0 =
       p.seed_dev ? Pcg::seeded(stream_seed2(seed, p.pl.salt, kCacheSalt)).state : p.fast_state0;
@@ -1271,8 +1283,10 @@ __global__ void __launch_bounds__(kB, SB_WIDE_SAMPLE_MINB) k_wide_sample(PlacePa
     const uint32_t inst = __ldcg(p.tile_list + (uint64_t)t * p.tile_inst + e);
     M34 pose;
     double rec[6];
-    bool placeable = compose_candidate(p, S, seed, state0, inst, 0,
-                                       draw_base + (uint64_t)__ldcg(p.w_toff + t) + (uint64_t)e,
+    // FIFO draw of round a: the draws of the earlier rounds (w_ctl[9]) + this entry's rank
+    const uint64_t d_a = a ? __ldcg(p.w_ctl + 9) : 0ull;
+    bool placeable = compose_candidate(p, S, seed, state0, inst, a,
+                                       draw_base + d_a + (uint64_t)__ldcg(p.w_toff + t) + (uint64_t)e,
                                        pose, rec);
     if constexpr (kReach) {
       if (placeable) placeable = reach_ok(p, inst, pose);
@@ -1385,7 +1399,7 @@ __global__ void __launch_bounds__(kB, SB_WIDE_SAMPLE_MINB) k_wide_sample(PlacePa
         double2 q[6];
 #pragma unroll
         for (int k = 0; k < 6; ++k) q[k] = make_double2(P.m[2 * k], P.m[2 * k + 1]);
-        accept_candidate<kGrid>(p, inst, q, box, 0);
+        accept_candidate<kGrid>(p, inst, q, box, a);
         ++L.accepted;
         flag = kWideDone;
       } else {
@@ -1426,7 +1440,7 @@ __global__ void __launch_bounds__(kB, SB_WIDE_SAMPLE_MINB) k_wide_sample(PlacePa
     for (int ob = ov.pop_lowest(); ob >= 0; ob = ov.pop_lowest())
       p.w_pairs[q++] = ((uint32_t)slot << 8) | (uint32_t)ob;
   }
-  if (threadIdx.x == 0 && n) atomicMax(p.ctrl + kRounds, 1u);  // reference round count
+  if (threadIdx.x == 0 && n) atomicMax(p.ctrl + kRounds, (uint32_t)(a + 1));  // reference rounds
   flush(p, L);
 }
 
@@ -1594,7 +1608,8 @@ __global__ void __launch_bounds__(kB) k_wide_accept(PlaceParams p) {
   __shared__ typename BlockScan::TempStorage scan;
   const uint32_t t = blockIdx.x;
   const int e = threadIdx.x;
-  const uint32_t n = __ldcg(p.tile_cnt + t);
+  const int32_t a = p.wide_round;
+  const uint32_t n = __ldcg(p.tile_cnt + (size_t)(a & 1) * p.cnt_stride + t);
   const int words = p.w.n_words;
   Local L;
   uint32_t keep = 0, inst = 0;
@@ -1637,7 +1652,7 @@ __global__ void __launch_bounds__(kB) k_wide_accept(PlaceParams p) {
           }
           xform_aabb(pose, c, h, box, box + 3);
         }
-        accept_candidate<kGrid>(p, inst, q, box, 0);
+        accept_candidate<kGrid>(p, inst, q, box, a);
         ++L.accepted;
       } else {
         keep = 1;
@@ -1648,7 +1663,7 @@ __global__ void __launch_bounds__(kB) k_wide_accept(PlaceParams p) {
   BlockScan(scan).ExclusiveSum(keep, rank, total);
   __syncthreads();  // every entry of the list has been read
   if (keep) p.tile_list[(uint64_t)t * p.tile_inst + rank] = inst;
-  if (e == 0) p.tile_cnt[p.cnt_stride + t] = total;
+  if (e == 0) p.tile_cnt[(size_t)((a + 1) & 1) * p.cnt_stride + t] = total;
   flush(p, L);
 }
 
@@ -1664,7 +1679,8 @@ __global__ void __launch_bounds__(kB) k_wide_spread(PlaceParams p, unsigned grid
   unsigned long long q = S ? (S + grid - 1) / grid : 1;  // at most one tile's capacity
   if (q > (unsigned long long)p.tile_inst) q = p.tile_inst;
   const uint32_t t = blockIdx.x;
-  const uint32_t n = __ldcg(p.tile_cnt + p.cnt_stride + t);
+  const size_t ob = (size_t)((p.wide_round + 1) & 1) * p.cnt_stride;  // the survivors' buffer
+  const uint32_t n = __ldcg(p.tile_cnt + ob + t);
   const unsigned long long off = __ldcg(p.w_toff + t);
   for (uint32_t e = threadIdx.x; e < n; e += kB) {
     const unsigned long long r = off + e;
@@ -1672,7 +1688,7 @@ __global__ void __launch_bounds__(kB) k_wide_spread(PlaceParams p, unsigned grid
   }
   for (uint32_t k = blockIdx.x * kB + threadIdx.x; k < p.ntiles; k += gridDim.x * kB) {
     const unsigned long long lo = (unsigned long long)k * q;
-    p.w_cnt2[p.cnt_stride + k] = S > lo ? (uint32_t)(S - lo < q ? S - lo : q) : 0u;
+    p.w_cnt2[ob + k] = S > lo ? (uint32_t)(S - lo < q ? S - lo : q) : 0u;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) p.w_ctl[6] = (S + q - 1) / q;  // tiles in use
 }
@@ -1784,8 +1800,7 @@ int place_wide_round0(const PlaceParams& p, unsigned init_grid, size_t init_smem
   return 1 + place_wide_round0_rest(p, init_grid, num_sms, s, spread_grid, true);
 }
 
-int place_wide_round0_rest(const PlaceParams& p, unsigned init_grid, int num_sms, sb_stream_t s,
-                           unsigned spread_grid, bool spread) {
+int place_wide_round0_a(const PlaceParams& p, int num_sms, sb_stream_t s) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
   k_wide_scan<<<1, kWideScanThreads, 0, st>>>(p, 0);
   check(cudaGetLastError(), "k_wide_scan");
@@ -1828,18 +1843,30 @@ int place_wide_round0_rest(const PlaceParams& p, unsigned init_grid, int num_sms
   else if (minb == 4) k_wide_narrow<true, 4><<<ngrid, kB, smem, st>>>(p, chunk, ahead);
   else k_wide_narrow<true><<<ngrid, kB, smem, st>>>(p, chunk, ahead);
   check(cudaGetLastError(), "k_wide_narrow");
+  return 4;
+}
+
+int place_wide_round0_c(const PlaceParams& p, unsigned init_grid, sb_stream_t s,
+                        unsigned spread_grid, bool spread) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
+  const bool g = p.grid.g != 0;
   if (g) k_wide_accept<true><<<p.ntiles, kB, 0, st>>>(p);
   else k_wide_accept<false><<<p.ntiles, kB, 0, st>>>(p);
   check(cudaGetLastError(), "k_wide_accept");
   k_wide_scan<<<1, kWideScanThreads, 0, st>>>(p, 1);
   check(cudaGetLastError(), "k_wide_scan");
-  if (!spread) return 6;  // sharded: rounds >= 1 read the compacted tiles in place
+  if (!spread) return 2;  // sharded: rounds >= 1 read the compacted tiles in place
   // round 1's survivors over the persistent kernel's grid (SB_SPREAD=0: full tiles instead)
   unsigned sg = spread_grid ? spread_grid : init_grid;
   if (const char* e = std::getenv("SB_SPREAD")) sg = std::atoi(e) ? sg : 1u;
   k_wide_spread<<<p.ntiles, kB, 0, st>>>(p, sg);
   check(cudaGetLastError(), "k_wide_spread");
-  return 7;
+  return 3;
+}
+
+int place_wide_round0_rest(const PlaceParams& p, unsigned init_grid, int num_sms, sb_stream_t s,
+                           unsigned spread_grid, bool spread) {
+  return place_wide_round0_a(p, num_sms, s) + place_wide_round0_c(p, init_grid, s, spread_grid, spread);
 }
 
 void place_fast_finish(const PlaceParams& p, int32_t attempt, unsigned grid, sb_stream_t s) {

@@ -115,6 +115,8 @@ struct PlaceParams {
   uint32_t* w_pairs;             // [<= n * n_objects] (slot << 8 | object)
   uint32_t* w_pairs2;            // [same] the pairs past the leaf-box filter
   uint32_t* w_pinst2;            // [same] their instance ids (no tile-list lookup to stage)
+  int32_t wide_round;            // attempt a of this wide round (0; dense later rounds too)
+  unsigned long long* w_surv;    // [kWideSurvRounds] survivors after each wide round, or null
   uint32_t* w_toff;              // [ntiles] first FIFO draw of each tile
   unsigned long long* w_ctl;     // [7] pairs appended, -, filtered pairs appended / claimed,
                                  // round-0 draws, round-1 active instances, tiles in use
@@ -131,6 +133,7 @@ struct PlaceParams {
 constexpr int kPlaceBlock = SB_PLACE_BLOCK;  // threads per placement CTA = max tile slots
 constexpr int kPlaceMaxOwnedTiles = 64;  // tiles per CTA on the fast path
 constexpr int kWideRec = 6;  // doubles per round-0 candidate record (w_pose)
+constexpr int kWideSurvRounds = 4;  // wide rounds per placement at most (the rest persistent)
 
 // Dynamic shared memory of one placement CTA for a world with `n_words` enable words.
 size_t place_smem_bytes(int n_words, int ws_bytes, int n_objects);
@@ -161,6 +164,11 @@ int place_wide_round0(const PlaceParams& p, unsigned init_grid, size_t init_smem
 // their tiles (tile_cnt buffer 1) for k_fast_round. Returns the number of launches.
 int place_wide_round0_rest(const PlaceParams& p, unsigned init_grid, int num_sms, sb_stream_t s,
                            unsigned spread_grid, bool spread);
+// The same for wide round p.wide_round in two steps: (A) scan, sample, filter, narrow;
+// (C) accept, scan, and (spread) the survivors re-dealt for the persistent kernel.
+int place_wide_round0_a(const PlaceParams& p, int num_sms, sb_stream_t s);
+int place_wide_round0_c(const PlaceParams& p, unsigned init_grid, sb_stream_t s,
+                        unsigned spread_grid, bool spread);
 // Narrow-kernel dynamic shared memory (per-warp scratch) for the given ws_bytes.
 size_t wide_narrow_smem(int ws_bytes);
 // ctrl word receiving the survivor total of round `attempt` (fast path, sharded)

@@ -422,6 +422,12 @@ struct sb_engine {
   DevArray<double> d_wpose;
   DevArray<int32_t> d_wcontact;
   DevArray<uint32_t> d_wovm, d_wpairs, d_wpairs2, d_wpinst2, d_wtoff, d_wlist2;
+  // dense placements: survivors after each wide round in the last run, and the wide rounds
+  // the next run gives each placement (1 = round 0 only)
+  DevArray<unsigned long long> d_wsurv;
+  PinnedArray<unsigned long long> h_wsurv;
+  std::vector<int> wide_rounds;
+  unsigned long long wide_more = 32768;
   DevArray<uint32_t> d_wcnt2;
   DevArray<uint8_t> d_wflag;
   DevArray<unsigned long long> d_wctl;
@@ -747,7 +753,11 @@ struct sb_engine {
         d_wpairs2.alloc(d_wpairs.count);
         d_wpinst2.alloc(d_wpairs.count);
         d_wtoff.alloc(ntiles);
-        d_wctl.alloc(8);
+        d_wctl.alloc(16);
+        d_wsurv.alloc(static_cast<size_t>(sbk::kWideSurvRounds) * std::max<size_t>(1, places.size()));
+        wide_rounds.assign(places.size(), 1);
+        if (const char* e = std::getenv("SB_WIDE_MORE"))  // survivors that earn another wide round
+          wide_more = std::strtoull(e, nullptr, 10);
         d_wcnt2.alloc(2 * static_cast<size_t>(ntiles));
         d_wlist2.alloc(static_cast<size_t>(ntiles) * tile_inst);
       }
@@ -1169,8 +1179,18 @@ struct sb_engine {
             pp.w_ctl = d_wctl.p;
             pp.w_list2 = d_wlist2.p;
             pp.w_cnt2 = d_wcnt2.p;
-            launches += sbk::place_wide_round0(pp, grid, smem, num_sms, s, wide_pgrid);
-            pp.start_round = 1;  // rounds 1.. on the re-dealt survivor list
+            pp.w_surv = d_wsurv.p + sbk::kWideSurvRounds * p;
+            // dense placements (the last run left >= wide_more survivors after round r) run
+            // round r + 1 grid-wide too; the persistent kernel takes the rounds after
+            const int R = std::min<int>(attempts, wide_rounds[p]);
+            sbk::place_fast_init(pp, grid, smem, s);
+            ++launches;
+            for (int r = 0; r < R; ++r) {
+              pp.wide_round = r;
+              launches += sbk::place_wide_round0_a(pp, num_sms, s);
+              launches += sbk::place_wide_round0_c(pp, grid, s, wide_pgrid, r + 1 == R);
+            }
+            pp.start_round = R;  // rounds R.. on the re-dealt survivor list
             pp.start_draws = d_wctl.p + 4;
             pp.tile_list = d_wlist2.p;
             pp.tile_cnt = d_wcnt2.p;
@@ -1406,6 +1426,12 @@ struct sb_engine {
     cuda_check(cudaMemcpyAsync(ctrl_all, d_ctrl.p, 32 * P1, cudaMemcpyDeviceToHost, stream), "D2H ctrl");
     cuda_check(cudaMemcpyAsync(rflags, d_rflags.p, 8 * P1, cudaMemcpyDeviceToHost, stream), "D2H flags");
     unsigned long long* nvalid = reinterpret_cast<unsigned long long*>(h_stat.p + 128 + 40 * P1);
+    const bool wide_hist = use_wide && world_size == 1 && full;
+    if (wide_hist) {
+      h_wsurv.ensure(d_wsurv.count);
+      cuda_check(cudaMemcpyAsync(h_wsurv.p, d_wsurv.p, d_wsurv.count * 8, cudaMemcpyDeviceToHost, stream),
+                 "D2H wide survivors");
+    }
     if (st) {  // valid instances counted on the device (no N-byte readback)
       d_nvalid.ensure(1);
       cuda_check(cudaMemsetAsync(d_nvalid.p, 0, 8, stream), "memset");
@@ -1416,6 +1442,15 @@ struct sb_engine {
     const auto th1 = std::chrono::steady_clock::now();
     cuda_check(cudaStreamSynchronize(stream), "sync");
     const auto th2 = std::chrono::steady_clock::now();
+    if (wide_hist) {  // the next run's wide rounds per placement from this run's survivors
+      for (size_t p = 0; p < P; ++p) {
+        const int R = wide_rounds[p];
+        const unsigned long long* sv = h_wsurv.p + sbk::kWideSurvRounds * p;
+        int r_next = 1;
+        while (r_next < std::min(R + 1, sbk::kWideSurvRounds) && sv[r_next - 1] >= wide_more) ++r_next;
+        wide_rounds[p] = r_next;
+      }
+    }
     for (size_t p = lo; p < hi; ++p) {
       if (rflags[2 * p + 1] != 0)
         throw std::runtime_error("constraint region build failed for placement " + std::to_string(p) +

@@ -431,6 +431,22 @@ def test_sharded_early_finisher_and_exhausted_shard(gpu, monkeypatch, attempts, 
         assert np.array_equal(np.concatenate([r.accepted for r in results], axis=1), whole.accepted), bounds
 
 
+@pytest.mark.parametrize("attempts", [3, 4, 64])
+def test_dense_wide_rounds_match_reference(gpu, ref, monkeypatch, attempts):
+    """Dense placements run later rounds grid-wide too once a run has seen many survivors
+    (SB_WIDE_MORE: the survivor count that earns another wide round; 1 here, so every
+    placement with a survivor goes up to 4 wide rounds on the repeated runs, including
+    K = 3 / 4 where the wide rounds reach the last attempt). Every run equals the reference."""
+    monkeypatch.setenv("SB_WIDE", "1")
+    monkeypatch.setenv("SB_WIDE_MORE", "1")
+    scene = scenes.tabletop_boxes(1500, n_objects=40, attempts=attempts)
+    want = ref.generate(scene, 5, threads=8)
+    eng = gpu.Engine(scene)
+    for _ in range(4):  # run 1 records survivors, later runs use 2, 3, 4 wide rounds
+        got = eng.generate(5)
+        assert_same(gpu, got, want)
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_sharded_generate_equals_single(gpu, ref, world):
     """Variation-batch sharding: G shards with the per-round count exchange
