@@ -133,7 +133,10 @@ struct PlaceParams {
 constexpr int kPlaceBlock = SB_PLACE_BLOCK;  // threads per placement CTA = max tile slots
 constexpr int kPlaceMaxOwnedTiles = 64;  // tiles per CTA on the fast path
 constexpr int kWideRec = 6;  // doubles per round-0 candidate record (w_pose)
-constexpr int kWideSurvRounds = 4;  // wide rounds per placement at most (the rest persistent)
+#ifndef SB_WIDE_ROUNDS_MAX
+#define SB_WIDE_ROUNDS_MAX 4
+#endif
+constexpr int kWideSurvRounds = SB_WIDE_ROUNDS_MAX;  // wide rounds per placement at most
 
 // Dynamic shared memory of one placement CTA for a world with `n_words` enable words.
 size_t place_smem_bytes(int n_words, int ws_bytes, int n_objects);
