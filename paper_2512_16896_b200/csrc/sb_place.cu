@@ -1163,7 +1163,9 @@ __global__ void __launch_bounds__(kB) k_fast_finish(PlaceParams p, int32_t a) {
 // the survivors from round 1 on (k_place with start_round = 1). Slot of a round-0 entry:
 // tile * kB + position in the tile's (ascending) list, the tiles of k_fast_init.
 constexpr uint8_t kWideDone = 8;  // accepted in k_wide_sample: no object overlaps its box
-constexpr int kWideChunk = 1;  // narrow pairs a warp claims at a time (C4: 1 / 2 / 4 / 8 = 31.0 / 31.2 / 32.5 / 35.6 ms)
+constexpr int kWideChunk = 0;  // narrow pairs a warp claims at a time; 0 = adaptive (1, or up to 4
+                               // when every warp has > 64 pairs: C4 1/2/4/8 = 31.0/31.2/32.5/35.6
+                               // ms, C5 x 100 1/4/8 = 342.7/334.3/336.0 ms)
 static_assert(kWideRec == 6, "compact candidate record: tx, ty, tz, cos, sin, pad");
 
 // A set of object ids < 32 * kW held in 64-bit registers with explicit members (no
@@ -1542,7 +1544,13 @@ __global__ void __launch_bounds__(kB, kMinB) k_wide_narrow(PlaceParams p, int ch
   // next chunk claimed one chunk ahead (lane 0's atomic is only waited for at the chunk
   // boundary), so staging stays one pair ahead across chunk boundaries.
   constexpr uint64_t kEnd = ~0ull;
-  const unsigned long long ck = (unsigned long long)chunk;
+  // chunk 0 = adaptive: one pair per claim unless every warp has > 64 pairs on average
+  // (dense launches: larger chunks keep the claim counter from becoming the bottleneck)
+  unsigned long long ck = (unsigned long long)chunk;
+  if (chunk == 0) {
+    const unsigned long long per_warp = np / ((unsigned long long)gridDim.x * kWarps);
+    ck = per_warp > 64 ? (per_warp / 64 < 4 ? per_warp / 64 : 4) : 1;
+  }
   unsigned long long ahead = 0;  // lane 0: start of the chunk claimed ahead (in flight)
   if (lane == 0 && claim_ahead) ahead = atomicAdd(p.w_ctl + 3, ck);
   uint64_t qe = 0;  // end of the current chunk
@@ -1833,7 +1841,7 @@ int place_wide_round0_a(const PlaceParams& p, int num_sms, sb_stream_t s) {
   const unsigned ngrid = (unsigned)(per > 0 ? per : 1) * num_sms;
   static const int chunk = [] {  // pairs a warp claims at a time (SB_NARROW_CHUNK)
     const char* e = std::getenv("SB_NARROW_CHUNK");
-    return e && std::atoi(e) > 0 ? std::atoi(e) : kWideChunk;
+    return e && std::atoi(e) >= 0 ? std::atoi(e) : kWideChunk;
   }();
   static const int ahead = [] {  // claim the next chunk one chunk ahead (SB_NARROW_AHEAD)
     const char* e = std::getenv("SB_NARROW_AHEAD");
