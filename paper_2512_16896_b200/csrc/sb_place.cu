@@ -935,13 +935,16 @@ __device__ void instance_tiles(const PlaceParams& p, const Sampling& S, const Sb
   for (;;) {
     if (threadIdx.x == 0) F.tile = atomicAdd(p.ctrl + kTileCtr, 1u);
     __syncthreads();
-    const uint32_t t = F.tile;
+    const uint32_t c = F.tile;
     __syncthreads();
-    if (t >= p.ntiles_pi) break;
+    if (c >= p.ntiles_pi) break;
+    // claim order -> tile: the previous run's slowest tiles first (longest processing time
+    // first, so a straggler does not start in the last wave); results do not depend on it
+    const uint32_t t = p.tile_perm ? __ldg(p.tile_perm + c) : c;
     uint32_t nt = tile_load_valid(p, T, F, t, p.tile_inst_pi);
     int32_t a = 0;
     unsigned rounds = 0;
-    const unsigned long long tt0 = p.dbg_inst && threadIdx.x == 0 ? global_ns() : 0;
+    const unsigned long long tt0 = (p.dbg_inst || p.tile_ns) && threadIdx.x == 0 ? global_ns() : 0;
     while (nt > 0 && a < p.attempts) {
       ++rounds;
       int W = p.spec_target / (int)nt;
@@ -968,6 +971,10 @@ __device__ void instance_tiles(const PlaceParams& p, const Sampling& S, const Sb
       }
     }
     mark_invalid(p, T, nt);
+    if (p.tile_ns && threadIdx.x == 0) {
+      const unsigned long long d = global_ns() - tt0;
+      p.tile_ns[t] = d < 0xffffffffull ? (uint32_t)d : 0xffffffffu;
+    }
     if (p.dbg_inst && threadIdx.x == 0) {  // per-tile debug: max / sum of ns and rounds
       const unsigned dt = (unsigned)(global_ns() - tt0);
       atomicMax(p.dbg_inst + 0, dt);

@@ -66,6 +66,8 @@ struct PlaceParams {
   uint32_t ntiles_pi;           // per-instance path: smaller tiles taken dynamically
   int32_t tile_inst_pi;
   int32_t spec_target;          // per-instance path: target slots per tile round
+  const uint32_t* tile_perm;     // per-instance path: claim order -> tile (null = identity)
+  uint32_t* tile_ns;             // ... and each tile's processing time (ns), or null
   int32_t solo_max;             // fast path: at most this many survivors -> CTA 0 alone
   int32_t solo_spec;            // fast path solo tail: target speculative slots per round
   int32_t ws_bytes;             // narrow-phase scratch per warp (sb_warp.cuh)

@@ -453,6 +453,12 @@ struct sb_engine {
   uint32_t ntiles = 0;
   int tile_inst = 0, tile_inst_pi = 0, max_tris = 1, max_nodes = 1, ws_bytes = 0;
   int spec_target = 64;
+  // per-instance placements: each tile's processing time in the last run and the claim
+  // order for the next one (slowest first); results do not depend on the order
+  DevArray<uint32_t> d_tile_ns, d_tile_perm;
+  PinnedArray<uint32_t> h_tile_ns;
+  std::vector<char> tile_perm_ok;
+  bool lpt_tiles = true;  // SB_LPT=0: claim order = tile order
   int solo_max = 0;  // SB_SOLO: CTA 0 alone below this many survivors (r02: off measured best, C2 +0.9 %, C4 -2.7 %)
   int solo_spec = 0;  // SB_SOLO_SPEC: speculative slots per solo round (0/1: one round at a time)
   unsigned grid = 0;
@@ -736,6 +742,21 @@ struct sb_engine {
         throw std::invalid_argument("shard too large for one device: " + std::to_string(n) + " instances");
     }
     d_tile_list.alloc(static_cast<size_t>(ntiles) * tile_inst);
+    if (const char* e = std::getenv("SB_LPT")) lpt_tiles = std::atoi(e) != 0;
+    {
+      bool any_rel = false;
+      for (const Placement& pl : places) any_rel = any_rel || pl.dev.anchor_object >= 0;
+      // only with several per-instance tiles per CTA (C3: 4 -> 18.80 to 17.35 ms; C2 at ~1
+      // per CTA: 3.72 -> 3.79 ms, so off there)
+      lpt_tiles = lpt_tiles && any_rel && pp_ntiles_pi() * 2 > 3 * static_cast<size_t>(grid);
+      if (lpt_tiles) {
+        const size_t cnt = std::max<size_t>(1, places.size()) * pp_ntiles_pi();
+        d_tile_ns.alloc(cnt);
+        d_tile_perm.alloc(cnt);
+        h_tile_ns.ensure(cnt);
+        tile_perm_ok.assign(places.size(), 0);
+      }
+    }
     d_tile_cnt.alloc(2 * static_cast<size_t>(ntiles));
     {  // wide round 0 scratch (use_wide decided above)
       wide_pgrid = grid;  // persistent grid for rounds >= 1 (SB_WIDE_PGRID: fewer CTAs)
@@ -1005,6 +1026,10 @@ struct sb_engine {
   uint64_t run_acc_rounds_host = 0, run_acc_per_inst = 0;
   std::vector<char> device_rounds_run;
 
+  size_t pp_ntiles_pi() const {
+    return static_cast<size_t>((n + tile_inst_pi - 1) / std::max(1, tile_inst_pi));
+  }
+
   void generate(uint64_t run_seed, sb_run_stats* st, sb_result* out = nullptr) {
     generate_range(run_seed, 0, places.size(), st, out);
   }
@@ -1161,6 +1186,10 @@ struct sb_engine {
         pp.dbg = round_debug ? d_dbg.p + 3 * static_cast<size_t>(attempts) * p : nullptr;
         pp.dbg_inst = round_debug ? d_dbg.p + d_dbg.count - 16 : nullptr;
         pp.vary_flag = (relation && world_size == 1) ? d_rflags.p + 2 * p : nullptr;
+        if (relation && lpt_tiles) {
+          pp.tile_ns = d_tile_ns.p + static_cast<size_t>(p) * pp_ntiles_pi();
+          pp.tile_perm = tile_perm_ok[p] ? d_tile_perm.p + static_cast<size_t>(p) * pp_ntiles_pi() : nullptr;
+        }
         if (p < reach.size() && reach[p].any) {
           pp.reach_any = reach[p].any;
           pp.reach_grid = reach[p].grid;
@@ -1426,6 +1455,9 @@ struct sb_engine {
     cuda_check(cudaMemcpyAsync(ctrl_all, d_ctrl.p, 32 * P1, cudaMemcpyDeviceToHost, stream), "D2H ctrl");
     cuda_check(cudaMemcpyAsync(rflags, d_rflags.p, 8 * P1, cudaMemcpyDeviceToHost, stream), "D2H flags");
     unsigned long long* nvalid = reinterpret_cast<unsigned long long*>(h_stat.p + 128 + 40 * P1);
+    if (lpt_tiles && full)
+      cuda_check(cudaMemcpyAsync(h_tile_ns.p, d_tile_ns.p, d_tile_ns.count * 4, cudaMemcpyDeviceToHost, stream),
+                 "D2H tile times");
     const bool wide_hist = use_wide && world_size == 1 && full;
     if (wide_hist) {
       h_wsurv.ensure(d_wsurv.count);
@@ -1462,6 +1494,18 @@ struct sb_engine {
     pending_per_inst.assign(P, 0);
     for (size_t p = lo; p < hi; ++p)
       pending_per_inst[p] = places[p].dev.anchor_object >= 0 && rflags[2 * p] != 0;
+    if (lpt_tiles && full) {  // next run: each per-instance placement's slowest tiles first
+      const size_t nt = pp_ntiles_pi();
+      std::vector<uint32_t> perm(nt);
+      for (size_t p = 0; p < P; ++p) {
+        if (!pending_per_inst[p]) continue;
+        const uint32_t* ns = h_tile_ns.p + p * nt;
+        for (size_t k = 0; k < nt; ++k) perm[k] = static_cast<uint32_t>(k);
+        std::stable_sort(perm.begin(), perm.end(), [&](uint32_t x, uint32_t y) { return ns[x] > ns[y]; });
+        cuda_check(cudaMemcpy(d_tile_perm.p + p * nt, perm.data(), nt * 4, cudaMemcpyHostToDevice), "H2D tile order");
+        tile_perm_ok[p] = 1;
+      }
+    }
     pending_rounds.assign(P, 0);
     for (size_t p = lo; p < hi; ++p) pending_rounds[p] = device_rounds[p] ? ctrl_all[8 * p + 2] : 0u;
     timing_pending = true;

@@ -447,6 +447,19 @@ def test_dense_wide_rounds_match_reference(gpu, ref, monkeypatch, attempts):
         assert_same(gpu, got, want)
 
 
+def test_per_instance_tile_order_from_history(gpu, ref):
+    """Per-instance placements claim their tiles slowest-first from the previous run's tile
+    times (several tiles per CTA: 30,000 instances here). Repeated runs -- the second and
+    third with the learned order -- equal the reference."""
+    scene = scenes.tabletop_mixed(30000)
+    want = ref.generate(scene, 3, threads=8)
+    eng = gpu.Engine(scene)
+    for _ in range(3):
+        got = eng.generate(3)
+        assert_same(gpu, got, want)
+        assert got.stats["per_instance_placements"] > 0
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_sharded_generate_equals_single(gpu, ref, world):
     """Variation-batch sharding: G shards with the per-round count exchange
