@@ -46,6 +46,16 @@ enum Ctrl { kRounds = 2, kErr = 3, kTileCtr = 4 /* kTotal0 = 5, kTotal1 = 6 */ }
 
 using BlockScan = cub::BlockScan<uint32_t, kB>;
 
+// Programmatic dependent launch (sm_90+): the engine's kernels are launched with
+// programmatic stream serialization (launch_pdl), so a kernel's CTAs are scheduled while
+// its predecessor's last wave drains. Every such kernel first waits for the predecessor's
+// completion and memory flush (griddepcontrol.wait; a no-op without the attribute), which
+// keeps stream order transitive, then lets its own successor launch.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // Per-round candidate state of the CTA's tile (dynamic shared memory).
 struct Tile {
   double* box;       // [kB][6]  candidate world AABB per slot
@@ -1004,6 +1014,7 @@ extern __shared__ __align__(16) unsigned char g_dsm[];
 
 template <bool kGrid, bool kReach>
 __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_place(PlaceParams p) {
+  pdl_enter();
   __shared__ Fixed F;
   Tile T = carve(g_dsm, p.w.n_words, p.ws_bytes);
   const bool timer = p.prof && blockIdx.x == 0 && threadIdx.x == 0;
@@ -1085,6 +1096,7 @@ __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_place(PlaceParams p
 // Sharded building blocks (no grid barrier inside a launch).
 template <bool kGrid, bool kReach>
 __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_place_instances(PlaceParams p) {
+  pdl_enter();
   __shared__ Fixed F;
   Tile T = carve(g_dsm, p.w.n_words, p.ws_bytes);
   SbGeom gA;
@@ -1097,6 +1109,7 @@ __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_place_instances(Pla
 }
 
 __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_fast_init(PlaceParams p) {
+  pdl_enter();
   __shared__ Fixed F;
   Tile T = carve(g_dsm, p.w.n_words, p.ws_bytes);
   if (p.shard_vary && __ldcg(p.shard_vary) != 0) return;  // per-instance: no FIFO rounds
@@ -1115,6 +1128,7 @@ __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_fast_init(PlacePara
 
 template <bool kGrid, bool kReach>
 __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_fast_round(PlaceParams p, int32_t a) {
+  pdl_enter();
   __shared__ Fixed F;
   Tile T = carve(g_dsm, p.w.n_words, p.ws_bytes);
   SbGeom gA;
@@ -1155,6 +1169,7 @@ __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_fast_round(PlacePar
 }
 
 __global__ void __launch_bounds__(kB) k_fast_finish(PlaceParams p, int32_t a) {
+  pdl_enter();
   const uint32_t* cin = p.tile_cnt + (size_t)(a & 1) * p.cnt_stride;
   for (uint32_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
     const uint32_t n = __ldcg(cin + t);
@@ -1224,6 +1239,7 @@ constexpr int kWideScanThreads = 1024;
 // post = 1, after its accept: offsets of the survivors (buffer (a + 1) & 1) for k_wide_spread,
 // their total into w_ctl[5] (and w_surv[a] when the engine records it).
 __global__ void __launch_bounds__(kWideScanThreads) k_wide_scan(PlaceParams p, int post) {
+  pdl_enter();
   using Scan = cub::BlockScan<uint32_t, kWideScanThreads>;
   __shared__ typename Scan::TempStorage scan;
   const int32_t a = p.wide_round;
@@ -1259,6 +1275,7 @@ __global__ void __launch_bounds__(kWideScanThreads) k_wide_scan(PlaceParams p, i
 // append one (slot, object) pair per overlap, ascending objects, for k_wide_narrow.
 template <bool kGrid, bool kReach, int kW>
 __global__ void __launch_bounds__(kB, SB_WIDE_SAMPLE_MINB) k_wide_sample(PlaceParams p) {
+  pdl_enter();
   static_assert(kW <= kGW && kGW % kW == 0, "enable words");
   constexpr int kWC = kW < 4 ? kW : 4;  // words of a cell loaded per batch
   const uint32_t t = blockIdx.x;
@@ -1460,6 +1477,7 @@ __global__ void __launch_bounds__(kB, SB_WIDE_SAMPLE_MINB) k_wide_sample(PlacePa
 // -- such pairs never reach k_wide_narrow. Survivors are appended to the second list.
 // Pairs behind a lower hit of their slot cannot matter and are dropped as well.
 __global__ void __launch_bounds__(kB) k_wide_filter(PlaceParams p) {
+  pdl_enter();
   __shared__ PlaceGeomCache gc;
   const WorldView& w = p.w;
   const int lane = threadIdx.x & 31;
@@ -1504,6 +1522,7 @@ __global__ void __launch_bounds__(kB) k_wide_filter(PlaceParams p) {
 // cp.async variant; DESIGN 3.3).
 template <bool kBulk, int kMinB = SB_WIDE_NARROW_MINB>
 __global__ void __launch_bounds__(kB, kMinB) k_wide_narrow(PlaceParams p, int chunk, int claim_ahead) {
+  pdl_enter();
   __shared__ PlaceGeomCache gc;
   __shared__ __align__(8) uint64_t bars[kWarps][2];
   __shared__ int4 ogeo[kGW * 32];  // obj_grec of every object (no dependent load per pair)
@@ -1620,6 +1639,7 @@ __global__ void __launch_bounds__(kB, kMinB) k_wide_narrow(PlaceParams p, int ch
 // compacted in place into the tile's list with round 1's count (tile_cnt buffer 1).
 template <bool kGrid>
 __global__ void __launch_bounds__(kB) k_wide_accept(PlaceParams p) {
+  pdl_enter();
   __shared__ typename BlockScan::TempStorage scan;
   const uint32_t t = blockIdx.x;
   const int e = threadIdx.x;
@@ -1689,6 +1709,7 @@ __global__ void __launch_bounds__(kB) k_wide_accept(PlaceParams p) {
 // rank / q, entry rank % q (tile_list2, tile_cnt2 buffer 1). Block per old tile; the
 // counts of all new tiles are written by a grid-stride loop.
 __global__ void __launch_bounds__(kB) k_wide_spread(PlaceParams p, unsigned grid) {
+  pdl_enter();
   const unsigned long long S = __ldcg(p.w_ctl + 5);
   if (grid > p.ntiles) grid = p.ntiles;  // S / q tiles must exist
   unsigned long long q = S ? (S + grid - 1) / grid : 1;  // at most one tile's capacity
@@ -1715,6 +1736,32 @@ void check(cudaError_t e, const char* what) {
 void set_smem(const void* fn, size_t smem) {
   check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
         "cudaFuncSetAttribute(smem)");
+}
+
+// Launch with programmatic stream serialization (the kernel starts with pdl_enter());
+// SB_PDL=0 launches plainly.
+bool pdl_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("SB_PDL");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_on() ? 1 : 0;
+  check(cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...), "cudaLaunchKernelEx");
 }
 
 }  // namespace
@@ -1768,7 +1815,7 @@ bool place_persistent(const PlaceParams& p, unsigned grid, size_t smem, sb_strea
 template <bool kGrid, bool kReach>
 void launch_instances(const PlaceParams& p, unsigned grid, size_t smem, sb_stream_t s) {
   set_smem((const void*)k_place_instances<kGrid, kReach>, smem);
-  k_place_instances<kGrid, kReach><<<grid, kB, smem, s>>>(p);
+  launch_pdl(k_place_instances<kGrid, kReach>, grid, kB, smem, reinterpret_cast<cudaStream_t>(s), p);
 }
 
 void place_instances(const PlaceParams& p, unsigned grid, size_t smem, sb_stream_t s) {
@@ -1780,7 +1827,7 @@ void place_instances(const PlaceParams& p, unsigned grid, size_t smem, sb_stream
 
 void place_fast_init(const PlaceParams& p, unsigned grid, size_t smem, sb_stream_t s) {
   set_smem((const void*)k_fast_init, smem);
-  k_fast_init<<<grid, kB, smem, s>>>(p);
+  launch_pdl(k_fast_init, grid, kB, smem, reinterpret_cast<cudaStream_t>(s), p);
   check(cudaGetLastError(), "k_fast_init");
 }
 
@@ -1788,7 +1835,7 @@ template <bool kGrid, bool kReach>
 void launch_fast_round(const PlaceParams& p, int32_t attempt, unsigned grid, size_t smem,
                        sb_stream_t s) {
   set_smem((const void*)k_fast_round<kGrid, kReach>, smem);
-  k_fast_round<kGrid, kReach><<<grid, kB, smem, s>>>(p, attempt);
+  launch_pdl(k_fast_round<kGrid, kReach>, grid, kB, smem, reinterpret_cast<cudaStream_t>(s), p, attempt);
 }
 
 void place_fast_round(const PlaceParams& p, int32_t attempt, unsigned grid, size_t smem,
@@ -1801,10 +1848,10 @@ void place_fast_round(const PlaceParams& p, int32_t attempt, unsigned grid, size
 
 template <bool kGrid, bool kReach>
 void launch_wide_sample(const PlaceParams& p, int nw, cudaStream_t st) {
-  if (nw <= 1) k_wide_sample<kGrid, kReach, 1><<<p.ntiles, kB, 0, st>>>(p);
-  else if (nw <= 2) k_wide_sample<kGrid, kReach, 2><<<p.ntiles, kB, 0, st>>>(p);
-  else if (nw <= 4) k_wide_sample<kGrid, kReach, 4><<<p.ntiles, kB, 0, st>>>(p);
-  else k_wide_sample<kGrid, kReach, kGW><<<p.ntiles, kB, 0, st>>>(p);
+  if (nw <= 1) launch_pdl(k_wide_sample<kGrid, kReach, 1>, p.ntiles, kB, 0, st, p);
+  else if (nw <= 2) launch_pdl(k_wide_sample<kGrid, kReach, 2>, p.ntiles, kB, 0, st, p);
+  else if (nw <= 4) launch_pdl(k_wide_sample<kGrid, kReach, 4>, p.ntiles, kB, 0, st, p);
+  else launch_pdl(k_wide_sample<kGrid, kReach, kGW>, p.ntiles, kB, 0, st, p);
 }
 
 size_t wide_narrow_smem(int ws_bytes) { return (size_t)kWarps * ws_bytes; }
@@ -1817,7 +1864,7 @@ int place_wide_round0(const PlaceParams& p, unsigned init_grid, size_t init_smem
 
 int place_wide_round0_a(const PlaceParams& p, int num_sms, sb_stream_t s) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
-  k_wide_scan<<<1, kWideScanThreads, 0, st>>>(p, 0);
+  launch_pdl(k_wide_scan, 1, kWideScanThreads, 0, st, p, 0);
   check(cudaGetLastError(), "k_wide_scan");
   const bool g = p.grid.g != 0, r = p.reach_any != nullptr;
   // register footprint sized by the enable words in use (cand / ov stay in registers)
@@ -1828,7 +1875,7 @@ int place_wide_round0_a(const PlaceParams& p, int num_sms, sb_stream_t s) {
   {
     int per = 0;
     check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void*)k_wide_filter, kB, 0), "occupancy");
-    k_wide_filter<<<(unsigned)(per > 0 ? per : 1) * num_sms, kB, 0, st>>>(p);
+    launch_pdl(k_wide_filter, (unsigned)(per > 0 ? per : 1) * num_sms, kB, 0, st, p);
     check(cudaGetLastError(), "k_wide_filter");
   }
   const size_t smem = wide_narrow_smem(p.ws_bytes);
@@ -1854,9 +1901,9 @@ int place_wide_round0_a(const PlaceParams& p, int num_sms, sb_stream_t s) {
     const char* e = std::getenv("SB_NARROW_AHEAD");
     return e ? std::atoi(e) : 0;
   }();
-  if (!bulk) k_wide_narrow<false><<<ngrid, kB, smem, st>>>(p, chunk, ahead);
-  else if (minb == 4) k_wide_narrow<true, 4><<<ngrid, kB, smem, st>>>(p, chunk, ahead);
-  else k_wide_narrow<true><<<ngrid, kB, smem, st>>>(p, chunk, ahead);
+  if (!bulk) launch_pdl(k_wide_narrow<false>, ngrid, kB, smem, st, p, chunk, ahead);
+  else if (minb == 4) launch_pdl(k_wide_narrow<true, 4>, ngrid, kB, smem, st, p, chunk, ahead);
+  else launch_pdl(k_wide_narrow<true>, ngrid, kB, smem, st, p, chunk, ahead);
   check(cudaGetLastError(), "k_wide_narrow");
   return 4;
 }
@@ -1865,16 +1912,16 @@ int place_wide_round0_c(const PlaceParams& p, unsigned init_grid, sb_stream_t s,
                         unsigned spread_grid, bool spread) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
   const bool g = p.grid.g != 0;
-  if (g) k_wide_accept<true><<<p.ntiles, kB, 0, st>>>(p);
-  else k_wide_accept<false><<<p.ntiles, kB, 0, st>>>(p);
+  if (g) launch_pdl(k_wide_accept<true>, p.ntiles, kB, 0, st, p);
+  else launch_pdl(k_wide_accept<false>, p.ntiles, kB, 0, st, p);
   check(cudaGetLastError(), "k_wide_accept");
-  k_wide_scan<<<1, kWideScanThreads, 0, st>>>(p, 1);
+  launch_pdl(k_wide_scan, 1, kWideScanThreads, 0, st, p, 1);
   check(cudaGetLastError(), "k_wide_scan");
   if (!spread) return 2;  // sharded: rounds >= 1 read the compacted tiles in place
   // round 1's survivors over the persistent kernel's grid (SB_SPREAD=0: full tiles instead)
   unsigned sg = spread_grid ? spread_grid : init_grid;
   if (const char* e = std::getenv("SB_SPREAD")) sg = std::atoi(e) ? sg : 1u;
-  k_wide_spread<<<p.ntiles, kB, 0, st>>>(p, sg);
+  launch_pdl(k_wide_spread, p.ntiles, kB, 0, st, p, sg);
   check(cudaGetLastError(), "k_wide_spread");
   return 3;
 }
@@ -1885,7 +1932,7 @@ int place_wide_round0_rest(const PlaceParams& p, unsigned init_grid, int num_sms
 }
 
 void place_fast_finish(const PlaceParams& p, int32_t attempt, unsigned grid, sb_stream_t s) {
-  k_fast_finish<<<grid, kB, 0, s>>>(p, attempt);
+  launch_pdl(k_fast_finish, grid, kB, 0, reinterpret_cast<cudaStream_t>(s), p, attempt);
   check(cudaGetLastError(), "k_fast_finish");
 }
 
