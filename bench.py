@@ -329,8 +329,10 @@ def run_ours(args, rank, world, local_rank):
     t_hbm = bytes_ / (hbm_peak * 1e9)
     t_fp64 = flops / (fp64_peak_tf * 1e12) if fp64_peak_tf > 0 else 0.0
     primary, secondary = (hbm, fp64) if t_hbm >= t_fp64 else (fp64, hbm)
-    # One "launch" here is one placement's kernel chain on the engine stream, timed by CUDA
-    # events around it: FIFO placements of large batches run round 0 as k_fast_init +
+    # One "launch" here is one placement's kernel chain on the engine stream. The chains are
+    # timed by CUDA events on that stream around the whole generation (per-placement events
+    # would break the programmatic-launch edges between the kernels; SB_PLACE_EVENTS=1 puts
+    # them back), so kernel_ms_per_step also holds the run's reset / grid-init kernels: FIFO placements of large batches run round 0 as k_fast_init +
     # k_wide_scan + k_wide_sample + k_wide_filter + k_wide_narrow + k_wide_accept +
     # k_wide_scan + k_wide_spread and later rounds in the persistent k_place; other
     # placements are one k_place (or k_place_instances). Per-kernel shares: the committed

@@ -1806,9 +1806,29 @@ bool place_persistent(const PlaceParams& p, unsigned grid, size_t smem, sb_strea
   if (grid == 0) return false;
   PlaceParams q = p;
   void* args[] = {&q};
-  check(cudaLaunchCooperativeKernel(place_fn(p), dim3(grid), dim3(kB), args, smem,
-                                    reinterpret_cast<cudaStream_t>(s)),
-        "cudaLaunchCooperativeKernel(k_place)");
+  static const bool pdl = [] {  // SB_PDL_COOP=0: plain cooperative launch
+    const char* e = std::getenv("SB_PDL_COOP");
+    return pdl_on() && (!e || std::atoi(e) != 0);
+  }();
+  if (!pdl) {
+    check(cudaLaunchCooperativeKernel(place_fn(p), dim3(grid), dim3(kB), args, smem,
+                                      reinterpret_cast<cudaStream_t>(s)),
+          "cudaLaunchCooperativeKernel(k_place)");
+    return true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kB);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = reinterpret_cast<cudaStream_t>(s);
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  check(cudaLaunchKernelExC(&cfg, place_fn(p), args), "cudaLaunchKernelEx(k_place, cooperative)");
   return true;
 }
 
