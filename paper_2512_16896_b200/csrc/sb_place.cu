@@ -11,6 +11,7 @@
 #include "sb_crmath.cuh"
 #include "sb_glibcm.cuh"
 #include "sb_dev.cuh"
+#include "sb_pdl.cuh"
 #include "sb_place.h"
 #include "sb_reachdev.cuh"
 #include "sb_poly.h"
@@ -46,15 +47,6 @@ enum Ctrl { kRounds = 2, kErr = 3, kTileCtr = 4 /* kTotal0 = 5, kTotal1 = 6 */ }
 
 using BlockScan = cub::BlockScan<uint32_t, kB>;
 
-// Programmatic dependent launch (sm_90+): the engine's kernels are launched with
-// programmatic stream serialization (launch_pdl), so a kernel's CTAs are scheduled while
-// its predecessor's last wave drains. Every such kernel first waits for the predecessor's
-// completion and memory flush (griddepcontrol.wait; a no-op without the attribute), which
-// keeps stream order transitive, then lets its own successor launch.
-__device__ __forceinline__ void pdl_enter() {
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
 
 // Per-round candidate state of the CTA's tile (dynamic shared memory).
 struct Tile {
@@ -1738,31 +1730,6 @@ void set_smem(const void* fn, size_t smem) {
         "cudaFuncSetAttribute(smem)");
 }
 
-// Launch with programmatic stream serialization (the kernel starts with pdl_enter());
-// SB_PDL=0 launches plainly.
-bool pdl_on() {
-  static const bool on = [] {
-    const char* e = std::getenv("SB_PDL");
-    return !e || std::atoi(e) != 0;
-  }();
-  return on;
-}
-
-template <typename... KArgs, typename... Args>
-void launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
-                Args... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(block);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = pdl_on() ? 1 : 0;
-  check(cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...), "cudaLaunchKernelEx");
-}
 
 }  // namespace
 

@@ -15,6 +15,7 @@
 #include "sb_crmath.cuh"
 #include "sb_glibcm.cuh"
 #include "sb_dev.cuh"
+#include "sb_pdl.cuh"
 #include "sb_poly.h"
 #include "sb_region.h"
 
@@ -638,6 +639,7 @@ __device__ __forceinline__ RegionStats group_region(const SbPlacementDev& pl, do
 // shard owns global instance 0, is recomputed per warp from local instance 0.
 template <bool kHole>
 __global__ void __launch_bounds__(kRB, kRegionMinBlocks) k_relation_regions(RelationRegionParams p) {
+  pdl_enter();
   __shared__ RegionScratch scratch[kRW];
   const SbArcTable* arcs = kHole ? nullptr : p.arcs;
   const Grp g;
@@ -782,8 +784,9 @@ void relation_regions(const RelationRegionParams& p, int num_sms, sb_stream_t s)
   const unsigned cap_blocks = (unsigned)(num_sms * 16);
   if (blocks > cap_blocks) blocks = cap_blocks;
   if (blocks == 0) blocks = 1;
-  if (p.hole) k_relation_regions<true><<<blocks, kRB, 0, s>>>(p);
-  else k_relation_regions<false><<<blocks, kRB, 0, s>>>(p);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
+  if (p.hole) launch_pdl(k_relation_regions<true>, blocks, kRB, 0, st, p);
+  else launch_pdl(k_relation_regions<false>, blocks, kRB, 0, st, p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("relation_regions: ") + cudaGetErrorString(e));
 }
