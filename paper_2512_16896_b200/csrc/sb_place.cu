@@ -894,6 +894,87 @@ __device__ uint64_t fast_round(const PlaceParams& p, const Sampling& S, const Sb
   return total;
 }
 
+// Fast rounds without a grid barrier (p.lb_board). Round a of tile t needs the draws before
+// round a (D_a = D_{a-1} + N_{a-1}: every tile's count of round a - 1, i.e. every tile done
+// with round a - 2) and the counts of round a of the tiles below t (those tiles done with
+// round a - 1). Each tile publishes its survivor count to the board with a release store;
+// readers spin on the entry's epoch. So a tile may run one round ahead of the slowest tile
+// instead of waiting for it at a grid barrier. Tile t stays with CTA t % gridDim, which alone
+// reads and writes its list; only the counts cross CTAs. The draws (and so every result) are
+// those of the barrier version. All CTAs are co-resident (cooperative launch).
+__device__ __forceinline__ uint32_t lb_get(const PlaceParams& p, int32_t a, uint32_t t) {
+  const unsigned long long* e = p.lb_board + (size_t)a * p.lb_stride + t;
+  unsigned long long v;
+  for (;;) {
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(e) : "memory");
+    if ((uint32_t)(v >> 32) == p.lb_epoch) return (uint32_t)v;
+    __nanosleep(64);
+  }
+}
+
+__device__ __forceinline__ void lb_put(const PlaceParams& p, int32_t a, uint32_t t, uint32_t n) {
+  unsigned long long* e = p.lb_board + (size_t)a * p.lb_stride + t;
+  const unsigned long long v = ((unsigned long long)p.lb_epoch << 32) | n;
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(e), "l"(v) : "memory");
+}
+
+// Counts of round a: from the launch's input buffer for the first round, else the board.
+__device__ __forceinline__ uint32_t lb_count(const PlaceParams& p, int32_t a, uint32_t t) {
+  return a == p.start_round ? __ldcg(p.tile_cnt + (size_t)(a & 1) * p.cnt_stride + t) : lb_get(p, a, t);
+}
+
+template <bool kGrid, bool kReach>
+__device__ void lookback_rounds(const PlaceParams& p, const Sampling& S, const SbGeom& gA,
+                                Tile& T, Fixed& F, int32_t a, uint64_t draws, Local& L) {
+  const uint32_t G = gridDim.x, b = blockIdx.x, ntu = tiles_in_use(p);
+  const bool resident = ntu <= G;
+  uint64_t n_prev = 0;  // N_{a-1}
+  for (; a < p.attempts; ++a) {
+    if (a > p.start_round) {  // D_a = D_{a-1} + N_{a-1}
+      uint32_t part = 0, ex, tot;
+      for (uint32_t t = threadIdx.x; t < ntu; t += kB) part += lb_count(p, a - 1, t);
+      BlockScan(F.scan).ExclusiveSum(part, ex, tot);
+      __syncthreads();
+      n_prev = tot;
+      draws += n_prev;
+      if (n_prev == 0) return;  // round a - 1 had no active instance: all placed
+    }
+    // exclusive prefix of round a's counts over the tiles below each of this CTA's tiles
+    uint32_t running = 0, k = 0;
+    for (uint32_t t = b; t < ntu; t += G, ++k) {
+      // tiles (t - G, t): the ones up to t - G are in `running` already
+      uint32_t part = 0, ex, s;
+      for (uint32_t u = (t >= G ? t - G + 1 : 0) + threadIdx.x; u < t; u += kB) part += lb_count(p, a, u);
+      BlockScan(F.scan).ExclusiveSum(part, ex, s);
+      __syncthreads();
+      running += s;
+      const uint32_t n = lb_count(p, a, t);  // own tile: published by this CTA (or the input)
+      if (n == 0) {
+        if (threadIdx.x == 0) lb_put(p, a + 1, t, 0u);
+      } else {
+        if (!resident || a == p.start_round) load_list(p, T, t, n);
+        const uint32_t ns = tile_round<kGrid, kReach>(p, S, gA, T, F, n, a, 1, draws + running, L);
+        if (!resident) {
+          uint32_t* dst = p.tile_list + (uint64_t)t * p.tile_inst;
+          for (uint32_t e = threadIdx.x; e < ns; e += kB) dst[e] = T.list[e];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) lb_put(p, a + 1, t, ns);
+      }
+      running += n;  // the next own tile's prefix continues from here
+      __syncthreads();
+    }
+  }
+  // K attempts exhausted: the survivors of this CTA's tiles are invalid
+  for (uint32_t t = b; t < ntu; t += G) {
+    const uint32_t n = lb_count(p, a, t);
+    if (n == 0) continue;
+    if (!resident || a == p.start_round) load_list(p, T, t, n);  // no round ran: not loaded
+    mark_invalid(p, T, n);
+    __syncthreads();
+  }
+}
+
 // Fast path tail: once at most p.solo_max instances remain, CTA 0 gathers them in global
 // active order (tile order, then position) and runs the remaining rounds alone -- no grid
 // barrier, no prefix scan; draw j of round a is draws + position, as in the grid rounds.
@@ -1041,7 +1122,11 @@ __global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_place(PlaceParams p
       a = p.start_round;
       draws = __ldcg(p.start_draws);
     }
-    for (; a < p.attempts; ++a) {
+    if (p.lb_board && p.solo_max == 0 && !p.dbg) {
+      lookback_rounds<kGrid, kReach>(p, S, gA, T, F, a, draws, L);
+      a = -1;  // survivors of exhausted instances marked inside
+    }
+    for (; a >= 0 && a < p.attempts; ++a) {
       unsigned long long r0 = 0;
       if (p.dbg && threadIdx.x == 0) {
         r0 = global_ns();

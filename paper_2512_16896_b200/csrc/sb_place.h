@@ -109,6 +109,12 @@ struct PlaceParams {
   // start_round = 1 from the survivors k_wide_accept left in tile_cnt buffer 1.
   int32_t start_round;
   const unsigned long long* start_draws;  // draws of the rounds before start_round
+  // Persistent fast rounds without a grid barrier (decoupled look-back), or null: entry
+  // lb_board[a * lb_stride + t] = lb_epoch << 32 | tile t's active count of round a, published
+  // by the CTA owning t when it finishes round a - 1 (lb_epoch is unique per launch).
+  unsigned long long* lb_board;
+  uint32_t lb_stride;
+  uint32_t lb_epoch;
   double* w_pose;                // [ntiles * kPlaceBlock][kWideRec] compact candidate record
                                  // per round-0 slot: tx, ty, tz, cos, sin, 0
   int32_t* w_contact;            // [..] lowest colliding object, INT32_MAX = free

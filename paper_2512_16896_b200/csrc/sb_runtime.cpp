@@ -429,6 +429,11 @@ struct sb_engine {
   std::vector<int> wide_rounds;
   unsigned long long wide_more = 32768;
   DevArray<uint32_t> d_wcnt2;
+  // persistent fast rounds with a decoupled look-back on the tile counts instead of a grid
+  // barrier per round (sbk lookback_rounds); SB_LOOKBACK=0: grid barrier
+  bool lookback = true;
+  DevArray<unsigned long long> d_lb;  // [attempts + 1][ntiles]
+  uint32_t lb_epoch = 0;
   DevArray<uint8_t> d_wflag;
   DevArray<unsigned long long> d_wctl;
   DevArray<uint64_t> d_jump;        // FIFO draw jump table (sbd::pcg_jump_table_host)
@@ -762,6 +767,11 @@ struct sb_engine {
       }
     }
     d_tile_cnt.alloc(2 * static_cast<size_t>(ntiles));
+    if (const char* e = std::getenv("SB_LOOKBACK")) lookback = std::atoi(e) != 0;
+    if (lookback) {  // look-back count board of the persistent fast rounds, epochs from 1
+      d_lb.alloc(static_cast<size_t>(attempts + 1) * ntiles);
+      cuda_check(cudaMemset(d_lb.p, 0, d_lb.count * sizeof(unsigned long long)), "memset");
+    }
     {  // wide round 0 scratch (use_wide decided above)
       wide_pgrid = grid;  // persistent grid for rounds >= 1 (SB_WIDE_PGRID: fewer CTAs)
       if (const char* e = std::getenv("SB_WIDE_PGRID"))
@@ -1230,6 +1240,13 @@ struct sb_engine {
             pp.tile_list = d_wlist2.p;
             pp.tile_cnt = d_wcnt2.p;
             pp.ntiles_dev = d_wctl.p + 6;
+          }
+          pp.lb_board = nullptr;
+          if (lookback && d_lb.p && !capturing) {
+            pp.lb_board = d_lb.p;
+            pp.lb_stride = ntiles;
+            if (++lb_epoch == 0) ++lb_epoch;
+            pp.lb_epoch = lb_epoch;
           }
           if (!sbk::place_persistent(pp, use_wide && !relation ? wide_pgrid : grid, smem, s))
             throw CudaError("cooperative launch of the placement kernel is not possible");

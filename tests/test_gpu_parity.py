@@ -447,6 +447,21 @@ def test_dense_wide_rounds_match_reference(gpu, ref, monkeypatch, attempts):
         assert_same(gpu, got, want)
 
 
+@pytest.mark.parametrize("lookback", ["0", "1"])
+@pytest.mark.parametrize("attempts", [2, 64])
+def test_fast_rounds_lookback_and_barrier_match_reference(gpu, ref, monkeypatch, lookback, attempts):
+    """The persistent fast rounds with the decoupled look-back on the tile counts (default)
+    and with a grid barrier per round (SB_LOOKBACK=0) both equal the reference, with and
+    without the grid-wide round 0, including K = 2 where the survivors exhaust K."""
+    monkeypatch.setenv("SB_LOOKBACK", lookback)
+    scene = scenes.tabletop_boxes(3000, n_objects=30, attempts=attempts)
+    want = ref.generate(scene, 11, threads=8)
+    for wide in ("0", "1"):
+        monkeypatch.setenv("SB_WIDE", wide)
+        got = gpu.Engine(scene).generate(11)
+        assert_same(gpu, got, want)
+
+
 def test_per_instance_tile_order_from_history(gpu, ref):
     """Per-instance placements claim their tiles slowest-first from the previous run's tile
     times (several tiles per CTA: 30,000 instances here). Repeated runs -- the second and
