@@ -1085,8 +1085,10 @@ __device__ __forceinline__ void block_setup(const PlaceParams& p, Fixed& F, Tile
 
 extern __shared__ __align__(16) unsigned char g_dsm[];
 
-template <bool kGrid, bool kReach>
-__global__ void __launch_bounds__(kB, SB_PLACE_MIN_BLOCKS) k_place(PlaceParams p) {
+// kMinB: CTAs per SM the register budget is sized for -- 2 (128 registers, spills) by
+// default, 1 (no spills, half the warps) for the FIFO placements with SB_PLACE1.
+template <bool kGrid, bool kReach, int kMinB = SB_PLACE_MIN_BLOCKS>
+__global__ void __launch_bounds__(kB, kMinB) k_place(PlaceParams p) {
   pdl_enter();
   __shared__ Fixed F;
   Tile T = carve(g_dsm, p.w.n_words, p.ws_bytes);
@@ -1834,16 +1836,27 @@ void narrow_profile(unsigned long long out[8], bool reset) {
 
 namespace {
 // kernel variant by (occupancy grid, fused reachability filter)
-const void* place_fn(const PlaceParams& p) {
+const void* place_fn(const PlaceParams& p, bool one = false) {
   const bool g = p.grid.g != 0, r = p.reach_any != nullptr;
+  if (one)
+    return g ? (r ? (const void*)k_place<true, true, 1> : (const void*)k_place<true, false, 1>)
+             : (r ? (const void*)k_place<false, true, 1> : (const void*)k_place<false, false, 1>);
   return g ? (r ? (const void*)k_place<true, true> : (const void*)k_place<true, false>)
            : (r ? (const void*)k_place<false, true> : (const void*)k_place<false, false>);
 }
 }  // namespace
 
-int place_grid(int num_sms, size_t smem) {
-  const void* fns[4] = {(const void*)k_place<false, false>, (const void*)k_place<true, false>,
-                        (const void*)k_place<false, true>, (const void*)k_place<true, true>};
+int place_grid(int num_sms, size_t smem, bool one) {
+  const void* fns[4] = {place_fn(PlaceParams{}, one), nullptr, nullptr, nullptr};
+  {
+    PlaceParams q = {};
+    q.grid.g = 1;
+    fns[1] = place_fn(q, one);
+    q.reach_any = reinterpret_cast<const unsigned long long*>(1);
+    fns[3] = place_fn(q, one);
+    q.grid.g = 0;
+    fns[2] = place_fn(q, one);
+  }
   int per = 1 << 30;
   for (const void* fn : fns) {
     set_smem(fn, smem);
@@ -1854,7 +1867,7 @@ int place_grid(int num_sms, size_t smem) {
   return per * num_sms;
 }
 
-bool place_persistent(const PlaceParams& p, unsigned grid, size_t smem, sb_stream_t s) {
+bool place_persistent(const PlaceParams& p, unsigned grid, size_t smem, sb_stream_t s, bool one) {
   if (grid == 0) return false;
   PlaceParams q = p;
   void* args[] = {&q};
@@ -1863,7 +1876,7 @@ bool place_persistent(const PlaceParams& p, unsigned grid, size_t smem, sb_strea
     return pdl_on() && (!e || std::atoi(e) != 0);
   }();
   if (!pdl) {
-    check(cudaLaunchCooperativeKernel(place_fn(p), dim3(grid), dim3(kB), args, smem,
+    check(cudaLaunchCooperativeKernel(place_fn(p, one), dim3(grid), dim3(kB), args, smem,
                                       reinterpret_cast<cudaStream_t>(s)),
           "cudaLaunchCooperativeKernel(k_place)");
     return true;
@@ -1880,7 +1893,7 @@ bool place_persistent(const PlaceParams& p, unsigned grid, size_t smem, sb_strea
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 2;
-  check(cudaLaunchKernelExC(&cfg, place_fn(p), args), "cudaLaunchKernelEx(k_place, cooperative)");
+  check(cudaLaunchKernelExC(&cfg, place_fn(p, one), args), "cudaLaunchKernelEx(k_place, cooperative)");
   return true;
 }
 

@@ -151,9 +151,10 @@ size_t place_smem_bytes(int n_words, int ws_bytes, int n_objects);
 // Narrow-phase scratch bytes per warp for the given geometry bounds.
 int place_ws_bytes(int max_tris, int max_nodes);
 // Co-resident CTAs of the persistent placement kernel (0 if it cannot be launched).
-int place_grid(int num_sms, size_t smem);
+// one: the 1-CTA-per-SM variant (no register spills) used by SB_PLACE1.
+int place_grid(int num_sms, size_t smem, bool one = false);
 // Single GPU: whole placement in one cooperative launch.
-bool place_persistent(const PlaceParams& p, unsigned grid, size_t smem, sb_stream_t s);
+bool place_persistent(const PlaceParams& p, unsigned grid, size_t smem, sb_stream_t s, bool one = false);
 // Cycle breakdown of the narrow phase (zeros unless built with -DSB_NARROW_PROF).
 void narrow_profile(unsigned long long out[8], bool reset);
 // Sharded runs. Per-instance path: one launch, no exchange (place_instances). Fast path:

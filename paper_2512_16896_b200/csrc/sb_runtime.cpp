@@ -432,6 +432,12 @@ struct sb_engine {
   // persistent fast rounds with a decoupled look-back on the tile counts instead of a grid
   // barrier per round (sbk lookback_rounds); SB_LOOKBACK=0: grid barrier
   bool lookback = true;
+  // SB_PLACE1=1: FIFO placements without a relation run the 1-CTA-per-SM persistent kernel
+  // (no register spills, half the warps) on grid1 CTAs
+  bool place1 = true;
+  unsigned grid1 = 0;
+  unsigned long long place1_max = 8192;  // SB_PLACE1_MAX: survivors below which it is taken
+  std::vector<char> place1_ok;           // per placement, from the previous run's survivors
   DevArray<unsigned long long> d_lb;  // [attempts + 1][ntiles]
   uint32_t lb_epoch = 0;
   DevArray<uint8_t> d_wflag;
@@ -718,6 +724,10 @@ struct sb_engine {
     smem = sbk::place_smem_bytes(world->view().n_words, ws_bytes, world->view().n_objects);
     grid = static_cast<unsigned>(sbk::place_grid(num_sms, smem));
     if (grid == 0) throw CudaError("placement kernel does not fit on the device (shared memory)");
+    if (const char* e = std::getenv("SB_PLACE1")) place1 = std::atoi(e) != 0;
+    grid1 = place1 ? static_cast<unsigned>(sbk::place_grid(num_sms, smem, true)) : 0u;
+    if (const char* e = std::getenv("SB_PLACE1_MAX")) place1_max = std::strtoull(e, nullptr, 10);
+    place1_ok.assign(places.size(), 0);
     bool any_fifo = false;
     for (const Placement& pl : places) any_fifo = any_fifo || pl.dev.anchor_object < 0;
     // wide round 0: single GPU, or sharded with the device-side exchange (round 0's counts
@@ -1212,6 +1222,8 @@ struct sb_engine {
           pp.reach_base = reach[p].base->p;
         }
         if (world_size == 1) {
+          const bool one = place1 && use_wide && !relation && grid1 > 0 && place1_ok[p] &&
+                           (ntiles + grid1 - 1) / grid1 <= static_cast<uint32_t>(sbk::kPlaceMaxOwnedTiles);
           if (use_wide && !relation) {  // round 0 grid-wide, then the persistent kernel
             pp.w_pose = d_wpose.p;
             pp.w_contact = d_wcontact.p;
@@ -1233,7 +1245,7 @@ struct sb_engine {
             for (int r = 0; r < R; ++r) {
               pp.wide_round = r;
               launches += sbk::place_wide_round0_a(pp, num_sms, s);
-              launches += sbk::place_wide_round0_c(pp, grid, s, wide_pgrid, r + 1 == R);
+              launches += sbk::place_wide_round0_c(pp, grid, s, one ? grid1 : wide_pgrid, r + 1 == R);
             }
             pp.start_round = R;  // rounds R.. on the re-dealt survivor list
             pp.start_draws = d_wctl.p + 4;
@@ -1248,7 +1260,7 @@ struct sb_engine {
             if (++lb_epoch == 0) ++lb_epoch;
             pp.lb_epoch = lb_epoch;
           }
-          if (!sbk::place_persistent(pp, use_wide && !relation ? wide_pgrid : grid, smem, s))
+          if (!sbk::place_persistent(pp, one ? grid1 : use_wide && !relation ? wide_pgrid : grid, smem, s, one))
             throw CudaError("cooperative launch of the placement kernel is not possible");
           ++launches;
           ++round_launches;
@@ -1504,6 +1516,9 @@ struct sb_engine {
         int r_next = 1;
         while (r_next < std::min(R + 1, sbk::kWideSurvRounds) && sv[r_next - 1] >= wide_more) ++r_next;
         wide_rounds[p] = r_next;
+        // few survivors after the wide rounds: the next run's persistent rounds take the
+        // 1-CTA-per-SM kernel (a latency chain of a handful of instances per CTA)
+        if (place1_ok.size() == P) place1_ok[p] = R >= 1 && sv[std::min(R, sbk::kWideSurvRounds) - 1] < place1_max;
       }
     }
     for (size_t p = lo; p < hi; ++p) {
