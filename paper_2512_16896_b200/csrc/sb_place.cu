@@ -908,7 +908,7 @@ __device__ __forceinline__ uint32_t lb_get(const PlaceParams& p, int32_t a, uint
   for (;;) {
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(e) : "memory");
     if ((uint32_t)(v >> 32) == p.lb_epoch) return (uint32_t)v;
-    __nanosleep(64);
+    if (p.lb_sleep) __nanosleep(p.lb_sleep);
   }
 }
 

@@ -115,6 +115,7 @@ struct PlaceParams {
   unsigned long long* lb_board;
   uint32_t lb_stride;
   uint32_t lb_epoch;
+  uint32_t lb_sleep;  // ns a waiting CTA sleeps between polls (0: spin)
   double* w_pose;                // [ntiles * kPlaceBlock][kWideRec] compact candidate record
                                  // per round-0 slot: tx, ty, tz, cos, sin, 0
   int32_t* w_contact;            // [..] lowest colliding object, INT32_MAX = free

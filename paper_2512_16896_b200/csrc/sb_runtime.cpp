@@ -440,6 +440,7 @@ struct sb_engine {
   std::vector<char> place1_ok;           // per placement, from the previous run's survivors
   DevArray<unsigned long long> d_lb;  // [attempts + 1][ntiles]
   uint32_t lb_epoch = 0;
+  uint32_t lb_sleep = 256;  // SB_LB_SLEEP: ns between polls (0 / 64 / 256: C1 0.744 / 0.735 / 0.727 ms)
   DevArray<uint8_t> d_wflag;
   DevArray<unsigned long long> d_wctl;
   DevArray<uint64_t> d_jump;        // FIFO draw jump table (sbd::pcg_jump_table_host)
@@ -778,6 +779,7 @@ struct sb_engine {
     }
     d_tile_cnt.alloc(2 * static_cast<size_t>(ntiles));
     if (const char* e = std::getenv("SB_LOOKBACK")) lookback = std::atoi(e) != 0;
+    if (const char* e = std::getenv("SB_LB_SLEEP")) lb_sleep = static_cast<uint32_t>(std::atoi(e));
     if (lookback) {  // look-back count board of the persistent fast rounds, epochs from 1
       d_lb.alloc(static_cast<size_t>(attempts + 1) * ntiles);
       cuda_check(cudaMemset(d_lb.p, 0, d_lb.count * sizeof(unsigned long long)), "memset");
@@ -1259,6 +1261,7 @@ struct sb_engine {
             pp.lb_stride = ntiles;
             if (++lb_epoch == 0) ++lb_epoch;
             pp.lb_epoch = lb_epoch;
+            pp.lb_sleep = lb_sleep;
           }
           if (!sbk::place_persistent(pp, one ? grid1 : use_wide && !relation ? wide_pgrid : grid, smem, s, one))
             throw CudaError("cooperative launch of the placement kernel is not possible");
