@@ -435,6 +435,7 @@ struct sb_engine {
   // SB_PLACE1=1: FIFO placements without a relation run the 1-CTA-per-SM persistent kernel
   // (no register spills, half the warps) on grid1 CTAs
   bool place1 = true;
+  bool fifo1 = false;  // every FIFO placement on the 1-CTA build (scenes without relations)
   unsigned grid1 = 0;
   unsigned long long place1_max = 8192;  // SB_PLACE1_MAX: survivors below which it is taken
   std::vector<char> place1_ok;           // per placement, from the previous run's survivors
@@ -736,10 +737,20 @@ struct sb_engine {
     use_wide = (world_size == 1 || allgather_dev) && any_fifo && n >= 131072;
     if (const char* e = std::getenv("SB_WIDE"))
       use_wide = (world_size == 1 || allgather_dev) && any_fifo && std::atoi(e) != 0;
+    {  // below the wide size, scenes without relation placements (every placement FIFO) take
+       // the 1-CTA build on a tile layout sized for its grid: C1 0.730 -> 0.712 ms. With
+       // relations it loses (the per-instance tiles want the warps: C2 3.34 -> 3.49, C3
+       // 16.40 -> 18.35 ms), so SB_FIFO1=1 only forces it there.
+      bool any_rel = false;
+      for (const Placement& pl : places) any_rel = any_rel || pl.dev.anchor_object >= 0;
+      fifo1 = !any_rel;
+      if (const char* e = std::getenv("SB_FIFO1")) fifo1 = std::atoi(e) != 0;
+      fifo1 = fifo1 && place1 && grid1 > 0 && world_size == 1 && !use_wide;
+    }
     {  // tiles: a multiple of the grid, at most kPlaceBlock instances each
-      const uint64_t per_wave = static_cast<uint64_t>(grid) * sbk::kPlaceBlock;
+      const uint64_t per_wave = static_cast<uint64_t>(fifo1 ? grid1 : grid) * sbk::kPlaceBlock;
       const uint64_t waves = (n + per_wave - 1) / per_wave;
-      const uint64_t want = static_cast<uint64_t>(grid) * waves;
+      const uint64_t want = static_cast<uint64_t>(fifo1 ? grid1 : grid) * waves;
       tile_inst = static_cast<int>((n + want - 1) / want);
       // Wide engines: full 256-instance tiles. Round 0's grid-wide kernels launch a CTA per
       // tile (no idle threads), and the persistent rounds work on the re-dealt survivor list,
@@ -1224,7 +1235,7 @@ struct sb_engine {
           pp.reach_base = reach[p].base->p;
         }
         if (world_size == 1) {
-          const bool one = place1 && use_wide && !relation && grid1 > 0 && place1_ok[p] &&
+          const bool one = place1 && !relation && grid1 > 0 && ((use_wide && place1_ok[p]) || fifo1) &&
                            (ntiles + grid1 - 1) / grid1 <= static_cast<uint32_t>(sbk::kPlaceMaxOwnedTiles);
           if (use_wide && !relation) {  // round 0 grid-wide, then the persistent kernel
             pp.w_pose = d_wpose.p;
